@@ -1,0 +1,176 @@
+/* ngdb_cuda.h — C ABI between the host scheduler and the sm_100a kernels.
+ *
+ * This is the drop-in boundary of the operator-level training step. In the
+ * reference it is the KernelRegistry: (OperatorType x backbone) -> batched
+ * forward/backward kernels, called by scheduler::run once per popped pool or
+ * cardinality class, plus the trainer's
+ * adam_step / compute_loss and the arena's gather /
+ * scatter_add. The reference ships no header for these (only
+ * proj/include/ngdb/{common,kg,query}.hpp exist), so each entry point below cites
+ * the SPEC operation it replaces.
+ *
+ * Conventions: plain C types only; every call returns an ngdb_status (0 = OK) and
+ * never throws; ngdb_last_error() returns a thread-local message. Calls after
+ * ngdb_ctx_create are asynchronous on the context's CUDA stream unless stated.
+ * All device memory (parameters, Adam moments, activation arena, gradient
+ * staging, frozen PTE store) is owned by the context.
+ */
+#ifndef NGDB_CUDA_H_
+#define NGDB_CUDA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes mirror the ngdb::Error taxonomy (common.hpp:23-56). */
+typedef enum ngdb_status {
+  NGDB_OK = 0,
+  NGDB_ERR_SHAPE_MISMATCH = 1,     /* ShapeMismatch      (kernels)   */
+  NGDB_ERR_INDEX_OUT_OF_RANGE = 2, /* IndexOutOfRange    (arena)     */
+  NGDB_ERR_PARAM_OUT_OF_RANGE = 3, /* ParamOutOfRange    (kernels)   */
+  NGDB_ERR_DOMAIN = 4,             /* DomainError        (kernels)   */
+  NGDB_ERR_MISSING_KERNEL = 5,     /* MissingKernel      (scheduler) */
+  NGDB_ERR_NON_FINITE = 6,         /* NonFinite          (trainer)   */
+  NGDB_ERR_CONFIG = 7,             /* ConfigError        (cli)       */
+  NGDB_ERR_CUDA = 8,               /* CUDA runtime failure           */
+  NGDB_ERR_NO_DEVICE = 9           /* no sm_100 device: no CPU fallback exists */
+} ngdb_status;
+
+typedef enum ngdb_backbone { NGDB_GQE = 0, NGDB_Q2B = 1, NGDB_BETAE = 2 } ngdb_backbone;
+
+/* Operator kinds in scheduler tie-break order (dag.hpp OpKind). */
+typedef enum ngdb_op_kind {
+  NGDB_OP_EMBED_ANCHOR = 0,
+  NGDB_OP_FUSE_SEMANTIC = 1,
+  NGDB_OP_PROJECT = 2,
+  NGDB_OP_NEGATE = 3,
+  NGDB_OP_INTERSECT = 4,
+  NGDB_OP_SCORE = 5,
+  NGDB_OP_UNION_SCORE = 6,
+  NGDB_OP_LOSS = 7
+} ngdb_op_kind;
+
+typedef struct ngdb_model_desc {
+  int32_t backbone;     /* ngdb_backbone */
+  int32_t n_entities;
+  int32_t n_relations;
+  int32_t dim;          /* d (GQE, Q2B) or d' (BetaE: rows are 2d' wide) */
+  int32_t n_neg;        /* K negatives per query */
+  int32_t semantic_dim; /* d_l of the frozen PTE store; 0 = no fusion */
+  float gamma;          /* margin, 12.0 */
+  float alpha_box;      /* Q2B inside weight, 0.02 */
+  float lr;             /* Adam, 1e-4 */
+  float beta1, beta2, eps_adam; /* 0.9, 0.999, 1e-8 */
+  int32_t max_batch;    /* B_max: widest kernel invocation */
+  int32_t max_queries;  /* queries per step the plan buffers are sized for */
+} ngdb_model_desc;
+
+/* One operator node of a kernel invocation. Offsets are float-element offsets
+ * into the context's activation arena (the statically planned Eq. 7 slots);
+ * -1 = absent. For Bwd nodes `in`/`self` describe the forward mirror. */
+typedef struct ngdb_node_desc {
+  int32_t out;   /* output tensor (fwd: T_X; bwd: G_X, one row per mirror input) */
+  int32_t in[3]; /* forward inputs' tensors */
+  int32_t grad;  /* bwd: upstream gradient row; -1 for the Loss mirror */
+  int32_t self;  /* bwd: the mirror's forward output */
+  int32_t id;    /* entity (EmbedAnchor/FuseSemantic), relation (Project), query (Score/Loss) */
+  int32_t aux;   /* anchor slot / project slot / score slot s; -1 = union Loss */
+} ngdb_node_desc;
+
+/* One kernel invocation = one PopBatch or one cardinality class of it. */
+typedef struct ngdb_pool_desc {
+  int32_t kind;   /* ngdb_op_kind */
+  int32_t dir;    /* 0 = Fwd, 1 = Bwd */
+  int32_t k;      /* cardinality class for Intersect/UnionScore, else 0 */
+  int32_t first;  /* index of the first node descriptor */
+  int32_t count;  /* number of nodes */
+} ngdb_pool_desc;
+
+/* A fully planned training step (host memory; copied by plan_create/step_begin).
+ * Sparse-gradient CSR: rows ascending; entity contribution code c >= 0 is the
+ * candidate slot s*(1+K)+j of score slot s, c < 0 is anchor slot (-c-1);
+ * relation contribution codes are project slots. */
+typedef struct ngdb_step_plan {
+  int32_t n_queries;
+  int32_t n_candidates;          /* 1 + K */
+  const int32_t* candidates;     /* [n_queries][n_candidates]: positive, then negatives */
+  int32_t n_pools;
+  const ngdb_pool_desc* pools;
+  int32_t n_nodes;
+  const ngdb_node_desc* nodes;
+  int64_t arena_elems;           /* activation arena high-water mark (floats) */
+  int32_t n_score_slots;         /* Loss (non-union) + Score nodes */
+  int32_t n_anchor_slots;        /* EmbedAnchor / FuseSemantic nodes */
+  int32_t n_project_slots;       /* Project nodes */
+  int32_t n_entity_rows;
+  const int32_t* entity_rows;    /* [n_entity_rows] ascending */
+  const int32_t* entity_seg;     /* [n_entity_rows + 1] */
+  const int32_t* entity_contrib; /* [entity_seg[n]] */
+  int32_t n_relation_rows;
+  const int32_t* relation_rows;
+  const int32_t* relation_seg;
+  const int32_t* relation_contrib;
+} ngdb_step_plan;
+
+typedef struct ngdb_ctx ngdb_ctx;
+typedef struct ngdb_plan ngdb_plan;
+
+const char* ngdb_last_error(void);
+
+/* Context: device memory for params + Adam state + arena; one CUDA stream. */
+int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out);
+int ngdb_ctx_destroy(ngdb_ctx* ctx);
+int ngdb_ctx_desc(const ngdb_ctx* ctx, ngdb_model_desc* out);
+
+/* Parameter registry (SPEC.md:337-352 GqeParams/Q2bParams/BetaParams/FusionParams).
+ * Names: see DESIGN.md §3.1. Prefix "m:" / "v:" selects Adam moments, "g:" the
+ * gradient of the last step (dense: accumulated; sparse: reduced touched rows,
+ * only when ngdb_set_debug(ctx, 1)). Synchronous. */
+int ngdb_param_count(ngdb_ctx* ctx, int32_t* n);
+int ngdb_param_info(ngdb_ctx* ctx, int32_t index, const char** name, int64_t* rows,
+                    int64_t* cols, int32_t* sparse);
+int ngdb_param_upload(ngdb_ctx* ctx, const char* name, const float* host, int64_t n);
+int ngdb_param_download(ngdb_ctx* ctx, const char* name, float* host, int64_t n);
+int ngdb_semantic_upload(ngdb_ctx* ctx, const float* host, int64_t n); /* frozen PTE store */
+int ngdb_set_debug(ngdb_ctx* ctx, int32_t keep_sparse_grads);
+
+/* Streaming step: packs the plan into pinned staging and issues one H2D copy. */
+int ngdb_step_begin(ngdb_ctx* ctx, const ngdb_step_plan* plan);
+/* Launch one kernel invocation of the current step (KernelRegistry fwd/bwd). */
+int ngdb_exec_pool(ngdb_ctx* ctx, const ngdb_pool_desc* pool);
+/* Sparse sorted-segment gradient reduce + touched-row Adam, then dense Adam
+ * (SPEC.md:550-558 adam_step; Alg. 1 l.21 OptimizerStep). `step` is 1-based. */
+int ngdb_optimizer_step(ngdb_ctx* ctx, int64_t step);
+/* Waits for the step; copies per-query losses (may be NULL) and the non-finite
+ * flag. */
+int ngdb_step_end(ngdb_ctx* ctx, float* per_query_loss, int32_t n_queries, double* loss_sum,
+                  int32_t* nonfinite);
+
+/* Resident plans: upload once, replay many times (benchmark / graph replay). */
+int ngdb_plan_create(ngdb_ctx* ctx, const ngdb_step_plan* plan, ngdb_plan** out);
+int ngdb_plan_run(ngdb_ctx* ctx, ngdb_plan* plan, int64_t step); /* all pools + optimizer */
+int ngdb_plan_destroy(ngdb_plan* plan);
+
+/* Device timing on the context stream (CUDA events). */
+int ngdb_sync(ngdb_ctx* ctx);
+int ngdb_timer_start(ngdb_ctx* ctx);
+int ngdb_timer_stop(ngdb_ctx* ctx, float* ms);
+/* Per-kernel-family timing: when enabled, exec/optimizer calls record CUDA
+ * events around every launch; read accumulated ms and launch counts by family. */
+int ngdb_profile_enable(ngdb_ctx* ctx, int32_t on);
+int ngdb_profile_read(ngdb_ctx* ctx, int32_t family, double* ms, int64_t* launches,
+                      double* bytes);
+int32_t ngdb_profile_families(void);
+const char* ngdb_profile_family_name(int32_t family);
+/* Kernel launches issued so far by this context (all families). */
+int64_t ngdb_launch_count(ngdb_ctx* ctx);
+/* Flush L2 by writing a buffer larger than it (timing hygiene). */
+int ngdb_flush_l2(ngdb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NGDB_CUDA_H_ */

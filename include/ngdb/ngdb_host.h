@@ -1,0 +1,77 @@
+/* ngdb_host.h — C ABI over the host C++ engine (graph, sampler, planner, trainer).
+ *
+ * The reference exposes these as C++ (kg.hpp, query.hpp, and the SPEC's sampler /
+ * scheduler / trainer modules); this flat C surface is what a foreign binding
+ * (ctypes here, see INTEGRATION.md for cgo/JNI stubs) links against. Every call
+ * returns an ngdb_status from ngdb_cuda.h; messages via ngdb_last_error().
+ */
+#ifndef NGDB_HOST_H_
+#define NGDB_HOST_H_
+
+#include <stdint.h>
+
+#include "ngdb/ngdb_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ngdb_graph ngdb_graph; /* GraphSplit (kg.hpp:72-77) */
+typedef struct ngdb_batch ngdb_batch; /* sampled training batch + negatives */
+typedef struct ngdb_step ngdb_step;   /* a planned step (trace + device plan) */
+
+/* --- knowledge graph (kg.hpp:25-89) ------------------------ */
+int ngdb_graph_synthetic(const char* shape, uint64_t seed, ngdb_graph** out);
+int ngdb_graph_from_triples(int32_t n_entities, int32_t n_relations, const int32_t* train,
+                            int64_t n_train, const int32_t* valid, int64_t n_valid,
+                            const int32_t* test, int64_t n_test, ngdb_graph** out);
+int ngdb_graph_load(const char* dir, ngdb_graph** out); /* load_graph (kg.hpp:79-81) */
+int ngdb_graph_info(const ngdb_graph* g, int32_t* n_entities, int32_t* n_relations,
+                    int64_t* n_train, int64_t* n_valid, int64_t* n_test);
+/* split: 0 train, 1 valid, 2 test; writes 3*n int32 (h, r, t) */
+int ngdb_graph_triples(const ngdb_graph* g, int32_t split, int32_t* out, int64_t n);
+/* answer_query on train (full=0) or full (full=1) graph; returns count via *n,
+ * writes up to cap ids (kg.hpp:83-85) */
+int ngdb_graph_answer(const ngdb_graph* g, int32_t full, int32_t pattern, const int32_t* anchors,
+                      const int32_t* relations, int32_t* out, int64_t cap, int64_t* n);
+int ngdb_graph_destroy(ngdb_graph* g);
+
+/* --- sampler ----------------------------------- */
+/* Samples b queries with patterns ~ weights (14, enum order) from
+ * Rng(seed).fork(tag), then negatives against full-graph answers. */
+int ngdb_batch_sample(const ngdb_graph* g, const double* pattern_weights, int32_t b,
+                      int32_t n_neg, uint64_t seed, uint64_t tag, ngdb_batch** out);
+/* Builds a batch from arrays: anchors [b][3], relations [b][4] (-1 padded). */
+int ngdb_batch_from_arrays(int32_t b, const int32_t* patterns, const int32_t* anchors,
+                           const int32_t* relations, const int32_t* positives, int32_t n_neg,
+                           const int32_t* negatives, ngdb_batch** out);
+int ngdb_batch_info(const ngdb_batch* bt, int32_t* b, int32_t* n_neg);
+int ngdb_batch_arrays(const ngdb_batch* bt, int32_t* patterns, int32_t* anchors,
+                      int32_t* relations, int32_t* positives, int32_t* negatives);
+int ngdb_batch_destroy(ngdb_batch* bt);
+
+/* --- planner (Alg. 1) ------------------------------------- */
+int ngdb_step_build(const ngdb_batch* bt, int32_t backbone, int32_t dim, int32_t b_max,
+                    int32_t semantic, ngdb_step** out);
+int ngdb_step_view(const ngdb_step* s, ngdb_step_plan* view);
+/* ExecutionTrace as JSON; with_nodes=1 includes popped node ids per record. */
+int ngdb_step_trace_json(const ngdb_step* s, int32_t with_nodes, char* buf, int64_t cap,
+                         int64_t* len);
+int ngdb_step_destroy(ngdb_step* s);
+
+/* --- parameters ------------------------------------------- */
+int ngdb_param_init(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
+                    const char* name, uint64_t seed, float* out, int64_t n);
+
+/* --- the public training call: plan + run one step on a context ----------- */
+int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t step,
+                    float* per_query_loss, double* loss_sum);
+/* Streaming run of an already built step (H2D of its plan inside the call). */
+int ngdb_run_step(ngdb_ctx* ctx, const ngdb_step* s, int64_t step, float* per_query_loss,
+                  double* loss_sum);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NGDB_HOST_H_ */

@@ -1,0 +1,164 @@
+"""ORACLE — test infrastructure only.
+
+ctypes binding of oracle/_build/liboracle.so, the independent CPU restatement of
+the reference training step (see oracle/src/oracle_internal.hpp for what pins
+it). Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
+import this package; the product never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from pathlib import Path
+
+import numpy as np
+
+_LIB = Path(__file__).resolve().parent / "_build" / "liboracle.so"
+if not _LIB.exists():
+    raise ImportError(f"{_LIB} missing: run `make -C oracle`")
+lib = C.CDLL(str(_LIB))
+
+i32, i64, u64, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+P = C.POINTER
+_SIG = {
+    "oracle_last_error": (C.c_char_p, []),
+    "oracle_rng_next": (u64, [u64, i64, i32]),
+    "oracle_rng_below": (C.c_int, [u64, P(u64), i32, i32, P(u64)]),
+    "oracle_rng_uniform": (C.c_int, [u64, i32, f64, f64, P(f64)]),
+    "oracle_rng_gaussian": (C.c_int, [u64, i32, P(f64)]),
+    "oracle_fnv1a64": (u64, [C.c_char_p, i64]),
+    "oracle_graph_create": (C.c_int, [i32, i32, P(i32), i64, P(i32), i64, P(i32), i64,
+                                      P(C.c_void_p)]),
+    "oracle_graph_answer": (C.c_int, [C.c_void_p, i32, i32, P(i32), P(i32), P(i32), i64, P(i64)]),
+    "oracle_graph_destroy": (C.c_int, [C.c_void_p]),
+    "oracle_sample_batch": (C.c_int, [C.c_void_p, P(f64), i32, i32, u64, u64, P(i32), P(i32),
+                                      P(i32), P(i32), P(i32)]),
+    "oracle_build_dag": (C.c_int, [i32, P(i32), P(i32), P(i32), P(i32), i64, P(i32), P(i32),
+                                   P(i32), i64, P(i32)]),
+    "oracle_model_create": (C.c_int, [i32, i32, i32, i32, i32, f64, f64, f64, i32,
+                                      P(C.c_void_p)]),
+    "oracle_model_init": (C.c_int, [C.c_void_p, u64]),
+    "oracle_model_set": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_float), i64]),
+    "oracle_model_get": (C.c_int, [C.c_void_p, C.c_char_p, P(f64), i64]),
+    "oracle_model_step": (C.c_int, [C.c_void_p, i32, P(i32), P(i32), P(i32), P(i32), P(i32), i32,
+                                    i64, i32, i32, i32, P(f64)]),
+    "oracle_model_trace_json": (C.c_int, [C.c_void_p, i32, C.c_char_p, i64, P(i64)]),
+    "oracle_model_destroy": (C.c_int, [C.c_void_p]),
+    "oracle_q2b_distance": (f64, [P(f64), P(f64), P(f64), i32, f64]),
+    "oracle_loss": (f64, [f64, f64, P(f64), i32]),
+}
+for _n, (_r, _a) in _SIG.items():
+    _f = getattr(lib, _n)
+    _f.restype, _f.argtypes = _r, _a
+
+BACKBONES = {"gqe": 0, "q2b": 1}
+
+
+def _p(a, t):
+    return a.ctypes.data_as(P(t))
+
+
+def _check(rc):
+    if rc != 0:
+        raise RuntimeError("oracle: " + lib.oracle_last_error().decode())
+
+
+class OracleGraph:
+    def __init__(self, n_entities, n_relations, train, valid=None, test=None):
+        def arr(x):
+            return np.ascontiguousarray(np.zeros((0, 3)) if x is None else x, dtype=np.int32)
+        tr, va, te = arr(train), arr(valid), arr(test)
+        self.n_entities = n_entities
+        self._h = C.c_void_p()
+        _check(lib.oracle_graph_create(n_entities, n_relations, _p(tr, i32), len(tr), _p(va, i32),
+                                       len(va), _p(te, i32), len(te), C.byref(self._h)))
+
+    def answer(self, pattern_idx, anchors, relations, full=False):
+        a = np.array(list(anchors) + [-1] * 3, dtype=np.int32)[:3]
+        r = np.array(list(relations) + [-1] * 4, dtype=np.int32)[:4]
+        out = np.zeros(self.n_entities, dtype=np.int32)
+        n = C.c_int64()
+        _check(lib.oracle_graph_answer(self._h, int(full), pattern_idx, _p(a, i32), _p(r, i32),
+                                       _p(out, i32), len(out), C.byref(n)))
+        return out[: n.value].copy()
+
+    def sample(self, weights, b, n_neg, seed=3, tag=0):
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        pat = np.zeros(b, np.int32)
+        anc = np.zeros((b, 3), np.int32)
+        rel = np.zeros((b, 4), np.int32)
+        pos = np.zeros(b, np.int32)
+        neg = np.zeros((b, n_neg), np.int32)
+        _check(lib.oracle_sample_batch(self._h, _p(w, f64), b, n_neg, seed, tag, _p(pat, i32),
+                                       _p(anc, i32), _p(rel, i32), _p(pos, i32), _p(neg, i32)))
+        return pat, anc, rel, pos, neg
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.oracle_graph_destroy(self._h)
+
+
+def build_dag(patterns, anchors, relations):
+    b = len(patterns)
+    cap = 40 * b * 11
+    out = np.zeros(cap, np.int32)
+    edges = np.zeros(80 * b, np.int32)
+    n, nf, ne = C.c_int32(), C.c_int32(), C.c_int32()
+    pa = [np.ascontiguousarray(x, dtype=np.int32) for x in (patterns, anchors, relations)]
+    _check(lib.oracle_build_dag(b, _p(pa[0], i32), _p(pa[1], i32), _p(pa[2], i32), _p(out, i32),
+                                cap, C.byref(n), C.byref(nf), _p(edges, i32), len(edges),
+                                C.byref(ne)))
+    return out[: n.value * 11].reshape(n.value, 11), nf.value, edges[: 2 * ne.value].reshape(-1, 2)
+
+
+class OracleModel:
+    def __init__(self, backbone, n_entities, n_relations, dim, n_neg, gamma=12.0,
+                 alpha_box=0.02, lr=1e-4, precision=64):
+        self._h = C.c_void_p()
+        self.backbone, self.dim = backbone, dim
+        self.n_entities, self.n_relations = n_entities, n_relations
+        _check(lib.oracle_model_create(BACKBONES[backbone], n_entities, n_relations, dim, n_neg,
+                                       gamma, alpha_box, lr, precision, C.byref(self._h)))
+
+    def init(self, seed=2):
+        _check(lib.oracle_model_init(self._h, seed))
+
+    def set(self, name, value):
+        a = np.ascontiguousarray(value, dtype=np.float32)
+        _check(lib.oracle_model_set(self._h, name.encode(), _p(a, C.c_float), a.size))
+
+    def get(self, name, shape):
+        out = np.zeros(shape, dtype=np.float64)
+        _check(lib.oracle_model_get(self._h, name.encode(), _p(out, f64), out.size))
+        return out
+
+    def step(self, patterns, anchors, relations, positives, negatives, b_max=512, step=1,
+             executor=0, adam=0, eager=True):
+        b = len(patterns)
+        arrs = [np.ascontiguousarray(x, dtype=np.int32)
+                for x in (patterns, anchors, relations, positives, negatives)]
+        losses = np.zeros(b, np.float64)
+        _check(lib.oracle_model_step(self._h, b, *[_p(x, i32) for x in arrs], b_max, step,
+                                     executor, adam, int(eager), _p(losses, f64)))
+        return losses
+
+    def trace(self, with_nodes=False):
+        n = C.c_int64()
+        _check(lib.oracle_model_trace_json(self._h, int(with_nodes), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib.oracle_model_trace_json(self._h, int(with_nodes), buf, n.value + 1, C.byref(n)))
+        return json.loads(buf.value.decode())
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.oracle_model_destroy(self._h)
+
+
+def q2b_distance(v, c, o, alpha=0.02):
+    v, c, o = (np.ascontiguousarray(x, dtype=np.float64) for x in (v, c, o))
+    return lib.oracle_q2b_distance(_p(v, f64), _p(c, f64), _p(o, f64), len(v), alpha)
+
+
+def loss(gamma, d_pos, d_neg):
+    dn = np.ascontiguousarray(d_neg, dtype=np.float64)
+    return lib.oracle_loss(gamma, d_pos, _p(dn, f64), len(dn))

@@ -1,0 +1,64 @@
+/* ORACLE C ABI — test infrastructure only (tests/, __graft_entry__.smoke(),
+ * bench.py's CPU-baseline leg). Never linked into the product library.
+ * All calls return 0 on success, nonzero on error (message: oracle_last_error). */
+#ifndef NGDB_ORACLE_H_
+#define NGDB_ORACLE_H_
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* oracle_last_error(void);
+
+/* RNG restatement (for golden-vector tests) */
+uint64_t oracle_rng_next(uint64_t seed, int64_t fork_tag, int32_t skip);
+int oracle_rng_below(uint64_t seed, const uint64_t* ns, int32_t count, int32_t reps, uint64_t* out);
+int oracle_rng_uniform(uint64_t seed, int32_t n, double lo, double hi, double* out);
+int oracle_rng_gaussian(uint64_t seed, int32_t n, double* out);
+uint64_t oracle_fnv1a64(const char* s, int64_t n);
+
+/* graph: triples as [n][3] (h, r, t) */
+int oracle_graph_create(int32_t n_entities, int32_t n_relations, const int32_t* train,
+                        int64_t n_train, const int32_t* valid, int64_t n_valid,
+                        const int32_t* test, int64_t n_test, void** out);
+int oracle_graph_answer(void* g, int32_t full, int32_t pattern, const int32_t* anchors,
+                        const int32_t* relations, int32_t* out, int64_t cap, int64_t* n);
+int oracle_graph_destroy(void* g);
+
+/* sampler: Rng(seed).fork(tag); outputs anchors [b][3], relations [b][4] (-1 pad) */
+int oracle_sample_batch(void* g, const double* weights, int32_t b, int32_t n_neg, uint64_t seed,
+                        uint64_t tag, int32_t* patterns, int32_t* anchors, int32_t* relations,
+                        int32_t* positives, int32_t* negatives);
+
+/* DAG node table of a batch: per node (kind, bwd, n_in, in0, in1, in2, payload, query,
+ * mirror, consumer, slot) as 11 int32; returns node count via *n and fwd count *nf */
+int oracle_build_dag(int32_t b, const int32_t* patterns, const int32_t* anchors,
+                     const int32_t* relations, int32_t* out, int64_t cap, int32_t* n, int32_t* nf,
+                     int32_t* edges, int64_t edge_cap, int32_t* n_edges);
+
+/* model: precision 64 or 32 */
+int oracle_model_create(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
+                        int32_t n_neg, double gamma, double alpha_box, double lr,
+                        int32_t precision, void** out);
+int oracle_model_init(void* m, uint64_t seed);
+int oracle_model_set(void* m, const char* name, const float* data, int64_t n);
+/* name may carry "g:" (last step gradient), "m:" or "v:" (Adam moments) */
+int oracle_model_get(void* m, const char* name, double* out, int64_t n);
+/* one training step; executor 0 = Alg. 1 scheduled, 1 = sequential reference;
+ * adam 0 = lazy touched rows, 1 = dense, -1 = no optimizer step */
+int oracle_model_step(void* m, int32_t b, const int32_t* patterns, const int32_t* anchors,
+                      const int32_t* relations, const int32_t* positives,
+                      const int32_t* negatives, int32_t b_max, int64_t step, int32_t executor,
+                      int32_t adam, int32_t eager, double* losses);
+int oracle_model_trace_json(void* m, int32_t with_nodes, char* buf, int64_t cap, int64_t* len);
+int oracle_model_destroy(void* m);
+
+/* scalar kernels for the SPEC known-answer tests */
+double oracle_q2b_distance(const double* v, const double* c, const double* o, int32_t d,
+                           double alpha);
+double oracle_loss(double gamma, double d_pos, const double* d_neg, int32_t k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

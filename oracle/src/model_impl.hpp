@@ -1,0 +1,683 @@
+// ORACLE (test infrastructure only). Literal Alg. 1 executor with a refcounted
+// arena and per-node f64/f32 kernels.
+//
+//   executor      Alg. 1; select_pool Eq. 4 + ledger tie rules
+//                 (SPEC.md:463-471, 499-500, 510); pop_cardinality_classes
+//                 (SPEC.md:481-489); release Eq. 7
+//   arena         alloc/release with size-class free list
+//   kernels       GQE SPEC.md:359-376; Q2B SPEC.md:377-385; union SPEC.md:404-412;
+//                 loss SPEC.md:541-549 with psi per SPEC.md:431
+//   adam          SPEC.md:550-558 (dense) and the lazy touched-row variant (A-9)
+// Every kernel runs node by node (the "looped" form); batching only changes
+// which nodes run together, never the arithmetic of one node.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <stdexcept>
+
+#include "oracle_internal.hpp"
+
+namespace oracle {
+
+template <class R>
+struct Model {
+  int backbone = 0;  // 0 GQE, 1 Q2B
+  int ne = 0, nr = 0, d = 0, k = 0;
+  double gamma = 12.0, alpha = 0.02, lr = 1e-4, b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  int wq = 0, ew = 0, rw = 0;
+  std::vector<std::string> names;
+  std::map<std::string, std::pair<int64_t, int64_t>> shape;
+  std::map<std::string, bool> sparse;
+  std::map<std::string, std::vector<R>> P, M, V, G;  // G: dense grads (all params, zero-filled)
+  std::set<int> touchedE, touchedR;
+  std::vector<R> losses;
+  OTrace trace;
+  int trace_elem_bytes = 4;
+
+  void setup(int bb, int ne_, int nr_, int d_, int k_) {
+    backbone = bb;
+    ne = ne_;
+    nr = nr_;
+    d = d_;
+    k = k_;
+    wq = bb == 0 ? d : 2 * d;
+    ew = d;
+    rw = bb == 1 ? 2 * d : d;
+    auto add = [&](const std::string& n, int64_t r, int64_t c, bool sp) {
+      names.push_back(n);
+      shape[n] = {r, c};
+      sparse[n] = sp;
+      P[n].assign(r * c, R(0));
+      M[n].assign(r * c, R(0));
+      V[n].assign(r * c, R(0));
+      G[n].assign(r * c, R(0));
+    };
+    add("entity", ne, ew, true);
+    add("relation", nr, rw, true);
+    if (bb == 0) {
+      add("int_w1", d, d, false);
+      add("int_w2", d, d, false);
+    } else {
+      for (const char* n : {"att_w1", "att_b1", "att_w2", "att_b2", "off_w1", "off_b1", "off_w2",
+                            "off_b2"})
+        add(n, std::string(n).find("_b") != std::string::npos ? 1 : d, d, false);
+    }
+  }
+
+  // ---- distances -----------------------------------------------------------
+  static R sgn(R x) { return R((x > 0) - (x < 0)); }
+  R dist(const R* q, const R* v) const {
+    R s = 0;
+    if (backbone == 0) {
+      for (int e = 0; e < d; ++e) s += std::fabs(v[e] - q[e]);
+    } else {
+      for (int e = 0; e < d; ++e) {
+        const R a = std::fabs(v[e] - q[e]), o = q[d + e];
+        s += std::max(a - o, R(0)) + R(alpha) * std::min(a, o);
+      }
+    }
+    return s;
+  }
+  // gq += coef * d dist / dq ; gv += coef * d dist / dv
+  void ddist(const R* q, const R* v, R coef, R* gq, R* gv) const {
+    for (int e = 0; e < d; ++e) {
+      const R delta = v[e] - q[e];
+      if (backbone == 0) {
+        if (gq) gq[e] -= coef * sgn(delta);
+        if (gv) gv[e] += coef * sgn(delta);
+      } else {
+        const R a = std::fabs(delta), o = q[d + e];
+        const R dv = (a > o ? R(1) : R(alpha)) * sgn(delta);
+        if (gq) {
+          gq[e] -= coef * dv;
+          gq[d + e] += coef * (a > o ? R(alpha) - R(1) : R(0));
+        }
+        if (gv) gv[e] += coef * dv;
+      }
+    }
+  }
+  static R softplus(R x) { return x > 0 ? x + std::log1p(std::exp(-x)) : std::log1p(std::exp(x)); }
+  static R sigm(R x) { return x >= 0 ? R(1) / (R(1) + std::exp(-x)) : std::exp(x) / (R(1) + std::exp(x)); }
+  // loss of one query from its 1+k distances; coef = dloss/dd
+  R loss_and_coef(const R* dists, R* coef) const {
+    R l = softplus(dists[0] - R(gamma));
+    coef[0] = sigm(dists[0] - R(gamma));
+    for (int j = 1; j <= k; ++j) {
+      l += softplus(R(gamma) - dists[j]) / R(k);
+      coef[j] = -sigm(R(gamma) - dists[j]) / R(k);
+    }
+    return l;
+  }
+  const R* erow(int e) const { return &P.at("entity")[(int64_t)e * ew]; }
+  R* gerow(int e) {
+    touchedE.insert(e);
+    return &G["entity"][(int64_t)e * ew];
+  }
+  R* grrow(int r) {
+    touchedR.insert(r);
+    return &G["relation"][(int64_t)r * rw];
+  }
+
+  // ---- small dense algebra: y = W x (+b), W [out][in] -----------------------
+  void mv(const std::string& w, const std::string& b, const R* x, R* y) const {
+    const auto& W = P.at(w);
+    for (int o = 0; o < d; ++o) {
+      R s = b.empty() ? R(0) : P.at(b)[o];
+      for (int i = 0; i < d; ++i) s += W[(int64_t)o * d + i] * x[i];
+      y[o] = s;
+    }
+  }
+  // gx += W^T gy ; gW += gy x^T ; gb += gy
+  void mv_bwd(const std::string& w, const std::string& b, const R* x, const R* gy, R* gx) {
+    const auto& W = P.at(w);
+    auto& gW = G[w];
+    for (int o = 0; o < d; ++o) {
+      if (!b.empty()) G[b][o] += gy[o];
+      for (int i = 0; i < d; ++i) {
+        gW[(int64_t)o * d + i] += gy[o] * x[i];
+        if (gx) gx[i] += W[(int64_t)o * d + i] * gy[o];
+      }
+    }
+  }
+
+  // ---- per-node kernels ------------------------------------------------------
+  void gqe_inter_fwd(const std::vector<const R*>& xs, R* out, std::vector<R>* mh = nullptr) {
+    const int kk = (int)xs.size();
+    std::vector<R> m(d, R(0)), h(d), a(d);
+    for (int e = 0; e < d; ++e) {
+      for (int l = 0; l < kk; ++l) m[e] += xs[l][e];
+      m[e] /= R(kk);
+    }
+    mv("int_w1", "", m.data(), h.data());
+    for (int e = 0; e < d; ++e) a[e] = std::max(h[e], R(0));
+    if (out) mv("int_w2", "", a.data(), out);
+    if (mh) {
+      mh->assign(m.begin(), m.end());
+      mh->insert(mh->end(), h.begin(), h.end());
+    }
+  }
+  void gqe_inter_bwd(const std::vector<const R*>& xs, const R* gy, R* gout) {
+    const int kk = (int)xs.size();
+    std::vector<R> mh;
+    gqe_inter_fwd(xs, nullptr, &mh);
+    const R* m = mh.data();
+    const R* h = mh.data() + d;
+    std::vector<R> a(d), ga(d, R(0)), gm(d, R(0));
+    for (int e = 0; e < d; ++e) a[e] = std::max(h[e], R(0));
+    mv_bwd("int_w2", "", a.data(), gy, ga.data());
+    for (int e = 0; e < d; ++e) ga[e] = h[e] > 0 ? ga[e] : R(0);
+    mv_bwd("int_w1", "", m, ga.data(), gm.data());
+    for (int l = 0; l < kk; ++l)
+      for (int e = 0; e < d; ++e) gout[(int64_t)l * d + e] = gm[e] / R(kk);
+  }
+
+  struct Q2bInter {
+    std::vector<std::vector<R>> z, s, p;
+    std::vector<R> lm, u;
+  };
+  void q2b_inter_fwd(const std::vector<const R*>& xs, R* out, Q2bInter* keep = nullptr) {
+    const int kk = (int)xs.size();
+    Q2bInter t;
+    t.z.assign(kk, std::vector<R>(d));
+    t.s.assign(kk, std::vector<R>(d));
+    t.p.assign(kk, std::vector<R>(d));
+    t.lm.assign(d, R(0));
+    t.u.assign(d, R(0));
+    std::vector<R> rz(d);
+    for (int l = 0; l < kk; ++l) {
+      mv("att_w1", "att_b1", xs[l], t.z[l].data());
+      for (int e = 0; e < d; ++e) rz[e] = std::max(t.z[l][e], R(0));
+      mv("att_w2", "att_b2", rz.data(), t.s[l].data());
+      mv("off_w1", "off_b1", xs[l] + d, t.p[l].data());
+      for (int e = 0; e < d; ++e) t.lm[e] += std::max(t.p[l][e], R(0)) / R(kk);
+    }
+    mv("off_w2", "off_b2", t.lm.data(), t.u.data());
+    if (out) {
+      for (int e = 0; e < d; ++e) {
+        R mx = t.s[0][e];
+        for (int l = 1; l < kk; ++l) mx = std::max(mx, t.s[l][e]);
+        R z = 0, c = 0, mn = xs[0][d + e];
+        for (int l = 0; l < kk; ++l) z += std::exp(t.s[l][e] - mx);
+        for (int l = 0; l < kk; ++l) {
+          c += std::exp(t.s[l][e] - mx) / z * xs[l][e];
+          mn = std::min(mn, xs[l][d + e]);
+        }
+        out[e] = c;
+        out[d + e] = mn * sigm(t.u[e]);
+      }
+    }
+    if (keep) *keep = t;
+  }
+  void q2b_inter_bwd(const std::vector<const R*>& xs, const R* gy, R* gout) {
+    const int kk = (int)xs.size();
+    Q2bInter t;
+    q2b_inter_fwd(xs, nullptr, &t);
+    std::vector<std::vector<R>> gs(kk, std::vector<R>(d)), gp(kk, std::vector<R>(d));
+    std::vector<R> gu(d);
+    for (int l = 0; l < kk; ++l)
+      for (int e = 0; e < 2 * d; ++e) gout[(int64_t)l * 2 * d + e] = R(0);
+    for (int e = 0; e < d; ++e) {
+      const R gC = gy[e], gO = gy[d + e];
+      R mx = t.s[0][e];
+      for (int l = 1; l < kk; ++l) mx = std::max(mx, t.s[l][e]);
+      std::vector<R> w(kk);
+      R z = 0;
+      for (int l = 0; l < kk; ++l) z += (w[l] = std::exp(t.s[l][e] - mx));
+      R dot = 0;
+      for (int l = 0; l < kk; ++l) {
+        w[l] /= z;
+        dot += w[l] * gC * xs[l][e];
+      }
+      int arg = 0;
+      for (int l = 1; l < kk; ++l)
+        if (xs[l][d + e] < xs[arg][d + e]) arg = l;
+      const R mn = xs[arg][d + e];
+      const R gate = sigm(t.u[e]);
+      for (int l = 0; l < kk; ++l) {
+        gs[l][e] = w[l] * (gC * xs[l][e] - dot);
+        gout[(int64_t)l * 2 * d + e] += gC * w[l];
+      }
+      gout[(int64_t)arg * 2 * d + d + e] += gO * gate;
+      gu[e] = gO * mn * gate * (R(1) - gate);
+    }
+    std::vector<R> glm(d, R(0));
+    mv_bwd("off_w2", "off_b2", t.lm.data(), gu.data(), glm.data());
+    std::vector<R> tmp(d), rz(d);
+    for (int l = 0; l < kk; ++l) {
+      for (int e = 0; e < d; ++e) gp[l][e] = t.p[l][e] > 0 ? glm[e] / R(kk) : R(0);
+      std::fill(tmp.begin(), tmp.end(), R(0));
+      mv_bwd("off_w1", "off_b1", xs[l] + d, gp[l].data(), tmp.data());
+      for (int e = 0; e < d; ++e) gout[(int64_t)l * 2 * d + d + e] += tmp[e];
+      for (int e = 0; e < d; ++e) rz[e] = std::max(t.z[l][e], R(0));
+      std::fill(tmp.begin(), tmp.end(), R(0));
+      mv_bwd("att_w2", "att_b2", rz.data(), gs[l].data(), tmp.data());
+      for (int e = 0; e < d; ++e) tmp[e] = t.z[l][e] > 0 ? tmp[e] : R(0);
+      std::vector<R> gc(d, R(0));
+      mv_bwd("att_w1", "att_b1", xs[l], tmp.data(), gc.data());
+      for (int e = 0; e < d; ++e) gout[(int64_t)l * 2 * d + e] += gc[e];
+    }
+  }
+
+  // ---- Adam -------------------------------------------------
+  void adam(int64_t step, bool lazy) {
+    const double bc1 = 1.0 - std::pow(b1, (double)step), bc2 = 1.0 - std::pow(b2, (double)step);
+    auto upd = [&](const std::string& n, int64_t lo, int64_t hi) {
+      auto &p = P[n], &m = M[n], &v = V[n], &g = G[n];
+      for (int64_t i = lo; i < hi; ++i) {
+        m[i] = R(b1) * m[i] + R(1 - b1) * g[i];
+        v[i] = R(b2) * v[i] + R(1 - b2) * g[i] * g[i];
+        const R mh = m[i] / R(bc1), vh = v[i] / R(bc2);
+        p[i] -= R(lr) * mh / (std::sqrt(vh) + R(eps));
+      }
+    };
+    for (const auto& n : names) {
+      if (sparse[n] && lazy) {
+        const std::set<int>& rows = n == "entity" ? touchedE : touchedR;
+        const int64_t c = shape[n].second;
+        for (int r : rows) upd(n, r * c, (r + 1) * c);
+      } else {
+        upd(n, 0, (int64_t)P[n].size());
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Executor: Alg. 1 with the refcount arena (or a naive sequential order).
+template <class R>
+struct Exec {
+  Model<R>& md;
+  const ODag& g;
+  const std::vector<int>& cand;  // [B][1+k]
+  int b_max;
+  bool eager;
+
+  struct Buf {
+    std::vector<R> v;
+    int rc = 0;
+    int64_t bytes = 0;
+  };
+  std::vector<Buf> bufs;
+  std::map<int64_t, std::vector<int>> free_list;
+  int64_t live = 0, peak = 0, hits = 0;
+  std::vector<int> T, Gt;
+  std::vector<int> release_step, last_use;
+  int cur_step = 0;
+
+  int width_fwd(int n) const {
+    const int kd = g.nodes[n].kind;
+    if (kd == K_SCORE || kd == K_UNION) return md.k + 1;
+    if (kd == K_LOSS) return 1;
+    return md.wq;
+  }
+  int alloc(int64_t elems, int rc) {
+    if (rc < 1) throw std::runtime_error("ZeroRefcount");
+    const int64_t bytes = elems * md.trace_elem_bytes;
+    int h;
+    auto& fl = free_list[bytes];
+    if (!fl.empty()) {
+      h = fl.back();
+      fl.pop_back();
+      ++hits;
+    } else {
+      h = (int)bufs.size();
+      bufs.push_back({});
+      release_step.push_back(-1);
+      last_use.push_back(-1);
+    }
+    bufs[h].v.assign(elems, R(0));  // zero-initialised buffer
+    bufs[h].rc = rc;
+    bufs[h].bytes = bytes;
+    live += bytes;
+    peak = std::max(peak, live);
+    release_step[h] = -1;
+    return h;
+  }
+  int64_t release(int h) {
+    Buf& b = bufs[h];
+    if (b.rc <= 0) throw std::runtime_error("DoubleRelease");
+    last_use[h] = cur_step;
+    if (--b.rc > 0) return 0;
+    release_step[h] = cur_step;
+    if (!eager) return 0;
+    free_list[b.bytes].push_back(h);
+    live -= b.bytes;
+    return b.bytes;
+  }
+  R* t(int h) {
+    if (bufs[h].rc <= 0) throw std::runtime_error("use after reclamation");
+    return bufs[h].v.data();
+  }
+  std::vector<int> consumed(int o) const {
+    const ONode& x = g.nodes[o];
+    std::vector<int> out;
+    if (!x.bwd) {
+      for (int i : x.in) out.push_back(T[i]);
+    } else {
+      const ONode& m = g.nodes[x.mirror];
+      if (m.consumer >= 0) out.push_back(Gt[g.nf + m.consumer]);
+      for (int i : m.in) out.push_back(T[i]);
+      out.push_back(T[x.mirror]);
+    }
+    return out;
+  }
+  void allocate(int o) {
+    const ONode& x = g.nodes[o];
+    if (!x.bwd) {
+      T[o] = alloc(width_fwd(o), x.consumer >= 0 ? 3 : 1);
+    } else {
+      const ONode& m = g.nodes[x.mirror];
+      if (m.in.empty()) return;
+      Gt[o] = alloc((int64_t)m.in.size() * width_fwd(m.in[0]), (int)m.in.size());
+    }
+  }
+  bool union_loss(const ONode& x) const { return g.nodes[x.in[0]].kind == K_UNION; }
+  const int* cands(int q) const { return &cand[(size_t)q * (md.k + 1)]; }
+
+  void run_fwd(int o) {
+    const ONode& x = g.nodes[o];
+    R* out = t(T[o]);
+    const int d = md.d;
+    switch (x.kind) {
+      case K_EMB: {
+        const R* e = md.erow(x.payload);
+        for (int i = 0; i < md.ew; ++i) out[i] = e[i];
+        break;
+      }
+      case K_PROJ: {
+        const R* in = t(T[x.in[0]]);
+        const R* r = &md.P["relation"][(int64_t)x.payload * md.rw];
+        for (int i = 0; i < d; ++i) out[i] = in[i] + r[i];
+        if (md.backbone == 1)
+          for (int i = 0; i < d; ++i) out[d + i] = std::max(in[d + i] + r[d + i], R(0));
+        break;
+      }
+      case K_NEG: {
+        const R* in = t(T[x.in[0]]);
+        for (int i = 0; i < md.wq; ++i) out[i] = i < d ? -in[i] : in[i];
+        break;
+      }
+      case K_INTER: {
+        std::vector<const R*> xs;
+        for (int i : x.in) xs.push_back(t(T[i]));
+        if (md.backbone == 0) md.gqe_inter_fwd(xs, out);
+        else md.q2b_inter_fwd(xs, out);
+        break;
+      }
+      case K_SCORE: {
+        const R* q = t(T[x.in[0]]);
+        const int* c = cands(x.query);
+        for (int j = 0; j <= md.k; ++j) out[j] = md.dist(q, md.erow(c[j]));
+        break;
+      }
+      case K_UNION: {
+        for (int j = 0; j <= md.k; ++j) {
+          R best = t(T[x.in[0]])[j];
+          for (size_t l = 1; l < x.in.size(); ++l) best = std::min(best, t(T[x.in[l]])[j]);
+          out[j] = best;
+        }
+        break;
+      }
+      case K_LOSS: {
+        std::vector<R> dists(md.k + 1), coef(md.k + 1);
+        if (union_loss(x)) {
+          const R* in = t(T[x.in[0]]);
+          for (int j = 0; j <= md.k; ++j) dists[j] = in[j];
+        } else {
+          const R* q = t(T[x.in[0]]);
+          const int* c = cands(x.query);
+          for (int j = 0; j <= md.k; ++j) dists[j] = md.dist(q, md.erow(c[j]));
+        }
+        out[0] = md.loss_and_coef(dists.data(), coef.data());
+        md.losses[x.query] = out[0];
+        break;
+      }
+      default: throw std::runtime_error("MissingKernel");
+    }
+  }
+
+  void run_bwd(int o) {
+    const ONode& x = g.nodes[o];
+    const ONode& m = g.nodes[x.mirror];
+    const int d = md.d;
+    const R* gin = m.consumer >= 0
+                       ? t(Gt[g.nf + m.consumer]) + (int64_t)m.slot * width_fwd(x.mirror)
+                       : nullptr;
+    R* gout = Gt[o] >= 0 ? t(Gt[o]) : nullptr;
+    switch (m.kind) {
+      case K_EMB: {
+        R* ge = md.gerow(m.payload);
+        for (int i = 0; i < md.ew; ++i) ge[i] += gin[i];
+        break;
+      }
+      case K_PROJ: {
+        const R* in = t(T[m.in[0]]);
+        const R* r = &md.P["relation"][(int64_t)m.payload * md.rw];
+        R* gr = md.grrow(m.payload);
+        for (int i = 0; i < d; ++i) {
+          gout[i] = gin[i];
+          gr[i] += gin[i];
+        }
+        if (md.backbone == 1)
+          for (int i = 0; i < d; ++i) {
+            const R gv = in[d + i] + r[d + i] > 0 ? gin[d + i] : R(0);
+            gout[d + i] = gv;
+            gr[d + i] += gv;
+          }
+        break;
+      }
+      case K_NEG:
+        for (int i = 0; i < md.wq; ++i) gout[i] = i < d ? -gin[i] : gin[i];
+        break;
+      case K_INTER: {
+        std::vector<const R*> xs;
+        for (int i : m.in) xs.push_back(t(T[i]));
+        if (md.backbone == 0) md.gqe_inter_bwd(xs, gin, gout);
+        else md.q2b_inter_bwd(xs, gin, gout);
+        break;
+      }
+      case K_SCORE: {
+        const R* q = t(T[m.in[0]]);
+        const int* c = cands(m.query);
+        for (int i = 0; i < md.wq; ++i) gout[i] = R(0);
+        for (int j = 0; j <= md.k; ++j) md.ddist(q, md.erow(c[j]), gin[j], gout, md.gerow(c[j]));
+        break;
+      }
+      case K_UNION: {
+        const int kk = (int)m.in.size();
+        for (int j = 0; j <= md.k; ++j) {
+          int arg = 0;
+          for (int l = 1; l < kk; ++l)
+            if (t(T[m.in[l]])[j] < t(T[m.in[arg]])[j]) arg = l;
+          for (int l = 0; l < kk; ++l) gout[(int64_t)l * (md.k + 1) + j] = l == arg ? gin[j] : R(0);
+        }
+        break;
+      }
+      case K_LOSS: {
+        std::vector<R> dists(md.k + 1), coef(md.k + 1);
+        if (union_loss(m)) {
+          const R* in = t(T[m.in[0]]);
+          for (int j = 0; j <= md.k; ++j) dists[j] = in[j];
+          md.loss_and_coef(dists.data(), coef.data());
+          for (int j = 0; j <= md.k; ++j) gout[j] = coef[j];
+        } else {
+          const R* q = t(T[m.in[0]]);
+          const int* c = cands(m.query);
+          for (int j = 0; j <= md.k; ++j) dists[j] = md.dist(q, md.erow(c[j]));
+          md.loss_and_coef(dists.data(), coef.data());
+          for (int i = 0; i < md.wq; ++i) gout[i] = R(0);
+          for (int j = 0; j <= md.k; ++j) md.ddist(q, md.erow(c[j]), coef[j], gout, md.gerow(c[j]));
+        }
+        break;
+      }
+      default: throw std::runtime_error("MissingKernel");
+    }
+  }
+
+  void exec(int o) {
+    if (g.nodes[o].bwd) run_bwd(o);
+    else run_fwd(o);
+  }
+
+  // sequential=true: naive topological order (fwd ids ascending, then bwd ids
+  // descending), one node per step — the SPEC's sequential reference executor.
+  OTrace run(bool sequential) {
+    const int n = (int)g.nodes.size();
+    T.assign(g.nf, -1);
+    Gt.assign(n, -1);
+    std::vector<std::vector<int>> succ(n);
+    std::vector<int> indeg(n, 0);
+    for (auto [u, v] : g.edges) {
+      succ[u].push_back(v);
+      ++indeg[v];
+    }
+    OTrace tr;
+    tr.total_nodes = n;
+    auto do_batch = [&](const std::vector<int>& batch, int kind, bool bwd, int cycle) {
+      ORecord rec;
+      rec.step = cur_step;
+      rec.cycle = cycle;
+      rec.kind = kind;
+      rec.bwd = bwd;
+      rec.batch = (int)batch.size();
+      rec.nodes = batch;
+      for (int o : batch)
+        for (int h : consumed(o)) t(h);  // every input must still be referenced
+      for (int o : batch) allocate(o);
+      if (kind == K_INTER || kind == K_UNION) {
+        for (int kk = 2; kk <= 3; ++kk) {
+          std::vector<int> cls;
+          for (int o : batch)
+            if ((int)g.nodes[g.nodes[o].bwd ? g.nodes[o].mirror : o].in.size() == kk) cls.push_back(o);
+          if (cls.empty()) continue;
+          rec.classes.push_back({kk, (int)cls.size()});
+          for (int o : cls) exec(o);
+          ++tr.invocations;
+        }
+      } else {
+        for (int o : batch) exec(o);
+        ++tr.invocations;
+      }
+      std::vector<int> newly;
+      for (int o : batch) {
+        for (int h : consumed(o)) rec.reclaimed += release(h);
+        for (int s : succ[o])
+          if (--indeg[s] == 0) newly.push_back(s);
+      }
+      rec.live = live;
+      tr.recs.push_back(rec);
+      ++cur_step;
+      return newly;
+    };
+
+    if (sequential) {
+      std::vector<int> order;
+      for (int i = 0; i < g.nf; ++i) order.push_back(i);
+      for (int i = n - 1; i >= g.nf; --i) order.push_back(i);
+      for (int o : order) do_batch({o}, g.nodes[o].kind, g.nodes[o].bwd, cur_step);
+    } else {
+      // pools keyed by type index = bwd*8 + kind; FIFO of (node, enqueue cycle)
+      std::vector<std::deque<std::pair<int, int>>> pools(16);
+      std::vector<int> ready;
+      for (int i = 0; i < n; ++i)
+        if (indeg[i] == 0) ready.push_back(i);
+      int executed = 0, cycle = 0;
+      while (executed < n) {
+        for (int v : ready) pools[g.nodes[v].bwd * 8 + g.nodes[v].kind].push_back({v, cycle});
+        ready.clear();
+        // Eq. 4: rho = |pool| / B_max; argmax, then oldest head, then type order
+        int best = -1;
+        for (int p = 0; p < 16; ++p) {
+          if (pools[p].empty()) continue;
+          if (best < 0) {
+            best = p;
+            continue;
+          }
+          const double rp = (double)pools[p].size() / b_max, rb = (double)pools[best].size() / b_max;
+          if (rp > rb || (rp == rb && pools[p].front().second < pools[best].front().second))
+            best = p;
+        }
+        if (best < 0) throw std::runtime_error("AllPoolsEmpty");
+        const int size_at_selection = (int)pools[best].size();
+        const int drains = (size_at_selection + b_max - 1) / b_max;
+        int left = size_at_selection;
+        for (int dr = 0; dr < drains; ++dr) {
+          std::vector<int> batch;
+          for (int i = 0; i < std::min(left, b_max); ++i) {
+            batch.push_back(pools[best].front().first);
+            pools[best].pop_front();
+          }
+          left -= (int)batch.size();
+          auto nw = do_batch(batch, best % 8, best >= 8, cycle);
+          ready.insert(ready.end(), nw.begin(), nw.end());
+          executed += (int)batch.size();
+        }
+        ++cycle;
+      }
+    }
+    tr.peak = peak;
+    tr.hits = hits;
+    tr.release_step = release_step;
+    tr.last_consumer_step = last_use;
+    return tr;
+  }
+};
+
+// ---- explicit instantiation helpers used by capi.cpp ------------------------
+template <class R>
+OTrace o_train_step(Model<R>& md, const ODag& g, const std::vector<int>& cand, int b_max,
+                    bool eager, bool sequential, int64_t step, bool lazy, bool apply_adam) {
+  for (auto& kv : md.G) std::fill(kv.second.begin(), kv.second.end(), R(0));
+  md.touchedE.clear();
+  md.touchedR.clear();
+  int nq = 0;
+  for (const auto& n : g.nodes) nq = std::max(nq, n.query + 1);
+  md.losses.assign(nq, R(0));
+  Exec<R> ex{md, g, cand, b_max, eager};
+  OTrace tr = ex.run(sequential);
+  if (apply_adam) md.adam(step, lazy);
+  md.trace = tr;
+  return tr;
+}
+
+template struct Model<double>;
+template struct Model<float>;
+template OTrace o_train_step<double>(Model<double>&, const ODag&, const std::vector<int>&, int,
+                                     bool, bool, int64_t, bool, bool);
+template OTrace o_train_step<float>(Model<float>&, const ODag&, const std::vector<int>&, int, bool,
+                                    bool, int64_t, bool, bool);
+
+std::string OTrace::json(bool with_nodes) const {
+  static const char* kNames[8] = {"EmbedAnchor", "FuseSemantic", "Project", "Negate",
+                                  "Intersect",   "Score",        "UnionScore", "Loss"};
+  std::string s = "{\"invocations\":" + std::to_string(invocations) +
+                  ",\"peak_bytes\":" + std::to_string(peak) +
+                  ",\"free_list_hits\":" + std::to_string(hits) +
+                  ",\"total_nodes\":" + std::to_string(total_nodes) + ",\"records\":[";
+  for (size_t i = 0; i < recs.size(); ++i) {
+    const ORecord& r = recs[i];
+    if (i) s += ",";
+    s += "{\"step\":" + std::to_string(r.step) + ",\"cycle\":" + std::to_string(r.cycle) +
+         ",\"kind\":\"" + kNames[r.kind] + "\",\"dir\":\"" + (r.bwd ? "bwd" : "fwd") +
+         "\",\"batch\":" + std::to_string(r.batch) + ",\"classes\":[";
+    for (size_t c = 0; c < r.classes.size(); ++c)
+      s += (c ? "," : "") + std::string("[") + std::to_string(r.classes[c].first) + "," +
+           std::to_string(r.classes[c].second) + "]";
+    s += "],\"bytes_reclaimed\":" + std::to_string(r.reclaimed) +
+         ",\"live_bytes\":" + std::to_string(r.live);
+    if (with_nodes) {
+      s += ",\"nodes\":[";
+      for (size_t k = 0; k < r.nodes.size(); ++k) s += (k ? "," : "") + std::to_string(r.nodes[k]);
+      s += "]";
+    }
+    s += "}";
+  }
+  s += "],\"release_step\":[";
+  for (size_t i = 0; i < release_step.size(); ++i)
+    s += (i ? "," : "") + std::to_string(release_step[i]);
+  s += "]}";
+  return s;
+}
+
+}  // namespace oracle

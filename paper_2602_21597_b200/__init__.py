@@ -1,0 +1,10 @@
+"""B200-native operator-level training step of NGDB-Zoo (arxiv 2602.21597).
+
+Host C++ Max-Fillness planner + hand-written sm_100a kernels behind the C ABI in
+include/ngdb/ngdb_cuda.h. See DESIGN.md.
+"""
+from .engine import (BACKBONES, OP_KINDS, PATTERNS, PATTERN_ARITY, Batch, BatchArrays, Engine,
+                     Graph, PlannedStep, init_params, param_specs, pattern_weights)
+
+__all__ = ["BACKBONES", "OP_KINDS", "PATTERNS", "PATTERN_ARITY", "Batch", "BatchArrays", "Engine",
+           "Graph", "PlannedStep", "init_params", "param_specs", "pattern_weights"]

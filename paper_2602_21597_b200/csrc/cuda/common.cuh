@@ -1,0 +1,116 @@
+// Shared device-side definitions for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ngdb/ngdb_cuda.h"
+
+namespace ngdb_dev {
+
+constexpr int kMaxDenseTensors = 16;
+
+// Named dense tensors (offsets into the flat dense parameter buffer).
+enum DenseName : int {
+  // GQE intersection MLP: out = W2 relu(W1 mean_k x)
+  GQE_W1 = 0, GQE_W2 = 1,
+  // Q2B attention (centre) and DeepSets (offset) MLPs
+  Q2B_A1 = 0, Q2B_A1B = 1, Q2B_A2 = 2, Q2B_A2B = 3,
+  Q2B_V1 = 4, Q2B_V1B = 5, Q2B_V2 = 6, Q2B_V2B = 7,
+};
+
+// Everything a kernel needs, passed by value.
+struct DevArgs {
+  int32_t backbone;
+  int32_t dim;        // d
+  int32_t wq;         // query width (GQE d, Q2B 2d)
+  int32_t ent_w;      // entity row width
+  int32_t rel_w;      // relation row width
+  int32_t ncand;      // 1 + K
+  int32_t n_neg;
+  int32_t n_entities;
+  int32_t n_relations;
+  float gamma;
+  float alpha_box;
+  float* arena;
+  const ngdb_node_desc* nodes;
+  const int32_t* cand;
+  float* ent;         // entity table
+  float* rel;         // relation table
+  float* dense;       // flat dense params
+  float* dense_g;     // flat dense grads
+  int64_t dense_off[kMaxDenseTensors];
+  float* qbuf;        // [S][wq]   query copy per score slot
+  float* dqbuf;       // [S][wq]   dL/dq per score slot (fused Loss)
+  float* coefbuf;     // [S][ncand] dL/dd per score slot and candidate
+  float* ddbuf;       // [B][ncand] dL/dd per union query
+  float* agbuf;       // [A][ent_w] anchor gradient rows
+  float* rgbuf;       // [P][rel_w] relation gradient rows
+  float* loss_out;    // [B]
+  int32_t* flags;     // [0] non-finite loss, [1] index out of range
+  float* scratch;     // GEMM scratch
+  int64_t scratch_cap;
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 ldg4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+// streaming load: do not allocate in L1 (each row is touched once per kernel)
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float sgnf(float x) { return (x > 0.f) - (x < 0.f); }
+// numerically stable softplus and logistic
+__device__ __forceinline__ float softplusf(float x) {
+  return x > 0.f ? x + log1pf(expf(-x)) : log1pf(expf(x));
+}
+__device__ __forceinline__ float sigmoidf(float x) {
+  return x >= 0.f ? 1.f / (1.f + expf(-x)) : expf(x) / (1.f + expf(x));
+}
+
+}  // namespace ngdb_dev
+
+// ---- launchers (defined in the k_*.cu files) --------------------------------
+namespace ngdb_dev {
+struct LaunchCtx {
+  cudaStream_t stream;
+  int num_sms;
+};
+// rows.cu
+int launch_embed(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
+int launch_project(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
+int launch_negate(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
+int launch_union(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc);
+int launch_loss_bwd(const DevArgs& a, int first, int n, const LaunchCtx& lc);
+// score.cu
+int launch_loss_fwd(const DevArgs& a, int first, int n, const LaunchCtx& lc);
+int launch_score(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
+// intersect.cu
+int launch_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc);
+// optim.cu
+struct SparseTable {
+  float* w; float* m; float* v; float* dbg_g;
+  int32_t width;
+  int32_t n_rows;
+  const int32_t* rows; const int32_t* seg; const int32_t* contrib;
+};
+int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, float lr, float b1,
+                               float b2, float eps, float bc1, float bc2, const LaunchCtx& lc);
+int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, float lr, float b1,
+                                 float b2, float eps, float bc1, float bc2, const LaunchCtx& lc);
+int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, float lr, float b1,
+                       float b2, float eps, float bc1, float bc2, const LaunchCtx& lc);
+}  // namespace ngdb_dev

@@ -1,0 +1,837 @@
+// Device context and the C ABI of include/ngdb/ngdb_cuda.h.
+//
+// The context owns all device memory for one training run on one GPU:
+// parameters + Adam moments, the activation arena
+// whose slots the host planner assigned (SPEC.md:257-330 as static offsets),
+// the per-step gradient staging buffers, and the packed step plans. All launches
+// go to one non-blocking stream; a step issues no host synchronisation until
+// ngdb_step_end.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace ngdb_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Fail{NGDB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+#define CK(x) ck((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return NGDB_OK;
+  } catch (const Fail& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return NGDB_ERR_CUDA;
+  }
+}
+
+enum Family : int {
+  F_EMBED = 0, F_PROJECT, F_NEGATE, F_INTERSECT, F_SCORE, F_UNION, F_LOSS_FWD, F_LOSS_BWD,
+  F_OPT_ENTITY, F_OPT_RELATION, F_OPT_DENSE, F_COUNT
+};
+const char* kFamilyNames[F_COUNT] = {"embed",     "project",   "negate",      "intersect",
+                                     "score",     "union",     "loss_fwd",    "loss_bwd",
+                                     "opt_entity", "opt_relation", "opt_dense"};
+
+struct Param {
+  std::string name;
+  int64_t rows = 0, cols = 0;
+  bool sparse = false;
+  float *w = nullptr, *m = nullptr, *v = nullptr, *g = nullptr;
+  int64_t n() const { return rows * cols; }
+};
+
+template <class T>
+T* dmalloc(int64_t count) {
+  void* p = nullptr;
+  if (count <= 0) count = 1;
+  CK(cudaMalloc(&p, static_cast<size_t>(count) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+// Packed plan blob: [nodes][cand][erows][eseg][econ][rrows][rseg][rcon] (int32)
+struct PlanLayout {
+  int64_t nodes, cand, erows, eseg, econ, rrows, rseg, rcon, total;
+  static int64_t up4(int64_t x) { return (x + 3) / 4 * 4; }
+  explicit PlanLayout(const ngdb_step_plan& p) {
+    int64_t o = 0;
+    nodes = o; o += up4(int64_t(p.n_nodes) * 8);
+    cand = o; o += up4(int64_t(p.n_queries) * p.n_candidates);
+    erows = o; o += up4(p.n_entity_rows);
+    eseg = o; o += up4(p.n_entity_rows + 1);
+    econ = o; o += up4(p.n_entity_rows ? p.entity_seg[p.n_entity_rows] : 0);
+    rrows = o; o += up4(p.n_relation_rows);
+    rseg = o; o += up4(p.n_relation_rows + 1);
+    rcon = o; o += up4(p.n_relation_rows ? p.relation_seg[p.n_relation_rows] : 0);
+    total = o;
+  }
+};
+
+void pack_plan(const ngdb_step_plan& p, const PlanLayout& L, int32_t* dst) {
+  std::memcpy(dst + L.nodes, p.nodes, sizeof(ngdb_node_desc) * p.n_nodes);
+  std::memcpy(dst + L.cand, p.candidates, sizeof(int32_t) * int64_t(p.n_queries) * p.n_candidates);
+  if (p.n_entity_rows) {
+    std::memcpy(dst + L.erows, p.entity_rows, sizeof(int32_t) * p.n_entity_rows);
+    std::memcpy(dst + L.eseg, p.entity_seg, sizeof(int32_t) * (p.n_entity_rows + 1));
+    std::memcpy(dst + L.econ, p.entity_contrib, sizeof(int32_t) * p.entity_seg[p.n_entity_rows]);
+  }
+  if (p.n_relation_rows) {
+    std::memcpy(dst + L.rrows, p.relation_rows, sizeof(int32_t) * p.n_relation_rows);
+    std::memcpy(dst + L.rseg, p.relation_seg, sizeof(int32_t) * (p.n_relation_rows + 1));
+    std::memcpy(dst + L.rcon, p.relation_contrib,
+                sizeof(int32_t) * p.relation_seg[p.n_relation_rows]);
+  }
+}
+
+// Host-side summary of a plan the device copy needs for dispatch.
+struct PlanMeta {
+  std::vector<ngdb_pool_desc> pools;
+  int32_t n_queries = 0, n_candidates = 0, n_nodes = 0;
+  int32_t n_score = 0, n_anchor = 0, n_project = 0;
+  int32_t n_erows = 0, n_rrows = 0, n_econ = 0, n_rcon = 0;
+  int64_t arena_elems = 0;
+  std::vector<int32_t> node_counts_by_kind;  // for algorithmic-byte accounting
+};
+
+PlanMeta meta_of(const ngdb_step_plan& p) {
+  PlanMeta m;
+  m.pools.assign(p.pools, p.pools + p.n_pools);
+  m.n_queries = p.n_queries;
+  m.n_candidates = p.n_candidates;
+  m.n_nodes = p.n_nodes;
+  m.n_score = p.n_score_slots;
+  m.n_anchor = p.n_anchor_slots;
+  m.n_project = p.n_project_slots;
+  m.n_erows = p.n_entity_rows;
+  m.n_rrows = p.n_relation_rows;
+  m.n_econ = p.n_entity_rows ? p.entity_seg[p.n_entity_rows] : 0;
+  m.n_rcon = p.n_relation_rows ? p.relation_seg[p.n_relation_rows] : 0;
+  m.arena_elems = p.arena_elems;
+  return m;
+}
+
+void validate_plan(const ngdb_step_plan& p) {
+  if (p.n_queries < 0 || p.n_nodes < 0 || p.n_pools < 0 || p.n_candidates < 2)
+    throw Fail{NGDB_ERR_SHAPE_MISMATCH, "invalid plan sizes"};
+  for (int i = 0; i < p.n_pools; ++i) {
+    const ngdb_pool_desc& d = p.pools[i];
+    if (d.first < 0 || d.count < 0 || d.first + d.count > p.n_nodes)
+      throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "pool descriptor out of range"};
+  }
+}
+
+}  // namespace
+
+struct ngdb_plan {
+  int32_t* blob = nullptr;
+  PlanLayout layout{ngdb_step_plan{}};
+  PlanMeta meta;
+};
+
+struct ngdb_ctx {
+  ngdb_model_desc desc{};
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::vector<Param> params;
+  int ent_idx = -1, rel_idx = -1;
+  float *dense_w = nullptr, *dense_m = nullptr, *dense_v = nullptr, *dense_g = nullptr;
+  int64_t dense_n = 0;
+  int64_t dense_off[kMaxDenseTensors] = {};
+  float* sem = nullptr;
+  int64_t sem_n = 0;
+  // per-step staging
+  float *qbuf = nullptr, *dqbuf = nullptr, *coefbuf = nullptr, *ddbuf = nullptr, *agbuf = nullptr,
+        *rgbuf = nullptr, *loss_out = nullptr;
+  int32_t* flags = nullptr;
+  int64_t cap_score = 0, cap_anchor = 0, cap_project = 0, cap_queries = 0, cap_cand = 0;
+  float* scratch = nullptr;
+  int64_t scratch_cap = 0;
+  float* arena = nullptr;
+  int64_t arena_cap = 0;
+  // streaming plans: double-buffered pinned staging + device blobs
+  int32_t* staging[2] = {nullptr, nullptr};
+  int64_t staging_cap[2] = {0, 0};
+  cudaEvent_t staged[2] = {nullptr, nullptr};
+  ngdb_plan stream_plan[2];
+  int64_t stream_cap[2] = {0, 0};
+  int cur = 0;
+  ngdb_plan* active = nullptr;
+  bool debug = false;
+  // timing / accounting
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  bool profiling = false;
+  struct Rec { int fam; cudaEvent_t a, b; double bytes; int launches; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> event_pool;
+  double fam_ms[F_COUNT] = {}, fam_bytes[F_COUNT] = {};
+  int64_t fam_launches[F_COUNT] = {};
+  int64_t launches = 0;
+  float* l2_flush = nullptr;
+  int64_t l2_flush_bytes = 0;
+
+  Param* find(const std::string& name) {
+    for (auto& p : params)
+      if (p.name == name) return &p;
+    return nullptr;
+  }
+  int32_t query_width() const {
+    return desc.backbone == NGDB_GQE ? desc.dim : 2 * desc.dim;
+  }
+  cudaEvent_t take_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+  void drain_profile() {
+    if (recs.empty()) return;
+    CK(cudaStreamSynchronize(stream));
+    for (auto& r : recs) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      fam_ms[r.fam] += ms;
+      fam_bytes[r.fam] += r.bytes;
+      fam_launches[r.fam] += r.launches;
+      event_pool.push_back(r.a);
+      event_pool.push_back(r.b);
+    }
+    recs.clear();
+  }
+};
+
+namespace {
+
+void add_param(ngdb_ctx* c, const char* name, int64_t rows, int64_t cols, bool sparse) {
+  Param p;
+  p.name = name;
+  p.rows = rows;
+  p.cols = cols;
+  p.sparse = sparse;
+  c->params.push_back(p);
+}
+
+void ensure_f(float*& p, int64_t& cap, int64_t need) {
+  if (need <= cap) return;
+  if (p) CK(cudaFree(p));
+  cap = std::max<int64_t>(need, cap + cap / 4);
+  p = dmalloc<float>(cap);
+}
+
+void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
+  const int64_t wq = c->query_width();
+  const int64_t ew = c->params[c->ent_idx].cols, rw = c->params[c->rel_idx].cols;
+  bool grow = m.n_score > c->cap_score || m.n_anchor > c->cap_anchor ||
+              m.n_project > c->cap_project || m.n_queries > c->cap_queries ||
+              m.n_candidates != c->cap_cand;
+  if (grow) {
+    CK(cudaStreamSynchronize(c->stream));
+    auto realloc_f = [&](float*& p, int64_t n) {
+      if (p) CK(cudaFree(p));
+      p = dmalloc<float>(n);
+    };
+    c->cap_score = std::max<int64_t>(m.n_score, c->cap_score);
+    c->cap_anchor = std::max<int64_t>(m.n_anchor, c->cap_anchor);
+    c->cap_project = std::max<int64_t>(m.n_project, c->cap_project);
+    c->cap_queries = std::max<int64_t>(m.n_queries, c->cap_queries);
+    c->cap_cand = m.n_candidates;
+    realloc_f(c->qbuf, c->cap_score * wq);
+    realloc_f(c->dqbuf, c->cap_score * wq);
+    realloc_f(c->coefbuf, c->cap_score * c->cap_cand);
+    realloc_f(c->ddbuf, c->cap_queries * c->cap_cand);
+    realloc_f(c->agbuf, c->cap_anchor * ew);
+    realloc_f(c->rgbuf, c->cap_project * rw);
+    realloc_f(c->loss_out, c->cap_queries);
+  }
+  if (m.arena_elems > c->arena_cap) {
+    CK(cudaStreamSynchronize(c->stream));
+    ensure_f(c->arena, c->arena_cap, m.arena_elems + 64);
+  }
+}
+
+DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
+  DevArgs a{};
+  a.backbone = c->desc.backbone;
+  a.dim = c->desc.dim;
+  a.wq = c->query_width();
+  a.ent_w = static_cast<int32_t>(c->params[c->ent_idx].cols);
+  a.rel_w = static_cast<int32_t>(c->params[c->rel_idx].cols);
+  a.ncand = p->meta.n_candidates;
+  a.n_neg = c->desc.n_neg;
+  a.n_entities = c->desc.n_entities;
+  a.n_relations = c->desc.n_relations;
+  a.gamma = c->desc.gamma;
+  a.alpha_box = c->desc.alpha_box;
+  a.arena = c->arena;
+  a.nodes = reinterpret_cast<const ngdb_node_desc*>(p->blob + p->layout.nodes);
+  a.cand = p->blob + p->layout.cand;
+  a.ent = c->params[c->ent_idx].w;
+  a.rel = c->params[c->rel_idx].w;
+  a.dense = c->dense_w;
+  a.dense_g = c->dense_g;
+  for (int i = 0; i < kMaxDenseTensors; ++i) a.dense_off[i] = c->dense_off[i];
+  a.qbuf = c->qbuf;
+  a.dqbuf = c->dqbuf;
+  a.coefbuf = c->coefbuf;
+  a.ddbuf = c->ddbuf;
+  a.agbuf = c->agbuf;
+  a.rgbuf = c->rgbuf;
+  a.loss_out = c->loss_out;
+  a.flags = c->flags;
+  a.scratch = c->scratch;
+  a.scratch_cap = c->scratch_cap;
+  return a;
+}
+
+// Algorithmic bytes of one invocation (unique bytes a kernel must
+// move; L2 re-reads inside a kernel are not counted).
+double pool_bytes(const ngdb_ctx* c, const ngdb_pool_desc& d, int ncand) {
+  const double wq = c->query_width() * 4.0, ew = c->params[c->ent_idx].cols * 4.0,
+               rw = c->params[c->rel_idx].cols * 4.0, n = d.count, k = d.k;
+  switch (d.kind) {
+    case NGDB_OP_EMBED_ANCHOR: return n * (d.dir == 0 ? ew + wq : 2 * ew) + n * 32;
+    case NGDB_OP_PROJECT: return n * (d.dir == 0 ? (wq + rw + wq) : (2 * wq + 2 * rw)) + n * 32;
+    case NGDB_OP_NEGATE: return n * 2 * wq + n * 32;
+    case NGDB_OP_INTERSECT: return n * (k + 1) * wq * (d.dir == 0 ? 1 : 2) + n * 32;
+    case NGDB_OP_UNION_SCORE: return n * (k + 1) * ncand * 4.0 * (d.dir == 0 ? 1 : 2) + n * 32;
+    case NGDB_OP_SCORE:
+      return n * (ncand * (ew + 4) + wq * (d.dir == 0 ? 2 : 2) + ncand * 4.0) + n * 32;
+    case NGDB_OP_LOSS:
+      if (d.dir == 1) return n * 2 * wq + n * 32;
+      return n * (ncand * (ew + 4) + 3 * wq + ncand * 4.0 + 8) + n * 32;
+  }
+  return 0.0;
+}
+
+int family_of(int kind, int dir) {
+  switch (kind) {
+    case NGDB_OP_EMBED_ANCHOR: return F_EMBED;
+    case NGDB_OP_PROJECT: return F_PROJECT;
+    case NGDB_OP_NEGATE: return F_NEGATE;
+    case NGDB_OP_INTERSECT: return F_INTERSECT;
+    case NGDB_OP_SCORE: return F_SCORE;
+    case NGDB_OP_UNION_SCORE: return F_UNION;
+    case NGDB_OP_LOSS: return dir == 0 ? F_LOSS_FWD : F_LOSS_BWD;
+  }
+  return F_EMBED;
+}
+
+template <class Launch>
+void timed(ngdb_ctx* c, int fam, double bytes, Launch&& launch) {
+  if (!c->profiling) {
+    c->launches += launch();
+    return;
+  }
+  cudaEvent_t a = c->take_event(), b = c->take_event();
+  CK(cudaEventRecord(a, c->stream));
+  const int n = launch();
+  CK(cudaEventRecord(b, c->stream));
+  c->launches += n;
+  c->recs.push_back({fam, a, b, bytes, n});
+}
+
+void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d) {
+  if (d.count <= 0) return;
+  const DevArgs a = make_args(c, p);
+  const LaunchCtx lc{c->stream, c->num_sms};
+  const int fam = family_of(d.kind, d.dir);
+  const double bytes = c->profiling ? pool_bytes(c, d, p->meta.n_candidates) : 0.0;
+  switch (d.kind) {
+    case NGDB_OP_EMBED_ANCHOR:
+      timed(c, fam, bytes, [&] { return launch_embed(a, d.dir, d.first, d.count, lc); });
+      break;
+    case NGDB_OP_PROJECT:
+      timed(c, fam, bytes, [&] { return launch_project(a, d.dir, d.first, d.count, lc); });
+      break;
+    case NGDB_OP_NEGATE:
+      timed(c, fam, bytes, [&] { return launch_negate(a, d.dir, d.first, d.count, lc); });
+      break;
+    case NGDB_OP_INTERSECT:
+      if (d.k < 2 || d.k > 3) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "intersect cardinality"};
+      timed(c, fam, bytes, [&] { return launch_intersect(a, d.dir, d.k, d.first, d.count, lc); });
+      break;
+    case NGDB_OP_SCORE:
+      timed(c, fam, bytes, [&] { return launch_score(a, d.dir, d.first, d.count, lc); });
+      break;
+    case NGDB_OP_UNION_SCORE:
+      if (d.k < 2 || d.k > 3) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "union cardinality"};
+      timed(c, fam, bytes, [&] { return launch_union(a, d.dir, d.k, d.first, d.count, lc); });
+      break;
+    case NGDB_OP_LOSS:
+      if (d.dir == 0)
+        timed(c, fam, bytes, [&] { return launch_loss_fwd(a, d.first, d.count, lc); });
+      else
+        timed(c, fam, bytes, [&] { return launch_loss_bwd(a, d.first, d.count, lc); });
+      break;
+    default:
+      throw Fail{NGDB_ERR_MISSING_KERNEL,
+                 "no kernel registered for operator kind " + std::to_string(d.kind)};
+  }
+  CK(cudaGetLastError());
+}
+
+void begin_step_device(ngdb_ctx* c) {
+  CK(cudaMemsetAsync(c->flags, 0, 4 * sizeof(int32_t), c->stream));
+  if (c->dense_n) CK(cudaMemsetAsync(c->dense_g, 0, c->dense_n * sizeof(float), c->stream));
+  if (c->debug)
+    for (auto& p : c->params)
+      if (p.sparse && p.g) CK(cudaMemsetAsync(p.g, 0, p.n() * sizeof(float), c->stream));
+}
+
+void optimizer(ngdb_ctx* c, const ngdb_plan* p, int64_t step) {
+  if (step < 1) throw Fail{NGDB_ERR_CONFIG, "optimizer step must be >= 1"};
+  const ngdb_model_desc& d = c->desc;
+  const float bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta1), double(step)));
+  const float bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta2), double(step)));
+  const DevArgs a = make_args(c, p);
+  const LaunchCtx lc{c->stream, c->num_sms};
+  Param& ent = c->params[c->ent_idx];
+  Param& rel = c->params[c->rel_idx];
+  SparseTable te{ent.w, ent.m, ent.v, c->debug ? ent.g : nullptr, static_cast<int32_t>(ent.cols),
+                 p->meta.n_erows, p->blob + p->layout.erows, p->blob + p->layout.eseg,
+                 p->blob + p->layout.econ};
+  SparseTable tr{rel.w, rel.m, rel.v, c->debug ? rel.g : nullptr, static_cast<int32_t>(rel.cols),
+                 p->meta.n_rrows, p->blob + p->layout.rrows, p->blob + p->layout.rseg,
+                 p->blob + p->layout.rcon};
+  const double eb = 6.0 * p->meta.n_erows * ent.cols * 4 + 8.0 * p->meta.n_econ +
+                    p->meta.n_score * double(c->query_width()) * 4;
+  timed(c, F_OPT_ENTITY, eb, [&] {
+    return launch_sparse_adam_entity(a, te, d.lr, d.beta1, d.beta2, d.eps_adam, bc1, bc2, lc);
+  });
+  const double rb = 6.0 * p->meta.n_rrows * rel.cols * 4 + p->meta.n_rcon * (4.0 + rel.cols * 4);
+  timed(c, F_OPT_RELATION, rb, [&] {
+    return launch_sparse_adam_relation(a, tr, d.lr, d.beta1, d.beta2, d.eps_adam, bc1, bc2, lc);
+  });
+  timed(c, F_OPT_DENSE, 28.0 * c->dense_n, [&] {
+    return launch_dense_adam(c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->dense_n, d.lr,
+                             d.beta1, d.beta2, d.eps_adam, bc1, bc2, lc);
+  });
+  CK(cudaGetLastError());
+}
+
+void upload_plan(ngdb_ctx* c, const ngdb_step_plan& plan, ngdb_plan* dst, int64_t& dst_cap,
+                 int32_t* staging, cudaStream_t s) {
+  PlanLayout L(plan);
+  if (L.total > dst_cap) {
+    if (dst->blob) {
+      CK(cudaStreamSynchronize(c->stream));
+      CK(cudaFree(dst->blob));
+    }
+    dst_cap = std::max<int64_t>(L.total, dst_cap + dst_cap / 4);
+    dst->blob = dmalloc<int32_t>(dst_cap);
+  }
+  pack_plan(plan, L, staging);
+  CK(cudaMemcpyAsync(dst->blob, staging, L.total * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  dst->layout = L;
+  dst->meta = meta_of(plan);
+}
+
+}  // namespace
+
+namespace ngdb_internal {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace ngdb_internal
+
+extern "C" {
+
+const char* ngdb_last_error(void) { return g_last_error.c_str(); }
+
+int ngdb_ctx_desc(const ngdb_ctx* c, ngdb_model_desc* out) {
+  if (!c || !out) return NGDB_ERR_CONFIG;
+  *out = c->desc;
+  return NGDB_OK;
+}
+
+int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
+  ngdb_ctx* c = nullptr;
+  int rc = guarded([&] {
+    if (!desc || !out) throw Fail{NGDB_ERR_CONFIG, "null argument"};
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0)
+      throw Fail{NGDB_ERR_NO_DEVICE, "no CUDA device visible (the sm_100a kernels have no CPU fallback)"};
+    if (device < 0 || device >= n_dev) throw Fail{NGDB_ERR_NO_DEVICE, "device index out of range"};
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw Fail{NGDB_ERR_NO_DEVICE, std::string("device is sm_") + std::to_string(prop.major) +
+                                         std::to_string(prop.minor) + ", kernels are built for sm_100a"};
+    const ngdb_model_desc& d = *desc;
+    if (d.backbone != NGDB_GQE && d.backbone != NGDB_Q2B)
+      throw Fail{NGDB_ERR_MISSING_KERNEL, "backbone not built into this library"};
+    if (d.dim <= 0 || d.dim % 4 != 0 || d.dim > 1024)
+      throw Fail{NGDB_ERR_CONFIG, "dim must be a positive multiple of 4, <= 1024"};
+    if (d.n_neg < 1 || d.n_neg + 1 > 1024) throw Fail{NGDB_ERR_CONFIG, "n_neg out of range"};
+    if (d.n_entities < 1 || d.n_relations < 1) throw Fail{NGDB_ERR_CONFIG, "empty tables"};
+    if (d.semantic_dim != 0) throw Fail{NGDB_ERR_MISSING_KERNEL, "FuseSemantic not built in this round"};
+    c = new ngdb_ctx();
+    c->desc = d;
+    if (c->desc.max_batch <= 0) c->desc.max_batch = 512;
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    const int64_t D = d.dim;
+    if (d.backbone == NGDB_GQE) {
+      add_param(c, "entity", d.n_entities, D, true);
+      add_param(c, "relation", d.n_relations, D, true);
+      add_param(c, "int_w1", D, D, false);
+      add_param(c, "int_w2", D, D, false);
+    } else {
+      add_param(c, "entity", d.n_entities, D, true);
+      add_param(c, "relation", d.n_relations, 2 * D, true);
+      add_param(c, "att_w1", D, D, false);
+      add_param(c, "att_b1", 1, D, false);
+      add_param(c, "att_w2", D, D, false);
+      add_param(c, "att_b2", 1, D, false);
+      add_param(c, "off_w1", D, D, false);
+      add_param(c, "off_b1", 1, D, false);
+      add_param(c, "off_w2", D, D, false);
+      add_param(c, "off_b2", 1, D, false);
+    }
+    // dense tensors share one flat buffer (one Adam launch, one memset)
+    int64_t off = 0;
+    int dense_i = 0;
+    for (auto& p : c->params) {
+      if (p.sparse) continue;
+      c->dense_off[dense_i++] = off;
+      off += (p.n() + 3) / 4 * 4;
+    }
+    c->dense_n = off;
+    if (off) {
+      c->dense_w = dmalloc<float>(off);
+      c->dense_m = dmalloc<float>(off);
+      c->dense_v = dmalloc<float>(off);
+      c->dense_g = dmalloc<float>(off);
+      CK(cudaMemset(c->dense_w, 0, off * 4));
+      CK(cudaMemset(c->dense_m, 0, off * 4));
+      CK(cudaMemset(c->dense_v, 0, off * 4));
+      CK(cudaMemset(c->dense_g, 0, off * 4));
+    }
+    dense_i = 0;
+    for (size_t i = 0; i < c->params.size(); ++i) {
+      Param& p = c->params[i];
+      if (p.sparse) {
+        p.w = dmalloc<float>(p.n());
+        p.m = dmalloc<float>(p.n());
+        p.v = dmalloc<float>(p.n());
+        CK(cudaMemset(p.w, 0, p.n() * 4));
+        CK(cudaMemset(p.m, 0, p.n() * 4));
+        CK(cudaMemset(p.v, 0, p.n() * 4));
+        if (p.name == "entity") c->ent_idx = static_cast<int>(i);
+        if (p.name == "relation") c->rel_idx = static_cast<int>(i);
+      } else {
+        const int64_t o = c->dense_off[dense_i++];
+        p.w = c->dense_w + o;
+        p.m = c->dense_m + o;
+        p.v = c->dense_v + o;
+        p.g = c->dense_g + o;
+      }
+    }
+    c->flags = reinterpret_cast<int32_t*>(dmalloc<float>(4));
+    CK(cudaMemset(c->flags, 0, 16));
+    const int64_t mb = c->desc.max_batch;
+    c->scratch_cap = d.backbone == NGDB_GQE ? 4 * mb * D : (9 * 3 * mb + 4 * mb) * D;
+    c->scratch = dmalloc<float>(c->scratch_cap);
+    CK(cudaEventCreate(&c->t0));
+    CK(cudaEventCreate(&c->t1));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->staged[i], cudaEventDisableTiming));
+    *out = c;
+  });
+  if (rc != NGDB_OK && c) ngdb_ctx_destroy(c);
+  return rc;
+}
+
+int ngdb_ctx_destroy(ngdb_ctx* c) {
+  if (!c) return NGDB_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& p : c->params)
+    if (p.sparse) {
+      cudaFree(p.w);
+      cudaFree(p.m);
+      cudaFree(p.v);
+      if (p.g) cudaFree(p.g);
+    }
+  for (float* p : {c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->sem, c->qbuf, c->dqbuf,
+                   c->coefbuf, c->ddbuf, c->agbuf, c->rgbuf, c->loss_out, c->scratch, c->arena,
+                   c->l2_flush})
+    if (p) cudaFree(p);
+  if (c->flags) cudaFree(c->flags);
+  for (int i = 0; i < 2; ++i) {
+    if (c->staging[i]) cudaFreeHost(c->staging[i]);
+    if (c->stream_plan[i].blob) cudaFree(c->stream_plan[i].blob);
+    if (c->staged[i]) cudaEventDestroy(c->staged[i]);
+  }
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return NGDB_OK;
+}
+
+int ngdb_param_count(ngdb_ctx* c, int32_t* n) {
+  return guarded([&] { *n = static_cast<int32_t>(c->params.size()); });
+}
+
+int ngdb_param_info(ngdb_ctx* c, int32_t i, const char** name, int64_t* rows, int64_t* cols,
+                    int32_t* sparse) {
+  return guarded([&] {
+    if (i < 0 || i >= static_cast<int32_t>(c->params.size()))
+      throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "param index"};
+    const Param& p = c->params[i];
+    if (name) *name = p.name.c_str();
+    if (rows) *rows = p.rows;
+    if (cols) *cols = p.cols;
+    if (sparse) *sparse = p.sparse ? 1 : 0;
+  });
+}
+
+namespace {
+float* resolve(ngdb_ctx* c, const char* name, int64_t n) {
+  std::string s(name);
+  char kind = 'w';
+  if (s.size() > 2 && s[1] == ':') {
+    kind = s[0];
+    s = s.substr(2);
+  }
+  Param* p = c->find(s);
+  if (!p) throw Fail{NGDB_ERR_CONFIG, "unknown parameter " + s};
+  if (n != p->n()) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "size mismatch for " + s};
+  switch (kind) {
+    case 'w': return p->w;
+    case 'm': return p->m;
+    case 'v': return p->v;
+    case 'g':
+      if (!p->g) throw Fail{NGDB_ERR_CONFIG, "gradient of " + s + " not kept (ngdb_set_debug)"};
+      return p->g;
+  }
+  throw Fail{NGDB_ERR_CONFIG, "unknown parameter prefix"};
+}
+}  // namespace
+
+int ngdb_param_upload(ngdb_ctx* c, const char* name, const float* host, int64_t n) {
+  return guarded([&] {
+    float* dst = resolve(c, name, n);
+    CK(cudaMemcpyAsync(dst, host, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ngdb_param_download(ngdb_ctx* c, const char* name, float* host, int64_t n) {
+  return guarded([&] {
+    const float* src = resolve(c, name, n);
+    CK(cudaMemcpyAsync(host, src, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ngdb_semantic_upload(ngdb_ctx* c, const float* host, int64_t n) {
+  return guarded([&] {
+    if (c->desc.semantic_dim <= 0) throw Fail{NGDB_ERR_CONFIG, "context has no semantic store"};
+    if (n != int64_t(c->desc.n_entities) * c->desc.semantic_dim)
+      throw Fail{NGDB_ERR_SHAPE_MISMATCH, "semantic store size"};
+    if (!c->sem) c->sem = dmalloc<float>(n);
+    CK(cudaMemcpy(c->sem, host, n * 4, cudaMemcpyHostToDevice));
+  });
+}
+
+int ngdb_set_debug(ngdb_ctx* c, int32_t keep) {
+  return guarded([&] {
+    c->debug = keep != 0;
+    if (c->debug)
+      for (auto& p : c->params)
+        if (p.sparse && !p.g) {
+          p.g = dmalloc<float>(p.n());
+          CK(cudaMemset(p.g, 0, p.n() * 4));
+        }
+  });
+}
+
+int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
+  return guarded([&] {
+    validate_plan(*plan);
+    const int i = c->cur;
+    c->cur ^= 1;
+    const PlanLayout L(*plan);
+    // the pinned buffer may still be feeding the H2D copy issued two steps ago
+    CK(cudaEventSynchronize(c->staged[i]));
+    if (L.total > c->staging_cap[i]) {
+      if (c->staging[i]) CK(cudaFreeHost(c->staging[i]));
+      c->staging_cap[i] = L.total + L.total / 4;
+      void* p = nullptr;
+      CK(cudaMallocHost(&p, c->staging_cap[i] * sizeof(int32_t)));
+      c->staging[i] = static_cast<int32_t*>(p);
+    }
+    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->stream);
+    CK(cudaEventRecord(c->staged[i], c->stream));
+    ensure_step_buffers(c, c->stream_plan[i].meta);
+    begin_step_device(c);
+    c->active = &c->stream_plan[i];
+  });
+}
+
+int ngdb_exec_pool(ngdb_ctx* c, const ngdb_pool_desc* pool) {
+  return guarded([&] {
+    if (!c->active) throw Fail{NGDB_ERR_CONFIG, "exec_pool outside a step"};
+    exec_pool(c, c->active, *pool);
+  });
+}
+
+int ngdb_optimizer_step(ngdb_ctx* c, int64_t step) {
+  return guarded([&] {
+    if (!c->active) throw Fail{NGDB_ERR_CONFIG, "optimizer_step outside a step"};
+    optimizer(c, c->active, step);
+  });
+}
+
+int ngdb_step_end(ngdb_ctx* c, float* per_query_loss, int32_t n_queries, double* loss_sum,
+                  int32_t* nonfinite) {
+  return guarded([&] {
+    if (!c->active) throw Fail{NGDB_ERR_CONFIG, "step_end outside a step"};
+    const int32_t nq = c->active->meta.n_queries;
+    std::vector<float> tmp;
+    float* dst = per_query_loss;
+    if (!dst || n_queries < nq) {
+      tmp.resize(nq);
+      dst = tmp.data();
+    }
+    int32_t flags[4] = {0, 0, 0, 0};
+    CK(cudaMemcpyAsync(dst, c->loss_out, nq * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(flags, c->flags, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->drain_profile();
+    if (loss_sum) {
+      double s = 0.0;
+      for (int32_t i = 0; i < nq; ++i) s += dst[i];
+      *loss_sum = s;
+    }
+    if (nonfinite) *nonfinite = flags[0];
+    c->active = nullptr;
+    if (flags[1]) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "embedding index out of range in plan"};
+  });
+}
+
+int ngdb_plan_create(ngdb_ctx* c, const ngdb_step_plan* plan, ngdb_plan** out) {
+  ngdb_plan* p = nullptr;
+  int rc = guarded([&] {
+    validate_plan(*plan);
+    p = new ngdb_plan();
+    const PlanLayout L(*plan);
+    std::vector<int32_t> host(L.total);
+    pack_plan(*plan, L, host.data());
+    p->blob = dmalloc<int32_t>(L.total);
+    CK(cudaMemcpy(p->blob, host.data(), L.total * sizeof(int32_t), cudaMemcpyHostToDevice));
+    p->layout = L;
+    p->meta = meta_of(*plan);
+    ensure_step_buffers(c, p->meta);
+    *out = p;
+  });
+  if (rc != NGDB_OK && p) ngdb_plan_destroy(p);
+  return rc;
+}
+
+int ngdb_plan_run(ngdb_ctx* c, ngdb_plan* p, int64_t step) {
+  return guarded([&] {
+    ensure_step_buffers(c, p->meta);
+    begin_step_device(c);
+    for (const auto& d : p->meta.pools) exec_pool(c, p, d);
+    optimizer(c, p, step);
+    c->active = p;
+  });
+}
+
+int ngdb_plan_destroy(ngdb_plan* p) {
+  if (!p) return NGDB_OK;
+  if (p->blob) cudaFree(p->blob);
+  delete p;
+  return NGDB_OK;
+}
+
+int ngdb_sync(ngdb_ctx* c) {
+  return guarded([&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+int ngdb_timer_start(ngdb_ctx* c) {
+  return guarded([&] { CK(cudaEventRecord(c->t0, c->stream)); });
+}
+
+int ngdb_timer_stop(ngdb_ctx* c, float* ms) {
+  return guarded([&] {
+    CK(cudaEventRecord(c->t1, c->stream));
+    CK(cudaEventSynchronize(c->t1));
+    CK(cudaEventElapsedTime(ms, c->t0, c->t1));
+  });
+}
+
+int ngdb_profile_enable(ngdb_ctx* c, int32_t on) {
+  return guarded([&] {
+    c->drain_profile();
+    c->profiling = on != 0;
+    for (int i = 0; i < F_COUNT; ++i) {
+      c->fam_ms[i] = 0;
+      c->fam_bytes[i] = 0;
+      c->fam_launches[i] = 0;
+    }
+  });
+}
+
+int ngdb_profile_read(ngdb_ctx* c, int32_t family, double* ms, int64_t* launches, double* bytes) {
+  return guarded([&] {
+    if (family < 0 || family >= F_COUNT) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "family"};
+    c->drain_profile();
+    if (ms) *ms = c->fam_ms[family];
+    if (launches) *launches = c->fam_launches[family];
+    if (bytes) *bytes = c->fam_bytes[family];
+  });
+}
+
+int32_t ngdb_profile_families(void) { return F_COUNT; }
+
+const char* ngdb_profile_family_name(int32_t f) {
+  return (f >= 0 && f < F_COUNT) ? kFamilyNames[f] : "?";
+}
+
+int64_t ngdb_launch_count(ngdb_ctx* c) { return c ? c->launches : 0; }
+
+int ngdb_flush_l2(ngdb_ctx* c) {
+  return guarded([&] {
+    if (!c->l2_flush) {
+      c->l2_flush_bytes = 512ll << 20;  // > 126 MB L2
+      c->l2_flush = dmalloc<float>(c->l2_flush_bytes / 4);
+    }
+    CK(cudaMemsetAsync(c->l2_flush, c->launches & 0xff, c->l2_flush_bytes, c->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// OptimizerStep (Alg. 1 l.21): sorted-segment gradient reduce fused with a
+// touched-rows-only Adam (SPEC.md:550-558 adam_step; north_star "fused Adam
+// update applied only to touched rows"; lazy semantics, SURVEY A-9), and the
+// dense Adam for MLP weights.
+//
+// Entity rows receive two kinds of contributions, listed per row in a host-
+// planned CSR (rows ascending, so the reduction order is fixed and the result
+// deterministic):
+//   anchor   (code < 0): an explicit gradient row from EmbedAnchor's mirror
+//   candidate(code >= 0): coef_j * d dist(v, q_s) / dv, recomputed here from the
+//            score slot's query copy (L2-resident) and the row itself, which
+//            this kernel reads anyway for the update. The 66k x 1600 B candidate
+//            gradient rows of a step are therefore never written to HBM.
+// HBM traffic per touched row: read theta, m, v; write theta, m, v (6 w bytes).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace ngdb_dev {
+namespace {
+
+constexpr int kWarps = 8;
+
+__device__ __forceinline__ float adam_update(float& w, float& m, float& v, float g, float lr,
+                                             float b1, float b2, float eps, float bc1, float bc2) {
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  const float mhat = m / bc1;
+  const float vhat = v / bc2;
+  w -= lr * mhat / (sqrtf(vhat) + eps);
+  return w;
+}
+
+__device__ __forceinline__ float4 adam4(float4 w, float4& m, float4& v, float4 g, float lr, float b1,
+                                        float b2, float eps, float bc1, float bc2) {
+  adam_update(w.x, m.x, v.x, g.x, lr, b1, b2, eps, bc1, bc2);
+  adam_update(w.y, m.y, v.y, g.y, lr, b1, b2, eps, bc1, bc2);
+  adam_update(w.z, m.z, v.z, g.z, lr, b1, b2, eps, bc1, bc2);
+  adam_update(w.w, m.w, v.w, g.w, lr, b1, b2, eps, bc1, bc2);
+  return w;
+}
+
+template <int BB>
+__device__ __forceinline__ float cand_grad(float v, float qc, float qo, float coef, float alpha) {
+  const float delta = v - qc;
+  if (BB == NGDB_GQE) return coef * sgnf(delta);
+  const float scale = fabsf(delta) > qo ? 1.f : alpha;
+  return coef * scale * sgnf(delta);
+}
+
+template <int BB>
+__global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, SparseTable t, float lr,
+                                                                  float b1, float b2, float eps,
+                                                                  float bc1, float bc2) {
+  const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row_idx >= t.n_rows) return;
+  const int64_t row = t.rows[row_idx];
+  const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
+  const int w4 = t.width / 4;
+  float* wp = t.w + row * t.width;
+  float* mp = t.m + row * t.width;
+  float* vp = t.v + row * t.width;
+  for (int c = lane; c < w4; c += 32) {
+    const float4 w = ld4(wp + 4 * c);
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = beg; k < end; ++k) {
+      const int32_t code = t.contrib[k];
+      if (code < 0) {
+        const float4 r = ld4(a.agbuf + static_cast<int64_t>(-code - 1) * t.width + 4 * c);
+        g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
+      } else {
+        const int s = code / a.ncand;
+        const float coef = a.coefbuf[code];
+        const float* q = a.qbuf + static_cast<int64_t>(s) * a.wq;
+        const float4 qc = ld4(q + 4 * c);
+        float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (BB == NGDB_Q2B) qo = ld4(q + a.dim + 4 * c);
+        g.x += cand_grad<BB>(w.x, qc.x, qo.x, coef, a.alpha_box);
+        g.y += cand_grad<BB>(w.y, qc.y, qo.y, coef, a.alpha_box);
+        g.z += cand_grad<BB>(w.z, qc.z, qo.z, coef, a.alpha_box);
+        g.w += cand_grad<BB>(w.w, qc.w, qo.w, coef, a.alpha_box);
+      }
+    }
+    if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g);
+    float4 m = ld4(mp + 4 * c), v = ld4(vp + 4 * c);
+    const float4 nw = adam4(w, m, v, g, lr, b1, b2, eps, bc1, bc2);
+    st4(wp + 4 * c, nw);
+    st4(mp + 4 * c, m);
+    st4(vp + 4 * c, v);
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) relation_adam_kernel(DevArgs a, SparseTable t,
+                                                                    float lr, float b1, float b2,
+                                                                    float eps, float bc1,
+                                                                    float bc2) {
+  const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row_idx >= t.n_rows) return;
+  const int64_t row = t.rows[row_idx];
+  const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
+  const int w4 = t.width / 4;
+  float* wp = t.w + row * t.width;
+  float* mp = t.m + row * t.width;
+  float* vp = t.v + row * t.width;
+  for (int c = lane; c < w4; c += 32) {
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = beg; k < end; ++k) {
+      const float4 r = ld4(a.rgbuf + static_cast<int64_t>(t.contrib[k]) * t.width + 4 * c);
+      g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
+    }
+    if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g);
+    float4 w = ld4(wp + 4 * c), m = ld4(mp + 4 * c), v = ld4(vp + 4 * c);
+    w = adam4(w, m, v, g, lr, b1, b2, eps, bc1, bc2);
+    st4(wp + 4 * c, w);
+    st4(mp + 4 * c, m);
+    st4(vp + 4 * c, v);
+  }
+}
+
+__global__ void dense_adam_kernel(float* w, float* m, float* v, const float* g, int64_t n, float lr,
+                                  float b1, float b2, float eps, float bc1, float bc2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float wi = w[i], mi = m[i], vi = v[i];
+    adam_update(wi, mi, vi, g[i], lr, b1, b2, eps, bc1, bc2);
+    w[i] = wi;
+    m[i] = mi;
+    v[i] = vi;
+  }
+}
+
+}  // namespace
+
+int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, float lr, float b1, float b2,
+                               float eps, float bc1, float bc2, const LaunchCtx& lc) {
+  if (t.n_rows <= 0) return 0;
+  const int blocks = (t.n_rows + kWarps - 1) / kWarps;
+  if (a.backbone == NGDB_GQE)
+    entity_adam_kernel<NGDB_GQE><<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, lr, b1, b2, eps, bc1, bc2);
+  else
+    entity_adam_kernel<NGDB_Q2B><<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, lr, b1, b2, eps, bc1, bc2);
+  return 1;
+}
+
+int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, float lr, float b1,
+                                 float b2, float eps, float bc1, float bc2, const LaunchCtx& lc) {
+  if (t.n_rows <= 0) return 0;
+  const int blocks = (t.n_rows + kWarps - 1) / kWarps;
+  relation_adam_kernel<<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, lr, b1, b2, eps, bc1, bc2);
+  return 1;
+}
+
+int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, float lr, float b1,
+                       float b2, float eps, float bc1, float bc2, const LaunchCtx& lc) {
+  if (n <= 0) return 0;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, lc.num_sms * 8));
+  dense_adam_kernel<<<blocks, 256, 0, lc.stream>>>(w, m, v, g, n, lr, b1, b2, eps, bc1, bc2);
+  return 1;
+}
+
+}  // namespace ngdb_dev

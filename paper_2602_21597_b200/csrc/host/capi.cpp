@@ -1,0 +1,300 @@
+// C ABI over the host engine (include/ngdb/ngdb_host.h).
+#include "ngdb/ngdb_host.h"
+
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "ngdb/kg.hpp"
+#include "ngdb/sampler.hpp"
+#include "ngdb/synth.hpp"
+#include "ngdb/trainer.hpp"
+
+namespace ngdb_internal {
+void set_last_error(const std::string& msg);  // ctx.cu
+}
+
+struct ngdb_graph {
+  ngdb::GraphSplit split;
+};
+struct ngdb_batch {
+  ngdb::TrainingBatch tb;
+};
+struct ngdb_step {
+  ngdb::StepPlanHost plan;
+};
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return NGDB_OK;
+  } catch (const ngdb::ShapeMismatch& e) {
+    ngdb_internal::set_last_error(e.what());
+    return NGDB_ERR_SHAPE_MISMATCH;
+  } catch (const ngdb::IndexOutOfRange& e) {
+    ngdb_internal::set_last_error(e.what());
+    return NGDB_ERR_INDEX_OUT_OF_RANGE;
+  } catch (const ngdb::IdOutOfRange& e) {
+    ngdb_internal::set_last_error(e.what());
+    return NGDB_ERR_INDEX_OUT_OF_RANGE;
+  } catch (const ngdb::MissingKernel& e) {
+    ngdb_internal::set_last_error(e.what());
+    return NGDB_ERR_MISSING_KERNEL;
+  } catch (const ngdb::NonFinite& e) {
+    ngdb_internal::set_last_error(e.what());
+    return NGDB_ERR_NON_FINITE;
+  } catch (const ngdb::Error& e) {
+    ngdb_internal::set_last_error(std::string(e.what()));
+    return NGDB_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    ngdb_internal::set_last_error(e.what());
+    return NGDB_ERR_CONFIG;
+  }
+}
+
+std::vector<ngdb::Triple> triples_of(const int32_t* p, int64_t n) {
+  std::vector<ngdb::Triple> out(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) out[i] = {p[3 * i], p[3 * i + 1], p[3 * i + 2]};
+  return out;
+}
+
+ngdb::QueryInstance query_of(int32_t pattern, const int32_t* anchors, const int32_t* relations) {
+  if (pattern < 0 || pattern >= ngdb::kPatternCount)
+    throw ngdb::UnsupportedPattern("pattern index " + std::to_string(pattern));
+  ngdb::QueryInstance q;
+  q.pattern = static_cast<ngdb::Pattern>(pattern);
+  const auto& info = ngdb::pattern_info(q.pattern);
+  q.anchors.assign(anchors, anchors + info.n_anchors);
+  q.relations.assign(relations, relations + info.n_relations);
+  q.validate();
+  return q;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ngdb_graph_synthetic(const char* shape, uint64_t seed, ngdb_graph** out) {
+  return guarded([&] {
+    auto* g = new ngdb_graph();
+    g->split = ngdb::make_synthetic(ngdb::synth_shape(shape), seed);
+    *out = g;
+  });
+}
+
+int ngdb_graph_from_triples(int32_t n_entities, int32_t n_relations, const int32_t* train,
+                            int64_t n_train, const int32_t* valid, int64_t n_valid,
+                            const int32_t* test, int64_t n_test, ngdb_graph** out) {
+  return guarded([&] {
+    ngdb::SynthTriples t;
+    t.train = triples_of(train, n_train);
+    t.valid = triples_of(valid, n_valid);
+    t.test = triples_of(test, n_test);
+    auto* g = new ngdb_graph();
+    g->split = ngdb::split_from_triples(n_entities, n_relations, t);
+    *out = g;
+  });
+}
+
+int ngdb_graph_load(const char* dir, ngdb_graph** out) {
+  return guarded([&] {
+    auto* g = new ngdb_graph();
+    g->split = ngdb::load_graph(dir);
+    *out = g;
+  });
+}
+
+int ngdb_graph_info(const ngdb_graph* g, int32_t* n_entities, int32_t* n_relations,
+                    int64_t* n_train, int64_t* n_valid, int64_t* n_test) {
+  return guarded([&] {
+    if (n_entities) *n_entities = g->split.full.n_entities();
+    if (n_relations) *n_relations = g->split.full.n_relations();
+    if (n_train) *n_train = static_cast<int64_t>(g->split.train.triples().size());
+    if (n_valid) *n_valid = static_cast<int64_t>(g->split.valid_edges.size());
+    if (n_test) *n_test = static_cast<int64_t>(g->split.test_edges.size());
+  });
+}
+
+int ngdb_graph_triples(const ngdb_graph* g, int32_t split, int32_t* out, int64_t n) {
+  return guarded([&] {
+    const std::vector<ngdb::Triple>* v = split == 0   ? &g->split.train.triples()
+                                         : split == 1 ? &g->split.valid_edges
+                                                      : &g->split.test_edges;
+    if (static_cast<int64_t>(v->size()) != n) throw ngdb::ShapeMismatch("triple count");
+    for (int64_t i = 0; i < n; ++i) {
+      out[3 * i] = (*v)[i].head;
+      out[3 * i + 1] = (*v)[i].rel;
+      out[3 * i + 2] = (*v)[i].tail;
+    }
+  });
+}
+
+int ngdb_graph_answer(const ngdb_graph* g, int32_t full, int32_t pattern, const int32_t* anchors,
+                      const int32_t* relations, int32_t* out, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    auto ans = ngdb::answer_query(full ? g->split.full : g->split.train,
+                                  query_of(pattern, anchors, relations));
+    *n = static_cast<int64_t>(ans.size());
+    const int64_t k = std::min<int64_t>(cap, *n);
+    if (k > 0) std::memcpy(out, ans.data(), k * sizeof(int32_t));
+  });
+}
+
+int ngdb_graph_destroy(ngdb_graph* g) {
+  delete g;
+  return NGDB_OK;
+}
+
+int ngdb_batch_sample(const ngdb_graph* g, const double* w, int32_t b, int32_t n_neg, uint64_t seed,
+                      uint64_t tag, ngdb_batch** out) {
+  return guarded([&] {
+    ngdb::SamplingDistribution pi;
+    for (int i = 0; i < ngdb::kPatternCount; ++i) pi.weights[i] = w[i];
+    ngdb::Rng rng = ngdb::Rng(seed).fork(tag);
+    auto* bt = new ngdb_batch();
+    bt->tb = ngdb::sample_training_batch(g->split.train, g->split.full, pi, b, n_neg, rng);
+    *out = bt;
+  });
+}
+
+int ngdb_batch_from_arrays(int32_t b, const int32_t* patterns, const int32_t* anchors,
+                           const int32_t* relations, const int32_t* positives, int32_t n_neg,
+                           const int32_t* negatives, ngdb_batch** out) {
+  return guarded([&] {
+    auto* bt = new ngdb_batch();
+    bt->tb.n_neg = n_neg;
+    for (int32_t i = 0; i < b; ++i) {
+      bt->tb.queries.push_back(query_of(patterns[i], anchors + 3 * i, relations + 4 * i));
+      bt->tb.positives.push_back(positives[i]);
+    }
+    bt->tb.negatives.assign(negatives, negatives + static_cast<int64_t>(b) * n_neg);
+    *out = bt;
+  });
+}
+
+int ngdb_batch_info(const ngdb_batch* bt, int32_t* b, int32_t* n_neg) {
+  return guarded([&] {
+    *b = static_cast<int32_t>(bt->tb.queries.size());
+    *n_neg = bt->tb.n_neg;
+  });
+}
+
+int ngdb_batch_arrays(const ngdb_batch* bt, int32_t* patterns, int32_t* anchors,
+                      int32_t* relations, int32_t* positives, int32_t* negatives) {
+  return guarded([&] {
+    const auto& tb = bt->tb;
+    for (size_t i = 0; i < tb.queries.size(); ++i) {
+      const auto& q = tb.queries[i];
+      if (patterns) patterns[i] = static_cast<int32_t>(q.pattern);
+      for (int k = 0; k < 3; ++k)
+        if (anchors) anchors[3 * i + k] = k < static_cast<int>(q.anchors.size()) ? q.anchors[k] : -1;
+      for (int k = 0; k < 4; ++k)
+        if (relations)
+          relations[4 * i + k] = k < static_cast<int>(q.relations.size()) ? q.relations[k] : -1;
+      if (positives) positives[i] = tb.positives[i];
+    }
+    if (negatives) std::memcpy(negatives, tb.negatives.data(), tb.negatives.size() * sizeof(int32_t));
+  });
+}
+
+int ngdb_batch_destroy(ngdb_batch* bt) {
+  delete bt;
+  return NGDB_OK;
+}
+
+int ngdb_step_build(const ngdb_batch* bt, int32_t backbone, int32_t dim, int32_t b_max,
+                    int32_t semantic, ngdb_step** out) {
+  return guarded([&] {
+    ngdb::TrainConfig cfg;
+    cfg.backbone = static_cast<ngdb::Backbone>(backbone);
+    cfg.dim = dim;
+    cfg.n_neg = bt->tb.n_neg;
+    cfg.b_max = b_max;
+    cfg.semantic = semantic != 0;
+    auto* s = new ngdb_step();
+    s->plan = ngdb::plan_training_step(bt->tb, cfg);
+    *out = s;
+  });
+}
+
+int ngdb_step_view(const ngdb_step* s, ngdb_step_plan* view) {
+  return guarded([&] { *view = s->plan.view(); });
+}
+
+int ngdb_step_trace_json(const ngdb_step* s, int32_t with_nodes, char* buf, int64_t cap,
+                         int64_t* len) {
+  return guarded([&] {
+    std::string js = s->plan.trace.to_json();
+    if (with_nodes) {
+      // append {"nodes":[[...],...]} as a sibling document after a newline
+      js += "\n[";
+      for (size_t i = 0; i < s->plan.trace.records.size(); ++i) {
+        if (i) js += ',';
+        js += '[';
+        const auto& nodes = s->plan.trace.records[i].nodes;
+        for (size_t k = 0; k < nodes.size(); ++k) {
+          if (k) js += ',';
+          js += std::to_string(nodes[k]);
+        }
+        js += ']';
+      }
+      js += ']';
+    }
+    *len = static_cast<int64_t>(js.size());
+    if (buf && cap > 0) {
+      const int64_t k = std::min<int64_t>(cap - 1, *len);
+      std::memcpy(buf, js.data(), k);
+      buf[k] = '\0';
+    }
+  });
+}
+
+int ngdb_step_destroy(ngdb_step* s) {
+  delete s;
+  return NGDB_OK;
+}
+
+int ngdb_param_init(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
+                    const char* name, uint64_t seed, float* out, int64_t n) {
+  return guarded([&] {
+    auto v = ngdb::init_param(static_cast<ngdb::Backbone>(backbone), n_entities, n_relations, dim,
+                              name, seed);
+    if (static_cast<int64_t>(v.size()) != n) throw ngdb::ShapeMismatch("param size");
+    std::memcpy(out, v.data(), n * sizeof(float));
+  });
+}
+
+int ngdb_run_step(ngdb_ctx* ctx, const ngdb_step* s, int64_t step, float* per_query_loss,
+                  double* loss_sum) {
+  return guarded([&] {
+    const ngdb_step_plan view = s->plan.view();
+    ngdb::check_status(ngdb_step_begin(ctx, &view));
+    for (const auto& p : s->plan.pools) ngdb::check_status(ngdb_exec_pool(ctx, &p));
+    ngdb::check_status(ngdb_optimizer_step(ctx, step));
+    int32_t nonfinite = 0;
+    ngdb::check_status(
+        ngdb_step_end(ctx, per_query_loss, s->plan.n_queries, loss_sum, &nonfinite));
+    if (nonfinite) throw ngdb::NonFinite("non-finite loss at step " + std::to_string(step));
+  });
+}
+
+int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t step,
+                    float* per_query_loss, double* loss_sum) {
+  return guarded([&] {
+    ngdb_model_desc d;
+    ngdb::check_status(ngdb_ctx_desc(ctx, &d));
+    ngdb::TrainConfig cfg;
+    cfg.backbone = static_cast<ngdb::Backbone>(d.backbone);
+    cfg.dim = d.dim;
+    cfg.n_neg = bt->tb.n_neg;
+    cfg.b_max = b_max;
+    ngdb_step s;
+    s.plan = ngdb::plan_training_step(bt->tb, cfg);
+    ngdb::check_status(ngdb_run_step(ctx, &s, step, per_query_loss, loss_sum));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,252 @@
+// Max-Fillness planner: Alg. 1 run symbolically on the host,
+// with Eq. 7 eager reclamation replayed as static device-arena slot reuse.
+// Scheduler rules follow SPEC.md:463-510 and DESIGN.md §2.6 (SURVEY A-4).
+#include "ngdb/scheduler.hpp"
+
+#include <algorithm>
+#include <unordered_map>
+
+namespace ngdb {
+
+int select_pool(const std::array<int64_t, kPoolCount>& counts,
+                const std::array<int64_t, kPoolCount>& head_timestamp) {
+  int best = -1;
+  for (int p = 0; p < kPoolCount; ++p) {
+    if (counts[p] <= 0) continue;
+    if (best < 0 || counts[p] > counts[best] ||
+        (counts[p] == counts[best] && head_timestamp[p] < head_timestamp[best]))
+      best = p;  // equal count + equal timestamp keeps the earlier pool (type order)
+  }
+  if (best < 0) throw AllPoolsEmpty("select_pool: every pool is empty");
+  return best;
+}
+
+int64_t TensorModel::fwd_elems(const FusedDag& f, const OperatorNode& x) const {
+  (void)f;
+  switch (x.op.kind) {
+    case OpKind::Score:
+    case OpKind::UnionScore: return n_candidates;
+    case OpKind::Loss: return 1;
+    default: return query_width;
+  }
+}
+
+int64_t TensorModel::bwd_rows(const FusedDag& f, const OperatorNode& bwd) const {
+  return f.nodes[bwd.mirror].n_inputs;
+}
+
+int64_t TensorModel::bwd_row_elems(const FusedDag& f, const OperatorNode& bwd) const {
+  const OperatorNode& x = f.nodes[bwd.mirror];
+  if (x.n_inputs == 0) return 0;
+  return fwd_elems(f, f.nodes[x.inputs[0]]);
+}
+
+namespace {
+
+struct Slot {
+  int64_t bytes = 0;
+  int64_t offset = -1;
+  int32_t rc = 0;
+};
+
+class SlotArena {
+ public:
+  SlotArena(ReleasePolicy policy) : policy_(policy) {}
+
+  int32_t alloc(int64_t bytes, int32_t rc) {
+    if (rc < 1) throw ZeroRefcount("alloc with refcount < 1");
+    Slot s;
+    s.bytes = bytes;
+    s.rc = rc;
+    auto& fl = free_[bytes];
+    if (!fl.empty()) {
+      s.offset = fl.back();
+      fl.pop_back();
+      ++hits_;
+    } else {
+      s.offset = top_;
+      top_ += (bytes + 15) / 16 * 16;
+    }
+    live_ += bytes;
+    peak_ = std::max(peak_, live_);
+    slots_.push_back(s);
+    return static_cast<int32_t>(slots_.size() - 1);
+  }
+  // returns bytes reclaimed (0 if still referenced)
+  int64_t release(int32_t id) {
+    Slot& s = slots_[id];
+    if (s.rc <= 0) throw DoubleRelease("tensor released with refcount 0");
+    if (--s.rc > 0) return 0;
+    if (policy_ == ReleasePolicy::EndOfDag) return 0;
+    free_[s.bytes].push_back(s.offset);
+    live_ -= s.bytes;
+    return s.bytes;
+  }
+  void check_live(int32_t id) const {
+    if (slots_[id].rc <= 0) throw ZeroRefcount("use after reclamation");
+  }
+  int64_t offset(int32_t id) const { return slots_[id].offset; }
+  int64_t live() const { return live_; }
+  int64_t peak() const { return peak_; }
+  int64_t hits() const { return hits_; }
+  int64_t top() const { return top_; }
+
+ private:
+  ReleasePolicy policy_;
+  std::vector<Slot> slots_;
+  std::unordered_map<int64_t, std::vector<int64_t>> free_;
+  int64_t live_ = 0, peak_ = 0, hits_ = 0, top_ = 0;
+};
+
+struct Pool {
+  std::vector<std::pair<int32_t, int32_t>> q;  // (node, enqueue cycle)
+  size_t head = 0;
+  int64_t size() const { return static_cast<int64_t>(q.size() - head); }
+};
+
+}  // namespace
+
+ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
+  if (!f.has_gradients) throw MissingKernel("planner requires a training DAG with gradient nodes");
+  const int32_t n = static_cast<int32_t>(f.nodes.size());
+  const int32_t nf = f.n_fwd;
+  const TensorModel tm{cfg_.query_width, cfg_.n_candidates};
+  const int64_t eb = cfg_.elem_bytes;
+
+  DagAdjacency adj = adjacency(f);
+  std::vector<int32_t> indeg = adj.indegree;
+
+  SlotArena arena(cfg_.policy);
+  std::vector<int32_t> t_fwd(nf, -1), t_bwd(n, -1);
+  fwd_slot_.assign(nf, -1);
+  bwd_slot_.assign(n, -1);
+
+  ExecutionTrace tr;
+  tr.total_nodes = n;
+  std::array<Pool, kPoolCount> pools;
+  std::vector<int32_t> ready;
+  ready.reserve(n);
+  for (int32_t i = 0; i < n; ++i)
+    if (indeg[i] == 0) ready.push_back(i);
+
+  std::vector<int32_t> batch, cls;
+  int64_t executed = 0;
+  int32_t cycle = 0, step = 0;
+
+  // Output allocation for node o (its T or G tensor).
+  auto allocate = [&](int32_t o) {
+    const OperatorNode& x = f.nodes[o];
+    if (x.op.dir == Direction::Fwd) {
+      const int32_t rc = x.consumer >= 0 ? 3 : 1;
+      t_fwd[o] = arena.alloc(tm.fwd_elems(f, x) * eb, rc);
+      fwd_slot_[o] = arena.offset(t_fwd[o]);
+    } else {
+      const int64_t rows = tm.bwd_rows(f, x);
+      if (rows == 0) return;
+      t_bwd[o] = arena.alloc(rows * tm.bwd_row_elems(f, x) * eb, static_cast<int32_t>(rows));
+      bwd_slot_[o] = arena.offset(t_bwd[o]);
+    }
+  };
+  // Tensors consumed by node o, in release order.
+  auto for_each_input = [&](int32_t o, auto&& fn) {
+    const OperatorNode& x = f.nodes[o];
+    if (x.op.dir == Direction::Fwd) {
+      for (int k = 0; k < x.n_inputs; ++k) fn(t_fwd[x.inputs[k]]);
+    } else {
+      const OperatorNode& m = f.nodes[x.mirror];
+      if (m.consumer >= 0) fn(t_bwd[nf + m.consumer]);
+      for (int k = 0; k < m.n_inputs; ++k) fn(t_fwd[m.inputs[k]]);
+      fn(t_fwd[x.mirror]);
+    }
+  };
+
+  while (!ready.empty() || executed < n) {
+    for (int32_t v : ready) pools[f.nodes[v].op.pool()].q.emplace_back(v, cycle);
+    ready.clear();
+    std::array<int64_t, kPoolCount> counts{}, heads{};
+    for (int p = 0; p < kPoolCount; ++p) {
+      counts[p] = pools[p].size();
+      heads[p] = counts[p] > 0 ? pools[p].q[pools[p].head].second : 0;
+    }
+    const int tau = select_pool(counts, heads);
+    const OperatorType type = OperatorType::from_pool(tau);
+    Pool& pool = pools[tau];
+    const int64_t total = pool.size();
+    const int64_t n_pops = (total + cfg_.b_max - 1) / cfg_.b_max;
+    int64_t remaining = total;
+    for (int64_t p = 0; p < n_pops; ++p) {
+      const int64_t take = std::min<int64_t>(remaining, cfg_.b_max);
+      remaining -= take;
+      batch.clear();
+      for (int64_t i = 0; i < take; ++i) batch.push_back(pool.q[pool.head++].first);
+
+      TraceRecord rec;
+      rec.step = step;
+      rec.cycle = cycle;
+      rec.type = type;
+      rec.batch = static_cast<int32_t>(take);
+      rec.nodes = batch;
+
+      // use-after-free guard: every consumed tensor must still be referenced
+      for (int32_t o : batch) for_each_input(o, [&](int32_t t) { arena.check_live(t); });
+      for (int32_t o : batch) allocate(o);
+
+      if (type.is_set_op()) {
+        for (int k = 2; k <= 3; ++k) {
+          cls.clear();
+          for (int32_t o : batch)
+            if (f.nodes[o].cardinality == k) cls.push_back(o);
+          if (cls.empty()) continue;
+          rec.classes.emplace_back(k, static_cast<int32_t>(cls.size()));
+          invoke(Invocation{type, k, cls.data(), static_cast<int32_t>(cls.size()), step});
+          ++tr.invocations;
+        }
+      } else {
+        invoke(Invocation{type, 0, batch.data(), static_cast<int32_t>(batch.size()), step});
+        ++tr.invocations;
+      }
+
+      for (int32_t o : batch) {
+        for_each_input(o, [&](int32_t t) { rec.bytes_reclaimed += arena.release(t); });
+        for (int32_t k = adj.succ_begin[o]; k < adj.succ_begin[o + 1]; ++k) {
+          const int32_t s = adj.succ[k];
+          if (--indeg[s] == 0) ready.push_back(s);
+        }
+      }
+      executed += take;
+      rec.live_bytes = arena.live();
+      tr.records.push_back(std::move(rec));
+      ++step;
+    }
+    ++cycle;
+  }
+  tr.peak_bytes = arena.peak();
+  tr.free_list_hits = arena.hits();
+  arena_top_ = arena.top();
+  return tr;
+}
+
+std::string ExecutionTrace::to_json() const {
+  std::string s = "{\"invocations\":" + std::to_string(invocations) +
+                  ",\"peak_bytes\":" + std::to_string(peak_bytes) +
+                  ",\"free_list_hits\":" + std::to_string(free_list_hits) +
+                  ",\"total_nodes\":" + std::to_string(total_nodes) + ",\"records\":[";
+  for (size_t i = 0; i < records.size(); ++i) {
+    const TraceRecord& r = records[i];
+    if (i) s += ',';
+    s += "{\"step\":" + std::to_string(r.step) + ",\"cycle\":" + std::to_string(r.cycle) +
+         ",\"kind\":\"" + op_kind_name(r.type.kind) + "\",\"dir\":\"" +
+         (r.type.dir == Direction::Fwd ? "fwd" : "bwd") + "\",\"batch\":" +
+         std::to_string(r.batch) + ",\"classes\":[";
+    for (size_t c = 0; c < r.classes.size(); ++c) {
+      if (c) s += ',';
+      s += "[" + std::to_string(r.classes[c].first) + "," + std::to_string(r.classes[c].second) + "]";
+    }
+    s += "],\"bytes_reclaimed\":" + std::to_string(r.bytes_reclaimed) +
+         ",\"live_bytes\":" + std::to_string(r.live_bytes) + "}";
+  }
+  s += "]}";
+  return s;
+}
+
+}  // namespace ngdb

@@ -1,0 +1,274 @@
+"""Python mirror of the reference interface for the training step.
+
+Names follow the reference C++ API (kg.hpp / query.hpp) and the SPEC's trainer,
+sampler and scheduler operations; everything computes in the native library
+(host C++ planner + sm_100a kernels). numpy arrays are the only currency.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from ._native import ModelDesc, NodeDesc, PoolDesc, StepPlan, check, lib
+
+# query.hpp:14-29 enum order == index order of π
+PATTERNS = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni", "inp"]
+PATTERN_ARITY = {  # (anchors, relations)
+    "1p": (1, 1), "2p": (1, 2), "3p": (1, 3), "2i": (2, 2), "3i": (3, 3), "pi": (2, 3),
+    "ip": (2, 3), "2u": (2, 2), "up": (2, 3), "2in": (2, 2), "3in": (3, 3), "pin": (2, 3),
+    "pni": (2, 3), "inp": (2, 3)}
+BACKBONES = {"gqe": 0, "q2b": 1, "betae": 2}
+OP_KINDS = ["EmbedAnchor", "FuseSemantic", "Project", "Negate", "Intersect", "Score",
+            "UnionScore", "Loss"]
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+def pattern_weights(mix: Sequence[str]) -> np.ndarray:
+    """Uniform π over the given patterns (SamplingDistribution::uniform_over)."""
+    w = np.zeros(14, dtype=np.float64)
+    for p in mix:
+        w[PATTERNS.index(p)] += 1.0 / len(mix)
+    return w
+
+
+class Graph:
+    """GraphSplit (kg.hpp:72-77): train graph, valid/test edges, full graph."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def synthetic(cls, shape: str, seed: int = 1) -> "Graph":
+        h = C.c_void_p()
+        check(lib.ngdb_graph_synthetic(shape.encode(), seed, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_triples(cls, n_entities: int, n_relations: int, train: np.ndarray,
+                     valid: Optional[np.ndarray] = None, test: Optional[np.ndarray] = None) -> "Graph":
+        def arr(x):
+            return np.ascontiguousarray(np.zeros((0, 3)) if x is None else x, dtype=np.int32)
+        tr, va, te = arr(train), arr(valid), arr(test)
+        h = C.c_void_p()
+        check(lib.ngdb_graph_from_triples(n_entities, n_relations, _p(tr, C.c_int32), len(tr),
+                                          _p(va, C.c_int32), len(va), _p(te, C.c_int32), len(te),
+                                          C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load(cls, directory: str) -> "Graph":
+        h = C.c_void_p()
+        check(lib.ngdb_graph_load(directory.encode(), C.byref(h)))
+        return cls(h)
+
+    def info(self) -> Dict[str, int]:
+        ne, nr = C.c_int32(), C.c_int32()
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.ngdb_graph_info(self._h, C.byref(ne), C.byref(nr), C.byref(a), C.byref(b),
+                                  C.byref(c)))
+        return {"n_entities": ne.value, "n_relations": nr.value, "n_train": a.value,
+                "n_valid": b.value, "n_test": c.value}
+
+    def triples(self, split: int = 0) -> np.ndarray:
+        info = self.info()
+        n = [info["n_train"], info["n_valid"], info["n_test"]][split]
+        out = np.zeros((n, 3), dtype=np.int32)
+        check(lib.ngdb_graph_triples(self._h, split, _p(out, C.c_int32), n))
+        return out
+
+    def answer(self, pattern: str, anchors, relations, full: bool = False) -> np.ndarray:
+        a = np.array(list(anchors) + [-1] * 3, dtype=np.int32)[:3]
+        r = np.array(list(relations) + [-1] * 4, dtype=np.int32)[:4]
+        n = C.c_int64()
+        cap = self.info()["n_entities"]
+        out = np.zeros(cap, dtype=np.int32)
+        check(lib.ngdb_graph_answer(self._h, int(full), PATTERNS.index(pattern), _p(a, C.c_int32),
+                                    _p(r, C.c_int32), _p(out, C.c_int32), cap, C.byref(n)))
+        return out[: n.value].copy()
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.ngdb_graph_destroy(self._h)
+            self._h = None
+
+
+@dataclass
+class BatchArrays:
+    patterns: np.ndarray   # [B] int32 (enum index)
+    anchors: np.ndarray    # [B,3] int32, -1 padded
+    relations: np.ndarray  # [B,4] int32, -1 padded
+    positives: np.ndarray  # [B]
+    negatives: np.ndarray  # [B,K]
+
+
+class Batch:
+    """A sampled training batch: queries, walked answers (positives), negatives."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def sample(cls, graph: Graph, weights: np.ndarray, b: int, n_neg: int, seed: int = 3,
+               tag: int = 0) -> "Batch":
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        h = C.c_void_p()
+        check(lib.ngdb_batch_sample(graph._h, _p(w, C.c_double), b, n_neg, seed, tag, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_arrays(cls, arrs: BatchArrays) -> "Batch":
+        b = len(arrs.patterns)
+        k = arrs.negatives.shape[1]
+        cv = [np.ascontiguousarray(x, dtype=np.int32) for x in
+              (arrs.patterns, arrs.anchors, arrs.relations, arrs.positives, arrs.negatives)]
+        h = C.c_void_p()
+        check(lib.ngdb_batch_from_arrays(b, _p(cv[0], C.c_int32), _p(cv[1], C.c_int32),
+                                         _p(cv[2], C.c_int32), _p(cv[3], C.c_int32), k,
+                                         _p(cv[4], C.c_int32), C.byref(h)))
+        return cls(h)
+
+    def arrays(self) -> BatchArrays:
+        b, k = C.c_int32(), C.c_int32()
+        check(lib.ngdb_batch_info(self._h, C.byref(b), C.byref(k)))
+        B, K = b.value, k.value
+        out = BatchArrays(np.zeros(B, np.int32), np.zeros((B, 3), np.int32),
+                          np.zeros((B, 4), np.int32), np.zeros(B, np.int32),
+                          np.zeros((B, K), np.int32))
+        check(lib.ngdb_batch_arrays(self._h, _p(out.patterns, C.c_int32), _p(out.anchors, C.c_int32),
+                                    _p(out.relations, C.c_int32), _p(out.positives, C.c_int32),
+                                    _p(out.negatives, C.c_int32)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.ngdb_batch_destroy(self._h)
+            self._h = None
+
+
+class PlannedStep:
+    """A step planned by the host Max-Fillness scheduler (trace + device plan)."""
+
+    def __init__(self, batch: Batch, backbone: str, dim: int, b_max: int = 512,
+                 semantic: bool = False):
+        h = C.c_void_p()
+        check(lib.ngdb_step_build(batch._h, BACKBONES[backbone], dim, b_max, int(semantic),
+                                  C.byref(h)))
+        self._h = h
+
+    def trace(self, with_nodes: bool = False) -> dict:
+        n = C.c_int64()
+        check(lib.ngdb_step_trace_json(self._h, int(with_nodes), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib.ngdb_step_trace_json(self._h, int(with_nodes), buf, n.value + 1, C.byref(n)))
+        text = buf.value.decode()
+        if with_nodes:
+            head, nodes = text.split("\n", 1)
+            tr = json.loads(head)
+            for rec, nd in zip(tr["records"], json.loads(nodes)):
+                rec["nodes"] = nd
+            return tr
+        return json.loads(text)
+
+    def view(self) -> StepPlan:
+        v = StepPlan()
+        check(lib.ngdb_step_view(self._h, C.byref(v)))
+        return v
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.ngdb_step_destroy(self._h)
+            self._h = None
+
+
+def param_specs(backbone: str, n_entities: int, n_relations: int, dim: int) -> List[tuple]:
+    """(name, rows, cols, sparse) in registry order (trainer.hpp param_specs)."""
+    if backbone == "gqe":
+        return [("entity", n_entities, dim, True), ("relation", n_relations, dim, True),
+                ("int_w1", dim, dim, False), ("int_w2", dim, dim, False)]
+    if backbone == "q2b":
+        out = [("entity", n_entities, dim, True), ("relation", n_relations, 2 * dim, True)]
+        for n in ("att_w1", "att_b1", "att_w2", "att_b2", "off_w1", "off_b1", "off_w2", "off_b2"):
+            out.append((n, 1 if "_b" in n else dim, dim, False))
+        return out
+    raise NotImplementedError(backbone)
+
+
+def init_params(backbone: str, n_entities: int, n_relations: int, dim: int,
+                seed: int = 2) -> Dict[str, np.ndarray]:
+    out = {}
+    for name, rows, cols, _ in param_specs(backbone, n_entities, n_relations, dim):
+        a = np.zeros((rows, cols), dtype=np.float32)
+        check(lib.ngdb_param_init(BACKBONES[backbone], n_entities, n_relations, dim, name.encode(),
+                                  seed, _p(a, C.c_float), a.size))
+        out[name] = a
+    return out
+
+
+class Engine:
+    """One GPU context (ngdb_ctx): parameters, Adam state, arena, stream."""
+
+    def __init__(self, backbone: str, n_entities: int, n_relations: int, dim: int = 400,
+                 n_neg: int = 128, b_max: int = 512, max_queries: int = 512, gamma: float = 12.0,
+                 lr: float = 1e-4, alpha_box: float = 0.02, device: int = 0,
+                 params: Optional[Dict[str, np.ndarray]] = None, seed: int = 2, debug: bool = False):
+        d = ModelDesc(BACKBONES[backbone], n_entities, n_relations, dim, n_neg, 0, gamma,
+                      alpha_box, lr, 0.9, 0.999, 1e-8, b_max, max_queries)
+        self.backbone, self.dim, self.b_max = backbone, dim, b_max
+        self.n_entities, self.n_relations = n_entities, n_relations
+        self._h = C.c_void_p()
+        check(lib.ngdb_ctx_create(C.byref(d), device, C.byref(self._h)))
+        self.step_count = 0
+        if params is None:
+            params = init_params(backbone, n_entities, n_relations, dim, seed)
+        for k, v in params.items():
+            self.upload(k, v)
+        if debug:
+            check(lib.ngdb_set_debug(self._h, 1))
+
+    def upload(self, name: str, value: np.ndarray) -> None:
+        a = np.ascontiguousarray(value, dtype=np.float32)
+        check(lib.ngdb_param_upload(self._h, name.encode(), _p(a, C.c_float), a.size))
+
+    def download(self, name: str) -> np.ndarray:
+        base = name.split(":")[-1]
+        spec = {s[0]: s for s in param_specs(self.backbone, self.n_entities, self.n_relations,
+                                             self.dim)}[base]
+        out = np.zeros((spec[1], spec[2]), dtype=np.float32)
+        check(lib.ngdb_param_download(self._h, name.encode(), _p(out, C.c_float), out.size))
+        return out
+
+    def train_step(self, batch: Batch) -> np.ndarray:
+        """Plan + run one step through the public C ABI; returns per-query losses."""
+        arr_b = C.c_int32()
+        k = C.c_int32()
+        check(lib.ngdb_batch_info(batch._h, C.byref(arr_b), C.byref(k)))
+        losses = np.zeros(arr_b.value, dtype=np.float32)
+        total = C.c_double()
+        self.step_count += 1
+        check(lib.ngdb_train_step(self._h, batch._h, self.b_max, self.step_count,
+                                  _p(losses, C.c_float), C.byref(total)))
+        return losses
+
+    def run_step(self, step: PlannedStep, n_queries: int) -> np.ndarray:
+        losses = np.zeros(n_queries, dtype=np.float32)
+        total = C.c_double()
+        self.step_count += 1
+        check(lib.ngdb_run_step(self._h, step._h, self.step_count, _p(losses, C.c_float),
+                                C.byref(total)))
+        return losses
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.ngdb_ctx_destroy(self._h)
+            self._h = None

@@ -1,0 +1,65 @@
+"""GPU parity: the sm_100a training step vs the CPU oracle (f64) on identical
+seeded inputs, through the C ABI. Losses, pre-Adam gradients of every
+parameter and post-Adam parameters within 1e-4 relative (tests/parity.py)."""
+import numpy as np
+import pytest
+
+from parity import rel_close, run_pair
+
+pytestmark = pytest.mark.gpu
+
+ALL = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni", "inp"]
+C1_MIX = ["1p", "2p", "3p", "2i", "3i"]
+
+
+def _check(res, allow_frac=1e-3):
+    for loss, ref in res["loss"]:
+        ok, nbad, worst = rel_close(loss, ref)
+        assert ok, f"loss mismatch: {nbad} bad, worst rel {worst:.3e}"
+    for name, (g, r) in res["grads"].items():
+        ok, nbad, worst = rel_close(g, r, allow_frac=allow_frac)
+        assert ok, f"grad {name}: {nbad}/{r.size} beyond 1e-4 (worst {worst:.3e})"
+    for name, (p, r) in res["params"].items():
+        # Adam maps |g| >> eps to -lr*sign(g): params agree to ~lr*1e-4 except
+        # where a gradient element is a sign-tie (see parity.py)
+        ok, nbad, worst = rel_close(p, r, allow_frac=allow_frac)
+        assert ok, f"param {name}: {nbad}/{r.size} beyond 1e-4 (worst {worst:.3e})"
+
+
+@pytest.mark.parametrize("backbone,mix", [("gqe", C1_MIX), ("q2b", ALL), ("gqe", ALL)])
+@pytest.mark.parametrize("dim", [32, 400])
+def test_one_step_parity(small_graph, small_oracle_graph, backbone, mix, dim):
+    res = run_pair(small_graph, small_oracle_graph, backbone, mix, b=128, k=32, dim=dim)
+    _check(res)
+
+
+@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+def test_small_bmax_drains(small_graph, small_oracle_graph, backbone):
+    # B_max=16 forces multi-pop drains and split cardinality classes
+    res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=96, k=8, dim=16, b_max=16)
+    _check(res)
+
+
+@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+def test_three_steps(small_graph, small_oracle_graph, backbone):
+    res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=64, k=16, dim=32, steps=3,
+                   compare_grads=True)
+    _check(res, allow_frac=2e-3)
+
+
+@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+def test_full_batch_k128(small_graph, small_oracle_graph, backbone):
+    # the benchmark's per-step shape: 512 queries, 128 negatives, d=400
+    res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=512, k=128, dim=400)
+    _check(res)
+
+
+@pytest.mark.parametrize("pattern", ALL)
+def test_single_pattern_batches(small_graph, small_oracle_graph, pattern):
+    res = run_pair(small_graph, small_oracle_graph, "q2b", [pattern], b=32, k=8, dim=16)
+    _check(res)
+
+
+def test_batch_of_one(small_graph, small_oracle_graph):
+    res = run_pair(small_graph, small_oracle_graph, "q2b", ["up"], b=1, k=4, dim=8)
+    _check(res)
