@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark of the operator-level training step (BASELINE.json metric:
+training queries/sec, mixed query types).
+
+Workload (N=1 line): configs[1] — Query2Box on a synthetic NELL995-shaped KG
+(63,361 entities, 200 relations, 114k/14k/14k edges), the full 14-type query
+mix, 512 queries/step, 128 negatives, d=400, fp32, Adam lr 1e-4.
+
+  value  device-timed q/s over K steps with the step plans already resident in
+         HBM (host planning excluded; every kernel of every step is launched
+         inside the timed region).
+  e2e    q/s through the public C ABI call ngdb_train_step with HOST buffers:
+         planning on the host, H2D of the packed plan, all kernels, D2H of the
+         per-query losses, every step.
+  roofline  the dominant kernel family, algorithmic bytes / CUDA-event time.
+  cpu_baseline  the CPU oracle (f32, 1 thread) on a bounded sample.
+
+`--impl reference` times the reference's CPU implementation of the path. The
+reference ships no implementation, so this is the oracle port of
+it (oracle/), with its own JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (backbone, shape, mix, dim, batch, n_neg)
+    "c2": ("q2b", "nell995", "all", 400, 512, 128),
+    "c1": ("gqe", "fb15k-237", "c1", 400, 512, 128),
+}
+MIXES = {"all": ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni",
+                 "inp"],
+         "c1": ["1p", "2p", "3p", "2i", "3i"]}
+METRIC = "training queries/sec (mixed query types)"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_batches(graph, mix, batch, n_neg, count, base_tag):
+    import paper_2602_21597_b200 as m
+    w = m.pattern_weights(MIXES[mix])
+    return [m.Batch.sample(graph, w, batch, n_neg, seed=3, tag=base_tag + i) for i in range(count)]
+
+
+def run_cpu_oracle(backbone, info, dim, n_neg, batches, budget_s, precision=32):
+    """Time the oracle on whole 512-query steps until budget_s elapses."""
+    import oracle as O
+    om = O.OracleModel(backbone, info["n_entities"], info["n_relations"], dim, n_neg,
+                       precision=precision)
+    om.init(2)
+    done, t0, q = 0, time.perf_counter(), 0
+    while True:
+        a = batches[done % len(batches)].arrays()
+        om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, b_max=512,
+                step=done + 1)
+        done += 1
+        q += len(a.patterns)
+        el = time.perf_counter() - t0
+        if el >= budget_s or done >= 10 * len(batches):
+            return q / el, done, el
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    backbone, shape, mix, dim, batch, n_neg = CONFIGS[args.config]
+    if rank != 0:
+        return
+    import paper_2602_21597_b200 as m
+    graph = m.Graph.synthetic(shape, 1)
+    info = graph.info()
+    batches = make_batches(graph, mix, batch, n_neg, max(1, min(args.steps, 4)), 1)
+    import oracle as O
+    om = O.OracleModel(backbone, info["n_entities"], info["n_relations"], dim, n_neg, precision=32)
+    om.init(2)
+    for i in range(args.warmup):
+        a = batches[i % len(batches)].arrays()
+        om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, step=i + 1)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        a = batches[i % len(batches)].arrays()
+        om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives,
+                step=args.warmup + i + 1)
+    el = time.perf_counter() - t0
+    qps = batch * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{backbone} {shape}-shaped synthetic KG, {mix} mix",
+                   "global_batch": batch, "n_neg": n_neg, "dim": dim},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} full {batch}-query steps (oracle/, f32, "
+                                   f"1 thread; the reference ships no implementation)"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=5)
+    ap.add_argument("--quiet", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+
+    import ctypes as C
+
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200._native import check, lib
+
+    backbone, shape, mix, dim, batch, n_neg = CONFIGS[args.config]
+    t_setup = time.perf_counter()
+    graph = m.Graph.synthetic(shape, 1)
+    info = graph.info()
+    n_steps = args.warmup + args.steps
+    # each rank draws its own batches: Rng(3).fork(step * world + rank)
+    batches = make_batches(graph, mix, batch, n_neg, n_steps, 1 + rank * 100000)
+    eng = m.Engine(backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=n_neg,
+                   b_max=512, max_queries=batch, device=local)
+    ctx = eng.handle
+    steps = [m.PlannedStep(b, backbone, dim, 512) for b in batches]
+    plans = []
+    for s in steps:
+        v = s.view()
+        h = C.c_void_p()
+        check(lib.ngdb_plan_create(ctx, C.byref(v), C.byref(h)))
+        plans.append(h)
+    setup_s = time.perf_counter() - t_setup
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    step_no = 0
+
+    def run_plan(i):
+        nonlocal step_no
+        step_no += 1
+        check(lib.ngdb_plan_run(ctx, plans[i], step_no))
+
+    # ---- value: device-timed, plans resident in HBM --------------------------
+    for i in range(args.warmup):
+        run_plan(i)
+    check(lib.ngdb_sync(ctx))
+    barrier()
+    launches0 = lib.ngdb_launch_count(ctx)
+    clocks = ClockSampler(local)
+    clocks.start()
+    check(lib.ngdb_timer_start(ctx))
+    for i in range(args.steps):
+        run_plan(args.warmup + i)
+    ms = C.c_float()
+    check(lib.ngdb_timer_stop(ctx, C.byref(ms)))
+    clk = clocks.stop()
+    launches = lib.ngdb_launch_count(ctx) - launches0
+    barrier()
+    ms_step = ms.value / args.steps
+    if dist is not None:
+        import torch
+        t = torch.tensor([ms_step], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = batch * world / (ms_step / 1000.0)
+
+    # ---- roofline: per-family CUDA-event times on a profiled replay ----------
+    check(lib.ngdb_profile_enable(ctx, 1))
+    for i in range(args.profile_steps):
+        run_plan(args.warmup + (i % args.steps))
+    check(lib.ngdb_sync(ctx))
+    fams = {}
+    for f in range(lib.ngdb_profile_families()):
+        fms, fl, fb = C.c_double(), C.c_int64(), C.c_double()
+        check(lib.ngdb_profile_read(ctx, f, C.byref(fms), C.byref(fl), C.byref(fb)))
+        if fl.value:
+            fams[lib.ngdb_profile_family_name(f).decode()] = {
+                "ms_per_step": fms.value / args.profile_steps,
+                "launches_per_step": fl.value / args.profile_steps,
+                "gbs": fb.value / (fms.value / 1000.0) / 1e9 if fms.value > 0 else 0.0,
+                "bytes_per_step": fb.value / args.profile_steps}
+    check(lib.ngdb_profile_enable(ctx, 0))
+    peak, peak_kind = load_peaks()
+    dom = max(fams.items(), key=lambda kv: kv[1]["ms_per_step"])
+    roof = {"bound": "hbm", "kernel": dom[0], "achieved": dom[1]["gbs"], "peak": peak,
+            "unit": "GB/s", "frac": dom[1]["gbs"] / peak, "traffic": None,
+            "peak_kind": peak_kind,
+            "share_of_step": dom[1]["ms_per_step"] / sum(v["ms_per_step"] for v in fams.values())}
+
+    # ---- e2e: public C ABI call with host buffers ----------------------------
+    losses = np.zeros(batch, dtype=np.float32)
+    total = C.c_double()
+    h2d = []
+    for s in steps:
+        v = s.view()
+        h2d.append(32 * v.n_nodes + 4 * v.n_queries * v.n_candidates + 4 * (
+            2 * v.n_entity_rows + 1 + v.entity_seg[v.n_entity_rows] + 2 * v.n_relation_rows + 1 +
+            v.relation_seg[v.n_relation_rows]))
+    for i in range(args.warmup):
+        step_no += 1
+        check(lib.ngdb_train_step(ctx, batches[i]._h, 512, step_no,
+                                  losses.ctypes.data_as(C.POINTER(C.c_float)), C.byref(total)))
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step_no += 1
+        check(lib.ngdb_train_step(ctx, batches[args.warmup + i]._h, 512, step_no,
+                                  losses.ctypes.data_as(C.POINTER(C.c_float)), C.byref(total)))
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        import torch
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = batch * world * args.steps / e2e_s
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        qps, done, el = run_cpu_oracle(backbone, info, dim, n_neg, batches[: min(4, n_steps)],
+                                       args.cpu_budget)
+        cpu = {"value": qps, "unit": "queries/s", "cores": 1, "kind": "port",
+               "sample": f"{done} full {batch}-query steps in {el:.1f}s (oracle/, f32, 1 thread)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{backbone} on {shape}-shaped synthetic KG "
+                                   f"({info['n_entities']} entities, {info['n_relations']} "
+                                   f"relations), {mix}-pattern mix",
+                       "global_batch": batch * world, "n_neg": n_neg, "dim": dim,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (entity table + Adam moments 304 MB)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "queries/s",
+                    "h2d_bytes_per_step": int(np.mean(h2d)), "d2h_bytes_per_step": 4 * batch + 16},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "families": fams if not args.quiet else None,
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    for h in plans:
+        lib.ngdb_plan_destroy(h)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

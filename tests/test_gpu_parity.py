@@ -4,7 +4,7 @@ parameter and post-Adam parameters within 1e-4 relative (tests/parity.py)."""
 import numpy as np
 import pytest
 
-from parity import rel_close, run_pair
+from parity import check_all, run_pair
 
 pytestmark = pytest.mark.gpu
 
@@ -12,18 +12,8 @@ ALL = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin"
 C1_MIX = ["1p", "2p", "3p", "2i", "3i"]
 
 
-def _check(res, allow_frac=1e-3):
-    for loss, ref in res["loss"]:
-        ok, nbad, worst = rel_close(loss, ref)
-        assert ok, f"loss mismatch: {nbad} bad, worst rel {worst:.3e}"
-    for name, (g, r) in res["grads"].items():
-        ok, nbad, worst = rel_close(g, r, allow_frac=allow_frac)
-        assert ok, f"grad {name}: {nbad}/{r.size} beyond 1e-4 (worst {worst:.3e})"
-    for name, (p, r) in res["params"].items():
-        # Adam maps |g| >> eps to -lr*sign(g): params agree to ~lr*1e-4 except
-        # where a gradient element is a sign-tie (see parity.py)
-        ok, nbad, worst = rel_close(p, r, allow_frac=allow_frac)
-        assert ok, f"param {name}: {nbad}/{r.size} beyond 1e-4 (worst {worst:.3e})"
+def _check(res, allow_frac=1e-3, steps=1):
+    check_all(res, allow_frac=allow_frac, steps=steps)
 
 
 @pytest.mark.parametrize("backbone,mix", [("gqe", C1_MIX), ("q2b", ALL), ("gqe", ALL)])
@@ -44,7 +34,7 @@ def test_small_bmax_drains(small_graph, small_oracle_graph, backbone):
 def test_three_steps(small_graph, small_oracle_graph, backbone):
     res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=64, k=16, dim=32, steps=3,
                    compare_grads=True)
-    _check(res, allow_frac=2e-3)
+    _check(res, allow_frac=2e-3, steps=3)
 
 
 @pytest.mark.parametrize("backbone", ["gqe", "q2b"])
