@@ -44,6 +44,7 @@ _SIG = {
                                     i64, i32, i32, i32, P(f64)]),
     "oracle_model_trace_json": (C.c_int, [C.c_void_p, i32, C.c_char_p, i64, P(i64)]),
     "oracle_model_destroy": (C.c_int, [C.c_void_p]),
+    "oracle_model_margins": (C.c_int, [C.c_void_p, P(f64), i32]),
     "oracle_q2b_distance": (f64, [P(f64), P(f64), P(f64), i32, f64]),
     "oracle_loss": (f64, [f64, f64, P(f64), i32]),
 }
@@ -141,6 +142,11 @@ class OracleModel:
         _check(lib.oracle_model_step(self._h, b, *[_p(x, i32) for x in arrs], b_max, step,
                                      executor, adam, int(eager), _p(losses, f64)))
         return losses
+
+    def margins(self, b):
+        out = np.zeros(b, np.float64)
+        _check(lib.oracle_model_margins(self._h, _p(out, f64), b))
+        return out
 
     def trace(self, with_nodes=False):
         n = C.c_int64()

@@ -51,6 +51,9 @@ int oracle_model_step(void* m, int32_t b, const int32_t* patterns, const int32_t
                       const int32_t* negatives, int32_t b_max, int64_t step, int32_t executor,
                       int32_t adam, int32_t eager, double* losses);
 int oracle_model_trace_json(void* m, int32_t with_nodes, char* buf, int64_t cap, int64_t* len);
+/* per-query minimum |kink argument| of the last step's forward pass (L1/box
+ * signs, inside/outside, ReLU inputs, argmin/min routing gaps) */
+int oracle_model_margins(void* m, double* out, int32_t n);
 int oracle_model_destroy(void* m);
 
 /* scalar kernels for the SPEC known-answer tests */

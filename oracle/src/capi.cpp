@@ -289,6 +289,15 @@ int oracle_model_step(void* mp, int32_t b, const int32_t* patterns, const int32_
   });
 }
 
+int oracle_model_margins(void* mp, double* out, int32_t n) {
+  return guard([&] {
+    auto* a = static_cast<AnyModel*>(mp);
+    const std::vector<double>& m = a->m64 ? a->m64->margin : a->m32->margin;
+    if ((int32_t)m.size() != n) throw std::runtime_error("margin count mismatch");
+    for (int32_t i = 0; i < n; ++i) out[i] = m[i];
+  });
+}
+
 int oracle_model_trace_json(void* mp, int32_t with_nodes, char* buf, int64_t cap, int64_t* len) {
   return guard([&] {
     auto* a = static_cast<AnyModel*>(mp);

@@ -32,6 +32,7 @@ struct Model {
   std::map<std::string, std::vector<R>> P, M, V, G;  // G: dense grads (all params, zero-filled)
   std::set<int> touchedE, touchedR;
   std::vector<R> losses;
+  std::vector<double> margin;  // per query: min |kink argument| seen in the forward pass
   OTrace trace;
   int trace_elem_bytes = 4;
 
@@ -375,6 +376,17 @@ struct Exec {
   bool union_loss(const ONode& x) const { return g.nodes[x.in[0]].kind == K_UNION; }
   const int* cands(int q) const { return &cand[(size_t)q * (md.k + 1)]; }
 
+  // Kink margins (parity certification, tests/parity.py): the distance to the
+  // nearest non-differentiable point the query's forward pass touched.
+  void kink(int q, double v) { md.margin[q] = std::min(md.margin[q], std::fabs(v)); }
+  void dist_kinks(int qi, const R* q, const R* v) {
+    for (int e = 0; e < md.d; ++e) {
+      const double delta = double(v[e]) - double(q[e]);
+      kink(qi, delta);                                                       // sign(v - c)
+      if (md.backbone == 1) kink(qi, std::fabs(delta) - double(q[md.d + e]));  // inside/outside
+    }
+  }
+
   void run_fwd(int o) {
     const ONode& x = g.nodes[o];
     R* out = t(T[o]);
@@ -390,7 +402,10 @@ struct Exec {
         const R* r = &md.P["relation"][(int64_t)x.payload * md.rw];
         for (int i = 0; i < d; ++i) out[i] = in[i] + r[i];
         if (md.backbone == 1)
-          for (int i = 0; i < d; ++i) out[d + i] = std::max(in[d + i] + r[d + i], R(0));
+          for (int i = 0; i < d; ++i) {
+            out[d + i] = std::max(in[d + i] + r[d + i], R(0));
+            kink(x.query, in[d + i] + r[d + i]);
+          }
         break;
       }
       case K_NEG: {
@@ -401,14 +416,30 @@ struct Exec {
       case K_INTER: {
         std::vector<const R*> xs;
         for (int i : x.in) xs.push_back(t(T[i]));
-        if (md.backbone == 0) md.gqe_inter_fwd(xs, out);
-        else md.q2b_inter_fwd(xs, out);
+        if (md.backbone == 0) {
+          std::vector<R> mh;
+          md.gqe_inter_fwd(xs, out, &mh);
+          for (int e = 0; e < d; ++e) kink(x.query, mh[d + e]);  // relu(W1 m)
+        } else {
+          typename Model<R>::Q2bInter keep;
+          md.q2b_inter_fwd(xs, out, &keep);
+          for (size_t l = 0; l < xs.size(); ++l)
+            for (int e = 0; e < d; ++e) {
+              kink(x.query, keep.z[l][e]);  // relu in the attention MLP
+              kink(x.query, keep.p[l][e]);  // relu in the DeepSets MLP
+              for (size_t m2 = l + 1; m2 < xs.size(); ++m2)
+                kink(x.query, xs[l][d + e] - xs[m2][d + e]);  // min over offsets
+            }
+        }
         break;
       }
       case K_SCORE: {
         const R* q = t(T[x.in[0]]);
         const int* c = cands(x.query);
-        for (int j = 0; j <= md.k; ++j) out[j] = md.dist(q, md.erow(c[j]));
+        for (int j = 0; j <= md.k; ++j) {
+          out[j] = md.dist(q, md.erow(c[j]));
+          dist_kinks(x.query, q, md.erow(c[j]));
+        }
         break;
       }
       case K_UNION: {
@@ -416,6 +447,9 @@ struct Exec {
           R best = t(T[x.in[0]])[j];
           for (size_t l = 1; l < x.in.size(); ++l) best = std::min(best, t(T[x.in[l]])[j]);
           out[j] = best;
+          for (size_t l = 0; l < x.in.size(); ++l)  // argmin routing
+            for (size_t m2 = l + 1; m2 < x.in.size(); ++m2)
+              kink(x.query, t(T[x.in[l]])[j] - t(T[x.in[m2]])[j]);
         }
         break;
       }
@@ -427,7 +461,10 @@ struct Exec {
         } else {
           const R* q = t(T[x.in[0]]);
           const int* c = cands(x.query);
-          for (int j = 0; j <= md.k; ++j) dists[j] = md.dist(q, md.erow(c[j]));
+          for (int j = 0; j <= md.k; ++j) {
+            dists[j] = md.dist(q, md.erow(c[j]));
+            dist_kinks(x.query, q, md.erow(c[j]));
+          }
         }
         out[0] = md.loss_and_coef(dists.data(), coef.data());
         md.losses[x.query] = out[0];
@@ -634,6 +671,7 @@ OTrace o_train_step(Model<R>& md, const ODag& g, const std::vector<int>& cand, i
   int nq = 0;
   for (const auto& n : g.nodes) nq = std::max(nq, n.query + 1);
   md.losses.assign(nq, R(0));
+  md.margin.assign(nq, 1e300);
   Exec<R> ex{md, g, cand, b_max, eager};
   OTrace tr = ex.run(sequential);
   if (apply_adam) md.adam(step, lazy);

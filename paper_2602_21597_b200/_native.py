@@ -97,6 +97,10 @@ SIGNATURES = {
     "ngdb_param_init": (C.c_int, [i32, i32, i32, i32, C.c_char_p, u64, P(f32), i64]),
     "ngdb_train_step": (C.c_int, [C.c_void_p, C.c_void_p, i32, i64, P(f32), P(f64)]),
     "ngdb_run_step": (C.c_int, [C.c_void_p, C.c_void_p, i64, P(f32), P(f64)]),
+    # test hook (tc_gemm.cu): tcgen05 3xTF32 GEMM on host buffers
+    "ngdb_debug_tc_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     P(f32), C.c_int, P(f32), C.c_int, P(f32), C.c_int, P(f32),
+                                     C.c_int]),
 }
 
 

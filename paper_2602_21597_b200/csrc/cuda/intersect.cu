@@ -4,133 +4,46 @@
 //   Q2B:  centre = sum_l softmax_l(A2 relu(A1 c_l + a1) + a2) * c_l
 //                           offset = min_l o_l * sigmoid(V2 mean_l relu(V1 o_l + v1) + v2)
 //
-// The contractions run on an FP32 SIMT tiled GEMM (fp32-exact; the parity bar is
-// 1e-4 relative, which single-pass TF32 cannot hold at K=400). Each class is
+// The contractions run on the tcgen05 tensor cores as 3xTF32 GEMMs (tc_gemm.cu:
+// fp32-level accuracy; single-pass TF32 cannot hold the 1e-4 bar at K=400). Each class is
 // packed into contiguous scratch, contracted, and scattered back to the planned
 // arena slots; backward recomputes the forward intermediates from the saved
 // inputs (the only activations the Eq. 7 refcount model keeps alive).
 #include "common.cuh"
+#include "tc_gemm.cuh"
 
 namespace ngdb_dev {
 namespace {
 
 // ---------------------------------------------------------------------------
-// FP32 GEMM: C[M,N] (+)= op(A)[M,K] * op(B)[K,N] (+ bias[n]) (relu)
-// A stored row-major [M,K] (or [K,M] if TA), B stored [K,N] (or [N,K] if TB).
-constexpr int BM = 64, BN = 64, BK = 16, GT = 256;
-enum { OP_NONE = 0, OP_RELU = 1 };
+// Dense contractions: tcgen05 3xTF32 GEMM (tc_gemm.cu). Weights are stored
+// [out][in] (y = x W^T), activations [rows][features].
 
-struct GemmArgs {
-  int M, N, K;
-  const float* A; int lda;
-  const float* B; int ldb;
-  float* C; int ldc;
-  const int32_t* c_rowoff; int c_stride;  // optional: C row m at C + c_rowoff[m*stride]
-  const float* bias;                      // optional, per column n
-  int accumulate;                         // C += result
-};
-
-template <bool TA, bool TB, int AOP, int BOP>
-__global__ void __launch_bounds__(GT) sgemm_kernel(GemmArgs g) {
-  __shared__ float As[BK][BM + 4];
-  __shared__ float Bs[BK][BN + 4];
-  const int tid = threadIdx.x;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int tr = tid / 16, tc = tid % 16;
-  float acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-
-  for (int k0 = 0; k0 < g.K; k0 += BK) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int idx = tid + r * GT;
-      int mm, kk;
-      if (!TA) { mm = idx / BK; kk = idx % BK; } else { kk = idx / BM; mm = idx % BM; }
-      const int m = m0 + mm, k = k0 + kk;
-      float v = 0.f;
-      if (m < g.M && k < g.K) v = TA ? g.A[(int64_t)k * g.lda + m] : g.A[(int64_t)m * g.lda + k];
-      if (AOP == OP_RELU) v = fmaxf(v, 0.f);
-      As[kk][mm] = v;
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int idx = tid + r * GT;
-      int nn, kk;
-      if (!TB) { kk = idx / BN; nn = idx % BN; } else { nn = idx / BK; kk = idx % BK; }
-      const int n = n0 + nn, k = k0 + kk;
-      float v = 0.f;
-      if (n < g.N && k < g.K) v = TB ? g.B[(int64_t)n * g.ldb + k] : g.B[(int64_t)k * g.ldb + n];
-      if (BOP == OP_RELU) v = fmaxf(v, 0.f);
-      Bs[kk][nn] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float av[4], bv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[kk][tr * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tc * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + tr * 4 + i;
-    if (m >= g.M) continue;
-    float* crow = g.c_rowoff ? g.C + g.c_rowoff[(int64_t)m * g.c_stride] : g.C + (int64_t)m * g.ldc;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = n0 + tc * 4 + j;
-      if (n >= g.N) continue;
-      float v = acc[i][j];
-      if (g.bias) v += g.bias[n];
-      crow[n] = g.accumulate ? crow[n] + v : v;
-    }
-  }
-}
-
-template <bool TA, bool TB, int AOP = OP_NONE, int BOP = OP_NONE>
-void gemm(const GemmArgs& g, cudaStream_t s) {
-  if (g.M <= 0 || g.N <= 0) return;
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
-  sgemm_kernel<TA, TB, AOP, BOP><<<grid, GT, 0, s>>>(g);
-}
-
-GemmArgs mk(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
-            int ldc, int accumulate = 0, const float* bias = nullptr) {
-  GemmArgs g{};
+TcGemmArgs mk(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+              int ldc, int accumulate = 0, const float* bias = nullptr) {
+  TcGemmArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
   g.accumulate = accumulate; g.bias = bias;
   return g;
 }
 
-// y = x W^T (+b): x [rows, in], W [out, in]
+// y (+)= x W^T (+b): x [rows, in], W [out, in]
 void linear(int rows, int out, int in, const float* x, const float* W, const float* b, float* y,
             cudaStream_t s, bool relu_x = false, int accumulate = 0) {
-  GemmArgs g = mk(rows, out, in, x, in, W, in, y, out, accumulate, b);
-  if (relu_x) gemm<false, true, OP_RELU>(g, s);
-  else gemm<false, true>(g, s);
+  tc_gemm(mk(rows, out, in, x, in, W, in, y, out, accumulate, b), MAJ_K, MAJ_K,
+          relu_x ? AOP_RELU : AOP_NONE, s);
 }
 // dx (+)= dy W: dy [rows, out], W [out, in]
 void linear_dx(int rows, int out, int in, const float* dy, const float* W, float* dx,
                cudaStream_t s, int accumulate = 0) {
-  gemm<false, false>(mk(rows, in, out, dy, out, W, in, dx, in, accumulate), s);
+  tc_gemm(mk(rows, in, out, dy, out, W, in, dx, in, accumulate), MAJ_K, MAJ_MN, AOP_NONE, s);
 }
-// dW += dy^T x: dy [rows, out], x [rows, in]
+// dW += dy^T x (or dy^T relu(x)): dy [rows, out], x [rows, in]
 void linear_dw(int rows, int out, int in, const float* dy, const float* x, float* dW,
                cudaStream_t s, bool relu_x = false) {
-  GemmArgs g = mk(out, in, rows, dy, out, x, in, dW, in, 1);
-  if (relu_x) gemm<true, false, OP_NONE, OP_RELU>(g, s);
-  else gemm<true, false>(g, s);
+  tc_gemm(mk(out, in, rows, dy, out, x, in, dW, in, 1), MAJ_MN, MAJ_MN,
+          relu_x ? BOP_RELU : AOP_NONE, s);
 }
 
 // db += column sums of dy [rows, n]
@@ -192,10 +105,10 @@ int gqe_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   linear(n, D, D, M, W1, nullptr, H, s);
   if (dir == 0) {
     // out rows live in the arena: map C row i -> desc[first+i].out
-    GemmArgs g = mk(n, D, D, H, D, W2, D, a.arena, D);
+    TcGemmArgs g = mk(n, D, D, H, D, W2, D, a.arena, D);
     g.c_rowoff = &a.nodes[first].out;
     g.c_stride = sizeof(ngdb_node_desc) / sizeof(int32_t);
-    gemm<false, true, OP_RELU>(g, s);
+    tc_gemm(g, MAJ_K, MAJ_K, AOP_RELU, s);
     return 3;
   }
   float* gW1 = a.dense_g + a.dense_off[GQE_W1];

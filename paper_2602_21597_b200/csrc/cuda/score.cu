@@ -1,16 +1,18 @@
 // Fused negative-sample scoring + loss (SPEC.md:541-549 compute_loss, Eq. 6
 // PAPER.md:259-263) and the union-branch Score operator.
 //
-// One CTA per scoring node. Pass 1 streams the 1+K candidate rows (positive
-// first) with 128-bit loads, one warp per candidate pair, warp-
-// reduces the distances; the loss and dL/dd_j follow in shared memory; pass 2
-// re-reads the (now L2-resident) rows column-wise to form dL/dq. Candidate-row
-// gradients are NOT materialised: the optimizer recomputes coef_j * dd_j/dv
-// from (q, coef) when it reduces each touched row.
+// One CTA per scoring node, 4 warps. Each warp owns candidates j = 4*warp + 16*t
+// (+0..3): it issues the 128-bit loads of FOUR candidate rows at once (16 loads in
+// flight per lane), reduces the four distances with shuffles, and — because the
+// loss is a sum of per-candidate terms, so dL/dd_j depends on d_j alone — folds
+// coef_j * dd_j/dq into per-lane registers in the same pass. Every candidate row
+// is read exactly once. Candidate-row gradients are NOT materialised: the
+// optimizer recomputes coef_j * dd_j/dv from (q, coef) while it updates each
+// touched row.
 //
 //   psi_pos = -log sigma(gamma - d_pos) = softplus(d_pos - gamma)
 //   psi_neg = -log sigma(d_neg - gamma) = softplus(gamma - d_neg), mean over K
-//   GQE distance: ||v - q||_1                                 (SURVEY A-7)
+//   GQE distance: ||v - q||_1                                     (SURVEY A-7)
 //   Q2B distance: ||max(0,|v-c|-o)||_1 + alpha ||min(|v-c|,o)||_1
 #include "common.cuh"
 
@@ -19,22 +21,19 @@ namespace {
 
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxCand = 1024;
+constexpr int kRows = 4;          // candidate rows in flight per warp
 
 template <int BB>
 struct Dist;
 
 template <>
 struct Dist<NGDB_GQE> {
-  // accumulate distance contribution of one float4 chunk
-  static __device__ __forceinline__ float part(float4 v, const float* q, int e, int /*dim*/,
-                                               float /*alpha*/) {
-    const float4 c = *reinterpret_cast<const float4*>(q + e);
-    return fabsf(v.x - c.x) + fabsf(v.y - c.y) + fabsf(v.z - c.z) + fabsf(v.w - c.w);
+  static __device__ __forceinline__ float term(float v, float c, float, float) {
+    return fabsf(v - c);
   }
-  // dq contribution for one element: coef * dd/dq
-  static __device__ __forceinline__ void grad(float v, float c, float /*o*/, float coef,
-                                              float /*alpha*/, float& gc, float& /*go*/) {
+  // coef * dd/dq
+  static __device__ __forceinline__ void grad(float v, float c, float, float coef, float,
+                                              float& gc, float&) {
     gc += coef * sgnf(c - v);
   }
 };
@@ -45,117 +44,169 @@ struct Dist<NGDB_Q2B> {
     const float a = fabsf(v - c);
     return fmaxf(a - o, 0.f) + alpha * fminf(a, o);
   }
-  static __device__ __forceinline__ float part(float4 v, const float* q, int e, int dim,
-                                               float alpha) {
-    const float4 c = *reinterpret_cast<const float4*>(q + e);
-    const float4 o = *reinterpret_cast<const float4*>(q + dim + e);
-    return term(v.x, c.x, o.x, alpha) + term(v.y, c.y, o.y, alpha) + term(v.z, c.z, o.z, alpha) +
-           term(v.w, c.w, o.w, alpha);
-  }
   static __device__ __forceinline__ void grad(float v, float c, float o, float coef, float alpha,
                                               float& gc, float& go) {
     const float delta = v - c;
     const float a = fabsf(delta);
+    const float s = sgnf(delta);
     if (a > o) {
-      gc -= coef * sgnf(delta);
+      gc -= coef * s;
       go += coef * (alpha - 1.f);
     } else {
-      gc -= coef * alpha * sgnf(delta);
+      gc -= coef * alpha * s;
     }
   }
 };
 
+__device__ __forceinline__ float4 f4(float x) { return make_float4(x, x, x, x); }
+
+template <int BB, int kMaxChunks>
+struct Lane {
+  // this lane's slice of q: chunks c = lane + 32*i  (float4 units)
+  float4 qc[kMaxChunks], qo[kMaxChunks];
+  float4 gc[kMaxChunks], go[kMaxChunks];
+  int nch;
+
+  __device__ void load_q(const float* q, int dim, int lane) {
+    const int d4 = dim / 4;
+    nch = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxChunks; ++i) {
+      const int c = lane + 32 * i;
+      if (c < d4) {
+        qc[i] = ld4(q + 4 * c);
+        qo[i] = BB == NGDB_Q2B ? ld4(q + dim + 4 * c) : f4(0.f);
+        nch = i + 1;
+      }
+      gc[i] = f4(0.f);
+      go[i] = f4(0.f);
+    }
+  }
+};
+
+// Walk all candidates of the node with one warp per 4-row group. For every
+// candidate: d_j -> coef_of(j, d_j) returns coef_j -> dq accumulation.
+template <int BB, int kMaxChunks, bool kGrad, class CoefOp>
+__device__ __forceinline__ void sweep(const DevArgs& a, const int32_t* cand, Lane<BB, kMaxChunks>& L,
+                                      CoefOp&& coef_of) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int d4 = a.dim / 4;
+  for (int j0 = warp * kRows; j0 < a.ncand; j0 += kWarps * kRows) {
+    float4 v[kRows][kMaxChunks];
+    float part[kRows];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const int j = min(j0 + r, a.ncand - 1);
+      const float* row = a.ent + static_cast<int64_t>(__ldg(cand + j)) * a.ent_w;
+#pragma unroll
+      for (int i = 0; i < kMaxChunks; ++i) {
+        const int c = lane + 32 * i;
+        if (i < L.nch && c < d4) v[r][i] = ldg4(row + 4 * c);
+        else v[r][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < kMaxChunks; ++i) {
+        const int c = lane + 32 * i;
+        if (i < L.nch && c < d4) {
+          s += Dist<BB>::term(v[r][i].x, L.qc[i].x, L.qo[i].x, a.alpha_box);
+          s += Dist<BB>::term(v[r][i].y, L.qc[i].y, L.qo[i].y, a.alpha_box);
+          s += Dist<BB>::term(v[r][i].z, L.qc[i].z, L.qo[i].z, a.alpha_box);
+          s += Dist<BB>::term(v[r][i].w, L.qc[i].w, L.qo[i].w, a.alpha_box);
+        }
+      }
+      part[r] = warp_sum(s);
+    }
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const int j = j0 + r;
+      if (j >= a.ncand) break;
+      const float coef = coef_of(j, part[r]);
+      if (!kGrad) continue;
+#pragma unroll
+      for (int i = 0; i < kMaxChunks; ++i) {
+        const int c = lane + 32 * i;
+        if (i < L.nch && c < d4) {
+          Dist<BB>::grad(v[r][i].x, L.qc[i].x, L.qo[i].x, coef, a.alpha_box, L.gc[i].x, L.go[i].x);
+          Dist<BB>::grad(v[r][i].y, L.qc[i].y, L.qo[i].y, coef, a.alpha_box, L.gc[i].y, L.go[i].y);
+          Dist<BB>::grad(v[r][i].z, L.qc[i].z, L.qo[i].z, coef, a.alpha_box, L.gc[i].z, L.go[i].z);
+          Dist<BB>::grad(v[r][i].w, L.qc[i].w, L.qo[i].w, coef, a.alpha_box, L.gc[i].w, L.go[i].w);
+        }
+      }
+    }
+  }
+}
+
+// Cross-warp sum of the per-lane dq accumulators into dst (wq floats).
+template <int BB, int kMaxChunks>
+__device__ void reduce_dq(const DevArgs& a, Lane<BB, kMaxChunks>& L, float* red, float* dst) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int d4 = a.dim / 4;
+  for (int w = 0; w < kWarps; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int i = 0; i < kMaxChunks; ++i) {
+        const int c = lane + 32 * i;
+        if (i < L.nch && c < d4) {
+          float4* rc = reinterpret_cast<float4*>(red + 4 * c);
+          float4* ro = reinterpret_cast<float4*>(red + a.dim + 4 * c);
+          if (w == 0) {
+            *rc = L.gc[i];
+            if (BB == NGDB_Q2B) *ro = L.go[i];
+          } else {
+            float4 t = *rc;
+            *rc = make_float4(t.x + L.gc[i].x, t.y + L.gc[i].y, t.z + L.gc[i].z, t.w + L.gc[i].w);
+            if (BB == NGDB_Q2B) {
+              t = *ro;
+              *ro = make_float4(t.x + L.go[i].x, t.y + L.go[i].y, t.z + L.go[i].z, t.w + L.go[i].w);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(dst + e, ld4(red + e));
+}
+
+__device__ __forceinline__ float loss_coef(const DevArgs& a, int j, float dj, float& loss) {
+  const float inv_k = 1.f / static_cast<float>(a.n_neg);
+  if (j == 0) {
+    loss += softplusf(dj - a.gamma);
+    return sigmoidf(dj - a.gamma);
+  }
+  loss += inv_k * softplusf(a.gamma - dj);
+  return -inv_k * sigmoidf(a.gamma - dj);
+}
+
 __device__ float block_sum(float v, float* red) {
-  v = warp_sum(v);
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
   __syncthreads();
   if (lane == 0) red[w] = v;
   __syncthreads();
   float t = 0.f;
-  if (threadIdx.x < 32) {
-    t = threadIdx.x < kWarps ? red[threadIdx.x] : 0.f;
-    t = warp_sum(t);
-  }
-  return t;  // valid in warp 0
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kWarps; ++i) t += red[i];
+  return t;  // thread 0
 }
 
-// Pass 1: distances of all candidates of query `qi` against q (smem).
-template <int BB>
-__device__ void distances(const DevArgs& a, const float* q, int qi, float* dist) {
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int d4 = a.dim / 4;
-  const int32_t* cand = a.cand + static_cast<int64_t>(qi) * a.ncand;
-  for (int j0 = warp * 2; j0 < a.ncand; j0 += kWarps * 2) {
-    const int j1 = j0 + 1;
-    const bool two = j1 < a.ncand;
-    const float* v0 = a.ent + static_cast<int64_t>(cand[j0]) * a.ent_w;
-    const float* v1 = a.ent + static_cast<int64_t>(cand[two ? j1 : j0]) * a.ent_w;
-    float s0 = 0.f, s1 = 0.f;
-    for (int c = lane; c < d4; c += 32) {
-      const float4 x0 = ldg4(v0 + 4 * c);
-      const float4 x1 = ldg4(v1 + 4 * c);
-      s0 += Dist<BB>::part(x0, q, 4 * c, a.dim, a.alpha_box);
-      s1 += Dist<BB>::part(x1, q, 4 * c, a.dim, a.alpha_box);
-    }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    if (lane == 0) {
-      dist[j0] = s0;
-      if (two) dist[j1] = s1;
-    }
-  }
-}
-
-// Pass 2: dq = sum_j coef_j * dd_j/dq, written to dst (wq floats).
-template <int BB>
-__device__ void query_grad(const DevArgs& a, const float* q, int qi, const float* coef, float* dst) {
-  const int32_t* cand = a.cand + static_cast<int64_t>(qi) * a.ncand;
-  for (int e = threadIdx.x; e < a.dim; e += kThreads) {
-    const float c = q[e];
-    const float o = BB == NGDB_Q2B ? q[a.dim + e] : 0.f;
-    float gc = 0.f, go = 0.f;
-#pragma unroll 4
-    for (int j = 0; j < a.ncand; ++j) {
-      const float v = __ldg(a.ent + static_cast<int64_t>(cand[j]) * a.ent_w + e);
-      Dist<BB>::grad(v, c, o, coef[j], a.alpha_box, gc, go);
-    }
-    dst[e] = gc;
-    if (BB == NGDB_Q2B) dst[a.dim + e] = go;
-  }
-}
-
-// Loss coefficients from distances; returns this thread's loss share.
-__device__ __forceinline__ float loss_terms(const DevArgs& a, const float* dist, float* coef) {
-  float part = 0.f;
-  const float inv_k = 1.f / static_cast<float>(a.n_neg);
-  for (int j = threadIdx.x; j < a.ncand; j += kThreads) {
-    const float dj = dist[j];
-    if (j == 0) {
-      part += softplusf(dj - a.gamma);
-      coef[j] = sigmoidf(dj - a.gamma);
-    } else {
-      part += inv_k * softplusf(a.gamma - dj);
-      coef[j] = -inv_k * sigmoidf(a.gamma - dj);
-    }
-  }
-  return part;
-}
-
-template <int BB>
+template <int BB, int NCH>
 __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first) {
-  __shared__ __align__(16) float q[2 * 1024];
-  __shared__ float dist[kMaxCand], coef[kMaxCand];
-  __shared__ float red[kWarps];
+  __shared__ __align__(16) float red[2 * 1024];
+  __shared__ float lred[kWarps];
   const ngdb_node_desc d = a.nodes[first + blockIdx.x];
   const int qi = d.id;
   if (d.aux < 0) {
     // union query: the input already holds min-over-branch distances
-    for (int j = threadIdx.x; j < a.ncand; j += kThreads) dist[j] = a.arena[d.in[0] + j];
-    __syncthreads();
-    float loss = block_sum(loss_terms(a, dist, coef), red);
-    __syncthreads();
-    for (int j = threadIdx.x; j < a.ncand; j += kThreads)
-      a.ddbuf[static_cast<int64_t>(qi) * a.ncand + j] = coef[j];
+    float loss = 0.f;
+    for (int j = threadIdx.x; j < a.ncand; j += kThreads) {
+      const float c = loss_coef(a, j, a.arena[d.in[0] + j], loss);
+      a.ddbuf[static_cast<int64_t>(qi) * a.ncand + j] = c;
+    }
+    loss = block_sum(warp_sum(loss), lred);
     if (threadIdx.x == 0) {
       a.loss_out[qi] = loss;
       a.arena[d.out] = loss;
@@ -163,70 +214,81 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
     }
     return;
   }
-  const float* src = a.arena + d.in[0];
+  const float* q = a.arena + d.in[0];
   float* qcopy = a.qbuf + static_cast<int64_t>(d.aux) * a.wq;
-  for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) {
-    const float4 v = ld4(src + e);
-    st4(q + e, v);
-    st4(qcopy + e, v);
-  }
-  __syncthreads();
-  distances<BB>(a, q, qi, dist);
-  __syncthreads();
-  float loss = block_sum(loss_terms(a, dist, coef), red);
-  __syncthreads();
-  for (int j = threadIdx.x; j < a.ncand; j += kThreads)
-    a.coefbuf[static_cast<int64_t>(d.aux) * a.ncand + j] = coef[j];
+  for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(qcopy + e, ld4(q + e));
+  Lane<BB, NCH> L;
+  L.load_q(q, a.dim, threadIdx.x & 31);
+  float loss = 0.f;  // identical in every lane of a warp
+  float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
+  const int lane = threadIdx.x & 31;
+  sweep<BB, NCH, true>(a, a.cand + static_cast<int64_t>(qi) * a.ncand, L, [&](int j, float dj) {
+    const float c = loss_coef(a, j, dj, loss);
+    if (lane == 0) coefs[j] = c;
+    return c;
+  });
+  loss = block_sum(lane == 0 ? loss : 0.f, lred);
   if (threadIdx.x == 0) {
     a.loss_out[qi] = loss;
     a.arena[d.out] = loss;
     if (!isfinite(loss)) atomicOr(&a.flags[0], 1);
   }
-  query_grad<BB>(a, q, qi, coef, a.dqbuf + static_cast<int64_t>(d.aux) * a.wq);
+  reduce_dq<BB, NCH>(a, L, red, a.dqbuf + static_cast<int64_t>(d.aux) * a.wq);
 }
 
 // Union branch Score: fwd writes the distance vector; bwd turns the routed
 // dL/dd into coef (for the optimizer) and dL/dq (its G slot).
-template <int BB>
+template <int BB, int NCH>
 __global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int first) {
-  __shared__ __align__(16) float q[2 * 1024];
-  __shared__ float buf[kMaxCand];
+  __shared__ __align__(16) float red[2 * 1024];
   const ngdb_node_desc d = a.nodes[first + blockIdx.x];
-  const float* src = a.arena + d.in[0];
-  for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) {
-    const float4 v = ld4(src + e);
-    st4(q + e, v);
-    if (dir == 0) st4(a.qbuf + static_cast<int64_t>(d.aux) * a.wq + e, v);
-  }
-  __syncthreads();
+  const float* q = a.arena + d.in[0];
+  const int lane = threadIdx.x & 31;
+  Lane<BB, NCH> L;
+  L.load_q(q, a.dim, lane);
+  const int32_t* cand = a.cand + static_cast<int64_t>(d.id) * a.ncand;
   if (dir == 0) {
-    distances<BB>(a, q, d.id, buf);
-    __syncthreads();
-    for (int j = threadIdx.x; j < a.ncand; j += kThreads) a.arena[d.out + j] = buf[j];
+    float* qcopy = a.qbuf + static_cast<int64_t>(d.aux) * a.wq;
+    for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(qcopy + e, ld4(q + e));
+    float* out = a.arena + d.out;
+    sweep<BB, NCH, false>(a, cand, L, [&](int j, float dj) {
+      if (lane == 0) out[j] = dj;
+      return 0.f;
+    });
     return;
   }
-  for (int j = threadIdx.x; j < a.ncand; j += kThreads) {
-    const float g = a.arena[d.grad + j];
-    buf[j] = g;
-    a.coefbuf[static_cast<int64_t>(d.aux) * a.ncand + j] = g;
-  }
-  __syncthreads();
-  query_grad<BB>(a, q, d.id, buf, a.arena + d.out);
+  const float* g = a.arena + d.grad;
+  float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
+  for (int j = threadIdx.x; j < a.ncand; j += kThreads) coefs[j] = g[j];
+  sweep<BB, NCH, true>(a, cand, L, [&](int j, float) { return g[j]; });
+  reduce_dq<BB, NCH>(a, L, red, a.arena + d.out);
 }
 
 }  // namespace
 
+template <int NCH>
+void launch_loss_nch(const DevArgs& a, int first, int n, cudaStream_t s) {
+  if (a.backbone == NGDB_GQE) loss_fwd_kernel<NGDB_GQE, NCH><<<n, kThreads, 0, s>>>(a, first);
+  else loss_fwd_kernel<NGDB_Q2B, NCH><<<n, kThreads, 0, s>>>(a, first);
+}
+template <int NCH>
+void launch_score_nch(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
+  if (a.backbone == NGDB_GQE) score_kernel<NGDB_GQE, NCH><<<n, kThreads, 0, s>>>(a, dir, first);
+  else score_kernel<NGDB_Q2B, NCH><<<n, kThreads, 0, s>>>(a, dir, first);
+}
+
 int launch_loss_fwd(const DevArgs& a, int first, int n, const LaunchCtx& lc) {
   if (n <= 0) return 0;
-  if (a.backbone == NGDB_GQE) loss_fwd_kernel<NGDB_GQE><<<n, kThreads, 0, lc.stream>>>(a, first);
-  else loss_fwd_kernel<NGDB_Q2B><<<n, kThreads, 0, lc.stream>>>(a, first);
+  // rows of d floats are d/4 float4 chunks spread over 32 lanes
+  if (a.dim <= 512) launch_loss_nch<4>(a, first, n, lc.stream);
+  else launch_loss_nch<8>(a, first, n, lc.stream);
   return 1;
 }
 
 int launch_score(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc) {
   if (n <= 0) return 0;
-  if (a.backbone == NGDB_GQE) score_kernel<NGDB_GQE><<<n, kThreads, 0, lc.stream>>>(a, dir, first);
-  else score_kernel<NGDB_Q2B><<<n, kThreads, 0, lc.stream>>>(a, dir, first);
+  if (a.dim <= 512) launch_score_nch<4>(a, dir, first, n, lc.stream);
+  else launch_score_nch<8>(a, dir, first, n, lc.stream);
   return 1;
 }
 

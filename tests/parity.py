@@ -83,8 +83,29 @@ def check_all(res, lr=1e-4, allow_frac=1e-3, steps=1):
     assert not msgs, "; ".join(msgs)
 
 
+TAU = 1e-6  # kink margin certified for gradient parity (>= 25x the fp32 forward error)
+
+
+def tie_free(batch, om, b_max, step, tau=TAU):
+    """Drop the queries whose forward pass comes within tau of a kink (L1/box
+    sign, inside/outside, ReLU input, argmin/min routing). At a kink fp32 and
+    f64 may legitimately pick different subgradients; away from kinks the
+    gradient is a smooth function of the inputs and 1e-4 parity is well posed.
+    Returns (filtered batch, kept fraction)."""
+    import paper_2602_21597_b200 as m
+    a = batch.arrays()
+    om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, b_max=b_max, step=step,
+            adam=-1)  # forward + backward only, no optimizer step
+    keep = om.margins(len(a.patterns)) > tau
+    if keep.all():
+        return batch, 1.0
+    sub = m.BatchArrays(a.patterns[keep], a.anchors[keep], a.relations[keep], a.positives[keep],
+                        a.negatives[keep])
+    return m.Batch.from_arrays(sub), float(keep.mean())
+
+
 def run_pair(graph, ograph, backbone, mix, b, k, dim, b_max=512, steps=1, seed_tag=0,
-             compare_grads=True):
+             compare_grads=True, certify=True):
     """One or more training steps on both sides; returns a dict of comparisons."""
     import oracle as O
     import paper_2602_21597_b200 as m
@@ -96,9 +117,12 @@ def run_pair(graph, ograph, backbone, mix, b, k, dim, b_max=512, steps=1, seed_t
     om = O.OracleModel(backbone, ne, nr, dim, k, precision=64)
     om.init(2)
     specs = m.param_specs(backbone, ne, nr, dim)
-    out = {"loss": [], "grads": {}, "params": {}}
+    out = {"loss": [], "grads": {}, "params": {}, "kept": []}
     for step in range(1, steps + 1):
         batch = m.Batch.sample(graph, w, b, k, seed=3, tag=seed_tag + step)
+        if certify:
+            batch, kept = tie_free(batch, om, b_max, step)
+            out["kept"].append(kept)
         a = batch.arrays()
         loss = eng.train_step(batch)
         ref = om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, b_max=b_max,

@@ -4,7 +4,7 @@ parameter and post-Adam parameters within 1e-4 relative (tests/parity.py)."""
 import numpy as np
 import pytest
 
-from parity import check_all, run_pair
+from parity import check_all, rel_close, run_pair
 
 pytestmark = pytest.mark.gpu
 
@@ -12,7 +12,7 @@ ALL = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin"
 C1_MIX = ["1p", "2p", "3p", "2i", "3i"]
 
 
-def _check(res, allow_frac=1e-3, steps=1):
+def _check(res, allow_frac=0.0, steps=1):
     check_all(res, allow_frac=allow_frac, steps=steps)
 
 
@@ -34,14 +34,27 @@ def test_small_bmax_drains(small_graph, small_oracle_graph, backbone):
 def test_three_steps(small_graph, small_oracle_graph, backbone):
     res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=64, k=16, dim=32, steps=3,
                    compare_grads=True)
-    _check(res, allow_frac=2e-3, steps=3)
+    _check(res, steps=3)
 
 
 @pytest.mark.parametrize("backbone", ["gqe", "q2b"])
 def test_full_batch_k128(small_graph, small_oracle_graph, backbone):
-    # the benchmark's per-step shape: 512 queries, 128 negatives, d=400
+    # the benchmark's per-step shape (512 queries, 128 negatives, d=400): at this
+    # size most queries touch an L1/box kink within 1e-6 (26M sign tests per
+    # step), so gradients are compared on the certified tie-free subset ...
     res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=512, k=128, dim=400)
+    assert res["kept"][0] * 512 >= 16
     _check(res)
+
+
+@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+def test_full_batch_k128_losses(small_graph, small_oracle_graph, backbone):
+    # ... while every per-query loss of the full 512-query batch must agree
+    res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=512, k=128, dim=400,
+                   compare_grads=False, certify=False)
+    for loss, ref in res["loss"]:
+        ok, nbad, worst = rel_close(loss, ref)
+        assert ok, f"loss: {nbad} bad, worst {worst:.3e}"
 
 
 @pytest.mark.parametrize("pattern", ALL)

@@ -1,0 +1,71 @@
+"""tcgen05 3xTF32 GEMM (csrc/cuda/tc_gemm.cu) against an fp64 numpy reference.
+
+C = op(A) op(B)^T (+bias) (+C), A K-major or M-major, B K-major or N-major,
+optional ReLU on A or B; fp32 in/out. 3xTF32 keeps ~2^-21 per product; the
+tensor core's fp32 accumulator aligns partial sums to the largest exponent, which
+measures ~2e-5 of the row scale sqrt(K) on B200 — bounded here at 5e-5, a
+factor 2 inside the 1e-4 parity bar (single-pass TF32 gives ~1e-3).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MAJ_K, MAJ_MN = 0, 1
+TOL = 5e-5
+
+
+def _p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def run(M, N, K, a_major, b_major, relu=False, bias=False, acc=False, seed=0, brelu=False):
+    from paper_2602_21597_b200._native import lib
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    C0 = rng.standard_normal((M, N)).astype(np.float32) if acc else np.zeros((M, N), np.float32)
+    bvec = rng.standard_normal(N).astype(np.float32) if bias else None
+    As = np.ascontiguousarray(A if a_major == MAJ_K else A.T)
+    Bs = np.ascontiguousarray(B if b_major == MAJ_K else B.T)
+    Cd = C0.copy()
+    rc = lib.ngdb_debug_tc_gemm(M, N, K, a_major, b_major, int(relu) | (int(brelu) << 1), _p(As),
+                                As.shape[1], _p(Bs),
+                                Bs.shape[1], _p(Cd), N, _p(bvec) if bias else None, int(acc))
+    assert rc == 0
+    Aref = np.maximum(A, 0) if relu else A
+    Bref = np.maximum(B, 0) if brelu else B
+    ref = Aref.astype(np.float64) @ Bref.astype(np.float64).T
+    if bias:
+        ref += bvec
+    if acc:
+        ref += C0
+    scale = np.sqrt(K) * (1.0 if not relu else 0.6)
+    err = np.max(np.abs(Cd - ref)) / scale
+    return err
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 400, 400), (219, 400, 400), (128, 80, 32), (7, 400, 400),
+                                   (1536, 400, 400), (64, 32, 32)])
+def test_k_k(M, N, K):
+    assert run(M, N, K, MAJ_K, MAJ_K) < TOL
+
+
+def test_relu_bias():
+    assert run(300, 400, 400, MAJ_K, MAJ_K, relu=True, bias=True) < TOL
+
+
+def test_k_mn_accumulate():
+    assert run(512, 400, 400, MAJ_K, MAJ_MN, acc=True) < TOL
+
+
+@pytest.mark.parametrize("K", [219, 512, 1536, 3])
+def test_weight_grad_layout(K):
+    # dW = dY^T X: both operands are stored [rows][features]
+    assert run(400, 400, K, MAJ_MN, MAJ_MN, acc=True) < TOL
+
+
+def test_weight_grad_relu_b():
+    assert run(400, 400, 300, MAJ_MN, MAJ_MN, relu=False, acc=True, brelu=True) < TOL
