@@ -40,6 +40,10 @@ struct DevArgs {
   float* dense;       // flat dense params
   float* dense_g;     // flat dense grads
   int64_t dense_off[kMaxDenseTensors];
+  // 3xTF32 operand splits of every dense weight matrix W [out][in], refreshed
+  // after each optimizer step: W_hi, W_lo, (W^T)_hi, (W^T)_lo at wsplit_off[i]
+  float* wsplit;
+  int64_t wsplit_off[kMaxDenseTensors];
   float* qbuf;        // [S][wq]   query copy per score slot
   float* dqbuf;       // [S][wq]   dL/dq per score slot (fused Loss)
   float* coefbuf;     // [S][ncand] dL/dd per score slot and candidate
@@ -100,6 +104,11 @@ int launch_loss_fwd(const DevArgs& a, int first, int n, const LaunchCtx& lc);
 int launch_score(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
 // intersect.cu
 int launch_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc);
+// scratch floats the intersect operators need for classes of up to max_nodes
+int64_t intersect_scratch_floats(int backbone, int dim, int max_nodes);
+// tc_gemm.cu: refresh the hi/lo (and transposed) splits of dense weight i
+int split_weight(const float* w, int rows, int cols, float* dst, cudaStream_t s);
+void tc_gemm_init();
 // optim.cu
 struct SparseTable {
   float* w; float* m; float* v; float* dbg_g;
@@ -107,10 +116,14 @@ struct SparseTable {
   int32_t n_rows;
   const int32_t* rows; const int32_t* seg; const int32_t* contrib;
 };
-int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, float lr, float b1,
-                               float b2, float eps, float bc1, float bc2, const LaunchCtx& lc);
-int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, float lr, float b1,
-                                 float b2, float eps, float bc1, float bc2, const LaunchCtx& lc);
-int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, float lr, float b1,
-                       float b2, float eps, float bc1, float bc2, const LaunchCtx& lc);
+struct AdamHyper {
+  float lr, b1, b2, eps;
+};
+// bc: device pointer to {1 - b1^t, 1 - b2^t} for the current step t
+int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
+                              const float* bc, const LaunchCtx& lc);
+int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
+                                const float* bc, const LaunchCtx& lc);
+int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, const AdamHyper& hp,
+                      const float* bc, const LaunchCtx& lc);
 }  // namespace ngdb_dev

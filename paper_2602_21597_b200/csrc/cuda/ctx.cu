@@ -59,6 +59,7 @@ struct Param {
   std::string name;
   int64_t rows = 0, cols = 0;
   bool sparse = false;
+  int dense_idx = -1;
   float *w = nullptr, *m = nullptr, *v = nullptr, *g = nullptr;
   int64_t n() const { return rows * cols; }
 };
@@ -148,6 +149,11 @@ struct ngdb_plan {
   int32_t* blob = nullptr;
   PlanLayout layout{ngdb_step_plan{}};
   PlanMeta meta;
+  // CUDA graph of the whole step (resident plans), valid while the context's
+  // buffer generation is unchanged
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_gen = -1;
+  int64_t graph_launches = 0;
 };
 
 struct ngdb_ctx {
@@ -162,6 +168,8 @@ struct ngdb_ctx {
   int64_t dense_off[kMaxDenseTensors] = {};
   float* sem = nullptr;
   int64_t sem_n = 0;
+  float* wsplit = nullptr;
+  int64_t wsplit_off[kMaxDenseTensors] = {};
   // per-step staging
   float *qbuf = nullptr, *dqbuf = nullptr, *coefbuf = nullptr, *ddbuf = nullptr, *agbuf = nullptr,
         *rgbuf = nullptr, *loss_out = nullptr;
@@ -189,6 +197,9 @@ struct ngdb_ctx {
   double fam_ms[F_COUNT] = {}, fam_bytes[F_COUNT] = {};
   int64_t fam_launches[F_COUNT] = {};
   int64_t launches = 0;
+  float* d_bc = nullptr;        // Adam bias corrections of the current step
+  int64_t buffer_gen = 0;       // bumped whenever a buffer captured by a graph moves
+  bool use_graphs = true;
   float* l2_flush = nullptr;
   int64_t l2_flush_bytes = 0;
 
@@ -268,10 +279,12 @@ void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
     realloc_f(c->agbuf, c->cap_anchor * ew);
     realloc_f(c->rgbuf, c->cap_project * rw);
     realloc_f(c->loss_out, c->cap_queries);
+    ++c->buffer_gen;
   }
   if (m.arena_elems > c->arena_cap) {
     CK(cudaStreamSynchronize(c->stream));
     ensure_f(c->arena, c->arena_cap, m.arena_elems + 64);
+    ++c->buffer_gen;
   }
 }
 
@@ -295,7 +308,11 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.rel = c->params[c->rel_idx].w;
   a.dense = c->dense_w;
   a.dense_g = c->dense_g;
-  for (int i = 0; i < kMaxDenseTensors; ++i) a.dense_off[i] = c->dense_off[i];
+  for (int i = 0; i < kMaxDenseTensors; ++i) {
+    a.dense_off[i] = c->dense_off[i];
+    a.wsplit_off[i] = c->wsplit_off[i];
+  }
+  a.wsplit = c->wsplit;
   a.qbuf = c->qbuf;
   a.dqbuf = c->dqbuf;
   a.coefbuf = c->coefbuf;
@@ -404,11 +421,33 @@ void begin_step_device(ngdb_ctx* c) {
       if (p.sparse && p.g) CK(cudaMemsetAsync(p.g, 0, p.n() * sizeof(float), c->stream));
 }
 
-void optimizer(ngdb_ctx* c, const ngdb_plan* p, int64_t step) {
+// 3xTF32 operand splits of the dense weight matrices (W and W^T, hi and lo),
+// consumed by every MLP GEMM of the next step.
+int refresh_weight_splits(ngdb_ctx* c) {
+  int launches = 0;
+  for (const auto& p : c->params)
+    if (!p.sparse && p.rows > 1)
+      launches += split_weight(p.w, static_cast<int>(p.rows), static_cast<int>(p.cols),
+                               c->wsplit + c->wsplit_off[p.dense_idx], c->stream);
+  return launches;
+}
+
+// Adam bias corrections of step t -> device scalars (read by the optimizer
+// kernels, so a captured graph of the step replays with the current t). The
+// source is pageable: the copy is staged before cudaMemcpyAsync returns.
+void set_step_scalars(ngdb_ctx* c, int64_t step) {
   if (step < 1) throw Fail{NGDB_ERR_CONFIG, "optimizer step must be >= 1"};
   const ngdb_model_desc& d = c->desc;
-  const float bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta1), double(step)));
-  const float bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta2), double(step)));
+  const float bc[2] = {
+      static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta1), double(step))),
+      static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta2), double(step)))};
+  CK(cudaMemcpyAsync(c->d_bc, bc, sizeof(bc), cudaMemcpyHostToDevice, c->stream));
+}
+
+void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
+  const ngdb_model_desc& d = c->desc;
+  const AdamHyper hp{d.lr, d.beta1, d.beta2, d.eps_adam};
+  const float* bc = c->d_bc;
   const DevArgs a = make_args(c, p);
   const LaunchCtx lc{c->stream, c->num_sms};
   Param& ent = c->params[c->ent_idx];
@@ -421,18 +460,23 @@ void optimizer(ngdb_ctx* c, const ngdb_plan* p, int64_t step) {
                  p->blob + p->layout.rcon};
   const double eb = 6.0 * p->meta.n_erows * ent.cols * 4 + 8.0 * p->meta.n_econ +
                     p->meta.n_score * double(c->query_width()) * 4;
-  timed(c, F_OPT_ENTITY, eb, [&] {
-    return launch_sparse_adam_entity(a, te, d.lr, d.beta1, d.beta2, d.eps_adam, bc1, bc2, lc);
-  });
+  timed(c, F_OPT_ENTITY, eb, [&] { return launch_sparse_adam_entity(a, te, hp, bc, lc); });
   const double rb = 6.0 * p->meta.n_rrows * rel.cols * 4 + p->meta.n_rcon * (4.0 + rel.cols * 4);
-  timed(c, F_OPT_RELATION, rb, [&] {
-    return launch_sparse_adam_relation(a, tr, d.lr, d.beta1, d.beta2, d.eps_adam, bc1, bc2, lc);
-  });
+  timed(c, F_OPT_RELATION, rb, [&] { return launch_sparse_adam_relation(a, tr, hp, bc, lc); });
   timed(c, F_OPT_DENSE, 28.0 * c->dense_n, [&] {
-    return launch_dense_adam(c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->dense_n, d.lr,
-                             d.beta1, d.beta2, d.eps_adam, bc1, bc2, lc);
+    return launch_dense_adam(c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->dense_n, hp, bc,
+                             lc) +
+           refresh_weight_splits(c);
   });
   CK(cudaGetLastError());
+}
+
+// Every launch of one planned step, in order (capturable: no host syncs,
+// no host-side allocation).
+void launch_step(ngdb_ctx* c, const ngdb_plan* p) {
+  begin_step_device(c);
+  for (const auto& d : p->meta.pools) exec_pool(c, p, d);
+  optimizer(c, p);
 }
 
 void upload_plan(ngdb_ctx* c, const ngdb_step_plan& plan, ngdb_plan* dst, int64_t& dst_cap,
@@ -546,6 +590,7 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
         if (p.name == "entity") c->ent_idx = static_cast<int>(i);
         if (p.name == "relation") c->rel_idx = static_cast<int>(i);
       } else {
+        p.dense_idx = dense_i;
         const int64_t o = c->dense_off[dense_i++];
         p.w = c->dense_w + o;
         p.m = c->dense_m + o;
@@ -553,11 +598,20 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
         p.g = c->dense_g + o;
       }
     }
+    int64_t woff = 0;
+    for (const auto& p : c->params)
+      if (!p.sparse) {
+        c->wsplit_off[p.dense_idx] = woff;
+        if (p.rows > 1) woff += 4 * p.n();
+      }
+    c->wsplit = dmalloc<float>(woff);
+    CK(cudaMemset(c->wsplit, 0, woff * 4));
     c->flags = reinterpret_cast<int32_t*>(dmalloc<float>(4));
     CK(cudaMemset(c->flags, 0, 16));
-    const int64_t mb = c->desc.max_batch;
-    c->scratch_cap = d.backbone == NGDB_GQE ? 4 * mb * D : (9 * 3 * mb + 4 * mb) * D;
+    c->scratch_cap = intersect_scratch_floats(d.backbone, d.dim, c->desc.max_batch);
     c->scratch = dmalloc<float>(c->scratch_cap);
+    c->d_bc = dmalloc<float>(4);
+    tc_gemm_init();
     CK(cudaEventCreate(&c->t0));
     CK(cudaEventCreate(&c->t1));
     for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->staged[i], cudaEventDisableTiming));
@@ -578,9 +632,9 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
       cudaFree(p.v);
       if (p.g) cudaFree(p.g);
     }
-  for (float* p : {c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->sem, c->qbuf, c->dqbuf,
+  for (float* p : {c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit, c->sem, c->qbuf, c->dqbuf,
                    c->coefbuf, c->ddbuf, c->agbuf, c->rgbuf, c->loss_out, c->scratch, c->arena,
-                   c->l2_flush})
+                   c->l2_flush, c->d_bc})
     if (p) cudaFree(p);
   if (c->flags) cudaFree(c->flags);
   for (int i = 0; i < 2; ++i) {
@@ -644,6 +698,7 @@ int ngdb_param_upload(ngdb_ctx* c, const char* name, const float* host, int64_t 
   return guarded([&] {
     float* dst = resolve(c, name, n);
     CK(cudaMemcpyAsync(dst, host, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    refresh_weight_splits(c);  // dense weights feed the GEMMs through their splits
     CK(cudaStreamSynchronize(c->stream));
   });
 }
@@ -711,7 +766,8 @@ int ngdb_exec_pool(ngdb_ctx* c, const ngdb_pool_desc* pool) {
 int ngdb_optimizer_step(ngdb_ctx* c, int64_t step) {
   return guarded([&] {
     if (!c->active) throw Fail{NGDB_ERR_CONFIG, "optimizer_step outside a step"};
-    optimizer(c, c->active, step);
+    set_step_scalars(c, step);
+    optimizer(c, c->active);
   });
 }
 
@@ -764,15 +820,43 @@ int ngdb_plan_create(ngdb_ctx* c, const ngdb_step_plan* plan, ngdb_plan** out) {
 int ngdb_plan_run(ngdb_ctx* c, ngdb_plan* p, int64_t step) {
   return guarded([&] {
     ensure_step_buffers(c, p->meta);
-    begin_step_device(c);
-    for (const auto& d : p->meta.pools) exec_pool(c, p, d);
-    optimizer(c, p, step);
+    set_step_scalars(c, step);
     c->active = p;
+    if (c->profiling || !c->use_graphs) {
+      launch_step(c, p);
+      return;
+    }
+    if (!p->graph || p->graph_gen != c->buffer_gen) {
+      // capture the step's ~100+ launches once; replays cost one launch
+      if (p->graph) CK(cudaGraphExecDestroy(p->graph));
+      p->graph = nullptr;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      const int64_t l0 = c->launches;
+      try {
+        launch_step(c, p);
+      } catch (...) {
+        cudaStreamEndCapture(c->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        c->launches = l0;
+        throw;
+      }
+      p->graph_launches = c->launches - l0;
+      c->launches = l0;
+      CK(cudaStreamEndCapture(c->stream, &g));
+      const cudaError_t e = cudaGraphInstantiate(&p->graph, g, 0);
+      cudaGraphDestroy(g);
+      CK(e);
+      p->graph_gen = c->buffer_gen;
+    }
+    CK(cudaGraphLaunch(p->graph, c->stream));
+    c->launches += p->graph_launches;
   });
 }
 
 int ngdb_plan_destroy(ngdb_plan* p) {
   if (!p) return NGDB_OK;
+  if (p->graph) cudaGraphExecDestroy(p->graph);
   if (p->blob) cudaFree(p->blob);
   delete p;
   return NGDB_OK;

@@ -4,82 +4,108 @@
 //   Q2B:  centre = sum_l softmax_l(A2 relu(A1 c_l + a1) + a2) * c_l
 //                           offset = min_l o_l * sigmoid(V2 mean_l relu(V1 o_l + v1) + v2)
 //
-// The contractions run on the tcgen05 tensor cores as 3xTF32 GEMMs (tc_gemm.cu:
-// fp32-level accuracy; single-pass TF32 cannot hold the 1e-4 bar at K=400). Each class is
-// packed into contiguous scratch, contracted, and scattered back to the planned
-// arena slots; backward recomputes the forward intermediates from the saved
-// inputs (the only activations the Eq. 7 refcount model keeps alive).
+// Every dense contraction runs on the tcgen05 tensor cores as a 3xTF32 GEMM
+// (tc_gemm.cu; fp32-grade accuracy — single-pass TF32 cannot hold the 1e-4
+// parity bar at K=400). Operands enter pre-split (hi/lo): weights once per
+// optimizer step, activations from the packing kernels or from the epilogue of
+// the GEMM that produced them; the weight-gradient operands (dY^T, X^T) are
+// transposed+split in one batched launch. Independent GEMMs of a dependency
+// level share one grouped launch. Backward recomputes the forward
+// intermediates from the saved inputs (the only activations the Eq. 7 refcount
+// model keeps alive). Rows are node-major: row = i*k + l.
+#include <algorithm>
+
 #include "common.cuh"
 #include "tc_gemm.cuh"
 
 namespace ngdb_dev {
 namespace {
 
-// ---------------------------------------------------------------------------
-// Dense contractions: tcgen05 3xTF32 GEMM (tc_gemm.cu). Weights are stored
-// [out][in] (y = x W^T), activations [rows][features].
+// bump allocator over the context scratch buffer
+struct Scratch {
+  float* p;
+  int64_t left;
+  float* take(int64_t n) {
+    n = (n + 3) / 4 * 4;
+    float* r = p;
+    p += n;
+    left -= n;
+    return left >= 0 ? r : nullptr;
+  }
+};
 
-TcGemmArgs mk(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
-              int ldc, int accumulate = 0, const float* bias = nullptr) {
+struct Split {
+  float* hi;
+  float* lo;
+};
+Split take_split(Scratch& s, int64_t n) { return {s.take(n), s.take(n)}; }
+
+SplitOperand op(Split x, int ld) { return {x.hi, x.lo, ld}; }
+// weight W_i [out][in] as B of y = x W^T (K = in), or its transpose as B of dx = dy W (K = out)
+SplitOperand wop(const DevArgs& a, int i, int rows, int cols, bool transposed) {
+  const int64_t n = (int64_t)rows * cols;
+  const float* base = a.wsplit + a.wsplit_off[i];
+  return transposed ? SplitOperand{base + 2 * n, base + 3 * n, rows} : SplitOperand{base, base + n, cols};
+}
+
+TcGemmArgs gemm_args(int M, int N, int K, SplitOperand A, SplitOperand B, float* C, int ldc) {
   TcGemmArgs g{};
   g.M = M; g.N = N; g.K = K;
-  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
-  g.accumulate = accumulate; g.bias = bias;
+  g.A = A; g.B = B; g.C = C; g.ldc = ldc;
   return g;
 }
 
-// y (+)= x W^T (+b): x [rows, in], W [out, in]
-void linear(int rows, int out, int in, const float* x, const float* W, const float* b, float* y,
-            cudaStream_t s, bool relu_x = false, int accumulate = 0) {
-  tc_gemm(mk(rows, out, in, x, in, W, in, y, out, accumulate, b), MAJ_K, MAJ_K,
-          relu_x ? AOP_RELU : AOP_NONE, s);
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  lo = x - hi;
 }
-// dx (+)= dy W: dy [rows, out], W [out, in]
-void linear_dx(int rows, int out, int in, const float* dy, const float* W, float* dx,
-               cudaStream_t s, int accumulate = 0) {
-  tc_gemm(mk(rows, in, out, dy, out, W, in, dx, in, accumulate), MAJ_K, MAJ_MN, AOP_NONE, s);
-}
-// dW += dy^T x (or dy^T relu(x)): dy [rows, out], x [rows, in]
-void linear_dw(int rows, int out, int in, const float* dy, const float* x, float* dW,
-               cudaStream_t s, bool relu_x = false) {
-  tc_gemm(mk(out, in, rows, dy, out, x, in, dW, in, 1), MAJ_MN, MAJ_MN,
-          relu_x ? BOP_RELU : AOP_NONE, s);
+__device__ __forceinline__ void put(float* plain, Split s, int64_t i, float v) {
+  if (plain) plain[i] = v;
+  float h, l;
+  split_tf32(v, h, l);
+  s.hi[i] = h;
+  s.lo[i] = l;
 }
 
-// db += column sums of dy [rows, n]
-__global__ void colsum_kernel(const float* dy, int rows, int n, float* db) {
+// bias gradients of a class in one launch: db_j += column sums of dy_j
+struct ColsumJob {
+  const float* dy;
+  int rows, n;
+  float* db;
+};
+struct ColsumJobs {
+  ColsumJob job[4];
+  int n;
+};
+__global__ void colsum_kernel(ColsumJobs jobs) {
+  const ColsumJob& j = jobs.job[blockIdx.y];
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
+  if (c >= j.n) return;
   float s = 0.f;
-  for (int r = 0; r < rows; ++r) s += dy[(int64_t)r * n + c];
-  db[c] += s;
+  for (int r = 0; r < j.rows; ++r) s += j.dy[(int64_t)r * j.n + c];
+  j.db[c] += s;
 }
-void colsum(const float* dy, int rows, int n, float* db, cudaStream_t s) {
-  colsum_kernel<<<(n + 127) / 128, 128, 0, s>>>(dy, rows, n, db);
+int colsums(const ColsumJobs& jobs, int n, cudaStream_t s) {
+  colsum_kernel<<<dim3((n + 127) / 128, jobs.n), 128, 0, s>>>(jobs);
+  return 1;
 }
 
 // ---------------------------------------------------------------------------
-// GQE helpers
+// GQE
 
-// M[i] = mean_l x_l ; optionally G[i] = grad row
-__global__ void gqe_pack_kernel(DevArgs a, int k, int first, int n, float* M, float* G) {
+// M[i] = mean_l x_l (plain + split); optionally G[i] = upstream grad (plain + split)
+__global__ void gqe_pack_kernel(DevArgs a, int k, int first, float* M, Split Ms, float* G,
+                                Split Gs) {
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < a.dim; e += blockDim.x) {
     float s = 0.f;
     for (int l = 0; l < k; ++l) s += a.arena[d.in[l] + e];
-    M[(int64_t)i * a.dim + e] = s * inv_k;
-    if (G) G[(int64_t)i * a.dim + e] = a.arena[d.grad + e];
+    const int64_t o = (int64_t)i * a.dim + e;
+    put(M, Ms, o, s * inv_k);
+    if (G) put(G, Gs, o, a.arena[d.grad + e]);
   }
-}
-// dH = dA * (H > 0), in place on dA
-__global__ void relu_mask_kernel(float* dA, const float* H, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && H[i] <= 0.f) dA[i] = 0.f;
-}
-void relu_mask(float* dA, const float* H, int64_t n, cudaStream_t s) {
-  relu_mask_kernel<<<(int)((n + 255) / 256), 256, 0, s>>>(dA, H, n);
 }
 // G_X row l of node i = dM[i] / k  (mean adjoint)
 __global__ void gqe_scatter_kernel(DevArgs a, int k, int first, const float* dM) {
@@ -95,53 +121,81 @@ __global__ void gqe_scatter_kernel(DevArgs a, int k, int first, const float* dM)
 int gqe_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream_t s) {
   const int D = a.dim;
   const int64_t nd = (int64_t)n * D;
-  float* M = a.scratch;
-  float* H = M + nd;
-  float* G = H + nd;
-  float* dA = G + nd;
-  const float* W1 = a.dense + a.dense_off[GQE_W1];
-  const float* W2 = a.dense + a.dense_off[GQE_W2];
-  gqe_pack_kernel<<<n, 128, 0, s>>>(a, k, first, n, M, dir ? G : nullptr);
-  linear(n, D, D, M, W1, nullptr, H, s);
+  const int nP = (n + 3) & ~3;  // transposed operands: rows padded for 16-B cp.async
+  const int64_t ndp = (int64_t)nP * D;
+  Scratch sc{a.scratch, a.scratch_cap};
+  float* M = sc.take(nd);
+  Split Ms = take_split(sc, nd);
+  float* H = sc.take(nd);
+  Split RHs = take_split(sc, nd);  // split(relu(H))
+  float* G = dir ? sc.take(nd) : nullptr;
+  Split Gs = dir ? take_split(sc, nd) : Split{nullptr, nullptr};
+  int launches = 0;
+
+  gqe_pack_kernel<<<n, 128, 0, s>>>(a, k, first, M, Ms, G, Gs);
+  ++launches;
+  TcGemmArgs h = gemm_args(n, D, D, op(Ms, D), wop(a, GQE_W1, D, D, false), H, D);
+  h.s_hi = RHs.hi; h.s_lo = RHs.lo; h.s_relu = 1;
+  launches += tc_gemm(h, s);
   if (dir == 0) {
-    // out rows live in the arena: map C row i -> desc[first+i].out
-    TcGemmArgs g = mk(n, D, D, H, D, W2, D, a.arena, D);
-    g.c_rowoff = &a.nodes[first].out;
-    g.c_stride = sizeof(ngdb_node_desc) / sizeof(int32_t);
-    tc_gemm(g, MAJ_K, MAJ_K, AOP_RELU, s);
-    return 3;
+    // y = relu(H) W2^T, scattered straight into the planned arena slots
+    TcGemmArgs y = gemm_args(n, D, D, op(RHs, D), wop(a, GQE_W2, D, D, false), a.arena, D);
+    y.c_rowoff = &a.nodes[first].out;
+    y.c_stride = sizeof(ngdb_node_desc) / sizeof(int32_t);
+    return launches + tc_gemm(y, s);
   }
+  float* dH = sc.take(nd);
+  Split dHs = take_split(sc, nd);
+  Split GT = take_split(sc, ndp), RHT = take_split(sc, ndp), dHT = take_split(sc, ndp),
+        MT = take_split(sc, ndp);
+  float* dM = sc.take(nd);
   float* gW1 = a.dense_g + a.dense_off[GQE_W1];
   float* gW2 = a.dense_g + a.dense_off[GQE_W2];
-  linear_dx(n, D, D, G, W2, dA, s);           // dA = G W2
-  linear_dw(n, D, D, G, H, gW2, s, true);     // gW2 += G^T relu(H)
-  relu_mask(dA, H, nd, s);                    // dH
-  linear_dw(n, D, D, dA, M, gW1, s);          // gW1 += dH^T M
-  linear_dx(n, D, D, dA, W1, H, s);           // dM = dH W1 (H reused)
-  gqe_scatter_kernel<<<n, 128, 0, s>>>(a, k, first, H);
-  return 8;
+  // dH = (G W2) * (H > 0), also split for dM = dH W1
+  TcGemmArgs da = gemm_args(n, D, D, op(Gs, D), wop(a, GQE_W2, D, D, true), dH, D);
+  da.mask = H;
+  da.s_hi = dHs.hi; da.s_lo = dHs.lo;
+  launches += tc_gemm(da, s);
+  SplitJobs jobs{};
+  jobs.job[0] = {G, n, D, D, 0, GT.hi, GT.lo};
+  jobs.job[1] = {H, n, D, D, 1, RHT.hi, RHT.lo};
+  jobs.job[2] = {dH, n, D, D, 0, dHT.hi, dHT.lo};
+  jobs.job[3] = {M, n, D, D, 0, MT.hi, MT.lo};
+  jobs.n = 4;
+  launches += split_transposed(jobs, s);
+  TcGemmArgs lvl[3];
+  lvl[0] = gemm_args(D, D, n, op(GT, nP), op(RHT, nP), gW2, D);  // gW2 += G^T relu(H)
+  lvl[0].accumulate = 1;
+  lvl[1] = gemm_args(D, D, n, op(dHT, nP), op(MT, nP), gW1, D);  // gW1 += dH^T M
+  lvl[1].accumulate = 1;
+  lvl[2] = gemm_args(n, D, D, op(dHs, D), wop(a, GQE_W1, D, D, true), dM, D);  // dM = dH W1
+  launches += tc_gemm_batch(lvl, 3, s);
+  gqe_scatter_kernel<<<n, 128, 0, s>>>(a, k, first, dM);
+  return launches + 1;
 }
 
 // ---------------------------------------------------------------------------
-// Q2B helpers (rows are node-major: row = i*k + l)
+// Q2B
 
-__global__ void q2b_pack_kernel(DevArgs a, int k, int first, float* Cin, float* Oin) {
+__global__ void q2b_pack_kernel(DevArgs a, int k, int first, float* Cin, Split Cs, float* Oin,
+                                Split Os) {
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
     for (int e = threadIdx.x; e < a.dim; e += blockDim.x) {
-      Cin[((int64_t)i * k + l) * a.dim + e] = a.arena[d.in[l] + e];
-      Oin[((int64_t)i * k + l) * a.dim + e] = a.arena[d.in[l] + a.dim + e];
+      const int64_t r = ((int64_t)i * k + l) * a.dim + e;
+      put(Cin, Cs, r, a.arena[d.in[l] + e]);
+      put(Oin, Os, r, a.arena[d.in[l] + a.dim + e]);
     }
 }
-// Lm[i] = mean_l relu(P[i*k+l])
-__global__ void q2b_mean_relu_kernel(const float* P, int k, int D, float* Lm) {
+// Lm[i] = mean_l relu(P[i*k+l]) (plain + split)
+__global__ void q2b_mean_relu_kernel(const float* P, int k, int D, float* Lm, Split Lms) {
   const int i = blockIdx.x;
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     float s = 0.f;
     for (int l = 0; l < k; ++l) s += fmaxf(P[((int64_t)i * k + l) * D + e], 0.f);
-    Lm[(int64_t)i * D + e] = s * inv_k;
+    put(Lm, Lms, (int64_t)i * D + e, s * inv_k);
   }
 }
 __device__ __forceinline__ void softmax_k(const float* S, int64_t base, int k, int D, int e,
@@ -175,8 +229,8 @@ __global__ void q2b_combine_kernel(DevArgs a, int k, int first, const float* S, 
   }
 }
 __global__ void q2b_combine_bwd_kernel(DevArgs a, int k, int first, const float* S, const float* U,
-                                       const float* Cin, const float* Oin, float* gS, float* dCin,
-                                       float* dOin, float* gU) {
+                                       const float* Cin, const float* Oin, float* gS, Split gSs,
+                                       float* dCin, float* dOin, float* gU, Split gUs) {
   const int i = blockIdx.x;
   const int D = a.dim;
   const ngdb_node_desc d = a.nodes[first + i];
@@ -200,21 +254,22 @@ __global__ void q2b_combine_bwd_kernel(DevArgs a, int k, int first, const float*
     const float gate = sigmoidf(U[(int64_t)i * D + e]);
     for (int l = 0; l < k; ++l) {
       const int64_t r = base + (int64_t)l * D + e;
-      gS[r] = w[l] * (ga[l] - dot);
+      put(gS, gSs, r, w[l] * (ga[l] - dot));
       dCin[r] = gC * w[l];
       dOin[r] = (l == arg) ? gO * gate : 0.f;
     }
-    gU[(int64_t)i * D + e] = gO * mn * gate * (1.f - gate);
+    put(gU, gUs, (int64_t)i * D + e, gO * mn * gate * (1.f - gate));
   }
 }
-// gP[i*k+l] = gLm[i] / k * (P > 0)
-__global__ void q2b_gp_kernel(const float* gLm, const float* P, int k, int D, float* gP) {
+// gP[i*k+l] = gLm[i] / k * (P > 0)  (plain + split)
+__global__ void q2b_gp_kernel(const float* gLm, const float* P, int k, int D, float* gP,
+                              Split gPs) {
   const int i = blockIdx.x;
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < D; e += blockDim.x)
     for (int l = 0; l < k; ++l) {
       const int64_t r = ((int64_t)i * k + l) * D + e;
-      gP[r] = P[r] > 0.f ? gLm[(int64_t)i * D + e] * inv_k : 0.f;
+      put(gP, gPs, r, P[r] > 0.f ? gLm[(int64_t)i * D + e] * inv_k : 0.f);
     }
 }
 __global__ void q2b_scatter_kernel(DevArgs a, int k, int first, const float* dCin,
@@ -234,59 +289,132 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   const int D = a.dim;
   const int R = n * k;
   const int64_t rd = (int64_t)R * D, nd = (int64_t)n * D;
-  float* Cin = a.scratch;
-  float* Oin = Cin + rd;
-  float* Z = Oin + rd;
-  float* S = Z + rd;
-  float* P = S + rd;
-  float* Lm = P + rd;
-  float* U = Lm + nd;
+  // transposed (weight-gradient) operands: rows padded for 16-byte cp.async
+  const int nP = (n + 3) & ~3, RP = (R + 3) & ~3;
+  const int64_t ndp = (int64_t)nP * D, rdp = (int64_t)RP * D;
+  Scratch sc{a.scratch, a.scratch_cap};
+  float* Cin = sc.take(rd);
+  Split Cs = take_split(sc, rd);
+  float* Oin = sc.take(rd);
+  Split Os = take_split(sc, rd);
+  float* Z = sc.take(rd);
+  Split RZs = take_split(sc, rd);  // split(relu(Z))
+  float* S = sc.take(rd);
+  float* P = sc.take(rd);
+  float* Lm = sc.take(nd);
+  Split Lms = take_split(sc, nd);
+  float* U = sc.take(nd);
   const float* p = a.dense;
-  const float *A1 = p + a.dense_off[Q2B_A1], *a1 = p + a.dense_off[Q2B_A1B];
-  const float *A2 = p + a.dense_off[Q2B_A2], *a2 = p + a.dense_off[Q2B_A2B];
-  const float *V1 = p + a.dense_off[Q2B_V1], *v1 = p + a.dense_off[Q2B_V1B];
-  const float *V2 = p + a.dense_off[Q2B_V2], *v2 = p + a.dense_off[Q2B_V2B];
+  const float* a1 = p + a.dense_off[Q2B_A1B];
+  const float* a2 = p + a.dense_off[Q2B_A2B];
+  const float* v1 = p + a.dense_off[Q2B_V1B];
+  const float* v2 = p + a.dense_off[Q2B_V2B];
+  int launches = 0;
 
-  q2b_pack_kernel<<<n, 128, 0, s>>>(a, k, first, Cin, Oin);
-  linear(R, D, D, Cin, A1, a1, Z, s);
-  linear(R, D, D, Z, A2, a2, S, s, /*relu_x=*/true);
-  linear(R, D, D, Oin, V1, v1, P, s);
-  q2b_mean_relu_kernel<<<n, 128, 0, s>>>(P, k, D, Lm);
-  linear(n, D, D, Lm, V2, v2, U, s);
+  q2b_pack_kernel<<<n, 128, 0, s>>>(a, k, first, Cin, Cs, Oin, Os);
+  ++launches;
+  {  // level 1: Z = A1 c + a1 (chained split of relu(Z)), P = V1 o + v1
+    TcGemmArgs lvl[2];
+    lvl[0] = gemm_args(R, D, D, op(Cs, D), wop(a, Q2B_A1, D, D, false), Z, D);
+    lvl[0].bias = a1;
+    lvl[0].s_hi = RZs.hi; lvl[0].s_lo = RZs.lo; lvl[0].s_relu = 1;
+    lvl[1] = gemm_args(R, D, D, op(Os, D), wop(a, Q2B_V1, D, D, false), P, D);
+    lvl[1].bias = v1;
+    launches += tc_gemm_batch(lvl, 2, s);
+  }
+  q2b_mean_relu_kernel<<<n, 128, 0, s>>>(P, k, D, Lm, Lms);
+  ++launches;
+  {  // level 2: S = A2 relu(Z) + a2, U = V2 Lm + v2
+    TcGemmArgs lvl[2];
+    lvl[0] = gemm_args(R, D, D, op(RZs, D), wop(a, Q2B_A2, D, D, false), S, D);
+    lvl[0].bias = a2;
+    lvl[1] = gemm_args(n, D, D, op(Lms, D), wop(a, Q2B_V2, D, D, false), U, D);
+    lvl[1].bias = v2;
+    launches += tc_gemm_batch(lvl, 2, s);
+  }
   if (dir == 0) {
     q2b_combine_kernel<<<n, 128, 0, s>>>(a, k, first, S, U, Cin, Oin);
-    return 7;
+    return launches + 1;
   }
-  float* gS = U + nd;
-  float* dCin = gS + rd;
-  float* dOin = dCin + rd;
-  float* gU = dOin + rd;
-  float* gLm = gU + nd;
-  float* gP = gLm + nd;
+  float* gS = sc.take(rd);
+  Split gSs = take_split(sc, rd);
+  float* dCin = sc.take(rd);
+  float* dOin = sc.take(rd);
+  float* gU = sc.take(nd);
+  Split gUs = take_split(sc, nd);
+  float* gLm = sc.take(nd);
+  float* gP = sc.take(rd);
+  Split gPs = take_split(sc, rd);
+  float* gZ = sc.take(rd);
+  Split gZs = take_split(sc, rd);
+  Split gUT = take_split(sc, ndp), LmT = take_split(sc, ndp), gST = take_split(sc, rdp),
+        RZT = take_split(sc, rdp), gPT = take_split(sc, rdp), OT = take_split(sc, rdp),
+        gZT = take_split(sc, rdp), CT = take_split(sc, rdp);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
-  q2b_combine_bwd_kernel<<<n, 128, 0, s>>>(a, k, first, S, U, Cin, Oin, gS, dCin, dOin, gU);
-  // offset branch: gate = sigmoid(V2 Lm + v2), Lm = mean relu(V1 o + v1)
-  linear_dw(n, D, D, gU, Lm, g + off[Q2B_V2], s);
-  colsum(gU, n, D, g + off[Q2B_V2B], s);
-  linear_dx(n, D, D, gU, V2, gLm, s);
-  q2b_gp_kernel<<<n, 128, 0, s>>>(gLm, P, k, D, gP);
-  linear_dw(R, D, D, gP, Oin, g + off[Q2B_V1], s);
-  colsum(gP, R, D, g + off[Q2B_V1B], s);
-  linear_dx(R, D, D, gP, V1, dOin, s, /*accumulate=*/1);
-  // centre branch: S = A2 relu(Z) + a2, Z = A1 c + a1
-  linear_dw(R, D, D, gS, Z, g + off[Q2B_A2], s, /*relu_x=*/true);
-  colsum(gS, R, D, g + off[Q2B_A2B], s);
-  linear_dx(R, D, D, gS, A2, gP, s);  // gR (gP buffer reused)
-  relu_mask(gP, Z, rd, s);            // gZ
-  linear_dw(R, D, D, gP, Cin, g + off[Q2B_A1], s);
-  colsum(gP, R, D, g + off[Q2B_A1B], s);
-  linear_dx(R, D, D, gP, A1, dCin, s, /*accumulate=*/1);
+
+  q2b_combine_bwd_kernel<<<n, 128, 0, s>>>(a, k, first, S, U, Cin, Oin, gS, gSs, dCin, dOin, gU,
+                                           gUs);
+  ++launches;
+  SplitJobs j1{};
+  j1.job[0] = {gU, n, D, D, 0, gUT.hi, gUT.lo};
+  j1.job[1] = {Lm, n, D, D, 0, LmT.hi, LmT.lo};
+  j1.job[2] = {gS, R, D, D, 0, gST.hi, gST.lo};
+  j1.job[3] = {Z, R, D, D, 1, RZT.hi, RZT.lo};
+  j1.n = 4;
+  launches += split_transposed(j1, s);
+  {  // level 3: weight grads of V2, A2; gLm = gU V2; gZ = (gS A2) * (Z > 0)
+    TcGemmArgs lvl[4];
+    lvl[0] = gemm_args(D, D, n, op(gUT, nP), op(LmT, nP), g + off[Q2B_V2], D);
+    lvl[0].accumulate = 1;
+    lvl[1] = gemm_args(D, D, R, op(gST, RP), op(RZT, RP), g + off[Q2B_A2], D);
+    lvl[1].accumulate = 1;
+    lvl[2] = gemm_args(n, D, D, op(gUs, D), wop(a, Q2B_V2, D, D, true), gLm, D);
+    lvl[3] = gemm_args(R, D, D, op(gSs, D), wop(a, Q2B_A2, D, D, true), gZ, D);
+    lvl[3].mask = Z;
+    lvl[3].s_hi = gZs.hi; lvl[3].s_lo = gZs.lo;
+    launches += tc_gemm_batch(lvl, 4, s);
+  }
+  q2b_gp_kernel<<<n, 128, 0, s>>>(gLm, P, k, D, gP, gPs);
+  ++launches;
+  SplitJobs j2{};
+  j2.job[0] = {gP, R, D, D, 0, gPT.hi, gPT.lo};
+  j2.job[1] = {Oin, R, D, D, 0, OT.hi, OT.lo};
+  j2.job[2] = {gZ, R, D, D, 0, gZT.hi, gZT.lo};
+  j2.job[3] = {Cin, R, D, D, 0, CT.hi, CT.lo};
+  j2.n = 4;
+  launches += split_transposed(j2, s);
+  {  // level 4: weight grads of V1, A1; input grads dOin += gP V1, dCin += gZ A1
+    TcGemmArgs lvl[4];
+    lvl[0] = gemm_args(D, D, R, op(gPT, RP), op(OT, RP), g + off[Q2B_V1], D);
+    lvl[0].accumulate = 1;
+    lvl[1] = gemm_args(D, D, R, op(gZT, RP), op(CT, RP), g + off[Q2B_A1], D);
+    lvl[1].accumulate = 1;
+    lvl[2] = gemm_args(R, D, D, op(gPs, D), wop(a, Q2B_V1, D, D, true), dOin, D);
+    lvl[2].accumulate = 1;
+    lvl[3] = gemm_args(R, D, D, op(gZs, D), wop(a, Q2B_A1, D, D, true), dCin, D);
+    lvl[3].accumulate = 1;
+    launches += tc_gemm_batch(lvl, 4, s);
+  }
+  ColsumJobs cj{};
+  cj.job[0] = {gU, n, D, g + off[Q2B_V2B]};
+  cj.job[1] = {gS, R, D, g + off[Q2B_A2B]};
+  cj.job[2] = {gP, R, D, g + off[Q2B_V1B]};
+  cj.job[3] = {gZ, R, D, g + off[Q2B_A1B]};
+  cj.n = 4;
+  launches += colsums(cj, D, s);
   q2b_scatter_kernel<<<n, 128, 0, s>>>(a, k, first, dCin, dOin);
-  return 22;
+  return launches + 1;
 }
 
 }  // namespace
+
+int64_t intersect_scratch_floats(int backbone, int dim, int max_nodes) {
+  const int64_t nd = (int64_t)max_nodes * dim, rd = 3 * nd;
+  // + padding of the transposed operands (<= 3 rows each)
+  if (backbone == NGDB_GQE) return 24 * nd + 32 * (int64_t)dim + 64;
+  return 36 * rd + 14 * nd + 64 * (int64_t)dim + 256;
+}
 
 int launch_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc) {
   if (n <= 0) return 0;

@@ -12,6 +12,9 @@
 //            this kernel reads anyway for the update. The 66k x 1600 B candidate
 //            gradient rows of a step are therefore never written to HBM.
 // HBM traffic per touched row: read theta, m, v; write theta, m, v (6 w bytes).
+//
+// Adam's bias corrections bc = (1 - b1^t, 1 - b2^t) are read from device
+// memory so a captured CUDA graph of the step replays with the current t.
 #include <algorithm>
 
 #include "common.cuh"
@@ -21,22 +24,27 @@ namespace {
 
 constexpr int kWarps = 8;
 
-__device__ __forceinline__ float adam_update(float& w, float& m, float& v, float g, float lr,
-                                             float b1, float b2, float eps, float bc1, float bc2) {
-  m = b1 * m + (1.f - b1) * g;
-  v = b2 * v + (1.f - b2) * g * g;
-  const float mhat = m / bc1;
-  const float vhat = v / bc2;
-  w -= lr * mhat / (sqrtf(vhat) + eps);
-  return w;
+struct AdamK {
+  float lr, b1, b2, eps, bc1, bc2;
+};
+
+__device__ __forceinline__ AdamK adam_consts(const AdamHyper& h, const float* bc) {
+  return AdamK{h.lr, h.b1, h.b2, h.eps, bc[0], bc[1]};
 }
 
-__device__ __forceinline__ float4 adam4(float4 w, float4& m, float4& v, float4 g, float lr, float b1,
-                                        float b2, float eps, float bc1, float bc2) {
-  adam_update(w.x, m.x, v.x, g.x, lr, b1, b2, eps, bc1, bc2);
-  adam_update(w.y, m.y, v.y, g.y, lr, b1, b2, eps, bc1, bc2);
-  adam_update(w.z, m.z, v.z, g.z, lr, b1, b2, eps, bc1, bc2);
-  adam_update(w.w, m.w, v.w, g.w, lr, b1, b2, eps, bc1, bc2);
+__device__ __forceinline__ void adam_update(float& w, float& m, float& v, float g, const AdamK& k) {
+  m = k.b1 * m + (1.f - k.b1) * g;
+  v = k.b2 * v + (1.f - k.b2) * g * g;
+  const float mhat = m / k.bc1;
+  const float vhat = v / k.bc2;
+  w -= k.lr * mhat / (sqrtf(vhat) + k.eps);
+}
+
+__device__ __forceinline__ float4 adam4(float4 w, float4& m, float4& v, float4 g, const AdamK& k) {
+  adam_update(w.x, m.x, v.x, g.x, k);
+  adam_update(w.y, m.y, v.y, g.y, k);
+  adam_update(w.z, m.z, v.z, g.z, k);
+  adam_update(w.w, m.w, v.w, g.w, k);
   return w;
 }
 
@@ -49,12 +57,12 @@ __device__ __forceinline__ float cand_grad(float v, float qc, float qo, float co
 }
 
 template <int BB>
-__global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, SparseTable t, float lr,
-                                                                  float b1, float b2, float eps,
-                                                                  float bc1, float bc2) {
+__global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, SparseTable t,
+                                                                  AdamHyper hp, const float* bc) {
   const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row_idx >= t.n_rows) return;
+  const AdamK k = adam_consts(hp, bc);
   const int64_t row = t.rows[row_idx];
   const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
   const int w4 = t.width / 4;
@@ -64,8 +72,8 @@ __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, Spa
   for (int c = lane; c < w4; c += 32) {
     const float4 w = ld4(wp + 4 * c);
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = beg; k < end; ++k) {
-      const int32_t code = t.contrib[k];
+    for (int kk = beg; kk < end; ++kk) {
+      const int32_t code = t.contrib[kk];
       if (code < 0) {
         const float4 r = ld4(a.agbuf + static_cast<int64_t>(-code - 1) * t.width + 4 * c);
         g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
@@ -84,7 +92,7 @@ __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, Spa
     }
     if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g);
     float4 m = ld4(mp + 4 * c), v = ld4(vp + 4 * c);
-    const float4 nw = adam4(w, m, v, g, lr, b1, b2, eps, bc1, bc2);
+    const float4 nw = adam4(w, m, v, g, k);
     st4(wp + 4 * c, nw);
     st4(mp + 4 * c, m);
     st4(vp + 4 * c, v);
@@ -92,12 +100,11 @@ __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, Spa
 }
 
 __global__ void __launch_bounds__(kWarps * 32) relation_adam_kernel(DevArgs a, SparseTable t,
-                                                                    float lr, float b1, float b2,
-                                                                    float eps, float bc1,
-                                                                    float bc2) {
+                                                                    AdamHyper hp, const float* bc) {
   const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row_idx >= t.n_rows) return;
+  const AdamK k = adam_consts(hp, bc);
   const int64_t row = t.rows[row_idx];
   const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
   const int w4 = t.width / 4;
@@ -106,25 +113,26 @@ __global__ void __launch_bounds__(kWarps * 32) relation_adam_kernel(DevArgs a, S
   float* vp = t.v + row * t.width;
   for (int c = lane; c < w4; c += 32) {
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = beg; k < end; ++k) {
-      const float4 r = ld4(a.rgbuf + static_cast<int64_t>(t.contrib[k]) * t.width + 4 * c);
+    for (int kk = beg; kk < end; ++kk) {
+      const float4 r = ld4(a.rgbuf + static_cast<int64_t>(t.contrib[kk]) * t.width + 4 * c);
       g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
     }
     if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g);
     float4 w = ld4(wp + 4 * c), m = ld4(mp + 4 * c), v = ld4(vp + 4 * c);
-    w = adam4(w, m, v, g, lr, b1, b2, eps, bc1, bc2);
+    w = adam4(w, m, v, g, k);
     st4(wp + 4 * c, w);
     st4(mp + 4 * c, m);
     st4(vp + 4 * c, v);
   }
 }
 
-__global__ void dense_adam_kernel(float* w, float* m, float* v, const float* g, int64_t n, float lr,
-                                  float b1, float b2, float eps, float bc1, float bc2) {
+__global__ void dense_adam_kernel(float* w, float* m, float* v, const float* g, int64_t n,
+                                  AdamHyper hp, const float* bc) {
+  const AdamK k = adam_consts(hp, bc);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float wi = w[i], mi = m[i], vi = v[i];
-    adam_update(wi, mi, vi, g[i], lr, b1, b2, eps, bc1, bc2);
+    adam_update(wi, mi, vi, g[i], k);
     w[i] = wi;
     m[i] = mi;
     v[i] = vi;
@@ -133,30 +141,30 @@ __global__ void dense_adam_kernel(float* w, float* m, float* v, const float* g, 
 
 }  // namespace
 
-int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, float lr, float b1, float b2,
-                               float eps, float bc1, float bc2, const LaunchCtx& lc) {
+int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
+                              const float* bc, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
   const int blocks = (t.n_rows + kWarps - 1) / kWarps;
   if (a.backbone == NGDB_GQE)
-    entity_adam_kernel<NGDB_GQE><<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, lr, b1, b2, eps, bc1, bc2);
+    entity_adam_kernel<NGDB_GQE><<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, hp, bc);
   else
-    entity_adam_kernel<NGDB_Q2B><<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, lr, b1, b2, eps, bc1, bc2);
+    entity_adam_kernel<NGDB_Q2B><<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, hp, bc);
   return 1;
 }
 
-int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, float lr, float b1,
-                                 float b2, float eps, float bc1, float bc2, const LaunchCtx& lc) {
+int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
+                                const float* bc, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
   const int blocks = (t.n_rows + kWarps - 1) / kWarps;
-  relation_adam_kernel<<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, lr, b1, b2, eps, bc1, bc2);
+  relation_adam_kernel<<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, hp, bc);
   return 1;
 }
 
-int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, float lr, float b1,
-                       float b2, float eps, float bc1, float bc2, const LaunchCtx& lc) {
+int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, const AdamHyper& hp,
+                      const float* bc, const LaunchCtx& lc) {
   if (n <= 0) return 0;
   const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, lc.num_sms * 8));
-  dense_adam_kernel<<<blocks, 256, 0, lc.stream>>>(w, m, v, g, n, lr, b1, b2, eps, bc1, bc2);
+  dense_adam_kernel<<<blocks, 256, 0, lc.stream>>>(w, m, v, g, n, hp, bc);
   return 1;
 }
 

@@ -1,13 +1,19 @@
-// tcgen05 3xTF32 GEMM (see tc_gemm.cuh for the contract).
+// tcgen05 3xTF32 GEMM on pre-split operands (contract in tc_gemm.cuh).
 //
-// Precision: the tensor core's fp32 accumulator aligns partial sums to the
-// running maximum exponent, which over a full K=400 accumulation measured ~5x
-// the error of a sequential fp32 sum. Each BK=32 chunk is therefore accumulated
-// in a FRESH TMEM buffer (12 UMMAs: 4 k-steps x {hi*hi, hi*lo, lo*hi}) and the
-// chunk partials are summed in fp32 registers by the epilogue threads, in chunk
-// order (deterministic). Two TMEM buffers alternate so the tensor core works on
-// chunk c while the threads drain chunk c-1.
+// One launch runs up to four independent problems (a dependency level of an
+// intersect class). The flattened grid enumerates (problem, 128x80 tile,
+// K-split); the S CTAs of a tile form a (S,1,1) thread-block cluster, each
+// streams its K range through a 3-stage cp.async ring into 128B-swizzled
+// K-major tiles, one thread issues the UMMAs, and the leader reduces the
+// peers' fp32 partials over DSMEM in rank order (deterministic). Each K chunk
+// accumulates in a fresh TMEM buffer and is folded into fp32 registers, which
+// keeps the contraction at fp32 accuracy (the tensor core's accumulator loses
+// precision over long runs). The epilogue stages the tile through shared
+// memory so global reads/writes of C are row-coalesced.
 #include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 #include "tc_gemm.cuh"
@@ -16,19 +22,24 @@ namespace ngdb_dev {
 namespace {
 
 constexpr int BM = 128, BN = 80, BK = 32;
-constexpr int kThreads = 256;   // 8 warps: all split; warps w and w+4 share TMEM lanes
-constexpr int kRawStages = 4;   // cp.async ring depth (chunks in flight)
-constexpr int kOpStages = 2;    // hi/lo operand stages consumed by the tensor core
+constexpr int kThreads = 256;   // 8 warps; warps w and w+4 share TMEM lane quarter w%4
+constexpr int kStages = 3;      // smem operand ring (chunks in flight)
 constexpr int kTmemCols = 256;  // 2 accumulator buffers of BN columns (power of two)
 constexpr int kHalfCols = BN / 2;
+constexpr int kMaxProblems = 4;
 
-constexpr int A_TILE = BM * BK * 4;  // 16 KB per operand tile (128 rows x 128 B)
+constexpr int A_TILE = BM * BK * 4;  // 16 KB (128 rows x 128 B)
 constexpr int B_TILE = BN * BK * 4;  // 10 KB
-constexpr int OP_STAGE = 2 * A_TILE + 2 * B_TILE;  // A_hi, A_lo, B_hi, B_lo
-constexpr int RAW_STAGE = A_TILE + B_TILE;
-constexpr int SMEM_OPS = kOpStages * OP_STAGE;
-constexpr int SMEM_RAW = kRawStages * RAW_STAGE;
-constexpr int SMEM_BYTES = SMEM_OPS + SMEM_RAW + 64;
+constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;  // A_hi, A_lo, B_hi, B_lo
+constexpr int SMEM_BYTES = kStages * STAGE + 64;
+constexpr int kTileStride = BN + 1;  // epilogue staging tile [BM][BN+1] (bank-conflict free)
+
+struct TcGemmBatch {
+  TcGemmArgs p[kMaxProblems];
+  int tile_begin[kMaxProblems + 1];
+  int n;
+  int S;  // K-split factor == cluster size
+};
 
 // UMMA instruction descriptor: D=f32, A=B=tf32, both K-major, M=128, N=80.
 constexpr uint32_t kInstrDesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -45,30 +56,14 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
          (static_cast<uint64_t>(2) << 61);
 }
 
-// byte offset of element (row r, k) inside a swizzled K-major tile
-__device__ __forceinline__ uint32_t swz(int r, int k) {
-  return static_cast<uint32_t>(r * 128 + ((((k >> 2) ^ (r & 7))) << 4) + ((k & 3) << 2));
+// byte offset of the 16-byte chunk (row r, k4 = k/4) in a swizzled K-major tile
+__device__ __forceinline__ uint32_t swz16(int r, int k4) {
+  return static_cast<uint32_t>(r * 128 + ((k4 ^ (r & 7)) << 4));
 }
 
-// hi = x rounded to the 10-bit TF32 mantissa (half away from zero), lo = x - hi
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);  // round to 10-bit mantissa
   lo = x - hi;
-}
-
-__device__ __forceinline__ void st_shared4(uint32_t addr, float4 v) {
-  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w));
-}
-__device__ __forceinline__ void st_shared1(uint32_t addr, float v) {
-  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v));
-}
-__device__ __forceinline__ float4 ld_shared4(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr));
-  return v;
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -100,86 +95,50 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t 
       "l"(a), "l"(b), "r"(kInstrDesc), "r"(acc));
 }
 
-__device__ __forceinline__ float4 relu4(float4 v) {
-  return make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+// Per-thread copy slots: every chunk this thread copies the same (row, k4)
+// 16-byte pieces — 4 rows of A and up to 3 rows of B, each for hi and lo.
+struct CopyPlan {
+  int64_t a_off[4], b_off[3];  // element offsets of (row, 4*k4) in the hi/lo arrays
+  uint32_t a_dst[4], b_dst[3];
+  bool a_ok[4], b_ok[3];
+  int kk;                      // 4*k4
+};
+
+__device__ __forceinline__ void make_copy_plan(const TcGemmArgs& g, int m0, int n0, CopyPlan& cp) {
+  const int k4 = threadIdx.x & 7, r0 = threadIdx.x >> 3;
+  cp.kk = 4 * k4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + 32 * i;
+    cp.a_ok[i] = (m0 + r) < g.M;
+    cp.a_off[i] = (int64_t)(m0 + r) * g.A.ld + cp.kk;
+    cp.a_dst[i] = swz16(r, k4);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int r = r0 + 32 * i;
+    cp.b_ok[i] = r < BN && (n0 + r) < g.N;
+    cp.b_off[i] = (int64_t)(n0 + r) * g.B.ld + cp.kk;
+    cp.b_dst[i] = swz16(r < BN ? r : 0, k4);
+  }
 }
 
-// Stage K-chunk `kc` of A and B into raw ring slot (cp.async, 16 B each).
-template <int AMAJ, int BMAJ>
-__device__ __forceinline__ void load_chunk(const TcGemmArgs& g, int m0, int n0, int kc,
-                                           uint32_t raw_a, uint32_t raw_b) {
+__device__ __forceinline__ void load_chunk(const TcGemmArgs& g, const CopyPlan& cp, int kc,
+                                           uint32_t st) {
   const int k0 = kc * BK;
+  const bool kok = (k0 + cp.kk) < g.K;
 #pragma unroll
-  for (int i = 0; i < (BM * BK / 4) / kThreads; ++i) {  // 1024 chunks of 16 B
-    const int c = threadIdx.x + i * kThreads;
-    if (AMAJ == MAJ_K) {  // raw[m][32]
-      const int m = c >> 3, kk = (c & 7) * 4;
-      const bool ok = (m0 + m) < g.M && (k0 + kk) < g.K;
-      const float* src = ok ? g.A + (int64_t)(m0 + m) * g.lda + k0 + kk : g.A;
-      cp_async16(raw_a + c * 16, src, ok);
-    } else {  // raw[k][128]
-      const int kk = c >> 5, m = (c & 31) * 4;
-      const bool ok = (k0 + kk) < g.K && (m0 + m) < g.M;
-      const float* src = ok ? g.A + (int64_t)(k0 + kk) * g.lda + m0 + m : g.A;
-      cp_async16(raw_a + c * 16, src, ok);
-    }
+  for (int i = 0; i < 4; ++i) {
+    const bool ok = cp.a_ok[i] && kok;
+    cp_async16(st + cp.a_dst[i], ok ? g.A.hi + cp.a_off[i] + k0 : g.A.hi, ok);
+    cp_async16(st + A_TILE + cp.a_dst[i], ok ? g.A.lo + cp.a_off[i] + k0 : g.A.lo, ok);
   }
-  for (int c = threadIdx.x; c < BN * BK / 4; c += kThreads) {  // 640 chunks
-    if (BMAJ == MAJ_K) {  // raw[n][32]
-      const int n = c >> 3, kk = (c & 7) * 4;
-      const bool ok = (n0 + n) < g.N && (k0 + kk) < g.K;
-      const float* src = ok ? g.B + (int64_t)(n0 + n) * g.ldb + k0 + kk : g.B;
-      cp_async16(raw_b + c * 16, src, ok);
-    } else {  // raw[k][80]
-      const int kk = c / 20, n = (c % 20) * 4;
-      const bool ok = (k0 + kk) < g.K && (n0 + n) < g.N;
-      const float* src = ok ? g.B + (int64_t)(k0 + kk) * g.ldb + n0 + n : g.B;
-      cp_async16(raw_b + c * 16, src, ok);
-    }
-  }
-}
-
-// raw ring slot -> hi/lo swizzled operand tiles (shared-space addresses)
-template <int AMAJ, int BMAJ, int OPS>
-__device__ __forceinline__ void split_chunk(uint32_t raw_a, uint32_t raw_b, uint32_t a_hi,
-                                            uint32_t a_lo, uint32_t b_hi, uint32_t b_lo) {
 #pragma unroll
-  for (int i = 0; i < (BM * BK / 4) / kThreads; ++i) {
-    const int c = threadIdx.x + i * kThreads;
-    float4 v = ld_shared4(raw_a + c * 16);
-    if (OPS & AOP_RELU) v = relu4(v);
-    float4 h, l;
-    split_tf32(v.x, h.x, l.x); split_tf32(v.y, h.y, l.y);
-    split_tf32(v.z, h.z, l.z); split_tf32(v.w, h.w, l.w);
-    if (AMAJ == MAJ_K) {
-      const uint32_t o = swz(c >> 3, (c & 7) * 4);
-      st_shared4(a_hi + o, h);
-      st_shared4(a_lo + o, l);
-    } else {
-      const int kk = c >> 5, m = (c & 31) * 4;
-      st_shared1(a_hi + swz(m, kk), h.x); st_shared1(a_lo + swz(m, kk), l.x);
-      st_shared1(a_hi + swz(m + 1, kk), h.y); st_shared1(a_lo + swz(m + 1, kk), l.y);
-      st_shared1(a_hi + swz(m + 2, kk), h.z); st_shared1(a_lo + swz(m + 2, kk), l.z);
-      st_shared1(a_hi + swz(m + 3, kk), h.w); st_shared1(a_lo + swz(m + 3, kk), l.w);
-    }
-  }
-  for (int c = threadIdx.x; c < BN * BK / 4; c += kThreads) {
-    float4 v = ld_shared4(raw_b + c * 16);
-    if (OPS & BOP_RELU) v = relu4(v);
-    float4 h, l;
-    split_tf32(v.x, h.x, l.x); split_tf32(v.y, h.y, l.y);
-    split_tf32(v.z, h.z, l.z); split_tf32(v.w, h.w, l.w);
-    if (BMAJ == MAJ_K) {
-      const uint32_t o = swz(c >> 3, (c & 7) * 4);
-      st_shared4(b_hi + o, h);
-      st_shared4(b_lo + o, l);
-    } else {
-      const int kk = c / 20, n = (c % 20) * 4;
-      st_shared1(b_hi + swz(n, kk), h.x); st_shared1(b_lo + swz(n, kk), l.x);
-      st_shared1(b_hi + swz(n + 1, kk), h.y); st_shared1(b_lo + swz(n + 1, kk), l.y);
-      st_shared1(b_hi + swz(n + 2, kk), h.z); st_shared1(b_lo + swz(n + 2, kk), l.z);
-      st_shared1(b_hi + swz(n + 3, kk), h.w); st_shared1(b_lo + swz(n + 3, kk), l.w);
-    }
+  for (int i = 0; i < 3; ++i) {
+    if (threadIdx.x + 256 * i >= BN * 8) break;  // rows beyond the 80-row tile
+    const bool ok = cp.b_ok[i] && kok;
+    cp_async16(st + 2 * A_TILE + cp.b_dst[i], ok ? g.B.hi + cp.b_off[i] + k0 : g.B.hi, ok);
+    cp_async16(st + 2 * A_TILE + B_TILE + cp.b_dst[i], ok ? g.B.lo + cp.b_off[i] + k0 : g.B.lo, ok);
   }
 }
 
@@ -188,33 +147,40 @@ __device__ __forceinline__ void drain(uint32_t tmem, int buf, float* acc) {
   const int warp = threadIdx.x / 32;
   const uint32_t base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + buf * BN +
                         (warp >> 2) * kHalfCols;
+  uint32_t r[kHalfCols];
 #pragma unroll
-  for (int j = 0; j < kHalfCols; j += 8) {
-    uint32_t r[8];
+  for (int j = 0; j < kHalfCols; j += 8)
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                   "=r"(r[6]), "=r"(r[7])
+                 : "=r"(r[j]), "=r"(r[j + 1]), "=r"(r[j + 2]), "=r"(r[j + 3]), "=r"(r[j + 4]),
+                   "=r"(r[j + 5]), "=r"(r[j + 6]), "=r"(r[j + 7])
                  : "r"(base + j));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
 #pragma unroll
-    for (int t = 0; t < 8; ++t) acc[j + t] += __uint_as_float(r[t]);
-  }
+  for (int j = 0; j < kHalfCols; ++j) acc[j] += __uint_as_float(r[j]);
 }
 
-template <int AMAJ, int BMAJ, int OPS>
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
+__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmBatch batch) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  const uint32_t s_ops = smem_u32(smem);
-  const uint32_t s_raw = s_ops + SMEM_OPS;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_OPS + SMEM_RAW);  // [kOpStages]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kOpStages);
+  const uint32_t s_base = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * STAGE);  // [kStages]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kStages);
 
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  // flattened grid -> (problem, tile, K-split rank)
+  const int S = batch.S;
+  const int tile = blockIdx.x / S, rank = blockIdx.x % S;
+  int pi = 0;
+  while (pi + 1 < batch.n && tile >= batch.tile_begin[pi + 1]) ++pi;
+  const TcGemmArgs& g = batch.p[pi];
+  const int lt = tile - batch.tile_begin[pi];
+  const int n_tiles_n = (g.N + BN - 1) / BN;
+  const int m0 = (lt / n_tiles_n) * BM, n0 = (lt % n_tiles_n) * BN;
   const int warp = threadIdx.x / 32;
-  const int n_chunks = (g.K + BK - 1) / BK;
+  const int total_chunks = (g.K + BK - 1) / BK;
+  const int c_beg = rank * total_chunks / S;
+  const int n_chunks = (rank + 1) * total_chunks / S - c_beg;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kOpStages; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(smem_u32(&bars[s]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
@@ -223,6 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
                  "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  CopyPlan cp;
+  make_copy_plan(g, m0, n0, cp);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -232,74 +200,106 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
 #pragma unroll
   for (int j = 0; j < kHalfCols; ++j) acc[j] = 0.f;
 
-  for (int c = 0; c < kRawStages - 1; ++c) {
-    if (c < n_chunks)
-      load_chunk<AMAJ, BMAJ>(g, m0, n0, c, s_raw + c * RAW_STAGE, s_raw + c * RAW_STAGE + A_TILE);
+  for (int c = 0; c < kStages - 1; ++c) {
+    if (c < n_chunks) load_chunk(g, cp, c_beg + c, s_base + c * STAGE);
     asm volatile("cp.async.commit_group;");
   }
-  uint32_t phase[kOpStages] = {0, 0};
   for (int c = 0; c < n_chunks; ++c) {
-    const int slot = c % kRawStages, st = c % kOpStages;
-    asm volatile("cp.async.wait_group %0;" ::"n"(kRawStages - 2));
-    // operand stage / TMEM buffer st were last used by chunk c-2: wait for its
-    // MMAs, then fold that chunk's partial into the fp32 register accumulator
-    if (c >= kOpStages) {
-      mbar_wait(smem_u32(&bars[st]), phase[st]);
-      phase[st] ^= 1;
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      drain(tmem, st, acc);
-      asm volatile("tcgen05.fence::before_thread_sync;");
-    }
-    __syncthreads();  // raw chunk c visible to all; TMEM buffer st drained
-    const uint32_t op = s_ops + st * OP_STAGE;
-    split_chunk<AMAJ, BMAJ, OPS>(s_raw + slot * RAW_STAGE, s_raw + slot * RAW_STAGE + A_TILE, op,
-                                 op + A_TILE, op + 2 * A_TILE, op + 2 * A_TILE + B_TILE);
-    const int nc = c + kRawStages - 1;  // refill the slot consumed at iteration c-1
-    if (nc < n_chunks) {
-      const int ns = nc % kRawStages;
-      load_chunk<AMAJ, BMAJ>(g, m0, n0, nc, s_raw + ns * RAW_STAGE,
-                             s_raw + ns * RAW_STAGE + A_TILE);
-    }
-    asm volatile("cp.async.commit_group;");
-    asm volatile("fence.proxy.async.shared::cta;");  // generic smem writes -> tensor-core proxy
+    const int st = c % kStages;
+    asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2));  // chunk c has landed
+    asm volatile("fence.proxy.async.shared::cta;");             // cp.async -> tensor-core proxy
     __syncthreads();
     if (threadIdx.x == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t a_hi = op, a_lo = op + A_TILE;
-      const uint32_t b_hi = op + 2 * A_TILE, b_lo = b_hi + B_TILE;
-      const uint32_t d = tmem + st * BN;
+      const uint32_t a_hi = s_base + st * STAGE, a_lo = a_hi + A_TILE;
+      const uint32_t b_hi = a_hi + 2 * A_TILE, b_lo = b_hi + B_TILE;
+      const uint32_t d = tmem + (c & 1) * BN;
 #pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {  // UMMA K = 8 tf32 = 32 bytes
+      for (int ks = 0; ks < BK / 8; ++ks) {  // UMMA K = 8 tf32 = 32 bytes; small terms first
         const uint32_t off = ks * 32;
-        umma_tf32(d, umma_desc(a_hi + off), umma_desc(b_hi + off), ks == 0 ? 0u : 1u);
+        umma_tf32(d, umma_desc(a_lo + off), umma_desc(b_hi + off), ks == 0 ? 0u : 1u);
         umma_tf32(d, umma_desc(a_hi + off), umma_desc(b_lo + off), 1u);
-        umma_tf32(d, umma_desc(a_lo + off), umma_desc(b_hi + off), 1u);
+        umma_tf32(d, umma_desc(a_hi + off), umma_desc(b_hi + off), 1u);
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(&bars[st])));
     }
+    // fold chunk c-1 (its MMAs ran while chunk c was landing): frees its ring
+    // stage and TMEM buffer
+    if (c >= 1) {
+      const int pc = c - 1;
+      mbar_wait(smem_u32(&bars[pc % kStages]), (pc / kStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      drain(tmem, pc & 1, acc);
+      asm volatile("tcgen05.fence::before_thread_sync;");
+    }
+    const int nc = c + kStages - 1;
+    if (nc < n_chunks) load_chunk(g, cp, c_beg + nc, s_base + (nc % kStages) * STAGE);
+    asm volatile("cp.async.commit_group;");
   }
-  // drain the last (up to two) chunks in chunk order
-  for (int c = (n_chunks >= kOpStages ? n_chunks - kOpStages : 0); c < n_chunks; ++c) {
-    const int st = c % kOpStages;
-    mbar_wait(smem_u32(&bars[st]), phase[st]);
-    phase[st] ^= 1;
+  if (n_chunks > 0) {
+    const int pc = n_chunks - 1;
+    mbar_wait(smem_u32(&bars[pc % kStages]), (pc / kStages) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    drain(tmem, st, acc);
+    drain(tmem, pc & 1, acc);
+  }
+  asm volatile("cp.async.wait_group 0;");
+
+  if (S > 1) {
+    // deterministic split-K reduction through distributed shared memory
+    float* park = reinterpret_cast<float*>(smem);
+    if (rank > 0)
+#pragma unroll
+      for (int j = 0; j < kHalfCols; ++j) park[j * kThreads + threadIdx.x] = acc[j];
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+    if (rank == 0) {
+      for (int p = 1; p < S; ++p) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                     : "=r"(remote)
+                     : "r"(smem_u32(park + threadIdx.x)), "r"(p));
+#pragma unroll
+        for (int j = 0; j < kHalfCols; ++j) {
+          float v;
+          asm volatile("ld.shared::cluster.f32 %0, [%1];"
+                       : "=f"(v)
+                       : "r"(remote + static_cast<uint32_t>(j * kThreads * 4)));
+          acc[j] += v;
+        }
+      }
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   }
 
-  // epilogue: warp w owns rows 32*(w%4).. and column half (w/4)
-  const int row = m0 + (warp & 3) * 32 + (threadIdx.x & 31);
-  if (row < g.M) {
-    float* crow = g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
-    const int cb = n0 + (warp >> 2) * kHalfCols;
+  if (rank == 0) {
+    // stage the tile row-major in shared memory, then write rows coalesced
+    float* tile_s = reinterpret_cast<float*>(smem);
+    {
+      const int r = (warp & 3) * 32 + (threadIdx.x & 31), cb = (warp >> 2) * kHalfCols;
 #pragma unroll
-    for (int j = 0; j < kHalfCols; ++j) {
-      const int n = cb + j;
-      if (n < g.N) {
-        float v = acc[j];
+      for (int j = 0; j < kHalfCols; ++j) tile_s[r * kTileStride + cb + j] = acc[j];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    for (int r = warp; r < BM; r += kThreads / 32) {
+      const int row = m0 + r;
+      if (row >= g.M) break;
+      float* crow =
+          g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
+      for (int cc = lane; cc < BN; cc += 32) {
+        const int n = n0 + cc;
+        if (n >= g.N) break;
+        float v = tile_s[r * kTileStride + cc];
         if (g.bias) v += g.bias[n];
-        crow[n] = g.accumulate ? crow[n] + v : v;
+        if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;
+        if (g.accumulate) v += crow[n];
+        crow[n] = v;
+        if (g.s_hi) {
+          float h, l;
+          split_tf32(g.s_relu ? fmaxf(v, 0.f) : v, h, l);
+          g.s_hi[(int64_t)row * g.ldc + n] = h;
+          g.s_lo[(int64_t)row * g.ldc + n] = l;
+        }
       }
     }
   }
@@ -310,64 +310,182 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(TcGemmArgs g) {
                  "n"(kTmemCols));
 }
 
-template <int AMAJ, int BMAJ, int OPS>
-void launch(const TcGemmArgs& g, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(tc_gemm_kernel<AMAJ, BMAJ, OPS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    configured = true;
+// --- operand split / transpose ------------------------------------------------
+__global__ void split_kernel(const float* src, int rows, int cols, int ld, int relu, float* hi,
+                             float* lo) {
+  const int64_t n = (int64_t)rows * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cols), c = (int)(i % cols);
+    float v = src[(int64_t)r * ld + c];
+    if (relu) v = fmaxf(v, 0.f);
+    float h, l;
+    split_tf32(v, h, l);
+    hi[i] = h;
+    lo[i] = l;
   }
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM);
-  tc_gemm_kernel<AMAJ, BMAJ, OPS><<<grid, kThreads, SMEM_BYTES, s>>>(g);
+}
+
+// dst[c][r] (row stride pad4(rows), zero padded) = split(op(src[r][c]))
+__global__ void split_t_multi_kernel(SplitJobs jobs) {
+  __shared__ float tile[32][33];
+  const SplitJob& j = jobs.job[blockIdx.z];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  if (r0 >= j.rows || c0 >= j.cols) return;  // grid sized for the largest job
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int r = r0 + y, c = c0 + threadIdx.x;
+    float v = (r < j.rows && c < j.cols) ? j.src[(int64_t)r * j.ld + c] : 0.f;
+    tile[y][threadIdx.x] = j.relu ? fmaxf(v, 0.f) : v;
+  }
+  __syncthreads();
+  const int ldp = (j.rows + 3) & ~3;  // 16-byte aligned rows for cp.async; zero padded
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int c = c0 + y, r = r0 + threadIdx.x;
+    if (c < j.cols && r < ldp) {
+      float h = 0.f, l = 0.f;
+      if (r < j.rows) split_tf32(tile[threadIdx.x][y], h, l);
+      j.hi[(int64_t)c * ldp + r] = h;
+      j.lo[(int64_t)c * ldp + r] = l;
+    }
+  }
 }
 
 }  // namespace
 
-int tc_gemm(const TcGemmArgs& g, int a_major, int b_major, int ops, cudaStream_t s) {
-  if (g.M <= 0 || g.N <= 0) return 0;
-#define NGDB_TC(AM, BMJ, OP)                                      \
-  if (a_major == AM && b_major == BMJ && ops == OP) {            \
-    launch<AM, BMJ, OP>(g, s);                                    \
-    return 1;                                                     \
+// Opt the kernel into > 48 KB dynamic shared memory (once per process, before
+// any launch or stream capture).
+void tc_gemm_init() {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    configured = true;
   }
-  NGDB_TC(MAJ_K, MAJ_K, AOP_NONE)       // y = x W^T
-  NGDB_TC(MAJ_K, MAJ_K, AOP_RELU)       // y = relu(x) W^T
-  NGDB_TC(MAJ_K, MAJ_MN, AOP_NONE)      // dx = dy W
-  NGDB_TC(MAJ_MN, MAJ_MN, AOP_NONE)     // dW += dy^T x
-  NGDB_TC(MAJ_MN, MAJ_MN, BOP_RELU)     // dW += dy^T relu(x)
-#undef NGDB_TC
-  return 0;
+}
+
+int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
+  tc_gemm_init();
+  TcGemmBatch b{};
+  int max_chunks = 0, tiles = 0;
+  b.n = 0;
+  for (int i = 0; i < n && b.n < kMaxProblems; ++i) {
+    const TcGemmArgs& g = probs[i];
+    if (g.M <= 0 || g.N <= 0) continue;
+    b.p[b.n] = g;
+    b.tile_begin[b.n] = tiles;
+    tiles += ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+    max_chunks = std::max(max_chunks, (g.K + BK - 1) / BK);
+    ++b.n;
+  }
+  if (b.n == 0) return 0;
+  b.tile_begin[b.n] = tiles;
+  // split-K: ~3 K-chunks per CTA, at most 8 CTAs per cluster (portable size)
+  b.S = std::max(1, std::min(8, max_chunks / 3));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(tiles * b.S);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = b.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, tc_gemm_kernel, b);
+  return 1;
+}
+
+int tc_gemm(const TcGemmArgs& g, cudaStream_t s) { return tc_gemm_batch(&g, 1, s); }
+
+int split_transposed(const SplitJobs& jobs, cudaStream_t s) {
+  if (jobs.n <= 0) return 0;
+  int mr = 0, mc = 0;
+  for (int i = 0; i < jobs.n; ++i) {
+    mr = std::max(mr, jobs.job[i].rows);
+    mc = std::max(mc, jobs.job[i].cols);
+  }
+  if (mr <= 0 || mc <= 0) return 0;
+  dim3 grid((mc + 31) / 32, (mr + 31) / 32, jobs.n);
+  split_t_multi_kernel<<<grid, dim3(32, 8), 0, s>>>(jobs);
+  return 1;
+}
+
+int split_matrix(const float* src, int rows, int cols, int ld_src, int transpose, int relu,
+                 float* dst_hi, float* dst_lo, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return 0;
+  if (!transpose) {
+    const int64_t n = (int64_t)rows * cols;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    split_kernel<<<blocks, 256, 0, s>>>(src, rows, cols, ld_src, relu, dst_hi, dst_lo);
+    return 1;
+  }
+  SplitJobs jobs{};
+  jobs.job[0] = {src, rows, cols, ld_src, relu, dst_hi, dst_lo};
+  jobs.n = 1;
+  return split_transposed(jobs, s);
+}
+
+int split_weight(const float* w, int rows, int cols, float* dst, cudaStream_t s) {
+  const int64_t n = (int64_t)rows * cols;
+  split_matrix(w, rows, cols, cols, 0, 0, dst, dst + n, s);
+  split_matrix(w, rows, cols, cols, 1, 0, dst + 2 * n, dst + 3 * n, s);
+  return 2;
 }
 
 }  // namespace ngdb_dev
 
-// Debug entry point for the GEMM unit test (host pointers, synchronous).
+// Debug entry point for the GEMM unit test (host pointers, synchronous):
+// C = op_a(A) op_b(B)^T with A [M][K] (a_major 0) or [K][M] (1), B [N][K] (0)
+// or [K][N] (1); ops bit0 = relu(A), bit1 = relu(B).
 extern "C" int ngdb_debug_tc_gemm(int M, int N, int K, int a_major, int b_major, int ops,
                                   const float* A, int lda, const float* B, int ldb, float* C,
                                   int ldc, const float* bias, int accumulate) {
   using namespace ngdb_dev;
-  const int64_t na = (a_major == MAJ_K) ? (int64_t)M * lda : (int64_t)K * lda;
-  const int64_t nb = (b_major == MAJ_K) ? (int64_t)N * ldb : (int64_t)K * ldb;
   const int64_t nc = (int64_t)M * ldc;
-  float *dA, *dB, *dC, *dbias = nullptr;
-  if (cudaMalloc(&dA, na * 4) || cudaMalloc(&dB, nb * 4) || cudaMalloc(&dC, nc * 4)) return 8;
-  cudaMemcpy(dA, A, na * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(dB, B, nb * 4, cudaMemcpyHostToDevice);
+  // Route every operand through the transposed split (which pads rows to a
+  // multiple of 4 floats): K-major inputs are transposed on the host first.
+  std::vector<float> At, Bt;
+  if (a_major == 0) {
+    At.resize((size_t)K * M);
+    for (int m = 0; m < M; ++m)
+      for (int k = 0; k < K; ++k) At[(size_t)k * M + m] = A[(size_t)m * lda + k];
+    A = At.data();
+    lda = M;
+  }
+  if (b_major == 0) {
+    Bt.resize((size_t)K * N);
+    for (int n = 0; n < N; ++n)
+      for (int k = 0; k < K; ++k) Bt[(size_t)k * N + n] = B[(size_t)n * ldb + k];
+    B = Bt.data();
+    ldb = N;
+  }
+  const int64_t na2 = (int64_t)K * lda, nb2 = (int64_t)K * ldb;
+  const int KP = (K + 3) & ~3;
+  float *dA, *dB, *dC, *dbias = nullptr, *sp;
+  if (cudaMalloc(&dA, na2 * 4) || cudaMalloc(&dB, nb2 * 4) || cudaMalloc(&dC, nc * 4)) return 8;
+  if (cudaMalloc(&sp, ((int64_t)M * KP + (int64_t)N * KP) * 2 * 4)) return 8;
+  cudaMemcpy(dA, A, na2 * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B, nb2 * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dC, C, nc * 4, cudaMemcpyHostToDevice);
   if (bias) {
     cudaMalloc(&dbias, N * 4);
     cudaMemcpy(dbias, bias, N * 4, cudaMemcpyHostToDevice);
   }
+  float *ahi = sp, *alo = ahi + (int64_t)M * KP, *bhi = alo + (int64_t)M * KP,
+        *blo = bhi + (int64_t)N * KP;
+  split_matrix(dA, K, M, lda, 1, ops & 1, ahi, alo, 0);
+  split_matrix(dB, K, N, ldb, 1, (ops >> 1) & 1, bhi, blo, 0);
   TcGemmArgs g{};
   g.M = M; g.N = N; g.K = K;
-  g.A = dA; g.lda = lda; g.B = dB; g.ldb = ldb; g.C = dC; g.ldc = ldc;
+  g.A = {ahi, alo, KP};
+  g.B = {bhi, blo, KP};
+  g.C = dC; g.ldc = ldc;
   g.bias = dbias; g.accumulate = accumulate;
-  const int n = tc_gemm(g, a_major, b_major, ops, 0);
+  tc_gemm(g, 0);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(C, dC, nc * 4, cudaMemcpyDeviceToHost);
-  cudaFree(dA); cudaFree(dB); cudaFree(dC);
+  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(sp);
   if (dbias) cudaFree(dbias);
-  if (n == 0) return 5;
   return e == cudaSuccess ? 0 : 8;
 }

@@ -2,19 +2,21 @@
 //
 //   C[M,N] (+)= A[M,K] * B[N,K]^T (+ bias[n])      fp32 in, fp32 out
 //
-// Each fp32 operand x is split into hi = tf32_rn(x) and lo = x - hi; the tensor
-// core accumulates hi*hi + hi*lo + lo*hi in fp32 TMEM accumulators, which keeps
-// the contraction within ~1e-6 relative of fp32 — the 1e-4 parity bar cannot be
-// met by single-pass TF32 at K = 400..1536.
+// Operands arrive PRE-SPLIT: x = hi + lo with hi = tf32_rn(x), lo = x - hi, both
+// stored row-major K-contiguous ("K-major"). Weights are split once per
+// optimizer step (refresh_weight_splits); activations are split by
+// split_matrix (optionally transposed / ReLU'd) or directly by the epilogue of
+// the GEMM that produced them. The tensor core accumulates hi*hi + hi*lo + lo*hi
+// per BK=32 chunk in a fresh TMEM buffer; chunk partials are summed in fp32
+// registers (the accumulator's exponent alignment loses ~5x fp32 precision over
+// a full K=400 run; per chunk it does not matter).
 //
-// Tile: BM = 128 rows (UMMA M=128, cta_group::1), BN = 80 columns (one UMMA
-// N=80; d = 400 is exactly 5 tiles), BK = 32 (one 128-byte swizzle atom of fp32).
-// 128 threads: all of them stream A/B K-chunks global -> shared with cp.async
-// into a 4-deep raw ring, split them into hi/lo operand tiles laid out K-major
-// with the 128B swizzle, and one elected thread issues 4 k-steps x 3 UMMAs per
-// chunk; tcgen05.commit on an mbarrier releases the operand stage. The epilogue
-// reads the accumulator with tcgen05.ld (thread t owns row t) and applies bias /
-// accumulate / row scatter.
+// Tile: BM = 128 rows (UMMA M=128, cta_group::1), BN = 80 (one UMMA N=80; d=400
+// is exactly five tiles), BK = 32 (one 128-byte swizzle atom of fp32). 256
+// threads stream hi/lo tiles global -> shared with cp.async straight into the
+// 128B-swizzled K-major layout the UMMA descriptors describe (3-stage ring);
+// one thread issues 4 k-steps x 3 UMMAs per chunk and commits to the stage's
+// mbarrier; two TMEM accumulator buffers alternate between chunks.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -22,21 +24,48 @@
 
 namespace ngdb_dev {
 
-enum : int { MAJ_K = 0, MAJ_MN = 1 };  // operand storage: K contiguous or M/N contiguous
-enum : int { AOP_NONE = 0, AOP_RELU = 1, BOP_RELU = 2 };  // operand-op bit mask
+struct SplitOperand {
+  const float* hi;
+  const float* lo;
+  int ld;  // row stride (elements); rows are K-contiguous
+};
 
 struct TcGemmArgs {
   int M, N, K;
-  const float* A; int lda;   // MAJ_K: A(m,k) = A[m*lda+k]; MAJ_MN: A[k*lda+m]
-  const float* B; int ldb;   // MAJ_K: B(n,k) = B[n*ldb+k]; MAJ_MN: B[k*ldb+n]
+  SplitOperand A;  // [M][K]
+  SplitOperand B;  // [N][K]
   float* C; int ldc;
   const int32_t* c_rowoff; int c_stride;  // optional row scatter: C + c_rowoff[m*stride]
   const float* bias;
   int accumulate;
+  // optional ReLU-derivative mask: result *= (mask[m*ldc + n] > 0)
+  const float* mask;
+  // optional chained output: split(relu?(C)) -> s_hi/s_lo [M][ldc] (no scatter)
+  float* s_hi; float* s_lo; int s_relu;
 };
 
-// Launch C = A * B^T with the given operand majorness and operand ops (ReLU on
-// A and/or B applied while splitting); returns the kernel count (1).
-int tc_gemm(const TcGemmArgs& g, int a_major, int b_major, int ops, cudaStream_t s);
+int tc_gemm(const TcGemmArgs& g, cudaStream_t s);
+// Up to four independent problems in one launch (one dependency level).
+int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s);
+
+// dst_hi/dst_lo[r][c] = split(op(src[r][c])) (transpose=0, dense [rows][cols]) or
+// dst[c][r] = split(op(src[r][c])) (transpose=1, [cols][pad4(rows)], zero padded
+// so every row is 16-byte aligned for cp.async); op = relu if relu != 0.
+int split_matrix(const float* src, int rows, int cols, int ld_src, int transpose, int relu,
+                 float* dst_hi, float* dst_lo, cudaStream_t s);
+
+// Up to four transposed splits in ONE launch (the weight-gradient operands of
+// a backward class: dY^T and X^T for each dW += dY^T X).
+struct SplitJob {
+  const float* src;
+  int rows, cols, ld, relu;
+  float* hi;
+  float* lo;
+};
+struct SplitJobs {
+  SplitJob job[4];
+  int n;
+};
+int split_transposed(const SplitJobs& jobs, cudaStream_t s);
 
 }  // namespace ngdb_dev
