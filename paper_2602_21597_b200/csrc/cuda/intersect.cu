@@ -77,16 +77,26 @@ struct ColsumJobs {
   ColsumJob job[4];
   int n;
 };
-__global__ void colsum_kernel(ColsumJobs jobs) {
+// 32 columns per block; warp w sums rows w, w+8, ...; the 8 warp partials are
+// combined in warp order (deterministic).
+__global__ void __launch_bounds__(256) colsum_kernel(ColsumJobs jobs) {
+  __shared__ float part[8][32];
   const ColsumJob& j = jobs.job[blockIdx.y];
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= j.n) return;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int r = 0; r < j.rows; ++r) s += j.dy[(int64_t)r * j.n + c];
-  j.db[c] += s;
+  if (c < j.n)
+    for (int r = warp; r < j.rows; r += 8) s += j.dy[(int64_t)r * j.n + c];
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && c < j.n) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    j.db[c] += t;
+  }
 }
 int colsums(const ColsumJobs& jobs, int n, cudaStream_t s) {
-  colsum_kernel<<<dim3((n + 127) / 128, jobs.n), 128, 0, s>>>(jobs);
+  colsum_kernel<<<dim3((n + 31) / 32, jobs.n), 256, 0, s>>>(jobs);
   return 1;
 }
 

@@ -48,14 +48,19 @@ __device__ __forceinline__ float4 adam4(float4 w, float4& m, float4& v, float4 g
   return w;
 }
 
+// coef * d dist / dv, branch-free: copysign of the magnitude, 0 at delta == 0
 template <int BB>
 __device__ __forceinline__ float cand_grad(float v, float qc, float qo, float coef, float alpha) {
   const float delta = v - qc;
-  if (BB == NGDB_GQE) return coef * sgnf(delta);
-  const float scale = fabsf(delta) > qo ? 1.f : alpha;
-  return coef * scale * sgnf(delta);
+  float mag = coef;
+  if (BB == NGDB_Q2B) mag = fabsf(delta) > qo ? coef : coef * alpha;
+  const float s = __int_as_float((__float_as_int(mag) ^ (__float_as_int(delta) & 0x80000000)));
+  return delta != 0.f ? s : 0.f;
 }
 
+// One warp per touched row; lane walks float4 chunks c = lane, lane+32, ...
+// (measured faster than keeping a whole row's theta/m/v in flight per lane:
+// the low register count keeps ~48 warps per SM resident).
 template <int BB>
 __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, SparseTable t,
                                                                   AdamHyper hp, const float* bc) {
@@ -73,13 +78,13 @@ __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, Spa
     const float4 w = ld4(wp + 4 * c);
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int kk = beg; kk < end; ++kk) {
-      const int32_t code = t.contrib[kk];
+      const int32_t code = __ldg(t.contrib + kk);
       if (code < 0) {
         const float4 r = ld4(a.agbuf + static_cast<int64_t>(-code - 1) * t.width + 4 * c);
         g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
       } else {
         const int s = code / a.ncand;
-        const float coef = a.coefbuf[code];
+        const float coef = __ldg(a.coefbuf + code);
         const float* q = a.qbuf + static_cast<int64_t>(s) * a.wq;
         const float4 qc = ld4(q + 4 * c);
         float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);

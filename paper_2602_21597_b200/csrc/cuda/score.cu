@@ -88,10 +88,12 @@ struct Lane {
 // candidate: d_j -> coef_of(j, d_j) returns coef_j -> dq accumulation.
 template <int BB, int kMaxChunks, bool kGrad, class CoefOp>
 __device__ __forceinline__ void sweep(const DevArgs& a, const int32_t* cand, Lane<BB, kMaxChunks>& L,
-                                      CoefOp&& coef_of) {
+                                      CoefOp&& coef_of, int part_idx = 0, int n_parts = 1) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int d4 = a.dim / 4;
-  for (int j0 = warp * kRows; j0 < a.ncand; j0 += kWarps * kRows) {
+  // candidate groups are dealt round-robin over (part, warp)
+  for (int j0 = (part_idx * kWarps + warp) * kRows; j0 < a.ncand;
+       j0 += n_parts * kWarps * kRows) {
     float4 v[kRows][kMaxChunks];
     float part[kRows];
 #pragma unroll
@@ -169,7 +171,8 @@ __device__ void reduce_dq(const DevArgs& a, Lane<BB, kMaxChunks>& L, float* red,
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(dst + e, ld4(red + e));
+  if (dst)
+    for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(dst + e, ld4(red + e));
 }
 
 __device__ __forceinline__ float loss_coef(const DevArgs& a, int j, float dj, float& loss) {
@@ -193,47 +196,81 @@ __device__ float block_sum(float v, float* red) {
   return t;  // thread 0
 }
 
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+}
+__device__ __forceinline__ float ld_peer(const float* local, uint32_t peer) {
+  uint32_t remote;
+  float v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(remote)
+               : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(local))), "r"(peer));
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote));
+  return v;
+}
+
+// A (2,1,1) cluster per Loss node: the two CTAs take alternate candidate
+// groups, then CTA 0 adds CTA 1's dL/dq and loss partials over DSMEM (fixed
+// order: own + peer, so the result is deterministic).
 template <int BB, int NCH>
 __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first) {
   __shared__ __align__(16) float red[2 * 1024];
-  __shared__ float lred[kWarps];
-  const ngdb_node_desc d = a.nodes[first + blockIdx.x];
+  __shared__ float lred[kWarps + 1];
+  const int part = blockIdx.x & 1;
+  const ngdb_node_desc d = a.nodes[first + (blockIdx.x >> 1)];
   const int qi = d.id;
   if (d.aux < 0) {
     // union query: the input already holds min-over-branch distances
-    float loss = 0.f;
-    for (int j = threadIdx.x; j < a.ncand; j += kThreads) {
-      const float c = loss_coef(a, j, a.arena[d.in[0] + j], loss);
-      a.ddbuf[static_cast<int64_t>(qi) * a.ncand + j] = c;
+    if (part == 0) {
+      float loss = 0.f;
+      for (int j = threadIdx.x; j < a.ncand; j += kThreads) {
+        const float c = loss_coef(a, j, a.arena[d.in[0] + j], loss);
+        a.ddbuf[static_cast<int64_t>(qi) * a.ncand + j] = c;
+      }
+      loss = block_sum(warp_sum(loss), lred);
+      if (threadIdx.x == 0) {
+        a.loss_out[qi] = loss;
+        a.arena[d.out] = loss;
+        if (!isfinite(loss)) atomicOr(&a.flags[0], 1);
+      }
     }
-    loss = block_sum(warp_sum(loss), lred);
-    if (threadIdx.x == 0) {
-      a.loss_out[qi] = loss;
-      a.arena[d.out] = loss;
-      if (!isfinite(loss)) atomicOr(&a.flags[0], 1);
-    }
+    cluster_sync_all();  // barrier count is uniform across both paths
+    cluster_sync_all();
     return;
   }
   const float* q = a.arena + d.in[0];
-  float* qcopy = a.qbuf + static_cast<int64_t>(d.aux) * a.wq;
-  for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(qcopy + e, ld4(q + e));
+  if (part == 0) {
+    float* qcopy = a.qbuf + static_cast<int64_t>(d.aux) * a.wq;
+    for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(qcopy + e, ld4(q + e));
+  }
   Lane<BB, NCH> L;
   L.load_q(q, a.dim, threadIdx.x & 31);
   float loss = 0.f;  // identical in every lane of a warp
   float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
   const int lane = threadIdx.x & 31;
-  sweep<BB, NCH, true>(a, a.cand + static_cast<int64_t>(qi) * a.ncand, L, [&](int j, float dj) {
-    const float c = loss_coef(a, j, dj, loss);
-    if (lane == 0) coefs[j] = c;
-    return c;
-  });
+  sweep<BB, NCH, true>(
+      a, a.cand + static_cast<int64_t>(qi) * a.ncand, L,
+      [&](int j, float dj) {
+        const float c = loss_coef(a, j, dj, loss);
+        if (lane == 0) coefs[j] = c;
+        return c;
+      },
+      part, 2);
   loss = block_sum(lane == 0 ? loss : 0.f, lred);
-  if (threadIdx.x == 0) {
-    a.loss_out[qi] = loss;
-    a.arena[d.out] = loss;
-    if (!isfinite(loss)) atomicOr(&a.flags[0], 1);
+  if (threadIdx.x == 0) lred[kWarps] = loss;
+  reduce_dq<BB, NCH>(a, L, red, nullptr);
+  cluster_sync_all();
+  if (part == 0) {
+    float* dst = a.dqbuf + static_cast<int64_t>(d.aux) * a.wq;
+    for (int e = threadIdx.x; e < a.wq; e += kThreads) dst[e] = red[e] + ld_peer(red + e, 1);
+    if (threadIdx.x == 0) {
+      const float total = lred[kWarps] + ld_peer(lred + kWarps, 1);
+      a.loss_out[qi] = total;
+      a.arena[d.out] = total;
+      if (!isfinite(total)) atomicOr(&a.flags[0], 1);
+    }
   }
-  reduce_dq<BB, NCH>(a, L, red, a.dqbuf + static_cast<int64_t>(d.aux) * a.wq);
+  cluster_sync_all();  // CTA 1 stays resident until its partials were read
 }
 
 // Union branch Score: fwd writes the distance vector; bwd turns the routed
@@ -268,8 +305,19 @@ __global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int
 
 template <int NCH>
 void launch_loss_nch(const DevArgs& a, int first, int n, cudaStream_t s) {
-  if (a.backbone == NGDB_GQE) loss_fwd_kernel<NGDB_GQE, NCH><<<n, kThreads, 0, s>>>(a, first);
-  else loss_fwd_kernel<NGDB_Q2B, NCH><<<n, kThreads, 0, s>>>(a, first);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * n);  // a CTA pair (cluster of 2) per Loss node
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (a.backbone == NGDB_GQE) cudaLaunchKernelEx(&cfg, loss_fwd_kernel<NGDB_GQE, NCH>, a, first);
+  else cudaLaunchKernelEx(&cfg, loss_fwd_kernel<NGDB_Q2B, NCH>, a, first);
 }
 template <int NCH>
 void launch_score_nch(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {

@@ -23,7 +23,7 @@ namespace {
 
 constexpr int BM = 128, BN = 80, BK = 32;
 constexpr int kThreads = 256;   // 8 warps; warps w and w+4 share TMEM lane quarter w%4
-constexpr int kStages = 3;      // smem operand ring (chunks in flight)
+constexpr int kStages = 2;      // smem operand ring; 104 KB -> two CTAs per SM
 constexpr int kTmemCols = 256;  // 2 accumulator buffers of BN columns (power of two)
 constexpr int kHalfCols = BN / 2;
 constexpr int kMaxProblems = 4;
@@ -159,7 +159,7 @@ __device__ __forceinline__ void drain(uint32_t tmem, int buf, float* acc) {
   for (int j = 0; j < kHalfCols; ++j) acc[j] += __uint_as_float(r[j]);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmBatch batch) {
+__global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_constant__ TcGemmBatch batch) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t s_base = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * STAGE);  // [kStages]
@@ -245,43 +245,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
   }
   asm volatile("cp.async.wait_group 0;");
 
-  if (S > 1) {
-    // deterministic split-K reduction through distributed shared memory
-    float* park = reinterpret_cast<float*>(smem);
-    if (rank > 0)
+  // Stage this CTA's (partial) tile row-major in its own shared memory.
+  float* tile_s = reinterpret_cast<float*>(smem);
+  {
+    const int r = (warp & 3) * 32 + (threadIdx.x & 31), cb = (warp >> 2) * kHalfCols;
 #pragma unroll
-      for (int j = 0; j < kHalfCols; ++j) park[j * kThreads + threadIdx.x] = acc[j];
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
-    if (rank == 0) {
-      for (int p = 1; p < S; ++p) {
-        uint32_t remote;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                     : "=r"(remote)
-                     : "r"(smem_u32(park + threadIdx.x)), "r"(p));
-#pragma unroll
-        for (int j = 0; j < kHalfCols; ++j) {
-          float v;
-          asm volatile("ld.shared::cluster.f32 %0, [%1];"
-                       : "=f"(v)
-                       : "r"(remote + static_cast<uint32_t>(j * kThreads * 4)));
-          acc[j] += v;
-        }
-      }
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+    for (int j = 0; j < kHalfCols; ++j) tile_s[r * kTileStride + cb + j] = acc[j];
   }
-
-  if (rank == 0) {
-    // stage the tile row-major in shared memory, then write rows coalesced
-    float* tile_s = reinterpret_cast<float*>(smem);
-    {
-      const int r = (warp & 3) * 32 + (threadIdx.x & 31), cb = (warp >> 2) * kHalfCols;
-#pragma unroll
-      for (int j = 0; j < kHalfCols; ++j) tile_s[r * kTileStride + cb + j] = acc[j];
-    }
-    __syncthreads();
+  // Split-K reduce-scatter over distributed shared memory: CTA `rank` owns rows
+  // [r_beg, r_end) of the tile, sums them over the S partial tiles in rank
+  // order (deterministic) and writes them out; all S CTAs share the work.
+  const int r_beg = rank * BM / S, r_end = (rank + 1) * BM / S;
+  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+  else __syncthreads();
+  {
     const int lane = threadIdx.x & 31;
-    for (int r = warp; r < BM; r += kThreads / 32) {
+    const uint32_t local = smem_u32(tile_s);
+    for (int r = r_beg + warp; r < r_end; r += kThreads / 32) {
       const int row = m0 + r;
       if (row >= g.M) break;
       float* crow =
@@ -289,7 +269,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       for (int cc = lane; cc < BN; cc += 32) {
         const int n = n0 + cc;
         if (n >= g.N) break;
-        float v = tile_s[r * kTileStride + cc];
+        float v = 0.f;
+        const uint32_t off = static_cast<uint32_t>((r * kTileStride + cc) * 4);
+        for (int p = 0; p < S; ++p) {
+          if (p == rank) {
+            v += tile_s[r * kTileStride + cc];
+          } else {
+            uint32_t remote;
+            float pv;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv) : "r"(remote));
+            v += pv;
+          }
+        }
         if (g.bias) v += g.bias[n];
         if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;
         if (g.accumulate) v += crow[n];
@@ -303,6 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_const
       }
     }
   }
+  // peers' partial tiles must stay resident until every slice has been read
+  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
@@ -378,8 +372,11 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   }
   if (b.n == 0) return 0;
   b.tile_begin[b.n] = tiles;
-  // split-K: ~3 K-chunks per CTA, at most 8 CTAs per cluster (portable size)
-  b.S = std::max(1, std::min(8, max_chunks / 3));
+  // split-K so the launch fills about one wave (2 CTAs per SM), at most 8 CTAs
+  // per cluster (portable size) and at least 2 chunks per CTA
+  int num_sms = 148;
+  cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
+  b.S = std::max(1, std::min({8, (2 * num_sms) / std::max(tiles, 1), max_chunks / 2}));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(tiles * b.S);
   cfg.blockDim = dim3(kThreads);
