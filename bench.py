@@ -107,6 +107,38 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def roofline(fams):
+    """Roofline of the dominant kernel family (largest share of the profiled
+    step): GEMM families against the measured dense tensor peak (bf16 cuBLAS,
+    the only measured tensor figure; our contractions are 3xTF32 on tcgen05),
+    bandwidth families against measured HBM. Also the top HBM-bound family."""
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (
+        ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    tensor = float(peaks.get("bf16_tflops", 1590.0))
+    kind = "measured" if peaks else "fallback"
+    total = sum(v["ms_per_step"] for v in fams.values())
+    name, f = max(fams.items(), key=lambda kv: kv[1]["ms_per_step"])
+
+    def hbm_entry(n, v):
+        return {"bound": "hbm", "kernel": n, "achieved": v["gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": v["gbs"] / hbm, "traffic": None, "peak_kind": kind,
+                "share_of_step": v["ms_per_step"] / total}
+
+    if f["flops_per_step"] > 0:
+        roof = {"bound": "tensor", "kernel": name, "achieved": f["tflops"], "peak": tensor,
+                "unit": "TFLOP/s", "frac": f["tflops"] / tensor, "traffic": None,
+                "peak_kind": kind + " (bf16 dense; kernels are 3xTF32)",
+                "share_of_step": f["ms_per_step"] / total}
+    else:
+        roof = hbm_entry(name, f)
+    bw = {k: v for k, v in fams.items() if v["flops_per_step"] == 0}
+    if bw:
+        n2, f2 = max(bw.items(), key=lambda kv: kv[1]["ms_per_step"])
+        roof["hbm_kernel"] = hbm_entry(n2, f2)
+    return roof
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -266,21 +298,19 @@ def main():
     check(lib.ngdb_sync(ctx))
     fams = {}
     for f in range(lib.ngdb_profile_families()):
-        fms, fl, fb = C.c_double(), C.c_int64(), C.c_double()
+        fms, fl, fb, ff = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         check(lib.ngdb_profile_read(ctx, f, C.byref(fms), C.byref(fl), C.byref(fb)))
+        check(lib.ngdb_profile_flops(ctx, f, C.byref(ff)))
         if fl.value:
             fams[lib.ngdb_profile_family_name(f).decode()] = {
                 "ms_per_step": fms.value / args.profile_steps,
                 "launches_per_step": fl.value / args.profile_steps,
                 "gbs": fb.value / (fms.value / 1000.0) / 1e9 if fms.value > 0 else 0.0,
-                "bytes_per_step": fb.value / args.profile_steps}
+                "tflops": ff.value / (fms.value / 1000.0) / 1e12 if fms.value > 0 else 0.0,
+                "bytes_per_step": fb.value / args.profile_steps,
+                "flops_per_step": ff.value / args.profile_steps}
     check(lib.ngdb_profile_enable(ctx, 0))
-    peak, peak_kind = load_peaks()
-    dom = max(fams.items(), key=lambda kv: kv[1]["ms_per_step"])
-    roof = {"bound": "hbm", "kernel": dom[0], "achieved": dom[1]["gbs"], "peak": peak,
-            "unit": "GB/s", "frac": dom[1]["gbs"] / peak, "traffic": None,
-            "peak_kind": peak_kind,
-            "share_of_step": dom[1]["ms_per_step"] / sum(v["ms_per_step"] for v in fams.values())}
+    roof = roofline(fams)
 
     # ---- e2e: public C ABI call with host buffers ----------------------------
     losses = np.zeros(batch, dtype=np.float32)

@@ -162,6 +162,8 @@ int ngdb_timer_stop(ngdb_ctx* ctx, float* ms);
 int ngdb_profile_enable(ngdb_ctx* ctx, int32_t on);
 int ngdb_profile_read(ngdb_ctx* ctx, int32_t family, double* ms, int64_t* launches,
                       double* bytes);
+/* algorithmic fp32 GEMM flops accumulated by a family while profiling */
+int ngdb_profile_flops(ngdb_ctx* ctx, int32_t family, double* flops);
 int32_t ngdb_profile_families(void);
 const char* ngdb_profile_family_name(int32_t family);
 /* Kernel launches issued so far by this context (all families). */

@@ -59,6 +59,16 @@ int ngdb_step_trace_json(const ngdb_step* s, int32_t with_nodes, char* buf, int6
                          int64_t* len);
 int ngdb_step_destroy(ngdb_step* s);
 
+/* --- reference-interface helpers (common.hpp:60-127) ----- */
+/* Rng(seed) (forked with fork_tag when >= 0), `skip` draws discarded, next draw */
+uint64_t ngdb_rng_next(uint64_t seed, int64_t fork_tag, int32_t skip);
+/* out[i*reps + j] = j-th Rng(seed).below(ns[i]) in draw order */
+int ngdb_rng_below(uint64_t seed, const uint64_t* ns, int32_t count, int32_t reps, uint64_t* out);
+/* Eq. 4 selection over the 16 pools (Fwd kinds then Bwd kinds) */
+int ngdb_select_pool(const int64_t* counts, const int64_t* head_timestamps, int32_t* pool);
+/* JSON-lines round trip of one query record (query.hpp:57-69) */
+int ngdb_jsonl_roundtrip(const char* line, char* out, int64_t cap);
+
 /* --- parameters ------------------------------------------- */
 int ngdb_param_init(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
                     const char* name, uint64_t seed, float* out, int64_t n);

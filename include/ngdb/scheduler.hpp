@@ -26,6 +26,7 @@ namespace ngdb {
 enum class ReleasePolicy : uint8_t { Eager = 0, EndOfDag = 1 };
 
 struct SchedulerConfig {
+  Backbone backbone = Backbone::GQE;
   int32_t b_max = 512;
   int32_t query_width = 400;  // elements of a query embedding (GQE d, Q2B 2d, BetaE 2d')
   int32_t n_candidates = 129; // 1 + K
@@ -59,9 +60,13 @@ struct ExecutionTrace {
 int select_pool(const std::array<int64_t, kPoolCount>& counts,
                 const std::array<int64_t, kPoolCount>& head_timestamp);
 
-// Tensor model (SURVEY A-2): forward node X owns T_X, consumed by
-// its forward consumer, by Bwd(consumer) and by Bwd(X); Bwd(X) owns G_X with
-// one row per forward input of X, consumed by Bwd(input_i).
+// Tensor model (SURVEY A-2): forward node X owns
+// T_X, consumed by its forward consumer and — when the consumer's backward
+// kernel re-reads its inputs (bwd_reads_inputs) — by Bwd(consumer); a Loss
+// sink's T_X is consumed by Bwd(Loss). Bwd(X) owns G_X with one row per
+// forward input of X, consumed by Bwd(input_i).
+bool bwd_reads_inputs(OpKind kind, Backbone backbone);
+
 struct TensorModel {
   int32_t query_width;
   int32_t n_candidates;

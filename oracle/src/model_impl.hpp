@@ -350,6 +350,15 @@ struct Exec {
     if (bufs[h].rc <= 0) throw std::runtime_error("use after reclamation");
     return bufs[h].v.data();
   }
+  // Backward kernels that re-read their forward inputs (everything else uses
+  // only the upstream gradient); the refcounts keep exactly those alive.
+  bool reads_inputs(int kind) const {
+    switch (kind) {
+      case K_INTER: case K_SCORE: case K_UNION: case K_LOSS: return true;
+      case K_PROJ: return md.backbone != 0;
+      default: return false;
+    }
+  }
   std::vector<int> consumed(int o) const {
     const ONode& x = g.nodes[o];
     std::vector<int> out;
@@ -358,15 +367,18 @@ struct Exec {
     } else {
       const ONode& m = g.nodes[x.mirror];
       if (m.consumer >= 0) out.push_back(Gt[g.nf + m.consumer]);
-      for (int i : m.in) out.push_back(T[i]);
-      out.push_back(T[x.mirror]);
+      if (reads_inputs(m.kind))
+        for (int i : m.in) out.push_back(T[i]);
+      if (m.consumer < 0) out.push_back(T[x.mirror]);  // the Loss sink
     }
     return out;
   }
   void allocate(int o) {
     const ONode& x = g.nodes[o];
     if (!x.bwd) {
-      T[o] = alloc(width_fwd(o), x.consumer >= 0 ? 3 : 1);
+      int rc = 1;
+      if (x.consumer >= 0 && reads_inputs(g.nodes[x.consumer].kind)) ++rc;
+      T[o] = alloc(width_fwd(o), rc);
     } else {
       const ONode& m = g.nodes[x.mirror];
       if (m.in.empty()) return;
@@ -489,13 +501,13 @@ struct Exec {
         break;
       }
       case K_PROJ: {
-        const R* in = t(T[m.in[0]]);
         const R* r = &md.P["relation"][(int64_t)m.payload * md.rw];
         R* gr = md.grrow(m.payload);
         for (int i = 0; i < d; ++i) {
           gout[i] = gin[i];
           gr[i] += gin[i];
         }
+        const R* in = md.backbone == 1 ? t(T[m.in[0]]) : nullptr;  // Q2B offset mask
         if (md.backbone == 1)
           for (int i = 0; i < d; ++i) {
             const R gv = in[d + i] + r[d + i] > 0 ? gin[d + i] : R(0);

@@ -72,6 +72,7 @@ SIGNATURES = {
     "ngdb_profile_enable": (C.c_int, [C.c_void_p, i32]),
     "ngdb_profile_read": (C.c_int, [C.c_void_p, i32, P(f64), P(i64), P(f64)]),
     "ngdb_profile_families": (i32, []),
+    "ngdb_profile_flops": (C.c_int, [C.c_void_p, i32, P(f64)]),
     "ngdb_profile_family_name": (C.c_char_p, [i32]),
     "ngdb_launch_count": (i64, [C.c_void_p]),
     "ngdb_flush_l2": (C.c_int, [C.c_void_p]),
@@ -95,6 +96,10 @@ SIGNATURES = {
     "ngdb_step_trace_json": (C.c_int, [C.c_void_p, i32, C.c_char_p, i64, P(i64)]),
     "ngdb_step_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_param_init": (C.c_int, [i32, i32, i32, i32, C.c_char_p, u64, P(f32), i64]),
+    "ngdb_rng_next": (u64, [u64, i64, i32]),
+    "ngdb_rng_below": (C.c_int, [u64, P(u64), i32, i32, P(u64)]),
+    "ngdb_select_pool": (C.c_int, [P(i64), P(i64), P(i32)]),
+    "ngdb_jsonl_roundtrip": (C.c_int, [C.c_char_p, C.c_char_p, i64]),
     "ngdb_train_step": (C.c_int, [C.c_void_p, C.c_void_p, i32, i64, P(f32), P(f64)]),
     "ngdb_run_step": (C.c_int, [C.c_void_p, C.c_void_p, i64, P(f32), P(f64)]),
     # test hook (tc_gemm.cu): tcgen05 3xTF32 GEMM on host buffers

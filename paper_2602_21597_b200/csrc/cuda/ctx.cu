@@ -194,7 +194,7 @@ struct ngdb_ctx {
   struct Rec { int fam; cudaEvent_t a, b; double bytes; int launches; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> event_pool;
-  double fam_ms[F_COUNT] = {}, fam_bytes[F_COUNT] = {};
+  double fam_ms[F_COUNT] = {}, fam_bytes[F_COUNT] = {}, fam_flops[F_COUNT] = {};
   int64_t fam_launches[F_COUNT] = {};
   int64_t launches = 0;
   float* d_bc = nullptr;        // Adam bias corrections of the current step
@@ -391,6 +391,15 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d) {
       break;
     case NGDB_OP_INTERSECT:
       if (d.k < 2 || d.k > 3) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "intersect cardinality"};
+      if (c->profiling) {
+        // algorithmic fp32 GEMM flops of the class (2*M*N*K per contraction,
+        // not counting the 3xTF32 split): DESIGN.md §4
+        const double n = d.count, R = double(d.count) * d.k, D2 = 2.0 * c->desc.dim * c->desc.dim;
+        double gemm_rows;
+        if (c->desc.backbone == NGDB_GQE) gemm_rows = d.dir == 0 ? 2 * n : 5 * n;
+        else gemm_rows = d.dir == 0 ? 3 * R + n : 9 * R + 3 * n;
+        c->fam_flops[fam] += gemm_rows * D2;
+      }
       timed(c, fam, bytes, [&] { return launch_intersect(a, d.dir, d.k, d.first, d.count, lc); });
       break;
     case NGDB_OP_SCORE:
@@ -885,8 +894,16 @@ int ngdb_profile_enable(ngdb_ctx* c, int32_t on) {
     for (int i = 0; i < F_COUNT; ++i) {
       c->fam_ms[i] = 0;
       c->fam_bytes[i] = 0;
+      c->fam_flops[i] = 0;
       c->fam_launches[i] = 0;
     }
+  });
+}
+
+int ngdb_profile_flops(ngdb_ctx* c, int32_t family, double* flops) {
+  return guarded([&] {
+    if (family < 0 || family >= F_COUNT) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "family"};
+    *flops = c->fam_flops[family];
   });
 }
 

@@ -5,8 +5,11 @@
 #include <exception>
 #include <string>
 
+#include <array>
+
 #include "ngdb/kg.hpp"
 #include "ngdb/sampler.hpp"
+#include "ngdb/scheduler.hpp"
 #include "ngdb/synth.hpp"
 #include "ngdb/trainer.hpp"
 
@@ -255,6 +258,41 @@ int ngdb_step_trace_json(const ngdb_step* s, int32_t with_nodes, char* buf, int6
 int ngdb_step_destroy(ngdb_step* s) {
   delete s;
   return NGDB_OK;
+}
+
+uint64_t ngdb_rng_next(uint64_t seed, int64_t fork_tag, int32_t skip) {
+  ngdb::Rng r(seed);
+  if (fork_tag >= 0) r = r.fork(static_cast<uint64_t>(fork_tag));
+  for (int32_t i = 0; i < skip; ++i) r.next();
+  return r.next();
+}
+
+int ngdb_rng_below(uint64_t seed, const uint64_t* ns, int32_t count, int32_t reps, uint64_t* out) {
+  return guarded([&] {
+    ngdb::Rng r(seed);
+    int64_t k = 0;
+    for (int32_t i = 0; i < count; ++i)
+      for (int32_t j = 0; j < reps; ++j) out[k++] = r.below(ns[i]);
+  });
+}
+
+int ngdb_select_pool(const int64_t* counts, const int64_t* heads, int32_t* pool) {
+  return guarded([&] {
+    std::array<int64_t, ngdb::kPoolCount> c{}, h{};
+    for (int i = 0; i < ngdb::kPoolCount; ++i) {
+      c[i] = counts[i];
+      h[i] = heads[i];
+    }
+    *pool = ngdb::select_pool(c, h);
+  });
+}
+
+int ngdb_jsonl_roundtrip(const char* line, char* out, int64_t cap) {
+  return guarded([&] {
+    const std::string s = ngdb::to_jsonl(ngdb::parse_jsonl(line));
+    if (static_cast<int64_t>(s.size()) + 1 > cap) throw ngdb::ShapeMismatch("buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
 }
 
 int ngdb_param_init(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,

@@ -21,6 +21,22 @@ int select_pool(const std::array<int64_t, kPoolCount>& counts,
   return best;
 }
 
+// Which backward kernels re-read their forward inputs (the activations the
+// refcount must keep alive): set operators and scoring recompute from inputs;
+// Q2B / BetaE projections need the pre-activation offset; BetaE negation needs
+// alpha, beta. GQE/Q2B Project/Negate backward use only the upstream gradient.
+bool bwd_reads_inputs(OpKind kind, Backbone backbone) {
+  switch (kind) {
+    case OpKind::Intersect:
+    case OpKind::Score:
+    case OpKind::UnionScore:
+    case OpKind::Loss: return true;
+    case OpKind::Project: return backbone != Backbone::GQE;
+    case OpKind::Negate: return backbone == Backbone::BETAE;
+    default: return false;
+  }
+}
+
 int64_t TensorModel::fwd_elems(const FusedDag& f, const OperatorNode& x) const {
   (void)f;
   switch (x.op.kind) {
@@ -137,7 +153,8 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
   auto allocate = [&](int32_t o) {
     const OperatorNode& x = f.nodes[o];
     if (x.op.dir == Direction::Fwd) {
-      const int32_t rc = x.consumer >= 0 ? 3 : 1;
+      int32_t rc = 1;  // the forward consumer, or Bwd(Loss) for the sink
+      if (x.consumer >= 0 && bwd_reads_inputs(f.nodes[x.consumer].op.kind, cfg_.backbone)) ++rc;
       t_fwd[o] = arena.alloc(tm.fwd_elems(f, x) * eb, rc);
       fwd_slot_[o] = arena.offset(t_fwd[o]);
     } else {
@@ -155,8 +172,9 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
     } else {
       const OperatorNode& m = f.nodes[x.mirror];
       if (m.consumer >= 0) fn(t_bwd[nf + m.consumer]);
-      for (int k = 0; k < m.n_inputs; ++k) fn(t_fwd[m.inputs[k]]);
-      fn(t_fwd[x.mirror]);
+      if (bwd_reads_inputs(m.op.kind, cfg_.backbone))
+        for (int k = 0; k < m.n_inputs; ++k) fn(t_fwd[m.inputs[k]]);
+      if (m.consumer < 0) fn(t_fwd[x.mirror]);
     }
   };
 

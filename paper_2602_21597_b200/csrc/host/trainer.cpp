@@ -162,6 +162,7 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
   build_csr(rkeys, plan.relation_rows, plan.relation_seg, plan.relation_contrib);
 
   SchedulerConfig sc;
+  sc.backbone = cfg.backbone;
   sc.b_max = cfg.b_max;
   sc.query_width = wq;
   sc.n_candidates = nc;

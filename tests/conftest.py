@@ -10,6 +10,7 @@ sys.path.insert(0, str(ROOT))
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) device")
+    config.addinivalue_line("markers", "slow: benchmark-shape host work (seconds)")
 
 
 def _has_gpu() -> bool:
