@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "ngdb/ngdb_cuda.h"
 
 namespace ngdb_dev {
@@ -56,6 +58,14 @@ struct DevArgs {
   int64_t scratch_cap;
 };
 
+// Programmatic dependent launch: let the next kernel in the stream start its
+// launch/prologue now, then wait until the previous kernel's results are
+// visible. Every kernel of the step calls this before touching step data.
+__device__ __forceinline__ void pdl_start() {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -89,6 +99,34 @@ __device__ __forceinline__ float sigmoidf(float x) {
 
 // ---- launchers (defined in the k_*.cu files) --------------------------------
 namespace ngdb_dev {
+
+// Launch with programmatic stream serialization (PDL) and an optional 1-D
+// cluster; kernels pair this with pdl_start().
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[n].val.programmaticStreamSerializationAllowed = 1;
+  ++n;
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 struct LaunchCtx {
   cudaStream_t stream;
   int num_sms;

@@ -80,6 +80,7 @@ struct ColsumJobs {
 // 32 columns per block; warp w sums rows w, w+8, ...; the 8 warp partials are
 // combined in warp order (deterministic).
 __global__ void __launch_bounds__(256) colsum_kernel(ColsumJobs jobs) {
+  pdl_start();
   __shared__ float part[8][32];
   const ColsumJob& j = jobs.job[blockIdx.y];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(ColsumJobs jobs) {
   }
 }
 int colsums(const ColsumJobs& jobs, int n, cudaStream_t s) {
-  colsum_kernel<<<dim3((n + 31) / 32, jobs.n), 256, 0, s>>>(jobs);
+  launch_pdl(colsum_kernel, dim3(dim3((n + 31) / 32, jobs.n)), dim3(256), 0, s, 1, jobs);
   return 1;
 }
 
@@ -106,6 +107,7 @@ int colsums(const ColsumJobs& jobs, int n, cudaStream_t s) {
 // M[i] = mean_l x_l (plain + split); optionally G[i] = upstream grad (plain + split)
 __global__ void gqe_pack_kernel(DevArgs a, int k, int first, float* M, Split Ms, float* G,
                                 Split Gs) {
+  pdl_start();
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
   const float inv_k = 1.f / static_cast<float>(k);
@@ -119,6 +121,7 @@ __global__ void gqe_pack_kernel(DevArgs a, int k, int first, float* M, Split Ms,
 }
 // G_X row l of node i = dM[i] / k  (mean adjoint)
 __global__ void gqe_scatter_kernel(DevArgs a, int k, int first, const float* dM) {
+  pdl_start();
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
   const float inv_k = 1.f / static_cast<float>(k);
@@ -142,7 +145,7 @@ int gqe_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   Split Gs = dir ? take_split(sc, nd) : Split{nullptr, nullptr};
   int launches = 0;
 
-  gqe_pack_kernel<<<n, 128, 0, s>>>(a, k, first, M, Ms, G, Gs);
+  launch_pdl(gqe_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, M, Ms, G, Gs);
   ++launches;
   TcGemmArgs h = gemm_args(n, D, D, op(Ms, D), wop(a, GQE_W1, D, D, false), H, D);
   h.s_hi = RHs.hi; h.s_lo = RHs.lo; h.s_relu = 1;
@@ -180,7 +183,7 @@ int gqe_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   lvl[1].accumulate = 1;
   lvl[2] = gemm_args(n, D, D, op(dHs, D), wop(a, GQE_W1, D, D, true), dM, D);  // dM = dH W1
   launches += tc_gemm_batch(lvl, 3, s);
-  gqe_scatter_kernel<<<n, 128, 0, s>>>(a, k, first, dM);
+  launch_pdl(gqe_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, dM);
   return launches + 1;
 }
 
@@ -189,6 +192,7 @@ int gqe_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
 
 __global__ void q2b_pack_kernel(DevArgs a, int k, int first, float* Cin, Split Cs, float* Oin,
                                 Split Os) {
+  pdl_start();
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
@@ -200,6 +204,7 @@ __global__ void q2b_pack_kernel(DevArgs a, int k, int first, float* Cin, Split C
 }
 // Lm[i] = mean_l relu(P[i*k+l]) (plain + split)
 __global__ void q2b_mean_relu_kernel(const float* P, int k, int D, float* Lm, Split Lms) {
+  pdl_start();
   const int i = blockIdx.x;
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
@@ -222,6 +227,7 @@ __device__ __forceinline__ void softmax_k(const float* S, int64_t base, int k, i
 }
 __global__ void q2b_combine_kernel(DevArgs a, int k, int first, const float* S, const float* U,
                                    const float* Cin, const float* Oin) {
+  pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim;
   const ngdb_node_desc d = a.nodes[first + i];
@@ -241,6 +247,7 @@ __global__ void q2b_combine_kernel(DevArgs a, int k, int first, const float* S, 
 __global__ void q2b_combine_bwd_kernel(DevArgs a, int k, int first, const float* S, const float* U,
                                        const float* Cin, const float* Oin, float* gS, Split gSs,
                                        float* dCin, float* dOin, float* gU, Split gUs) {
+  pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim;
   const ngdb_node_desc d = a.nodes[first + i];
@@ -274,6 +281,7 @@ __global__ void q2b_combine_bwd_kernel(DevArgs a, int k, int first, const float*
 // gP[i*k+l] = gLm[i] / k * (P > 0)  (plain + split)
 __global__ void q2b_gp_kernel(const float* gLm, const float* P, int k, int D, float* gP,
                               Split gPs) {
+  pdl_start();
   const int i = blockIdx.x;
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < D; e += blockDim.x)
@@ -284,6 +292,7 @@ __global__ void q2b_gp_kernel(const float* gLm, const float* P, int k, int D, fl
 }
 __global__ void q2b_scatter_kernel(DevArgs a, int k, int first, const float* dCin,
                                    const float* dOin) {
+  pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim;
   const ngdb_node_desc d = a.nodes[first + i];
@@ -321,7 +330,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   const float* v2 = p + a.dense_off[Q2B_V2B];
   int launches = 0;
 
-  q2b_pack_kernel<<<n, 128, 0, s>>>(a, k, first, Cin, Cs, Oin, Os);
+  launch_pdl(q2b_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, Cin, Cs, Oin, Os);
   ++launches;
   {  // level 1: Z = A1 c + a1 (chained split of relu(Z)), P = V1 o + v1
     TcGemmArgs lvl[2];
@@ -332,7 +341,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
     lvl[1].bias = v1;
     launches += tc_gemm_batch(lvl, 2, s);
   }
-  q2b_mean_relu_kernel<<<n, 128, 0, s>>>(P, k, D, Lm, Lms);
+  launch_pdl(q2b_mean_relu_kernel, dim3(n), dim3(128), 0, s, 1, P, k, D, Lm, Lms);
   ++launches;
   {  // level 2: S = A2 relu(Z) + a2, U = V2 Lm + v2
     TcGemmArgs lvl[2];
@@ -343,7 +352,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
     launches += tc_gemm_batch(lvl, 2, s);
   }
   if (dir == 0) {
-    q2b_combine_kernel<<<n, 128, 0, s>>>(a, k, first, S, U, Cin, Oin);
+    launch_pdl(q2b_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, S, U, Cin, Oin);
     return launches + 1;
   }
   float* gS = sc.take(rd);
@@ -363,7 +372,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
 
-  q2b_combine_bwd_kernel<<<n, 128, 0, s>>>(a, k, first, S, U, Cin, Oin, gS, gSs, dCin, dOin, gU,
+  launch_pdl(q2b_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, S, U, Cin, Oin, gS, gSs, dCin, dOin, gU,
                                            gUs);
   ++launches;
   SplitJobs j1{};
@@ -385,7 +394,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
     lvl[3].s_hi = gZs.hi; lvl[3].s_lo = gZs.lo;
     launches += tc_gemm_batch(lvl, 4, s);
   }
-  q2b_gp_kernel<<<n, 128, 0, s>>>(gLm, P, k, D, gP, gPs);
+  launch_pdl(q2b_gp_kernel, dim3(n), dim3(128), 0, s, 1, gLm, P, k, D, gP, gPs);
   ++launches;
   SplitJobs j2{};
   j2.job[0] = {gP, R, D, D, 0, gPT.hi, gPT.lo};
@@ -413,7 +422,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   cj.job[3] = {gZ, R, D, g + off[Q2B_A1B]};
   cj.n = 4;
   launches += colsums(cj, D, s);
-  q2b_scatter_kernel<<<n, 128, 0, s>>>(a, k, first, dCin, dOin);
+  launch_pdl(q2b_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, dCin, dOin);
   return launches + 1;
 }
 

@@ -64,6 +64,7 @@ __device__ __forceinline__ float cand_grad(float v, float qc, float qo, float co
 template <int BB>
 __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, SparseTable t,
                                                                   AdamHyper hp, const float* bc) {
+  pdl_start();
   const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row_idx >= t.n_rows) return;
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, Spa
 
 __global__ void __launch_bounds__(kWarps * 32) relation_adam_kernel(DevArgs a, SparseTable t,
                                                                     AdamHyper hp, const float* bc) {
+  pdl_start();
   const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row_idx >= t.n_rows) return;
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(kWarps * 32) relation_adam_kernel(DevArgs a, S
 
 __global__ void dense_adam_kernel(float* w, float* m, float* v, const float* g, int64_t n,
                                   AdamHyper hp, const float* bc) {
+  pdl_start();
   const AdamK k = adam_consts(hp, bc);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -151,9 +154,9 @@ int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const Adam
   if (t.n_rows <= 0) return 0;
   const int blocks = (t.n_rows + kWarps - 1) / kWarps;
   if (a.backbone == NGDB_GQE)
-    entity_adam_kernel<NGDB_GQE><<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, hp, bc);
+    launch_pdl(entity_adam_kernel<NGDB_GQE>, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
   else
-    entity_adam_kernel<NGDB_Q2B><<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, hp, bc);
+    launch_pdl(entity_adam_kernel<NGDB_Q2B>, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
   return 1;
 }
 
@@ -161,7 +164,7 @@ int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, const Ad
                                 const float* bc, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
   const int blocks = (t.n_rows + kWarps - 1) / kWarps;
-  relation_adam_kernel<<<blocks, kWarps * 32, 0, lc.stream>>>(a, t, hp, bc);
+  launch_pdl(relation_adam_kernel, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
   return 1;
 }
 
@@ -169,7 +172,7 @@ int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, const A
                       const float* bc, const LaunchCtx& lc) {
   if (n <= 0) return 0;
   const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, lc.num_sms * 8));
-  dense_adam_kernel<<<blocks, 256, 0, lc.stream>>>(w, m, v, g, n, hp, bc);
+  launch_pdl(dense_adam_kernel, dim3(blocks), dim3(256), 0, lc.stream, 1, w, m, v, g, n, hp, bc);
   return 1;
 }
 

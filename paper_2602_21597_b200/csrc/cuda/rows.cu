@@ -22,6 +22,7 @@ __device__ __forceinline__ bool bad_index(const DevArgs& a, int32_t id, int32_t 
 
 __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, int first, int n,
                                                             int n_entities) {
+  pdl_start();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
@@ -45,6 +46,7 @@ __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, 
 
 __global__ void __launch_bounds__(kWarps * 32) project_kernel(DevArgs a, int dir, int first, int n,
                                                               int n_relations) {
+  pdl_start();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
@@ -100,6 +102,7 @@ __global__ void __launch_bounds__(kWarps * 32) project_kernel(DevArgs a, int dir
 }
 
 __global__ void __launch_bounds__(kWarps * 32) negate_kernel(DevArgs a, int dir, int first, int n) {
+  pdl_start();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(kWarps * 32) negate_kernel(DevArgs a, int dir,
 
 __global__ void __launch_bounds__(kWarps * 32) union_kernel(DevArgs a, int dir, int k, int first,
                                                             int n) {
+  pdl_start();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
@@ -147,6 +151,7 @@ __global__ void __launch_bounds__(kWarps * 32) union_kernel(DevArgs a, int dir, 
 // Loss mirror: the fused Loss forward already produced dL/dq (non-union) or
 // dL/dd (union); the mirror materialises it into its planned arena slot.
 __global__ void __launch_bounds__(kWarps * 32) loss_bwd_kernel(DevArgs a, int first, int n) {
+  pdl_start();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
@@ -166,23 +171,23 @@ inline int blocks_for(int n) { return (n + kWarps - 1) / kWarps; }
 }  // namespace
 
 int launch_embed(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc) {
-  embed_kernel<<<blocks_for(n), kWarps * 32, 0, lc.stream>>>(a, dir, first, n, a.n_entities);
+  launch_pdl(embed_kernel, dim3(blocks_for(n)), dim3(kWarps * 32), 0, lc.stream, 1, a, dir, first, n, a.n_entities);
   return 1;
 }
 int launch_project(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc) {
-  project_kernel<<<blocks_for(n), kWarps * 32, 0, lc.stream>>>(a, dir, first, n, a.n_relations);
+  launch_pdl(project_kernel, dim3(blocks_for(n)), dim3(kWarps * 32), 0, lc.stream, 1, a, dir, first, n, a.n_relations);
   return 1;
 }
 int launch_negate(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc) {
-  negate_kernel<<<blocks_for(n), kWarps * 32, 0, lc.stream>>>(a, dir, first, n);
+  launch_pdl(negate_kernel, dim3(blocks_for(n)), dim3(kWarps * 32), 0, lc.stream, 1, a, dir, first, n);
   return 1;
 }
 int launch_union(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc) {
-  union_kernel<<<blocks_for(n), kWarps * 32, 0, lc.stream>>>(a, dir, k, first, n);
+  launch_pdl(union_kernel, dim3(blocks_for(n)), dim3(kWarps * 32), 0, lc.stream, 1, a, dir, k, first, n);
   return 1;
 }
 int launch_loss_bwd(const DevArgs& a, int first, int n, const LaunchCtx& lc) {
-  loss_bwd_kernel<<<blocks_for(n), kWarps * 32, 0, lc.stream>>>(a, first, n);
+  launch_pdl(loss_bwd_kernel, dim3(blocks_for(n)), dim3(kWarps * 32), 0, lc.stream, 1, a, first, n);
   return 1;
 }
 

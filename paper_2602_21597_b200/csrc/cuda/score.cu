@@ -14,6 +14,8 @@
 //   psi_neg = -log sigma(d_neg - gamma) = softplus(gamma - d_neg), mean over K
 //   GQE distance: ||v - q||_1                                     (SURVEY A-7)
 //   Q2B distance: ||max(0,|v-c|-o)||_1 + alpha ||min(|v-c|,o)||_1
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ngdb_dev {
@@ -209,15 +211,17 @@ __device__ __forceinline__ float ld_peer(const float* local, uint32_t peer) {
   return v;
 }
 
-// A (2,1,1) cluster per Loss node: the two CTAs take alternate candidate
-// groups, then CTA 0 adds CTA 1's dL/dq and loss partials over DSMEM (fixed
-// order: own + peer, so the result is deterministic).
+// A (S,1,1) cluster per Loss node (S = 2..8, chosen so a pop fills the GPU):
+// the CTAs take candidate groups round-robin, then reduce-scatter their dL/dq
+// partials over DSMEM — CTA p sums dims [p*wq/S, (p+1)*wq/S) over all S
+// partials in rank order (deterministic); CTA 0 sums the loss partials.
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first) {
+__global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first, int S) {
+  pdl_start();
   __shared__ __align__(16) float red[2 * 1024];
   __shared__ float lred[kWarps + 1];
-  const int part = blockIdx.x & 1;
-  const ngdb_node_desc d = a.nodes[first + (blockIdx.x >> 1)];
+  const int part = blockIdx.x % S;
+  const ngdb_node_desc d = a.nodes[first + blockIdx.x / S];
   const int qi = d.id;
   if (d.aux < 0) {
     // union query: the input already holds min-over-branch distances
@@ -255,28 +259,35 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
         if (lane == 0) coefs[j] = c;
         return c;
       },
-      part, 2);
+      part, S);
   loss = block_sum(lane == 0 ? loss : 0.f, lred);
   if (threadIdx.x == 0) lred[kWarps] = loss;
   reduce_dq<BB, NCH>(a, L, red, nullptr);
   cluster_sync_all();
-  if (part == 0) {
+  {
     float* dst = a.dqbuf + static_cast<int64_t>(d.aux) * a.wq;
-    for (int e = threadIdx.x; e < a.wq; e += kThreads) dst[e] = red[e] + ld_peer(red + e, 1);
-    if (threadIdx.x == 0) {
-      const float total = lred[kWarps] + ld_peer(lred + kWarps, 1);
+    const int e0 = part * a.wq / S, e1 = (part + 1) * a.wq / S;
+    for (int e = e0 + threadIdx.x; e < e1; e += kThreads) {
+      float v = 0.f;
+      for (int p = 0; p < S; ++p) v += (p == part) ? red[e] : ld_peer(red + e, p);
+      dst[e] = v;
+    }
+    if (part == 0 && threadIdx.x == 0) {
+      float total = 0.f;
+      for (int p = 0; p < S; ++p) total += (p == 0) ? lred[kWarps] : ld_peer(lred + kWarps, p);
       a.loss_out[qi] = total;
       a.arena[d.out] = total;
       if (!isfinite(total)) atomicOr(&a.flags[0], 1);
     }
   }
-  cluster_sync_all();  // CTA 1 stays resident until its partials were read
+  cluster_sync_all();  // partial tiles stay resident until every slice was read
 }
 
 // Union branch Score: fwd writes the distance vector; bwd turns the routed
 // dL/dd into coef (for the optimizer) and dL/dq (its G slot).
 template <int BB, int NCH>
 __global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int first) {
+  pdl_start();
   __shared__ __align__(16) float red[2 * 1024];
   const ngdb_node_desc d = a.nodes[first + blockIdx.x];
   const float* q = a.arena + d.in[0];
@@ -305,24 +316,17 @@ __global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int
 
 template <int NCH>
 void launch_loss_nch(const DevArgs& a, int first, int n, cudaStream_t s) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * n);  // a CTA pair (cluster of 2) per Loss node
-  cfg.blockDim = dim3(kThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (a.backbone == NGDB_GQE) cudaLaunchKernelEx(&cfg, loss_fwd_kernel<NGDB_GQE, NCH>, a, first);
-  else cudaLaunchKernelEx(&cfg, loss_fwd_kernel<NGDB_Q2B, NCH>, a, first);
+  // cluster size: enough CTAs for ~4 per SM, 2..8 per node (portable limit)
+  const int S = std::max(2, std::min(8, (4 * 148 + n - 1) / std::max(n, 1)));
+  if (a.backbone == NGDB_GQE)
+    launch_pdl(loss_fwd_kernel<NGDB_GQE, NCH>, dim3(S * n), dim3(kThreads), 0, s, S, a, first, S);
+  else
+    launch_pdl(loss_fwd_kernel<NGDB_Q2B, NCH>, dim3(S * n), dim3(kThreads), 0, s, S, a, first, S);
 }
 template <int NCH>
 void launch_score_nch(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
-  if (a.backbone == NGDB_GQE) score_kernel<NGDB_GQE, NCH><<<n, kThreads, 0, s>>>(a, dir, first);
-  else score_kernel<NGDB_Q2B, NCH><<<n, kThreads, 0, s>>>(a, dir, first);
+  if (a.backbone == NGDB_GQE) launch_pdl(score_kernel<NGDB_GQE, NCH>, dim3(n), dim3(kThreads), 0, s, 1, a, dir, first);
+  else launch_pdl(score_kernel<NGDB_Q2B, NCH>, dim3(n), dim3(kThreads), 0, s, 1, a, dir, first);
 }
 
 int launch_loss_fwd(const DevArgs& a, int first, int n, const LaunchCtx& lc) {

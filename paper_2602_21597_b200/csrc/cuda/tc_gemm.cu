@@ -196,6 +196,8 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
+  // barrier init, TMEM allocation and copy planning overlap the previous kernel
+  pdl_start();
   float acc[kHalfCols];
 #pragma unroll
   for (int j = 0; j < kHalfCols; ++j) acc[j] = 0.f;
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
 // --- operand split / transpose ------------------------------------------------
 __global__ void split_kernel(const float* src, int rows, int cols, int ld, int relu, float* hi,
                              float* lo) {
+  pdl_start();
   const int64_t n = (int64_t)rows * cols;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -322,6 +325,7 @@ __global__ void split_kernel(const float* src, int rows, int cols, int ld, int r
 
 // dst[c][r] (row stride pad4(rows), zero padded) = split(op(src[r][c]))
 __global__ void split_t_multi_kernel(SplitJobs jobs) {
+  pdl_start();
   __shared__ float tile[32][33];
   const SplitJob& j = jobs.job[blockIdx.z];
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
@@ -377,19 +381,7 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
   b.S = std::max(1, std::min({8, (2 * num_sms) / std::max(tiles, 1), max_chunks / 2}));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(tiles * b.S);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = b.S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, tc_gemm_kernel, b);
+  launch_pdl(tc_gemm_kernel, dim3(tiles * b.S), dim3(kThreads), SMEM_BYTES, s, b.S, b);
   return 1;
 }
 
@@ -404,7 +396,7 @@ int split_transposed(const SplitJobs& jobs, cudaStream_t s) {
   }
   if (mr <= 0 || mc <= 0) return 0;
   dim3 grid((mc + 31) / 32, (mr + 31) / 32, jobs.n);
-  split_t_multi_kernel<<<grid, dim3(32, 8), 0, s>>>(jobs);
+  launch_pdl(split_t_multi_kernel, dim3(grid), dim3(dim3(32, 8)), 0, s, 1, jobs);
   return 1;
 }
 
@@ -414,7 +406,7 @@ int split_matrix(const float* src, int rows, int cols, int ld_src, int transpose
   if (!transpose) {
     const int64_t n = (int64_t)rows * cols;
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    split_kernel<<<blocks, 256, 0, s>>>(src, rows, cols, ld_src, relu, dst_hi, dst_lo);
+    launch_pdl(split_kernel, dim3(blocks), dim3(256), 0, s, 1, src, rows, cols, ld_src, relu, dst_hi, dst_lo);
     return 1;
   }
   SplitJobs jobs{};
