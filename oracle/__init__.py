@@ -47,12 +47,16 @@ _SIG = {
     "oracle_model_margins": (C.c_int, [C.c_void_p, P(f64), i32]),
     "oracle_q2b_distance": (f64, [P(f64), P(f64), P(f64), i32, f64]),
     "oracle_loss": (f64, [f64, f64, P(f64), i32]),
+    "oracle_lgamma": (f64, [f64]),
+    "oracle_digamma": (f64, [f64]),
+    "oracle_trigamma": (f64, [f64]),
+    "oracle_beta_kl": (f64, [f64, f64, f64, f64]),
 }
 for _n, (_r, _a) in _SIG.items():
     _f = getattr(lib, _n)
     _f.restype, _f.argtypes = _r, _a
 
-BACKBONES = {"gqe": 0, "q2b": 1}
+BACKBONES = {"gqe": 0, "q2b": 1, "betae": 2}
 
 
 def _p(a, t):
@@ -168,3 +172,19 @@ def q2b_distance(v, c, o, alpha=0.02):
 def loss(gamma, d_pos, d_neg):
     dn = np.ascontiguousarray(d_neg, dtype=np.float64)
     return lib.oracle_loss(gamma, d_pos, _p(dn, f64), len(dn))
+
+
+def lgamma(x):
+    return lib.oracle_lgamma(float(x))
+
+
+def digamma(x):
+    return lib.oracle_digamma(float(x))
+
+
+def trigamma(x):
+    return lib.oracle_trigamma(float(x))
+
+
+def beta_kl(a1, b1, a2, b2):
+    return lib.oracle_beta_kl(float(a1), float(b1), float(a2), float(b2))

@@ -60,6 +60,11 @@ int oracle_model_destroy(void* m);
 double oracle_q2b_distance(const double* v, const double* c, const double* o, int32_t d,
                            double alpha);
 double oracle_loss(double gamma, double d_pos, const double* d_neg, int32_t k);
+/* BetaE special functions and KL(Beta(a1,b1) || Beta(a2,b2)) */
+double oracle_lgamma(double x);
+double oracle_digamma(double x);
+double oracle_trigamma(double x);
+double oracle_beta_kl(double a1, double b1, double a2, double b2);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,17 @@ void get_tensor(Model<R>& md, const char* name, double* out, int64_t n) {
   for (int64_t i = 0; i < n; ++i) out[i] = double(v[i]);
 }
 
+// special functions: NaN (and oracle_last_error) on DomainError
+template <class F>
+double special(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return std::nan("");
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -217,7 +228,7 @@ int oracle_build_dag(int32_t b, const int32_t* patterns, const int32_t* anchors,
 int oracle_model_create(int32_t backbone, int32_t ne, int32_t nr, int32_t dim, int32_t k,
                         double gamma, double alpha, double lr, int32_t precision, void** out) {
   return guard([&] {
-    if (backbone != 0 && backbone != 1) throw std::runtime_error("backbone not restated");
+    if (backbone < 0 || backbone > 2) throw std::runtime_error("backbone not restated");
     auto* a = new AnyModel();
     a->precision = precision;
     auto setup = [&](auto& md) {
@@ -328,6 +339,13 @@ double oracle_q2b_distance(const double* v, const double* c, const double* o, in
     q[d + i] = o[i];
   }
   return md.dist(q.data(), v);
+}
+
+double oracle_lgamma(double x) { return special([&] { return sp_lgamma(x); }); }
+double oracle_digamma(double x) { return special([&] { return sp_digamma(x); }); }
+double oracle_trigamma(double x) { return special([&] { return sp_trigamma(x); }); }
+double oracle_beta_kl(double a1, double b1, double a2, double b2) {
+  return special([&] { return beta_kl(a1, b1, a2, b2); });
 }
 
 double oracle_loss(double gamma, double d_pos, const double* d_neg, int32_t k) {

@@ -5,7 +5,8 @@
 //                 (SPEC.md:463-471, 499-500, 510); pop_cardinality_classes
 //                 (SPEC.md:481-489); release Eq. 7
 //   arena         alloc/release with size-class free list
-//   kernels       GQE SPEC.md:359-376; Q2B SPEC.md:377-385; union SPEC.md:404-412;
+//   kernels       GQE SPEC.md:359-376; Q2B SPEC.md:377-385; BetaE SPEC.md:386-403
+//                 (forms of SURVEY A-7); union SPEC.md:404-412;
 //                 loss SPEC.md:541-549 with psi per SPEC.md:431
 //   adam          SPEC.md:550-558 (dense) and the lazy touched-row variant (A-9)
 // Every kernel runs node by node (the "looped" form); batching only changes
@@ -17,12 +18,13 @@
 #include <stdexcept>
 
 #include "oracle_internal.hpp"
+#include "special.hpp"
 
 namespace oracle {
 
 template <class R>
 struct Model {
-  int backbone = 0;  // 0 GQE, 1 Q2B
+  int backbone = 0;  // 0 GQE, 1 Q2B, 2 BetaE
   int ne = 0, nr = 0, d = 0, k = 0;
   double gamma = 12.0, alpha = 0.02, lr = 1e-4, b1 = 0.9, b2 = 0.999, eps = 1e-8;
   int wq = 0, ew = 0, rw = 0;
@@ -43,7 +45,7 @@ struct Model {
     d = d_;
     k = k_;
     wq = bb == 0 ? d : 2 * d;
-    ew = d;
+    ew = bb == 2 ? 2 * d : d;
     rw = bb == 1 ? 2 * d : d;
     auto add = [&](const std::string& n, int64_t r, int64_t c, bool sp) {
       names.push_back(n);
@@ -59,6 +61,16 @@ struct Model {
     if (bb == 0) {
       add("int_w1", d, d, false);
       add("int_w2", d, d, false);
+    } else if (bb == 2) {
+      // projection MLP [q (2d) | r (d)] -> 2d -> 2d; attention MLP 2d -> 2d -> d
+      add("prj_w1", 2 * d, 3 * d, false);
+      add("prj_b1", 1, 2 * d, false);
+      add("prj_w2", 2 * d, 2 * d, false);
+      add("prj_b2", 1, 2 * d, false);
+      add("att_w1", 2 * d, 2 * d, false);
+      add("att_b1", 1, 2 * d, false);
+      add("att_w2", d, 2 * d, false);
+      add("att_b2", 1, d, false);
     } else {
       for (const char* n : {"att_w1", "att_b1", "att_w2", "att_b2", "off_w1", "off_b1", "off_w2",
                             "off_b2"})
@@ -67,9 +79,23 @@ struct Model {
   }
 
   // ---- distances -----------------------------------------------------------
+  static R softplus(R x) { return x > 0 ? x + std::log1p(std::exp(-x)) : std::log1p(std::exp(x)); }
+  static R sigm(R x) { return x >= 0 ? R(1) / (R(1) + std::exp(-x)) : std::exp(x) / (R(1) + std::exp(x)); }
   static R sgn(R x) { return R((x > 0) - (x < 0)); }
+  // BetaE: realised Beta parameter clamp(softplus(x), 0.05, 1e9) (SURVEY A-7)
+  static R bclamp(R x) { return std::min(std::max(x, R(0.05)), R(1e9)); }
+  static R realize(R x) { return bclamp(softplus(x)); }
+  static R drealize(R x) {  // d realize / dx (0 where the clamp binds)
+    const R sp = softplus(x);
+    return (sp > R(0.05) && sp < R(1e9)) ? sigm(x) : R(0);
+  }
   R dist(const R* q, const R* v) const {
     R s = 0;
+    if (backbone == 2) {  // sum over dims of KL(entity || query)
+      for (int e = 0; e < d; ++e)
+        s += beta_kl(realize(v[e]), realize(v[d + e]), q[e], q[d + e]);
+      return s;
+    }
     if (backbone == 0) {
       for (int e = 0; e < d; ++e) s += std::fabs(v[e] - q[e]);
     } else {
@@ -82,6 +108,21 @@ struct Model {
   }
   // gq += coef * d dist / dq ; gv += coef * d dist / dv
   void ddist(const R* q, const R* v, R coef, R* gq, R* gv) const {
+    if (backbone == 2) {
+      for (int e = 0; e < d; ++e) {
+        R g[4];
+        beta_kl_grad(realize(v[e]), realize(v[d + e]), q[e], q[d + e], g);
+        if (gv) {
+          gv[e] += coef * g[0] * drealize(v[e]);
+          gv[d + e] += coef * g[1] * drealize(v[d + e]);
+        }
+        if (gq) {
+          gq[e] += coef * g[2];
+          gq[d + e] += coef * g[3];
+        }
+      }
+      return;
+    }
     for (int e = 0; e < d; ++e) {
       const R delta = v[e] - q[e];
       if (backbone == 0) {
@@ -98,8 +139,6 @@ struct Model {
       }
     }
   }
-  static R softplus(R x) { return x > 0 ? x + std::log1p(std::exp(-x)) : std::log1p(std::exp(x)); }
-  static R sigm(R x) { return x >= 0 ? R(1) / (R(1) + std::exp(-x)) : std::exp(x) / (R(1) + std::exp(x)); }
   // loss of one query from its 1+k distances; coef = dloss/dd
   R loss_and_coef(const R* dists, R* coef) const {
     R l = softplus(dists[0] - R(gamma));
@@ -123,21 +162,23 @@ struct Model {
   // ---- small dense algebra: y = W x (+b), W [out][in] -----------------------
   void mv(const std::string& w, const std::string& b, const R* x, R* y) const {
     const auto& W = P.at(w);
-    for (int o = 0; o < d; ++o) {
+    const auto [rows, cols] = shape.at(w);
+    for (int64_t o = 0; o < rows; ++o) {
       R s = b.empty() ? R(0) : P.at(b)[o];
-      for (int i = 0; i < d; ++i) s += W[(int64_t)o * d + i] * x[i];
+      for (int64_t i = 0; i < cols; ++i) s += W[o * cols + i] * x[i];
       y[o] = s;
     }
   }
   // gx += W^T gy ; gW += gy x^T ; gb += gy
   void mv_bwd(const std::string& w, const std::string& b, const R* x, const R* gy, R* gx) {
     const auto& W = P.at(w);
+    const auto [rows, cols] = shape.at(w);
     auto& gW = G[w];
-    for (int o = 0; o < d; ++o) {
+    for (int64_t o = 0; o < rows; ++o) {
       if (!b.empty()) G[b][o] += gy[o];
-      for (int i = 0; i < d; ++i) {
-        gW[(int64_t)o * d + i] += gy[o] * x[i];
-        if (gx) gx[i] += W[(int64_t)o * d + i] * gy[o];
+      for (int64_t i = 0; i < cols; ++i) {
+        gW[o * cols + i] += gy[o] * x[i];
+        if (gx) gx[i] += W[o * cols + i] * gy[o];
       }
     }
   }
@@ -260,6 +301,105 @@ struct Model {
     }
   }
 
+  // ---- BetaE (forms DESIGN.md §3.5) --------------------------
+  // project: out = realize(W2 relu(W1 [q | r] + b1) + b2)
+  struct BetaProj {
+    std::vector<R> x, h, a, z;
+  };
+  void beta_proj_fwd(const R* in, const R* r, R* out, BetaProj* keep = nullptr) {
+    BetaProj t;
+    t.x.assign(in, in + 2 * d);
+    t.x.insert(t.x.end(), r, r + d);
+    t.h.resize(2 * d);
+    t.a.resize(2 * d);
+    t.z.resize(2 * d);
+    mv("prj_w1", "prj_b1", t.x.data(), t.h.data());
+    for (int e = 0; e < 2 * d; ++e) t.a[e] = std::max(t.h[e], R(0));
+    mv("prj_w2", "prj_b2", t.a.data(), t.z.data());
+    if (out)
+      for (int e = 0; e < 2 * d; ++e) out[e] = realize(t.z[e]);
+    if (keep) *keep = std::move(t);
+  }
+  void beta_proj_bwd(const R* in, const R* r, const R* gy, R* gin, R* gr) {
+    BetaProj t;
+    beta_proj_fwd(in, r, nullptr, &t);
+    std::vector<R> gz(2 * d), ga(2 * d, R(0)), gx(3 * d, R(0));
+    for (int e = 0; e < 2 * d; ++e) gz[e] = gy[e] * drealize(t.z[e]);
+    mv_bwd("prj_w2", "prj_b2", t.a.data(), gz.data(), ga.data());
+    for (int e = 0; e < 2 * d; ++e) ga[e] = t.h[e] > 0 ? ga[e] : R(0);
+    mv_bwd("prj_w1", "prj_b1", t.x.data(), ga.data(), gx.data());
+    for (int e = 0; e < 2 * d; ++e) gin[e] = gx[e];
+    for (int e = 0; e < d; ++e) gr[e] += gx[2 * d + e];
+  }
+  // intersect: w = softmax_l(A2 relu(A1 q_l + a1) + a2) per dim;
+  // alpha = sum_l w_l alpha_l, beta = sum_l w_l beta_l (a convex combination of
+  // clamped values, so the SPEC's re-clamp is the identity)
+  struct BetaInter {
+    std::vector<std::vector<R>> z, s;
+  };
+  void beta_inter_fwd(const std::vector<const R*>& xs, R* out, BetaInter* keep = nullptr) {
+    const int kk = (int)xs.size();
+    BetaInter t;
+    t.z.assign(kk, std::vector<R>(2 * d));
+    t.s.assign(kk, std::vector<R>(d));
+    std::vector<R> rz(2 * d);
+    for (int l = 0; l < kk; ++l) {
+      mv("att_w1", "att_b1", xs[l], t.z[l].data());
+      for (int e = 0; e < 2 * d; ++e) rz[e] = std::max(t.z[l][e], R(0));
+      mv("att_w2", "att_b2", rz.data(), t.s[l].data());
+    }
+    if (out)
+      for (int e = 0; e < d; ++e) {
+        R mx = t.s[0][e];
+        for (int l = 1; l < kk; ++l) mx = std::max(mx, t.s[l][e]);
+        R z = 0, al = 0, be = 0;
+        for (int l = 0; l < kk; ++l) z += std::exp(t.s[l][e] - mx);
+        for (int l = 0; l < kk; ++l) {
+          const R w = std::exp(t.s[l][e] - mx) / z;
+          al += w * xs[l][e];
+          be += w * xs[l][d + e];
+        }
+        out[e] = al;
+        out[d + e] = be;
+      }
+    if (keep) *keep = t;
+  }
+  void beta_inter_bwd(const std::vector<const R*>& xs, const R* gy, R* gout) {
+    const int kk = (int)xs.size();
+    BetaInter t;
+    beta_inter_fwd(xs, nullptr, &t);
+    for (int64_t i = 0; i < (int64_t)kk * 2 * d; ++i) gout[i] = R(0);
+    std::vector<std::vector<R>> gs(kk, std::vector<R>(d));
+    for (int e = 0; e < d; ++e) {
+      R mx = t.s[0][e];
+      for (int l = 1; l < kk; ++l) mx = std::max(mx, t.s[l][e]);
+      std::vector<R> w(kk), gw(kk);
+      R z = 0, dot = 0;
+      for (int l = 0; l < kk; ++l) z += (w[l] = std::exp(t.s[l][e] - mx));
+      const R gA = gy[e], gB = gy[d + e];
+      for (int l = 0; l < kk; ++l) {
+        w[l] /= z;
+        gw[l] = gA * xs[l][e] + gB * xs[l][d + e];
+        dot += w[l] * gw[l];
+      }
+      for (int l = 0; l < kk; ++l) {
+        gs[l][e] = w[l] * (gw[l] - dot);
+        gout[(int64_t)l * 2 * d + e] += gA * w[l];
+        gout[(int64_t)l * 2 * d + d + e] += gB * w[l];
+      }
+    }
+    std::vector<R> rz(2 * d), tmp(2 * d), gc(2 * d);
+    for (int l = 0; l < kk; ++l) {
+      for (int e = 0; e < 2 * d; ++e) rz[e] = std::max(t.z[l][e], R(0));
+      std::fill(tmp.begin(), tmp.end(), R(0));
+      mv_bwd("att_w2", "att_b2", rz.data(), gs[l].data(), tmp.data());
+      for (int e = 0; e < 2 * d; ++e) tmp[e] = t.z[l][e] > 0 ? tmp[e] : R(0);
+      std::fill(gc.begin(), gc.end(), R(0));
+      mv_bwd("att_w1", "att_b1", xs[l], tmp.data(), gc.data());
+      for (int e = 0; e < 2 * d; ++e) gout[(int64_t)l * 2 * d + e] += gc[e];
+    }
+  }
+
   // ---- Adam -------------------------------------------------
   void adam(int64_t step, bool lazy) {
     const double bc1 = 1.0 - std::pow(b1, (double)step), bc2 = 1.0 - std::pow(b2, (double)step);
@@ -356,6 +496,7 @@ struct Exec {
     switch (kind) {
       case K_INTER: case K_SCORE: case K_UNION: case K_LOSS: return true;
       case K_PROJ: return md.backbone != 0;
+      case K_NEG: return md.backbone == 2;
       default: return false;
     }
   }
@@ -392,6 +533,10 @@ struct Exec {
   // nearest non-differentiable point the query's forward pass touched.
   void kink(int q, double v) { md.margin[q] = std::min(md.margin[q], std::fabs(v)); }
   void dist_kinks(int qi, const R* q, const R* v) {
+    if (md.backbone == 2) {  // KL is smooth; only the entity clamp has kinks
+      for (int e = 0; e < 2 * md.d; ++e) kink(qi, double(Model<R>::softplus(v[e])) - 0.05);
+      return;
+    }
     for (int e = 0; e < md.d; ++e) {
       const double delta = double(v[e]) - double(q[e]);
       kink(qi, delta);                                                       // sign(v - c)
@@ -406,12 +551,28 @@ struct Exec {
     switch (x.kind) {
       case K_EMB: {
         const R* e = md.erow(x.payload);
+        if (md.backbone == 2) {
+          for (int i = 0; i < md.ew; ++i) {
+            out[i] = Model<R>::realize(e[i]);
+            kink(x.query, double(Model<R>::softplus(e[i])) - 0.05);
+          }
+          break;
+        }
         for (int i = 0; i < md.ew; ++i) out[i] = e[i];
         break;
       }
       case K_PROJ: {
         const R* in = t(T[x.in[0]]);
         const R* r = &md.P["relation"][(int64_t)x.payload * md.rw];
+        if (md.backbone == 2) {
+          typename Model<R>::BetaProj keep;
+          md.beta_proj_fwd(in, r, out, &keep);
+          for (int e = 0; e < 2 * d; ++e) {
+            kink(x.query, keep.h[e]);
+            kink(x.query, double(Model<R>::softplus(keep.z[e])) - 0.05);
+          }
+          break;
+        }
         for (int i = 0; i < d; ++i) out[i] = in[i] + r[i];
         if (md.backbone == 1)
           for (int i = 0; i < d; ++i) {
@@ -422,6 +583,13 @@ struct Exec {
       }
       case K_NEG: {
         const R* in = t(T[x.in[0]]);
+        if (md.backbone == 2) {  // (alpha, beta) -> (1/alpha, 1/beta), re-clamped
+          for (int i = 0; i < md.wq; ++i) {
+            out[i] = Model<R>::bclamp(R(1) / in[i]);
+            kink(x.query, double(R(1) / in[i]) - 0.05);
+          }
+          break;
+        }
         for (int i = 0; i < md.wq; ++i) out[i] = i < d ? -in[i] : in[i];
         break;
       }
@@ -432,6 +600,11 @@ struct Exec {
           std::vector<R> mh;
           md.gqe_inter_fwd(xs, out, &mh);
           for (int e = 0; e < d; ++e) kink(x.query, mh[d + e]);  // relu(W1 m)
+        } else if (md.backbone == 2) {
+          typename Model<R>::BetaInter keep;
+          md.beta_inter_fwd(xs, out, &keep);
+          for (size_t l = 0; l < xs.size(); ++l)
+            for (int e = 0; e < 2 * d; ++e) kink(x.query, keep.z[l][e]);
         } else {
           typename Model<R>::Q2bInter keep;
           md.q2b_inter_fwd(xs, out, &keep);
@@ -497,12 +670,21 @@ struct Exec {
     switch (m.kind) {
       case K_EMB: {
         R* ge = md.gerow(m.payload);
+        if (md.backbone == 2) {
+          const R* e = md.erow(m.payload);
+          for (int i = 0; i < md.ew; ++i) ge[i] += gin[i] * Model<R>::drealize(e[i]);
+          break;
+        }
         for (int i = 0; i < md.ew; ++i) ge[i] += gin[i];
         break;
       }
       case K_PROJ: {
         const R* r = &md.P["relation"][(int64_t)m.payload * md.rw];
         R* gr = md.grrow(m.payload);
+        if (md.backbone == 2) {
+          md.beta_proj_bwd(t(T[m.in[0]]), r, gin, gout, gr);
+          break;
+        }
         for (int i = 0; i < d; ++i) {
           gout[i] = gin[i];
           gr[i] += gin[i];
@@ -517,12 +699,21 @@ struct Exec {
         break;
       }
       case K_NEG:
+        if (md.backbone == 2) {
+          const R* in = t(T[m.in[0]]);
+          for (int i = 0; i < md.wq; ++i) {
+            const R inv = R(1) / in[i];
+            gout[i] = (inv > R(0.05) && inv < R(1e9)) ? -gin[i] * inv * inv : R(0);
+          }
+          break;
+        }
         for (int i = 0; i < md.wq; ++i) gout[i] = i < d ? -gin[i] : gin[i];
         break;
       case K_INTER: {
         std::vector<const R*> xs;
         for (int i : m.in) xs.push_back(t(T[i]));
         if (md.backbone == 0) md.gqe_inter_bwd(xs, gin, gout);
+        else if (md.backbone == 2) md.beta_inter_bwd(xs, gin, gout);
         else md.q2b_inter_bwd(xs, gin, gout);
         break;
       }

@@ -19,6 +19,10 @@ enum DenseName : int {
   // Q2B attention (centre) and DeepSets (offset) MLPs
   Q2B_A1 = 0, Q2B_A1B = 1, Q2B_A2 = 2, Q2B_A2B = 3,
   Q2B_V1 = 4, Q2B_V1B = 5, Q2B_V2 = 6, Q2B_V2B = 7,
+  // BetaE projection MLP [q | r] -> 2d -> 2d and attention MLP 2d -> 2d -> d
+  //
+  BETA_P1 = 0, BETA_P1B = 1, BETA_P2 = 2, BETA_P2B = 3,
+  BETA_A1 = 4, BETA_A1B = 5, BETA_A2 = 6, BETA_A2B = 7,
 };
 
 // Everything a kernel needs, passed by value.
@@ -56,6 +60,14 @@ struct DevArgs {
   int32_t* flags;     // [0] non-finite loss, [1] index out of range
   float* scratch;     // GEMM scratch
   int64_t scratch_cap;
+  // BetaE per-step entity table: for every touched entity row
+  // r (the optimizer CSR order) etab[r] = [psi(s)-psi(a) | psi(s)-psi(b)] and
+  // etab_c[r] = sum_e (-lnB(a,b) + a psi(a) + b psi(b) - s psi(s)), so that
+  // KL(entity || query) = lnB(query) + etab_c[r] + <query, etab[r]>.
+  // cand_local[slot*ncand + j] = CSR row of candidate j of score slot `slot`.
+  float* etab;
+  float* etab_c;
+  int32_t* cand_local;
 };
 
 // Programmatic dependent launch: let the next kernel in the stream start its
@@ -140,6 +152,10 @@ int launch_loss_bwd(const DevArgs& a, int first, int n, const LaunchCtx& lc);
 // score.cu
 int launch_loss_fwd(const DevArgs& a, int first, int n, const LaunchCtx& lc);
 int launch_score(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
+// beta.cu (BetaE backbone)
+int launch_beta_project(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
+int launch_beta_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc);
+int64_t beta_scratch_floats(int dim, int max_nodes);
 // intersect.cu
 int launch_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc);
 // scratch floats the intersect operators need for classes of up to max_nodes
@@ -162,6 +178,10 @@ int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const Adam
                               const float* bc, const LaunchCtx& lc);
 int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
                                 const float* bc, const LaunchCtx& lc);
+// BetaE: per-step entity table + candidate -> CSR-row map (before any pool)
+int launch_beta_prep(const DevArgs& a, const SparseTable& t, const LaunchCtx& lc);
+int launch_beta_entity_adam(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
+                            const float* bc, const LaunchCtx& lc);
 int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, const AdamHyper& hp,
                       const float* bc, const LaunchCtx& lc);
 }  // namespace ngdb_dev

@@ -49,11 +49,11 @@ int guarded(F&& f) {
 
 enum Family : int {
   F_EMBED = 0, F_PROJECT, F_NEGATE, F_INTERSECT, F_SCORE, F_UNION, F_LOSS_FWD, F_LOSS_BWD,
-  F_OPT_ENTITY, F_OPT_RELATION, F_OPT_DENSE, F_COUNT
+  F_OPT_ENTITY, F_OPT_RELATION, F_OPT_DENSE, F_ENTITY_PREP, F_COUNT
 };
 const char* kFamilyNames[F_COUNT] = {"embed",     "project",   "negate",      "intersect",
                                      "score",     "union",     "loss_fwd",    "loss_bwd",
-                                     "opt_entity", "opt_relation", "opt_dense"};
+                                     "opt_entity", "opt_relation", "opt_dense", "entity_prep"};
 
 struct Param {
   std::string name;
@@ -179,6 +179,10 @@ struct ngdb_ctx {
   int64_t scratch_cap = 0;
   float* arena = nullptr;
   int64_t arena_cap = 0;
+  // BetaE per-step entity table (beta.cu) and candidate -> CSR-row map
+  float *etab = nullptr, *etab_c = nullptr;
+  int32_t* cand_local = nullptr;
+  int64_t cap_erows = 0;
   // streaming plans: double-buffered pinned staging + device blobs
   int32_t* staging[2] = {nullptr, nullptr};
   int64_t staging_cap[2] = {0, 0};
@@ -211,6 +215,7 @@ struct ngdb_ctx {
   int32_t query_width() const {
     return desc.backbone == NGDB_GQE ? desc.dim : 2 * desc.dim;
   }
+  bool beta() const { return desc.backbone == NGDB_BETAE; }
   cudaEvent_t take_event() {
     if (!event_pool.empty()) {
       cudaEvent_t e = event_pool.back();
@@ -279,6 +284,19 @@ void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
     realloc_f(c->agbuf, c->cap_anchor * ew);
     realloc_f(c->rgbuf, c->cap_project * rw);
     realloc_f(c->loss_out, c->cap_queries);
+    if (c->beta()) {
+      if (c->cand_local) CK(cudaFree(c->cand_local));
+      c->cand_local = dmalloc<int32_t>(c->cap_score * c->cap_cand);
+    }
+    ++c->buffer_gen;
+  }
+  if (c->beta() && m.n_erows > c->cap_erows) {
+    CK(cudaStreamSynchronize(c->stream));
+    c->cap_erows = std::max<int64_t>(m.n_erows, c->cap_erows + c->cap_erows / 4);
+    if (c->etab) CK(cudaFree(c->etab));
+    if (c->etab_c) CK(cudaFree(c->etab_c));
+    c->etab = dmalloc<float>(c->cap_erows * ew);
+    c->etab_c = dmalloc<float>(c->cap_erows);
     ++c->buffer_gen;
   }
   if (m.arena_elems > c->arena_cap) {
@@ -323,6 +341,9 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.flags = c->flags;
   a.scratch = c->scratch;
   a.scratch_cap = c->scratch_cap;
+  a.etab = c->etab;
+  a.etab_c = c->etab_c;
+  a.cand_local = c->cand_local;
   return a;
 }
 
@@ -384,6 +405,8 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d) {
       timed(c, fam, bytes, [&] { return launch_embed(a, d.dir, d.first, d.count, lc); });
       break;
     case NGDB_OP_PROJECT:
+      if (c->profiling && c->beta())  // [q|r] 3d -> 2d -> 2d MLP, in units of 2 d^2 flops
+        c->fam_flops[fam] += (d.dir == 0 ? 10.0 : 30.0) * d.count * 2.0 * c->desc.dim * c->desc.dim;
       timed(c, fam, bytes, [&] { return launch_project(a, d.dir, d.first, d.count, lc); });
       break;
     case NGDB_OP_NEGATE:
@@ -397,6 +420,7 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d) {
         const double n = d.count, R = double(d.count) * d.k, D2 = 2.0 * c->desc.dim * c->desc.dim;
         double gemm_rows;
         if (c->desc.backbone == NGDB_GQE) gemm_rows = d.dir == 0 ? 2 * n : 5 * n;
+        else if (c->beta()) gemm_rows = d.dir == 0 ? 6 * R : 18 * R;  // 2d->2d->d attention
         else gemm_rows = d.dir == 0 ? 3 * R + n : 9 * R + 3 * n;
         c->fam_flops[fam] += gemm_rows * D2;
       }
@@ -453,6 +477,13 @@ void set_step_scalars(ngdb_ctx* c, int64_t step) {
   CK(cudaMemcpyAsync(c->d_bc, bc, sizeof(bc), cudaMemcpyHostToDevice, c->stream));
 }
 
+SparseTable entity_table(ngdb_ctx* c, const ngdb_plan* p) {
+  Param& ent = c->params[c->ent_idx];
+  return SparseTable{ent.w, ent.m, ent.v, c->debug ? ent.g : nullptr, static_cast<int32_t>(ent.cols),
+                     p->meta.n_erows, p->blob + p->layout.erows, p->blob + p->layout.eseg,
+                     p->blob + p->layout.econ};
+}
+
 void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
   const ngdb_model_desc& d = c->desc;
   const AdamHyper hp{d.lr, d.beta1, d.beta2, d.eps_adam};
@@ -461,9 +492,7 @@ void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
   const LaunchCtx lc{c->stream, c->num_sms};
   Param& ent = c->params[c->ent_idx];
   Param& rel = c->params[c->rel_idx];
-  SparseTable te{ent.w, ent.m, ent.v, c->debug ? ent.g : nullptr, static_cast<int32_t>(ent.cols),
-                 p->meta.n_erows, p->blob + p->layout.erows, p->blob + p->layout.eseg,
-                 p->blob + p->layout.econ};
+  const SparseTable te = entity_table(c, p);
   SparseTable tr{rel.w, rel.m, rel.v, c->debug ? rel.g : nullptr, static_cast<int32_t>(rel.cols),
                  p->meta.n_rrows, p->blob + p->layout.rrows, p->blob + p->layout.rseg,
                  p->blob + p->layout.rcon};
@@ -480,10 +509,24 @@ void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
   CK(cudaGetLastError());
 }
 
+// Step prologue of the BetaE backbone: the entity table of the step's touched
+// rows (beta.cu). Parameters are fixed within a step, so evaluating the entity
+// side of every KL once up front is exact.
+void prep_step(ngdb_ctx* c, const ngdb_plan* p) {
+  if (!c->beta()) return;
+  const DevArgs a = make_args(c, p);
+  const LaunchCtx lc{c->stream, c->num_sms};
+  const SparseTable te = entity_table(c, p);
+  timed(c, F_ENTITY_PREP, p->meta.n_erows * (2.0 * te.width * 4 + 4) + 4.0 * p->meta.n_econ,
+        [&] { return launch_beta_prep(a, te, lc); });
+  CK(cudaGetLastError());
+}
+
 // Every launch of one planned step, in order (capturable: no host syncs,
 // no host-side allocation).
 void launch_step(ngdb_ctx* c, const ngdb_plan* p) {
   begin_step_device(c);
+  prep_step(c, p);
   for (const auto& d : p->meta.pools) exec_pool(c, p, d);
   optimizer(c, p);
 }
@@ -535,7 +578,7 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       throw Fail{NGDB_ERR_NO_DEVICE, std::string("device is sm_") + std::to_string(prop.major) +
                                          std::to_string(prop.minor) + ", kernels are built for sm_100a"};
     const ngdb_model_desc& d = *desc;
-    if (d.backbone != NGDB_GQE && d.backbone != NGDB_Q2B)
+    if (d.backbone != NGDB_GQE && d.backbone != NGDB_Q2B && d.backbone != NGDB_BETAE)
       throw Fail{NGDB_ERR_MISSING_KERNEL, "backbone not built into this library"};
     if (d.dim <= 0 || d.dim % 4 != 0 || d.dim > 1024)
       throw Fail{NGDB_ERR_CONFIG, "dim must be a positive multiple of 4, <= 1024"};
@@ -555,6 +598,17 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       add_param(c, "relation", d.n_relations, D, true);
       add_param(c, "int_w1", D, D, false);
       add_param(c, "int_w2", D, D, false);
+    } else if (d.backbone == NGDB_BETAE) {  // DESIGN.md §3.5; order = trainer.hpp param_specs
+      add_param(c, "entity", d.n_entities, 2 * D, true);
+      add_param(c, "relation", d.n_relations, D, true);
+      add_param(c, "prj_w1", 2 * D, 3 * D, false);
+      add_param(c, "prj_b1", 1, 2 * D, false);
+      add_param(c, "prj_w2", 2 * D, 2 * D, false);
+      add_param(c, "prj_b2", 1, 2 * D, false);
+      add_param(c, "att_w1", 2 * D, 2 * D, false);
+      add_param(c, "att_b1", 1, 2 * D, false);
+      add_param(c, "att_w2", D, 2 * D, false);
+      add_param(c, "att_b2", 1, D, false);
     } else {
       add_param(c, "entity", d.n_entities, D, true);
       add_param(c, "relation", d.n_relations, 2 * D, true);
@@ -641,7 +695,8 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
       cudaFree(p.v);
       if (p.g) cudaFree(p.g);
     }
-  for (float* p : {c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit, c->sem, c->qbuf, c->dqbuf,
+  if (c->cand_local) cudaFree(c->cand_local);
+  for (float* p : {c->etab, c->etab_c, c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit, c->sem, c->qbuf, c->dqbuf,
                    c->coefbuf, c->ddbuf, c->agbuf, c->rgbuf, c->loss_out, c->scratch, c->arena,
                    c->l2_flush, c->d_bc})
     if (p) cudaFree(p);
@@ -761,6 +816,7 @@ int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
     CK(cudaEventRecord(c->staged[i], c->stream));
     ensure_step_buffers(c, c->stream_plan[i].meta);
     begin_step_device(c);
+    prep_step(c, &c->stream_plan[i]);
     c->active = &c->stream_plan[i];
   });
 }

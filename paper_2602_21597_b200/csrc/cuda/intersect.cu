@@ -16,67 +16,11 @@
 #include <algorithm>
 
 #include "common.cuh"
-#include "tc_gemm.cuh"
+#include "mlp_util.cuh"
 
 namespace ngdb_dev {
-namespace {
-
-// bump allocator over the context scratch buffer
-struct Scratch {
-  float* p;
-  int64_t left;
-  float* take(int64_t n) {
-    n = (n + 3) / 4 * 4;
-    float* r = p;
-    p += n;
-    left -= n;
-    return left >= 0 ? r : nullptr;
-  }
-};
-
-struct Split {
-  float* hi;
-  float* lo;
-};
-Split take_split(Scratch& s, int64_t n) { return {s.take(n), s.take(n)}; }
-
-SplitOperand op(Split x, int ld) { return {x.hi, x.lo, ld}; }
-// weight W_i [out][in] as B of y = x W^T (K = in), or its transpose as B of dx = dy W (K = out)
-SplitOperand wop(const DevArgs& a, int i, int rows, int cols, bool transposed) {
-  const int64_t n = (int64_t)rows * cols;
-  const float* base = a.wsplit + a.wsplit_off[i];
-  return transposed ? SplitOperand{base + 2 * n, base + 3 * n, rows} : SplitOperand{base, base + n, cols};
-}
-
-TcGemmArgs gemm_args(int M, int N, int K, SplitOperand A, SplitOperand B, float* C, int ldc) {
-  TcGemmArgs g{};
-  g.M = M; g.N = N; g.K = K;
-  g.A = A; g.B = B; g.C = C; g.ldc = ldc;
-  return g;
-}
-
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
-  lo = x - hi;
-}
-__device__ __forceinline__ void put(float* plain, Split s, int64_t i, float v) {
-  if (plain) plain[i] = v;
-  float h, l;
-  split_tf32(v, h, l);
-  s.hi[i] = h;
-  s.lo[i] = l;
-}
 
 // bias gradients of a class in one launch: db_j += column sums of dy_j
-struct ColsumJob {
-  const float* dy;
-  int rows, n;
-  float* db;
-};
-struct ColsumJobs {
-  ColsumJob job[4];
-  int n;
-};
 // 32 columns per block; warp w sums rows w, w+8, ...; the 8 warp partials are
 // combined in warp order (deterministic).
 __global__ void __launch_bounds__(256) colsum_kernel(ColsumJobs jobs) {
@@ -100,6 +44,9 @@ int colsums(const ColsumJobs& jobs, int n, cudaStream_t s) {
   launch_pdl(colsum_kernel, dim3(dim3((n + 31) / 32, jobs.n)), dim3(256), 0, s, 1, jobs);
   return 1;
 }
+
+
+namespace {
 
 // ---------------------------------------------------------------------------
 // GQE
@@ -432,12 +379,14 @@ int64_t intersect_scratch_floats(int backbone, int dim, int max_nodes) {
   const int64_t nd = (int64_t)max_nodes * dim, rd = 3 * nd;
   // + padding of the transposed operands (<= 3 rows each)
   if (backbone == NGDB_GQE) return 24 * nd + 32 * (int64_t)dim + 64;
+  if (backbone == NGDB_BETAE) return beta_scratch_floats(dim, max_nodes);
   return 36 * rd + 14 * nd + 64 * (int64_t)dim + 256;
 }
 
 int launch_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc) {
   if (n <= 0) return 0;
   if (a.backbone == NGDB_GQE) return gqe_intersect(a, dir, k, first, n, lc.stream);
+  if (a.backbone == NGDB_BETAE) return launch_beta_intersect(a, dir, k, first, n, lc);
   return q2b_intersect(a, dir, k, first, n, lc.stream);
 }
 

@@ -152,6 +152,7 @@ __global__ void dense_adam_kernel(float* w, float* m, float* v, const float* g, 
 int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
                               const float* bc, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
+  if (a.backbone == NGDB_BETAE) return launch_beta_entity_adam(a, t, hp, bc, lc);
   const int blocks = (t.n_rows + kWarps - 1) / kWarps;
   if (a.backbone == NGDB_GQE)
     launch_pdl(entity_adam_kernel<NGDB_GQE>, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);

@@ -6,6 +6,7 @@
 // (gather / scatter_add), 404-412 (union_score) and DESIGN.md §3.2 (the Q2B
 // negation convention, SURVEY A-8).
 #include "common.cuh"
+#include "special.cuh"
 
 namespace ngdb_dev {
 namespace {
@@ -32,6 +33,14 @@ __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, 
   if (dir == 0) {
     float* out = a.arena + d.out;
     const float* src = a.ent + static_cast<int64_t>(d.id) * a.ent_w;
+    if (a.backbone == NGDB_BETAE) {  // realised (alpha | beta); the mirror's
+      for (int c = lane; c < ew4; c += 32) {  // chain rule runs in the optimizer
+        const float4 x = ldg4(src + 4 * c);
+        st4(out + 4 * c, make_float4(beta_realize(x.x), beta_realize(x.y), beta_realize(x.z),
+                                     beta_realize(x.w)));
+      }
+      return;
+    }
     for (int c = lane; c < ew4; c += 32) st4(out + 4 * c, ldg4(src + 4 * c));
     // Q2B anchors are point boxes: offset half is zero
     for (int c = ew4 + lane; c < a.wq / 4; c += 32) st4(out + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
@@ -109,6 +118,23 @@ __global__ void __launch_bounds__(kWarps * 32) negate_kernel(DevArgs a, int dir,
   const ngdb_node_desc d = a.nodes[first + node];
   const float* src = a.arena + (dir == 0 ? d.in[0] : d.grad);
   float* out = a.arena + d.out;
+  if (a.backbone == NGDB_BETAE) {
+    // (alpha, beta) -> clamp(1/alpha, 1/beta); bwd: g * -1/x^2 where unclamped
+    const float* x = a.arena + d.in[0];
+    for (int c = lane; c < a.wq / 4; c += 32) {
+      const float4 u = ld4(x + 4 * c), g = ld4(src + 4 * c);
+      const float xs[4] = {u.x, u.y, u.z, u.w}, gs[4] = {g.x, g.y, g.z, g.w};
+      float o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float inv = 1.f / xs[t];
+        if (dir == 0) o[t] = fminf(fmaxf(inv, kBetaMin), kBetaMax);
+        else o[t] = (inv > kBetaMin && inv < kBetaMax) ? -gs[t] * inv * inv : 0.f;
+      }
+      st4(out + 4 * c, make_float4(o[0], o[1], o[2], o[3]));
+    }
+    return;
+  }
   // GQE: x -> -x. Q2B: (c, o) -> (-c, o). Both are their own adjoints.
   const int neg4 = a.dim / 4;
   for (int c = lane; c < a.wq / 4; c += 32) {
@@ -175,6 +201,7 @@ int launch_embed(const DevArgs& a, int dir, int first, int n, const LaunchCtx& l
   return 1;
 }
 int launch_project(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc) {
+  if (a.backbone == NGDB_BETAE) return launch_beta_project(a, dir, first, n, lc);
   launch_pdl(project_kernel, dim3(blocks_for(n)), dim3(kWarps * 32), 0, lc.stream, 1, a, dir, first, n, a.n_relations);
   return 1;
 }

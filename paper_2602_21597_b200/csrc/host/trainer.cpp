@@ -26,7 +26,16 @@ std::vector<ParamSpec> param_specs(Backbone b, int32_t n_ent, int32_t n_rel, int
       s.push_back({n, bias ? 1 : d, d, false});
     }
   } else {
-    throw MissingKernel("BetaE parameters are not built in this round");
+    // BetaE: projection MLP [q (2d) | r (d)] -> 2d -> 2d,
+    // attention MLP 2d -> 2d -> d
+    s.push_back({"prj_w1", 2 * d, 3 * d, false});
+    s.push_back({"prj_b1", 1, 2 * d, false});
+    s.push_back({"prj_w2", 2 * d, 2 * d, false});
+    s.push_back({"prj_b2", 1, 2 * d, false});
+    s.push_back({"att_w1", 2 * d, 2 * d, false});
+    s.push_back({"att_b1", 1, 2 * d, false});
+    s.push_back({"att_w2", d, 2 * d, false});
+    s.push_back({"att_b2", 1, d, false});
   }
   return s;
 }

@@ -197,6 +197,13 @@ def param_specs(backbone: str, n_entities: int, n_relations: int, dim: int) -> L
         for n in ("att_w1", "att_b1", "att_w2", "att_b2", "off_w1", "off_b1", "off_w2", "off_b2"):
             out.append((n, 1 if "_b" in n else dim, dim, False))
         return out
+    if backbone == "betae":
+        d = dim
+        return [("entity", n_entities, 2 * d, True), ("relation", n_relations, d, True),
+                ("prj_w1", 2 * d, 3 * d, False), ("prj_b1", 1, 2 * d, False),
+                ("prj_w2", 2 * d, 2 * d, False), ("prj_b2", 1, 2 * d, False),
+                ("att_w1", 2 * d, 2 * d, False), ("att_b1", 1, 2 * d, False),
+                ("att_w2", d, 2 * d, False), ("att_b2", 1, d, False)]
     raise NotImplementedError(backbone)
 
 

@@ -49,6 +49,13 @@ def grad_scale(name, grads):
     return 0.0
 
 
+def weak_mask(name, grads):
+    """Elements whose oracle gradient is below the fp32 noise of its tensor."""
+    g_ref = grads[name][1]
+    noise = 1e-5 * max(rms(g_ref), grad_scale(name, grads))
+    return np.abs(g_ref) <= noise
+
+
 def check_all(res, lr=1e-4, allow_frac=1e-3, steps=1):
     """Assert losses, gradients and post-Adam parameters agree (see module doc)."""
     msgs = []
@@ -65,10 +72,10 @@ def check_all(res, lr=1e-4, allow_frac=1e-3, steps=1):
         # Adam turns |g| >> eps into -lr*sign(g). Where the oracle gradient is
         # below fp32 noise of its tensor the update direction is not defined by
         # the data; those elements are held to the Adam step bound lr*steps.
-        if name in grads:
-            g_ref = grads[name][1]
-            noise = 1e-5 * max(rms(g_ref), grad_scale(name, grads))
-            weak = np.abs(g_ref) <= noise
+        if name in res.get("weak", {}):
+            weak = res["weak"][name]  # weak at ANY step of a multi-step run
+        elif name in grads:
+            weak = weak_mask(name, grads)
         else:
             weak = np.zeros(r.shape, dtype=bool)
         strong = ~weak
@@ -117,7 +124,7 @@ def run_pair(graph, ograph, backbone, mix, b, k, dim, b_max=512, steps=1, seed_t
     om = O.OracleModel(backbone, ne, nr, dim, k, precision=64)
     om.init(2)
     specs = m.param_specs(backbone, ne, nr, dim)
-    out = {"loss": [], "grads": {}, "params": {}, "kept": []}
+    out = {"loss": [], "grads": {}, "params": {}, "kept": [], "weak": {}}
     for step in range(1, steps + 1):
         batch = m.Batch.sample(graph, w, b, k, seed=3, tag=seed_tag + step)
         if certify:
@@ -128,9 +135,19 @@ def run_pair(graph, ograph, backbone, mix, b, k, dim, b_max=512, steps=1, seed_t
         ref = om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, b_max=b_max,
                       step=step)
         out["loss"].append((loss, ref))
+        if steps > 1 and step < steps:
+            # Adam maps a sub-noise gradient at ANY step to an arbitrary +-lr move
+            g = {name: (None, om.get("g:" + name, (rows, cols))) for name, rows, cols, _ in specs}
+            for name in g:
+                wk = weak_mask(name, g)
+                out["weak"][name] = out["weak"].get(name, np.zeros_like(wk)) | wk
     if compare_grads:
         for name, rows, cols, sparse in specs:
             out["grads"][name] = (eng.download("g:" + name), om.get("g:" + name, (rows, cols)))
+    if steps > 1:
+        g = {name: (None, om.get("g:" + name, (rows, cols))) for name, rows, cols, _ in specs}
+        for name in g:
+            out["weak"][name] = out["weak"].get(name, np.zeros(g[name][1].shape, bool)) | weak_mask(name, g)
     for name, rows, cols, sparse in specs:
         out["params"][name] = (eng.download(name), om.get(name, (rows, cols)))
     return out

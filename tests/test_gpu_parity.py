@@ -10,34 +10,36 @@ pytestmark = pytest.mark.gpu
 
 ALL = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni", "inp"]
 C1_MIX = ["1p", "2p", "3p", "2i", "3i"]
+C3_MIX = ["2in", "3in", "inp", "pin", "pni"]
 
 
 def _check(res, allow_frac=0.0, steps=1):
     check_all(res, allow_frac=allow_frac, steps=steps)
 
 
-@pytest.mark.parametrize("backbone,mix", [("gqe", C1_MIX), ("q2b", ALL), ("gqe", ALL)])
+@pytest.mark.parametrize("backbone,mix", [("gqe", C1_MIX), ("q2b", ALL), ("gqe", ALL),
+                                          ("betae", C3_MIX), ("betae", ALL)])
 @pytest.mark.parametrize("dim", [32, 400])
 def test_one_step_parity(small_graph, small_oracle_graph, backbone, mix, dim):
     res = run_pair(small_graph, small_oracle_graph, backbone, mix, b=128, k=32, dim=dim)
     _check(res)
 
 
-@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
 def test_small_bmax_drains(small_graph, small_oracle_graph, backbone):
     # B_max=16 forces multi-pop drains and split cardinality classes
     res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=96, k=8, dim=16, b_max=16)
     _check(res)
 
 
-@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
 def test_three_steps(small_graph, small_oracle_graph, backbone):
     res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=64, k=16, dim=32, steps=3,
                    compare_grads=True)
     _check(res, steps=3)
 
 
-@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
 def test_full_batch_k128(small_graph, small_oracle_graph, backbone):
     # the benchmark's per-step shape (512 queries, 128 negatives, d=400): at this
     # size most queries touch an L1/box kink within 1e-6 (26M sign tests per
@@ -47,7 +49,7 @@ def test_full_batch_k128(small_graph, small_oracle_graph, backbone):
     _check(res)
 
 
-@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
 def test_full_batch_k128_losses(small_graph, small_oracle_graph, backbone):
     # ... while every per-query loss of the full 512-query batch must agree
     res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=512, k=128, dim=400,
@@ -65,4 +67,10 @@ def test_single_pattern_batches(small_graph, small_oracle_graph, pattern):
 
 def test_batch_of_one(small_graph, small_oracle_graph):
     res = run_pair(small_graph, small_oracle_graph, "q2b", ["up"], b=1, k=4, dim=8)
+    _check(res)
+
+
+@pytest.mark.parametrize("pattern", ALL)
+def test_single_pattern_batches_betae(small_graph, small_oracle_graph, pattern):
+    res = run_pair(small_graph, small_oracle_graph, "betae", [pattern], b=32, k=8, dim=16)
     _check(res)

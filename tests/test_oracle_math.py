@@ -26,7 +26,7 @@ def _loss(om, a):
     return om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, adam=-1).sum()
 
 
-@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
 def test_finite_difference_gradients(tiny, backbone):
     g, info = tiny
     d, k = 4, 3
@@ -65,7 +65,7 @@ def test_finite_difference_gradients(tiny, backbone):
     assert checked >= 10
 
 
-@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
 def test_scheduled_equals_sequential(tiny, backbone):
     g, info = tiny
     a = _batch(g, P, 60, 4)

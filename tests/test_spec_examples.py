@@ -217,3 +217,33 @@ def test_benchmark_shape_counts():
     info = m.Graph.synthetic("nell995", 1).info()
     assert (info["n_entities"], info["n_relations"], info["n_train"], info["n_valid"],
             info["n_test"]) == (63361, 200, 114213, 14324, 14267)
+
+
+# ---- BetaE special functions and KL ----------------------------
+
+def test_special_function_known_answers():
+    assert abs(O.lgamma(1.0)) < 1e-12 and abs(O.lgamma(2.0)) < 1e-12
+    assert abs(O.digamma(1.0) - (-0.5772156649015329)) < 1e-10
+    for x in (0.1, 1.0, 10.0, 100.0):  # recurrence identity
+        assert abs(O.digamma(x + 1) - O.digamma(x) - 1.0 / x) < 1e-10
+        assert abs(O.trigamma(x) - O.trigamma(x + 1) - 1.0 / (x * x)) < 1e-10 * max(1, 1 / x**2)
+    assert math.isnan(O.lgamma(0.0)) and math.isnan(O.digamma(-1.0))
+
+
+def test_special_functions_vs_scipy():
+    sp = pytest.importorskip("scipy.special")
+    xs = np.concatenate([np.linspace(0.05, 8, 300), np.logspace(0.5, 6, 100)])
+    for x in xs:
+        assert abs(O.lgamma(x) - sp.gammaln(x)) < 1e-10 * max(1.0, abs(sp.gammaln(x)))
+        assert abs(O.digamma(x) - sp.digamma(x)) < 1e-10 * max(1.0, abs(sp.digamma(x)))
+        assert abs(O.trigamma(x) - sp.polygamma(1, x)) < 1e-10 * max(1.0, sp.polygamma(1, x))
+
+
+def test_beta_kl_examples():
+    assert abs(O.beta_kl(1, 1, 1, 1)) < 1e-14
+    # mpmath-verified closed form; SPEC.md:394 quotes ~0.1251
+    assert abs(O.beta_kl(2, 2, 1, 1) - 0.125092802561388) < 1e-12
+    rng = np.random.default_rng(0)
+    for a1, b1, a2, b2 in rng.uniform(0.05, 20, size=(50, 4)):
+        assert O.beta_kl(a1, b1, a2, b2) >= -1e-12  # KL >= 0
+
