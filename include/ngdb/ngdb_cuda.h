@@ -151,6 +151,10 @@ int ngdb_step_end(ngdb_ctx* ctx, float* per_query_loss, int32_t n_queries, doubl
 /* Resident plans: upload once, replay many times (benchmark / graph replay). */
 int ngdb_plan_create(ngdb_ctx* ctx, const ngdb_step_plan* plan, ngdb_plan** out);
 int ngdb_plan_run(ngdb_ctx* ctx, ngdb_plan* plan, int64_t step); /* all pools + optimizer */
+/* Capture (without running) the CUDA graph plan_run replays, so a resident
+ * plan's first run costs one graph launch. Call after the last plan_create of
+ * a context (a later buffer growth invalidates the capture). */
+int ngdb_plan_prepare(ngdb_ctx* ctx, ngdb_plan* plan);
 int ngdb_plan_destroy(ngdb_plan* plan);
 
 /* Device timing on the context stream (CUDA events). */

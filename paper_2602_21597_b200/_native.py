@@ -65,6 +65,7 @@ SIGNATURES = {
     "ngdb_step_end": (C.c_int, [C.c_void_p, P(f32), i32, P(f64), P(i32)]),
     "ngdb_plan_create": (C.c_int, [C.c_void_p, P(StepPlan), P(C.c_void_p)]),
     "ngdb_plan_run": (C.c_int, [C.c_void_p, C.c_void_p, i64]),
+    "ngdb_plan_prepare": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ngdb_plan_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_sync": (C.c_int, [C.c_void_p]),
     "ngdb_timer_start": (C.c_int, [C.c_void_p]),

@@ -882,6 +882,44 @@ int ngdb_plan_create(ngdb_ctx* c, const ngdb_step_plan* plan, ngdb_plan** out) {
   return rc;
 }
 
+namespace {
+// capture the step's ~100+ launches once; replays cost one launch
+void capture_plan(ngdb_ctx* c, ngdb_plan* p) {
+  if (p->graph) CK(cudaGraphExecDestroy(p->graph));
+  p->graph = nullptr;
+  cudaGraph_t g = nullptr;
+  ngdb_plan* prev = c->active;
+  c->active = p;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t l0 = c->launches;
+  try {
+    launch_step(c, p);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    c->launches = l0;
+    c->active = prev;
+    throw;
+  }
+  p->graph_launches = c->launches - l0;
+  c->launches = l0;
+  c->active = prev;
+  CK(cudaStreamEndCapture(c->stream, &g));
+  const cudaError_t e = cudaGraphInstantiate(&p->graph, g, 0);
+  cudaGraphDestroy(g);
+  CK(e);
+  p->graph_gen = c->buffer_gen;
+}
+}  // namespace
+
+int ngdb_plan_prepare(ngdb_ctx* c, ngdb_plan* p) {
+  return guarded([&] {
+    ensure_step_buffers(c, p->meta);
+    if (!c->use_graphs) return;
+    if (!p->graph || p->graph_gen != c->buffer_gen) capture_plan(c, p);
+  });
+}
+
 int ngdb_plan_run(ngdb_ctx* c, ngdb_plan* p, int64_t step) {
   return guarded([&] {
     ensure_step_buffers(c, p->meta);
@@ -891,29 +929,7 @@ int ngdb_plan_run(ngdb_ctx* c, ngdb_plan* p, int64_t step) {
       launch_step(c, p);
       return;
     }
-    if (!p->graph || p->graph_gen != c->buffer_gen) {
-      // capture the step's ~100+ launches once; replays cost one launch
-      if (p->graph) CK(cudaGraphExecDestroy(p->graph));
-      p->graph = nullptr;
-      cudaGraph_t g = nullptr;
-      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      const int64_t l0 = c->launches;
-      try {
-        launch_step(c, p);
-      } catch (...) {
-        cudaStreamEndCapture(c->stream, &g);
-        if (g) cudaGraphDestroy(g);
-        c->launches = l0;
-        throw;
-      }
-      p->graph_launches = c->launches - l0;
-      c->launches = l0;
-      CK(cudaStreamEndCapture(c->stream, &g));
-      const cudaError_t e = cudaGraphInstantiate(&p->graph, g, 0);
-      cudaGraphDestroy(g);
-      CK(e);
-      p->graph_gen = c->buffer_gen;
-    }
+    if (!p->graph || p->graph_gen != c->buffer_gen) capture_plan(c, p);
     CK(cudaGraphLaunch(p->graph, c->stream));
     c->launches += p->graph_launches;
   });
