@@ -40,7 +40,9 @@ CONFIGS = {
     "c1": ("gqe", "fb15k-237", "c1", 400, 512, 128),
     "c2": ("q2b", "nell995", "all", 400, 512, 128),
     "c3": ("betae", "fb15k-237", "c3", 400, 512, 128),
+    "c4": ("gqe", "fb15k-237", "c1", 400, 512, 128),  # + 768-d frozen PTE store
 }
+SEMANTIC_DIM = {"c4": 768}
 MIXES = {"all": ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni",
                  "inp"],
          "c1": ["1p", "2p", "3p", "2i", "3i"],
@@ -150,11 +152,13 @@ def make_batches(graph, mix, batch, n_neg, count, base_tag):
     return [m.Batch.sample(graph, w, batch, n_neg, seed=3, tag=base_tag + i) for i in range(count)]
 
 
-def run_cpu_oracle(backbone, info, dim, n_neg, batches, budget_s, precision=32):
+def run_cpu_oracle(backbone, info, dim, n_neg, batches, budget_s, precision=32, store=None):
     """Time the oracle on whole 512-query steps until budget_s elapses."""
     import oracle as O
     om = O.OracleModel(backbone, info["n_entities"], info["n_relations"], dim, n_neg,
                        precision=precision)
+    if store is not None:
+        om.set_semantic(store)
     om.init(2)
     done, t0, q = 0, time.perf_counter(), 0
     while True:
@@ -179,6 +183,8 @@ def reference_arm(args):
     batches = make_batches(graph, mix, batch, n_neg, max(1, min(args.steps, 4)), 1)
     import oracle as O
     om = O.OracleModel(backbone, info["n_entities"], info["n_relations"], dim, n_neg, precision=32)
+    if SEMANTIC_DIM.get(args.config):
+        om.set_semantic(m.semantic_store(info["n_entities"], SEMANTIC_DIM[args.config], seed=5))
     om.init(2)
     for i in range(args.warmup):
         a = batches[i % len(batches)].arrays()
@@ -195,7 +201,8 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * el / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{backbone} {shape}-shaped synthetic KG, {mix} mix",
+        "config": {"workload": f"{backbone} {shape}-shaped synthetic KG, {mix} mix"
+                               + (" + PTE fusion" if SEMANTIC_DIM.get(args.config) else ""),
                    "global_batch": batch, "n_neg": n_neg, "dim": dim},
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "port",
                          "sample": f"{args.steps} full {batch}-query steps (oracle/, f32, "
@@ -242,10 +249,12 @@ def main():
     n_steps = args.warmup + args.steps
     # each rank draws its own batches: Rng(3).fork(step * world + rank)
     batches = make_batches(graph, mix, batch, n_neg, n_steps, 1 + rank * 100000)
+    sdim = SEMANTIC_DIM.get(args.config, 0)
+    store = m.semantic_store(info["n_entities"], sdim, seed=5) if sdim else None
     eng = m.Engine(backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=n_neg,
-                   b_max=512, max_queries=batch, device=local)
+                   b_max=512, max_queries=batch, device=local, semantic=store)
     ctx = eng.handle
-    steps = [m.PlannedStep(b, backbone, dim, 512) for b in batches]
+    steps = [m.PlannedStep(b, backbone, dim, 512, semantic=bool(sdim)) for b in batches]
     plans = []
     for s in steps:
         v = s.view()
@@ -359,7 +368,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         qps, done, el = run_cpu_oracle(backbone, info, dim, n_neg, batches[: min(4, n_steps)],
-                                       args.cpu_budget)
+                                       args.cpu_budget, store=store)
         cpu = {"value": qps, "unit": "queries/s", "cores": 1, "kind": "port",
                "sample": f"{done} full {batch}-query steps in {el:.1f}s (oracle/, f32, 1 thread)"}
 
@@ -377,7 +386,9 @@ def main():
             "data": "synthetic",
             "config": {"workload": f"{backbone} on {shape}-shaped synthetic KG "
                                    f"({info['n_entities']} entities, {info['n_relations']} "
-                                   f"relations), {mix}-pattern mix",
+                                   f"relations), {mix}-pattern mix"
+                                   + (f", FuseSemantic over a frozen {sdim}-d PTE store"
+                                      if sdim else ""),
                        "global_batch": batch * world, "n_neg": n_neg, "dim": dim,
                        "parallelism": f"replicas{world}" if world > 1 else "single",
                        "l2": l2_note},

@@ -72,6 +72,19 @@ int ngdb_jsonl_roundtrip(const char* line, char* out, int64_t cap);
 /* --- parameters ------------------------------------------- */
 int ngdb_param_init(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
                     const char* name, uint64_t seed, float* out, int64_t n);
+/* same, for a model with semantic fusion of a d_l-wide store (fus_f, fus_wp,
+ * fus_bp follow the backbone's tensors in the registry) */
+int ngdb_param_init_ex(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
+                       int32_t semantic_dim, const char* name, uint64_t seed, float* out,
+                       int64_t n);
+
+/* --- semantic store (NGSE format SPEC.md:593) ---- */
+/* Synthetic frozen PTE rows: N(0,1)/sqrt(d_l) from Rng(seed), row-major. */
+int ngdb_semantic_synth(int32_t n_entities, int32_t dim, uint64_t seed, float* out);
+/* NGSE file: "NGSE", u32 version 1, u64 count, u32 dim, count*dim f32 (all LE). */
+int ngdb_ngse_write(const char* path, const float* data, int64_t count, int32_t dim);
+/* *count, *dim from the header; rows copied when out != NULL and cap >= count*dim. */
+int ngdb_ngse_read(const char* path, float* out, int64_t cap, int64_t* count, int32_t* dim);
 
 /* --- the public training call: plan + run one step on a context ----------- */
 int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t step,

@@ -45,10 +45,18 @@ struct ParamSpec {
   int64_t rows = 0, cols = 0;
   bool sparse = false;
 };
+// semantic_dim > 0 appends the fusion tensors fus_f [d][d_l], fus_wp [d][2d],
+// fus_bp [1][d] (no bias on F, SURVEY A-7).
 std::vector<ParamSpec> param_specs(Backbone b, int32_t n_entities, int32_t n_relations,
-                                   int32_t dim);
+                                   int32_t dim, int32_t semantic_dim = 0);
 std::vector<float> init_param(Backbone b, int32_t n_entities, int32_t n_relations, int32_t dim,
-                              const std::string& name, uint64_t seed, double gamma = 12.0);
+                              const std::string& name, uint64_t seed, double gamma = 12.0,
+                              int32_t semantic_dim = 0);
+
+// Frozen semantic store helpers.
+std::vector<float> synth_semantic_store(int32_t n_entities, int32_t dim, uint64_t seed);
+void write_ngse(const std::string& path, const float* data, int64_t count, int32_t dim);
+std::vector<float> read_ngse(const std::string& path, int64_t* count, int32_t* dim);
 
 struct StepPlanHost {
   std::vector<ngdb_pool_desc> pools;

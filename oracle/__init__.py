@@ -48,6 +48,7 @@ _SIG = {
     "oracle_q2b_distance": (f64, [P(f64), P(f64), P(f64), i32, f64]),
     "oracle_loss": (f64, [f64, f64, P(f64), i32]),
     "oracle_lgamma": (f64, [f64]),
+    "oracle_model_set_semantic": (C.c_int, [C.c_void_p, i32, P(C.c_float), i64]),
     "oracle_digamma": (f64, [f64]),
     "oracle_trigamma": (f64, [f64]),
     "oracle_beta_kl": (f64, [f64, f64, f64, f64]),
@@ -124,6 +125,11 @@ class OracleModel:
         self.n_entities, self.n_relations = n_entities, n_relations
         _check(lib.oracle_model_create(BACKBONES[backbone], n_entities, n_relations, dim, n_neg,
                                        gamma, alpha_box, lr, precision, C.byref(self._h)))
+
+    def set_semantic(self, store):
+        """Frozen semantic store [n_entities][d_l] + fusion params (before init)."""
+        a = np.ascontiguousarray(store, dtype=np.float32)
+        _check(lib.oracle_model_set_semantic(self._h, a.shape[1], _p(a, C.c_float), a.size))
 
     def init(self, seed=2):
         _check(lib.oracle_model_init(self._h, seed))

@@ -59,6 +59,8 @@ int oracle_model_destroy(void* m);
 /* scalar kernels for the SPEC known-answer tests */
 double oracle_q2b_distance(const double* v, const double* c, const double* o, int32_t d,
                            double alpha);
+/* frozen semantic store [ne][dl] + fusion params (call before oracle_model_init) */
+int oracle_model_set_semantic(void* model, int32_t dl, const float* store, int64_t n);
 double oracle_loss(double gamma, double d_pos, const double* d_neg, int32_t k);
 /* BetaE special functions and KL(Beta(a1,b1) || Beta(a2,b2)) */
 double oracle_lgamma(double x);

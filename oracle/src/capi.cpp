@@ -248,6 +248,20 @@ int oracle_model_create(int32_t backbone, int32_t ne, int32_t nr, int32_t dim, i
   });
 }
 
+int oracle_model_set_semantic(void* mp, int32_t dl, const float* store, int64_t n) {
+  return guard([&] {
+    auto* a = static_cast<AnyModel*>(mp);
+    auto set = [&](auto& md) {
+      if (md.backbone == 2) throw std::runtime_error("BetaE fusion (Psi_theta) not restated");
+      if (md.dl) throw std::runtime_error("semantic store already set");
+      if (n != (int64_t)md.ne * dl) throw std::runtime_error("semantic store size");
+      md.setup_semantic(dl, store);
+    };
+    if (a->m64) set(*a->m64);
+    else set(*a->m32);
+  });
+}
+
 int oracle_model_init(void* mp, uint64_t seed) {
   return guard([&] {
     auto* a = static_cast<AnyModel*>(mp);
@@ -285,6 +299,9 @@ int oracle_model_step(void* mp, int32_t b, const int32_t* patterns, const int32_
   return guard([&] {
     auto* a = static_cast<AnyModel*>(mp);
     ODag d = o_build_training_dag(queries_of(b, patterns, anchors, relations));
+    if (a->m64 ? a->m64->dl : a->m32->dl)  // FuseSemantic replaces EmbedAnchor
+      for (auto& nd : d.nodes)
+        if (nd.kind == K_EMB) nd.kind = K_FUSE;
     auto run = [&](auto& md) {
       std::vector<int> cand((size_t)b * (md.k + 1));
       for (int i = 0; i < b; ++i) {

@@ -8,6 +8,8 @@
 //   kernels       GQE SPEC.md:359-376; Q2B SPEC.md:377-385; BetaE SPEC.md:386-403
 //                 (forms of SURVEY A-7); union SPEC.md:404-412;
 //                 loss SPEC.md:541-549 with psi per SPEC.md:431
+//   fusion        fuse_semantic SPEC.md:413-421 (Eq. 12): sigma(W_p [h | F s] + b_p) for
+//                 anchors AND candidates; the store s is frozen
 //   adam          SPEC.md:550-558 (dense) and the lazy touched-row variant (A-9)
 // Every kernel runs node by node (the "looped" form); batching only changes
 // which nodes run together, never the arithmetic of one node.
@@ -33,6 +35,12 @@ struct Model {
   std::map<std::string, bool> sparse;
   std::map<std::string, std::vector<R>> P, M, V, G;  // G: dense grads (all params, zero-filled)
   std::set<int> touchedE, touchedR;
+  // semantic fusion: frozen store [ne][dl]; fused
+  // candidate rows are cached per step (parameters are fixed within a step) and
+  // their gradients accumulated, then pushed through the fusion once per entity
+  int dl = 0;
+  std::vector<R> sem;
+  std::map<int, std::vector<R>> fcache, fgrad;
   std::vector<R> losses;
   std::vector<double> margin;  // per query: min |kink argument| seen in the forward pass
   OTrace trace;
@@ -76,6 +84,20 @@ struct Model {
                             "off_b2"})
         add(n, std::string(n).find("_b") != std::string::npos ? 1 : d, d, false);
     }
+  }
+
+  void setup_semantic(int dl_, const float* store) {
+    dl = dl_;
+    sem.assign(store, store + (int64_t)ne * dl);
+    auto add = [&](const std::string& n, int64_t r, int64_t c) {
+      names.push_back(n);
+      shape[n] = {r, c};
+      sparse[n] = false;
+      for (auto* m : {&P, &M, &V, &G}) (*m)[n].assign(r * c, R(0));
+    };
+    add("fus_f", d, dl);       // F: d_l -> d, no bias (SURVEY A-7)
+    add("fus_wp", d, 2 * d);   // W_p: [h | F s] -> d
+    add("fus_bp", 1, d);       // b_p
   }
 
   // ---- distances -----------------------------------------------------------
@@ -400,6 +422,48 @@ struct Model {
     }
   }
 
+  // ---- FuseSemantic -----------------------------------------
+  void fuse_fwd(int e, R* out, std::vector<R>* xkeep = nullptr) const {
+    std::vector<R> x(2 * d), z(d);
+    const R* h = erow(e);
+    for (int i = 0; i < d; ++i) x[i] = h[i];
+    mv("fus_f", "", &sem[(int64_t)e * dl], x.data() + d);
+    mv("fus_wp", "fus_bp", x.data(), z.data());
+    for (int i = 0; i < d; ++i) out[i] = sigm(z[i]);
+    if (xkeep) *xkeep = std::move(x);
+  }
+  // g = dL/d e_fused: grads to h (entity row), F, W_p, b_p; never to the store
+  void fuse_bwd(int e, const R* g) {
+    std::vector<R> x, y(d), gz(d), gx(2 * d, R(0));
+    fuse_fwd(e, y.data(), &x);
+    for (int i = 0; i < d; ++i) gz[i] = g[i] * y[i] * (R(1) - y[i]);
+    mv_bwd("fus_wp", "fus_bp", x.data(), gz.data(), gx.data());
+    R* ge = gerow(e);
+    for (int i = 0; i < d; ++i) ge[i] += gx[i];
+    mv_bwd("fus_f", "", &sem[(int64_t)e * dl], gx.data() + d, nullptr);
+  }
+  // candidate row (fused when the store is on) and its gradient accumulator
+  const R* crow(int e) {
+    if (!dl) return erow(e);
+    auto& v = fcache[e];
+    if (v.empty()) {
+      v.resize(d);
+      fuse_fwd(e, v.data());
+    }
+    return v.data();
+  }
+  R* cgrow(int e) {
+    if (!dl) return gerow(e);
+    auto& v = fgrad[e];
+    if (v.empty()) v.assign(d, R(0));
+    return v.data();
+  }
+  void flush_fused_grads() {
+    for (auto& kv : fgrad) fuse_bwd(kv.first, kv.second.data());
+    fgrad.clear();
+    fcache.clear();
+  }
+
   // ---- Adam -------------------------------------------------
   void adam(int64_t step, bool lazy) {
     const double bc1 = 1.0 - std::pow(b1, (double)step), bc2 = 1.0 - std::pow(b2, (double)step);
@@ -561,6 +625,11 @@ struct Exec {
         for (int i = 0; i < md.ew; ++i) out[i] = e[i];
         break;
       }
+      case K_FUSE: {  // fused anchor row; Q2B point box (zero offset)
+        const R* e = md.crow(x.payload);
+        for (int i = 0; i < md.wq; ++i) out[i] = i < d ? e[i] : R(0);
+        break;
+      }
       case K_PROJ: {
         const R* in = t(T[x.in[0]]);
         const R* r = &md.P["relation"][(int64_t)x.payload * md.rw];
@@ -622,8 +691,8 @@ struct Exec {
         const R* q = t(T[x.in[0]]);
         const int* c = cands(x.query);
         for (int j = 0; j <= md.k; ++j) {
-          out[j] = md.dist(q, md.erow(c[j]));
-          dist_kinks(x.query, q, md.erow(c[j]));
+          out[j] = md.dist(q, md.crow(c[j]));
+          dist_kinks(x.query, q, md.crow(c[j]));
         }
         break;
       }
@@ -647,8 +716,8 @@ struct Exec {
           const R* q = t(T[x.in[0]]);
           const int* c = cands(x.query);
           for (int j = 0; j <= md.k; ++j) {
-            dists[j] = md.dist(q, md.erow(c[j]));
-            dist_kinks(x.query, q, md.erow(c[j]));
+            dists[j] = md.dist(q, md.crow(c[j]));
+            dist_kinks(x.query, q, md.crow(c[j]));
           }
         }
         out[0] = md.loss_and_coef(dists.data(), coef.data());
@@ -678,6 +747,9 @@ struct Exec {
         for (int i = 0; i < md.ew; ++i) ge[i] += gin[i];
         break;
       }
+      case K_FUSE:
+        md.fuse_bwd(m.payload, gin);
+        break;
       case K_PROJ: {
         const R* r = &md.P["relation"][(int64_t)m.payload * md.rw];
         R* gr = md.grrow(m.payload);
@@ -721,7 +793,7 @@ struct Exec {
         const R* q = t(T[m.in[0]]);
         const int* c = cands(m.query);
         for (int i = 0; i < md.wq; ++i) gout[i] = R(0);
-        for (int j = 0; j <= md.k; ++j) md.ddist(q, md.erow(c[j]), gin[j], gout, md.gerow(c[j]));
+        for (int j = 0; j <= md.k; ++j) md.ddist(q, md.crow(c[j]), gin[j], gout, md.cgrow(c[j]));
         break;
       }
       case K_UNION: {
@@ -744,10 +816,10 @@ struct Exec {
         } else {
           const R* q = t(T[m.in[0]]);
           const int* c = cands(m.query);
-          for (int j = 0; j <= md.k; ++j) dists[j] = md.dist(q, md.erow(c[j]));
+          for (int j = 0; j <= md.k; ++j) dists[j] = md.dist(q, md.crow(c[j]));
           md.loss_and_coef(dists.data(), coef.data());
           for (int i = 0; i < md.wq; ++i) gout[i] = R(0);
-          for (int j = 0; j <= md.k; ++j) md.ddist(q, md.erow(c[j]), coef[j], gout, md.gerow(c[j]));
+          for (int j = 0; j <= md.k; ++j) md.ddist(q, md.crow(c[j]), coef[j], gout, md.cgrow(c[j]));
         }
         break;
       }
@@ -875,8 +947,11 @@ OTrace o_train_step(Model<R>& md, const ODag& g, const std::vector<int>& cand, i
   for (const auto& n : g.nodes) nq = std::max(nq, n.query + 1);
   md.losses.assign(nq, R(0));
   md.margin.assign(nq, 1e300);
+  md.fcache.clear();
+  md.fgrad.clear();
   Exec<R> ex{md, g, cand, b_max, eager};
   OTrace tr = ex.run(sequential);
+  md.flush_fused_grads();
   if (apply_adam) md.adam(step, lazy);
   md.trace = tr;
   return tr;

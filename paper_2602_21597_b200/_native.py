@@ -97,6 +97,10 @@ SIGNATURES = {
     "ngdb_step_trace_json": (C.c_int, [C.c_void_p, i32, C.c_char_p, i64, P(i64)]),
     "ngdb_step_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_param_init": (C.c_int, [i32, i32, i32, i32, C.c_char_p, u64, P(f32), i64]),
+    "ngdb_param_init_ex": (C.c_int, [i32, i32, i32, i32, i32, C.c_char_p, u64, P(f32), i64]),
+    "ngdb_semantic_synth": (C.c_int, [i32, i32, u64, P(f32)]),
+    "ngdb_ngse_write": (C.c_int, [C.c_char_p, P(f32), i64, i32]),
+    "ngdb_ngse_read": (C.c_int, [C.c_char_p, P(f32), i64, P(i64), P(i32)]),
     "ngdb_rng_next": (u64, [u64, i64, i32]),
     "ngdb_rng_below": (C.c_int, [u64, P(u64), i32, i32, P(u64)]),
     "ngdb_select_pool": (C.c_int, [P(i64), P(i64), P(i32)]),

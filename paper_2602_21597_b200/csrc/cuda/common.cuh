@@ -68,6 +68,13 @@ struct DevArgs {
   float* etab;
   float* etab_c;
   int32_t* cand_local;
+  // FuseSemantic (fuse.cu): etab holds e_fused of every touched row; anchors
+  // map to rows through anchor_local[anchor slot]
+  int32_t fused;
+  int32_t sem_dim;
+  const float* sem;      // frozen store [n_entities][sem_dim]
+  int32_t* anchor_local;
+  int32_t fus_idx;       // dense index of fus_f (fus_wp = +1, fus_bp = +2)
 };
 
 // Programmatic dependent launch: let the next kernel in the stream start its
@@ -180,6 +187,12 @@ int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, const Ad
                                 const float* bc, const LaunchCtx& lc);
 // BetaE: per-step entity table + candidate -> CSR-row map (before any pool)
 int launch_beta_prep(const DevArgs& a, const SparseTable& t, const LaunchCtx& lc);
+// fuse.cu: step prologue (etab = e_fused of the touched rows) and the fused
+// backward + entity Adam
+int64_t fuse_scratch_floats(int d, int dl, int64_t rows);
+int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const LaunchCtx& lc);
+int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const AdamHyper& hp,
+                  const float* bc, const LaunchCtx& lc);
 int launch_beta_entity_adam(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
                             const float* bc, const LaunchCtx& lc);
 int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, const AdamHyper& hp,

@@ -183,6 +183,11 @@ struct ngdb_ctx {
   float *etab = nullptr, *etab_c = nullptr;
   int32_t* cand_local = nullptr;
   int64_t cap_erows = 0;
+  // FuseSemantic: anchor slot -> etab row, fusion scratch (fuse.cu)
+  int32_t* anchor_local = nullptr;
+  float* fscratch = nullptr;
+  int64_t fscratch_cap = 0;
+  int fus_idx = -1;
   // streaming plans: double-buffered pinned staging + device blobs
   int32_t* staging[2] = {nullptr, nullptr};
   int64_t staging_cap[2] = {0, 0};
@@ -216,6 +221,8 @@ struct ngdb_ctx {
     return desc.backbone == NGDB_GQE ? desc.dim : 2 * desc.dim;
   }
   bool beta() const { return desc.backbone == NGDB_BETAE; }
+  bool fused() const { return desc.semantic_dim > 0; }
+  bool step_table() const { return beta() || fused(); }  // per-step entity table
   cudaEvent_t take_event() {
     if (!event_pool.empty()) {
       cudaEvent_t e = event_pool.back();
@@ -284,19 +291,28 @@ void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
     realloc_f(c->agbuf, c->cap_anchor * ew);
     realloc_f(c->rgbuf, c->cap_project * rw);
     realloc_f(c->loss_out, c->cap_queries);
-    if (c->beta()) {
+    if (c->step_table()) {
       if (c->cand_local) CK(cudaFree(c->cand_local));
       c->cand_local = dmalloc<int32_t>(c->cap_score * c->cap_cand);
     }
+    if (c->fused()) {
+      if (c->anchor_local) CK(cudaFree(c->anchor_local));
+      c->anchor_local = dmalloc<int32_t>(c->cap_anchor);
+    }
     ++c->buffer_gen;
   }
-  if (c->beta() && m.n_erows > c->cap_erows) {
+  if (c->step_table() && m.n_erows > c->cap_erows) {
     CK(cudaStreamSynchronize(c->stream));
     c->cap_erows = std::max<int64_t>(m.n_erows, c->cap_erows + c->cap_erows / 4);
     if (c->etab) CK(cudaFree(c->etab));
     if (c->etab_c) CK(cudaFree(c->etab_c));
     c->etab = dmalloc<float>(c->cap_erows * ew);
     c->etab_c = dmalloc<float>(c->cap_erows);
+    if (c->fused()) {
+      if (c->fscratch) CK(cudaFree(c->fscratch));
+      c->fscratch_cap = fuse_scratch_floats(c->desc.dim, c->desc.semantic_dim, c->cap_erows);
+      c->fscratch = dmalloc<float>(c->fscratch_cap);
+    }
     ++c->buffer_gen;
   }
   if (m.arena_elems > c->arena_cap) {
@@ -344,6 +360,11 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.etab = c->etab;
   a.etab_c = c->etab_c;
   a.cand_local = c->cand_local;
+  a.fused = c->fused() ? 1 : 0;
+  a.sem_dim = c->desc.semantic_dim;
+  a.sem = c->sem;
+  a.anchor_local = c->anchor_local;
+  a.fus_idx = c->fus_idx;
   return a;
 }
 
@@ -402,6 +423,11 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d) {
   const double bytes = c->profiling ? pool_bytes(c, d, p->meta.n_candidates) : 0.0;
   switch (d.kind) {
     case NGDB_OP_EMBED_ANCHOR:
+      if (c->fused()) throw Fail{NGDB_ERR_CONFIG, "EmbedAnchor pool on a FuseSemantic context"};
+      timed(c, fam, bytes, [&] { return launch_embed(a, d.dir, d.first, d.count, lc); });
+      break;
+    case NGDB_OP_FUSE_SEMANTIC:  // gather of the prologue's fused rows / its adjoint
+      if (!c->fused()) throw Fail{NGDB_ERR_MISSING_KERNEL, "FuseSemantic pool without a semantic store"};
       timed(c, fam, bytes, [&] { return launch_embed(a, d.dir, d.first, d.count, lc); });
       break;
     case NGDB_OP_PROJECT:
@@ -493,12 +519,20 @@ void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
   Param& ent = c->params[c->ent_idx];
   Param& rel = c->params[c->rel_idx];
   const SparseTable te = entity_table(c, p);
+  if (c->fused()) {
+    const double u = p->meta.n_erows, D = c->desc.dim, L = c->desc.semantic_dim;
+    if (c->profiling) c->fam_flops[F_OPT_ENTITY] += 2.0 * u * D * (2 * D + 2 * D + L);
+    timed(c, F_OPT_ENTITY, 6.0 * u * D * 4 + 8.0 * p->meta.n_econ + u * L * 4, [&] {
+      return fuse_backward(a, te, c->fscratch, c->fscratch_cap, hp, bc, lc);
+    });
+  }
   SparseTable tr{rel.w, rel.m, rel.v, c->debug ? rel.g : nullptr, static_cast<int32_t>(rel.cols),
                  p->meta.n_rrows, p->blob + p->layout.rrows, p->blob + p->layout.rseg,
                  p->blob + p->layout.rcon};
   const double eb = 6.0 * p->meta.n_erows * ent.cols * 4 + 8.0 * p->meta.n_econ +
                     p->meta.n_score * double(c->query_width()) * 4;
-  timed(c, F_OPT_ENTITY, eb, [&] { return launch_sparse_adam_entity(a, te, hp, bc, lc); });
+  if (!c->fused())
+    timed(c, F_OPT_ENTITY, eb, [&] { return launch_sparse_adam_entity(a, te, hp, bc, lc); });
   const double rb = 6.0 * p->meta.n_rrows * rel.cols * 4 + p->meta.n_rcon * (4.0 + rel.cols * 4);
   timed(c, F_OPT_RELATION, rb, [&] { return launch_sparse_adam_relation(a, tr, hp, bc, lc); });
   timed(c, F_OPT_DENSE, 28.0 * c->dense_n, [&] {
@@ -513,10 +547,19 @@ void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
 // rows (beta.cu). Parameters are fixed within a step, so evaluating the entity
 // side of every KL once up front is exact.
 void prep_step(ngdb_ctx* c, const ngdb_plan* p) {
-  if (!c->beta()) return;
+  if (!c->step_table()) return;
   const DevArgs a = make_args(c, p);
   const LaunchCtx lc{c->stream, c->num_sms};
   const SparseTable te = entity_table(c, p);
+  if (c->fused()) {
+    if (!c->sem) throw Fail{NGDB_ERR_CONFIG, "semantic store not uploaded (ngdb_semantic_upload)"};
+    const double u = p->meta.n_erows, D = c->desc.dim, L = c->desc.semantic_dim;
+    if (c->profiling) c->fam_flops[F_ENTITY_PREP] += 2.0 * u * D * (L + 2 * D);
+    timed(c, F_ENTITY_PREP, u * (L * 4 + D * 4 * 2) + 4.0 * p->meta.n_econ,
+          [&] { return fuse_prologue(a, te, c->fscratch, c->fscratch_cap, lc); });
+    CK(cudaGetLastError());
+    return;
+  }
   timed(c, F_ENTITY_PREP, p->meta.n_erows * (2.0 * te.width * 4 + 4) + 4.0 * p->meta.n_econ,
         [&] { return launch_beta_prep(a, te, lc); });
   CK(cudaGetLastError());
@@ -584,7 +627,10 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       throw Fail{NGDB_ERR_CONFIG, "dim must be a positive multiple of 4, <= 1024"};
     if (d.n_neg < 1 || d.n_neg + 1 > 1024) throw Fail{NGDB_ERR_CONFIG, "n_neg out of range"};
     if (d.n_entities < 1 || d.n_relations < 1) throw Fail{NGDB_ERR_CONFIG, "empty tables"};
-    if (d.semantic_dim != 0) throw Fail{NGDB_ERR_MISSING_KERNEL, "FuseSemantic not built in this round"};
+    if (d.semantic_dim < 0 || d.semantic_dim % 4 != 0 || d.semantic_dim > 4096)
+      throw Fail{NGDB_ERR_CONFIG, "semantic_dim must be a multiple of 4, <= 4096"};
+    if (d.semantic_dim > 0 && d.backbone == NGDB_BETAE)
+      throw Fail{NGDB_ERR_MISSING_KERNEL, "BetaE + FuseSemantic (Psi_theta) not built"};
     c = new ngdb_ctx();
     c->desc = d;
     if (c->desc.max_batch <= 0) c->desc.max_batch = 512;
@@ -620,6 +666,14 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       add_param(c, "off_b1", 1, D, false);
       add_param(c, "off_w2", D, D, false);
       add_param(c, "off_b2", 1, D, false);
+    }
+    if (d.semantic_dim > 0) {  // FusionParams, after the backbone's
+      int n_dense = 0;
+      for (const auto& p : c->params) n_dense += p.sparse ? 0 : 1;
+      c->fus_idx = n_dense;
+      add_param(c, "fus_f", D, d.semantic_dim, false);
+      add_param(c, "fus_wp", D, 2 * D, false);
+      add_param(c, "fus_bp", 1, D, false);
     }
     // dense tensors share one flat buffer (one Adam launch, one memset)
     int64_t off = 0;
@@ -696,6 +750,8 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
       if (p.g) cudaFree(p.g);
     }
   if (c->cand_local) cudaFree(c->cand_local);
+  if (c->anchor_local) cudaFree(c->anchor_local);
+  if (c->fscratch) cudaFree(c->fscratch);
   for (float* p : {c->etab, c->etab_c, c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit, c->sem, c->qbuf, c->dqbuf,
                    c->coefbuf, c->ddbuf, c->agbuf, c->rgbuf, c->loss_out, c->scratch, c->arena,
                    c->l2_flush, c->d_bc})

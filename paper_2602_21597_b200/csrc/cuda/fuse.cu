@@ -1,0 +1,241 @@
+// FuseSemantic: frozen PTE vectors fused into the structural embedding by a
+// GPU-resident projection (Eq. 12):
+//
+//   e_fused = sigma(W_p [h | F s] + b_p)        h: entity row (d), s: store row (d_l)
+//
+// applied to anchors AND candidates. Parameters are fixed within
+// a step, so the B200 layout evaluates e_fused ONCE per touched entity row of
+// the step (the optimizer CSR rows: ~14k for FB15k-237 instead of 66k
+// candidate + ~1k anchor evaluations — the "deduped" 19 GFLOP of SURVEY §8(d))
+// as two tcgen05 GEMMs in the step prologue, into the same per-step entity
+// table (etab) the BetaE path uses. FuseSemantic nodes then gather from etab
+// and the fused score+loss kernel streams candidate rows from it.
+//
+// Backward (in the optimizer): dL/de_fused per row = anchor gradient rows +
+// candidate terms recomputed from (q, coef) as for the plain backbones, times
+// sigma' -> dZ; then dX = dZ W_p, dW_p += dZ^T X, db_p += colsum dZ,
+// dF += (dX[:, d:])^T S, and the entity rows take Adam on dX[:, :d]. The store
+// is never written (frozen: its gradient is exactly zero).
+#include <algorithm>
+
+#include "common.cuh"
+#include "mlp_util.cuh"
+
+namespace ngdb_dev {
+namespace {
+
+constexpr int kWarps = 8;
+
+struct FuseBufs {
+  int u, uP, d, dl;
+  float* S;  Split Ss;    // [u][dl]   gathered store rows
+  float* X;  Split Xs;    // [u][2d]   [h | F s]
+  float* Zf;              // [u][d]    pre-activation
+  float* dZ; Split dZs;   // [u][d]
+  float* dX;              // [u][2d]   dZ W_p
+  Split dZT, XT, dFsT, ST;  // transposed splits, rows padded to uP
+};
+
+FuseBufs carve(float* base, int64_t cap, int u, int d, int dl) {
+  Scratch sc{base, cap};
+  FuseBufs f{};
+  f.u = u;
+  f.uP = (u + 3) & ~3;
+  f.d = d;
+  f.dl = dl;
+  const int64_t U = u, UP = f.uP;
+  f.S = sc.take(U * dl);
+  f.Ss = take_split(sc, U * dl);
+  f.X = sc.take(U * 2 * d);
+  f.Xs = take_split(sc, U * 2 * d);
+  f.Zf = sc.take(U * d);
+  f.dZ = sc.take(U * d);
+  f.dZs = take_split(sc, U * d);
+  f.dX = sc.take(U * 2 * d);
+  f.dZT = take_split(sc, UP * d);
+  f.XT = take_split(sc, UP * 2 * d);
+  f.dFsT = take_split(sc, UP * d);
+  f.ST = take_split(sc, UP * dl);
+  return f;
+}
+
+// Per touched row r: candidate / anchor -> row maps, the gathered store row
+// (plain + split) and X[r][0:d] = h (plain + split).
+__global__ void __launch_bounds__(kWarps * 32) fuse_gather_kernel(DevArgs a, SparseTable t, FuseBufs f) {
+  pdl_start();
+  const int r = blockIdx.x * kWarps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= t.n_rows) return;
+  for (int kk = t.seg[r] + lane; kk < t.seg[r + 1]; kk += 32) {
+    const int32_t code = t.contrib[kk];
+    if (code >= 0) a.cand_local[code] = r;
+    else a.anchor_local[-code - 1] = r;
+  }
+  const int64_t e = t.rows[r];
+  const float* s = a.sem + e * f.dl;
+  for (int c = lane; c < f.dl / 4; c += 32) {
+    const float4 v = ldg4(s + 4 * c);
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) put(f.S, f.Ss, (int64_t)r * f.dl + 4 * c + q, vv[q]);
+  }
+  const float* h = a.ent + e * a.ent_w;
+  for (int c = lane; c < f.d / 4; c += 32) {
+    const float4 v = ld4(h + 4 * c);
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) put(f.X, f.Xs, (int64_t)r * 2 * f.d + 4 * c + q, vv[q]);
+  }
+}
+
+__global__ void fuse_sigmoid_kernel(const float* Z, float* E, int64_t n) {
+  pdl_start();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    E[i] = sigmoidf(Z[i]);
+}
+
+template <int BB>
+__device__ __forceinline__ float cand_term(float v, float qc, float qo, float coef, float alpha) {
+  const float delta = v - qc;
+  float mag = coef;
+  if (BB == NGDB_Q2B) mag = fabsf(delta) > qo ? coef : coef * alpha;
+  return delta > 0.f ? mag : (delta < 0.f ? -mag : 0.f);
+}
+
+// dZ[r] = (anchor grads + candidate grads of row r) * E (1 - E), plain + split
+template <int BB>
+__global__ void __launch_bounds__(kWarps * 32) fuse_grad_kernel(DevArgs a, SparseTable t, FuseBufs f) {
+  pdl_start();
+  const int r = blockIdx.x * kWarps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= t.n_rows) return;
+  const int beg = t.seg[r], end = t.seg[r + 1];
+  const float* E = a.etab + (int64_t)r * a.ent_w;
+  for (int c = lane; c < f.d / 4; c += 32) {
+    const float4 ev = ld4(E + 4 * c);
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
+    const float e4[4] = {ev.x, ev.y, ev.z, ev.w};
+    for (int kk = beg; kk < end; ++kk) {
+      const int32_t code = __ldg(t.contrib + kk);
+      if (code < 0) {
+        const float4 u = ld4(a.agbuf + (int64_t)(-code - 1) * a.ent_w + 4 * c);
+        g[0] += u.x; g[1] += u.y; g[2] += u.z; g[3] += u.w;
+      } else {
+        const float coef = __ldg(a.coefbuf + code);
+        const float* q = a.qbuf + (int64_t)(code / a.ncand) * a.wq;
+        const float4 qc = ld4(q + 4 * c);
+        const float4 qo = BB == NGDB_Q2B ? ld4(q + a.dim + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        g[0] += cand_term<BB>(e4[0], qc.x, qo.x, coef, a.alpha_box);
+        g[1] += cand_term<BB>(e4[1], qc.y, qo.y, coef, a.alpha_box);
+        g[2] += cand_term<BB>(e4[2], qc.z, qo.z, coef, a.alpha_box);
+        g[3] += cand_term<BB>(e4[3], qc.w, qo.w, coef, a.alpha_box);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      put(f.dZ, f.dZs, (int64_t)r * f.d + 4 * c + q, g[q] * e4[q] * (1.f - e4[q]));
+  }
+}
+
+// lazy Adam on the touched entity rows with gradient rows G[r][0:width] (stride ldg)
+__global__ void __launch_bounds__(kWarps * 32) rows_adam_kernel(SparseTable t, const float* G, int ldg,
+                                                                AdamHyper hp, const float* bc) {
+  pdl_start();
+  const int r = blockIdx.x * kWarps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= t.n_rows) return;
+  const float bc1 = bc[0], bc2 = bc[1];
+  const int64_t row = t.rows[r];
+  for (int c = lane; c < t.width / 4; c += 32) {
+    const float4 g4 = ld4(G + (int64_t)r * ldg + 4 * c);
+    if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g4);
+    const int64_t o = row * t.width + 4 * c;
+    float4 w = ld4(t.w + o), m = ld4(t.m + o), v = ld4(t.v + o);
+    float* wv = &w.x;
+    float* mv = &m.x;
+    float* vv = &v.x;
+    const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mv[q] = hp.b1 * mv[q] + (1.f - hp.b1) * g[q];
+      vv[q] = hp.b2 * vv[q] + (1.f - hp.b2) * g[q] * g[q];
+      wv[q] -= hp.lr * (mv[q] / bc1) / (sqrtf(vv[q] / bc2) + hp.eps);
+    }
+    st4(t.w + o, w);
+    st4(t.m + o, m);
+    st4(t.v + o, v);
+  }
+}
+
+inline int row_blocks(int n) { return (n + kWarps - 1) / kWarps; }
+
+}  // namespace
+
+int64_t fuse_scratch_floats(int d, int dl, int64_t rows) {
+  const int64_t U = rows + 4;
+  return U * (3 * dl + 6 * d + d + 3 * d + 2 * d) + U * (2 * d + 4 * d + 2 * d + 2 * dl) + 4096;
+}
+
+int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const LaunchCtx& lc) {
+  if (t.n_rows <= 0) return 0;
+  const int d = a.dim, dl = a.sem_dim, u = t.n_rows;
+  FuseBufs f = carve(fs, cap, u, d, dl);
+  const float* p = a.dense;
+  int launches = 0;
+  launch_pdl(fuse_gather_kernel, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
+  ++launches;
+  // F s -> X[:, d:2d] (plain + chained split)
+  TcGemmArgs g1 = gemm_args(u, d, dl, op(f.Ss, dl), wop(a, a.fus_idx, d, dl, false), f.X + d, 2 * d);
+  g1.s_hi = f.Xs.hi + d;
+  g1.s_lo = f.Xs.lo + d;
+  launches += tc_gemm(g1, lc.stream);
+  // Z = [h | F s] W_p^T + b_p
+  TcGemmArgs g2 = gemm_args(u, d, 2 * d, op(f.Xs, 2 * d), wop(a, a.fus_idx + 1, d, 2 * d, false), f.Zf, d);
+  g2.bias = p + a.dense_off[a.fus_idx + 2];
+  launches += tc_gemm(g2, lc.stream);
+  const int64_t n = (int64_t)u * d;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)lc.num_sms * 8);
+  launch_pdl(fuse_sigmoid_kernel, dim3(blocks), dim3(256), 0, lc.stream, 1, (const float*)f.Zf, a.etab, n);
+  return launches + 1;
+}
+
+int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const AdamHyper& hp,
+                  const float* bc, const LaunchCtx& lc) {
+  if (t.n_rows <= 0) return 0;
+  const int d = a.dim, dl = a.sem_dim, u = t.n_rows;
+  FuseBufs f = carve(fs, cap, u, d, dl);
+  float* g = a.dense_g;
+  const int64_t* off = a.dense_off;
+  int launches = 0;
+  if (a.backbone == NGDB_GQE)
+    launch_pdl(fuse_grad_kernel<NGDB_GQE>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
+  else
+    launch_pdl(fuse_grad_kernel<NGDB_Q2B>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
+  ++launches;
+  // dX = dZ W_p  ([u][2d]; first half -> entity rows, second half -> F s)
+  TcGemmArgs g3 = gemm_args(u, 2 * d, d, op(f.dZs, d), wop(a, a.fus_idx + 1, d, 2 * d, true), f.dX, 2 * d);
+  launches += tc_gemm(g3, lc.stream);
+  SplitJobs jobs{};
+  jobs.job[0] = {f.dZ, u, d, d, 0, f.dZT.hi, f.dZT.lo};
+  jobs.job[1] = {f.X, u, 2 * d, 2 * d, 0, f.XT.hi, f.XT.lo};
+  jobs.job[2] = {f.dX + d, u, d, 2 * d, 0, f.dFsT.hi, f.dFsT.lo};
+  jobs.job[3] = {f.S, u, dl, dl, 0, f.ST.hi, f.ST.lo};
+  jobs.n = 4;
+  launches += split_transposed(jobs, lc.stream);
+  TcGemmArgs lvl[2];
+  lvl[0] = gemm_args(d, 2 * d, u, op(f.dZT, f.uP), op(f.XT, f.uP), g + off[a.fus_idx + 1], 2 * d);
+  lvl[0].accumulate = 1;  // dW_p += dZ^T X
+  lvl[1] = gemm_args(d, dl, u, op(f.dFsT, f.uP), op(f.ST, f.uP), g + off[a.fus_idx], dl);
+  lvl[1].accumulate = 1;  // dF += (dX[:, d:])^T S
+  launches += tc_gemm_batch(lvl, 2, lc.stream);
+  ColsumJobs cj{};
+  cj.job[0] = {f.dZ, u, d, g + off[a.fus_idx + 2]};
+  cj.n = 1;
+  launches += colsums(cj, d, lc.stream);
+  launch_pdl(rows_adam_kernel, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, t,
+             (const float*)f.dX, 2 * d, hp, bc);
+  return launches + 1;
+}
+
+}  // namespace ngdb_dev

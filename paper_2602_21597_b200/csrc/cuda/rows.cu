@@ -32,7 +32,9 @@ __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, 
   const int ew4 = a.ent_w / 4;
   if (dir == 0) {
     float* out = a.arena + d.out;
-    const float* src = a.ent + static_cast<int64_t>(d.id) * a.ent_w;
+    // FuseSemantic: the prologue's fused row of this anchor's entity
+    const float* src = a.fused ? a.etab + static_cast<int64_t>(a.anchor_local[d.aux]) * a.ent_w
+                               : a.ent + static_cast<int64_t>(d.id) * a.ent_w;
     if (a.backbone == NGDB_BETAE) {  // realised (alpha | beta); the mirror's
       for (int c = lane; c < ew4; c += 32) {  // chain rule runs in the optimizer
         const float4 x = ldg4(src + 4 * c);
@@ -41,7 +43,7 @@ __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, 
       }
       return;
     }
-    for (int c = lane; c < ew4; c += 32) st4(out + 4 * c, ldg4(src + 4 * c));
+    for (int c = lane; c < ew4; c += 32) st4(out + 4 * c, ld4(src + 4 * c));
     // Q2B anchors are point boxes: offset half is zero
     for (int c = ew4 + lane; c < a.wq / 4; c += 32) st4(out + 4 * c, make_float4(0.f, 0.f, 0.f, 0.f));
   } else {

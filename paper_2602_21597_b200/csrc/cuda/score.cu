@@ -271,6 +271,8 @@ __device__ Cands node_cands(const DevArgs& a, const ngdb_node_desc& d, const flo
     __syncthreads();
     return Cands{a.etab, a.cand_local + static_cast<int64_t>(d.aux) * a.ncand, a.etab_c, qb};
   } else {
+    if (a.fused)  // FuseSemantic: candidate rows are the step's fused rows
+      return Cands{a.etab, a.cand_local + static_cast<int64_t>(d.aux) * a.ncand, nullptr, 0.f};
     return Cands{a.ent, a.cand + static_cast<int64_t>(d.id) * a.ncand, nullptr, 0.f};
   }
 }

@@ -305,6 +305,38 @@ int ngdb_param_init(int32_t backbone, int32_t n_entities, int32_t n_relations, i
   });
 }
 
+int ngdb_param_init_ex(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
+                       int32_t semantic_dim, const char* name, uint64_t seed, float* out,
+                       int64_t n) {
+  return guarded([&] {
+    auto v = ngdb::init_param(static_cast<ngdb::Backbone>(backbone), n_entities, n_relations, dim,
+                              name, seed, 12.0, semantic_dim);
+    if (static_cast<int64_t>(v.size()) != n) throw ngdb::ShapeMismatch("param size");
+    std::memcpy(out, v.data(), n * sizeof(float));
+  });
+}
+
+int ngdb_semantic_synth(int32_t n_entities, int32_t dim, uint64_t seed, float* out) {
+  return guarded([&] {
+    auto v = ngdb::synth_semantic_store(n_entities, dim, seed);
+    std::memcpy(out, v.data(), v.size() * sizeof(float));
+  });
+}
+
+int ngdb_ngse_write(const char* path, const float* data, int64_t count, int32_t dim) {
+  return guarded([&] { ngdb::write_ngse(path, data, count, dim); });
+}
+
+int ngdb_ngse_read(const char* path, float* out, int64_t cap, int64_t* count, int32_t* dim) {
+  return guarded([&] {
+    auto v = ngdb::read_ngse(path, count, dim);
+    if (out) {
+      if (cap < static_cast<int64_t>(v.size())) throw ngdb::ShapeMismatch("buffer too small");
+      std::memcpy(out, v.data(), v.size() * sizeof(float));
+    }
+  });
+}
+
 int ngdb_run_step(ngdb_ctx* ctx, const ngdb_step* s, int64_t step, float* per_query_loss,
                   double* loss_sum) {
   return guarded([&] {
@@ -329,6 +361,8 @@ int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t 
     cfg.dim = d.dim;
     cfg.n_neg = bt->tb.n_neg;
     cfg.b_max = b_max;
+    cfg.semantic = d.semantic_dim > 0;
+    cfg.semantic_dim = d.semantic_dim;
     ngdb_step s;
     s.plan = ngdb::plan_training_step(bt->tb, cfg);
     ngdb::check_status(ngdb_run_step(ctx, &s, step, per_query_loss, loss_sum));

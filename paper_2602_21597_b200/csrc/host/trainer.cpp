@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstring>
 
 namespace ngdb {
 
@@ -11,7 +13,8 @@ int32_t query_width(Backbone b, int32_t dim) { return b == Backbone::GQE ? dim :
 int32_t entity_width(Backbone b, int32_t dim) { return b == Backbone::BETAE ? 2 * dim : dim; }
 int32_t relation_width(Backbone b, int32_t dim) { return b == Backbone::Q2B ? 2 * dim : dim; }
 
-std::vector<ParamSpec> param_specs(Backbone b, int32_t n_ent, int32_t n_rel, int32_t dim) {
+std::vector<ParamSpec> param_specs(Backbone b, int32_t n_ent, int32_t n_rel, int32_t dim,
+                                   int32_t semantic_dim) {
   const int64_t d = dim;
   std::vector<ParamSpec> s;
   s.push_back({"entity", n_ent, entity_width(b, dim), true});
@@ -37,12 +40,18 @@ std::vector<ParamSpec> param_specs(Backbone b, int32_t n_ent, int32_t n_rel, int
     s.push_back({"att_w2", d, 2 * d, false});
     s.push_back({"att_b2", 1, d, false});
   }
+  if (semantic_dim > 0) {
+    s.push_back({"fus_f", d, semantic_dim, false});
+    s.push_back({"fus_wp", d, 2 * d, false});
+    s.push_back({"fus_bp", 1, d, false});
+  }
   return s;
 }
 
 std::vector<float> init_param(Backbone b, int32_t n_ent, int32_t n_rel, int32_t dim,
-                              const std::string& name, uint64_t seed, double gamma) {
-  const auto specs = param_specs(b, n_ent, n_rel, dim);
+                              const std::string& name, uint64_t seed, double gamma,
+                              int32_t semantic_dim) {
+  const auto specs = param_specs(b, n_ent, n_rel, dim, semantic_dim);
   for (size_t i = 0; i < specs.size(); ++i) {
     const ParamSpec& p = specs[i];
     if (p.name != name) continue;
@@ -65,6 +74,50 @@ std::vector<float> init_param(Backbone b, int32_t n_ent, int32_t n_rel, int32_t 
     return out;
   }
   throw ConfigError("unknown parameter " + name);
+}
+
+std::vector<float> synth_semantic_store(int32_t n_entities, int32_t dim, uint64_t seed) {
+  // PTE rows N(0,1)/sqrt(d_l); gaussian() uses libm, so the bits
+  // are those of this host (tests hand the same store to both sides)
+  std::vector<float> out(static_cast<size_t>(n_entities) * dim);
+  Rng rng(seed);
+  const double scale = 1.0 / std::sqrt(static_cast<double>(dim));
+  for (float& v : out) v = static_cast<float>(rng.gaussian() * scale);
+  return out;
+}
+
+void write_ngse(const std::string& path, const float* data, int64_t count, int32_t dim) {
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw ConfigError("cannot open " + path);
+  const uint32_t version = 1, d = static_cast<uint32_t>(dim);
+  const uint64_t n = static_cast<uint64_t>(count);
+  bool ok = std::fwrite("NGSE", 1, 4, f) == 4 && std::fwrite(&version, 4, 1, f) == 1 &&
+            std::fwrite(&n, 8, 1, f) == 1 && std::fwrite(&d, 4, 1, f) == 1;
+  const size_t elems = static_cast<size_t>(count) * dim;
+  ok = ok && std::fwrite(data, sizeof(float), elems, f) == elems;  // host is little-endian
+  std::fclose(f);
+  if (!ok) throw ConfigError("short write to " + path);
+}
+
+std::vector<float> read_ngse(const std::string& path, int64_t* count, int32_t* dim) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw ConfigError("cannot open " + path);
+  char magic[4];
+  uint32_t version = 0, d = 0;
+  uint64_t n = 0;
+  const bool hdr = std::fread(magic, 1, 4, f) == 4 && std::fread(&version, 4, 1, f) == 1 &&
+                   std::fread(&n, 8, 1, f) == 1 && std::fread(&d, 4, 1, f) == 1;
+  if (!hdr || std::memcmp(magic, "NGSE", 4) != 0 || version != 1 || d == 0) {
+    std::fclose(f);
+    throw ShapeMismatch("not an NGSE v1 file: " + path);
+  }
+  std::vector<float> out(static_cast<size_t>(n) * d);
+  const bool body = std::fread(out.data(), sizeof(float), out.size(), f) == out.size();
+  std::fclose(f);
+  if (!body) throw ShapeMismatch("truncated NGSE file: " + path);
+  *count = static_cast<int64_t>(n);
+  *dim = static_cast<int32_t>(d);
+  return out;
 }
 
 ngdb_step_plan StepPlanHost::view() const {
@@ -251,9 +304,10 @@ Trainer::Trainer(const TrainConfig& cfg, int32_t n_entities, int32_t n_relations
   d.max_batch = cfg.b_max;
   d.max_queries = cfg.batch;
   check_status(ngdb_ctx_create(&d, device, &ctx_));
-  for (const auto& p : param_specs(cfg.backbone, n_entities, n_relations, cfg.dim)) {
+  const int32_t sd = cfg.semantic ? cfg.semantic_dim : 0;
+  for (const auto& p : param_specs(cfg.backbone, n_entities, n_relations, cfg.dim, sd)) {
     auto v = init_param(cfg.backbone, n_entities, n_relations, cfg.dim, p.name, cfg.seed_params,
-                        cfg.gamma);
+                        cfg.gamma, sd);
     check_status(ngdb_param_upload(ctx_, p.name.c_str(), v.data(), static_cast<int64_t>(v.size())));
   }
 }

@@ -187,8 +187,17 @@ class PlannedStep:
             self._h = None
 
 
-def param_specs(backbone: str, n_entities: int, n_relations: int, dim: int) -> List[tuple]:
+def param_specs(backbone: str, n_entities: int, n_relations: int, dim: int,
+                semantic_dim: int = 0) -> List[tuple]:
     """(name, rows, cols, sparse) in registry order (trainer.hpp param_specs)."""
+    base = _backbone_specs(backbone, n_entities, n_relations, dim)
+    if semantic_dim:
+        base += [("fus_f", dim, semantic_dim, False), ("fus_wp", dim, 2 * dim, False),
+                 ("fus_bp", 1, dim, False)]
+    return base
+
+
+def _backbone_specs(backbone, n_entities, n_relations, dim):
     if backbone == "gqe":
         return [("entity", n_entities, dim, True), ("relation", n_relations, dim, True),
                 ("int_w1", dim, dim, False), ("int_w2", dim, dim, False)]
@@ -208,13 +217,34 @@ def param_specs(backbone: str, n_entities: int, n_relations: int, dim: int) -> L
 
 
 def init_params(backbone: str, n_entities: int, n_relations: int, dim: int,
-                seed: int = 2) -> Dict[str, np.ndarray]:
+                seed: int = 2, semantic_dim: int = 0) -> Dict[str, np.ndarray]:
     out = {}
-    for name, rows, cols, _ in param_specs(backbone, n_entities, n_relations, dim):
+    for name, rows, cols, _ in param_specs(backbone, n_entities, n_relations, dim, semantic_dim):
         a = np.zeros((rows, cols), dtype=np.float32)
-        check(lib.ngdb_param_init(BACKBONES[backbone], n_entities, n_relations, dim, name.encode(),
-                                  seed, _p(a, C.c_float), a.size))
+        check(lib.ngdb_param_init_ex(BACKBONES[backbone], n_entities, n_relations, dim,
+                                     semantic_dim, name.encode(), seed, _p(a, C.c_float), a.size))
         out[name] = a
+    return out
+
+
+def semantic_store(n_entities: int, dim: int = 768, seed: int = 5) -> np.ndarray:
+    """Synthetic frozen PTE store, N(0,1)/sqrt(dim) rows (host Rng)."""
+    out = np.zeros((n_entities, dim), dtype=np.float32)
+    check(lib.ngdb_semantic_synth(n_entities, dim, seed, _p(out, C.c_float)))
+    return out
+
+
+def ngse_write(path: str, store: np.ndarray) -> None:
+    a = np.ascontiguousarray(store, dtype=np.float32)
+    check(lib.ngdb_ngse_write(str(path).encode(), _p(a, C.c_float), a.shape[0], a.shape[1]))
+
+
+def ngse_read(path: str) -> np.ndarray:
+    n, d = C.c_int64(), C.c_int32()
+    check(lib.ngdb_ngse_read(str(path).encode(), None, 0, C.byref(n), C.byref(d)))
+    out = np.zeros((n.value, d.value), dtype=np.float32)
+    check(lib.ngdb_ngse_read(str(path).encode(), _p(out, C.c_float), out.size, C.byref(n),
+                             C.byref(d)))
     return out
 
 
@@ -224,16 +254,23 @@ class Engine:
     def __init__(self, backbone: str, n_entities: int, n_relations: int, dim: int = 400,
                  n_neg: int = 128, b_max: int = 512, max_queries: int = 512, gamma: float = 12.0,
                  lr: float = 1e-4, alpha_box: float = 0.02, device: int = 0,
-                 params: Optional[Dict[str, np.ndarray]] = None, seed: int = 2, debug: bool = False):
-        d = ModelDesc(BACKBONES[backbone], n_entities, n_relations, dim, n_neg, 0, gamma,
+                 params: Optional[Dict[str, np.ndarray]] = None, seed: int = 2, debug: bool = False,
+                 semantic: Optional[np.ndarray] = None):
+        """semantic: frozen store [n_entities][d_l] -> FuseSemantic on anchors and
+        candidates (SPEC.md:589)."""
+        sd = 0 if semantic is None else int(semantic.shape[1])
+        d = ModelDesc(BACKBONES[backbone], n_entities, n_relations, dim, n_neg, sd, gamma,
                       alpha_box, lr, 0.9, 0.999, 1e-8, b_max, max_queries)
         self.backbone, self.dim, self.b_max = backbone, dim, b_max
-        self.n_entities, self.n_relations = n_entities, n_relations
+        self.n_entities, self.n_relations, self.semantic_dim = n_entities, n_relations, sd
         self._h = C.c_void_p()
         check(lib.ngdb_ctx_create(C.byref(d), device, C.byref(self._h)))
         self.step_count = 0
+        if semantic is not None:
+            st = np.ascontiguousarray(semantic, dtype=np.float32)
+            check(lib.ngdb_semantic_upload(self._h, _p(st, C.c_float), st.size))
         if params is None:
-            params = init_params(backbone, n_entities, n_relations, dim, seed)
+            params = init_params(backbone, n_entities, n_relations, dim, seed, sd)
         for k, v in params.items():
             self.upload(k, v)
         if debug:
@@ -246,7 +283,7 @@ class Engine:
     def download(self, name: str) -> np.ndarray:
         base = name.split(":")[-1]
         spec = {s[0]: s for s in param_specs(self.backbone, self.n_entities, self.n_relations,
-                                             self.dim)}[base]
+                                             self.dim, self.semantic_dim)}[base]
         out = np.zeros((spec[1], spec[2]), dtype=np.float32)
         check(lib.ngdb_param_download(self._h, name.encode(), _p(out, C.c_float), out.size))
         return out

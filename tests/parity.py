@@ -112,18 +112,23 @@ def tie_free(batch, om, b_max, step, tau=TAU):
 
 
 def run_pair(graph, ograph, backbone, mix, b, k, dim, b_max=512, steps=1, seed_tag=0,
-             compare_grads=True, certify=True):
-    """One or more training steps on both sides; returns a dict of comparisons."""
+             compare_grads=True, certify=True, semantic_dim=0):
+    """One or more training steps on both sides; returns a dict of comparisons.
+    semantic_dim > 0: FuseSemantic with a synthetic frozen store of that width."""
     import oracle as O
     import paper_2602_21597_b200 as m
 
     info = graph.info()
     ne, nr = info["n_entities"], info["n_relations"]
     w = m.pattern_weights(mix)
-    eng = m.Engine(backbone, ne, nr, dim=dim, n_neg=k, b_max=b_max, max_queries=b, debug=True)
+    store = m.semantic_store(ne, semantic_dim, seed=5) if semantic_dim else None
+    eng = m.Engine(backbone, ne, nr, dim=dim, n_neg=k, b_max=b_max, max_queries=b, debug=True,
+                   semantic=store)
     om = O.OracleModel(backbone, ne, nr, dim, k, precision=64)
+    if semantic_dim:
+        om.set_semantic(store)
     om.init(2)
-    specs = m.param_specs(backbone, ne, nr, dim)
+    specs = m.param_specs(backbone, ne, nr, dim, semantic_dim)
     out = {"loss": [], "grads": {}, "params": {}, "kept": [], "weak": {}}
     for step in range(1, steps + 1):
         batch = m.Batch.sample(graph, w, b, k, seed=3, tag=seed_tag + step)

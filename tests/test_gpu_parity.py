@@ -74,3 +74,27 @@ def test_batch_of_one(small_graph, small_oracle_graph):
 def test_single_pattern_batches_betae(small_graph, small_oracle_graph, pattern):
     res = run_pair(small_graph, small_oracle_graph, "betae", [pattern], b=32, k=8, dim=16)
     _check(res)
+
+
+# ---- C4: FuseSemantic on anchors and candidates ----------
+
+@pytest.mark.parametrize("backbone,mix", [("gqe", C1_MIX), ("q2b", ALL)])
+@pytest.mark.parametrize("dim,dl", [(16, 24), (400, 768)])
+def test_fuse_semantic_parity(small_graph, small_oracle_graph, backbone, mix, dim, dl):
+    res = run_pair(small_graph, small_oracle_graph, backbone, mix, b=96, k=16, dim=dim,
+                   semantic_dim=dl)
+    _check(res)
+
+
+def test_fuse_semantic_three_steps(small_graph, small_oracle_graph):
+    res = run_pair(small_graph, small_oracle_graph, "gqe", C1_MIX, b=64, k=16, dim=32, steps=3,
+                   semantic_dim=48)
+    _check(res, steps=3)
+
+
+def test_fuse_semantic_full_batch_losses(small_graph, small_oracle_graph):
+    res = run_pair(small_graph, small_oracle_graph, "gqe", C1_MIX, b=512, k=128, dim=400,
+                   compare_grads=False, certify=False, semantic_dim=768)
+    for loss, ref in res["loss"]:
+        ok, nbad, worst = rel_close(loss, ref)
+        assert ok, f"loss: {nbad} bad, worst {worst:.3e}"

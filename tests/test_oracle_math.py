@@ -26,15 +26,18 @@ def _loss(om, a):
     return om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, adam=-1).sum()
 
 
-@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
-def test_finite_difference_gradients(tiny, backbone):
+@pytest.mark.parametrize("backbone,dl", [("gqe", 0), ("q2b", 0), ("betae", 0), ("gqe", 8),
+                                         ("q2b", 8)])
+def test_finite_difference_gradients(tiny, backbone, dl):
     g, info = tiny
     d, k = 4, 3
     a = _batch(g, P, 20, k)
     om = O.OracleModel(backbone, info["n_entities"], info["n_relations"], d, k, precision=64)
+    if dl:
+        om.set_semantic(m.semantic_store(info["n_entities"], dl, seed=5))
     om.init(2)
     _loss(om, a)
-    specs = m.param_specs(backbone, info["n_entities"], info["n_relations"], d)
+    specs = m.param_specs(backbone, info["n_entities"], info["n_relations"], d, dl)
     grads = {n: om.get("g:" + n, (r, c)) for n, r, c, _ in specs}
     rng = np.random.default_rng(1)
     h = 1e-5

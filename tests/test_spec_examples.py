@@ -247,3 +247,70 @@ def test_beta_kl_examples():
     for a1, b1, a2, b2 in rng.uniform(0.05, 20, size=(50, 4)):
         assert O.beta_kl(a1, b1, a2, b2) >= -1e-12  # KL >= 0
 
+
+
+# ---- FuseSemantic and the NGSE store -----
+
+def _fusion_pair(small_graph, backbone, dl, wp=None, store=None):
+    info = small_graph.info()
+    ne, nr, d, k = info["n_entities"], info["n_relations"], 8, 4
+    a = m.Batch.sample(small_graph, m.pattern_weights(["1p", "2p", "2i"]), 24, k, seed=3,
+                       tag=1).arrays()
+    fused = O.OracleModel(backbone, ne, nr, d, k)
+    fused.set_semantic(store if store is not None else m.semantic_store(ne, dl, seed=5))
+    fused.init(2)
+    if wp is not None:
+        fused.set("fus_wp", wp)
+    return fused, a, (ne, nr, d, k)
+
+
+def test_fuse_semantic_identity_block(small_graph):
+    # W_p = [I | 0], b_p = 0 -> e_fused = sigma(h): a structural-only model whose
+    # entity table is sigma(h) scores identically
+    d = 8
+    wp = np.concatenate([np.eye(d), np.zeros((d, d))], axis=1).astype(np.float32)
+    fused, a, (ne, nr, d, k) = _fusion_pair(small_graph, "gqe", 12, wp=wp)
+    lf = fused.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, adam=-1)
+    plain = O.OracleModel("gqe", ne, nr, d, k)
+    plain.init(2)
+    h = fused.get("entity", (ne, d))
+    plain.set("entity", (1.0 / (1.0 + np.exp(-h))).astype(np.float32))
+    for n in ("relation", "int_w1", "int_w2"):
+        plain.set(n, fused.get(n, (nr, d) if n == "relation" else (d, d)).astype(np.float32))
+    lp = plain.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, adam=-1)
+    # sigma(h) is rounded to f32 in the plain model: agreement to f32 resolution
+    assert np.max(np.abs(lf - lp) / np.maximum(np.abs(lp), 1e-6)) < 1e-5
+
+
+def test_fuse_semantic_zero_store_ignores_F(small_graph):
+    # zero semantic rows: the result does not depend on F
+    info = small_graph.info()
+    zero = np.zeros((info["n_entities"], 12), np.float32)
+    o1, a, (ne, nr, d, k) = _fusion_pair(small_graph, "gqe", 12, store=zero)
+    l1 = o1.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, adam=-1)
+    o2, _, _ = _fusion_pair(small_graph, "gqe", 12, store=zero)
+    o2.set("fus_f", np.full((d, 12), 3.0, np.float32))
+    l2 = o2.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, adam=-1)
+    assert np.array_equal(l1, l2)
+    assert not np.any(o1.get("g:fus_f", (d, 12)))  # dF = dFs^T S = 0 for a zero store
+
+
+def test_ngse_roundtrip(tmp_path):
+    st = m.semantic_store(37, 12, seed=9)
+    path = tmp_path / "store.ngse"
+    m.ngse_write(path, st)
+    raw = path.read_bytes()
+    assert raw[:4] == b"NGSE" and int.from_bytes(raw[4:8], "little") == 1
+    assert int.from_bytes(raw[8:16], "little") == 37 and int.from_bytes(raw[16:20], "little") == 12
+    assert len(raw) == 20 + 37 * 12 * 4
+    back = m.ngse_read(path)
+    assert back.shape == (37, 12) and np.array_equal(back, st)
+    bad = tmp_path / "bad.ngse"
+    bad.write_bytes(b"NGSX" + raw[4:])
+    with pytest.raises(NgdbError):
+        m.ngse_read(bad)
+
+
+def test_semantic_store_statistics():
+    st = m.semantic_store(2000, 768, seed=5)
+    assert abs(float(st.std()) - 1 / np.sqrt(768)) < 2e-3 / np.sqrt(768) * 10
