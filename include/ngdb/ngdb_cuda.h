@@ -65,6 +65,8 @@ typedef struct ngdb_model_desc {
   float beta1, beta2, eps_adam; /* 0.9, 0.999, 1e-8 */
   int32_t max_batch;    /* B_max: widest kernel invocation */
   int32_t max_queries;  /* queries per step the plan buffers are sized for */
+  int32_t world;        /* > 1: entity table row-sharded over `world` ranks; this */
+  int32_t rank;         /*   context holds rows e = rank (mod world) */
 } ngdb_model_desc;
 
 /* One operator node of a kernel invocation. Offsets are float-element offsets
@@ -114,6 +116,46 @@ typedef struct ngdb_step_plan {
   const int32_t* relation_contrib;
 } ngdb_step_plan;
 
+/* Owner-side work of one rank in the row-sharded step (ngdb/shard.hpp). */
+typedef struct ngdb_shard_plan {
+  int32_t world, rank, batch, max_anchors, max_slots, n_candidates;
+  const int32_t* anchor_ids; /* [world][max_anchors] entity of every rank's anchor slot */
+  const int32_t* unit_k;     /* [world][batch] score slots of each query (1, or 2-3 union branches) */
+  const int32_t* unit_slots; /* [world][batch][3] */
+  const int32_t* cand;       /* [world][batch][n_candidates] global entity ids */
+  const int32_t* unit_off;   /* [world*batch + 1] owned candidate positions per unit */
+  const int32_t* owned;
+  int32_t n_rows;            /* owner CSR over local entity rows */
+  const int32_t* rows;
+  const int32_t* seg;
+  const int32_t* contrib;
+} ngdb_shard_plan;
+
+/* Exchange buffers of the sharded step, owned by the context (device memory,
+ * float32, sizes in elements). The caller runs the collectives between stages:
+ *   reduce-scatter(sum) anchor_send [world][A][ew]  -> anchor_rows [A][ew]
+ *   all-gather          query_mine [S][wq]          -> query_all [world][S][wq]
+ *   reduce-scatter(sum) dq_part [world][S][wq]      -> dq_mine [S][wq]
+ *   reduce-scatter(sum) loss_part [world][B]        -> loss_mine [B]
+ *   all-to-all          grad_send [world][A][ew]    -> grad_all [world][A][ew]
+ *   all-reduce(sum)     reduce [dense grads | relation grads | relation touched] */
+typedef struct ngdb_shard_buffers {
+  float *anchor_send, *anchor_rows, *query_mine, *query_all, *dq_part, *dq_mine, *loss_part,
+      *loss_mine, *grad_send, *grad_all, *reduce;
+  int64_t n_anchor_send, n_anchor_rows, n_query_mine, n_query_all, n_dq_part, n_dq_mine,
+      n_loss_part, n_loss_mine, n_grad_send, n_grad_all, n_reduce;
+} ngdb_shard_buffers;
+
+typedef enum ngdb_shard_stage {
+  NGDB_SHARD_ANCHOR_PACK = 0, /* owned rows of every rank's anchors -> anchor_send */
+  NGDB_SHARD_FORWARD = 1,     /* forward pools except Score / UnionScore / Loss (trace order) */
+  NGDB_SHARD_QUERY_PACK = 2,  /* score-slot queries -> query_mine */
+  NGDB_SHARD_SCORE = 3,       /* owner scoring of all ranks' units over owned candidates */
+  NGDB_SHARD_SCORE_DONE = 4,  /* dq_mine / loss_mine -> this rank's Loss results */
+  NGDB_SHARD_BACKWARD = 5,    /* backward pools (trace order) */
+  NGDB_SHARD_GRAD_PACK = 6    /* anchor grads -> grad_send; dense + relation grads -> reduce */
+} ngdb_shard_stage;
+
 typedef struct ngdb_ctx ngdb_ctx;
 typedef struct ngdb_plan ngdb_plan;
 
@@ -155,6 +197,16 @@ int ngdb_plan_run(ngdb_ctx* ctx, ngdb_plan* plan, int64_t step); /* all pools + 
  * plan's first run costs one graph launch. Call after the last plan_create of
  * a context (a later buffer growth invalidates the capture). */
 int ngdb_plan_prepare(ngdb_ctx* ctx, ngdb_plan* plan);
+
+/* Row-sharded step: begin, then stages with the collectives of
+ * ngdb_shard_buffers between them, then ngdb_shard_optimizer and ngdb_step_end. */
+int ngdb_shard_begin(ngdb_ctx* ctx, const ngdb_step_plan* plan, const ngdb_shard_plan* shard,
+                     ngdb_shard_buffers* bufs);
+int ngdb_shard_run(ngdb_ctx* ctx, int32_t stage);
+int ngdb_shard_optimizer(ngdb_ctx* ctx, int64_t step);
+/* Run the context's launches on an external stream (e.g. the framework stream
+ * that also carries the collectives); NULL restores the private stream. */
+int ngdb_ctx_set_stream(ngdb_ctx* ctx, void* cuda_stream);
 int ngdb_plan_destroy(ngdb_plan* plan);
 
 /* Device timing on the context stream (CUDA events). */

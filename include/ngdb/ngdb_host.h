@@ -59,6 +59,24 @@ int ngdb_step_trace_json(const ngdb_step* s, int32_t with_nodes, char* buf, int6
                          int64_t* len);
 int ngdb_step_destroy(ngdb_step* s);
 
+/* --- row-sharded step (ngdb/shard.hpp) ---------------------- */
+typedef struct ngdb_shard ngdb_shard;
+/* this rank's metadata for the host all-gather */
+int ngdb_step_shard_info(const ngdb_step* s, int32_t* n_anchor_slots, int32_t* n_score_slots,
+                         int32_t* batch, int32_t* n_candidates);
+int ngdb_step_shard_meta(const ngdb_step* s, int32_t* anchor_ids, int32_t* unit_k,
+                         int32_t* unit_slots, int32_t* cand);
+int ngdb_shard_build(int32_t world, int32_t rank, int32_t batch, int32_t max_anchors,
+                     int32_t max_slots, int32_t n_candidates, const int32_t* anchor_ids_all,
+                     const int32_t* unit_k_all, const int32_t* unit_slots_all,
+                     const int32_t* cand_all, ngdb_shard** out);
+int ngdb_shard_view(const ngdb_shard* s, ngdb_shard_plan* view);
+int ngdb_shard_destroy(ngdb_shard* s);
+/* rows e = rank (mod world) of a parameter's deterministic init (entity table) */
+int ngdb_param_init_shard(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
+                          const char* name, uint64_t seed, int32_t world, int32_t rank,
+                          float* out, int64_t n);
+
 /* --- reference-interface helpers (common.hpp:60-127) ----- */
 /* Rng(seed) (forked with fork_tag when >= 0), `skip` draws discarded, next draw */
 uint64_t ngdb_rng_next(uint64_t seed, int64_t fork_tag, int32_t skip);

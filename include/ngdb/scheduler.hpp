@@ -32,6 +32,11 @@ struct SchedulerConfig {
   int32_t n_candidates = 129; // 1 + K
   int32_t elem_bytes = 4;     // trace byte accounting (f32 throughput mode)
   ReleasePolicy policy = ReleasePolicy::Eager;
+  // Device slots: reuse freed slots (the Eq. 7 replay) or give every tensor its
+  // own slot. The sharded step runs forward / scoring / backward as phases
+  // (DESIGN.md §6), an order the reuse plan does not cover; the trace itself is
+  // always the Eq. 7 replay of `policy`.
+  bool device_reuse = true;
 };
 
 // One PopBatch: a drain of the selected pool.

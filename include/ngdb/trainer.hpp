@@ -30,6 +30,7 @@ struct TrainConfig {
   int32_t b_max = 512;
   bool semantic = false;
   int32_t semantic_dim = 0;
+  bool sharded = false;  // entity table row-sharded across ranks
   uint64_t seed_params = 2;
   uint64_t seed_sampler = 3;
 };
@@ -67,6 +68,11 @@ struct StepPlanHost {
   int32_t n_queries = 0, n_candidates = 0;
   int32_t n_score_slots = 0, n_anchor_slots = 0, n_project_slots = 0;
   int64_t arena_elems = 0;
+  // scoring units (sharded step): per query, its score slots — the Loss slot,
+  // or the branch Score slots of a union in UnionScore input order — and the
+  // entity of every anchor slot
+  std::vector<int32_t> unit_k, unit_slots;  // [B], [B][3] (-1 padded)
+  std::vector<int32_t> anchor_ids;          // [n_anchor_slots]
   ExecutionTrace trace;
   ngdb_step_plan view() const;
 };

@@ -48,6 +48,8 @@ _SIG = {
     "oracle_q2b_distance": (f64, [P(f64), P(f64), P(f64), i32, f64]),
     "oracle_loss": (f64, [f64, f64, P(f64), i32]),
     "oracle_lgamma": (f64, [f64]),
+    "oracle_model_step_multi": (C.c_int, [C.c_void_p, i32, P(i32), P(i32), P(i32), P(i32), P(i32),
+                                          P(i32), i32, i64, i32, P(f64)]),
     "oracle_model_set_semantic": (C.c_int, [C.c_void_p, i32, P(C.c_float), i64]),
     "oracle_digamma": (f64, [f64]),
     "oracle_trigamma": (f64, [f64]),
@@ -152,6 +154,18 @@ class OracleModel:
         _check(lib.oracle_model_step(self._h, b, *[_p(x, i32) for x in arrs], b_max, step,
                                      executor, adam, int(eager), _p(losses, f64)))
         return losses
+
+    def step_multi(self, batches, b_max=512, step=1, adam=0):
+        """Sub-batches (one per rank) scheduled independently, gradients summed,
+        one Adam step: the parity reference of the row-sharded step."""
+        sizes = np.array([len(x.patterns) for x in batches], np.int32)
+        cat = [np.ascontiguousarray(np.concatenate([getattr(x, f) for x in batches]), dtype=np.int32)
+               for f in ("patterns", "anchors", "relations", "positives", "negatives")]
+        losses = np.zeros(int(sizes.sum()), np.float64)
+        _check(lib.oracle_model_step_multi(self._h, len(batches), _p(sizes, i32),
+                                           *[_p(x, i32) for x in cat], b_max, step, adam,
+                                           _p(losses, f64)))
+        return np.split(losses, np.cumsum(sizes)[:-1])
 
     def margins(self, b):
         out = np.zeros(b, np.float64)

@@ -59,6 +59,11 @@ int oracle_model_destroy(void* m);
 /* scalar kernels for the SPEC known-answer tests */
 double oracle_q2b_distance(const double* v, const double* c, const double* o, int32_t d,
                            double alpha);
+/* sub-batches scheduled independently, gradients summed, one Adam (sharded parity) */
+int oracle_model_step_multi(void* model, int32_t n, const int32_t* sizes, const int32_t* patterns,
+                            const int32_t* anchors, const int32_t* relations,
+                            const int32_t* positives, const int32_t* negatives, int32_t b_max,
+                            int64_t step, int32_t adam, double* losses);
 /* frozen semantic store [ne][dl] + fusion params (call before oracle_model_init) */
 int oracle_model_set_semantic(void* model, int32_t dl, const float* store, int64_t n);
 double oracle_loss(double gamma, double d_pos, const double* d_neg, int32_t k);

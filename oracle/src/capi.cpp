@@ -309,8 +309,39 @@ int oracle_model_step(void* mp, int32_t b, const int32_t* patterns, const int32_
         for (int j = 0; j < md.k; ++j) cand[(size_t)i * (md.k + 1) + 1 + j] = negatives[(size_t)i * md.k + j];
       }
       a->last = o_train_step(md, d, cand, b_max, eager != 0, executor == 1, step, adam == 0,
-                             adam >= 0);
+                             adam >= 0, true);
       for (int i = 0; i < b; ++i) losses[i] = double(md.losses[i]);
+    };
+    if (a->m64) run(*a->m64);
+    else run(*a->m32);
+  });
+}
+
+// SURVEY §8(e) parity mode of the row-sharded step: each of n sub-batches (one
+// per rank) is scheduled independently, their gradients summed, then ONE Adam.
+int oracle_model_step_multi(void* mp, int32_t n, const int32_t* sizes, const int32_t* patterns,
+                            const int32_t* anchors, const int32_t* relations,
+                            const int32_t* positives, const int32_t* negatives, int32_t b_max,
+                            int64_t step, int32_t adam, double* losses) {
+  return guard([&] {
+    auto* a = static_cast<AnyModel*>(mp);
+    auto run = [&](auto& md) {
+      int64_t off = 0;
+      for (int32_t t = 0; t < n; ++t) {
+        const int32_t b = sizes[t];
+        ODag d = o_build_training_dag(queries_of(b, patterns + off, anchors + 3 * off,
+                                                 relations + 4 * off));
+        std::vector<int> cand((size_t)b * (md.k + 1));
+        for (int i = 0; i < b; ++i) {
+          cand[(size_t)i * (md.k + 1)] = positives[off + i];
+          for (int j = 0; j < md.k; ++j)
+            cand[(size_t)i * (md.k + 1) + 1 + j] = negatives[(off + i) * md.k + j];
+        }
+        a->last = o_train_step(md, d, cand, b_max, true, false, step, adam == 0,
+                               adam >= 0 && t == n - 1, t == 0);
+        for (int i = 0; i < b; ++i) losses[off + i] = double(md.losses[i]);
+        off += b;
+      }
     };
     if (a->m64) run(*a->m64);
     else run(*a->m32);

@@ -939,10 +939,13 @@ struct Exec {
 // ---- explicit instantiation helpers used by capi.cpp ------------------------
 template <class R>
 OTrace o_train_step(Model<R>& md, const ODag& g, const std::vector<int>& cand, int b_max,
-                    bool eager, bool sequential, int64_t step, bool lazy, bool apply_adam) {
-  for (auto& kv : md.G) std::fill(kv.second.begin(), kv.second.end(), R(0));
-  md.touchedE.clear();
-  md.touchedR.clear();
+                    bool eager, bool sequential, int64_t step, bool lazy, bool apply_adam,
+                    bool zero_grads) {
+  if (zero_grads) {
+    for (auto& kv : md.G) std::fill(kv.second.begin(), kv.second.end(), R(0));
+    md.touchedE.clear();
+    md.touchedR.clear();
+  }
   int nq = 0;
   for (const auto& n : g.nodes) nq = std::max(nq, n.query + 1);
   md.losses.assign(nq, R(0));
@@ -960,9 +963,9 @@ OTrace o_train_step(Model<R>& md, const ODag& g, const std::vector<int>& cand, i
 template struct Model<double>;
 template struct Model<float>;
 template OTrace o_train_step<double>(Model<double>&, const ODag&, const std::vector<int>&, int,
-                                     bool, bool, int64_t, bool, bool);
+                                     bool, bool, int64_t, bool, bool, bool);
 template OTrace o_train_step<float>(Model<float>&, const ODag&, const std::vector<int>&, int, bool,
-                                    bool, int64_t, bool, bool);
+                                    bool, int64_t, bool, bool, bool);
 
 std::string OTrace::json(bool with_nodes) const {
   static const char* kNames[8] = {"EmbedAnchor", "FuseSemantic", "Project", "Negate",

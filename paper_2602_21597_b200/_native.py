@@ -22,7 +22,7 @@ class ModelDesc(C.Structure):
         ("backbone", i32), ("n_entities", i32), ("n_relations", i32), ("dim", i32),
         ("n_neg", i32), ("semantic_dim", i32), ("gamma", f32), ("alpha_box", f32),
         ("lr", f32), ("beta1", f32), ("beta2", f32), ("eps_adam", f32),
-        ("max_batch", i32), ("max_queries", i32),
+        ("max_batch", i32), ("max_queries", i32), ("world", i32), ("rank", i32),
     ]
 
 
@@ -46,6 +46,24 @@ class StepPlan(C.Structure):
     ]
 
 
+class ShardPlan(C.Structure):
+    _fields_ = [
+        ("world", i32), ("rank", i32), ("batch", i32), ("max_anchors", i32), ("max_slots", i32),
+        ("n_candidates", i32), ("anchor_ids", P(i32)), ("unit_k", P(i32)),
+        ("unit_slots", P(i32)), ("cand", P(i32)), ("unit_off", P(i32)), ("owned", P(i32)),
+        ("n_rows", i32), ("rows", P(i32)), ("seg", P(i32)), ("contrib", P(i32)),
+    ]
+
+
+SHARD_BUFFERS = ("anchor_send", "anchor_rows", "query_mine", "query_all", "dq_part", "dq_mine",
+                 "loss_part", "loss_mine", "grad_send", "grad_all", "reduce")
+
+
+class ShardBuffers(C.Structure):
+    _fields_ = ([(n, C.c_void_p) for n in SHARD_BUFFERS] +
+                [("n_" + n, i64) for n in SHARD_BUFFERS])
+
+
 # (name, restype, argtypes) for every exported entry point of include/ngdb/*.h
 SIGNATURES = {
     # ngdb_cuda.h
@@ -66,6 +84,10 @@ SIGNATURES = {
     "ngdb_plan_create": (C.c_int, [C.c_void_p, P(StepPlan), P(C.c_void_p)]),
     "ngdb_plan_run": (C.c_int, [C.c_void_p, C.c_void_p, i64]),
     "ngdb_plan_prepare": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ngdb_shard_begin": (C.c_int, [C.c_void_p, P(StepPlan), P(ShardPlan), P(ShardBuffers)]),
+    "ngdb_shard_run": (C.c_int, [C.c_void_p, i32]),
+    "ngdb_shard_optimizer": (C.c_int, [C.c_void_p, i64]),
+    "ngdb_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ngdb_plan_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_sync": (C.c_int, [C.c_void_p]),
     "ngdb_timer_start": (C.c_int, [C.c_void_p]),
@@ -98,6 +120,14 @@ SIGNATURES = {
     "ngdb_step_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_param_init": (C.c_int, [i32, i32, i32, i32, C.c_char_p, u64, P(f32), i64]),
     "ngdb_param_init_ex": (C.c_int, [i32, i32, i32, i32, i32, C.c_char_p, u64, P(f32), i64]),
+    "ngdb_param_init_shard": (C.c_int, [i32, i32, i32, i32, C.c_char_p, u64, i32, i32, P(f32),
+                                        i64]),
+    "ngdb_step_shard_info": (C.c_int, [C.c_void_p, P(i32), P(i32), P(i32), P(i32)]),
+    "ngdb_step_shard_meta": (C.c_int, [C.c_void_p, P(i32), P(i32), P(i32), P(i32)]),
+    "ngdb_shard_build": (C.c_int, [i32, i32, i32, i32, i32, i32, P(i32), P(i32), P(i32), P(i32),
+                                   P(C.c_void_p)]),
+    "ngdb_shard_view": (C.c_int, [C.c_void_p, P(ShardPlan)]),
+    "ngdb_shard_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_semantic_synth": (C.c_int, [i32, i32, u64, P(f32)]),
     "ngdb_ngse_write": (C.c_int, [C.c_char_p, P(f32), i64, i32]),
     "ngdb_ngse_read": (C.c_int, [C.c_char_p, P(f32), i64, P(i64), P(i32)]),

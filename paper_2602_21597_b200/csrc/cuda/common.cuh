@@ -75,6 +75,23 @@ struct DevArgs {
   const float* sem;      // frozen store [n_entities][sem_dim]
   int32_t* anchor_local;
   int32_t fus_idx;       // dense index of fus_f (fus_wp = +1, fus_bp = +2)
+  // row-sharded step (shard.cu): anchor rows fetched from their owners [A][ent_w]
+  const float* anc_rows;
+};
+
+// Device view of the sharded step's owner work (ngdb_shard_plan + buffers).
+struct ShardDev {
+  int32_t world, rank, batch, max_anchors, max_slots;
+  const int32_t* anchor_ids;
+  const int32_t* unit_k;
+  const int32_t* unit_slots;
+  const int32_t* cand;
+  const int32_t* unit_off;
+  const int32_t* owned;
+  const float* query_all;  // [world*max_slots][wq]
+  float* dq_part;          // [world*max_slots][wq]
+  float* loss_part;        // [world*batch]
+  float* coef_all;         // [world*max_slots][ncand]
 };
 
 // Programmatic dependent launch: let the next kernel in the stream start its
@@ -194,6 +211,19 @@ int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
 int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const AdamHyper& hp,
                   const float* bc, const LaunchCtx& lc);
 int launch_beta_entity_adam(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
+                            const float* bc, const LaunchCtx& lc);
+// shard.cu (row-sharded step)
+int launch_shard_anchor_pack(const DevArgs& a, const ShardDev& sd, float* send, const LaunchCtx& lc);
+int launch_shard_query_pack(const DevArgs& a, int first, int n, float* dst, const LaunchCtx& lc);
+int launch_shard_score(const DevArgs& a, const ShardDev& sd, const LaunchCtx& lc);
+int launch_shard_score_done(const DevArgs& a, const float* dq_mine, int64_t n_dq,
+                            const float* loss_mine, int nq, const LaunchCtx& lc);
+int launch_shard_grad_pack(const DevArgs& a, const ShardDev& sd, int n_anchor, float* send,
+                           const LaunchCtx& lc);
+int launch_shard_rel_pack(const DevArgs& a, const SparseTable& t, float* rel_g, float* touched,
+                          const LaunchCtx& lc);
+int launch_masked_rows_adam(float* w, float* m, float* v, float* dbg, const float* g,
+                            const float* touched, int rows, int width, const AdamHyper& hp,
                             const float* bc, const LaunchCtx& lc);
 int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, const AdamHyper& hp,
                       const float* bc, const LaunchCtx& lc);

@@ -188,6 +188,25 @@ struct ngdb_ctx {
   float* fscratch = nullptr;
   int64_t fscratch_cap = 0;
   int fus_idx = -1;
+  // row-sharded step (shard.cu)
+  int world = 1, rank = 0;
+  cudaStream_t own_stream = nullptr;
+  const float* anc_rows = nullptr;  // set while a sharded step runs
+  struct ShardState {
+    int32_t* blob = nullptr;
+    int64_t blob_cap = 0;
+    int32_t* staging = nullptr;
+    int64_t staging_cap = 0;
+    cudaEvent_t staged = nullptr;
+    float* buf = nullptr;
+    int64_t buf_cap = 0;
+    ShardDev dev{};
+    ngdb_shard_buffers bufs{};
+    float* coef_all = nullptr;
+    int32_t n_rows = 0;
+    const int32_t *rows = nullptr, *seg = nullptr, *contrib = nullptr;
+    bool active = false;
+  } sh;
   // streaming plans: double-buffered pinned staging + device blobs
   int32_t* staging[2] = {nullptr, nullptr};
   int64_t staging_cap[2] = {0, 0};
@@ -365,6 +384,7 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.sem = c->sem;
   a.anchor_local = c->anchor_local;
   a.fus_idx = c->fus_idx;
+  a.anc_rows = c->anc_rows;
   return a;
 }
 
@@ -631,16 +651,26 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       throw Fail{NGDB_ERR_CONFIG, "semantic_dim must be a multiple of 4, <= 4096"};
     if (d.semantic_dim > 0 && d.backbone == NGDB_BETAE)
       throw Fail{NGDB_ERR_MISSING_KERNEL, "BetaE + FuseSemantic (Psi_theta) not built"};
+    const int world = d.world > 1 ? d.world : 1;
+    if (world > 1 && (d.rank < 0 || d.rank >= world)) throw Fail{NGDB_ERR_CONFIG, "rank out of range"};
+    if (world > 1 && (d.backbone == NGDB_BETAE || d.semantic_dim > 0))
+      throw Fail{NGDB_ERR_MISSING_KERNEL, "row-sharded step is built for GQE / Q2B without fusion"};
     c = new ngdb_ctx();
     c->desc = d;
+    c->world = world;
+    c->rank = world > 1 ? d.rank : 0;
     if (c->desc.max_batch <= 0) c->desc.max_batch = 512;
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     CK(cudaSetDevice(device));
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    CK(cudaEventCreateWithFlags(&c->sh.staged, cudaEventDisableTiming));
     const int64_t D = d.dim;
+    // this rank's entity rows e = rank (mod world), local row e div world
+    const int64_t n_ent_local = (d.n_entities - c->rank + world - 1) / world;
     if (d.backbone == NGDB_GQE) {
-      add_param(c, "entity", d.n_entities, D, true);
+      add_param(c, "entity", n_ent_local, D, true);
       add_param(c, "relation", d.n_relations, D, true);
       add_param(c, "int_w1", D, D, false);
       add_param(c, "int_w2", D, D, false);
@@ -656,7 +686,7 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       add_param(c, "att_w2", D, 2 * D, false);
       add_param(c, "att_b2", 1, D, false);
     } else {
-      add_param(c, "entity", d.n_entities, D, true);
+      add_param(c, "entity", n_ent_local, D, true);
       add_param(c, "relation", d.n_relations, 2 * D, true);
       add_param(c, "att_w1", D, D, false);
       add_param(c, "att_b1", 1, D, false);
@@ -742,6 +772,7 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   if (!c) return NGDB_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   for (auto& p : c->params)
     if (p.sparse) {
       cudaFree(p.w);
@@ -769,7 +800,11 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->sh.blob) cudaFree(c->sh.blob);
+  if (c->sh.buf) cudaFree(c->sh.buf);
+  if (c->sh.staging) cudaFreeHost(c->sh.staging);
+  if (c->sh.staged) cudaEventDestroy(c->sh.staged);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return NGDB_OK;
 }
@@ -855,6 +890,7 @@ int ngdb_set_debug(ngdb_ctx* c, int32_t keep) {
 
 int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
   return guarded([&] {
+    if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "context is row-sharded: use ngdb_shard_begin"};
     validate_plan(*plan);
     const int i = c->cur;
     c->cur ^= 1;
@@ -922,6 +958,7 @@ int ngdb_step_end(ngdb_ctx* c, float* per_query_loss, int32_t n_queries, double*
 int ngdb_plan_create(ngdb_ctx* c, const ngdb_step_plan* plan, ngdb_plan** out) {
   ngdb_plan* p = nullptr;
   int rc = guarded([&] {
+    if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "context is row-sharded: use ngdb_shard_begin"};
     validate_plan(*plan);
     p = new ngdb_plan();
     const PlanLayout L(*plan);
@@ -1063,4 +1100,256 @@ int ngdb_flush_l2(ngdb_ctx* c) {
   });
 }
 
+// ---- row-sharded step -----------------------------------------
+
+int ngdb_ctx_set_stream(ngdb_ctx* c, void* stream) {
+  return guarded([&] {
+    CK(cudaStreamSynchronize(c->stream));
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  });
+}
+
+namespace {
+int64_t up64(int64_t x) { return (x + 63) / 64 * 64; }
+}  // namespace
+
+int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_plan* sp,
+                     ngdb_shard_buffers* out) {
+  return guarded([&] {
+    if (sp->world != c->world || sp->rank != c->rank)
+      throw Fail{NGDB_ERR_CONFIG, "shard plan world/rank do not match the context"};
+    if (c->beta() || c->fused()) throw Fail{NGDB_ERR_MISSING_KERNEL, "sharded BetaE / fusion"};
+    validate_plan(*plan);
+    if (plan->n_score_slots > sp->max_slots || plan->n_anchor_slots > sp->max_anchors ||
+        plan->n_queries > sp->batch || plan->n_candidates != sp->n_candidates)
+      throw Fail{NGDB_ERR_SHAPE_MISMATCH, "step plan exceeds the shard plan's padding"};
+    // 1) the rank's own step plan, as ngdb_step_begin
+    const int i = c->cur;
+    c->cur ^= 1;
+    const PlanLayout L(*plan);
+    CK(cudaEventSynchronize(c->staged[i]));
+    if (L.total > c->staging_cap[i]) {
+      if (c->staging[i]) CK(cudaFreeHost(c->staging[i]));
+      c->staging_cap[i] = L.total + L.total / 4;
+      void* hp = nullptr;
+      CK(cudaMallocHost(&hp, c->staging_cap[i] * sizeof(int32_t)));
+      c->staging[i] = static_cast<int32_t*>(hp);
+    }
+    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->stream);
+    CK(cudaEventRecord(c->staged[i], c->stream));
+    ensure_step_buffers(c, c->stream_plan[i].meta);
+    begin_step_device(c);
+    c->active = &c->stream_plan[i];
+
+    // 2) the owner work lists
+    const int64_t G = sp->world, B = sp->batch, A = sp->max_anchors, S = sp->max_slots,
+                  nc = sp->n_candidates, U = G * B;
+    const int64_t n_owned = sp->unit_off[U], n_con = sp->seg[sp->n_rows];
+    const int64_t o_anc = 0, o_k = o_anc + up64(G * A), o_slots = o_k + up64(U),
+                  o_cand = o_slots + up64(U * 3), o_off = o_cand + up64(U * nc),
+                  o_owned = o_off + up64(U + 1), o_rows = o_owned + up64(n_owned),
+                  o_seg = o_rows + up64(sp->n_rows), o_con = o_seg + up64(sp->n_rows + 1),
+                  total = o_con + up64(n_con);
+    auto& sh = c->sh;
+    CK(cudaEventSynchronize(sh.staged));
+    if (total > sh.staging_cap) {
+      if (sh.staging) CK(cudaFreeHost(sh.staging));
+      sh.staging_cap = total + total / 4;
+      void* hp = nullptr;
+      CK(cudaMallocHost(&hp, sh.staging_cap * sizeof(int32_t)));
+      sh.staging = static_cast<int32_t*>(hp);
+    }
+    if (total > sh.blob_cap) {
+      CK(cudaStreamSynchronize(c->stream));
+      if (sh.blob) CK(cudaFree(sh.blob));
+      sh.blob_cap = total + total / 4;
+      sh.blob = dmalloc<int32_t>(sh.blob_cap);
+    }
+    int32_t* h = sh.staging;
+    std::memcpy(h + o_anc, sp->anchor_ids, G * A * 4);
+    std::memcpy(h + o_k, sp->unit_k, U * 4);
+    std::memcpy(h + o_slots, sp->unit_slots, U * 3 * 4);
+    std::memcpy(h + o_cand, sp->cand, U * nc * 4);
+    std::memcpy(h + o_off, sp->unit_off, (U + 1) * 4);
+    if (n_owned) std::memcpy(h + o_owned, sp->owned, n_owned * 4);
+    if (sp->n_rows) {
+      std::memcpy(h + o_rows, sp->rows, sp->n_rows * 4);
+      std::memcpy(h + o_seg, sp->seg, (sp->n_rows + 1) * 4);
+      std::memcpy(h + o_con, sp->contrib, n_con * 4);
+    }
+    CK(cudaMemcpyAsync(sh.blob, h, total * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(sh.staged, c->stream));
+
+    // 3) exchange buffers
+    const int64_t ew = c->params[c->ent_idx].cols, wq = c->query_width();
+    const Param& rel = c->params[c->rel_idx];
+    const int64_t n_red = c->dense_n + rel.n() + rel.rows;
+    const int64_t sizes[12] = {G * A * ew, A * ew,      S * wq,     G * S * wq, G * S * wq, S * wq,
+                               G * B,      B,           G * A * ew, G * A * ew, n_red,      G * S * nc};
+    int64_t need = 0;
+    for (int64_t z : sizes) need += up64(std::max<int64_t>(z, 1));
+    if (need > sh.buf_cap) {
+      CK(cudaStreamSynchronize(c->stream));
+      if (sh.buf) CK(cudaFree(sh.buf));
+      sh.buf_cap = need + need / 4;
+      sh.buf = dmalloc<float>(sh.buf_cap);
+      ++c->buffer_gen;
+    }
+    float* ptr[12];
+    float* cur = sh.buf;
+    for (int k = 0; k < 12; ++k) {
+      ptr[k] = cur;
+      cur += up64(std::max<int64_t>(sizes[k], 1));
+    }
+    ngdb_shard_buffers& b = sh.bufs;
+    b.anchor_send = ptr[0]; b.n_anchor_send = sizes[0];
+    b.anchor_rows = ptr[1]; b.n_anchor_rows = sizes[1];
+    b.query_mine = ptr[2]; b.n_query_mine = sizes[2];
+    b.query_all = ptr[3]; b.n_query_all = sizes[3];
+    b.dq_part = ptr[4]; b.n_dq_part = sizes[4];
+    b.dq_mine = ptr[5]; b.n_dq_mine = sizes[5];
+    b.loss_part = ptr[6]; b.n_loss_part = sizes[6];
+    b.loss_mine = ptr[7]; b.n_loss_mine = sizes[7];
+    b.grad_send = ptr[8]; b.n_grad_send = sizes[8];
+    b.grad_all = ptr[9]; b.n_grad_all = sizes[9];
+    b.reduce = ptr[10]; b.n_reduce = sizes[10];
+    sh.coef_all = ptr[11];
+    // unset query slots stay defined (their rows are gathered but never read)
+    CK(cudaMemsetAsync(b.query_mine, 0, sizes[2] * 4, c->stream));
+    ShardDev& d = sh.dev;
+    d.world = sp->world;
+    d.rank = sp->rank;
+    d.batch = sp->batch;
+    d.max_anchors = sp->max_anchors;
+    d.max_slots = sp->max_slots;
+    d.anchor_ids = sh.blob + o_anc;
+    d.unit_k = sh.blob + o_k;
+    d.unit_slots = sh.blob + o_slots;
+    d.cand = sh.blob + o_cand;
+    d.unit_off = sh.blob + o_off;
+    d.owned = sh.blob + o_owned;
+    d.query_all = b.query_all;
+    d.dq_part = b.dq_part;
+    d.loss_part = b.loss_part;
+    d.coef_all = sh.coef_all;
+    sh.n_rows = sp->n_rows;
+    sh.rows = sh.blob + o_rows;
+    sh.seg = sh.blob + o_seg;
+    sh.contrib = sh.blob + o_con;
+    sh.active = true;
+    c->anc_rows = b.anchor_rows;
+    if (out) *out = b;
+  });
+}
+
+int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
+  return guarded([&] {
+    auto& sh = c->sh;
+    if (!sh.active || !c->active) throw Fail{NGDB_ERR_CONFIG, "ngdb_shard_run outside a sharded step"};
+    const ngdb_plan* p = c->active;
+    const DevArgs a = make_args(c, p);
+    const LaunchCtx lc{c->stream, c->num_sms};
+    const ngdb_shard_buffers& b = sh.bufs;
+    switch (stage) {
+      case NGDB_SHARD_ANCHOR_PACK:
+        timed(c, F_EMBED, double(b.n_anchor_send) * 4,
+              [&] { return launch_shard_anchor_pack(a, sh.dev, b.anchor_send, lc); });
+        break;
+      case NGDB_SHARD_FORWARD:
+        for (const auto& d : p->meta.pools)
+          if (d.dir == 0 && d.kind != NGDB_OP_SCORE && d.kind != NGDB_OP_UNION_SCORE &&
+              d.kind != NGDB_OP_LOSS)
+            exec_pool(c, p, d);
+        break;
+      case NGDB_SHARD_QUERY_PACK:
+        for (const auto& d : p->meta.pools)
+          if (d.dir == 0 && (d.kind == NGDB_OP_SCORE || d.kind == NGDB_OP_LOSS))
+            timed(c, F_SCORE, 0.0, [&] { return launch_shard_query_pack(a, d.first, d.count, b.query_mine, lc); });
+        break;
+      case NGDB_SHARD_SCORE: {
+        const double nc = p->meta.n_candidates, ew = c->params[c->ent_idx].cols * 4.0;
+        const double owned = double(sh.dev.world) * sh.dev.batch * nc / sh.dev.world;
+        timed(c, F_LOSS_FWD, owned * (ew + 8) + 2.0 * b.n_dq_part * 4, [&] {
+          CK(cudaMemsetAsync(b.dq_part, 0, b.n_dq_part * 4, c->stream));
+          return launch_shard_score(a, sh.dev, lc);
+        });
+        break;
+      }
+      case NGDB_SHARD_SCORE_DONE:
+        timed(c, F_LOSS_FWD, 0.0, [&] {
+          return launch_shard_score_done(a, b.dq_mine, int64_t(p->meta.n_score) * c->query_width(),
+                                         b.loss_mine, p->meta.n_queries, lc);
+        });
+        break;
+      case NGDB_SHARD_BACKWARD:
+        for (const auto& d : p->meta.pools) {
+          if (d.dir != 1 || d.kind == NGDB_OP_UNION_SCORE) continue;  // routing done by the owners
+          if (d.kind == NGDB_OP_SCORE)  // dL/dq of a union branch arrived in dqbuf
+            timed(c, F_SCORE, 0.0, [&] { return launch_loss_bwd(a, d.first, d.count, lc); });
+          else
+            exec_pool(c, p, d);
+        }
+        break;
+      case NGDB_SHARD_GRAD_PACK: {
+        const Param& rel = c->params[c->rel_idx];
+        SparseTable tr{rel.w, rel.m, rel.v, nullptr, static_cast<int32_t>(rel.cols),
+                       p->meta.n_rrows, p->blob + p->layout.rrows, p->blob + p->layout.rseg,
+                       p->blob + p->layout.rcon};
+        timed(c, F_OPT_RELATION, double(b.n_reduce) * 4 + double(b.n_grad_send) * 4, [&] {
+          CK(cudaMemsetAsync(b.grad_send, 0, b.n_grad_send * 4, c->stream));
+          CK(cudaMemsetAsync(b.reduce, 0, b.n_reduce * 4, c->stream));
+          if (c->dense_n)
+            CK(cudaMemcpyAsync(b.reduce, c->dense_g, c->dense_n * 4, cudaMemcpyDeviceToDevice, c->stream));
+          return launch_shard_grad_pack(a, sh.dev, p->meta.n_anchor, b.grad_send, lc) +
+                 launch_shard_rel_pack(a, tr, b.reduce + c->dense_n, b.reduce + c->dense_n + rel.n(), lc);
+        });
+        break;
+      }
+      default: throw Fail{NGDB_ERR_CONFIG, "unknown shard stage"};
+    }
+    CK(cudaGetLastError());
+  });
+}
+
+int ngdb_shard_optimizer(ngdb_ctx* c, int64_t step) {
+  return guarded([&] {
+    auto& sh = c->sh;
+    if (!sh.active || !c->active) throw Fail{NGDB_ERR_CONFIG, "ngdb_shard_optimizer outside a sharded step"};
+    const ngdb_plan* p = c->active;
+    set_step_scalars(c, step);
+    const ngdb_model_desc& d = c->desc;
+    const AdamHyper hp{d.lr, d.beta1, d.beta2, d.eps_adam};
+    const LaunchCtx lc{c->stream, c->num_sms};
+    const ngdb_shard_buffers& b = sh.bufs;
+    if (c->dense_n)
+      CK(cudaMemcpyAsync(c->dense_g, b.reduce, c->dense_n * 4, cudaMemcpyDeviceToDevice, c->stream));
+    // entity rows this rank owns: anchors of every rank + owned candidates of every rank's slots
+    DevArgs a = make_args(c, p);
+    a.agbuf = b.grad_all;
+    a.qbuf = b.query_all;
+    a.coefbuf = sh.coef_all;
+    Param& ent = c->params[c->ent_idx];
+    Param& rel = c->params[c->rel_idx];
+    SparseTable te{ent.w, ent.m, ent.v, c->debug ? ent.g : nullptr, static_cast<int32_t>(ent.cols),
+                   sh.n_rows, sh.rows, sh.seg, sh.contrib};
+    timed(c, F_OPT_ENTITY, 6.0 * sh.n_rows * ent.cols * 4,
+          [&] { return launch_sparse_adam_entity(a, te, hp, c->d_bc, lc); });
+    timed(c, F_OPT_RELATION, 6.0 * rel.n() * 4, [&] {
+      return launch_masked_rows_adam(rel.w, rel.m, rel.v, c->debug ? rel.g : nullptr,
+                                     b.reduce + c->dense_n, b.reduce + c->dense_n + rel.n(),
+                                     static_cast<int>(rel.rows), static_cast<int>(rel.cols), hp,
+                                     c->d_bc, lc);
+    });
+    timed(c, F_OPT_DENSE, 28.0 * c->dense_n, [&] {
+      return launch_dense_adam(c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->dense_n, hp,
+                               c->d_bc, lc) +
+             refresh_weight_splits(c);
+    });
+    CK(cudaGetLastError());
+    sh.active = false;
+    c->anc_rows = nullptr;
+  });
+}
+
 }  // extern "C"
+

@@ -33,8 +33,10 @@ __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, 
   if (dir == 0) {
     float* out = a.arena + d.out;
     // FuseSemantic: the prologue's fused row of this anchor's entity
-    const float* src = a.fused ? a.etab + static_cast<int64_t>(a.anchor_local[d.aux]) * a.ent_w
-                               : a.ent + static_cast<int64_t>(d.id) * a.ent_w;
+    // row-sharded: the row fetched from its owner into this anchor slot
+    const float* src = a.fused      ? a.etab + static_cast<int64_t>(a.anchor_local[d.aux]) * a.ent_w
+                       : a.anc_rows ? a.anc_rows + static_cast<int64_t>(d.aux) * a.ent_w
+                                    : a.ent + static_cast<int64_t>(d.id) * a.ent_w;
     if (a.backbone == NGDB_BETAE) {  // realised (alpha | beta); the mirror's
       for (int c = lane; c < ew4; c += 32) {  // chain rule runs in the optimizer
         const float4 x = ldg4(src + 4 * c);

@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "dist.cuh"
 #include "special.cuh"
 
 namespace ngdb_dev {
@@ -28,49 +29,6 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRows = 4;          // candidate rows in flight per warp
-
-template <int BB>
-struct Dist;
-
-template <>
-struct Dist<NGDB_GQE> {
-  static __device__ __forceinline__ float term(float v, float c, float, float) {
-    return fabsf(v - c);
-  }
-  // coef * dd/dq
-  static __device__ __forceinline__ void grad(float v, float c, float, float coef, float,
-                                              float& gc, float&) {
-    gc += coef * sgnf(c - v);
-  }
-};
-
-// BetaE: v = etab row halves (P | Q); "c", "o" = query alpha, beta
-template <>
-struct Dist<NGDB_BETAE> {
-  static __device__ __forceinline__ float term(float p, float q, float A, float B) {
-    return A * p + B * q;
-  }
-};
-
-template <>
-struct Dist<NGDB_Q2B> {
-  static __device__ __forceinline__ float term(float v, float c, float o, float alpha) {
-    const float a = fabsf(v - c);
-    return fmaxf(a - o, 0.f) + alpha * fminf(a, o);
-  }
-  static __device__ __forceinline__ void grad(float v, float c, float o, float coef, float alpha,
-                                              float& gc, float& go) {
-    const float delta = v - c;
-    const float a = fabsf(delta);
-    const float s = sgnf(delta);
-    if (a > o) {
-      gc -= coef * s;
-      go += coef * (alpha - 1.f);
-    } else {
-      gc -= coef * alpha * s;
-    }
-  }
-};
 
 __device__ __forceinline__ float4 f4(float x) { return make_float4(x, x, x, x); }
 
@@ -222,16 +180,6 @@ __device__ void reduce_dq(const DevArgs& a, Lane<BB, kMaxChunks>& L, float* red,
   }
   if (dst)
     for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(dst + e, ld4(red + e));
-}
-
-__device__ __forceinline__ float loss_coef(const DevArgs& a, int j, float dj, float& loss) {
-  const float inv_k = 1.f / static_cast<float>(a.n_neg);
-  if (j == 0) {
-    loss += softplusf(dj - a.gamma);
-    return sigmoidf(dj - a.gamma);
-  }
-  loss += inv_k * softplusf(a.gamma - dj);
-  return -inv_k * sigmoidf(a.gamma - dj);
 }
 
 __device__ float block_sum(float v, float* red) {

@@ -1,0 +1,249 @@
+// Row-sharded step kernels (BASELINE.json configs[4]).
+//
+// Entity e lives on rank e mod G at local row e div G. Scoring ships queries,
+// not rows: after the score-slot query vectors are all-gathered, every rank
+// evaluates the loss terms of the candidates it OWNS for every rank's queries
+// (the loss is a sum of per-candidate terms and coef_j depends on d_j alone;
+// a union's min/argmin is per candidate too), writes coef for its own
+// optimizer, and emits partial dL/dq + partial losses that a reduce-scatter
+// returns to the query's rank. The collectives themselves run between the
+// stages (ngdb_shard_run), on the framework's NCCL communicator.
+#include <algorithm>
+
+#include "common.cuh"
+#include "dist.cuh"
+
+namespace ngdb_dev {
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
+
+// owned rows of every rank's anchors -> send[q][a] (zeros where not owned)
+__global__ void shard_anchor_pack_kernel(DevArgs a, ShardDev sd, float* send) {
+  pdl_start();
+  const int64_t slot = blockIdx.x;  // q * A + a
+  const int32_t e = sd.anchor_ids[slot];
+  float* dst = send + slot * a.ent_w;
+  const bool own = e >= 0 && e % sd.world == sd.rank;
+  const float* src = a.ent + static_cast<int64_t>(own ? e / sd.world : 0) * a.ent_w;
+  for (int c = threadIdx.x; c < a.ent_w / 4; c += blockDim.x)
+    st4(dst + 4 * c, own ? ld4(src + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f));
+}
+
+// query tensors of a Score / Loss pool -> query_mine[slot]
+__global__ void shard_query_pack_kernel(DevArgs a, int first, float* dst) {
+  pdl_start();
+  const ngdb_node_desc d = a.nodes[first + blockIdx.x];
+  if (d.aux < 0) return;  // union Loss: its branches are the Score nodes
+  const float* q = a.arena + d.in[0];
+  float* o = dst + static_cast<int64_t>(d.aux) * a.wq;
+  for (int e = threadIdx.x * 4; e < a.wq; e += blockDim.x * 4) st4(o + e, ld4(q + e));
+}
+
+// One CTA per scoring unit (rank q, query i) of ANY rank: the owned candidates'
+// distances to the unit's 1..3 score-slot queries, union min/argmin (ties ->
+// lowest branch), loss terms, coef (routed to the argmin branch), and the
+// partial dL/dq of each branch slot. Shared: queries [3][wq], per-warp partial
+// dq [4][3][wq] summed in warp order (deterministic).
+template <int BB>
+__global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardDev sd) {
+  pdl_start();
+  extern __shared__ __align__(16) float sm[];
+  __shared__ float lred[kWarps];
+  const int u = blockIdx.x;
+  const int q = u / sd.batch, i = u % sd.batch;
+  const int k = sd.unit_k[u];
+  const int wq = a.wq, D = a.dim, d4 = D / 4;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  float* qs = sm;              // [3][wq]
+  float* part = sm + 3 * wq;   // [kWarps][3][wq]
+  int gslot[3];
+  for (int b = 0; b < 3; ++b)
+    gslot[b] = b < k ? q * sd.max_slots + sd.unit_slots[static_cast<int64_t>(u) * 3 + b] : 0;
+  for (int b = 0; b < k; ++b)
+    for (int e = threadIdx.x; e < wq; e += kThreads)
+      qs[b * wq + e] = sd.query_all[static_cast<int64_t>(gslot[b]) * wq + e];
+  for (int e = threadIdx.x; e < kWarps * 3 * wq; e += kThreads) part[e] = 0.f;
+  __syncthreads();
+  float loss = 0.f;  // identical in all lanes of a warp
+  const int32_t* cand = sd.cand + static_cast<int64_t>(u) * a.ncand;
+  for (int t = sd.unit_off[u] + warp; t < sd.unit_off[u + 1]; t += kWarps) {
+    const int j = sd.owned[t];
+    const int32_t ent = cand[j];
+    const float* row = a.ent + static_cast<int64_t>(ent / sd.world) * a.ent_w;
+    float dist[3];
+    for (int b = 0; b < k; ++b) {
+      const float* qc = qs + b * wq;
+      float s = 0.f;
+      for (int c = lane; c < d4; c += 32) {
+        const float4 v = ld4(row + 4 * c), cc = ld4(qc + 4 * c);
+        const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        s += Dist<BB>::term(v.x, cc.x, oo.x, a.alpha_box) + Dist<BB>::term(v.y, cc.y, oo.y, a.alpha_box) +
+             Dist<BB>::term(v.z, cc.z, oo.z, a.alpha_box) + Dist<BB>::term(v.w, cc.w, oo.w, a.alpha_box);
+      }
+      dist[b] = warp_sum(s);
+    }
+    int bm = 0;
+    for (int b = 1; b < k; ++b)
+      if (dist[b] < dist[bm]) bm = b;  // min distance == max score; ties -> lowest branch
+    const float coef = loss_coef(a, j, dist[bm], loss);
+    if (lane == 0)
+      for (int b = 0; b < k; ++b)
+        sd.coef_all[static_cast<int64_t>(gslot[b]) * a.ncand + j] = b == bm ? coef : 0.f;
+    const float* qc = qs + bm * wq;
+    float* pw = part + (warp * 3 + bm) * wq;
+    for (int c = lane; c < d4; c += 32) {
+      const float4 v = ld4(row + 4 * c), cc = ld4(qc + 4 * c);
+      const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float gc[4] = {0.f, 0.f, 0.f, 0.f}, go[4] = {0.f, 0.f, 0.f, 0.f};
+      Dist<BB>::grad(v.x, cc.x, oo.x, coef, a.alpha_box, gc[0], go[0]);
+      Dist<BB>::grad(v.y, cc.y, oo.y, coef, a.alpha_box, gc[1], go[1]);
+      Dist<BB>::grad(v.z, cc.z, oo.z, coef, a.alpha_box, gc[2], go[2]);
+      Dist<BB>::grad(v.w, cc.w, oo.w, coef, a.alpha_box, gc[3], go[3]);
+      for (int t2 = 0; t2 < 4; ++t2) {
+        pw[4 * c + t2] += gc[t2];
+        if (BB == NGDB_Q2B) pw[D + 4 * c + t2] += go[t2];
+      }
+    }
+  }
+  if (lane == 0) lred[warp] = loss;
+  __syncthreads();
+  for (int b = 0; b < k; ++b)
+    for (int e = threadIdx.x; e < wq; e += kThreads) {
+      float v = 0.f;
+      for (int w = 0; w < kWarps; ++w) v += part[(w * 3 + b) * wq + e];
+      sd.dq_part[static_cast<int64_t>(gslot[b]) * wq + e] = v;
+    }
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < kWarps; ++w) t += lred[w];
+    sd.loss_part[static_cast<int64_t>(q) * sd.batch + i] = t;
+  }
+}
+
+// this rank's results: dqbuf <- dq_mine, loss_out <- loss_mine
+__global__ void shard_score_done_kernel(DevArgs a, const float* dq_mine, int64_t n_dq,
+                                        const float* loss_mine, int nq) {
+  pdl_start();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_dq;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    a.dqbuf[e] = dq_mine[e];
+    if (e < nq) {
+      a.loss_out[e] = loss_mine[e];
+      if (!isfinite(loss_mine[e])) atomicOr(&a.flags[0], 1);
+    }
+  }
+}
+
+// my anchors' gradient rows -> send[owner][slot]
+__global__ void shard_grad_pack_kernel(DevArgs a, ShardDev sd, int n_anchor, float* send) {
+  pdl_start();
+  const int slot = blockIdx.x;
+  if (slot >= n_anchor) return;
+  const int32_t e = sd.anchor_ids[static_cast<int64_t>(sd.rank) * sd.max_anchors + slot];
+  const int owner = e % sd.world;
+  float* dst = send + (static_cast<int64_t>(owner) * sd.max_anchors + slot) * a.ent_w;
+  const float* g = a.agbuf + static_cast<int64_t>(slot) * a.ent_w;
+  for (int c = threadIdx.x; c < a.ent_w / 4; c += blockDim.x) st4(dst + 4 * c, ld4(g + 4 * c));
+}
+
+// relation CSR rows -> dense relation gradient rows + touched flags
+__global__ void shard_rel_pack_kernel(DevArgs a, SparseTable t, float* rel_g, float* touched) {
+  pdl_start();
+  const int r = blockIdx.x;
+  if (r >= t.n_rows) return;
+  const int64_t row = t.rows[r];
+  for (int e = threadIdx.x; e < t.width; e += blockDim.x) {
+    float s = 0.f;
+    for (int kk = t.seg[r]; kk < t.seg[r + 1]; ++kk)
+      s += a.rgbuf[static_cast<int64_t>(t.contrib[kk]) * t.width + e];
+    rel_g[row * t.width + e] = s;
+  }
+  if (threadIdx.x == 0) touched[row] = 1.f;
+}
+
+// lazy Adam on the rows any rank touched, from all-reduced dense rows
+__global__ void masked_rows_adam_kernel(float* w, float* m, float* v, float* dbg, const float* g,
+                                        const float* touched, int rows, int width, AdamHyper hp,
+                                        const float* bc) {
+  pdl_start();
+  const int r = blockIdx.x;
+  if (r >= rows || !(touched[r] > 0.f)) return;
+  const float bc1 = bc[0], bc2 = bc[1];
+  for (int e = threadIdx.x; e < width; e += blockDim.x) {
+    const int64_t o = static_cast<int64_t>(r) * width + e;
+    const float gi = g[o];
+    if (dbg) dbg[o] = gi;
+    const float mi = hp.b1 * m[o] + (1.f - hp.b1) * gi;
+    const float vi = hp.b2 * v[o] + (1.f - hp.b2) * gi * gi;
+    m[o] = mi;
+    v[o] = vi;
+    w[o] -= hp.lr * (mi / bc1) / (sqrtf(vi / bc2) + hp.eps);
+  }
+}
+
+}  // namespace
+
+int launch_shard_anchor_pack(const DevArgs& a, const ShardDev& sd, float* send, const LaunchCtx& lc) {
+  const int n = sd.world * sd.max_anchors;
+  if (n <= 0) return 0;
+  launch_pdl(shard_anchor_pack_kernel, dim3(n), dim3(128), 0, lc.stream, 1, a, sd, send);
+  return 1;
+}
+
+int launch_shard_query_pack(const DevArgs& a, int first, int n, float* dst, const LaunchCtx& lc) {
+  if (n <= 0) return 0;
+  launch_pdl(shard_query_pack_kernel, dim3(n), dim3(128), 0, lc.stream, 1, a, first, dst);
+  return 1;
+}
+
+int launch_shard_score(const DevArgs& a, const ShardDev& sd, const LaunchCtx& lc) {
+  const int units = sd.world * sd.batch;
+  if (units <= 0) return 0;
+  const size_t smem = static_cast<size_t>(3 + kWarps * 3) * a.wq * sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(shard_score_kernel<NGDB_GQE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(shard_score_kernel<NGDB_Q2B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    configured = true;
+  }
+  if (a.backbone == NGDB_GQE)
+    launch_pdl(shard_score_kernel<NGDB_GQE>, dim3(units), dim3(kThreads), smem, lc.stream, 1, a, sd);
+  else
+    launch_pdl(shard_score_kernel<NGDB_Q2B>, dim3(units), dim3(kThreads), smem, lc.stream, 1, a, sd);
+  return 1;
+}
+
+int launch_shard_score_done(const DevArgs& a, const float* dq_mine, int64_t n_dq,
+                            const float* loss_mine, int nq, const LaunchCtx& lc) {
+  const int blocks = static_cast<int>(std::min<int64_t>((n_dq + 255) / 256, lc.num_sms * 4));
+  launch_pdl(shard_score_done_kernel, dim3(std::max(blocks, 1)), dim3(256), 0, lc.stream, 1, a,
+             dq_mine, n_dq, loss_mine, nq);
+  return 1;
+}
+
+int launch_shard_grad_pack(const DevArgs& a, const ShardDev& sd, int n_anchor, float* send,
+                           const LaunchCtx& lc) {
+  if (n_anchor <= 0) return 0;
+  launch_pdl(shard_grad_pack_kernel, dim3(n_anchor), dim3(128), 0, lc.stream, 1, a, sd, n_anchor, send);
+  return 1;
+}
+
+int launch_shard_rel_pack(const DevArgs& a, const SparseTable& t, float* rel_g, float* touched,
+                          const LaunchCtx& lc) {
+  if (t.n_rows <= 0) return 0;
+  launch_pdl(shard_rel_pack_kernel, dim3(t.n_rows), dim3(128), 0, lc.stream, 1, a, t, rel_g, touched);
+  return 1;
+}
+
+int launch_masked_rows_adam(float* w, float* m, float* v, float* dbg, const float* g,
+                            const float* touched, int rows, int width, const AdamHyper& hp,
+                            const float* bc, const LaunchCtx& lc) {
+  if (rows <= 0) return 0;
+  launch_pdl(masked_rows_adam_kernel, dim3(rows), dim3(128), 0, lc.stream, 1, w, m, v, dbg, g,
+             touched, rows, width, hp, bc);
+  return 1;
+}
+
+}  // namespace ngdb_dev

@@ -10,6 +10,7 @@
 #include "ngdb/kg.hpp"
 #include "ngdb/sampler.hpp"
 #include "ngdb/scheduler.hpp"
+#include "ngdb/shard.hpp"
 #include "ngdb/synth.hpp"
 #include "ngdb/trainer.hpp"
 
@@ -25,6 +26,9 @@ struct ngdb_batch {
 };
 struct ngdb_step {
   ngdb::StepPlanHost plan;
+};
+struct ngdb_shard {
+  ngdb::ShardPlanHost plan;
 };
 
 namespace {
@@ -334,6 +338,89 @@ int ngdb_ngse_read(const char* path, float* out, int64_t cap, int64_t* count, in
       if (cap < static_cast<int64_t>(v.size())) throw ngdb::ShapeMismatch("buffer too small");
       std::memcpy(out, v.data(), v.size() * sizeof(float));
     }
+  });
+}
+
+int ngdb_step_shard_info(const ngdb_step* s, int32_t* n_anchor_slots, int32_t* n_score_slots,
+                         int32_t* batch, int32_t* n_candidates) {
+  return guarded([&] {
+    *n_anchor_slots = s->plan.n_anchor_slots;
+    *n_score_slots = s->plan.n_score_slots;
+    *batch = s->plan.n_queries;
+    *n_candidates = s->plan.n_candidates;
+  });
+}
+
+int ngdb_step_shard_meta(const ngdb_step* s, int32_t* anchor_ids, int32_t* unit_k,
+                         int32_t* unit_slots, int32_t* cand) {
+  return guarded([&] {
+    const auto& p = s->plan;
+    std::memcpy(anchor_ids, p.anchor_ids.data(), p.anchor_ids.size() * sizeof(int32_t));
+    std::memcpy(unit_k, p.unit_k.data(), p.unit_k.size() * sizeof(int32_t));
+    std::memcpy(unit_slots, p.unit_slots.data(), p.unit_slots.size() * sizeof(int32_t));
+    std::memcpy(cand, p.candidates.data(), p.candidates.size() * sizeof(int32_t));
+  });
+}
+
+int ngdb_shard_build(int32_t world, int32_t rank, int32_t batch, int32_t max_anchors,
+                     int32_t max_slots, int32_t n_candidates, const int32_t* anchor_ids_all,
+                     const int32_t* unit_k_all, const int32_t* unit_slots_all,
+                     const int32_t* cand_all, ngdb_shard** out) {
+  return guarded([&] {
+    ngdb::ShardSpec spec{world, rank, batch, max_anchors, max_slots, n_candidates};
+    auto* s = new ngdb_shard();
+    s->plan = ngdb::build_shard_plan(spec, anchor_ids_all, unit_k_all, unit_slots_all, cand_all);
+    *out = s;
+  });
+}
+
+int ngdb_shard_view(const ngdb_shard* s, ngdb_shard_plan* v) {
+  return guarded([&] {
+    const auto& p = s->plan;
+    *v = ngdb_shard_plan{};
+    v->world = p.spec.world;
+    v->rank = p.spec.rank;
+    v->batch = p.spec.batch;
+    v->max_anchors = p.spec.max_anchors;
+    v->max_slots = p.spec.max_slots;
+    v->n_candidates = p.spec.n_candidates;
+    v->anchor_ids = p.anchor_ids.data();
+    v->unit_k = p.unit_k.data();
+    v->unit_slots = p.unit_slots.data();
+    v->cand = p.cand.data();
+    v->unit_off = p.unit_off.data();
+    v->owned = p.owned.data();
+    v->n_rows = static_cast<int32_t>(p.rows.size());
+    v->rows = p.rows.data();
+    v->seg = p.seg.data();
+    v->contrib = p.contrib.data();
+  });
+}
+
+int ngdb_shard_destroy(ngdb_shard* s) {
+  delete s;
+  return NGDB_OK;
+}
+
+int ngdb_param_init_shard(int32_t backbone, int32_t n_entities, int32_t n_relations, int32_t dim,
+                          const char* name, uint64_t seed, int32_t world, int32_t rank,
+                          float* out, int64_t n) {
+  return guarded([&] {
+    auto v = ngdb::init_param(static_cast<ngdb::Backbone>(backbone), n_entities, n_relations, dim,
+                              name, seed);
+    const auto specs = ngdb::param_specs(static_cast<ngdb::Backbone>(backbone), n_entities,
+                                         n_relations, dim);
+    int64_t cols = 0;
+    for (const auto& p : specs)
+      if (p.name == name) cols = p.cols;
+    const int64_t rows = static_cast<int64_t>(v.size()) / cols;
+    int64_t k = 0;
+    for (int64_t r = rank; r < rows; r += world) {
+      if ((k + 1) * cols > n) throw ngdb::ShapeMismatch("shard buffer too small");
+      std::memcpy(out + k * cols, v.data() + r * cols, cols * sizeof(float));
+      ++k;
+    }
+    if (k * cols != n) throw ngdb::ShapeMismatch("shard size");
   });
 }
 

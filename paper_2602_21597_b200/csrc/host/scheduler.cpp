@@ -67,7 +67,7 @@ struct Slot {
 
 class SlotArena {
  public:
-  SlotArena(ReleasePolicy policy) : policy_(policy) {}
+  SlotArena(ReleasePolicy policy, bool reuse) : policy_(policy), reuse_(reuse) {}
 
   int32_t alloc(int64_t bytes, int32_t rc) {
     if (rc < 1) throw ZeroRefcount("alloc with refcount < 1");
@@ -82,6 +82,10 @@ class SlotArena {
     } else {
       s.offset = top_;
       top_ += (bytes + 15) / 16 * 16;
+    }
+    if (!reuse_) {  // private device slot; the trace statistics are unchanged
+      s.offset = dev_top_;
+      dev_top_ += (bytes + 15) / 16 * 16;
     }
     live_ += bytes;
     peak_ = std::max(peak_, live_);
@@ -105,10 +109,12 @@ class SlotArena {
   int64_t live() const { return live_; }
   int64_t peak() const { return peak_; }
   int64_t hits() const { return hits_; }
-  int64_t top() const { return top_; }
+  int64_t top() const { return reuse_ ? top_ : dev_top_; }
 
  private:
   ReleasePolicy policy_;
+  bool reuse_;
+  int64_t dev_top_ = 0;
   std::vector<Slot> slots_;
   std::unordered_map<int64_t, std::vector<int64_t>> free_;
   int64_t live_ = 0, peak_ = 0, hits_ = 0, top_ = 0;
@@ -132,7 +138,7 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
   DagAdjacency adj = adjacency(f);
   std::vector<int32_t> indeg = adj.indegree;
 
-  SlotArena arena(cfg_.policy);
+  SlotArena arena(cfg_.policy, cfg_.device_reuse);
   std::vector<int32_t> t_fwd(nf, -1), t_bwd(n, -1);
   fwd_slot_.assign(nf, -1);
   bwd_slot_.assign(n, -1);

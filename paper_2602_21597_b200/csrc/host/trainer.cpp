@@ -223,12 +223,32 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
   build_csr(ekeys, plan.entity_rows, plan.entity_seg, plan.entity_contrib);
   build_csr(rkeys, plan.relation_rows, plan.relation_seg, plan.relation_contrib);
 
+  plan.anchor_ids.assign(plan.n_anchor_slots, -1);
+  plan.unit_k.assign(B, 0);
+  plan.unit_slots.assign(static_cast<size_t>(B) * 3, -1);
+  for (int32_t i = 0; i < nf; ++i) {
+    const OperatorNode& x = f.nodes[i];
+    if (x.op.kind == OpKind::EmbedAnchor || x.op.kind == OpKind::FuseSemantic)
+      plan.anchor_ids[aux[i]] = x.payload;
+    if (x.op.kind != OpKind::Loss) continue;
+    const OperatorNode& in = f.nodes[x.inputs[0]];
+    int32_t* us = &plan.unit_slots[static_cast<size_t>(x.query) * 3];
+    if (in.op.kind == OpKind::UnionScore) {
+      plan.unit_k[x.query] = in.n_inputs;
+      for (int k = 0; k < in.n_inputs; ++k) us[k] = aux[in.inputs[k]];
+    } else {
+      plan.unit_k[x.query] = 1;
+      us[0] = aux[i];
+    }
+  }
+
   SchedulerConfig sc;
   sc.backbone = cfg.backbone;
   sc.b_max = cfg.b_max;
   sc.query_width = wq;
   sc.n_candidates = nc;
   sc.elem_bytes = 4;
+  sc.device_reuse = !cfg.sharded;
   Planner planner(sc);
   const TensorModel tm{wq, nc};
   auto elems = [](int64_t bytes) { return static_cast<int32_t>(bytes / 4); };

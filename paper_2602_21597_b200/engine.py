@@ -260,7 +260,7 @@ class Engine:
         candidates (SPEC.md:589)."""
         sd = 0 if semantic is None else int(semantic.shape[1])
         d = ModelDesc(BACKBONES[backbone], n_entities, n_relations, dim, n_neg, sd, gamma,
-                      alpha_box, lr, 0.9, 0.999, 1e-8, b_max, max_queries)
+                      alpha_box, lr, 0.9, 0.999, 1e-8, b_max, max_queries, 1, 0)
         self.backbone, self.dim, self.b_max = backbone, dim, b_max
         self.n_entities, self.n_relations, self.semantic_dim = n_entities, n_relations, sd
         self._h = C.c_void_p()

@@ -1,0 +1,93 @@
+"""Worker processes of the sharded-step tests (spawned, world_size 2, gloo on
+127.0.0.1). Each returns its results through a file in `out_dir`."""
+import os
+import pickle
+
+
+def _init(rank, world, port):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    return dist
+
+
+def host_plan_worker(rank, world, port, out_dir, shape, mix, b, k, dim):
+    """CPU only: plan this rank's batch, exchange metadata, build the owner lists;
+    also exercise the host-staged collectives on CPU tensors."""
+    dist = _init(rank, world, port)
+    import numpy as np
+    import torch
+
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200.sharded import Comm, plan_shard_step
+
+    comm = Comm()
+    g = m.Graph.synthetic(shape, 1)
+    batch = m.Batch.sample(g, m.pattern_weights(mix), b, k, seed=3, tag=rank)
+    st = plan_shard_step(comm, batch, "q2b", dim)
+    v, s = st.views()
+    U = s.world * s.batch
+    n_owned = s.unit_off[U]
+    plan = {
+        "world": s.world, "rank": s.rank, "batch": s.batch, "A": s.max_anchors,
+        "S": s.max_slots, "nc": s.n_candidates,
+        "anchor_ids": np.ctypeslib.as_array(s.anchor_ids, (s.world * s.max_anchors,)).copy(),
+        "unit_k": np.ctypeslib.as_array(s.unit_k, (U,)).copy(),
+        "unit_slots": np.ctypeslib.as_array(s.unit_slots, (U * 3,)).copy(),
+        "cand": np.ctypeslib.as_array(s.cand, (U * s.n_candidates,)).copy(),
+        "unit_off": np.ctypeslib.as_array(s.unit_off, (U + 1,)).copy(),
+        "owned": np.ctypeslib.as_array(s.owned, (max(n_owned, 1),))[:n_owned].copy(),
+        "rows": np.ctypeslib.as_array(s.rows, (max(s.n_rows, 1),))[: s.n_rows].copy(),
+        "seg": np.ctypeslib.as_array(s.seg, (s.n_rows + 1,)).copy(),
+    }
+    plan["contrib"] = np.ctypeslib.as_array(s.contrib, (max(int(plan["seg"][-1]), 1),))[
+        : int(plan["seg"][-1])].copy()
+    plan["n_score_slots"] = v.n_score_slots
+    # collectives (host-staged path) on CPU tensors
+    x = torch.arange(6, dtype=torch.float32) + 10 * rank
+    ag = torch.zeros(6 * world)
+    comm.all_gather(ag, x)
+    rs = torch.zeros(6 // world)
+    comm.reduce_scatter(rs, x)
+    a2a = torch.zeros(6)
+    comm.all_to_all(a2a, x)
+    ar = x.clone()
+    comm.all_reduce(ar)
+    plan["coll"] = {"ag": ag.numpy(), "rs": rs.numpy(), "a2a": a2a.numpy(), "ar": ar.numpy()}
+    with open(os.path.join(out_dir, f"plan{rank}.pkl"), "wb") as f:
+        pickle.dump(plan, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def gpu_step_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
+    """Two ranks sharing GPU 0: the row-sharded step through ngdb_shard_*."""
+    dist = _init(rank, world, port)
+    import numpy as np
+
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200.sharded import Comm, ShardedEngine
+
+    comm = Comm()
+    g = m.Graph.synthetic(shape, 1)
+    info = g.info()
+    eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=k,
+                        max_queries=b, device=0, debug=True)
+    w = m.pattern_weights(mix)
+    res = {"loss": [], "batches": []}
+    for step in range(1, steps + 1):
+        batch = m.Batch.from_arrays(_load_batch(out_dir, step, rank))
+        res["loss"].append(eng.train_step(batch))
+    specs = m.param_specs(backbone, info["n_entities"], info["n_relations"], dim)
+    res["params"] = {n: eng.download(n) for n, *_ in specs}
+    res["grads"] = {n: eng.download("g:" + n) for n, *_ in specs}
+    with open(os.path.join(out_dir, f"gpu{rank}.pkl"), "wb") as f:
+        pickle.dump(res, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _load_batch(out_dir, step, rank):
+    with open(os.path.join(out_dir, f"batch_{step}_{rank}.pkl"), "rb") as f:
+        return pickle.load(f)

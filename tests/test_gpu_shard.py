@@ -1,0 +1,77 @@
+"""Row-sharded step on the GPU: two ranks share GPU 0 over gloo
+(host-staged collectives; NCCL needs one GPU per rank). Every per-query loss,
+the summed gradients and the post-Adam parameters must match the oracle's
+"G sub-batches" mode — each rank's batch scheduled independently, gradients
+summed, one Adam step (SURVEY §8(e) parity) — at the 1e-4 bar."""
+import pickle
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2602_21597_b200 as m
+from parity import check_all, tie_free
+
+pytestmark = pytest.mark.gpu
+ALL = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni", "inp"]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("backbone,dim,b,k,steps", [("q2b", 32, 64, 16, 1), ("gqe", 16, 48, 8, 2),
+                                                      ("q2b", 400, 128, 32, 2)])
+def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone, dim, b, k, steps):
+    import torch.multiprocessing as mp
+
+    import oracle as O
+    import shard_workers
+    G = 2
+    info = small_graph.info()
+    ne, nr = info["n_entities"], info["n_relations"]
+    w = m.pattern_weights(ALL)
+    om = O.OracleModel(backbone, ne, nr, dim, k, precision=64)
+    om.init(2)
+    batches = []
+    for step in range(1, steps + 1):
+        per_rank = []
+        for r in range(G):
+            bt = m.Batch.sample(small_graph, w, b, k, seed=3, tag=step * G + r)
+            if step == 1:  # certify kink-free queries at the initial parameters
+                probe = O.OracleModel(backbone, ne, nr, dim, k, precision=64)
+                probe.init(2)
+                bt, _ = tie_free(bt, probe, 512, 1)
+            arr = bt.arrays()
+            per_rank.append(arr)
+            with open(tmp_path / f"batch_{step}_{r}.pkl", "wb") as f:
+                pickle.dump(arr, f)
+        batches.append(per_rank)
+    mp.spawn(shard_workers.gpu_step_worker,
+             args=(G, _port(), str(tmp_path), "small", ALL, b, k, dim, steps, backbone),
+             nprocs=G, join=True)
+    outs = [pickle.load(open(tmp_path / f"gpu{r}.pkl", "rb")) for r in range(G)]
+
+    res = {"loss": [], "grads": {}, "params": {}, "weak": {}}
+    for step in range(1, steps + 1):
+        refs = om.step_multi(batches[step - 1], step=step)
+        for r in range(G):
+            res["loss"].append((outs[r]["loss"][step - 1], refs[r]))
+    specs = m.param_specs(backbone, ne, nr, dim)
+    for name, rows, cols, sparse in specs:
+        def full(key):
+            if name != "entity":
+                return outs[0][key][name]
+            t = np.zeros((rows, cols), np.float32)
+            for r in range(G):
+                t[r::G] = outs[r][key][name]
+            return t
+        res["grads"][name] = (full("grads"), om.get("g:" + name, (rows, cols)))
+        res["params"][name] = (full("params"), om.get(name, (rows, cols)))
+        if name != "entity":  # replicated tensors are identical on every rank
+            assert np.array_equal(outs[0]["params"][name], outs[1]["params"][name]), name
+    check_all(res, allow_frac=1e-3, steps=steps)
