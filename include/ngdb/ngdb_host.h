@@ -53,6 +53,11 @@ int ngdb_batch_destroy(ngdb_batch* bt);
 /* --- planner (Alg. 1) ------------------------------------- */
 int ngdb_step_build(const ngdb_batch* bt, int32_t backbone, int32_t dim, int32_t b_max,
                     int32_t semantic, ngdb_step** out);
+/* flags: bit0 semantic (FuseSemantic anchors), bit1 sharded (phase-ordered
+ * execution of the row-sharded step: every tensor gets a private device slot;
+ * the trace is unchanged) */
+int ngdb_step_build_ex(const ngdb_batch* bt, int32_t backbone, int32_t dim, int32_t b_max,
+                       int32_t flags, ngdb_step** out);
 int ngdb_step_view(const ngdb_step* s, ngdb_step_plan* view);
 /* ExecutionTrace as JSON; with_nodes=1 includes popped node ids per record. */
 int ngdb_step_trace_json(const ngdb_step* s, int32_t with_nodes, char* buf, int64_t cap,

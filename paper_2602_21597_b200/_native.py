@@ -115,6 +115,7 @@ SIGNATURES = {
     "ngdb_batch_arrays": (C.c_int, [C.c_void_p, P(i32), P(i32), P(i32), P(i32), P(i32)]),
     "ngdb_batch_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_step_build": (C.c_int, [C.c_void_p, i32, i32, i32, i32, P(C.c_void_p)]),
+    "ngdb_step_build_ex": (C.c_int, [C.c_void_p, i32, i32, i32, i32, P(C.c_void_p)]),
     "ngdb_step_view": (C.c_int, [C.c_void_p, P(StepPlan)]),
     "ngdb_step_trace_json": (C.c_int, [C.c_void_p, i32, C.c_char_p, i64, P(i64)]),
     "ngdb_step_destroy": (C.c_int, [C.c_void_p]),

@@ -227,6 +227,22 @@ int ngdb_step_build(const ngdb_batch* bt, int32_t backbone, int32_t dim, int32_t
   });
 }
 
+int ngdb_step_build_ex(const ngdb_batch* bt, int32_t backbone, int32_t dim, int32_t b_max,
+                       int32_t flags, ngdb_step** out) {
+  return guarded([&] {
+    ngdb::TrainConfig cfg;
+    cfg.backbone = static_cast<ngdb::Backbone>(backbone);
+    cfg.dim = dim;
+    cfg.n_neg = bt->tb.n_neg;
+    cfg.b_max = b_max;
+    cfg.semantic = (flags & 1) != 0;
+    cfg.sharded = (flags & 2) != 0;
+    auto* s = new ngdb_step();
+    s->plan = ngdb::plan_training_step(bt->tb, cfg);
+    *out = s;
+  });
+}
+
 int ngdb_step_view(const ngdb_step* s, ngdb_step_plan* view) {
   return guarded([&] { *view = s->plan.view(); });
 }

@@ -133,7 +133,7 @@ class ShardStep:
 
 def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: int = 512) -> ShardStep:
     """Plan this rank's batch, exchange the metadata, build the owner work lists."""
-    ps = PlannedStep(batch, backbone, dim, b_max)
+    ps = PlannedStep(batch, backbone, dim, b_max, sharded=True)
     na, ns, b, nc = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
     check(lib.ngdb_step_shard_info(ps._h, C.byref(na), C.byref(ns), C.byref(b), C.byref(nc)))
     anchors = np.zeros(na.value, np.int32)
@@ -183,7 +183,9 @@ class ShardedEngine:
         self._h = C.c_void_p()
         check(lib.ngdb_ctx_create(C.byref(d), device, C.byref(self._h)))
         torch.cuda.set_device(device)
-        self.stream = torch.cuda.current_stream()
+        # one explicit stream carries the context's kernels AND the collectives
+        # (the legacy default stream would not order against the context)
+        self.stream = torch.cuda.Stream(device=device)
         check(lib.ngdb_ctx_set_stream(self._h, C.c_void_p(self.stream.cuda_stream)))
         self.n_local = (n_entities - r + G - 1) // G
         for name, rows, cols, _ in param_specs(backbone, n_entities, n_relations, dim):
@@ -222,6 +224,10 @@ class ShardedEngine:
         if step_no is None:
             self.step_count += 1
             step_no = self.step_count
+        with self.torch.cuda.stream(self.stream):
+            return self._run(step, step_no)
+
+    def _run(self, step: ShardStep, step_no: int) -> np.ndarray:
         v, s = step.views()
         b = ShardBuffers()
         check(lib.ngdb_shard_begin(self._h, C.byref(v), C.byref(s), C.byref(b)))
@@ -258,7 +264,7 @@ class ShardedEngine:
         return self._h
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.ngdb_ctx_destroy(self._h)
             self._h = None
 
