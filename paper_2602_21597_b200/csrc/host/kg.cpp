@@ -130,6 +130,47 @@ std::vector<Triple> read_triples(const std::string& path, int32_t n_ent, int32_t
 
 }  // namespace
 
+const uint32_t* KnowledgeGraph::RelIndex::find(int32_t e, int32_t r) const {
+  if (e < 0 || static_cast<size_t>(e) + 1 >= off.size()) return nullptr;
+  const int32_t* b = rels.data() + off[e];
+  const int32_t* en = rels.data() + off[e + 1];
+  const int32_t* it = std::lower_bound(b, en, r);
+  return (it != en && *it == r) ? &ids[it - rels.data()] : nullptr;
+}
+
+namespace {
+// Appends the (e, r) runs of `t` (sorted by (e, r, x)) as lists of x; e = E(t),
+// x = X(t). Fills the per-entity relation index and per-entity edge lists.
+template <class E, class X>
+void build_side(const std::vector<Triple>& t, int32_t n_entities, E ent, X other,
+                std::vector<std::vector<int32_t>>& lists,
+                std::vector<std::vector<std::pair<int32_t, int32_t>>>& edges,
+                KnowledgeGraph::RelIndex& idx) {
+  const size_t n = t.size();
+  idx.off.assign(static_cast<size_t>(n_entities) + 1, 0);
+  std::vector<int32_t> deg(n_entities, 0);
+  for (size_t i = 0; i < n; ++i) ++deg[ent(t[i])];
+  for (int32_t e = 0; e < n_entities; ++e) edges[e].reserve(deg[e]);
+  for (size_t i = 0; i < n;) {
+    const int32_t e = ent(t[i]), r = t[i].rel;
+    size_t j = i;
+    while (j < n && ent(t[j]) == e && t[j].rel == r) ++j;
+    std::vector<int32_t> l;
+    l.reserve(j - i);
+    for (size_t k = i; k < j; ++k) {
+      l.push_back(other(t[k]));
+      edges[e].emplace_back(r, other(t[k]));
+    }
+    ++idx.off[static_cast<size_t>(e) + 1];
+    idx.rels.push_back(r);
+    idx.ids.push_back(static_cast<uint32_t>(lists.size()));
+    lists.push_back(std::move(l));
+    i = j;
+  }
+  for (int32_t e = 0; e < n_entities; ++e) idx.off[e + 1] += idx.off[e];
+}
+}  // namespace
+
 KnowledgeGraph KnowledgeGraph::from_triples(int32_t n_entities, int32_t n_relations,
                                             std::vector<Triple> triples) {
   for (const Triple& t : triples) {
@@ -145,44 +186,18 @@ KnowledgeGraph KnowledgeGraph::from_triples(int32_t n_entities, int32_t n_relati
   g.n_relations_ = n_relations;
   g.out_edges_.assign(n_entities, {});
   g.in_edges_.assign(n_entities, {});
-
-  // Degrees first so every edge list is reserved exactly once.
-  std::vector<int32_t> out_deg(n_entities, 0), in_deg(n_entities, 0);
-  for (const Triple& t : triples) {
-    ++out_deg[t.head];
-    ++in_deg[t.tail];
-  }
-  for (int32_t e = 0; e < n_entities; ++e) {
-    g.out_edges_[e].reserve(out_deg[e]);
-    g.in_edges_[e].reserve(in_deg[e]);
-  }
-  // Triples are sorted by (h, r, t): forward lists come out sorted by (r, t).
-  g.fwd_index_.reserve(triples.size());
-  for (const Triple& t : triples) {
-    g.out_edges_[t.head].emplace_back(t.rel, t.tail);
-    auto [it, fresh] = g.fwd_index_.try_emplace(key(t.head, t.rel),
-                                                static_cast<uint32_t>(g.lists_.size()));
-    if (fresh) g.lists_.emplace_back();
-    g.lists_[it->second].push_back(t.tail);
-  }
-  // Inverse side: visit in (t, r, h) order so lists come out sorted.
-  std::vector<uint32_t> order(triples.size());
-  for (uint32_t i = 0; i < order.size(); ++i) order[i] = i;
-  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    const Triple &x = triples[a], &y = triples[b];
+  // forward side: (h, r, t) order, lists sorted by t
+  build_side(triples, n_entities, [](const Triple& t) { return t.head; },
+             [](const Triple& t) { return t.tail; }, g.lists_, g.out_edges_, g.fwd_index_);
+  // inverse side: (t, r, h) order, lists sorted by h
+  std::vector<Triple> inv = triples;
+  std::sort(inv.begin(), inv.end(), [](const Triple& x, const Triple& y) {
     if (x.tail != y.tail) return x.tail < y.tail;
     if (x.rel != y.rel) return x.rel < y.rel;
     return x.head < y.head;
   });
-  g.inv_index_.reserve(triples.size());
-  for (uint32_t idx : order) {
-    const Triple& t = triples[idx];
-    g.in_edges_[t.tail].emplace_back(t.rel, t.head);
-    auto [it, fresh] = g.inv_index_.try_emplace(key(t.tail, t.rel),
-                                                static_cast<uint32_t>(g.lists_.size()));
-    if (fresh) g.lists_.emplace_back();
-    g.lists_[it->second].push_back(t.head);
-  }
+  build_side(inv, n_entities, [](const Triple& t) { return t.tail; },
+             [](const Triple& t) { return t.head; }, g.lists_, g.in_edges_, g.inv_index_);
   for (int32_t e = 0; e < n_entities; ++e)
     if (!g.in_edges_[e].empty()) g.has_in_.push_back(e);
   g.triples_ = std::move(triples);
@@ -190,13 +205,13 @@ KnowledgeGraph KnowledgeGraph::from_triples(int32_t n_entities, int32_t n_relati
 }
 
 const std::vector<int32_t>& KnowledgeGraph::neighbors(int32_t e, int32_t r) const {
-  auto it = fwd_index_.find(key(e, r));
-  return it == fwd_index_.end() ? kEmpty : lists_[it->second];
+  const uint32_t* v = fwd_index_.find(e, r);
+  return v ? lists_[*v] : kEmpty;
 }
 
 const std::vector<int32_t>& KnowledgeGraph::inverse_neighbors(int32_t e, int32_t r) const {
-  auto it = inv_index_.find(key(e, r));
-  return it == inv_index_.end() ? kEmpty : lists_[it->second];
+  const uint32_t* v = inv_index_.find(e, r);
+  return v ? lists_[*v] : kEmpty;
 }
 
 bool KnowledgeGraph::has_triple(int32_t h, int32_t r, int32_t t) const {
