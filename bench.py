@@ -41,6 +41,7 @@ CONFIGS = {
     "c2": ("q2b", "nell995", "all", 400, 512, 128),
     "c3": ("betae", "fb15k-237", "c3", 400, 512, 128),
     "c4": ("gqe", "fb15k-237", "c1", 400, 512, 128),  # + 768-d frozen PTE store
+    "c5": ("q2b", "wikikg2", "all", 400, 512, 128),   # entity table row-sharded over ranks
 }
 SEMANTIC_DIM = {"c4": 768}
 MIXES = {"all": ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni",
@@ -213,6 +214,121 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def bench_sharded(args):
+    """configs[4]: Q2B on the wikikg2 shape, entity table row-sharded over the
+    ranks (one process per GPU, NCCL), 512 queries per rank (weak scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200._native import check, lib
+    from paper_2602_21597_b200.sharded import Comm, ShardedEngine, plan_shard_step
+
+    rank, world, local = dist_env()
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+    if "MASTER_ADDR" not in os.environ:  # single process: a one-rank NCCL group
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", local))
+    comm = Comm()
+    backbone, shape, mix, dim, batch, n_neg = CONFIGS[args.config]
+    t_setup = time.perf_counter()
+    graph = m.Graph.synthetic(shape, 1)
+    info = graph.info()
+    w = m.pattern_weights(MIXES[mix])
+    n_steps = args.warmup + args.steps
+    # rank r's batch of step s: Rng(3).fork(s * world + r) (SURVEY §8(e))
+    batches = [m.Batch.sample(graph, w, batch, n_neg, seed=3, tag=(1 + s) * world + rank)
+               for s in range(n_steps)]
+    eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
+                        n_neg=n_neg, max_queries=batch, device=local)
+    plans = [plan_shard_step(comm, b, backbone, dim) for b in batches]
+    setup_s = time.perf_counter() - t_setup
+    ctx = eng.handle
+    step_no = 0
+    for i in range(args.warmup):
+        step_no += 1
+        eng.run(plans[i], step_no)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = lib.ngdb_launch_count(ctx)
+    clocks = ClockSampler(local)
+    clocks.start()
+    import ctypes as C
+    ms = C.c_float()
+    check(lib.ngdb_timer_start(ctx))
+    for i in range(args.steps):
+        step_no += 1
+        eng.run(plans[args.warmup + i], step_no)
+    check(lib.ngdb_timer_stop(ctx, C.byref(ms)))
+    clk = clocks.stop()
+    launches = lib.ngdb_launch_count(ctx) - launches0
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([ms.value / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    value = batch * world / (ms_step / 1000.0)
+    # per-family CUDA-event times on a profiled replay of a few steps
+    check(lib.ngdb_profile_enable(ctx, 1))
+    n_prof = min(args.profile_steps, args.steps)
+    for i in range(n_prof):
+        step_no += 1
+        eng.run(plans[args.warmup + i], step_no)
+    torch.cuda.synchronize()
+    fams = {}
+    for f in range(lib.ngdb_profile_families()):
+        fms, fl, fb = C.c_double(), C.c_int64(), C.c_double()
+        check(lib.ngdb_profile_read(ctx, f, C.byref(fms), C.byref(fl), C.byref(fb)))
+        if fl.value:
+            fams[lib.ngdb_profile_family_name(f).decode()] = {
+                "ms_per_step": fms.value / n_prof, "launches_per_step": fl.value / n_prof,
+                "gbs": fb.value / (fms.value / 1000.0) / 1e9 if fms.value > 0 else 0.0,
+                "bytes_per_step": fb.value / n_prof, "flops_per_step": 0.0, "tflops": 0.0}
+    check(lib.ngdb_profile_enable(ctx, 0))
+    # e2e: host planning (sampling, DAG, Max-Fillness, metadata all-gather, owner
+    # lists) + every stage and collective, per step
+    e2e_batches = [m.Batch.sample(graph, w, batch, n_neg, seed=3,
+                                  tag=(1 + n_steps + s) * world + rank) for s in range(args.steps)]
+    dist.barrier()
+    t0 = time.perf_counter()
+    for b in e2e_batches:
+        step_no += 1
+        eng.run(plan_shard_step(comm, b, backbone, dim), step_no)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e = batch * world * args.steps / float(t.item())
+    if rank == 0:
+        G = world
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{backbone} on {shape}-shaped synthetic KG "
+                                   f"({info['n_entities']} entities, {info['n_relations']} "
+                                   f"relations), {mix}-pattern mix, entity table row-sharded",
+                       "global_batch": batch * world, "n_neg": n_neg, "dim": dim,
+                       "parallelism": f"rowshard{G}+dp{G}",
+                       "l2": "inputs larger than L2: local entity table + Adam moments "
+                             f"{3 * info['n_entities'] * dim * 4 / G / 1e9:.1f} GB per rank"},
+            "roofline": roofline(fams) if fams else None,
+            "cpu_baseline": None,
+            "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": None,
+                    "d2h_bytes_per_step": 4 * batch + 16},
+            "families": fams,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -230,6 +346,8 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args)
+    if args.config == "c5":
+        return bench_sharded(args)
 
     rank, world, local = dist_env()
     dist = None

@@ -195,9 +195,9 @@ struct ngdb_ctx {
   struct ShardState {
     int32_t* blob = nullptr;
     int64_t blob_cap = 0;
-    int32_t* staging = nullptr;
-    int64_t staging_cap = 0;
-    cudaEvent_t staged = nullptr;
+    int32_t* staging[2] = {nullptr, nullptr};  // pinned, alternating with the plan staging
+    int64_t staging_cap[2] = {0, 0};
+    cudaEvent_t staged[2] = {nullptr, nullptr};
     float* buf = nullptr;
     int64_t buf_cap = 0;
     ShardDev dev{};
@@ -282,7 +282,7 @@ void add_param(ngdb_ctx* c, const char* name, int64_t rows, int64_t cols, bool s
 void ensure_f(float*& p, int64_t& cap, int64_t need) {
   if (need <= cap) return;
   if (p) CK(cudaFree(p));
-  cap = std::max<int64_t>(need, cap + cap / 4);
+  cap = std::max<int64_t>(need + need / 2, cap + cap / 2);
   p = dmalloc<float>(cap);
 }
 
@@ -602,7 +602,7 @@ void upload_plan(ngdb_ctx* c, const ngdb_step_plan& plan, ngdb_plan* dst, int64_
       CK(cudaStreamSynchronize(c->stream));
       CK(cudaFree(dst->blob));
     }
-    dst_cap = std::max<int64_t>(L.total, dst_cap + dst_cap / 4);
+    dst_cap = std::max<int64_t>(L.total + L.total / 2, dst_cap + dst_cap / 2);
     dst->blob = dmalloc<int32_t>(dst_cap);
   }
   pack_plan(plan, L, staging);
@@ -665,7 +665,7 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
-    CK(cudaEventCreateWithFlags(&c->sh.staged, cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k) CK(cudaEventCreateWithFlags(&c->sh.staged[k], cudaEventDisableTiming));
     const int64_t D = d.dim;
     // this rank's entity rows e = rank (mod world), local row e div world
     const int64_t n_ent_local = (d.n_entities - c->rank + world - 1) / world;
@@ -802,8 +802,10 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   if (c->t1) cudaEventDestroy(c->t1);
   if (c->sh.blob) cudaFree(c->sh.blob);
   if (c->sh.buf) cudaFree(c->sh.buf);
-  if (c->sh.staging) cudaFreeHost(c->sh.staging);
-  if (c->sh.staged) cudaEventDestroy(c->sh.staged);
+  for (int k = 0; k < 2; ++k) {
+    if (c->sh.staging[k]) cudaFreeHost(c->sh.staging[k]);
+    if (c->sh.staged[k]) cudaEventDestroy(c->sh.staged[k]);
+  }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return NGDB_OK;
@@ -899,7 +901,7 @@ int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
     CK(cudaEventSynchronize(c->staged[i]));
     if (L.total > c->staging_cap[i]) {
       if (c->staging[i]) CK(cudaFreeHost(c->staging[i]));
-      c->staging_cap[i] = L.total + L.total / 4;
+      c->staging_cap[i] = L.total + L.total / 2;
       void* p = nullptr;
       CK(cudaMallocHost(&p, c->staging_cap[i] * sizeof(int32_t)));
       c->staging[i] = static_cast<int32_t*>(p);
@@ -1130,7 +1132,7 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
     CK(cudaEventSynchronize(c->staged[i]));
     if (L.total > c->staging_cap[i]) {
       if (c->staging[i]) CK(cudaFreeHost(c->staging[i]));
-      c->staging_cap[i] = L.total + L.total / 4;
+      c->staging_cap[i] = L.total + L.total / 2;
       void* hp = nullptr;
       CK(cudaMallocHost(&hp, c->staging_cap[i] * sizeof(int32_t)));
       c->staging[i] = static_cast<int32_t*>(hp);
@@ -1151,21 +1153,22 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
                   o_seg = o_rows + up64(sp->n_rows), o_con = o_seg + up64(sp->n_rows + 1),
                   total = o_con + up64(n_con);
     auto& sh = c->sh;
-    CK(cudaEventSynchronize(sh.staged));
-    if (total > sh.staging_cap) {
-      if (sh.staging) CK(cudaFreeHost(sh.staging));
-      sh.staging_cap = total + total / 4;
+    // the pinned buffer of two steps ago may still feed its H2D copy
+    CK(cudaEventSynchronize(sh.staged[i]));
+    if (total > sh.staging_cap[i]) {
+      if (sh.staging[i]) CK(cudaFreeHost(sh.staging[i]));
+      sh.staging_cap[i] = total + total / 2;
       void* hp = nullptr;
-      CK(cudaMallocHost(&hp, sh.staging_cap * sizeof(int32_t)));
-      sh.staging = static_cast<int32_t*>(hp);
+      CK(cudaMallocHost(&hp, sh.staging_cap[i] * sizeof(int32_t)));
+      sh.staging[i] = static_cast<int32_t*>(hp);
     }
     if (total > sh.blob_cap) {
       CK(cudaStreamSynchronize(c->stream));
       if (sh.blob) CK(cudaFree(sh.blob));
-      sh.blob_cap = total + total / 4;
+      sh.blob_cap = total + total / 2;
       sh.blob = dmalloc<int32_t>(sh.blob_cap);
     }
-    int32_t* h = sh.staging;
+    int32_t* h = sh.staging[i];
     std::memcpy(h + o_anc, sp->anchor_ids, G * A * 4);
     std::memcpy(h + o_k, sp->unit_k, U * 4);
     std::memcpy(h + o_slots, sp->unit_slots, U * 3 * 4);
@@ -1178,7 +1181,7 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
       std::memcpy(h + o_con, sp->contrib, n_con * 4);
     }
     CK(cudaMemcpyAsync(sh.blob, h, total * 4, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaEventRecord(sh.staged, c->stream));
+    CK(cudaEventRecord(sh.staged[i], c->stream));
 
     // 3) exchange buffers
     const int64_t ew = c->params[c->ent_idx].cols, wq = c->query_width();
@@ -1191,7 +1194,7 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
     if (need > sh.buf_cap) {
       CK(cudaStreamSynchronize(c->stream));
       if (sh.buf) CK(cudaFree(sh.buf));
-      sh.buf_cap = need + need / 4;
+      sh.buf_cap = need + need / 2;
       sh.buf = dmalloc<float>(sh.buf_cap);
       ++c->buffer_gen;
     }
