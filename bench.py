@@ -340,6 +340,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--quiet", action="store_true")
+    ap.add_argument("--producers", type=int, default=0, help="e2e host producer threads (0: cores-1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -457,31 +458,48 @@ def main():
     roof = roofline(fams)
 
     # ---- e2e: public C ABI call with host buffers ----------------------------
-    losses = np.zeros(batch, dtype=np.float32)
-    total = C.c_double()
-    h2d = []
-    for s in steps:
-        v = s.view()
-        h2d.append(32 * v.n_nodes + 4 * v.n_queries * v.n_candidates + 4 * (
-            2 * v.n_entity_rows + 1 + v.entity_seg[v.n_entity_rows] + 2 * v.n_relation_rows + 1 +
-            v.relation_seg[v.n_relation_rows]))
-    for i in range(args.warmup):
-        step_no += 1
-        check(lib.ngdb_train_step(ctx, batches[i]._h, 512, step_no,
-                                  losses.ctypes.data_as(C.POINTER(C.c_float)), C.byref(total)))
+    # The trainer loop (ngdb_train_run): host producer threads sample and plan
+    # every step's batch, the calling thread uploads each plan (one H2D from
+    # pinned staging), launches its pools + optimizer and reads the step's
+    # per-query losses back (D2H) while the next step runs. Sampling, planning,
+    # copies and kernels of every step are inside the timed region.
+    w = m.pattern_weights(MIXES[mix])
+    tag0 = 1_000_000 + rank * 100_000
+
+    def loop(n, tag):
+        eng.step_count = step_no
+        return eng.train(graph, w, n, batch=batch, n_neg=n_neg, seed=3, first_tag=tag,
+                         n_producers=args.producers)
+    loop(args.warmup, tag0)
+    step_no += args.warmup
+    b0, d0 = C.c_int64(), C.c_int64()
+    check(lib.ngdb_transfer_bytes(ctx, C.byref(b0), C.byref(d0)))
     barrier()
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        step_no += 1
-        check(lib.ngdb_train_step(ctx, batches[args.warmup + i]._h, 512, step_no,
-                                  losses.ctypes.data_as(C.POINTER(C.c_float)), C.byref(total)))
+    loop(args.steps, tag0 + args.warmup)
     e2e_s = time.perf_counter() - t0
+    step_no += args.steps
+    b1, d1 = C.c_int64(), C.c_int64()
+    check(lib.ngdb_transfer_bytes(ctx, C.byref(b1), C.byref(d1)))
+    plan_wait = eng.last_plan_wait_s
     if dist is not None:
         import torch
         t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = batch * world * args.steps / e2e_s
+    producers = args.producers if args.producers > 0 else max(1, (os.cpu_count() or 2) - 1)
+    # the same public API one step at a time, no overlap (ngdb_train_step on
+    # pre-sampled batches): what a synchronous caller gets
+    losses = np.zeros(batch, dtype=np.float32)
+    total = C.c_double()
+    n_seq = min(args.steps, 20)
+    t0 = time.perf_counter()
+    for i in range(n_seq):
+        step_no += 1
+        check(lib.ngdb_train_step(ctx, batches[args.warmup + i]._h, 512, step_no,
+                                  losses.ctypes.data_as(C.POINTER(C.c_float)), C.byref(total)))
+    seq_qps = batch * n_seq / (time.perf_counter() - t0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -513,7 +531,13 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "queries/s",
-                    "h2d_bytes_per_step": int(np.mean(h2d)), "d2h_bytes_per_step": 4 * batch + 16},
+                    "h2d_bytes_per_step": int((b1.value - b0.value) / args.steps),
+                    "d2h_bytes_per_step": int((d1.value - d0.value) / args.steps),
+                    "api": "ngdb_train_run (sampling + planning on host producer threads, "
+                           "plan H2D, kernels, loss D2H per step)",
+                    "producers": producers,
+                    "consumer_wait_ms_per_step": 1000 * plan_wait / args.steps,
+                    "sequential_train_step": seq_qps},
             "gpu_launches": int(launches),
             "clocks": clk,
             "families": fams if not args.quiet else None,

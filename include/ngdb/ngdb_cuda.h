@@ -189,6 +189,13 @@ int ngdb_optimizer_step(ngdb_ctx* ctx, int64_t step);
  * flag. */
 int ngdb_step_end(ngdb_ctx* ctx, float* per_query_loss, int32_t n_queries, double* loss_sum,
                   int32_t* nonfinite);
+/* Asynchronous step end: enqueues the D2H of the per-query losses and device
+ * flags into a pinned result slot and returns a ticket at once, so the host can
+ * plan and launch step i+1 while step i runs. At most 4 tickets outstanding;
+ * ngdb_step_wait blocks on one and reports it like ngdb_step_end. */
+int ngdb_step_end_async(ngdb_ctx* ctx, int64_t* ticket);
+int ngdb_step_wait(ngdb_ctx* ctx, int64_t ticket, float* per_query_loss, int32_t n_queries,
+                   double* loss_sum, int32_t* nonfinite);
 
 /* Resident plans: upload once, replay many times (benchmark / graph replay). */
 int ngdb_plan_create(ngdb_ctx* ctx, const ngdb_step_plan* plan, ngdb_plan** out);
@@ -224,6 +231,9 @@ int32_t ngdb_profile_families(void);
 const char* ngdb_profile_family_name(int32_t family);
 /* Kernel launches issued so far by this context (all families). */
 int64_t ngdb_launch_count(ngdb_ctx* ctx);
+/* Cumulative bytes of step data the streaming ABI copied: plan uploads (H2D)
+ * and loss/flag read-backs (D2H). */
+int ngdb_transfer_bytes(ngdb_ctx* ctx, int64_t* h2d, int64_t* d2h);
 /* Flush L2 by writing a buffer larger than it (timing hygiene). */
 int ngdb_flush_l2(ngdb_ctx* ctx);
 

@@ -112,6 +112,28 @@ int ngdb_ngse_read(const char* path, float* out, int64_t cap, int64_t* count, in
 /* --- the public training call: plan + run one step on a context ----------- */
 int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t step,
                     float* per_query_loss, double* loss_sum);
+/* The trainer loop (SPEC.md:568-576 train; producers SPEC.md:591): n_steps
+ * steps of freshly sampled batches, batch i from Rng(seed).fork(first_tag + i)
+ * with patterns ~ pattern_weights. n_producers host threads sample and plan
+ * (0 = hardware threads - 1); the calling thread uploads each plan, launches
+ * it and reads step i's losses back while step i+1 runs. Same batches, plans
+ * and update order as sampling + ngdb_train_step in a loop. Adam steps are
+ * first_step+1 .. first_step+n_steps. loss_per_step [n_steps] (may be NULL),
+ * per_query_loss [n_steps][batch] (may be NULL). */
+typedef struct ngdb_train_opts {
+  const double* pattern_weights; /* 14, enum order (query.hpp:14-29) */
+  int32_t batch;                 /* queries per step (512) */
+  int32_t n_neg;                 /* must equal the context's n_neg */
+  int32_t b_max;                 /* Max-Fillness B_max (512) */
+  int32_t n_producers;           /* 0: hardware threads - 1 */
+  int32_t queue_depth;           /* planned batches ahead; 0: 2 * n_producers */
+  uint64_t seed;                 /* sampler seed (3) */
+  uint64_t first_tag;
+} ngdb_train_opts;
+int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
+                   int64_t first_step, int32_t n_steps, double* loss_per_step,
+                   float* per_query_loss, double* plan_wait_s);
+
 /* Streaming run of an already built step (H2D of its plan inside the call). */
 int ngdb_run_step(ngdb_ctx* ctx, const ngdb_step* s, int64_t step, float* per_query_loss,
                   double* loss_sum);

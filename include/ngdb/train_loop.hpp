@@ -1,0 +1,48 @@
+// ngdb/train_loop.hpp — the trainer's producer/consumer loop (SPEC.md:568-576
+// train consumer loop, SPEC.md:591 producers never touch kernels).
+//
+// Producers sample batch i from Rng(seed).fork(first_tag + i) and plan it
+// (DAG, Max-Fillness trace, device plan: all pure host work on the batch); the
+// consumer thread takes the plans strictly in index order, uploads each one
+// (one H2D), launches its pools and the optimizer, and collects the losses of
+// step i after it has launched step i+1 (ngdb_step_end_async), so host
+// planning, launch and the device step overlap. Batch contents, plans and the
+// parameter update order are exactly those of the sequential
+// sample -> ngdb_train_step loop; only the host work is spread over threads.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "ngdb/kg.hpp"
+#include "ngdb/ngdb_cuda.h"
+#include "ngdb/sampler.hpp"
+#include "ngdb/trainer.hpp"
+
+namespace ngdb {
+
+struct TrainLoopConfig {
+  SamplingDistribution pi;
+  int32_t batch = 512;
+  int32_t n_neg = 128;
+  int32_t b_max = 512;
+  uint64_t seed = 3;        // sampler seed (seeds kg 1, params 2, sampler 3)
+  uint64_t first_tag = 0;   // batch i uses Rng(seed).fork(first_tag + i)
+  int32_t n_producers = 0;  // 0: hardware threads - 1 (at least 1)
+  int32_t queue_depth = 0;  // planned batches buffered ahead of the consumer; 0: 2 * producers
+};
+
+struct TrainLoopStats {
+  double plan_wait_s = 0.0;  // consumer time spent waiting for a planned batch
+  int32_t producers = 0;
+};
+
+// Runs n_steps training steps on ctx; step numbers first_step + 1 .. first_step
+// + n_steps (1-based Adam step). loss_per_step[i] = Σ_q ℓ_q of step i;
+// per_query_loss (optional) is [n_steps][batch]. Throws the ngdb::Error of the
+// first failure (a producer's error surfaces at its step).
+TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const TrainLoopConfig& cfg,
+                              int64_t first_step, int32_t n_steps, double* loss_per_step,
+                              float* per_query_loss);
+
+}  // namespace ngdb

@@ -55,6 +55,11 @@ class ShardPlan(C.Structure):
     ]
 
 
+class TrainOpts(C.Structure):
+    _fields_ = [("pattern_weights", P(f64)), ("batch", i32), ("n_neg", i32), ("b_max", i32),
+                ("n_producers", i32), ("queue_depth", i32), ("seed", u64), ("first_tag", u64)]
+
+
 SHARD_BUFFERS = ("anchor_send", "anchor_rows", "query_mine", "query_all", "dq_part", "dq_mine",
                  "loss_part", "loss_mine", "grad_send", "grad_all", "reduce")
 
@@ -81,6 +86,8 @@ SIGNATURES = {
     "ngdb_exec_pool": (C.c_int, [C.c_void_p, P(PoolDesc)]),
     "ngdb_optimizer_step": (C.c_int, [C.c_void_p, i64]),
     "ngdb_step_end": (C.c_int, [C.c_void_p, P(f32), i32, P(f64), P(i32)]),
+    "ngdb_step_end_async": (C.c_int, [C.c_void_p, P(i64)]),
+    "ngdb_step_wait": (C.c_int, [C.c_void_p, i64, P(f32), i32, P(f64), P(i32)]),
     "ngdb_plan_create": (C.c_int, [C.c_void_p, P(StepPlan), P(C.c_void_p)]),
     "ngdb_plan_run": (C.c_int, [C.c_void_p, C.c_void_p, i64]),
     "ngdb_plan_prepare": (C.c_int, [C.c_void_p, C.c_void_p]),
@@ -98,6 +105,7 @@ SIGNATURES = {
     "ngdb_profile_flops": (C.c_int, [C.c_void_p, i32, P(f64)]),
     "ngdb_profile_family_name": (C.c_char_p, [i32]),
     "ngdb_launch_count": (i64, [C.c_void_p]),
+    "ngdb_transfer_bytes": (C.c_int, [C.c_void_p, P(i64), P(i64)]),
     "ngdb_flush_l2": (C.c_int, [C.c_void_p]),
     # ngdb_host.h
     "ngdb_graph_synthetic": (C.c_int, [C.c_char_p, u64, P(C.c_void_p)]),
@@ -137,6 +145,8 @@ SIGNATURES = {
     "ngdb_select_pool": (C.c_int, [P(i64), P(i64), P(i32)]),
     "ngdb_jsonl_roundtrip": (C.c_int, [C.c_char_p, C.c_char_p, i64]),
     "ngdb_train_step": (C.c_int, [C.c_void_p, C.c_void_p, i32, i64, P(f32), P(f64)]),
+    "ngdb_train_run": (C.c_int, [C.c_void_p, C.c_void_p, P(TrainOpts), i64, i32, P(f64), P(f32),
+                                 P(f64)]),
     "ngdb_run_step": (C.c_int, [C.c_void_p, C.c_void_p, i64, P(f32), P(f64)]),
     # test hook (tc_gemm.cu): tcgen05 3xTF32 GEMM on host buffers
     "ngdb_debug_tc_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -215,6 +215,16 @@ struct ngdb_ctx {
   int64_t stream_cap[2] = {0, 0};
   int cur = 0;
   ngdb_plan* active = nullptr;
+  // asynchronous step ends: a ring of pinned result slots (losses + flags)
+  static constexpr int kResultSlots = 4;
+  struct ResultSlot {
+    float* host = nullptr;  // [cap] losses, then 4 int32 flags
+    int64_t cap = 0;
+    int32_t n_queries = 0;
+    int64_t ticket = -1;    // outstanding ticket, -1 when free
+    cudaEvent_t done = nullptr;
+  } results[kResultSlots];
+  int64_t next_ticket = 0;
   bool debug = false;
   // timing / accounting
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -225,6 +235,7 @@ struct ngdb_ctx {
   double fam_ms[F_COUNT] = {}, fam_bytes[F_COUNT] = {}, fam_flops[F_COUNT] = {};
   int64_t fam_launches[F_COUNT] = {};
   int64_t launches = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;  // step data copied by the streaming ABI
   float* d_bc = nullptr;        // Adam bias corrections of the current step
   int64_t buffer_gen = 0;       // bumped whenever a buffer captured by a graph moves
   bool use_graphs = true;
@@ -607,6 +618,7 @@ void upload_plan(ngdb_ctx* c, const ngdb_step_plan& plan, ngdb_plan* dst, int64_
   }
   pack_plan(plan, L, staging);
   CK(cudaMemcpyAsync(dst->blob, staging, L.total * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  c->h2d_bytes += L.total * sizeof(int32_t);
   dst->layout = L;
   dst->meta = meta_of(plan);
 }
@@ -793,6 +805,10 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
     if (c->stream_plan[i].blob) cudaFree(c->stream_plan[i].blob);
     if (c->staged[i]) cudaEventDestroy(c->staged[i]);
   }
+  for (auto& r : c->results) {
+    if (r.host) cudaFreeHost(r.host);
+    if (r.done) cudaEventDestroy(r.done);
+  }
   for (auto& r : c->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -944,6 +960,7 @@ int ngdb_step_end(ngdb_ctx* c, float* per_query_loss, int32_t n_queries, double*
     int32_t flags[4] = {0, 0, 0, 0};
     CK(cudaMemcpyAsync(dst, c->loss_out, nq * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(flags, c->flags, sizeof(flags), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes += nq * sizeof(float) + sizeof(flags);
     CK(cudaStreamSynchronize(c->stream));
     c->drain_profile();
     if (loss_sum) {
@@ -953,6 +970,57 @@ int ngdb_step_end(ngdb_ctx* c, float* per_query_loss, int32_t n_queries, double*
     }
     if (nonfinite) *nonfinite = flags[0];
     c->active = nullptr;
+    if (flags[1]) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "embedding index out of range in plan"};
+  });
+}
+
+int ngdb_step_end_async(ngdb_ctx* c, int64_t* ticket) {
+  return guarded([&] {
+    if (!c->active) throw Fail{NGDB_ERR_CONFIG, "step_end outside a step"};
+    if (c->profiling) throw Fail{NGDB_ERR_CONFIG, "step_end_async while profiling"};
+    const int64_t t = c->next_ticket;
+    auto& r = c->results[t % ngdb_ctx::kResultSlots];
+    if (r.ticket >= 0) throw Fail{NGDB_ERR_CONFIG, "too many outstanding steps (ngdb_step_wait)"};
+    const int32_t nq = c->active->meta.n_queries;
+    if (nq + 4 > r.cap) {
+      if (r.host) CK(cudaFreeHost(r.host));
+      void* p = nullptr;
+      r.cap = std::max<int64_t>(nq + 4, 1024);
+      CK(cudaMallocHost(&p, r.cap * sizeof(float)));
+      r.host = static_cast<float*>(p);
+    }
+    if (!r.done) CK(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
+    CK(cudaMemcpyAsync(r.host, c->loss_out, nq * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(r.host + nq, c->flags, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->d2h_bytes += nq * sizeof(float) + 4 * sizeof(int32_t);
+    CK(cudaEventRecord(r.done, c->stream));
+    r.n_queries = nq;
+    r.ticket = t;
+    ++c->next_ticket;
+    c->active = nullptr;
+    *ticket = t;
+  });
+}
+
+int ngdb_step_wait(ngdb_ctx* c, int64_t ticket, float* per_query_loss, int32_t n_queries,
+                   double* loss_sum, int32_t* nonfinite) {
+  return guarded([&] {
+    if (ticket < 0) throw Fail{NGDB_ERR_CONFIG, "invalid ticket"};
+    auto& r = c->results[ticket % ngdb_ctx::kResultSlots];
+    if (r.ticket != ticket) throw Fail{NGDB_ERR_CONFIG, "unknown or already collected ticket"};
+    CK(cudaEventSynchronize(r.done));
+    r.ticket = -1;
+    const int32_t nq = r.n_queries;
+    if (per_query_loss && n_queries >= nq) std::memcpy(per_query_loss, r.host, nq * sizeof(float));
+    if (loss_sum) {
+      double s = 0.0;
+      for (int32_t i = 0; i < nq; ++i) s += r.host[i];
+      *loss_sum = s;
+    }
+    int32_t flags[4];
+    std::memcpy(flags, r.host + nq, sizeof(flags));
+    if (nonfinite) *nonfinite = flags[0];
     if (flags[1]) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "embedding index out of range in plan"};
   });
 }
@@ -1091,6 +1159,13 @@ const char* ngdb_profile_family_name(int32_t f) {
 }
 
 int64_t ngdb_launch_count(ngdb_ctx* c) { return c ? c->launches : 0; }
+
+int ngdb_transfer_bytes(ngdb_ctx* c, int64_t* h2d, int64_t* d2h) {
+  return guarded([&] {
+    if (h2d) *h2d = c->h2d_bytes;
+    if (d2h) *d2h = c->d2h_bytes;
+  });
+}
 
 int ngdb_flush_l2(ngdb_ctx* c) {
   return guarded([&] {

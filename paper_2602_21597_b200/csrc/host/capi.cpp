@@ -13,6 +13,7 @@
 #include "ngdb/shard.hpp"
 #include "ngdb/synth.hpp"
 #include "ngdb/trainer.hpp"
+#include "ngdb/train_loop.hpp"
 
 namespace ngdb_internal {
 void set_last_error(const std::string& msg);  // ctx.cu
@@ -469,6 +470,26 @@ int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t 
     ngdb_step s;
     s.plan = ngdb::plan_training_step(bt->tb, cfg);
     ngdb::check_status(ngdb_run_step(ctx, &s, step, per_query_loss, loss_sum));
+  });
+}
+
+int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
+                   int64_t first_step, int32_t n_steps, double* loss_per_step,
+                   float* per_query_loss, double* plan_wait_s) {
+  return guarded([&] {
+    if (!ctx || !g || !o || !o->pattern_weights) throw ngdb::ConfigError("null argument");
+    ngdb::TrainLoopConfig cfg;
+    for (int i = 0; i < ngdb::kPatternCount; ++i) cfg.pi.weights[i] = o->pattern_weights[i];
+    cfg.batch = o->batch;
+    cfg.n_neg = o->n_neg;
+    cfg.b_max = o->b_max;
+    cfg.n_producers = o->n_producers;
+    cfg.queue_depth = o->queue_depth;
+    cfg.seed = o->seed;
+    cfg.first_tag = o->first_tag;
+    const auto st = ngdb::run_train_loop(ctx, g->split, cfg, first_step, n_steps, loss_per_step,
+                                         per_query_loss);
+    if (plan_wait_s) *plan_wait_s = st.plan_wait_s;
   });
 }
 

@@ -3,6 +3,8 @@
 
 #include <algorithm>
 
+#include "ngdb/radix.hpp"
+
 #include "ngdb/common.hpp"
 
 namespace ngdb {
@@ -51,7 +53,7 @@ ShardPlanHost build_shard_plan(const ShardSpec& spec, const int32_t* anchor_ids_
     }
     p.unit_off[u + 1] = static_cast<int32_t>(p.owned.size());
   }
-  std::sort(keys.begin(), keys.end());
+  radix_sort_u64(keys);
   p.contrib.resize(keys.size());
   for (size_t i = 0; i < keys.size(); ++i) {
     const int32_t row = static_cast<int32_t>(keys[i] >> 32);

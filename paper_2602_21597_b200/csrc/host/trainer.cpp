@@ -3,6 +3,8 @@
 #include "ngdb/trainer.hpp"
 
 #include <algorithm>
+
+#include "ngdb/radix.hpp"
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -147,9 +149,11 @@ ngdb_step_plan StepPlanHost::view() const {
 namespace {
 
 // (row, code) pairs -> CSR with rows ascending and codes ascending within a row.
+// The caller emits the keys with codes ascending in input order, so a stable
+// sort by row alone yields the (row, code) order.
 void build_csr(std::vector<uint64_t>& keys, std::vector<int32_t>& rows, std::vector<int32_t>& seg,
                std::vector<int32_t>& contrib) {
-  std::sort(keys.begin(), keys.end());
+  radix_sort_u64(keys, 32);
   rows.clear();
   seg.clear();
   contrib.resize(keys.size());
@@ -194,8 +198,9 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
 
   // Slots of the persistent per-step staging buffers, in forward-id order.
   std::vector<int32_t> aux(nf, -1);
-  std::vector<uint64_t> ekeys, rkeys;
+  std::vector<uint64_t> ekeys, akeys, rkeys;
   ekeys.reserve(static_cast<size_t>(B) * nc * 2 + 4 * B);
+  akeys.reserve(4 * static_cast<size_t>(B));
   rkeys.reserve(4 * static_cast<size_t>(B));
   for (int32_t i = 0; i < nf; ++i) {
     const OperatorNode& x = f.nodes[i];
@@ -203,7 +208,7 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
       case OpKind::EmbedAnchor:
       case OpKind::FuseSemantic:
         aux[i] = plan.n_anchor_slots++;
-        ekeys.push_back(pack_key(x.payload, -aux[i] - 1));
+        akeys.push_back(pack_key(x.payload, -aux[i] - 1));
         break;
       case OpKind::Project:
         aux[i] = plan.n_project_slots++;
@@ -220,6 +225,9 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
       default: break;
     }
   }
+  // anchor codes -aux-1 descend in slot order: reversed, they precede the
+  // ascending scoring codes
+  ekeys.insert(ekeys.begin(), akeys.rbegin(), akeys.rend());
   build_csr(ekeys, plan.entity_rows, plan.entity_seg, plan.entity_contrib);
   build_csr(rkeys, plan.relation_rows, plan.relation_seg, plan.relation_contrib);
 

@@ -13,7 +13,7 @@ from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
-from ._native import ModelDesc, NodeDesc, PoolDesc, StepPlan, check, lib
+from ._native import ModelDesc, NodeDesc, PoolDesc, StepPlan, TrainOpts, check, lib
 
 # query.hpp:14-29 enum order == index order of π
 PATTERNS = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni", "inp"]
@@ -299,6 +299,26 @@ class Engine:
         check(lib.ngdb_train_step(self._h, batch._h, self.b_max, self.step_count,
                                   _p(losses, C.c_float), C.byref(total)))
         return losses
+
+    def train(self, graph: Graph, weights: np.ndarray, n_steps: int, batch: int = 512,
+              n_neg: int = 128, seed: int = 3, first_tag: int = 0, n_producers: int = 0,
+              queue_depth: int = 0, per_query: bool = False):
+        """The trainer loop: n_steps steps of batches sampled
+        from Rng(seed).fork(first_tag + i) by host producer threads, planned,
+        uploaded and run back to back (ngdb_train_run). Returns the per-step loss
+        sums (and [n_steps][batch] per-query losses with per_query=True)."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        opts = TrainOpts(_p(w, C.c_double), batch, n_neg, self.b_max, n_producers, queue_depth,
+                         seed, first_tag)
+        sums = np.zeros(n_steps, dtype=np.float64)
+        pq = np.zeros((n_steps, batch), dtype=np.float32) if per_query else None
+        wait = C.c_double()
+        check(lib.ngdb_train_run(self._h, graph._h, C.byref(opts), self.step_count, n_steps,
+                                 _p(sums, C.c_double),
+                                 _p(pq, C.c_float) if pq is not None else None, C.byref(wait)))
+        self.step_count += n_steps
+        self.last_plan_wait_s = wait.value
+        return (sums, pq) if per_query else sums
 
     def run_step(self, step: PlannedStep, n_queries: int) -> np.ndarray:
         losses = np.zeros(n_queries, dtype=np.float32)

@@ -1,0 +1,82 @@
+"""The producer/consumer trainer loop (ngdb_train_run) runs
+exactly the sequential loop: batch i from Rng(seed).fork(first_tag + i),
+planned and executed in index order. Per-query losses and the parameters after
+the run are bit-identical to sampling + ngdb_train_step step by step, for any
+producer count; the first step is also checked against the CPU oracle."""
+import numpy as np
+import pytest
+
+import paper_2602_21597_b200 as m
+from parity import rel_close
+
+pytestmark = pytest.mark.gpu
+
+ALL = m.engine.PATTERNS
+
+
+def _engine(graph, backbone, dim, k, b):
+    info = graph.info()
+    return m.Engine(backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=k,
+                    max_queries=b)
+
+
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
+@pytest.mark.parametrize("producers", [1, 3])
+def test_loop_matches_sequential(small_graph, backbone, producers):
+    b, k, dim, steps = 128, 16, 32, 5
+    w = m.pattern_weights(ALL)
+    seq = _engine(small_graph, backbone, dim, k, b)
+    ref = []
+    for i in range(steps):
+        batch = m.Batch.sample(small_graph, w, b, k, seed=3, tag=7 + i)
+        ref.append(seq.train_step(batch))
+    loop = _engine(small_graph, backbone, dim, k, b)
+    sums, pq = loop.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=7,
+                          n_producers=producers, queue_depth=2, per_query=True)
+    for i in range(steps):
+        np.testing.assert_array_equal(pq[i], ref[i])
+        assert sums[i] == pytest.approx(float(np.sum(ref[i], dtype=np.float64)), rel=1e-12)
+    for name in ("entity", "relation"):
+        np.testing.assert_array_equal(loop.download(name), seq.download(name))
+    assert loop.step_count == seq.step_count == steps
+
+
+def test_loop_continues_step_numbering(small_graph):
+    # two runs of 2 + 3 steps == one run of 5 (Adam bias correction uses the global step)
+    b, k, dim = 64, 8, 16
+    w = m.pattern_weights(ALL)
+    one = _engine(small_graph, "q2b", dim, k, b)
+    s1 = one.train(small_graph, w, 5, batch=b, n_neg=k, first_tag=0, n_producers=2)
+    two = _engine(small_graph, "q2b", dim, k, b)
+    s2 = np.concatenate([two.train(small_graph, w, 2, batch=b, n_neg=k, first_tag=0),
+                         two.train(small_graph, w, 3, batch=b, n_neg=k, first_tag=2)])
+    np.testing.assert_array_equal(s1, s2)
+    np.testing.assert_array_equal(one.download("entity"), two.download("entity"))
+
+
+def test_loop_first_step_vs_oracle(small_graph, small_oracle_graph):
+    import oracle as O
+    b, k, dim = 128, 16, 32
+    info = small_graph.info()
+    w = m.pattern_weights(ALL)
+    eng = _engine(small_graph, "q2b", dim, k, b)
+    _, pq = eng.train(small_graph, w, 1, batch=b, n_neg=k, seed=3, first_tag=11, per_query=True)
+    a = m.Batch.sample(small_graph, w, b, k, seed=3, tag=11).arrays()
+    om = O.OracleModel("q2b", info["n_entities"], info["n_relations"], dim, k, precision=64)
+    om.init(2)
+    ref = om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, b_max=512, step=1)
+    ok, nbad, worst = rel_close(pq[0], np.asarray(ref))
+    assert ok, f"{nbad} bad, worst {worst:.3e}"
+
+
+def test_loop_errors_surface(small_graph):
+    b, k, dim = 32, 8, 16
+    eng = _engine(small_graph, "gqe", dim, k, b)
+    w = m.pattern_weights(ALL)
+    from paper_2602_21597_b200._native import NgdbError
+    with pytest.raises(NgdbError) as e:  # n_neg differs from the context's
+        eng.train(small_graph, w, 2, batch=b, n_neg=k + 1)
+    assert e.value.kind == "ShapeMismatch"
+    # a failed run leaves the context usable
+    sums = eng.train(small_graph, w, 2, batch=b, n_neg=k)
+    assert np.all(np.isfinite(sums))
