@@ -481,7 +481,7 @@ def main():
     step_no += args.steps
     b1, d1 = C.c_int64(), C.c_int64()
     check(lib.ngdb_transfer_bytes(ctx, C.byref(b1), C.byref(d1)))
-    plan_wait = eng.last_plan_wait_s
+    tim = eng.last_timings
     if dist is not None:
         import torch
         t = torch.tensor([e2e_s], dtype=torch.float64)
@@ -536,7 +536,7 @@ def main():
                     "api": "ngdb_train_run (sampling + planning on host producer threads, "
                            "plan H2D, kernels, loss D2H per step)",
                     "producers": producers,
-                    "consumer_wait_ms_per_step": 1000 * plan_wait / args.steps,
+                    "consumer_ms_per_step": {k[:-2]: 1000 * v / args.steps for k, v in tim.items()},
                     "sequential_train_step": seq_qps},
             "gpu_launches": int(launches),
             "clocks": clk,

@@ -119,7 +119,7 @@ int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t 
  * it and reads step i's losses back while step i+1 runs. Same batches, plans
  * and update order as sampling + ngdb_train_step in a loop. Adam steps are
  * first_step+1 .. first_step+n_steps. loss_per_step [n_steps] (may be NULL),
- * per_query_loss [n_steps][batch] (may be NULL). */
+ * per_query_loss [n_steps][batch] (may be NULL). timings: see below. */
 typedef struct ngdb_train_opts {
   const double* pattern_weights; /* 14, enum order (query.hpp:14-29) */
   int32_t batch;                 /* queries per step (512) */
@@ -132,7 +132,10 @@ typedef struct ngdb_train_opts {
 } ngdb_train_opts;
 int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
                    int64_t first_step, int32_t n_steps, double* loss_per_step,
-                   float* per_query_loss, double* plan_wait_s);
+                   float* per_query_loss, double* timings);
+/* timings (may be NULL) receives 3 doubles: seconds the calling thread spent
+ * waiting for planned batches, submitting (upload + launches), and waiting for
+ * step results. */
 
 /* Streaming run of an already built step (H2D of its plan inside the call). */
 int ngdb_run_step(ngdb_ctx* ctx, const ngdb_step* s, int64_t step, float* per_query_loss,

@@ -33,7 +33,9 @@ struct TrainLoopConfig {
 };
 
 struct TrainLoopStats {
-  double plan_wait_s = 0.0;  // consumer time spent waiting for a planned batch
+  double plan_wait_s = 0.0;     // consumer waiting for a planned batch
+  double submit_s = 0.0;        // consumer uploading + launching steps
+  double collect_wait_s = 0.0;  // consumer waiting for a step's losses
   int32_t producers = 0;
 };
 

@@ -58,50 +58,76 @@ __device__ __forceinline__ float cand_grad(float v, float qc, float qo, float co
   return delta != 0.f ? s : 0.f;
 }
 
-// One warp per touched row; lane walks float4 chunks c = lane, lane+32, ...
-// (measured faster than keeping a whole row's theta/m/v in flight per lane:
-// the low register count keeps ~48 warps per SM resident).
-template <int BB>
+// One warp per touched row; lane owns float4 chunks c = lane + 32*i. The row's
+// theta, m and v loads are all issued before the contribution walk (they do
+// not depend on g), so a row costs one HBM round trip plus the L2-resident
+// contribution reads, with 12 independent 16-byte loads in flight per lane.
+template <int BB, int NCH>
 __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, SparseTable t,
                                                                   AdamHyper hp, const float* bc) {
   pdl_start();
   const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row_idx >= t.n_rows) return;
-  const AdamK k = adam_consts(hp, bc);
   const int64_t row = t.rows[row_idx];
   const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
   const int w4 = t.width / 4;
   float* wp = t.w + row * t.width;
   float* mp = t.m + row * t.width;
   float* vp = t.v + row * t.width;
-  for (int c = lane; c < w4; c += 32) {
-    const float4 w = ld4(wp + 4 * c);
-    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int kk = beg; kk < end; ++kk) {
-      const int32_t code = __ldg(t.contrib + kk);
-      if (code < 0) {
-        const float4 r = ld4(a.agbuf + static_cast<int64_t>(-code - 1) * t.width + 4 * c);
-        g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
-      } else {
-        const int s = code / a.ncand;
-        const float coef = __ldg(a.coefbuf + code);
-        const float* q = a.qbuf + static_cast<int64_t>(s) * a.wq;
-        const float4 qc = ld4(q + 4 * c);
-        float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (BB == NGDB_Q2B) qo = ld4(q + a.dim + 4 * c);
-        g.x += cand_grad<BB>(w.x, qc.x, qo.x, coef, a.alpha_box);
-        g.y += cand_grad<BB>(w.y, qc.y, qo.y, coef, a.alpha_box);
-        g.z += cand_grad<BB>(w.z, qc.z, qo.z, coef, a.alpha_box);
-        g.w += cand_grad<BB>(w.w, qc.w, qo.w, coef, a.alpha_box);
+  float4 w[NCH], m[NCH], v[NCH], g[NCH];
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < w4) {
+      w[i] = ld4(wp + 4 * c);
+      m[i] = ld4(mp + 4 * c);
+      v[i] = ld4(vp + 4 * c);
+    }
+    g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int kk = beg; kk < end; ++kk) {
+    const int32_t code = __ldg(t.contrib + kk);
+    if (code < 0) {
+      const float* r = a.agbuf + static_cast<int64_t>(-code - 1) * t.width;
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int c = lane + 32 * i;
+        if (c < w4) {
+          const float4 x = ld4(r + 4 * c);
+          g[i].x += x.x; g[i].y += x.y; g[i].z += x.z; g[i].w += x.w;
+        }
+      }
+    } else {
+      const int s = code / a.ncand;
+      const float coef = __ldg(a.coefbuf + code);
+      const float* q = a.qbuf + static_cast<int64_t>(s) * a.wq;
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int c = lane + 32 * i;
+        if (c < w4) {
+          const float4 qc = ld4(q + 4 * c);
+          float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (BB == NGDB_Q2B) qo = ld4(q + a.dim + 4 * c);
+          g[i].x += cand_grad<BB>(w[i].x, qc.x, qo.x, coef, a.alpha_box);
+          g[i].y += cand_grad<BB>(w[i].y, qc.y, qo.y, coef, a.alpha_box);
+          g[i].z += cand_grad<BB>(w[i].z, qc.z, qo.z, coef, a.alpha_box);
+          g[i].w += cand_grad<BB>(w[i].w, qc.w, qo.w, coef, a.alpha_box);
+        }
       }
     }
-    if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g);
-    float4 m = ld4(mp + 4 * c), v = ld4(vp + 4 * c);
-    const float4 nw = adam4(w, m, v, g, k);
-    st4(wp + 4 * c, nw);
-    st4(mp + 4 * c, m);
-    st4(vp + 4 * c, v);
+  }
+  const AdamK k = adam_consts(hp, bc);
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < w4) {
+      if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g[i]);
+      const float4 nw = adam4(w[i], m[i], v[i], g[i], k);
+      st4(wp + 4 * c, nw);
+      st4(mp + 4 * c, m[i]);
+      st4(vp + 4 * c, v[i]);
+    }
   }
 }
 
@@ -154,10 +180,16 @@ int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const Adam
   if (t.n_rows <= 0) return 0;
   if (a.backbone == NGDB_BETAE) return launch_beta_entity_adam(a, t, hp, bc, lc);
   const int blocks = (t.n_rows + kWarps - 1) / kWarps;
-  if (a.backbone == NGDB_GQE)
-    launch_pdl(entity_adam_kernel<NGDB_GQE>, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
-  else
-    launch_pdl(entity_adam_kernel<NGDB_Q2B>, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
+  auto go = [&](auto kernel) {
+    launch_pdl(kernel, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
+  };
+  if (t.width <= 512) {
+    if (a.backbone == NGDB_GQE) go(entity_adam_kernel<NGDB_GQE, 4>);
+    else go(entity_adam_kernel<NGDB_Q2B, 4>);
+  } else {
+    if (a.backbone == NGDB_GQE) go(entity_adam_kernel<NGDB_GQE, 8>);
+    else go(entity_adam_kernel<NGDB_Q2B, 8>);
+  }
   return 1;
 }
 

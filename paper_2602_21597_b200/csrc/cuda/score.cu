@@ -1,12 +1,16 @@
 // Fused negative-sample scoring + loss (SPEC.md:541-549 compute_loss, Eq. 6
 // PAPER.md:259-263) and the union-branch Score operator.
 //
-// One CTA per scoring node, 4 warps. Each warp owns candidates j = 4*warp + 16*t
-// (+0..3): it issues the 128-bit loads of FOUR candidate rows at once (16 loads in
-// flight per lane), reduces the four distances with shuffles, and — because the
-// loss is a sum of per-candidate terms, so dL/dd_j depends on d_j alone — folds
-// coef_j * dd_j/dq into per-lane registers in the same pass. Every candidate row
-// is read exactly once. Candidate-row gradients are NOT materialised: the
+// A cluster of S CTAs per scoring node, each taking a contiguous range of its
+// candidates. Candidate rows are staged in shared memory by the bulk-copy (TMA
+// 1-D) engine: a producer warp keeps a ring of kRing rows in flight
+// (cp.async.bulk + mbarrier complete_tx), four consumer warps take rows
+// round-robin, read them with 128-bit shared loads, reduce the distance with
+// shuffles and — because the loss is a sum of per-candidate terms, so dL/dd_j
+// depends on d_j alone — fold coef_j * dd_j/dq into per-lane registers in the
+// same pass. Loads never wait on math: the ring decouples HBM latency from the
+// per-row work. Every candidate row is read exactly once. Candidate-row
+// gradients are NOT materialised: the
 // optimizer recomputes coef_j * dd_j/dv from (q, coef) while it updates each
 // touched row.
 //
@@ -26,9 +30,37 @@
 namespace ngdb_dev {
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kCWarps = 4;                // consumer warps
+constexpr int kThreads = 32 * (kCWarps + 1);  // + one producer warp
 constexpr int kWarps = kThreads / 32;
-constexpr int kRows = 4;          // candidate rows in flight per warp
+constexpr int kRing = 16;                 // candidate rows staged per CTA
+
+// Shared-memory ring of candidate rows: kRing slots of ent_w floats + barriers.
+struct Ring {
+  float* rows;
+  uint64_t* full;
+  uint64_t* empty;
+  int width;  // floats per row
+};
+inline size_t ring_bytes(int width) {
+  return static_cast<size_t>(kRing) * width * sizeof(float) + 2 * kRing * sizeof(uint64_t);
+}
+__device__ __forceinline__ Ring make_ring(float* smem, int width) {
+  Ring r;
+  r.rows = smem;
+  r.full = reinterpret_cast<uint64_t*>(smem + kRing * width);
+  r.empty = r.full + kRing;
+  r.width = width;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&r.full[i], 1);
+      mbar_init(&r.empty[i], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  return r;
+}
 
 __device__ __forceinline__ float4 f4(float x) { return make_float4(x, x, x, x); }
 
@@ -66,83 +98,86 @@ struct Cands {
   float qbias;
 };
 
-// Walk all candidates of the node with one warp per 4-row group. For every
+// Walk candidates [j_beg, j_end) of the node: the producer warp streams their
+// rows into the ring, consumer warp w takes local rows w, w+4, ... For every
 // candidate: d_j -> coef_of(j, d_j) returns coef_j -> dq accumulation.
 template <int BB, int kMaxChunks, bool kGrad, class CoefOp>
 __device__ __forceinline__ void sweep(const DevArgs& a, const Cands& cs, Lane<BB, kMaxChunks>& L,
-                                      CoefOp&& coef_of, int part_idx = 0, int n_parts = 1) {
+                                      const Ring& ring, CoefOp&& coef_of, int part_idx = 0,
+                                      int n_parts = 1) {
   constexpr bool kBeta = BB == NGDB_BETAE;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int d4 = a.dim / 4;
-  // candidate groups are dealt round-robin over (part, warp)
-  for (int j0 = (part_idx * kWarps + warp) * kRows; j0 < a.ncand;
-       j0 += n_parts * kWarps * kRows) {
-    float4 v[kRows][kMaxChunks];
-    float4 v2[kBeta ? kRows : 1][kBeta ? kMaxChunks : 1];
-    float part[kRows];
+  const int j_beg = part_idx * a.ncand / n_parts, j_end = (part_idx + 1) * a.ncand / n_parts;
+  const int n_mine = j_end - j_beg;
+  if (warp == kCWarps) {  // producer
+    if (lane == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(ring.width * sizeof(float));
+      for (int t = 0; t < n_mine; ++t) {
+        const int slot = t % kRing, round = t / kRing;
+        if (round > 0) mbar_wait_parity(&ring.empty[slot], (round - 1) & 1);
+        const float* src = cs.base + static_cast<int64_t>(__ldg(cs.idx + j_beg + t)) * a.ent_w;
+        mbar_arrive_expect_tx(&ring.full[slot], bytes);
+        bulk_g2s(ring.rows + slot * ring.width, src, bytes, &ring.full[slot]);
+      }
+    }
+    return;
+  }
+  for (int t = warp; t < n_mine; t += kCWarps) {
+    const int slot = t % kRing, round = t / kRing, j = j_beg + t;
+    const float* row = ring.rows + slot * ring.width;
+    mbar_wait_parity(&ring.full[slot], round & 1);
+    float4 v[kMaxChunks];
+    float4 v2[kBeta ? kMaxChunks : 1];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const int j = min(j0 + r, a.ncand - 1);
-      const float* row = cs.base + static_cast<int64_t>(__ldg(cs.idx + j)) * a.ent_w;
+    for (int i = 0; i < kMaxChunks; ++i) {
+      const int c = lane + 32 * i;
+      if (i < L.nch && c < d4) {
+        v[i] = ld4(row + 4 * c);
+        if constexpr (kBeta) v2[i] = ld4(row + a.dim + 4 * c);
+      } else {
+        v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (kBeta) v2[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring.empty[slot]);  // row is in registers: slot free
+    float s = 0.f;
 #pragma unroll
-      for (int i = 0; i < kMaxChunks; ++i) {
-        const int c = lane + 32 * i;
-        if (i < L.nch && c < d4) {
-          v[r][i] = ldg4(row + 4 * c);
-          if constexpr (kBeta) v2[r][i] = ldg4(row + a.dim + 4 * c);
+    for (int i = 0; i < kMaxChunks; ++i) {
+      const int c = lane + 32 * i;
+      if (i < L.nch && c < d4) {
+        if constexpr (kBeta) {
+          s += Dist<BB>::term(v[i].x, v2[i].x, L.qc[i].x, L.qo[i].x);
+          s += Dist<BB>::term(v[i].y, v2[i].y, L.qc[i].y, L.qo[i].y);
+          s += Dist<BB>::term(v[i].z, v2[i].z, L.qc[i].z, L.qo[i].z);
+          s += Dist<BB>::term(v[i].w, v2[i].w, L.qc[i].w, L.qo[i].w);
         } else {
-          v[r][i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if constexpr (kBeta) v2[r][i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          s += Dist<BB>::term(v[i].x, L.qc[i].x, L.qo[i].x, a.alpha_box);
+          s += Dist<BB>::term(v[i].y, L.qc[i].y, L.qo[i].y, a.alpha_box);
+          s += Dist<BB>::term(v[i].z, L.qc[i].z, L.qo[i].z, a.alpha_box);
+          s += Dist<BB>::term(v[i].w, L.qc[i].w, L.qo[i].w, a.alpha_box);
         }
       }
     }
+    float dj = warp_sum(s);
+    if constexpr (kBeta) dj += cs.qbias + __ldg(cs.cbias + __ldg(cs.idx + j));
+    const float coef = coef_of(j, dj);
+    if (!kGrad) continue;
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      float s = 0.f;
-#pragma unroll
-      for (int i = 0; i < kMaxChunks; ++i) {
-        const int c = lane + 32 * i;
-        if (i < L.nch && c < d4) {
-          if constexpr (kBeta) {
-            s += Dist<BB>::term(v[r][i].x, v2[r][i].x, L.qc[i].x, L.qo[i].x);
-            s += Dist<BB>::term(v[r][i].y, v2[r][i].y, L.qc[i].y, L.qo[i].y);
-            s += Dist<BB>::term(v[r][i].z, v2[r][i].z, L.qc[i].z, L.qo[i].z);
-            s += Dist<BB>::term(v[r][i].w, v2[r][i].w, L.qc[i].w, L.qo[i].w);
-          } else {
-            s += Dist<BB>::term(v[r][i].x, L.qc[i].x, L.qo[i].x, a.alpha_box);
-            s += Dist<BB>::term(v[r][i].y, L.qc[i].y, L.qo[i].y, a.alpha_box);
-            s += Dist<BB>::term(v[r][i].z, L.qc[i].z, L.qo[i].z, a.alpha_box);
-            s += Dist<BB>::term(v[r][i].w, L.qc[i].w, L.qo[i].w, a.alpha_box);
-          }
-        }
-      }
-      part[r] = warp_sum(s);
-      if constexpr (kBeta) {
-        const int j = min(j0 + r, a.ncand - 1);
-        part[r] += cs.qbias + __ldg(cs.cbias + __ldg(cs.idx + j));
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const int j = j0 + r;
-      if (j >= a.ncand) break;
-      const float coef = coef_of(j, part[r]);
-      if (!kGrad) continue;
-#pragma unroll
-      for (int i = 0; i < kMaxChunks; ++i) {
-        const int c = lane + 32 * i;
-        if (i < L.nch && c < d4) {
-          if constexpr (kBeta) {
-            L.gc[i].x += coef * v[r][i].x; L.go[i].x += coef * v2[r][i].x;
-            L.gc[i].y += coef * v[r][i].y; L.go[i].y += coef * v2[r][i].y;
-            L.gc[i].z += coef * v[r][i].z; L.go[i].z += coef * v2[r][i].z;
-            L.gc[i].w += coef * v[r][i].w; L.go[i].w += coef * v2[r][i].w;
-          } else {
-            Dist<BB>::grad(v[r][i].x, L.qc[i].x, L.qo[i].x, coef, a.alpha_box, L.gc[i].x, L.go[i].x);
-            Dist<BB>::grad(v[r][i].y, L.qc[i].y, L.qo[i].y, coef, a.alpha_box, L.gc[i].y, L.go[i].y);
-            Dist<BB>::grad(v[r][i].z, L.qc[i].z, L.qo[i].z, coef, a.alpha_box, L.gc[i].z, L.go[i].z);
-            Dist<BB>::grad(v[r][i].w, L.qc[i].w, L.qo[i].w, coef, a.alpha_box, L.gc[i].w, L.go[i].w);
-          }
+    for (int i = 0; i < kMaxChunks; ++i) {
+      const int c = lane + 32 * i;
+      if (i < L.nch && c < d4) {
+        if constexpr (kBeta) {
+          L.gc[i].x += coef * v[i].x; L.go[i].x += coef * v2[i].x;
+          L.gc[i].y += coef * v[i].y; L.go[i].y += coef * v2[i].y;
+          L.gc[i].z += coef * v[i].z; L.go[i].z += coef * v2[i].z;
+          L.gc[i].w += coef * v[i].w; L.go[i].w += coef * v2[i].w;
+        } else {
+          Dist<BB>::grad(v[i].x, L.qc[i].x, L.qo[i].x, coef, a.alpha_box, L.gc[i].x, L.go[i].x);
+          Dist<BB>::grad(v[i].y, L.qc[i].y, L.qo[i].y, coef, a.alpha_box, L.gc[i].y, L.go[i].y);
+          Dist<BB>::grad(v[i].z, L.qc[i].z, L.qo[i].z, coef, a.alpha_box, L.gc[i].z, L.go[i].z);
+          Dist<BB>::grad(v[i].w, L.qc[i].w, L.qo[i].w, coef, a.alpha_box, L.gc[i].w, L.go[i].w);
         }
       }
     }
@@ -154,7 +189,7 @@ template <int BB, int kMaxChunks>
 __device__ void reduce_dq(const DevArgs& a, Lane<BB, kMaxChunks>& L, float* red, float* dst) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int d4 = a.dim / 4;
-  for (int w = 0; w < kWarps; ++w) {
+  for (int w = 0; w < kCWarps; ++w) {
     if (warp == w) {
 #pragma unroll
       for (int i = 0; i < kMaxChunks; ++i) {
@@ -239,9 +274,11 @@ __device__ __forceinline__ float beta_qterm(const DevArgs& a, const float* q, in
 // partials in rank order (deterministic); CTA 0 sums the loss partials.
 template <int BB, int NCH>
 __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first, int S) {
-  pdl_start();
+  extern __shared__ __align__(128) float ring_smem[];
   __shared__ __align__(16) float red[2 * 1024];
   __shared__ float lred[kWarps + 2];
+  const Ring ring = make_ring(ring_smem, a.ent_w);
+  pdl_start();
   const int part = blockIdx.x % S;
   const ngdb_node_desc d = a.nodes[first + blockIdx.x / S];
   const int qi = d.id;
@@ -276,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
   float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
   const int lane = threadIdx.x & 31;
   sweep<BB, NCH, true>(
-      a, cs, L,
+      a, cs, L, ring,
       [&](int j, float dj) {
         const float c = loss_coef(a, j, dj, loss);
         csum += c;
@@ -315,66 +352,99 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
   cluster_sync_all();  // partial tiles stay resident until every slice was read
 }
 
-// Union branch Score: fwd writes the distance vector; bwd turns the routed
-// dL/dd into coef (for the optimizer) and dL/dq (its G slot).
+// Union branch Score, a (S,1,1) cluster per node like the Loss kernel: fwd
+// writes the distance vector; bwd turns the routed dL/dd into coef (for the
+// optimizer) and dL/dq (its G slot), the S partials of dL/dq reduce-scattered
+// over DSMEM in rank order.
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int first) {
-  pdl_start();
+__global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int first, int S) {
+  extern __shared__ __align__(128) float ring_smem[];
   __shared__ __align__(16) float red[2 * 1024];
   __shared__ float lred[kWarps + 1];
-  const ngdb_node_desc d = a.nodes[first + blockIdx.x];
+  const Ring ring = make_ring(ring_smem, a.ent_w);
+  pdl_start();
+  const int part = blockIdx.x % S;
+  const ngdb_node_desc d = a.nodes[first + blockIdx.x / S];
   const float* q = a.arena + d.in[0];
   const int lane = threadIdx.x & 31;
   Lane<BB, NCH> L;
   L.load_q(q, a.dim, lane);
   const Cands cs = node_cands<BB>(a, d, q, lred);
   if (dir == 0) {
-    float* qcopy = a.qbuf + static_cast<int64_t>(d.aux) * a.wq;
-    for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(qcopy + e, ld4(q + e));
+    if (part == 0) {
+      float* qcopy = a.qbuf + static_cast<int64_t>(d.aux) * a.wq;
+      for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(qcopy + e, ld4(q + e));
+    }
     float* out = a.arena + d.out;
-    sweep<BB, NCH, false>(a, cs, L, [&](int j, float dj) {
-      if (lane == 0) out[j] = dj;
-      return 0.f;
-    });
+    sweep<BB, NCH, false>(
+        a, cs, L, ring,
+        [&](int j, float dj) {
+          if (lane == 0) out[j] = dj;
+          return 0.f;
+        },
+        part, S);
     return;
   }
   const float* g = a.arena + d.grad;
-  float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
-  for (int j = threadIdx.x; j < a.ncand; j += kThreads) coefs[j] = g[j];
-  sweep<BB, NCH, true>(a, cs, L, [&](int j, float) { return g[j]; });
+  if (part == 0) {
+    float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
+    for (int j = threadIdx.x; j < a.ncand; j += kThreads) coefs[j] = g[j];
+  }
+  sweep<BB, NCH, true>(a, cs, L, ring, [&](int j, float) { return g[j]; }, part, S);
+  float sc = 0.f;
   if constexpr (BB == NGDB_BETAE) {
-    reduce_dq<BB, NCH>(a, L, red, nullptr);
     float t = 0.f;
     for (int j = threadIdx.x; j < a.ncand; j += kThreads) t += g[j];
     t = block_sum(warp_sum(t), lred);
     if (threadIdx.x == 0) lred[kWarps] = t;
-    __syncthreads();
-    const float sc = lred[kWarps];
-    float* dst = a.arena + d.out;
-    for (int e = threadIdx.x; e < a.wq; e += kThreads) dst[e] = red[e] + sc * beta_qterm(a, q, e);
-  } else {
-    reduce_dq<BB, NCH>(a, L, red, a.arena + d.out);
   }
+  reduce_dq<BB, NCH>(a, L, red, nullptr);  // ends with __syncthreads
+  if constexpr (BB == NGDB_BETAE) sc = lred[kWarps];
+  cluster_sync_all();
+  float* dst = a.arena + d.out;
+  const int e0 = part * a.wq / S, e1 = (part + 1) * a.wq / S;
+  for (int e = e0 + threadIdx.x; e < e1; e += kThreads) {
+    float v = 0.f;
+    for (int p = 0; p < S; ++p) v += (p == part) ? red[e] : ld_peer(red + e, p);
+    if constexpr (BB == NGDB_BETAE) v += sc * beta_qterm(a, q, e);
+    dst[e] = v;
+  }
+  cluster_sync_all();  // partials stay resident until every slice was read
 }
 
 }  // namespace
 
+// cluster size: enough CTAs for ~4 per SM, 1..8 per node (portable limit)
+inline int parts_for(int n) { return std::max(1, std::min(8, (4 * 148 + n - 1) / std::max(n, 1))); }
+
+template <class K>
+void launch_ring_kernel(K kernel, int ent_w, int S, int n, cudaStream_t s, const DevArgs& a,
+                        int x, int first) {
+  const size_t smem = ring_bytes(ent_w);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_pdl(kernel, dim3(S * n), dim3(kThreads), smem, s, S, a, x, first, S);
+}
+
 template <int NCH>
 void launch_loss_nch(const DevArgs& a, int first, int n, cudaStream_t s) {
-  // cluster size: enough CTAs for ~4 per SM, 2..8 per node (portable limit)
-  const int S = std::max(2, std::min(8, (4 * 148 + n - 1) / std::max(n, 1)));
-  if (a.backbone == NGDB_GQE)
-    launch_pdl(loss_fwd_kernel<NGDB_GQE, NCH>, dim3(S * n), dim3(kThreads), 0, s, S, a, first, S);
-  else if (a.backbone == NGDB_BETAE)
-    launch_pdl(loss_fwd_kernel<NGDB_BETAE, NCH>, dim3(S * n), dim3(kThreads), 0, s, S, a, first, S);
-  else
-    launch_pdl(loss_fwd_kernel<NGDB_Q2B, NCH>, dim3(S * n), dim3(kThreads), 0, s, S, a, first, S);
+  const int S = std::max(2, parts_for(n));
+  auto go = [&](auto k) {
+    const size_t smem = ring_bytes(a.ent_w);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(k, dim3(S * n), dim3(kThreads), smem, s, S, a, first, S);
+  };
+  if (a.backbone == NGDB_GQE) go(loss_fwd_kernel<NGDB_GQE, NCH>);
+  else if (a.backbone == NGDB_BETAE) go(loss_fwd_kernel<NGDB_BETAE, NCH>);
+  else go(loss_fwd_kernel<NGDB_Q2B, NCH>);
 }
 template <int NCH>
 void launch_score_nch(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
-  if (a.backbone == NGDB_GQE) launch_pdl(score_kernel<NGDB_GQE, NCH>, dim3(n), dim3(kThreads), 0, s, 1, a, dir, first);
-  else if (a.backbone == NGDB_BETAE) launch_pdl(score_kernel<NGDB_BETAE, NCH>, dim3(n), dim3(kThreads), 0, s, 1, a, dir, first);
-  else launch_pdl(score_kernel<NGDB_Q2B, NCH>, dim3(n), dim3(kThreads), 0, s, 1, a, dir, first);
+  const int S = std::max(2, parts_for(n));
+  if (a.backbone == NGDB_GQE) launch_ring_kernel(score_kernel<NGDB_GQE, NCH>, a.ent_w, S, n, s, a, dir, first);
+  else if (a.backbone == NGDB_BETAE) launch_ring_kernel(score_kernel<NGDB_BETAE, NCH>, a.ent_w, S, n, s, a, dir, first);
+  else launch_ring_kernel(score_kernel<NGDB_Q2B, NCH>, a.ent_w, S, n, s, a, dir, first);
 }
 
 int launch_loss_fwd(const DevArgs& a, int first, int n, const LaunchCtx& lc) {

@@ -475,7 +475,7 @@ int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t 
 
 int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
                    int64_t first_step, int32_t n_steps, double* loss_per_step,
-                   float* per_query_loss, double* plan_wait_s) {
+                   float* per_query_loss, double* timings) {
   return guarded([&] {
     if (!ctx || !g || !o || !o->pattern_weights) throw ngdb::ConfigError("null argument");
     ngdb::TrainLoopConfig cfg;
@@ -489,7 +489,11 @@ int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
     cfg.first_tag = o->first_tag;
     const auto st = ngdb::run_train_loop(ctx, g->split, cfg, first_step, n_steps, loss_per_step,
                                          per_query_loss);
-    if (plan_wait_s) *plan_wait_s = st.plan_wait_s;
+    if (timings) {
+      timings[0] = st.plan_wait_s;
+      timings[1] = st.submit_s;
+      timings[2] = st.collect_wait_s;
+    }
   });
 }
 

@@ -14,6 +14,10 @@ namespace ngdb {
 
 namespace {
 
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 struct PlannedSlot {
   std::optional<StepPlanHost> plan;
   std::exception_ptr error;
@@ -100,7 +104,9 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
     double loss = 0.0;
     int32_t nonfinite = 0;
     float* out = per_query_loss ? per_query_loss + static_cast<int64_t>(i) * cfg.batch : nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     check_status(ngdb_step_wait(ctx, ticket, out, out ? cfg.batch : 0, &loss, &nonfinite));
+    stats.collect_wait_s += seconds_since(t0);
     if (nonfinite) throw NonFinite("non-finite loss at step " + std::to_string(first_step + i + 1));
     if (loss_per_step) loss_per_step[i] = loss;
   };
@@ -112,13 +118,14 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
         PlannedSlot& s = ring[i % depth];
         const auto t0 = std::chrono::steady_clock::now();
         cv_ready.wait(lk, [&] { return s.ready; });
-        stats.plan_wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        stats.plan_wait_s += seconds_since(t0);
         if (s.error) std::rethrow_exception(s.error);
         plan = std::move(*s.plan);
         s = PlannedSlot{};
         consumed = i + 1;
       }
       cv_space.notify_all();
+      const auto t_submit = std::chrono::steady_clock::now();
       const ngdb_step_plan view = plan.view();
       check_status(ngdb_step_begin(ctx, &view));  // packs into pinned staging + one H2D
       for (const auto& p : plan.pools) check_status(ngdb_exec_pool(ctx, &p));
@@ -126,6 +133,7 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
       int64_t ticket = -1;
       check_status(ngdb_step_end_async(ctx, &ticket));
       pending.emplace_back(i, ticket);
+      stats.submit_s += seconds_since(t_submit);
       // step i-1's losses, read back while step i runs on the device
       while (pending.size() > 1) collect();
     }
