@@ -180,7 +180,10 @@ int ngdb_set_debug(ngdb_ctx* ctx, int32_t keep_sparse_grads);
 
 /* Streaming step: packs the plan into pinned staging and issues one H2D copy. */
 int ngdb_step_begin(ngdb_ctx* ctx, const ngdb_step_plan* plan);
-/* Launch one kernel invocation of the current step (KernelRegistry fwd/bwd). */
+/* Launch one kernel invocation of the current step (KernelRegistry fwd/bwd).
+ * An Intersect class is held until the next call, so that the next class of
+ * the same PopBatch shares its launches; errors of a held class surface at the
+ * next exec_pool / optimizer_step / step_end call. */
 int ngdb_exec_pool(ngdb_ctx* ctx, const ngdb_pool_desc* pool);
 /* Sparse sorted-segment gradient reduce + touched-row Adam, then dense Adam
  * (SPEC.md:550-558 adam_step; Alg. 1 l.21 OptimizerStep). `step` is 1-based. */

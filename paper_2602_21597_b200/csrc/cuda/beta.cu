@@ -252,14 +252,15 @@ int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
 }
 
 // ---- Intersect ---------------------------------------------------------------
-__global__ void beta_inter_pack_kernel(DevArgs a, int k, int first, float* Q, Split Qs) {
+__global__ void beta_inter_pack_kernel(DevArgs a, KSpan ks, int first, float* Q, Split Qs) {
   pdl_start();
   const int i = blockIdx.x;
+  const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   const int W = 2 * a.dim;
   for (int l = 0; l < k; ++l)
     for (int e = threadIdx.x; e < W; e += blockDim.x)
-      put(Q, Qs, (static_cast<int64_t>(i) * k + l) * W + e, a.arena[d.in[l] + e]);
+      put(Q, Qs, (static_cast<int64_t>(r0) + l) * W + e, a.arena[d.in[l] + e]);
 }
 __device__ __forceinline__ void softmax3(const float* S, int64_t base, int k, int D, int e, float* w) {
   float mx = S[base + e];
@@ -272,17 +273,18 @@ __device__ __forceinline__ void softmax3(const float* S, int64_t base, int k, in
   const float inv = 1.f / z;
   for (int l = 0; l < k; ++l) w[l] *= inv;
 }
-__global__ void beta_inter_combine_kernel(DevArgs a, int k, int first, const float* S, const float* Q) {
+__global__ void beta_inter_combine_kernel(DevArgs a, KSpan ks, int first, const float* S, const float* Q) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim, W = 2 * D;
+  const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     float w[3];
-    softmax3(S, static_cast<int64_t>(i) * k * D, k, D, e, w);
+    softmax3(S, static_cast<int64_t>(r0) * D, k, D, e, w);
     float al = 0.f, be = 0.f;
     for (int l = 0; l < k; ++l) {
-      const float* q = Q + (static_cast<int64_t>(i) * k + l) * W;
+      const float* q = Q + (static_cast<int64_t>(r0) + l) * W;
       al += w[l] * q[e];
       be += w[l] * q[D + e];
     }
@@ -290,42 +292,44 @@ __global__ void beta_inter_combine_kernel(DevArgs a, int k, int first, const flo
     a.arena[d.out + D + e] = be;
   }
 }
-__global__ void beta_inter_combine_bwd_kernel(DevArgs a, int k, int first, const float* S,
+__global__ void beta_inter_combine_bwd_kernel(DevArgs a, KSpan ks, int first, const float* S,
                                               const float* Q, float* gS, Split gSs, float* dQ) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim, W = 2 * D;
+  const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     const float gA = a.arena[d.grad + e], gB = a.arena[d.grad + D + e];
     float w[3], gw[3], dot = 0.f;
-    softmax3(S, static_cast<int64_t>(i) * k * D, k, D, e, w);
+    softmax3(S, static_cast<int64_t>(r0) * D, k, D, e, w);
     for (int l = 0; l < k; ++l) {
-      const float* q = Q + (static_cast<int64_t>(i) * k + l) * W;
+      const float* q = Q + (static_cast<int64_t>(r0) + l) * W;
       gw[l] = gA * q[e] + gB * q[D + e];
       dot += w[l] * gw[l];
     }
     for (int l = 0; l < k; ++l) {
-      const int64_t r = static_cast<int64_t>(i) * k + l;
+      const int64_t r = static_cast<int64_t>(r0) + l;
       put(gS, gSs, r * D + e, w[l] * (gw[l] - dot));
       dQ[r * W + e] = gA * w[l];
       dQ[r * W + D + e] = gB * w[l];
     }
   }
 }
-__global__ void beta_inter_scatter_kernel(DevArgs a, int k, int first, const float* dQ) {
+__global__ void beta_inter_scatter_kernel(DevArgs a, KSpan ks, int first, const float* dQ) {
   pdl_start();
   const int i = blockIdx.x;
   const int W = 2 * a.dim;
+  const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
     for (int e = threadIdx.x; e < W; e += blockDim.x)
-      a.arena[d.out + l * W + e] = dQ[(static_cast<int64_t>(i) * k + l) * W + e];
+      a.arena[d.out + l * W + e] = dQ[(static_cast<int64_t>(r0) + l) * W + e];
 }
 
-int beta_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream_t s) {
+int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStream_t s) {
   const int D = a.dim, W = 2 * D;
-  const int R = n * k, RP = (R + 3) & ~3;
+  const int R = ks.row0(n), RP = (R + 3) & ~3;
   Scratch sc{a.scratch, a.scratch_cap};
   float* Q = sc.take((int64_t)R * W);
   Split Qs = take_split(sc, (int64_t)R * W);
@@ -334,7 +338,7 @@ int beta_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStrea
   float* S = sc.take((int64_t)R * D);
   const float* p = a.dense;
   int launches = 0;
-  launch_pdl(beta_inter_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, Q, Qs);
+  launch_pdl(beta_inter_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, Q, Qs);
   ++launches;
   TcGemmArgs z = gemm_args(R, W, W, op(Qs, W), wop(a, BETA_A1, W, W, false), Z, W);
   z.bias = p + a.dense_off[BETA_A1B];
@@ -344,7 +348,7 @@ int beta_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStrea
   sg.bias = p + a.dense_off[BETA_A2B];
   launches += tc_gemm(sg, s);
   if (dir == 0) {
-    launch_pdl(beta_inter_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, (const float*)S,
+    launch_pdl(beta_inter_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, (const float*)S,
                (const float*)Q);
     return launches + 1;
   }
@@ -357,7 +361,7 @@ int beta_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStrea
         gZT = take_split(sc, (int64_t)RP * W), QT = take_split(sc, (int64_t)RP * W);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
-  launch_pdl(beta_inter_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first,
+  launch_pdl(beta_inter_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first,
              (const float*)S, (const float*)Q, gS, gSs, dQ);
   ++launches;
   // gZ = (gS A2) * (Z > 0)
@@ -385,7 +389,7 @@ int beta_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStrea
   cj.job[1] = {gZ, R, W, g + off[BETA_A1B]};
   cj.n = 2;
   launches += colsums(cj, W, s);
-  launch_pdl(beta_inter_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, (const float*)dQ);
+  launch_pdl(beta_inter_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, (const float*)dQ);
   return launches + 1;
 }
 
@@ -418,9 +422,9 @@ int launch_beta_project(const DevArgs& a, int dir, int first, int n, const Launc
   return beta_project(a, dir, first, n, lc.stream);
 }
 
-int launch_beta_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc) {
+int launch_beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, const LaunchCtx& lc) {
   if (n <= 0) return 0;
-  return beta_intersect(a, dir, k, first, n, lc.stream);
+  return beta_intersect(a, dir, ks, first, n, lc.stream);
 }
 
 }  // namespace ngdb_dev

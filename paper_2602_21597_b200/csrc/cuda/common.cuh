@@ -206,6 +206,16 @@ struct LaunchCtx {
   cudaStream_t stream;
   int num_sms;
 };
+// Cardinality layout of an Intersect invocation: one class (k2 == k1), or the
+// two classes of one PopBatch run as one set of launches — nodes [0, n1) take
+// k1 inputs, the rest k2. Per-input rows are node-major: node i owns rows
+// [row0(i), row0(i) + k(i)).
+struct KSpan {
+  int n1, k1, k2;
+  __host__ __device__ int k(int i) const { return i < n1 ? k1 : k2; }
+  __host__ __device__ int row0(int i) const { return i < n1 ? i * k1 : n1 * k1 + (i - n1) * k2; }
+  static KSpan single(int n, int k) { return KSpan{n, k, k}; }
+};
 // rows.cu
 int launch_embed(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
 int launch_project(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
@@ -217,10 +227,10 @@ int launch_loss_fwd(const DevArgs& a, int first, int n, const LaunchCtx& lc);
 int launch_score(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
 // beta.cu (BetaE backbone)
 int launch_beta_project(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
-int launch_beta_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc);
+int launch_beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, const LaunchCtx& lc);
 int64_t beta_scratch_floats(int dim, int max_nodes);
 // intersect.cu
-int launch_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc);
+int launch_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, const LaunchCtx& lc);
 // scratch floats the intersect operators need for classes of up to max_nodes
 int64_t intersect_scratch_floats(int backbone, int dim, int max_nodes);
 // tc_gemm.cu: refresh the hi/lo (and transposed) splits of dense weight i

@@ -215,6 +215,10 @@ struct ngdb_ctx {
   int64_t stream_cap[2] = {0, 0};
   int cur = 0;
   ngdb_plan* active = nullptr;
+  // streaming ABI: an Intersect class held back one call so the next class of
+  // the same PopBatch can share its launches (exec_pools / mergeable)
+  ngdb_pool_desc held{};
+  bool has_held = false;
   // asynchronous step ends: a ring of pinned result slots (losses + flags)
   static constexpr int kResultSlots = 4;
   struct ResultSlot {
@@ -446,7 +450,10 @@ void timed(ngdb_ctx* c, int fam, double bytes, Launch&& launch) {
   c->recs.push_back({fam, a, b, bytes, n});
 }
 
-void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d) {
+// `merged` (optional): the next Intersect class of the same PopBatch, run in
+// the same set of launches (see mergeable()).
+void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d,
+               const ngdb_pool_desc* merged = nullptr) {
   if (d.count <= 0) return;
   const DevArgs a = make_args(c, p);
   const LaunchCtx lc{c->stream, c->num_sms};
@@ -469,20 +476,25 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d) {
     case NGDB_OP_NEGATE:
       timed(c, fam, bytes, [&] { return launch_negate(a, d.dir, d.first, d.count, lc); });
       break;
-    case NGDB_OP_INTERSECT:
+    case NGDB_OP_INTERSECT: {
       if (d.k < 2 || d.k > 3) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "intersect cardinality"};
+      const KSpan ks = merged ? KSpan{d.count, d.k, merged->k} : KSpan::single(d.count, d.k);
+      const int n_all = d.count + (merged ? merged->count : 0);
       if (c->profiling) {
-        // algorithmic fp32 GEMM flops of the class (2*M*N*K per contraction,
+        // algorithmic fp32 GEMM flops of the classes (2*M*N*K per contraction,
         // not counting the 3xTF32 split): DESIGN.md §4
-        const double n = d.count, R = double(d.count) * d.k, D2 = 2.0 * c->desc.dim * c->desc.dim;
+        const double n = n_all, R = ks.row0(n_all), D2 = 2.0 * c->desc.dim * c->desc.dim;
         double gemm_rows;
         if (c->desc.backbone == NGDB_GQE) gemm_rows = d.dir == 0 ? 2 * n : 5 * n;
         else if (c->beta()) gemm_rows = d.dir == 0 ? 6 * R : 18 * R;  // 2d->2d->d attention
         else gemm_rows = d.dir == 0 ? 3 * R + n : 9 * R + 3 * n;
         c->fam_flops[fam] += gemm_rows * D2;
       }
-      timed(c, fam, bytes, [&] { return launch_intersect(a, d.dir, d.k, d.first, d.count, lc); });
+      const double all_bytes =
+          merged && c->profiling ? bytes + pool_bytes(c, *merged, p->meta.n_candidates) : bytes;
+      timed(c, fam, all_bytes, [&] { return launch_intersect(a, d.dir, ks, d.first, n_all, lc); });
       break;
+    }
     case NGDB_OP_SCORE:
       timed(c, fam, bytes, [&] { return launch_score(a, d.dir, d.first, d.count, lc); });
       break;
@@ -501,6 +513,34 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d) {
                  "no kernel registered for operator kind " + std::to_string(d.kind)};
   }
   CK(cudaGetLastError());
+}
+
+// The cardinality classes of one Intersect PopBatch (consecutive invocations of
+// the same direction over contiguous node ranges, ascending k) are independent
+// of each other, so they share one set of launches: half the intersect
+// launches and larger GEMMs. The invocation list (the trace) is unchanged.
+bool mergeable(const ngdb_ctx* c, const ngdb_pool_desc& a, const ngdb_pool_desc& b) {
+  return a.kind == NGDB_OP_INTERSECT && b.kind == NGDB_OP_INTERSECT && a.dir == b.dir &&
+         a.count > 0 && b.count > 0 && b.first == a.first + a.count && a.k < b.k && b.k <= 3 &&
+         a.k >= 2 && a.count + b.count <= c->desc.max_batch;
+}
+
+void flush_held(ngdb_ctx* c) {
+  if (!c->has_held) return;
+  c->has_held = false;
+  exec_pool(c, c->active, c->held);
+}
+
+// Runs invocations in order, merging Intersect classes (mergeable()).
+void exec_pools(ngdb_ctx* c, const ngdb_plan* p, const std::vector<ngdb_pool_desc>& v) {
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (i + 1 < v.size() && mergeable(c, v[i], v[i + 1])) {
+      exec_pool(c, p, v[i], &v[i + 1]);
+      ++i;
+    } else {
+      exec_pool(c, p, v[i]);
+    }
+  }
 }
 
 void begin_step_device(ngdb_ctx* c) {
@@ -601,7 +641,7 @@ void prep_step(ngdb_ctx* c, const ngdb_plan* p) {
 void launch_step(ngdb_ctx* c, const ngdb_plan* p) {
   begin_step_device(c);
   prep_step(c, p);
-  for (const auto& d : p->meta.pools) exec_pool(c, p, d);
+  exec_pools(c, p, p->meta.pools);
   optimizer(c, p);
 }
 
@@ -908,6 +948,7 @@ int ngdb_set_debug(ngdb_ctx* c, int32_t keep) {
 
 int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
   return guarded([&] {
+    c->has_held = false;
     if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "context is row-sharded: use ngdb_shard_begin"};
     validate_plan(*plan);
     const int i = c->cur;
@@ -934,6 +975,19 @@ int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
 int ngdb_exec_pool(ngdb_ctx* c, const ngdb_pool_desc* pool) {
   return guarded([&] {
     if (!c->active) throw Fail{NGDB_ERR_CONFIG, "exec_pool outside a step"};
+    if (c->has_held) {
+      c->has_held = false;
+      if (mergeable(c, c->held, *pool)) {
+        exec_pool(c, c->active, c->held, pool);
+        return;
+      }
+      exec_pool(c, c->active, c->held);
+    }
+    if (pool->kind == NGDB_OP_INTERSECT && pool->count > 0) {
+      c->held = *pool;
+      c->has_held = true;
+      return;
+    }
     exec_pool(c, c->active, *pool);
   });
 }
@@ -941,6 +995,7 @@ int ngdb_exec_pool(ngdb_ctx* c, const ngdb_pool_desc* pool) {
 int ngdb_optimizer_step(ngdb_ctx* c, int64_t step) {
   return guarded([&] {
     if (!c->active) throw Fail{NGDB_ERR_CONFIG, "optimizer_step outside a step"};
+    flush_held(c);
     set_step_scalars(c, step);
     optimizer(c, c->active);
   });
@@ -950,6 +1005,7 @@ int ngdb_step_end(ngdb_ctx* c, float* per_query_loss, int32_t n_queries, double*
                   int32_t* nonfinite) {
   return guarded([&] {
     if (!c->active) throw Fail{NGDB_ERR_CONFIG, "step_end outside a step"};
+    flush_held(c);
     const int32_t nq = c->active->meta.n_queries;
     std::vector<float> tmp;
     float* dst = per_query_loss;
@@ -977,6 +1033,7 @@ int ngdb_step_end(ngdb_ctx* c, float* per_query_loss, int32_t n_queries, double*
 int ngdb_step_end_async(ngdb_ctx* c, int64_t* ticket) {
   return guarded([&] {
     if (!c->active) throw Fail{NGDB_ERR_CONFIG, "step_end outside a step"};
+    flush_held(c);
     if (c->profiling) throw Fail{NGDB_ERR_CONFIG, "step_end_async while profiling"};
     const int64_t t = c->next_ticket;
     auto& r = c->results[t % ngdb_ctx::kResultSlots];
@@ -1333,12 +1390,15 @@ int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
         timed(c, F_EMBED, double(b.n_anchor_send) * 4,
               [&] { return launch_shard_anchor_pack(a, sh.dev, b.anchor_send, lc); });
         break;
-      case NGDB_SHARD_FORWARD:
+      case NGDB_SHARD_FORWARD: {
+        std::vector<ngdb_pool_desc> v;
         for (const auto& d : p->meta.pools)
           if (d.dir == 0 && d.kind != NGDB_OP_SCORE && d.kind != NGDB_OP_UNION_SCORE &&
               d.kind != NGDB_OP_LOSS)
-            exec_pool(c, p, d);
+            v.push_back(d);
+        exec_pools(c, p, v);
         break;
+      }
       case NGDB_SHARD_QUERY_PACK:
         for (const auto& d : p->meta.pools)
           if (d.dir == 0 && (d.kind == NGDB_OP_SCORE || d.kind == NGDB_OP_LOSS))
@@ -1359,15 +1419,22 @@ int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
                                          b.loss_mine, p->meta.n_queries, lc);
         });
         break;
-      case NGDB_SHARD_BACKWARD:
-        for (const auto& d : p->meta.pools) {
+      case NGDB_SHARD_BACKWARD: {
+        const auto& pools = p->meta.pools;
+        for (size_t i = 0; i < pools.size(); ++i) {
+          const auto& d = pools[i];
           if (d.dir != 1 || d.kind == NGDB_OP_UNION_SCORE) continue;  // routing done by the owners
-          if (d.kind == NGDB_OP_SCORE)  // dL/dq of a union branch arrived in dqbuf
+          if (d.kind == NGDB_OP_SCORE) {  // dL/dq of a union branch arrived in dqbuf
             timed(c, F_SCORE, 0.0, [&] { return launch_loss_bwd(a, d.first, d.count, lc); });
-          else
+          } else if (i + 1 < pools.size() && mergeable(c, d, pools[i + 1])) {
+            exec_pool(c, p, d, &pools[i + 1]);
+            ++i;
+          } else {
             exec_pool(c, p, d);
+          }
         }
         break;
+      }
       case NGDB_SHARD_GRAD_PACK: {
         const Param& rel = c->params[c->rel_idx];
         SparseTable tr{rel.w, rel.m, rel.v, nullptr, static_cast<int32_t>(rel.cols),

@@ -52,10 +52,11 @@ namespace {
 // GQE
 
 // M[i] = mean_l x_l (plain + split); optionally G[i] = upstream grad (plain + split)
-__global__ void gqe_pack_kernel(DevArgs a, int k, int first, float* M, Split Ms, float* G,
+__global__ void gqe_pack_kernel(DevArgs a, KSpan ks, int first, float* M, Split Ms, float* G,
                                 Split Gs) {
   pdl_start();
   const int i = blockIdx.x;
+  const int k = ks.k(i);
   const ngdb_node_desc d = a.nodes[first + i];
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < a.dim; e += blockDim.x) {
@@ -67,9 +68,10 @@ __global__ void gqe_pack_kernel(DevArgs a, int k, int first, float* M, Split Ms,
   }
 }
 // G_X row l of node i = dM[i] / k  (mean adjoint)
-__global__ void gqe_scatter_kernel(DevArgs a, int k, int first, const float* dM) {
+__global__ void gqe_scatter_kernel(DevArgs a, KSpan ks, int first, const float* dM) {
   pdl_start();
   const int i = blockIdx.x;
+  const int k = ks.k(i);
   const ngdb_node_desc d = a.nodes[first + i];
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < a.dim; e += blockDim.x) {
@@ -78,7 +80,7 @@ __global__ void gqe_scatter_kernel(DevArgs a, int k, int first, const float* dM)
   }
 }
 
-int gqe_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream_t s) {
+int gqe_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStream_t s) {
   const int D = a.dim;
   const int64_t nd = (int64_t)n * D;
   const int nP = (n + 3) & ~3;  // transposed operands: rows padded for 16-B cp.async
@@ -92,7 +94,7 @@ int gqe_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   Split Gs = dir ? take_split(sc, nd) : Split{nullptr, nullptr};
   int launches = 0;
 
-  launch_pdl(gqe_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, M, Ms, G, Gs);
+  launch_pdl(gqe_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, M, Ms, G, Gs);
   ++launches;
   TcGemmArgs h = gemm_args(n, D, D, op(Ms, D), wop(a, GQE_W1, D, D, false), H, D);
   h.s_hi = RHs.hi; h.s_lo = RHs.lo; h.s_relu = 1;
@@ -130,33 +132,35 @@ int gqe_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   lvl[1].accumulate = 1;
   lvl[2] = gemm_args(n, D, D, op(dHs, D), wop(a, GQE_W1, D, D, true), dM, D);  // dM = dH W1
   launches += tc_gemm_batch(lvl, 3, s);
-  launch_pdl(gqe_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, dM);
+  launch_pdl(gqe_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, dM);
   return launches + 1;
 }
 
 // ---------------------------------------------------------------------------
 // Q2B
 
-__global__ void q2b_pack_kernel(DevArgs a, int k, int first, float* Cin, Split Cs, float* Oin,
+__global__ void q2b_pack_kernel(DevArgs a, KSpan ks, int first, float* Cin, Split Cs, float* Oin,
                                 Split Os) {
   pdl_start();
   const int i = blockIdx.x;
+  const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
     for (int e = threadIdx.x; e < a.dim; e += blockDim.x) {
-      const int64_t r = ((int64_t)i * k + l) * a.dim + e;
+      const int64_t r = ((int64_t)r0 + l) * a.dim + e;
       put(Cin, Cs, r, a.arena[d.in[l] + e]);
       put(Oin, Os, r, a.arena[d.in[l] + a.dim + e]);
     }
 }
 // Lm[i] = mean_l relu(P[i*k+l]) (plain + split)
-__global__ void q2b_mean_relu_kernel(const float* P, int k, int D, float* Lm, Split Lms) {
+__global__ void q2b_mean_relu_kernel(const float* P, KSpan ks, int D, float* Lm, Split Lms) {
   pdl_start();
   const int i = blockIdx.x;
+  const int k = ks.k(i), r0 = ks.row0(i);
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     float s = 0.f;
-    for (int l = 0; l < k; ++l) s += fmaxf(P[((int64_t)i * k + l) * D + e], 0.f);
+    for (int l = 0; l < k; ++l) s += fmaxf(P[((int64_t)r0 + l) * D + e], 0.f);
     put(Lm, Lms, (int64_t)i * D + e, s * inv_k);
   }
 }
@@ -172,13 +176,14 @@ __device__ __forceinline__ void softmax_k(const float* S, int64_t base, int k, i
   const float inv = 1.f / z;
   for (int l = 0; l < k; ++l) w[l] *= inv;
 }
-__global__ void q2b_combine_kernel(DevArgs a, int k, int first, const float* S, const float* U,
+__global__ void q2b_combine_kernel(DevArgs a, KSpan ks, int first, const float* S, const float* U,
                                    const float* Cin, const float* Oin) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim;
+  const int k = ks.k(i);
   const ngdb_node_desc d = a.nodes[first + i];
-  const int64_t base = (int64_t)i * k * D;
+  const int64_t base = (int64_t)ks.row0(i) * D;
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     float w[3];
     softmax_k(S, base, k, D, e, w);
@@ -191,14 +196,15 @@ __global__ void q2b_combine_kernel(DevArgs a, int k, int first, const float* S, 
     a.arena[d.out + D + e] = mn * sigmoidf(U[(int64_t)i * D + e]);
   }
 }
-__global__ void q2b_combine_bwd_kernel(DevArgs a, int k, int first, const float* S, const float* U,
+__global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, const float* S, const float* U,
                                        const float* Cin, const float* Oin, float* gS, Split gSs,
                                        float* dCin, float* dOin, float* gU, Split gUs) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim;
+  const int k = ks.k(i);
   const ngdb_node_desc d = a.nodes[first + i];
-  const int64_t base = (int64_t)i * k * D;
+  const int64_t base = (int64_t)ks.row0(i) * D;
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     const float gC = a.arena[d.grad + e];
     const float gO = a.arena[d.grad + D + e];
@@ -226,34 +232,36 @@ __global__ void q2b_combine_bwd_kernel(DevArgs a, int k, int first, const float*
   }
 }
 // gP[i*k+l] = gLm[i] / k * (P > 0)  (plain + split)
-__global__ void q2b_gp_kernel(const float* gLm, const float* P, int k, int D, float* gP,
+__global__ void q2b_gp_kernel(const float* gLm, const float* P, KSpan ks, int D, float* gP,
                               Split gPs) {
   pdl_start();
   const int i = blockIdx.x;
+  const int k = ks.k(i), r0 = ks.row0(i);
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < D; e += blockDim.x)
     for (int l = 0; l < k; ++l) {
-      const int64_t r = ((int64_t)i * k + l) * D + e;
+      const int64_t r = ((int64_t)r0 + l) * D + e;
       put(gP, gPs, r, P[r] > 0.f ? gLm[(int64_t)i * D + e] * inv_k : 0.f);
     }
 }
-__global__ void q2b_scatter_kernel(DevArgs a, int k, int first, const float* dCin,
+__global__ void q2b_scatter_kernel(DevArgs a, KSpan ks, int first, const float* dCin,
                                    const float* dOin) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim;
+  const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
     for (int e = threadIdx.x; e < D; e += blockDim.x) {
-      const int64_t r = ((int64_t)i * k + l) * D + e;
+      const int64_t r = ((int64_t)r0 + l) * D + e;
       a.arena[d.out + l * 2 * D + e] = dCin[r];
       a.arena[d.out + l * 2 * D + D + e] = dOin[r];
     }
 }
 
-int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream_t s) {
+int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStream_t s) {
   const int D = a.dim;
-  const int R = n * k;
+  const int R = ks.row0(n);
   const int64_t rd = (int64_t)R * D, nd = (int64_t)n * D;
   // transposed (weight-gradient) operands: rows padded for 16-byte cp.async
   const int nP = (n + 3) & ~3, RP = (R + 3) & ~3;
@@ -277,7 +285,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   const float* v2 = p + a.dense_off[Q2B_V2B];
   int launches = 0;
 
-  launch_pdl(q2b_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, Cin, Cs, Oin, Os);
+  launch_pdl(q2b_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, Cin, Cs, Oin, Os);
   ++launches;
   {  // level 1: Z = A1 c + a1 (chained split of relu(Z)), P = V1 o + v1
     TcGemmArgs lvl[2];
@@ -288,7 +296,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
     lvl[1].bias = v1;
     launches += tc_gemm_batch(lvl, 2, s);
   }
-  launch_pdl(q2b_mean_relu_kernel, dim3(n), dim3(128), 0, s, 1, P, k, D, Lm, Lms);
+  launch_pdl(q2b_mean_relu_kernel, dim3(n), dim3(128), 0, s, 1, P, ks, D, Lm, Lms);
   ++launches;
   {  // level 2: S = A2 relu(Z) + a2, U = V2 Lm + v2
     TcGemmArgs lvl[2];
@@ -299,7 +307,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
     launches += tc_gemm_batch(lvl, 2, s);
   }
   if (dir == 0) {
-    launch_pdl(q2b_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, S, U, Cin, Oin);
+    launch_pdl(q2b_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, S, U, Cin, Oin);
     return launches + 1;
   }
   float* gS = sc.take(rd);
@@ -319,7 +327,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
 
-  launch_pdl(q2b_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, S, U, Cin, Oin, gS, gSs, dCin, dOin, gU,
+  launch_pdl(q2b_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, S, U, Cin, Oin, gS, gSs, dCin, dOin, gU,
                                            gUs);
   ++launches;
   SplitJobs j1{};
@@ -341,7 +349,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
     lvl[3].s_hi = gZs.hi; lvl[3].s_lo = gZs.lo;
     launches += tc_gemm_batch(lvl, 4, s);
   }
-  launch_pdl(q2b_gp_kernel, dim3(n), dim3(128), 0, s, 1, gLm, P, k, D, gP, gPs);
+  launch_pdl(q2b_gp_kernel, dim3(n), dim3(128), 0, s, 1, gLm, P, ks, D, gP, gPs);
   ++launches;
   SplitJobs j2{};
   j2.job[0] = {gP, R, D, D, 0, gPT.hi, gPT.lo};
@@ -369,7 +377,7 @@ int q2b_intersect(const DevArgs& a, int dir, int k, int first, int n, cudaStream
   cj.job[3] = {gZ, R, D, g + off[Q2B_A1B]};
   cj.n = 4;
   launches += colsums(cj, D, s);
-  launch_pdl(q2b_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, k, first, dCin, dOin);
+  launch_pdl(q2b_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, dCin, dOin);
   return launches + 1;
 }
 
@@ -383,11 +391,11 @@ int64_t intersect_scratch_floats(int backbone, int dim, int max_nodes) {
   return 36 * rd + 14 * nd + 64 * (int64_t)dim + 256;
 }
 
-int launch_intersect(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc) {
+int launch_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, const LaunchCtx& lc) {
   if (n <= 0) return 0;
-  if (a.backbone == NGDB_GQE) return gqe_intersect(a, dir, k, first, n, lc.stream);
-  if (a.backbone == NGDB_BETAE) return launch_beta_intersect(a, dir, k, first, n, lc);
-  return q2b_intersect(a, dir, k, first, n, lc.stream);
+  if (a.backbone == NGDB_GQE) return gqe_intersect(a, dir, ks, first, n, lc.stream);
+  if (a.backbone == NGDB_BETAE) return launch_beta_intersect(a, dir, ks, first, n, lc);
+  return q2b_intersect(a, dir, ks, first, n, lc.stream);
 }
 
 }  // namespace ngdb_dev

@@ -86,33 +86,45 @@ __global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, Spa
     }
     g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  for (int kk = beg; kk < end; ++kk) {
-    const int32_t code = __ldg(t.contrib + kk);
-    if (code < 0) {
-      const float* r = a.agbuf + static_cast<int64_t>(-code - 1) * t.width;
+  // contribution codes and coefficients of up to 32 contributions at a time,
+  // one per lane, then broadcast: the q / anchor-row loads of a contribution
+  // do not wait on a dependent code load
+  for (int k0 = beg; k0 < end; k0 += 32) {
+    const int nk = min(32, end - k0);
+    int32_t my_code = 0;
+    float my_coef = 0.f;
+    if (lane < nk) {
+      my_code = __ldg(t.contrib + k0 + lane);
+      if (my_code >= 0) my_coef = __ldg(a.coefbuf + my_code);
+    }
+    for (int j = 0; j < nk; ++j) {
+      const int32_t code = __shfl_sync(0xffffffffu, my_code, j);
+      const float coef = __shfl_sync(0xffffffffu, my_coef, j);
+      if (code < 0) {
+        const float* r = a.agbuf + static_cast<int64_t>(-code - 1) * t.width;
 #pragma unroll
-      for (int i = 0; i < NCH; ++i) {
-        const int c = lane + 32 * i;
-        if (c < w4) {
-          const float4 x = ld4(r + 4 * c);
-          g[i].x += x.x; g[i].y += x.y; g[i].z += x.z; g[i].w += x.w;
+        for (int i = 0; i < NCH; ++i) {
+          const int c = lane + 32 * i;
+          if (c < w4) {
+            const float4 x = ld4(r + 4 * c);
+            g[i].x += x.x; g[i].y += x.y; g[i].z += x.z; g[i].w += x.w;
+          }
         }
-      }
-    } else {
-      const int s = code / a.ncand;
-      const float coef = __ldg(a.coefbuf + code);
-      const float* q = a.qbuf + static_cast<int64_t>(s) * a.wq;
+      } else {
+        const int s = code / a.ncand;
+        const float* q = a.qbuf + static_cast<int64_t>(s) * a.wq;
 #pragma unroll
-      for (int i = 0; i < NCH; ++i) {
-        const int c = lane + 32 * i;
-        if (c < w4) {
-          const float4 qc = ld4(q + 4 * c);
-          float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (BB == NGDB_Q2B) qo = ld4(q + a.dim + 4 * c);
-          g[i].x += cand_grad<BB>(w[i].x, qc.x, qo.x, coef, a.alpha_box);
-          g[i].y += cand_grad<BB>(w[i].y, qc.y, qo.y, coef, a.alpha_box);
-          g[i].z += cand_grad<BB>(w[i].z, qc.z, qo.z, coef, a.alpha_box);
-          g[i].w += cand_grad<BB>(w[i].w, qc.w, qo.w, coef, a.alpha_box);
+        for (int i = 0; i < NCH; ++i) {
+          const int c = lane + 32 * i;
+          if (c < w4) {
+            const float4 qc = ld4(q + 4 * c);
+            float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (BB == NGDB_Q2B) qo = ld4(q + a.dim + 4 * c);
+            g[i].x += cand_grad<BB>(w[i].x, qc.x, qo.x, coef, a.alpha_box);
+            g[i].y += cand_grad<BB>(w[i].y, qc.y, qo.y, coef, a.alpha_box);
+            g[i].z += cand_grad<BB>(w[i].z, qc.z, qo.z, coef, a.alpha_box);
+            g[i].w += cand_grad<BB>(w[i].w, qc.w, qo.w, coef, a.alpha_box);
+          }
         }
       }
     }
