@@ -184,37 +184,51 @@ __device__ __forceinline__ void sweep(const DevArgs& a, const Cands& cs, Lane<BB
   }
 }
 
-// Cross-warp sum of the per-lane dq accumulators into dst (wq floats).
+// Cross-warp sum of the per-lane dq accumulators: every consumer warp stores
+// its partial (and its loss / coefficient-sum partials) in its own shared row,
+// one barrier, then the block sums the kCWarps rows in warp order
+// (deterministic) into part[0]; lred[kWarps] / lred[kWarps + 1] receive the
+// loss and coefficient sums. Ends with a barrier.
+constexpr int kMaxWq = 1024;
 template <int BB, int kMaxChunks>
-__device__ void reduce_dq(const DevArgs& a, Lane<BB, kMaxChunks>& L, float* red, float* dst) {
+__device__ void reduce_partials(const DevArgs& a, const Lane<BB, kMaxChunks>& L, float (*part)[kMaxWq],
+                                float* lred, float loss, float csum) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int d4 = a.dim / 4;
-  for (int w = 0; w < kCWarps; ++w) {
-    if (warp == w) {
+  if (warp < kCWarps) {
 #pragma unroll
-      for (int i = 0; i < kMaxChunks; ++i) {
-        const int c = lane + 32 * i;
-        if (i < L.nch && c < d4) {
-          float4* rc = reinterpret_cast<float4*>(red + 4 * c);
-          float4* ro = reinterpret_cast<float4*>(red + a.dim + 4 * c);
-          if (w == 0) {
-            *rc = L.gc[i];
-            if (BB != NGDB_GQE) *ro = L.go[i];
-          } else {
-            float4 t = *rc;
-            *rc = make_float4(t.x + L.gc[i].x, t.y + L.gc[i].y, t.z + L.gc[i].z, t.w + L.gc[i].w);
-            if (BB != NGDB_GQE) {
-              t = *ro;
-              *ro = make_float4(t.x + L.go[i].x, t.y + L.go[i].y, t.z + L.go[i].z, t.w + L.go[i].w);
-            }
-          }
-        }
+    for (int i = 0; i < kMaxChunks; ++i) {
+      const int c = lane + 32 * i;
+      if (i < L.nch && c < d4) {
+        st4(part[warp] + 4 * c, L.gc[i]);
+        if (BB != NGDB_GQE) st4(part[warp] + a.dim + 4 * c, L.go[i]);
       }
     }
-    __syncthreads();
+    if (lane == 0) {
+      lred[2 * warp] = loss;
+      lred[2 * warp + 1] = csum;
+    }
   }
-  if (dst)
-    for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(dst + e, ld4(red + e));
+  __syncthreads();
+  for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) {
+    float4 t = ld4(part[0] + e);
+#pragma unroll
+    for (int w = 1; w < kCWarps; ++w) {
+      const float4 u = ld4(part[w] + e);
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    st4(part[0] + e, t);
+  }
+  if (threadIdx.x == 0) {
+    float l = 0.f, cs = 0.f;
+    for (int w = 0; w < kCWarps; ++w) {
+      l += lred[2 * w];
+      cs += lred[2 * w + 1];
+    }
+    lred[kWarps] = l;
+    lred[kWarps + 1] = cs;
+  }
+  __syncthreads();
 }
 
 __device__ float block_sum(float v, float* red) {
@@ -275,8 +289,9 @@ __device__ __forceinline__ float beta_qterm(const DevArgs& a, const float* q, in
 template <int BB, int NCH>
 __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first, int S) {
   extern __shared__ __align__(128) float ring_smem[];
-  __shared__ __align__(16) float red[2 * 1024];
-  __shared__ float lred[kWarps + 2];
+  __shared__ __align__(16) float parts[kCWarps][kMaxWq];
+  __shared__ float lred[2 * kCWarps + 2];
+  static_assert(kWarps + 1 < 2 * kCWarps + 2, "lred layout");
   const Ring ring = make_ring(ring_smem, a.ent_w);
   pdl_start();
   const int part = blockIdx.x % S;
@@ -321,13 +336,8 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
         return c;
       },
       part, S);
-  loss = block_sum(lane == 0 ? loss : 0.f, lred);
-  if (threadIdx.x == 0) lred[kWarps] = loss;
-  if constexpr (BB == NGDB_BETAE) {
-    csum = block_sum(lane == 0 ? csum : 0.f, lred);
-    if (threadIdx.x == 0) lred[kWarps + 1] = csum;
-  }
-  reduce_dq<BB, NCH>(a, L, red, nullptr);
+  reduce_partials<BB, NCH>(a, L, parts, lred, loss, csum);
+  const float* red = parts[0];
   cluster_sync_all();
   {
     float* dst = a.dqbuf + static_cast<int64_t>(d.aux) * a.wq;
@@ -359,8 +369,8 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
 template <int BB, int NCH>
 __global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int first, int S) {
   extern __shared__ __align__(128) float ring_smem[];
-  __shared__ __align__(16) float red[2 * 1024];
-  __shared__ float lred[kWarps + 1];
+  __shared__ __align__(16) float parts[kCWarps][kMaxWq];
+  __shared__ float lred[2 * kCWarps + 2];
   const Ring ring = make_ring(ring_smem, a.ent_w);
   pdl_start();
   const int part = blockIdx.x % S;
@@ -390,17 +400,20 @@ __global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int
     float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
     for (int j = threadIdx.x; j < a.ncand; j += kThreads) coefs[j] = g[j];
   }
-  sweep<BB, NCH, true>(a, cs, L, ring, [&](int j, float) { return g[j]; }, part, S);
-  float sc = 0.f;
-  if constexpr (BB == NGDB_BETAE) {
-    float t = 0.f;
-    for (int j = threadIdx.x; j < a.ncand; j += kThreads) t += g[j];
-    t = block_sum(warp_sum(t), lred);
-    if (threadIdx.x == 0) lred[kWarps] = t;
-  }
-  reduce_dq<BB, NCH>(a, L, red, nullptr);  // ends with __syncthreads
-  if constexpr (BB == NGDB_BETAE) sc = lred[kWarps];
+  float csum = 0.f;  // Σ_j g[j] over this CTA's candidates (BetaE query term)
+  sweep<BB, NCH, true>(
+      a, cs, L, ring,
+      [&](int j, float) {
+        csum += g[j];
+        return g[j];
+      },
+      part, S);
+  reduce_partials<BB, NCH>(a, L, parts, lred, 0.f, csum);
+  const float* red = parts[0];
   cluster_sync_all();
+  float sc = 0.f;
+  if constexpr (BB == NGDB_BETAE)  // over all S parts, in rank order
+    for (int p = 0; p < S; ++p) sc += (p == part) ? lred[kWarps + 1] : ld_peer(lred + kWarps + 1, p);
   float* dst = a.arena + d.out;
   const int e0 = part * a.wq / S, e1 = (part + 1) * a.wq / S;
   for (int e = e0 + threadIdx.x; e < e1; e += kThreads) {
