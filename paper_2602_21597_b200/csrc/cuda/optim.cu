@@ -58,88 +58,141 @@ __device__ __forceinline__ float cand_grad(float v, float qc, float qo, float co
   return delta != 0.f ? s : 0.f;
 }
 
-// One warp per touched row; lane owns float4 chunks c = lane + 32*i. The row's
-// theta, m and v loads are all issued before the contribution walk (they do
-// not depend on g), so a row costs one HBM round trip plus the L2-resident
-// contribution reads, with 12 independent 16-byte loads in flight per lane.
+// Touched-row entity Adam, TMA-staged: each CTA owns a contiguous range of
+// touched rows; a producer warp streams every row's theta, m and v (3 x w
+// bytes) into a shared-memory ring with bulk copies (cp.async.bulk +
+// mbarrier complete_tx), so kAdamRing rows per CTA are always in flight
+// regardless of what the consumers are doing. Consumer warps take rows
+// round-robin: the gradient is summed along the row's CSR contributions
+// (codes and coefficients fetched lane-parallel, then broadcast), Adam runs in
+// registers and theta, m, v are stored straight back to HBM.
+constexpr int kAdamConsumers = 8;
+constexpr int kAdamThreads = 32 * (kAdamConsumers + 1);
+constexpr int kAdamRing = 8;
+
+inline size_t adam_smem_bytes(int width) {
+  return static_cast<size_t>(kAdamRing) * 3 * width * sizeof(float) + 2 * kAdamRing * sizeof(uint64_t);
+}
+
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kWarps * 32) entity_adam_kernel(DevArgs a, SparseTable t,
-                                                                  AdamHyper hp, const float* bc) {
-  pdl_start();
-  const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (row_idx >= t.n_rows) return;
-  const int64_t row = t.rows[row_idx];
-  const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
-  const int w4 = t.width / 4;
-  float* wp = t.w + row * t.width;
-  float* mp = t.m + row * t.width;
-  float* vp = t.v + row * t.width;
-  float4 w[NCH], m[NCH], v[NCH], g[NCH];
-#pragma unroll
-  for (int i = 0; i < NCH; ++i) {
-    const int c = lane + 32 * i;
-    if (c < w4) {
-      w[i] = ld4(wp + 4 * c);
-      m[i] = ld4(mp + 4 * c);
-      v[i] = ld4(vp + 4 * c);
+__global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a, SparseTable t,
+                                                                   AdamHyper hp, const float* bc,
+                                                                   int rows_per_cta) {
+  extern __shared__ __align__(128) float smem[];
+  const int W = t.width;
+  float* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kAdamRing * 3 * W);
+  uint64_t* empty = full + kAdamRing;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kAdamRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
     }
-    g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    mbar_fence_init();
   }
-  // contribution codes and coefficients of up to 32 contributions at a time,
-  // one per lane, then broadcast: the q / anchor-row loads of a contribution
-  // do not wait on a dependent code load
-  for (int k0 = beg; k0 < end; k0 += 32) {
-    const int nk = min(32, end - k0);
+  __syncthreads();
+  pdl_start();
+  const int r_beg = blockIdx.x * rows_per_cta;
+  const int n_mine = max(0, min(t.n_rows, r_beg + rows_per_cta) - r_beg);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (warp == kAdamConsumers) {  // producer
+    if (lane == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(W * sizeof(float));
+      for (int u = 0; u < n_mine; ++u) {
+        const int slot = u % kAdamRing, round = u / kAdamRing;
+        if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
+        const int64_t row = __ldg(t.rows + r_beg + u);
+        float* dst = ring + slot * 3 * W;
+        mbar_arrive_expect_tx(&full[slot], 3 * bytes);
+        bulk_g2s(dst, t.w + row * W, bytes, &full[slot]);
+        bulk_g2s(dst + W, t.m + row * W, bytes, &full[slot]);
+        bulk_g2s(dst + 2 * W, t.v + row * W, bytes, &full[slot]);
+      }
+    }
+    return;
+  }
+  const int w4 = W / 4;
+  const AdamK k = adam_consts(hp, bc);
+  for (int u = warp; u < n_mine; u += kAdamConsumers) {
+    const int slot = u % kAdamRing, round = u / kAdamRing;
+    const int row_idx = r_beg + u;
+    const int64_t row = __ldg(t.rows + row_idx);
+    const int beg = __ldg(t.seg + row_idx), end = __ldg(t.seg + row_idx + 1);
+    // contribution codes / coefficients of the row's first 32 contributions
+    // are fetched before waiting for the row itself
     int32_t my_code = 0;
     float my_coef = 0.f;
-    if (lane < nk) {
-      my_code = __ldg(t.contrib + k0 + lane);
+    if (lane < end - beg) {
+      my_code = __ldg(t.contrib + beg + lane);
       if (my_code >= 0) my_coef = __ldg(a.coefbuf + my_code);
     }
-    for (int j = 0; j < nk; ++j) {
-      const int32_t code = __shfl_sync(0xffffffffu, my_code, j);
-      const float coef = __shfl_sync(0xffffffffu, my_coef, j);
-      if (code < 0) {
-        const float* r = a.agbuf + static_cast<int64_t>(-code - 1) * t.width;
+    const float* ws = ring + slot * 3 * W;
+    mbar_wait_parity(&full[slot], round & 1);
+    float4 w[NCH], g[NCH];
 #pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const int c = lane + 32 * i;
-          if (c < w4) {
-            const float4 x = ld4(r + 4 * c);
-            g[i].x += x.x; g[i].y += x.y; g[i].z += x.z; g[i].w += x.w;
-          }
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      if (c < w4) w[i] = ld4(ws + 4 * c);
+      g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int k0 = beg; k0 < end; k0 += 32) {
+      const int nk = min(32, end - k0);
+      if (k0 > beg) {
+        my_code = 0;
+        my_coef = 0.f;
+        if (lane < nk) {
+          my_code = __ldg(t.contrib + k0 + lane);
+          if (my_code >= 0) my_coef = __ldg(a.coefbuf + my_code);
         }
-      } else {
-        const int s = code / a.ncand;
-        const float* q = a.qbuf + static_cast<int64_t>(s) * a.wq;
+      }
+      for (int j = 0; j < nk; ++j) {
+        const int32_t code = __shfl_sync(0xffffffffu, my_code, j);
+        const float coef = __shfl_sync(0xffffffffu, my_coef, j);
+        if (code < 0) {
+          const float* r = a.agbuf + static_cast<int64_t>(-code - 1) * W;
 #pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const int c = lane + 32 * i;
-          if (c < w4) {
-            const float4 qc = ld4(q + 4 * c);
-            float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (BB == NGDB_Q2B) qo = ld4(q + a.dim + 4 * c);
-            g[i].x += cand_grad<BB>(w[i].x, qc.x, qo.x, coef, a.alpha_box);
-            g[i].y += cand_grad<BB>(w[i].y, qc.y, qo.y, coef, a.alpha_box);
-            g[i].z += cand_grad<BB>(w[i].z, qc.z, qo.z, coef, a.alpha_box);
-            g[i].w += cand_grad<BB>(w[i].w, qc.w, qo.w, coef, a.alpha_box);
+          for (int i = 0; i < NCH; ++i) {
+            const int c = lane + 32 * i;
+            if (c < w4) {
+              const float4 x = ld4(r + 4 * c);
+              g[i].x += x.x; g[i].y += x.y; g[i].z += x.z; g[i].w += x.w;
+            }
+          }
+        } else {
+          const float* q = a.qbuf + static_cast<int64_t>(code / a.ncand) * a.wq;
+#pragma unroll
+          for (int i = 0; i < NCH; ++i) {
+            const int c = lane + 32 * i;
+            if (c < w4) {
+              const float4 qc = ld4(q + 4 * c);
+              float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (BB == NGDB_Q2B) qo = ld4(q + a.dim + 4 * c);
+              g[i].x += cand_grad<BB>(w[i].x, qc.x, qo.x, coef, a.alpha_box);
+              g[i].y += cand_grad<BB>(w[i].y, qc.y, qo.y, coef, a.alpha_box);
+              g[i].z += cand_grad<BB>(w[i].z, qc.z, qo.z, coef, a.alpha_box);
+              g[i].w += cand_grad<BB>(w[i].w, qc.w, qo.w, coef, a.alpha_box);
+            }
           }
         }
       }
     }
-  }
-  const AdamK k = adam_consts(hp, bc);
+    float* wp = t.w + row * W;
+    float* mp = t.m + row * W;
+    float* vp = t.v + row * W;
 #pragma unroll
-  for (int i = 0; i < NCH; ++i) {
-    const int c = lane + 32 * i;
-    if (c < w4) {
-      if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g[i]);
-      const float4 nw = adam4(w[i], m[i], v[i], g[i], k);
-      st4(wp + 4 * c, nw);
-      st4(mp + 4 * c, m[i]);
-      st4(vp + 4 * c, v[i]);
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      if (c < w4) {
+        if (t.dbg_g) st4(t.dbg_g + row * W + 4 * c, g[i]);
+        float4 m = ld4(ws + W + 4 * c), v = ld4(ws + 2 * W + 4 * c);
+        const float4 nw = adam4(w[i], m, v, g[i], k);
+        st4(wp + 4 * c, nw);
+        st4(mp + 4 * c, m);
+        st4(vp + 4 * c, v);
+      }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);  // slot's smem fully read
   }
 }
 
@@ -191,9 +244,16 @@ int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const Adam
                               const float* bc, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
   if (a.backbone == NGDB_BETAE) return launch_beta_entity_adam(a, t, hp, bc, lc);
-  const int blocks = (t.n_rows + kWarps - 1) / kWarps;
+  const size_t smem = adam_smem_bytes(t.width);
+  // persistent-style grid: ~3 CTAs per SM, contiguous row ranges
+  const int ctas = std::max(1, std::min(t.n_rows, 3 * lc.num_sms));
+  const int rows_per_cta = (t.n_rows + ctas - 1) / ctas;
+  const int grid = (t.n_rows + rows_per_cta - 1) / rows_per_cta;
   auto go = [&](auto kernel) {
-    launch_pdl(kernel, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(kernel, dim3(grid), dim3(kAdamThreads), smem, lc.stream, 1, a, t, hp, bc,
+               rows_per_cta);
   };
   if (t.width <= 512) {
     if (a.backbone == NGDB_GQE) go(entity_adam_kernel<NGDB_GQE, 4>);
