@@ -22,6 +22,7 @@
 //                 over the per-step entity table of beta.cu;
 //                 dL/dq = sum_j coef_j etab[r_j] + (sum_j coef_j) [psi(A)-psi(A+B) | psi(B)-psi(A+B)]
 #include <algorithm>
+#include <map>
 
 #include "common.cuh"
 #include "dist.cuh"
@@ -30,7 +31,7 @@
 namespace ngdb_dev {
 namespace {
 
-constexpr int kCWarps = 4;                // consumer warps
+constexpr int kCWarps = 8;                // consumer warps
 constexpr int kThreads = 32 * (kCWarps + 1);  // + one producer warp
 constexpr int kWarps = kThreads / 32;
 constexpr int kRing = 16;                 // candidate rows staged per CTA
@@ -142,25 +143,25 @@ __device__ __forceinline__ void sweep(const DevArgs& a, const Cands& cs, Lane<BB
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring.empty[slot]);  // row is in registers: slot free
-    float s = 0.f;
+    float sx = 0.f, sy = 0.f, sz = 0.f, sw = 0.f;  // independent chains (ILP)
 #pragma unroll
     for (int i = 0; i < kMaxChunks; ++i) {
       const int c = lane + 32 * i;
       if (i < L.nch && c < d4) {
         if constexpr (kBeta) {
-          s += Dist<BB>::term(v[i].x, v2[i].x, L.qc[i].x, L.qo[i].x);
-          s += Dist<BB>::term(v[i].y, v2[i].y, L.qc[i].y, L.qo[i].y);
-          s += Dist<BB>::term(v[i].z, v2[i].z, L.qc[i].z, L.qo[i].z);
-          s += Dist<BB>::term(v[i].w, v2[i].w, L.qc[i].w, L.qo[i].w);
+          sx += Dist<BB>::term(v[i].x, v2[i].x, L.qc[i].x, L.qo[i].x);
+          sy += Dist<BB>::term(v[i].y, v2[i].y, L.qc[i].y, L.qo[i].y);
+          sz += Dist<BB>::term(v[i].z, v2[i].z, L.qc[i].z, L.qo[i].z);
+          sw += Dist<BB>::term(v[i].w, v2[i].w, L.qc[i].w, L.qo[i].w);
         } else {
-          s += Dist<BB>::term(v[i].x, L.qc[i].x, L.qo[i].x, a.alpha_box);
-          s += Dist<BB>::term(v[i].y, L.qc[i].y, L.qo[i].y, a.alpha_box);
-          s += Dist<BB>::term(v[i].z, L.qc[i].z, L.qo[i].z, a.alpha_box);
-          s += Dist<BB>::term(v[i].w, L.qc[i].w, L.qo[i].w, a.alpha_box);
+          sx += Dist<BB>::term(v[i].x, L.qc[i].x, L.qo[i].x, a.alpha_box);
+          sy += Dist<BB>::term(v[i].y, L.qc[i].y, L.qo[i].y, a.alpha_box);
+          sz += Dist<BB>::term(v[i].z, L.qc[i].z, L.qo[i].z, a.alpha_box);
+          sw += Dist<BB>::term(v[i].w, L.qc[i].w, L.qo[i].w, a.alpha_box);
         }
       }
     }
-    float dj = warp_sum(s);
+    float dj = warp_sum((sx + sy) + (sz + sw));
     if constexpr (kBeta) dj += cs.qbias + __ldg(cs.cbias + __ldg(cs.idx + j));
     const float coef = coef_of(j, dj);
     if (!kGrad) continue;
@@ -187,9 +188,10 @@ __device__ __forceinline__ void sweep(const DevArgs& a, const Cands& cs, Lane<BB
 // Cross-warp sum of the per-lane dq accumulators: every consumer warp stores
 // its partial (and its loss / coefficient-sum partials) in its own shared row,
 // one barrier, then the block sums the kCWarps rows in warp order
-// (deterministic) into part[0]; lred[kWarps] / lred[kWarps + 1] receive the
+// (deterministic) into part[0]; lred[kLossTot] / lred[kCsumTot] receive the
 // loss and coefficient sums. Ends with a barrier.
 constexpr int kMaxWq = 1024;
+constexpr int kLossTot = 2 * kCWarps, kCsumTot = 2 * kCWarps + 1, kLred = 2 * kCWarps + 2;
 template <int BB, int kMaxChunks>
 __device__ void reduce_partials(const DevArgs& a, const Lane<BB, kMaxChunks>& L, float (*part)[kMaxWq],
                                 float* lred, float loss, float csum) {
@@ -225,8 +227,8 @@ __device__ void reduce_partials(const DevArgs& a, const Lane<BB, kMaxChunks>& L,
       l += lred[2 * w];
       cs += lred[2 * w + 1];
     }
-    lred[kWarps] = l;
-    lred[kWarps + 1] = cs;
+    lred[kLossTot] = l;
+    lred[kCsumTot] = cs;
   }
   __syncthreads();
 }
@@ -287,11 +289,10 @@ __device__ __forceinline__ float beta_qterm(const DevArgs& a, const float* q, in
 // partials over DSMEM — CTA p sums dims [p*wq/S, (p+1)*wq/S) over all S
 // partials in rank order (deterministic); CTA 0 sums the loss partials.
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first, int S) {
+__global__ void __launch_bounds__(kThreads, 2) loss_fwd_kernel(DevArgs a, int /*unused*/, int first, int S) {
   extern __shared__ __align__(128) float ring_smem[];
   __shared__ __align__(16) float parts[kCWarps][kMaxWq];
-  __shared__ float lred[2 * kCWarps + 2];
-  static_assert(kWarps + 1 < 2 * kCWarps + 2, "lred layout");
+  __shared__ float lred[kLred];
   const Ring ring = make_ring(ring_smem, a.ent_w);
   pdl_start();
   const int part = blockIdx.x % S;
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
     const int e0 = part * a.wq / S, e1 = (part + 1) * a.wq / S;
     float sc = 0.f;
     if constexpr (BB == NGDB_BETAE)
-      for (int p = 0; p < S; ++p) sc += (p == part) ? lred[kWarps + 1] : ld_peer(lred + kWarps + 1, p);
+      for (int p = 0; p < S; ++p) sc += (p == part) ? lred[kCsumTot] : ld_peer(lred + kCsumTot, p);
     for (int e = e0 + threadIdx.x; e < e1; e += kThreads) {
       float v = 0.f;
       for (int p = 0; p < S; ++p) v += (p == part) ? red[e] : ld_peer(red + e, p);
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
     }
     if (part == 0 && threadIdx.x == 0) {
       float total = 0.f;
-      for (int p = 0; p < S; ++p) total += (p == 0) ? lred[kWarps] : ld_peer(lred + kWarps, p);
+      for (int p = 0; p < S; ++p) total += (p == 0) ? lred[kLossTot] : ld_peer(lred + kLossTot, p);
       a.loss_out[qi] = total;
       a.arena[d.out] = total;
       if (!isfinite(total)) atomicOr(&a.flags[0], 1);
@@ -367,10 +368,10 @@ __global__ void __launch_bounds__(kThreads) loss_fwd_kernel(DevArgs a, int first
 // optimizer) and dL/dq (its G slot), the S partials of dL/dq reduce-scattered
 // over DSMEM in rank order.
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int first, int S) {
+__global__ void __launch_bounds__(kThreads, 2) score_kernel(DevArgs a, int dir, int first, int S) {
   extern __shared__ __align__(128) float ring_smem[];
   __shared__ __align__(16) float parts[kCWarps][kMaxWq];
-  __shared__ float lred[2 * kCWarps + 2];
+  __shared__ float lred[kLred];
   const Ring ring = make_ring(ring_smem, a.ent_w);
   pdl_start();
   const int part = blockIdx.x % S;
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int
   cluster_sync_all();
   float sc = 0.f;
   if constexpr (BB == NGDB_BETAE)  // over all S parts, in rank order
-    for (int p = 0; p < S; ++p) sc += (p == part) ? lred[kWarps + 1] : ld_peer(lred + kWarps + 1, p);
+    for (int p = 0; p < S; ++p) sc += (p == part) ? lred[kCsumTot] : ld_peer(lred + kCsumTot, p);
   float* dst = a.arena + d.out;
   const int e0 = part * a.wq / S, e1 = (part + 1) * a.wq / S;
   for (int e = e0 + threadIdx.x; e < e1; e += kThreads) {
@@ -427,37 +428,42 @@ __global__ void __launch_bounds__(kThreads) score_kernel(DevArgs a, int dir, int
 
 }  // namespace
 
-// cluster size: enough CTAs for ~4 per SM, 1..8 per node (portable limit)
-inline int parts_for(int n) { return std::max(1, std::min(8, (4 * 148 + n - 1) / std::max(n, 1))); }
+// CTAs of `kernel` resident at once on the device (dynamic smem `smem`)
+template <class K>
+int resident_ctas(K kernel, size_t smem, int num_sms) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  return std::max(1, per_sm) * num_sms;
+}
+// parts per node (cluster size, 1..8): as many as fit in ONE wave, so no CTA
+// waits for a second wave
+inline int parts_for(int n, int resident) {
+  return std::max(1, std::min(8, resident / std::max(n, 1)));
+}
 
 template <class K>
-void launch_ring_kernel(K kernel, int ent_w, int S, int n, cudaStream_t s, const DevArgs& a,
-                        int x, int first) {
+void launch_ring_kernel(K kernel, int ent_w, int n, cudaStream_t s, const DevArgs& a, int x,
+                        int first) {
   const size_t smem = ring_bytes(ent_w);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static std::map<std::pair<const void*, size_t>, int> cache;  // (kernel, smem) -> resident CTAs
+  int& resident = cache[{reinterpret_cast<const void*>(kernel), smem}];
+  if (!resident) resident = resident_ctas(kernel, smem, 148);
+  const int S = parts_for(n, resident);
   launch_pdl(kernel, dim3(S * n), dim3(kThreads), smem, s, S, a, x, first, S);
 }
 
 template <int NCH>
 void launch_loss_nch(const DevArgs& a, int first, int n, cudaStream_t s) {
-  const int S = std::max(2, parts_for(n));
-  auto go = [&](auto k) {
-    const size_t smem = ring_bytes(a.ent_w);
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(k, dim3(S * n), dim3(kThreads), smem, s, S, a, first, S);
-  };
-  if (a.backbone == NGDB_GQE) go(loss_fwd_kernel<NGDB_GQE, NCH>);
-  else if (a.backbone == NGDB_BETAE) go(loss_fwd_kernel<NGDB_BETAE, NCH>);
-  else go(loss_fwd_kernel<NGDB_Q2B, NCH>);
+  if (a.backbone == NGDB_GQE) launch_ring_kernel(loss_fwd_kernel<NGDB_GQE, NCH>, a.ent_w, n, s, a, first, first);
+  else if (a.backbone == NGDB_BETAE) launch_ring_kernel(loss_fwd_kernel<NGDB_BETAE, NCH>, a.ent_w, n, s, a, first, first);
+  else launch_ring_kernel(loss_fwd_kernel<NGDB_Q2B, NCH>, a.ent_w, n, s, a, first, first);
 }
 template <int NCH>
 void launch_score_nch(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
-  const int S = std::max(2, parts_for(n));
-  if (a.backbone == NGDB_GQE) launch_ring_kernel(score_kernel<NGDB_GQE, NCH>, a.ent_w, S, n, s, a, dir, first);
-  else if (a.backbone == NGDB_BETAE) launch_ring_kernel(score_kernel<NGDB_BETAE, NCH>, a.ent_w, S, n, s, a, dir, first);
-  else launch_ring_kernel(score_kernel<NGDB_Q2B, NCH>, a.ent_w, S, n, s, a, dir, first);
+  if (a.backbone == NGDB_GQE) launch_ring_kernel(score_kernel<NGDB_GQE, NCH>, a.ent_w, n, s, a, dir, first);
+  else if (a.backbone == NGDB_BETAE) launch_ring_kernel(score_kernel<NGDB_BETAE, NCH>, a.ent_w, n, s, a, dir, first);
+  else launch_ring_kernel(score_kernel<NGDB_Q2B, NCH>, a.ent_w, n, s, a, dir, first);
 }
 
 int launch_loss_fwd(const DevArgs& a, int first, int n, const LaunchCtx& lc) {
