@@ -22,6 +22,7 @@
 //                 over the per-step entity table of beta.cu;
 //                 dL/dq = sum_j coef_j etab[r_j] + (sum_j coef_j) [psi(A)-psi(A+B) | psi(B)-psi(A+B)]
 #include <algorithm>
+#include <cstdio>
 #include <map>
 
 #include "common.cuh"
@@ -428,28 +429,52 @@ __global__ void __launch_bounds__(kThreads, 2) score_kernel(DevArgs a, int dir, 
 
 }  // namespace
 
-// CTAs of `kernel` resident at once on the device (dynamic smem `smem`)
+// Launch geometry of a ring kernel for a given dynamic smem size: CTAs
+// resident at once and the largest cluster the device can co-schedule. The
+// function's max-dynamic-smem attribute is set to exactly `smem` before each
+// launch whose size differs from the last one: cluster launches are validated
+// against that attribute, not against the bytes actually requested.
+struct RingGeom {
+  int resident = 0, max_cluster = 1;
+};
 template <class K>
-int resident_ctas(K kernel, size_t smem, int num_sms) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+RingGeom ring_geometry(K kernel, size_t smem, int num_sms) {
+  RingGeom g;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
-  return std::max(1, per_sm) * num_sms;
+  g.resident = std::max(1, per_sm) * num_sms;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(8 * 64);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  int mc = 1;
+  if (cudaOccupancyMaxPotentialClusterSize(&mc, kernel, &cfg) != cudaSuccess) mc = 1;
+  g.max_cluster = std::max(1, std::min(8, mc));
+  cudaGetLastError();  // a failed query must not leak into the launch checks
+  return g;
 }
-// parts per node (cluster size, 1..8): as many as fit in ONE wave, so no CTA
-// waits for a second wave
-inline int parts_for(int n, int resident) {
-  return std::max(1, std::min(8, resident / std::max(n, 1)));
+// parts per node (cluster size): as many as fit in ONE wave, so no CTA waits
+// for a second wave
+inline int parts_for(int n, const RingGeom& g) {
+  // >= 2 keeps every launch a real cluster (the kernels use cluster barriers)
+  return std::max(std::min(2, g.max_cluster), std::min(g.max_cluster, g.resident / std::max(n, 1)));
 }
 
 template <class K>
 void launch_ring_kernel(K kernel, int ent_w, int n, cudaStream_t s, const DevArgs& a, int x,
                         int first) {
   const size_t smem = ring_bytes(ent_w);
-  static std::map<std::pair<const void*, size_t>, int> cache;  // (kernel, smem) -> resident CTAs
-  int& resident = cache[{reinterpret_cast<const void*>(kernel), smem}];
-  if (!resident) resident = resident_ctas(kernel, smem, 148);
-  const int S = parts_for(n, resident);
+  static std::map<const void*, size_t> attr;                         // kernel -> attribute set
+  static std::map<std::pair<const void*, size_t>, RingGeom> cache;  // (kernel, smem) -> geometry
+  const void* key = reinterpret_cast<const void*>(kernel);
+  auto it = attr.find(key);
+  if (it == attr.end() || it->second != smem) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[key] = smem;
+  }
+  RingGeom& g = cache[{key, smem}];
+  if (!g.resident) g = ring_geometry(kernel, smem, 148);
+  const int S = parts_for(n, g);
   launch_pdl(kernel, dim3(S * n), dim3(kThreads), smem, s, S, a, x, first, S);
 }
 
