@@ -133,9 +133,10 @@ typedef struct ngdb_train_opts {
 int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
                    int64_t first_step, int32_t n_steps, double* loss_per_step,
                    float* per_query_loss, double* timings);
-/* timings (may be NULL) receives 3 doubles: seconds the calling thread spent
- * waiting for planned batches, submitting (upload + launches), and waiting for
- * step results. */
+/* timings (may be NULL) receives 6 doubles: seconds the calling thread spent
+ * waiting for planned batches, submitting (upload + launches), waiting for
+ * step results, and of the submit time: step_begin, exec_pool calls,
+ * optimizer_step. */
 
 /* Streaming run of an already built step (H2D of its plan inside the call). */
 int ngdb_run_step(ngdb_ctx* ctx, const ngdb_step* s, int64_t step, float* per_query_loss,

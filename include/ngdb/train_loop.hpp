@@ -34,7 +34,10 @@ struct TrainLoopConfig {
 
 struct TrainLoopStats {
   double plan_wait_s = 0.0;     // consumer waiting for a planned batch
-  double submit_s = 0.0;        // consumer uploading + launching steps
+  double submit_s = 0.0;        // consumer uploading + launching steps, of which:
+  double begin_s = 0.0;         //   ngdb_step_begin (pack + H2D + step prologue)
+  double pools_s = 0.0;         //   ngdb_exec_pool calls
+  double optim_s = 0.0;         //   ngdb_optimizer_step
   double collect_wait_s = 0.0;  // consumer waiting for a step's losses
   int32_t producers = 0;
 };

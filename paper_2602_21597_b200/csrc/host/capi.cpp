@@ -493,6 +493,9 @@ int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
       timings[0] = st.plan_wait_s;
       timings[1] = st.submit_s;
       timings[2] = st.collect_wait_s;
+      timings[3] = st.begin_s;
+      timings[4] = st.pools_s;
+      timings[5] = st.optim_s;
     }
   });
 }

@@ -312,14 +312,15 @@ class Engine:
                          seed, first_tag)
         sums = np.zeros(n_steps, dtype=np.float64)
         pq = np.zeros((n_steps, batch), dtype=np.float32) if per_query else None
-        timings = (C.c_double * 3)()
+        timings = (C.c_double * 6)()
         check(lib.ngdb_train_run(self._h, graph._h, C.byref(opts), self.step_count, n_steps,
                                  _p(sums, C.c_double),
                                  _p(pq, C.c_float) if pq is not None else None, timings))
         self.step_count += n_steps
         # host seconds of the calling thread: waiting for plans, submitting, waiting for results
         self.last_timings = {"plan_wait_s": timings[0], "submit_s": timings[1],
-                             "collect_wait_s": timings[2]}
+                             "collect_wait_s": timings[2], "submit_begin_s": timings[3],
+                             "submit_pools_s": timings[4], "submit_optimizer_s": timings[5]}
         return (sums, pq) if per_query else sums
 
     def run_step(self, step: PlannedStep, n_queries: int) -> np.ndarray:
