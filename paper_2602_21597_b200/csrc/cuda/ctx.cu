@@ -313,10 +313,18 @@ void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
       if (p) CK(cudaFree(p));
       p = dmalloc<float>(n);
     };
-    c->cap_score = std::max<int64_t>(m.n_score, c->cap_score);
-    c->cap_anchor = std::max<int64_t>(m.n_anchor, c->cap_anchor);
-    c->cap_project = std::max<int64_t>(m.n_project, c->cap_project);
-    c->cap_queries = std::max<int64_t>(m.n_queries, c->cap_queries);
+    // grow with headroom: every growth is a device sync + reallocation, and
+    // streaming plans vary from step to step. First sizing covers any batch of
+    // max_queries queries (<= 2 score slots, 3 anchors, 4 projects per query
+    // after DNF, query.hpp:14-29)
+    auto grow_to = [](int64_t need, int64_t cap, int64_t floor) {
+      return need <= cap ? cap : std::max<int64_t>({need + need / 4, cap + cap / 4, floor});
+    };
+    const int64_t B = std::max<int64_t>(c->desc.max_queries, 1);
+    c->cap_score = grow_to(m.n_score, c->cap_score, 2 * B);
+    c->cap_anchor = grow_to(m.n_anchor, c->cap_anchor, 3 * B);
+    c->cap_project = grow_to(m.n_project, c->cap_project, 4 * B);
+    c->cap_queries = grow_to(m.n_queries, c->cap_queries, B);
     c->cap_cand = m.n_candidates;
     realloc_f(c->qbuf, c->cap_score * wq);
     realloc_f(c->dqbuf, c->cap_score * wq);
