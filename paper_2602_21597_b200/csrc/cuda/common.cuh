@@ -276,4 +276,18 @@ int launch_masked_rows_adam(float* w, float* m, float* v, float* dbg, const floa
                             const float* bc, const LaunchCtx& lc);
 int launch_dense_adam(float* w, float* m, float* v, float* g, int64_t n, const AdamHyper& hp,
                       const float* bc, const LaunchCtx& lc);
+// dense tensors of the flat buffer: Adam + (weights) the 3xTF32 split refresh
+struct DenseJob {
+  int64_t off;        // element offset in the flat dense buffers
+  int rows, cols;
+  int64_t split_off;  // W_hi offset in the split buffer (W_lo, W^T_hi, W^T_lo follow); -1: none
+  int tile_begin;     // first 32x32 tile of this tensor in the launch grid
+};
+struct DenseJobs {
+  DenseJob job[kMaxDenseTensors];
+  int n, tiles;
+};
+int launch_dense_adam_split(float* w, float* m, float* v, const float* g, float* wsplit,
+                            const DenseJobs& jobs, const AdamHyper& hp, const float* bc,
+                            const LaunchCtx& lc);
 }  // namespace ngdb_dev

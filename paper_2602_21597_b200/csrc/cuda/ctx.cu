@@ -570,6 +570,22 @@ int refresh_weight_splits(ngdb_ctx* c) {
   return launches;
 }
 
+// Every dense tensor as one job of the fused dense Adam + split refresh.
+DenseJobs dense_jobs(const ngdb_ctx* c) {
+  DenseJobs j{};
+  for (const auto& p : c->params) {
+    if (p.sparse || j.n >= kMaxDenseTensors) continue;
+    DenseJob& d = j.job[j.n++];
+    d.off = c->dense_off[p.dense_idx];
+    d.rows = static_cast<int>(p.rows);
+    d.cols = static_cast<int>(p.cols);
+    d.split_off = p.rows > 1 ? c->wsplit_off[p.dense_idx] : -1;
+    d.tile_begin = j.tiles;
+    j.tiles += static_cast<int>(((p.rows + 31) / 32) * ((p.cols + 31) / 32));
+  }
+  return j;
+}
+
 // Adam bias corrections of step t -> device scalars (read by the optimizer
 // kernels, so a captured graph of the step replays with the current t). The
 // source is pageable: the copy is staged before cudaMemcpyAsync returns.
@@ -615,9 +631,8 @@ void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
   const double rb = 6.0 * p->meta.n_rrows * rel.cols * 4 + p->meta.n_rcon * (4.0 + rel.cols * 4);
   timed(c, F_OPT_RELATION, rb, [&] { return launch_sparse_adam_relation(a, tr, hp, bc, lc); });
   timed(c, F_OPT_DENSE, 28.0 * c->dense_n, [&] {
-    return launch_dense_adam(c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->dense_n, hp, bc,
-                             lc) +
-           refresh_weight_splits(c);
+    return launch_dense_adam_split(c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit,
+                                   dense_jobs(c), hp, bc, lc);
   });
   CK(cudaGetLastError());
 }
@@ -1494,9 +1509,8 @@ int ngdb_shard_optimizer(ngdb_ctx* c, int64_t step) {
                                      c->d_bc, lc);
     });
     timed(c, F_OPT_DENSE, 28.0 * c->dense_n, [&] {
-      return launch_dense_adam(c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->dense_n, hp,
-                               c->d_bc, lc) +
-             refresh_weight_splits(c);
+      return launch_dense_adam_split(c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit,
+                                     dense_jobs(c), hp, c->d_bc, lc);
     });
     CK(cudaGetLastError());
     sh.active = false;

@@ -238,7 +238,73 @@ __global__ void dense_adam_kernel(float* w, float* m, float* v, const float* g, 
   }
 }
 
+// Dense Adam fused with the 3xTF32 operand refresh of the MLP weights: one
+// 32x32 tile per CTA updates theta, m, v and writes W_hi, W_lo and, through a
+// shared-memory transpose, (W^T)_hi, (W^T)_lo — the split layout wop()
+// reads (mlp_util.cuh). Replaces one Adam launch + two split launches per
+// weight matrix.
+__device__ __forceinline__ void split_hi_lo(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+  lo = x - hi;
+}
+
+__global__ void __launch_bounds__(256) dense_adam_split_kernel(float* w, float* m, float* v,
+                                                               const float* g, float* wsplit,
+                                                               DenseJobs jobs, AdamHyper hp,
+                                                               const float* bc) {
+  pdl_start();
+  __shared__ float tile[32][33];
+  const int t = blockIdx.x;
+  int j = 0;
+  while (j + 1 < jobs.n && t >= jobs.job[j + 1].tile_begin) ++j;
+  const DenseJob& J = jobs.job[j];
+  const int lt = t - J.tile_begin;
+  const int tiles_c = (J.cols + 31) / 32;
+  const int r0 = (lt / tiles_c) * 32, c0 = (lt % tiles_c) * 32;
+  const AdamK k = adam_consts(hp, bc);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x / 32;
+  const int64_t n = static_cast<int64_t>(J.rows) * J.cols;
+  for (int y = ty; y < 32; y += 8) {
+    const int r = r0 + y, c = c0 + tx;
+    if (r < J.rows && c < J.cols) {
+      const int64_t i = J.off + static_cast<int64_t>(r) * J.cols + c;
+      float wi = w[i], mi = m[i], vi = v[i];
+      adam_update(wi, mi, vi, g[i], k);
+      w[i] = wi;
+      m[i] = mi;
+      v[i] = vi;
+      if (J.split_off >= 0) {
+        float hi, lo;
+        split_hi_lo(wi, hi, lo);
+        wsplit[J.split_off + static_cast<int64_t>(r) * J.cols + c] = hi;
+        wsplit[J.split_off + n + static_cast<int64_t>(r) * J.cols + c] = lo;
+      }
+      tile[y][tx] = wi;
+    }
+  }
+  if (J.split_off < 0) return;  // uniform per CTA
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int c = c0 + y, r = r0 + tx;  // W^T [cols][rows]
+    if (r < J.rows && c < J.cols) {
+      float hi, lo;
+      split_hi_lo(tile[tx][y], hi, lo);
+      wsplit[J.split_off + 2 * n + static_cast<int64_t>(c) * J.rows + r] = hi;
+      wsplit[J.split_off + 3 * n + static_cast<int64_t>(c) * J.rows + r] = lo;
+    }
+  }
+}
+
 }  // namespace
+
+int launch_dense_adam_split(float* w, float* m, float* v, const float* g, float* wsplit,
+                            const DenseJobs& jobs, const AdamHyper& hp, const float* bc,
+                            const LaunchCtx& lc) {
+  if (jobs.n <= 0 || jobs.tiles <= 0) return 0;
+  launch_pdl(dense_adam_split_kernel, dim3(jobs.tiles), dim3(256), 0, lc.stream, 1, w, m, v, g,
+             wsplit, jobs, hp, bc);
+  return 1;
+}
 
 int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
                               const float* bc, const LaunchCtx& lc) {
