@@ -78,7 +78,8 @@ typedef struct ngdb_node_desc {
   int32_t grad;  /* bwd: upstream gradient row; -1 for the Loss mirror */
   int32_t self;  /* bwd: the mirror's forward output */
   int32_t id;    /* entity (EmbedAnchor/FuseSemantic), relation (Project), query (Score/Loss) */
-  int32_t aux;   /* anchor slot / project slot / score slot s; -1 = union Loss */
+  int32_t aux;   /* anchor slot / project slot / score slot s / intersect stash slot;
+                    -1 = union Loss */
 } ngdb_node_desc;
 
 /* One kernel invocation = one PopBatch or one cardinality class of it. */

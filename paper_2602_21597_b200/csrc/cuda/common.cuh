@@ -11,6 +11,8 @@
 namespace ngdb_dev {
 
 constexpr int kMaxDenseTensors = 16;
+// Intersect stash slot size in units of d floats: Q2B Z, S, P [3][d] + U, Lm [d]
+constexpr int kStashPerSlot = 11;
 
 // Named dense tensors (offsets into the flat dense parameter buffer).
 enum DenseName : int {
@@ -77,6 +79,11 @@ struct DevArgs {
   int32_t fus_idx;       // dense index of fus_f (fus_wp = +1, fus_bp = +2)
   // row-sharded step (shard.cu): anchor rows fetched from their owners [A][ent_w]
   const float* anc_rows;
+  // Intersect stash: per forward node (slot = node aux) the MLP intermediates
+  // its mirror reads instead of recomputing them; istash_slots slots of
+  // kStashPerSlot * dim floats
+  float* istash;
+  int32_t istash_slots;
 };
 
 // Device view of the sharded step's owner work (ngdb_shard_plan + buffers).

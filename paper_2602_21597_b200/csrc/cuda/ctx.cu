@@ -192,6 +192,8 @@ struct ngdb_ctx {
   int world = 1, rank = 0;
   cudaStream_t own_stream = nullptr;
   const float* anc_rows = nullptr;  // set while a sharded step runs
+  float* istash = nullptr;           // Intersect stash (DevArgs::istash)
+  int32_t istash_slots = 0;
   struct ShardState {
     int32_t* blob = nullptr;
     int64_t blob_cap = 0;
@@ -408,6 +410,8 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.anchor_local = c->anchor_local;
   a.fus_idx = c->fus_idx;
   a.anc_rows = c->anc_rows;
+  a.istash = c->istash;
+  a.istash_slots = c->istash_slots;
   return a;
 }
 
@@ -831,6 +835,8 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     c->flags = reinterpret_cast<int32_t*>(dmalloc<float>(4));
     CK(cudaMemset(c->flags, 0, 16));
     c->scratch_cap = intersect_scratch_floats(d.backbone, d.dim, c->desc.max_batch);
+    c->istash_slots = std::max(c->desc.max_queries, 1);
+    c->istash = dmalloc<float>(int64_t(c->istash_slots) * kStashPerSlot * d.dim);
     c->scratch = dmalloc<float>(c->scratch_cap);
     c->d_bc = dmalloc<float>(4);
     tc_gemm_init();
@@ -858,6 +864,7 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   if (c->cand_local) cudaFree(c->cand_local);
   if (c->anchor_local) cudaFree(c->anchor_local);
   if (c->fscratch) cudaFree(c->fscratch);
+  if (c->istash) cudaFree(c->istash);
   for (float* p : {c->etab, c->etab_c, c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit, c->sem, c->qbuf, c->dqbuf,
                    c->coefbuf, c->ddbuf, c->agbuf, c->rgbuf, c->loss_out, c->scratch, c->arena,
                    c->l2_flush, c->d_bc})

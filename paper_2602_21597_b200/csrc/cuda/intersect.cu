@@ -176,14 +176,27 @@ __device__ __forceinline__ void softmax_k(const float* S, int64_t base, int k, i
   const float inv = 1.f / z;
   for (int l = 0; l < k; ++l) w[l] *= inv;
 }
+// stash of a forward node: Z, S, P rows [3][D], then U, Lm [D] (kStashPerSlot)
+__device__ __forceinline__ float* q2b_stash(const DevArgs& a, int slot) {
+  if (slot < 0 || slot >= a.istash_slots) {
+    atomicOr(&a.flags[1], 1);
+    slot = 0;
+  }
+  return a.istash + static_cast<int64_t>(slot) * kStashPerSlot * a.dim;
+}
+
+// Forward combine; also stashes the node's MLP intermediates (Z, S, P rows,
+// U, Lm) for its mirror, which then skips the forward recomputation.
 __global__ void q2b_combine_kernel(DevArgs a, KSpan ks, int first, const float* S, const float* U,
-                                   const float* Cin, const float* Oin) {
+                                   const float* Cin, const float* Oin, const float* Z,
+                                   const float* P, const float* Lm) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim;
   const int k = ks.k(i);
   const ngdb_node_desc d = a.nodes[first + i];
   const int64_t base = (int64_t)ks.row0(i) * D;
+  float* st = q2b_stash(a, d.aux);
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     float w[3];
     softmax_k(S, base, k, D, e, w);
@@ -191,37 +204,52 @@ __global__ void q2b_combine_kernel(DevArgs a, KSpan ks, int first, const float* 
     for (int l = 0; l < k; ++l) {
       c += w[l] * Cin[base + (int64_t)l * D + e];
       mn = fminf(mn, Oin[base + (int64_t)l * D + e]);
+      st[l * D + e] = Z[base + (int64_t)l * D + e];
+      st[3 * D + l * D + e] = S[base + (int64_t)l * D + e];
+      st[6 * D + l * D + e] = P[base + (int64_t)l * D + e];
     }
+    const float u = U[(int64_t)i * D + e];
+    st[9 * D + e] = u;
+    st[10 * D + e] = Lm[(int64_t)i * D + e];
     a.arena[d.out + e] = c;
-    a.arena[d.out + D + e] = mn * sigmoidf(U[(int64_t)i * D + e]);
+    a.arena[d.out + D + e] = mn * sigmoidf(u);
   }
 }
-__global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, const float* S, const float* U,
-                                       const float* Cin, const float* Oin, float* gS, Split gSs,
-                                       float* dCin, float* dOin, float* gU, Split gUs) {
+// Backward combine. Also gathers the node's inputs (arena) and its stashed Z
+// rows and Lm into class order: the operands of the weight-gradient GEMMs.
+__global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Cin, float* Oin,
+                                       float* Z, float* Lm, float* gS, Split gSs, float* dCin,
+                                       float* dOin, float* gU, Split gUs) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim;
   const int k = ks.k(i);
   const ngdb_node_desc d = a.nodes[first + i];
   const int64_t base = (int64_t)ks.row0(i) * D;
+  const float* st = q2b_stash(a, d.aux);
+  const float* S = st + 3 * D;  // the node's k score rows, stashed by the forward
   for (int e = threadIdx.x; e < D; e += blockDim.x) {
     const float gC = a.arena[d.grad + e];
     const float gO = a.arena[d.grad + D + e];
-    float w[3];
-    softmax_k(S, base, k, D, e, w);
+    float w[3], cin[3], oin[3];
+    softmax_k(S, 0, k, D, e, w);
     float ga[3], dot = 0.f;
     for (int l = 0; l < k; ++l) {
-      ga[l] = gC * Cin[base + (int64_t)l * D + e];
+      const int64_t r = base + (int64_t)l * D + e;
+      cin[l] = a.arena[d.in[l] + e];
+      oin[l] = a.arena[d.in[l] + D + e];
+      Cin[r] = cin[l];
+      Oin[r] = oin[l];
+      Z[r] = st[l * D + e];
+      ga[l] = gC * cin[l];
       dot += w[l] * ga[l];
     }
+    Lm[(int64_t)i * D + e] = st[10 * D + e];
     int arg = 0;
-    float mn = Oin[base + e];
-    for (int l = 1; l < k; ++l) {
-      const float o = Oin[base + (int64_t)l * D + e];
-      if (o < mn) { mn = o; arg = l; }  // ties -> lowest index
-    }
-    const float gate = sigmoidf(U[(int64_t)i * D + e]);
+    float mn = oin[0];
+    for (int l = 1; l < k; ++l)
+      if (oin[l] < mn) { mn = oin[l]; arg = l; }  // ties -> lowest index
+    const float gate = sigmoidf(st[9 * D + e]);
     for (int l = 0; l < k; ++l) {
       const int64_t r = base + (int64_t)l * D + e;
       put(gS, gSs, r, w[l] * (ga[l] - dot));
@@ -232,16 +260,18 @@ __global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, const flo
   }
 }
 // gP[i*k+l] = gLm[i] / k * (P > 0)  (plain + split)
-__global__ void q2b_gp_kernel(const float* gLm, const float* P, KSpan ks, int D, float* gP,
+__global__ void q2b_gp_kernel(DevArgs a, const float* gLm, KSpan ks, int first, float* gP,
                               Split gPs) {
   pdl_start();
   const int i = blockIdx.x;
+  const int D = a.dim;
   const int k = ks.k(i), r0 = ks.row0(i);
+  const float* P = q2b_stash(a, a.nodes[first + i].aux) + 6 * D;
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = threadIdx.x; e < D; e += blockDim.x)
     for (int l = 0; l < k; ++l) {
       const int64_t r = ((int64_t)r0 + l) * D + e;
-      put(gP, gPs, r, P[r] > 0.f ? gLm[(int64_t)i * D + e] * inv_k : 0.f);
+      put(gP, gPs, r, P[l * D + e] > 0.f ? gLm[(int64_t)i * D + e] * inv_k : 0.f);
     }
 }
 __global__ void q2b_scatter_kernel(DevArgs a, KSpan ks, int first, const float* dCin,
@@ -268,48 +298,50 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   const int64_t ndp = (int64_t)nP * D, rdp = (int64_t)RP * D;
   Scratch sc{a.scratch, a.scratch_cap};
   float* Cin = sc.take(rd);
-  Split Cs = take_split(sc, rd);
   float* Oin = sc.take(rd);
-  Split Os = take_split(sc, rd);
   float* Z = sc.take(rd);
-  Split RZs = take_split(sc, rd);  // split(relu(Z))
-  float* S = sc.take(rd);
-  float* P = sc.take(rd);
   float* Lm = sc.take(nd);
-  Split Lms = take_split(sc, nd);
-  float* U = sc.take(nd);
-  const float* p = a.dense;
-  const float* a1 = p + a.dense_off[Q2B_A1B];
-  const float* a2 = p + a.dense_off[Q2B_A2B];
-  const float* v1 = p + a.dense_off[Q2B_V1B];
-  const float* v2 = p + a.dense_off[Q2B_V2B];
   int launches = 0;
-
-  launch_pdl(q2b_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, Cin, Cs, Oin, Os);
-  ++launches;
-  {  // level 1: Z = A1 c + a1 (chained split of relu(Z)), P = V1 o + v1
-    TcGemmArgs lvl[2];
-    lvl[0] = gemm_args(R, D, D, op(Cs, D), wop(a, Q2B_A1, D, D, false), Z, D);
-    lvl[0].bias = a1;
-    lvl[0].s_hi = RZs.hi; lvl[0].s_lo = RZs.lo; lvl[0].s_relu = 1;
-    lvl[1] = gemm_args(R, D, D, op(Os, D), wop(a, Q2B_V1, D, D, false), P, D);
-    lvl[1].bias = v1;
-    launches += tc_gemm_batch(lvl, 2, s);
-  }
-  launch_pdl(q2b_mean_relu_kernel, dim3(n), dim3(128), 0, s, 1, P, ks, D, Lm, Lms);
-  ++launches;
-  {  // level 2: S = A2 relu(Z) + a2, U = V2 Lm + v2
-    TcGemmArgs lvl[2];
-    lvl[0] = gemm_args(R, D, D, op(RZs, D), wop(a, Q2B_A2, D, D, false), S, D);
-    lvl[0].bias = a2;
-    lvl[1] = gemm_args(n, D, D, op(Lms, D), wop(a, Q2B_V2, D, D, false), U, D);
-    lvl[1].bias = v2;
-    launches += tc_gemm_batch(lvl, 2, s);
-  }
   if (dir == 0) {
-    launch_pdl(q2b_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, S, U, Cin, Oin);
+    Split Cs = take_split(sc, rd);
+    Split Os = take_split(sc, rd);
+    Split RZs = take_split(sc, rd);  // split(relu(Z))
+    float* S = sc.take(rd);
+    float* P = sc.take(rd);
+    Split Lms = take_split(sc, nd);
+    float* U = sc.take(nd);
+    const float* p = a.dense;
+    const float* a1 = p + a.dense_off[Q2B_A1B];
+    const float* a2 = p + a.dense_off[Q2B_A2B];
+    const float* v1 = p + a.dense_off[Q2B_V1B];
+    const float* v2 = p + a.dense_off[Q2B_V2B];
+    launch_pdl(q2b_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, Cin, Cs, Oin, Os);
+    ++launches;
+    {  // level 1: Z = A1 c + a1 (chained split of relu(Z)), P = V1 o + v1
+      TcGemmArgs lvl[2];
+      lvl[0] = gemm_args(R, D, D, op(Cs, D), wop(a, Q2B_A1, D, D, false), Z, D);
+      lvl[0].bias = a1;
+      lvl[0].s_hi = RZs.hi; lvl[0].s_lo = RZs.lo; lvl[0].s_relu = 1;
+      lvl[1] = gemm_args(R, D, D, op(Os, D), wop(a, Q2B_V1, D, D, false), P, D);
+      lvl[1].bias = v1;
+      launches += tc_gemm_batch(lvl, 2, s);
+    }
+    launch_pdl(q2b_mean_relu_kernel, dim3(n), dim3(128), 0, s, 1, P, ks, D, Lm, Lms);
+    ++launches;
+    {  // level 2: S = A2 relu(Z) + a2, U = V2 Lm + v2
+      TcGemmArgs lvl[2];
+      lvl[0] = gemm_args(R, D, D, op(RZs, D), wop(a, Q2B_A2, D, D, false), S, D);
+      lvl[0].bias = a2;
+      lvl[1] = gemm_args(n, D, D, op(Lms, D), wop(a, Q2B_V2, D, D, false), U, D);
+      lvl[1].bias = v2;
+      launches += tc_gemm_batch(lvl, 2, s);
+    }
+    launch_pdl(q2b_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, (const float*)S,
+               (const float*)U, (const float*)Cin, (const float*)Oin, (const float*)Z,
+               (const float*)P, (const float*)Lm);
     return launches + 1;
   }
+  // Backward: the forward's Z, S, P, U, Lm come from the node's stash slot
   float* gS = sc.take(rd);
   Split gSs = take_split(sc, rd);
   float* dCin = sc.take(rd);
@@ -327,8 +359,8 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
 
-  launch_pdl(q2b_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, S, U, Cin, Oin, gS, gSs, dCin, dOin, gU,
-                                           gUs);
+  launch_pdl(q2b_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, Cin, Oin, Z, Lm,
+             gS, gSs, dCin, dOin, gU, gUs);
   ++launches;
   SplitJobs j1{};
   j1.job[0] = {gU, n, D, D, 0, gUT.hi, gUT.lo};
@@ -349,7 +381,7 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
     lvl[3].s_hi = gZs.hi; lvl[3].s_lo = gZs.lo;
     launches += tc_gemm_batch(lvl, 4, s);
   }
-  launch_pdl(q2b_gp_kernel, dim3(n), dim3(128), 0, s, 1, gLm, P, ks, D, gP, gPs);
+  launch_pdl(q2b_gp_kernel, dim3(n), dim3(128), 0, s, 1, a, (const float*)gLm, ks, first, gP, gPs);
   ++launches;
   SplitJobs j2{};
   j2.job[0] = {gP, R, D, D, 0, gPT.hi, gPT.lo};

@@ -196,32 +196,45 @@ __global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a,
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) relation_adam_kernel(DevArgs a, SparseTable t,
-                                                                    AdamHyper hp, const float* bc) {
+// Relation rows: few rows (|R| <= a few hundred) with many contributions each
+// (every Project node of the step), so one THREAD per (row, float4 chunk): the
+// contribution loads of a chunk are independent and issued 4 at a time, and
+// the whole table is covered by ~|R| * w/4 threads instead of |R| warps.
+__global__ void __launch_bounds__(256) relation_adam_kernel(DevArgs a, SparseTable t,
+                                                           AdamHyper hp, const float* bc) {
   pdl_start();
-  const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (row_idx >= t.n_rows) return;
+  const int w4 = t.width / 4;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= static_cast<int64_t>(t.n_rows) * w4) return;
+  const int row_idx = static_cast<int>(item / w4), c = static_cast<int>(item % w4);
   const AdamK k = adam_consts(hp, bc);
   const int64_t row = t.rows[row_idx];
   const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
-  const int w4 = t.width / 4;
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  int kk = beg;
+  for (; kk + 4 <= end; kk += 4) {
+    float4 r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      r[u] = ld4(a.rgbuf + static_cast<int64_t>(__ldg(t.contrib + kk + u)) * t.width + 4 * c);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // contribution order kept (deterministic)
+      g.x += r[u].x; g.y += r[u].y; g.z += r[u].z; g.w += r[u].w;
+    }
+  }
+  for (; kk < end; ++kk) {
+    const float4 r = ld4(a.rgbuf + static_cast<int64_t>(__ldg(t.contrib + kk)) * t.width + 4 * c);
+    g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
+  }
   float* wp = t.w + row * t.width;
   float* mp = t.m + row * t.width;
   float* vp = t.v + row * t.width;
-  for (int c = lane; c < w4; c += 32) {
-    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int kk = beg; kk < end; ++kk) {
-      const float4 r = ld4(a.rgbuf + static_cast<int64_t>(t.contrib[kk]) * t.width + 4 * c);
-      g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
-    }
-    if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g);
-    float4 w = ld4(wp + 4 * c), m = ld4(mp + 4 * c), v = ld4(vp + 4 * c);
-    w = adam4(w, m, v, g, k);
-    st4(wp + 4 * c, w);
-    st4(mp + 4 * c, m);
-    st4(vp + 4 * c, v);
-  }
+  if (t.dbg_g) st4(t.dbg_g + row * t.width + 4 * c, g);
+  float4 w = ld4(wp + 4 * c), m = ld4(mp + 4 * c), v = ld4(vp + 4 * c);
+  w = adam4(w, m, v, g, k);
+  st4(wp + 4 * c, w);
+  st4(mp + 4 * c, m);
+  st4(vp + 4 * c, v);
 }
 
 __global__ void dense_adam_kernel(float* w, float* m, float* v, const float* g, int64_t n,
@@ -334,8 +347,9 @@ int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const Adam
 int launch_sparse_adam_relation(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
                                 const float* bc, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
-  const int blocks = (t.n_rows + kWarps - 1) / kWarps;
-  launch_pdl(relation_adam_kernel, dim3(blocks), dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
+  const int64_t items = static_cast<int64_t>(t.n_rows) * (t.width / 4);
+  launch_pdl(relation_adam_kernel, dim3(static_cast<int>((items + 255) / 256)), dim3(256), 0,
+             lc.stream, 1, a, t, hp, bc);
   return 1;
 }
 

@@ -182,33 +182,26 @@ __global__ void __launch_bounds__(kWarps * 32) negate_kernel(DevArgs a, int dir,
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) union_kernel(DevArgs a, int dir, int k, int first,
-                                                            int n) {
+// One thread per (node, candidate): the k branch distances of a candidate are
+// independent loads.
+__global__ void __launch_bounds__(256) union_kernel(DevArgs a, int dir, int k, int first, int n) {
   pdl_start();
-  const int node = blockIdx.x * kWarps + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (node >= n) return;
-  const ngdb_node_desc d = a.nodes[first + node];
   const int nc = a.ncand;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= static_cast<int64_t>(n) * nc) return;
+  const int node = static_cast<int>(item / nc), j = static_cast<int>(item % nc);
+  const ngdb_node_desc d = a.nodes[first + node];
+  float v[3];
+  for (int l = 0; l < k; ++l) v[l] = a.arena[d.in[l] + j];
+  int arg = 0;
+  float best = v[0];
+  for (int l = 1; l < k; ++l)
+    if (v[l] < best) { best = v[l]; arg = l; }  // ties -> lowest branch index
   if (dir == 0) {
-    float* out = a.arena + d.out;
-    for (int j = lane; j < nc; j += 32) {
-      float best = a.arena[d.in[0] + j];
-      for (int l = 1; l < k; ++l) best = fminf(best, a.arena[d.in[l] + j]);
-      out[j] = best;  // min distance == max score
-    }
+    a.arena[d.out + j] = best;  // min distance == max score
   } else {
-    const float* g = a.arena + d.grad;
-    float* out = a.arena + d.out;
-    for (int j = lane; j < nc; j += 32) {
-      int arg = 0;
-      float best = a.arena[d.in[0] + j];
-      for (int l = 1; l < k; ++l) {
-        const float v = a.arena[d.in[l] + j];
-        if (v < best) { best = v; arg = l; }  // ties -> lowest branch index
-      }
-      for (int l = 0; l < k; ++l) out[l * nc + j] = (l == arg) ? g[j] : 0.f;
-    }
+    const float g = a.arena[d.grad + j];
+    for (int l = 0; l < k; ++l) a.arena[d.out + l * nc + j] = (l == arg) ? g : 0.f;
   }
 }
 
@@ -285,7 +278,9 @@ int launch_negate(const DevArgs& a, int dir, int first, int n, const LaunchCtx& 
   return 1;
 }
 int launch_union(const DevArgs& a, int dir, int k, int first, int n, const LaunchCtx& lc) {
-  launch_pdl(union_kernel, dim3(blocks_for(n)), dim3(kWarps * 32), 0, lc.stream, 1, a, dir, k, first, n);
+  const int64_t items = static_cast<int64_t>(n) * a.ncand;
+  launch_pdl(union_kernel, dim3(static_cast<int>((items + 255) / 256)), dim3(256), 0, lc.stream, 1,
+             a, dir, k, first, n);
   return 1;
 }
 int launch_loss_bwd(const DevArgs& a, int first, int n, const LaunchCtx& lc) {

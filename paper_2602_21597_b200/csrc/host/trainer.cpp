@@ -198,6 +198,7 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
 
   // Slots of the persistent per-step staging buffers, in forward-id order.
   std::vector<int32_t> aux(nf, -1);
+  int32_t n_intersect = 0;
   std::vector<uint64_t> ekeys, akeys, rkeys;
   ekeys.reserve(static_cast<size_t>(B) * nc * 2 + 4 * B);
   akeys.reserve(4 * static_cast<size_t>(B));
@@ -213,6 +214,11 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
       case OpKind::Project:
         aux[i] = plan.n_project_slots++;
         rkeys.push_back(pack_key(x.payload, aux[i]));
+        break;
+      case OpKind::Intersect:
+        // stash slot: the forward kernel keeps its MLP intermediates there for
+        // the mirror (at most one Intersect per query, query.hpp:14-29)
+        aux[i] = n_intersect++;
         break;
       case OpKind::Score:
       case OpKind::Loss: {
