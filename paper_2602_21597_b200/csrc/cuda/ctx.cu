@@ -493,13 +493,14 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d,
       const KSpan ks = merged ? KSpan{d.count, d.k, merged->k} : KSpan::single(d.count, d.k);
       const int n_all = d.count + (merged ? merged->count : 0);
       if (c->profiling) {
-        // algorithmic fp32 GEMM flops of the classes (2*M*N*K per contraction,
-        // not counting the 3xTF32 split): DESIGN.md §4
+        // algorithmic fp32 GEMM flops of the classes (2*M*N*K per contraction;
+        // neither the 3xTF32 split nor any forward recomputation in backward
+        // counts): DESIGN.md §4
         const double n = n_all, R = ks.row0(n_all), D2 = 2.0 * c->desc.dim * c->desc.dim;
         double gemm_rows;
-        if (c->desc.backbone == NGDB_GQE) gemm_rows = d.dir == 0 ? 2 * n : 5 * n;
-        else if (c->beta()) gemm_rows = d.dir == 0 ? 6 * R : 18 * R;  // 2d->2d->d attention
-        else gemm_rows = d.dir == 0 ? 3 * R + n : 9 * R + 3 * n;
+        if (c->desc.backbone == NGDB_GQE) gemm_rows = d.dir == 0 ? 2 * n : 4 * n;
+        else if (c->beta()) gemm_rows = d.dir == 0 ? 6 * R : 12 * R;  // 2d->2d->d attention
+        else gemm_rows = d.dir == 0 ? 3 * R + n : 6 * R + 2 * n;
         c->fam_flops[fam] += gemm_rows * D2;
       }
       const double all_bytes =
