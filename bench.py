@@ -295,10 +295,16 @@ def bench_sharded(args):
     clocks.start()
     import ctypes as C
     ms = C.c_float()
+    # resident steps: each step's stages + NCCL collectives captured once into
+    # a CUDA graph (before the timed region) and replayed, like the resident
+    # plans of the single-GPU bench
+    graphs = eng.capture(plans[args.warmup:])
+    torch.cuda.synchronize()
+    dist.barrier()
     check(lib.ngdb_timer_start(ctx))
     for i in range(args.steps):
         step_no += 1
-        eng.run(plans[args.warmup + i], step_no)
+        graphs[i].replay(step_no)
     check(lib.ngdb_timer_stop(ctx, C.byref(ms)))
     clk = clocks.stop()
     launches = lib.ngdb_launch_count(ctx) - launches0

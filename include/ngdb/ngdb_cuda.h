@@ -214,7 +214,20 @@ int ngdb_plan_prepare(ngdb_ctx* ctx, ngdb_plan* plan);
 int ngdb_shard_begin(ngdb_ctx* ctx, const ngdb_step_plan* plan, const ngdb_shard_plan* shard,
                      ngdb_shard_buffers* bufs);
 int ngdb_shard_run(ngdb_ctx* ctx, int32_t stage);
+/* step <= 0: keep the Adam step scalars of the last ngdb_set_step (graph capture) */
 int ngdb_shard_optimizer(ngdb_ctx* ctx, int64_t step);
+/* Resident sharded step: the step plan and owner lists uploaded once into
+ * device memory owned by the handle, every context buffer sized at create.
+ * ngdb_shard_step_begin then only enqueues the step prologue and sets the
+ * device views, so begin + stages + collectives + ngdb_shard_optimizer(ctx, 0)
+ * can be captured into a CUDA graph and replayed (after ngdb_set_step). */
+typedef struct ngdb_shard_step ngdb_shard_step;
+int ngdb_shard_step_create(ngdb_ctx* ctx, const ngdb_step_plan* plan,
+                           const ngdb_shard_plan* shard, ngdb_shard_step** out);
+int ngdb_shard_step_begin(ngdb_ctx* ctx, ngdb_shard_step* step, ngdb_shard_buffers* bufs);
+int ngdb_shard_step_destroy(ngdb_shard_step* step);
+/* Adam bias-correction scalars of 1-based step t (host -> device, not capturable). */
+int ngdb_set_step(ngdb_ctx* ctx, int64_t step);
 /* Run the context's launches on an external stream (e.g. the framework stream
  * that also carries the collectives); NULL restores the private stream. */
 int ngdb_ctx_set_stream(ngdb_ctx* ctx, void* cuda_stream);

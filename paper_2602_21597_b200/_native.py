@@ -93,6 +93,10 @@ SIGNATURES = {
     "ngdb_plan_prepare": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ngdb_shard_begin": (C.c_int, [C.c_void_p, P(StepPlan), P(ShardPlan), P(ShardBuffers)]),
     "ngdb_shard_run": (C.c_int, [C.c_void_p, i32]),
+    "ngdb_shard_step_create": (C.c_int, [C.c_void_p, P(StepPlan), P(ShardPlan), P(C.c_void_p)]),
+    "ngdb_shard_step_begin": (C.c_int, [C.c_void_p, C.c_void_p, P(ShardBuffers)]),
+    "ngdb_shard_step_destroy": (C.c_int, [C.c_void_p]),
+    "ngdb_set_step": (C.c_int, [C.c_void_p, i64]),
     "ngdb_shard_optimizer": (C.c_int, [C.c_void_p, i64]),
     "ngdb_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ngdb_plan_destroy": (C.c_int, [C.c_void_p]),

@@ -1278,16 +1278,165 @@ namespace {
 int64_t up64(int64_t x) { return (x + 63) / 64 * 64; }
 }  // namespace
 
+}  // extern "C"
+
+namespace {
+
+// Device blob layout of a rank's owner work lists (ngdb_shard_plan).
+struct ShardLayout {
+  int64_t o_anc = 0, o_k = 0, o_slots = 0, o_cand = 0, o_off = 0, o_owned = 0, o_rows = 0,
+          o_seg = 0, o_con = 0, total = 0, n_owned = 0, n_con = 0;
+  ShardLayout() = default;
+  explicit ShardLayout(const ngdb_shard_plan& sp) {
+    const int64_t G = sp.world, B = sp.batch, A = sp.max_anchors, nc = sp.n_candidates, U = G * B;
+    n_owned = sp.unit_off[U];
+    n_con = sp.n_rows ? sp.seg[sp.n_rows] : 0;
+    o_k = o_anc + up64(G * A);
+    o_slots = o_k + up64(U);
+    o_cand = o_slots + up64(U * 3);
+    o_off = o_cand + up64(U * nc);
+    o_owned = o_off + up64(U + 1);
+    o_rows = o_owned + up64(n_owned);
+    o_seg = o_rows + up64(sp.n_rows);
+    o_con = o_seg + up64(sp.n_rows + 1);
+    total = o_con + up64(n_con);
+  }
+  void pack(const ngdb_shard_plan& sp, int32_t* h) const {
+    const int64_t G = sp.world, B = sp.batch, A = sp.max_anchors, nc = sp.n_candidates, U = G * B;
+    std::memcpy(h + o_anc, sp.anchor_ids, G * A * 4);
+    std::memcpy(h + o_k, sp.unit_k, U * 4);
+    std::memcpy(h + o_slots, sp.unit_slots, U * 3 * 4);
+    std::memcpy(h + o_cand, sp.cand, U * nc * 4);
+    std::memcpy(h + o_off, sp.unit_off, (U + 1) * 4);
+    if (n_owned) std::memcpy(h + o_owned, sp.owned, n_owned * 4);
+    if (sp.n_rows) {
+      std::memcpy(h + o_rows, sp.rows, sp.n_rows * 4);
+      std::memcpy(h + o_seg, sp.seg, (sp.n_rows + 1) * 4);
+      std::memcpy(h + o_con, sp.contrib, n_con * 4);
+    }
+  }
+};
+
+// the scalars of a shard plan a device step needs
+struct ShardShape {
+  int32_t world = 1, rank = 0, batch = 0, max_anchors = 0, max_slots = 0, n_candidates = 0,
+          n_rows = 0;
+  ShardShape() = default;
+  explicit ShardShape(const ngdb_shard_plan& sp)
+      : world(sp.world), rank(sp.rank), batch(sp.batch), max_anchors(sp.max_anchors),
+        max_slots(sp.max_slots), n_candidates(sp.n_candidates), n_rows(sp.n_rows) {}
+};
+
+void validate_shard(ngdb_ctx* c, const ngdb_step_plan& plan, const ngdb_shard_plan& sp) {
+  if (sp.world != c->world || sp.rank != c->rank)
+    throw Fail{NGDB_ERR_CONFIG, "shard plan world/rank do not match the context"};
+  if (c->beta() || c->fused()) throw Fail{NGDB_ERR_MISSING_KERNEL, "sharded BetaE / fusion"};
+  validate_plan(plan);
+  if (plan.n_score_slots > sp.max_slots || plan.n_anchor_slots > sp.max_anchors ||
+      plan.n_queries > sp.batch || plan.n_candidates != sp.n_candidates)
+    throw Fail{NGDB_ERR_SHAPE_MISMATCH, "step plan exceeds the shard plan's padding"};
+}
+
+// Exchange buffer sizes of a shard shape (ngdb_shard_buffers order + coef_all).
+void shard_buffer_sizes(const ngdb_ctx* c, const ShardShape& sp, int64_t sizes[12]) {
+  const int64_t G = sp.world, B = sp.batch, A = sp.max_anchors, S = sp.max_slots,
+                nc = sp.n_candidates;
+  const int64_t ew = c->params[c->ent_idx].cols, wq = c->query_width();
+  const Param& rel = c->params[c->rel_idx];
+  const int64_t n_red = c->dense_n + rel.n() + rel.rows;
+  const int64_t z[12] = {G * A * ew, A * ew,      S * wq,     G * S * wq, G * S * wq, S * wq,
+                         G * B,      B,           G * A * ew, G * A * ew, n_red,      G * S * nc};
+  for (int k = 0; k < 12; ++k) sizes[k] = z[k];
+}
+bool shard_buffers_fit(const ngdb_ctx* c, const ShardShape& sp) {
+  int64_t sizes[12], need = 0;
+  shard_buffer_sizes(c, sp, sizes);
+  for (int64_t z : sizes) need += up64(std::max<int64_t>(z, 1));
+  return need <= c->sh.buf_cap;
+}
+// (Re)size the exchange buffers (may synchronize) and point sh.bufs at them.
+void shard_exchange_buffers(ngdb_ctx* c, const ShardShape& sp) {
+  auto& sh = c->sh;
+  int64_t sizes[12], need = 0;
+  shard_buffer_sizes(c, sp, sizes);
+  for (int64_t z : sizes) need += up64(std::max<int64_t>(z, 1));
+  if (need > sh.buf_cap) {
+    CK(cudaStreamSynchronize(c->stream));
+    if (sh.buf) CK(cudaFree(sh.buf));
+    sh.buf_cap = need + need / 2;
+    sh.buf = dmalloc<float>(sh.buf_cap);
+    ++c->buffer_gen;
+  }
+  float* ptr[12];
+  float* cur = sh.buf;
+  for (int k = 0; k < 12; ++k) {
+    ptr[k] = cur;
+    cur += up64(std::max<int64_t>(sizes[k], 1));
+  }
+  ngdb_shard_buffers& b = sh.bufs;
+  b.anchor_send = ptr[0]; b.n_anchor_send = sizes[0];
+  b.anchor_rows = ptr[1]; b.n_anchor_rows = sizes[1];
+  b.query_mine = ptr[2]; b.n_query_mine = sizes[2];
+  b.query_all = ptr[3]; b.n_query_all = sizes[3];
+  b.dq_part = ptr[4]; b.n_dq_part = sizes[4];
+  b.dq_mine = ptr[5]; b.n_dq_mine = sizes[5];
+  b.loss_part = ptr[6]; b.n_loss_part = sizes[6];
+  b.loss_mine = ptr[7]; b.n_loss_mine = sizes[7];
+  b.grad_send = ptr[8]; b.n_grad_send = sizes[8];
+  b.grad_all = ptr[9]; b.n_grad_all = sizes[9];
+  b.reduce = ptr[10]; b.n_reduce = sizes[10];
+  sh.coef_all = ptr[11];
+}
+// Make (plan, owner lists in `blob`) the active sharded step: the step
+// prologue on the stream (capturable) and the device views.
+void shard_activate(ngdb_ctx* c, ngdb_plan* plan, const ShardShape& sp, const int32_t* blob,
+                    const ShardLayout& L) {
+  auto& sh = c->sh;
+  c->active = plan;
+  begin_step_device(c);
+  const ngdb_shard_buffers& b = sh.bufs;
+  // unset query slots stay defined (their rows are gathered but never read)
+  CK(cudaMemsetAsync(b.query_mine, 0, b.n_query_mine * 4, c->stream));
+  ShardDev& d = sh.dev;
+  d.world = sp.world;
+  d.rank = sp.rank;
+  d.batch = sp.batch;
+  d.max_anchors = sp.max_anchors;
+  d.max_slots = sp.max_slots;
+  d.anchor_ids = blob + L.o_anc;
+  d.unit_k = blob + L.o_k;
+  d.unit_slots = blob + L.o_slots;
+  d.cand = blob + L.o_cand;
+  d.unit_off = blob + L.o_off;
+  d.owned = blob + L.o_owned;
+  d.query_all = b.query_all;
+  d.dq_part = b.dq_part;
+  d.loss_part = b.loss_part;
+  d.coef_all = sh.coef_all;
+  sh.n_rows = sp.n_rows;
+  sh.rows = blob + L.o_rows;
+  sh.seg = blob + L.o_seg;
+  sh.contrib = blob + L.o_con;
+  sh.active = true;
+  c->anc_rows = b.anchor_rows;
+}
+
+}  // namespace
+
+// Resident sharded step: both blobs in device memory owned by the handle.
+struct ngdb_shard_step {
+  ngdb_plan plan;
+  int32_t* blob = nullptr;
+  ShardLayout layout;
+  ShardShape shape;
+};
+
+extern "C" {
+
 int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_plan* sp,
                      ngdb_shard_buffers* out) {
   return guarded([&] {
-    if (sp->world != c->world || sp->rank != c->rank)
-      throw Fail{NGDB_ERR_CONFIG, "shard plan world/rank do not match the context"};
-    if (c->beta() || c->fused()) throw Fail{NGDB_ERR_MISSING_KERNEL, "sharded BetaE / fusion"};
-    validate_plan(*plan);
-    if (plan->n_score_slots > sp->max_slots || plan->n_anchor_slots > sp->max_anchors ||
-        plan->n_queries > sp->batch || plan->n_candidates != sp->n_candidates)
-      throw Fail{NGDB_ERR_SHAPE_MISMATCH, "step plan exceeds the shard plan's padding"};
+    validate_shard(c, *plan, *sp);
     // 1) the rank's own step plan, as ngdb_step_begin
     const int i = c->cur;
     c->cur ^= 1;
@@ -1303,109 +1452,90 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
     upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->stream);
     CK(cudaEventRecord(c->staged[i], c->stream));
     ensure_step_buffers(c, c->stream_plan[i].meta);
-    begin_step_device(c);
-    c->active = &c->stream_plan[i];
 
     // 2) the owner work lists
-    const int64_t G = sp->world, B = sp->batch, A = sp->max_anchors, S = sp->max_slots,
-                  nc = sp->n_candidates, U = G * B;
-    const int64_t n_owned = sp->unit_off[U], n_con = sp->seg[sp->n_rows];
-    const int64_t o_anc = 0, o_k = o_anc + up64(G * A), o_slots = o_k + up64(U),
-                  o_cand = o_slots + up64(U * 3), o_off = o_cand + up64(U * nc),
-                  o_owned = o_off + up64(U + 1), o_rows = o_owned + up64(n_owned),
-                  o_seg = o_rows + up64(sp->n_rows), o_con = o_seg + up64(sp->n_rows + 1),
-                  total = o_con + up64(n_con);
     auto& sh = c->sh;
+    const ShardLayout SL(*sp);
     // the pinned buffer of two steps ago may still feed its H2D copy
     CK(cudaEventSynchronize(sh.staged[i]));
-    if (total > sh.staging_cap[i]) {
+    if (SL.total > sh.staging_cap[i]) {
       if (sh.staging[i]) CK(cudaFreeHost(sh.staging[i]));
-      sh.staging_cap[i] = total + total / 2;
+      sh.staging_cap[i] = SL.total + SL.total / 2;
       void* hp = nullptr;
       CK(cudaMallocHost(&hp, sh.staging_cap[i] * sizeof(int32_t)));
       sh.staging[i] = static_cast<int32_t*>(hp);
     }
-    if (total > sh.blob_cap) {
+    if (SL.total > sh.blob_cap) {
       CK(cudaStreamSynchronize(c->stream));
       if (sh.blob) CK(cudaFree(sh.blob));
-      sh.blob_cap = total + total / 2;
+      sh.blob_cap = SL.total + SL.total / 2;
       sh.blob = dmalloc<int32_t>(sh.blob_cap);
     }
-    int32_t* h = sh.staging[i];
-    std::memcpy(h + o_anc, sp->anchor_ids, G * A * 4);
-    std::memcpy(h + o_k, sp->unit_k, U * 4);
-    std::memcpy(h + o_slots, sp->unit_slots, U * 3 * 4);
-    std::memcpy(h + o_cand, sp->cand, U * nc * 4);
-    std::memcpy(h + o_off, sp->unit_off, (U + 1) * 4);
-    if (n_owned) std::memcpy(h + o_owned, sp->owned, n_owned * 4);
-    if (sp->n_rows) {
-      std::memcpy(h + o_rows, sp->rows, sp->n_rows * 4);
-      std::memcpy(h + o_seg, sp->seg, (sp->n_rows + 1) * 4);
-      std::memcpy(h + o_con, sp->contrib, n_con * 4);
-    }
-    CK(cudaMemcpyAsync(sh.blob, h, total * 4, cudaMemcpyHostToDevice, c->stream));
+    SL.pack(*sp, sh.staging[i]);
+    CK(cudaMemcpyAsync(sh.blob, sh.staging[i], SL.total * 4, cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += SL.total * 4;
     CK(cudaEventRecord(sh.staged[i], c->stream));
 
-    // 3) exchange buffers
-    const int64_t ew = c->params[c->ent_idx].cols, wq = c->query_width();
-    const Param& rel = c->params[c->rel_idx];
-    const int64_t n_red = c->dense_n + rel.n() + rel.rows;
-    const int64_t sizes[12] = {G * A * ew, A * ew,      S * wq,     G * S * wq, G * S * wq, S * wq,
-                               G * B,      B,           G * A * ew, G * A * ew, n_red,      G * S * nc};
-    int64_t need = 0;
-    for (int64_t z : sizes) need += up64(std::max<int64_t>(z, 1));
-    if (need > sh.buf_cap) {
-      CK(cudaStreamSynchronize(c->stream));
-      if (sh.buf) CK(cudaFree(sh.buf));
-      sh.buf_cap = need + need / 2;
-      sh.buf = dmalloc<float>(sh.buf_cap);
-      ++c->buffer_gen;
-    }
-    float* ptr[12];
-    float* cur = sh.buf;
-    for (int k = 0; k < 12; ++k) {
-      ptr[k] = cur;
-      cur += up64(std::max<int64_t>(sizes[k], 1));
-    }
-    ngdb_shard_buffers& b = sh.bufs;
-    b.anchor_send = ptr[0]; b.n_anchor_send = sizes[0];
-    b.anchor_rows = ptr[1]; b.n_anchor_rows = sizes[1];
-    b.query_mine = ptr[2]; b.n_query_mine = sizes[2];
-    b.query_all = ptr[3]; b.n_query_all = sizes[3];
-    b.dq_part = ptr[4]; b.n_dq_part = sizes[4];
-    b.dq_mine = ptr[5]; b.n_dq_mine = sizes[5];
-    b.loss_part = ptr[6]; b.n_loss_part = sizes[6];
-    b.loss_mine = ptr[7]; b.n_loss_mine = sizes[7];
-    b.grad_send = ptr[8]; b.n_grad_send = sizes[8];
-    b.grad_all = ptr[9]; b.n_grad_all = sizes[9];
-    b.reduce = ptr[10]; b.n_reduce = sizes[10];
-    sh.coef_all = ptr[11];
-    // unset query slots stay defined (their rows are gathered but never read)
-    CK(cudaMemsetAsync(b.query_mine, 0, sizes[2] * 4, c->stream));
-    ShardDev& d = sh.dev;
-    d.world = sp->world;
-    d.rank = sp->rank;
-    d.batch = sp->batch;
-    d.max_anchors = sp->max_anchors;
-    d.max_slots = sp->max_slots;
-    d.anchor_ids = sh.blob + o_anc;
-    d.unit_k = sh.blob + o_k;
-    d.unit_slots = sh.blob + o_slots;
-    d.cand = sh.blob + o_cand;
-    d.unit_off = sh.blob + o_off;
-    d.owned = sh.blob + o_owned;
-    d.query_all = b.query_all;
-    d.dq_part = b.dq_part;
-    d.loss_part = b.loss_part;
-    d.coef_all = sh.coef_all;
-    sh.n_rows = sp->n_rows;
-    sh.rows = sh.blob + o_rows;
-    sh.seg = sh.blob + o_seg;
-    sh.contrib = sh.blob + o_con;
-    sh.active = true;
-    c->anc_rows = b.anchor_rows;
-    if (out) *out = b;
+    // 3) exchange buffers, then the step prologue and device views
+    const ShardShape shape(*sp);
+    shard_exchange_buffers(c, shape);
+    shard_activate(c, &c->stream_plan[i], shape, sh.blob, SL);
+    if (out) *out = sh.bufs;
   });
+}
+
+int ngdb_shard_step_create(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_plan* sp,
+                           ngdb_shard_step** out) {
+  ngdb_shard_step* r = nullptr;
+  const int rc = guarded([&] {
+    validate_shard(c, *plan, *sp);
+    r = new ngdb_shard_step();
+    const PlanLayout L(*plan);
+    std::vector<int32_t> host(L.total);
+    pack_plan(*plan, L, host.data());
+    r->plan.blob = dmalloc<int32_t>(L.total);
+    CK(cudaMemcpy(r->plan.blob, host.data(), L.total * 4, cudaMemcpyHostToDevice));
+    r->plan.layout = L;
+    r->plan.meta = meta_of(*plan);
+    r->layout = ShardLayout(*sp);
+    r->shape = ShardShape(*sp);
+    host.assign(r->layout.total, 0);
+    r->layout.pack(*sp, host.data());
+    r->blob = dmalloc<int32_t>(r->layout.total);
+    CK(cudaMemcpy(r->blob, host.data(), r->layout.total * 4, cudaMemcpyHostToDevice));
+    // size every buffer now: a later begin inside a stream capture must not grow
+    ensure_step_buffers(c, r->plan.meta);
+    shard_exchange_buffers(c, r->shape);
+    *out = r;
+  });
+  if (rc != NGDB_OK && r) ngdb_shard_step_destroy(r);
+  return rc;
+}
+
+int ngdb_shard_step_begin(ngdb_ctx* c, ngdb_shard_step* r, ngdb_shard_buffers* out) {
+  return guarded([&] {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c->stream, &cs));
+    const bool fits = shard_buffers_fit(c, r->shape);
+    if (cs != cudaStreamCaptureStatusNone && !fits)
+      throw Fail{NGDB_ERR_CONFIG, "sharded step buffers must be sized before capture"};
+    ensure_step_buffers(c, r->plan.meta);
+    shard_exchange_buffers(c, r->shape);
+    shard_activate(c, &r->plan, r->shape, r->blob, r->layout);
+    if (out) *out = c->sh.bufs;
+  });
+}
+
+int ngdb_shard_step_destroy(ngdb_shard_step* r) {
+  if (!r) return NGDB_OK;
+  if (r->plan.blob) cudaFree(r->plan.blob);
+  if (r->blob) cudaFree(r->blob);
+  delete r;
+  return NGDB_OK;
+}
+
+int ngdb_set_step(ngdb_ctx* c, int64_t step) {
+  return guarded([&] { set_step_scalars(c, step); });
 }
 
 int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
@@ -1492,7 +1622,7 @@ int ngdb_shard_optimizer(ngdb_ctx* c, int64_t step) {
     auto& sh = c->sh;
     if (!sh.active || !c->active) throw Fail{NGDB_ERR_CONFIG, "ngdb_shard_optimizer outside a sharded step"};
     const ngdb_plan* p = c->active;
-    set_step_scalars(c, step);
+    if (step > 0) set_step_scalars(c, step);  // else: ngdb_set_step (capturable)
     const ngdb_model_desc& d = c->desc;
     const AdamHyper hp{d.lr, d.beta1, d.beta2, d.eps_adam};
     const LaunchCtx lc{c->stream, c->num_sms};

@@ -232,21 +232,7 @@ class ShardedEngine:
         b = ShardBuffers()
         check(lib.ngdb_shard_begin(self._h, C.byref(v), C.byref(s), C.byref(b)))
         t = {n: _device_view(self.torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
-        run = lambda stage: check(lib.ngdb_shard_run(self._h, FORWARD_STAGES[stage]))  # noqa: E731
-        comm = self.comm
-        run("anchor_pack")
-        comm.reduce_scatter(t["anchor_rows"], t["anchor_send"])
-        run("forward")
-        run("query_pack")
-        comm.all_gather(t["query_all"], t["query_mine"])
-        run("score")
-        comm.reduce_scatter(t["dq_mine"], t["dq_part"])
-        comm.reduce_scatter(t["loss_mine"], t["loss_part"])
-        run("score_done")
-        run("backward")
-        run("grad_pack")
-        comm.all_to_all(t["grad_all"], t["grad_send"])
-        comm.all_reduce(t["reduce"])
+        _stages(self, t)
         check(lib.ngdb_shard_optimizer(self._h, step_no))
         losses = np.zeros(step.n_queries, np.float32)
         total, nonfinite = C.c_double(), C.c_int32()
@@ -259,6 +245,20 @@ class ShardedEngine:
     def train_step(self, batch: Batch) -> np.ndarray:
         return self.run(self.plan(batch))
 
+    def capture(self, steps: List[ShardStep]) -> List["ShardGraph"]:
+        """Resident copies of `steps` whose stages AND collectives replay as one
+        CUDA graph each (NCCL only; the communicator must have run eagerly
+        first). Every resident step is created — and the context's buffers
+        sized for all of them — before the first capture, so no later growth
+        invalidates a captured graph."""
+        handles = []
+        for st in steps:
+            v, s = st.views()
+            h = C.c_void_p()
+            check(lib.ngdb_shard_step_create(self._h, C.byref(v), C.byref(s), C.byref(h)))
+            handles.append((h, st.n_queries))
+        return [ShardGraph(self, h, nq) for h, nq in handles]
+
     @property
     def handle(self):
         return self._h
@@ -267,6 +267,58 @@ class ShardedEngine:
         if getattr(self, "_h", None) and lib is not None:
             lib.ngdb_ctx_destroy(self._h)
             self._h = None
+
+
+class ShardGraph:
+    """A resident sharded step (ngdb_shard_step_create: plan + owner lists in
+    device memory, buffers sized up front) captured with its NCCL collectives
+    into one CUDA graph on the engine's stream. replay(step_no) sets the Adam
+    step scalars and launches the graph: no host work per stage."""
+
+    def __init__(self, eng: ShardedEngine, handle, n_queries: int):
+        self._h = handle  # owned from here on (destroyed with the graph)
+        if not eng.comm.nccl:
+            raise RuntimeError("graph capture of the sharded step needs the NCCL backend")
+        torch = eng.torch
+        self.eng = eng
+        self.n_queries = n_queries
+        self.graph = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(self.graph, stream=eng.stream):
+            b = ShardBuffers()
+            check(lib.ngdb_shard_step_begin(eng._h, self._h, C.byref(b)))
+            t = {n: _device_view(torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
+            _stages(eng, t)
+            check(lib.ngdb_shard_optimizer(eng._h, 0))
+
+    def replay(self, step_no: int) -> None:
+        check(lib.ngdb_set_step(self.eng._h, step_no))
+        with self.eng.torch.cuda.stream(self.eng.stream):
+            self.graph.replay()
+
+    def __del__(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.ngdb_shard_step_destroy(self._h)
+            self._h = None
+
+
+def _stages(eng: ShardedEngine, t) -> None:
+    """The device stages of a sharded step with the collectives between them."""
+    run = lambda stage: check(lib.ngdb_shard_run(eng._h, FORWARD_STAGES[stage]))  # noqa: E731
+    comm = eng.comm
+    run("anchor_pack")
+    comm.reduce_scatter(t["anchor_rows"], t["anchor_send"])
+    run("forward")
+    run("query_pack")
+    comm.all_gather(t["query_all"], t["query_mine"])
+    run("score")
+    comm.reduce_scatter(t["dq_mine"], t["dq_part"])
+    comm.reduce_scatter(t["loss_mine"], t["loss_part"])
+    run("score_done")
+    run("backward")
+    run("grad_pack")
+    comm.all_to_all(t["grad_all"], t["grad_send"])
+    comm.all_reduce(t["reduce"])
 
 
 def gather_entity_table(comm: Comm, local: np.ndarray, n_entities: int) -> Optional[np.ndarray]:

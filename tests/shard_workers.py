@@ -91,3 +91,41 @@ def gpu_step_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, ba
 def _load_batch(out_dir, step, rank):
     with open(os.path.join(out_dir, f"batch_{step}_{rank}.pkl"), "rb") as f:
         return pickle.load(f)
+
+
+def graph_replay_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
+    """One NCCL rank on GPU 0: the same steps run eagerly on one engine and as
+    captured CUDA graphs (stages + collectives) replayed on another."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200.sharded import Comm, ShardedEngine, plan_shard_step
+
+    comm = Comm()
+    g = m.Graph.synthetic(shape, 1)
+    info = g.info()
+    w = m.pattern_weights(mix)
+    batches = [m.Batch.sample(g, w, b, k, seed=3, tag=s * world + rank) for s in range(steps + 1)]
+    plans = [plan_shard_step(comm, bt, backbone, dim) for bt in batches]
+    out = {}
+    for mode in ("eager", "graph"):
+        eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
+                            n_neg=k, max_queries=b)
+        eng.run(plans[0], 1)  # communicator warm-up (eager)
+        if mode == "eager":
+            for s in range(1, steps + 1):
+                eng.run(plans[s], s + 1)
+        else:
+            graphs = eng.capture(plans[1:])
+            for s in range(1, steps + 1):
+                graphs[s - 1].replay(s + 1)
+        torch.cuda.synchronize()
+        out[mode] = {n: eng.download(n) for n, *_ in m.param_specs(backbone, info["n_entities"],
+                                                                  info["n_relations"], dim)}
+    with open(os.path.join(out_dir, f"graph{rank}.pkl"), "wb") as f:
+        pickle.dump(out, f)
+    dist.destroy_process_group()

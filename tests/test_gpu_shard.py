@@ -75,3 +75,19 @@ def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone
         if name != "entity":  # replicated tensors are identical on every rank
             assert np.array_equal(outs[0]["params"][name], outs[1]["params"][name]), name
     check_all(res, allow_frac=1e-3, steps=steps)
+
+
+@pytest.mark.parametrize("backbone,dim", [("q2b", 32), ("gqe", 16)])
+def test_sharded_graph_replay_matches_eager(tmp_path, backbone, dim):
+    # the resident sharded step (stages + NCCL collectives captured in one CUDA
+    # graph, bench.py --config c5) updates the parameters bit-identically to the
+    # eager stage-by-stage run
+    import torch.multiprocessing as mp
+
+    import shard_workers
+    mp.spawn(shard_workers.graph_replay_worker,
+             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, dim, 3, backbone),
+             nprocs=1, join=True)
+    out = pickle.load(open(tmp_path / "graph0.pkl", "rb"))
+    for name, v in out["eager"].items():
+        assert np.array_equal(v, out["graph"][name]), name
