@@ -84,6 +84,13 @@ struct DevArgs {
   // kStashPerSlot * dim floats
   float* istash;
   int32_t istash_slots;
+  // fused score+loss: per-(node, part) partials of dL/dq [items][wq] and of
+  // (loss, coefficient sum) [items][2], and per-node arrival counters (zero
+  // between launches)
+  float* lpart;
+  float* lpart_scalar;
+  int32_t* lcount;
+  int32_t lpart_items;
 };
 
 // Device view of the sharded step's owner work (ngdb_shard_plan + buffers).

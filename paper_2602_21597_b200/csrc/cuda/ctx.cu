@@ -194,6 +194,10 @@ struct ngdb_ctx {
   const float* anc_rows = nullptr;  // set while a sharded step runs
   float* istash = nullptr;           // Intersect stash (DevArgs::istash)
   int32_t istash_slots = 0;
+  float* lpart = nullptr;            // fused score+loss partials (DevArgs::lpart)
+  float* lpart_scalar = nullptr;
+  int32_t* lcount = nullptr;
+  int32_t lpart_items = 0;
   struct ShardState {
     int32_t* blob = nullptr;
     int64_t blob_cap = 0;
@@ -412,6 +416,10 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.anc_rows = c->anc_rows;
   a.istash = c->istash;
   a.istash_slots = c->istash_slots;
+  a.lpart = c->lpart;
+  a.lpart_scalar = c->lpart_scalar;
+  a.lcount = c->lcount;
+  a.lpart_items = c->lpart_items;
   return a;
 }
 
@@ -838,6 +846,12 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     c->scratch_cap = intersect_scratch_floats(d.backbone, d.dim, c->desc.max_batch);
     c->istash_slots = std::max(c->desc.max_queries, 1);
     c->istash = dmalloc<float>(int64_t(c->istash_slots) * kStashPerSlot * d.dim);
+    // (node, part) items of one loss launch: at most 8 parts of max_batch nodes
+    c->lpart_items = 8 * c->desc.max_batch;
+    c->lpart = dmalloc<float>(int64_t(c->lpart_items) * c->query_width());
+    c->lpart_scalar = dmalloc<float>(2 * int64_t(c->lpart_items));
+    c->lcount = reinterpret_cast<int32_t*>(dmalloc<float>(c->desc.max_batch));
+    CK(cudaMemset(c->lcount, 0, sizeof(int32_t) * c->desc.max_batch));
     c->scratch = dmalloc<float>(c->scratch_cap);
     c->d_bc = dmalloc<float>(4);
     tc_gemm_init();
@@ -866,6 +880,9 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   if (c->anchor_local) cudaFree(c->anchor_local);
   if (c->fscratch) cudaFree(c->fscratch);
   if (c->istash) cudaFree(c->istash);
+  if (c->lpart) cudaFree(c->lpart);
+  if (c->lpart_scalar) cudaFree(c->lpart_scalar);
+  if (c->lcount) cudaFree(c->lcount);
   for (float* p : {c->etab, c->etab_c, c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit, c->sem, c->qbuf, c->dqbuf,
                    c->coefbuf, c->ddbuf, c->agbuf, c->rgbuf, c->loss_out, c->scratch, c->arena,
                    c->l2_flush, c->d_bc})

@@ -3,7 +3,7 @@
 //
 // A cluster of S CTAs per scoring node, each taking a contiguous range of its
 // candidates. Candidate rows are staged in shared memory by the bulk-copy (TMA
-// 1-D) engine: a producer warp keeps a ring of kRing rows in flight
+// 1-D) engine: a producer warp keeps a ring of ~48 KB of rows in flight
 // (cp.async.bulk + mbarrier complete_tx), four consumer warps take rows
 // round-robin, read them with 128-bit shared loads, reduce the distance with
 // shuffles and — because the loss is a sum of per-candidate terms, so dL/dd_j
@@ -35,26 +35,32 @@ namespace {
 constexpr int kCWarps = 8;                // consumer warps
 constexpr int kThreads = 32 * (kCWarps + 1);  // + one producer warp
 constexpr int kWarps = kThreads / 32;
-constexpr int kRing = 16;                 // candidate rows staged per CTA
-
-// Shared-memory ring of candidate rows: kRing slots of ent_w floats + barriers.
+// Shared-memory ring of candidate rows: `depth` slots of ent_w floats +
+// barriers; ~48 KB of rows in flight per CTA (8..32 rows).
+__host__ __device__ inline int ring_depth(int width) {
+  const int d = 49152 / (width * 4);
+  return d < 8 ? 8 : (d > 32 ? 32 : d);
+}
 struct Ring {
   float* rows;
   uint64_t* full;
   uint64_t* empty;
   int width;  // floats per row
+  int depth;  // slots
 };
 inline size_t ring_bytes(int width) {
-  return static_cast<size_t>(kRing) * width * sizeof(float) + 2 * kRing * sizeof(uint64_t);
+  const int depth = ring_depth(width);
+  return static_cast<size_t>(depth) * width * sizeof(float) + 2 * depth * sizeof(uint64_t);
 }
 __device__ __forceinline__ Ring make_ring(float* smem, int width) {
   Ring r;
+  r.depth = ring_depth(width);
   r.rows = smem;
-  r.full = reinterpret_cast<uint64_t*>(smem + kRing * width);
-  r.empty = r.full + kRing;
+  r.full = reinterpret_cast<uint64_t*>(smem + r.depth * width);
+  r.empty = r.full + r.depth;
   r.width = width;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kRing; ++i) {
+    for (int i = 0; i < r.depth; ++i) {
       mbar_init(&r.full[i], 1);
       mbar_init(&r.empty[i], 1);
     }
@@ -116,7 +122,7 @@ __device__ __forceinline__ void sweep(const DevArgs& a, const Cands& cs, Lane<BB
     if (lane == 0) {
       const uint32_t bytes = static_cast<uint32_t>(ring.width * sizeof(float));
       for (int t = 0; t < n_mine; ++t) {
-        const int slot = t % kRing, round = t / kRing;
+        const int slot = t % ring.depth, round = t / ring.depth;
         if (round > 0) mbar_wait_parity(&ring.empty[slot], (round - 1) & 1);
         const float* src = cs.base + static_cast<int64_t>(__ldg(cs.idx + j_beg + t)) * a.ent_w;
         mbar_arrive_expect_tx(&ring.full[slot], bytes);
@@ -126,7 +132,7 @@ __device__ __forceinline__ void sweep(const DevArgs& a, const Cands& cs, Lane<BB
     return;
   }
   for (int t = warp; t < n_mine; t += kCWarps) {
-    const int slot = t % kRing, round = t / kRing, j = j_beg + t;
+    const int slot = t % ring.depth, round = t / ring.depth, j = j_beg + t;
     const float* row = ring.rows + slot * ring.width;
     mbar_wait_parity(&ring.full[slot], round & 1);
     float4 v[kMaxChunks];
@@ -285,83 +291,290 @@ __device__ __forceinline__ float beta_qterm(const DevArgs& a, const float* q, in
   return dg_digamma(e < D ? A : B) - dg_digamma(A + B);
 }
 
-// A (S,1,1) cluster per Loss node (S = 2..8, chosen so a pop fills the GPU):
-// the CTAs take candidate groups round-robin, then reduce-scatter their dL/dq
-// partials over DSMEM — CTA p sums dims [p*wq/S, (p+1)*wq/S) over all S
-// partials in rank order (deterministic); CTA 0 sums the loss partials.
+// Fused score + loss, persistent and streaming. Work items are (Loss node,
+// part): the S parts of a node split its candidates into contiguous ranges.
+// Each CTA walks items blockIdx.x, +gridDim.x, ...; its producer warp streams
+// the query row of every item (double-buffered) and the candidate rows of
+// every item (ring) ahead of the consumers without ever draining between
+// items, so HBM stays busy through the per-item reductions. An item's dL/dq
+// and loss partials are combined in part order by the last CTA to finish the
+// node (global partials + arrival counter: deterministic, no cluster needed).
+constexpr int kConsumerThreads = kCWarps * 32;
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerThreads) : "memory");
+}
+
+struct LossSmem {  // dynamic shared memory of loss_stream_kernel, after the ring
+  float* q[2];     // query rows of the current / next item
+  uint64_t* qfull;
+  uint64_t* qempty;
+};
+inline size_t loss_smem_bytes(int ent_w, int wq) {
+  return ring_bytes(ent_w) + 2 * static_cast<size_t>(wq) * sizeof(float) + 4 * sizeof(uint64_t);
+}
+
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kThreads, 2) loss_fwd_kernel(DevArgs a, int /*unused*/, int first, int S) {
+__global__ void __launch_bounds__(kThreads, 2) loss_stream_kernel(DevArgs a, int first, int n,
+                                                                  int S) {
   extern __shared__ __align__(128) float ring_smem[];
   __shared__ __align__(16) float parts[kCWarps][kMaxWq];
   __shared__ float lred[kLred];
-  const Ring ring = make_ring(ring_smem, a.ent_w);
+  __shared__ int last_flag;
+  __shared__ float qbias_s;
+  constexpr bool kBeta = BB == NGDB_BETAE;
+  LossSmem ls;
+  const int depth = ring_depth(a.ent_w);
+  ls.q[0] = ring_smem + depth * a.ent_w + 4 * depth;  // after rows + 2*depth barriers
+  ls.q[1] = ls.q[0] + a.wq;
+  ls.qfull = reinterpret_cast<uint64_t*>(ls.q[1] + a.wq);
+  ls.qempty = ls.qfull + 2;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&ls.qfull[i], 1);
+      mbar_init(&ls.qempty[i], 1);
+    }
+  }
+  const Ring ring = make_ring(ring_smem, a.ent_w);  // inits its barriers + fence + __syncthreads
   pdl_start();
-  const int part = blockIdx.x % S;
-  const ngdb_node_desc d = a.nodes[first + blockIdx.x / S];
-  const int qi = d.id;
-  if (d.aux < 0) {
-    // union query: the input already holds min-over-branch distances
-    if (part == 0) {
-      float loss = 0.f;
-      for (int j = threadIdx.x; j < a.ncand; j += kThreads) {
-        const float c = loss_coef(a, j, a.arena[d.in[0] + j], loss);
-        a.ddbuf[static_cast<int64_t>(qi) * a.ncand + j] = c;
-      }
-      loss = block_sum(warp_sum(loss), lred);
-      if (threadIdx.x == 0) {
-        a.loss_out[qi] = loss;
-        a.arena[d.out] = loss;
-        if (!isfinite(loss)) atomicOr(&a.flags[0], 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int n_items = S * n;
+  auto cand_index = [&](const ngdb_node_desc& d) -> const int32_t* {
+    if (kBeta || a.fused) return a.cand_local + static_cast<int64_t>(d.aux) * a.ncand;
+    return a.cand + static_cast<int64_t>(d.id) * a.ncand;
+  };
+  const float* rows_base = (kBeta || a.fused) ? a.etab : a.ent;
+
+  if (warp == kCWarps) {  // ---- producer ----
+    if (lane != 0) return;
+    const uint32_t row_bytes = static_cast<uint32_t>(a.ent_w * sizeof(float));
+    const uint32_t q_bytes = static_cast<uint32_t>(a.wq * sizeof(float));
+    int pos = 0, qi = 0;
+    for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+      const int node = t / S, part = t % S;
+      const ngdb_node_desc d = a.nodes[first + node];
+      if (d.aux < 0) continue;  // union query: no candidate rows
+      const int qs = qi & 1;
+      if (qi >= 2) mbar_wait_parity(&ls.qempty[qs], ((qi >> 1) - 1) & 1);
+      mbar_arrive_expect_tx(&ls.qfull[qs], q_bytes);
+      bulk_g2s(ls.q[qs], a.arena + d.in[0], q_bytes, &ls.qfull[qs]);
+      ++qi;
+      const int32_t* idx = cand_index(d);
+      const int j_beg = part * a.ncand / S, j_end = (part + 1) * a.ncand / S;
+      for (int j = j_beg; j < j_end; ++j, ++pos) {
+        const int slot = pos % ring.depth, round = pos / ring.depth;
+        if (round > 0) mbar_wait_parity(&ring.empty[slot], (round - 1) & 1);
+        mbar_arrive_expect_tx(&ring.full[slot], row_bytes);
+        bulk_g2s(ring.rows + slot * ring.width,
+                 rows_base + static_cast<int64_t>(__ldg(idx + j)) * a.ent_w, row_bytes,
+                 &ring.full[slot]);
       }
     }
-    cluster_sync_all();  // barrier count is uniform across both paths
-    cluster_sync_all();
     return;
   }
-  const float* q = a.arena + d.in[0];
-  if (part == 0) {
-    float* qcopy = a.qbuf + static_cast<int64_t>(d.aux) * a.wq;
-    for (int e = threadIdx.x * 4; e < a.wq; e += kThreads * 4) st4(qcopy + e, ld4(q + e));
-  }
-  Lane<BB, NCH> L;
-  L.load_q(q, a.dim, threadIdx.x & 31);
-  const Cands cs = node_cands<BB>(a, d, q, lred);
-  float loss = 0.f, csum = 0.f;  // identical in every lane of a warp
-  float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
-  const int lane = threadIdx.x & 31;
-  sweep<BB, NCH, true>(
-      a, cs, L, ring,
-      [&](int j, float dj) {
-        const float c = loss_coef(a, j, dj, loss);
-        csum += c;
-        if (lane == 0) coefs[j] = c;
-        return c;
-      },
-      part, S);
-  reduce_partials<BB, NCH>(a, L, parts, lred, loss, csum);
-  const float* red = parts[0];
-  cluster_sync_all();
-  {
-    float* dst = a.dqbuf + static_cast<int64_t>(d.aux) * a.wq;
-    const int e0 = part * a.wq / S, e1 = (part + 1) * a.wq / S;
-    float sc = 0.f;
-    if constexpr (BB == NGDB_BETAE)
-      for (int p = 0; p < S; ++p) sc += (p == part) ? lred[kCsumTot] : ld_peer(lred + kCsumTot, p);
-    for (int e = e0 + threadIdx.x; e < e1; e += kThreads) {
-      float v = 0.f;
-      for (int p = 0; p < S; ++p) v += (p == part) ? red[e] : ld_peer(red + e, p);
-      if constexpr (BB == NGDB_BETAE) v += sc * beta_qterm(a, q, e);
-      dst[e] = v;
+
+  // ---- consumers (kCWarps warps) ----
+  const int ctid = threadIdx.x;  // < kConsumerThreads
+  const int d4 = a.dim / 4;
+  int pos = 0, qi = 0;
+  for (int t = blockIdx.x; t < n_items; t += gridDim.x) {
+    const int node = t / S, part = t % S;
+    const ngdb_node_desc d = a.nodes[first + node];
+    const int qid = d.id;
+    if (d.aux < 0) {
+      // union query: the input already holds min-over-branch distances; part 0
+      // computes the whole loss, the other parts have nothing to do
+      if (part == 0) {
+        float loss = 0.f;
+        for (int j = ctid; j < a.ncand; j += kConsumerThreads) {
+          const float c = loss_coef(a, j, a.arena[d.in[0] + j], loss);
+          a.ddbuf[static_cast<int64_t>(qid) * a.ncand + j] = c;
+        }
+        loss = warp_sum(loss);
+        if (lane == 0) lred[warp] = loss;
+        consumers_sync();
+        if (ctid == 0) {
+          float total = 0.f;
+          for (int w = 0; w < kCWarps; ++w) total += lred[w];
+          a.loss_out[qid] = total;
+          a.arena[d.out] = total;
+          if (!isfinite(total)) atomicOr(&a.flags[0], 1);
+        }
+        consumers_sync();
+      }
+      continue;
     }
-    if (part == 0 && threadIdx.x == 0) {
-      float total = 0.f;
-      for (int p = 0; p < S; ++p) total += (p == 0) ? lred[kLossTot] : ld_peer(lred + kLossTot, p);
-      a.loss_out[qi] = total;
-      a.arena[d.out] = total;
-      if (!isfinite(total)) atomicOr(&a.flags[0], 1);
+    const int qs = qi & 1;
+    mbar_wait_parity(&ls.qfull[qs], (qi >> 1) & 1);
+    const float* q = ls.q[qs];
+    Lane<BB, NCH> L;
+    L.load_q(q, a.dim, lane);
+    if (part == 0) {
+      float* qcopy = a.qbuf + static_cast<int64_t>(d.aux) * a.wq;
+      for (int e = ctid * 4; e < a.wq; e += kConsumerThreads * 4) st4(qcopy + e, ld4(q + e));
     }
+    float qbias = 0.f;
+    if constexpr (kBeta) {  // lnB(query) summed over the dims
+      float tq = 0.f;
+      for (int e = ctid; e < a.dim; e += kConsumerThreads) tq += dg_lbeta(q[e], q[a.dim + e]);
+      tq = warp_sum(tq);
+      if (lane == 0) lred[warp] = tq;
+      consumers_sync();
+      if (ctid == 0) {
+        float tt = 0.f;
+        for (int w = 0; w < kCWarps; ++w) tt += lred[w];
+        qbias_s = tt;
+      }
+      consumers_sync();
+      qbias = qbias_s;
+    }
+    const int32_t* idx = cand_index(d);
+    const int j_beg = part * a.ncand / S, j_end = (part + 1) * a.ncand / S;
+    const int n_mine = j_end - j_beg;
+    float* coefs = a.coefbuf + static_cast<int64_t>(d.aux) * a.ncand;
+    float loss = 0.f, csum = 0.f;  // identical in every lane of a warp
+    for (int u = warp; u < n_mine; u += kCWarps) {
+      const int p = pos + u, slot = p % ring.depth, j = j_beg + u;
+      const float* row = ring.rows + slot * ring.width;
+      mbar_wait_parity(&ring.full[slot], (p / ring.depth) & 1);
+      float4 v[NCH];
+      float4 v2[kBeta ? NCH : 1];
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int c = lane + 32 * i;
+        if (i < L.nch && c < d4) {
+          v[i] = ld4(row + 4 * c);
+          if constexpr (kBeta) v2[i] = ld4(row + a.dim + 4 * c);
+        } else {
+          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (kBeta) v2[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring.empty[slot]);
+      float sx = 0.f, sy = 0.f, sz = 0.f, sw = 0.f;
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int c = lane + 32 * i;
+        if (i < L.nch && c < d4) {
+          if constexpr (kBeta) {
+            sx += Dist<BB>::term(v[i].x, v2[i].x, L.qc[i].x, L.qo[i].x);
+            sy += Dist<BB>::term(v[i].y, v2[i].y, L.qc[i].y, L.qo[i].y);
+            sz += Dist<BB>::term(v[i].z, v2[i].z, L.qc[i].z, L.qo[i].z);
+            sw += Dist<BB>::term(v[i].w, v2[i].w, L.qc[i].w, L.qo[i].w);
+          } else {
+            sx += Dist<BB>::term(v[i].x, L.qc[i].x, L.qo[i].x, a.alpha_box);
+            sy += Dist<BB>::term(v[i].y, L.qc[i].y, L.qo[i].y, a.alpha_box);
+            sz += Dist<BB>::term(v[i].z, L.qc[i].z, L.qo[i].z, a.alpha_box);
+            sw += Dist<BB>::term(v[i].w, L.qc[i].w, L.qo[i].w, a.alpha_box);
+          }
+        }
+      }
+      float dj = warp_sum((sx + sy) + (sz + sw));
+      if constexpr (kBeta) dj += qbias + __ldg(a.etab_c + __ldg(idx + j));
+      const float coef = loss_coef(a, j, dj, loss);
+      csum += coef;
+      if (lane == 0) coefs[j] = coef;
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int c = lane + 32 * i;
+        if (i < L.nch && c < d4) {
+          if constexpr (kBeta) {
+            L.gc[i].x += coef * v[i].x; L.go[i].x += coef * v2[i].x;
+            L.gc[i].y += coef * v[i].y; L.go[i].y += coef * v2[i].y;
+            L.gc[i].z += coef * v[i].z; L.go[i].z += coef * v2[i].z;
+            L.gc[i].w += coef * v[i].w; L.go[i].w += coef * v2[i].w;
+          } else {
+            Dist<BB>::grad(v[i].x, L.qc[i].x, L.qo[i].x, coef, a.alpha_box, L.gc[i].x, L.go[i].x);
+            Dist<BB>::grad(v[i].y, L.qc[i].y, L.qo[i].y, coef, a.alpha_box, L.gc[i].y, L.go[i].y);
+            Dist<BB>::grad(v[i].z, L.qc[i].z, L.qo[i].z, coef, a.alpha_box, L.gc[i].z, L.go[i].z);
+            Dist<BB>::grad(v[i].w, L.qc[i].w, L.qo[i].w, coef, a.alpha_box, L.gc[i].w, L.go[i].w);
+          }
+        }
+      }
+    }
+    pos += n_mine;
+    // cross-warp partials (consumer threads only): every warp stores its
+    // row, one consumer barrier, then the rows are summed in warp order
+    if (lane == 0) {
+      lred[2 * warp] = loss;
+      lred[2 * warp + 1] = csum;
+    }
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      if (i < L.nch && c < d4) {
+        st4(parts[warp] + 4 * c, L.gc[i]);
+        if (BB != NGDB_GQE) st4(parts[warp] + a.dim + 4 * c, L.go[i]);
+      }
+    }
+    consumers_sync();
+    if (ctid == 0) mbar_arrive(&ls.qempty[qs]);  // every consumer is done with q
+    ++qi;
+    float* dst = S == 1 ? a.dqbuf + static_cast<int64_t>(d.aux) * a.wq
+                        : a.lpart + static_cast<int64_t>(t) * a.wq;
+    for (int e = ctid * 4; e < a.wq; e += kConsumerThreads * 4) {
+      float4 s4 = ld4(parts[0] + e);
+#pragma unroll
+      for (int w = 1; w < kCWarps; ++w) {
+        const float4 u4 = ld4(parts[w] + e);
+        s4.x += u4.x; s4.y += u4.y; s4.z += u4.z; s4.w += u4.w;
+      }
+      st4(dst + e, s4);
+    }
+    float l_item = 0.f, c_item = 0.f;
+    if (ctid == 0)
+      for (int w = 0; w < kCWarps; ++w) {
+        l_item += lred[2 * w];
+        c_item += lred[2 * w + 1];
+      }
+    if (S > 1) {
+      if (ctid == 0) {
+        a.lpart_scalar[2 * t] = l_item;
+        a.lpart_scalar[2 * t + 1] = c_item;
+      }
+      __threadfence();
+      consumers_sync();
+      if (ctid == 0) last_flag = atomicAdd(&a.lcount[node], 1) == S - 1;
+      consumers_sync();
+      if (!last_flag) continue;
+      __threadfence();  // the other parts' partials are visible
+      // the last part of the node combines all S partials in part order
+      float* out = a.dqbuf + static_cast<int64_t>(d.aux) * a.wq;
+      const float* base = a.lpart + static_cast<int64_t>(node) * S * a.wq;
+      for (int e = ctid * 4; e < a.wq; e += kConsumerThreads * 4) {
+        float4 s4 = ld4(base + e);
+        for (int p2 = 1; p2 < S; ++p2) {
+          const float4 u4 = ld4(base + static_cast<int64_t>(p2) * a.wq + e);
+          s4.x += u4.x; s4.y += u4.y; s4.z += u4.z; s4.w += u4.w;
+        }
+        st4(out + e, s4);
+      }
+      if (ctid == 0) {
+        l_item = c_item = 0.f;
+        for (int p2 = 0; p2 < S; ++p2) {
+          l_item += a.lpart_scalar[2 * (node * S + p2)];
+          c_item += a.lpart_scalar[2 * (node * S + p2) + 1];
+        }
+        a.lcount[node] = 0;  // ready for the next launch
+      }
+    }
+    if constexpr (kBeta) {
+      // dL/dq += (sum_j coef_j) [psi(A)-psi(A+B) | psi(B)-psi(A+B)] (query term)
+      consumers_sync();
+      if (ctid == 0) qbias_s = c_item;
+      consumers_sync();
+      const float sc = qbias_s;
+      float* out = a.dqbuf + static_cast<int64_t>(d.aux) * a.wq;
+      const float* qq = a.arena + d.in[0];
+      for (int e = ctid; e < a.wq; e += kConsumerThreads) out[e] += sc * beta_qterm(a, qq, e);
+    }
+    if (ctid == 0) {
+      a.loss_out[qid] = l_item;
+      a.arena[d.out] = l_item;
+      if (!isfinite(l_item)) atomicOr(&a.flags[0], 1);
+    }
+    consumers_sync();  // parts[] / lred reused by the next item
   }
-  cluster_sync_all();  // partial tiles stay resident until every slice was read
 }
 
 // Union branch Score, a (S,1,1) cluster per node like the Loss kernel: fwd
@@ -480,9 +693,26 @@ void launch_ring_kernel(K kernel, int ent_w, int n, cudaStream_t s, const DevArg
 
 template <int NCH>
 void launch_loss_nch(const DevArgs& a, int first, int n, cudaStream_t s) {
-  if (a.backbone == NGDB_GQE) launch_ring_kernel(loss_fwd_kernel<NGDB_GQE, NCH>, a.ent_w, n, s, a, first, first);
-  else if (a.backbone == NGDB_BETAE) launch_ring_kernel(loss_fwd_kernel<NGDB_BETAE, NCH>, a.ent_w, n, s, a, first, first);
-  else launch_ring_kernel(loss_fwd_kernel<NGDB_Q2B, NCH>, a.ent_w, n, s, a, first, first);
+  auto go = [&](auto kernel) {
+    const size_t smem = loss_smem_bytes(a.ent_w, a.wq);
+    static std::map<std::pair<const void*, size_t>, int> cache;  // -> resident CTAs
+    int& resident = cache[{reinterpret_cast<const void*>(kernel), smem}];
+    if (!resident) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+      resident = std::max(1, per_sm) * 148;
+    }
+    // parts per node: enough items for every resident CTA, within the
+    // partial-buffer capacity (a.lpart_items)
+    int S = std::max(1, std::min(8, (resident + n - 1) / n));
+    while (S > 1 && S * n > a.lpart_items) --S;
+    const int grid = std::min(resident, S * n);
+    launch_pdl(kernel, dim3(grid), dim3(kThreads), smem, s, 1, a, first, n, S);
+  };
+  if (a.backbone == NGDB_GQE) go(loss_stream_kernel<NGDB_GQE, NCH>);
+  else if (a.backbone == NGDB_BETAE) go(loss_stream_kernel<NGDB_BETAE, NCH>);
+  else go(loss_stream_kernel<NGDB_Q2B, NCH>);
 }
 template <int NCH>
 void launch_score_nch(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
