@@ -673,18 +673,27 @@ inline int parts_for(int n, const RingGeom& g) {
   return std::max(std::min(2, g.max_cluster), std::min(g.max_cluster, g.resident / std::max(n, 1)));
 }
 
+// A kernel's max-dynamic-smem attribute must cover every launch, and cluster
+// launches are validated against the attribute itself: keep it equal to the
+// size of the launch at hand (set only when it changes).
 template <class K>
-void launch_ring_kernel(K kernel, int ent_w, int n, cudaStream_t s, const DevArgs& a, int x,
-                        int first) {
-  const size_t smem = ring_bytes(ent_w);
-  static std::map<const void*, size_t> attr;                         // kernel -> attribute set
-  static std::map<std::pair<const void*, size_t>, RingGeom> cache;  // (kernel, smem) -> geometry
+void ensure_smem_attr(K kernel, size_t smem) {
+  static std::map<const void*, size_t> attr;  // kernel -> value last set
   const void* key = reinterpret_cast<const void*>(kernel);
   auto it = attr.find(key);
   if (it == attr.end() || it->second != smem) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr[key] = smem;
   }
+}
+
+template <class K>
+void launch_ring_kernel(K kernel, int ent_w, int n, cudaStream_t s, const DevArgs& a, int x,
+                        int first) {
+  const size_t smem = ring_bytes(ent_w);
+  static std::map<std::pair<const void*, size_t>, RingGeom> cache;  // (kernel, smem) -> geometry
+  const void* key = reinterpret_cast<const void*>(kernel);
+  ensure_smem_attr(kernel, smem);
   RingGeom& g = cache[{key, smem}];
   if (!g.resident) g = ring_geometry(kernel, smem, 148);
   const int S = parts_for(n, g);
@@ -697,8 +706,8 @@ void launch_loss_nch(const DevArgs& a, int first, int n, cudaStream_t s) {
     const size_t smem = loss_smem_bytes(a.ent_w, a.wq);
     static std::map<std::pair<const void*, size_t>, int> cache;  // -> resident CTAs
     int& resident = cache[{reinterpret_cast<const void*>(kernel), smem}];
+    ensure_smem_attr(kernel, smem);
     if (!resident) {
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
       resident = std::max(1, per_sm) * 148;
