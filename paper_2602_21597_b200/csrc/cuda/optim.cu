@@ -95,19 +95,22 @@ __global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a,
   const int r_beg = blockIdx.x * rows_per_cta;
   const int n_mine = max(0, min(t.n_rows, r_beg + rows_per_cta) - r_beg);
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  if (warp == kAdamConsumers) {  // producer
-    if (lane == 0) {
-      const uint32_t bytes = static_cast<uint32_t>(W * sizeof(float));
-      for (int u = 0; u < n_mine; ++u) {
+  if (warp == kAdamConsumers) {  // producer warp: lane r issues row r of each group
+    constexpr int kGroup = kAdamRing;
+    const uint32_t bytes = static_cast<uint32_t>(W * sizeof(float));
+    for (int u0 = 0; u0 < n_mine; u0 += kGroup) {
+      const int u = u0 + lane;
+      if (lane < kGroup && u < n_mine) {
         const int slot = u % kAdamRing, round = u / kAdamRing;
-        if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
         const int64_t row = __ldg(t.rows + r_beg + u);
+        if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
         float* dst = ring + slot * 3 * W;
         mbar_arrive_expect_tx(&full[slot], 3 * bytes);
         bulk_g2s(dst, t.w + row * W, bytes, &full[slot]);
         bulk_g2s(dst + W, t.m + row * W, bytes, &full[slot]);
         bulk_g2s(dst + 2 * W, t.v + row * W, bytes, &full[slot]);
       }
+      __syncwarp();
     }
     return;
   }

@@ -208,8 +208,12 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(DevArgs a, int firs
   const float* rows_base = rows_local ? a.etab : a.ent;
   const int D = a.dim;
 
-  if (warp == kCWarps) {  // ---- producer ----
-    if (lane != 0) return;
+  if (warp == kCWarps) {  // ---- producer warp ----
+    // lane r issues row r of every 16-row group: the candidate-index loads of
+    // a group are one coalesced load instead of a serial chain of round trips
+    // a group never exceeds the ring depth, so a lane only ever waits for a
+    // slot freed from an earlier group
+    const int kGroup = L.depth < 16 ? L.depth : 16;
     const uint32_t half_bytes = static_cast<uint32_t>(D * sizeof(float));
     const int q_halves = a.wq / D;
     int pos = 0, qi = 0;
@@ -218,23 +222,31 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(DevArgs a, int firs
       const ngdb_node_desc d = a.nodes[first + node];
       if (MODE == kLoss && d.aux < 0) continue;  // union query: no candidate rows
       const int qs = qi & 1;
-      if (qi >= 2) mbar_wait_parity(&qempty[qs], ((qi >> 1) - 1) & 1);
-      float* qdst = qs ? qbuf1 : qbuf0;
-      mbar_arrive_expect_tx(&qfull[qs], q_halves * half_bytes);
-      for (int h = 0; h < q_halves; ++h)
-        bulk_g2s(qdst + h * HP, a.arena + d.in[0] + h * D, half_bytes, &qfull[qs]);
+      if (lane == 0) {
+        if (qi >= 2) mbar_wait_parity(&qempty[qs], ((qi >> 1) - 1) & 1);
+        float* qdst = qs ? qbuf1 : qbuf0;
+        mbar_arrive_expect_tx(&qfull[qs], q_halves * half_bytes);
+        for (int h = 0; h < q_halves; ++h)
+          bulk_g2s(qdst + h * HP, a.arena + d.in[0] + h * D, half_bytes, &qfull[qs]);
+      }
       ++qi;
       const int32_t* idx = rows_local ? a.cand_local + static_cast<int64_t>(d.aux) * a.ncand
                                       : a.cand + static_cast<int64_t>(d.id) * a.ncand;
       const int j_beg = part * a.ncand / S, j_end = (part + 1) * a.ncand / S;
-      for (int j = j_beg; j < j_end; ++j, ++pos) {
-        const int slot = pos % L.depth, round = pos / L.depth;
-        if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
-        const float* src = rows_base + static_cast<int64_t>(__ldg(idx + j)) * a.ent_w;
-        mbar_arrive_expect_tx(&full[slot], L.halves * half_bytes);
-        for (int h = 0; h < L.halves; ++h)
-          bulk_g2s(rows + slot * RW + h * HP, src + h * D, half_bytes, &full[slot]);
+      for (int j0 = j_beg; j0 < j_end; j0 += kGroup) {
+        const int j = j0 + lane;
+        if (lane < kGroup && j < j_end) {
+          const int p = pos + (j - j_beg);
+          const int slot = p % L.depth, round = p / L.depth;
+          const float* src = rows_base + static_cast<int64_t>(__ldg(idx + j)) * a.ent_w;
+          if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
+          mbar_arrive_expect_tx(&full[slot], L.halves * half_bytes);
+          for (int h = 0; h < L.halves; ++h)
+            bulk_g2s(rows + slot * RW + h * HP, src + h * D, half_bytes, &full[slot]);
+        }
+        __syncwarp();
       }
+      pos += j_end - j_beg;
     }
     return;
   }
