@@ -68,7 +68,7 @@ __device__ __forceinline__ float cand_grad(float v, float qc, float qo, float co
 // registers and theta, m, v are stored straight back to HBM.
 constexpr int kAdamConsumers = 8;
 constexpr int kAdamThreads = 32 * (kAdamConsumers + 1);
-constexpr int kAdamRing = 8;
+constexpr int kAdamRing = 8;  // a multiple of kAdamConsumers (see the score ring)
 
 inline size_t adam_smem_bytes(int width) {
   return static_cast<size_t>(kAdamRing) * 3 * width * sizeof(float) + 2 * kAdamRing * sizeof(uint64_t);
@@ -95,22 +95,25 @@ __global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a,
   const int r_beg = blockIdx.x * rows_per_cta;
   const int n_mine = max(0, min(t.n_rows, r_beg + rows_per_cta) - r_beg);
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  if (warp == kAdamConsumers) {  // producer warp: lane r issues row r of each group
-    constexpr int kGroup = kAdamRing;
+  if (warp == kAdamConsumers) {  // producer warp: row ids 32 at a time, lane 0 issues
     const uint32_t bytes = static_cast<uint32_t>(W * sizeof(float));
-    for (int u0 = 0; u0 < n_mine; u0 += kGroup) {
-      const int u = u0 + lane;
-      if (lane < kGroup && u < n_mine) {
-        const int slot = u % kAdamRing, round = u / kAdamRing;
-        const int64_t row = __ldg(t.rows + r_beg + u);
-        if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
-        float* dst = ring + slot * 3 * W;
-        mbar_arrive_expect_tx(&full[slot], 3 * bytes);
-        bulk_g2s(dst, t.w + row * W, bytes, &full[slot]);
-        bulk_g2s(dst + W, t.m + row * W, bytes, &full[slot]);
-        bulk_g2s(dst + 2 * W, t.v + row * W, bytes, &full[slot]);
+    for (int u0 = 0; u0 < n_mine; u0 += 32) {
+      const int64_t my_row = u0 + lane < n_mine ? __ldg(t.rows + r_beg + u0 + lane) : 0;
+      const int cnt = min(32, n_mine - u0);
+      for (int r = 0; r < cnt; ++r) {
+        const int64_t row = __shfl_sync(0xffffffffu, my_row, r);
+        if (lane == 0) {
+          const int u = u0 + r;
+          const int slot = u % kAdamRing, round = u / kAdamRing;
+          if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
+          float* dst = ring + slot * 3 * W;
+          mbar_arrive_expect_tx(&full[slot], 3 * bytes);
+          bulk_g2s(dst, t.w + row * W, bytes, &full[slot]);
+          bulk_g2s(dst + W, t.m + row * W, bytes, &full[slot]);
+          bulk_g2s(dst + 2 * W, t.v + row * W, bytes, &full[slot]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
     return;
   }

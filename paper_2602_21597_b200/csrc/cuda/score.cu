@@ -57,10 +57,13 @@ template <int NCH>
 struct Layout {
   static constexpr int HP = 128 * NCH;  // floats per padded half
   int halves, depth;
+  // depth is a multiple of kCWarps: slot s is then always consumed by warp
+  // s % kCWarps, in order, so no consumer ever waits on a slot two phases
+  // ahead of its last completion (mbarrier parity waits see one phase back)
   __host__ __device__ explicit Layout(int backbone) {
     halves = backbone == NGDB_BETAE ? 2 : 1;
-    const int d = 49152 / (halves * HP * 4);
-    depth = d < 8 ? 8 : (d > 32 ? 32 : d);
+    const int d = 49152 / (halves * HP * 4) / kCWarps * kCWarps;
+    depth = d < kCWarps ? kCWarps : (d > 32 ? 32 : d);
   }
   __host__ __device__ int row_floats() const { return halves * HP; }
   // ring rows, two query slots, kCWarps partial rows of dL/dq (two halves)
@@ -209,11 +212,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(DevArgs a, int firs
   const int D = a.dim;
 
   if (warp == kCWarps) {  // ---- producer warp ----
-    // lane r issues row r of every 16-row group: the candidate-index loads of
-    // a group are one coalesced load instead of a serial chain of round trips
-    // a group never exceeds the ring depth, so a lane only ever waits for a
-    // slot freed from an earlier group
-    const int kGroup = L.depth < 16 ? L.depth : 16;
+    // the warp loads the candidate indices of 32 rows at a time (one coalesced
+    // load instead of a serial chain of round trips); lane 0 issues the copies
     const uint32_t half_bytes = static_cast<uint32_t>(D * sizeof(float));
     const int q_halves = a.wq / D;
     int pos = 0, qi = 0;
@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(DevArgs a, int firs
       const int node = t / S, part = t % S;
       const ngdb_node_desc d = a.nodes[first + node];
       if (MODE == kLoss && d.aux < 0) continue;  // union query: no candidate rows
-      const int qs = qi & 1;
       if (lane == 0) {
+        const int qs = qi & 1;
         if (qi >= 2) mbar_wait_parity(&qempty[qs], ((qi >> 1) - 1) & 1);
         float* qdst = qs ? qbuf1 : qbuf0;
         mbar_arrive_expect_tx(&qfull[qs], q_halves * half_bytes);
@@ -233,20 +233,22 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(DevArgs a, int firs
       const int32_t* idx = rows_local ? a.cand_local + static_cast<int64_t>(d.aux) * a.ncand
                                       : a.cand + static_cast<int64_t>(d.id) * a.ncand;
       const int j_beg = part * a.ncand / S, j_end = (part + 1) * a.ncand / S;
-      for (int j0 = j_beg; j0 < j_end; j0 += kGroup) {
-        const int j = j0 + lane;
-        if (lane < kGroup && j < j_end) {
-          const int p = pos + (j - j_beg);
-          const int slot = p % L.depth, round = p / L.depth;
-          const float* src = rows_base + static_cast<int64_t>(__ldg(idx + j)) * a.ent_w;
-          if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
-          mbar_arrive_expect_tx(&full[slot], L.halves * half_bytes);
-          for (int h = 0; h < L.halves; ++h)
-            bulk_g2s(rows + slot * RW + h * HP, src + h * D, half_bytes, &full[slot]);
+      for (int j0 = j_beg; j0 < j_end; j0 += 32) {
+        const int32_t my_idx = j0 + lane < j_end ? __ldg(idx + j0 + lane) : 0;
+        const int cnt = min(32, j_end - j0);
+        for (int r = 0; r < cnt; ++r, ++pos) {
+          const int32_t row_id = __shfl_sync(0xffffffffu, my_idx, r);
+          if (lane == 0) {
+            const int slot = pos % L.depth, round = pos / L.depth;
+            if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
+            const float* src = rows_base + static_cast<int64_t>(row_id) * a.ent_w;
+            mbar_arrive_expect_tx(&full[slot], L.halves * half_bytes);
+            for (int h = 0; h < L.halves; ++h)
+              bulk_g2s(rows + slot * RW + h * HP, src + h * D, half_bytes, &full[slot]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
-      pos += j_end - j_beg;
     }
     return;
   }
