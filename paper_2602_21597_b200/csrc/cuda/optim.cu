@@ -95,15 +95,17 @@ __global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a,
   const int r_beg = blockIdx.x * rows_per_cta;
   const int n_mine = max(0, min(t.n_rows, r_beg + rows_per_cta) - r_beg);
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  if (warp == kAdamConsumers) {  // producer warp: row ids 32 at a time, lane 0 issues
+  if (warp == kAdamConsumers) {  // producer warp: row ids staged 32 at a time, lane 0 issues
+    __shared__ int32_t rows_s[32];
     const uint32_t bytes = static_cast<uint32_t>(W * sizeof(float));
     for (int u0 = 0; u0 < n_mine; u0 += 32) {
-      const int64_t my_row = u0 + lane < n_mine ? __ldg(t.rows + r_beg + u0 + lane) : 0;
+      if (u0 + lane < n_mine) rows_s[lane] = __ldg(t.rows + r_beg + u0 + lane);
+      __syncwarp();
       const int cnt = min(32, n_mine - u0);
-      for (int r = 0; r < cnt; ++r) {
-        const int64_t row = __shfl_sync(0xffffffffu, my_row, r);
-        if (lane == 0) {
+      if (lane == 0)
+        for (int r = 0; r < cnt; ++r) {
           const int u = u0 + r;
+          const int64_t row = rows_s[r];
           const int slot = u % kAdamRing, round = u / kAdamRing;
           if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
           float* dst = ring + slot * 3 * W;
@@ -112,8 +114,7 @@ __global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a,
           bulk_g2s(dst + W, t.m + row * W, bytes, &full[slot]);
           bulk_g2s(dst + 2 * W, t.v + row * W, bytes, &full[slot]);
         }
-        __syncwarp();
-      }
+      __syncwarp();  // rows_s is reused by the next chunk
     }
     return;
   }

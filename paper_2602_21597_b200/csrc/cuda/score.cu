@@ -212,8 +212,10 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(DevArgs a, int firs
   const int D = a.dim;
 
   if (warp == kCWarps) {  // ---- producer warp ----
-    // the warp loads the candidate indices of 32 rows at a time (one coalesced
-    // load instead of a serial chain of round trips); lane 0 issues the copies
+    // the warp stages the candidate indices of 32 rows at a time in shared
+    // memory (one coalesced load instead of a serial chain of round trips);
+    // lane 0 issues the copies
+    __shared__ int32_t idx_s[32];
     const uint32_t half_bytes = static_cast<uint32_t>(D * sizeof(float));
     const int q_halves = a.wq / D;
     int pos = 0, qi = 0;
@@ -234,20 +236,21 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(DevArgs a, int firs
                                       : a.cand + static_cast<int64_t>(d.id) * a.ncand;
       const int j_beg = part * a.ncand / S, j_end = (part + 1) * a.ncand / S;
       for (int j0 = j_beg; j0 < j_end; j0 += 32) {
-        const int32_t my_idx = j0 + lane < j_end ? __ldg(idx + j0 + lane) : 0;
+        if (j0 + lane < j_end) idx_s[lane] = __ldg(idx + j0 + lane);
+        __syncwarp();
         const int cnt = min(32, j_end - j0);
-        for (int r = 0; r < cnt; ++r, ++pos) {
-          const int32_t row_id = __shfl_sync(0xffffffffu, my_idx, r);
-          if (lane == 0) {
-            const int slot = pos % L.depth, round = pos / L.depth;
+        if (lane == 0)
+          for (int r = 0; r < cnt; ++r) {
+            const int p = pos + r;
+            const int slot = p % L.depth, round = p / L.depth;
             if (round > 0) mbar_wait_parity(&empty[slot], (round - 1) & 1);
-            const float* src = rows_base + static_cast<int64_t>(row_id) * a.ent_w;
+            const float* src = rows_base + static_cast<int64_t>(idx_s[r]) * a.ent_w;
             mbar_arrive_expect_tx(&full[slot], L.halves * half_bytes);
             for (int h = 0; h < L.halves; ++h)
               bulk_g2s(rows + slot * RW + h * HP, src + h * D, half_bytes, &full[slot]);
           }
-          __syncwarp();
-        }
+        pos += cnt;
+        __syncwarp();  // idx_s is reused by the next chunk
       }
     }
     return;
