@@ -155,7 +155,7 @@ __global__ void beta_proj_pack_kernel(DevArgs a, int first, float* X, Split Xs) 
   if (!ok && threadIdx.x == 0) atomicOr(&a.flags[1], 1);
   const float* q = a.arena + d.in[0];
   const float* r = a.rel + static_cast<int64_t>(ok ? d.id : 0) * a.rel_w;
-  for (int e = threadIdx.x; e < 3 * D; e += blockDim.x)
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < 3 * D; e += blockDim.x * gridDim.y)
     put(X, Xs, static_cast<int64_t>(i) * 3 * D + e, e < 2 * D ? q[e] : r[e - 2 * D]);
 }
 __global__ void beta_proj_out_kernel(DevArgs a, int first, const float* Z) {
@@ -163,7 +163,7 @@ __global__ void beta_proj_out_kernel(DevArgs a, int first, const float* Z) {
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
   const int W = 2 * a.dim;
-  for (int e = threadIdx.x; e < W; e += blockDim.x)
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y)
     a.arena[d.out + e] = beta_realize(Z[static_cast<int64_t>(i) * W + e]);
 }
 __global__ void beta_proj_gz_kernel(DevArgs a, int first, const float* Z, float* gZ, Split gZs) {
@@ -171,7 +171,7 @@ __global__ void beta_proj_gz_kernel(DevArgs a, int first, const float* Z, float*
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
   const int W = 2 * a.dim;
-  for (int e = threadIdx.x; e < W; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y) {
     const int64_t o = static_cast<int64_t>(i) * W + e;
     put(gZ, gZs, o, a.arena[d.grad + e] * beta_drealize(Z[o]));
   }
@@ -182,7 +182,7 @@ __global__ void beta_proj_scatter_kernel(DevArgs a, int first, const float* gX) 
   const ngdb_node_desc d = a.nodes[first + i];
   const int D = a.dim;
   const float* g = gX + static_cast<int64_t>(i) * 3 * D;
-  for (int e = threadIdx.x; e < 3 * D; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < 3 * D; e += blockDim.x * gridDim.y) {
     if (e < 2 * D) a.arena[d.out + e] = g[e];
     else a.rgbuf[static_cast<int64_t>(d.aux) * a.rel_w + (e - 2 * D)] = g[e];
   }
@@ -199,7 +199,7 @@ int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
   float* Z = sc.take((int64_t)n * D2);
   const float* p = a.dense;
   int launches = 0;
-  launch_pdl(beta_proj_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, first, X, Xs);
+  launch_pdl(beta_proj_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, X, Xs);
   ++launches;
   TcGemmArgs h = gemm_args(n, D2, D3, op(Xs, D3), wop(a, BETA_P1, D2, D3, false), H, D2);
   h.bias = p + a.dense_off[BETA_P1B];
@@ -209,7 +209,7 @@ int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
   z.bias = p + a.dense_off[BETA_P2B];
   launches += tc_gemm(z, s);
   if (dir == 0) {
-    launch_pdl(beta_proj_out_kernel, dim3(n), dim3(128), 0, s, 1, a, first, (const float*)Z);
+    launch_pdl(beta_proj_out_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, (const float*)Z);
     return launches + 1;
   }
   float* gZ = sc.take((int64_t)n * D2);
@@ -221,7 +221,7 @@ int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
   float* gX = sc.take((int64_t)n * D3);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
-  launch_pdl(beta_proj_gz_kernel, dim3(n), dim3(128), 0, s, 1, a, first, (const float*)Z, gZ, gZs);
+  launch_pdl(beta_proj_gz_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, (const float*)Z, gZ, gZs);
   ++launches;
   // gH = (gZ W2) * (H > 0)
   TcGemmArgs gh = gemm_args(n, D2, D2, op(gZs, D2), wop(a, BETA_P2, D2, D2, true), gH, D2);
@@ -247,7 +247,7 @@ int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
   cj.job[1] = {gH, n, D2, g + off[BETA_P1B]};
   cj.n = 2;
   launches += colsums(cj, D2, s);
-  launch_pdl(beta_proj_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, first, (const float*)gX);
+  launch_pdl(beta_proj_scatter_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, (const float*)gX);
   return launches + 1;
 }
 
@@ -259,7 +259,7 @@ __global__ void beta_inter_pack_kernel(DevArgs a, KSpan ks, int first, float* Q,
   const ngdb_node_desc d = a.nodes[first + i];
   const int W = 2 * a.dim;
   for (int l = 0; l < k; ++l)
-    for (int e = threadIdx.x; e < W; e += blockDim.x)
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y)
       put(Q, Qs, (static_cast<int64_t>(r0) + l) * W + e, a.arena[d.in[l] + e]);
 }
 __device__ __forceinline__ void softmax3(const float* S, int64_t base, int k, int D, int e, float* w) {
@@ -279,7 +279,7 @@ __global__ void beta_inter_combine_kernel(DevArgs a, KSpan ks, int first, const 
   const int D = a.dim, W = 2 * D;
   const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
-  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
     float w[3];
     softmax3(S, static_cast<int64_t>(r0) * D, k, D, e, w);
     float al = 0.f, be = 0.f;
@@ -299,7 +299,7 @@ __global__ void beta_inter_combine_bwd_kernel(DevArgs a, KSpan ks, int first, co
   const int D = a.dim, W = 2 * D;
   const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
-  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
     const float gA = a.arena[d.grad + e], gB = a.arena[d.grad + D + e];
     float w[3], gw[3], dot = 0.f;
     softmax3(S, static_cast<int64_t>(r0) * D, k, D, e, w);
@@ -323,7 +323,7 @@ __global__ void beta_inter_scatter_kernel(DevArgs a, KSpan ks, int first, const 
   const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
-    for (int e = threadIdx.x; e < W; e += blockDim.x)
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y)
       a.arena[d.out + l * W + e] = dQ[(static_cast<int64_t>(r0) + l) * W + e];
 }
 
@@ -338,7 +338,7 @@ int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaSt
   float* S = sc.take((int64_t)R * D);
   const float* p = a.dense;
   int launches = 0;
-  launch_pdl(beta_inter_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, Q, Qs);
+  launch_pdl(beta_inter_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Q, Qs);
   ++launches;
   TcGemmArgs z = gemm_args(R, W, W, op(Qs, W), wop(a, BETA_A1, W, W, false), Z, W);
   z.bias = p + a.dense_off[BETA_A1B];
@@ -348,7 +348,7 @@ int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaSt
   sg.bias = p + a.dense_off[BETA_A2B];
   launches += tc_gemm(sg, s);
   if (dir == 0) {
-    launch_pdl(beta_inter_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, (const float*)S,
+    launch_pdl(beta_inter_combine_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, (const float*)S,
                (const float*)Q);
     return launches + 1;
   }
@@ -361,7 +361,7 @@ int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaSt
         gZT = take_split(sc, (int64_t)RP * W), QT = take_split(sc, (int64_t)RP * W);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
-  launch_pdl(beta_inter_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first,
+  launch_pdl(beta_inter_combine_bwd_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first,
              (const float*)S, (const float*)Q, gS, gSs, dQ);
   ++launches;
   // gZ = (gS A2) * (Z > 0)
@@ -389,7 +389,7 @@ int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaSt
   cj.job[1] = {gZ, R, W, g + off[BETA_A1B]};
   cj.n = 2;
   launches += colsums(cj, W, s);
-  launch_pdl(beta_inter_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, (const float*)dQ);
+  launch_pdl(beta_inter_scatter_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, (const float*)dQ);
   return launches + 1;
 }
 

@@ -59,7 +59,7 @@ __global__ void gqe_pack_kernel(DevArgs a, KSpan ks, int first, float* M, Split 
   const int k = ks.k(i);
   const ngdb_node_desc d = a.nodes[first + i];
   const float inv_k = 1.f / static_cast<float>(k);
-  for (int e = threadIdx.x; e < a.dim; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < a.dim; e += blockDim.x * gridDim.y) {
     float s = 0.f;
     for (int l = 0; l < k; ++l) s += a.arena[d.in[l] + e];
     const int64_t o = (int64_t)i * a.dim + e;
@@ -74,7 +74,7 @@ __global__ void gqe_scatter_kernel(DevArgs a, KSpan ks, int first, const float* 
   const int k = ks.k(i);
   const ngdb_node_desc d = a.nodes[first + i];
   const float inv_k = 1.f / static_cast<float>(k);
-  for (int e = threadIdx.x; e < a.dim; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < a.dim; e += blockDim.x * gridDim.y) {
     const float v = dM[(int64_t)i * a.dim + e] * inv_k;
     for (int l = 0; l < k; ++l) a.arena[d.out + l * a.dim + e] = v;
   }
@@ -94,7 +94,7 @@ int gqe_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   Split Gs = dir ? take_split(sc, nd) : Split{nullptr, nullptr};
   int launches = 0;
 
-  launch_pdl(gqe_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, M, Ms, G, Gs);
+  launch_pdl(gqe_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, M, Ms, G, Gs);
   ++launches;
   TcGemmArgs h = gemm_args(n, D, D, op(Ms, D), wop(a, GQE_W1, D, D, false), H, D);
   h.s_hi = RHs.hi; h.s_lo = RHs.lo; h.s_relu = 1;
@@ -132,7 +132,7 @@ int gqe_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   lvl[1].accumulate = 1;
   lvl[2] = gemm_args(n, D, D, op(dHs, D), wop(a, GQE_W1, D, D, true), dM, D);  // dM = dH W1
   launches += tc_gemm_batch(lvl, 3, s);
-  launch_pdl(gqe_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, dM);
+  launch_pdl(gqe_scatter_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, dM);
   return launches + 1;
 }
 
@@ -146,7 +146,7 @@ __global__ void q2b_pack_kernel(DevArgs a, KSpan ks, int first, float* Cin, Spli
   const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
-    for (int e = threadIdx.x; e < a.dim; e += blockDim.x) {
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < a.dim; e += blockDim.x * gridDim.y) {
       const int64_t r = ((int64_t)r0 + l) * a.dim + e;
       put(Cin, Cs, r, a.arena[d.in[l] + e]);
       put(Oin, Os, r, a.arena[d.in[l] + a.dim + e]);
@@ -158,7 +158,7 @@ __global__ void q2b_mean_relu_kernel(const float* P, KSpan ks, int D, float* Lm,
   const int i = blockIdx.x;
   const int k = ks.k(i), r0 = ks.row0(i);
   const float inv_k = 1.f / static_cast<float>(k);
-  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
     float s = 0.f;
     for (int l = 0; l < k; ++l) s += fmaxf(P[((int64_t)r0 + l) * D + e], 0.f);
     put(Lm, Lms, (int64_t)i * D + e, s * inv_k);
@@ -197,7 +197,7 @@ __global__ void q2b_combine_kernel(DevArgs a, KSpan ks, int first, const float* 
   const ngdb_node_desc d = a.nodes[first + i];
   const int64_t base = (int64_t)ks.row0(i) * D;
   float* st = q2b_stash(a, d.aux);
-  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
     float w[3];
     softmax_k(S, base, k, D, e, w);
     float c = 0.f, mn = Oin[base + e];
@@ -228,7 +228,7 @@ __global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Ci
   const int64_t base = (int64_t)ks.row0(i) * D;
   const float* st = q2b_stash(a, d.aux);
   const float* S = st + 3 * D;  // the node's k score rows, stashed by the forward
-  for (int e = threadIdx.x; e < D; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
     const float gC = a.arena[d.grad + e];
     const float gO = a.arena[d.grad + D + e];
     float w[3], cin[3], oin[3];
@@ -268,7 +268,7 @@ __global__ void q2b_gp_kernel(DevArgs a, const float* gLm, KSpan ks, int first, 
   const int k = ks.k(i), r0 = ks.row0(i);
   const float* P = q2b_stash(a, a.nodes[first + i].aux) + 6 * D;
   const float inv_k = 1.f / static_cast<float>(k);
-  for (int e = threadIdx.x; e < D; e += blockDim.x)
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y)
     for (int l = 0; l < k; ++l) {
       const int64_t r = ((int64_t)r0 + l) * D + e;
       put(gP, gPs, r, P[l * D + e] > 0.f ? gLm[(int64_t)i * D + e] * inv_k : 0.f);
@@ -282,7 +282,7 @@ __global__ void q2b_scatter_kernel(DevArgs a, KSpan ks, int first, const float* 
   const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
-    for (int e = threadIdx.x; e < D; e += blockDim.x) {
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
       const int64_t r = ((int64_t)r0 + l) * D + e;
       a.arena[d.out + l * 2 * D + e] = dCin[r];
       a.arena[d.out + l * 2 * D + D + e] = dOin[r];
@@ -315,7 +315,7 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
     const float* a2 = p + a.dense_off[Q2B_A2B];
     const float* v1 = p + a.dense_off[Q2B_V1B];
     const float* v2 = p + a.dense_off[Q2B_V2B];
-    launch_pdl(q2b_pack_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, Cin, Cs, Oin, Os);
+    launch_pdl(q2b_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Cin, Cs, Oin, Os);
     ++launches;
     {  // level 1: Z = A1 c + a1 (chained split of relu(Z)), P = V1 o + v1
       TcGemmArgs lvl[2];
@@ -326,7 +326,7 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
       lvl[1].bias = v1;
       launches += tc_gemm_batch(lvl, 2, s);
     }
-    launch_pdl(q2b_mean_relu_kernel, dim3(n), dim3(128), 0, s, 1, P, ks, D, Lm, Lms);
+    launch_pdl(q2b_mean_relu_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, P, ks, D, Lm, Lms);
     ++launches;
     {  // level 2: S = A2 relu(Z) + a2, U = V2 Lm + v2
       TcGemmArgs lvl[2];
@@ -336,7 +336,7 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
       lvl[1].bias = v2;
       launches += tc_gemm_batch(lvl, 2, s);
     }
-    launch_pdl(q2b_combine_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, (const float*)S,
+    launch_pdl(q2b_combine_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, (const float*)S,
                (const float*)U, (const float*)Cin, (const float*)Oin, (const float*)Z,
                (const float*)P, (const float*)Lm);
     return launches + 1;
@@ -359,7 +359,7 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
 
-  launch_pdl(q2b_combine_bwd_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, Cin, Oin, Z, Lm,
+  launch_pdl(q2b_combine_bwd_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Cin, Oin, Z, Lm,
              gS, gSs, dCin, dOin, gU, gUs);
   ++launches;
   SplitJobs j1{};
@@ -381,7 +381,7 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
     lvl[3].s_hi = gZs.hi; lvl[3].s_lo = gZs.lo;
     launches += tc_gemm_batch(lvl, 4, s);
   }
-  launch_pdl(q2b_gp_kernel, dim3(n), dim3(128), 0, s, 1, a, (const float*)gLm, ks, first, gP, gPs);
+  launch_pdl(q2b_gp_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, (const float*)gLm, ks, first, gP, gPs);
   ++launches;
   SplitJobs j2{};
   j2.job[0] = {gP, R, D, D, 0, gPT.hi, gPT.lo};
@@ -409,7 +409,7 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   cj.job[3] = {gZ, R, D, g + off[Q2B_A1B]};
   cj.n = 4;
   launches += colsums(cj, D, s);
-  launch_pdl(q2b_scatter_kernel, dim3(n), dim3(128), 0, s, 1, a, ks, first, dCin, dOin);
+  launch_pdl(q2b_scatter_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, dCin, dOin);
   return launches + 1;
 }
 

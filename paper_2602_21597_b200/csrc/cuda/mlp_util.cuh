@@ -27,6 +27,11 @@ struct Split {
 inline Split take_split(Scratch& s, int64_t n) { return {s.take(n), s.take(n)}; }
 
 inline SplitOperand op(Split x, int ld) { return {x.hi, x.lo, ld}; }
+
+// Grid of the per-node elementwise kernels: blockIdx.x = node, blockIdx.y
+// strides the row elements (128 threads each), so every thread handles ~one
+// element of a 2d-wide row and all of a node's loads are in flight at once.
+inline dim3 node_grid(int n, int dim) { return dim3(n, (2 * dim + 127) / 128); }
 // weight W_i [out][in] as B of y = x W^T (K = in), or its transpose as B of dx = dy W (K = out)
 inline SplitOperand wop(const DevArgs& a, int i, int rows, int cols, bool transposed) {
   const int64_t n = (int64_t)rows * cols;
