@@ -189,6 +189,12 @@ int ngdb_exec_pool(ngdb_ctx* ctx, const ngdb_pool_desc* pool);
 /* Sparse sorted-segment gradient reduce + touched-row Adam, then dense Adam
  * (SPEC.md:550-558 adam_step; Alg. 1 l.21 OptimizerStep). `step` is 1-based. */
 int ngdb_optimizer_step(ngdb_ctx* ctx, int64_t step);
+/* Every pool of the active streaming step + the optimizer in one call: with
+ * use_graph, captured into a CUDA graph (an executable graph is updated in
+ * place when the step's topology allows, else instantiated) and launched —
+ * ~60 stream launches become one graph launch. Same kernels, same results as
+ * ngdb_exec_pool for each pool + ngdb_optimizer_step. */
+int ngdb_step_launch(ngdb_ctx* ctx, int64_t step, int32_t use_graph);
 /* Waits for the step; copies per-query losses (may be NULL) and the non-finite
  * flag. */
 int ngdb_step_end(ngdb_ctx* ctx, float* per_query_loss, int32_t n_queries, double* loss_sum,

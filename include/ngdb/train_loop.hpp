@@ -30,6 +30,7 @@ struct TrainLoopConfig {
   uint64_t first_tag = 0;   // batch i uses Rng(seed).fork(first_tag + i)
   int32_t n_producers = 0;  // 0: hardware threads - 1 (at least 1)
   int32_t queue_depth = 0;  // planned batches buffered ahead of the consumer; 0: 2 * producers
+  bool graphs = true;       // launch each step as one CUDA graph (ngdb_step_launch)
 };
 
 struct TrainLoopStats {

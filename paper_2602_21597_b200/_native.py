@@ -87,6 +87,7 @@ SIGNATURES = {
     "ngdb_optimizer_step": (C.c_int, [C.c_void_p, i64]),
     "ngdb_step_end": (C.c_int, [C.c_void_p, P(f32), i32, P(f64), P(i32)]),
     "ngdb_step_end_async": (C.c_int, [C.c_void_p, P(i64)]),
+    "ngdb_step_launch": (C.c_int, [C.c_void_p, i64, i32]),
     "ngdb_step_wait": (C.c_int, [C.c_void_p, i64, P(f32), i32, P(f64), P(i32)]),
     "ngdb_plan_create": (C.c_int, [C.c_void_p, P(StepPlan), P(C.c_void_p)]),
     "ngdb_plan_run": (C.c_int, [C.c_void_p, C.c_void_p, i64]),

@@ -235,6 +235,10 @@ struct ngdb_ctx {
     cudaEvent_t done = nullptr;
   } results[kResultSlots];
   int64_t next_ticket = 0;
+  // streaming steps launched as CUDA graphs (ngdb_step_launch): two
+  // alternating executable graphs, updated in place when the topology allows
+  cudaGraphExec_t step_exec[2] = {nullptr, nullptr};
+  int step_exec_cur = 0;
   bool debug = false;
   // timing / accounting
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -893,6 +897,8 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
     if (c->stream_plan[i].blob) cudaFree(c->stream_plan[i].blob);
     if (c->staged[i]) cudaEventDestroy(c->staged[i]);
   }
+  for (auto& e : c->step_exec)
+    if (e) cudaGraphExecDestroy(e);
   for (auto& r : c->results) {
     if (r.host) cudaFreeHost(r.host);
     if (r.done) cudaEventDestroy(r.done);
@@ -1046,6 +1052,57 @@ int ngdb_optimizer_step(ngdb_ctx* c, int64_t step) {
     flush_held(c);
     set_step_scalars(c, step);
     optimizer(c, c->active);
+  });
+}
+
+int ngdb_step_launch(ngdb_ctx* c, int64_t step, int32_t use_graph) {
+  return guarded([&] {
+    if (!c->active) throw Fail{NGDB_ERR_CONFIG, "step_launch outside a step"};
+    flush_held(c);
+    set_step_scalars(c, step);
+    ngdb_plan* p = c->active;
+    if (!use_graph || c->profiling) {
+      exec_pools(c, p, p->meta.pools);
+      optimizer(c, p);
+      return;
+    }
+    // every pool + the optimizer as one graph: the device runs the step with
+    // graph-launch overheads instead of ~60 stream launches
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t l0 = c->launches;
+    try {
+      exec_pools(c, p, p->meta.pools);
+      optimizer(c, p);
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->stream, &g));
+    const int k = c->step_exec_cur;
+    c->step_exec_cur ^= 1;
+    cudaGraphExec_t& e = c->step_exec[k];
+    bool updated = false;
+    if (e) {
+      cudaGraphExecUpdateResultInfo info{};
+      updated = cudaGraphExecUpdate(e, g, &info) == cudaSuccess;
+      if (!updated) {
+        cudaGetLastError();
+        CK(cudaGraphExecDestroy(e));
+        e = nullptr;
+      }
+    }
+    if (!updated) {
+      const cudaError_t err = cudaGraphInstantiate(&e, g, 0);
+      if (err != cudaSuccess) {
+        cudaGraphDestroy(g);
+        CK(err);
+      }
+    }
+    CK(cudaGraphDestroy(g));
+    CK(cudaGraphLaunch(e, c->stream));
+    (void)l0;
   });
 }
 

@@ -130,11 +130,8 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
       check_status(ngdb_step_begin(ctx, &view));  // packs into pinned staging + one H2D
       const auto t_pools = std::chrono::steady_clock::now();
       stats.begin_s += std::chrono::duration<double>(t_pools - t_submit).count();
-      for (const auto& p : plan.pools) check_status(ngdb_exec_pool(ctx, &p));
-      const auto t_optim = std::chrono::steady_clock::now();
-      stats.pools_s += std::chrono::duration<double>(t_optim - t_pools).count();
-      check_status(ngdb_optimizer_step(ctx, first_step + i + 1));
-      stats.optim_s += seconds_since(t_optim);
+      check_status(ngdb_step_launch(ctx, first_step + i + 1, cfg.graphs ? 1 : 0));
+      stats.pools_s += seconds_since(t_pools);
       int64_t ticket = -1;
       check_status(ngdb_step_end_async(ctx, &ticket));
       pending.emplace_back(i, ticket);
