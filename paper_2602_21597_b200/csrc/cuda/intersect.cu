@@ -21,27 +21,38 @@
 namespace ngdb_dev {
 
 // bias gradients of a class in one launch: db_j += column sums of dy_j
-// 32 columns per block; warp w sums rows w, w+8, ...; the 8 warp partials are
+// 32 columns per block; warp w of 16 sums rows w, w+16, ... with four
+// independent accumulators (loads in flight), then the 16 warp partials are
 // combined in warp order (deterministic).
-__global__ void __launch_bounds__(256) colsum_kernel(ColsumJobs jobs) {
+constexpr int kColsumWarps = 16;
+__global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(ColsumJobs jobs) {
   pdl_start();
-  __shared__ float part[8][32];
+  __shared__ float part[kColsumWarps][32];
   const ColsumJob& j = jobs.job[blockIdx.y];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 32 + lane;
-  float s = 0.f;
-  if (c < j.n)
-    for (int r = warp; r < j.rows; r += 8) s += j.dy[(int64_t)r * j.n + c];
-  part[warp][lane] = s;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (c < j.n) {
+    constexpr int W = kColsumWarps;
+    int r = warp;
+    for (; r + 3 * W < j.rows; r += 4 * W) {
+      s0 += j.dy[(int64_t)r * j.n + c];
+      s1 += j.dy[(int64_t)(r + W) * j.n + c];
+      s2 += j.dy[(int64_t)(r + 2 * W) * j.n + c];
+      s3 += j.dy[(int64_t)(r + 3 * W) * j.n + c];
+    }
+    for (; r < j.rows; r += W) s0 += j.dy[(int64_t)r * j.n + c];
+  }
+  part[warp][lane] = (s0 + s1) + (s2 + s3);
   __syncthreads();
   if (warp == 0 && c < j.n) {
     float t = 0.f;
-    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    for (int w = 0; w < kColsumWarps; ++w) t += part[w][lane];
     j.db[c] += t;
   }
 }
 int colsums(const ColsumJobs& jobs, int n, cudaStream_t s) {
-  launch_pdl(colsum_kernel, dim3(dim3((n + 31) / 32, jobs.n)), dim3(256), 0, s, 1, jobs);
+  launch_pdl(colsum_kernel, dim3(dim3((n + 31) / 32, jobs.n)), dim3(kColsumWarps * 32), 0, s, 1, jobs);
   return 1;
 }
 

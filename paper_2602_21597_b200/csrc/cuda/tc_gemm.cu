@@ -32,7 +32,10 @@ constexpr int A_TILE = BM * BK * 4;  // 16 KB (128 rows x 128 B)
 constexpr int B_TILE = BN * BK * 4;  // 10 KB
 constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;  // A_hi, A_lo, B_hi, B_lo
 constexpr int SMEM_BYTES = kStages * STAGE + 64;
-constexpr int kTileStride = BN + 1;  // epilogue staging tile [BM][BN+1] (bank-conflict free)
+// epilogue staging tile [BM][BN+4]: 16-byte aligned rows; float4 stores of a
+// quarter-warp (8 consecutive rows) and float4 reads along a row are
+// bank-conflict free
+constexpr int kTileStride = BN + 4;
 
 struct TcGemmBatch {
   TcGemmArgs p[kMaxProblems];
@@ -252,7 +255,9 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
   {
     const int r = (warp & 3) * 32 + (threadIdx.x & 31), cb = (warp >> 2) * kHalfCols;
 #pragma unroll
-    for (int j = 0; j < kHalfCols; ++j) tile_s[r * kTileStride + cb + j] = acc[j];
+    for (int j = 0; j < kHalfCols; j += 4)
+      *reinterpret_cast<float4*>(&tile_s[r * kTileStride + cb + j]) =
+          make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
   }
   // Split-K reduce-scatter over distributed shared memory: CTA `rank` owns rows
   // [r_beg, r_end) of the tile, sums them over the S partial tiles in rank
@@ -260,9 +265,70 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
   const int r_beg = rank * BM / S, r_end = (rank + 1) * BM / S;
   if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   else __syncthreads();
-  {
+  const uint32_t local = smem_u32(tile_s);
+  if (((g.N | g.ldc) & 3) == 0) {
+    // float4 epilogue: thread t takes 16-byte column groups of the CTA's rows;
+    // the S partial loads are all issued before they are summed
+    constexpr int kQ = BN / 4;
+    const int n_items = (r_end - r_beg) * kQ;
+    for (int it = threadIdx.x; it < n_items; it += kThreads) {
+      const int r = r_beg + it / kQ, cq = (it % kQ) * 4;
+      const int row = m0 + r, n = n0 + cq;
+      if (row >= g.M || n >= g.N) continue;
+      const uint32_t off = static_cast<uint32_t>((r * kTileStride + cq) * 4);
+      float4 part[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        if (p >= S) break;
+        if (p == rank) {
+          part[p] = *reinterpret_cast<const float4*>(&tile_s[r * kTileStride + cq]);
+        } else {
+          uint32_t remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
+          asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(part[p].x), "=f"(part[p].y), "=f"(part[p].z), "=f"(part[p].w)
+                       : "r"(remote));
+        }
+      }
+      float4 v = part[0];
+#pragma unroll
+      for (int p = 1; p < 8; ++p) {
+        if (p >= S) break;
+        v.x += part[p].x; v.y += part[p].y; v.z += part[p].z; v.w += part[p].w;
+      }
+      float* crow =
+          g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
+      if (g.bias) {
+        const float4 b = *reinterpret_cast<const float4*>(g.bias + n);
+        v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
+      }
+      if (g.mask) {
+        const float4 mk = *reinterpret_cast<const float4*>(g.mask + (int64_t)row * g.ldc + n);
+        if (!(mk.x > 0.f)) v.x = 0.f;
+        if (!(mk.y > 0.f)) v.y = 0.f;
+        if (!(mk.z > 0.f)) v.z = 0.f;
+        if (!(mk.w > 0.f)) v.w = 0.f;
+      }
+      if (g.accumulate) {
+        const float4 c0 = *reinterpret_cast<const float4*>(crow + n);
+        v.x += c0.x; v.y += c0.y; v.z += c0.z; v.w += c0.w;
+      }
+      *reinterpret_cast<float4*>(crow + n) = v;
+      if (g.s_hi) {
+        float4 h, l;
+        const float4 u = g.s_relu ? make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f),
+                                                fmaxf(v.w, 0.f))
+                                  : v;
+        split_tf32(u.x, h.x, l.x);
+        split_tf32(u.y, h.y, l.y);
+        split_tf32(u.z, h.z, l.z);
+        split_tf32(u.w, h.w, l.w);
+        *reinterpret_cast<float4*>(g.s_hi + (int64_t)row * g.ldc + n) = h;
+        *reinterpret_cast<float4*>(g.s_lo + (int64_t)row * g.ldc + n) = l;
+      }
+    }
+  } else {
     const int lane = threadIdx.x & 31;
-    const uint32_t local = smem_u32(tile_s);
     for (int r = r_beg + warp; r < r_end; r += kThreads / 32) {
       const int row = m0 + r;
       if (row >= g.M) break;
