@@ -158,13 +158,49 @@ __global__ void beta_proj_pack_kernel(DevArgs a, int first, float* X, Split Xs) 
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < 3 * D; e += blockDim.x * gridDim.y)
     put(X, Xs, static_cast<int64_t>(i) * 3 * D + e, e < 2 * D ? q[e] : r[e - 2 * D]);
 }
-__global__ void beta_proj_out_kernel(DevArgs a, int first, const float* Z) {
+// stash of a Project node (slot = its project slot, node aux): H, Z [2d] each
+__device__ __forceinline__ float* proj_stash(const DevArgs& a, int slot) {
+  if (slot < 0 || slot >= a.pstash_slots) {
+    atomicOr(&a.flags[1], 1);
+    slot = 0;
+  }
+  return a.pstash + static_cast<int64_t>(slot) * 4 * a.dim;
+}
+// output = realize(Z); H and Z are stashed for the mirror
+__global__ void beta_proj_out_kernel(DevArgs a, int first, const float* Z, const float* H) {
   pdl_start();
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
   const int W = 2 * a.dim;
-  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y)
-    a.arena[d.out + e] = beta_realize(Z[static_cast<int64_t>(i) * W + e]);
+  float* st = proj_stash(a, d.aux);
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y) {
+    const float z = Z[static_cast<int64_t>(i) * W + e];
+    a.arena[d.out + e] = beta_realize(z);
+    st[e] = H[static_cast<int64_t>(i) * W + e];
+    st[W + e] = z;
+  }
+}
+// Backward gather: X = [q | r] (plain; the weight-gradient operand), the
+// stashed H (the ReLU mask) and gZ = dL/dout * realize'(Z) (plain + split)
+__global__ void beta_proj_bwd_pack_kernel(DevArgs a, int first, float* X, float* H, float* gZ,
+                                          Split gZs) {
+  pdl_start();
+  const int i = blockIdx.x;
+  const ngdb_node_desc d = a.nodes[first + i];
+  const int D = a.dim, W = 2 * D;
+  const bool ok = d.id >= 0 && d.id < a.n_relations;
+  if (!ok && threadIdx.x == 0) atomicOr(&a.flags[1], 1);
+  const float* q = a.arena + d.in[0];
+  const float* r = a.rel + static_cast<int64_t>(ok ? d.id : 0) * a.rel_w;
+  const float* st = proj_stash(a, d.aux);
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < 3 * D; e += blockDim.x * gridDim.y) {
+    X[static_cast<int64_t>(i) * 3 * D + e] = e < W ? q[e] : r[e - W];
+    if (e < W) {
+      const int64_t o = static_cast<int64_t>(i) * W + e;
+      H[o] = st[e];
+      put(gZ, gZs, o, a.arena[d.grad + e] * beta_drealize(st[W + e]));
+    }
+  }
 }
 __global__ void beta_proj_gz_kernel(DevArgs a, int first, const float* Z, float* gZ, Split gZs) {
   pdl_start();
@@ -193,25 +229,27 @@ int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
   const int nP = (n + 3) & ~3;
   Scratch sc{a.scratch, a.scratch_cap};
   float* X = sc.take((int64_t)n * D3);
-  Split Xs = take_split(sc, (int64_t)n * D3);
   float* H = sc.take((int64_t)n * D2);
-  Split RHs = take_split(sc, (int64_t)n * D2);
-  float* Z = sc.take((int64_t)n * D2);
   const float* p = a.dense;
   int launches = 0;
-  launch_pdl(beta_proj_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, X, Xs);
-  ++launches;
-  TcGemmArgs h = gemm_args(n, D2, D3, op(Xs, D3), wop(a, BETA_P1, D2, D3, false), H, D2);
-  h.bias = p + a.dense_off[BETA_P1B];
-  h.s_hi = RHs.hi; h.s_lo = RHs.lo; h.s_relu = 1;
-  launches += tc_gemm(h, s);
-  TcGemmArgs z = gemm_args(n, D2, D2, op(RHs, D2), wop(a, BETA_P2, D2, D2, false), Z, D2);
-  z.bias = p + a.dense_off[BETA_P2B];
-  launches += tc_gemm(z, s);
   if (dir == 0) {
-    launch_pdl(beta_proj_out_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, (const float*)Z);
+    Split Xs = take_split(sc, (int64_t)n * D3);
+    Split RHs = take_split(sc, (int64_t)n * D2);
+    float* Z = sc.take((int64_t)n * D2);
+    launch_pdl(beta_proj_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, X, Xs);
+    ++launches;
+    TcGemmArgs h = gemm_args(n, D2, D3, op(Xs, D3), wop(a, BETA_P1, D2, D3, false), H, D2);
+    h.bias = p + a.dense_off[BETA_P1B];
+    h.s_hi = RHs.hi; h.s_lo = RHs.lo; h.s_relu = 1;
+    launches += tc_gemm(h, s);
+    TcGemmArgs z = gemm_args(n, D2, D2, op(RHs, D2), wop(a, BETA_P2, D2, D2, false), Z, D2);
+    z.bias = p + a.dense_off[BETA_P2B];
+    launches += tc_gemm(z, s);
+    launch_pdl(beta_proj_out_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first,
+               (const float*)Z, (const float*)H);
     return launches + 1;
   }
+  // Backward: H and Z come from the node's stash (no forward recomputation)
   float* gZ = sc.take((int64_t)n * D2);
   Split gZs = take_split(sc, (int64_t)n * D2);
   float* gH = sc.take((int64_t)n * D2);
@@ -221,7 +259,8 @@ int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
   float* gX = sc.take((int64_t)n * D3);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
-  launch_pdl(beta_proj_gz_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, (const float*)Z, gZ, gZs);
+  launch_pdl(beta_proj_bwd_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, X, H,
+             gZ, gZs);
   ++launches;
   // gH = (gZ W2) * (H > 0)
   TcGemmArgs gh = gemm_args(n, D2, D2, op(gZs, D2), wop(a, BETA_P2, D2, D2, true), gH, D2);
@@ -273,12 +312,28 @@ __device__ __forceinline__ void softmax3(const float* S, int64_t base, int k, in
   const float inv = 1.f / z;
   for (int l = 0; l < k; ++l) w[l] *= inv;
 }
-__global__ void beta_inter_combine_kernel(DevArgs a, KSpan ks, int first, const float* S, const float* Q) {
+// stash of an Intersect node (slot = node aux): Z rows [3][2d], then S rows [3][d]
+__device__ __forceinline__ float* inter_stash(const DevArgs& a, int slot) {
+  if (slot < 0 || slot >= a.istash_slots) {
+    atomicOr(&a.flags[1], 1);
+    slot = 0;
+  }
+  return a.istash + static_cast<int64_t>(slot) * kStashPerSlot * a.dim;
+}
+__global__ void beta_inter_combine_kernel(DevArgs a, KSpan ks, int first, const float* S,
+                                          const float* Q, const float* Z) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim, W = 2 * D;
   const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
+  float* st = inter_stash(a, d.aux);
+  // stash Z and S rows for the mirror
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y)
+    for (int l = 0; l < k; ++l) {
+      st[l * W + e] = Z[(static_cast<int64_t>(r0) + l) * W + e];
+      if (e < D) st[3 * W + l * D + e] = S[(static_cast<int64_t>(r0) + l) * D + e];
+    }
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
     float w[3];
     softmax3(S, static_cast<int64_t>(r0) * D, k, D, e, w);
@@ -292,19 +347,29 @@ __global__ void beta_inter_combine_kernel(DevArgs a, KSpan ks, int first, const 
     a.arena[d.out + D + e] = be;
   }
 }
-__global__ void beta_inter_combine_bwd_kernel(DevArgs a, KSpan ks, int first, const float* S,
-                                              const float* Q, float* gS, Split gSs, float* dQ) {
+// Backward combine from the node's stash; also gathers the inputs Q and the
+// stashed Z rows into class order (weight-gradient operands, ReLU mask).
+__global__ void beta_inter_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Q, float* Z,
+                                              float* gS, Split gSs, float* dQ) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim, W = 2 * D;
   const int k = ks.k(i), r0 = ks.row0(i);
   const ngdb_node_desc d = a.nodes[first + i];
+  const float* st = inter_stash(a, d.aux);
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y)
+    for (int l = 0; l < k; ++l) {
+      const int64_t r = (static_cast<int64_t>(r0) + l) * W + e;
+      Q[r] = a.arena[d.in[l] + e];
+      Z[r] = st[l * W + e];
+    }
+  const float* S = st + 3 * W;  // the node's k score rows [k][D]
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
     const float gA = a.arena[d.grad + e], gB = a.arena[d.grad + D + e];
     float w[3], gw[3], dot = 0.f;
-    softmax3(S, static_cast<int64_t>(r0) * D, k, D, e, w);
+    softmax3(S, 0, k, D, e, w);
     for (int l = 0; l < k; ++l) {
-      const float* q = Q + (static_cast<int64_t>(r0) + l) * W;
+      const float* q = a.arena + d.in[l];
       gw[l] = gA * q[e] + gB * q[D + e];
       dot += w[l] * gw[l];
     }
@@ -332,26 +397,27 @@ int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaSt
   const int R = ks.row0(n), RP = (R + 3) & ~3;
   Scratch sc{a.scratch, a.scratch_cap};
   float* Q = sc.take((int64_t)R * W);
-  Split Qs = take_split(sc, (int64_t)R * W);
   float* Z = sc.take((int64_t)R * W);
-  Split RZs = take_split(sc, (int64_t)R * W);
-  float* S = sc.take((int64_t)R * D);
   const float* p = a.dense;
   int launches = 0;
-  launch_pdl(beta_inter_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Q, Qs);
-  ++launches;
-  TcGemmArgs z = gemm_args(R, W, W, op(Qs, W), wop(a, BETA_A1, W, W, false), Z, W);
-  z.bias = p + a.dense_off[BETA_A1B];
-  z.s_hi = RZs.hi; z.s_lo = RZs.lo; z.s_relu = 1;
-  launches += tc_gemm(z, s);
-  TcGemmArgs sg = gemm_args(R, D, W, op(RZs, W), wop(a, BETA_A2, D, W, false), S, D);
-  sg.bias = p + a.dense_off[BETA_A2B];
-  launches += tc_gemm(sg, s);
   if (dir == 0) {
-    launch_pdl(beta_inter_combine_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, (const float*)S,
-               (const float*)Q);
+    Split Qs = take_split(sc, (int64_t)R * W);
+    Split RZs = take_split(sc, (int64_t)R * W);
+    float* S = sc.take((int64_t)R * D);
+    launch_pdl(beta_inter_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Q, Qs);
+    ++launches;
+    TcGemmArgs z = gemm_args(R, W, W, op(Qs, W), wop(a, BETA_A1, W, W, false), Z, W);
+    z.bias = p + a.dense_off[BETA_A1B];
+    z.s_hi = RZs.hi; z.s_lo = RZs.lo; z.s_relu = 1;
+    launches += tc_gemm(z, s);
+    TcGemmArgs sg = gemm_args(R, D, W, op(RZs, W), wop(a, BETA_A2, D, W, false), S, D);
+    sg.bias = p + a.dense_off[BETA_A2B];
+    launches += tc_gemm(sg, s);
+    launch_pdl(beta_inter_combine_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first,
+               (const float*)S, (const float*)Q, (const float*)Z);
     return launches + 1;
   }
+  // Backward: Z and S come from the node's stash (no forward recomputation)
   float* gS = sc.take((int64_t)R * D);
   Split gSs = take_split(sc, (int64_t)R * D);
   float* dQ = sc.take((int64_t)R * W);
@@ -362,7 +428,7 @@ int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaSt
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
   launch_pdl(beta_inter_combine_bwd_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first,
-             (const float*)S, (const float*)Q, gS, gSs, dQ);
+             Q, Z, gS, gSs, dQ);
   ++launches;
   // gZ = (gS A2) * (Z > 0)
   TcGemmArgs gz = gemm_args(R, W, D, op(gSs, D), wop(a, BETA_A2, D, W, true), gZ, W);

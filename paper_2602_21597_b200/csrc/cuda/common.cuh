@@ -84,6 +84,9 @@ struct DevArgs {
   // kStashPerSlot * dim floats
   float* istash;
   int32_t istash_slots;
+  // BetaE Project stash: per project slot (node aux) H, Z [2d] each
+  float* pstash;
+  int32_t pstash_slots;
   // fused score+loss: per-(node, part) partials of dL/dq [items][wq] and of
   // (loss, coefficient sum) [items][2], and per-node arrival counters (zero
   // between launches)

@@ -194,6 +194,8 @@ struct ngdb_ctx {
   const float* anc_rows = nullptr;  // set while a sharded step runs
   float* istash = nullptr;           // Intersect stash (DevArgs::istash)
   int32_t istash_slots = 0;
+  float* pstash = nullptr;           // BetaE Project stash (DevArgs::pstash)
+  int32_t pstash_slots = 0;
   float* lpart = nullptr;            // fused score+loss partials (DevArgs::lpart)
   float* lpart_scalar = nullptr;
   int32_t* lcount = nullptr;
@@ -420,6 +422,8 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.anc_rows = c->anc_rows;
   a.istash = c->istash;
   a.istash_slots = c->istash_slots;
+  a.pstash = c->pstash;
+  a.pstash_slots = c->pstash_slots;
   a.lpart = c->lpart;
   a.lpart_scalar = c->lpart_scalar;
   a.lcount = c->lcount;
@@ -850,6 +854,10 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     c->scratch_cap = intersect_scratch_floats(d.backbone, d.dim, c->desc.max_batch);
     c->istash_slots = std::max(c->desc.max_queries, 1);
     c->istash = dmalloc<float>(int64_t(c->istash_slots) * kStashPerSlot * d.dim);
+    if (d.backbone == NGDB_BETAE) {  // <= 4 Project nodes per query after DNF
+      c->pstash_slots = 4 * std::max(c->desc.max_queries, 1);
+      c->pstash = dmalloc<float>(int64_t(c->pstash_slots) * 4 * d.dim);
+    }
     // (node, part) items of one loss launch: at most 8 parts of max_batch nodes
     c->lpart_items = 8 * c->desc.max_batch;
     c->lpart = dmalloc<float>(int64_t(c->lpart_items) * c->query_width());
@@ -884,6 +892,7 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   if (c->anchor_local) cudaFree(c->anchor_local);
   if (c->fscratch) cudaFree(c->fscratch);
   if (c->istash) cudaFree(c->istash);
+  if (c->pstash) cudaFree(c->pstash);
   if (c->lpart) cudaFree(c->lpart);
   if (c->lpart_scalar) cudaFree(c->lpart_scalar);
   if (c->lcount) cudaFree(c->lcount);
