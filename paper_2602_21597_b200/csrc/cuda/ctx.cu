@@ -498,7 +498,7 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d,
       break;
     case NGDB_OP_PROJECT:
       if (c->profiling && c->beta())  // [q|r] 3d -> 2d -> 2d MLP, in units of 2 d^2 flops
-        c->fam_flops[fam] += (d.dir == 0 ? 10.0 : 30.0) * d.count * 2.0 * c->desc.dim * c->desc.dim;
+        c->fam_flops[fam] += (d.dir == 0 ? 10.0 : 20.0) * d.count * 2.0 * c->desc.dim * c->desc.dim;
       timed(c, fam, bytes, [&] { return launch_project(a, d.dir, d.first, d.count, lc); });
       break;
     case NGDB_OP_NEGATE:
