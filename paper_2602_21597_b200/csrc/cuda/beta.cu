@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kWarps * 32) beta_entity_adam_kernel(DevArgs a
   const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row_idx >= t.n_rows) return;
-  const float bc1 = bc[0], bc2 = bc[1];
+  const float ibc1 = 1.f / bc[0], ibc2 = 1.f / bc[1];  // bias corrections as reciprocals
   const int64_t row = t.rows[row_idx];
   const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
   const int D = a.dim, d4 = D / 4;
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kWarps * 32) beta_entity_adam_kernel(DevArgs a
       for (int u = 0; u < 4; ++u) {
         mv[u] = hp.b1 * mv[u] + (1.f - hp.b1) * g[u];
         vv[u] = hp.b2 * vv[u] + (1.f - hp.b2) * g[u] * g[u];
-        wv[u] -= hp.lr * (mv[u] / bc1) / (sqrtf(vv[u] / bc2) + hp.eps);
+        wv[u] -= hp.lr * (mv[u] * ibc1) / (sqrtf(vv[u] * ibc2) + hp.eps);
       }
       st4(wp + off, w);
       st4(mp + off, m);

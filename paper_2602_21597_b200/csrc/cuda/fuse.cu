@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kWarps * 32) rows_adam_kernel(SparseTable t, c
   const int r = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (r >= t.n_rows) return;
-  const float bc1 = bc[0], bc2 = bc[1];
+  const float ibc1 = 1.f / bc[0], ibc2 = 1.f / bc[1];  // bias corrections as reciprocals
   const int64_t row = t.rows[r];
   for (int c = lane; c < t.width / 4; c += 32) {
     const float4 g4 = ld4(G + (int64_t)r * ldg + 4 * c);
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kWarps * 32) rows_adam_kernel(SparseTable t, c
     for (int q = 0; q < 4; ++q) {
       mv[q] = hp.b1 * mv[q] + (1.f - hp.b1) * g[q];
       vv[q] = hp.b2 * vv[q] + (1.f - hp.b2) * g[q] * g[q];
-      wv[q] -= hp.lr * (mv[q] / bc1) / (sqrtf(vv[q] / bc2) + hp.eps);
+      wv[q] -= hp.lr * (mv[q] * ibc1) / (sqrtf(vv[q] * ibc2) + hp.eps);
     }
     st4(t.w + o, w);
     st4(t.m + o, m);

@@ -24,19 +24,21 @@ namespace {
 
 constexpr int kWarps = 8;
 
+// bias corrections as reciprocals, computed once per thread: the per-element
+// update keeps one division
 struct AdamK {
-  float lr, b1, b2, eps, bc1, bc2;
+  float lr, b1, b2, eps, inv_bc1, inv_bc2;
 };
 
 __device__ __forceinline__ AdamK adam_consts(const AdamHyper& h, const float* bc) {
-  return AdamK{h.lr, h.b1, h.b2, h.eps, bc[0], bc[1]};
+  return AdamK{h.lr, h.b1, h.b2, h.eps, 1.f / bc[0], 1.f / bc[1]};
 }
 
 __device__ __forceinline__ void adam_update(float& w, float& m, float& v, float g, const AdamK& k) {
   m = k.b1 * m + (1.f - k.b1) * g;
   v = k.b2 * v + (1.f - k.b2) * g * g;
-  const float mhat = m / k.bc1;
-  const float vhat = v / k.bc2;
+  const float mhat = m * k.inv_bc1;
+  const float vhat = v * k.inv_bc2;
   w -= k.lr * mhat / (sqrtf(vhat) + k.eps);
 }
 

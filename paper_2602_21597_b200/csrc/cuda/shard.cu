@@ -170,7 +170,7 @@ __global__ void masked_rows_adam_kernel(float* w, float* m, float* v, float* dbg
   pdl_start();
   const int r = blockIdx.x;
   if (r >= rows || !(touched[r] > 0.f)) return;
-  const float bc1 = bc[0], bc2 = bc[1];
+  const float ibc1 = 1.f / bc[0], ibc2 = 1.f / bc[1];  // bias corrections as reciprocals
   for (int e = threadIdx.x; e < width; e += blockDim.x) {
     const int64_t o = static_cast<int64_t>(r) * width + e;
     const float gi = g[o];
@@ -179,7 +179,7 @@ __global__ void masked_rows_adam_kernel(float* w, float* m, float* v, float* dbg
     const float vi = hp.b2 * v[o] + (1.f - hp.b2) * gi * gi;
     m[o] = mi;
     v[o] = vi;
-    w[o] -= hp.lr * (mi / bc1) / (sqrtf(vi / bc2) + hp.eps);
+    w[o] -= hp.lr * (mi * ibc1) / (sqrtf(vi * ibc2) + hp.eps);
   }
 }
 
