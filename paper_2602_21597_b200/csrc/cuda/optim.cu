@@ -70,14 +70,14 @@ __device__ __forceinline__ float cand_grad(float v, float qc, float qo, float co
 // registers and theta, m, v are stored straight back to HBM.
 constexpr int kAdamConsumers = 8;
 constexpr int kAdamThreads = 32 * (kAdamConsumers + 1);
-constexpr int kAdamRing = 16;  // a multiple of kAdamConsumers (see the score ring)
+constexpr int kAdamRing = 8;  // a multiple of kAdamConsumers (see the score ring)
 
 inline size_t adam_smem_bytes(int width) {
   return static_cast<size_t>(kAdamRing) * 3 * width * sizeof(float) + 2 * kAdamRing * sizeof(uint64_t);
 }
 
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kAdamThreads, 2) entity_adam_kernel(DevArgs a, SparseTable t,
+__global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a, SparseTable t,
                                                                    AdamHyper hp, const float* bc,
                                                                    int rows_per_cta) {
   extern __shared__ __align__(128) float smem[];
@@ -333,8 +333,8 @@ int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const Adam
   if (t.n_rows <= 0) return 0;
   if (a.backbone == NGDB_BETAE) return launch_beta_entity_adam(a, t, hp, bc, lc);
   const size_t smem = adam_smem_bytes(t.width);
-  // persistent-style grid: 2 CTAs per SM (77 KB rings), contiguous row ranges
-  const int ctas = std::max(1, std::min(t.n_rows, 2 * lc.num_sms));  // 2 resident per SM
+  // persistent-style grid: ~3 CTAs per SM, contiguous row ranges
+  const int ctas = std::max(1, std::min(t.n_rows, 3 * lc.num_sms));
   const int rows_per_cta = (t.n_rows + ctas - 1) / ctas;
   const int grid = (t.n_rows + rows_per_cta - 1) / rows_per_cta;
   auto go = [&](auto kernel) {
