@@ -191,6 +191,11 @@ struct ngdb_ctx {
   // row-sharded step (shard.cu)
   int world = 1, rank = 0;
   cudaStream_t own_stream = nullptr;
+  // streaming plans are uploaded on a copy stream one step ahead, overlapping
+  // the previous step's kernels: blob_free[i] marks the end of the last step
+  // that read stream_plan[i], blob_ready[i] the end of its upload
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t blob_free[2] = {nullptr, nullptr}, blob_ready[2] = {nullptr, nullptr};
   const float* anc_rows = nullptr;  // set while a sharded step runs
   float* istash = nullptr;           // Intersect stash (DevArgs::istash)
   int32_t istash_slots = 0;
@@ -608,15 +613,21 @@ DenseJobs dense_jobs(const ngdb_ctx* c) {
 }
 
 // Adam bias corrections of step t -> device scalars (read by the optimizer
-// kernels, so a captured graph of the step replays with the current t). The
-// source is pageable: the copy is staged before cudaMemcpyAsync returns.
+// kernels, so a captured graph of the step replays with the current t).
+__global__ void set_bc_kernel(float* bc, float bc1, float bc2) {
+  bc[0] = bc1;
+  bc[1] = bc2;
+}
+// A one-thread kernel with the values as arguments: no host-to-device copy in
+// the kernel stream (a pageable memcpy would put a copy-engine op between
+// kernels), and capturable.
 void set_step_scalars(ngdb_ctx* c, int64_t step) {
   if (step < 1) throw Fail{NGDB_ERR_CONFIG, "optimizer step must be >= 1"};
   const ngdb_model_desc& d = c->desc;
-  const float bc[2] = {
-      static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta1), double(step))),
-      static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta2), double(step)))};
-  CK(cudaMemcpyAsync(c->d_bc, bc, sizeof(bc), cudaMemcpyHostToDevice, c->stream));
+  const float bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta1), double(step)));
+  const float bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(d.beta2), double(step)));
+  set_bc_kernel<<<1, 1, 0, c->stream>>>(c->d_bc, bc1, bc2);
+  CK(cudaGetLastError());
 }
 
 SparseTable entity_table(ngdb_ctx* c, const ngdb_plan* p) {
@@ -695,6 +706,7 @@ void upload_plan(ngdb_ctx* c, const ngdb_step_plan& plan, ngdb_plan* dst, int64_
   if (L.total > dst_cap) {
     if (dst->blob) {
       CK(cudaStreamSynchronize(c->stream));
+      if (c->copy_stream) CK(cudaStreamSynchronize(c->copy_stream));
       CK(cudaFree(dst->blob));
     }
     dst_cap = std::max<int64_t>(L.total + L.total / 2, dst_cap + dst_cap / 2);
@@ -869,7 +881,12 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     tc_gemm_init();
     CK(cudaEventCreate(&c->t0));
     CK(cudaEventCreate(&c->t1));
-    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c->staged[i], cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&c->staged[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->blob_free[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->blob_ready[i], cudaEventDisableTiming));
+    }
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     *out = c;
   });
   if (rc != NGDB_OK && c) ngdb_ctx_destroy(c);
@@ -905,6 +922,8 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
     if (c->staging[i]) cudaFreeHost(c->staging[i]);
     if (c->stream_plan[i].blob) cudaFree(c->stream_plan[i].blob);
     if (c->staged[i]) cudaEventDestroy(c->staged[i]);
+    if (c->blob_free[i]) cudaEventDestroy(c->blob_free[i]);
+    if (c->blob_ready[i]) cudaEventDestroy(c->blob_ready[i]);
   }
   for (auto& e : c->step_exec)
     if (e) cudaGraphExecDestroy(e);
@@ -924,6 +943,10 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   for (int k = 0; k < 2; ++k) {
     if (c->sh.staging[k]) cudaFreeHost(c->sh.staging[k]);
     if (c->sh.staged[k]) cudaEventDestroy(c->sh.staged[k]);
+  }
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
   }
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
@@ -1026,8 +1049,16 @@ int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
       CK(cudaMallocHost(&p, c->staging_cap[i] * sizeof(int32_t)));
       c->staging[i] = static_cast<int32_t*>(p);
     }
-    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->stream);
-    CK(cudaEventRecord(c->staged[i], c->stream));
+    // everything enqueued so far on the context stream belongs to the steps
+    // before this one: the last reader of stream_plan[1-i] is among them
+    CK(cudaEventRecord(c->blob_free[i ^ 1], c->stream));
+    // upload on the copy stream once the step two back (the last reader of
+    // stream_plan[i]) is done; the kernels of this step wait for the upload
+    CK(cudaStreamWaitEvent(c->copy_stream, c->blob_free[i], 0));
+    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->copy_stream);
+    CK(cudaEventRecord(c->staged[i], c->copy_stream));
+    CK(cudaEventRecord(c->blob_ready[i], c->copy_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->blob_ready[i], 0));
     ensure_step_buffers(c, c->stream_plan[i].meta);
     begin_step_device(c);
     prep_step(c, &c->stream_plan[i]);
