@@ -23,7 +23,7 @@ namespace {
 
 constexpr int BM = 128, BN = 80, BK = 32;
 constexpr int kThreads = 256;   // 8 warps; warps w and w+4 share TMEM lane quarter w%4
-constexpr int kStages = 4;      // smem operand ring; 208 KB -> one CTA per SM, 3 chunks in flight
+constexpr int kStages = 2;      // smem operand ring; 104 KB -> two CTAs per SM
 constexpr int kTmemCols = 256;  // 2 accumulator buffers of BN columns (power of two)
 constexpr int kHalfCols = BN / 2;
 constexpr int kMaxProblems = 4;
@@ -162,7 +162,7 @@ __device__ __forceinline__ void drain(uint32_t tmem, int buf, float* acc) {
   for (int j = 0; j < kHalfCols; ++j) acc[j] += __uint_as_float(r[j]);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) tc_gemm_kernel(const __grid_constant__ TcGemmBatch batch) {
+__global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_constant__ TcGemmBatch batch) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t s_base = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * STAGE);  // [kStages]
@@ -442,12 +442,11 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   }
   if (b.n == 0) return 0;
   b.tile_begin[b.n] = tiles;
+  // split-K so the launch fills about one wave (2 CTAs per SM), at most 8 CTAs
+  // per cluster (portable size) and at least 2 chunks per CTA
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
-  // split-K only when the tiles alone leave SMs idle (one CTA per SM), and
-  // never below 4 K chunks per CTA: most launches run unsplit, with no
-  // cluster barriers or DSMEM reduction
-  b.S = std::max(1, std::min({8, num_sms / std::max(tiles, 1), max_chunks / 4}));
+  b.S = std::max(1, std::min({8, (2 * num_sms) / std::max(tiles, 1), max_chunks / 2}));
   launch_pdl(tc_gemm_kernel, dim3(tiles * b.S), dim3(kThreads), SMEM_BYTES, s, b.S, b);
   return 1;
 }
