@@ -179,8 +179,14 @@ int ngdb_param_download(ngdb_ctx* ctx, const char* name, float* host, int64_t n)
 int ngdb_semantic_upload(ngdb_ctx* ctx, const float* host, int64_t n); /* frozen PTE store */
 int ngdb_set_debug(ngdb_ctx* ctx, int32_t keep_sparse_grads);
 
-/* Streaming step: packs the plan into pinned staging and issues one H2D copy. */
+/* Streaming step: packs the plan into pinned staging and issues one H2D copy
+ * (on a copy stream, overlapping the previous step's kernels). */
 int ngdb_step_begin(ngdb_ctx* ctx, const ngdb_step_plan* plan);
+/* flags: NGDB_BEGIN_DEFER_PROLOGUE leaves the step prologue (flag and
+ * dense-gradient resets) to the first ngdb_exec_pool / ngdb_step_launch, so a
+ * graph-launched step carries it inside its graph. */
+#define NGDB_BEGIN_DEFER_PROLOGUE 1
+int ngdb_step_begin_ex(ngdb_ctx* ctx, const ngdb_step_plan* plan, int32_t flags);
 /* Launch one kernel invocation of the current step (KernelRegistry fwd/bwd).
  * An Intersect class is held until the next call, so that the next class of
  * the same PopBatch shares its launches; errors of a held class surface at the

@@ -83,6 +83,7 @@ SIGNATURES = {
     "ngdb_semantic_upload": (C.c_int, [C.c_void_p, P(f32), i64]),
     "ngdb_set_debug": (C.c_int, [C.c_void_p, i32]),
     "ngdb_step_begin": (C.c_int, [C.c_void_p, P(StepPlan)]),
+    "ngdb_step_begin_ex": (C.c_int, [C.c_void_p, P(StepPlan), i32]),
     "ngdb_exec_pool": (C.c_int, [C.c_void_p, P(PoolDesc)]),
     "ngdb_optimizer_step": (C.c_int, [C.c_void_p, i64]),
     "ngdb_step_end": (C.c_int, [C.c_void_p, P(f32), i32, P(f64), P(i32)]),

@@ -232,6 +232,9 @@ struct ngdb_ctx {
   // the same PopBatch can share its launches (exec_pools / mergeable)
   ngdb_pool_desc held{};
   bool has_held = false;
+  // ngdb_step_begin_ex(NGDB_BEGIN_DEFER_PROLOGUE): the step prologue (flag and
+  // dense-gradient resets, step table) runs inside ngdb_step_launch's graph
+  bool prologue_pending = false;
   // asynchronous step ends: a ring of pinned result slots (losses + flags)
   static constexpr int kResultSlots = 4;
   struct ResultSlot {
@@ -1033,6 +1036,10 @@ int ngdb_set_debug(ngdb_ctx* c, int32_t keep) {
 }
 
 int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
+  return ngdb_step_begin_ex(c, plan, 0);
+}
+
+int ngdb_step_begin_ex(ngdb_ctx* c, const ngdb_step_plan* plan, int32_t flags) {
   return guarded([&] {
     c->has_held = false;
     if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "context is row-sharded: use ngdb_shard_begin"};
@@ -1060,15 +1067,23 @@ int ngdb_step_begin(ngdb_ctx* c, const ngdb_step_plan* plan) {
     CK(cudaEventRecord(c->blob_ready[i], c->copy_stream));
     CK(cudaStreamWaitEvent(c->stream, c->blob_ready[i], 0));
     ensure_step_buffers(c, c->stream_plan[i].meta);
-    begin_step_device(c);
-    prep_step(c, &c->stream_plan[i]);
     c->active = &c->stream_plan[i];
+    c->prologue_pending = (flags & NGDB_BEGIN_DEFER_PROLOGUE) != 0;
+    if (!c->prologue_pending) {
+      begin_step_device(c);
+      prep_step(c, &c->stream_plan[i]);
+    }
   });
 }
 
 int ngdb_exec_pool(ngdb_ctx* c, const ngdb_pool_desc* pool) {
   return guarded([&] {
     if (!c->active) throw Fail{NGDB_ERR_CONFIG, "exec_pool outside a step"};
+    if (c->prologue_pending) {
+      begin_step_device(c);
+      prep_step(c, c->active);
+      c->prologue_pending = false;
+    }
     if (c->has_held) {
       c->has_held = false;
       if (mergeable(c, c->held, *pool)) {
@@ -1089,6 +1104,11 @@ int ngdb_exec_pool(ngdb_ctx* c, const ngdb_pool_desc* pool) {
 int ngdb_optimizer_step(ngdb_ctx* c, int64_t step) {
   return guarded([&] {
     if (!c->active) throw Fail{NGDB_ERR_CONFIG, "optimizer_step outside a step"};
+    if (c->prologue_pending) {
+      begin_step_device(c);
+      prep_step(c, c->active);
+      c->prologue_pending = false;
+    }
     flush_held(c);
     set_step_scalars(c, step);
     optimizer(c, c->active);
@@ -1099,27 +1119,35 @@ int ngdb_step_launch(ngdb_ctx* c, int64_t step, int32_t use_graph) {
   return guarded([&] {
     if (!c->active) throw Fail{NGDB_ERR_CONFIG, "step_launch outside a step"};
     flush_held(c);
-    set_step_scalars(c, step);
     ngdb_plan* p = c->active;
-    if (!use_graph || c->profiling) {
+    auto body = [&] {
+      if (c->prologue_pending) {
+        begin_step_device(c);
+        prep_step(c, p);
+      }
+      set_step_scalars(c, step);
       exec_pools(c, p, p->meta.pools);
       optimizer(c, p);
+    };
+    if (!use_graph || c->profiling) {
+      body();
+      c->prologue_pending = false;
       return;
     }
-    // every pool + the optimizer as one graph: the device runs the step with
-    // graph-launch overheads instead of ~60 stream launches
+    // the whole step (prologue, step scalars, every pool, the optimizer) as one
+    // graph: the device runs it with graph-launch overheads instead of ~60
+    // stream operations
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    const int64_t l0 = c->launches;
     try {
-      exec_pools(c, p, p->meta.pools);
-      optimizer(c, p);
+      body();
     } catch (...) {
       cudaStreamEndCapture(c->stream, &g);
       if (g) cudaGraphDestroy(g);
       throw;
     }
     CK(cudaStreamEndCapture(c->stream, &g));
+    c->prologue_pending = false;
     const int k = c->step_exec_cur;
     c->step_exec_cur ^= 1;
     cudaGraphExec_t& e = c->step_exec[k];
@@ -1142,7 +1170,6 @@ int ngdb_step_launch(ngdb_ctx* c, int64_t step, int32_t use_graph) {
     }
     CK(cudaGraphDestroy(g));
     CK(cudaGraphLaunch(e, c->stream));
-    (void)l0;
   });
 }
 

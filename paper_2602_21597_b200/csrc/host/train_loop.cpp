@@ -127,7 +127,8 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
       cv_space.notify_all();
       const auto t_submit = std::chrono::steady_clock::now();
       const ngdb_step_plan view = plan.view();
-      check_status(ngdb_step_begin(ctx, &view));  // packs into pinned staging + one H2D
+      // packs into pinned staging + one H2D; the step prologue goes into the graph
+      check_status(ngdb_step_begin_ex(ctx, &view, cfg.graphs ? NGDB_BEGIN_DEFER_PROLOGUE : 0));
       const auto t_pools = std::chrono::steady_clock::now();
       stats.begin_s += std::chrono::duration<double>(t_pools - t_submit).count();
       check_status(ngdb_step_launch(ctx, first_step + i + 1, cfg.graphs ? 1 : 0));
