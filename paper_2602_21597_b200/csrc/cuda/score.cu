@@ -5,7 +5,7 @@
 // node, part): the S parts of a node split its 1+K candidates into contiguous
 // ranges, S chosen so that every resident CTA has items. A CTA walks items
 // blockIdx.x, +gridDim.x, ...; its producer warp streams each item's query
-// row (double-buffered) and candidate rows (a ring of ~48 KB) into shared
+// row (double-buffered) and candidate rows (a ring of ~32 KB) into shared
 // memory with bulk copies (cp.async.bulk + mbarrier complete_tx), running
 // ahead across items so HBM never idles through per-item reductions. Eight
 // consumer warps take rows round-robin, read them with 128-bit shared loads,
@@ -62,7 +62,7 @@ struct Layout {
   // ahead of its last completion (mbarrier parity waits see one phase back)
   __host__ __device__ explicit Layout(int backbone) {
     halves = backbone == NGDB_BETAE ? 2 : 1;
-    const int d = 49152 / (halves * HP * 4) / kCWarps * kCWarps;
+    const int d = 32768 / (halves * HP * 4) / kCWarps * kCWarps;
     depth = d < kCWarps ? kCWarps : (d > 32 ? 32 : d);
   }
   __host__ __device__ int row_floats() const { return halves * HP; }
@@ -89,43 +89,51 @@ __device__ __forceinline__ float mul_sign(float m, float t) {
 
 // Per-backbone distance of one padded row against the lane's query slice and
 // its gradient contribution coef * dd/dq.
+// The query slice is NOT held in registers: it is re-read from the shared
+// query buffer for every row (LDS.128; the mbarrier waits clobber memory), which
+// keeps the consumers at <= 72 registers -> 3 CTAs (24 consumer warps) per SM.
 template <int BB, int NCH>
 struct RowMath {
-  float4 qc[NCH], qo[NCH];  // query halves (Q2B centre / offset; BetaE alpha / beta)
+  const float* qs;          // padded query in shared memory (two halves)
+  int lane;
   float4 gc[NCH], go[NCH];  // dL/dq accumulators
   float4 t[NCH], t2[NCH];   // per-row values kept between distance and gradient
 
-  __device__ void load_q(const float* qs, int lane) {
+  __device__ float4 qc(int i) const { return ld4(qs + 4 * (lane + 32 * i)); }
+  __device__ float4 qo(int i) const { return ld4(qs + Layout<NCH>::HP + 4 * (lane + 32 * i)); }
+
+  __device__ void load_q(const float* q, int l) {
+    qs = q;
+    lane = l;
 #pragma unroll
-    for (int i = 0; i < NCH; ++i) {
-      qc[i] = ld4(qs + 4 * (lane + 32 * i));
-      qo[i] = BB != NGDB_GQE ? ld4(qs + Layout<NCH>::HP + 4 * (lane + 32 * i)) : f4(0.f);
-      gc[i] = go[i] = f4(0.f);
-    }
+    for (int i = 0; i < NCH; ++i) gc[i] = go[i] = f4(0.f);
   }
   // the lane's part of d_j (warp-summed by the caller)
-  __device__ float distance(const float* row, int lane, float alpha) {
+  __device__ float distance(const float* row, int /*lane*/, float alpha) {
     float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
     for (int i = 0; i < NCH; ++i) {
       const float4 v = ld4(row + 4 * (lane + 32 * i));
+      const float4 c = qc(i);
       if constexpr (BB == NGDB_BETAE) {
         const float4 v2 = ld4(row + Layout<NCH>::HP + 4 * (lane + 32 * i));
+        const float4 o = qo(i);
         t[i] = v;
         t2[i] = v2;
-        s0 += qc[i].x * v.x + qo[i].x * v2.x;
-        s1 += qc[i].y * v.y + qo[i].y * v2.y;
-        s2 += qc[i].z * v.z + qo[i].z * v2.z;
-        s3 += qc[i].w * v.w + qo[i].w * v2.w;
+        s0 += c.x * v.x + o.x * v2.x;
+        s1 += c.y * v.y + o.y * v2.y;
+        s2 += c.z * v.z + o.z * v2.z;
+        s3 += c.w * v.w + o.w * v2.w;
       } else {
-        t[i] = make_float4(v.x - qc[i].x, v.y - qc[i].y, v.z - qc[i].z, v.w - qc[i].w);
+        t[i] = make_float4(v.x - c.x, v.y - c.y, v.z - c.z, v.w - c.w);
         if constexpr (BB == NGDB_GQE) {
           s0 += fabsf(t[i].x); s1 += fabsf(t[i].y); s2 += fabsf(t[i].z); s3 += fabsf(t[i].w);
         } else {  // outside part max(|t|-o, 0) in s0/s1, inside part min(|t|, o) in s2/s3
-          s0 += fmaxf(fabsf(t[i].x) - qo[i].x, 0.f) + fmaxf(fabsf(t[i].y) - qo[i].y, 0.f);
-          s1 += fmaxf(fabsf(t[i].z) - qo[i].z, 0.f) + fmaxf(fabsf(t[i].w) - qo[i].w, 0.f);
-          s2 += fminf(fabsf(t[i].x), qo[i].x) + fminf(fabsf(t[i].y), qo[i].y);
-          s3 += fminf(fabsf(t[i].z), qo[i].z) + fminf(fabsf(t[i].w), qo[i].w);
+          const float4 o = qo(i);
+          s0 += fmaxf(fabsf(t[i].x) - o.x, 0.f) + fmaxf(fabsf(t[i].y) - o.y, 0.f);
+          s1 += fmaxf(fabsf(t[i].z) - o.z, 0.f) + fmaxf(fabsf(t[i].w) - o.w, 0.f);
+          s2 += fminf(fabsf(t[i].x), o.x) + fminf(fabsf(t[i].y), o.y);
+          s3 += fminf(fabsf(t[i].z), o.z) + fminf(fabsf(t[i].w), o.w);
         }
       }
     }
@@ -147,9 +155,10 @@ struct RowMath {
         gc[i].w -= mul_sign(coef, t[i].w);
       } else {  // outside the box: dc = -sign, do = alpha - 1; inside: dc = -alpha sign
         const float ca = coef * alpha, co = coef * (alpha - 1.f);
+        const float4 o = qo(i);
 #define NGDB_Q2B_GRAD(X)                               \
   {                                                    \
-    const bool out = fabsf(t[i].X) > qo[i].X;          \
+    const bool out = fabsf(t[i].X) > o.X;              \
     gc[i].X -= mul_sign(out ? coef : ca, t[i].X);      \
     go[i].X += out ? co : 0.f;                         \
   }
@@ -170,7 +179,7 @@ __device__ __forceinline__ float beta_qterm(const DevArgs& a, const float* q, in
 }
 
 template <int BB, int NCH, int MODE>
-__global__ void __launch_bounds__(kThreads, 2) stream_kernel(DevArgs a, int first, int n, int S) {
+__global__ void __launch_bounds__(kThreads, 3) stream_kernel(DevArgs a, int first, int n, int S) {
   extern __shared__ __align__(128) float smem[];
   __shared__ float lred[2 * kCWarps];
   __shared__ int last_flag;
