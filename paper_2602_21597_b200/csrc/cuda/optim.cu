@@ -77,7 +77,7 @@ inline size_t adam_smem_bytes(int width) {
 }
 
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a, SparseTable t,
+__global__ void __launch_bounds__(kAdamThreads, 4) entity_adam_kernel(DevArgs a, SparseTable t,
                                                                    AdamHyper hp, const float* bc,
                                                                    int rows_per_cta) {
   extern __shared__ __align__(128) float smem[];
@@ -135,15 +135,11 @@ __global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a,
       my_code = __ldg(t.contrib + beg + lane);
       if (my_code >= 0) my_coef = __ldg(a.coefbuf + my_code);
     }
-    const float* ws = ring + slot * 3 * W;
+    const float* ws = ring + slot * 3 * W;  // theta, m, v stay in shared memory
     mbar_wait_parity(&full[slot], round & 1);
-    float4 w[NCH], g[NCH];
+    float4 g[NCH];
 #pragma unroll
-    for (int i = 0; i < NCH; ++i) {
-      const int c = lane + 32 * i;
-      if (c < w4) w[i] = ld4(ws + 4 * c);
-      g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int i = 0; i < NCH; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k0 = beg; k0 < end; k0 += 32) {
       const int nk = min(32, end - k0);
       if (k0 > beg) {
@@ -176,10 +172,11 @@ __global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a,
               const float4 qc = ld4(q + 4 * c);
               float4 qo = make_float4(0.f, 0.f, 0.f, 0.f);
               if (BB == NGDB_Q2B) qo = ld4(q + a.dim + 4 * c);
-              g[i].x += cand_grad<BB>(w[i].x, qc.x, qo.x, coef, a.alpha_box);
-              g[i].y += cand_grad<BB>(w[i].y, qc.y, qo.y, coef, a.alpha_box);
-              g[i].z += cand_grad<BB>(w[i].z, qc.z, qo.z, coef, a.alpha_box);
-              g[i].w += cand_grad<BB>(w[i].w, qc.w, qo.w, coef, a.alpha_box);
+              const float4 w = ld4(ws + 4 * c);
+              g[i].x += cand_grad<BB>(w.x, qc.x, qo.x, coef, a.alpha_box);
+              g[i].y += cand_grad<BB>(w.y, qc.y, qo.y, coef, a.alpha_box);
+              g[i].z += cand_grad<BB>(w.z, qc.z, qo.z, coef, a.alpha_box);
+              g[i].w += cand_grad<BB>(w.w, qc.w, qo.w, coef, a.alpha_box);
             }
           }
         }
@@ -194,7 +191,7 @@ __global__ void __launch_bounds__(kAdamThreads, 3) entity_adam_kernel(DevArgs a,
       if (c < w4) {
         if (t.dbg_g) st4(t.dbg_g + row * W + 4 * c, g[i]);
         float4 m = ld4(ws + W + 4 * c), v = ld4(ws + 2 * W + 4 * c);
-        const float4 nw = adam4(w[i], m, v, g[i], k);
+        const float4 nw = adam4(ld4(ws + 4 * c), m, v, g[i], k);
         st4(wp + 4 * c, nw);
         st4(mp + 4 * c, m);
         st4(vp + 4 * c, v);
@@ -333,8 +330,8 @@ int launch_sparse_adam_entity(const DevArgs& a, const SparseTable& t, const Adam
   if (t.n_rows <= 0) return 0;
   if (a.backbone == NGDB_BETAE) return launch_beta_entity_adam(a, t, hp, bc, lc);
   const size_t smem = adam_smem_bytes(t.width);
-  // persistent-style grid: ~3 CTAs per SM, contiguous row ranges
-  const int ctas = std::max(1, std::min(t.n_rows, 3 * lc.num_sms));
+  // persistent-style grid: 4 CTAs per SM (56 registers, 38 KB rings), contiguous row ranges
+  const int ctas = std::max(1, std::min(t.n_rows, 4 * lc.num_sms));
   const int rows_per_cta = (t.n_rows + ctas - 1) / ctas;
   const int grid = (t.n_rows + rows_per_cta - 1) / rows_per_cta;
   auto go = [&](auto kernel) {
