@@ -23,9 +23,7 @@ namespace {
 
 constexpr int BM = 128, BN = 80, BK = 32;
 constexpr int kThreads = 256;   // 8 warps; warps w and w+4 share TMEM lane quarter w%4
-// smem operand ring depth: 2 stages (104 KB, two CTAs per SM) for the
-// latency-bound small-M launches, 4 stages (208 KB, one CTA per SM, three
-// chunks in flight) for launches of more tiles than two waves can hold
+constexpr int kStages = 2;      // smem operand ring; 104 KB -> two CTAs per SM
 constexpr int kTmemCols = 256;  // 2 accumulator buffers of BN columns (power of two)
 constexpr int kHalfCols = BN / 2;
 constexpr int kMaxProblems = 4;
@@ -33,7 +31,7 @@ constexpr int kMaxProblems = 4;
 constexpr int A_TILE = BM * BK * 4;  // 16 KB (128 rows x 128 B)
 constexpr int B_TILE = BN * BK * 4;  // 10 KB
 constexpr int STAGE = 2 * A_TILE + 2 * B_TILE;  // A_hi, A_lo, B_hi, B_lo
-constexpr int smem_bytes(int stages) { return stages * STAGE + 64; }
+constexpr int SMEM_BYTES = kStages * STAGE + 64;
 // epilogue staging tile [BM][BN+4]: 16-byte aligned rows; float4 stores of a
 // quarter-warp (8 consecutive rows) and float4 reads along a row are
 // bank-conflict free
@@ -164,9 +162,7 @@ __device__ __forceinline__ void drain(uint32_t tmem, int buf, float* acc) {
   for (int j = 0; j < kHalfCols; ++j) acc[j] += __uint_as_float(r[j]);
 }
 
-template <int kStages>
-__global__ void __launch_bounds__(kThreads, kStages == 2 ? 2 : 1)
-    tc_gemm_kernel(const __grid_constant__ TcGemmBatch batch) {
+__global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_constant__ TcGemmBatch batch) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t s_base = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * STAGE);  // [kStages]
@@ -425,8 +421,7 @@ __global__ void split_t_multi_kernel(SplitJobs jobs) {
 void tc_gemm_init() {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(2));
-    cudaFuncSetAttribute(tc_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(4));
+    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     configured = true;
   }
 }
@@ -451,13 +446,8 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   // per cluster (portable size) and at least 2 chunks per CTA
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
-  if (tiles > 2 * num_sms) {  // large M: throughput-bound, deep pipeline, no split-K
-    b.S = 1;
-    launch_pdl(tc_gemm_kernel<4>, dim3(tiles), dim3(kThreads), smem_bytes(4), s, 1, b);
-    return 1;
-  }
   b.S = std::max(1, std::min({8, (2 * num_sms) / std::max(tiles, 1), max_chunks / 2}));
-  launch_pdl(tc_gemm_kernel<2>, dim3(tiles * b.S), dim3(kThreads), smem_bytes(2), s, b.S, b);
+  launch_pdl(tc_gemm_kernel, dim3(tiles * b.S), dim3(kThreads), SMEM_BYTES, s, b.S, b);
   return 1;
 }
 
