@@ -46,7 +46,7 @@ __global__ void shard_query_pack_kernel(DevArgs a, int first, float* dst) {
 // lowest branch), loss terms, coef (routed to the argmin branch), and the
 // partial dL/dq of each branch slot. Shared: queries [3][wq], per-warp partial
 // dq [4][3][wq] summed in warp order (deterministic).
-template <int BB>
+template <int BB, int NCH>
 __global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardDev sd) {
   pdl_start();
   extern __shared__ __align__(16) float sm[];
@@ -72,15 +72,26 @@ __global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardD
     const int j = sd.owned[t];
     const int32_t ent = cand[j];
     const float* row = a.ent + static_cast<int64_t>(ent / sd.world) * a.ent_w;
+    // the candidate row once into registers, every 16-byte load in flight
+    float4 v[NCH];
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      v[i] = c < d4 ? ld4(row + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float dist[3];
     for (int b = 0; b < k; ++b) {
       const float* qc = qs + b * wq;
       float s = 0.f;
-      for (int c = lane; c < d4; c += 32) {
-        const float4 v = ld4(row + 4 * c), cc = ld4(qc + 4 * c);
-        const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        s += Dist<BB>::term(v.x, cc.x, oo.x, a.alpha_box) + Dist<BB>::term(v.y, cc.y, oo.y, a.alpha_box) +
-             Dist<BB>::term(v.z, cc.z, oo.z, a.alpha_box) + Dist<BB>::term(v.w, cc.w, oo.w, a.alpha_box);
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int c = lane + 32 * i;
+        if (c < d4) {
+          const float4 cc = ld4(qc + 4 * c);
+          const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          s += Dist<BB>::term(v[i].x, cc.x, oo.x, a.alpha_box) + Dist<BB>::term(v[i].y, cc.y, oo.y, a.alpha_box) +
+               Dist<BB>::term(v[i].z, cc.z, oo.z, a.alpha_box) + Dist<BB>::term(v[i].w, cc.w, oo.w, a.alpha_box);
+        }
       }
       dist[b] = warp_sum(s);
     }
@@ -93,17 +104,23 @@ __global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardD
         sd.coef_all[static_cast<int64_t>(gslot[b]) * a.ncand + j] = b == bm ? coef : 0.f;
     const float* qc = qs + bm * wq;
     float* pw = part + (warp * 3 + bm) * wq;
-    for (int c = lane; c < d4; c += 32) {
-      const float4 v = ld4(row + 4 * c), cc = ld4(qc + 4 * c);
-      const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-      float gc[4] = {0.f, 0.f, 0.f, 0.f}, go[4] = {0.f, 0.f, 0.f, 0.f};
-      Dist<BB>::grad(v.x, cc.x, oo.x, coef, a.alpha_box, gc[0], go[0]);
-      Dist<BB>::grad(v.y, cc.y, oo.y, coef, a.alpha_box, gc[1], go[1]);
-      Dist<BB>::grad(v.z, cc.z, oo.z, coef, a.alpha_box, gc[2], go[2]);
-      Dist<BB>::grad(v.w, cc.w, oo.w, coef, a.alpha_box, gc[3], go[3]);
-      for (int t2 = 0; t2 < 4; ++t2) {
-        pw[4 * c + t2] += gc[t2];
-        if (BB == NGDB_Q2B) pw[D + 4 * c + t2] += go[t2];
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const int c = lane + 32 * i;
+      if (c < d4) {
+        const float4 cc = ld4(qc + 4 * c);
+        const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 gc = make_float4(0.f, 0.f, 0.f, 0.f), go = gc;
+        Dist<BB>::grad(v[i].x, cc.x, oo.x, coef, a.alpha_box, gc.x, go.x);
+        Dist<BB>::grad(v[i].y, cc.y, oo.y, coef, a.alpha_box, gc.y, go.y);
+        Dist<BB>::grad(v[i].z, cc.z, oo.z, coef, a.alpha_box, gc.z, go.z);
+        Dist<BB>::grad(v[i].w, cc.w, oo.w, coef, a.alpha_box, gc.w, go.w);
+        float4 p = ld4(pw + 4 * c);
+        st4(pw + 4 * c, make_float4(p.x + gc.x, p.y + gc.y, p.z + gc.z, p.w + gc.w));
+        if (BB == NGDB_Q2B) {
+          p = ld4(pw + D + 4 * c);
+          st4(pw + D + 4 * c, make_float4(p.x + go.x, p.y + go.y, p.z + go.z, p.w + go.w));
+        }
       }
     }
   }
@@ -202,16 +219,21 @@ int launch_shard_score(const DevArgs& a, const ShardDev& sd, const LaunchCtx& lc
   const int units = sd.world * sd.batch;
   if (units <= 0) return 0;
   const size_t smem = static_cast<size_t>(3 + kWarps * 3) * a.wq * sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(shard_score_kernel<NGDB_GQE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(shard_score_kernel<NGDB_Q2B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    configured = true;
+  auto go = [&](auto kernel) {
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      configured = true;
+    }
+    launch_pdl(kernel, dim3(units), dim3(kThreads), smem, lc.stream, 1, a, sd);
+  };
+  if (a.dim <= 512) {
+    if (a.backbone == NGDB_GQE) go(shard_score_kernel<NGDB_GQE, 4>);
+    else go(shard_score_kernel<NGDB_Q2B, 4>);
+  } else {
+    if (a.backbone == NGDB_GQE) go(shard_score_kernel<NGDB_GQE, 8>);
+    else go(shard_score_kernel<NGDB_Q2B, 8>);
   }
-  if (a.backbone == NGDB_GQE)
-    launch_pdl(shard_score_kernel<NGDB_GQE>, dim3(units), dim3(kThreads), smem, lc.stream, 1, a, sd);
-  else
-    launch_pdl(shard_score_kernel<NGDB_Q2B>, dim3(units), dim3(kThreads), smem, lc.stream, 1, a, sd);
   return 1;
 }
 
