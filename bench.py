@@ -323,13 +323,15 @@ def bench_sharded(args):
     torch.cuda.synchronize()
     fams = {}
     for f in range(lib.ngdb_profile_families()):
-        fms, fl, fb = C.c_double(), C.c_int64(), C.c_double()
+        fms, fl, fb, ff = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
         check(lib.ngdb_profile_read(ctx, f, C.byref(fms), C.byref(fl), C.byref(fb)))
+        check(lib.ngdb_profile_flops(ctx, f, C.byref(ff)))
         if fl.value:
             fams[lib.ngdb_profile_family_name(f).decode()] = {
                 "ms_per_step": fms.value / n_prof, "launches_per_step": fl.value / n_prof,
                 "gbs": fb.value / (fms.value / 1000.0) / 1e9 if fms.value > 0 else 0.0,
-                "bytes_per_step": fb.value / n_prof, "flops_per_step": 0.0, "tflops": 0.0}
+                "tflops": ff.value / (fms.value / 1000.0) / 1e12 if fms.value > 0 else 0.0,
+                "bytes_per_step": fb.value / n_prof, "flops_per_step": ff.value / n_prof}
     check(lib.ngdb_profile_enable(ctx, 0))
     # e2e: host planning (sampling, DAG, Max-Fillness, metadata all-gather, owner
     # lists) + every stage and collective, per step
