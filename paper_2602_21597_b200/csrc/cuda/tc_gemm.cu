@@ -276,28 +276,25 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
       const int row = m0 + r, n = n0 + cq;
       if (row >= g.M || n >= g.N) continue;
       const uint32_t off = static_cast<uint32_t>((r * kTileStride + cq) * 4);
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int p0 = 0; p0 < S; p0 += 8) {  // rank order; 8 partial loads in flight
-        float4 part[8];
+      float4 part[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int p = p0 + q;
-          if (p >= S) break;
-          if (p == rank) {
-            part[q] = *reinterpret_cast<const float4*>(&tile_s[r * kTileStride + cq]);
-          } else {
-            uint32_t remote;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
-            asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(part[q].x), "=f"(part[q].y), "=f"(part[q].z), "=f"(part[q].w)
-                         : "r"(remote));
-          }
+      for (int p = 0; p < 8; ++p) {
+        if (p >= S) break;
+        if (p == rank) {
+          part[p] = *reinterpret_cast<const float4*>(&tile_s[r * kTileStride + cq]);
+        } else {
+          uint32_t remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
+          asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(part[p].x), "=f"(part[p].y), "=f"(part[p].z), "=f"(part[p].w)
+                       : "r"(remote));
         }
+      }
+      float4 v = part[0];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (p0 + q >= S) break;
-          v.x += part[q].x; v.y += part[q].y; v.z += part[q].z; v.w += part[q].w;
-        }
+      for (int p = 1; p < 8; ++p) {
+        if (p >= S) break;
+        v.x += part[p].x; v.y += part[p].y; v.z += part[p].z; v.w += part[p].w;
       }
       float* crow =
           g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
@@ -425,7 +422,6 @@ void tc_gemm_init() {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     configured = true;
   }
 }
@@ -447,25 +443,10 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   if (b.n == 0) return 0;
   b.tile_begin[b.n] = tiles;
   // split-K so the launch fills about one wave (2 CTAs per SM), at most 8 CTAs
-  // per cluster (portable size) and at least 2 chunks per CTA; a long K (the
-  // weight gradients over thousands of rows) is split further — up to the
-  // largest cluster the device co-schedules (16, non-portable) — so that no
-  // CTA walks more than ~32 chunks, even at the cost of extra waves
+  // per cluster (portable size) and at least 2 chunks per CTA
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
-  static int max_cluster = 0;
-  if (!max_cluster) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(16 * 64);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
-    int mc = 8;
-    if (cudaOccupancyMaxPotentialClusterSize(&mc, tc_gemm_kernel, &cfg) != cudaSuccess) mc = 8;
-    cudaGetLastError();
-    max_cluster = std::max(1, std::min(16, mc));
-  }
   b.S = std::max(1, std::min({8, (2 * num_sms) / std::max(tiles, 1), max_chunks / 2}));
-  if (max_chunks / b.S > 32) b.S = std::max(b.S, std::min(max_cluster, max_chunks / 32));
   launch_pdl(tc_gemm_kernel, dim3(tiles * b.S), dim3(kThreads), SMEM_BYTES, s, b.S, b);
   return 1;
 }
