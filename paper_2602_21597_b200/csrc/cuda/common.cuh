@@ -119,6 +119,13 @@ __device__ __forceinline__ void pdl_start() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// The two halves of pdl_start(), for kernels that read step-invariant plan
+// data (node descriptors, CSR) before waiting: the descriptor loads then
+// overlap the previous kernel's tail. Nothing written by an earlier kernel may
+// be read before pdl_wait().
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -65,10 +65,11 @@ namespace {
 // M[i] = mean_l x_l (plain + split); optionally G[i] = upstream grad (plain + split)
 __global__ void gqe_pack_kernel(DevArgs a, KSpan ks, int first, float* M, Split Ms, float* G,
                                 Split Gs) {
-  pdl_start();
+  pdl_launch();
   const int i = blockIdx.x;
   const int k = ks.k(i);
-  const ngdb_node_desc d = a.nodes[first + i];
+  const ngdb_node_desc d = a.nodes[first + i];  // plan data: before the wait
+  pdl_wait();
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < a.dim; e += blockDim.x * gridDim.y) {
     float s = 0.f;
@@ -80,10 +81,11 @@ __global__ void gqe_pack_kernel(DevArgs a, KSpan ks, int first, float* M, Split 
 }
 // G_X row l of node i = dM[i] / k  (mean adjoint)
 __global__ void gqe_scatter_kernel(DevArgs a, KSpan ks, int first, const float* dM) {
-  pdl_start();
+  pdl_launch();
   const int i = blockIdx.x;
   const int k = ks.k(i);
-  const ngdb_node_desc d = a.nodes[first + i];
+  const ngdb_node_desc d = a.nodes[first + i];  // plan data: before the wait
+  pdl_wait();
   const float inv_k = 1.f / static_cast<float>(k);
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < a.dim; e += blockDim.x * gridDim.y) {
     const float v = dM[(int64_t)i * a.dim + e] * inv_k;
@@ -152,10 +154,11 @@ int gqe_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
 
 __global__ void q2b_pack_kernel(DevArgs a, KSpan ks, int first, float* Cin, Split Cs, float* Oin,
                                 Split Os) {
-  pdl_start();
+  pdl_launch();
   const int i = blockIdx.x;
   const int k = ks.k(i), r0 = ks.row0(i);
-  const ngdb_node_desc d = a.nodes[first + i];
+  const ngdb_node_desc d = a.nodes[first + i];  // plan data: before the wait
+  pdl_wait();
   for (int l = 0; l < k; ++l)
     for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < a.dim; e += blockDim.x * gridDim.y) {
       const int64_t r = ((int64_t)r0 + l) * a.dim + e;
@@ -201,11 +204,12 @@ __device__ __forceinline__ float* q2b_stash(const DevArgs& a, int slot) {
 __global__ void q2b_combine_kernel(DevArgs a, KSpan ks, int first, const float* S, const float* U,
                                    const float* Cin, const float* Oin, const float* Z,
                                    const float* P, const float* Lm) {
-  pdl_start();
+  pdl_launch();
   const int i = blockIdx.x;
   const int D = a.dim;
   const int k = ks.k(i);
-  const ngdb_node_desc d = a.nodes[first + i];
+  const ngdb_node_desc d = a.nodes[first + i];  // plan data: before the wait
+  pdl_wait();
   const int64_t base = (int64_t)ks.row0(i) * D;
   float* st = q2b_stash(a, d.aux);
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
@@ -231,11 +235,12 @@ __global__ void q2b_combine_kernel(DevArgs a, KSpan ks, int first, const float* 
 __global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Cin, float* Oin,
                                        float* Z, float* Lm, float* gS, Split gSs, float* dCin,
                                        float* dOin, float* gU, Split gUs) {
-  pdl_start();
+  pdl_launch();
   const int i = blockIdx.x;
   const int D = a.dim;
   const int k = ks.k(i);
-  const ngdb_node_desc d = a.nodes[first + i];
+  const ngdb_node_desc d = a.nodes[first + i];  // plan data: before the wait
+  pdl_wait();
   const int64_t base = (int64_t)ks.row0(i) * D;
   const float* st = q2b_stash(a, d.aux);
   const float* S = st + 3 * D;  // the node's k score rows, stashed by the forward
@@ -287,11 +292,12 @@ __global__ void q2b_gp_kernel(DevArgs a, const float* gLm, KSpan ks, int first, 
 }
 __global__ void q2b_scatter_kernel(DevArgs a, KSpan ks, int first, const float* dCin,
                                    const float* dOin) {
-  pdl_start();
+  pdl_launch();
   const int i = blockIdx.x;
   const int D = a.dim;
   const int k = ks.k(i), r0 = ks.row0(i);
-  const ngdb_node_desc d = a.nodes[first + i];
+  const ngdb_node_desc d = a.nodes[first + i];  // plan data: before the wait
+  pdl_wait();
   for (int l = 0; l < k; ++l)
     for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
       const int64_t r = ((int64_t)r0 + l) * D + e;

@@ -32,11 +32,12 @@ __device__ __forceinline__ bool bad_index(const DevArgs& a, int32_t id, int32_t 
 template <int NCH>
 __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, int first, int n,
                                                             int n_entities) {
-  pdl_start();
+  pdl_launch();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
-  const ngdb_node_desc d = a.nodes[first + node];
+  const ngdb_node_desc d = a.nodes[first + node];  // plan data: before the wait
+  pdl_wait();
   if (bad_index(a, d.id, n_entities)) return;
   const int ew4 = a.ent_w / 4;
   float4 u[NCH];
@@ -74,11 +75,12 @@ __device__ __forceinline__ float4 add4(float4 u, float4 v) {
 template <int NCH>
 __global__ void __launch_bounds__(kWarps * 32) project_kernel(DevArgs a, int dir, int first, int n,
                                                               int n_relations) {
-  pdl_start();
+  pdl_launch();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
-  const ngdb_node_desc d = a.nodes[first + node];
+  const ngdb_node_desc d = a.nodes[first + node];  // plan data: before the wait
+  pdl_wait();
   if (bad_index(a, d.id, n_relations)) return;
   const float* r = a.rel + static_cast<int64_t>(d.id) * a.rel_w;
   const float* x = a.arena + d.in[0];
@@ -142,11 +144,12 @@ __global__ void __launch_bounds__(kWarps * 32) project_kernel(DevArgs a, int dir
 
 template <int NCH>
 __global__ void __launch_bounds__(kWarps * 32) negate_kernel(DevArgs a, int dir, int first, int n) {
-  pdl_start();
+  pdl_launch();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
-  const ngdb_node_desc d = a.nodes[first + node];
+  const ngdb_node_desc d = a.nodes[first + node];  // plan data: before the wait
+  pdl_wait();
   const float* src = a.arena + (dir == 0 ? d.in[0] : d.grad);
   float* out = a.arena + d.out;
   const int w4 = a.wq / 4;
@@ -209,11 +212,12 @@ __global__ void __launch_bounds__(256) union_kernel(DevArgs a, int dir, int k, i
 // dL/dd (union); the mirror materialises it into its planned arena slot.
 template <int NCH>
 __global__ void __launch_bounds__(kWarps * 32) loss_bwd_kernel(DevArgs a, int first, int n) {
-  pdl_start();
+  pdl_launch();
   const int node = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (node >= n) return;
-  const ngdb_node_desc d = a.nodes[first + node];
+  const ngdb_node_desc d = a.nodes[first + node];  // plan data: before the wait
+  pdl_wait();
   float* out = a.arena + d.out;
   if (d.aux >= 0) {
     const float* src = a.dqbuf + static_cast<int64_t>(d.aux) * a.wq;
