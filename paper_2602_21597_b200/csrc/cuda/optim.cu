@@ -93,7 +93,11 @@ __global__ void __launch_bounds__(kAdamThreads, 4) entity_adam_kernel(DevArgs a,
     mbar_fence_init();
   }
   __syncthreads();
-  pdl_start();
+  // The producer streams theta, m, v before waiting on the previous kernel:
+  // they are written only by this kernel (plus the row ids: plan data), so
+  // the reads overlap the tail of the step's last pool. The consumers wait
+  // before they read any gradient input or write a row.
+  pdl_launch();
   const int r_beg = blockIdx.x * rows_per_cta;
   const int n_mine = max(0, min(t.n_rows, r_beg + rows_per_cta) - r_beg);
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -120,6 +124,7 @@ __global__ void __launch_bounds__(kAdamThreads, 4) entity_adam_kernel(DevArgs a,
     }
     return;
   }
+  pdl_wait();
   const int w4 = W / 4;
   const AdamK k = adam_consts(hp, bc);
   for (int u = warp; u < n_mine; u += kAdamConsumers) {
