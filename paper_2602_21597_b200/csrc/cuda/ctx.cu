@@ -16,7 +16,6 @@
 #include <vector>
 
 #include "common.cuh"
-#include "tc_gemm.cuh"
 
 using namespace ngdb_dev;
 
@@ -202,8 +201,6 @@ struct ngdb_ctx {
   int32_t istash_slots = 0;
   float* pstash = nullptr;           // BetaE Project stash (DevArgs::pstash)
   int32_t pstash_slots = 0;
-  float* gemm_ws = nullptr;          // split-K partial tiles (tc_gemm_bind_workspace)
-  int* gemm_counters = nullptr;
   float* lpart = nullptr;            // fused score+loss partials (DevArgs::lpart)
   float* lpart_scalar = nullptr;
   int32_t* lcount = nullptr;
@@ -388,9 +385,6 @@ void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
 }
 
 DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
-  // every launch sequence builds its args here first: bind this context's
-  // GEMM split-K workspace for the calling thread
-  tc_gemm_bind_workspace(c->gemm_ws, kGemmWsFloats, c->gemm_counters, kGemmCounters);
   DevArgs a{};
   a.backbone = c->desc.backbone;
   a.dim = c->desc.dim;
@@ -875,9 +869,6 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     c->scratch_cap = intersect_scratch_floats(d.backbone, d.dim, c->desc.max_batch);
     c->istash_slots = std::max(c->desc.max_queries, 1);
     c->istash = dmalloc<float>(int64_t(c->istash_slots) * kStashPerSlot * d.dim);
-    c->gemm_ws = dmalloc<float>(kGemmWsFloats);
-    c->gemm_counters = reinterpret_cast<int*>(dmalloc<float>(kGemmCounters));
-    CK(cudaMemset(c->gemm_counters, 0, kGemmCounters * sizeof(int)));
     if (d.backbone == NGDB_BETAE) {  // <= 4 Project nodes per query after DNF
       c->pstash_slots = 4 * std::max(c->desc.max_queries, 1);
       c->pstash = dmalloc<float>(int64_t(c->pstash_slots) * 4 * d.dim);
@@ -921,8 +912,6 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   if (c->anchor_local) cudaFree(c->anchor_local);
   if (c->fscratch) cudaFree(c->fscratch);
   if (c->istash) cudaFree(c->istash);
-  if (c->gemm_ws) cudaFree(c->gemm_ws);
-  if (c->gemm_counters) cudaFree(c->gemm_counters);
   if (c->pstash) cudaFree(c->pstash);
   if (c->lpart) cudaFree(c->lpart);
   if (c->lpart_scalar) cudaFree(c->lpart_scalar);

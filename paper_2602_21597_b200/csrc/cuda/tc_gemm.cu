@@ -41,15 +41,8 @@ struct TcGemmBatch {
   TcGemmArgs p[kMaxProblems];
   int tile_begin[kMaxProblems + 1];
   int n;
-  int S;          // K-split factor
-  float* ws;      // split-K partial tiles [tiles][S][BM][BN]
-  int* counters;  // per-tile arrival counters (zero between launches)
+  int S;  // K-split factor == cluster size
 };
-
-// split-K workspace of the calling thread's context (tc_gemm_bind_workspace)
-thread_local float* g_ws = nullptr;
-thread_local int* g_counters = nullptr;
-thread_local int64_t g_ws_floats = 0, g_n_counters = 0;
 
 // UMMA instruction descriptor: D=f32, A=B=tf32, both K-major, M=128, N=80.
 constexpr uint32_t kInstrDesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -257,54 +250,52 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
   }
   asm volatile("cp.async.wait_group 0;");
 
-  // Split-K: every CTA of a tile writes its partial tile to the workspace (L2)
-  // and bumps the tile's counter; the last one sums the S partials in rank
-  // order (deterministic) and runs the epilogue for the whole tile. No cluster,
-  // no barriers between CTAs: the other CTAs exit at once.
-  __shared__ int last_flag;
-  float* tile_s = reinterpret_cast<float*>(smem);  // [BM][kTileStride] staging (S == 1)
-  const int r_own = (warp & 3) * 32 + (threadIdx.x & 31), cb = (warp >> 2) * kHalfCols;
-  const float* src_tile = tile_s;  // rows of the summed tile
-  int src_stride = kTileStride;
-  if (S > 1) {
-    float* part = batch.ws + (static_cast<int64_t>(tile) * S + rank) * (BM * BN);
+  // Stage this CTA's (partial) tile row-major in its own shared memory.
+  float* tile_s = reinterpret_cast<float*>(smem);
+  {
+    const int r = (warp & 3) * 32 + (threadIdx.x & 31), cb = (warp >> 2) * kHalfCols;
 #pragma unroll
     for (int j = 0; j < kHalfCols; j += 4)
-      *reinterpret_cast<float4*>(&part[r_own * BN + cb + j]) =
-          make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last_flag = atomicAdd(&batch.counters[tile], 1) == S - 1;
-    __syncthreads();
-    if (!last_flag) goto done;
-    __threadfence();  // the other ranks' partials are visible
-    // sum the S partials (rank order) into the staging tile
-    const float* base = batch.ws + static_cast<int64_t>(tile) * S * (BM * BN);
-    for (int it = threadIdx.x; it < BM * BN / 4; it += kThreads) {
-      const int r = it / (BN / 4), cq = (it % (BN / 4)) * 4;
-      float4 v = *reinterpret_cast<const float4*>(base + r * BN + cq);
-      for (int p = 1; p < S; ++p) {
-        const float4 u = *reinterpret_cast<const float4*>(base + static_cast<int64_t>(p) * (BM * BN) + r * BN + cq);
-        v.x += u.x; v.y += u.y; v.z += u.z; v.w += u.w;
-      }
-      *reinterpret_cast<float4*>(&tile_s[r * kTileStride + cq]) = v;
-    }
-    if (threadIdx.x == 0) batch.counters[tile] = 0;  // ready for the next launch
-  } else {
-#pragma unroll
-    for (int j = 0; j < kHalfCols; j += 4)
-      *reinterpret_cast<float4*>(&tile_s[r_own * kTileStride + cb + j]) =
+      *reinterpret_cast<float4*>(&tile_s[r * kTileStride + cb + j]) =
           make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
   }
-  __syncthreads();
+  // Split-K reduce-scatter over distributed shared memory: CTA `rank` owns rows
+  // [r_beg, r_end) of the tile, sums them over the S partial tiles in rank
+  // order (deterministic) and writes them out; all S CTAs share the work.
+  const int r_beg = rank * BM / S, r_end = (rank + 1) * BM / S;
+  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+  else __syncthreads();
+  const uint32_t local = smem_u32(tile_s);
   if (((g.N | g.ldc) & 3) == 0) {
-    // float4 epilogue over the whole tile
+    // float4 epilogue: thread t takes 16-byte column groups of the CTA's rows;
+    // the S partial loads are all issued before they are summed
     constexpr int kQ = BN / 4;
-    for (int it = threadIdx.x; it < BM * kQ; it += kThreads) {
-      const int r = it / kQ, cq = (it % kQ) * 4;
+    const int n_items = (r_end - r_beg) * kQ;
+    for (int it = threadIdx.x; it < n_items; it += kThreads) {
+      const int r = r_beg + it / kQ, cq = (it % kQ) * 4;
       const int row = m0 + r, n = n0 + cq;
       if (row >= g.M || n >= g.N) continue;
-      float4 v = *reinterpret_cast<const float4*>(&src_tile[r * src_stride + cq]);
+      const uint32_t off = static_cast<uint32_t>((r * kTileStride + cq) * 4);
+      float4 part[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        if (p >= S) break;
+        if (p == rank) {
+          part[p] = *reinterpret_cast<const float4*>(&tile_s[r * kTileStride + cq]);
+        } else {
+          uint32_t remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
+          asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(part[p].x), "=f"(part[p].y), "=f"(part[p].z), "=f"(part[p].w)
+                       : "r"(remote));
+        }
+      }
+      float4 v = part[0];
+#pragma unroll
+      for (int p = 1; p < 8; ++p) {
+        if (p >= S) break;
+        v.x += part[p].x; v.y += part[p].y; v.z += part[p].z; v.w += part[p].w;
+      }
       float* crow =
           g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
       if (g.bias) {
@@ -337,26 +328,43 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
       }
     }
   } else {
-    for (int it = threadIdx.x; it < BM * BN; it += kThreads) {
-      const int r = it / BN, cc = it % BN;
-      const int row = m0 + r, n = n0 + cc;
-      if (row >= g.M || n >= g.N) continue;
-      float v = src_tile[r * src_stride + cc];
+    const int lane = threadIdx.x & 31;
+    for (int r = r_beg + warp; r < r_end; r += kThreads / 32) {
+      const int row = m0 + r;
+      if (row >= g.M) break;
       float* crow =
           g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
-      if (g.bias) v += g.bias[n];
-      if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;
-      if (g.accumulate) v += crow[n];
-      crow[n] = v;
-      if (g.s_hi) {
-        float h, l;
-        split_tf32(g.s_relu ? fmaxf(v, 0.f) : v, h, l);
-        g.s_hi[(int64_t)row * g.ldc + n] = h;
-        g.s_lo[(int64_t)row * g.ldc + n] = l;
+      for (int cc = lane; cc < BN; cc += 32) {
+        const int n = n0 + cc;
+        if (n >= g.N) break;
+        float v = 0.f;
+        const uint32_t off = static_cast<uint32_t>((r * kTileStride + cc) * 4);
+        for (int p = 0; p < S; ++p) {
+          if (p == rank) {
+            v += tile_s[r * kTileStride + cc];
+          } else {
+            uint32_t remote;
+            float pv;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv) : "r"(remote));
+            v += pv;
+          }
+        }
+        if (g.bias) v += g.bias[n];
+        if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;
+        if (g.accumulate) v += crow[n];
+        crow[n] = v;
+        if (g.s_hi) {
+          float h, l;
+          split_tf32(g.s_relu ? fmaxf(v, 0.f) : v, h, l);
+          g.s_hi[(int64_t)row * g.ldc + n] = h;
+          g.s_lo[(int64_t)row * g.ldc + n] = l;
+        }
       }
     }
   }
-done:
+  // peers' partial tiles must stay resident until every slice has been read
+  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
@@ -439,22 +447,11 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
   b.S = std::max(1, std::min({8, (2 * num_sms) / std::max(tiles, 1), max_chunks / 2}));
-  if (b.S > 1 && (!g_ws || int64_t(tiles) * b.S * BM * BN > g_ws_floats || tiles > g_n_counters))
-    b.S = 1;  // no (large enough) workspace bound: run unsplit
-  b.ws = g_ws;
-  b.counters = g_counters;
-  launch_pdl(tc_gemm_kernel, dim3(tiles * b.S), dim3(kThreads), SMEM_BYTES, s, 1, b);
+  launch_pdl(tc_gemm_kernel, dim3(tiles * b.S), dim3(kThreads), SMEM_BYTES, s, b.S, b);
   return 1;
 }
 
 int tc_gemm(const TcGemmArgs& g, cudaStream_t s) { return tc_gemm_batch(&g, 1, s); }
-
-void tc_gemm_bind_workspace(float* ws, int64_t ws_floats, int* counters, int64_t n_counters) {
-  g_ws = ws;
-  g_ws_floats = ws_floats;
-  g_counters = counters;
-  g_n_counters = n_counters;
-}
 
 int split_transposed(const SplitJobs& jobs, cudaStream_t s) {
   if (jobs.n <= 0) return 0;

@@ -45,13 +45,6 @@ struct TcGemmArgs {
 };
 
 int tc_gemm(const TcGemmArgs& g, cudaStream_t s);
-// Split-K workspace for the GEMMs launched from this host thread (the
-// context's; bound before each launch sequence): partial tiles + per-tile
-// counters that start at zero and are reset by the kernel. Without one, GEMMs
-// run unsplit.
-constexpr int64_t kGemmWsFloats = 296LL * 128 * 80;  // <= 2 CTAs per SM of 128x80 partials
-constexpr int64_t kGemmCounters = 1024;
-void tc_gemm_bind_workspace(float* ws, int64_t ws_floats, int* counters, int64_t n_counters);
 // Up to four independent problems in one launch (one dependency level).
 int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s);
 
