@@ -89,6 +89,8 @@ typedef struct ngdb_pool_desc {
   int32_t k;      /* cardinality class for Intersect/UnionScore, else 0 */
   int32_t first;  /* index of the first node descriptor */
   int32_t count;  /* number of nodes */
+  int32_t cycle;  /* Alg. 1 selection index: the invocations of one cycle drain one
+                     pool snapshot, so their nodes are independent of each other */
 } ngdb_pool_desc;
 
 /* A fully planned training step (host memory; copied by plan_create/step_begin).

@@ -86,6 +86,7 @@ struct Invocation {
   const int32_t* nodes = nullptr;
   int32_t n = 0;
   int32_t step = 0;
+  int32_t cycle = 0;  // selection index: the pops of one cycle are one drain
 };
 
 class Planner {

@@ -32,7 +32,8 @@ class NodeDesc(C.Structure):
 
 
 class PoolDesc(C.Structure):
-    _fields_ = [("kind", i32), ("dir", i32), ("k", i32), ("first", i32), ("count", i32)]
+    _fields_ = [("kind", i32), ("dir", i32), ("k", i32), ("first", i32), ("count", i32),
+                ("cycle", i32)]
 
 
 class StepPlan(C.Structure):

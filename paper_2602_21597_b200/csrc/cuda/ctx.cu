@@ -558,8 +558,29 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d,
 // launches and larger GEMMs. The invocation list (the trace) is unchanged.
 bool mergeable(const ngdb_ctx* c, const ngdb_pool_desc& a, const ngdb_pool_desc& b) {
   return a.kind == NGDB_OP_INTERSECT && b.kind == NGDB_OP_INTERSECT && a.dir == b.dir &&
-         a.count > 0 && b.count > 0 && b.first == a.first + a.count && a.k < b.k && b.k <= 3 &&
-         a.k >= 2 && a.count + b.count <= c->desc.max_batch;
+         a.cycle == b.cycle && a.count > 0 && b.count > 0 && b.first == a.first + a.count &&
+         a.k < b.k && b.k <= 3 && a.k >= 2 && a.count + b.count <= c->desc.max_batch;
+}
+
+// The ⌈n/B_max⌉ pops that drain one pool snapshot (same cycle) are
+// independent; for operators whose kernels have no per-invocation scratch they
+// run as one launch over the concatenated node range.
+bool drain_mergeable(const ngdb_ctx* c, const ngdb_pool_desc& a, const ngdb_pool_desc& b) {
+  if (a.kind != b.kind || a.dir != b.dir || a.cycle != b.cycle || a.k != b.k) return false;
+  if (a.count <= 0 || b.count <= 0 || b.first != a.first + a.count) return false;
+  switch (a.kind) {
+    case NGDB_OP_EMBED_ANCHOR:
+    case NGDB_OP_FUSE_SEMANTIC:
+    case NGDB_OP_NEGATE:
+    case NGDB_OP_UNION_SCORE:
+    case NGDB_OP_SCORE:
+    case NGDB_OP_LOSS:
+      return true;
+    case NGDB_OP_PROJECT:  // the BetaE projection MLP has B_max-sized scratch
+      return !c->beta();
+    default:
+      return false;
+  }
 }
 
 void flush_held(ngdb_ctx* c) {
@@ -568,15 +589,18 @@ void flush_held(ngdb_ctx* c) {
   exec_pool(c, c->active, c->held);
 }
 
-// Runs invocations in order, merging Intersect classes (mergeable()).
+// Runs invocations in order, merging Intersect classes (mergeable()) and the
+// pops of one drain (drain_mergeable()).
 void exec_pools(ngdb_ctx* c, const ngdb_plan* p, const std::vector<ngdb_pool_desc>& v) {
   for (size_t i = 0; i < v.size(); ++i) {
     if (i + 1 < v.size() && mergeable(c, v[i], v[i + 1])) {
       exec_pool(c, p, v[i], &v[i + 1]);
       ++i;
-    } else {
-      exec_pool(c, p, v[i]);
+      continue;
     }
+    ngdb_pool_desc d = v[i];
+    while (i + 1 < v.size() && drain_mergeable(c, d, v[i + 1])) d.count += v[++i].count;
+    exec_pool(c, p, d);
   }
 }
 

@@ -222,11 +222,11 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
             if (f.nodes[o].cardinality == k) cls.push_back(o);
           if (cls.empty()) continue;
           rec.classes.emplace_back(k, static_cast<int32_t>(cls.size()));
-          invoke(Invocation{type, k, cls.data(), static_cast<int32_t>(cls.size()), step});
+          invoke(Invocation{type, k, cls.data(), static_cast<int32_t>(cls.size()), step, cycle});
           ++tr.invocations;
         }
       } else {
-        invoke(Invocation{type, 0, batch.data(), static_cast<int32_t>(batch.size()), step});
+        invoke(Invocation{type, 0, batch.data(), static_cast<int32_t>(batch.size()), step, cycle});
         ++tr.invocations;
       }
 

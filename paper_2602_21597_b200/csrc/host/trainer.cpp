@@ -275,6 +275,7 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
     pd.k = inv.k;
     pd.first = static_cast<int32_t>(plan.nodes.size());
     pd.count = inv.n;
+    pd.cycle = inv.cycle;
     plan.pools.push_back(pd);
     for (int32_t t = 0; t < inv.n; ++t) {
       const int32_t o = inv.nodes[t];
