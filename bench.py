@@ -526,6 +526,8 @@ def main():
     step_no += args.steps
     b1, d1 = C.c_int64(), C.c_int64()
     check(lib.ngdb_transfer_bytes(ctx, C.byref(b1), C.byref(d1)))
+    gu, gi = C.c_int64(), C.c_int64()
+    check(lib.ngdb_graph_stats(ctx, C.byref(gu), C.byref(gi)))
     tim = eng.last_timings
     if dist is not None:
         import torch
@@ -584,7 +586,8 @@ def main():
                            "plan H2D, kernels, loss D2H per step)",
                     "producers": producers,
                     "consumer_ms_per_step": {k[:-2]: 1000 * v / args.steps for k, v in tim.items()},
-                    "sequential_train_step": seq_qps},
+                    "sequential_train_step": seq_qps,
+                    "step_graphs": {"updated": gu.value, "instantiated": gi.value}},
             "gpu_launches": int(launches),
             "clocks": clk,
             "families": fams if not args.quiet else None,

@@ -265,6 +265,9 @@ int64_t ngdb_launch_count(ngdb_ctx* ctx);
 /* Cumulative bytes of step data the streaming ABI copied: plan uploads (H2D)
  * and loss/flag read-backs (D2H). */
 int ngdb_transfer_bytes(ngdb_ctx* ctx, int64_t* h2d, int64_t* d2h);
+/* ngdb_step_launch graphs: launches served by updating a cached executable
+ * graph of the same invocation structure vs fresh instantiations. */
+int ngdb_graph_stats(ngdb_ctx* ctx, int64_t* updates, int64_t* instantiations);
 /* Flush L2 by writing a buffer larger than it (timing hygiene). */
 int ngdb_flush_l2(ngdb_ctx* ctx);
 

@@ -247,8 +247,21 @@ struct ngdb_ctx {
   int64_t next_ticket = 0;
   // streaming steps launched as CUDA graphs (ngdb_step_launch): two
   // alternating executable graphs, updated in place when the topology allows
-  cudaGraphExec_t step_exec[2] = {nullptr, nullptr};
-  int step_exec_cur = 0;
+  // small cache of executable step graphs keyed by the step's invocation
+  // structure: a step whose structure was seen before is launched through
+  // cudaGraphExecUpdate (new parameters, same topology) instead of a fresh
+  // instantiation; an entry is only touched once its last launch completed
+  struct ExecEntry {
+    uint64_t sig = 0;
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t done = nullptr;
+    int64_t used = 0;
+  };
+  static constexpr int kExecCache = 16;
+  ExecEntry exec_cache[kExecCache];
+  int64_t exec_clock = 0;
+  int64_t exec_updates = 0, exec_instantiations = 0;
+  uint64_t launch_sig = 0;  // FNV-1a over the merged invocation structure (exec_pools)
   bool debug = false;
   // timing / accounting
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -591,15 +604,21 @@ void flush_held(ngdb_ctx* c) {
 
 // Runs invocations in order, merging Intersect classes (mergeable()) and the
 // pops of one drain (drain_mergeable()).
+void sig_mix(ngdb_ctx* c, uint64_t x) {
+  c->launch_sig = (c->launch_sig ^ x) * 1099511628211ull;
+}
+
 void exec_pools(ngdb_ctx* c, const ngdb_plan* p, const std::vector<ngdb_pool_desc>& v) {
   for (size_t i = 0; i < v.size(); ++i) {
     if (i + 1 < v.size() && mergeable(c, v[i], v[i + 1])) {
+      sig_mix(c, 0x100u | (v[i].dir << 4) | v[i].kind);
       exec_pool(c, p, v[i], &v[i + 1]);
       ++i;
       continue;
     }
     ngdb_pool_desc d = v[i];
     while (i + 1 < v.size() && drain_mergeable(c, d, v[i + 1])) d.count += v[++i].count;
+    sig_mix(c, (static_cast<uint64_t>(d.k) << 8) | (d.dir << 4) | d.kind);
     exec_pool(c, p, d);
   }
 }
@@ -952,8 +971,10 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
     if (c->blob_free[i]) cudaEventDestroy(c->blob_free[i]);
     if (c->blob_ready[i]) cudaEventDestroy(c->blob_ready[i]);
   }
-  for (auto& e : c->step_exec)
-    if (e) cudaGraphExecDestroy(e);
+  for (auto& e : c->exec_cache) {
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (e.done) cudaEventDestroy(e.done);
+  }
   for (auto& r : c->results) {
     if (r.host) cudaFreeHost(r.host);
     if (r.done) cudaEventDestroy(r.done);
@@ -1162,6 +1183,7 @@ int ngdb_step_launch(ngdb_ctx* c, int64_t step, int32_t use_graph) {
     // graph: the device runs it with graph-launch overheads instead of ~60
     // stream operations
     cudaGraph_t g = nullptr;
+    c->launch_sig = 1469598103934665603ull;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     try {
       body();
@@ -1172,28 +1194,46 @@ int ngdb_step_launch(ngdb_ctx* c, int64_t step, int32_t use_graph) {
     }
     CK(cudaStreamEndCapture(c->stream, &g));
     c->prologue_pending = false;
-    const int k = c->step_exec_cur;
-    c->step_exec_cur ^= 1;
-    cudaGraphExec_t& e = c->step_exec[k];
-    bool updated = false;
-    if (e) {
+    const uint64_t sig = c->launch_sig;
+    ngdb_ctx::ExecEntry* hit = nullptr;
+    ngdb_ctx::ExecEntry* victim = nullptr;
+    for (auto& en : c->exec_cache) {
+      const bool idle = !en.exec || cudaEventQuery(en.done) == cudaSuccess;
+      cudaGetLastError();  // cudaErrorNotReady is not an error here
+      if (!idle) continue;
+      if (en.exec && en.sig == sig && !hit) hit = &en;
+      if (!victim || !en.exec || (victim->exec && en.used < victim->used)) victim = &en;
+    }
+    cudaGraphExec_t e = nullptr;
+    if (hit) {
       cudaGraphExecUpdateResultInfo info{};
-      updated = cudaGraphExecUpdate(e, g, &info) == cudaSuccess;
-      if (!updated) {
+      if (cudaGraphExecUpdate(hit->exec, g, &info) == cudaSuccess) {
+        e = hit->exec;
+        ++c->exec_updates;
+      } else {
         cudaGetLastError();
-        CK(cudaGraphExecDestroy(e));
-        e = nullptr;
+        victim = hit;  // same structure, incompatible parameters: replace it
       }
     }
-    if (!updated) {
-      const cudaError_t err = cudaGraphInstantiate(&e, g, 0);
+    if (!e) {
+      if (!victim) throw Fail{NGDB_ERR_CONFIG, "no idle step-graph slot"};
+      if (victim->exec) CK(cudaGraphExecDestroy(victim->exec));
+      victim->exec = nullptr;
+      const cudaError_t err = cudaGraphInstantiate(&victim->exec, g, 0);
       if (err != cudaSuccess) {
         cudaGraphDestroy(g);
         CK(err);
       }
+      if (!victim->done) CK(cudaEventCreateWithFlags(&victim->done, cudaEventDisableTiming));
+      victim->sig = sig;
+      e = victim->exec;
+      hit = victim;
+      ++c->exec_instantiations;
     }
+    hit->used = ++c->exec_clock;
     CK(cudaGraphDestroy(g));
     CK(cudaGraphLaunch(e, c->stream));
+    CK(cudaEventRecord(hit->done, c->stream));
   });
 }
 
@@ -1412,6 +1452,13 @@ const char* ngdb_profile_family_name(int32_t f) {
 }
 
 int64_t ngdb_launch_count(ngdb_ctx* c) { return c ? c->launches : 0; }
+
+int ngdb_graph_stats(ngdb_ctx* c, int64_t* updates, int64_t* instantiations) {
+  return guarded([&] {
+    if (updates) *updates = c->exec_updates;
+    if (instantiations) *instantiations = c->exec_instantiations;
+  });
+}
 
 int ngdb_transfer_bytes(ngdb_ctx* c, int64_t* h2d, int64_t* d2h) {
   return guarded([&] {
