@@ -71,83 +71,51 @@ __global__ void __launch_bounds__(kWarps * 32) beta_prep_kernel(DevArgs a, Spars
 }
 
 // ---- lazy Adam on touched entity rows (see the header for the gradient) ----
-// One warp per touched row. The row's contribution codes and coefficients are
-// fetched lane-parallel (32 at a time) and broadcast, and every contribution
-// accumulates into per-lane registers for ALL of the row's chunks at once, so a
-// row costs one pass over its contributions (loads in flight together) instead
-// of one per chunk.
-template <int NCH>
 __global__ void __launch_bounds__(kWarps * 32) beta_entity_adam_kernel(DevArgs a, SparseTable t,
                                                                        AdamHyper hp,
                                                                        const float* bc) {
-  pdl_launch();
+  pdl_start();
   const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row_idx >= t.n_rows) return;
-  const int64_t row = t.rows[row_idx];  // plan data
-  const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
-  pdl_wait();
   const float ibc1 = 1.f / bc[0], ibc2 = 1.f / bc[1];  // bias corrections as reciprocals
+  const int64_t row = t.rows[row_idx];
+  const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
   const int D = a.dim, d4 = D / 4;
-  float4 gA[NCH], gB[NCH], GA[NCH], GB[NCH];
-#pragma unroll
-  for (int i = 0; i < NCH; ++i) gA[i] = gB[i] = GA[i] = GB[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  float S = 0.f;  // sum of candidate coefficients
-  for (int k0 = beg; k0 < end; k0 += 32) {
-    const int nk = min(32, end - k0);
-    int32_t my_code = 0;
-    float my_coef = 0.f;
-    if (lane < nk) {
-      my_code = __ldg(t.contrib + k0 + lane);
-      if (my_code >= 0) my_coef = __ldg(a.coefbuf + my_code);
-    }
-    S += warp_sum(my_coef);
-    for (int j = 0; j < nk; ++j) {
-      const int32_t code = __shfl_sync(0xffffffffu, my_code, j);
-      const float coef = __shfl_sync(0xffffffffu, my_coef, j);
-      if (code < 0) {
-        const float* g = a.agbuf + static_cast<int64_t>(-code - 1) * t.width;
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const int ch = lane + 32 * i;
-          if (ch < d4) {
-            const float4 u = ld4(g + 4 * ch), v = ld4(g + D + 4 * ch);
-            gA[i].x += u.x; gA[i].y += u.y; gA[i].z += u.z; gA[i].w += u.w;
-            gB[i].x += v.x; gB[i].y += v.y; gB[i].z += v.z; gB[i].w += v.w;
-          }
-        }
-      } else {
-        const float* q = a.qbuf + static_cast<int64_t>(code / a.ncand) * a.wq;
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-          const int ch = lane + 32 * i;
-          if (ch < d4) {
-            const float4 u = ld4(q + 4 * ch), v = ld4(q + D + 4 * ch);
-            GA[i].x += coef * u.x; GA[i].y += coef * u.y; GA[i].z += coef * u.z; GA[i].w += coef * u.w;
-            GB[i].x += coef * v.x; GB[i].y += coef * v.y; GB[i].z += coef * v.z; GB[i].w += coef * v.w;
-          }
-        }
-      }
-    }
+  float S = 0.f;  // sum of candidate coefficients (identical in every lane)
+  for (int kk = beg; kk < end; ++kk) {
+    const int32_t code = __ldg(t.contrib + kk);
+    if (code >= 0) S += __ldg(a.coefbuf + code);
   }
   float* wp = t.w + row * t.width;
   float* mp = t.m + row * t.width;
   float* vp = t.v + row * t.width;
-#pragma unroll
-  for (int i = 0; i < NCH; ++i) {
-    const int ch = lane + 32 * i;
-    if (ch >= d4) continue;
+  for (int ch = lane; ch < d4; ch += 32) {
+    float gA[4] = {0, 0, 0, 0}, gB[4] = {0, 0, 0, 0}, GA[4] = {0, 0, 0, 0}, GB[4] = {0, 0, 0, 0};
+    for (int kk = beg; kk < end; ++kk) {
+      const int32_t code = __ldg(t.contrib + kk);
+      if (code < 0) {
+        const float* g = a.agbuf + static_cast<int64_t>(-code - 1) * t.width;
+        const float4 u = ld4(g + 4 * ch), v = ld4(g + D + 4 * ch);
+        gA[0] += u.x; gA[1] += u.y; gA[2] += u.z; gA[3] += u.w;
+        gB[0] += v.x; gB[1] += v.y; gB[2] += v.z; gB[3] += v.w;
+      } else {
+        const float coef = __ldg(a.coefbuf + code);
+        const float* q = a.qbuf + static_cast<int64_t>(code / a.ncand) * a.wq;
+        const float4 u = ld4(q + 4 * ch), v = ld4(q + D + 4 * ch);
+        GA[0] += coef * u.x; GA[1] += coef * u.y; GA[2] += coef * u.z; GA[3] += coef * u.w;
+        GB[0] += coef * v.x; GB[1] += coef * v.y; GB[2] += coef * v.z; GB[3] += coef * v.w;
+      }
+    }
     const float4 xa = ld4(wp + 4 * ch), xb = ld4(wp + D + 4 * ch);
     const float va[4] = {xa.x, xa.y, xa.z, xa.w}, vb[4] = {xb.x, xb.y, xb.z, xb.w};
-    const float gAv[4] = {gA[i].x, gA[i].y, gA[i].z, gA[i].w}, gBv[4] = {gB[i].x, gB[i].y, gB[i].z, gB[i].w};
-    const float GAv[4] = {GA[i].x, GA[i].y, GA[i].z, GA[i].w}, GBv[4] = {GB[i].x, GB[i].y, GB[i].z, GB[i].w};
     float ga[4], gb[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const float al = beta_realize(va[u]), be = beta_realize(vb[u]), s = al + be;
       const float ta = dg_trigamma(al), tb = dg_trigamma(be), ts = dg_trigamma(s);
-      const float dA = gAv[u] + S * (al * ta - s * ts) + GAv[u] * (ts - ta) + GBv[u] * ts;
-      const float dB = gBv[u] + S * (be * tb - s * ts) + GAv[u] * ts + GBv[u] * (ts - tb);
+      const float dA = gA[u] + S * (al * ta - s * ts) + GA[u] * (ts - ta) + GB[u] * ts;
+      const float dB = gB[u] + S * (be * tb - s * ts) + GA[u] * ts + GB[u] * (ts - tb);
       ga[u] = dA * beta_drealize(va[u]);
       gb[u] = dB * beta_drealize(vb[u]);
     }
@@ -158,7 +126,7 @@ __global__ void __launch_bounds__(kWarps * 32) beta_entity_adam_kernel(DevArgs a
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int off = half * D + 4 * ch;
-      float4 w = half ? xb : xa, m = ld4(mp + off), v = ld4(vp + off);
+      float4 w = ld4(wp + off), m = ld4(mp + off), v = ld4(vp + off);
       float* wv = &w.x;
       float* mv = &m.x;
       float* vv = &v.x;
@@ -510,11 +478,8 @@ int launch_beta_prep(const DevArgs& a, const SparseTable& t, const LaunchCtx& lc
 int launch_beta_entity_adam(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
                             const float* bc, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
-  const dim3 grid((t.n_rows + kWarps - 1) / kWarps);
-  if (a.dim <= 512)
-    launch_pdl(beta_entity_adam_kernel<4>, grid, dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
-  else
-    launch_pdl(beta_entity_adam_kernel<8>, grid, dim3(kWarps * 32), 0, lc.stream, 1, a, t, hp, bc);
+  launch_pdl(beta_entity_adam_kernel, dim3((t.n_rows + kWarps - 1) / kWarps), dim3(kWarps * 32), 0,
+             lc.stream, 1, a, t, hp, bc);
   return 1;
 }
 
