@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kWarps * 32) beta_prep_kernel(DevArgs a, Spars
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const float al = beta_realize(va[u]), be = beta_realize(vb[u]), s = al + be;
-      const float da = dg_digamma(al), db = dg_digamma(be), ds = dg_digamma(s);
+      const float da = dg_digamma_fast(al), db = dg_digamma_fast(be), ds = dg_digamma_fast(s);
       pa[u] = ds - da;
       pb[u] = ds - db;
       c += -dg_lbeta(al, be) + al * da + be * db - s * ds;
@@ -112,12 +112,15 @@ __global__ void __launch_bounds__(kWarps * 32) beta_entity_adam_kernel(DevArgs a
     float ga[4], gb[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const float al = beta_realize(va[u]), be = beta_realize(vb[u]), s = al + be;
-      const float ta = dg_trigamma(al), tb = dg_trigamma(be), ts = dg_trigamma(s);
+      float al, dal, be, dbe;
+      beta_realize_pair(va[u], al, dal);
+      beta_realize_pair(vb[u], be, dbe);
+      const float s = al + be;
+      const float ta = dg_trigamma_fast(al), tb = dg_trigamma_fast(be), ts = dg_trigamma_fast(s);
       const float dA = gA[u] + S * (al * ta - s * ts) + GA[u] * (ts - ta) + GB[u] * ts;
       const float dB = gB[u] + S * (be * tb - s * ts) + GA[u] * ts + GB[u] * (ts - tb);
-      ga[u] = dA * beta_drealize(va[u]);
-      gb[u] = dB * beta_drealize(vb[u]);
+      ga[u] = dA * dal;
+      gb[u] = dB * dbe;
     }
     if (t.dbg_g) {
       st4(t.dbg_g + row * t.width + 4 * ch, make_float4(ga[0], ga[1], ga[2], ga[3]));

@@ -40,6 +40,39 @@ __device__ __forceinline__ float dg_trigamma(float x) {
   return acc + series;
 }
 
+// Branch-free variants for the per-element loops of the BetaE step table and
+// Adam (x in the realised range [0.05, 1e9]): always six recurrence steps
+// (x + 6 >= 6.05 is in the asymptotic regime) with the MUFU reciprocal
+// (rcp.approx, <= 1 ulp) — no divergent while loop, no IEEE division.
+__device__ __forceinline__ float rcp_fast(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float dg_trigamma_fast(float x) {
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const float r = rcp_fast(x + static_cast<float>(k));
+    acc += r * r;
+  }
+  const float i1 = rcp_fast(x + 6.f), i2 = i1 * i1;
+  const float series =
+      i1 + 0.5f * i2 +
+      i1 * i2 * (1.f / 6 - i2 * (1.f / 30 - i2 * (1.f / 42 - i2 * (1.f / 30 - i2 * (5.f / 66)))));
+  return acc + series;
+}
+__device__ __forceinline__ float dg_digamma_fast(float x) {
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) acc -= rcp_fast(x + static_cast<float>(k));
+  const float y = x + 6.f;
+  const float i1 = rcp_fast(y), i2 = i1 * i1;
+  const float series =
+      i2 * (1.f / 12 - i2 * (1.f / 120 - i2 * (1.f / 252 - i2 * (1.f / 240 - i2 * (1.f / 132)))));
+  return acc + logf(y) - 0.5f * i1 - series;
+}
+
 __device__ __forceinline__ float dg_lbeta(float a, float b) {
   return lgammaf(a) + lgammaf(b) - lgammaf(a + b);
 }
@@ -50,6 +83,14 @@ __device__ __forceinline__ float beta_softplus(float x) {
 }
 __device__ __forceinline__ float beta_realize(float x) {
   return fminf(fmaxf(beta_softplus(x), kBetaMin), kBetaMax);
+}
+// realize(x) and realize'(x) from ONE exponential
+__device__ __forceinline__ void beta_realize_pair(float x, float& val, float& dval) {
+  const float e = expf(-fabsf(x));
+  const float sp = fmaxf(x, 0.f) + log1pf(e);
+  val = fminf(fmaxf(sp, kBetaMin), kBetaMax);
+  const float inv = rcp_fast(1.f + e);
+  dval = (sp > kBetaMin && sp < kBetaMax) ? (x >= 0.f ? inv : e * inv) : 0.f;
 }
 __device__ __forceinline__ float beta_drealize(float x) {
   const float sp = beta_softplus(x);
