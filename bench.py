@@ -108,11 +108,13 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
 
 
-def roofline(fams):
+def roofline(fams, config=None):
     """Roofline of the dominant kernel family (largest share of the profiled
     step): GEMM families against the measured dense tensor peak (bf16 cuBLAS,
     the only measured tensor figure; our contractions are 3xTF32 on tcgen05),
-    bandwidth families against measured HBM. Also the top HBM-bound family."""
+    bandwidth families against measured HBM. Also the top HBM-bound family.
+    `traffic` = DRAM bytes per launch from the committed ncu capture of this
+    config (profiles/ncu_traffic.json), when there is one."""
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (
         ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm = float(peaks.get("hbm_gbs", 6650.0))
@@ -120,15 +122,28 @@ def roofline(fams):
     kind = "measured" if peaks else "fallback"
     total = sum(v["ms_per_step"] for v in fams.values())
     name, f = max(fams.items(), key=lambda kv: kv[1]["ms_per_step"])
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    traffic = json.loads(tf.read_text()).get(config, {}) if tf.exists() and config else {}
+
+    def traffic_of(n, v):
+        t = traffic.get(n)
+        if not t:
+            return None
+        alg = v["bytes_per_step"] / max(v["launches_per_step"], 1e-9)
+        return {"dram_bytes_per_launch": t["bytes_per_launch"],
+                "algorithmic_bytes_per_launch": alg, "kernel": t["kernel"], "source": t["source"]}
 
     def hbm_entry(n, v):
+        t = traffic_of(n, v)
         return {"bound": "hbm", "kernel": n, "achieved": v["gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": v["gbs"] / hbm, "traffic": None, "peak_kind": kind,
-                "share_of_step": v["ms_per_step"] / total}
+                "frac": v["gbs"] / hbm, "traffic": t["dram_bytes_per_launch"] if t else None,
+                "traffic_detail": t, "peak_kind": kind, "share_of_step": v["ms_per_step"] / total}
 
     if f["flops_per_step"] > 0:
         roof = {"bound": "tensor", "kernel": name, "achieved": f["tflops"], "peak": tensor,
-                "unit": "TFLOP/s", "frac": f["tflops"] / tensor, "traffic": None,
+                "unit": "TFLOP/s", "frac": f["tflops"] / tensor,
+                "traffic": (traffic_of(name, f) or {}).get("dram_bytes_per_launch"),
+                "traffic_detail": traffic_of(name, f),
                 "peak_kind": kind + " (bf16 dense; kernels are 3xTF32)",
                 "share_of_step": f["ms_per_step"] / total}
     else:
@@ -500,7 +515,7 @@ def main():
                 "bytes_per_step": fb.value / args.profile_steps,
                 "flops_per_step": ff.value / args.profile_steps}
     check(lib.ngdb_profile_enable(ctx, 0))
-    roof = roofline(fams)
+    roof = roofline(fams, args.config)
 
     # ---- e2e: public C ABI call with host buffers ----------------------------
     # The trainer loop (ngdb_train_run): host producer threads sample and plan
