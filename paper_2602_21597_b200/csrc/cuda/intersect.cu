@@ -230,11 +230,12 @@ __global__ void q2b_combine_kernel(DevArgs a, KSpan ks, int first, const float* 
     a.arena[d.out + D + e] = mn * sigmoidf(u);
   }
 }
-// Backward combine. Also gathers the node's inputs (arena) and its stashed Z
-// rows and Lm into class order: the operands of the weight-gradient GEMMs.
+// Backward combine. Also gathers the node's inputs (arena) and its stashed Z,
+// P rows and Lm into class order: the operands of the weight-gradient GEMMs
+// and the ReLU masks.
 __global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Cin, float* Oin,
-                                       float* Z, float* Lm, float* gS, Split gSs, float* dCin,
-                                       float* dOin, float* gU, Split gUs) {
+                                       float* Z, float* P, float* Lm, float* gS, Split gSs,
+                                       float* dCin, float* dOin, float* gU, Split gUs) {
   pdl_launch();
   const int i = blockIdx.x;
   const int D = a.dim;
@@ -257,6 +258,7 @@ __global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Ci
       Cin[r] = cin[l];
       Oin[r] = oin[l];
       Z[r] = st[l * D + e];
+      P[r] = st[6 * D + l * D + e];
       ga[l] = gC * cin[l];
       dot += w[l] * ga[l];
     }
@@ -275,31 +277,47 @@ __global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Ci
     put(gU, gUs, (int64_t)i * D + e, gO * mn * gate * (1.f - gate));
   }
 }
-// gP[i*k+l] = gLm[i] / k * (P > 0)  (plain + split)
-__global__ void q2b_gp_kernel(DevArgs a, const float* gLm, KSpan ks, int first, float* gP,
-                              Split gPs) {
+// The backward tail in ONE launch: blocks [0, n_col) compute the bias
+// gradients (the colsum kernel's work), the rest scatter dCin / dOin into the
+// planned G slots, one node per block.
+__global__ void __launch_bounds__(kColsumWarps * 32) q2b_bwd_tail_kernel(DevArgs a, KSpan ks, int first,
+                                                                         const float* dCin,
+                                                                         const float* dOin,
+                                                                         ColsumJobs jobs, int n_colx) {
   pdl_start();
-  const int i = blockIdx.x;
-  const int D = a.dim;
-  const int k = ks.k(i), r0 = ks.row0(i);
-  const float* P = q2b_stash(a, a.nodes[first + i].aux) + 6 * D;
-  const float inv_k = 1.f / static_cast<float>(k);
-  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y)
-    for (int l = 0; l < k; ++l) {
-      const int64_t r = ((int64_t)r0 + l) * D + e;
-      put(gP, gPs, r, P[l * D + e] > 0.f ? gLm[(int64_t)i * D + e] * inv_k : 0.f);
+  const int n_col = n_colx * jobs.n;
+  if (static_cast<int>(blockIdx.x) < n_col) {
+    __shared__ float part[kColsumWarps][32];
+    const ColsumJob& j = jobs.job[blockIdx.x / n_colx];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int c = (blockIdx.x % n_colx) * 32 + lane;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    if (c < j.n) {
+      constexpr int W = kColsumWarps;
+      int r = warp;
+      for (; r + 3 * W < j.rows; r += 4 * W) {
+        s0 += j.dy[(int64_t)r * j.n + c];
+        s1 += j.dy[(int64_t)(r + W) * j.n + c];
+        s2 += j.dy[(int64_t)(r + 2 * W) * j.n + c];
+        s3 += j.dy[(int64_t)(r + 3 * W) * j.n + c];
+      }
+      for (; r < j.rows; r += W) s0 += j.dy[(int64_t)r * j.n + c];
     }
-}
-__global__ void q2b_scatter_kernel(DevArgs a, KSpan ks, int first, const float* dCin,
-                                   const float* dOin) {
-  pdl_launch();
-  const int i = blockIdx.x;
+    part[warp][lane] = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+    if (warp == 0 && c < j.n) {
+      float t = 0.f;
+      for (int w = 0; w < kColsumWarps; ++w) t += part[w][lane];
+      j.db[c] += t;
+    }
+    return;
+  }
+  const int i = blockIdx.x - n_col;
   const int D = a.dim;
   const int k = ks.k(i), r0 = ks.row0(i);
-  const ngdb_node_desc d = a.nodes[first + i];  // plan data: before the wait
-  pdl_wait();
+  const ngdb_node_desc d = a.nodes[first + i];
   for (int l = 0; l < k; ++l)
-    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
+    for (int e = threadIdx.x; e < D; e += blockDim.x) {
       const int64_t r = ((int64_t)r0 + l) * D + e;
       a.arena[d.out + l * 2 * D + e] = dCin[r];
       a.arena[d.out + l * 2 * D + D + e] = dOin[r];
@@ -376,8 +394,9 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
 
-  launch_pdl(q2b_combine_bwd_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Cin, Oin, Z, Lm,
-             gS, gSs, dCin, dOin, gU, gUs);
+  float* Pc = sc.take(rd);  // stashed P rows in class order (ReLU mask of gP)
+  launch_pdl(q2b_combine_bwd_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Cin, Oin, Z, Pc,
+             Lm, gS, gSs, dCin, dOin, gU, gUs);
   ++launches;
   SplitJobs j1{};
   j1.job[0] = {gU, n, D, D, 0, gUT.hi, gUT.lo};
@@ -398,10 +417,10 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
     lvl[3].s_hi = gZs.hi; lvl[3].s_lo = gZs.lo;
     launches += tc_gemm_batch(lvl, 4, s);
   }
-  launch_pdl(q2b_gp_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, (const float*)gLm, ks, first, gP, gPs);
-  ++launches;
   SplitJobs j2{};
-  j2.job[0] = {gP, R, D, D, 0, gPT.hi, gPT.lo};
+  // gP = gLm / k * (P > 0), computed inside the transposing split (plain,
+  // row-major split and transposed split in one pass)
+  j2.job[0] = {gP, R, D, D, 0, gPT.hi, gPT.lo, gLm, Pc, ks.n1, ks.k1, ks.k2, gP, gPs.hi, gPs.lo};
   j2.job[1] = {Oin, R, D, D, 0, OT.hi, OT.lo};
   j2.job[2] = {gZ, R, D, D, 0, gZT.hi, gZT.lo};
   j2.job[3] = {Cin, R, D, D, 0, CT.hi, CT.lo};
@@ -425,8 +444,9 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   cj.job[2] = {gP, R, D, g + off[Q2B_V1B]};
   cj.job[3] = {gZ, R, D, g + off[Q2B_A1B]};
   cj.n = 4;
-  launches += colsums(cj, D, s);
-  launch_pdl(q2b_scatter_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, dCin, dOin);
+  const int n_colx = (D + 31) / 32;  // bias gradients and the G-slot scatter: one launch
+  launch_pdl(q2b_bwd_tail_kernel, dim3(n_colx * cj.n + n), dim3(kColsumWarps * 32), 0, s, 1, a, ks,
+             first, (const float*)dCin, (const float*)dOin, cj, n_colx);
   return launches + 1;
 }
 

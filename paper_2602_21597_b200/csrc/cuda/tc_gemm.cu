@@ -398,7 +398,22 @@ __global__ void split_t_multi_kernel(SplitJobs jobs) {
   if (r0 >= j.rows || c0 >= j.cols) return;  // grid sized for the largest job
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int r = r0 + y, c = c0 + threadIdx.x;
-    float v = (r < j.rows && c < j.cols) ? j.src[(int64_t)r * j.ld + c] : 0.f;
+    float v = 0.f;
+    if (r < j.rows && c < j.cols) {
+      if (j.node_grad) {  // computed source (see SplitJob)
+        const int node = r < j.n1 * j.k1 ? r / j.k1 : j.n1 + (r - j.n1 * j.k1) / j.k2;
+        const int k = r < j.n1 * j.k1 ? j.k1 : j.k2;
+        const int64_t o = (int64_t)r * j.ld + c;
+        v = j.mask[o] > 0.f ? j.node_grad[(int64_t)node * j.cols + c] / static_cast<float>(k) : 0.f;
+        float h, l;
+        split_tf32(v, h, l);
+        j.plain[o] = v;
+        j.rhi[o] = h;
+        j.rlo[o] = l;
+      } else {
+        v = j.src[(int64_t)r * j.ld + c];
+      }
+    }
     tile[y][threadIdx.x] = j.relu ? fmaxf(v, 0.f) : v;
   }
   __syncthreads();

@@ -61,6 +61,16 @@ struct SplitJob {
   int rows, cols, ld, relu;
   float* hi;
   float* lo;
+  // optional computed source (the mean-adjoint of a DeepSets layer):
+  // v[r][c] = mask[r][c] > 0 ? node_grad[node(r)][c] / k(node) : 0, with the
+  // node layout of a two-class (n1 nodes of k1 rows, then k2) Intersect
+  // invocation; v is also written plain (plain) and split row-major (rhi/rlo)
+  const float* node_grad;
+  const float* mask;
+  int n1, k1, k2;
+  float* plain;
+  float* rhi;
+  float* rlo;
 };
 struct SplitJobs {
   SplitJob job[4];
