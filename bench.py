@@ -350,15 +350,23 @@ def bench_sharded(args):
     check(lib.ngdb_profile_enable(ctx, 0))
     # e2e: host planning (sampling, DAG, Max-Fillness, metadata all-gather, owner
     # lists) + every stage and collective, per step
-    e2e_batches = [m.Batch.sample(graph, w, batch, n_neg, seed=3,
-                                  tag=(1 + n_steps + s) * world + rank) for s in range(args.steps)]
+    # e2e: the pipelined sharded trainer loop — sampling + planning on host
+    # threads, metadata all-gather, owner lists, every stage and collective,
+    # losses read back per step
+    producers = max(1, min(8, (os.cpu_count() or 2) - 1))
+    eng.step_count = step_no
+    eng.train(graph, w, 3, batch, n_neg, lambda s: (1 + n_steps + s) * world + rank, producers)
+    b0, d0 = C.c_int64(), C.c_int64()
+    check(lib.ngdb_transfer_bytes(ctx, C.byref(b0), C.byref(d0)))
     dist.barrier()
     t0 = time.perf_counter()
-    for b in e2e_batches:
-        step_no += 1
-        eng.run(plan_shard_step(comm, b, backbone, dim), step_no)
+    eng.train(graph, w, args.steps, batch, n_neg,
+              lambda s: (1 + n_steps + 3 + s) * world + rank, producers)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    b1, d1 = C.c_int64(), C.c_int64()
+    check(lib.ngdb_transfer_bytes(ctx, C.byref(b1), C.byref(d1)))
+    step_no = eng.step_count
     t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e = batch * world * args.steps / float(t.item())
@@ -378,7 +386,10 @@ def bench_sharded(args):
                              f"{3 * info['n_entities'] * dim * 4 / G / 1e9:.1f} GB per rank"},
             "roofline": roofline(fams) if fams else None,
             "cpu_baseline": None,
-            "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": None,
+            "e2e": {"value": e2e, "unit": "queries/s",
+                    "h2d_bytes_per_step": int((b1.value - b0.value) / args.steps),
+                    "api": "ShardedEngine.train (host planning threads, metadata all-gather, "
+                           "stages + NCCL collectives, loss read-back per step)",
                     "d2h_bytes_per_step": 4 * batch + 16},
             "families": fams,
             "gpu_launches": int(launches),

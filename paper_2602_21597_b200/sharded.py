@@ -131,9 +131,8 @@ class ShardStep:
             self._h = None
 
 
-def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: int = 512) -> ShardStep:
-    """Plan this rank's batch, exchange the metadata, build the owner work lists."""
-    ps = PlannedStep(batch, backbone, dim, b_max, sharded=True)
+def _local_meta(ps: PlannedStep):
+    """This rank's scoring metadata of a planned step (host arrays)."""
     na, ns, b, nc = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
     check(lib.ngdb_step_shard_info(ps._h, C.byref(na), C.byref(ns), C.byref(b), C.byref(nc)))
     anchors = np.zeros(na.value, np.int32)
@@ -142,7 +141,13 @@ def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: in
     cand = np.zeros(b.value * nc.value, np.int32)
     check(lib.ngdb_step_shard_meta(ps._h, _p(anchors, C.c_int32), _p(unit_k, C.c_int32),
                                    _p(unit_slots, C.c_int32), _p(cand, C.c_int32)))
-    meta = comm.all_gather_object((anchors, unit_k, unit_slots, cand, ns.value))
+    return (anchors, unit_k, unit_slots, cand, ns.value), b.value, nc.value
+
+
+def _finish_shard_step(comm: Comm, ps: PlannedStep, local) -> ShardStep:
+    """Exchange the metadata (gloo all-gather) and build the owner work lists."""
+    mine, b, nc = local
+    meta = comm.all_gather_object(mine)
     G = comm.world
     A = max(1, max(m[0].size for m in meta))
     S = max(1, max(m[4] for m in meta))
@@ -150,18 +155,24 @@ def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: in
     anc_all = np.full((G, A), -1, np.int32)
     k_all = np.zeros((G, B), np.int32)
     slots_all = np.full((G, B, 3), -1, np.int32)
-    cand_all = np.zeros((G, B, nc.value), np.int32)
+    cand_all = np.zeros((G, B, nc), np.int32)
     for q, (an, uk, us, ca, _) in enumerate(meta):
         bq = uk.size
         anc_all[q, :an.size] = an
         k_all[q, :bq] = uk
         slots_all[q, :bq] = us.reshape(bq, 3)
-        cand_all[q, :bq] = ca.reshape(bq, nc.value)
+        cand_all[q, :bq] = ca.reshape(bq, nc)
     h = C.c_void_p()
-    check(lib.ngdb_shard_build(G, comm.rank, B, A, S, nc.value, _p(anc_all, C.c_int32),
+    check(lib.ngdb_shard_build(G, comm.rank, B, A, S, nc, _p(anc_all, C.c_int32),
                                _p(k_all, C.c_int32), _p(slots_all, C.c_int32),
                                _p(cand_all, C.c_int32), C.byref(h)))
-    return ShardStep(ps, h, b.value)
+    return ShardStep(ps, h, b)
+
+
+def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: int = 512) -> ShardStep:
+    """Plan this rank's batch, exchange the metadata, build the owner work lists."""
+    ps = PlannedStep(batch, backbone, dim, b_max, sharded=True)
+    return _finish_shard_step(comm, ps, _local_meta(ps))
 
 
 class ShardedEngine:
@@ -244,6 +255,64 @@ class ShardedEngine:
 
     def train_step(self, batch: Batch) -> np.ndarray:
         return self.run(self.plan(batch))
+
+    def _launch(self, step: ShardStep, step_no: int) -> int:
+        """All stages + collectives of one step, enqueued; returns the ticket of
+        its asynchronous loss read-back (ngdb_step_end_async)."""
+        with self.torch.cuda.stream(self.stream):
+            v, s = step.views()
+            b = ShardBuffers()
+            check(lib.ngdb_shard_begin(self._h, C.byref(v), C.byref(s), C.byref(b)))
+            t = {n: _device_view(self.torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
+            _stages(self, t)
+            check(lib.ngdb_shard_optimizer(self._h, step_no))
+            ticket = C.c_int64()
+            check(lib.ngdb_step_end_async(self._h, C.byref(ticket)))
+        return ticket.value
+
+    def train(self, graph, weights, n_steps: int, batch: int, n_neg: int, tag_of,
+              producers: int = 8) -> np.ndarray:
+        """Pipelined sharded trainer loop (the sharded counterpart of
+        ngdb_train_run): host threads sample + plan upcoming batches (the C++
+        calls release the GIL), the calling thread exchanges each step's
+        metadata, builds its owner lists, enqueues its stages and collectives,
+        and reads step i's losses back while step i+1 runs. Batch of step s is
+        Rng(3).fork(tag_of(s)). Returns the per-step loss sums of this rank."""
+        import concurrent.futures as cf
+
+        def prep(s):
+            b = Batch.sample(graph, weights, batch, n_neg, seed=3, tag=tag_of(s))
+            ps = PlannedStep(b, self.backbone, self.dim, self.b_max, sharded=True)
+            return ps, _local_meta(ps)
+
+        sums = np.zeros(n_steps, np.float64)
+        losses = np.zeros(batch, np.float32)
+        pending = []
+        ahead = 2 * producers
+
+        def collect():
+            i, ticket, _step = pending.pop(0)
+            total, nonfinite = C.c_double(), C.c_int32()
+            check(lib.ngdb_step_wait(self._h, ticket, _p(losses, C.c_float), batch,
+                                     C.byref(total), C.byref(nonfinite)))
+            if nonfinite.value:
+                raise FloatingPointError(f"non-finite loss at step {i}")
+            sums[i] = total.value
+
+        with cf.ThreadPoolExecutor(producers) as pool:
+            futs = {s: pool.submit(prep, s) for s in range(min(n_steps, ahead))}
+            for s in range(n_steps):
+                ps, local = futs.pop(s).result()
+                if s + ahead < n_steps:
+                    futs[s + ahead] = pool.submit(prep, s + ahead)
+                step = _finish_shard_step(self.comm, ps, local)
+                self.step_count += 1
+                pending.append((s, self._launch(step, self.step_count), step))
+                while len(pending) > 1:
+                    collect()
+            while pending:
+                collect()
+        return sums
 
     def capture(self, steps: List[ShardStep]) -> List["ShardGraph"]:
         """Resident copies of `steps` whose stages AND collectives replay as one

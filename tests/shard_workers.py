@@ -129,3 +129,45 @@ def graph_replay_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps
     with open(os.path.join(out_dir, f"graph{rank}.pkl"), "wb") as f:
         pickle.dump(out, f)
     dist.destroy_process_group()
+
+
+def train_loop_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
+    """One NCCL rank on GPU 0: ShardedEngine.train (pipelined: planning
+    threads, async loss read-back) vs the same batches step by step."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    import numpy as np
+
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200.sharded import Comm, ShardedEngine, plan_shard_step
+
+    comm = Comm()
+    g = m.Graph.synthetic(shape, 1)
+    info = g.info()
+    w = m.pattern_weights(mix)
+    tag = lambda s: (s + 1) * world + rank  # noqa: E731
+    out = {}
+    eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
+                        n_neg=k, max_queries=b)
+    seq = []
+    for s in range(steps):
+        batch = m.Batch.sample(g, w, b, k, seed=3, tag=tag(s))
+        seq.append(float(np.sum(eng.run(plan_shard_step(comm, batch, backbone, dim)),
+                                dtype=np.float64)))
+    out["seq"] = {n: eng.download(n) for n, *_ in m.param_specs(backbone, info["n_entities"],
+                                                               info["n_relations"], dim)}
+    eng2 = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
+                         n_neg=k, max_queries=b)
+    sums = eng2.train(g, w, steps, b, k, tag, producers=3)
+    torch.cuda.synchronize()
+    out["loop"] = {n: eng2.download(n) for n, *_ in m.param_specs(backbone, info["n_entities"],
+                                                                 info["n_relations"], dim)}
+    out["seq_sums"] = seq
+    out["loop_sums"] = sums.tolist()
+    with open(os.path.join(out_dir, f"loop{rank}.pkl"), "wb") as f:
+        pickle.dump(out, f)
+    dist.destroy_process_group()

@@ -91,3 +91,18 @@ def test_sharded_graph_replay_matches_eager(tmp_path, backbone, dim):
     out = pickle.load(open(tmp_path / "graph0.pkl", "rb"))
     for name, v in out["eager"].items():
         assert np.array_equal(v, out["graph"][name]), name
+
+
+def test_sharded_train_loop_matches_steps(tmp_path):
+    # ShardedEngine.train (bench.py --config c5 e2e) = the same batches run
+    # step by step: identical parameters and per-step losses
+    import torch.multiprocessing as mp
+
+    import shard_workers
+    mp.spawn(shard_workers.train_loop_worker,
+             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, 32, 4, "q2b"),
+             nprocs=1, join=True)
+    out = pickle.load(open(tmp_path / "loop0.pkl", "rb"))
+    for name, v in out["seq"].items():
+        assert np.array_equal(v, out["loop"][name]), name
+    np.testing.assert_allclose(out["loop_sums"], out["seq_sums"], rtol=1e-12)
