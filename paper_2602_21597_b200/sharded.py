@@ -144,8 +144,9 @@ def _local_meta(ps: PlannedStep):
     return (anchors, unit_k, unit_slots, cand, ns.value), b.value, nc.value
 
 
-def _finish_shard_step(comm: Comm, ps: PlannedStep, local) -> ShardStep:
-    """Exchange the metadata (gloo all-gather) and build the owner work lists."""
+def _gather_meta(comm: Comm, local):
+    """All-gather the ranks' scoring metadata (gloo, ordered per step) and pad
+    it into the dense [G][...] arrays of ngdb_shard_build."""
     mine, b, nc = local
     meta = comm.all_gather_object(mine)
     G = comm.world
@@ -162,11 +163,22 @@ def _finish_shard_step(comm: Comm, ps: PlannedStep, local) -> ShardStep:
         k_all[q, :bq] = uk
         slots_all[q, :bq] = us.reshape(bq, 3)
         cand_all[q, :bq] = ca.reshape(bq, nc)
+    return (G, comm.rank, B, A, S, nc, anc_all, k_all, slots_all, cand_all), b
+
+
+def _build_shard_step(ps: PlannedStep, gathered) -> ShardStep:
+    """Owner work lists of this rank (C++; releases the GIL)."""
+    (G, rank, B, A, S, nc, anc_all, k_all, slots_all, cand_all), b = gathered
     h = C.c_void_p()
-    check(lib.ngdb_shard_build(G, comm.rank, B, A, S, nc, _p(anc_all, C.c_int32),
+    check(lib.ngdb_shard_build(G, rank, B, A, S, nc, _p(anc_all, C.c_int32),
                                _p(k_all, C.c_int32), _p(slots_all, C.c_int32),
                                _p(cand_all, C.c_int32), C.byref(h)))
     return ShardStep(ps, h, b)
+
+
+def _finish_shard_step(comm: Comm, ps: PlannedStep, local) -> ShardStep:
+    """Exchange the metadata (gloo all-gather) and build the owner work lists."""
+    return _build_shard_step(ps, _gather_meta(comm, local))
 
 
 def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: int = 512) -> ShardStep:
@@ -299,13 +311,31 @@ class ShardedEngine:
                 raise FloatingPointError(f"non-finite loss at step {i}")
             sums[i] = total.value
 
-        with cf.ThreadPoolExecutor(producers) as pool:
-            futs = {s: pool.submit(prep, s) for s in range(min(n_steps, ahead))}
+        # three stages ahead of the launching thread: sample + plan (pool), the
+        # ordered metadata all-gather (one thread: collectives run in step
+        # order on every rank), owner lists (pool)
+        with cf.ThreadPoolExecutor(producers) as pool, cf.ThreadPoolExecutor(1) as exch:
+            def gather(s, prep_fut):
+                ps, local = prep_fut.result()
+                return ps, _gather_meta(self.comm, local)
+
+            def build(gather_fut):
+                ps, gathered = gather_fut.result()
+                return _build_shard_step(ps, gathered)
+
+            futs = {}
+
+            def submit(s):
+                pf = pool.submit(prep, s)
+                gf = exch.submit(gather, s, pf)
+                futs[s] = pool.submit(build, gf)
+
+            for s in range(min(n_steps, ahead)):
+                submit(s)
             for s in range(n_steps):
-                ps, local = futs.pop(s).result()
+                step = futs.pop(s).result()
                 if s + ahead < n_steps:
-                    futs[s + ahead] = pool.submit(prep, s + ahead)
-                step = _finish_shard_step(self.comm, ps, local)
+                    submit(s + ahead)
                 self.step_count += 1
                 pending.append((s, self._launch(step, self.step_count), step))
                 while len(pending) > 1:
