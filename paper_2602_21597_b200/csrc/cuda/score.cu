@@ -459,9 +459,11 @@ void launch_stream(const DevArgs& a, int first, int n, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     resident = std::max(1, per_sm) * sms;
   }
-  // parts per node: enough items for every resident CTA (within the partial
+  // parts per node: at most one item per resident CTA (measured: fewer,
+  // larger items beat an even spread — the per-item reduction is not free;
+  // within the partial
   // buffer's capacity); the persistent grid never exceeds one wave
-  int S = std::max(1, std::min(8, (resident + n - 1) / n));
+  int S = std::max(1, std::min(8, resident / n));
   while (S > 1 && S * n > a.lpart_items) --S;
   const int grid = std::min(resident, S * n);
   launch_pdl(kernel, dim3(grid), dim3(kThreads), smem, s, 1, a, first, n, S);
