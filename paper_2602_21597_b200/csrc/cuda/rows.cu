@@ -11,7 +11,7 @@
 namespace ngdb_dev {
 namespace {
 
-constexpr int kWarps = 8;  // 256 threads, one node per warp
+constexpr int kWarps = 2;  // 64 threads, one node per warp: a 512-node pop spreads over 256 CTAs
 
 __device__ __forceinline__ bool bad_index(const DevArgs& a, int32_t id, int32_t limit) {
   if (id < 0 || id >= limit) {
