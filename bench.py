@@ -412,6 +412,8 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--producers", type=int, default=0, help="e2e host producer threads (0: cores-1)")
+    ap.add_argument("--in-flight", type=int, default=0,
+                    help="e2e steps on the device before the oldest one's losses are read (0: 2)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -527,6 +529,12 @@ def main():
                 "flops_per_step": ff.value / args.profile_steps}
     check(lib.ngdb_profile_enable(ctx, 0))
     roof = roofline(fams, args.config)
+    # the resident plans (and their captured graphs) are released before the
+    # e2e leg, which streams fresh plans
+    check(lib.ngdb_sync(ctx))
+    for h in plans:
+        check(lib.ngdb_plan_destroy(h))
+    plans.clear()
 
     # ---- e2e: public C ABI call with host buffers ----------------------------
     # The trainer loop (ngdb_train_run): host producer threads sample and plan
@@ -540,7 +548,7 @@ def main():
     def loop(n, tag):
         eng.step_count = step_no
         return eng.train(graph, w, n, batch=batch, n_neg=n_neg, seed=3, first_tag=tag,
-                         n_producers=args.producers)
+                         n_producers=args.producers, in_flight=args.in_flight)
     loop(args.warmup, tag0)
     step_no += args.warmup
     b0, d0 = C.c_int64(), C.c_int64()
@@ -620,8 +628,6 @@ def main():
             "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
-    for h in plans:
-        lib.ngdb_plan_destroy(h)
     if dist is not None:
         dist.destroy_process_group()
 

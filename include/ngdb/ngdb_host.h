@@ -129,7 +129,10 @@ typedef struct ngdb_train_opts {
   int32_t queue_depth;           /* planned batches ahead; 0: 2 * n_producers */
   uint64_t seed;                 /* sampler seed (3) */
   uint64_t first_tag;
+  int32_t in_flight;             /* steps submitted ahead of the oldest uncollected one; 0: 2 */
+  int32_t flags;                 /* NGDB_TRAIN_NO_GRAPHS: stream launches instead of step graphs */
 } ngdb_train_opts;
+#define NGDB_TRAIN_NO_GRAPHS 1
 int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
                    int64_t first_step, int32_t n_steps, double* loss_per_step,
                    float* per_query_loss, double* timings);

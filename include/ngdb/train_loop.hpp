@@ -31,6 +31,7 @@ struct TrainLoopConfig {
   int32_t n_producers = 0;  // 0: hardware threads - 1 (at least 1)
   int32_t queue_depth = 0;  // planned batches buffered ahead of the consumer; 0: 2 * producers
   bool graphs = true;       // launch each step as one CUDA graph (ngdb_step_launch)
+  int32_t in_flight = 2;    // steps on the device before the oldest one's losses are read back
 };
 
 struct TrainLoopStats {

@@ -487,6 +487,8 @@ int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
     cfg.queue_depth = o->queue_depth;
     cfg.seed = o->seed;
     cfg.first_tag = o->first_tag;
+    if (o->in_flight > 0) cfg.in_flight = o->in_flight;
+    cfg.graphs = (o->flags & NGDB_TRAIN_NO_GRAPHS) == 0;
     const auto st = ngdb::run_train_loop(ctx, g->split, cfg, first_step, n_steps, loss_per_step,
                                          per_query_loss);
     if (timings) {

@@ -50,6 +50,8 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
   P = std::min(P, n_steps);
   const int32_t depth = std::max(cfg.queue_depth > 0 ? cfg.queue_depth : 2 * P, 1);
   stats.producers = P;
+  // the context keeps 4 result slots (ngdb_step_end_async)
+  const int32_t in_flight = std::clamp(cfg.in_flight, 1, 3);
 
   std::vector<PlannedSlot> ring(depth);
   std::mutex mu;
@@ -137,8 +139,8 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
       check_status(ngdb_step_end_async(ctx, &ticket));
       pending.emplace_back(i, ticket);
       stats.submit_s += seconds_since(t_submit);
-      // step i-1's losses, read back while step i runs on the device
-      while (pending.size() > 1) collect();
+      // the oldest step's losses, read back while the newer ones run on the device
+      while (static_cast<int32_t>(pending.size()) >= in_flight) collect();
     }
     while (!pending.empty()) collect();
   } catch (...) {

@@ -302,14 +302,15 @@ class Engine:
 
     def train(self, graph: Graph, weights: np.ndarray, n_steps: int, batch: int = 512,
               n_neg: int = 128, seed: int = 3, first_tag: int = 0, n_producers: int = 0,
-              queue_depth: int = 0, per_query: bool = False):
+              queue_depth: int = 0, per_query: bool = False, in_flight: int = 0,
+              graphs: bool = True):
         """The trainer loop: n_steps steps of batches sampled
         from Rng(seed).fork(first_tag + i) by host producer threads, planned,
         uploaded and run back to back (ngdb_train_run). Returns the per-step loss
         sums (and [n_steps][batch] per-query losses with per_query=True)."""
         w = np.ascontiguousarray(weights, dtype=np.float64)
         opts = TrainOpts(_p(w, C.c_double), batch, n_neg, self.b_max, n_producers, queue_depth,
-                         seed, first_tag)
+                         seed, first_tag, in_flight, 0 if graphs else 1)
         sums = np.zeros(n_steps, dtype=np.float64)
         pq = np.zeros((n_steps, batch), dtype=np.float32) if per_query else None
         timings = (C.c_double * 6)()

@@ -1,0 +1,34 @@
+"""e2e trainer-loop sweep (GPU box): C2 q/s for in-flight depth x step graphs x producers.
+Usage: python tools/e2e_sweep.py [steps]"""
+import itertools
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2602_21597_b200 as m  # noqa: E402
+
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+backbone, shape, mix, dim, batch, n_neg = bench.CONFIGS["c2"]
+graph = m.Graph.synthetic(shape, 1)
+info = graph.info()
+eng = m.Engine(backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=n_neg,
+               b_max=512, max_queries=batch, device=0)
+w = m.pattern_weights(bench.MIXES[mix])
+ncpu = os.cpu_count() or 2
+tag = 1_000_000
+for fl, gr, pr in itertools.product([1, 2, 3], [True, False], [ncpu - 1, max(1, ncpu // 2)]):
+    eng.train(graph, w, 5, batch=batch, n_neg=n_neg, first_tag=tag, n_producers=pr,
+              in_flight=fl, graphs=gr)
+    tag += 5
+    t0 = time.perf_counter()
+    eng.train(graph, w, steps, batch=batch, n_neg=n_neg, first_tag=tag, n_producers=pr,
+              in_flight=fl, graphs=gr)
+    dt = time.perf_counter() - t0
+    tag += steps
+    tim = {k: round(v / steps * 1e3, 4) for k, v in eng.last_timings.items()}
+    print(json.dumps({"in_flight": fl, "graphs": gr, "producers": pr,
+                      "qps": round(batch * steps / dt), "ms_per_step": round(dt / steps * 1e3, 4),
+                      "consumer_ms": tim}), flush=True)
