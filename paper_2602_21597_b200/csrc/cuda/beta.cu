@@ -28,6 +28,7 @@
 // the saved inputs.
 #include <algorithm>
 
+#include "adam.cuh"
 #include "common.cuh"
 #include "mlp_util.cuh"
 #include "special.cuh"
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(kWarps * 32) beta_entity_adam_kernel(DevArgs a
   const int row_idx = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row_idx >= t.n_rows) return;
-  const float ibc1 = 1.f / bc[0], ibc2 = 1.f / bc[1];  // bias corrections as reciprocals
+  const AdamK k = adam_consts(hp, bc);
   const int64_t row = t.rows[row_idx];
   const int beg = t.seg[row_idx], end = t.seg[row_idx + 1];
   const int D = a.dim, d4 = D / 4;
@@ -130,16 +131,8 @@ __global__ void __launch_bounds__(kWarps * 32) beta_entity_adam_kernel(DevArgs a
     for (int half = 0; half < 2; ++half) {
       const int off = half * D + 4 * ch;
       float4 w = ld4(wp + off), m = ld4(mp + off), v = ld4(vp + off);
-      float* wv = &w.x;
-      float* mv = &m.x;
-      float* vv = &v.x;
       const float* g = half ? gb : ga;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        mv[u] = hp.b1 * mv[u] + (1.f - hp.b1) * g[u];
-        vv[u] = hp.b2 * vv[u] + (1.f - hp.b2) * g[u] * g[u];
-        wv[u] -= hp.lr * (mv[u] * ibc1) / (sqrtf(vv[u] * ibc2) + hp.eps);
-      }
+      w = adam4(w, m, v, make_float4(g[0], g[1], g[2], g[3]), k);
       st4(wp + off, w);
       st4(mp + off, m);
       st4(vp + off, v);
