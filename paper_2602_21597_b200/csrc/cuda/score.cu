@@ -87,6 +87,19 @@ __device__ __forceinline__ float mul_sign(float m, float t) {
   return t != 0.f ? s : 0.f;
 }
 
+// -(m * sign(t)) with sign(0) = 0: the sign bit of t, inverted, onto m (one LOP3)
+__device__ __forceinline__ float neg_sign(float m, float t) {
+  const float s = __int_as_float(__float_as_int(m) ^ (~__float_as_int(t) & 0x80000000));
+  return t != 0.f ? s : 0.f;
+}
+
+// a += (x, y, z, w) as two packed FADD2
+__device__ __forceinline__ void add2(float4& a, float x, float y, float z, float w) {
+  const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(x, y));
+  const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(z, w));
+  a = make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
 // Per-backbone distance of one padded row against the lane's query slice and
 // its gradient contribution coef * dd/dq.
 // The query slice is NOT held in registers: it is re-read from the shared
@@ -125,15 +138,21 @@ struct RowMath {
         s2 += c.z * v.z + o.z * v2.z;
         s3 += c.w * v.w + o.w * v2.w;
       } else {
-        t[i] = make_float4(v.x - c.x, v.y - c.y, v.z - c.z, v.w - c.w);
+        // t = v - c as two packed FFMA2 (v + (-1) c: exact product, one rounding)
+        const float2 m1 = make_float2(-1.f, -1.f);
+        const float2 t01 = __ffma2_rn(make_float2(c.x, c.y), m1, make_float2(v.x, v.y));
+        const float2 t23 = __ffma2_rn(make_float2(c.z, c.w), m1, make_float2(v.z, v.w));
+        t[i] = make_float4(t01.x, t01.y, t23.x, t23.y);
         if constexpr (BB == NGDB_GQE) {
           s0 += fabsf(t[i].x); s1 += fabsf(t[i].y); s2 += fabsf(t[i].z); s3 += fabsf(t[i].w);
-        } else {  // outside part max(|t|-o, 0) in s0/s1, inside part min(|t|, o) in s2/s3
+        } else {  // outside part max(|t|-o, 0) in (s0, s1), inside part min(|t|, o) in (s2, s3)
           const float4 o = qo(i);
-          s0 += fmaxf(fabsf(t[i].x) - o.x, 0.f) + fmaxf(fabsf(t[i].y) - o.y, 0.f);
-          s1 += fmaxf(fabsf(t[i].z) - o.z, 0.f) + fmaxf(fabsf(t[i].w) - o.w, 0.f);
-          s2 += fminf(fabsf(t[i].x), o.x) + fminf(fabsf(t[i].y), o.y);
-          s3 += fminf(fabsf(t[i].z), o.z) + fminf(fabsf(t[i].w), o.w);
+          float2 so = make_float2(s0, s1), si = make_float2(s2, s3);
+          so = __fadd2_rn(so, make_float2(fmaxf(fabsf(t[i].x) - o.x, 0.f), fmaxf(fabsf(t[i].y) - o.y, 0.f)));
+          so = __fadd2_rn(so, make_float2(fmaxf(fabsf(t[i].z) - o.z, 0.f), fmaxf(fabsf(t[i].w) - o.w, 0.f)));
+          si = __fadd2_rn(si, make_float2(fminf(fabsf(t[i].x), o.x), fminf(fabsf(t[i].y), o.y)));
+          si = __fadd2_rn(si, make_float2(fminf(fabsf(t[i].z), o.z), fminf(fabsf(t[i].w), o.w)));
+          s0 = so.x; s1 = so.y; s2 = si.x; s3 = si.y;
         }
       }
     }
@@ -149,21 +168,16 @@ struct RowMath {
         gc[i].z += coef * t[i].z; go[i].z += coef * t2[i].z;
         gc[i].w += coef * t[i].w; go[i].w += coef * t2[i].w;
       } else if constexpr (BB == NGDB_GQE) {  // d|v-c|/dc = -sign(v-c)
-        gc[i].x -= mul_sign(coef, t[i].x);
-        gc[i].y -= mul_sign(coef, t[i].y);
-        gc[i].z -= mul_sign(coef, t[i].z);
-        gc[i].w -= mul_sign(coef, t[i].w);
+        add2(gc[i], neg_sign(coef, t[i].x), neg_sign(coef, t[i].y), neg_sign(coef, t[i].z),
+             neg_sign(coef, t[i].w));
       } else {  // outside the box: dc = -sign, do = alpha - 1; inside: dc = -alpha sign
         const float ca = coef * alpha, co = coef * (alpha - 1.f);
         const float4 o = qo(i);
-#define NGDB_Q2B_GRAD(X)                               \
-  {                                                    \
-    const bool out = fabsf(t[i].X) > o.X;              \
-    gc[i].X -= mul_sign(out ? coef : ca, t[i].X);      \
-    go[i].X += out ? co : 0.f;                         \
-  }
-        NGDB_Q2B_GRAD(x) NGDB_Q2B_GRAD(y) NGDB_Q2B_GRAD(z) NGDB_Q2B_GRAD(w)
-#undef NGDB_Q2B_GRAD
+        const bool ox = fabsf(t[i].x) > o.x, oy = fabsf(t[i].y) > o.y;
+        const bool oz = fabsf(t[i].z) > o.z, ow = fabsf(t[i].w) > o.w;
+        add2(gc[i], neg_sign(ox ? coef : ca, t[i].x), neg_sign(oy ? coef : ca, t[i].y),
+             neg_sign(oz ? coef : ca, t[i].z), neg_sign(ow ? coef : ca, t[i].w));
+        add2(go[i], ox ? co : 0.f, oy ? co : 0.f, oz ? co : 0.f, ow ? co : 0.f);
       }
     }
   }
