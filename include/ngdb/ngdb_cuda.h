@@ -264,6 +264,17 @@ const char* ngdb_profile_family_name(int32_t family);
 int64_t ngdb_launch_count(ngdb_ctx* ctx);
 /* Cumulative bytes of step data the streaming ABI copied: plan uploads (H2D)
  * and loss/flag read-backs (D2H). */
+/* Evaluator hot path (SPEC.md:602-646 `evaluator`: filtered_rank over all
+ * entities, mean-rank ties; replaces the per-query full-entity scoring loop of
+ * evaluate()). queries [n_queries][wq] (GQE: q; Q2B: centre |
+ * offset) scored against the context's current entity table; targets [n];
+ * filter CSR filter_offsets [n+1] (offsets[0] = 0), filter_ids (sets; duplicates
+ * ignored). ranks[q] = 1 + #{e not in filter+target: d(e) < d(target)}
+ * + floor(#ties / 2). Synchronous. GQE and Q2B only (BetaE / fusion:
+ * NGDB_ERR_MISSING_KERNEL); a target inside its own filter is NGDB_ERR_DOMAIN
+ * (SPEC TargetFiltered). */
+int ngdb_eval_ranks(ngdb_ctx* ctx, const float* queries, int32_t n_queries, const int32_t* targets,
+                    const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks);
 int ngdb_transfer_bytes(ngdb_ctx* ctx, int64_t* h2d, int64_t* d2h);
 /* ngdb_step_launch graphs: launches served by updating a cached executable
  * graph of the same invocation structure vs fresh instantiations. */

@@ -208,3 +208,59 @@ def trigamma(x):
 
 def beta_kl(a1, b1, a2, b2):
     return lib.oracle_beta_kl(float(a1), float(b1), float(a2), float(b2))
+
+
+# ---- evaluator (module `evaluator`) -------------------------
+# Pure numpy restatement. Distances follow the backbone formulas (GQE ||v-q||_1,
+# SURVEY A-7; Q2B SPEC.md:378) in float32 with the dimensions summed in order
+# (np.cumsum is a sequential accumulation), i.e. the rounding of a sequential
+# fp32 loop; scores are negated distances.
+
+class TargetFiltered(ValueError):
+    """SPEC.md:617 errors: TargetFiltered (target inside its filter set)."""
+
+
+def filtered_rank(scores, target, filt):
+    """SPEC.md:614-618: 1 + |{e not in filter+{target}: s(e) > s(t)}| + floor(ties/2)."""
+    filt = set(int(f) for f in filt)
+    if int(target) in filt:
+        raise TargetFiltered(f"target {target} is in its filter set")
+    s = np.asarray(scores)
+    st = s[target]
+    keep = np.ones(len(s), dtype=bool)
+    keep[list(filt)] = False
+    keep[target] = False
+    better = int(np.count_nonzero(s[keep] > st))
+    ties = int(np.count_nonzero(s[keep] == st))
+    return 1 + better + ties // 2
+
+
+def filtered_rank_sorted(scores, target, filt):
+    """The SPEC's derived check: rank by sorting the filtered list
+    (descending score); ties are the run of equal scores, mean-rank rounded down."""
+    filt = set(int(f) for f in filt)
+    cand = [e for e in range(len(scores)) if e not in filt]
+    order = sorted(cand, key=lambda e: -scores[e])
+    st = scores[target]
+    first = next(i for i, e in enumerate(order) if scores[e] == st)
+    n_eq = sum(1 for e in cand if scores[e] == st) - 1  # equal competitors
+    return 1 + first + n_eq // 2
+
+
+def eval_distances(backbone, ent, q, dim, alpha=0.02):
+    """[n_ent] float32 distances of every entity row to one query (GQE: q [d];
+    Q2B: centre | offset [2d]), summed sequentially over the dimensions."""
+    ent = np.asarray(ent, dtype=np.float32)[:, :dim]
+    q = np.asarray(q, dtype=np.float32)
+    t = np.abs(ent - q[None, :dim])
+    if backbone == "gqe":
+        return np.cumsum(t, axis=1, dtype=np.float32)[:, -1]
+    o = q[None, dim:2 * dim]
+    out = np.cumsum(np.maximum(t - o, np.float32(0)), axis=1, dtype=np.float32)[:, -1]
+    inn = np.cumsum(np.minimum(t, o), axis=1, dtype=np.float32)[:, -1]
+    return out + np.float32(alpha) * inn
+
+
+def eval_ranks(backbone, ent, queries, targets, filters, dim, alpha=0.02):
+    return np.array([filtered_rank(-eval_distances(backbone, ent, q, dim, alpha), t, f)
+                     for q, t, f in zip(queries, targets, filters)], dtype=np.int64)

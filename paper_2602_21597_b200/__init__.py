@@ -5,8 +5,8 @@ include/ngdb/ngdb_cuda.h. See DESIGN.md.
 """
 from .engine import (BACKBONES, OP_KINDS, PATTERNS, PATTERN_ARITY, Batch, BatchArrays, Engine,
                      Graph, PlannedStep, init_params, ngse_read, ngse_write, param_specs,
-                     pattern_weights, semantic_store)
+                     pattern_weights, rank_metrics, semantic_store)
 
 __all__ = ["BACKBONES", "OP_KINDS", "PATTERNS", "PATTERN_ARITY", "Batch", "BatchArrays", "Engine",
            "Graph", "PlannedStep", "init_params", "ngse_read", "ngse_write", "param_specs",
-           "pattern_weights", "semantic_store"]
+           "pattern_weights", "rank_metrics", "semantic_store"]

@@ -241,6 +241,23 @@ struct KSpan {
   static KSpan single(int n, int k) { return KSpan{n, k, k}; }
 };
 // rows.cu
+// evaluator (evaluate.cu): full-entity scoring + filtered rank counts
+struct EvalArgs {
+  const float* ent;  // entity table [n_ent][ent_w] (GQE/Q2B rows are d-wide points)
+  int64_t ent_w;
+  int32_t n_ent, dim, backbone;
+  float alpha;       // Q2B inside weight
+  const float* q;    // [nq][wq]: GQE q; Q2B centre | offset
+  int32_t wq, nq;
+  const int32_t* target;
+  const int32_t* f_off;  // [nq + 1] CSR of filter entities
+  const int32_t* f_ids;
+  float* dt;             // [nq] target distances
+  int32_t* better;       // [nq]
+  int32_t* ties;         // [nq]
+};
+int launch_eval_ranks(const EvalArgs& a, int32_t n_filter, cudaStream_t s);
+
 int launch_embed(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
 int launch_project(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
 int launch_negate(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);

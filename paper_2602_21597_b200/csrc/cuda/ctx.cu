@@ -278,6 +278,9 @@ struct ngdb_ctx {
   bool use_graphs = true;
   float* l2_flush = nullptr;
   int64_t l2_flush_bytes = 0;
+  // evaluator staging (ngdb_eval_ranks)
+  char* eval_buf = nullptr;
+  int64_t eval_cap = 0;
 
   Param* find(const std::string& name) {
     for (auto& p : params)
@@ -951,6 +954,7 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
       cudaFree(p.v);
       if (p.g) cudaFree(p.g);
     }
+  if (c->eval_buf) cudaFree(c->eval_buf);
   if (c->cand_local) cudaFree(c->cand_local);
   if (c->anchor_local) cudaFree(c->anchor_local);
   if (c->fscratch) cudaFree(c->fscratch);
@@ -1457,6 +1461,85 @@ int ngdb_graph_stats(ngdb_ctx* c, int64_t* updates, int64_t* instantiations) {
   return guarded([&] {
     if (updates) *updates = c->exec_updates;
     if (instantiations) *instantiations = c->exec_instantiations;
+  });
+}
+
+int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const int32_t* targets,
+                    const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks) {
+  return guarded([&] {
+    if (n_queries < 0 || (n_queries > 0 && (!queries || !targets || !filter_offsets || !ranks)))
+      throw Fail{NGDB_ERR_CONFIG, "eval_ranks: null argument"};
+    if (c->desc.backbone == NGDB_BETAE || c->fused())
+      throw Fail{NGDB_ERR_MISSING_KERNEL, "eval_ranks: GQE and Q2B backbones only"};
+    if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "eval_ranks: row-sharded context"};
+    if (n_queries == 0) return;
+    const Param& ent = c->params[c->ent_idx];
+    const int32_t n_ent = c->desc.n_entities, wq = c->query_width();
+    if (filter_offsets[0] != 0) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "eval_ranks: filter_offsets[0] != 0"};
+    // filter sets: validated, sorted and de-duplicated per query (they are sets)
+    std::vector<int32_t> off(n_queries + 1, 0), ids;
+    ids.reserve(filter_offsets[n_queries] > 0 ? filter_offsets[n_queries] : 0);
+    for (int32_t q = 0; q < n_queries; ++q) {
+      const int32_t t = targets[q];
+      if (t < 0 || t >= n_ent) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "eval_ranks: target out of range"};
+      const int32_t b = filter_offsets[q], e = filter_offsets[q + 1];
+      if (e < b) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "eval_ranks: filter_offsets not ascending"};
+      const size_t first = ids.size();
+      for (int32_t i = b; i < e; ++i) {
+        const int32_t f = filter_ids[i];
+        if (f < 0 || f >= n_ent) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "eval_ranks: filter id out of range"};
+        if (f == t) throw Fail{NGDB_ERR_DOMAIN, "eval_ranks: TargetFiltered (target in its filter set)"};
+        ids.push_back(f);
+      }
+      std::sort(ids.begin() + first, ids.end());
+      ids.erase(std::unique(ids.begin() + first, ids.end()), ids.end());
+      off[q + 1] = static_cast<int32_t>(ids.size());
+    }
+    const int64_t nq = n_queries, nf = static_cast<int64_t>(ids.size());
+    auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+    const int64_t b_q = al(nq * wq * 4), b_t = al(nq * 4), b_off = al((nq + 1) * 4),
+                  b_ids = al(std::max<int64_t>(nf, 1) * 4);
+    const int64_t need = b_q + b_off + b_ids + 4 * b_t;
+    if (need > c->eval_cap) {
+      CK(cudaStreamSynchronize(c->stream));
+      if (c->eval_buf) CK(cudaFree(c->eval_buf));
+      c->eval_cap = need + need / 2;
+      CK(cudaMalloc(&c->eval_buf, c->eval_cap));
+    }
+    char* p = c->eval_buf;
+    EvalArgs a{};
+    a.ent = ent.w;
+    a.ent_w = ent.cols;
+    a.n_ent = n_ent;
+    a.dim = c->desc.dim;
+    a.backbone = c->desc.backbone;
+    a.alpha = c->desc.alpha_box;
+    a.wq = wq;
+    a.nq = n_queries;
+    float* dq = reinterpret_cast<float*>(p);            p += b_q;
+    int32_t* dtg = reinterpret_cast<int32_t*>(p);       p += b_t;
+    int32_t* doff = reinterpret_cast<int32_t*>(p);      p += b_off;
+    int32_t* dids = reinterpret_cast<int32_t*>(p);      p += b_ids;
+    a.dt = reinterpret_cast<float*>(p);                 p += b_t;
+    a.better = reinterpret_cast<int32_t*>(p);           p += b_t;
+    a.ties = reinterpret_cast<int32_t*>(p);
+    a.q = dq;
+    a.target = dtg;
+    a.f_off = doff;
+    a.f_ids = dids;
+    CK(cudaMemcpyAsync(dq, queries, nq * wq * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dtg, targets, nq * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(doff, off.data(), (nq + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+    if (nf) CK(cudaMemcpyAsync(dids, ids.data(), nf * 4, cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += nq * wq * 4 + nq * 4 + (nq + 1) * 4 + nf * 4;
+    c->launches += launch_eval_ranks(a, static_cast<int32_t>(nf), c->stream);
+    CK(cudaGetLastError());
+    std::vector<int32_t> cnt(2 * nq);
+    CK(cudaMemcpyAsync(cnt.data(), a.better, nq * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(cnt.data() + nq, a.ties, nq * 4, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes += 2 * nq * 4;
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t q = 0; q < nq; ++q) ranks[q] = 1 + cnt[q] + cnt[nq + q] / 2;
   });
 }
 

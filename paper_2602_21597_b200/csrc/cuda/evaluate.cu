@@ -1,0 +1,169 @@
+// Evaluator hot path: full-entity scoring + filtered rank (SPEC.md:602-646,
+// module `evaluator`).
+//
+//   filtered_rank(scores, target, filter) =
+//       1 + |{e not in filter+{target} : score(e) > score(target)}| + floor(ties / 2)
+//   (mean-rank tie rule), score = -distance.
+//
+// Three launches per batch of queries, all on the context stream:
+//   1. eval_target_kernel: d_t = dist(target, q) for every query (one thread per
+//      query, sequential over the d dimensions);
+//   2. eval_count_kernel:  every (entity, query) distance, tiled 64 entities x 32
+//      queries per CTA with 32-dimension slices of both staged in shared memory
+//      (each entity value is reused by 8 queries per thread, each query slice by
+//      64 entities); counts d < d_t and d == d_t over all non-target entities,
+//      warp-reduced, one integer atomic per (warp, query);
+//   3. eval_filter_kernel: the filtered entities' contributions are removed again
+//      (one thread per (query, filter entry)).
+// Every distance is accumulated in the same order (dimension 0..d-1, one fp32
+// rounding per step, __fadd_rn so nothing is contracted into an FMA), so the
+// distance of an entity is bit-identical in all three kernels: comparisons
+// against d_t — including exact ties — are consistent, and the counts are
+// integers (deterministic regardless of atomic order).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace ngdb_dev {
+
+namespace {
+
+constexpr int TE = 64;   // entities per CTA
+constexpr int TQ = 32;   // queries per CTA
+constexpr int KS = 32;   // dimensions per shared-memory slice
+constexpr int QPT = 8;   // queries per thread (256 threads = 64 entities x 4 query groups)
+constexpr int ES = KS + 4;  // padded entity row: float4-aligned, conflict-free LDS.128
+
+// one dimension of the distance, accumulated in dimension order
+template <int BB>
+__device__ __forceinline__ void acc_dim(float& out, float& in, float v, float c, float o) {
+  const float t = fabsf(__fsub_rn(v, c));
+  if constexpr (BB == NGDB_GQE) {
+    out = __fadd_rn(out, t);
+  } else {
+    out = __fadd_rn(out, fmaxf(__fsub_rn(t, o), 0.f));
+    in = __fadd_rn(in, fminf(t, o));
+  }
+}
+template <int BB>
+__device__ __forceinline__ float finish(float out, float in, float alpha) {
+  return BB == NGDB_GQE ? out : __fadd_rn(out, __fmul_rn(alpha, in));
+}
+
+template <int BB>
+__device__ float row_distance(const EvalArgs& a, int e, int q) {
+  const float* v = a.ent + static_cast<int64_t>(e) * a.ent_w;
+  const float* qc = a.q + static_cast<int64_t>(q) * a.wq;
+  float out = 0.f, in = 0.f;
+  for (int k = 0; k < a.dim; ++k)
+    acc_dim<BB>(out, in, v[k], qc[k], BB == NGDB_GQE ? 0.f : qc[a.dim + k]);
+  return finish<BB>(out, in, a.alpha);
+}
+
+template <int BB>
+__global__ void eval_target_kernel(EvalArgs a) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= a.nq) return;
+  a.dt[q] = row_distance<BB>(a, a.target[q], q);
+  a.better[q] = 0;
+  a.ties[q] = 0;
+}
+
+template <int BB>
+__global__ void __launch_bounds__(256) eval_count_kernel(EvalArgs a) {
+  __shared__ __align__(16) float es[TE][ES];
+  __shared__ __align__(16) float qcs[TQ][KS];
+  __shared__ __align__(16) float qos[BB == NGDB_GQE ? 1 : TQ][KS];
+  const int e0 = blockIdx.x * TE, q0 = blockIdx.y * TQ;
+  const int tid = threadIdx.x;
+  const int el = tid & (TE - 1), qg = tid / TE;  // a warp shares its query group
+  float out[QPT], in[QPT];
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) out[j] = in[j] = 0.f;
+  for (int k0 = 0; k0 < a.dim; k0 += KS) {
+    // stage the slice: 64 entity rows x 32 dims, 32 queries x 32 dims (zero padded)
+    for (int i = tid; i < TE * KS; i += 256) {
+      const int r = i / KS, k = i % KS, e = e0 + r;
+      es[r][k] = (e < a.n_ent && k0 + k < a.dim) ? a.ent[static_cast<int64_t>(e) * a.ent_w + k0 + k] : 0.f;
+    }
+    for (int i = tid; i < TQ * KS; i += 256) {
+      const int r = i / KS, k = i % KS, q = q0 + r;
+      const bool ok = q < a.nq && k0 + k < a.dim;
+      const float* qr = a.q + static_cast<int64_t>(q) * a.wq;
+      qcs[r][k] = ok ? qr[k0 + k] : 0.f;
+      if constexpr (BB != NGDB_GQE) qos[r][k] = ok ? qr[a.dim + k0 + k] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int k = 0; k < KS; k += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(&es[el][k]);
+#pragma unroll
+      for (int j = 0; j < QPT; ++j) {
+        const int ql = qg * QPT + j;
+        const float4 c = *reinterpret_cast<const float4*>(&qcs[ql][k]);
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (BB != NGDB_GQE) o = *reinterpret_cast<const float4*>(&qos[ql][k]);
+        acc_dim<BB>(out[j], in[j], v.x, c.x, o.x);
+        acc_dim<BB>(out[j], in[j], v.y, c.y, o.y);
+        acc_dim<BB>(out[j], in[j], v.z, c.z, o.z);
+        acc_dim<BB>(out[j], in[j], v.w, c.w, o.w);
+      }
+    }
+    __syncthreads();
+  }
+  const int e = e0 + el;
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) {
+    const int q = q0 + qg * QPT + j;
+    bool b = false, t = false;
+    if (q < a.nq && e < a.n_ent && e != a.target[q]) {
+      const float d = finish<BB>(out[j], in[j], a.alpha), d_t = a.dt[q];
+      b = d < d_t;
+      t = d == d_t;
+    }
+    const unsigned nb = __popc(__ballot_sync(0xffffffffu, b));
+    const unsigned nt = __popc(__ballot_sync(0xffffffffu, t));
+    if ((tid & 31) == 0 && q < a.nq) {
+      if (nb) atomicAdd(&a.better[q], static_cast<int32_t>(nb));
+      if (nt) atomicAdd(&a.ties[q], static_cast<int32_t>(nt));
+    }
+  }
+}
+
+// one thread per (query, filter entry): remove the filtered entities again
+template <int BB>
+__global__ void eval_filter_kernel(EvalArgs a, int32_t n_filter) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_filter) return;
+  int lo = 0, hi = a.nq;  // query of entry i: last q with f_off[q] <= i
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (a.f_off[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  const int q = lo, e = a.f_ids[i];
+  if (e == a.target[q]) return;  // excluded by the host (TargetFiltered)
+  const float d = row_distance<BB>(a, e, q), d_t = a.dt[q];
+  if (d < d_t) atomicSub(&a.better[q], 1);
+  else if (d == d_t) atomicSub(&a.ties[q], 1);
+}
+
+template <int BB>
+void launch_eval(const EvalArgs& a, int32_t n_filter, cudaStream_t s) {
+  eval_target_kernel<BB><<<(a.nq + 127) / 128, 128, 0, s>>>(a);
+  const dim3 grid((a.n_ent + TE - 1) / TE, (a.nq + TQ - 1) / TQ);
+  eval_count_kernel<BB><<<grid, 256, 0, s>>>(a);
+  if (n_filter > 0) eval_filter_kernel<BB><<<(n_filter + 127) / 128, 128, 0, s>>>(a, n_filter);
+}
+
+}  // namespace
+
+// 3 launches; the caller validated shapes and indices
+int launch_eval_ranks(const EvalArgs& a, int32_t n_filter, cudaStream_t s) {
+  if (a.nq <= 0) return 0;
+  if (a.backbone == NGDB_GQE) launch_eval<NGDB_GQE>(a, n_filter, s);
+  else launch_eval<NGDB_Q2B>(a, n_filter, s);
+  return n_filter > 0 ? 3 : 2;
+}
+
+}  // namespace ngdb_dev

@@ -187,6 +187,16 @@ class PlannedStep:
             self._h = None
 
 
+def rank_metrics(ranks: Sequence[int]) -> Dict[str, float]:
+    """MRR and Hits@{1,3,10} of filtered ranks (SPEC.md:625-630 EvalReport)."""
+    r = np.asarray(ranks, dtype=np.float64)
+    if r.size == 0:
+        return {"mrr": 0.0, "hits@1": 0.0, "hits@3": 0.0, "hits@10": 0.0, "count": 0}
+    return {"mrr": float(np.mean(1.0 / r)), "hits@1": float(np.mean(r <= 1)),
+            "hits@3": float(np.mean(r <= 3)), "hits@10": float(np.mean(r <= 10)),
+            "count": int(r.size)}
+
+
 def param_specs(backbone: str, n_entities: int, n_relations: int, dim: int,
                 semantic_dim: int = 0) -> List[tuple]:
     """(name, rows, cols, sparse) in registry order (trainer.hpp param_specs)."""
@@ -323,6 +333,24 @@ class Engine:
                              "collect_wait_s": timings[2], "submit_begin_s": timings[3],
                              "submit_pools_s": timings[4], "submit_optimizer_s": timings[5]}
         return (sums, pq) if per_query else sums
+
+    def eval_ranks(self, queries: np.ndarray, targets: Sequence[int],
+                   filters: Sequence[Sequence[int]]) -> np.ndarray:
+        """Filtered ranks of `targets` among all entities (SPEC.md:614-618,
+        `filtered_rank`; score = -distance, mean-rank ties) for query embeddings
+        [n][wq] (GQE: q; Q2B: centre | offset) against the current entity table
+        (ngdb_eval_ranks). filters[i] is query i's filter set (other known answers)."""
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        n = q.shape[0]
+        t = np.ascontiguousarray(targets, dtype=np.int32)
+        off = np.zeros(n + 1, dtype=np.int32)
+        off[1:] = np.cumsum([len(f) for f in filters]) if n else []
+        ids = np.ascontiguousarray(np.concatenate([np.asarray(f, dtype=np.int32) for f in filters])
+                                   if n and off[-1] else np.zeros(1, dtype=np.int32))
+        ranks = np.zeros(n, dtype=np.int32)
+        check(lib.ngdb_eval_ranks(self._h, _p(q, C.c_float), n, _p(t, C.c_int32),
+                                  _p(off, C.c_int32), _p(ids, C.c_int32), _p(ranks, C.c_int32)))
+        return ranks
 
     def run_step(self, step: PlannedStep, n_queries: int) -> np.ndarray:
         losses = np.zeros(n_queries, dtype=np.float32)

@@ -19,7 +19,10 @@ eng = m.Engine(backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg
 w = m.pattern_weights(bench.MIXES[mix])
 ncpu = os.cpu_count() or 2
 tag = 1_000_000
-for fl, gr, pr in itertools.product([1, 2, 3], [True, False], [ncpu - 1, max(1, ncpu // 2)]):
+combos = list(itertools.product([1, 2, 3], [True, False], [ncpu - 1, max(1, ncpu // 2)]))
+if os.environ.get("SWEEP_DEFAULT_ONLY"):
+    combos = [(2, True, ncpu - 1)] * 3
+for fl, gr, pr in combos:
     eng.train(graph, w, 5, batch=batch, n_neg=n_neg, first_tag=tag, n_producers=pr,
               in_flight=fl, graphs=gr)
     tag += 5
