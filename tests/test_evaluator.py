@@ -77,7 +77,7 @@ def _case(backbone, n_ent, dim, nq, seed, integer=False, n_filter=12):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("backbone", ["gqe", "q2b"])
-@pytest.mark.parametrize("dim,integer", [(40, False), (400, False), (37, True), (400, True)])
+@pytest.mark.parametrize("dim,integer", [(40, False), (400, False), (36, True), (400, True)])
 def test_gpu_ranks_match_oracle(backbone, dim, integer):
     eng, ent, q, t, f = _case(backbone, 1000, dim, 70, seed=dim + integer, integer=integer)
     got = eng.eval_ranks(q, t, f)
