@@ -1491,7 +1491,7 @@ int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const 
         if (f == t) throw Fail{NGDB_ERR_DOMAIN, "eval_ranks: TargetFiltered (target in its filter set)"};
         ids.push_back(f);
       }
-      std::sort(ids.begin() + first, ids.end());
+      if (!std::is_sorted(ids.begin() + first, ids.end())) std::sort(ids.begin() + first, ids.end());
       ids.erase(std::unique(ids.begin() + first, ids.end()), ids.end());
       off[q + 1] = static_cast<int32_t>(ids.size());
     }

@@ -7,6 +7,7 @@ sampler and scheduler operations; everything computes in the native library
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import json
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence
@@ -340,13 +341,23 @@ class Engine:
         `filtered_rank`; score = -distance, mean-rank ties) for query embeddings
         [n][wq] (GQE: q; Q2B: centre | offset) against the current entity table
         (ngdb_eval_ranks). filters[i] is query i's filter set (other known answers)."""
+        n = len(targets)
+        off = np.zeros(n + 1, dtype=np.int32)
+        np.cumsum(np.fromiter(map(len, filters), dtype=np.int64, count=n), out=off[1:])
+        ids = np.fromiter(itertools.chain.from_iterable(filters), dtype=np.int32,
+                          count=int(off[-1]))
+        return self.eval_ranks_csr(queries, targets, off, ids)
+
+    def eval_ranks_csr(self, queries: np.ndarray, targets: np.ndarray, filter_offsets: np.ndarray,
+                       filter_ids: np.ndarray) -> np.ndarray:
+        """eval_ranks with the filter sets as a CSR (offsets [n+1], ids)."""
         q = np.ascontiguousarray(queries, dtype=np.float32)
         n = q.shape[0]
         t = np.ascontiguousarray(targets, dtype=np.int32)
-        off = np.zeros(n + 1, dtype=np.int32)
-        off[1:] = np.cumsum([len(f) for f in filters]) if n else []
-        ids = np.ascontiguousarray(np.concatenate([np.asarray(f, dtype=np.int32) for f in filters])
-                                   if n and off[-1] else np.zeros(1, dtype=np.int32))
+        off = np.ascontiguousarray(filter_offsets, dtype=np.int32)
+        ids = np.ascontiguousarray(filter_ids, dtype=np.int32)
+        if ids.size == 0:
+            ids = np.zeros(1, dtype=np.int32)
         ranks = np.zeros(n, dtype=np.int32)
         check(lib.ngdb_eval_ranks(self._h, _p(q, C.c_float), n, _p(t, C.c_int32),
                                   _p(off, C.c_int32), _p(ids, C.c_int32), _p(ranks, C.c_int32)))

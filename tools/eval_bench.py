@@ -21,11 +21,14 @@ for bb in ("gqe", "q2b"):
     q[:, dim:] = np.abs(q[:, dim:])
     t = rng.integers(0, n_ent, size=nq).astype(np.int32)
     f = [[int(x) for x in rng.integers(0, n_ent, size=100) if x != t[i]] for i in range(nq)]
+    off = np.zeros(nq + 1, dtype=np.int32)
+    off[1:] = np.cumsum([len(x) for x in f])
+    ids = np.concatenate([np.asarray(x, dtype=np.int32) for x in f])
     for _ in range(3):
-        eng.eval_ranks(q, t, f)
+        eng.eval_ranks_csr(q, t, off, ids)
     t0 = time.perf_counter()
     for _ in range(reps):
-        r = eng.eval_ranks(q, t, f)
+        r = eng.eval_ranks_csr(q, t, off, ids)
     dt = (time.perf_counter() - t0) / reps
     print(json.dumps({"evaluator": bb, "entities": n_ent, "dim": dim, "queries_per_call": nq,
                       "ms_per_call": dt * 1e3, "queries_per_s": nq / dt,
