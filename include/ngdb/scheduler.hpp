@@ -37,6 +37,11 @@ struct SchedulerConfig {
   // (DESIGN.md §6), an order the reuse plan does not cover; the trace itself is
   // always the Eq. 7 replay of `policy`.
   bool device_reuse = true;
+  // Query-level baseline executor (SPEC.md:664-672 run_query_level): queries
+  // are grouped by pattern and the groups run one after another (enum order),
+  // each group's DAG stage by stage with its own kernel invocations (Alg. 1
+  // restricted to the group) — no operator batching across patterns.
+  bool query_level = false;
 };
 
 // One PopBatch: a drain of the selected pool.

@@ -31,6 +31,7 @@ struct TrainConfig {
   bool semantic = false;
   int32_t semantic_dim = 0;
   bool sharded = false;  // entity table row-sharded across ranks
+  bool query_level = false;  // query-level baseline executor (SchedulerConfig::query_level)
   uint64_t seed_params = 2;
   uint64_t seed_sampler = 3;
 };

@@ -155,6 +155,17 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
   int64_t executed = 0;
   int32_t cycle = 0, step = 0;
 
+  // query-level mode: nodes of later pattern groups wait in `deferred` until
+  // every node of the current group has executed
+  const bool ql = cfg_.query_level;
+  std::vector<int32_t> deferred;
+  int32_t group = -1;
+  auto group_of = [&](int32_t v) { return static_cast<int32_t>(f.patterns[f.origin[v]]); };
+  if (ql) {
+    for (int32_t v : ready) deferred.push_back(v);
+    ready.clear();
+  }
+
   // Output allocation for node o (its T or G tensor).
   auto allocate = [&](int32_t o) {
     const OperatorNode& x = f.nodes[o];
@@ -185,12 +196,28 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
   };
 
   while (!ready.empty() || executed < n) {
-    for (int32_t v : ready) pools[f.nodes[v].op.pool()].q.emplace_back(v, cycle);
+    for (int32_t v : ready) {
+      if (ql && group_of(v) != group) deferred.push_back(v);
+      else pools[f.nodes[v].op.pool()].q.emplace_back(v, cycle);
+    }
     ready.clear();
     std::array<int64_t, kPoolCount> counts{}, heads{};
+    int64_t queued = 0;
     for (int p = 0; p < kPoolCount; ++p) {
       counts[p] = pools[p].size();
       heads[p] = counts[p] > 0 ? pools[p].q[pools[p].head].second : 0;
+      queued += counts[p];
+    }
+    if (ql && queued == 0) {
+      // the current group is done: the next pattern present, its ready nodes in id order
+      if (deferred.empty()) throw MissingKernel("query-level planner: no ready node");
+      group = kPatternCount;
+      for (int32_t v : deferred) group = std::min(group, group_of(v));
+      std::vector<int32_t> keep;
+      for (int32_t v : deferred) (group_of(v) == group ? ready : keep).push_back(v);
+      deferred.swap(keep);
+      std::sort(ready.begin(), ready.end());
+      continue;
     }
     const int tau = select_pool(counts, heads);
     const OperatorType type = OperatorType::from_pool(tau);

@@ -263,6 +263,7 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
   sc.n_candidates = nc;
   sc.elem_bytes = 4;
   sc.device_reuse = !cfg.sharded;
+  sc.query_level = cfg.query_level;
   Planner planner(sc);
   const TensorModel tm{wq, nc};
   auto elems = [](int64_t bytes) { return static_cast<int32_t>(bytes / 4); };

@@ -157,10 +157,12 @@ class PlannedStep:
     """A step planned by the host Max-Fillness scheduler (trace + device plan)."""
 
     def __init__(self, batch: Batch, backbone: str, dim: int, b_max: int = 512,
-                 semantic: bool = False, sharded: bool = False):
+                 semantic: bool = False, sharded: bool = False, query_level: bool = False):
+        """query_level: the SPEC's query-level baseline executor."""
         h = C.c_void_p()
         check(lib.ngdb_step_build_ex(batch._h, BACKBONES[backbone], dim, b_max,
-                                     int(semantic) | (2 if sharded else 0), C.byref(h)))
+                                     int(semantic) | (2 if sharded else 0) |
+                                     (4 if query_level else 0), C.byref(h)))
         self._h = h
 
     def trace(self, with_nodes: bool = False) -> dict:
