@@ -264,6 +264,15 @@ const char* ngdb_profile_family_name(int32_t family);
 int64_t ngdb_launch_count(ngdb_ctx* ctx);
 /* Cumulative bytes of step data the streaming ABI copied: plan uploads (H2D)
  * and loss/flag read-backs (D2H). */
+/* Checkpoint (versioned binary blob of named parameter tensors +
+ * config hash; cadence SPEC.md:587). Writes every registry tensor's theta and
+ * Adam m, v plus `step` (so a resumed run continues bit-identically) with an
+ * FNV-1a trailer. Load checks magic/version/checksum (NGDB_ERR_DOMAIN when
+ * corrupt), backbone + dim (NGDB_ERR_CONFIG: BackboneMismatch), config_hash
+ * unless 0 (NGDB_ERR_CONFIG), tensor names/shapes (NGDB_ERR_SHAPE_MISMATCH). */
+int ngdb_checkpoint_save(ngdb_ctx* ctx, const char* path, uint64_t config_hash, int64_t step);
+int ngdb_checkpoint_load(ngdb_ctx* ctx, const char* path, uint64_t config_hash, int64_t* step);
+
 /* Evaluator hot path (SPEC.md:602-646 `evaluator`: filtered_rank over all
  * entities, mean-rank ties; replaces the per-query full-entity scoring loop of
  * evaluate()). queries [n_queries][wq] (GQE: q; Q2B: centre |

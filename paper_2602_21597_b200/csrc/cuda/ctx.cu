@@ -1,3 +1,4 @@
+#include <cstdio>
 // Device context and the C ABI of include/ngdb/ngdb_cuda.h.
 //
 // The context owns all device memory for one training run on one GPU:
@@ -1461,6 +1462,133 @@ int ngdb_graph_stats(ngdb_ctx* c, int64_t* updates, int64_t* instantiations) {
   return guarded([&] {
     if (updates) *updates = c->exec_updates;
     if (instantiations) *instantiations = c->exec_instantiations;
+  });
+}
+
+// ---- checkpoint ("versioned binary blob of named parameter
+// tensors + config hash"; cadence SPEC.md:587) --------------------------------
+// Layout, little-endian: "NGCK", u32 version = 1, u64 config hash, i64 step,
+// i32 backbone, i32 dim, u32 tensor count; per tensor (registry order): u32 name
+// length, name, i64 rows, i64 cols, then theta, Adam m, Adam v as rows*cols f32
+// each; trailer: u64 FNV-1a of every preceding byte. The Adam moments and the
+// step make a resumed run bit-identical to an uninterrupted one.
+namespace {
+constexpr uint32_t kCkptVersion = 1;
+struct Fnv {
+  uint64_t h = 1469598103934665603ull;
+  void add(const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  }
+};
+}  // namespace
+
+int ngdb_checkpoint_save(ngdb_ctx* c, const char* path, uint64_t config_hash, int64_t step) {
+  return guarded([&] {
+    if (!path) throw Fail{NGDB_ERR_CONFIG, "checkpoint: null path"};
+    std::vector<char> blob;
+    auto put = [&](const void* p, size_t n) {
+      const char* b = static_cast<const char*>(p);
+      blob.insert(blob.end(), b, b + n);
+    };
+    const uint32_t ver = kCkptVersion, nt = static_cast<uint32_t>(c->params.size());
+    const int32_t bb = c->desc.backbone, dim = c->desc.dim;
+    put("NGCK", 4);
+    put(&ver, 4);
+    put(&config_hash, 8);
+    put(&step, 8);
+    put(&bb, 4);
+    put(&dim, 4);
+    put(&nt, 4);
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<float> host;
+    for (const auto& p : c->params) {
+      const uint32_t len = static_cast<uint32_t>(p.name.size());
+      put(&len, 4);
+      put(p.name.data(), len);
+      put(&p.rows, 8);
+      put(&p.cols, 8);
+      host.resize(p.n());
+      for (const float* src : {p.w, p.m, p.v}) {
+        CK(cudaMemcpy(host.data(), src, p.n() * sizeof(float), cudaMemcpyDeviceToHost));
+        put(host.data(), p.n() * sizeof(float));
+      }
+    }
+    Fnv f;
+    f.add(blob.data(), blob.size());
+    put(&f.h, 8);
+    FILE* fp = std::fopen(path, "wb");
+    if (!fp) throw Fail{NGDB_ERR_CONFIG, std::string("checkpoint: cannot write ") + path};
+    const size_t wrote = std::fwrite(blob.data(), 1, blob.size(), fp);
+    const bool ok = std::fclose(fp) == 0 && wrote == blob.size();
+    if (!ok) throw Fail{NGDB_ERR_CONFIG, std::string("checkpoint: short write to ") + path};
+  });
+}
+
+int ngdb_checkpoint_load(ngdb_ctx* c, const char* path, uint64_t config_hash, int64_t* step) {
+  return guarded([&] {
+    if (!path) throw Fail{NGDB_ERR_CONFIG, "checkpoint: null path"};
+    FILE* fp = std::fopen(path, "rb");
+    if (!fp) throw Fail{NGDB_ERR_CONFIG, std::string("checkpoint: cannot read ") + path};
+    std::vector<char> blob;
+    char buf[1 << 16];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof(buf), fp)) > 0) blob.insert(blob.end(), buf, buf + got);
+    std::fclose(fp);
+    if (blob.size() < 44 || std::memcmp(blob.data(), "NGCK", 4) != 0)
+      throw Fail{NGDB_ERR_DOMAIN, "checkpoint: not an NGCK blob"};
+    uint64_t stored;
+    std::memcpy(&stored, blob.data() + blob.size() - 8, 8);
+    Fnv f;
+    f.add(blob.data(), blob.size() - 8);
+    if (f.h != stored) throw Fail{NGDB_ERR_DOMAIN, "checkpoint: checksum mismatch (corrupt file)"};
+    size_t at = 4;
+    auto get = [&](void* p, size_t n) {
+      if (at + n > blob.size() - 8) throw Fail{NGDB_ERR_DOMAIN, "checkpoint: truncated"};
+      std::memcpy(p, blob.data() + at, n);
+      at += n;
+    };
+    uint32_t ver, nt;
+    uint64_t hash;
+    int64_t st;
+    int32_t bb, dim;
+    get(&ver, 4);
+    get(&hash, 8);
+    get(&st, 8);
+    get(&bb, 4);
+    get(&dim, 4);
+    get(&nt, 4);
+    if (ver != kCkptVersion) throw Fail{NGDB_ERR_CONFIG, "checkpoint: unsupported version"};
+    if (bb != c->desc.backbone || dim != c->desc.dim)
+      throw Fail{NGDB_ERR_CONFIG, "checkpoint: BackboneMismatch (backbone / dim differ from the context)"};
+    if (config_hash && hash != config_hash) throw Fail{NGDB_ERR_CONFIG, "checkpoint: config hash mismatch"};
+    if (nt != c->params.size()) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "checkpoint: tensor count"};
+    std::vector<std::pair<const char*, Param*>> plan;
+    for (auto& p : c->params) {
+      uint32_t len;
+      get(&len, 4);
+      std::string name(len, '\0');
+      get(name.data(), len);
+      int64_t rows, cols;
+      get(&rows, 8);
+      get(&cols, 8);
+      if (name != p.name || rows != p.rows || cols != p.cols)
+        throw Fail{NGDB_ERR_SHAPE_MISMATCH, "checkpoint: tensor " + name + " does not match " + p.name};
+      if (at + 3 * p.n() * sizeof(float) > blob.size() - 8) throw Fail{NGDB_ERR_DOMAIN, "checkpoint: truncated"};
+      plan.emplace_back(blob.data() + at, &p);
+      at += 3 * p.n() * sizeof(float);
+    }
+    if (at != blob.size() - 8) throw Fail{NGDB_ERR_DOMAIN, "checkpoint: trailing bytes"};
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto& [src, p] : plan) {
+      const size_t nb = p->n() * sizeof(float);
+      CK(cudaMemcpy(p->w, src, nb, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(p->m, src + nb, nb, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(p->v, src + 2 * nb, nb, cudaMemcpyHostToDevice));
+    }
+    refresh_weight_splits(c);
+    CK(cudaStreamSynchronize(c->stream));
+    if (step) *step = st;
   });
 }
 

@@ -337,6 +337,17 @@ class Engine:
                              "submit_pools_s": timings[4], "submit_optimizer_s": timings[5]}
         return (sums, pq) if per_query else sums
 
+    def save_checkpoint(self, path: str, config_hash: int = 0) -> None:
+        """Parameters, Adam moments and the step counter as an NGCK blob."""
+        check(lib.ngdb_checkpoint_save(self._h, str(path).encode(), config_hash, self.step_count))
+
+    def load_checkpoint(self, path: str, config_hash: int = 0) -> int:
+        """Restore a blob written by save_checkpoint; resumes the step counter."""
+        st = C.c_int64()
+        check(lib.ngdb_checkpoint_load(self._h, str(path).encode(), config_hash, C.byref(st)))
+        self.step_count = st.value
+        return st.value
+
     def eval_ranks(self, queries: np.ndarray, targets: Sequence[int],
                    filters: Sequence[Sequence[int]]) -> np.ndarray:
         """Filtered ranks of `targets` among all entities (SPEC.md:614-618,

@@ -1,0 +1,62 @@
+"""Checkpoint blob (resume determinism SPEC.md:576, 755): saving
+theta + Adam moments + step and resuming reproduces the uninterrupted run
+bit for bit; corrupt / mismatched blobs fail with the SPEC's error kinds."""
+import numpy as np
+import pytest
+
+import paper_2602_21597_b200 as m
+from paper_2602_21597_b200._native import NgdbError
+
+pytestmark = pytest.mark.gpu
+
+ALL = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni", "inp"]
+
+
+def _names(backbone, info, dim):
+    return [s[0] for s in m.param_specs(backbone, info["n_entities"], info["n_relations"], dim)]
+
+
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
+def test_resume_is_bit_identical(small_graph, tmp_path, backbone):
+    info = small_graph.info()
+    dim = 32
+    w = m.pattern_weights(ALL)
+    steps = [m.PlannedStep(m.Batch.sample(small_graph, w, 64, 8, seed=3, tag=t), backbone, dim)
+             for t in range(3)]
+    a = m.Engine(backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=8,
+                 max_queries=64)
+    a.run_step(steps[0], 64)
+    a.run_step(steps[1], 64)
+    path = tmp_path / "ck.ngck"
+    a.save_checkpoint(path, config_hash=0xC0FFEE)
+    la = a.run_step(steps[2], 64)
+    b = m.Engine(backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=8,
+                 max_queries=64, seed=99)  # different init: everything comes from the blob
+    assert b.load_checkpoint(path, config_hash=0xC0FFEE) == 2
+    lb = b.run_step(steps[2], 64)
+    np.testing.assert_array_equal(la, lb)
+    for n in _names(backbone, info, dim):
+        for pre in ("", "m:", "v:"):
+            np.testing.assert_array_equal(a.download(pre + n), b.download(pre + n))
+
+
+def test_checkpoint_errors(small_graph, tmp_path):
+    info = small_graph.info()
+    a = m.Engine("gqe", info["n_entities"], info["n_relations"], dim=16, n_neg=4, max_queries=8)
+    path = tmp_path / "ck.ngck"
+    a.save_checkpoint(path, config_hash=7)
+    with pytest.raises(NgdbError) as e:
+        a.load_checkpoint(path, config_hash=8)
+    assert e.value.kind == "ConfigError"
+    q = m.Engine("q2b", info["n_entities"], info["n_relations"], dim=16, n_neg=4, max_queries=8)
+    with pytest.raises(NgdbError) as e:  # BackboneMismatch
+        q.load_checkpoint(path)
+    assert e.value.kind == "ConfigError"
+    raw = bytearray(path.read_bytes())
+    raw[100] ^= 0xFF
+    bad = tmp_path / "bad.ngck"
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(NgdbError) as e:
+        a.load_checkpoint(bad)
+    assert e.value.kind == "DomainError"
+    assert a.load_checkpoint(path) == 0  # hash 0: not checked
