@@ -255,7 +255,9 @@ def reference_arm(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{backbone} {shape}-shaped synthetic KG, {mix} mix"
                                + (" + PTE fusion" if SEMANTIC_DIM.get(args.config) else ""),
-                   "global_batch": batch, "n_neg": n_neg, "dim": dim},
+                   # our arm's config at this N (N replicas of 512-query steps); the host
+                   # runs 512-query steps on every worker process
+                   "global_batch": batch * max(1, args.gpus), "n_neg": n_neg, "dim": dim},
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": workers, "kind": "port",
                          "sample": f"{done} full {batch}-query steps (oracle sampler + step, f32) "
                                    f"on {workers} host processes in parallel, {el:.1f}s; the "
