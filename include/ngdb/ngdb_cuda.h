@@ -284,6 +284,10 @@ int ngdb_checkpoint_load(ngdb_ctx* ctx, const char* path, uint64_t config_hash, 
  * (SPEC TargetFiltered). */
 int ngdb_eval_ranks(ngdb_ctx* ctx, const float* queries, int32_t n_queries, const int32_t* targets,
                     const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks);
+/* Diagnostics: with NGDB_STEP_TIMELINE=1 in the environment, graph-launched
+ * steps record device timestamps; returns the summed device time of the steps
+ * and the summed idle gaps between them, then clears the record. */
+int ngdb_step_timeline(ngdb_ctx* ctx, double* busy_ms, double* gap_ms, int64_t* n_steps);
 int ngdb_transfer_bytes(ngdb_ctx* ctx, int64_t* h2d, int64_t* d2h);
 /* ngdb_step_launch graphs: launches served by updating a cached executable
  * graph of the same invocation structure vs fresh instantiations. */
