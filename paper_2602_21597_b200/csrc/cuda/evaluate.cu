@@ -92,17 +92,24 @@ __global__ void __launch_bounds__(256) eval_count_kernel(EvalArgs a) {
 #pragma unroll
   for (int j = 0; j < QPT; ++j) out[j] = in[j] = 0.f;
   for (int k0 = 0; k0 < a.dim; k0 += KS) {
-    // stage the slice: 64 entity rows x 32 dims, 32 queries x 32 dims (zero padded)
-    for (int i = tid; i < TE * KS; i += 256) {
-      const int r = i / KS, k = i % KS, e = e0 + r;
-      es[r][k] = (e < a.n_ent && k0 + k < a.dim) ? a.ent[static_cast<int64_t>(e) * a.ent_w + k0 + k] : 0.f;
+    // stage the slice: 64 entity rows x 32 dims, 32 queries x 32 dims, as float4
+    // pieces (d is a multiple of 4: a piece is wholly inside or zero padding)
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = tid; i < TE * KS / 4; i += 256) {
+      const int r = i / (KS / 4), k = 4 * (i % (KS / 4)), e = e0 + r;
+      *reinterpret_cast<float4*>(&es[r][k]) =
+          (e < a.n_ent && k0 + k < a.dim)
+              ? __ldg(reinterpret_cast<const float4*>(a.ent + static_cast<int64_t>(e) * a.ent_w + k0 + k))
+              : z4;
     }
-    for (int i = tid; i < TQ * KS; i += 256) {
-      const int r = i / KS, k = i % KS, q = q0 + r;
+    for (int i = tid; i < TQ * KS / 4; i += 256) {
+      const int r = i / (KS / 4), k = 4 * (i % (KS / 4)), q = q0 + r;
       const bool ok = q < a.nq && k0 + k < a.dim;
-      const float* qr = a.q + static_cast<int64_t>(q) * a.wq;
-      qcs[r][k] = ok ? qr[k0 + k] : 0.f;
-      if constexpr (BB != NGDB_GQE) qos[r][k] = ok ? qr[a.dim + k0 + k] : 0.f;
+      const float* qr = a.q + static_cast<int64_t>(q) * a.wq + k0 + k;
+      *reinterpret_cast<float4*>(&qcs[r][k]) = ok ? __ldg(reinterpret_cast<const float4*>(qr)) : z4;
+      if constexpr (BB != NGDB_GQE)
+        *reinterpret_cast<float4*>(&qos[r][k]) =
+            ok ? __ldg(reinterpret_cast<const float4*>(qr + a.dim)) : z4;
     }
     __syncthreads();
 #pragma unroll 2
