@@ -234,6 +234,68 @@ def oracle_throughput(args_cfg, graph, workers, warmup, steps_total, budget=None
     return q / el, workers, q // batch, el
 
 
+QL_STEPS = 20
+
+
+def executor_comparison(m, lib, check, ctx, batches, backbone, dim, batch, sdim, step_no):
+    """Device time per step of the same batches planned by Max-Fillness
+    (operator-level) and by the query-level baseline executor,
+    each step a resident plan replayed as a CUDA graph on this context."""
+    import ctypes as C
+    out = {}
+    bs = batches[:QL_STEPS]
+    for ql in (False, True):
+        steps = [m.PlannedStep(b, backbone, dim, 512, semantic=bool(sdim), query_level=ql)
+                 for b in bs]
+        inv = sum(s.trace()["invocations"] for s in steps) / len(steps)
+        plans = []
+        for s in steps:
+            v = s.view()
+            h = C.c_void_p()
+            check(lib.ngdb_plan_create(ctx, C.byref(v), C.byref(h)))
+            check(lib.ngdb_plan_prepare(ctx, h))
+            plans.append(h)
+        step_no += 1
+        check(lib.ngdb_plan_run(ctx, plans[0], step_no))  # warm the graph path
+        check(lib.ngdb_sync(ctx))
+        ms = C.c_float()
+        check(lib.ngdb_timer_start(ctx))
+        for h in plans:
+            step_no += 1
+            check(lib.ngdb_plan_run(ctx, h, step_no))
+        check(lib.ngdb_timer_stop(ctx, C.byref(ms)))
+        for h in plans:
+            check(lib.ngdb_plan_destroy(h))
+        out["query_level" if ql else "operator_level"] = {
+            "queries_per_s": batch * len(plans) / (ms.value / 1e3),
+            "ms_per_step": ms.value / len(plans), "invocations_per_step": inv}
+    out["operator_over_query_level"] = (out["operator_level"]["queries_per_s"] /
+                                        out["query_level"]["queries_per_s"])
+    out["steps"] = len(bs)
+    return out
+
+
+def evaluator_measure(eng, info, dim, backbone, nq=512, reps=5):
+    """ngdb_eval_ranks: nq random query embeddings ranked against every entity
+    of the trained table (filters of 100 entities), end to end per call."""
+    rng = np.random.default_rng(1)
+    n_ent = info["n_entities"]
+    wq = dim if backbone == "gqe" else 2 * dim
+    q = rng.uniform(-0.035, 0.035, size=(nq, wq)).astype(np.float32)
+    q[:, dim:] = np.abs(q[:, dim:])
+    t = rng.integers(0, n_ent, size=nq).astype(np.int32)
+    ids = rng.integers(0, n_ent, size=(nq, 100)).astype(np.int32)
+    ids[ids == t[:, None]] = (ids[ids == t[:, None]] + 1) % n_ent
+    off = np.arange(0, 100 * nq + 1, 100, dtype=np.int32)
+    eng.eval_ranks_csr(q, t, off, ids.ravel())
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        eng.eval_ranks_csr(q, t, off, ids.ravel())
+    dt = (time.perf_counter() - t0) / reps
+    return {"queries_per_s": nq / dt, "ms_per_call": dt * 1e3, "queries_per_call": nq,
+            "entities": n_ent, "api": "ngdb_eval_ranks (host queries/targets/filters, ranks back)"}
+
+
 def host_workers():
     return max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
                else (os.cpu_count() or 1))
@@ -414,6 +476,8 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--producers", type=int, default=0, help="e2e host producer threads (0: cores-1)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the query-level executor and evaluator side measurements")
     ap.add_argument("--in-flight", type=int, default=0,
                     help="e2e steps on the device before the oldest one's losses are read (0: 2)")
     args = ap.parse_args()
@@ -584,6 +648,24 @@ def main():
                                   losses.ctypes.data_as(C.POINTER(C.c_float)), C.byref(total)))
     seq_qps = batch * n_seq / (time.perf_counter() - t0)
 
+    # ---- side measurements: operator-level vs the query-level
+    # baseline executor on the same kernels and batches, and the evaluator's
+    # full-entity filtered ranking. Reported beside the headline; a failure
+    # here is recorded in the line instead of aborting it.
+    extras = {}
+    if not args.no_extras:
+        try:
+            extras["query_level"] = executor_comparison(m, lib, check, ctx, batches[args.warmup:],
+                                                        backbone, dim, batch, sdim, step_no)
+            step_no += 2 * len(batches[args.warmup:][:QL_STEPS]) + 2
+        except Exception as exc:  # noqa: BLE001
+            extras["query_level"] = {"error": repr(exc)}
+        if backbone in ("gqe", "q2b") and not sdim:
+            try:
+                extras["evaluator"] = evaluator_measure(eng, info, dim, backbone)
+            except Exception as exc:  # noqa: BLE001
+                extras["evaluator"] = {"error": repr(exc)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = host_workers()
@@ -629,6 +711,7 @@ def main():
             "families": fams if not args.quiet else None,
             "setup_s": setup_s,
         }
+        line.update(extras)
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
