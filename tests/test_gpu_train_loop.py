@@ -80,3 +80,20 @@ def test_loop_errors_surface(small_graph):
     # a failed run leaves the context usable
     sums = eng.train(small_graph, w, 2, batch=b, n_neg=k)
     assert np.all(np.isfinite(sums))
+
+
+@pytest.mark.parametrize("in_flight,graphs", [(1, True), (3, True), (2, False)])
+def test_loop_depth_and_launch_mode(small_graph, in_flight, graphs):
+    # ngdb_train_opts.in_flight / NGDB_TRAIN_NO_GRAPHS change only how far the
+    # host runs ahead and how steps are launched: results stay bit-identical
+    b, k, dim, steps = 96, 8, 32, 4
+    w = m.pattern_weights(ALL)
+    base = _engine(small_graph, "q2b", dim, k, b)
+    ref = base.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=21,
+                     n_producers=2, per_query=True)[1]
+    eng = _engine(small_graph, "q2b", dim, k, b)
+    pq = eng.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=21, n_producers=2,
+                   per_query=True, in_flight=in_flight, graphs=graphs)[1]
+    np.testing.assert_array_equal(pq, ref)
+    for name in ("entity", "relation"):
+        np.testing.assert_array_equal(eng.download(name), base.download(name))
