@@ -273,6 +273,12 @@ int64_t ngdb_launch_count(ngdb_ctx* ctx);
 int ngdb_checkpoint_save(ngdb_ctx* ctx, const char* path, uint64_t config_hash, int64_t step);
 int ngdb_checkpoint_load(ngdb_ctx* ctx, const char* path, uint64_t config_hash, int64_t* step);
 
+/* Query embeddings of the last executed step's score slots (each query's Loss
+ * slot, or its union branches' Score slots; ngdb_node_desc.aux), [n_slots][wq],
+ * copied back synchronously. With the forward pools of a plan executed alone
+ * (no backward, no optimizer) this is the evaluator's query encoder. */
+int ngdb_read_score_queries(ngdb_ctx* ctx, float* host, int64_t n_slots);
+
 /* Evaluator hot path (SPEC.md:602-646 `evaluator`: filtered_rank over all
  * entities, mean-rank ties; replaces the per-query full-entity scoring loop of
  * evaluate()). queries [n_queries][wq] (GQE: q; Q2B: centre |

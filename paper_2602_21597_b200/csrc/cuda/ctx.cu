@@ -1630,6 +1630,18 @@ int ngdb_checkpoint_load(ngdb_ctx* c, const char* path, uint64_t config_hash, in
   });
 }
 
+int ngdb_read_score_queries(ngdb_ctx* c, float* host, int64_t n_slots) {
+  return guarded([&] {
+    if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "read_score_queries: row-sharded context"};
+    if (n_slots <= 0) return;
+    if (!c->qbuf || n_slots > c->cap_score)
+      throw Fail{NGDB_ERR_SHAPE_MISMATCH, "read_score_queries: more slots than the last step had"};
+    CK(cudaMemcpyAsync(host, c->qbuf, n_slots * c->query_width() * sizeof(float),
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const int32_t* targets,
                     const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks) {
   return guarded([&] {

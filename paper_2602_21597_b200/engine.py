@@ -348,6 +348,35 @@ class Engine:
         self.step_count = st.value
         return st.value
 
+    def query_embeddings(self, step: "PlannedStep"):
+        """Forward pools of a planned batch only (no backward, no optimizer:
+        parameters unchanged) -> {query index: [n_branches][wq]} embeddings read
+        from the score slots (SPEC.md:620-622 `evaluate`: score with the
+        backbone's distance). Union queries have one row per DNF branch.
+        Returns (embeddings, per-query forward losses)."""
+        v = step.view()
+        check(lib.ngdb_step_begin(self._h, C.byref(v)))
+        for i in range(v.n_pools):
+            if v.pools[i].dir == 0:
+                check(lib.ngdb_exec_pool(self._h, C.byref(v.pools[i])))
+        losses = np.zeros(v.n_queries, dtype=np.float32)
+        total, bad = C.c_double(), C.c_int32()
+        check(lib.ngdb_step_end(self._h, _p(losses, C.c_float), v.n_queries, C.byref(total),
+                                C.byref(bad)))
+        wq = self.dim if self.backbone == "gqe" else 2 * self.dim
+        emb = np.zeros((max(v.n_score_slots, 1), wq), dtype=np.float32)
+        check(lib.ngdb_read_score_queries(self._h, _p(emb, C.c_float), v.n_score_slots))
+        slots: Dict[int, List[int]] = {}
+        for i in range(v.n_pools):
+            p = v.pools[i]
+            if p.dir != 0 or p.kind not in (OP_KINDS.index("Score"), OP_KINDS.index("Loss")):
+                continue
+            for j in range(p.first, p.first + p.count):
+                nd = v.nodes[j]
+                if nd.aux >= 0:
+                    slots.setdefault(int(nd.id), []).append(int(nd.aux))
+        return {q: emb[sorted(ss)] for q, ss in slots.items()}, losses
+
     def eval_ranks(self, queries: np.ndarray, targets: Sequence[int],
                    filters: Sequence[Sequence[int]]) -> np.ndarray:
         """Filtered ranks of `targets` among all entities (SPEC.md:614-618,
