@@ -290,6 +290,13 @@ int ngdb_read_score_queries(ngdb_ctx* ctx, float* host, int64_t n_slots);
  * (SPEC TargetFiltered). */
 int ngdb_eval_ranks(ngdb_ctx* ctx, const float* queries, int32_t n_queries, const int32_t* targets,
                     const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks);
+/* The same for queries with several embeddings (union patterns: one per DNF
+ * branch): query q's branches are units[unit_offsets[q] ..
+ * unit_offsets[q+1]) (1..8), an entity's distance is the nearest branch's
+ * (UnionScore = max score). */
+int ngdb_eval_ranks_multi(ngdb_ctx* ctx, const float* units, int32_t n_queries,
+                          const int32_t* unit_offsets, const int32_t* targets,
+                          const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks);
 /* Diagnostics: with NGDB_STEP_TIMELINE=1 in the environment, graph-launched
  * steps record device timestamps; returns the summed device time of the steps
  * and the summed idle gaps between them, then clears the record. */

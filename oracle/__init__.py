@@ -264,3 +264,13 @@ def eval_distances(backbone, ent, q, dim, alpha=0.02):
 def eval_ranks(backbone, ent, queries, targets, filters, dim, alpha=0.02):
     return np.array([filtered_rank(-eval_distances(backbone, ent, q, dim, alpha), t, f)
                      for q, t, f in zip(queries, targets, filters)], dtype=np.int64)
+
+
+def eval_ranks_multi(backbone, ent, embeddings, targets, filters, dim, alpha=0.02):
+    """Union queries: an entity's distance is the nearest branch's."""
+    out = []
+    for e, t, f in zip(embeddings, targets, filters):
+        d = np.min(np.stack([eval_distances(backbone, ent, b, dim, alpha)
+                             for b in np.atleast_2d(e)]), axis=0)
+        out.append(filtered_rank(-d, t, f))
+    return np.array(out, dtype=np.int64)

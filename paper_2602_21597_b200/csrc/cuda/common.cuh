@@ -247,14 +247,18 @@ struct EvalArgs {
   int64_t ent_w;
   int32_t n_ent, dim, backbone;
   float alpha;       // Q2B inside weight
-  const float* q;    // [nq][wq]: GQE q; Q2B centre | offset
-  int32_t wq, nq;
-  const int32_t* target;
-  const int32_t* f_off;  // [nq + 1] CSR of filter entities
+  const float* q;    // [nq][wq] query slots: GQE q; Q2B centre | offset
+  int32_t wq, nq;    // nq = slots (a union query has one slot per DNF branch)
+  int32_t n_queries;
+  const int32_t* slot_query;  // [nq] query of the slot, -1 = padding
+  const int32_t* slot_nb;     // [nq] branches starting at this slot (its query's first), else 0
+  const int32_t* first_slot;  // [n_queries]
+  const int32_t* target;      // per query
+  const int32_t* f_off;  // [n_queries + 1] CSR of filter entities
   const int32_t* f_ids;
-  float* dt;             // [nq] target distances
-  int32_t* better;       // [nq]
-  int32_t* ties;         // [nq]
+  float* dt;             // [n_queries] target distances (nearest branch)
+  int32_t* better;       // [n_queries]
+  int32_t* ties;         // [n_queries]
 };
 int launch_eval_ranks(const EvalArgs& a, int32_t n_filter, cudaStream_t s);
 

@@ -1642,10 +1642,12 @@ int ngdb_read_score_queries(ngdb_ctx* c, float* host, int64_t n_slots) {
   });
 }
 
-int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const int32_t* targets,
-                    const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks) {
+int ngdb_eval_ranks_multi(ngdb_ctx* c, const float* units, int32_t n_queries,
+                          const int32_t* unit_offsets, const int32_t* targets,
+                          const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks) {
   return guarded([&] {
-    if (n_queries < 0 || (n_queries > 0 && (!queries || !targets || !filter_offsets || !ranks)))
+    if (n_queries < 0 || (n_queries > 0 && (!units || !unit_offsets || !targets ||
+                                            !filter_offsets || !ranks)))
       throw Fail{NGDB_ERR_CONFIG, "eval_ranks: null argument"};
     if (c->desc.backbone == NGDB_BETAE || c->fused())
       throw Fail{NGDB_ERR_MISSING_KERNEL, "eval_ranks: GQE and Q2B backbones only"};
@@ -1653,7 +1655,34 @@ int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const 
     if (n_queries == 0) return;
     const Param& ent = c->params[c->ent_idx];
     const int32_t n_ent = c->desc.n_entities, wq = c->query_width();
-    if (filter_offsets[0] != 0) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "eval_ranks: filter_offsets[0] != 0"};
+    if (filter_offsets[0] != 0 || unit_offsets[0] != 0)
+      throw Fail{NGDB_ERR_SHAPE_MISMATCH, "eval_ranks: offsets[0] != 0"};
+    // slots: a query's branch units packed inside one aligned group of 8 (the
+    // count kernel takes the nearest branch over a thread's 8 slots)
+    constexpr int kGroup = 8;
+    std::vector<int32_t> slot_query, slot_nb, first(n_queries);
+    std::vector<int32_t> slot_unit;
+    for (int32_t q = 0; q < n_queries; ++q) {
+      const int32_t nb = unit_offsets[q + 1] - unit_offsets[q];
+      if (nb < 1 || nb > kGroup) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "eval_ranks: 1..8 branches per query"};
+      if (static_cast<int>(slot_query.size() % kGroup) + nb > kGroup)
+        while (slot_query.size() % kGroup) {
+          slot_query.push_back(-1);
+          slot_nb.push_back(0);
+          slot_unit.push_back(-1);
+        }
+      first[q] = static_cast<int32_t>(slot_query.size());
+      for (int32_t b = 0; b < nb; ++b) {
+        slot_query.push_back(q);
+        slot_nb.push_back(b == 0 ? nb : 0);
+        slot_unit.push_back(unit_offsets[q] + b);
+      }
+    }
+    const int64_t ns = static_cast<int64_t>(slot_query.size());
+    std::vector<float> packed(ns * wq, 0.f);
+    for (int64_t i = 0; i < ns; ++i)
+      if (slot_unit[i] >= 0)
+        std::memcpy(&packed[i * wq], units + static_cast<int64_t>(slot_unit[i]) * wq, wq * 4);
     // filter sets: validated, sorted and de-duplicated per query (they are sets)
     std::vector<int32_t> off(n_queries + 1, 0), ids;
     ids.reserve(filter_offsets[n_queries] > 0 ? filter_offsets[n_queries] : 0);
@@ -1662,22 +1691,22 @@ int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const 
       if (t < 0 || t >= n_ent) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "eval_ranks: target out of range"};
       const int32_t b = filter_offsets[q], e = filter_offsets[q + 1];
       if (e < b) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "eval_ranks: filter_offsets not ascending"};
-      const size_t first = ids.size();
+      const size_t first_id = ids.size();
       for (int32_t i = b; i < e; ++i) {
         const int32_t f = filter_ids[i];
         if (f < 0 || f >= n_ent) throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "eval_ranks: filter id out of range"};
         if (f == t) throw Fail{NGDB_ERR_DOMAIN, "eval_ranks: TargetFiltered (target in its filter set)"};
         ids.push_back(f);
       }
-      if (!std::is_sorted(ids.begin() + first, ids.end())) std::sort(ids.begin() + first, ids.end());
-      ids.erase(std::unique(ids.begin() + first, ids.end()), ids.end());
+      if (!std::is_sorted(ids.begin() + first_id, ids.end())) std::sort(ids.begin() + first_id, ids.end());
+      ids.erase(std::unique(ids.begin() + first_id, ids.end()), ids.end());
       off[q + 1] = static_cast<int32_t>(ids.size());
     }
     const int64_t nq = n_queries, nf = static_cast<int64_t>(ids.size());
     auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
-    const int64_t b_q = al(nq * wq * 4), b_t = al(nq * 4), b_off = al((nq + 1) * 4),
+    const int64_t b_q = al(ns * wq * 4), b_s = al(ns * 4), b_t = al(nq * 4), b_off = al((nq + 1) * 4),
                   b_ids = al(std::max<int64_t>(nf, 1) * 4);
-    const int64_t need = b_q + b_off + b_ids + 4 * b_t;
+    const int64_t need = b_q + 2 * b_s + b_off + b_ids + 5 * b_t;
     if (need > c->eval_cap) {
       CK(cudaStreamSynchronize(c->stream));
       if (c->eval_buf) CK(cudaFree(c->eval_buf));
@@ -1693,23 +1722,33 @@ int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const 
     a.backbone = c->desc.backbone;
     a.alpha = c->desc.alpha_box;
     a.wq = wq;
-    a.nq = n_queries;
-    float* dq = reinterpret_cast<float*>(p);            p += b_q;
-    int32_t* dtg = reinterpret_cast<int32_t*>(p);       p += b_t;
-    int32_t* doff = reinterpret_cast<int32_t*>(p);      p += b_off;
-    int32_t* dids = reinterpret_cast<int32_t*>(p);      p += b_ids;
-    a.dt = reinterpret_cast<float*>(p);                 p += b_t;
-    a.better = reinterpret_cast<int32_t*>(p);           p += b_t;
+    a.nq = static_cast<int32_t>(ns);
+    a.n_queries = n_queries;
+    float* dq = reinterpret_cast<float*>(p);        p += b_q;
+    int32_t* dsq = reinterpret_cast<int32_t*>(p);   p += b_s;
+    int32_t* dsn = reinterpret_cast<int32_t*>(p);   p += b_s;
+    int32_t* dfs = reinterpret_cast<int32_t*>(p);   p += b_t;
+    int32_t* dtg = reinterpret_cast<int32_t*>(p);   p += b_t;
+    int32_t* doff = reinterpret_cast<int32_t*>(p);  p += b_off;
+    int32_t* dids = reinterpret_cast<int32_t*>(p);  p += b_ids;
+    a.dt = reinterpret_cast<float*>(p);             p += b_t;
+    a.better = reinterpret_cast<int32_t*>(p);       p += b_t;
     a.ties = reinterpret_cast<int32_t*>(p);
     a.q = dq;
+    a.slot_query = dsq;
+    a.slot_nb = dsn;
+    a.first_slot = dfs;
     a.target = dtg;
     a.f_off = doff;
     a.f_ids = dids;
-    CK(cudaMemcpyAsync(dq, queries, nq * wq * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dq, packed.data(), ns * wq * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dsq, slot_query.data(), ns * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dsn, slot_nb.data(), ns * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dfs, first.data(), nq * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dtg, targets, nq * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(doff, off.data(), (nq + 1) * 4, cudaMemcpyHostToDevice, c->stream));
     if (nf) CK(cudaMemcpyAsync(dids, ids.data(), nf * 4, cudaMemcpyHostToDevice, c->stream));
-    c->h2d_bytes += nq * wq * 4 + nq * 4 + (nq + 1) * 4 + nf * 4;
+    c->h2d_bytes += ns * wq * 4 + 2 * ns * 4 + 2 * nq * 4 + (nq + 1) * 4 + nf * 4;
     c->launches += launch_eval_ranks(a, static_cast<int32_t>(nf), c->stream);
     CK(cudaGetLastError());
     std::vector<int32_t> cnt(2 * nq);
@@ -1719,6 +1758,16 @@ int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const 
     CK(cudaStreamSynchronize(c->stream));
     for (int64_t q = 0; q < nq; ++q) ranks[q] = 1 + cnt[q] + cnt[nq + q] / 2;
   });
+}
+
+int ngdb_eval_ranks(ngdb_ctx* c, const float* queries, int32_t n_queries, const int32_t* targets,
+                    const int32_t* filter_offsets, const int32_t* filter_ids, int32_t* ranks) {
+  if (n_queries < 0) return ngdb_eval_ranks_multi(c, queries, n_queries, nullptr, targets,
+                                                  filter_offsets, filter_ids, ranks);
+  std::vector<int32_t> uo(static_cast<size_t>(n_queries) + 1);
+  for (int32_t i = 0; i <= n_queries; ++i) uo[i] = i;
+  return ngdb_eval_ranks_multi(c, queries, n_queries, uo.data(), targets, filter_offsets,
+                               filter_ids, ranks);
 }
 
 // Diagnostics of graph-launched steps recorded under NGDB_STEP_TIMELINE=1:

@@ -71,11 +71,21 @@ __device__ float row_distance(const EvalArgs& a, int e, int q) {
   return finish<BB>(out, in, a.alpha);
 }
 
+// distance of entity e to query qi: the nearest of its branch slots (UnionScore
+// takes the max score); one branch for every other pattern
+template <int BB>
+__device__ float query_distance(const EvalArgs& a, int e, int qi) {
+  const int s0 = a.first_slot[qi], nb = a.slot_nb[s0];
+  float d = row_distance<BB>(a, e, s0);
+  for (int b = 1; b < nb; ++b) d = fminf(d, row_distance<BB>(a, e, s0 + b));
+  return d;
+}
+
 template <int BB>
 __global__ void eval_target_kernel(EvalArgs a) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= a.nq) return;
-  a.dt[q] = row_distance<BB>(a, a.target[q], q);
+  if (q >= a.n_queries) return;
+  a.dt[q] = query_distance<BB>(a, a.target[q], q);
   a.better[q] = 0;
   a.ties[q] = 0;
 }
@@ -130,20 +140,30 @@ __global__ void __launch_bounds__(256) eval_count_kernel(EvalArgs a) {
     __syncthreads();
   }
   const int e = e0 + el;
+  // the host packs a query's branch slots inside one 8-slot group, so the
+  // nearest-branch distance is a min over this thread's own registers
+  float d[QPT];
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) d[j] = finish<BB>(out[j], in[j], a.alpha);
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
-    const int q = q0 + qg * QPT + j;
+    const int slot = q0 + qg * QPT + j;
+    const int nbr = slot < a.nq ? a.slot_nb[slot] : 0;  // > 0: first slot of a query
+    const int qi = nbr > 0 ? a.slot_query[slot] : -1;
+    float dm = d[j];
+    if (j + 1 < QPT && nbr > 1) dm = fminf(dm, d[j + 1 < QPT ? j + 1 : j]);
+    if (j + 2 < QPT && nbr > 2) dm = fminf(dm, d[j + 2 < QPT ? j + 2 : j]);
     bool b = false, t = false;
-    if (q < a.nq && e < a.n_ent && e != a.target[q]) {
-      const float d = finish<BB>(out[j], in[j], a.alpha), d_t = a.dt[q];
-      b = d < d_t;
-      t = d == d_t;
+    if (qi >= 0 && e < a.n_ent && e != a.target[qi]) {
+      const float d_t = a.dt[qi];
+      b = dm < d_t;
+      t = dm == d_t;
     }
     const unsigned nb = __popc(__ballot_sync(0xffffffffu, b));
     const unsigned nt = __popc(__ballot_sync(0xffffffffu, t));
-    if ((tid & 31) == 0 && q < a.nq) {
-      if (nb) atomicAdd(&a.better[q], static_cast<int32_t>(nb));
-      if (nt) atomicAdd(&a.ties[q], static_cast<int32_t>(nt));
+    if ((tid & 31) == 0 && qi >= 0) {
+      if (nb) atomicAdd(&a.better[qi], static_cast<int32_t>(nb));
+      if (nt) atomicAdd(&a.ties[qi], static_cast<int32_t>(nt));
     }
   }
 }
@@ -153,7 +173,7 @@ template <int BB>
 __global__ void eval_filter_kernel(EvalArgs a, int32_t n_filter) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_filter) return;
-  int lo = 0, hi = a.nq;  // query of entry i: last q with f_off[q] <= i
+  int lo = 0, hi = a.n_queries;  // query of entry i: last q with f_off[q] <= i
   while (hi - lo > 1) {
     const int mid = (lo + hi) / 2;
     if (a.f_off[mid] <= i) lo = mid;
@@ -161,14 +181,14 @@ __global__ void eval_filter_kernel(EvalArgs a, int32_t n_filter) {
   }
   const int q = lo, e = a.f_ids[i];
   if (e == a.target[q]) return;  // excluded by the host (TargetFiltered)
-  const float d = row_distance<BB>(a, e, q), d_t = a.dt[q];
+  const float d = query_distance<BB>(a, e, q), d_t = a.dt[q];
   if (d < d_t) atomicSub(&a.better[q], 1);
   else if (d == d_t) atomicSub(&a.ties[q], 1);
 }
 
 template <int BB>
 void launch_eval(const EvalArgs& a, int32_t n_filter, cudaStream_t s) {
-  eval_target_kernel<BB><<<(a.nq + 127) / 128, 128, 0, s>>>(a);
+  eval_target_kernel<BB><<<(a.n_queries + 127) / 128, 128, 0, s>>>(a);
   const dim3 grid((a.n_ent + TE - 1) / TE, (a.nq + TQ - 1) / TQ);
   eval_count_kernel<BB><<<grid, 256, 0, s>>>(a);
   if (n_filter > 0) eval_filter_kernel<BB><<<(n_filter + 127) / 128, 128, 0, s>>>(a, n_filter);
@@ -178,7 +198,7 @@ void launch_eval(const EvalArgs& a, int32_t n_filter, cudaStream_t s) {
 
 // 3 launches; the caller validated shapes and indices
 int launch_eval_ranks(const EvalArgs& a, int32_t n_filter, cudaStream_t s) {
-  if (a.nq <= 0) return 0;
+  if (a.n_queries <= 0) return 0;
   if (a.backbone == NGDB_GQE) launch_eval<NGDB_GQE>(a, n_filter, s);
   else launch_eval<NGDB_Q2B>(a, n_filter, s);
   return n_filter > 0 ? 3 : 2;

@@ -377,6 +377,29 @@ class Engine:
                     slots.setdefault(int(nd.id), []).append(int(nd.aux))
         return {q: emb[sorted(ss)] for q, ss in slots.items()}, losses
 
+    def eval_ranks_multi(self, embeddings: Sequence[np.ndarray], targets: Sequence[int],
+                         filters: Sequence[Sequence[int]]) -> np.ndarray:
+        """eval_ranks for queries given as [n_branches][wq] embeddings (union
+        patterns: one per DNF branch; an entity's distance is the nearest
+        branch's), e.g. the output of query_embeddings (ngdb_eval_ranks_multi)."""
+        n = len(targets)
+        units = np.ascontiguousarray(np.concatenate([np.atleast_2d(e) for e in embeddings])
+                                     if n else np.zeros((1, 1)), dtype=np.float32)
+        uo = np.zeros(n + 1, dtype=np.int32)
+        np.cumsum([np.atleast_2d(e).shape[0] for e in embeddings], out=uo[1:])
+        off = np.zeros(n + 1, dtype=np.int32)
+        np.cumsum(np.fromiter(map(len, filters), dtype=np.int64, count=n), out=off[1:])
+        ids = np.fromiter(itertools.chain.from_iterable(filters), dtype=np.int32,
+                          count=int(off[-1]))
+        if ids.size == 0:
+            ids = np.zeros(1, dtype=np.int32)
+        t = np.ascontiguousarray(targets, dtype=np.int32)
+        ranks = np.zeros(n, dtype=np.int32)
+        check(lib.ngdb_eval_ranks_multi(self._h, _p(units, C.c_float), n, _p(uo, C.c_int32),
+                                        _p(t, C.c_int32), _p(off, C.c_int32), _p(ids, C.c_int32),
+                                        _p(ranks, C.c_int32)))
+        return ranks
+
     def eval_ranks(self, queries: np.ndarray, targets: Sequence[int],
                    filters: Sequence[Sequence[int]]) -> np.ndarray:
         """Filtered ranks of `targets` among all entities (SPEC.md:614-618,

@@ -51,3 +51,36 @@ def test_forward_embeddings_reproduce_losses_and_rank(small_graph, backbone):
     f = [[int(x) for x in arr.negatives[q][:5] if x != arr.positives[q]] for q in qs]
     np.testing.assert_array_equal(eng.eval_ranks(qv, t, f),
                                   oracle.eval_ranks(backbone, ent0, qv, t, f, dim))
+
+
+@pytest.mark.parametrize("backbone", ["gqe", "q2b"])
+def test_union_queries_rank_by_nearest_branch(small_graph, backbone):
+    # the full 14-pattern evaluation path: forward embeddings (unions with two
+    # branches) -> ngdb_eval_ranks_multi, bit-exact against the oracle
+    info = small_graph.info()
+    dim, k, b = 32, 8, 80
+    bt = m.Batch.sample(small_graph, m.pattern_weights(m.PATTERNS), b, k, seed=3, tag=41)
+    arr = bt.arrays()
+    eng = m.Engine(backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=k,
+                   max_queries=b)
+    emb, _ = eng.query_embeddings(m.PlannedStep(bt, backbone, dim))
+    assert any(emb[q].shape[0] == 2 for q in range(b))  # unions present
+    embs = [emb[q] for q in range(b)]
+    t = arr.positives.astype(np.int32)
+    f = [[int(x) for x in arr.negatives[q][:4] if x != arr.positives[q]] for q in range(b)]
+    ent = eng.download("entity")
+    np.testing.assert_array_equal(eng.eval_ranks_multi(embs, t, f),
+                                  oracle.eval_ranks_multi(backbone, ent, embs, t, f, dim))
+    # synthetic branch counts 1..3 straddling the 8-slot groups
+    rng = np.random.default_rng(5)
+    wq = dim if backbone == "gqe" else 2 * dim
+    embs = []
+    for i in range(40):
+        e = rng.uniform(-0.04, 0.04, size=(1 + i % 3, wq)).astype(np.float32)
+        e[:, dim:] = np.abs(e[:, dim:])
+        embs.append(e)
+    t = rng.integers(0, info["n_entities"], size=40).astype(np.int32)
+    f = [[int(x) for x in rng.integers(0, info["n_entities"], size=6) if x != t[i]]
+         for i in range(40)]
+    np.testing.assert_array_equal(eng.eval_ranks_multi(embs, t, f),
+                                  oracle.eval_ranks_multi(backbone, ent, embs, t, f, dim))
