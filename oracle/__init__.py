@@ -51,6 +51,9 @@ _SIG = {
     "oracle_model_step_multi": (C.c_int, [C.c_void_p, i32, P(i32), P(i32), P(i32), P(i32), P(i32),
                                           P(i32), i32, i64, i32, P(f64)]),
     "oracle_model_set_semantic": (C.c_int, [C.c_void_p, i32, P(C.c_float), i64]),
+    "oracle_model_qmargins": (C.c_int, [C.c_void_p, P(f64), i32]),
+    "oracle_model_set_dev_tau": (C.c_int, [C.c_void_p, f64]),
+    "oracle_model_dev": (C.c_int, [C.c_void_p, C.c_char_p, P(f64), i64]),
     "oracle_digamma": (f64, [f64]),
     "oracle_trigamma": (f64, [f64]),
     "oracle_beta_kl": (f64, [f64, f64, f64, f64]),
@@ -170,6 +173,20 @@ class OracleModel:
     def margins(self, b):
         out = np.zeros(b, np.float64)
         _check(lib.oracle_model_margins(self._h, _p(out, f64), b))
+        return out
+
+    def set_dev_tau(self, tau):
+        """precision=65 only: kinks within tau inject fp32 deviation bounds."""
+        _check(lib.oracle_model_set_dev_tau(self._h, float(tau)))
+
+    def dev(self, name, shape):
+        out = np.zeros(shape, dtype=np.float64)
+        _check(lib.oracle_model_dev(self._h, name.encode(), _p(out, f64), out.size))
+        return out
+
+    def qmargins(self, b):
+        out = np.zeros(b, np.float64)
+        _check(lib.oracle_model_qmargins(self._h, _p(out, f64), b))
         return out
 
     def trace(self, with_nodes=False):

@@ -41,6 +41,7 @@ int oracle_model_create(int32_t backbone, int32_t n_entities, int32_t n_relation
                         int32_t n_neg, double gamma, double alpha_box, double lr,
                         int32_t precision, void** out);
 int oracle_model_init(void* m, uint64_t seed);
+/* name may carry "m:" or "v:" (Adam moments) */
 int oracle_model_set(void* m, const char* name, const float* data, int64_t n);
 /* name may carry "g:" (last step gradient), "m:" or "v:" (Adam moments) */
 int oracle_model_get(void* m, const char* name, double* out, int64_t n);
@@ -55,6 +56,13 @@ int oracle_model_trace_json(void* m, int32_t with_nodes, char* buf, int64_t cap,
  * signs, inside/outside, ReLU inputs, argmin/min routing gaps) */
 int oracle_model_margins(void* m, double* out, int32_t n);
 int oracle_model_destroy(void* m);
+/* per-query min over query-level kinks only (those that change dL/dq) */
+int oracle_model_qmargins(void* m, double* out, int32_t n);
+/* precision 65 (f64 values with first-order fp32 deviation bounds, oracle/src/dual.hpp):
+ * kinks within tau inject bounds; dev(name) = bound per element ("g:" gradients, "m:"/"v:"
+ * moments, plain = parameters). Values via oracle_model_get are the f64 model's. */
+int oracle_model_set_dev_tau(void* m, double tau);
+int oracle_model_dev(void* m, const char* name, double* out, int64_t n);
 
 /* scalar kernels for the SPEC known-answer tests */
 double oracle_q2b_distance(const double* v, const double* c, const double* o, int32_t d,

@@ -50,6 +50,13 @@ struct AnyModel {
   int precision = 64;
   std::unique_ptr<Model<double>> m64;
   std::unique_ptr<Model<float>> m32;
+  std::unique_ptr<Model<Dual>> mdv;  // precision 65: f64 values + fp32 deviation bounds
+  template <class F>
+  void visit(F&& f) {
+    if (m64) f(*m64);
+    else if (m32) f(*m32);
+    else f(*mdv);
+  }
   OTrace last;
 };
 
@@ -240,6 +247,9 @@ int oracle_model_create(int32_t backbone, int32_t ne, int32_t nr, int32_t dim, i
     if (precision == 64) {
       a->m64 = std::make_unique<Model<double>>();
       setup(*a->m64);
+    } else if (precision == 65) {
+      a->mdv = std::make_unique<Model<Dual>>();
+      setup(*a->mdv);
     } else {
       a->m32 = std::make_unique<Model<float>>();
       setup(*a->m32);
@@ -257,16 +267,14 @@ int oracle_model_set_semantic(void* mp, int32_t dl, const float* store, int64_t 
       if (n != (int64_t)md.ne * dl) throw std::runtime_error("semantic store size");
       md.setup_semantic(dl, store);
     };
-    if (a->m64) set(*a->m64);
-    else set(*a->m32);
+    a->visit([&](auto& md) { set(md); });
   });
 }
 
 int oracle_model_init(void* mp, uint64_t seed) {
   return guard([&] {
     auto* a = static_cast<AnyModel*>(mp);
-    if (a->m64) init_model(*a->m64, seed);
-    else init_model(*a->m32, seed);
+    a->visit([&](auto& md) { init_model(md, seed); });
   });
 }
 
@@ -275,20 +283,24 @@ int oracle_model_set(void* mp, const char* name, const float* data, int64_t n) {
     auto* a = static_cast<AnyModel*>(mp);
     auto set = [&](auto& md) {
       using R = typename std::remove_reference_t<decltype(md.P[name])>::value_type;
-      auto& v = md.P.at(name);
+      std::string s(name);
+      char kind = 'w';
+      if (s.size() > 2 && s[1] == ':') {  // "m:" / "v:" set the Adam moments
+        kind = s[0];
+        s = s.substr(2);
+      }
+      auto& v = (kind == 'm' ? md.M : kind == 'v' ? md.V : md.P).at(s);
       if ((int64_t)v.size() != n) throw std::runtime_error("size mismatch");
       for (int64_t i = 0; i < n; ++i) v[i] = R(data[i]);
     };
-    if (a->m64) set(*a->m64);
-    else set(*a->m32);
+    a->visit([&](auto& md) { set(md); });
   });
 }
 
 int oracle_model_get(void* mp, const char* name, double* out, int64_t n) {
   return guard([&] {
     auto* a = static_cast<AnyModel*>(mp);
-    if (a->m64) get_tensor(*a->m64, name, out, n);
-    else get_tensor(*a->m32, name, out, n);
+    a->visit([&](auto& md) { get_tensor(md, name, out, n); });
   });
 }
 
@@ -299,7 +311,9 @@ int oracle_model_step(void* mp, int32_t b, const int32_t* patterns, const int32_
   return guard([&] {
     auto* a = static_cast<AnyModel*>(mp);
     ODag d = o_build_training_dag(queries_of(b, patterns, anchors, relations));
-    if (a->m64 ? a->m64->dl : a->m32->dl)  // FuseSemantic replaces EmbedAnchor
+    int dl = 0;
+    a->visit([&](auto& md) { dl = md.dl; });
+    if (dl)  // FuseSemantic replaces EmbedAnchor
       for (auto& nd : d.nodes)
         if (nd.kind == K_EMB) nd.kind = K_FUSE;
     auto run = [&](auto& md) {
@@ -312,8 +326,7 @@ int oracle_model_step(void* mp, int32_t b, const int32_t* patterns, const int32_
                              adam >= 0, true);
       for (int i = 0; i < b; ++i) losses[i] = double(md.losses[i]);
     };
-    if (a->m64) run(*a->m64);
-    else run(*a->m32);
+    a->visit([&](auto& md) { run(md); });
   });
 }
 
@@ -343,15 +356,51 @@ int oracle_model_step_multi(void* mp, int32_t n, const int32_t* sizes, const int
         off += b;
       }
     };
-    if (a->m64) run(*a->m64);
-    else run(*a->m32);
+    a->visit([&](auto& md) { run(md); });
   });
 }
 
 int oracle_model_margins(void* mp, double* out, int32_t n) {
   return guard([&] {
     auto* a = static_cast<AnyModel*>(mp);
-    const std::vector<double>& m = a->m64 ? a->m64->margin : a->m32->margin;
+    std::vector<double> m;
+    a->visit([&](auto& md) { m = md.margin; });
+    if ((int32_t)m.size() != n) throw std::runtime_error("margin count mismatch");
+    for (int32_t i = 0; i < n; ++i) out[i] = m[i];
+  });
+}
+
+int oracle_model_set_dev_tau(void* mp, double tau) {
+  return guard([&] {
+    auto* a = static_cast<AnyModel*>(mp);
+    if (!a->mdv) throw std::runtime_error("deviation bounds need precision 65");
+    a->mdv->dev_tau = tau;
+  });
+}
+
+int oracle_model_dev(void* mp, const char* name, double* out, int64_t n) {
+  return guard([&] {
+    auto* a = static_cast<AnyModel*>(mp);
+    if (!a->mdv) throw std::runtime_error("deviation bounds need precision 65");
+    std::string s(name);
+    char kind = 'w';
+    if (s.size() > 2 && s[1] == ':') {
+      kind = s[0];
+      s = s.substr(2);
+    }
+    auto& md = *a->mdv;
+    if (!md.P.count(s)) throw std::runtime_error("unknown tensor " + s);
+    const auto& v = kind == 'w' ? md.P[s] : kind == 'g' ? md.G[s] : kind == 'm' ? md.M[s] : md.V[s];
+    if ((int64_t)v.size() != n) throw std::runtime_error("size mismatch for " + s);
+    for (int64_t i = 0; i < n; ++i) out[i] = v[i].d;
+  });
+}
+
+int oracle_model_qmargins(void* mp, double* out, int32_t n) {
+  return guard([&] {
+    auto* a = static_cast<AnyModel*>(mp);
+    std::vector<double> m;
+    a->visit([&](auto& md) { m = md.qmargin; });
     if ((int32_t)m.size() != n) throw std::runtime_error("margin count mismatch");
     for (int32_t i = 0; i < n; ++i) out[i] = m[i];
   });

@@ -19,6 +19,7 @@
 #include <deque>
 #include <stdexcept>
 
+#include "dual.hpp"
 #include "oracle_internal.hpp"
 #include "special.hpp"
 
@@ -42,7 +43,8 @@ struct Model {
   std::vector<R> sem;
   std::map<int, std::vector<R>> fcache, fgrad;
   std::vector<R> losses;
-  std::vector<double> margin;  // per query: min |kink argument| seen in the forward pass
+  std::vector<double> margin;   // per query: min |kink argument| seen in the forward pass
+  std::vector<double> qmargin;  // per query: query-level kinks only (those that change dL/dq)
   OTrace trace;
   int trace_elem_bytes = 4;
 
@@ -101,8 +103,8 @@ struct Model {
   }
 
   // ---- distances -----------------------------------------------------------
-  static R softplus(R x) { return x > 0 ? x + std::log1p(std::exp(-x)) : std::log1p(std::exp(x)); }
-  static R sigm(R x) { return x >= 0 ? R(1) / (R(1) + std::exp(-x)) : std::exp(x) / (R(1) + std::exp(x)); }
+  static R softplus(R x) { return x > 0 ? x + mlog1p(mexp(-x)) : mlog1p(mexp(x)); }
+  static R sigm(R x) { return x >= 0 ? R(1) / (R(1) + mexp(-x)) : mexp(x) / (R(1) + mexp(x)); }
   static R sgn(R x) { return R((x > 0) - (x < 0)); }
   // BetaE: realised Beta parameter clamp(softplus(x), 0.05, 1e9) (SURVEY A-7)
   static R bclamp(R x) { return std::min(std::max(x, R(0.05)), R(1e9)); }
@@ -111,18 +113,45 @@ struct Model {
     const R sp = softplus(x);
     return (sp > R(0.05) && sp < R(1e9)) ? sigm(x) : R(0);
   }
+  // ---- kink resolution (Dual: deviation bounds; f32/f64: plain selection) ----
+  double dev_tau = 0.0;  // > 0 in the deviation-bound model (precision 65)
+  // Exact ties (argument exactly 0: identical inputs, e.g. two branches through the
+  // same relation) are not kinks an fp32 run can resolve differently — both sides
+  // compute the same bits and apply the same tie rule (lowest index, relu'(0) = 0).
+  bool near(double m) const { return dev_tau > 0 && m != 0.0 && std::fabs(m) < dev_tau; }
+  // relu'(h) * g: g or 0; near the kink either is legitimate
+  R relu_k(const R& h, const R& g) const {
+    R r = h > R(0) ? g : R(0);
+    if (near(val(h))) add_dev(r, std::fabs(val(g)) + dev(g) - dev(r));
+    return r;
+  }
+  // realize'(x): sigma(x) inside the clamp, 0 where it binds
+  R drealize_k(const R& x) const {
+    R r = drealize(x);
+    if (near(val(softplus(x)) - 0.05)) add_dev(r, std::fabs(val(sigm(x))));
+    return r;
+  }
+  // sign(delta): +-1 (0 exactly at 0); near 0 the fp32 side may be either
+  R sgn_k(const R& delta) const {
+    R r = sgn(delta);
+    if (near(val(delta))) add_dev(r, 2.0);
+    return r;
+  }
   R dist(const R* q, const R* v) const {
     R s = 0;
     if (backbone == 2) {  // sum over dims of KL(entity || query)
+      std::vector<double> kl(d);  // per-dim terms in parallel, summed in dim order
+#pragma omp parallel for schedule(static) if (d >= 64)
       for (int e = 0; e < d; ++e)
-        s += beta_kl(realize(v[e]), realize(v[d + e]), q[e], q[d + e]);
+        kl[e] = beta_kl(val(realize(v[e])), val(realize(v[d + e])), val(q[e]), val(q[d + e]));
+      for (int e = 0; e < d; ++e) s += R(kl[e]);
       return s;
     }
     if (backbone == 0) {
-      for (int e = 0; e < d; ++e) s += std::fabs(v[e] - q[e]);
+      for (int e = 0; e < d; ++e) s += mfabs(v[e] - q[e]);
     } else {
       for (int e = 0; e < d; ++e) {
-        const R a = std::fabs(v[e] - q[e]), o = q[d + e];
+        const R a = mfabs(v[e] - q[e]), o = q[d + e];
         s += std::max(a - o, R(0)) + R(alpha) * std::min(a, o);
       }
     }
@@ -130,32 +159,40 @@ struct Model {
   }
   // gq += coef * d dist / dq ; gv += coef * d dist / dv
   void ddist(const R* q, const R* v, R coef, R* gq, R* gv) const {
-    if (backbone == 2) {
+    if (backbone == 2) {  // dims are independent: each writes only its own elements
+#pragma omp parallel for schedule(static) if (d >= 64)
       for (int e = 0; e < d; ++e) {
-        R g[4];
-        beta_kl_grad(realize(v[e]), realize(v[d + e]), q[e], q[d + e], g);
+        double g[4];
+        beta_kl_grad(val(realize(v[e])), val(realize(v[d + e])), val(q[e]), val(q[d + e]), g);
         if (gv) {
-          gv[e] += coef * g[0] * drealize(v[e]);
-          gv[d + e] += coef * g[1] * drealize(v[d + e]);
+          gv[e] += coef * R(g[0]) * drealize_k(v[e]);
+          gv[d + e] += coef * R(g[1]) * drealize_k(v[d + e]);
         }
         if (gq) {
-          gq[e] += coef * g[2];
-          gq[d + e] += coef * g[3];
+          gq[e] += coef * R(g[2]);
+          gq[d + e] += coef * R(g[3]);
         }
       }
       return;
     }
     for (int e = 0; e < d; ++e) {
       const R delta = v[e] - q[e];
+      const R s = sgn_k(delta);
       if (backbone == 0) {
-        if (gq) gq[e] -= coef * sgn(delta);
-        if (gv) gv[e] += coef * sgn(delta);
+        if (gq) gq[e] -= coef * s;
+        if (gv) gv[e] += coef * s;
       } else {
-        const R a = std::fabs(delta), o = q[d + e];
-        const R dv = (a > o ? R(1) : R(alpha)) * sgn(delta);
+        const R a = mfabs(delta), o = q[d + e];
+        R io = a > o ? R(1) : R(alpha);             // outside: 1, inside: alpha
+        R go = a > o ? R(alpha) - R(1) : R(0);      // d/do
+        if (near(val(a) - val(o))) {
+          add_dev(io, 1.0 - alpha);
+          add_dev(go, 1.0 - alpha);
+        }
+        const R dv = io * s;
         if (gq) {
           gq[e] -= coef * dv;
-          gq[d + e] += coef * (a > o ? R(alpha) - R(1) : R(0));
+          gq[d + e] += coef * go;
         }
         if (gv) gv[e] += coef * dv;
       }
@@ -182,26 +219,39 @@ struct Model {
   }
 
   // ---- small dense algebra: y = W x (+b), W [out][in] -----------------------
+  // Row-parallel (OpenMP, SPEC.md:435 allows rowwise parallelism inside kernels):
+  // every output element keeps its sequential summation order, so results are
+  // bit-identical for any thread count.
+  static constexpr int64_t kParMin = int64_t(1) << 16;
   void mv(const std::string& w, const std::string& b, const R* x, R* y) const {
     const auto& W = P.at(w);
     const auto [rows, cols] = shape.at(w);
+    const R* bias = b.empty() ? nullptr : P.at(b).data();
+#pragma omp parallel for schedule(static) if (rows * cols >= kParMin)
     for (int64_t o = 0; o < rows; ++o) {
-      R s = b.empty() ? R(0) : P.at(b)[o];
+      R s = bias ? bias[o] : R(0);
       for (int64_t i = 0; i < cols; ++i) s += W[o * cols + i] * x[i];
       y[o] = s;
     }
   }
-  // gx += W^T gy ; gW += gy x^T ; gb += gy
+  // gx += W^T gy ; gW += gy x^T ; gb += gy  (gx[i] accumulates over o ascending)
   void mv_bwd(const std::string& w, const std::string& b, const R* x, const R* gy, R* gx) {
     const auto& W = P.at(w);
     const auto [rows, cols] = shape.at(w);
-    auto& gW = G[w];
-    for (int64_t o = 0; o < rows; ++o) {
-      if (!b.empty()) G[b][o] += gy[o];
-      for (int64_t i = 0; i < cols; ++i) {
-        gW[o * cols + i] += gy[o] * x[i];
-        if (gx) gx[i] += W[o * cols + i] * gy[o];
-      }
+    R* gW = G[w].data();
+    R* gb = b.empty() ? nullptr : G[b].data();
+    if (gb)
+      for (int64_t o = 0; o < rows; ++o) gb[o] += gy[o];
+#pragma omp parallel for schedule(static) if (rows * cols >= kParMin)
+    for (int64_t o = 0; o < rows; ++o)
+      for (int64_t i = 0; i < cols; ++i) gW[o * cols + i] += gy[o] * x[i];
+    if (!gx) return;
+    constexpr int64_t kBlk = 32;
+#pragma omp parallel for schedule(static) if (rows * cols >= kParMin)
+    for (int64_t i0 = 0; i0 < cols; i0 += kBlk) {
+      const int64_t i1 = std::min(cols, i0 + kBlk);
+      for (int64_t o = 0; o < rows; ++o)
+        for (int64_t i = i0; i < i1; ++i) gx[i] += W[o * cols + i] * gy[o];
     }
   }
 
@@ -230,7 +280,7 @@ struct Model {
     std::vector<R> a(d), ga(d, R(0)), gm(d, R(0));
     for (int e = 0; e < d; ++e) a[e] = std::max(h[e], R(0));
     mv_bwd("int_w2", "", a.data(), gy, ga.data());
-    for (int e = 0; e < d; ++e) ga[e] = h[e] > 0 ? ga[e] : R(0);
+    for (int e = 0; e < d; ++e) ga[e] = relu_k(h[e], ga[e]);
     mv_bwd("int_w1", "", m, ga.data(), gm.data());
     for (int l = 0; l < kk; ++l)
       for (int e = 0; e < d; ++e) gout[(int64_t)l * d + e] = gm[e] / R(kk);
@@ -262,9 +312,9 @@ struct Model {
         R mx = t.s[0][e];
         for (int l = 1; l < kk; ++l) mx = std::max(mx, t.s[l][e]);
         R z = 0, c = 0, mn = xs[0][d + e];
-        for (int l = 0; l < kk; ++l) z += std::exp(t.s[l][e] - mx);
+        for (int l = 0; l < kk; ++l) z += mexp(t.s[l][e] - mx);
         for (int l = 0; l < kk; ++l) {
-          c += std::exp(t.s[l][e] - mx) / z * xs[l][e];
+          c += mexp(t.s[l][e] - mx) / z * xs[l][e];
           mn = std::min(mn, xs[l][d + e]);
         }
         out[e] = c;
@@ -287,7 +337,7 @@ struct Model {
       for (int l = 1; l < kk; ++l) mx = std::max(mx, t.s[l][e]);
       std::vector<R> w(kk);
       R z = 0;
-      for (int l = 0; l < kk; ++l) z += (w[l] = std::exp(t.s[l][e] - mx));
+      for (int l = 0; l < kk; ++l) z += (w[l] = mexp(t.s[l][e] - mx));
       R dot = 0;
       for (int l = 0; l < kk; ++l) {
         w[l] /= z;
@@ -302,21 +352,27 @@ struct Model {
         gs[l][e] = w[l] * (gC * xs[l][e] - dot);
         gout[(int64_t)l * 2 * d + e] += gC * w[l];
       }
-      gout[(int64_t)arg * 2 * d + d + e] += gO * gate;
+      const R route = gO * gate;
+      gout[(int64_t)arg * 2 * d + d + e] += route;
+      for (int l = 0; l < kk; ++l)  // a near-tied offset may take the route instead
+        if (l != arg && near(val(xs[l][d + e]) - val(mn))) {
+          add_dev(gout[(int64_t)l * 2 * d + d + e], std::fabs(val(route)) + dev(route));
+          add_dev(gout[(int64_t)arg * 2 * d + d + e], std::fabs(val(route)));
+        }
       gu[e] = gO * mn * gate * (R(1) - gate);
     }
     std::vector<R> glm(d, R(0));
     mv_bwd("off_w2", "off_b2", t.lm.data(), gu.data(), glm.data());
     std::vector<R> tmp(d), rz(d);
     for (int l = 0; l < kk; ++l) {
-      for (int e = 0; e < d; ++e) gp[l][e] = t.p[l][e] > 0 ? glm[e] / R(kk) : R(0);
+      for (int e = 0; e < d; ++e) gp[l][e] = relu_k(t.p[l][e], glm[e] / R(kk));
       std::fill(tmp.begin(), tmp.end(), R(0));
       mv_bwd("off_w1", "off_b1", xs[l] + d, gp[l].data(), tmp.data());
       for (int e = 0; e < d; ++e) gout[(int64_t)l * 2 * d + d + e] += tmp[e];
       for (int e = 0; e < d; ++e) rz[e] = std::max(t.z[l][e], R(0));
       std::fill(tmp.begin(), tmp.end(), R(0));
       mv_bwd("att_w2", "att_b2", rz.data(), gs[l].data(), tmp.data());
-      for (int e = 0; e < d; ++e) tmp[e] = t.z[l][e] > 0 ? tmp[e] : R(0);
+      for (int e = 0; e < d; ++e) tmp[e] = relu_k(t.z[l][e], tmp[e]);
       std::vector<R> gc(d, R(0));
       mv_bwd("att_w1", "att_b1", xs[l], tmp.data(), gc.data());
       for (int e = 0; e < d; ++e) gout[(int64_t)l * 2 * d + e] += gc[e];
@@ -346,9 +402,9 @@ struct Model {
     BetaProj t;
     beta_proj_fwd(in, r, nullptr, &t);
     std::vector<R> gz(2 * d), ga(2 * d, R(0)), gx(3 * d, R(0));
-    for (int e = 0; e < 2 * d; ++e) gz[e] = gy[e] * drealize(t.z[e]);
+    for (int e = 0; e < 2 * d; ++e) gz[e] = gy[e] * drealize_k(t.z[e]);
     mv_bwd("prj_w2", "prj_b2", t.a.data(), gz.data(), ga.data());
-    for (int e = 0; e < 2 * d; ++e) ga[e] = t.h[e] > 0 ? ga[e] : R(0);
+    for (int e = 0; e < 2 * d; ++e) ga[e] = relu_k(t.h[e], ga[e]);
     mv_bwd("prj_w1", "prj_b1", t.x.data(), ga.data(), gx.data());
     for (int e = 0; e < 2 * d; ++e) gin[e] = gx[e];
     for (int e = 0; e < d; ++e) gr[e] += gx[2 * d + e];
@@ -375,9 +431,9 @@ struct Model {
         R mx = t.s[0][e];
         for (int l = 1; l < kk; ++l) mx = std::max(mx, t.s[l][e]);
         R z = 0, al = 0, be = 0;
-        for (int l = 0; l < kk; ++l) z += std::exp(t.s[l][e] - mx);
+        for (int l = 0; l < kk; ++l) z += mexp(t.s[l][e] - mx);
         for (int l = 0; l < kk; ++l) {
-          const R w = std::exp(t.s[l][e] - mx) / z;
+          const R w = mexp(t.s[l][e] - mx) / z;
           al += w * xs[l][e];
           be += w * xs[l][d + e];
         }
@@ -397,7 +453,7 @@ struct Model {
       for (int l = 1; l < kk; ++l) mx = std::max(mx, t.s[l][e]);
       std::vector<R> w(kk), gw(kk);
       R z = 0, dot = 0;
-      for (int l = 0; l < kk; ++l) z += (w[l] = std::exp(t.s[l][e] - mx));
+      for (int l = 0; l < kk; ++l) z += (w[l] = mexp(t.s[l][e] - mx));
       const R gA = gy[e], gB = gy[d + e];
       for (int l = 0; l < kk; ++l) {
         w[l] /= z;
@@ -415,7 +471,7 @@ struct Model {
       for (int e = 0; e < 2 * d; ++e) rz[e] = std::max(t.z[l][e], R(0));
       std::fill(tmp.begin(), tmp.end(), R(0));
       mv_bwd("att_w2", "att_b2", rz.data(), gs[l].data(), tmp.data());
-      for (int e = 0; e < 2 * d; ++e) tmp[e] = t.z[l][e] > 0 ? tmp[e] : R(0);
+      for (int e = 0; e < 2 * d; ++e) tmp[e] = relu_k(t.z[l][e], tmp[e]);
       std::fill(gc.begin(), gc.end(), R(0));
       mv_bwd("att_w1", "att_b1", xs[l], tmp.data(), gc.data());
       for (int e = 0; e < 2 * d; ++e) gout[(int64_t)l * 2 * d + e] += gc[e];
@@ -473,7 +529,7 @@ struct Model {
         m[i] = R(b1) * m[i] + R(1 - b1) * g[i];
         v[i] = R(b2) * v[i] + R(1 - b2) * g[i] * g[i];
         const R mh = m[i] / R(bc1), vh = v[i] / R(bc2);
-        p[i] -= R(lr) * mh / (std::sqrt(vh) + R(eps));
+        p[i] -= R(lr) * mh / (msqrt(vh) + R(eps));
       }
     };
     for (const auto& n : names) {
@@ -595,10 +651,20 @@ struct Exec {
 
   // Kink margins (parity certification, tests/parity.py): the distance to the
   // nearest non-differentiable point the query's forward pass touched.
-  void kink(int q, double v) { md.margin[q] = std::min(md.margin[q], std::fabs(v)); }
+  // kink(): query-level (changes dL/dq); ekink(): gates only an entity element
+  template <class X>
+  void kink(int q, const X& x) {
+    const double v = val(x);
+    md.margin[q] = std::min(md.margin[q], std::fabs(v));
+    md.qmargin[q] = std::min(md.qmargin[q], std::fabs(v));
+  }
+  template <class X>
+  void ekink(int q, const X& x) {
+    md.margin[q] = std::min(md.margin[q], std::fabs(val(x)));
+  }
   void dist_kinks(int qi, const R* q, const R* v) {
     if (md.backbone == 2) {  // KL is smooth; only the entity clamp has kinks
-      for (int e = 0; e < 2 * md.d; ++e) kink(qi, double(Model<R>::softplus(v[e])) - 0.05);
+      for (int e = 0; e < 2 * md.d; ++e) ekink(qi, double(Model<R>::softplus(v[e])) - 0.05);
       return;
     }
     for (int e = 0; e < md.d; ++e) {
@@ -618,7 +684,7 @@ struct Exec {
         if (md.backbone == 2) {
           for (int i = 0; i < md.ew; ++i) {
             out[i] = Model<R>::realize(e[i]);
-            kink(x.query, double(Model<R>::softplus(e[i])) - 0.05);
+            ekink(x.query, double(Model<R>::softplus(e[i])) - 0.05);
           }
           break;
         }
@@ -741,7 +807,7 @@ struct Exec {
         R* ge = md.gerow(m.payload);
         if (md.backbone == 2) {
           const R* e = md.erow(m.payload);
-          for (int i = 0; i < md.ew; ++i) ge[i] += gin[i] * Model<R>::drealize(e[i]);
+          for (int i = 0; i < md.ew; ++i) ge[i] += gin[i] * md.drealize_k(e[i]);
           break;
         }
         for (int i = 0; i < md.ew; ++i) ge[i] += gin[i];
@@ -764,7 +830,7 @@ struct Exec {
         const R* in = md.backbone == 1 ? t(T[m.in[0]]) : nullptr;  // Q2B offset mask
         if (md.backbone == 1)
           for (int i = 0; i < d; ++i) {
-            const R gv = in[d + i] + r[d + i] > 0 ? gin[d + i] : R(0);
+            const R gv = md.relu_k(in[d + i] + r[d + i], gin[d + i]);
             gout[d + i] = gv;
             gr[d + i] += gv;
           }
@@ -776,6 +842,7 @@ struct Exec {
           for (int i = 0; i < md.wq; ++i) {
             const R inv = R(1) / in[i];
             gout[i] = (inv > R(0.05) && inv < R(1e9)) ? -gin[i] * inv * inv : R(0);
+            if (md.near(val(inv) - 0.05)) add_dev(gout[i], std::fabs(val(gin[i] * inv * inv)));
           }
           break;
         }
@@ -803,6 +870,11 @@ struct Exec {
           for (int l = 1; l < kk; ++l)
             if (t(T[m.in[l]])[j] < t(T[m.in[arg]])[j]) arg = l;
           for (int l = 0; l < kk; ++l) gout[(int64_t)l * (md.k + 1) + j] = l == arg ? gin[j] : R(0);
+          for (int l = 0; l < kk; ++l)  // near-tied branches may take the routed gradient
+            if (l != arg && md.near(val(t(T[m.in[l]])[j]) - val(t(T[m.in[arg]])[j]))) {
+              add_dev(gout[(int64_t)l * (md.k + 1) + j], std::fabs(val(gin[j])) + dev(gin[j]));
+              add_dev(gout[(int64_t)arg * (md.k + 1) + j], std::fabs(val(gin[j])));
+            }
         }
         break;
       }
@@ -950,6 +1022,7 @@ OTrace o_train_step(Model<R>& md, const ODag& g, const std::vector<int>& cand, i
   for (const auto& n : g.nodes) nq = std::max(nq, n.query + 1);
   md.losses.assign(nq, R(0));
   md.margin.assign(nq, 1e300);
+  md.qmargin.assign(nq, 1e300);
   md.fcache.clear();
   md.fgrad.clear();
   Exec<R> ex{md, g, cand, b_max, eager};
@@ -962,10 +1035,13 @@ OTrace o_train_step(Model<R>& md, const ODag& g, const std::vector<int>& cand, i
 
 template struct Model<double>;
 template struct Model<float>;
+template struct Model<Dual>;
 template OTrace o_train_step<double>(Model<double>&, const ODag&, const std::vector<int>&, int,
                                      bool, bool, int64_t, bool, bool, bool);
 template OTrace o_train_step<float>(Model<float>&, const ODag&, const std::vector<int>&, int, bool,
                                     bool, int64_t, bool, bool, bool);
+template OTrace o_train_step<Dual>(Model<Dual>&, const ODag&, const std::vector<int>&, int, bool,
+                                   bool, int64_t, bool, bool, bool);
 
 std::string OTrace::json(bool with_nodes) const {
   static const char* kNames[8] = {"EmbedAnchor", "FuseSemantic", "Project", "Negate",

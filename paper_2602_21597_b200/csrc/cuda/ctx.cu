@@ -1505,13 +1505,16 @@ int ngdb_graph_stats(ngdb_ctx* c, int64_t* updates, int64_t* instantiations) {
 
 // ---- checkpoint ("versioned binary blob of named parameter
 // tensors + config hash"; cadence SPEC.md:587) --------------------------------
-// Layout, little-endian: "NGCK", u32 version = 1, u64 config hash, i64 step,
-// i32 backbone, i32 dim, u32 tensor count; per tensor (registry order): u32 name
+// Layout, little-endian: "NGCK", u32 version = 2, u64 config hash, i64 step,
+// i32 backbone, i32 dim, i32 world, i32 rank, u32 tensor count; per tensor (registry order): u32 name
 // length, name, i64 rows, i64 cols, then theta, Adam m, Adam v as rows*cols f32
 // each; trailer: u64 FNV-1a of every preceding byte. The Adam moments and the
-// step make a resumed run bit-identical to an uninterrupted one.
+// step make a resumed run bit-identical to an uninterrupted one. A row-sharded
+// context (world > 1) writes its own rows only; world and rank are recorded and a
+// blob loads only into the same (world, rank) slot. Version-1 blobs (no world /
+// rank fields) load into unsharded contexts.
 namespace {
-constexpr uint32_t kCkptVersion = 1;
+constexpr uint32_t kCkptVersion = 2;
 struct Fnv {
   uint64_t h = 1469598103934665603ull;
   void add(const void* p, size_t n) {
@@ -1530,13 +1533,15 @@ int ngdb_checkpoint_save(ngdb_ctx* c, const char* path, uint64_t config_hash, in
       blob.insert(blob.end(), b, b + n);
     };
     const uint32_t ver = kCkptVersion, nt = static_cast<uint32_t>(c->params.size());
-    const int32_t bb = c->desc.backbone, dim = c->desc.dim;
+    const int32_t bb = c->desc.backbone, dim = c->desc.dim, world = c->world, rank = c->rank;
     put("NGCK", 4);
     put(&ver, 4);
     put(&config_hash, 8);
     put(&step, 8);
     put(&bb, 4);
     put(&dim, 4);
+    put(&world, 4);
+    put(&rank, 4);
     put(&nt, 4);
     CK(cudaStreamSynchronize(c->stream));
     std::vector<float> host;
@@ -1589,14 +1594,22 @@ int ngdb_checkpoint_load(ngdb_ctx* c, const char* path, uint64_t config_hash, in
     uint32_t ver, nt;
     uint64_t hash;
     int64_t st;
-    int32_t bb, dim;
+    int32_t bb, dim, world = 1, rank = 0;
     get(&ver, 4);
+    if (ver != 1 && ver != kCkptVersion) throw Fail{NGDB_ERR_CONFIG, "checkpoint: unsupported version"};
     get(&hash, 8);
     get(&st, 8);
     get(&bb, 4);
     get(&dim, 4);
+    if (ver >= 2) {
+      get(&world, 4);
+      get(&rank, 4);
+    }
     get(&nt, 4);
-    if (ver != kCkptVersion) throw Fail{NGDB_ERR_CONFIG, "checkpoint: unsupported version"};
+    if (world != c->world || rank != c->rank)
+      throw Fail{NGDB_ERR_CONFIG, "checkpoint: written by rank " + std::to_string(rank) + " of " +
+                                      std::to_string(world) + ", context is rank " +
+                                      std::to_string(c->rank) + " of " + std::to_string(c->world)};
     if (bb != c->desc.backbone || dim != c->desc.dim)
       throw Fail{NGDB_ERR_CONFIG, "checkpoint: BackboneMismatch (backbone / dim differ from the context)"};
     if (config_hash && hash != config_hash) throw Fail{NGDB_ERR_CONFIG, "checkpoint: config hash mismatch"};

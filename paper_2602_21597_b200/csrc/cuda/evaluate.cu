@@ -150,9 +150,10 @@ __global__ void __launch_bounds__(256) eval_count_kernel(EvalArgs a) {
     const int slot = q0 + qg * QPT + j;
     const int nbr = slot < a.nq ? a.slot_nb[slot] : 0;  // > 0: first slot of a query
     const int qi = nbr > 0 ? a.slot_query[slot] : -1;
-    float dm = d[j];
-    if (j + 1 < QPT && nbr > 1) dm = fminf(dm, d[j + 1 < QPT ? j + 1 : j]);
-    if (j + 2 < QPT && nbr > 2) dm = fminf(dm, d[j + 2 < QPT ? j + 2 : j]);
+    float dm = d[j];  // min over the query's nbr (1..QPT) consecutive branch slots
+#pragma unroll
+    for (int b = 1; b < QPT; ++b)
+      if (b < nbr && j + b < QPT) dm = fminf(dm, d[j + b < QPT ? j + b : j]);
     bool b = false, t = false;
     if (qi >= 0 && e < a.n_ent && e != a.target[qi]) {
       const float d_t = a.dt[qi];

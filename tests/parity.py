@@ -1,6 +1,11 @@
 """Shared helpers: run the product (GPU) and the oracle (CPU, f64) on identical
 seeded inputs and compare with the tolerance the north_star states.
 
+Two ways to handle kinks (see below): `run_pair` certifies whole queries
+(tie_free; small batches), `run_masked` compares every gradient / parameter
+element except those the oracle's per-element kink taint marks (full
+benchmark-shape batches; allow_frac = 0 on everything compared).
+
 Tolerance: |a - b| <= rtol * max(|b|, s) with s the RMS
 of the reference tensor, rtol = 1e-4 for fp32 vs the f64 oracle.
 
@@ -56,7 +61,7 @@ def weak_mask(name, grads):
     return np.abs(g_ref) <= noise
 
 
-def check_all(res, lr=1e-4, allow_frac=1e-3, steps=1):
+def check_all(res, lr=1e-4, allow_frac=0.0, steps=1):
     """Assert losses, gradients and post-Adam parameters agree (see module doc)."""
     msgs = []
     for loss, ref in res["loss"]:
@@ -109,6 +114,119 @@ def tie_free(batch, om, b_max, step, tau=TAU):
     sub = m.BatchArrays(a.patterns[keep], a.anchors[keep], a.relations[keep], a.positives[keep],
                         a.negatives[keep])
     return m.Batch.from_arrays(sub), float(keep.mean())
+
+
+def compare_masked(name, a, b, mask, scale=0.0):
+    """|a-b| <= 1e-4*max(|b|, s) on every element outside `mask`, no allowance.
+    Returns (ok, n_bad, worst, n_compared, n_live) with n_live = elements whose
+    oracle value is nonzero (the ones a step actually produced)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    keep = ~mask
+    s = max(rms(b), scale)
+    tol = RTOL * np.maximum(np.abs(b), s) + 1e-12
+    bad = (np.abs(a - b) > tol) & keep
+    live = b != 0
+    worst = float(np.max(np.where(keep, np.abs(a - b) / np.maximum(np.maximum(np.abs(b), s), 1e-30),
+                                  0.0))) if b.size else 0.0
+    return (not bad.any(), int(bad.sum()), worst, int((keep & live).sum()), int(live.sum()))
+
+
+def kink_mask(ref, dev, scale=0.0, frac=0.1):
+    """Elements whose fp32 deviation bound (oracle precision 65, oracle/src/dual.hpp)
+    exceeds frac of the 1e-4 tolerance: there a kink resolved the other way in fp32
+    could move the value by more than the comparison allows. Everything else must
+    match within 1e-4 with the bound's remainder inside the tolerance."""
+    s = max(rms(ref), scale)
+    return dev > frac * RTOL * np.maximum(np.abs(ref), s)
+
+
+def run_masked(graph, backbone, mix, b, k, dim, steps=1, b_max=512, seed_tag=0, semantic_dim=0,
+               tau=TAU, resync=True, query_level=False, log=print):
+    """Benchmark-shape parity with per-element kink masks.
+
+    Every step: the GPU step and the oracle step (f64 values + first-order fp32
+    deviation bounds, precision 65) on the same batch; per-query losses compared
+    on ALL queries; pre-Adam gradients of every parameter and the post-Adam
+    parameters compared element by element with no allowance everywhere
+    outside `kink_mask` (a kink within tau of its switch point, where fp32 and
+    f64 may legitimately take different subgradients, bounds the element's
+    possible deviation above a tenth of the tolerance). Post-Adam parameters
+    additionally skip elements whose oracle gradient is below fp32 noise (Adam's
+    direction is undefined there; held to the 2*lr step bound instead).
+
+    resync: before steps 2.., the oracle takes the GPU's parameters and Adam
+    moments, so every step is compared from an identical state (a masked
+    element's +-lr Adam move would otherwise shift later forwards).
+    query_level: the GPU runs the query-level baseline executor
+    while the oracle runs Alg. 1 — same per-node arithmetic, different order.
+    Returns {"compared": fraction of live gradient elements compared, ...}."""
+    import oracle as O
+    import paper_2602_21597_b200 as m
+
+    info = graph.info()
+    ne, nr = info["n_entities"], info["n_relations"]
+    w = m.pattern_weights(mix)
+    store = m.semantic_store(ne, semantic_dim, seed=5) if semantic_dim else None
+    eng = m.Engine(backbone, ne, nr, dim=dim, n_neg=k, b_max=b_max, max_queries=b, debug=True,
+                   semantic=store)
+    om = O.OracleModel(backbone, ne, nr, dim, k, precision=65)
+    if semantic_dim:
+        om.set_semantic(store)
+    om.init(2)
+    om.set_dev_tau(tau)
+    specs = m.param_specs(backbone, ne, nr, dim, semantic_dim)
+    msgs, compared, live, per = [], 0, 0, {}
+    for step in range(1, steps + 1):
+        batch = m.Batch.sample(graph, w, b, k, seed=3, tag=seed_tag + step)
+        a = batch.arrays()
+        if query_level:
+            plan = m.PlannedStep(batch, backbone, dim, b_max, semantic=bool(semantic_dim),
+                                 query_level=True)
+            eng_loss = eng.run_step(plan, b)
+        else:
+            eng_loss = eng.train_step(batch)
+        ref = om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, b_max=b_max,
+                      step=step)
+        ok, nbad, worst = rel_close(eng_loss, ref)
+        if not ok:
+            msgs.append(f"step {step} loss: {nbad}/{len(ref)} bad, worst rel {worst:.3e}")
+        grads = {}
+        for name, rows, cols, _ in specs:
+            grads[name] = (eng.download("g:" + name), om.get("g:" + name, (rows, cols)))
+        for name, rows, cols, _ in specs:
+            g, r = grads[name]
+            gmask = kink_mask(r, om.dev("g:" + name, (rows, cols)), grad_scale(name, grads))
+            ok, nbad, worst, nc, nl = compare_masked(name, g, r, gmask, grad_scale(name, grads))
+            compared += nc
+            live += nl
+            c0, l0 = per.get(name, (0, 0))
+            per[name] = (c0 + nc, l0 + nl)
+            if not ok:
+                msgs.append(f"step {step} grad {name}: {nbad} of {nc} compared beyond 1e-4 "
+                            f"(worst {worst:.3e})")
+            p, pr = eng.download(name), om.get(name, (rows, cols))
+            weak = weak_mask(name, grads)
+            pmask = gmask | weak | kink_mask(pr, om.dev(name, (rows, cols)))
+            ok, nbad, worst, _, _ = compare_masked(name, p, pr, pmask, rms(pr))
+            if not ok:
+                msgs.append(f"step {step} param {name}: {nbad} beyond 1e-4 (worst {worst:.3e})")
+            wk = weak & ~gmask
+            if wk.any():
+                d = float(np.max(np.abs(p[wk] - pr[wk])))
+                if d > 2 * 1e-4 * 1.0001 + 1e-9:
+                    msgs.append(f"step {step} param {name}: weak-gradient elements differ {d:.3e}")
+        if resync and step < steps:
+            for name, rows, cols, _ in specs:
+                for pre in ("", "m:", "v:"):
+                    om.set(pre + name, eng.download(pre + name))
+    frac = compared / max(live, 1)
+    log(f"parity[{backbone} b={b} k={k} d={dim} steps={steps}"
+        f"{' query-level' if query_level else ''}]: compared {compared}/{live} live gradient "
+        f"elements ({frac:.4f}); per tensor " +
+        ", ".join(f"{n} {c / max(l, 1):.3f}" for n, (c, l) in per.items()))
+    assert not msgs, "; ".join(msgs)
+    return {"compared": frac, "per_tensor": {n: c / max(l, 1) for n, (c, l) in per.items()}}
 
 
 def run_pair(graph, ograph, backbone, mix, b, k, dim, b_max=512, steps=1, seed_tag=0,

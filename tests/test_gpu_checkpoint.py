@@ -60,3 +60,32 @@ def test_checkpoint_errors(small_graph, tmp_path):
         a.load_checkpoint(bad)
     assert e.value.kind == "DomainError"
     assert a.load_checkpoint(path) == 0  # hash 0: not checked
+
+
+def test_sharded_blob_loads_only_into_its_rank(tmp_path):
+    # a row-sharded context's blob holds only its e mod G rows; it
+    # records (world, rank) and refuses any other slot, even when shapes match
+    import ctypes as C
+
+    from paper_2602_21597_b200._native import ModelDesc, check, lib
+
+    def ctx(world, rank):
+        d = ModelDesc(1, 200, 5, 16, 8, 0, 12.0, 0.02, 1e-4, 0.9, 0.999, 1e-8, 512, 64, world,
+                      rank)
+        h = C.c_void_p()
+        check(lib.ngdb_ctx_create(C.byref(d), 0, C.byref(h)))
+        return h
+
+    r0, r1, solo = ctx(2, 0), ctx(2, 1), ctx(1, 0)
+    try:
+        p = str(tmp_path / "r0.ngck").encode()
+        check(lib.ngdb_checkpoint_save(r0, p, 0, 3))
+        st = C.c_int64()
+        check(lib.ngdb_checkpoint_load(r0, p, 0, C.byref(st)))
+        assert st.value == 3
+        for other in (r1, solo):  # 200 entities, G = 2: rank 1 has the same 100-row shape
+            with pytest.raises(NgdbError, match="rank 0 of 2"):
+                check(lib.ngdb_checkpoint_load(other, p, 0, C.byref(st)))
+    finally:
+        for h in (r0, r1, solo):
+            lib.ngdb_ctx_destroy(h)

@@ -71,12 +71,13 @@ def test_union_queries_rank_by_nearest_branch(small_graph, backbone):
     ent = eng.download("entity")
     np.testing.assert_array_equal(eng.eval_ranks_multi(embs, t, f),
                                   oracle.eval_ranks_multi(backbone, ent, embs, t, f, dim))
-    # synthetic branch counts 1..3 straddling the 8-slot groups
+    # synthetic branch counts 1..8 straddling the 8-slot groups (the
+    # count pass must take the min over all of a query's branch slots)
     rng = np.random.default_rng(5)
     wq = dim if backbone == "gqe" else 2 * dim
     embs = []
     for i in range(40):
-        e = rng.uniform(-0.04, 0.04, size=(1 + i % 3, wq)).astype(np.float32)
+        e = rng.uniform(-0.04, 0.04, size=(1 + (i * 5) % 8, wq)).astype(np.float32)
         e[:, dim:] = np.abs(e[:, dim:])
         embs.append(e)
     t = rng.integers(0, info["n_entities"], size=40).astype(np.int32)
