@@ -168,14 +168,55 @@ def make_batches(graph, mix, batch, n_neg, count, base_tag):
     return [m.Batch.sample(graph, w, batch, n_neg, seed=3, tag=base_tag + i) for i in range(count)]
 
 
+# entity / relation counts of the synthetic shapes
+SHAPES = {"fb15k-237": (14505, 237), "nell995": (63361, 200), "wikikg2": (2500604, 535)}
+
+
+def config_dict(cfg, world):
+    """The `config` object of the JSON line — identical in both arms (ours and
+    --impl reference) for the same --config and N."""
+    backbone, shape, mix, dim, batch, n_neg = CONFIGS[cfg]
+    ne, nr = SHAPES[shape]
+    sdim = SEMANTIC_DIM.get(cfg, 0)
+    ent_cols = 2 * dim if backbone == "betae" else dim
+    out = {"workload": f"{backbone} on {shape}-shaped synthetic KG ({ne} entities, {nr} "
+                       f"relations), {mix}-pattern mix"
+                       + (f", FuseSemantic over a frozen {sdim}-d PTE store" if sdim else "")
+                       + (", entity table row-sharded" if cfg == "c5" else ""),
+           "config": cfg, "global_batch": batch * world, "n_neg": n_neg, "dim": dim}
+    table_mb = 3 * ne * ent_cols * 4 / 1e6 / (world if cfg == "c5" else 1)
+    if cfg == "c5":
+        out["parallelism"] = f"rowshard{world}+dp{world}"
+        out["l2"] = (f"inputs larger than L2: local entity table + Adam moments "
+                     f"{table_mb / 1e3:.1f} GB per rank")
+    else:
+        out["parallelism"] = f"replicas{world}" if world > 1 else "single"
+        out["l2"] = (f"L2 flushed (512 MB write) before every timed step; entity table + Adam "
+                     f"moments {table_mb:.0f} MB" if l2_flush(cfg) else
+                     f"inputs larger than L2: entity table + Adam moments {table_mb:.0f} MB; "
+                     f"no flush between steps")
+    return out
+
+
+def l2_flush(cfg):
+    backbone, shape, mix, dim, batch, n_neg = CONFIGS[cfg]
+    ent_cols = 2 * dim if backbone == "betae" else dim
+    return 3 * SHAPES[shape][0] * ent_cols * 4 / 1e6 < 2 * 126  # L2 is 126 MB
+
+
+# ---- the CPU reference (oracle/ only: never the product library) -------------
+_REF = {}
+
+
 def _oracle_worker(job):
-    """One host process of the CPU reference: its own oracle graph (from the
-    KG triples), sampler and model; `warmup` untimed steps, then `steps` timed
-    steps, each = sample a batch with the oracle's sampler + one training step
-    (the reference's train loop body)."""
-    (backbone, info, dim, n_neg, batch, mix_w, triples, store, wid, warmup, steps, budget) = job
+    """One host process of the CPU reference: the oracle's own sampler and model
+    on the oracle's graph (built before the fork); `warmup` untimed steps, then
+    up to `steps` timed steps, each = sample a batch + one training step (the
+    reference's train loop body), one OpenMP thread."""
+    backbone, dim, n_neg, batch, mix_w, wid, warmup, steps, budget, threads = job
     import oracle as O
-    g = O.OracleGraph(info["n_entities"], info["n_relations"], *triples)
+    O.set_threads(threads)
+    g, info, store = _REF["graph"], _REF["info"], _REF["store"]
     om = O.OracleModel(backbone, info["n_entities"], info["n_relations"], dim, n_neg,
                        precision=32)
     if store is not None:
@@ -198,23 +239,28 @@ def _oracle_worker(job):
     return done * batch, time.perf_counter() - t0
 
 
-def oracle_throughput(args_cfg, graph, workers, warmup, steps_total, budget=None):
-    """The CPU reference on `workers` host processes in parallel (data-parallel
-    replicas, one core each: an upper bound for any shared-model CPU run).
-    Returns (aggregate q/s, workers, steps done, seconds)."""
+def cpu_reference(cfg, workers, warmup, steps_total, budget=None, threads=1):
+    """The CPU reference (the oracle port: graph, sampler, Alg. 1 step, Adam; f32)
+    on `workers` forked host processes in parallel (data-parallel replicas of
+    `threads` OpenMP threads each: an upper bound for any shared-model CPU run).
+    Loads only oracle/. Returns (aggregate q/s, workers, steps done, seconds)."""
     import multiprocessing as mp
-    import paper_2602_21597_b200 as m
-    backbone, shape, mix, dim, batch, n_neg = CONFIGS[args_cfg]
-    info = graph.info()
-    triples = (graph.triples(0), graph.triples(1), graph.triples(2))
-    sdim = SEMANTIC_DIM.get(args_cfg, 0)
-    store = m.semantic_store(info["n_entities"], sdim, seed=5) if sdim else None
-    w = m.pattern_weights(MIXES[mix])
-    # bounded by host memory: each process holds its own model (θ, m, v, grad in
-    # f32) and graph
+
+    import oracle as O
+    backbone, shape, mix, dim, batch, n_neg = CONFIGS[cfg]
+    if _REF.get("shape") != shape or _REF.get("cfg") != cfg:
+        info = O.synth_info(shape)
+        sdim = SEMANTIC_DIM.get(cfg, 0)
+        _REF.update(shape=shape, cfg=cfg, info=info, graph=O.OracleGraph.synthetic(shape, 1),
+                    store=O.semantic_store(info["n_entities"], sdim, seed=5) if sdim else None)
+    info = _REF["info"]
+    w = np.zeros(len(MIXES["all"]), np.float64)
+    for p in MIXES[mix]:
+        w[MIXES["all"].index(p)] = 1.0
+    w /= w.sum()
+    # bounded by host memory: each process holds its own model (θ, m, v, grad in f32)
     ent_w = 2 * dim if backbone == "betae" else dim
-    per_worker = 5 * 4 * info["n_entities"] * ent_w + 200 * (info["n_train"] + info["n_valid"]
-                                                               + info["n_test"]) + (1 << 29)
+    per_worker = 5 * 4 * info["n_entities"] * ent_w + (1 << 29)
     try:
         import psutil
         avail = psutil.virtual_memory().available
@@ -222,7 +268,7 @@ def oracle_throughput(args_cfg, graph, workers, warmup, steps_total, budget=None
         avail = 16 << 30
     workers = max(1, min(workers, int(0.6 * avail // per_worker)))
     per = max(1, -(-steps_total // workers))
-    jobs = [(backbone, info, dim, n_neg, batch, w, triples, store, i, warmup, per, budget)
+    jobs = [(backbone, dim, n_neg, batch, w, i, warmup, per, budget, threads)
             for i in range(workers)]
     if workers == 1:
         res = [_oracle_worker(jobs[0])]
@@ -232,6 +278,21 @@ def oracle_throughput(args_cfg, graph, workers, warmup, steps_total, budget=None
     q = sum(r[0] for r in res)
     el = max(r[1] for r in res)
     return q / el, workers, q // batch, el
+
+
+def cpu_baseline_entry(cfg, steps_total, budget):
+    """cpu_baseline of the JSON line: all host cores (forked replicas) and one
+    core (--threads nproc and --threads 1)."""
+    batch = CONFIGS[cfg][4]
+    qps, workers, done, el = cpu_reference(cfg, host_workers(), 1, steps_total, budget)
+    q1, _, done1, el1 = cpu_reference(cfg, 1, 1, max(1, steps_total // workers), budget)
+    return {"value": qps, "unit": "queries/s", "cores": workers, "kind": "port",
+            "sample": f"{done} full {batch}-query steps (oracle sampler + Alg. 1 step + Adam, "
+                      f"f32) on {workers} forked host processes (1 thread each), {el:.1f}s; "
+                      f"the reference ships no implementation (SURVEY §0), so this is the "
+                      f"oracle port of it (oracle/ only)",
+            "single_core": {"value": q1, "unit": "queries/s", "cores": 1,
+                            "sample": f"{done1} steps on 1 process / 1 thread, {el1:.1f}s"}}
 
 
 QL_STEPS = 20
@@ -302,31 +363,30 @@ def host_workers():
 
 
 def reference_arm(args):
+    """--impl reference: the reference's CPU implementation of the path (the
+    oracle port) on every host core, same config / metric / unit as
+    our arm. Imports only oracle/ — the product library is never loaded here."""
     rank, world, _ = dist_env()
-    backbone, shape, mix, dim, batch, n_neg = CONFIGS[args.config]
     if rank != 0:
         return
-    import paper_2602_21597_b200 as m
-    graph = m.Graph.synthetic(shape, 1)  # the KG triples (input data); everything timed is oracle/
-    workers = host_workers()
-    qps, workers, done, el = oracle_throughput(args.config, graph, workers, 1, args.steps)
+    cfg = args.config
+    batch = CONFIGS[cfg][4]
+    base = cpu_baseline_entry(cfg, args.steps, args.cpu_budget * 3)
+    qps = base["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * batch / qps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{backbone} {shape}-shaped synthetic KG, {mix} mix"
-                               + (" + PTE fusion" if SEMANTIC_DIM.get(args.config) else ""),
-                   # our arm's config at this N (N replicas of 512-query steps); the host
-                   # runs 512-query steps on every worker process
-                   "global_batch": batch * max(1, args.gpus), "n_neg": n_neg, "dim": dim},
-        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": workers, "kind": "port",
-                         "sample": f"{done} full {batch}-query steps (oracle sampler + step, f32) "
-                                   f"on {workers} host processes in parallel, {el:.1f}s; the "
-                                   f"reference ships no implementation (SURVEY §0)"},
+        "config": config_dict(cfg, max(1, args.gpus)),
+        "cpu_baseline": base,
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    # the arm's contract: nothing of the product was imported or mapped
+    assert "paper_2602_21597_b200" not in sys.modules
+    with open("/proc/self/maps") as f:
+        assert "libngdb_b200" not in f.read()
     print(json.dumps(line), flush=True)
 
 
@@ -435,19 +495,12 @@ def bench_sharded(args):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e = batch * world * args.steps / float(t.item())
     if rank == 0:
-        G = world
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{backbone} on {shape}-shaped synthetic KG "
-                                   f"({info['n_entities']} entities, {info['n_relations']} "
-                                   f"relations), {mix}-pattern mix, entity table row-sharded",
-                       "global_batch": batch * world, "n_neg": n_neg, "dim": dim,
-                       "parallelism": f"rowshard{G}+dp{G}",
-                       "l2": "inputs larger than L2: local entity table + Adam moments "
-                             f"{3 * info['n_entities'] * dim * 4 / G / 1e9:.1f} GB per rank"},
+            "config": config_dict(args.config, world),
             "roofline": roofline(fams) if fams else None,
             "cpu_baseline": None,
             "e2e": {"value": e2e, "unit": "queries/s",
@@ -543,10 +596,7 @@ def main():
     clocks = ClockSampler(local)
     if not os.environ.get("BENCH_NO_CLOCKS"):
         clocks.start()
-    ent_cols = {s[0]: s[2] for s in m.param_specs(backbone, info["n_entities"],
-                                                  info["n_relations"], dim)}["entity"]
-    table_mb = 3 * info["n_entities"] * ent_cols * 4 / 1e6  # entity table + Adam m, v
-    flush = table_mb < 2 * 126  # L2 is 126 MB: flush between timed steps unless far larger
+    flush = l2_flush(args.config)  # entity table + Adam m, v vs the 126 MB L2
     ms = C.c_float()
     if flush:
         # each step timed on its own (CUDA events on the ctx stream) after a
@@ -668,33 +718,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        workers = host_workers()
-        qps, workers, done, el = oracle_throughput(args.config, graph, workers, 0, 10 ** 6,
-                                                   budget=args.cpu_budget)
-        cpu = {"value": qps, "unit": "queries/s", "cores": workers, "kind": "port",
-               "sample": f"{done} full {batch}-query steps (oracle sampler + step, f32) on "
-                         f"{workers} host processes, ~{args.cpu_budget:.0f}s each"}
-
-    if flush:
-        l2_note = (f"L2 flushed (512 MB write) before every timed step; entity table + Adam "
-                   f"moments {table_mb:.0f} MB")
-    else:
-        l2_note = (f"inputs larger than L2: entity table + Adam moments {table_mb:.0f} MB, "
-                   f"{len(batches)} distinct step plans; no flush between steps")
+        cpu = cpu_baseline_entry(args.config, 10 ** 6, args.cpu_budget)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{backbone} on {shape}-shaped synthetic KG "
-                                   f"({info['n_entities']} entities, {info['n_relations']} "
-                                   f"relations), {mix}-pattern mix"
-                                   + (f", FuseSemantic over a frozen {sdim}-d PTE store"
-                                      if sdim else ""),
-                       "global_batch": batch * world, "n_neg": n_neg, "dim": dim,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": l2_note},
+            "config": config_dict(args.config, world),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "queries/s",

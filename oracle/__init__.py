@@ -54,6 +54,10 @@ _SIG = {
     "oracle_model_qmargins": (C.c_int, [C.c_void_p, P(f64), i32]),
     "oracle_model_set_dev_tau": (C.c_int, [C.c_void_p, f64]),
     "oracle_model_dev": (C.c_int, [C.c_void_p, C.c_char_p, P(f64), i64]),
+    "oracle_synth_shape": (C.c_int, [C.c_char_p, P(i32), P(i32), P(i64)]),
+    "oracle_synth_triples": (C.c_int, [C.c_char_p, u64, P(i32)]),
+    "oracle_semantic_store": (C.c_int, [i32, i32, u64, P(C.c_float)]),
+    "oracle_set_threads": (C.c_int, [i32]),
     "oracle_digamma": (f64, [f64]),
     "oracle_trigamma": (f64, [f64]),
     "oracle_beta_kl": (f64, [f64, f64, f64, f64]),
@@ -74,7 +78,40 @@ def _check(rc):
         raise RuntimeError("oracle: " + lib.oracle_last_error().decode())
 
 
+def set_threads(n):
+    """OpenMP threads of the oracle's row-parallel loops (results do not depend on it)."""
+    lib.oracle_set_threads(int(n))
+
+
+def synth_info(shape):
+    ne, nr, c = i32(), i32(), (i64 * 3)()
+    _check(lib.oracle_synth_shape(shape.encode(), C.byref(ne), C.byref(nr), c))
+    return {"n_entities": ne.value, "n_relations": nr.value, "n_train": c[0], "n_valid": c[1],
+            "n_test": c[2]}
+
+
+def synth_triples(shape, seed=1):
+    """(train, valid, test) [n][3] int32 of the synthetic benchmark KG (oracle/src/synth.cpp)."""
+    info = synth_info(shape)
+    n = info["n_train"] + info["n_valid"] + info["n_test"]
+    out = np.zeros((n, 3), np.int32)
+    _check(lib.oracle_synth_triples(shape.encode(), seed, _p(out, i32)))
+    a, b = info["n_train"], info["n_train"] + info["n_valid"]
+    return out[:a], out[a:b], out[b:]
+
+
+def semantic_store(n_entities, dim=768, seed=5):
+    out = np.zeros((n_entities, dim), np.float32)
+    _check(lib.oracle_semantic_store(n_entities, dim, seed, _p(out, C.c_float)))
+    return out
+
+
 class OracleGraph:
+    @classmethod
+    def synthetic(cls, shape, seed=1):
+        info = synth_info(shape)
+        return cls(info["n_entities"], info["n_relations"], *synth_triples(shape, seed))
+
     def __init__(self, n_entities, n_relations, train, valid=None, test=None):
         def arr(x):
             return np.ascontiguousarray(np.zeros((0, 3)) if x is None else x, dtype=np.int32)

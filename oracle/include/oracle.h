@@ -74,6 +74,14 @@ int oracle_model_step_multi(void* model, int32_t n, const int32_t* sizes, const 
                             int64_t step, int32_t adam, double* losses);
 /* frozen semantic store [ne][dl] + fusion params (call before oracle_model_init) */
 int oracle_model_set_semantic(void* model, int32_t dl, const float* store, int64_t n);
+/* synthetic benchmark KGs: shape table; all triples of the shape
+ * [n_train + n_valid + n_test][3] (train first, then valid, then test); PTE store */
+int oracle_synth_shape(const char* name, int32_t* n_entities, int32_t* n_relations,
+                       int64_t* counts /* train, valid, test */);
+int oracle_synth_triples(const char* name, uint64_t seed, int32_t* out);
+int oracle_semantic_store(int32_t n_entities, int32_t dl, uint64_t seed, float* out);
+/* OpenMP threads of the row-parallel GEMVs / KL dims (results independent of it) */
+int oracle_set_threads(int32_t n);
 double oracle_loss(double gamma, double d_pos, const double* d_neg, int32_t k);
 /* BetaE special functions and KL(Beta(a1,b1) || Beta(a2,b2)) */
 double oracle_lgamma(double x);

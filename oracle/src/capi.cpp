@@ -1,5 +1,8 @@
 // ORACLE (test infrastructure only). C ABI for tests / smoke / CPU baseline.
 #include <cmath>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -436,6 +439,42 @@ double oracle_q2b_distance(const double* v, const double* c, const double* o, in
     q[d + i] = o[i];
   }
   return md.dist(q.data(), v);
+}
+
+int oracle_synth_shape(const char* name, int32_t* ne, int32_t* nr, int64_t* counts) {
+  return guard([&] {
+    const OShape sh = o_shape(name);
+    *ne = sh.ne;
+    *nr = sh.nr;
+    counts[0] = sh.ntr;
+    counts[1] = sh.nva;
+    counts[2] = sh.nte;
+  });
+}
+
+int oracle_synth_triples(const char* name, uint64_t seed, int32_t* out) {
+  return guard([&] {
+    const auto all = o_synth_triples(o_shape(name), seed);
+    for (size_t i = 0; i < all.size(); ++i) {
+      out[3 * i] = all[i].h;
+      out[3 * i + 1] = all[i].r;
+      out[3 * i + 2] = all[i].t;
+    }
+  });
+}
+
+int oracle_semantic_store(int32_t ne, int32_t dl, uint64_t seed, float* out) {
+  return guard([&] {
+    const auto v = o_semantic_store(ne, dl, seed);
+    std::memcpy(out, v.data(), v.size() * sizeof(float));
+  });
+}
+
+int oracle_set_threads(int32_t n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n > 0 ? n : 1);
+#endif
+  return 0;
 }
 
 double oracle_lgamma(double x) { return special([&] { return sp_lgamma(x); }); }

@@ -7,7 +7,7 @@
 // so this restatement is pinned by (a) golden vectors from the reference's own
 // executable header (tests/golden/rng_golden.json, oracle/ref/), and (b) every
 // [TRIVIAL]/[DERIVED] known-answer example of /root/reference/SPEC.md on this path
-// (tests/test_oracle_golden.py). Beyond those it is "parity unpinned" against a
+// (tests/test_spec_examples.py, tests/test_golden_rng.py). Beyond those it is "parity unpinned" against a
 // running reference — none exists.
 #pragma once
 
@@ -100,5 +100,14 @@ struct OTrace {
   std::vector<int> last_consumer_step;
   std::string json(bool with_nodes) const;
 };
+
+// ---------------- synthetic KGs — oracle/src/synth.cpp ----------
+struct OShape {
+  int ne, nr;
+  int64_t ntr, nva, nte;
+};
+OShape o_shape(const std::string& name);
+std::vector<OTriple> o_synth_triples(const OShape& sh, uint64_t seed);  // train|valid|test
+std::vector<float> o_semantic_store(int ne, int dl, uint64_t seed);
 
 }  // namespace oracle
