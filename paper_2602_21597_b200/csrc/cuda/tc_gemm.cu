@@ -10,9 +10,24 @@
 // keeps the contraction at fp32 accuracy (the tensor core's accumulator loses
 // precision over long runs). The epilogue stages the tile through shared
 // memory so global reads/writes of C are row-coalesced.
+//
+// Two mainloops share that contract and epilogue:
+//  * tc_gemm_tma_kernel (used whenever every operand row stride is a multiple
+//    of 16 bytes): warp-specialised. Warp 0 streams hi/lo tiles of A and B with
+//    TMA (cp.async.bulk.tensor, 128B swizzle, out-of-bounds rows / K zero-filled
+//    by the copy engine) into a 4-stage mbarrier ring; warp 1's elected lane
+//    issues the 12 UMMAs of a K chunk into one of two TMEM buffers and commits
+//    to the stage's "empty" and the buffer's "full" barriers; warps 2-5 drain a
+//    full buffer (tcgen05.ld), free it, and fold the chunk into fp32 registers
+//    while the tensor core already works on the next chunk. The per-chunk fold
+//    keeps the arithmetic (and the results) identical to the cp.async kernel.
+//  * tc_gemm_kernel: all threads stream with cp.async (any row stride).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -162,6 +177,113 @@ __device__ __forceinline__ void drain(uint32_t tmem, int buf, float* acc) {
   for (int j = 0; j < kHalfCols; ++j) acc[j] += __uint_as_float(r[j]);
 }
 
+// Split-K reduce-scatter over distributed shared memory plus the epilogue:
+// CTA `rank` owns rows [r_beg, r_end) of the tile, sums them over the S
+// partial tiles in rank order (deterministic) and writes them out (bias, ReLU
+// mask, accumulate, row scatter, chained split).
+__device__ __forceinline__ void store_tile(const TcGemmArgs& g, float* tile_s, int m0, int n0,
+                                           int r_beg, int r_end, int rank, int S, int nthreads) {
+  const int warp = threadIdx.x / 32;
+  const uint32_t local = smem_u32(tile_s);
+  if (((g.N | g.ldc) & 3) == 0) {
+    // float4 epilogue: thread t takes 16-byte column groups of the CTA's rows;
+    // the S partial loads are all issued before they are summed
+    constexpr int kQ = BN / 4;
+    const int n_items = (r_end - r_beg) * kQ;
+    for (int it = threadIdx.x; it < n_items; it += nthreads) {
+      const int r = r_beg + it / kQ, cq = (it % kQ) * 4;
+      const int row = m0 + r, n = n0 + cq;
+      if (row >= g.M || n >= g.N) continue;
+      const uint32_t off = static_cast<uint32_t>((r * kTileStride + cq) * 4);
+      float4 part[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        if (p >= S) break;
+        if (p == rank) {
+          part[p] = *reinterpret_cast<const float4*>(&tile_s[r * kTileStride + cq]);
+        } else {
+          uint32_t remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
+          asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                       : "=f"(part[p].x), "=f"(part[p].y), "=f"(part[p].z), "=f"(part[p].w)
+                       : "r"(remote));
+        }
+      }
+      float4 v = part[0];
+#pragma unroll
+      for (int p = 1; p < 8; ++p) {
+        if (p >= S) break;
+        v.x += part[p].x; v.y += part[p].y; v.z += part[p].z; v.w += part[p].w;
+      }
+      float* crow =
+          g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
+      if (g.bias) {
+        const float4 b = *reinterpret_cast<const float4*>(g.bias + n);
+        v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
+      }
+      if (g.mask) {
+        const float4 mk = *reinterpret_cast<const float4*>(g.mask + (int64_t)row * g.ldc + n);
+        if (!(mk.x > 0.f)) v.x = 0.f;
+        if (!(mk.y > 0.f)) v.y = 0.f;
+        if (!(mk.z > 0.f)) v.z = 0.f;
+        if (!(mk.w > 0.f)) v.w = 0.f;
+      }
+      if (g.accumulate) {
+        const float4 c0 = *reinterpret_cast<const float4*>(crow + n);
+        v.x += c0.x; v.y += c0.y; v.z += c0.z; v.w += c0.w;
+      }
+      *reinterpret_cast<float4*>(crow + n) = v;
+      if (g.s_hi) {
+        float4 h, l;
+        const float4 u = g.s_relu ? make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f),
+                                                fmaxf(v.w, 0.f))
+                                  : v;
+        split_tf32(u.x, h.x, l.x);
+        split_tf32(u.y, h.y, l.y);
+        split_tf32(u.z, h.z, l.z);
+        split_tf32(u.w, h.w, l.w);
+        *reinterpret_cast<float4*>(g.s_hi + (int64_t)row * g.ldc + n) = h;
+        *reinterpret_cast<float4*>(g.s_lo + (int64_t)row * g.ldc + n) = l;
+      }
+    }
+  } else {
+    const int lane = threadIdx.x & 31;
+    for (int r = r_beg + warp; r < r_end; r += nthreads / 32) {
+      const int row = m0 + r;
+      if (row >= g.M) break;
+      float* crow =
+          g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
+      for (int cc = lane; cc < BN; cc += 32) {
+        const int n = n0 + cc;
+        if (n >= g.N) break;
+        float v = 0.f;
+        const uint32_t off = static_cast<uint32_t>((r * kTileStride + cc) * 4);
+        for (int p = 0; p < S; ++p) {
+          if (p == rank) {
+            v += tile_s[r * kTileStride + cc];
+          } else {
+            uint32_t remote;
+            float pv;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv) : "r"(remote));
+            v += pv;
+          }
+        }
+        if (g.bias) v += g.bias[n];
+        if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;
+        if (g.accumulate) v += crow[n];
+        crow[n] = v;
+        if (g.s_hi) {
+          float h, l;
+          split_tf32(g.s_relu ? fmaxf(v, 0.f) : v, h, l);
+          g.s_hi[(int64_t)row * g.ldc + n] = h;
+          g.s_lo[(int64_t)row * g.ldc + n] = l;
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_constant__ TcGemmBatch batch) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t s_base = smem_u32(smem);
@@ -265,109 +387,184 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
   const int r_beg = rank * BM / S, r_end = (rank + 1) * BM / S;
   if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   else __syncthreads();
-  const uint32_t local = smem_u32(tile_s);
-  if (((g.N | g.ldc) & 3) == 0) {
-    // float4 epilogue: thread t takes 16-byte column groups of the CTA's rows;
-    // the S partial loads are all issued before they are summed
-    constexpr int kQ = BN / 4;
-    const int n_items = (r_end - r_beg) * kQ;
-    for (int it = threadIdx.x; it < n_items; it += kThreads) {
-      const int r = r_beg + it / kQ, cq = (it % kQ) * 4;
-      const int row = m0 + r, n = n0 + cq;
-      if (row >= g.M || n >= g.N) continue;
-      const uint32_t off = static_cast<uint32_t>((r * kTileStride + cq) * 4);
-      float4 part[8];
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        if (p >= S) break;
-        if (p == rank) {
-          part[p] = *reinterpret_cast<const float4*>(&tile_s[r * kTileStride + cq]);
-        } else {
-          uint32_t remote;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
-          asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
-                       : "=f"(part[p].x), "=f"(part[p].y), "=f"(part[p].z), "=f"(part[p].w)
-                       : "r"(remote));
-        }
-      }
-      float4 v = part[0];
-#pragma unroll
-      for (int p = 1; p < 8; ++p) {
-        if (p >= S) break;
-        v.x += part[p].x; v.y += part[p].y; v.z += part[p].z; v.w += part[p].w;
-      }
-      float* crow =
-          g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
-      if (g.bias) {
-        const float4 b = *reinterpret_cast<const float4*>(g.bias + n);
-        v.x += b.x; v.y += b.y; v.z += b.z; v.w += b.w;
-      }
-      if (g.mask) {
-        const float4 mk = *reinterpret_cast<const float4*>(g.mask + (int64_t)row * g.ldc + n);
-        if (!(mk.x > 0.f)) v.x = 0.f;
-        if (!(mk.y > 0.f)) v.y = 0.f;
-        if (!(mk.z > 0.f)) v.z = 0.f;
-        if (!(mk.w > 0.f)) v.w = 0.f;
-      }
-      if (g.accumulate) {
-        const float4 c0 = *reinterpret_cast<const float4*>(crow + n);
-        v.x += c0.x; v.y += c0.y; v.z += c0.z; v.w += c0.w;
-      }
-      *reinterpret_cast<float4*>(crow + n) = v;
-      if (g.s_hi) {
-        float4 h, l;
-        const float4 u = g.s_relu ? make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f),
-                                                fmaxf(v.w, 0.f))
-                                  : v;
-        split_tf32(u.x, h.x, l.x);
-        split_tf32(u.y, h.y, l.y);
-        split_tf32(u.z, h.z, l.z);
-        split_tf32(u.w, h.w, l.w);
-        *reinterpret_cast<float4*>(g.s_hi + (int64_t)row * g.ldc + n) = h;
-        *reinterpret_cast<float4*>(g.s_lo + (int64_t)row * g.ldc + n) = l;
-      }
-    }
-  } else {
-    const int lane = threadIdx.x & 31;
-    for (int r = r_beg + warp; r < r_end; r += kThreads / 32) {
-      const int row = m0 + r;
-      if (row >= g.M) break;
-      float* crow =
-          g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
-      for (int cc = lane; cc < BN; cc += 32) {
-        const int n = n0 + cc;
-        if (n >= g.N) break;
-        float v = 0.f;
-        const uint32_t off = static_cast<uint32_t>((r * kTileStride + cc) * 4);
-        for (int p = 0; p < S; ++p) {
-          if (p == rank) {
-            v += tile_s[r * kTileStride + cc];
-          } else {
-            uint32_t remote;
-            float pv;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local + off), "r"(p));
-            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(pv) : "r"(remote));
-            v += pv;
-          }
-        }
-        if (g.bias) v += g.bias[n];
-        if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;
-        if (g.accumulate) v += crow[n];
-        crow[n] = v;
-        if (g.s_hi) {
-          float h, l;
-          split_tf32(g.s_relu ? fmaxf(v, 0.f) : v, h, l);
-          g.s_hi[(int64_t)row * g.ldc + n] = h;
-          g.s_lo[(int64_t)row * g.ldc + n] = l;
-        }
-      }
-    }
-  }
+  store_tile(g, tile_s, m0, n0, r_beg, r_end, rank, S, kThreads);
   // peers' partial tiles must stay resident until every slice has been read
   if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(kTmemCols));
+}
+
+
+// ---------------------------------------------------------------------------
+// TMA + warp-specialised mainloop (see the file comment).
+constexpr int kTmaStages = 4;
+constexpr int kTmaThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 drain/epilogue
+constexpr int TMA_SMEM_BYTES = kTmaStages * STAGE + 1024 + 256;
+
+struct TmaProblem {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;  // 2-D {K, rows} fp32 maps, box {32, BM | BN}
+};
+struct TcGemmTmaBatch {
+  TmaProblem maps[kMaxProblems];
+  TcGemmArgs p[kMaxProblems];
+  int tile_begin[kMaxProblems + 1];
+  int n;
+  int S;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    tc_gemm_tma_kernel(const __grid_constant__ TcGemmTmaBatch batch) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 128B-swizzled tiles need 1024-byte aligned stage bases
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const uint32_t s_base = smem_u32(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * STAGE);
+  uint64_t* empty = full + kTmaStages;
+  uint64_t* tfull = empty + kTmaStages;   // [2] TMEM buffer holds a finished chunk
+  uint64_t* tempty = tfull + 2;           // [2] TMEM buffer drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int S = batch.S;
+  const int tile = blockIdx.x / S, rank = blockIdx.x % S;
+  int pi = 0;
+  while (pi + 1 < batch.n && tile >= batch.tile_begin[pi + 1]) ++pi;
+  const TcGemmArgs& g = batch.p[pi];
+  const TmaProblem& mp = batch.maps[pi];
+  const int lt = tile - batch.tile_begin[pi];
+  const int n_tiles_n = (g.N + BN - 1) / BN;
+  const int m0 = (lt / n_tiles_n) * BM, n0 = (lt % n_tiles_n) * BN;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int total_chunks = (g.K + BK - 1) / BK;
+  const int c_beg = rank * total_chunks / S;
+  const int n_chunks = (rank + 1) * total_chunks / S - c_beg;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaStages; ++i) {
+      mbar_init(smem_u32(&full[i]), 1);
+      mbar_init(smem_u32(&empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&tfull[i]), 1);
+      mbar_init(smem_u32(&tempty[i]), 4);  // one arrive per drain warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.a_hi)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.a_lo)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.b_hi)));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.b_lo)));
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  pdl_start();  // everything above overlapped the previous kernel's tail
+
+  float acc[BN];
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      for (int c = 0; c < n_chunks; ++c) {
+        const int st = c % kTmaStages, ph = (c / kTmaStages) & 1;
+        mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+        const uint32_t bar = smem_u32(&full[st]), dst = s_base + st * STAGE;
+        mbar_expect_tx(bar, STAGE);
+        const int k0 = (c_beg + c) * BK;
+        tma_load_2d(dst, &mp.a_hi, bar, k0, m0);
+        tma_load_2d(dst + A_TILE, &mp.a_lo, bar, k0, m0);
+        tma_load_2d(dst + 2 * A_TILE, &mp.b_hi, bar, k0, n0);
+        tma_load_2d(dst + 2 * A_TILE + B_TILE, &mp.b_lo, bar, k0, n0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      for (int c = 0; c < n_chunks; ++c) {
+        const int st = c % kTmaStages, ph = (c / kTmaStages) & 1;
+        const int buf = c & 1, bph = (c >> 1) & 1;
+        mbar_wait(smem_u32(&tempty[buf]), bph ^ 1);
+        mbar_wait(smem_u32(&full[st]), ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t a_hi = s_base + st * STAGE, a_lo = a_hi + A_TILE;
+        const uint32_t b_hi = a_hi + 2 * A_TILE, b_lo = b_hi + B_TILE;
+        const uint32_t d = tmem + buf * BN;
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first, fresh accumulator per chunk
+          const uint32_t off = ks * 32;
+          umma_tf32(d, umma_desc(a_lo + off), umma_desc(b_hi + off), ks == 0 ? 0u : 1u);
+          umma_tf32(d, umma_desc(a_hi + off), umma_desc(b_lo + off), 1u);
+          umma_tf32(d, umma_desc(a_hi + off), umma_desc(b_hi + off), 1u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&empty[st])));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&tfull[buf])));
+      }
+    }
+    __syncwarp();
+  } else {  // ---- drain warps 2..5: TMEM lane quarter (warp % 4), one row per thread
+#pragma unroll
+    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
+    const uint32_t lanes = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    for (int c = 0; c < n_chunks; ++c) {
+      const int buf = c & 1, bph = (c >> 1) & 1;
+      mbar_wait(smem_u32(&tfull[buf]), bph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint32_t r[BN];
+#pragma unroll
+      for (int j = 0; j < BN; j += 8)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[j]), "=r"(r[j + 1]), "=r"(r[j + 2]), "=r"(r[j + 3]), "=r"(r[j + 4]),
+                       "=r"(r[j + 5]), "=r"(r[j + 6]), "=r"(r[j + 7])
+                     : "r"(tmem + lanes + buf * BN + j));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+#pragma unroll
+      for (int j = 0; j < BN; ++j) acc[j] += __uint_as_float(r[j]);
+    }
+  }
+  // every chunk has been consumed by the tensor core and drained: the ring is free
+  __syncthreads();
+  float* tile_s = reinterpret_cast<float*>(smem);
+  if (warp >= 2) {
+    const int r = (warp & 3) * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < BN; j += 4)
+      *reinterpret_cast<float4*>(&tile_s[r * kTileStride + j]) =
+          make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+  }
+  const int r_beg = rank * BM / S, r_end = (rank + 1) * BM / S;
+  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+  else __syncthreads();
+  store_tile(g, tile_s, m0, n0, r_beg, r_end, rank, S, kTmaThreads);
+  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "n"(kTmemCols));
 }
@@ -431,20 +628,56 @@ __global__ void split_t_multi_kernel(SplitJobs jobs) {
 
 }  // namespace
 
-// Opt the kernel into > 48 KB dynamic shared memory (once per process, before
+// Opt the kernels into > 48 KB dynamic shared memory (once per process, before
 // any launch or stream capture).
 void tc_gemm_init() {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_gemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TMA_SMEM_BYTES);
     configured = true;
   }
 }
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// TMA needs 16-byte aligned bases and row strides
+bool tma_ok(const SplitOperand& o) {
+  return (o.ld & 3) == 0 && ((reinterpret_cast<uintptr_t>(o.hi) | reinterpret_cast<uintptr_t>(o.lo)) & 15) == 0;
+}
+
+// {K, rows} fp32, box {32, box_rows}, 128B swizzle (the UMMA K-major layout),
+// out-of-bounds elements read as zero
+bool encode(CUtensorMap* m, const float* base, int rows, int K, int ld, int box_rows) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  return tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
 
 int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   tc_gemm_init();
   TcGemmBatch b{};
   int max_chunks = 0, tiles = 0;
+  bool tma = tensor_map_encoder() != nullptr && !std::getenv("NGDB_GEMM_CPASYNC");
   b.n = 0;
   for (int i = 0; i < n && b.n < kMaxProblems; ++i) {
     const TcGemmArgs& g = probs[i];
@@ -453,14 +686,36 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
     b.tile_begin[b.n] = tiles;
     tiles += ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
     max_chunks = std::max(max_chunks, (g.K + BK - 1) / BK);
+    tma = tma && tma_ok(g.A) && tma_ok(g.B) && g.K > 0;
     ++b.n;
   }
   if (b.n == 0) return 0;
   b.tile_begin[b.n] = tiles;
-  // split-K so the launch fills about one wave (2 CTAs per SM), at most 8 CTAs
-  // per cluster (portable size) and at least 2 chunks per CTA
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
+  if (tma) {
+    TcGemmTmaBatch t{};  // ~2.6 KB of kernel parameters (4 tensor maps per problem)
+    for (int i = 0; i < b.n && tma; ++i) {
+      const TcGemmArgs& g = b.p[i];
+      t.p[i] = g;
+      tma = encode(&t.maps[i].a_hi, g.A.hi, g.M, g.K, g.A.ld, BM) &&
+            encode(&t.maps[i].a_lo, g.A.lo, g.M, g.K, g.A.ld, BM) &&
+            encode(&t.maps[i].b_hi, g.B.hi, g.N, g.K, g.B.ld, BN) &&
+            encode(&t.maps[i].b_lo, g.B.lo, g.N, g.K, g.B.ld, BN);
+      t.tile_begin[i] = b.tile_begin[i];
+    }
+    if (tma) {
+      t.tile_begin[b.n] = tiles;
+      t.n = b.n;
+      // one CTA per SM (208 KB ring): split-K so the launch fills about one wave,
+      // at most 8 CTAs per cluster and at least 2 chunks per CTA
+      t.S = std::max(1, std::min({8, num_sms / std::max(tiles, 1), max_chunks / 2}));
+      launch_pdl(tc_gemm_tma_kernel, dim3(tiles * t.S), dim3(kTmaThreads), TMA_SMEM_BYTES, s, t.S, t);
+      return 1;
+    }
+  }
+  // split-K so the launch fills about one wave (2 CTAs per SM), at most 8 CTAs
+  // per cluster (portable size) and at least 2 chunks per CTA
   b.S = std::max(1, std::min({8, (2 * num_sms) / std::max(tiles, 1), max_chunks / 2}));
   launch_pdl(tc_gemm_kernel, dim3(tiles * b.S), dim3(kThreads), SMEM_BYTES, s, b.S, b);
   return 1;
@@ -557,5 +812,53 @@ extern "C" int ngdb_debug_tc_gemm(int M, int N, int K, int a_major, int b_major,
   cudaMemcpy(C, dC, nc * 4, cudaMemcpyDeviceToHost);
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(sp);
   if (dbias) cudaFree(dbias);
+  return e == cudaSuccess ? 0 : 8;
+}
+
+// Timing entry point (tools/gemm_bench.py): `reps` back-to-back launches of one
+// M x N x K problem (or `batch` independent copies in one grouped launch) on
+// random pre-split operands; returns the mean CUDA-event time per launch.
+extern "C" int ngdb_debug_tc_gemm_time(int M, int N, int K, int batch, int reps, float* ms_out) {
+  using namespace ngdb_dev;
+  const int KP = (K + 3) & ~3;
+  batch = std::max(1, std::min(batch, 4));
+  const int64_t na = (int64_t)M * KP, nb = (int64_t)N * KP, nc = (int64_t)M * N;
+  float* buf = nullptr;
+  const int64_t per = 2 * na + 2 * nb + nc;
+  if (cudaMalloc(&buf, per * batch * 4)) return 8;
+  std::vector<float> host(per);
+  uint32_t x = 12345;
+  for (auto& v : host) {
+    x = x * 1664525u + 1013904223u;
+    v = ((x >> 8) * (1.0f / 16777216.0f) - 0.5f) * 0.1f;
+  }
+  TcGemmArgs gs[4];
+  for (int i = 0; i < batch; ++i) {
+    float* p = buf + i * per;
+    cudaMemcpy(p, host.data(), per * 4, cudaMemcpyHostToDevice);
+    TcGemmArgs g{};
+    g.M = M; g.N = N; g.K = K;
+    g.A = {p, p + na, KP};
+    g.B = {p + 2 * na, p + 2 * na + nb, KP};
+    g.C = p + 2 * na + 2 * nb; g.ldc = N;
+    gs[i] = g;
+  }
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  tc_gemm_batch(gs, batch, s);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, s);
+  for (int r = 0; r < reps; ++r) tc_gemm_batch(gs, batch, s);
+  cudaEventRecord(b, s);
+  cudaError_t e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *ms_out = ms / reps;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaStreamDestroy(s);
+  cudaFree(buf);
   return e == cudaSuccess ? 0 : 8;
 }
