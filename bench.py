@@ -182,20 +182,25 @@ def config_dict(cfg, world):
     out = {"workload": f"{backbone} on {shape}-shaped synthetic KG ({ne} entities, {nr} "
                        f"relations), {mix}-pattern mix"
                        + (f", FuseSemantic over a frozen {sdim}-d PTE store" if sdim else "")
-                       + (", entity table row-sharded" if cfg == "c5" else ""),
+                       + (", entity table row-sharded" if sharded(cfg, world) else ""),
            "config": cfg, "global_batch": batch * world, "n_neg": n_neg, "dim": dim}
-    table_mb = 3 * ne * ent_cols * 4 / 1e6 / (world if cfg == "c5" else 1)
-    if cfg == "c5":
+    table_mb = 3 * ne * ent_cols * 4 / 1e6 / (world if sharded(cfg, world) else 1)
+    if sharded(cfg, world):
         out["parallelism"] = f"rowshard{world}+dp{world}"
         out["l2"] = (f"inputs larger than L2: local entity table + Adam moments "
                      f"{table_mb / 1e3:.1f} GB per rank")
     else:
-        out["parallelism"] = f"replicas{world}" if world > 1 else "single"
+        out["parallelism"] = "single"
         out["l2"] = (f"L2 flushed (512 MB write) before every timed step; entity table + Adam "
                      f"moments {table_mb:.0f} MB" if l2_flush(cfg) else
                      f"inputs larger than L2: entity table + Adam moments {table_mb:.0f} MB; "
                      f"no flush between steps")
     return out
+
+
+def sharded(cfg, world):
+    """The row-sharded step runs C5 at every N and C1 / C2 at N > 1."""
+    return cfg == "c5" or world > 1
 
 
 def l2_flush(cfg):
@@ -391,8 +396,13 @@ def reference_arm(args):
 
 
 def bench_sharded(args):
-    """configs[4]: Q2B on the wikikg2 shape, entity table row-sharded over the
-    ranks (one process per GPU, NCCL), 512 queries per rank (weak scaling)."""
+    """Row-sharded step (configs[4]: Q2B on the wikikg2 shape; also C1/C2 when
+    N > 1): entity table row-sharded over the ranks, one process per GPU, 512
+    queries per rank (weak scaling). The device collectives run on the
+    context's own NCCL communicator inside libngdb (uneven all-to-alls of owned
+    rows, all-gather, reduce-scatter, all-reduce — captured with the stages in
+    one CUDA graph per step); torch.distributed (gloo) carries only the packed
+    int32 metadata records, the NCCL id and the barrier / max-over-ranks timing."""
     import torch
     import torch.distributed as dist
 
@@ -402,13 +412,18 @@ def bench_sharded(args):
 
     rank, world, local = dist_env()
     os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
-    if "MASTER_ADDR" not in os.environ:  # single process: a one-rank NCCL group
+    if "MASTER_ADDR" not in os.environ:  # single process: a one-rank group
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", rank=rank, world_size=world,
-                            device_id=torch.device("cuda", local))
-    comm = Comm()
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = Comm(transport="nccl")
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     backbone, shape, mix, dim, batch, n_neg = CONFIGS[args.config]
     t_setup = time.perf_counter()
     graph = m.Graph.synthetic(shape, 1)
@@ -420,7 +435,7 @@ def bench_sharded(args):
                for s in range(n_steps)]
     eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
                         n_neg=n_neg, max_queries=batch, device=local)
-    plans = [plan_shard_step(comm, b, backbone, dim) for b in batches]
+    plans = [plan_shard_step(comm, b, backbone, dim, batch_cap=batch) for b in batches]
     setup_s = time.perf_counter() - t_setup
     ctx = eng.handle
     step_no = 0
@@ -449,9 +464,7 @@ def bench_sharded(args):
     launches = lib.ngdb_launch_count(ctx) - launches0
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([ms.value / args.steps], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_step = float(t.item())
+    ms_step = max_over_ranks(ms.value / args.steps)
     value = batch * world / (ms_step / 1000.0)
     # per-family CUDA-event times on a profiled replay of a few steps
     check(lib.ngdb_profile_enable(ctx, 1))
@@ -491,9 +504,7 @@ def bench_sharded(args):
     b1, d1 = C.c_int64(), C.c_int64()
     check(lib.ngdb_transfer_bytes(ctx, C.byref(b1), C.byref(d1)))
     step_no = eng.step_count
-    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e = batch * world * args.steps / float(t.item())
+    e2e = batch * world * args.steps / max_over_ranks(e2e_s)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
@@ -505,8 +516,9 @@ def bench_sharded(args):
             "cpu_baseline": None,
             "e2e": {"value": e2e, "unit": "queries/s",
                     "h2d_bytes_per_step": int((b1.value - b0.value) / args.steps),
-                    "api": "ShardedEngine.train (host planning threads, metadata all-gather, "
-                           "stages + NCCL collectives, loss read-back per step)",
+                    "api": "ShardedEngine.train (host planning threads, packed metadata "
+                           "all-gather, stages + libngdb NCCL collectives, loss read-back "
+                           "per step)",
                     "d2h_bytes_per_step": 4 * batch + 16},
             "families": fams,
             "gpu_launches": int(launches),
@@ -523,7 +535,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: c2 at N=1, c5 (row-sharded wikikg2) at N>1")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=5)
@@ -536,17 +549,27 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `--gpus N` without a launcher: one process per GPU via torchrun
+        port = 29400 + os.getpid() % 500
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+    if world > 1 and world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if args.config is None:
+        args.config = "c5" if world > 1 else "c2"
 
     if args.impl == "reference":
         return reference_arm(args)
-    if args.config == "c5":
+    if args.config == "c5" or world > 1:
+        if args.config in ("c3", "c4"):
+            raise SystemExit(f"bench.py: --config {args.config} has no row-sharded step "
+                             "(BetaE / fusion); N > 1 runs c1, c2 or c5 row-sharded")
         return bench_sharded(args)
-
-    rank, world, local = dist_env()
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo")
 
     import ctypes as C
 

@@ -131,22 +131,33 @@ typedef struct ngdb_shard_plan {
   int32_t n_rows;            /* owner CSR over local entity rows */
   const int32_t* rows;
   const int32_t* seg;
-  const int32_t* contrib;
+  const int32_t* contrib;    /* code < 0: anchor row at lookup send position -code-1 */
+  /* uneven lookup all-to-all (the anchor-gradient return is its reverse) */
+  const int32_t* send_cnt;   /* [world] rows sent to each rank (its anchors this rank owns) */
+  const int32_t* recv_cnt;   /* [world] rows received from each owner */
+  int32_t n_send, n_recv;    /* sums of send_cnt / recv_cnt */
+  const int32_t* send_rows;  /* [n_send] local entity rows, requester-major */
+  const int32_t* recv_slot;  /* [n_recv] this rank's anchor slots, owner-major */
+  int32_t n_anchor_pos;
+  const int32_t* anchor_pos; /* [n_anchor_pos] anchor slot -> receive position */
 } ngdb_shard_plan;
 
 /* Exchange buffers of the sharded step, owned by the context (device memory,
- * float32, sizes in elements). The caller runs the collectives between stages:
- *   reduce-scatter(sum) anchor_send [world][A][ew]  -> anchor_rows [A][ew]
+ * float32, sizes in elements; ew = entity row width, wq = query width,
+ * S = max_slots, B = batch). The collectives between the stages:
+ *   all-to-all(v)       anchor_send [n_send][ew]    -> anchor_rows [n_recv][ew]
+ *                       (rows send_cnt[r] to rank r, recv_cnt[q] from rank q)
  *   all-gather          query_mine [S][wq]          -> query_all [world][S][wq]
- *   reduce-scatter(sum) dq_part [world][S][wq]      -> dq_mine [S][wq]
- *   reduce-scatter(sum) loss_part [world][B]        -> loss_mine [B]
- *   all-to-all          grad_send [world][A][ew]    -> grad_all [world][A][ew]
+ *   reduce-scatter(sum) dq_part [world][S*wq + B]   -> dq_mine [S*wq + B]
+ *                       (per rank block: dL/dq of its score slots, then its losses)
+ *   all-to-all(v)       grad_send [n_recv][ew]      -> grad_all [n_send][ew]
+ *                       (the lookup exchange reversed)
  *   all-reduce(sum)     reduce [dense grads | relation grads | relation touched] */
 typedef struct ngdb_shard_buffers {
-  float *anchor_send, *anchor_rows, *query_mine, *query_all, *dq_part, *dq_mine, *loss_part,
-      *loss_mine, *grad_send, *grad_all, *reduce;
+  float *anchor_send, *anchor_rows, *query_mine, *query_all, *dq_part, *dq_mine, *grad_send,
+      *grad_all, *reduce;
   int64_t n_anchor_send, n_anchor_rows, n_query_mine, n_query_all, n_dq_part, n_dq_mine,
-      n_loss_part, n_loss_mine, n_grad_send, n_grad_all, n_reduce;
+      n_grad_send, n_grad_all, n_reduce;
 } ngdb_shard_buffers;
 
 typedef enum ngdb_shard_stage {
@@ -240,6 +251,26 @@ int ngdb_shard_step_create(ngdb_ctx* ctx, const ngdb_step_plan* plan,
                            const ngdb_shard_plan* shard, ngdb_shard_step** out);
 int ngdb_shard_step_begin(ngdb_ctx* ctx, ngdb_shard_step* step, ngdb_shard_buffers* bufs);
 int ngdb_shard_step_destroy(ngdb_shard_step* step);
+/* --- NCCL owned by the context (no framework needed) -------
+ * Rank 0 creates an id, the caller ships its NGDB_COMM_ID_BYTES to every rank
+ * by any channel (MPI, a file, a TCP store), and every rank's context calls
+ * ngdb_comm_init (world / rank from ngdb_model_desc). libnccl.so.2 is loaded at
+ * run time (the framework's copy when one is already loaded). */
+#define NGDB_COMM_ID_BYTES 128
+int ngdb_comm_unique_id(uint8_t* id);
+int ngdb_comm_init(ngdb_ctx* ctx, const uint8_t* id);
+/* Host all-gather of `count` int32 per rank (the packed step metadata of
+ * ngdb_step_shard_pack), ordered on the context stream; synchronous. */
+int ngdb_comm_allgather_i32(ngdb_ctx* ctx, const int32_t* send, int64_t count, int32_t* recv);
+/* The whole active sharded step (after ngdb_shard_begin / ngdb_shard_step_begin):
+ * stages, NCCL collectives (uneven all-to-alls of owned rows, all-gather,
+ * reduce-scatter, all-reduce) and the optimizer, enqueued on the context
+ * stream. step <= 0: Adam scalars of the last ngdb_set_step. */
+int ngdb_shard_step_exec(ngdb_ctx* ctx, int64_t step);
+/* Capture begin + exec of a resident sharded step into one CUDA graph (NCCL
+ * collectives inside); replay sets the Adam scalars of `step` and launches it. */
+int ngdb_shard_step_capture(ngdb_ctx* ctx, ngdb_shard_step* step);
+int ngdb_shard_step_replay(ngdb_ctx* ctx, ngdb_shard_step* step, int64_t step_no);
 /* Adam bias-correction scalars of 1-based step t (host -> device, not capturable). */
 int ngdb_set_step(ngdb_ctx* ctx, int64_t step);
 /* Run the context's launches on an external stream (e.g. the framework stream

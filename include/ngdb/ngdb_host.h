@@ -77,6 +77,14 @@ int ngdb_shard_build(int32_t world, int32_t rank, int32_t batch, int32_t max_anc
                      int32_t max_slots, int32_t n_candidates, const int32_t* anchor_ids_all,
                      const int32_t* unit_k_all, const int32_t* unit_slots_all,
                      const int32_t* cand_all, ngdb_shard** out);
+/* Packed metadata: ONE int32 record per rank (fixed stride for a batch
+ * capacity; layout in ngdb/shard.hpp). Each rank packs its planned step, the
+ * records are all-gathered (ngdb_comm_allgather_i32, or any host channel) and
+ * ngdb_shard_build_packed turns the rank-major records into this rank's plan. */
+int64_t ngdb_shard_meta_stride(int32_t batch_cap, int32_t n_candidates);
+int ngdb_step_shard_pack(const ngdb_step* s, int32_t batch_cap, int32_t* out, int64_t stride);
+int ngdb_shard_build_packed(int32_t world, int32_t rank, const int32_t* gathered, int64_t stride,
+                            int32_t batch_cap, ngdb_shard** out);
 int ngdb_shard_view(const ngdb_shard* s, ngdb_shard_plan* view);
 int ngdb_shard_destroy(ngdb_shard* s);
 /* rows e = rank (mod world) of a parameter's deterministic init (entity table) */

@@ -3,10 +3,15 @@
 //
 // Entity e lives on rank e mod G at local row e div G; relations and MLPs are
 // replicated. Every rank plans its own 512-query batch exactly as on one GPU
-// (bit-exact per-rank trace). Scoring is query-shipping: the score-slot query
-// vectors are all-gathered, each rank scores the candidates it OWNS for every
-// rank's queries and the partial dL/dq are reduce-scattered back. This module
-// turns the all-gathered per-rank metadata into the owner's work lists.
+// (bit-exact per-rank trace). Each rank publishes its scoring metadata as ONE
+// packed int32 record (shard_meta_pack); the records are all-gathered and
+// turned into this rank's work lists:
+//   * embedding lookups: an uneven all-to-all — owner q sends rank r exactly the
+//     rows of r's anchors it owns (send_rows), r places them by recv_slot /
+//     anchor_pos; the anchor-gradient return is the same exchange reversed;
+//   * scoring is query-shipping: the score-slot query vectors are all-gathered,
+//     each rank scores the candidates it OWNS for every rank's queries and the
+//     partial dL/dq (+ partial losses) are reduce-scattered back.
 #pragma once
 
 #include <cstdint>
@@ -29,8 +34,16 @@ struct ShardPlanHost {
   std::vector<int32_t> anchor_ids, unit_k, unit_slots, cand;
   // candidate positions j of unit u this rank owns: owned[unit_off[u] .. unit_off[u+1])
   std::vector<int32_t> unit_off, owned;
+  // lookup all-to-all (the gradient return runs it in reverse):
+  //   send_cnt[r]  rows this rank sends rank r = rows of r's anchors it owns
+  //   recv_cnt[q]  rows this rank receives from owner q
+  //   send_rows    [sum send_cnt] local entity rows, requester-major, slot-ascending
+  //   recv_slot    [sum recv_cnt] this rank's anchor slots, owner-major, slot-ascending
+  //   anchor_pos   [A_mine] anchor slot -> its position in the receive order
+  std::vector<int32_t> send_cnt, recv_cnt, send_rows, recv_slot, anchor_pos;
   // owner CSR over LOCAL entity rows (e div G), rows ascending, codes ascending:
-  //   anchor of rank q, slot a:        code = -(q*A_max + a) - 1
+  //   anchor sent at lookup position p: code = -p - 1 (its gradient row comes
+  //                                     back at position p of the reverse exchange)
   //   candidate j of global slot g:    code = g*nc + j,  g = q*S_max + slot
   std::vector<int32_t> rows, seg, contrib;
 };
@@ -44,5 +57,16 @@ inline int32_t shard_local_rows(int32_t n_entities, int32_t world, int32_t rank)
 ShardPlanHost build_shard_plan(const ShardSpec& spec, const int32_t* anchor_ids_all,
                                const int32_t* unit_k_all, const int32_t* unit_slots_all,
                                const int32_t* cand_all);
+
+// Packed per-rank metadata record (int32, fixed stride for a batch capacity):
+//   [0] n_anchor_slots  [1] n_score_slots  [2] n_queries  [3] n_candidates
+//   [4 ..)              anchor ids   [3*B_cap]  (a query has at most 3 anchors)
+//                       unit_k       [B_cap]
+//                       unit_slots   [3*B_cap]
+//                       candidates   [B_cap * nc]
+int64_t shard_meta_stride(int32_t batch_cap, int32_t n_candidates);
+// All-gathered records (rank-major, `stride` apart) -> this rank's plan.
+ShardPlanHost build_shard_plan_packed(int32_t world, int32_t rank, const int32_t* gathered,
+                                      int64_t stride, int32_t batch_cap);
 
 }  // namespace ngdb

@@ -53,6 +53,9 @@ class ShardPlan(C.Structure):
         ("n_candidates", i32), ("anchor_ids", P(i32)), ("unit_k", P(i32)),
         ("unit_slots", P(i32)), ("cand", P(i32)), ("unit_off", P(i32)), ("owned", P(i32)),
         ("n_rows", i32), ("rows", P(i32)), ("seg", P(i32)), ("contrib", P(i32)),
+        ("send_cnt", P(i32)), ("recv_cnt", P(i32)), ("n_send", i32), ("n_recv", i32),
+        ("send_rows", P(i32)), ("recv_slot", P(i32)), ("n_anchor_pos", i32),
+        ("anchor_pos", P(i32)),
     ]
 
 
@@ -63,7 +66,7 @@ class TrainOpts(C.Structure):
 
 
 SHARD_BUFFERS = ("anchor_send", "anchor_rows", "query_mine", "query_all", "dq_part", "dq_mine",
-                 "loss_part", "loss_mine", "grad_send", "grad_all", "reduce")
+                 "grad_send", "grad_all", "reduce")
 
 
 class ShardBuffers(C.Structure):
@@ -102,6 +105,12 @@ SIGNATURES = {
     "ngdb_shard_step_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_set_step": (C.c_int, [C.c_void_p, i64]),
     "ngdb_shard_optimizer": (C.c_int, [C.c_void_p, i64]),
+    "ngdb_comm_unique_id": (C.c_int, [P(C.c_uint8)]),
+    "ngdb_comm_init": (C.c_int, [C.c_void_p, P(C.c_uint8)]),
+    "ngdb_comm_allgather_i32": (C.c_int, [C.c_void_p, P(i32), i64, P(i32)]),
+    "ngdb_shard_step_exec": (C.c_int, [C.c_void_p, i64]),
+    "ngdb_shard_step_capture": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ngdb_shard_step_replay": (C.c_int, [C.c_void_p, C.c_void_p, i64]),
     "ngdb_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ngdb_plan_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_sync": (C.c_int, [C.c_void_p]),
@@ -152,6 +161,9 @@ SIGNATURES = {
     "ngdb_shard_build": (C.c_int, [i32, i32, i32, i32, i32, i32, P(i32), P(i32), P(i32), P(i32),
                                    P(C.c_void_p)]),
     "ngdb_shard_view": (C.c_int, [C.c_void_p, P(ShardPlan)]),
+    "ngdb_shard_meta_stride": (i64, [i32, i32]),
+    "ngdb_step_shard_pack": (C.c_int, [C.c_void_p, i32, P(i32), i64]),
+    "ngdb_shard_build_packed": (C.c_int, [i32, i32, P(i32), i64, i32, P(C.c_void_p)]),
     "ngdb_shard_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_semantic_synth": (C.c_int, [i32, i32, u64, P(f32)]),
     "ngdb_ngse_write": (C.c_int, [C.c_char_p, P(f32), i64, i32]),

@@ -77,8 +77,10 @@ struct DevArgs {
   const float* sem;      // frozen store [n_entities][sem_dim]
   int32_t* anchor_local;
   int32_t fus_idx;       // dense index of fus_f (fus_wp = +1, fus_bp = +2)
-  // row-sharded step (shard.cu): anchor rows fetched from their owners [A][ent_w]
+  // row-sharded step (shard.cu): anchor rows fetched from their owners, in
+  // receive order [n_recv][ent_w]; anc_pos[anchor slot] = its receive position
   const float* anc_rows;
+  const int32_t* anc_pos;
   // Intersect stash: per forward node (slot = node aux) the MLP intermediates
   // its mirror reads instead of recomputing them; istash_slots slots of
   // kStashPerSlot * dim floats
@@ -98,16 +100,18 @@ struct DevArgs {
 
 // Device view of the sharded step's owner work (ngdb_shard_plan + buffers).
 struct ShardDev {
-  int32_t world, rank, batch, max_anchors, max_slots;
-  const int32_t* anchor_ids;
+  int32_t world, rank, batch, max_slots;
+  int32_t n_send, n_recv;
+  int64_t dq_block;         // floats per rank block of dq_part: max_slots*wq + batch
+  const int32_t* send_rows; // [n_send] local entity rows of the lookup send, requester-major
+  const int32_t* recv_slot; // [n_recv] this rank's anchor slots, owner-major
   const int32_t* unit_k;
   const int32_t* unit_slots;
   const int32_t* cand;
   const int32_t* unit_off;
   const int32_t* owned;
   const float* query_all;  // [world*max_slots][wq]
-  float* dq_part;          // [world*max_slots][wq]
-  float* loss_part;        // [world*batch]
+  float* dq_part;          // [world][max_slots*wq + batch]: partial dL/dq, then partial losses
   float* coef_all;         // [world*max_slots][ncand]
 };
 
@@ -312,8 +316,7 @@ int launch_shard_query_pack(const DevArgs& a, int first, int n, float* dst, cons
 int launch_shard_score(const DevArgs& a, const ShardDev& sd, const LaunchCtx& lc);
 int launch_shard_score_done(const DevArgs& a, const float* dq_mine, int64_t n_dq,
                             const float* loss_mine, int nq, const LaunchCtx& lc);
-int launch_shard_grad_pack(const DevArgs& a, const ShardDev& sd, int n_anchor, float* send,
-                           const LaunchCtx& lc);
+int launch_shard_grad_pack(const DevArgs& a, const ShardDev& sd, float* send, const LaunchCtx& lc);
 int launch_shard_rel_pack(const DevArgs& a, const SparseTable& t, float* rel_g, float* touched,
                           const LaunchCtx& lc);
 int launch_masked_rows_adam(float* w, float* m, float* v, float* dbg, const float* g,

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "nccl_loader.hpp"
 
 using namespace ngdb_dev;
 
@@ -199,6 +200,14 @@ struct ngdb_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t blob_free[2] = {nullptr, nullptr}, blob_ready[2] = {nullptr, nullptr};
   const float* anc_rows = nullptr;  // set while a sharded step runs
+  const int32_t* anc_pos = nullptr;
+  // NCCL communicators owned by the context (ngdb_comm_init): `comm` carries
+  // the step's collectives on the context stream, `meta_comm` the host
+  // metadata all-gather of upcoming steps on its own stream (another thread)
+  ncclComm_t comm = nullptr, meta_comm = nullptr;
+  cudaStream_t meta_stream = nullptr;
+  int32_t* meta_dev = nullptr;
+  int64_t meta_cap = 0;
   float* istash = nullptr;           // Intersect stash (DevArgs::istash)
   int32_t istash_slots = 0;
   float* pstash = nullptr;           // BetaE Project stash (DevArgs::pstash)
@@ -217,6 +226,7 @@ struct ngdb_ctx {
     int64_t buf_cap = 0;
     ShardDev dev{};
     ngdb_shard_buffers bufs{};
+    std::vector<int32_t> send_cnt, recv_cnt;  // host copies: NCCL send/recv counts (rows)
     float* coef_all = nullptr;
     int32_t n_rows = 0;
     const int32_t *rows = nullptr, *seg = nullptr, *contrib = nullptr;
@@ -448,6 +458,7 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.anchor_local = c->anchor_local;
   a.fus_idx = c->fus_idx;
   a.anc_rows = c->anc_rows;
+  a.anc_pos = c->anc_pos;
   a.istash = c->istash;
   a.istash_slots = c->istash_slots;
   a.pstash = c->pstash;
@@ -951,6 +962,10 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+  if (c->comm) nccl_api().CommDestroy(c->comm);
+  if (c->meta_comm) nccl_api().CommDestroy(c->meta_comm);
+  if (c->meta_stream) cudaStreamDestroy(c->meta_stream);
+  if (c->meta_dev) cudaFree(c->meta_dev);
   for (auto& p : c->params)
     if (p.sparse) {
       cudaFree(p.w);
@@ -1847,14 +1862,13 @@ namespace {
 
 // Device blob layout of a rank's owner work lists (ngdb_shard_plan).
 struct ShardLayout {
-  int64_t o_anc = 0, o_k = 0, o_slots = 0, o_cand = 0, o_off = 0, o_owned = 0, o_rows = 0,
-          o_seg = 0, o_con = 0, total = 0, n_owned = 0, n_con = 0;
+  int64_t o_k = 0, o_slots = 0, o_cand = 0, o_off = 0, o_owned = 0, o_rows = 0, o_seg = 0,
+          o_con = 0, o_send = 0, o_recv = 0, o_pos = 0, total = 0, n_owned = 0, n_con = 0;
   ShardLayout() = default;
   explicit ShardLayout(const ngdb_shard_plan& sp) {
-    const int64_t G = sp.world, B = sp.batch, A = sp.max_anchors, nc = sp.n_candidates, U = G * B;
+    const int64_t G = sp.world, B = sp.batch, nc = sp.n_candidates, U = G * B;
     n_owned = sp.unit_off[U];
     n_con = sp.n_rows ? sp.seg[sp.n_rows] : 0;
-    o_k = o_anc + up64(G * A);
     o_slots = o_k + up64(U);
     o_cand = o_slots + up64(U * 3);
     o_off = o_cand + up64(U * nc);
@@ -1862,11 +1876,13 @@ struct ShardLayout {
     o_rows = o_owned + up64(n_owned);
     o_seg = o_rows + up64(sp.n_rows);
     o_con = o_seg + up64(sp.n_rows + 1);
-    total = o_con + up64(n_con);
+    o_send = o_con + up64(n_con);
+    o_recv = o_send + up64(sp.n_send);
+    o_pos = o_recv + up64(sp.n_recv);
+    total = o_pos + up64(sp.n_anchor_pos);
   }
   void pack(const ngdb_shard_plan& sp, int32_t* h) const {
-    const int64_t G = sp.world, B = sp.batch, A = sp.max_anchors, nc = sp.n_candidates, U = G * B;
-    std::memcpy(h + o_anc, sp.anchor_ids, G * A * 4);
+    const int64_t G = sp.world, B = sp.batch, nc = sp.n_candidates, U = G * B;
     std::memcpy(h + o_k, sp.unit_k, U * 4);
     std::memcpy(h + o_slots, sp.unit_slots, U * 3 * 4);
     std::memcpy(h + o_cand, sp.cand, U * nc * 4);
@@ -1877,17 +1893,23 @@ struct ShardLayout {
       std::memcpy(h + o_seg, sp.seg, (sp.n_rows + 1) * 4);
       std::memcpy(h + o_con, sp.contrib, n_con * 4);
     }
+    if (sp.n_send) std::memcpy(h + o_send, sp.send_rows, int64_t(sp.n_send) * 4);
+    if (sp.n_recv) std::memcpy(h + o_recv, sp.recv_slot, int64_t(sp.n_recv) * 4);
+    if (sp.n_anchor_pos) std::memcpy(h + o_pos, sp.anchor_pos, int64_t(sp.n_anchor_pos) * 4);
   }
 };
 
-// the scalars of a shard plan a device step needs
+// the scalars of a shard plan a device step needs (+ the exchange counts)
 struct ShardShape {
   int32_t world = 1, rank = 0, batch = 0, max_anchors = 0, max_slots = 0, n_candidates = 0,
-          n_rows = 0;
+          n_rows = 0, n_send = 0, n_recv = 0;
+  std::vector<int32_t> send_cnt, recv_cnt;
   ShardShape() = default;
   explicit ShardShape(const ngdb_shard_plan& sp)
       : world(sp.world), rank(sp.rank), batch(sp.batch), max_anchors(sp.max_anchors),
-        max_slots(sp.max_slots), n_candidates(sp.n_candidates), n_rows(sp.n_rows) {}
+        max_slots(sp.max_slots), n_candidates(sp.n_candidates), n_rows(sp.n_rows),
+        n_send(sp.n_send), n_recv(sp.n_recv), send_cnt(sp.send_cnt, sp.send_cnt + sp.world),
+        recv_cnt(sp.recv_cnt, sp.recv_cnt + sp.world) {}
 };
 
 void validate_shard(ngdb_ctx* c, const ngdb_step_plan& plan, const ngdb_shard_plan& sp) {
@@ -1898,21 +1920,31 @@ void validate_shard(ngdb_ctx* c, const ngdb_step_plan& plan, const ngdb_shard_pl
   if (plan.n_score_slots > sp.max_slots || plan.n_anchor_slots > sp.max_anchors ||
       plan.n_queries > sp.batch || plan.n_candidates != sp.n_candidates)
     throw Fail{NGDB_ERR_SHAPE_MISMATCH, "step plan exceeds the shard plan's padding"};
+  if (!sp.send_cnt || !sp.recv_cnt || sp.n_anchor_pos < plan.n_anchor_slots)
+    throw Fail{NGDB_ERR_SHAPE_MISMATCH, "shard plan without lookup exchange lists"};
+  int64_t ns = 0, nr = 0;
+  for (int q = 0; q < sp.world; ++q) {
+    ns += sp.send_cnt[q];
+    nr += sp.recv_cnt[q];
+  }
+  if (ns != sp.n_send || nr != sp.n_recv)
+    throw Fail{NGDB_ERR_SHAPE_MISMATCH, "shard plan exchange counts do not add up"};
 }
 
 // Exchange buffer sizes of a shard shape (ngdb_shard_buffers order + coef_all).
-void shard_buffer_sizes(const ngdb_ctx* c, const ShardShape& sp, int64_t sizes[12]) {
-  const int64_t G = sp.world, B = sp.batch, A = sp.max_anchors, S = sp.max_slots,
-                nc = sp.n_candidates;
+constexpr int kShardBufs = 10;
+void shard_buffer_sizes(const ngdb_ctx* c, const ShardShape& sp, int64_t sizes[kShardBufs]) {
+  const int64_t G = sp.world, B = sp.batch, S = sp.max_slots, nc = sp.n_candidates;
   const int64_t ew = c->params[c->ent_idx].cols, wq = c->query_width();
   const Param& rel = c->params[c->rel_idx];
   const int64_t n_red = c->dense_n + rel.n() + rel.rows;
-  const int64_t z[12] = {G * A * ew, A * ew,      S * wq,     G * S * wq, G * S * wq, S * wq,
-                         G * B,      B,           G * A * ew, G * A * ew, n_red,      G * S * nc};
-  for (int k = 0; k < 12; ++k) sizes[k] = z[k];
+  const int64_t blk = S * wq + B;
+  const int64_t z[kShardBufs] = {sp.n_send * ew, sp.n_recv * ew, S * wq,     G * S * wq, G * blk,
+                                 blk,            sp.n_recv * ew, sp.n_send * ew, n_red, G * S * nc};
+  for (int k = 0; k < kShardBufs; ++k) sizes[k] = z[k];
 }
 bool shard_buffers_fit(const ngdb_ctx* c, const ShardShape& sp) {
-  int64_t sizes[12], need = 0;
+  int64_t sizes[kShardBufs], need = 0;
   shard_buffer_sizes(c, sp, sizes);
   for (int64_t z : sizes) need += up64(std::max<int64_t>(z, 1));
   return need <= c->sh.buf_cap;
@@ -1920,7 +1952,7 @@ bool shard_buffers_fit(const ngdb_ctx* c, const ShardShape& sp) {
 // (Re)size the exchange buffers (may synchronize) and point sh.bufs at them.
 void shard_exchange_buffers(ngdb_ctx* c, const ShardShape& sp) {
   auto& sh = c->sh;
-  int64_t sizes[12], need = 0;
+  int64_t sizes[kShardBufs], need = 0;
   shard_buffer_sizes(c, sp, sizes);
   for (int64_t z : sizes) need += up64(std::max<int64_t>(z, 1));
   if (need > sh.buf_cap) {
@@ -1930,9 +1962,9 @@ void shard_exchange_buffers(ngdb_ctx* c, const ShardShape& sp) {
     sh.buf = dmalloc<float>(sh.buf_cap);
     ++c->buffer_gen;
   }
-  float* ptr[12];
+  float* ptr[kShardBufs];
   float* cur = sh.buf;
-  for (int k = 0; k < 12; ++k) {
+  for (int k = 0; k < kShardBufs; ++k) {
     ptr[k] = cur;
     cur += up64(std::max<int64_t>(sizes[k], 1));
   }
@@ -1943,12 +1975,10 @@ void shard_exchange_buffers(ngdb_ctx* c, const ShardShape& sp) {
   b.query_all = ptr[3]; b.n_query_all = sizes[3];
   b.dq_part = ptr[4]; b.n_dq_part = sizes[4];
   b.dq_mine = ptr[5]; b.n_dq_mine = sizes[5];
-  b.loss_part = ptr[6]; b.n_loss_part = sizes[6];
-  b.loss_mine = ptr[7]; b.n_loss_mine = sizes[7];
-  b.grad_send = ptr[8]; b.n_grad_send = sizes[8];
-  b.grad_all = ptr[9]; b.n_grad_all = sizes[9];
-  b.reduce = ptr[10]; b.n_reduce = sizes[10];
-  sh.coef_all = ptr[11];
+  b.grad_send = ptr[6]; b.n_grad_send = sizes[6];
+  b.grad_all = ptr[7]; b.n_grad_all = sizes[7];
+  b.reduce = ptr[8]; b.n_reduce = sizes[8];
+  sh.coef_all = ptr[9];
 }
 // Make (plan, owner lists in `blob`) the active sharded step: the step
 // prologue on the stream (capturable) and the device views.
@@ -1964,9 +1994,12 @@ void shard_activate(ngdb_ctx* c, ngdb_plan* plan, const ShardShape& sp, const in
   d.world = sp.world;
   d.rank = sp.rank;
   d.batch = sp.batch;
-  d.max_anchors = sp.max_anchors;
   d.max_slots = sp.max_slots;
-  d.anchor_ids = blob + L.o_anc;
+  d.n_send = sp.n_send;
+  d.n_recv = sp.n_recv;
+  d.dq_block = int64_t(sp.max_slots) * c->query_width() + sp.batch;
+  d.send_rows = blob + L.o_send;
+  d.recv_slot = blob + L.o_recv;
   d.unit_k = blob + L.o_k;
   d.unit_slots = blob + L.o_slots;
   d.cand = blob + L.o_cand;
@@ -1974,13 +2007,15 @@ void shard_activate(ngdb_ctx* c, ngdb_plan* plan, const ShardShape& sp, const in
   d.owned = blob + L.o_owned;
   d.query_all = b.query_all;
   d.dq_part = b.dq_part;
-  d.loss_part = b.loss_part;
   d.coef_all = sh.coef_all;
   sh.n_rows = sp.n_rows;
   sh.rows = blob + L.o_rows;
   sh.seg = blob + L.o_seg;
   sh.contrib = blob + L.o_con;
+  sh.send_cnt = sp.send_cnt;
+  sh.recv_cnt = sp.recv_cnt;
   sh.active = true;
+  c->anc_pos = blob + L.o_pos;
   c->anc_rows = b.anchor_rows;
 }
 
@@ -1992,6 +2027,7 @@ struct ngdb_shard_step {
   int32_t* blob = nullptr;
   ShardLayout layout;
   ShardShape shape;
+  cudaGraphExec_t exec = nullptr;  // ngdb_shard_step_capture
 };
 
 extern "C" {
@@ -2091,6 +2127,7 @@ int ngdb_shard_step_begin(ngdb_ctx* c, ngdb_shard_step* r, ngdb_shard_buffers* o
 
 int ngdb_shard_step_destroy(ngdb_shard_step* r) {
   if (!r) return NGDB_OK;
+  if (r->exec) cudaGraphExecDestroy(r->exec);
   if (r->plan.blob) cudaFree(r->plan.blob);
   if (r->blob) cudaFree(r->blob);
   delete r;
@@ -2140,7 +2177,8 @@ int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
       case NGDB_SHARD_SCORE_DONE:
         timed(c, F_LOSS_FWD, 0.0, [&] {
           return launch_shard_score_done(a, b.dq_mine, int64_t(p->meta.n_score) * c->query_width(),
-                                         b.loss_mine, p->meta.n_queries, lc);
+                                         b.dq_mine + int64_t(sh.dev.max_slots) * c->query_width(),
+                                         p->meta.n_queries, lc);
         });
         break;
       case NGDB_SHARD_BACKWARD: {
@@ -2165,11 +2203,10 @@ int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
                        p->meta.n_rrows, p->blob + p->layout.rrows, p->blob + p->layout.rseg,
                        p->blob + p->layout.rcon};
         timed(c, F_OPT_RELATION, double(b.n_reduce) * 4 + double(b.n_grad_send) * 4, [&] {
-          CK(cudaMemsetAsync(b.grad_send, 0, b.n_grad_send * 4, c->stream));
           CK(cudaMemsetAsync(b.reduce, 0, b.n_reduce * 4, c->stream));
           if (c->dense_n)
             CK(cudaMemcpyAsync(b.reduce, c->dense_g, c->dense_n * 4, cudaMemcpyDeviceToDevice, c->stream));
-          return launch_shard_grad_pack(a, sh.dev, p->meta.n_anchor, b.grad_send, lc) +
+          return launch_shard_grad_pack(a, sh.dev, b.grad_send, lc) +
                  launch_shard_rel_pack(a, tr, b.reduce + c->dense_n, b.reduce + c->dense_n + rel.n(), lc);
         });
         break;
@@ -2216,8 +2253,157 @@ int ngdb_shard_optimizer(ngdb_ctx* c, int64_t step) {
     CK(cudaGetLastError());
     sh.active = false;
     c->anc_rows = nullptr;
+    c->anc_pos = nullptr;
+  });
+}
+
+// ---- NCCL owned by the context -------------------------------
+
+}  // extern "C"
+
+namespace {
+
+const NcclApi& nccl_or_fail() {
+  const NcclApi& n = nccl_api();
+  if (!n.error.empty()) throw Fail{NGDB_ERR_CONFIG, n.error};
+  return n;
+}
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Fail{NGDB_ERR_CUDA, std::string(what) + ": " + nccl_api().GetErrorString(r)};
+}
+void rc_throw(int rc) {
+  if (rc != NGDB_OK) throw Fail{rc, g_last_error};
+}
+
+// Uneven all-to-all of rows (`width` floats each): scnt[q] rows to rank q from
+// `send` (rank-major), rcnt[q] rows from rank q into `recv` (rank-major). One
+// NCCL group of point-to-point calls: only rows that are needed travel.
+void all_to_all_rows(ngdb_ctx* c, const float* send, const std::vector<int32_t>& scnt, float* recv,
+                     const std::vector<int32_t>& rcnt, int64_t width) {
+  const NcclApi& n = nccl_api();
+  nck(n.GroupStart(), "ncclGroupStart");
+  int64_t so = 0, ro = 0;
+  for (int q = 0; q < c->world; ++q) {
+    if (scnt[q])
+      nck(n.Send(send + so * width, size_t(scnt[q]) * width, ncclFloat32, q, c->comm, c->stream),
+          "ncclSend");
+    if (rcnt[q])
+      nck(n.Recv(recv + ro * width, size_t(rcnt[q]) * width, ncclFloat32, q, c->comm, c->stream),
+          "ncclRecv");
+    so += scnt[q];
+    ro += rcnt[q];
+  }
+  nck(n.GroupEnd(), "ncclGroupEnd");
+}
+
+// Stages + collectives + optimizer of the active sharded step, all enqueued on
+// the context stream (capturable: no host synchronisation).
+void shard_exec(ngdb_ctx* c, int64_t step) {
+  if (!c->comm) throw Fail{NGDB_ERR_CONFIG, "ngdb_shard_step_exec: call ngdb_comm_init first"};
+  auto& sh = c->sh;
+  if (!sh.active) throw Fail{NGDB_ERR_CONFIG, "ngdb_shard_step_exec outside a sharded step"};
+  const NcclApi& n = nccl_api();
+  const ngdb_shard_buffers b = sh.bufs;
+  const int64_t ew = c->params[c->ent_idx].cols;
+  const int64_t blk = sh.dev.dq_block;
+  rc_throw(ngdb_shard_run(c, NGDB_SHARD_ANCHOR_PACK));
+  all_to_all_rows(c, b.anchor_send, sh.send_cnt, b.anchor_rows, sh.recv_cnt, ew);
+  rc_throw(ngdb_shard_run(c, NGDB_SHARD_FORWARD));
+  rc_throw(ngdb_shard_run(c, NGDB_SHARD_QUERY_PACK));
+  nck(n.AllGather(b.query_mine, b.query_all, size_t(b.n_query_mine), ncclFloat32, c->comm,
+                  c->stream), "ncclAllGather");
+  rc_throw(ngdb_shard_run(c, NGDB_SHARD_SCORE));
+  nck(n.ReduceScatter(b.dq_part, b.dq_mine, size_t(blk), ncclFloat32, ncclSum, c->comm, c->stream),
+      "ncclReduceScatter");
+  rc_throw(ngdb_shard_run(c, NGDB_SHARD_SCORE_DONE));
+  rc_throw(ngdb_shard_run(c, NGDB_SHARD_BACKWARD));
+  rc_throw(ngdb_shard_run(c, NGDB_SHARD_GRAD_PACK));
+  all_to_all_rows(c, b.grad_send, sh.recv_cnt, b.grad_all, sh.send_cnt, ew);
+  nck(n.AllReduce(b.reduce, b.reduce, size_t(b.n_reduce), ncclFloat32, ncclSum, c->comm, c->stream),
+      "ncclAllReduce");
+  rc_throw(ngdb_shard_optimizer(c, step));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ngdb_comm_unique_id(uint8_t* id) {
+  return guarded([&] {
+    static_assert(sizeof(ncclUniqueId) == NGDB_COMM_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId u;
+    nck(nccl_or_fail().GetUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int ngdb_comm_init(ngdb_ctx* c, const uint8_t* id) {
+  return guarded([&] {
+    const NcclApi& n = nccl_or_fail();
+    if (c->comm) throw Fail{NGDB_ERR_CONFIG, "ngdb_comm_init: communicator already set"};
+    CK(cudaSetDevice(c->device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    nck(n.CommInitRank(&c->comm, c->world, u, c->rank), "ncclCommInitRank");
+  });
+}
+
+int ngdb_comm_allgather_i32(ngdb_ctx* c, const int32_t* send, int64_t count, int32_t* recv) {
+  return guarded([&] {
+    if (!c->comm) throw Fail{NGDB_ERR_CONFIG, "ngdb_comm_allgather_i32: call ngdb_comm_init first"};
+    const int64_t need = count * (c->world + 1);
+    if (need > c->meta_cap) {
+      CK(cudaStreamSynchronize(c->stream));
+      if (c->meta_dev) CK(cudaFree(c->meta_dev));
+      c->meta_cap = need;
+      c->meta_dev = dmalloc<int32_t>(need);
+    }
+    int32_t* dsend = c->meta_dev + count * c->world;
+    CK(cudaMemcpyAsync(dsend, send, count * 4, cudaMemcpyHostToDevice, c->stream));
+    nck(nccl_api().AllGather(dsend, c->meta_dev, size_t(count), ncclInt32, c->comm, c->stream),
+        "ncclAllGather");
+    CK(cudaMemcpyAsync(recv, c->meta_dev, count * c->world * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ngdb_shard_step_exec(ngdb_ctx* c, int64_t step) {
+  return guarded([&] { shard_exec(c, step); });
+}
+
+int ngdb_shard_step_capture(ngdb_ctx* c, ngdb_shard_step* r) {
+  return guarded([&] {
+    if (!c->comm) throw Fail{NGDB_ERR_CONFIG, "ngdb_shard_step_capture: call ngdb_comm_init first"};
+    if (r->exec) CK(cudaGraphExecDestroy(r->exec));
+    r->exec = nullptr;
+    ensure_step_buffers(c, r->plan.meta);
+    shard_exchange_buffers(c, r->shape);  // sized before capture
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    cudaGraph_t g = nullptr;
+    try {
+      rc_throw(ngdb_shard_step_begin(c, r, nullptr));
+      shard_exec(c, 0);
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c->sh.active = false;
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->stream, &g));
+    const cudaError_t e = cudaGraphInstantiate(&r->exec, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+  });
+}
+
+int ngdb_shard_step_replay(ngdb_ctx* c, ngdb_shard_step* r, int64_t step) {
+  return guarded([&] {
+    if (!r->exec) throw Fail{NGDB_ERR_CONFIG, "ngdb_shard_step_replay: capture the step first"};
+    set_step_scalars(c, step);
+    CK(cudaGraphLaunch(r->exec, c->stream));
   });
 }
 
 }  // extern "C"
-

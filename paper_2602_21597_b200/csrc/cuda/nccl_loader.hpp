@@ -1,0 +1,75 @@
+// NCCL entry points of the row-sharded step, resolved at run time.
+//
+// The context owns its communicators (ngdb_comm_init) so a C/C++ caller can
+// drive the whole sharded step through the C ABI with no Python framework.
+// libnccl is dlopen'ed by soname: inside a process that already loaded a
+// framework's NCCL (torch bundles one) the dynamic linker returns that copy,
+// otherwise the system library is used — the product never links a second
+// NCCL next to the framework's.
+#pragma once
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+
+namespace ngdb_dev {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
+  std::string error;  // non-empty: NCCL unavailable (why)
+};
+
+inline const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    bool ok = true;
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn) {
+        ok = false;
+        api.error += std::string(" missing ") + name;
+      }
+    };
+    sym(api.GetUniqueId, "ncclGetUniqueId");
+    sym(api.CommInitRank, "ncclCommInitRank");
+    sym(api.CommDestroy, "ncclCommDestroy");
+    sym(api.GroupStart, "ncclGroupStart");
+    sym(api.GroupEnd, "ncclGroupEnd");
+    sym(api.Send, "ncclSend");
+    sym(api.Recv, "ncclRecv");
+    sym(api.AllGather, "ncclAllGather");
+    sym(api.ReduceScatter, "ncclReduceScatter");
+    sym(api.AllReduce, "ncclAllReduce");
+    sym(api.GetErrorString, "ncclGetErrorString");
+    sym(api.GetVersion, "ncclGetVersion");
+    if (!ok) api.error = "libnccl.so.2:" + api.error;
+  });
+  return api;
+}
+
+}  // namespace ngdb_dev

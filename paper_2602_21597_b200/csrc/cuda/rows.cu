@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, 
     // FuseSemantic: the prologue's fused row of this anchor's entity
     // row-sharded: the row fetched from its owner into this anchor slot
     const float* src = a.fused      ? a.etab + static_cast<int64_t>(a.anchor_local[d.aux]) * a.ent_w
-                       : a.anc_rows ? a.anc_rows + static_cast<int64_t>(d.aux) * a.ent_w
+                       : a.anc_rows ? a.anc_rows + static_cast<int64_t>(a.anc_pos[d.aux]) * a.ent_w
                                     : a.ent + static_cast<int64_t>(d.id) * a.ent_w;
     FOR_CHUNKS(ew4) u[i] = ldg4(src + 4 * c);
     if (a.backbone == NGDB_BETAE) {  // realised (alpha | beta); the mirror's

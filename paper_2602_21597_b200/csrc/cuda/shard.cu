@@ -19,16 +19,15 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
 
-// owned rows of every rank's anchors -> send[q][a] (zeros where not owned)
+// lookup send: the owned rows every rank asked for, requester-major
+// (send[p] = local row send_rows[p]); one warp per row
 __global__ void shard_anchor_pack_kernel(DevArgs a, ShardDev sd, float* send) {
   pdl_start();
-  const int64_t slot = blockIdx.x;  // q * A + a
-  const int32_t e = sd.anchor_ids[slot];
-  float* dst = send + slot * a.ent_w;
-  const bool own = e >= 0 && e % sd.world == sd.rank;
-  const float* src = a.ent + static_cast<int64_t>(own ? e / sd.world : 0) * a.ent_w;
-  for (int c = threadIdx.x; c < a.ent_w / 4; c += blockDim.x)
-    st4(dst + 4 * c, own ? ld4(src + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f));
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * 4 + threadIdx.x / 32;
+  if (p >= sd.n_send) return;
+  const float* src = a.ent + static_cast<int64_t>(sd.send_rows[p]) * a.ent_w;
+  float* dst = send + p * a.ent_w;
+  for (int c = threadIdx.x & 31; c < a.ent_w / 4; c += 32) st4(dst + 4 * c, ld4(src + 4 * c));
 }
 
 // query tensors of a Score / Loss pool -> query_mine[slot]
@@ -61,6 +60,7 @@ __global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardD
   int gslot[3];
   for (int b = 0; b < 3; ++b)
     gslot[b] = b < k ? q * sd.max_slots + sd.unit_slots[static_cast<int64_t>(u) * 3 + b] : 0;
+  float* dq_blk = sd.dq_part + static_cast<int64_t>(q) * sd.dq_block;  // rank q's block
   for (int b = 0; b < k; ++b)
     for (int e = threadIdx.x; e < wq; e += kThreads)
       qs[b * wq + e] = sd.query_all[static_cast<int64_t>(gslot[b]) * wq + e];
@@ -130,12 +130,12 @@ __global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardD
     for (int e = threadIdx.x; e < wq; e += kThreads) {
       float v = 0.f;
       for (int w = 0; w < kWarps; ++w) v += part[(w * 3 + b) * wq + e];
-      sd.dq_part[static_cast<int64_t>(gslot[b]) * wq + e] = v;
+      dq_blk[static_cast<int64_t>(gslot[b] - q * sd.max_slots) * wq + e] = v;
     }
   if (threadIdx.x == 0) {
     float t = 0.f;
     for (int w = 0; w < kWarps; ++w) t += lred[w];
-    sd.loss_part[static_cast<int64_t>(q) * sd.batch + i] = t;
+    dq_blk[static_cast<int64_t>(sd.max_slots) * wq + i] = t;
   }
 }
 
@@ -153,16 +153,15 @@ __global__ void shard_score_done_kernel(DevArgs a, const float* dq_mine, int64_t
   }
 }
 
-// my anchors' gradient rows -> send[owner][slot]
-__global__ void shard_grad_pack_kernel(DevArgs a, ShardDev sd, int n_anchor, float* send) {
+// gradient return: my anchors' gradient rows in receive order (owner-major),
+// send[p] = agbuf[recv_slot[p]]; one warp per row
+__global__ void shard_grad_pack_kernel(DevArgs a, ShardDev sd, float* send) {
   pdl_start();
-  const int slot = blockIdx.x;
-  if (slot >= n_anchor) return;
-  const int32_t e = sd.anchor_ids[static_cast<int64_t>(sd.rank) * sd.max_anchors + slot];
-  const int owner = e % sd.world;
-  float* dst = send + (static_cast<int64_t>(owner) * sd.max_anchors + slot) * a.ent_w;
-  const float* g = a.agbuf + static_cast<int64_t>(slot) * a.ent_w;
-  for (int c = threadIdx.x; c < a.ent_w / 4; c += blockDim.x) st4(dst + 4 * c, ld4(g + 4 * c));
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * 4 + threadIdx.x / 32;
+  if (p >= sd.n_recv) return;
+  const float* g = a.agbuf + static_cast<int64_t>(sd.recv_slot[p]) * a.ent_w;
+  float* dst = send + p * a.ent_w;
+  for (int c = threadIdx.x & 31; c < a.ent_w / 4; c += 32) st4(dst + 4 * c, ld4(g + 4 * c));
 }
 
 // relation CSR rows -> dense relation gradient rows + touched flags
@@ -203,9 +202,9 @@ __global__ void masked_rows_adam_kernel(float* w, float* m, float* v, float* dbg
 }  // namespace
 
 int launch_shard_anchor_pack(const DevArgs& a, const ShardDev& sd, float* send, const LaunchCtx& lc) {
-  const int n = sd.world * sd.max_anchors;
-  if (n <= 0) return 0;
-  launch_pdl(shard_anchor_pack_kernel, dim3(n), dim3(128), 0, lc.stream, 1, a, sd, send);
+  if (sd.n_send <= 0) return 0;
+  launch_pdl(shard_anchor_pack_kernel, dim3((sd.n_send + 3) / 4), dim3(128), 0, lc.stream, 1, a,
+             sd, send);
   return 1;
 }
 
@@ -245,10 +244,10 @@ int launch_shard_score_done(const DevArgs& a, const float* dq_mine, int64_t n_dq
   return 1;
 }
 
-int launch_shard_grad_pack(const DevArgs& a, const ShardDev& sd, int n_anchor, float* send,
-                           const LaunchCtx& lc) {
-  if (n_anchor <= 0) return 0;
-  launch_pdl(shard_grad_pack_kernel, dim3(n_anchor), dim3(128), 0, lc.stream, 1, a, sd, n_anchor, send);
+int launch_shard_grad_pack(const DevArgs& a, const ShardDev& sd, float* send, const LaunchCtx& lc) {
+  if (sd.n_recv <= 0) return 0;
+  launch_pdl(shard_grad_pack_kernel, dim3((sd.n_recv + 3) / 4), dim3(128), 0, lc.stream, 1, a,
+             sd, send);
   return 1;
 }
 

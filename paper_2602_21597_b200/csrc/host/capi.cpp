@@ -412,6 +412,56 @@ int ngdb_shard_view(const ngdb_shard* s, ngdb_shard_plan* v) {
     v->rows = p.rows.data();
     v->seg = p.seg.data();
     v->contrib = p.contrib.data();
+    v->send_cnt = p.send_cnt.data();
+    v->recv_cnt = p.recv_cnt.data();
+    v->n_send = static_cast<int32_t>(p.send_rows.size());
+    v->n_recv = static_cast<int32_t>(p.recv_slot.size());
+    v->send_rows = p.send_rows.data();
+    v->recv_slot = p.recv_slot.data();
+    v->n_anchor_pos = static_cast<int32_t>(p.anchor_pos.size());
+    v->anchor_pos = p.anchor_pos.data();
+  });
+}
+
+int64_t ngdb_shard_meta_stride(int32_t batch_cap, int32_t n_candidates) {
+  return ngdb::shard_meta_stride(batch_cap, n_candidates);
+}
+
+int ngdb_step_shard_pack(const ngdb_step* s, int32_t batch_cap, int32_t* out, int64_t stride) {
+  return guarded([&] {
+    const auto& p = s->plan;
+    const int32_t nc = p.n_candidates, B = p.n_queries;
+    if (stride != ngdb::shard_meta_stride(batch_cap, nc))
+      throw ngdb::ShapeMismatch("shard metadata stride");
+    if (B > batch_cap || p.n_anchor_slots > 3 * batch_cap)
+      throw ngdb::ShapeMismatch("step exceeds the metadata record's batch capacity");
+    std::fill(out, out + stride, -1);
+    out[0] = p.n_anchor_slots;
+    out[1] = p.n_score_slots;
+    out[2] = B;
+    out[3] = nc;
+    int32_t* a = out + 4;
+    int32_t* k = a + 3 * int64_t(batch_cap);
+    int32_t* us = k + batch_cap;
+    int32_t* c = us + 3 * int64_t(batch_cap);
+    std::copy(p.anchor_ids.begin(), p.anchor_ids.end(), a);
+    std::copy(p.unit_k.begin(), p.unit_k.end(), k);
+    std::copy(p.unit_slots.begin(), p.unit_slots.end(), us);
+    std::copy(p.candidates.begin(), p.candidates.end(), c);
+  });
+}
+
+int ngdb_shard_build_packed(int32_t world, int32_t rank, const int32_t* gathered, int64_t stride,
+                            int32_t batch_cap, ngdb_shard** out) {
+  return guarded([&] {
+    auto* s = new ngdb_shard();
+    try {
+      s->plan = ngdb::build_shard_plan_packed(world, rank, gathered, stride, batch_cap);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
   });
 }
 

@@ -1,23 +1,32 @@
-"""Row-sharded training step over torch.distributed (
-BASELINE.json configs[4]: Query2Box on the ogbl-wikikg2 shape, 2/4/8 B200).
+"""Row-sharded training step (BASELINE.json
+configs[4]: Query2Box on the ogbl-wikikg2 shape, 2/4/8 B200).
 
 One process per GPU. Entity e lives on rank e mod G (local row e div G);
 relations and MLPs are replicated and their gradients all-reduced. Each rank
 plans its own batch with the host Max-Fillness planner (bit-exact per-rank
-trace); the device work runs in stages of ngdb_shard_run with the collectives
-between them, all on the framework stream the context is bound to:
+trace) and publishes ONE packed int32 metadata record (ngdb_step_shard_pack);
+the records are all-gathered and every rank builds its owner work lists
+(ngdb_shard_build_packed). The device step, in stages with the collectives
+between them:
 
-  anchors    reduce-scatter  owned rows of every rank's anchor ids
+  lookups    uneven all-to-all: each owner sends a rank exactly the rows of
+             that rank's anchors it owns
   forward    local pools (all but Score / UnionScore / Loss)
   scoring    all-gather of the score-slot queries; every rank scores the
-             candidates it owns for every rank's queries; reduce-scatter of
-             the partial dL/dq and losses back to the query's rank
+             candidates it owns for every rank's queries; ONE reduce-scatter
+             returns the partial dL/dq and partial losses to the query's rank
   backward   local pools
-  gradients  all-to-all of anchor-gradient rows to their owners, all-reduce
-             of dense + relation gradients, then owner-local Adam
+  gradients  the lookup all-to-all reversed (anchor-gradient rows to their
+             owners), all-reduce of dense + relation gradients, owner-local Adam
 
-`Comm` maps these onto NCCL device collectives; with the gloo backend (tests:
-two processes sharing one GPU) the same calls are staged through host memory.
+Transports (`Comm.transport`):
+  "nccl"  the context's own NCCL communicator (libngdb: ngdb_comm_init; the
+          stages + collectives + optimizer run inside ngdb_shard_step_exec or
+          a captured CUDA graph) — no framework collective on the data path;
+  "host"  the same collectives staged through host memory over the gloo group
+          (tests: two ranks sharing one GPU, where NCCL cannot run).
+torch.distributed (gloo) only carries the host metadata, the NCCL unique id
+and the benchmark's barrier / max-over-ranks timing.
 """
 from __future__ import annotations
 
@@ -31,6 +40,7 @@ from .engine import BACKBONES, Batch, PlannedStep, param_specs
 
 FORWARD_STAGES = {"anchor_pack": 0, "forward": 1, "query_pack": 2, "score": 3, "score_done": 4,
                   "backward": 5, "grad_pack": 6}
+NCCL_ID_BYTES = 128
 
 
 def _p(a, t):
@@ -38,34 +48,35 @@ def _p(a, t):
 
 
 class Comm:
-    """The five collectives of the sharded step over a torch.distributed group.
+    """Host side of the sharded step over a torch.distributed process group.
 
-    NCCL: device tensors straight into the NCCL collectives (NVLink/NVSwitch).
-    gloo: host-staged equivalents (used by the tests, where two ranks share one
-    GPU). Host metadata always travels over a gloo group."""
+    transport "nccl" (default when the default group is NCCL, or when asked):
+    device collectives run on the context's own NCCL communicator inside
+    libngdb; "host": host-staged equivalents over the gloo group (tests).
+    Host metadata always travels over a gloo group as packed int32 records."""
 
-    def __init__(self, group=None, meta_group=None):
+    def __init__(self, group=None, transport: Optional[str] = None):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.group = torch, dist, group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.nccl = dist.get_backend(group) == "nccl"
-        self.meta_group = meta_group if meta_group is not None else (
-            dist.new_group(backend="gloo") if self.nccl else group)
+        backend = dist.get_backend(group)
+        self.transport = transport or ("nccl" if backend == "nccl" else "host")
+        if self.transport not in ("nccl", "host"):
+            raise ValueError(f"unknown transport {self.transport!r}")
+        self.meta_group = group if backend == "gloo" else dist.new_group(backend="gloo")
 
-    # -- device tensors ---------------------------------------------------------
+    @property
+    def nccl(self) -> bool:
+        return self.transport == "nccl"
+
+    # -- host-staged device collectives (transport "host") ----------------------
     def all_gather(self, out, inp):
-        if self.nccl:
-            self.dist.all_gather_into_tensor(out, inp, group=self.group)
-            return
         parts = self._gather_host(inp)
         out.copy_(self.torch.cat(parts).to(out.device))
 
     def reduce_scatter(self, out, inp):
-        if self.nccl:
-            self.dist.reduce_scatter_tensor(out, inp, group=self.group)
-            return
         n = out.numel()
         parts = self._gather_host(inp)
         acc = parts[0][self.rank * n:(self.rank + 1) * n].clone()
@@ -73,19 +84,28 @@ class Comm:
             acc += parts[q][self.rank * n:(self.rank + 1) * n]
         out.copy_(acc.to(out.device))
 
-    def all_to_all(self, out, inp):
-        if self.nccl:
-            self.dist.all_to_all_single(out, inp, group=self.group)
-            return
-        n = out.numel() // self.world
-        parts = self._gather_host(inp)
-        out.copy_(self.torch.cat([parts[q][self.rank * n:(self.rank + 1) * n]
-                                  for q in range(self.world)]).to(out.device))
+    def all_to_all_v(self, out, inp, send_counts, recv_counts):
+        """Uneven all-to-all: send_counts[q] elements of `inp` (rank-major) go
+        to rank q; recv_counts[q] elements from rank q land in `out`."""
+        sc = [int(x) for x in send_counts]
+        rc = [int(x) for x in recv_counts]
+        cap = int(self.all_gather_i32(np.asarray([sum(sc)], np.int32)).max())
+        buf = self.torch.zeros(max(1, cap), dtype=self.torch.float32)
+        buf[:sum(sc)] = inp.detach().view(-1)[:sum(sc)].to("cpu")
+        parts = [self.torch.empty_like(buf) for _ in range(self.world)]
+        self.dist.all_gather(parts, buf, group=self.meta_group)
+        counts = self.all_gather_i32(np.asarray(sc, np.int32)).reshape(self.world, self.world)
+        pieces = []
+        for q in range(self.world):  # rank q's block addressed to me
+            if int(counts[q, self.rank]) != rc[q]:
+                raise RuntimeError("all_to_all_v: send/receive counts disagree")
+            off = int(counts[q, :self.rank].sum())
+            pieces.append(parts[q][off:off + rc[q]])
+        res = self.torch.cat(pieces)
+        if res.numel():
+            out.view(-1)[:res.numel()].copy_(res.to(out.device))
 
     def all_reduce(self, t):
-        if self.nccl:
-            self.dist.all_reduce(t, group=self.group)
-            return
         parts = self._gather_host(t)
         acc = parts[0].clone()
         for q in range(1, self.world):
@@ -95,14 +115,23 @@ class Comm:
     def _gather_host(self, t):
         h = t.detach().to("cpu")
         parts = [self.torch.empty_like(h) for _ in range(self.world)]
-        self.dist.all_gather(parts, h, group=self.group)
+        self.dist.all_gather(parts, h, group=self.meta_group)
         return parts
 
     # -- host metadata ----------------------------------------------------------
-    def all_gather_object(self, obj):
-        out = [None] * self.world
-        self.dist.all_gather_object(out, obj, group=self.meta_group)
-        return out
+    def all_gather_i32(self, rec: np.ndarray) -> np.ndarray:
+        """All-gather one fixed-size int32 record per rank -> [world * n] (rank-major)."""
+        t = self.torch.from_numpy(np.ascontiguousarray(rec, np.int32))
+        parts = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t, group=self.meta_group)
+        return self.torch.cat(parts).numpy()
+
+    def broadcast_bytes(self, data: bytes, n: int) -> bytes:
+        t = self.torch.zeros(n, dtype=self.torch.uint8)
+        if self.rank == 0:
+            t[:] = self.torch.frombuffer(bytearray(data), dtype=self.torch.uint8)
+        self.dist.broadcast(t, 0, group=self.meta_group)
+        return bytes(t.numpy().tobytes())
 
 
 def _device_view(torch, ptr, n):
@@ -111,6 +140,11 @@ def _device_view(torch, ptr, n):
         __cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f4",
                                     "data": (int(ptr), False), "version": 3, "strides": None}
     return torch.as_tensor(_CAI(), device="cuda")
+
+
+def _arr(ptr, n):
+    return np.ctypeslib.as_array(ptr, (max(int(n), 1),))[:int(n)].copy() if n else \
+        np.zeros(0, np.int32)
 
 
 class ShardStep:
@@ -125,66 +159,48 @@ class ShardStep:
         check(lib.ngdb_shard_view(self._h, C.byref(s)))
         return v, s
 
+    def counts(self):
+        """(send_cnt, recv_cnt) rows of the lookup all-to-all, per rank."""
+        _, s = self.views()
+        return _arr(s.send_cnt, s.world), _arr(s.recv_cnt, s.world)
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib.ngdb_shard_destroy(self._h)
             self._h = None
 
 
-def _local_meta(ps: PlannedStep):
-    """This rank's scoring metadata of a planned step (host arrays)."""
-    na, ns, b, nc = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
-    check(lib.ngdb_step_shard_info(ps._h, C.byref(na), C.byref(ns), C.byref(b), C.byref(nc)))
-    anchors = np.zeros(na.value, np.int32)
-    unit_k = np.zeros(b.value, np.int32)
-    unit_slots = np.zeros(b.value * 3, np.int32)
-    cand = np.zeros(b.value * nc.value, np.int32)
-    check(lib.ngdb_step_shard_meta(ps._h, _p(anchors, C.c_int32), _p(unit_k, C.c_int32),
-                                   _p(unit_slots, C.c_int32), _p(cand, C.c_int32)))
-    return (anchors, unit_k, unit_slots, cand, ns.value), b.value, nc.value
+def _local_meta(ps: PlannedStep, batch_cap: int):
+    """This rank's packed metadata record (ngdb_step_shard_pack)."""
+    nc = ps.view().n_candidates
+    stride = int(lib.ngdb_shard_meta_stride(batch_cap, nc))
+    rec = np.empty(stride, np.int32)
+    check(lib.ngdb_step_shard_pack(ps._h, batch_cap, _p(rec, C.c_int32), stride))
+    return rec, batch_cap
 
 
 def _gather_meta(comm: Comm, local):
-    """All-gather the ranks' scoring metadata (gloo, ordered per step) and pad
-    it into the dense [G][...] arrays of ngdb_shard_build."""
-    mine, b, nc = local
-    meta = comm.all_gather_object(mine)
-    G = comm.world
-    A = max(1, max(m[0].size for m in meta))
-    S = max(1, max(m[4] for m in meta))
-    B = max(m[1].size for m in meta)
-    anc_all = np.full((G, A), -1, np.int32)
-    k_all = np.zeros((G, B), np.int32)
-    slots_all = np.full((G, B, 3), -1, np.int32)
-    cand_all = np.zeros((G, B, nc), np.int32)
-    for q, (an, uk, us, ca, _) in enumerate(meta):
-        bq = uk.size
-        anc_all[q, :an.size] = an
-        k_all[q, :bq] = uk
-        slots_all[q, :bq] = us.reshape(bq, 3)
-        cand_all[q, :bq] = ca.reshape(bq, nc)
-    return (G, comm.rank, B, A, S, nc, anc_all, k_all, slots_all, cand_all), b
+    """All-gather the ranks' packed records (gloo, one int32 tensor per rank)."""
+    rec, batch_cap = local
+    return comm.all_gather_i32(rec), rec.size, batch_cap, comm.world, comm.rank
 
 
 def _build_shard_step(ps: PlannedStep, gathered) -> ShardStep:
     """Owner work lists of this rank (C++; releases the GIL)."""
-    (G, rank, B, A, S, nc, anc_all, k_all, slots_all, cand_all), b = gathered
+    allrec, stride, batch_cap, world, rank = gathered
     h = C.c_void_p()
-    check(lib.ngdb_shard_build(G, rank, B, A, S, nc, _p(anc_all, C.c_int32),
-                               _p(k_all, C.c_int32), _p(slots_all, C.c_int32),
-                               _p(cand_all, C.c_int32), C.byref(h)))
-    return ShardStep(ps, h, b)
+    check(lib.ngdb_shard_build_packed(world, rank, _p(allrec, C.c_int32), stride, batch_cap,
+                                      C.byref(h)))
+    return ShardStep(ps, h, ps.view().n_queries)
 
 
-def _finish_shard_step(comm: Comm, ps: PlannedStep, local) -> ShardStep:
-    """Exchange the metadata (gloo all-gather) and build the owner work lists."""
-    return _build_shard_step(ps, _gather_meta(comm, local))
-
-
-def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: int = 512) -> ShardStep:
-    """Plan this rank's batch, exchange the metadata, build the owner work lists."""
+def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: int = 512,
+                    batch_cap: Optional[int] = None) -> ShardStep:
+    """Plan this rank's batch, exchange the packed metadata, build the owner lists.
+    batch_cap (the record's query capacity) must be the same on every rank."""
     ps = PlannedStep(batch, backbone, dim, b_max, sharded=True)
-    return _finish_shard_step(comm, ps, _local_meta(ps))
+    cap = batch_cap or ps.view().n_queries
+    return _build_shard_step(ps, _gather_meta(comm, _local_meta(ps, cap)))
 
 
 class ShardedEngine:
@@ -199,6 +215,7 @@ class ShardedEngine:
             raise NotImplementedError("row-sharded step: GQE / Q2B")
         self.torch, self.comm = torch, comm
         self.backbone, self.dim, self.b_max = backbone, dim, b_max
+        self.max_queries = max_queries
         self.n_entities, self.n_relations = n_entities, n_relations
         G, r = comm.world, comm.rank
         d = ModelDesc(BACKBONES[backbone], n_entities, n_relations, dim, n_neg, 0, gamma,
@@ -206,10 +223,17 @@ class ShardedEngine:
         self._h = C.c_void_p()
         check(lib.ngdb_ctx_create(C.byref(d), device, C.byref(self._h)))
         torch.cuda.set_device(device)
-        # one explicit stream carries the context's kernels AND the collectives
-        # (the legacy default stream would not order against the context)
+        # one explicit stream carries the context's kernels (and, for the host
+        # transport, the torch copies staging the collectives)
         self.stream = torch.cuda.Stream(device=device)
         check(lib.ngdb_ctx_set_stream(self._h, C.c_void_p(self.stream.cuda_stream)))
+        if comm.nccl:  # the context's own communicator: rank 0's id over gloo
+            uid = (C.c_uint8 * NCCL_ID_BYTES)()
+            if r == 0:
+                check(lib.ngdb_comm_unique_id(uid))
+            got = comm.broadcast_bytes(bytes(uid), NCCL_ID_BYTES)
+            uid = (C.c_uint8 * NCCL_ID_BYTES).from_buffer_copy(got)
+            check(lib.ngdb_comm_init(self._h, uid))
         self.n_local = (n_entities - r + G - 1) // G
         for name, rows, cols, _ in param_specs(backbone, n_entities, n_relations, dim):
             if name == "entity":
@@ -240,23 +264,27 @@ class ShardedEngine:
         return out
 
     def plan(self, batch: Batch) -> ShardStep:
-        return plan_shard_step(self.comm, batch, self.backbone, self.dim, self.b_max)
+        return plan_shard_step(self.comm, batch, self.backbone, self.dim, self.b_max,
+                               self.max_queries)
+
+    def _enqueue(self, step: ShardStep, step_no: int) -> None:
+        """begin + stages + collectives + optimizer of one step, enqueued."""
+        v, s = step.views()
+        b = ShardBuffers()
+        with self.torch.cuda.stream(self.stream):
+            check(lib.ngdb_shard_begin(self._h, C.byref(v), C.byref(s), C.byref(b)))
+            if self.comm.nccl:
+                check(lib.ngdb_shard_step_exec(self._h, step_no))
+            else:
+                _host_stages(self, b, _arr(s.send_cnt, s.world), _arr(s.recv_cnt, s.world))
+                check(lib.ngdb_shard_optimizer(self._h, step_no))
 
     def run(self, step: ShardStep, step_no: Optional[int] = None) -> np.ndarray:
         """All stages + collectives of one step; returns this rank's per-query losses."""
         if step_no is None:
             self.step_count += 1
             step_no = self.step_count
-        with self.torch.cuda.stream(self.stream):
-            return self._run(step, step_no)
-
-    def _run(self, step: ShardStep, step_no: int) -> np.ndarray:
-        v, s = step.views()
-        b = ShardBuffers()
-        check(lib.ngdb_shard_begin(self._h, C.byref(v), C.byref(s), C.byref(b)))
-        t = {n: _device_view(self.torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
-        _stages(self, t)
-        check(lib.ngdb_shard_optimizer(self._h, step_no))
+        self._enqueue(step, step_no)
         losses = np.zeros(step.n_queries, np.float32)
         total, nonfinite = C.c_double(), C.c_int32()
         check(lib.ngdb_step_end(self._h, _p(losses, C.c_float), step.n_queries, C.byref(total),
@@ -269,33 +297,30 @@ class ShardedEngine:
         return self.run(self.plan(batch))
 
     def _launch(self, step: ShardStep, step_no: int) -> int:
-        """All stages + collectives of one step, enqueued; returns the ticket of
-        its asynchronous loss read-back (ngdb_step_end_async)."""
-        with self.torch.cuda.stream(self.stream):
-            v, s = step.views()
-            b = ShardBuffers()
-            check(lib.ngdb_shard_begin(self._h, C.byref(v), C.byref(s), C.byref(b)))
-            t = {n: _device_view(self.torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
-            _stages(self, t)
-            check(lib.ngdb_shard_optimizer(self._h, step_no))
-            ticket = C.c_int64()
-            check(lib.ngdb_step_end_async(self._h, C.byref(ticket)))
+        """One step enqueued; returns the ticket of its asynchronous loss
+        read-back (ngdb_step_end_async)."""
+        self._enqueue(step, step_no)
+        ticket = C.c_int64()
+        check(lib.ngdb_step_end_async(self._h, C.byref(ticket)))
         return ticket.value
 
     def train(self, graph, weights, n_steps: int, batch: int, n_neg: int, tag_of,
               producers: int = 8) -> np.ndarray:
         """Pipelined sharded trainer loop (the sharded counterpart of
         ngdb_train_run): host threads sample + plan upcoming batches (the C++
-        calls release the GIL), the calling thread exchanges each step's
-        metadata, builds its owner lists, enqueues its stages and collectives,
-        and reads step i's losses back while step i+1 runs. Batch of step s is
-        Rng(3).fork(tag_of(s)). Returns the per-step loss sums of this rank."""
+        calls release the GIL), one ordered thread all-gathers each step's
+        packed metadata record, the pool builds the owner lists, and the
+        calling thread enqueues the step (stages + NCCL collectives + Adam in
+        libngdb) and reads step i's losses back while step i+1 runs. Batch of
+        step s is Rng(3).fork(tag_of(s)). Returns the per-step loss sums of this
+        rank."""
         import concurrent.futures as cf
+        cap = self.max_queries
 
         def prep(s):
             b = Batch.sample(graph, weights, batch, n_neg, seed=3, tag=tag_of(s))
             ps = PlannedStep(b, self.backbone, self.dim, self.b_max, sharded=True)
-            return ps, _local_meta(ps)
+            return ps, _local_meta(ps, cap)
 
         sums = np.zeros(n_steps, np.float64)
         losses = np.zeros(batch, np.float32)
@@ -312,7 +337,7 @@ class ShardedEngine:
             sums[i] = total.value
 
         # three stages ahead of the launching thread: sample + plan (pool), the
-        # ordered metadata all-gather (one thread: collectives run in step
+        # ordered metadata all-gather (one thread: the gloo calls run in step
         # order on every rank), owner lists (pool)
         with cf.ThreadPoolExecutor(producers) as pool, cf.ThreadPoolExecutor(1) as exch:
             def gather(s, prep_fut):
@@ -345,11 +370,12 @@ class ShardedEngine:
         return sums
 
     def capture(self, steps: List[ShardStep]) -> List["ShardGraph"]:
-        """Resident copies of `steps` whose stages AND collectives replay as one
-        CUDA graph each (NCCL only; the communicator must have run eagerly
-        first). Every resident step is created — and the context's buffers
-        sized for all of them — before the first capture, so no later growth
-        invalidates a captured graph."""
+        """Resident copies of `steps`, each captured with its NCCL collectives
+        into one CUDA graph by libngdb (ngdb_shard_step_capture). Every resident
+        step is created — and the context's buffers sized for all of them —
+        before the first capture, so no later growth invalidates a graph."""
+        if not self.comm.nccl:
+            raise RuntimeError("graph capture of the sharded step needs the NCCL transport")
         handles = []
         for st in steps:
             v, s = st.views()
@@ -371,29 +397,18 @@ class ShardedEngine:
 class ShardGraph:
     """A resident sharded step (ngdb_shard_step_create: plan + owner lists in
     device memory, buffers sized up front) captured with its NCCL collectives
-    into one CUDA graph on the engine's stream. replay(step_no) sets the Adam
+    into one CUDA graph (ngdb_shard_step_capture). replay(step_no) sets the Adam
     step scalars and launches the graph: no host work per stage."""
 
     def __init__(self, eng: ShardedEngine, handle, n_queries: int):
-        self._h = handle  # owned from here on (destroyed with the graph)
-        if not eng.comm.nccl:
-            raise RuntimeError("graph capture of the sharded step needs the NCCL backend")
-        torch = eng.torch
+        self._h = handle  # owned from here on
         self.eng = eng
         self.n_queries = n_queries
-        self.graph = torch.cuda.CUDAGraph()
-        torch.cuda.synchronize()
-        with torch.cuda.graph(self.graph, stream=eng.stream):
-            b = ShardBuffers()
-            check(lib.ngdb_shard_step_begin(eng._h, self._h, C.byref(b)))
-            t = {n: _device_view(torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
-            _stages(eng, t)
-            check(lib.ngdb_shard_optimizer(eng._h, 0))
+        eng.torch.cuda.synchronize()
+        check(lib.ngdb_shard_step_capture(eng._h, self._h))
 
     def replay(self, step_no: int) -> None:
-        check(lib.ngdb_set_step(self.eng._h, step_no))
-        with self.eng.torch.cuda.stream(self.eng.stream):
-            self.graph.replay()
+        check(lib.ngdb_shard_step_replay(self.eng._h, self._h, step_no))
 
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:
@@ -401,28 +416,31 @@ class ShardGraph:
             self._h = None
 
 
-def _stages(eng: ShardedEngine, t) -> None:
-    """The device stages of a sharded step with the collectives between them."""
+def _host_stages(eng: ShardedEngine, b: ShardBuffers, send_cnt, recv_cnt) -> None:
+    """The device stages with host-staged collectives between them (transport
+    "host"; the NCCL transport runs the same sequence inside libngdb)."""
+    t = {n: _device_view(eng.torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
     run = lambda stage: check(lib.ngdb_shard_run(eng._h, FORWARD_STAGES[stage]))  # noqa: E731
     comm = eng.comm
+    ew = eng.dim  # GQE / Q2B entity rows are d wide
     run("anchor_pack")
-    comm.reduce_scatter(t["anchor_rows"], t["anchor_send"])
+    comm.all_to_all_v(t["anchor_rows"], t["anchor_send"], send_cnt * ew, recv_cnt * ew)
     run("forward")
     run("query_pack")
     comm.all_gather(t["query_all"], t["query_mine"])
     run("score")
     comm.reduce_scatter(t["dq_mine"], t["dq_part"])
-    comm.reduce_scatter(t["loss_mine"], t["loss_part"])
     run("score_done")
     run("backward")
     run("grad_pack")
-    comm.all_to_all(t["grad_all"], t["grad_send"])
+    comm.all_to_all_v(t["grad_all"], t["grad_send"], recv_cnt * ew, send_cnt * ew)
     comm.all_reduce(t["reduce"])
 
 
 def gather_entity_table(comm: Comm, local: np.ndarray, n_entities: int) -> Optional[np.ndarray]:
     """Reassemble the full entity table (rank 0 gets it; others None)."""
-    parts = comm.all_gather_object(local)
+    parts = [None] * comm.world
+    comm.dist.all_gather_object(parts, local, group=comm.meta_group)
     if comm.rank != 0:
         return None
     out = np.zeros((n_entities, local.shape[1]), np.float32)

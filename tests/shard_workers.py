@@ -43,6 +43,11 @@ def host_plan_worker(rank, world, port, out_dir, shape, mix, b, k, dim):
     }
     plan["contrib"] = np.ctypeslib.as_array(s.contrib, (max(int(plan["seg"][-1]), 1),))[
         : int(plan["seg"][-1])].copy()
+    from paper_2602_21597_b200.sharded import _arr
+    plan["send_cnt"], plan["recv_cnt"] = _arr(s.send_cnt, s.world), _arr(s.recv_cnt, s.world)
+    plan["send_rows"] = _arr(s.send_rows, s.n_send)
+    plan["recv_slot"] = _arr(s.recv_slot, s.n_recv)
+    plan["anchor_pos"] = _arr(s.anchor_pos, s.n_anchor_pos)
     plan["n_score_slots"] = v.n_score_slots
     # collectives (host-staged path) on CPU tensors
     x = torch.arange(6, dtype=torch.float32) + 10 * rank
@@ -50,8 +55,11 @@ def host_plan_worker(rank, world, port, out_dir, shape, mix, b, k, dim):
     comm.all_gather(ag, x)
     rs = torch.zeros(6 // world)
     comm.reduce_scatter(rs, x)
-    a2a = torch.zeros(6)
-    comm.all_to_all(a2a, x)
+    # uneven all-to-all: rank r sends r+1 elements to rank 0 and 2-r to rank 1
+    sc = [rank + 1, 2 - rank]
+    rc = [q + 1 if rank == 0 else 2 - q for q in range(world)]
+    a2a = torch.zeros(sum(rc))
+    comm.all_to_all_v(a2a, x, sc, rc)
     ar = x.clone()
     comm.all_reduce(ar)
     plan["coll"] = {"ag": ag.numpy(), "rs": rs.numpy(), "a2a": a2a.numpy(), "ar": ar.numpy()}
@@ -101,11 +109,11 @@ def graph_replay_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2602_21597_b200 as m
     from paper_2602_21597_b200.sharded import Comm, ShardedEngine, plan_shard_step
 
-    comm = Comm()
+    comm = Comm(transport="nccl")  # the context's own NCCL communicator
     g = m.Graph.synthetic(shape, 1)
     info = g.info()
     w = m.pattern_weights(mix)
@@ -139,13 +147,13 @@ def train_loop_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     import numpy as np
 
     import paper_2602_21597_b200 as m
     from paper_2602_21597_b200.sharded import Comm, ShardedEngine, plan_shard_step
 
-    comm = Comm()
+    comm = Comm(transport="nccl")
     g = m.Graph.synthetic(shape, 1)
     info = g.info()
     w = m.pattern_weights(mix)
@@ -169,5 +177,36 @@ def train_loop_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, 
     out["seq_sums"] = seq
     out["loop_sums"] = sums.tolist()
     with open(os.path.join(out_dir, f"loop{rank}.pkl"), "wb") as f:
+        pickle.dump(out, f)
+    dist.destroy_process_group()
+
+
+def transport_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
+    """One rank on GPU 0: the same steps through the context's NCCL transport
+    (ngdb_shard_step_exec: uneven all-to-alls, all-gather, reduce-scatter,
+    all-reduce inside libngdb) and through the host-staged transport."""
+    import torch
+    dist = _init(rank, world, port)
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200.sharded import Comm, ShardedEngine
+
+    g = m.Graph.synthetic(shape, 1)
+    info = g.info()
+    w = m.pattern_weights(mix)
+    out = {}
+    for transport in ("host", "nccl"):
+        comm = Comm(transport=transport)
+        eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
+                            n_neg=k, max_queries=b)
+        losses = []
+        for s in range(steps):
+            batch = m.Batch.sample(g, w, b, k, seed=3, tag=(s + 1) * world + rank)
+            losses.append(eng.train_step(batch))
+        torch.cuda.synchronize()
+        out[transport] = {"loss": losses,
+                          "params": {n: eng.download(n) for n, *_ in m.param_specs(
+                              backbone, info["n_entities"], info["n_relations"], dim)}}
+        del eng
+    with open(os.path.join(out_dir, f"transport{rank}.pkl"), "wb") as f:
         pickle.dump(out, f)
     dist.destroy_process_group()

@@ -106,3 +106,20 @@ def test_sharded_train_loop_matches_steps(tmp_path):
     for name, v in out["seq"].items():
         assert np.array_equal(v, out["loop"][name]), name
     np.testing.assert_allclose(out["loop_sums"], out["seq_sums"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("backbone,dim", [("q2b", 400), ("gqe", 32)])
+def test_nccl_transport_matches_host_transport(tmp_path, backbone, dim):
+    # the libngdb NCCL path (ngdb_shard_step_exec) and the host-staged path run
+    # the same stages over the same exchange layouts: bit-identical results
+    import torch.multiprocessing as mp
+
+    import shard_workers
+    mp.spawn(shard_workers.transport_worker,
+             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, dim, 3, backbone),
+             nprocs=1, join=True)
+    out = pickle.load(open(tmp_path / "transport0.pkl", "rb"))
+    for a, b in zip(out["host"]["loss"], out["nccl"]["loss"]):
+        assert np.array_equal(a, b)
+    for name, v in out["host"]["params"].items():
+        assert np.array_equal(v, out["nccl"]["params"][name]), name

@@ -39,7 +39,9 @@ def test_collectives_host_staged(plans):
         c = p["coll"]
         assert np.array_equal(c["ag"], np.concatenate(x))
         assert np.array_equal(c["rs"], (x[0] + x[1])[3 * r:3 * r + 3])
-        assert np.array_equal(c["a2a"], np.concatenate([x[0][3 * r:3 * r + 3], x[1][3 * r:3 * r + 3]]))
+        # rank q sends [q+1, 2-q] elements (rank-major) -> rank r gets q's block r
+        blocks = [np.split(x[q][:3], [q + 1]) for q in range(2)]
+        assert np.array_equal(c["a2a"], np.concatenate([blocks[q][r] for q in range(2)]))
         assert np.array_equal(c["ar"], x[0] + x[1])
 
 
@@ -74,17 +76,51 @@ def test_owner_csr_partitions_contributions(plans):
         for i, lr in enumerate(rows):
             ent = lr * G + r  # local row -> global entity
             for code in con[seg[i]:seg[i + 1]]:
-                if code < 0:
-                    q, a = divmod(-code - 1, A)
-                    assert p0["anchor_ids"][q * A + a] == ent
+                if code < 0:  # anchor row sent at lookup position -code-1
+                    assert p["send_rows"][-code - 1] == lr
                 else:
                     gslot, j = divmod(code, nc)
                     q, slot = divmod(gslot, S)
                     units = np.where((p0["unit_slots"].reshape(G * B, 3)[q * B:(q + 1) * B] == slot).any(1))[0]
                     assert len(units) == 1
                     assert p0["cand"].reshape(G * B, nc)[q * B + units[0], j] == ent
-                codes.append(code)
+                codes.append((r, code) if code < 0 else code)  # send positions are per rank
     assert len(codes) == len(set(codes))
     n_anchor = int((p0["anchor_ids"] >= 0).sum())
     n_cand = int(sum(p0["unit_k"][u] * nc for u in range(G * B)))
     assert len(codes) == n_anchor + n_cand
+
+
+def test_lookup_exchange_lists(plans):
+    # the uneven all-to-all carries exactly the owned rows: owner q's block for
+    # rank r lists r's anchors owned by q in slot order; r places them by
+    # recv_slot / anchor_pos; counts agree on both sides
+    G = 2
+    p0 = plans[0]
+    A = p0["A"]
+    anc = p0["anchor_ids"].reshape(G, A)
+    for q in range(G):
+        for r in range(G):
+            assert plans[q]["send_cnt"][r] == plans[r]["recv_cnt"][q]
+    for r, p in enumerate(plans):
+        assert len(p["send_rows"]) == p["send_cnt"].sum()
+        assert len(p["recv_slot"]) == p["recv_cnt"].sum()
+        mine = anc[r][anc[r] >= 0]
+        assert len(p["recv_slot"]) == len(mine)
+        # anchor_pos inverts recv_slot
+        for pos, slot in enumerate(p["recv_slot"]):
+            assert p["anchor_pos"][slot] == pos
+        # receive order = owner-major, slots ascending within an owner
+        off = 0
+        for q in range(G):
+            n = p["recv_cnt"][q]
+            slots = p["recv_slot"][off:off + n]
+            assert np.all(np.diff(slots) > 0)
+            assert np.all(anc[r][slots] % G == q)
+            # owner q sends the same rows in the same order
+            soff = int(plans[q]["send_cnt"][:r].sum())
+            rows = plans[q]["send_rows"][soff:soff + n]
+            assert np.array_equal(rows * G + q, anc[r][slots])
+            off += n
+    # only owned rows travel: total rows sent = anchors of all ranks
+    assert sum(len(p["send_rows"]) for p in plans) == int((anc >= 0).sum())
