@@ -17,8 +17,14 @@ HEADERS   := $(wildcard include/ngdb/*.hpp include/ngdb/*.h) $(wildcard $(PKG)/c
 
 LIB       := $(LIBDIR)/libngdb_b200.so
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib oracle examples clean
+all: lib oracle examples
+
+# C++ driver of the row-sharded step (no Python): links the product library
+EXAMPLES := $(LIBDIR)/sharded_train
+examples: $(EXAMPLES)
+$(LIBDIR)/sharded_train: tools/cpp/sharded_train.cpp $(LIB) $(HEADERS)
+	$(CXX) $(CXXFLAGS) $< -o $@ -L$(LIBDIR) -lngdb_b200 -Wl,-rpath,'$$ORIGIN'
 
 lib: $(LIB)
 

@@ -260,7 +260,10 @@ int ngdb_shard_step_destroy(ngdb_shard_step* step);
 int ngdb_comm_unique_id(uint8_t* id);
 int ngdb_comm_init(ngdb_ctx* ctx, const uint8_t* id);
 /* Host all-gather of `count` int32 per rank (the packed step metadata of
- * ngdb_step_shard_pack), ordered on the context stream; synchronous. */
+ * ngdb_step_shard_pack) over the context's metadata communicator (split from
+ * the step communicator, own stream): synchronous, and safe to call from ONE
+ * exchange thread while another thread launches steps (call order must be the
+ * same on every rank). */
 int ngdb_comm_allgather_i32(ngdb_ctx* ctx, const int32_t* send, int64_t count, int32_t* recv);
 /* The whole active sharded step (after ngdb_shard_begin / ngdb_shard_step_begin):
  * stages, NCCL collectives (uneven all-to-alls of owned rows, all-gather,

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -206,6 +207,7 @@ struct ngdb_ctx {
   // metadata all-gather of upcoming steps on its own stream (another thread)
   ncclComm_t comm = nullptr, meta_comm = nullptr;
   cudaStream_t meta_stream = nullptr;
+  std::mutex meta_mu;
   int32_t* meta_dev = nullptr;
   int64_t meta_cap = 0;
   float* istash = nullptr;           // Intersect stash (DevArgs::istash)
@@ -2346,25 +2348,34 @@ int ngdb_comm_init(ngdb_ctx* c, const uint8_t* id) {
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof(u));
     nck(n.CommInitRank(&c->comm, c->world, u, c->rank), "ncclCommInitRank");
+    // the metadata channel: same ranks, its own communicator and stream, so an
+    // exchange thread can all-gather upcoming steps' records while this
+    // thread's step collectives are in flight
+    nck(n.CommSplit(c->comm, 0, c->rank, &c->meta_comm, nullptr), "ncclCommSplit");
+    CK(cudaStreamCreateWithFlags(&c->meta_stream, cudaStreamNonBlocking));
   });
 }
 
 int ngdb_comm_allgather_i32(ngdb_ctx* c, const int32_t* send, int64_t count, int32_t* recv) {
   return guarded([&] {
-    if (!c->comm) throw Fail{NGDB_ERR_CONFIG, "ngdb_comm_allgather_i32: call ngdb_comm_init first"};
+    if (!c->meta_comm) throw Fail{NGDB_ERR_CONFIG, "ngdb_comm_allgather_i32: call ngdb_comm_init first"};
+    std::lock_guard<std::mutex> lock(c->meta_mu);
+    CK(cudaSetDevice(c->device));
     const int64_t need = count * (c->world + 1);
     if (need > c->meta_cap) {
-      CK(cudaStreamSynchronize(c->stream));
+      CK(cudaStreamSynchronize(c->meta_stream));
       if (c->meta_dev) CK(cudaFree(c->meta_dev));
+      c->meta_dev = nullptr;
+      CK(cudaMalloc(&c->meta_dev, need * sizeof(int32_t)));
       c->meta_cap = need;
-      c->meta_dev = dmalloc<int32_t>(need);
     }
     int32_t* dsend = c->meta_dev + count * c->world;
-    CK(cudaMemcpyAsync(dsend, send, count * 4, cudaMemcpyHostToDevice, c->stream));
-    nck(nccl_api().AllGather(dsend, c->meta_dev, size_t(count), ncclInt32, c->comm, c->stream),
-        "ncclAllGather");
-    CK(cudaMemcpyAsync(recv, c->meta_dev, count * c->world * 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(dsend, send, count * 4, cudaMemcpyHostToDevice, c->meta_stream));
+    nck(nccl_api().AllGather(dsend, c->meta_dev, size_t(count), ncclInt32, c->meta_comm,
+                             c->meta_stream), "ncclAllGather");
+    CK(cudaMemcpyAsync(recv, c->meta_dev, count * c->world * 4, cudaMemcpyDeviceToHost,
+                       c->meta_stream));
+    CK(cudaStreamSynchronize(c->meta_stream));
   });
 }
 

@@ -22,6 +22,7 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -58,6 +59,7 @@ inline const NcclApi& nccl_api() {
     sym(api.GetUniqueId, "ncclGetUniqueId");
     sym(api.CommInitRank, "ncclCommInitRank");
     sym(api.CommDestroy, "ncclCommDestroy");
+    sym(api.CommSplit, "ncclCommSplit");
     sym(api.GroupStart, "ncclGroupStart");
     sym(api.GroupEnd, "ncclGroupEnd");
     sym(api.Send, "ncclSend");

@@ -210,3 +210,24 @@ def transport_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, b
     with open(os.path.join(out_dir, f"transport{rank}.pkl"), "wb") as f:
         pickle.dump(out, f)
     dist.destroy_process_group()
+
+
+def python_sums_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
+    """One rank on GPU 0 through ShardedEngine (NCCL transport): per-step loss
+    sums of the batches tagged (s+1)*world + rank (the C++ driver's convention)."""
+    import numpy as np
+    dist = _init(rank, world, port)
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200.sharded import Comm, ShardedEngine
+
+    g = m.Graph.synthetic(shape, 1)
+    info = g.info()
+    w = m.pattern_weights(mix)
+    eng = ShardedEngine(Comm(transport="nccl"), backbone, info["n_entities"], info["n_relations"],
+                        dim=dim, n_neg=k, max_queries=b)
+    sums = [float(np.sum(eng.train_step(m.Batch.sample(g, w, b, k, seed=3,
+                                                         tag=(s + 1) * world + rank)),
+                         dtype=np.float64)) for s in range(steps)]
+    with open(os.path.join(out_dir, f"pysums{rank}.pkl"), "wb") as f:
+        pickle.dump(sums, f)
+    dist.destroy_process_group()

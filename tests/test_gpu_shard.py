@@ -123,3 +123,26 @@ def test_nccl_transport_matches_host_transport(tmp_path, backbone, dim):
         assert np.array_equal(a, b)
     for name, v in out["host"]["params"].items():
         assert np.array_equal(v, out["nccl"]["params"][name]), name
+
+
+def test_cpp_driver_matches_python_engine(tmp_path):
+    # tools/cpp/sharded_train.cpp drives the whole sharded step from C++ alone
+    # (libngdb's NCCL communicator, packed metadata all-gather over NCCL, owner
+    # lists, ngdb_shard_step_exec): the same per-step losses as ShardedEngine
+    import subprocess
+    from pathlib import Path
+
+    import torch.multiprocessing as mp
+
+    import shard_workers
+    exe = Path(m.__file__).parent / "_lib" / "sharded_train"
+    assert exe.exists(), "make examples"
+    r = subprocess.run([str(exe), "1", "0", "0", str(tmp_path / "nccl.id"), "small", "3", "64",
+                        "16", "32"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    cpp = [float(line.split()[2]) for line in r.stdout.splitlines() if line.startswith("step")]
+    mp.spawn(shard_workers.python_sums_worker,
+             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, 32, 3, "q2b"),
+             nprocs=1, join=True)
+    py = pickle.load(open(tmp_path / "pysums0.pkl", "rb"))
+    assert len(cpp) == 3 and cpp == py, (cpp, py)
