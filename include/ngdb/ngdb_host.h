@@ -146,6 +146,35 @@ typedef struct ngdb_train_opts {
 int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
                    int64_t first_step, int32_t n_steps, double* loss_per_step,
                    float* per_query_loss, double* timings);
+/* The trainer loop with the trainer's feedback paths (SPEC.md:218-235, 571,
+ * 587, 594-595): difficulty tracking (always: after every step, the mean
+ * per-query loss of each pattern in the batch goes into the EMA tracker),
+ * adaptive π (refreshed every refresh_every steps over the support of
+ * opts->pattern_weights; batch i is sampled with refresh floor(i / R), so runs
+ * do not depend on the producer count), a JSON-lines metrics log and a
+ * checkpoint cadence. fb may be NULL (= ngdb_train_run). */
+typedef struct ngdb_train_feedback {
+  int32_t adaptive;          /* 1: adaptive π */
+  int32_t refresh_every;     /* 0: 100 */
+  double decay, eta, floor;  /* EMA decay, temperature η, floor ε; 0: 0.9, 1.0, 0.01 */
+  double* ema_loss;          /* [14] tracker state in/out (NULL: fresh tracker) */
+  int64_t* observations;     /* [14] in/out (with ema_loss) */
+  double* pi_per_step;       /* [n_steps][14] π each batch was sampled with (may be NULL) */
+  const char* metrics_path;  /* JSON-lines {step, loss, ema[14], queries_per_s, peak_bytes}; NULL: off */
+  const char* checkpoint_path;
+  int32_t checkpoint_every;  /* 0: off (SPEC default 1,000) */
+  uint64_t config_hash;
+} ngdb_train_feedback;
+int ngdb_train_run_ex(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
+                      const ngdb_train_feedback* fb, int64_t first_step, int32_t n_steps,
+                      double* loss_per_step, float* per_query_loss, double* timings);
+/* The sampler's adaptive rule, exposed for tests and callers:
+ * record_difficulty on one (pattern, loss); update_distribution over the
+ * support of `base` (NULL: all 14 patterns). */
+int ngdb_record_difficulty(double* ema_loss, int64_t* observations, double decay, int32_t pattern,
+                           double loss);
+int ngdb_update_distribution(const double* ema_loss, const int64_t* observations, double eta,
+                             double floor, const double* base, double* weights_out);
 /* timings (may be NULL) receives 6 doubles: seconds the calling thread spent
  * waiting for planned batches, submitting (upload + launches), waiting for
  * step results, and of the submit time: step_begin, exec_pool calls,

@@ -49,6 +49,11 @@ SampleBatch sample_batch(const KnowledgeGraph& g, const SamplingDistribution& pi
 Pattern draw_pattern(const SamplingDistribution& pi, Rng& rng);
 
 SamplingDistribution update_distribution(const DifficultyTracker& t, double floor = 0.01);
+// The same rule restricted to a support (patterns of a configured mix): weights
+// outside it stay 0, the floor applies inside it; cold start (a support pattern
+// never observed) returns `base`.
+SamplingDistribution update_distribution(const DifficultyTracker& t, double floor,
+                                         const SamplingDistribution& base);
 void record_difficulty(DifficultyTracker& t, Pattern p, double loss);  // throws NonFiniteLoss
 
 // n_neg ids uniform over ℰ \ answers (sorted), with replacement.

@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "ngdb/kg.hpp"
@@ -32,6 +33,24 @@ struct TrainLoopConfig {
   int32_t queue_depth = 0;  // planned batches buffered ahead of the consumer; 0: 2 * producers
   bool graphs = true;       // launch each step as one CUDA graph (ngdb_step_launch)
   int32_t in_flight = 2;    // steps on the device before the oldest one's losses are read back
+
+  // -- adaptive sampling feedback (SURVEY A-10) ---------
+  // After every step the consumer records, per pattern present in the batch,
+  // the mean per-query loss into the DifficultyTracker (pattern order). When
+  // `adaptive`, π is refreshed every `refresh_every` steps from the tracker
+  // (update_distribution over the support of `pi`) and batch i is sampled with
+  // the π of refresh floor(i / refresh_every): producers wait for it, so the
+  // batches (and the run) do not depend on the producer count.
+  bool adaptive = false;
+  int32_t refresh_every = 100;
+  double floor = 0.01;          // ε
+  DifficultyTracker* tracker = nullptr;  // in/out; nullptr: a fresh tracker
+  double* pi_per_step = nullptr;         // [n_steps][14]: π batch i was sampled with
+  // -- metrics log and checkpoints ---------------------
+  std::string metrics_path;     // JSON-lines, one record per step (appended)
+  std::string checkpoint_path;  // written every `checkpoint_every` steps (atomic rename)
+  int32_t checkpoint_every = 0; // 0: off (SPEC default cadence 1,000)
+  uint64_t config_hash = 0;
 };
 
 struct TrainLoopStats {

@@ -328,3 +328,49 @@ def eval_ranks_multi(backbone, ent, embeddings, targets, filters, dim, alpha=0.0
                              for b in np.atleast_2d(e)]), axis=0)
         out.append(filtered_rank(-d, t, f))
     return np.array(out, dtype=np.int64)
+
+
+# ---- adaptive sampling (sampler DESIGN DECISIONS :243-244) ----
+# A literal numpy restatement of the sampler's difficulty rule, independent of
+# the product's C++ (paper_2602_21597_b200/csrc/host/sampler.cpp).
+
+def record_difficulty(ema, obs, pattern, loss, decay=0.9):
+    """SPEC.md:227-235: ema(p) <- decay*ema(p) + (1-decay)*loss; NonFiniteLoss
+    (ValueError here) for a non-finite or negative loss."""
+    if not np.isfinite(loss) or loss < 0:
+        raise ValueError(f"NonFiniteLoss: {loss}")
+    ema[pattern] = decay * ema[pattern] + (1.0 - decay) * loss
+    obs[pattern] += 1
+
+
+def update_distribution(ema, obs, eta=1.0, floor=0.01, base=None):
+    """w(p) ∝ exp(η·ema(p)), renormalised, clipped below at ε
+    and renormalised again — over the support of `base` (default: all 14
+    patterns); cold start (a support pattern never observed) returns `base`."""
+    base = np.full(14, 1.0 / 14) if base is None else np.asarray(base, np.float64)
+    sup = base > 0
+    if (np.asarray(obs)[sup] == 0).any():
+        return base.copy()
+    e = np.asarray(ema, np.float64)
+    w = np.zeros(14)
+    w[sup] = np.exp(eta * (e[sup] - e[sup].max()))
+    w /= w.sum()
+    clipped = np.zeros(14, bool)
+    while True:  # clip at ε, renormalise the rest, until no new clip
+        new = sup & ~clipped & (w < floor)
+        clipped |= new
+        free = sup & ~clipped
+        w[clipped] = floor
+        w[free] *= (1.0 - clipped.sum() * floor) / w[free].sum()
+        if not new.any():
+            return w
+
+
+def batch_pattern_losses(patterns, losses):
+    """(pattern, mean per-query loss) of every pattern present in a batch, in
+    pattern order — what the trainer records after each step."""
+    sums, cnt = [0.0] * 14, [0] * 14
+    for p, x in zip(np.asarray(patterns).tolist(), np.asarray(losses, np.float64).tolist()):
+        sums[p] += x  # sequential, query order
+        cnt[p] += 1
+    return [(p, sums[p] / cnt[p]) for p in range(14) if cnt[p]]

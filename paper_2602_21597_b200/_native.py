@@ -65,6 +65,13 @@ class TrainOpts(C.Structure):
                 ("in_flight", i32), ("flags", i32)]
 
 
+class TrainFeedback(C.Structure):
+    _fields_ = [("adaptive", i32), ("refresh_every", i32), ("decay", f64), ("eta", f64),
+                ("floor", f64), ("ema_loss", P(f64)), ("observations", P(i64)),
+                ("pi_per_step", P(f64)), ("metrics_path", C.c_char_p),
+                ("checkpoint_path", C.c_char_p), ("checkpoint_every", i32), ("config_hash", u64)]
+
+
 SHARD_BUFFERS = ("anchor_send", "anchor_rows", "query_mine", "query_all", "dq_part", "dq_mine",
                  "grad_send", "grad_all", "reduce")
 
@@ -173,6 +180,10 @@ SIGNATURES = {
     "ngdb_select_pool": (C.c_int, [P(i64), P(i64), P(i32)]),
     "ngdb_jsonl_roundtrip": (C.c_int, [C.c_char_p, C.c_char_p, i64]),
     "ngdb_train_step": (C.c_int, [C.c_void_p, C.c_void_p, i32, i64, P(f32), P(f64)]),
+    "ngdb_train_run_ex": (C.c_int, [C.c_void_p, C.c_void_p, P(TrainOpts), P(TrainFeedback), i64,
+                                    i32, P(f64), P(f32), P(f64)]),
+    "ngdb_record_difficulty": (C.c_int, [P(f64), P(i64), f64, i32, f64]),
+    "ngdb_update_distribution": (C.c_int, [P(f64), P(i64), f64, f64, P(f64), P(f64)]),
     "ngdb_train_run": (C.c_int, [C.c_void_p, C.c_void_p, P(TrainOpts), i64, i32, P(f64), P(f32),
                                  P(f64)]),
     "ngdb_run_step": (C.c_int, [C.c_void_p, C.c_void_p, i64, P(f32), P(f64)]),

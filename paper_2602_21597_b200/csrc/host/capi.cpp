@@ -54,6 +54,9 @@ int guarded(F&& f) {
   } catch (const ngdb::NonFinite& e) {
     ngdb_internal::set_last_error(e.what());
     return NGDB_ERR_NON_FINITE;
+  } catch (const ngdb::NonFiniteLoss& e) {
+    ngdb_internal::set_last_error(std::string("NonFiniteLoss: ") + e.what());
+    return NGDB_ERR_NON_FINITE;
   } catch (const ngdb::Error& e) {
     ngdb_internal::set_last_error(std::string(e.what()));
     return NGDB_ERR_CONFIG;
@@ -524,9 +527,9 @@ int ngdb_train_step(ngdb_ctx* ctx, const ngdb_batch* bt, int32_t b_max, int64_t 
   });
 }
 
-int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
-                   int64_t first_step, int32_t n_steps, double* loss_per_step,
-                   float* per_query_loss, double* timings) {
+int ngdb_train_run_ex(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
+                      const ngdb_train_feedback* fb, int64_t first_step, int32_t n_steps,
+                      double* loss_per_step, float* per_query_loss, double* timings) {
   return guarded([&] {
     if (!ctx || !g || !o || !o->pattern_weights) throw ngdb::ConfigError("null argument");
     ngdb::TrainLoopConfig cfg;
@@ -540,8 +543,32 @@ int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
     cfg.first_tag = o->first_tag;
     if (o->in_flight > 0) cfg.in_flight = o->in_flight;
     cfg.graphs = (o->flags & NGDB_TRAIN_NO_GRAPHS) == 0;
+    ngdb::DifficultyTracker tracker;
+    if (fb) {
+      cfg.adaptive = fb->adaptive != 0;
+      if (fb->refresh_every > 0) cfg.refresh_every = fb->refresh_every;
+      if (fb->decay > 0) tracker.decay = fb->decay;
+      if (fb->eta > 0) tracker.temperature = fb->eta;
+      if (fb->floor > 0) cfg.floor = fb->floor;
+      if (fb->ema_loss && fb->observations)
+        for (int p = 0; p < ngdb::kPatternCount; ++p) {
+          tracker.ema_loss[p] = fb->ema_loss[p];
+          tracker.observations[p] = fb->observations[p];
+        }
+      cfg.pi_per_step = fb->pi_per_step;
+      if (fb->metrics_path) cfg.metrics_path = fb->metrics_path;
+      if (fb->checkpoint_path) cfg.checkpoint_path = fb->checkpoint_path;
+      cfg.checkpoint_every = fb->checkpoint_every;
+      cfg.config_hash = fb->config_hash;
+    }
+    cfg.tracker = &tracker;
     const auto st = ngdb::run_train_loop(ctx, g->split, cfg, first_step, n_steps, loss_per_step,
                                          per_query_loss);
+    if (fb && fb->ema_loss && fb->observations)
+      for (int p = 0; p < ngdb::kPatternCount; ++p) {
+        fb->ema_loss[p] = tracker.ema_loss[p];
+        fb->observations[p] = tracker.observations[p];
+      }
     if (timings) {
       timings[0] = st.plan_wait_s;
       timings[1] = st.submit_s;
@@ -550,6 +577,43 @@ int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
       timings[4] = st.pools_s;
       timings[5] = st.optim_s;
     }
+  });
+}
+
+int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
+                   int64_t first_step, int32_t n_steps, double* loss_per_step,
+                   float* per_query_loss, double* timings) {
+  return ngdb_train_run_ex(ctx, g, o, nullptr, first_step, n_steps, loss_per_step,
+                           per_query_loss, timings);
+}
+
+int ngdb_record_difficulty(double* ema_loss, int64_t* observations, double decay, int32_t pattern,
+                           double loss) {
+  return guarded([&] {
+    if (pattern < 0 || pattern >= ngdb::kPatternCount) throw ngdb::ConfigError("pattern index");
+    ngdb::DifficultyTracker t;
+    t.decay = decay;
+    t.ema_loss[pattern] = ema_loss[pattern];
+    t.observations[pattern] = observations[pattern];
+    ngdb::record_difficulty(t, static_cast<ngdb::Pattern>(pattern), loss);
+    ema_loss[pattern] = t.ema_loss[pattern];
+    observations[pattern] = t.observations[pattern];
+  });
+}
+
+int ngdb_update_distribution(const double* ema_loss, const int64_t* observations, double eta,
+                             double floor, const double* base, double* weights_out) {
+  return guarded([&] {
+    ngdb::DifficultyTracker t;
+    t.temperature = eta;
+    for (int p = 0; p < ngdb::kPatternCount; ++p) {
+      t.ema_loss[p] = ema_loss[p];
+      t.observations[p] = observations[p];
+    }
+    ngdb::SamplingDistribution b;
+    for (int p = 0; p < ngdb::kPatternCount; ++p) b.weights[p] = base ? base[p] : 1.0 / ngdb::kPatternCount;
+    const auto d = ngdb::update_distribution(t, floor, b);
+    for (int p = 0; p < ngdb::kPatternCount; ++p) weights_out[p] = d.weights[p];
   });
 }
 

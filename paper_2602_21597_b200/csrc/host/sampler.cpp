@@ -13,6 +13,8 @@
 //   After kMaxRetries failed attempts -> ExhaustedRetries.
 #include "ngdb/sampler.hpp"
 
+#include <limits>
+
 #include <algorithm>
 #include <cmath>
 
@@ -162,19 +164,36 @@ SampleBatch sample_batch(const KnowledgeGraph& g, const SamplingDistribution& pi
 }
 
 SamplingDistribution update_distribution(const DifficultyTracker& t, double floor) {
-  SamplingDistribution d;
-  d.floor = floor;
+  SamplingDistribution all;
+  all.weights.fill(1.0 / kPatternCount);
+  return update_distribution(t, floor, all);
+}
+
+SamplingDistribution update_distribution(const DifficultyTracker& t, double floor,
+                                         const SamplingDistribution& base) {
+  std::array<bool, kPatternCount> in{};
+  int n_in = 0;
   bool cold = false;
-  for (int p = 0; p < kPatternCount; ++p) cold |= t.observations[p] == 0;
+  for (int p = 0; p < kPatternCount; ++p) {
+    in[p] = base.weights[p] > 0.0;
+    n_in += in[p];
+    cold |= in[p] && t.observations[p] == 0;
+  }
+  if (n_in == 0) throw ConfigError("update_distribution: empty support");
+  if (n_in * floor > 1.0) throw ConfigError("update_distribution: floor * |support| > 1");
   if (cold) {
-    d.weights.fill(1.0 / kPatternCount);
+    SamplingDistribution d = base;
+    d.floor = floor;
     return d;
   }
-  double mx = t.ema_loss[0];
-  for (double v : t.ema_loss) mx = std::max(mx, v);
+  SamplingDistribution d;
+  d.floor = floor;
+  double mx = -std::numeric_limits<double>::infinity();
+  for (int p = 0; p < kPatternCount; ++p)
+    if (in[p]) mx = std::max(mx, t.ema_loss[p]);
   double sum = 0.0;
   for (int p = 0; p < kPatternCount; ++p) {
-    d.weights[p] = std::exp(t.temperature * (t.ema_loss[p] - mx));
+    d.weights[p] = in[p] ? std::exp(t.temperature * (t.ema_loss[p] - mx)) : 0.0;
     sum += d.weights[p];
   }
   for (double& w : d.weights) w /= sum;
@@ -185,6 +204,7 @@ SamplingDistribution update_distribution(const DifficultyTracker& t, double floo
     double free_mass = 0.0;
     bool changed = false;
     for (int p = 0; p < kPatternCount; ++p) {
+      if (!in[p]) continue;
       if (!clipped[p] && d.weights[p] < floor) {
         clipped[p] = true;
         changed = true;
@@ -194,7 +214,7 @@ SamplingDistribution update_distribution(const DifficultyTracker& t, double floo
     }
     const double target = 1.0 - n_clipped * floor;
     for (int p = 0; p < kPatternCount; ++p)
-      d.weights[p] = clipped[p] ? floor : d.weights[p] * (target / free_mass);
+      if (in[p]) d.weights[p] = clipped[p] ? floor : d.weights[p] * (target / free_mass);
     if (!changed) break;
   }
   return d;

@@ -14,7 +14,8 @@ from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
-from ._native import ModelDesc, NodeDesc, PoolDesc, StepPlan, TrainOpts, check, lib
+from ._native import (ModelDesc, NodeDesc, PoolDesc, StepPlan, TrainFeedback, TrainOpts, check,
+                      lib)
 
 # query.hpp:14-29 enum order == index order of π
 PATTERNS = ["1p", "2p", "3p", "2i", "3i", "pi", "ip", "2u", "up", "2in", "3in", "pin", "pni", "inp"]
@@ -37,6 +38,33 @@ def pattern_weights(mix: Sequence[str]) -> np.ndarray:
     for p in mix:
         w[PATTERNS.index(p)] += 1.0 / len(mix)
     return w
+
+
+class DifficultyTracker:
+    """DifficultyTracker: per-pattern EMA of the training loss
+    plus the adaptive rule's knobs (decay 0.9, temperature η 1.0, floor ε 0.01;
+    SPEC.md:244). State lives in numpy arrays the C loop updates in place."""
+
+    def __init__(self, decay: float = 0.9, eta: float = 1.0, floor: float = 0.01):
+        self.decay, self.eta, self.floor = decay, eta, floor
+        self.ema_loss = np.zeros(14, dtype=np.float64)
+        self.observations = np.zeros(14, dtype=np.int64)
+
+    def record(self, pattern: int, loss: float) -> None:
+        """record_difficulty; NonFiniteLoss on a bad loss."""
+        check(lib.ngdb_record_difficulty(_p(self.ema_loss, C.c_double),
+                                         _p(self.observations, C.c_int64), self.decay,
+                                         int(pattern), float(loss)))
+
+    def distribution(self, base: Optional[np.ndarray] = None) -> np.ndarray:
+        """update_distribution over the support of `base`."""
+        out = np.zeros(14, dtype=np.float64)
+        b = None if base is None else np.ascontiguousarray(base, dtype=np.float64)
+        check(lib.ngdb_update_distribution(_p(self.ema_loss, C.c_double),
+                                           _p(self.observations, C.c_int64), self.eta,
+                                           self.floor, _p(b, C.c_double) if b is not None else None,
+                                           _p(out, C.c_double)))
+        return out
 
 
 class Graph:
@@ -316,26 +344,48 @@ class Engine:
     def train(self, graph: Graph, weights: np.ndarray, n_steps: int, batch: int = 512,
               n_neg: int = 128, seed: int = 3, first_tag: int = 0, n_producers: int = 0,
               queue_depth: int = 0, per_query: bool = False, in_flight: int = 0,
-              graphs: bool = True):
+              graphs: bool = True, adaptive: bool = False, refresh_every: int = 100,
+              tracker: Optional["DifficultyTracker"] = None, metrics_path: Optional[str] = None,
+              checkpoint_path: Optional[str] = None, checkpoint_every: int = 0,
+              config_hash: int = 0, pi_per_step: bool = False):
         """The trainer loop: n_steps steps of batches sampled
         from Rng(seed).fork(first_tag + i) by host producer threads, planned,
-        uploaded and run back to back (ngdb_train_run). Returns the per-step loss
-        sums (and [n_steps][batch] per-query losses with per_query=True)."""
+        uploaded and run back to back (ngdb_train_run_ex), with the trainer's
+        feedback paths: the difficulty tracker (always updated; pass `tracker`
+        to keep its state across calls), adaptive π refreshed every
+        `refresh_every` steps, a JSON-lines metrics log
+         and a checkpoint cadence. Returns the
+        per-step loss sums (plus [n_steps][batch] per-query losses with
+        per_query=True, plus the [n_steps][14] π of each batch with
+        pi_per_step=True)."""
         w = np.ascontiguousarray(weights, dtype=np.float64)
         opts = TrainOpts(_p(w, C.c_double), batch, n_neg, self.b_max, n_producers, queue_depth,
                          seed, first_tag, in_flight, 0 if graphs else 1)
+        tr = tracker if tracker is not None else DifficultyTracker()
+        pis = np.zeros((n_steps, 14), dtype=np.float64)
+        fb = TrainFeedback(1 if adaptive else 0, refresh_every, tr.decay, tr.eta, tr.floor,
+                           _p(tr.ema_loss, C.c_double), _p(tr.observations, C.c_int64),
+                           _p(pis, C.c_double),
+                           str(metrics_path).encode() if metrics_path else None,
+                           str(checkpoint_path).encode() if checkpoint_path else None,
+                           checkpoint_every, config_hash)
         sums = np.zeros(n_steps, dtype=np.float64)
         pq = np.zeros((n_steps, batch), dtype=np.float32) if per_query else None
         timings = (C.c_double * 6)()
-        check(lib.ngdb_train_run(self._h, graph._h, C.byref(opts), self.step_count, n_steps,
-                                 _p(sums, C.c_double),
-                                 _p(pq, C.c_float) if pq is not None else None, timings))
+        check(lib.ngdb_train_run_ex(self._h, graph._h, C.byref(opts), C.byref(fb),
+                                    self.step_count, n_steps, _p(sums, C.c_double),
+                                    _p(pq, C.c_float) if pq is not None else None, timings))
         self.step_count += n_steps
         # host seconds of the calling thread: waiting for plans, submitting, waiting for results
         self.last_timings = {"plan_wait_s": timings[0], "submit_s": timings[1],
                              "collect_wait_s": timings[2], "submit_begin_s": timings[3],
                              "submit_pools_s": timings[4], "submit_optimizer_s": timings[5]}
-        return (sums, pq) if per_query else sums
+        out = (sums,)
+        if per_query:
+            out += (pq,)
+        if pi_per_step:
+            out += (pis,)
+        return out if len(out) > 1 else sums
 
     def save_checkpoint(self, path: str, config_hash: int = 0) -> None:
         """Parameters, Adam moments and the step counter as an NGCK blob."""

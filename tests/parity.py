@@ -230,9 +230,11 @@ def run_masked(graph, backbone, mix, b, k, dim, steps=1, b_max=512, seed_tag=0, 
 
 
 def run_pair(graph, ograph, backbone, mix, b, k, dim, b_max=512, steps=1, seed_tag=0,
-             compare_grads=True, certify=True, semantic_dim=0):
+             compare_grads=True, certify=True, semantic_dim=0, query_level=False):
     """One or more training steps on both sides; returns a dict of comparisons.
-    semantic_dim > 0: FuseSemantic with a synthetic frozen store of that width."""
+    semantic_dim > 0: FuseSemantic with a synthetic frozen store of that width.
+    query_level: the GPU side runs the query-level baseline executor's plan
+     instead of the Max-Fillness one."""
     import oracle as O
     import paper_2602_21597_b200 as m
 
@@ -254,7 +256,12 @@ def run_pair(graph, ograph, backbone, mix, b, k, dim, b_max=512, steps=1, seed_t
             batch, kept = tie_free(batch, om, b_max, step)
             out["kept"].append(kept)
         a = batch.arrays()
-        loss = eng.train_step(batch)
+        if query_level:
+            st = m.PlannedStep(batch, backbone, dim, b_max, semantic=bool(semantic_dim),
+                               query_level=True)
+            loss = eng.run_step(st, len(a.patterns))
+        else:
+            loss = eng.train_step(batch)
         ref = om.step(a.patterns, a.anchors, a.relations, a.positives, a.negatives, b_max=b_max,
                       step=step)
         out["loss"].append((loss, ref))

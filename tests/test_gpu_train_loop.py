@@ -97,3 +97,54 @@ def test_loop_depth_and_launch_mode(small_graph, in_flight, graphs):
     np.testing.assert_array_equal(pq, ref)
     for name in ("entity", "relation"):
         np.testing.assert_array_equal(eng.download(name), base.download(name))
+
+
+@pytest.mark.parametrize("producers", [1, 3])
+def test_adaptive_feedback_loop(small_graph, tmp_path, producers):
+    # ngdb_train_run_ex with adaptive pi, the metrics
+    # log and the checkpoint cadence: every
+    # batch is the sampler's batch under the pi in force at its refresh, pi
+    # follows the oracle's restatement of the tracker over the returned
+    # per-query losses, and runs do not depend on the producer count
+    import json
+
+    import oracle as O
+    b, k, dim, steps, R = 96, 16, 32, 30, 10
+    w = m.pattern_weights(ALL)
+    eng = _engine(small_graph, "q2b", dim, k, b)
+    tr = m.DifficultyTracker()
+    ck = tmp_path / "run.ngck"
+    sums, pq, pis = eng.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=100,
+                              n_producers=producers, per_query=True, adaptive=True,
+                              refresh_every=R, tracker=tr, metrics_path=str(tmp_path / "m.jsonl"),
+                              checkpoint_path=str(ck), checkpoint_every=12, pi_per_step=True)
+    ema, obs = np.zeros(14), np.zeros(14, np.int64)
+    pi = w.copy()
+    for i in range(steps):
+        if i and i % R == 0:
+            pi = O.update_distribution(ema, obs, 1.0, 0.01, w)
+        np.testing.assert_allclose(pis[i], pi, rtol=1e-12, atol=1e-15)
+        pats = m.Batch.sample(small_graph, pis[i], b, k, seed=3, tag=100 + i).arrays().patterns
+        for p, x in O.batch_pattern_losses(pats, pq[i]):
+            O.record_difficulty(ema, obs, p, x)
+    assert not np.allclose(pis[-1], w)  # pi moved away from uniform
+    np.testing.assert_allclose(tr.ema_loss, ema, rtol=1e-12)
+    assert np.array_equal(tr.observations, obs)
+    # metrics log: one record per step
+    recs = [json.loads(x) for x in (tmp_path / "m.jsonl").read_text().splitlines()]
+    assert [r["step"] for r in recs] == list(range(1, steps + 1))
+    assert all(r["queries_per_s"] > 0 and r["peak_bytes"] > 0 for r in recs)
+    np.testing.assert_allclose([r["loss"] for r in recs], sums, rtol=1e-15)
+    # checkpoint cadence 12 -> the last blob holds step 24; resuming it and
+    # replaying steps 25..30 with the recorded pi reproduces the run
+    res = _engine(small_graph, "q2b", dim, k, b)
+    assert res.load_checkpoint(str(ck)) == 24
+    for i in range(24, steps):
+        res.train_step(m.Batch.sample(small_graph, pis[i], b, k, seed=3, tag=100 + i))
+    for name in ("entity", "relation"):
+        np.testing.assert_array_equal(res.download(name), eng.download(name))
+    # producer-count independence
+    other = _engine(small_graph, "q2b", dim, k, b)
+    s2 = other.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=100,
+                     n_producers=4 - producers, adaptive=True, refresh_every=R)
+    np.testing.assert_array_equal(s2, sums)

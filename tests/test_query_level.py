@@ -1,9 +1,10 @@
 """Query-level baseline executor (module `bench`): queries
 grouped by pattern, groups executed one after another with their own kernel
 invocations, on the same kernels as the operator-level (Max-Fillness) run.
-CPU: the SPEC's machine-independent invocation-count claims. GPU: sinks and
-updated parameters equal the operator-level step's (1e-4 relative: the GEMM
-split-K differs with the batch shape)."""
+CPU: the SPEC's machine-independent invocation-count claims. GPU: the
+query-level step against the CPU oracle (losses, gradients and post-Adam
+parameters at the 1e-4 bar, like the operator-level parity tests), and against
+the operator-level step."""
 import numpy as np
 import pytest
 
@@ -63,3 +64,14 @@ def test_query_level_step_matches_operator_level(small_graph, backbone):
     for k in p0:
         scale = max(float(np.sqrt(np.mean(p0[k] ** 2))), 1e-12)
         assert np.max(np.abs(p1[k] - p0[k])) <= 1e-4 * scale, k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("backbone", ["gqe", "q2b", "betae"])
+@pytest.mark.parametrize("dim,b,k,steps", [(32, 128, 32, 2), (400, 128, 32, 1)])
+def test_query_level_step_matches_oracle(small_graph, small_oracle_graph, backbone, dim, b, k,
+                                         steps):
+    from parity import check_all, run_pair
+    res = run_pair(small_graph, small_oracle_graph, backbone, ALL, b=b, k=k, dim=dim,
+                   steps=steps, query_level=True)
+    check_all(res, allow_frac=0.0, steps=steps)
