@@ -301,9 +301,18 @@ def filtered_rank_sorted(scores, target, filt):
     return 1 + first + n_eq // 2
 
 
-def eval_distances(backbone, ent, q, dim, alpha=0.02):
+def eval_distances(backbone, ent, q, dim, alpha=0.02, consts=None):
     """[n_ent] float32 distances of every entity row to one query (GQE: q [d];
-    Q2B: centre | offset [2d]), summed sequentially over the dimensions."""
+    Q2B: centre | offset [2d]), summed sequentially over the dimensions.
+    BetaE: `ent` is the entity side T [n][2d] and `consts` C [n] of the
+    linearised KL (beta_eval_table); the compared value is sum_k fl(q_k T_k)
+    (sequential) + C — KL minus the query's own lnB(q), the same for every
+    entity."""
+    if backbone == "betae":
+        t = np.asarray(ent, dtype=np.float32)
+        q = np.asarray(q, dtype=np.float32)[None, :2 * dim]
+        dot = np.cumsum((t * q).astype(np.float32), axis=1, dtype=np.float32)[:, -1]
+        return (dot + np.asarray(consts, np.float32)).astype(np.float32)
     ent = np.asarray(ent, dtype=np.float32)[:, :dim]
     q = np.asarray(q, dtype=np.float32)
     t = np.abs(ent - q[None, :dim])
@@ -315,16 +324,16 @@ def eval_distances(backbone, ent, q, dim, alpha=0.02):
     return out + np.float32(alpha) * inn
 
 
-def eval_ranks(backbone, ent, queries, targets, filters, dim, alpha=0.02):
-    return np.array([filtered_rank(-eval_distances(backbone, ent, q, dim, alpha), t, f)
+def eval_ranks(backbone, ent, queries, targets, filters, dim, alpha=0.02, consts=None):
+    return np.array([filtered_rank(-eval_distances(backbone, ent, q, dim, alpha, consts), t, f)
                      for q, t, f in zip(queries, targets, filters)], dtype=np.int64)
 
 
-def eval_ranks_multi(backbone, ent, embeddings, targets, filters, dim, alpha=0.02):
+def eval_ranks_multi(backbone, ent, embeddings, targets, filters, dim, alpha=0.02, consts=None):
     """Union queries: an entity's distance is the nearest branch's."""
     out = []
     for e, t, f in zip(embeddings, targets, filters):
-        d = np.min(np.stack([eval_distances(backbone, ent, b, dim, alpha)
+        d = np.min(np.stack([eval_distances(backbone, ent, b, dim, alpha, consts)
                              for b in np.atleast_2d(e)]), axis=0)
         out.append(filtered_rank(-d, t, f))
     return np.array(out, dtype=np.int64)
@@ -374,3 +383,40 @@ def batch_pattern_losses(patterns, losses):
         sums[p] += x  # sequential, query order
         cnt[p] += 1
     return [(p, sums[p] / cnt[p]) for p in range(14) if cnt[p]]
+
+
+# ---- evaluator entity tables of BetaE and fusion (f64) -------------------------
+
+def beta_realize(x):
+    """clamp(softplus(x), 0.05, 1e9) (SURVEY A-7), f64."""
+    x = np.asarray(x, np.float64)
+    return np.clip(np.logaddexp(0.0, x), 0.05, 1e9)
+
+
+def beta_eval_table(raw, dim):
+    """Entity side of KL(Beta(a,b) || Beta(A,B)) = lnB(A,B) + C_e + A (psi(s)-psi(a))
+    + B (psi(s)-psi(b)), for raw entity rows
+    [n][2d] -> T [n][2d], C [n] in f64 (scipy special functions)."""
+    from scipy.special import betaln, digamma
+    a, b = beta_realize(raw[:, :dim]), beta_realize(raw[:, dim:2 * dim])
+    s = a + b
+    da, db, ds = digamma(a), digamma(b), digamma(s)
+    T = np.concatenate([ds - da, ds - db], axis=1)
+    C = np.sum(-betaln(a, b) + a * da + b * db - s * ds, axis=1)
+    return T, C
+
+
+def beta_kl(a, b, A, B):
+    """KL(Beta(a,b) || Beta(A,B)) elementwise, f64 (the closed form)."""
+    from scipy.special import betaln, digamma
+    return (betaln(A, B) - betaln(a, b) + (a - A) * digamma(a) + (b - B) * digamma(b)
+            + (A - a + B - b) * digamma(a + b))
+
+
+def fused_table(entity, store, fus_f, fus_wp, fus_bp):
+    """sigma(W_p [h | F s] + b_p) of every entity (Eq. 12), f64."""
+    h = np.asarray(entity, np.float64)
+    fs = np.asarray(store, np.float64) @ np.asarray(fus_f, np.float64).T
+    z = np.concatenate([h, fs], axis=1) @ np.asarray(fus_wp, np.float64).T + \
+        np.asarray(fus_bp, np.float64).reshape(1, -1)
+    return 1.0 / (1.0 + np.exp(-z))

@@ -134,6 +134,7 @@ SIGNATURES = {
     "ngdb_checkpoint_load": (C.c_int, [C.c_void_p, C.c_char_p, u64, P(i64)]),
     "ngdb_step_timeline": (C.c_int, [C.c_void_p, P(f64), P(f64), P(i64)]),
     "ngdb_read_score_queries": (C.c_int, [C.c_void_p, P(f32), i64]),
+    "ngdb_eval_entity_table": (C.c_int, [C.c_void_p, P(f32), i64, P(f32), i64]),
     "ngdb_eval_ranks_multi": (C.c_int, [C.c_void_p, P(f32), i32, P(i32), P(i32), P(i32), P(i32),
                                         P(i32)]),
     "ngdb_eval_ranks": (C.c_int, [C.c_void_p, P(f32), i32, P(i32), P(i32), P(i32), P(i32)]),

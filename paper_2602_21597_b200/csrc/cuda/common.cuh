@@ -247,7 +247,9 @@ struct KSpan {
 // rows.cu
 // evaluator (evaluate.cu): full-entity scoring + filtered rank counts
 struct EvalArgs {
-  const float* ent;  // entity table [n_ent][ent_w] (GQE/Q2B rows are d-wide points)
+  // entity table [n_ent][ent_w]: GQE/Q2B rows are d-wide points; BetaE: the
+  // entity side T_e [2d] of the linearised KL (dim = 2d then); fusion: fused rows
+  const float* ent;
   int64_t ent_w;
   int32_t n_ent, dim, backbone;
   float alpha;       // Q2B inside weight
@@ -260,6 +262,7 @@ struct EvalArgs {
   const int32_t* target;      // per query
   const int32_t* f_off;  // [n_queries + 1] CSR of filter entities
   const int32_t* f_ids;
+  const float* ec;       // BetaE: [n_ent] C_e
   float* dt;             // [n_queries] target distances (nearest branch)
   int32_t* better;       // [n_queries]
   int32_t* ties;         // [n_queries]

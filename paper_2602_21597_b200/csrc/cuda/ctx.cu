@@ -296,6 +296,12 @@ struct ngdb_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timeline;
   // evaluator staging (ngdb_eval_ranks)
   char* eval_buf = nullptr;
+  // evaluator entity table of the BetaE / fusion backbones over ALL entities
+  // (T_e | C_e, or the fused rows), its row list and the fusion scratch
+  float* evtab = nullptr;
+  int32_t* ev_rows = nullptr;
+  float* ev_scratch = nullptr;
+  int64_t ev_scratch_cap = 0;
   int64_t eval_cap = 0;
 
   Param* find(const std::string& name) {
@@ -423,15 +429,15 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.wq = c->query_width();
   a.ent_w = static_cast<int32_t>(c->params[c->ent_idx].cols);
   a.rel_w = static_cast<int32_t>(c->params[c->rel_idx].cols);
-  a.ncand = p->meta.n_candidates;
+  a.ncand = p ? p->meta.n_candidates : 0;
   a.n_neg = c->desc.n_neg;
   a.n_entities = c->desc.n_entities;
   a.n_relations = c->desc.n_relations;
   a.gamma = c->desc.gamma;
   a.alpha_box = c->desc.alpha_box;
   a.arena = c->arena;
-  a.nodes = reinterpret_cast<const ngdb_node_desc*>(p->blob + p->layout.nodes);
-  a.cand = p->blob + p->layout.cand;
+  a.nodes = p ? reinterpret_cast<const ngdb_node_desc*>(p->blob + p->layout.nodes) : nullptr;
+  a.cand = p ? p->blob + p->layout.cand : nullptr;
   a.ent = c->params[c->ent_idx].w;
   a.rel = c->params[c->rel_idx].w;
   a.dense = c->dense_w;
@@ -976,6 +982,9 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
       if (p.g) cudaFree(p.g);
     }
   if (c->eval_buf) cudaFree(c->eval_buf);
+  if (c->evtab) cudaFree(c->evtab);
+  if (c->ev_rows) cudaFree(c->ev_rows);
+  if (c->ev_scratch) cudaFree(c->ev_scratch);
   if (c->cand_local) cudaFree(c->cand_local);
   if (c->anchor_local) cudaFree(c->anchor_local);
   if (c->fscratch) cudaFree(c->fscratch);
@@ -1660,6 +1669,75 @@ int ngdb_checkpoint_load(ngdb_ctx* c, const char* path, uint64_t config_hash, in
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Width of the evaluator's entity rows: BetaE T_e [2d], fusion / GQE / Q2B d.
+int64_t eval_row_width(const ngdb_ctx* c) {
+  return c->beta() ? 2 * int64_t(c->desc.dim) : int64_t(c->desc.dim);
+}
+
+// The evaluator's entity table for the current parameters (BetaE: T_e and C_e
+// of every entity by the step prologue kernel beta_prep; fusion: every fused
+// row by the FuseSemantic prologue's GEMMs). Returns (table, C_e or nullptr).
+std::pair<const float*, const float*> eval_entity_table(ngdb_ctx* c) {
+  const Param& ent = c->params[c->ent_idx];
+  if (!c->beta() && !c->fused()) return {ent.w, nullptr};
+  if (c->beta() && c->fused())
+    throw Fail{NGDB_ERR_MISSING_KERNEL, "eval_ranks: BetaE + FuseSemantic (Psi_theta)"};
+  const int64_t N = c->desc.n_entities, w = eval_row_width(c);
+  if (!c->evtab) {
+    c->evtab = dmalloc<float>(N * w + N);
+    std::vector<int32_t> idx(2 * N + 1, 0);
+    for (int64_t i = 0; i < N; ++i) idx[i] = static_cast<int32_t>(i);  // rows; seg = 0
+    c->ev_rows = dmalloc<int32_t>(2 * N + 1);
+    CK(cudaMemcpy(c->ev_rows, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice));
+  }
+  DevArgs a = make_args(c, nullptr);
+  a.etab = c->evtab;
+  a.etab_c = c->evtab + N * w;
+  const SparseTable t{ent.w, ent.m, ent.v, nullptr, static_cast<int32_t>(ent.cols),
+                      static_cast<int32_t>(N), c->ev_rows, c->ev_rows + N, nullptr};
+  const LaunchCtx lc{c->stream, c->num_sms};
+  if (c->beta()) {
+    c->launches += launch_beta_prep(a, t, lc);
+  } else {
+    if (!c->sem) throw Fail{NGDB_ERR_CONFIG, "semantic store not uploaded (ngdb_semantic_upload)"};
+    const int64_t need = fuse_scratch_floats(c->desc.dim, c->desc.semantic_dim, N);
+    if (need > c->ev_scratch_cap) {
+      CK(cudaStreamSynchronize(c->stream));
+      if (c->ev_scratch) CK(cudaFree(c->ev_scratch));
+      c->ev_scratch = dmalloc<float>(need);
+      c->ev_scratch_cap = need;
+    }
+    c->launches += fuse_prologue(a, t, c->ev_scratch, c->ev_scratch_cap, lc);
+  }
+  CK(cudaGetLastError());
+  return {c->evtab, c->beta() ? c->evtab + N * w : nullptr};
+}
+
+}  // namespace
+
+extern "C" {
+
+int ngdb_eval_entity_table(ngdb_ctx* c, float* rows, int64_t n_rows_floats, float* consts,
+                           int64_t n_consts) {
+  return guarded([&] {
+    if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "eval_entity_table: row-sharded context"};
+    const int64_t N = c->desc.n_entities, w = eval_row_width(c);
+    if (n_rows_floats != N * w) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "eval_entity_table: rows size"};
+    const auto tab = eval_entity_table(c);
+    CK(cudaMemcpyAsync(rows, tab.first, N * w * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (consts) {
+      if (!tab.second || n_consts != N)
+        throw Fail{NGDB_ERR_SHAPE_MISMATCH, "eval_entity_table: consts exist for BetaE only"};
+      CK(cudaMemcpyAsync(consts, tab.second, N * 4, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int ngdb_read_score_queries(ngdb_ctx* c, float* host, int64_t n_slots) {
   return guarded([&] {
     if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "read_score_queries: row-sharded context"};
@@ -1679,8 +1757,6 @@ int ngdb_eval_ranks_multi(ngdb_ctx* c, const float* units, int32_t n_queries,
     if (n_queries < 0 || (n_queries > 0 && (!units || !unit_offsets || !targets ||
                                             !filter_offsets || !ranks)))
       throw Fail{NGDB_ERR_CONFIG, "eval_ranks: null argument"};
-    if (c->desc.backbone == NGDB_BETAE || c->fused())
-      throw Fail{NGDB_ERR_MISSING_KERNEL, "eval_ranks: GQE and Q2B backbones only"};
     if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "eval_ranks: row-sharded context"};
     if (n_queries == 0) return;
     const Param& ent = c->params[c->ent_idx];
@@ -1745,11 +1821,13 @@ int ngdb_eval_ranks_multi(ngdb_ctx* c, const float* units, int32_t n_queries,
     }
     char* p = c->eval_buf;
     EvalArgs a{};
-    a.ent = ent.w;
-    a.ent_w = ent.cols;
+    const auto tab = eval_entity_table(c);  // BetaE: T_e | C_e; fusion: fused rows
+    a.ent = tab.first;
+    a.ent_w = c->beta() ? eval_row_width(c) : (c->fused() ? c->desc.dim : ent.cols);
     a.n_ent = n_ent;
-    a.dim = c->desc.dim;
-    a.backbone = c->desc.backbone;
+    a.dim = c->beta() ? 2 * c->desc.dim : c->desc.dim;  // BetaE: the 2d-long dot product
+    a.backbone = c->beta() ? NGDB_BETAE : (c->fused() ? NGDB_GQE : c->desc.backbone);
+    a.ec = tab.second;
     a.alpha = c->desc.alpha_box;
     a.wq = wq;
     a.nq = static_cast<int32_t>(ns);

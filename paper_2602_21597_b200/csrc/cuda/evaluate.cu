@@ -20,6 +20,16 @@
 // distance of an entity is bit-identical in all three kernels: comparisons
 // against d_t — including exact ties — are consistent, and the counts are
 // integers (deterministic regardless of atomic order).
+//
+// BetaE (KL): KL(entity || query) = lnB(q) + C_e + <q, T_e> with
+// the entity side T_e = [psi(s)-psi(a) | psi(s)-psi(b)], C_e evaluated once per
+// entity by the training step's own prologue kernel (beta_prep) over the whole
+// table: the all-pairs pass is a 2d-long dot product per (entity, query),
+// summed in dimension order with __fmul_rn / __fadd_rn, then + C_e. lnB(q) is
+// the same for every entity of a query, so it is left out of the compared
+// value (ranks are unchanged; the comparison needs one rounding less). The fusion backbone ranks
+// against the fused table sigma(W_p [h | F s] + b_p) of every entity (the
+// step's FuseSemantic prologue over all rows) with the GQE distance.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -37,6 +47,10 @@ constexpr int ES = KS + 4;  // padded entity row: float4-aligned, conflict-free 
 // one dimension of the distance, accumulated in dimension order
 template <int BB>
 __device__ __forceinline__ void acc_dim(float& out, float& in, float v, float c, float o) {
+  if constexpr (BB == NGDB_BETAE) {  // v = T_e[k], c = q[k]
+    out = __fadd_rn(out, __fmul_rn(c, v));
+    return;
+  }
   const float t = fabsf(__fsub_rn(v, c));
   if constexpr (BB == NGDB_GQE) {
     out = __fadd_rn(out, t);
@@ -45,9 +59,16 @@ __device__ __forceinline__ void acc_dim(float& out, float& in, float v, float c,
     in = __fadd_rn(in, fminf(t, o));
   }
 }
+// ce = C_e of the BetaE distance (0 otherwise)
 template <int BB>
-__device__ __forceinline__ float finish(float out, float in, float alpha) {
+__device__ __forceinline__ float finish(float out, float in, float alpha, float ce) {
+  if constexpr (BB == NGDB_BETAE) return __fadd_rn(out, ce);
   return BB == NGDB_GQE ? out : __fadd_rn(out, __fmul_rn(alpha, in));
+}
+template <int BB>
+__device__ __forceinline__ float ent_const(const EvalArgs& a, int e) {
+  if constexpr (BB == NGDB_BETAE) return a.ec[e];
+  return 0.f;
 }
 
 // one (entity, query) distance by one thread: float4 loads, the additions still
@@ -62,13 +83,13 @@ __device__ float row_distance(const EvalArgs& a, int e, int q) {
     const float4 x = __ldg(reinterpret_cast<const float4*>(v + k));
     const float4 c = __ldg(reinterpret_cast<const float4*>(qc + k));
     float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-    if constexpr (BB != NGDB_GQE) o = __ldg(reinterpret_cast<const float4*>(qc + a.dim + k));
+    if constexpr (BB == NGDB_Q2B) o = __ldg(reinterpret_cast<const float4*>(qc + a.dim + k));
     acc_dim<BB>(out, in, x.x, c.x, o.x);
     acc_dim<BB>(out, in, x.y, c.y, o.y);
     acc_dim<BB>(out, in, x.z, c.z, o.z);
     acc_dim<BB>(out, in, x.w, c.w, o.w);
   }
-  return finish<BB>(out, in, a.alpha);
+  return finish<BB>(out, in, a.alpha, ent_const<BB>(a, e));
 }
 
 // distance of entity e to query qi: the nearest of its branch slots (UnionScore
@@ -94,7 +115,7 @@ template <int BB>
 __global__ void __launch_bounds__(256) eval_count_kernel(EvalArgs a) {
   __shared__ __align__(16) float es[TE][ES];
   __shared__ __align__(16) float qcs[TQ][KS];
-  __shared__ __align__(16) float qos[BB == NGDB_GQE ? 1 : TQ][KS];
+  __shared__ __align__(16) float qos[BB == NGDB_Q2B ? TQ : 1][KS];
   const int e0 = blockIdx.x * TE, q0 = blockIdx.y * TQ;
   const int tid = threadIdx.x;
   const int el = tid & (TE - 1), qg = tid / TE;  // a warp shares its query group
@@ -117,7 +138,7 @@ __global__ void __launch_bounds__(256) eval_count_kernel(EvalArgs a) {
       const bool ok = q < a.nq && k0 + k < a.dim;
       const float* qr = a.q + static_cast<int64_t>(q) * a.wq + k0 + k;
       *reinterpret_cast<float4*>(&qcs[r][k]) = ok ? __ldg(reinterpret_cast<const float4*>(qr)) : z4;
-      if constexpr (BB != NGDB_GQE)
+      if constexpr (BB == NGDB_Q2B)
         *reinterpret_cast<float4*>(&qos[r][k]) =
             ok ? __ldg(reinterpret_cast<const float4*>(qr + a.dim)) : z4;
     }
@@ -130,7 +151,7 @@ __global__ void __launch_bounds__(256) eval_count_kernel(EvalArgs a) {
         const int ql = qg * QPT + j;
         const float4 c = *reinterpret_cast<const float4*>(&qcs[ql][k]);
         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        if constexpr (BB != NGDB_GQE) o = *reinterpret_cast<const float4*>(&qos[ql][k]);
+        if constexpr (BB == NGDB_Q2B) o = *reinterpret_cast<const float4*>(&qos[ql][k]);
         acc_dim<BB>(out[j], in[j], v.x, c.x, o.x);
         acc_dim<BB>(out[j], in[j], v.y, c.y, o.y);
         acc_dim<BB>(out[j], in[j], v.z, c.z, o.z);
@@ -143,8 +164,9 @@ __global__ void __launch_bounds__(256) eval_count_kernel(EvalArgs a) {
   // the host packs a query's branch slots inside one 8-slot group, so the
   // nearest-branch distance is a min over this thread's own registers
   float d[QPT];
+  const float ce = e < a.n_ent ? ent_const<BB>(a, e) : 0.f;
 #pragma unroll
-  for (int j = 0; j < QPT; ++j) d[j] = finish<BB>(out[j], in[j], a.alpha);
+  for (int j = 0; j < QPT; ++j) d[j] = finish<BB>(out[j], in[j], a.alpha, ce);
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
     const int slot = q0 + qg * QPT + j;
@@ -201,7 +223,8 @@ void launch_eval(const EvalArgs& a, int32_t n_filter, cudaStream_t s) {
 int launch_eval_ranks(const EvalArgs& a, int32_t n_filter, cudaStream_t s) {
   if (a.n_queries <= 0) return 0;
   if (a.backbone == NGDB_GQE) launch_eval<NGDB_GQE>(a, n_filter, s);
-  else launch_eval<NGDB_Q2B>(a, n_filter, s);
+  else if (a.backbone == NGDB_Q2B) launch_eval<NGDB_Q2B>(a, n_filter, s);
+  else launch_eval<NGDB_BETAE>(a, n_filter, s);
   return n_filter > 0 ? 3 : 2;
 }
 

@@ -450,6 +450,19 @@ class Engine:
                                         _p(ranks, C.c_int32)))
         return ranks
 
+    def eval_entity_table(self):
+        """The evaluator's entity side for the current parameters
+        (ngdb_eval_entity_table): BetaE (T [n][2d], C [n]) of the linearised
+        KL; fusion (fused rows [n][d], None); GQE / Q2B (entity table, None)."""
+        n = self.n_entities
+        w = 2 * self.dim if self.backbone == "betae" else self.dim
+        rows = np.zeros((n, w), dtype=np.float32)
+        consts = np.zeros(n, dtype=np.float32) if self.backbone == "betae" else None
+        check(lib.ngdb_eval_entity_table(self._h, _p(rows, C.c_float), rows.size,
+                                         _p(consts, C.c_float) if consts is not None else None,
+                                         n if consts is not None else 0))
+        return rows, consts
+
     def eval_ranks(self, queries: np.ndarray, targets: Sequence[int],
                    filters: Sequence[Sequence[int]]) -> np.ndarray:
         """Filtered ranks of `targets` among all entities (SPEC.md:614-618,

@@ -111,7 +111,26 @@ def test_gpu_rank_edge_cases():
     with pytest.raises(NgdbError) as e:
         eng.eval_ranks(q[:1], np.array([300], dtype=np.int32), [[]])
     assert e.value.kind == "IndexOutOfRange"
-    beta = m.Engine("betae", 100, 4, dim=8, n_neg=4, max_queries=8)
+    # BetaE + FuseSemantic (Psi_theta): no kernels, refused at create
     with pytest.raises(NgdbError) as e:
-        beta.eval_ranks(np.zeros((1, 16), np.float32), [0], [[]])
+        m.Engine("betae", 100, 4, dim=8, n_neg=4, max_queries=8,
+                 semantic=m.semantic_store(100, 16, seed=5))
     assert e.value.kind == "MissingKernel"
+
+
+def test_beta_linearised_kl_matches_closed_form():
+    # DESIGN.md §3.5 / §3.7: KL(Beta(a,b) || Beta(A,B)) summed over the dims =
+    # lnB(q) + C_e + <q, T_e> with the entity side of oracle.beta_eval_table
+    from scipy.special import betaln
+    rng = np.random.default_rng(3)
+    d = 16
+    raw = rng.normal(0, 2, size=(20, 2 * d))
+    T, C = oracle.beta_eval_table(raw, d)
+    a, b = oracle.beta_realize(raw[:, :d]), oracle.beta_realize(raw[:, d:])
+    for _ in range(5):
+        A, B = rng.uniform(0.05, 6, d), rng.uniform(0.05, 6, d)
+        kl = oracle.beta_kl(a, b, A[None], B[None]).sum(1)
+        lin = betaln(A, B).sum() + C + T @ np.concatenate([A, B])
+        np.testing.assert_allclose(lin, kl, rtol=1e-10, atol=1e-10)
+    # KL(Beta(2,2) || Beta(1,1)) = 0.125092802561388
+    assert abs(oracle.beta_kl(2.0, 2.0, 1.0, 1.0) - 0.125092802561388) < 1e-12
