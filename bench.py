@@ -347,8 +347,11 @@ def evaluator_measure(eng, info, dim, backbone, nq=512, reps=5):
     rng = np.random.default_rng(1)
     n_ent = info["n_entities"]
     wq = dim if backbone == "gqe" else 2 * dim
-    q = rng.uniform(-0.035, 0.035, size=(nq, wq)).astype(np.float32)
-    q[:, dim:] = np.abs(q[:, dim:])
+    if backbone == "betae":  # (alpha | beta) > 0
+        q = rng.uniform(0.05, 3.0, size=(nq, wq)).astype(np.float32)
+    else:
+        q = rng.uniform(-0.035, 0.035, size=(nq, wq)).astype(np.float32)
+        q[:, dim:] = np.abs(q[:, dim:])
     t = rng.integers(0, n_ent, size=nq).astype(np.int32)
     ids = rng.integers(0, n_ent, size=(nq, 100)).astype(np.int32)
     ids[ids == t[:, None]] = (ids[ids == t[:, None]] + 1) % n_ent
@@ -733,11 +736,25 @@ def main():
             step_no += 2 * len(batches[args.warmup:][:QL_STEPS]) + 2
         except Exception as exc:  # noqa: BLE001
             extras["query_level"] = {"error": repr(exc)}
-        if backbone in ("gqe", "q2b") and not sdim:
+        if not (backbone == "betae" and sdim):
             try:
                 extras["evaluator"] = evaluator_measure(eng, info, dim, backbone)
             except Exception as exc:  # noqa: BLE001
                 extras["evaluator"] = {"error": repr(exc)}
+        if backbone in ("gqe", "q2b"):
+            # SPEC.md:682-690 operator_microbench at acceptance 6's shape
+            # (n=1024, k=2, d=400), on this config's graph and backbone
+            from paper_2602_21597_b200.microbench import operator_microbench
+            mb = {}
+            for op, k in (("Intersect", 2), ("UnionScore", 2), ("Project", 1),
+                          ("EmbedAnchor", 1)):
+                try:
+                    r = operator_microbench(graph, op, n=1024, k=k, dim=dim, backbone=backbone)
+                    mb[f"{op}_k{k}"] = {x: r[x] for x in ("loop_ms", "batched_ms", "speedup",
+                                                           "outputs_equal")}
+                except Exception as exc:  # noqa: BLE001
+                    mb[f"{op}_k{k}"] = {"error": repr(exc)}
+            extras["operator_microbench"] = mb
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

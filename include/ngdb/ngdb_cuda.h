@@ -274,6 +274,14 @@ int ngdb_shard_step_exec(ngdb_ctx* ctx, int64_t step);
  * collectives inside); replay sets the Adam scalars of `step` and launches it. */
 int ngdb_shard_step_capture(ngdb_ctx* ctx, ngdb_shard_step* step);
 int ngdb_shard_step_replay(ngdb_ctx* ctx, ngdb_shard_step* step, int64_t step_no);
+/* Streaming ABI helpers of the operator microbench: run an
+ * Intersect invocation held back for class merging now; read arena floats
+ * [offset, offset + n) (synchronous); fix the tcgen05 GEMMs' split-K for the
+ * process (0 = per launch; 1 makes a row's result independent of the rows
+ * sharing its launch, so batched and per-op executions agree bit for bit). */
+int ngdb_exec_flush(ngdb_ctx* ctx);
+int ngdb_read_arena(ngdb_ctx* ctx, int64_t offset, int64_t n, float* out);
+int ngdb_set_gemm_split(int32_t split);
 /* Adam bias-correction scalars of 1-based step t (host -> device, not capturable). */
 int ngdb_set_step(ngdb_ctx* ctx, int64_t step);
 /* Run the context's launches on an external stream (e.g. the framework stream

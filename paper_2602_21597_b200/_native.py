@@ -112,6 +112,9 @@ SIGNATURES = {
     "ngdb_shard_step_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_set_step": (C.c_int, [C.c_void_p, i64]),
     "ngdb_shard_optimizer": (C.c_int, [C.c_void_p, i64]),
+    "ngdb_exec_flush": (C.c_int, [C.c_void_p]),
+    "ngdb_read_arena": (C.c_int, [C.c_void_p, i64, i64, P(f32)]),
+    "ngdb_set_gemm_split": (C.c_int, [i32]),
     "ngdb_comm_unique_id": (C.c_int, [P(C.c_uint8)]),
     "ngdb_comm_init": (C.c_int, [C.c_void_p, P(C.c_uint8)]),
     "ngdb_comm_allgather_i32": (C.c_int, [C.c_void_p, P(i32), i64, P(i32)]),

@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "nccl_loader.hpp"
+#include "tc_gemm.cuh"
 
 using namespace ngdb_dev;
 
@@ -1177,6 +1178,32 @@ int ngdb_exec_pool(ngdb_ctx* c, const ngdb_pool_desc* pool) {
       return;
     }
     exec_pool(c, c->active, *pool);
+  });
+}
+
+int ngdb_exec_flush(ngdb_ctx* c) {
+  return guarded([&] {
+    if (!c->active) throw Fail{NGDB_ERR_CONFIG, "exec_flush outside a step"};
+    if (c->has_held) {
+      c->has_held = false;
+      exec_pool(c, c->active, c->held);
+    }
+  });
+}
+
+int ngdb_read_arena(ngdb_ctx* c, int64_t offset, int64_t n, float* out) {
+  return guarded([&] {
+    if (!c->arena || offset < 0 || n < 0 || offset + n > c->arena_cap)
+      throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "read_arena: range outside the arena"};
+    CK(cudaMemcpyAsync(out, c->arena + offset, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int ngdb_set_gemm_split(int32_t split) {
+  return guarded([&] {
+    if (split < 0 || split > 8) throw Fail{NGDB_ERR_CONFIG, "gemm split-K must be 0 (auto) or 1..8"};
+    ngdb_dev::set_gemm_split_override(split);
   });
 }
 

@@ -24,6 +24,8 @@
 //  * tc_gemm_kernel: all threads stream with cp.async (any row stride).
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -34,6 +36,13 @@
 #include "tc_gemm.cuh"
 
 namespace ngdb_dev {
+namespace {
+// 0: split-K chosen per launch to fill the GPU; S > 0: every GEMM uses S (with
+// S = 1 a row's result no longer depends on how many rows share the launch —
+// the operator microbench verifies batched == per-op loop bit for bit)
+std::atomic<int> g_split_override{0};
+}  // namespace
+
 namespace {
 
 constexpr int BM = 128, BN = 80, BK = 32;
@@ -710,6 +719,7 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
       // one CTA per SM (208 KB ring): split-K so the launch fills about one wave,
       // at most 8 CTAs per cluster and at least 2 chunks per CTA
       t.S = std::max(1, std::min({8, num_sms / std::max(tiles, 1), max_chunks / 2}));
+      if (const int o = g_split_override.load(std::memory_order_relaxed)) t.S = std::min(o, std::max(1, max_chunks));
       launch_pdl(tc_gemm_tma_kernel, dim3(tiles * t.S), dim3(kTmaThreads), TMA_SMEM_BYTES, s, t.S, t);
       return 1;
     }
@@ -717,11 +727,14 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   // split-K so the launch fills about one wave (2 CTAs per SM), at most 8 CTAs
   // per cluster (portable size) and at least 2 chunks per CTA
   b.S = std::max(1, std::min({8, (2 * num_sms) / std::max(tiles, 1), max_chunks / 2}));
+  if (const int o = g_split_override.load(std::memory_order_relaxed)) b.S = std::min(o, std::max(1, max_chunks));
   launch_pdl(tc_gemm_kernel, dim3(tiles * b.S), dim3(kThreads), SMEM_BYTES, s, b.S, b);
   return 1;
 }
 
 int tc_gemm(const TcGemmArgs& g, cudaStream_t s) { return tc_gemm_batch(&g, 1, s); }
+
+void set_gemm_split_override(int s) { g_split_override.store(s, std::memory_order_relaxed); }
 
 int split_transposed(const SplitJobs& jobs, cudaStream_t s) {
   if (jobs.n <= 0) return 0;

@@ -45,6 +45,8 @@ struct TcGemmArgs {
 };
 
 int tc_gemm(const TcGemmArgs& g, cudaStream_t s);
+// Process-wide split-K override: 0 = per launch (default), 1..8 = fixed.
+void set_gemm_split_override(int s);
 // Up to four independent problems in one launch (one dependency level).
 int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s);
 
