@@ -493,7 +493,7 @@ def bench_sharded(args):
     # e2e: the pipelined sharded trainer loop — sampling + planning on host
     # threads, metadata all-gather, owner lists, every stage and collective,
     # losses read back per step
-    producers = max(1, min(8, (os.cpu_count() or 2) - 1))
+    producers = max(2, host_workers() // world - 1)  # this rank's share of the host cores
     eng.step_count = step_no
     eng.train(graph, w, 3, batch, n_neg, lambda s: (1 + n_steps + s) * world + rank, producers)
     b0, d0 = C.c_int64(), C.c_int64()

@@ -21,38 +21,66 @@
 namespace ngdb_dev {
 
 // bias gradients of a class in one launch: db_j += column sums of dy_j
-// 32 columns per block; warp w of 16 sums rows w, w+16, ... with four
-// independent accumulators (loads in flight), then the 16 warp partials are
-// combined in warp order (deterministic).
+// 32 columns per CTA; the rows are split over a cluster of P CTAs (consecutive
+// blockIdx.x), each summing its row range — warp w of 16 takes rows w, w+16,
+// ... with four independent accumulators (loads in flight) and the 16 warp
+// partials are combined in warp order — then cluster rank 0 adds the P CTA
+// partials in rank order through distributed shared memory (deterministic,
+// no global scratch). Tall gradients (the fusion backward's 14.5k rows) thus
+// spread over 8 x (n / 32) CTAs instead of n / 32.
 constexpr int kColsumWarps = 16;
-__global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(ColsumJobs jobs) {
+__global__ void __launch_bounds__(kColsumWarps * 32) colsum_kernel(ColsumJobs jobs, int P) {
   pdl_start();
   __shared__ float part[kColsumWarps][32];
+  __shared__ float total[32];
   const ColsumJob& j = jobs.job[blockIdx.y];
+  const int rank = blockIdx.x % P, cg = blockIdx.x / P;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 32 + lane;
+  const int c = cg * 32 + lane;
+  const int r_beg = static_cast<int>((int64_t)rank * j.rows / P);
+  const int r_end = static_cast<int>((int64_t)(rank + 1) * j.rows / P);
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   if (c < j.n) {
     constexpr int W = kColsumWarps;
-    int r = warp;
-    for (; r + 3 * W < j.rows; r += 4 * W) {
+    int r = r_beg + warp;
+    for (; r + 3 * W < r_end; r += 4 * W) {
       s0 += j.dy[(int64_t)r * j.n + c];
       s1 += j.dy[(int64_t)(r + W) * j.n + c];
       s2 += j.dy[(int64_t)(r + 2 * W) * j.n + c];
       s3 += j.dy[(int64_t)(r + 3 * W) * j.n + c];
     }
-    for (; r < j.rows; r += W) s0 += j.dy[(int64_t)r * j.n + c];
+    for (; r < r_end; r += W) s0 += j.dy[(int64_t)r * j.n + c];
   }
   part[warp][lane] = (s0 + s1) + (s2 + s3);
   __syncthreads();
-  if (warp == 0 && c < j.n) {
+  if (warp == 0) {
     float t = 0.f;
     for (int w = 0; w < kColsumWarps; ++w) t += part[w][lane];
+    total[lane] = t;
+  }
+  if (P > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
+  else __syncthreads();
+  if (rank == 0 && warp == 0 && c < j.n) {
+    float t = total[lane];
+    const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&total[lane]));
+    for (int q = 1; q < P; ++q) {  // peers in rank order
+      uint32_t remote;
+      float v;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(q));
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote));
+      t += v;
+    }
     j.db[c] += t;
   }
+  // peers' partials stay resident until rank 0 has read them
+  if (P > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
 }
 int colsums(const ColsumJobs& jobs, int n, cudaStream_t s) {
-  launch_pdl(colsum_kernel, dim3(dim3((n + 31) / 32, jobs.n)), dim3(kColsumWarps * 32), 0, s, 1, jobs);
+  int rows = 0;
+  for (int i = 0; i < jobs.n; ++i) rows = std::max(rows, jobs.job[i].rows);
+  const int P = std::max(1, std::min(8, rows / 512));  // >= 512 rows per CTA
+  launch_pdl(colsum_kernel, dim3(dim3((n + 31) / 32 * P, jobs.n)), dim3(kColsumWarps * 32), 0, s,
+             P, jobs, P);
   return 1;
 }
 
