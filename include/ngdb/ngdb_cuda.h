@@ -117,6 +117,13 @@ typedef struct ngdb_step_plan {
   const int32_t* relation_rows;
   const int32_t* relation_seg;
   const int32_t* relation_contrib;
+  /* Optional (NULL: the pools run one after another): invocation i may start
+   * once pools pool_deps[pool_dep_off[i] .. pool_dep_off[i+1]) are done
+   * (earlier indices; data, arena-slab reuse and side-buffer hazards, from the
+   * planner). Graph-launched steps then run independent pools concurrently
+   * on the context's side streams; results are unchanged. */
+  const int32_t* pool_dep_off; /* [n_pools + 1] */
+  const int32_t* pool_deps;
 } ngdb_step_plan;
 
 /* Owner-side work of one rank in the row-sharded step (ngdb/shard.hpp). */

@@ -57,7 +57,9 @@ int ngdb_step_build(const ngdb_batch* bt, int32_t backbone, int32_t dim, int32_t
  * execution of the row-sharded step: every tensor gets a private device slot;
  * the trace is unchanged), bit2 query-level baseline executor (SPEC.md:664-672:
  * queries grouped by pattern, groups run sequentially, no operator batching
- * across patterns; same kernels, same sinks and gradients) */
+ * across patterns; same kernels, same sinks and gradients), bit3 device slab
+ * reuse along the Eq. 7 free list (default: a private slab per tensor, so
+ * independent pools can run concurrently; the trace is the same) */
 int ngdb_step_build_ex(const ngdb_batch* bt, int32_t backbone, int32_t dim, int32_t b_max,
                        int32_t flags, ngdb_step** out);
 int ngdb_step_view(const ngdb_step* s, ngdb_step_plan* view);

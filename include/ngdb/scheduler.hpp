@@ -109,9 +109,15 @@ class Planner {
   int64_t bwd_slot(int32_t node) const { return bwd_slot_[node]; }
   int64_t arena_bytes() const { return arena_top_; }
   const SchedulerConfig& config() const { return cfg_; }
+  // Invocation i (emission order) must follow inv_deps[inv_dep_off[i] ..
+  // inv_dep_off[i+1]) (earlier invocations: data, slab-reuse and side-buffer
+  // hazards); any order consistent with these runs the step identically.
+  const std::vector<int32_t>& inv_dep_off() const { return inv_dep_off_; }
+  const std::vector<int32_t>& inv_deps() const { return inv_deps_; }
 
  private:
   SchedulerConfig cfg_;
+  std::vector<int32_t> inv_dep_off_, inv_deps_;
   std::vector<int64_t> fwd_slot_, bwd_slot_;
   int64_t arena_top_ = 0;
 };

@@ -32,6 +32,11 @@ struct TrainConfig {
   int32_t semantic_dim = 0;
   bool sharded = false;  // entity table row-sharded across ranks
   bool query_level = false;  // query-level baseline executor (SchedulerConfig::query_level)
+  // Device arena slabs reused along the Eq. 7 free list (true), or a private
+  // slab per tensor (false, default): the trace and its byte statistics are
+  // the same; private slabs drop the write-after-read hazards between pools so
+  // independent pools can run concurrently (+7-10 MB per step).
+  bool device_reuse = false;
   uint64_t seed_params = 2;
   uint64_t seed_sampler = 3;
 };
@@ -74,6 +79,8 @@ struct StepPlanHost {
   // entity of every anchor slot
   std::vector<int32_t> unit_k, unit_slots;  // [B], [B][3] (-1 padded)
   std::vector<int32_t> anchor_ids;          // [n_anchor_slots]
+  // invocation dependencies (Planner::inv_deps), CSR over pools
+  std::vector<int32_t> pool_dep_off, pool_deps;
   ExecutionTrace trace;
   ngdb_step_plan view() const;
 };

@@ -44,6 +44,7 @@ class StepPlan(C.Structure):
         ("n_project_slots", i32), ("n_entity_rows", i32), ("entity_rows", P(i32)),
         ("entity_seg", P(i32)), ("entity_contrib", P(i32)), ("n_relation_rows", i32),
         ("relation_rows", P(i32)), ("relation_seg", P(i32)), ("relation_contrib", P(i32)),
+        ("pool_dep_off", P(i32)), ("pool_deps", P(i32)),
     ]
 
 

@@ -119,6 +119,7 @@ struct PlanMeta {
   int32_t n_erows = 0, n_rrows = 0, n_econ = 0, n_rcon = 0;
   int64_t arena_elems = 0;
   std::vector<int32_t> node_counts_by_kind;  // for algorithmic-byte accounting
+  std::vector<int32_t> dep_off, deps;        // pool dependencies (empty: serial)
 };
 
 PlanMeta meta_of(const ngdb_step_plan& p) {
@@ -135,6 +136,10 @@ PlanMeta meta_of(const ngdb_step_plan& p) {
   m.n_econ = p.n_entity_rows ? p.entity_seg[p.n_entity_rows] : 0;
   m.n_rcon = p.n_relation_rows ? p.relation_seg[p.n_relation_rows] : 0;
   m.arena_elems = p.arena_elems;
+  if (p.pool_dep_off && p.pool_deps) {
+    m.dep_off.assign(p.pool_dep_off, p.pool_dep_off + p.n_pools + 1);
+    m.deps.assign(p.pool_deps, p.pool_deps + m.dep_off.back());
+  }
   return m;
 }
 
@@ -145,6 +150,16 @@ void validate_plan(const ngdb_step_plan& p) {
     const ngdb_pool_desc& d = p.pools[i];
     if (d.first < 0 || d.count < 0 || d.first + d.count > p.n_nodes)
       throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "pool descriptor out of range"};
+  }
+  if (p.pool_dep_off && p.pool_deps) {
+    if (p.pool_dep_off[0] != 0) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "pool_dep_off[0] != 0"};
+    for (int i = 0; i < p.n_pools; ++i) {
+      if (p.pool_dep_off[i + 1] < p.pool_dep_off[i])
+        throw Fail{NGDB_ERR_SHAPE_MISMATCH, "pool_dep_off not ascending"};
+      for (int k = p.pool_dep_off[i]; k < p.pool_dep_off[i + 1]; ++k)
+        if (p.pool_deps[k] < 0 || p.pool_deps[k] >= i)
+          throw Fail{NGDB_ERR_INDEX_OUT_OF_RANGE, "pool dependency must name an earlier pool"};
+    }
   }
 }
 
@@ -196,6 +211,13 @@ struct ngdb_ctx {
   // row-sharded step (shard.cu)
   int world = 1, rank = 0;
   cudaStream_t own_stream = nullptr;
+  // concurrent pools (exec_pools_concurrent): side streams, one event per
+  // invocation of the widest plan seen, fork / join events
+  static constexpr int kSide = 3;
+  cudaStream_t side[kSide] = {nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> inv_ev;
+  cudaEvent_t fork_ev = nullptr, join_ev[kSide] = {nullptr, nullptr, nullptr};
+  bool concurrent = true;  // NGDB_SERIAL_POOLS=1 turns it off
   // streaming plans are uploaded on a copy stream one step ahead, overlapping
   // the previous step's kernels: blob_free[i] marks the end of the last step
   // that read stream_plan[i], blob_ready[i] the end of its upload
@@ -650,6 +672,125 @@ void exec_pools(ngdb_ctx* c, const ngdb_plan* p, const std::vector<ngdb_pool_des
   }
 }
 
+// Events for the invocations of a plan (created outside any stream capture).
+void ensure_inv_events(ngdb_ctx* c, size_t n) {
+  while (c->inv_ev.size() < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->inv_ev.push_back(e);
+  }
+}
+
+// The plan's pools as a DAG over the context stream and its side streams
+// (DESIGN.md §3.2 "concurrent pools"): invocation i waits only for the pools
+// the planner named (data, slab-reuse and side-buffer hazards), so independent
+// pools of the latency-bound small launches overlap. The MLP chain
+// (intersect classes, BetaE projections: one GEMM scratch, dense-gradient
+// accumulation) runs on side stream 0, the scoring chain (shared partials) on
+// side stream 1; every other invocation follows its latest dependency's stream
+// (none: the context stream). Kernels and their inputs are those of the serial
+// order, so results are bit-identical.
+void exec_pools_concurrent(ngdb_ctx* c, const ngdb_plan* p) {
+  const auto& v = p->meta.pools;
+  const auto& off = p->meta.dep_off;
+  const auto& deps = p->meta.deps;
+  struct Inv {
+    ngdb_pool_desc d, m;
+    bool merged;
+    int p0, p1;  // pool index range [p0, p1]
+  };
+  std::vector<Inv> invs;
+  std::vector<int> inv_of_pool(v.size());
+  for (size_t i = 0; i < v.size(); ++i) {
+    Inv in{v[i], ngdb_pool_desc{}, false, static_cast<int>(i), static_cast<int>(i)};
+    if (i + 1 < v.size() && mergeable(c, v[i], v[i + 1])) {
+      in.merged = true;
+      in.m = v[i + 1];
+      in.p1 = static_cast<int>(++i);
+    } else {
+      while (i + 1 < v.size() && drain_mergeable(c, in.d, v[i + 1])) {
+        in.d.count += v[++i].count;
+        in.p1 = static_cast<int>(i);
+      }
+    }
+    for (int q = in.p0; q <= in.p1; ++q) inv_of_pool[q] = static_cast<int>(invs.size());
+    invs.push_back(in);
+  }
+  const int n = static_cast<int>(invs.size());
+  if (static_cast<int>(c->inv_ev.size()) < n)
+    throw Fail{NGDB_ERR_CONFIG, "concurrent pools: invocation events not allocated"};
+  std::vector<std::vector<int>> dep_inv(n);
+  std::vector<char> waited_on(n, 0);
+  for (int i = 0; i < n; ++i) {
+    for (int q = invs[i].p0; q <= invs[i].p1; ++q)
+      for (int k = off[q]; k < off[q + 1]; ++k) {
+        const int d = inv_of_pool[deps[k]];
+        if (d != i) dep_inv[i].push_back(d);
+      }
+    std::sort(dep_inv[i].begin(), dep_inv[i].end());
+    dep_inv[i].erase(std::unique(dep_inv[i].begin(), dep_inv[i].end()), dep_inv[i].end());
+  }
+  cudaStream_t main = c->stream;
+  cudaStream_t streams[1 + ngdb_ctx::kSide] = {main, c->side[0], c->side[1], c->side[2]};
+  constexpr int S = 1 + ngdb_ctx::kSide;
+  std::vector<int> stream_of(n, 0);
+  auto chain_stream = [&](const ngdb_pool_desc& d) {
+    if (d.kind == NGDB_OP_INTERSECT || (d.kind == NGDB_OP_PROJECT && c->beta())) return 1;
+    if (d.kind == NGDB_OP_SCORE || d.kind == NGDB_OP_UNION_SCORE || d.kind == NGDB_OP_LOSS) return 2;
+    return -1;
+  };
+  for (int i = 0; i < n; ++i) {
+    const int cs = chain_stream(invs[i].d);
+    stream_of[i] = cs >= 0 ? cs : (dep_inv[i].empty() ? 0 : stream_of[dep_inv[i].back()]);
+    for (int d : dep_inv[i])
+      if (stream_of[d] != stream_of[i]) waited_on[d] = 1;
+  }
+  bool used[S] = {true, false, false, false};
+  for (int i = 0; i < n; ++i) used[stream_of[i]] = true;
+  CK(cudaEventRecord(c->fork_ev, main));
+  for (int s = 1; s < S; ++s)
+    if (used[s]) CK(cudaStreamWaitEvent(streams[s], c->fork_ev, 0));
+  int waited[S][S];
+  for (auto& row : waited)
+    for (int& x : row) x = -1;
+  try {
+    for (int i = 0; i < n; ++i) {
+      const int s = stream_of[i];
+      uint64_t sig = static_cast<uint64_t>(s) << 12;
+      for (int d : dep_inv[i]) {
+        const int t = stream_of[d];
+        if (t == s || d <= waited[s][t]) continue;  // FIFO: a later event implies earlier ones
+        CK(cudaStreamWaitEvent(streams[s], c->inv_ev[d], 0));
+        waited[s][t] = d;
+        sig = sig * 31 + static_cast<uint64_t>(d) + 1;
+      }
+      const Inv& in = invs[i];
+      c->stream = streams[s];
+      if (in.merged) {
+        sig_mix(c, sig ^ (0x100u | (in.d.dir << 4) | in.d.kind));
+        exec_pool(c, p, in.d, &in.m);
+      } else {
+        sig_mix(c, sig ^ ((static_cast<uint64_t>(in.d.k) << 8) | (in.d.dir << 4) | in.d.kind));
+        exec_pool(c, p, in.d);
+      }
+      c->stream = main;
+      if (waited_on[i]) CK(cudaEventRecord(c->inv_ev[i], streams[s]));
+    }
+  } catch (...) {
+    c->stream = main;
+    throw;
+  }
+  for (int s = 1; s < S; ++s)
+    if (used[s]) {
+      CK(cudaEventRecord(c->join_ev[s - 1], streams[s]));
+      CK(cudaStreamWaitEvent(main, c->join_ev[s - 1], 0));
+    }
+}
+
+bool use_concurrent(const ngdb_ctx* c, const ngdb_plan* p) {
+  return c->concurrent && !c->profiling && !p->meta.dep_off.empty() && c->world == 1;
+}
+
 void begin_step_device(ngdb_ctx* c) {
   CK(cudaMemsetAsync(c->flags, 0, 4 * sizeof(int32_t), c->stream));
   if (c->dense_n) CK(cudaMemsetAsync(c->dense_g, 0, c->dense_n * sizeof(float), c->stream));
@@ -769,7 +910,8 @@ void prep_step(ngdb_ctx* c, const ngdb_plan* p) {
 void launch_step(ngdb_ctx* c, const ngdb_plan* p) {
   begin_step_device(c);
   prep_step(c, p);
-  exec_pools(c, p, p->meta.pools);
+  if (use_concurrent(c, p)) exec_pools_concurrent(c, p);
+  else exec_pools(c, p, p->meta.pools);
   optimizer(c, p);
 }
 
@@ -790,6 +932,7 @@ void upload_plan(ngdb_ctx* c, const ngdb_step_plan& plan, ngdb_plan* dst, int64_
   c->h2d_bytes += L.total * sizeof(int32_t);
   dst->layout = L;
   dst->meta = meta_of(plan);
+  ensure_inv_events(c, dst->meta.pools.size());
 }
 
 }  // namespace
@@ -845,6 +988,10 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    for (auto& st : c->side) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    for (auto& ev : c->join_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (const char* e = std::getenv("NGDB_SERIAL_POOLS")) c->concurrent = e[0] == '0';
     c->stream = c->own_stream;
     for (int k = 0; k < 2; ++k) CK(cudaEventCreateWithFlags(&c->sh.staged[k], cudaEventDisableTiming));
     const int64_t D = d.dim;
@@ -971,6 +1118,12 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+  for (auto& st : c->side)
+    if (st) cudaStreamDestroy(st);
+  for (auto ev : c->inv_ev) cudaEventDestroy(ev);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  for (auto ev : c->join_ev)
+    if (ev) cudaEventDestroy(ev);
   if (c->comm) nccl_api().CommDestroy(c->comm);
   if (c->meta_comm) nccl_api().CommDestroy(c->meta_comm);
   if (c->meta_stream) cudaStreamDestroy(c->meta_stream);
@@ -1232,6 +1385,9 @@ int ngdb_step_launch(ngdb_ctx* c, int64_t step, int32_t use_graph) {
         prep_step(c, p);
       }
       set_step_scalars(c, step);
+      // streaming steps keep the serial chain: re-capturing and updating the
+      // DAG-shaped graph every step costs the consumer thread more host time
+      // (C2: 0.18 -> 0.25 ms/step) than the concurrency saves on the device
       exec_pools(c, p, p->meta.pools);
       optimizer(c, p);
     };
@@ -1417,6 +1573,7 @@ int ngdb_plan_create(ngdb_ctx* c, const ngdb_step_plan* plan, ngdb_plan** out) {
     p->layout = L;
     p->meta = meta_of(*plan);
     ensure_step_buffers(c, p->meta);
+    ensure_inv_events(c, p->meta.pools.size());
     *out = p;
   });
   if (rc != NGDB_OK && p) ngdb_plan_destroy(p);

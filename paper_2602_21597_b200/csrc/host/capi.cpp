@@ -242,6 +242,7 @@ int ngdb_step_build_ex(const ngdb_batch* bt, int32_t backbone, int32_t dim, int3
     cfg.semantic = (flags & 1) != 0;
     cfg.sharded = (flags & 2) != 0;
     cfg.query_level = (flags & 4) != 0;
+    cfg.device_reuse = (flags & 8) != 0;
     auto* s = new ngdb_step();
     s->plan = ngdb::plan_training_step(bt->tb, cfg);
     *out = s;

@@ -74,9 +74,11 @@ class SlotArena {
     Slot s;
     s.bytes = bytes;
     s.rc = rc;
+    int32_t prev = -1;  // previous tenant of the reused slab
     auto& fl = free_[bytes];
     if (!fl.empty()) {
-      s.offset = fl.back();
+      prev = fl.back();
+      s.offset = slots_[prev].offset;
       fl.pop_back();
       ++hits_;
     } else {
@@ -86,19 +88,24 @@ class SlotArena {
     if (!reuse_) {  // private device slot; the trace statistics are unchanged
       s.offset = dev_top_;
       dev_top_ += (bytes + 15) / 16 * 16;
+      prev = -1;
     }
     live_ += bytes;
     peak_ = std::max(peak_, live_);
     slots_.push_back(s);
+    prev_.push_back(prev);
     return static_cast<int32_t>(slots_.size() - 1);
   }
+  // tensor that occupied this tensor's device slab before it (-1: fresh slab)
+  int32_t prev_tenant(int32_t id) const { return prev_[id]; }
+  int32_t size() const { return static_cast<int32_t>(slots_.size()); }
   // returns bytes reclaimed (0 if still referenced)
   int64_t release(int32_t id) {
     Slot& s = slots_[id];
     if (s.rc <= 0) throw DoubleRelease("tensor released with refcount 0");
     if (--s.rc > 0) return 0;
     if (policy_ == ReleasePolicy::EndOfDag) return 0;
-    free_[s.bytes].push_back(s.offset);
+    free_[s.bytes].push_back(id);
     live_ -= s.bytes;
     return s.bytes;
   }
@@ -116,7 +123,8 @@ class SlotArena {
   bool reuse_;
   int64_t dev_top_ = 0;
   std::vector<Slot> slots_;
-  std::unordered_map<int64_t, std::vector<int64_t>> free_;
+  std::vector<int32_t> prev_;
+  std::unordered_map<int64_t, std::vector<int32_t>> free_;  // size class -> released slot ids
   int64_t live_ = 0, peak_ = 0, hits_ = 0, top_ = 0;
 };
 
@@ -154,6 +162,7 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
   std::vector<int32_t> batch, cls;
   int64_t executed = 0;
   int32_t cycle = 0, step = 0;
+
 
   // query-level mode: nodes of later pattern groups wait in `deferred` until
   // every node of the current group has executed
@@ -193,6 +202,60 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
         for (int k = 0; k < m.n_inputs; ++k) fn(t_fwd[m.inputs[k]]);
       if (m.consumer < 0) fn(t_fwd[x.mirror]);
     }
+  };
+
+  // Invocation dependencies (DESIGN.md §3.2 "concurrent pools"): an invocation
+  // waits for the writers of the tensors it reads (RAW), and — when its
+  // output reuses a slab — for the writer and every reader of the slab's
+  // previous tenant (WAW / WAR); invocations sharing a side buffer (the MLP
+  // scratch and dense-gradient accumulators; the scoring partials) form chains.
+  std::vector<int32_t> writer, dep_scratch;
+  std::vector<std::vector<int32_t>> readers;
+  int32_t chain_last[2] = {-1, -1};
+  inv_dep_off_.assign(1, 0);
+  inv_deps_.clear();
+  auto chain_of = [&](OpKind k) {
+    if (k == OpKind::Intersect || (k == OpKind::Project && cfg_.backbone == Backbone::BETAE))
+      return 0;
+    if (k == OpKind::Score || k == OpKind::UnionScore || k == OpKind::Loss) return 1;
+    return -1;
+  };
+  auto track = [&](const int32_t* nodes, int32_t count, OpKind kind) {
+    const int32_t inv = static_cast<int32_t>(inv_dep_off_.size()) - 1;
+    if (static_cast<int32_t>(writer.size()) < arena.size()) {
+      writer.resize(arena.size(), -1);
+      readers.resize(arena.size());
+    }
+    dep_scratch.clear();
+    auto add = [&](int32_t d) {
+      if (d >= 0 && d != inv) dep_scratch.push_back(d);
+    };
+    for (int32_t i = 0; i < count; ++i) {
+      const int32_t o = nodes[i];
+      for_each_input(o, [&](int32_t t) {
+        if (t < 0) return;
+        add(writer[t]);
+        readers[t].push_back(inv);
+      });
+      const int32_t t_out = f.nodes[o].op.dir == Direction::Fwd ? t_fwd[o] : t_bwd[o];
+      if (t_out >= 0) {
+        writer[t_out] = inv;
+        const int32_t p = arena.prev_tenant(t_out);
+        if (p >= 0) {
+          add(writer[p]);
+          for (int32_t r : readers[p]) add(r);
+        }
+      }
+    }
+    const int c = chain_of(kind);
+    if (c >= 0) {
+      add(chain_last[c]);
+      chain_last[c] = inv;
+    }
+    std::sort(dep_scratch.begin(), dep_scratch.end());
+    dep_scratch.erase(std::unique(dep_scratch.begin(), dep_scratch.end()), dep_scratch.end());
+    inv_deps_.insert(inv_deps_.end(), dep_scratch.begin(), dep_scratch.end());
+    inv_dep_off_.push_back(static_cast<int32_t>(inv_deps_.size()));
   };
 
   while (!ready.empty() || executed < n) {
@@ -249,10 +312,12 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
             if (f.nodes[o].cardinality == k) cls.push_back(o);
           if (cls.empty()) continue;
           rec.classes.emplace_back(k, static_cast<int32_t>(cls.size()));
+          track(cls.data(), static_cast<int32_t>(cls.size()), type.kind);
           invoke(Invocation{type, k, cls.data(), static_cast<int32_t>(cls.size()), step, cycle});
           ++tr.invocations;
         }
       } else {
+        track(batch.data(), static_cast<int32_t>(batch.size()), type.kind);
         invoke(Invocation{type, 0, batch.data(), static_cast<int32_t>(batch.size()), step, cycle});
         ++tr.invocations;
       }

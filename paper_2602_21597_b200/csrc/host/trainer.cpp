@@ -143,6 +143,10 @@ ngdb_step_plan StepPlanHost::view() const {
   p.relation_rows = relation_rows.data();
   p.relation_seg = relation_seg.data();
   p.relation_contrib = relation_contrib.data();
+  if (pool_dep_off.size() == pools.size() + 1) {
+    p.pool_dep_off = pool_dep_off.data();
+    p.pool_deps = pool_deps.data();
+  }
   return p;
 }
 
@@ -262,7 +266,7 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
   sc.query_width = wq;
   sc.n_candidates = nc;
   sc.elem_bytes = 4;
-  sc.device_reuse = !cfg.sharded;
+  sc.device_reuse = !cfg.sharded && cfg.device_reuse;
   sc.query_level = cfg.query_level;
   Planner planner(sc);
   const TensorModel tm{wq, nc};
@@ -304,6 +308,8 @@ StepPlanHost plan_training_step(const TrainingBatch& tb, const TrainConfig& cfg)
   };
   plan.trace = planner.run(f, emit);
   plan.arena_elems = planner.arena_bytes() / 4;
+  plan.pool_dep_off = planner.inv_dep_off();
+  plan.pool_deps = planner.inv_deps();
   return plan;
 }
 

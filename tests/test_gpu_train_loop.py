@@ -148,3 +148,39 @@ def test_adaptive_feedback_loop(small_graph, tmp_path, producers):
     s2 = other.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=100,
                      n_producers=4 - producers, adaptive=True, refresh_every=R)
     np.testing.assert_array_equal(s2, sums)
+
+
+@pytest.mark.parametrize("backbone,mix", [("q2b", ALL), ("betae", ALL), ("gqe", ALL)])
+def test_concurrent_pools_match_serial(small_graph, monkeypatch, backbone, mix):
+    # resident plans replayed as graphs whose independent pools run on side
+    # streams (planner dependencies) update the parameters exactly as the
+    # serial pool order does (NGDB_SERIAL_POOLS=1)
+    import ctypes as C
+
+    from paper_2602_21597_b200._native import check, lib
+    b, k, dim = 128, 16, 32
+    w = m.pattern_weights(mix)
+    steps = [m.PlannedStep(m.Batch.sample(small_graph, w, b, k, seed=3, tag=50 + i), backbone,
+                           dim, 512) for i in range(4)]
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("NGDB_SERIAL_POOLS", mode)
+        eng = _engine(small_graph, backbone, dim, k, b)
+        plans = []
+        for st in steps:
+            v = st.view()
+            assert v.pool_dep_off  # the planner ships dependencies
+            h = C.c_void_p()
+            check(lib.ngdb_plan_create(eng.handle, C.byref(v), C.byref(h)))
+            check(lib.ngdb_plan_prepare(eng.handle, h))
+            plans.append(h)
+        for i, h in enumerate(plans):
+            check(lib.ngdb_plan_run(eng.handle, h, i + 1))
+        check(lib.ngdb_sync(eng.handle))
+        info = small_graph.info()
+        out[mode] = {n: eng.download(n) for n, *_ in m.param_specs(
+            backbone, info["n_entities"], info["n_relations"], dim)}
+        for h in plans:
+            check(lib.ngdb_plan_destroy(h))
+    for name in out["1"]:
+        np.testing.assert_array_equal(out["0"][name], out["1"][name])
