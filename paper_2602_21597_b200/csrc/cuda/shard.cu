@@ -16,8 +16,10 @@
 namespace ngdb_dev {
 namespace {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 128;  // pack / elementwise kernels
 constexpr int kWarps = kThreads / 32;
+constexpr int kScoreThreads = 256;  // owner scoring: 8 warps per unit
+constexpr int kScoreWarps = kScoreThreads / 32;
 
 // lookup send: the owned rows every rank asked for, requester-major
 // (send[p] = local row send_rows[p]); one warp per row
@@ -46,51 +48,104 @@ __global__ void shard_query_pack_kernel(DevArgs a, int first, float* dst) {
 // partial dL/dq of each branch slot. Shared: queries [3][wq], per-warp partial
 // dq [4][3][wq] summed in warp order (deterministic).
 template <int BB, int NCH>
-__global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardDev sd) {
+__global__ void __launch_bounds__(kScoreThreads) shard_score_kernel(DevArgs a, ShardDev sd) {
   pdl_start();
   extern __shared__ __align__(16) float sm[];
-  __shared__ float lred[kWarps];
+  __shared__ float lred[kScoreWarps];
   const int u = blockIdx.x;
   const int q = u / sd.batch, i = u % sd.batch;
   const int k = sd.unit_k[u];
   const int wq = a.wq, D = a.dim, d4 = D / 4;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   float* qs = sm;              // [3][wq]
-  float* part = sm + 3 * wq;   // [kWarps][3][wq]
+  float* part = sm + 3 * wq;   // [kScoreWarps][3][wq]
   int gslot[3];
   for (int b = 0; b < 3; ++b)
     gslot[b] = b < k ? q * sd.max_slots + sd.unit_slots[static_cast<int64_t>(u) * 3 + b] : 0;
   float* dq_blk = sd.dq_part + static_cast<int64_t>(q) * sd.dq_block;  // rank q's block
   for (int b = 0; b < k; ++b)
-    for (int e = threadIdx.x; e < wq; e += kThreads)
+    for (int e = threadIdx.x; e < wq; e += kScoreThreads)
       qs[b * wq + e] = sd.query_all[static_cast<int64_t>(gslot[b]) * wq + e];
-  for (int e = threadIdx.x; e < kWarps * 3 * wq; e += kThreads) part[e] = 0.f;
+  for (int e = threadIdx.x; e < kScoreWarps * 3 * wq; e += kScoreThreads) part[e] = 0.f;
   __syncthreads();
   float loss = 0.f;  // identical in all lanes of a warp
   const int32_t* cand = sd.cand + static_cast<int64_t>(u) * a.ncand;
-  for (int t = sd.unit_off[u] + warp; t < sd.unit_off[u + 1]; t += kWarps) {
-    const int j = sd.owned[t];
-    const int32_t ent = cand[j];
-    const float* row = a.ent + static_cast<int64_t>(ent / sd.world) * a.ent_w;
-    // the candidate row once into registers, every 16-byte load in flight
-    float4 v[NCH];
+  const int t_end = sd.unit_off[u + 1];
+  // candidate rows into registers one step ahead: two rows of loads in
+  // flight per warp while the current one is reduced
+  auto load_row = [&](int t, float4* v) {
+    const float* row = a.ent + static_cast<int64_t>(cand[sd.owned[t]] / sd.world) * a.ent_w;
 #pragma unroll
-    for (int i = 0; i < NCH; ++i) {
-      const int c = lane + 32 * i;
-      v[i] = c < d4 ? ld4(row + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c4 = 0; c4 < NCH; ++c4) {
+      const int c = lane + 32 * c4;
+      v[c4] = c < d4 ? ld4(row + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+  };
+  float4 v[NCH], vn[NCH];
+  int t = sd.unit_off[u] + warp;
+  if (t < t_end) load_row(t, v);
+  if (k == 1) {
+    // one score slot (every pattern but the unions): dL/dq accumulates in
+    // registers across the warp's rows, one shared-memory write at the end
+    float4 gcs[NCH], gos[NCH];
+#pragma unroll
+    for (int c4 = 0; c4 < NCH; ++c4) gcs[c4] = gos[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (; t < t_end; t += kScoreWarps) {
+      const int j = sd.owned[t];
+      if (t + kScoreWarps < t_end) load_row(t + kScoreWarps, vn);
+      float s = 0.f;
+#pragma unroll
+      for (int c4 = 0; c4 < NCH; ++c4) {
+        const int c = lane + 32 * c4;
+        if (c < d4) {
+          const float4 cc = ld4(qs + 4 * c);
+          const float4 oo = BB == NGDB_Q2B ? ld4(qs + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          s += Dist<BB>::term(v[c4].x, cc.x, oo.x, a.alpha_box) + Dist<BB>::term(v[c4].y, cc.y, oo.y, a.alpha_box) +
+               Dist<BB>::term(v[c4].z, cc.z, oo.z, a.alpha_box) + Dist<BB>::term(v[c4].w, cc.w, oo.w, a.alpha_box);
+        }
+      }
+      const float coef = loss_coef(a, j, warp_sum(s), loss);
+      if (lane == 0) sd.coef_all[static_cast<int64_t>(gslot[0]) * a.ncand + j] = coef;
+#pragma unroll
+      for (int c4 = 0; c4 < NCH; ++c4) {
+        const int c = lane + 32 * c4;
+        if (c < d4) {
+          const float4 cc = ld4(qs + 4 * c);
+          const float4 oo = BB == NGDB_Q2B ? ld4(qs + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          Dist<BB>::grad(v[c4].x, cc.x, oo.x, coef, a.alpha_box, gcs[c4].x, gos[c4].x);
+          Dist<BB>::grad(v[c4].y, cc.y, oo.y, coef, a.alpha_box, gcs[c4].y, gos[c4].y);
+          Dist<BB>::grad(v[c4].z, cc.z, oo.z, coef, a.alpha_box, gcs[c4].z, gos[c4].z);
+          Dist<BB>::grad(v[c4].w, cc.w, oo.w, coef, a.alpha_box, gcs[c4].w, gos[c4].w);
+        }
+      }
+#pragma unroll
+      for (int c4 = 0; c4 < NCH; ++c4) v[c4] = vn[c4];
+    }
+    float* pw = part + (warp * 3) * wq;
+#pragma unroll
+    for (int c4 = 0; c4 < NCH; ++c4) {
+      const int c = lane + 32 * c4;
+      if (c < d4) {
+        st4(pw + 4 * c, gcs[c4]);
+        if (BB == NGDB_Q2B) st4(pw + D + 4 * c, gos[c4]);
+      }
+    }
+  }
+  for (; k > 1 && t < t_end; t += kScoreWarps) {  // union branches: smem partials per branch
+    const int j = sd.owned[t];
+    if (t + kScoreWarps < t_end) load_row(t + kScoreWarps, vn);
     float dist[3];
     for (int b = 0; b < k; ++b) {
       const float* qc = qs + b * wq;
       float s = 0.f;
 #pragma unroll
-      for (int i = 0; i < NCH; ++i) {
-        const int c = lane + 32 * i;
+      for (int c4 = 0; c4 < NCH; ++c4) {
+        const int c = lane + 32 * c4;
         if (c < d4) {
           const float4 cc = ld4(qc + 4 * c);
           const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          s += Dist<BB>::term(v[i].x, cc.x, oo.x, a.alpha_box) + Dist<BB>::term(v[i].y, cc.y, oo.y, a.alpha_box) +
-               Dist<BB>::term(v[i].z, cc.z, oo.z, a.alpha_box) + Dist<BB>::term(v[i].w, cc.w, oo.w, a.alpha_box);
+          s += Dist<BB>::term(v[c4].x, cc.x, oo.x, a.alpha_box) + Dist<BB>::term(v[c4].y, cc.y, oo.y, a.alpha_box) +
+               Dist<BB>::term(v[c4].z, cc.z, oo.z, a.alpha_box) + Dist<BB>::term(v[c4].w, cc.w, oo.w, a.alpha_box);
         }
       }
       dist[b] = warp_sum(s);
@@ -105,16 +160,16 @@ __global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardD
     const float* qc = qs + bm * wq;
     float* pw = part + (warp * 3 + bm) * wq;
 #pragma unroll
-    for (int i = 0; i < NCH; ++i) {
-      const int c = lane + 32 * i;
+    for (int c4 = 0; c4 < NCH; ++c4) {
+      const int c = lane + 32 * c4;
       if (c < d4) {
         const float4 cc = ld4(qc + 4 * c);
         const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 gc = make_float4(0.f, 0.f, 0.f, 0.f), go = gc;
-        Dist<BB>::grad(v[i].x, cc.x, oo.x, coef, a.alpha_box, gc.x, go.x);
-        Dist<BB>::grad(v[i].y, cc.y, oo.y, coef, a.alpha_box, gc.y, go.y);
-        Dist<BB>::grad(v[i].z, cc.z, oo.z, coef, a.alpha_box, gc.z, go.z);
-        Dist<BB>::grad(v[i].w, cc.w, oo.w, coef, a.alpha_box, gc.w, go.w);
+        Dist<BB>::grad(v[c4].x, cc.x, oo.x, coef, a.alpha_box, gc.x, go.x);
+        Dist<BB>::grad(v[c4].y, cc.y, oo.y, coef, a.alpha_box, gc.y, go.y);
+        Dist<BB>::grad(v[c4].z, cc.z, oo.z, coef, a.alpha_box, gc.z, go.z);
+        Dist<BB>::grad(v[c4].w, cc.w, oo.w, coef, a.alpha_box, gc.w, go.w);
         float4 p = ld4(pw + 4 * c);
         st4(pw + 4 * c, make_float4(p.x + gc.x, p.y + gc.y, p.z + gc.z, p.w + gc.w));
         if (BB == NGDB_Q2B) {
@@ -123,19 +178,21 @@ __global__ void __launch_bounds__(kThreads) shard_score_kernel(DevArgs a, ShardD
         }
       }
     }
+#pragma unroll
+    for (int c4 = 0; c4 < NCH; ++c4) v[c4] = vn[c4];
   }
   if (lane == 0) lred[warp] = loss;
   __syncthreads();
   for (int b = 0; b < k; ++b)
-    for (int e = threadIdx.x; e < wq; e += kThreads) {
-      float v = 0.f;
-      for (int w = 0; w < kWarps; ++w) v += part[(w * 3 + b) * wq + e];
-      dq_blk[static_cast<int64_t>(gslot[b] - q * sd.max_slots) * wq + e] = v;
+    for (int e = threadIdx.x; e < wq; e += kScoreThreads) {
+      float acc = 0.f;
+      for (int w = 0; w < kScoreWarps; ++w) acc += part[(w * 3 + b) * wq + e];
+      dq_blk[static_cast<int64_t>(gslot[b] - q * sd.max_slots) * wq + e] = acc;
     }
   if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < kWarps; ++w) t += lred[w];
-    dq_blk[static_cast<int64_t>(sd.max_slots) * wq + i] = t;
+    float tl = 0.f;
+    for (int w = 0; w < kScoreWarps; ++w) tl += lred[w];
+    dq_blk[static_cast<int64_t>(sd.max_slots) * wq + i] = tl;
   }
 }
 
@@ -217,14 +274,14 @@ int launch_shard_query_pack(const DevArgs& a, int first, int n, float* dst, cons
 int launch_shard_score(const DevArgs& a, const ShardDev& sd, const LaunchCtx& lc) {
   const int units = sd.world * sd.batch;
   if (units <= 0) return 0;
-  const size_t smem = static_cast<size_t>(3 + kWarps * 3) * a.wq * sizeof(float);
+  const size_t smem = static_cast<size_t>(3 + kScoreWarps * 3) * a.wq * sizeof(float);
   auto go = [&](auto kernel) {
     static bool configured = false;  // per instantiation
     if (!configured) {
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured = true;
     }
-    launch_pdl(kernel, dim3(units), dim3(kThreads), smem, lc.stream, 1, a, sd);
+    launch_pdl(kernel, dim3(units), dim3(kScoreThreads), smem, lc.stream, 1, a, sd);
   };
   if (a.dim <= 512) {
     if (a.backbone == NGDB_GQE) go(shard_score_kernel<NGDB_GQE, 4>);
