@@ -211,6 +211,19 @@ int ngdb_step_begin_ex(ngdb_ctx* ctx, const ngdb_step_plan* plan, int32_t flags)
  * An Intersect class is held until the next call, so that the next class of
  * the same PopBatch shares its launches; errors of a held class surface at the
  * next exec_pool / optimizer_step / step_end call. */
+/* Pre-packed plans (the trainer loop's producers pack off the consumer
+ * thread): the packed blob of a plan, pinned host memory for it, and a
+ * step_begin that only issues its H2D. The packed buffer must stay unchanged
+ * until the step's results have been collected (its copy is then long done). */
+int64_t ngdb_plan_packed_size(const ngdb_step_plan* plan);
+int ngdb_plan_pack(const ngdb_step_plan* plan, int32_t* out, int64_t cap);
+int ngdb_host_alloc(int64_t bytes, void** out); /* pinned (cudaMallocHost) */
+/* A context-owned pinned ring of at least `ints` int32 (kept across calls, so
+ * only the first trainer-loop call pays for the allocation). */
+int ngdb_ctx_pinned_ring(ngdb_ctx* ctx, int64_t ints, int32_t** base);
+int ngdb_host_free(void* p);
+int ngdb_step_begin_packed(ngdb_ctx* ctx, const ngdb_step_plan* plan, const int32_t* packed,
+                           int64_t n, int32_t flags);
 int ngdb_exec_pool(ngdb_ctx* ctx, const ngdb_pool_desc* pool);
 /* Sparse sorted-segment gradient reduce + touched-row Adam, then dense Adam
  * (SPEC.md:550-558 adam_step; Alg. 1 l.21 OptimizerStep). `step` is 1-based. */

@@ -317,6 +317,9 @@ struct ngdb_ctx {
   int64_t l2_flush_bytes = 0;
   // step timeline (NGDB_STEP_TIMELINE=1): timing events around each graph-launched step
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timeline;
+  // pinned ring of pre-packed plans (ngdb_ctx_pinned_ring; the trainer loop)
+  int32_t* pinned_ring = nullptr;
+  int64_t pinned_ring_ints = 0;
   // evaluator staging (ngdb_eval_ranks)
   char* eval_buf = nullptr;
   // evaluator entity table of the BetaE / fusion backbones over ALL entities
@@ -916,7 +919,7 @@ void launch_step(ngdb_ctx* c, const ngdb_plan* p) {
 }
 
 void upload_plan(ngdb_ctx* c, const ngdb_step_plan& plan, ngdb_plan* dst, int64_t& dst_cap,
-                 int32_t* staging, cudaStream_t s) {
+                 int32_t* staging, cudaStream_t s, const int32_t* prepacked = nullptr) {
   PlanLayout L(plan);
   if (L.total > dst_cap) {
     if (dst->blob) {
@@ -927,8 +930,9 @@ void upload_plan(ngdb_ctx* c, const ngdb_step_plan& plan, ngdb_plan* dst, int64_
     dst_cap = std::max<int64_t>(L.total + L.total / 2, dst_cap + dst_cap / 2);
     dst->blob = dmalloc<int32_t>(dst_cap);
   }
-  pack_plan(plan, L, staging);
-  CK(cudaMemcpyAsync(dst->blob, staging, L.total * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (!prepacked) pack_plan(plan, L, staging);
+  CK(cudaMemcpyAsync(dst->blob, prepacked ? prepacked : staging, L.total * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, s));
   c->h2d_bytes += L.total * sizeof(int32_t);
   dst->layout = L;
   dst->meta = meta_of(plan);
@@ -1136,6 +1140,7 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
       if (p.g) cudaFree(p.g);
     }
   if (c->eval_buf) cudaFree(c->eval_buf);
+  if (c->pinned_ring) cudaFreeHost(c->pinned_ring);
   if (c->evtab) cudaFree(c->evtab);
   if (c->ev_rows) cudaFree(c->ev_rows);
   if (c->ev_scratch) cudaFree(c->ev_scratch);
@@ -1297,6 +1302,66 @@ int ngdb_step_begin_ex(ngdb_ctx* c, const ngdb_step_plan* plan, int32_t flags) {
     CK(cudaStreamWaitEvent(c->copy_stream, c->blob_free[i], 0));
     upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->copy_stream);
     CK(cudaEventRecord(c->staged[i], c->copy_stream));
+    CK(cudaEventRecord(c->blob_ready[i], c->copy_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->blob_ready[i], 0));
+    ensure_step_buffers(c, c->stream_plan[i].meta);
+    c->active = &c->stream_plan[i];
+    c->prologue_pending = (flags & NGDB_BEGIN_DEFER_PROLOGUE) != 0;
+    if (!c->prologue_pending) {
+      begin_step_device(c);
+      prep_step(c, &c->stream_plan[i]);
+    }
+  });
+}
+
+int64_t ngdb_plan_packed_size(const ngdb_step_plan* plan) { return PlanLayout(*plan).total; }
+
+int ngdb_plan_pack(const ngdb_step_plan* plan, int32_t* out, int64_t cap) {
+  return guarded([&] {
+    validate_plan(*plan);
+    const PlanLayout L(*plan);
+    if (cap < L.total) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "plan_pack: buffer too small"};
+    pack_plan(*plan, L, out);
+  });
+}
+
+int ngdb_ctx_pinned_ring(ngdb_ctx* c, int64_t ints, int32_t** base) {
+  return guarded([&] {
+    if (ints > c->pinned_ring_ints) {
+      CK(cudaDeviceSynchronize());  // no copy may still read the old ring
+      if (c->pinned_ring) CK(cudaFreeHost(c->pinned_ring));
+      c->pinned_ring = nullptr;
+      void* p = nullptr;
+      CK(cudaMallocHost(&p, static_cast<size_t>(ints) * sizeof(int32_t)));
+      c->pinned_ring = static_cast<int32_t*>(p);
+      c->pinned_ring_ints = ints;
+    }
+    *base = c->pinned_ring;
+  });
+}
+
+int ngdb_host_alloc(int64_t bytes, void** out) {
+  return guarded([&] { CK(cudaMallocHost(out, static_cast<size_t>(bytes))); });
+}
+
+int ngdb_host_free(void* p) {
+  return guarded([&] {
+    if (p) CK(cudaFreeHost(p));
+  });
+}
+
+int ngdb_step_begin_packed(ngdb_ctx* c, const ngdb_step_plan* plan, const int32_t* packed,
+                           int64_t n, int32_t flags) {
+  return guarded([&] {
+    c->has_held = false;
+    if (c->world > 1) throw Fail{NGDB_ERR_CONFIG, "context is row-sharded: use ngdb_shard_begin"};
+    const PlanLayout L(*plan);
+    if (n != L.total) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "step_begin_packed: packed size"};
+    const int i = c->cur;
+    c->cur ^= 1;
+    CK(cudaEventRecord(c->blob_free[i ^ 1], c->stream));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->blob_free[i], 0));
+    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], nullptr, c->copy_stream, packed);
     CK(cudaEventRecord(c->blob_ready[i], c->copy_stream));
     CK(cudaStreamWaitEvent(c->stream, c->blob_ready[i], 0));
     ensure_step_buffers(c, c->stream_plan[i].meta);

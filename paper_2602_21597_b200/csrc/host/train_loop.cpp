@@ -23,6 +23,7 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 
 struct PlannedSlot {
   std::optional<StepPlanHost> plan;
+  int64_t packed_n = 0;          // the plan packed into the pinned ring slot of its index
   std::vector<int8_t> patterns;  // per query (difficulty feedback)
   SamplingDistribution pi;       // the π the batch was sampled with
   std::exception_ptr error;
@@ -66,6 +67,9 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
 
   int32_t P = cfg.n_producers;
   if (P <= 0) P = std::max(1, static_cast<int32_t>(std::thread::hardware_concurrency()) - 1);
+  // the pinned plan ring is sized from the configured depth (not the clamped
+  // one) so a short warm-up call allocates what later calls reuse
+  const int32_t depth_cfg = std::max(cfg.queue_depth > 0 ? cfg.queue_depth : 2 * P, 1);
   P = std::min(P, n_steps);
   const int32_t depth = std::max(cfg.queue_depth > 0 ? cfg.queue_depth : 2 * P, 1);
   stats.producers = P;
@@ -87,6 +91,17 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
     metrics.open(cfg.metrics_path, std::ios::app);
     if (!metrics) throw MissingFile("cannot open metrics log " + cfg.metrics_path);
   }
+
+  // pinned ring of packed plans: producers pack batch i into slot i % RP; a
+  // producer may claim i only while i < consumed + depth, and batch i - RP was
+  // collected by then (in_flight <= 3), so its H2D has long completed
+  // (one context-owned allocation, reused by later calls; a plan larger than
+  // its slot is packed by the consumer instead)
+  const int32_t RP = std::max(depth, depth_cfg) + 4;
+  const int64_t slot_ints = int64_t(cfg.batch) * (1 + cfg.n_neg) * 3 + int64_t(cfg.batch) * 512 + 65536;
+  int32_t* ring_base = nullptr;
+  check_status(ngdb_ctx_pinned_ring(ctx, slot_ints * RP, &ring_base));
+  auto slot_ptr = [&](int64_t i) { return ring_base + (i % RP) * slot_ints; };
 
   auto producer = [&] {
     for (;;) {
@@ -111,6 +126,12 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
         out.patterns.reserve(tb.queries.size());
         for (const auto& q : tb.queries) out.patterns.push_back(static_cast<int8_t>(q.pattern));
         out.plan.emplace(plan_training_step(tb, tc));
+        const ngdb_step_plan v = out.plan->view();
+        const int64_t need = ngdb_plan_packed_size(&v);
+        if (need <= slot_ints) {
+          check_status(ngdb_plan_pack(&v, slot_ptr(i), slot_ints));
+          out.packed_n = need;
+        }
       } catch (...) {
         out.error = std::current_exception();
       }
@@ -118,6 +139,7 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
         std::lock_guard<std::mutex> lk(mu);
         PlannedSlot& s = ring[i % depth];
         s.plan = std::move(out.plan);
+        s.packed_n = out.packed_n;
         s.patterns = std::move(out.patterns);
         s.pi = out.pi;
         s.error = out.error;
@@ -193,6 +215,7 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
         cv_space.notify_all();
       }
       StepPlanHost plan;
+      int64_t packed_n = 0;
       Pending pd;
       pd.index = i;
       {
@@ -203,6 +226,7 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
         stats.plan_wait_s += seconds_since(t0);
         if (s.error) std::rethrow_exception(s.error);
         plan = std::move(*s.plan);
+        packed_n = s.packed_n;
         pd.patterns = std::move(s.patterns);
         if (cfg.pi_per_step)
           std::copy(s.pi.weights.begin(), s.pi.weights.end(), cfg.pi_per_step + int64_t(i) * kPatternCount);
@@ -213,8 +237,11 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
       pd.peak_bytes = plan.trace.peak_bytes;
       const auto t_submit = std::chrono::steady_clock::now();
       const ngdb_step_plan view = plan.view();
-      // packs into pinned staging + one H2D; the step prologue goes into the graph
-      check_status(ngdb_step_begin_ex(ctx, &view, cfg.graphs ? NGDB_BEGIN_DEFER_PROLOGUE : 0));
+      // the producer packed the plan into pinned memory: one H2D; the step
+      // prologue goes into the graph
+      const int32_t bflags = cfg.graphs ? NGDB_BEGIN_DEFER_PROLOGUE : 0;
+      if (packed_n > 0) check_status(ngdb_step_begin_packed(ctx, &view, slot_ptr(i), packed_n, bflags));
+      else check_status(ngdb_step_begin_ex(ctx, &view, bflags));
       const auto t_pools = std::chrono::steady_clock::now();
       stats.begin_s += std::chrono::duration<double>(t_pools - t_submit).count();
       const int64_t step_no = first_step + i + 1;
@@ -238,9 +265,11 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
   } catch (...) {
     shutdown();
     for (const auto& pd : pending) ngdb_step_wait(ctx, pd.ticket, nullptr, 0, nullptr, nullptr);
+    ngdb_sync(ctx);  // no H2D may still read the ring
     throw;
   }
   shutdown();
+  ngdb_sync(ctx);
   return stats;
 }
 
