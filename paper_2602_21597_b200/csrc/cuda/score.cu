@@ -192,8 +192,12 @@ __device__ __forceinline__ float beta_qterm(const DevArgs& a, const float* q, in
   return dg_digamma(e < D ? A : B) - dg_digamma(A + B);
 }
 
+// 3 CTAs per SM (<= 72 registers) where that costs no spills; the BetaE
+// (linearised KL: query-side digamma terms) and d > 512 variants need more
+// registers and run 2 CTAs per SM spill-free
 template <int BB, int NCH, int MODE>
-__global__ void __launch_bounds__(kThreads, 3) stream_kernel(DevArgs a, int first, int n, int S) {
+__global__ void __launch_bounds__(kThreads, (BB == NGDB_BETAE || NCH > 4) ? 2 : 3)
+    stream_kernel(DevArgs a, int first, int n, int S) {
   extern __shared__ __align__(128) float smem[];
   __shared__ float lred[2 * kCWarps];
   __shared__ int last_flag;
