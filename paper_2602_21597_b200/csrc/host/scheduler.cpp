@@ -209,8 +209,9 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
   // output reuses a slab — for the writer and every reader of the slab's
   // previous tenant (WAW / WAR); invocations sharing a side buffer (the MLP
   // scratch and dense-gradient accumulators; the scoring partials) form chains.
-  std::vector<int32_t> writer, dep_scratch;
-  std::vector<std::vector<int32_t>> readers;
+  std::vector<int32_t> writer, rhead, dep_scratch;  // per tensor: writer, first reader entry
+  std::vector<std::pair<int32_t, int32_t>> rlist;   // reader entries (invocation, next)
+  rlist.reserve(4 * static_cast<size_t>(n));
   int32_t chain_last[2] = {-1, -1};
   inv_dep_off_.assign(1, 0);
   inv_deps_.clear();
@@ -223,8 +224,8 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
   auto track = [&](const int32_t* nodes, int32_t count, OpKind kind) {
     const int32_t inv = static_cast<int32_t>(inv_dep_off_.size()) - 1;
     if (static_cast<int32_t>(writer.size()) < arena.size()) {
-      writer.resize(arena.size(), -1);
-      readers.resize(arena.size());
+      writer.resize(arena.size() + 1024, -1);
+      rhead.resize(arena.size() + 1024, -1);
     }
     dep_scratch.clear();
     auto add = [&](int32_t d) {
@@ -235,7 +236,8 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
       for_each_input(o, [&](int32_t t) {
         if (t < 0) return;
         add(writer[t]);
-        readers[t].push_back(inv);
+        rlist.emplace_back(inv, rhead[t]);
+        rhead[t] = static_cast<int32_t>(rlist.size()) - 1;
       });
       const int32_t t_out = f.nodes[o].op.dir == Direction::Fwd ? t_fwd[o] : t_bwd[o];
       if (t_out >= 0) {
@@ -243,7 +245,7 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
         const int32_t p = arena.prev_tenant(t_out);
         if (p >= 0) {
           add(writer[p]);
-          for (int32_t r : readers[p]) add(r);
+          for (int32_t r = rhead[p]; r >= 0; r = rlist[r].second) add(rlist[r].first);
         }
       }
     }
