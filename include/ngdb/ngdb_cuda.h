@@ -349,14 +349,14 @@ int ngdb_read_score_queries(ngdb_ctx* ctx, float* host, int64_t n_slots);
  * ignored). ranks[q] = 1 + #{e not in filter+target: d(e) < d(target)}
  * + floor(#ties / 2). Synchronous. Backbones: GQE (L1), Q2B (box), BetaE
  * (queries alpha | beta, distance KL(entity || query)), GQE + FuseSemantic (L1
- * against the fused rows); BetaE + FuseSemantic (Psi_theta) is
- * NGDB_ERR_MISSING_KERNEL. A target inside its own filter is NGDB_ERR_DOMAIN
- * (SPEC TargetFiltered). */
+ * against the fused rows), BetaE + FuseSemantic (KL against Psi_theta's Beta
+ * parameters). A target inside its own filter is NGDB_ERR_DOMAIN (SPEC
+ * TargetFiltered). */
 /* The evaluator's entity table for the current parameters (tests / callers):
  * BetaE rows T_e = [psi(s)-psi(a) | psi(s)-psi(b)] [n_entities][2d] and consts
  * C_e [n_entities] of KL(entity || query) = lnB(q) + C_e + <q, T_e>; fusion
- * rows sigma(W_p [h | F s] + b_p) [n_entities][d] (consts NULL); GQE / Q2B the
- * entity table itself. */
+ * rows sigma(W_p [h | F s] + b_p) [n_entities][d] (consts NULL; BetaE +
+ * fusion: T_e, C_e of Psi_theta's rows); GQE / Q2B the entity table itself. */
 int ngdb_eval_entity_table(ngdb_ctx* ctx, float* rows, int64_t n_rows_floats, float* consts,
                            int64_t n_consts);
 int ngdb_eval_ranks(ngdb_ctx* ctx, const float* queries, int32_t n_queries, const int32_t* targets,

@@ -265,7 +265,6 @@ int oracle_model_set_semantic(void* mp, int32_t dl, const float* store, int64_t 
   return guard([&] {
     auto* a = static_cast<AnyModel*>(mp);
     auto set = [&](auto& md) {
-      if (md.backbone == 2) throw std::runtime_error("BetaE fusion (Psi_theta) not restated");
       if (md.dl) throw std::runtime_error("semantic store already set");
       if (n != (int64_t)md.ne * dl) throw std::runtime_error("semantic store size");
       md.setup_semantic(dl, store);

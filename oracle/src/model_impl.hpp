@@ -9,7 +9,10 @@
 //                 (forms of SURVEY A-7); union SPEC.md:404-412;
 //                 loss SPEC.md:541-549 with psi per SPEC.md:431
 //   fusion        fuse_semantic SPEC.md:413-421 (Eq. 12): sigma(W_p [h | F s] + b_p) for
-//                 anchors AND candidates; the store s is frozen
+//                 anchors AND candidates; the store s is frozen. BetaE
+//                 additionally routes the fused vector through Psi_theta (Eq. 3,
+//                 PAPER.md:165-168): a linear map d -> 2d' whose
+//                 output is realised by the softplus clamp; h is then d wide
 //   adam          SPEC.md:550-558 (dense) and the lazy touched-row variant (A-9)
 // Every kernel runs node by node (the "looped" form); batching only changes
 // which nodes run together, never the arithmetic of one node.
@@ -100,7 +103,17 @@ struct Model {
     add("fus_f", d, dl);       // F: d_l -> d, no bias (SURVEY A-7)
     add("fus_wp", d, 2 * d);   // W_p: [h | F s] -> d
     add("fus_bp", 1, d);       // b_p
+    if (backbone == 2) {  // Psi_theta: fused d -> pre-activation [alpha | beta] (2d')
+      add("fus_psi", 2 * d, d);
+      add("fus_psi_b", 1, 2 * d);
+      // the structural embedding h is d wide (the entity table of the joint space)
+      ew = d;
+      shape["entity"] = {ne, ew};
+      for (auto* m : {&P, &M, &V, &G}) (*m)["entity"].assign((int64_t)ne * ew, R(0));
+    }
   }
+  // width of a fused row: d, or the 2d' pre-activation Beta parameters (BetaE)
+  int fuse_width() const { return backbone == 2 ? 2 * d : d; }
 
   // ---- distances -----------------------------------------------------------
   static R softplus(R x) { return x > 0 ? x + mlog1p(mexp(-x)) : mlog1p(mexp(x)); }
@@ -479,20 +492,29 @@ struct Model {
   }
 
   // ---- FuseSemantic -----------------------------------------
-  void fuse_fwd(int e, R* out, std::vector<R>* xkeep = nullptr) const {
+  void fuse_fwd(int e, R* out, std::vector<R>* xkeep = nullptr,
+                std::vector<R>* ekeep = nullptr) const {
     std::vector<R> x(2 * d), z(d);
     const R* h = erow(e);
     for (int i = 0; i < d; ++i) x[i] = h[i];
     mv("fus_f", "", &sem[(int64_t)e * dl], x.data() + d);
     mv("fus_wp", "fus_bp", x.data(), z.data());
-    for (int i = 0; i < d; ++i) out[i] = sigm(z[i]);
+    std::vector<R> ef(d);
+    for (int i = 0; i < d; ++i) ef[i] = sigm(z[i]);
+    if (backbone == 2) mv("fus_psi", "fus_psi_b", ef.data(), out);  // Psi_theta
+    else for (int i = 0; i < d; ++i) out[i] = ef[i];
     if (xkeep) *xkeep = std::move(x);
+    if (ekeep) *ekeep = std::move(ef);
   }
-  // g = dL/d e_fused: grads to h (entity row), F, W_p, b_p; never to the store
+  // g = dL/d(fused row): grads to h (entity row), F, W_p, b_p (and Psi_theta for
+  // BetaE); never to the store
   void fuse_bwd(int e, const R* g) {
-    std::vector<R> x, y(d), gz(d), gx(2 * d, R(0));
-    fuse_fwd(e, y.data(), &x);
-    for (int i = 0; i < d; ++i) gz[i] = g[i] * y[i] * (R(1) - y[i]);
+    std::vector<R> x, ef, y(fuse_width()), gz(d), gx(2 * d, R(0));
+    fuse_fwd(e, y.data(), &x, &ef);
+    std::vector<R> gef(d, R(0));  // dL / d sigma(z)
+    if (backbone == 2) mv_bwd("fus_psi", "fus_psi_b", ef.data(), g, gef.data());
+    else for (int i = 0; i < d; ++i) gef[i] = g[i];
+    for (int i = 0; i < d; ++i) gz[i] = gef[i] * ef[i] * (R(1) - ef[i]);
     mv_bwd("fus_wp", "fus_bp", x.data(), gz.data(), gx.data());
     R* ge = gerow(e);
     for (int i = 0; i < d; ++i) ge[i] += gx[i];
@@ -503,7 +525,7 @@ struct Model {
     if (!dl) return erow(e);
     auto& v = fcache[e];
     if (v.empty()) {
-      v.resize(d);
+      v.resize(fuse_width());
       fuse_fwd(e, v.data());
     }
     return v.data();
@@ -511,7 +533,7 @@ struct Model {
   R* cgrow(int e) {
     if (!dl) return gerow(e);
     auto& v = fgrad[e];
-    if (v.empty()) v.assign(d, R(0));
+    if (v.empty()) v.assign(fuse_width(), R(0));
     return v.data();
   }
   void flush_fused_grads() {
@@ -691,8 +713,15 @@ struct Exec {
         for (int i = 0; i < md.ew; ++i) out[i] = e[i];
         break;
       }
-      case K_FUSE: {  // fused anchor row; Q2B point box (zero offset)
+      case K_FUSE: {  // fused anchor row; Q2B point box (zero offset); BetaE realised
         const R* e = md.crow(x.payload);
+        if (md.backbone == 2) {
+          for (int i = 0; i < md.wq; ++i) {
+            out[i] = Model<R>::realize(e[i]);
+            ekink(x.query, double(Model<R>::softplus(e[i])) - 0.05);
+          }
+          break;
+        }
         for (int i = 0; i < md.wq; ++i) out[i] = i < d ? e[i] : R(0);
         break;
       }
@@ -814,6 +843,12 @@ struct Exec {
         break;
       }
       case K_FUSE:
+        if (md.backbone == 2) {  // through the realisation, into the fused row
+          const R* e = md.crow(m.payload);
+          R* gy = md.cgrow(m.payload);
+          for (int i = 0; i < md.wq; ++i) gy[i] += gin[i] * md.drealize_k(e[i]);
+          break;
+        }
         md.fuse_bwd(m.payload, gin);
         break;
       case K_PROJ: {

@@ -114,6 +114,12 @@ SIGNATURES = {
     "ngdb_set_step": (C.c_int, [C.c_void_p, i64]),
     "ngdb_shard_optimizer": (C.c_int, [C.c_void_p, i64]),
     "ngdb_exec_flush": (C.c_int, [C.c_void_p]),
+    "ngdb_plan_packed_size": (i64, [P(StepPlan)]),
+    "ngdb_plan_pack": (C.c_int, [P(StepPlan), P(i32), i64]),
+    "ngdb_host_alloc": (C.c_int, [i64, P(C.c_void_p)]),
+    "ngdb_host_free": (C.c_int, [C.c_void_p]),
+    "ngdb_ctx_pinned_ring": (C.c_int, [C.c_void_p, i64, P(P(i32))]),
+    "ngdb_step_begin_packed": (C.c_int, [C.c_void_p, P(StepPlan), P(i32), i64, i32]),
     "ngdb_read_arena": (C.c_int, [C.c_void_p, i64, i64, P(f32)]),
     "ngdb_set_gemm_split": (C.c_int, [i32]),
     "ngdb_comm_unique_id": (C.c_int, [P(C.c_uint8)]),

@@ -49,7 +49,9 @@ __global__ void __launch_bounds__(kWarps * 32) beta_prep_kernel(DevArgs a, Spars
     if (code >= 0) a.cand_local[code] = r;
   }
   const int D = a.dim, d4 = D / 4;
-  const float* x = a.ent + static_cast<int64_t>(t.rows[r]) * a.ent_w;
+  // the raw Beta pre-activations: the entity row, or (FuseSemantic) Psi_theta's row
+  const float* x = a.ytab ? a.ytab + static_cast<int64_t>(r) * a.ent_w
+                          : a.ent + static_cast<int64_t>(t.rows[r]) * a.ent_w;
   float* L = a.etab + static_cast<int64_t>(r) * a.ent_w;
   float c = 0.f;
   for (int ch = lane; ch < d4; ch += 32) {
@@ -136,6 +138,57 @@ __global__ void __launch_bounds__(kWarps * 32) beta_entity_adam_kernel(DevArgs a
       st4(wp + off, w);
       st4(mp + off, m);
       st4(vp + off, v);
+    }
+  }
+}
+
+// ---- FuseSemantic (Psi_theta): dL/dY instead of an Adam update ----------------
+// The same gradient as beta_entity_adam_kernel with the pre-activations read
+// from Y (CSR row order) and the result written out for Psi_theta's backward.
+__global__ void __launch_bounds__(kWarps * 32) beta_fuse_grad_kernel(DevArgs a, SparseTable t,
+                                                                     float* gY, Split gYs) {
+  pdl_start();
+  const int r = blockIdx.x * kWarps + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= t.n_rows) return;
+  const int beg = t.seg[r], end = t.seg[r + 1];
+  const int D = a.dim, d4 = D / 4, W = a.ent_w;  // W = 2d
+  float S = 0.f;
+  for (int kk = beg; kk < end; ++kk) {
+    const int32_t code = __ldg(t.contrib + kk);
+    if (code >= 0) S += __ldg(a.coefbuf + code);
+  }
+  const float* yp = a.ytab + static_cast<int64_t>(r) * W;
+  for (int ch = lane; ch < d4; ch += 32) {
+    float gA[4] = {0, 0, 0, 0}, gB[4] = {0, 0, 0, 0}, GA[4] = {0, 0, 0, 0}, GB[4] = {0, 0, 0, 0};
+    for (int kk = beg; kk < end; ++kk) {
+      const int32_t code = __ldg(t.contrib + kk);
+      if (code < 0) {
+        const float* g = a.agbuf + static_cast<int64_t>(-code - 1) * W;
+        const float4 u = ld4(g + 4 * ch), v = ld4(g + D + 4 * ch);
+        gA[0] += u.x; gA[1] += u.y; gA[2] += u.z; gA[3] += u.w;
+        gB[0] += v.x; gB[1] += v.y; gB[2] += v.z; gB[3] += v.w;
+      } else {
+        const float coef = __ldg(a.coefbuf + code);
+        const float* q = a.qbuf + static_cast<int64_t>(code / a.ncand) * a.wq;
+        const float4 u = ld4(q + 4 * ch), v = ld4(q + D + 4 * ch);
+        GA[0] += coef * u.x; GA[1] += coef * u.y; GA[2] += coef * u.z; GA[3] += coef * u.w;
+        GB[0] += coef * v.x; GB[1] += coef * v.y; GB[2] += coef * v.z; GB[3] += coef * v.w;
+      }
+    }
+    const float4 xa = ld4(yp + 4 * ch), xb = ld4(yp + D + 4 * ch);
+    const float va[4] = {xa.x, xa.y, xa.z, xa.w}, vb[4] = {xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float al, dal, be, dbe;
+      beta_realize_pair(va[u], al, dal);
+      beta_realize_pair(vb[u], be, dbe);
+      const float s = al + be;
+      const float ta = dg_trigamma_fast(al), tb = dg_trigamma_fast(be), ts = dg_trigamma_fast(s);
+      const float dA = gA[u] + S * (al * ta - s * ts) + GA[u] * (ts - ta) + GB[u] * ts;
+      const float dB = gB[u] + S * (be * tb - s * ts) + GA[u] * ts + GB[u] * (ts - tb);
+      put(gY, gYs, static_cast<int64_t>(r) * W + 4 * ch + u, dA * dal);
+      put(gY, gYs, static_cast<int64_t>(r) * W + D + 4 * ch + u, dB * dbe);
     }
   }
 }
@@ -468,6 +521,14 @@ int launch_beta_prep(const DevArgs& a, const SparseTable& t, const LaunchCtx& lc
   if (t.n_rows <= 0) return 0;
   launch_pdl(beta_prep_kernel, dim3((t.n_rows + kWarps - 1) / kWarps), dim3(kWarps * 32), 0,
              lc.stream, 1, a, t);
+  return 1;
+}
+
+int launch_beta_fuse_grad(const DevArgs& a, const SparseTable& t, float* gY, Split gYs,
+                          const LaunchCtx& lc) {
+  if (t.n_rows <= 0) return 0;
+  launch_pdl(beta_fuse_grad_kernel, dim3((t.n_rows + kWarps - 1) / kWarps), dim3(kWarps * 32), 0,
+             lc.stream, 1, a, t, gY, gYs);
   return 1;
 }
 

@@ -81,6 +81,9 @@ struct DevArgs {
   // receive order [n_recv][ent_w]; anc_pos[anchor slot] = its receive position
   const float* anc_rows;
   const int32_t* anc_pos;
+  // BetaE with FuseSemantic: Psi_theta output rows Y [touched row][2d] (the
+  // pre-activation Beta parameters, CSR row order); nullptr otherwise
+  const float* ytab;
   // Intersect stash: per forward node (slot = node aux) the MLP intermediates
   // its mirror reads instead of recomputing them; istash_slots slots of
   // kStashPerSlot * dim floats
@@ -308,6 +311,9 @@ int launch_beta_prep(const DevArgs& a, const SparseTable& t, const LaunchCtx& lc
 // fuse.cu: step prologue (etab = e_fused of the touched rows) and the fused
 // backward + entity Adam
 int64_t fuse_scratch_floats(int d, int dl, int64_t rows);
+// BetaE with FuseSemantic: the Psi_theta output rows Y [u][2d] inside the scratch
+float* fuse_y_table(float* fs, int64_t cap, int u, int d, int dl);
+
 int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const LaunchCtx& lc);
 int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const AdamHyper& hp,
                   const float* bc, const LaunchCtx& lc);

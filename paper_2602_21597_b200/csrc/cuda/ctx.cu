@@ -341,6 +341,9 @@ struct ngdb_ctx {
   bool beta() const { return desc.backbone == NGDB_BETAE; }
   bool fused() const { return desc.semantic_dim > 0; }
   bool step_table() const { return beta() || fused(); }  // per-step entity table
+  // width of the entity rows the operators see (anchors, candidates, anchor
+  // gradients, the step table): BetaE 2d (with FuseSemantic: Psi_theta's rows)
+  int64_t op_ent_w() const { return beta() ? 2 * int64_t(desc.dim) : params[ent_idx].cols; }
   cudaEvent_t take_event() {
     if (!event_pool.empty()) {
       cudaEvent_t e = event_pool.back();
@@ -387,7 +390,7 @@ void ensure_f(float*& p, int64_t& cap, int64_t need) {
 
 void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
   const int64_t wq = c->query_width();
-  const int64_t ew = c->params[c->ent_idx].cols, rw = c->params[c->rel_idx].cols;
+  const int64_t ew = c->op_ent_w(), rw = c->params[c->rel_idx].cols;
   bool grow = m.n_score > c->cap_score || m.n_anchor > c->cap_anchor ||
               m.n_project > c->cap_project || m.n_queries > c->cap_queries ||
               m.n_candidates != c->cap_cand;
@@ -453,7 +456,7 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.backbone = c->desc.backbone;
   a.dim = c->desc.dim;
   a.wq = c->query_width();
-  a.ent_w = static_cast<int32_t>(c->params[c->ent_idx].cols);
+  a.ent_w = static_cast<int32_t>(c->op_ent_w());
   a.rel_w = static_cast<int32_t>(c->params[c->rel_idx].cols);
   a.ncand = p ? p->meta.n_candidates : 0;
   a.n_neg = c->desc.n_neg;
@@ -493,6 +496,10 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.fus_idx = c->fus_idx;
   a.anc_rows = c->anc_rows;
   a.anc_pos = c->anc_pos;
+  a.ytab = (c->beta() && c->fused() && p && c->fscratch)
+               ? fuse_y_table(c->fscratch, c->fscratch_cap, p->meta.n_erows, c->desc.dim,
+                              c->desc.semantic_dim)
+               : nullptr;
   a.istash = c->istash;
   a.istash_slots = c->istash_slots;
   a.pstash = c->pstash;
@@ -977,8 +984,6 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     if (d.n_entities < 1 || d.n_relations < 1) throw Fail{NGDB_ERR_CONFIG, "empty tables"};
     if (d.semantic_dim < 0 || d.semantic_dim % 4 != 0 || d.semantic_dim > 4096)
       throw Fail{NGDB_ERR_CONFIG, "semantic_dim must be a multiple of 4, <= 4096"};
-    if (d.semantic_dim > 0 && d.backbone == NGDB_BETAE)
-      throw Fail{NGDB_ERR_MISSING_KERNEL, "BetaE + FuseSemantic (Psi_theta) not built"};
     const int world = d.world > 1 ? d.world : 1;
     if (world > 1 && (d.rank < 0 || d.rank >= world)) throw Fail{NGDB_ERR_CONFIG, "rank out of range"};
     if (world > 1 && (d.backbone == NGDB_BETAE || d.semantic_dim > 0))
@@ -1007,7 +1012,8 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       add_param(c, "int_w1", D, D, false);
       add_param(c, "int_w2", D, D, false);
     } else if (d.backbone == NGDB_BETAE) {  // DESIGN.md §3.5; order = trainer.hpp param_specs
-      add_param(c, "entity", d.n_entities, 2 * D, true);
+      // with FuseSemantic the structural row h is d wide; Psi_theta makes the 2d
+      add_param(c, "entity", d.n_entities, d.semantic_dim > 0 ? D : 2 * D, true);
       add_param(c, "relation", d.n_relations, D, true);
       add_param(c, "prj_w1", 2 * D, 3 * D, false);
       add_param(c, "prj_b1", 1, 2 * D, false);
@@ -1036,6 +1042,10 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       add_param(c, "fus_f", D, d.semantic_dim, false);
       add_param(c, "fus_wp", D, 2 * D, false);
       add_param(c, "fus_bp", 1, D, false);
+      if (d.backbone == NGDB_BETAE) {  // Psi_theta (Eq. 3)
+        add_param(c, "fus_psi", 2 * D, D, false);
+        add_param(c, "fus_psi_b", 1, 2 * D, false);
+      }
     }
     // dense tensors share one flat buffer (one Adam launch, one memset)
     int64_t off = 0;
@@ -1933,8 +1943,6 @@ int64_t eval_row_width(const ngdb_ctx* c) {
 std::pair<const float*, const float*> eval_entity_table(ngdb_ctx* c) {
   const Param& ent = c->params[c->ent_idx];
   if (!c->beta() && !c->fused()) return {ent.w, nullptr};
-  if (c->beta() && c->fused())
-    throw Fail{NGDB_ERR_MISSING_KERNEL, "eval_ranks: BetaE + FuseSemantic (Psi_theta)"};
   const int64_t N = c->desc.n_entities, w = eval_row_width(c);
   if (!c->evtab) {
     c->evtab = dmalloc<float>(N * w + N);
@@ -1949,9 +1957,9 @@ std::pair<const float*, const float*> eval_entity_table(ngdb_ctx* c) {
   const SparseTable t{ent.w, ent.m, ent.v, nullptr, static_cast<int32_t>(ent.cols),
                       static_cast<int32_t>(N), c->ev_rows, c->ev_rows + N, nullptr};
   const LaunchCtx lc{c->stream, c->num_sms};
-  if (c->beta()) {
+  if (c->beta() && !c->fused()) {
     c->launches += launch_beta_prep(a, t, lc);
-  } else {
+  } else {  // fusion (BetaE: Psi_theta rows, then the same prologue kernel)
     if (!c->sem) throw Fail{NGDB_ERR_CONFIG, "semantic store not uploaded (ngdb_semantic_upload)"};
     const int64_t need = fuse_scratch_floats(c->desc.dim, c->desc.semantic_dim, N);
     if (need > c->ev_scratch_cap) {

@@ -16,6 +16,15 @@
 // sigma' -> dZ; then dX = dZ W_p, dW_p += dZ^T X, db_p += colsum dZ,
 // dF += (dX[:, d:])^T S, and the entity rows take Adam on dX[:, :d]. The store
 // is never written (frozen: its gradient is exactly zero).
+//
+// BetaE (Psi_theta, Eq. 3): h is d wide and the
+// fused vector E = sigma(Z) is mapped to the 2d' Beta pre-activations
+// Y = E W_psi^T + b_psi by one more GEMM; the step's BetaE entity table (the
+// KL linearisation T_e, C_e) is then evaluated from Y by the same prologue
+// kernel as the plain backbone (beta_prep), FuseSemantic anchors realise their
+// Y rows, and the backward starts from dL/dY (beta_fuse_grad: anchor and
+// candidate terms through realize') -> dE = dY W_psi, dW_psi += dY^T E,
+// db_psi += colsum dY, dZ = dE * E (1 - E), then the chain above.
 #include <algorithm>
 
 #include "common.cuh"
@@ -28,21 +37,29 @@ constexpr int kWarps = 8;
 
 struct FuseBufs {
   int u, uP, d, dl;
+  bool beta;
   float* S;  Split Ss;    // [u][dl]   gathered store rows
   float* X;  Split Xs;    // [u][2d]   [h | F s]
   float* Zf;              // [u][d]    pre-activation
   float* dZ; Split dZs;   // [u][d]
   float* dX;              // [u][2d]   dZ W_p
   Split dZT, XT, dFsT, ST;  // transposed splits, rows padded to uP
+  // BetaE (Psi_theta)
+  float* E;  Split Es;    // [u][d]    sigma(Z)
+  float* Y;               // [u][2d]   Beta pre-activations (read by the step's kernels)
+  float* dY; Split dYs;   // [u][2d]
+  float* dE;              // [u][d]
+  Split dYT, ET;          // transposed splits [uP][2d], [uP][d]
 };
 
-FuseBufs carve(float* base, int64_t cap, int u, int d, int dl) {
+FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
   Scratch sc{base, cap};
   FuseBufs f{};
   f.u = u;
   f.uP = (u + 3) & ~3;
   f.d = d;
   f.dl = dl;
+  f.beta = beta;
   const int64_t U = u, UP = f.uP;
   f.S = sc.take(U * dl);
   f.Ss = take_split(sc, U * dl);
@@ -56,6 +73,16 @@ FuseBufs carve(float* base, int64_t cap, int u, int d, int dl) {
   f.XT = take_split(sc, UP * 2 * d);
   f.dFsT = take_split(sc, UP * d);
   f.ST = take_split(sc, UP * dl);
+  if (beta) {
+    f.E = sc.take(U * d);
+    f.Es = take_split(sc, U * d);
+    f.Y = sc.take(U * 2 * d);
+    f.dY = sc.take(U * 2 * d);
+    f.dYs = take_split(sc, U * 2 * d);
+    f.dE = sc.take(U * d);
+    f.dYT = take_split(sc, UP * 2 * d);
+    f.ET = take_split(sc, UP * d);
+  }
   return f;
 }
 
@@ -79,7 +106,7 @@ __global__ void __launch_bounds__(kWarps * 32) fuse_gather_kernel(DevArgs a, Spa
 #pragma unroll
     for (int q = 0; q < 4; ++q) put(f.S, f.Ss, (int64_t)r * f.dl + 4 * c + q, vv[q]);
   }
-  const float* h = a.ent + e * a.ent_w;
+  const float* h = a.ent + e * f.d;  // the structural row (d wide)
   for (int c = lane; c < f.d / 4; c += 32) {
     const float4 v = ld4(h + 4 * c);
     const float vv[4] = {v.x, v.y, v.z, v.w};
@@ -88,11 +115,23 @@ __global__ void __launch_bounds__(kWarps * 32) fuse_gather_kernel(DevArgs a, Spa
   }
 }
 
-__global__ void fuse_sigmoid_kernel(const float* Z, float* E, int64_t n) {
+__global__ void fuse_sigmoid_kernel(const float* Z, float* E, Split Es, int64_t n) {
   pdl_start();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    E[i] = sigmoidf(Z[i]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (Es.hi) put(E, Es, i, sigmoidf(Z[i]));
+    else E[i] = sigmoidf(Z[i]);
+  }
+}
+
+// BetaE: dZ = dE * E (1 - E), plain + split
+__global__ void fuse_dz_kernel(const float* dE, const float* E, float* dZ, Split dZs, int64_t n) {
+  pdl_start();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float e = E[i];
+    put(dZ, dZs, i, dE[i] * e * (1.f - e));
+  }
 }
 
 template <int BB>
@@ -174,13 +213,19 @@ inline int row_blocks(int n) { return (n + kWarps - 1) / kWarps; }
 
 int64_t fuse_scratch_floats(int d, int dl, int64_t rows) {
   const int64_t U = rows + 4;
-  return U * (3 * dl + 6 * d + d + 3 * d + 2 * d) + U * (2 * d + 4 * d + 2 * d + 2 * dl) + 4096;
+  return U * (3 * dl + 6 * d + d + 3 * d + 2 * d) + U * (2 * d + 4 * d + 2 * d + 2 * dl) +
+         U * (3 * d + 2 * d + 6 * d + d + 4 * d + 2 * d) + 4096;  // + the BetaE (Psi) buffers
+}
+
+float* fuse_y_table(float* fs, int64_t cap, int u, int d, int dl) {
+  return carve(fs, cap, u, d, dl, true).Y;
 }
 
 int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
+  const bool beta = a.backbone == NGDB_BETAE;
   const int d = a.dim, dl = a.sem_dim, u = t.n_rows;
-  FuseBufs f = carve(fs, cap, u, d, dl);
+  FuseBufs f = carve(fs, cap, u, d, dl, beta);
   const float* p = a.dense;
   int launches = 0;
   launch_pdl(fuse_gather_kernel, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
@@ -196,23 +241,63 @@ int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
   launches += tc_gemm(g2, lc.stream);
   const int64_t n = (int64_t)u * d;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)lc.num_sms * 8);
-  launch_pdl(fuse_sigmoid_kernel, dim3(blocks), dim3(256), 0, lc.stream, 1, (const float*)f.Zf, a.etab, n);
-  return launches + 1;
+  if (!beta) {
+    launch_pdl(fuse_sigmoid_kernel, dim3(blocks), dim3(256), 0, lc.stream, 1, (const float*)f.Zf,
+               a.etab, Split{nullptr, nullptr}, n);
+    return launches + 1;
+  }
+  launch_pdl(fuse_sigmoid_kernel, dim3(blocks), dim3(256), 0, lc.stream, 1, (const float*)f.Zf, f.E,
+             f.Es, n);
+  // Psi_theta: Y = E W_psi^T + b_psi, then the BetaE entity table from Y
+  TcGemmArgs gy = gemm_args(u, 2 * d, d, op(f.Es, d), wop(a, a.fus_idx + 3, 2 * d, d, false), f.Y, 2 * d);
+  gy.bias = p + a.dense_off[a.fus_idx + 4];
+  launches += tc_gemm(gy, lc.stream);
+  DevArgs ay = a;
+  ay.ytab = f.Y;
+  return launches + 1 + launch_beta_prep(ay, t, lc);
 }
 
 int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const AdamHyper& hp,
                   const float* bc, const LaunchCtx& lc) {
   if (t.n_rows <= 0) return 0;
+  const bool beta = a.backbone == NGDB_BETAE;
   const int d = a.dim, dl = a.sem_dim, u = t.n_rows;
-  FuseBufs f = carve(fs, cap, u, d, dl);
+  FuseBufs f = carve(fs, cap, u, d, dl, beta);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
   int launches = 0;
-  if (a.backbone == NGDB_GQE)
+  if (beta) {
+    // dL/dY through realize' (anchor + candidate terms), then Psi_theta's backward
+    DevArgs ay = a;
+    ay.ytab = f.Y;
+    launches += launch_beta_fuse_grad(ay, t, f.dY, f.dYs, lc);
+    TcGemmArgs ge = gemm_args(u, d, 2 * d, op(f.dYs, 2 * d), wop(a, a.fus_idx + 3, 2 * d, d, true),
+                              f.dE, d);  // dE = dY W_psi
+    launches += tc_gemm(ge, lc.stream);
+    SplitJobs pj{};
+    pj.job[0] = {f.dY, u, 2 * d, 2 * d, 0, f.dYT.hi, f.dYT.lo};
+    pj.job[1] = {f.E, u, d, d, 0, f.ET.hi, f.ET.lo};
+    pj.n = 2;
+    launches += split_transposed(pj, lc.stream);
+    TcGemmArgs gw = gemm_args(2 * d, d, u, op(f.dYT, f.uP), op(f.ET, f.uP), g + off[a.fus_idx + 3], d);
+    gw.accumulate = 1;  // dW_psi += dY^T E
+    launches += tc_gemm(gw, lc.stream);
+    ColsumJobs pc{};
+    pc.job[0] = {f.dY, u, 2 * d, g + off[a.fus_idx + 4]};
+    pc.n = 1;
+    launches += colsums(pc, 2 * d, lc.stream);
+    const int64_t n = (int64_t)u * d;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)lc.num_sms * 8);
+    launch_pdl(fuse_dz_kernel, dim3(blocks), dim3(256), 0, lc.stream, 1, (const float*)f.dE,
+               (const float*)f.E, f.dZ, f.dZs, n);
+    ++launches;
+  } else if (a.backbone == NGDB_GQE) {
     launch_pdl(fuse_grad_kernel<NGDB_GQE>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
-  else
+    ++launches;
+  } else {
     launch_pdl(fuse_grad_kernel<NGDB_Q2B>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
-  ++launches;
+    ++launches;
+  }
   // dX = dZ W_p  ([u][2d]; first half -> entity rows, second half -> F s)
   TcGemmArgs g3 = gemm_args(u, 2 * d, d, op(f.dZs, d), wop(a, a.fus_idx + 1, d, 2 * d, true), f.dX, 2 * d);
   launches += tc_gemm(g3, lc.stream);

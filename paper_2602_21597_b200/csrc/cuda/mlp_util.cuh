@@ -26,6 +26,10 @@ struct Split {
 };
 inline Split take_split(Scratch& s, int64_t n) { return {s.take(n), s.take(n)}; }
 
+// BetaE with FuseSemantic (beta.cu): dL/dY of the touched rows (plain + split)
+int launch_beta_fuse_grad(const DevArgs& a, const SparseTable& t, float* gY, Split gYs,
+                          const LaunchCtx& lc);
+
 inline SplitOperand op(Split x, int ld) { return {x.hi, x.lo, ld}; }
 
 // Grid of the per-node elementwise kernels: blockIdx.x = node, blockIdx.y

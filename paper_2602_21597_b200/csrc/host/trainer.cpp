@@ -19,7 +19,10 @@ std::vector<ParamSpec> param_specs(Backbone b, int32_t n_ent, int32_t n_rel, int
                                    int32_t semantic_dim) {
   const int64_t d = dim;
   std::vector<ParamSpec> s;
-  s.push_back({"entity", n_ent, entity_width(b, dim), true});
+  // BetaE with FuseSemantic: the structural embedding h is d wide and Psi_theta
+  // maps the fused vector to the 2d' Beta parameters (Eq. 3)
+  const bool beta_fused = b == Backbone::BETAE && semantic_dim > 0;
+  s.push_back({"entity", n_ent, beta_fused ? d : entity_width(b, dim), true});
   s.push_back({"relation", n_rel, relation_width(b, dim), true});
   if (b == Backbone::GQE) {
     s.push_back({"int_w1", d, d, false});
@@ -46,6 +49,10 @@ std::vector<ParamSpec> param_specs(Backbone b, int32_t n_ent, int32_t n_rel, int
     s.push_back({"fus_f", d, semantic_dim, false});
     s.push_back({"fus_wp", d, 2 * d, false});
     s.push_back({"fus_bp", 1, d, false});
+    if (beta_fused) {
+      s.push_back({"fus_psi", 2 * d, d, false});
+      s.push_back({"fus_psi_b", 1, 2 * d, false});
+    }
   }
   return s;
 }

@@ -239,6 +239,9 @@ def param_specs(backbone: str, n_entities: int, n_relations: int, dim: int,
     if semantic_dim:
         base += [("fus_f", dim, semantic_dim, False), ("fus_wp", dim, 2 * dim, False),
                  ("fus_bp", 1, dim, False)]
+        if backbone == "betae":  # Psi_theta (Eq. 3); h is d wide
+            base[0] = ("entity", n_entities, dim, True)
+            base += [("fus_psi", 2 * dim, dim, False), ("fus_psi_b", 1, 2 * dim, False)]
     return base
 
 

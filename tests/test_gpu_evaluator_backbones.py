@@ -85,3 +85,28 @@ def test_fusion_ranks(shape, dim, dl):
     got = eng.eval_ranks(q, t, f)
     want = O.eval_ranks("gqe", rows, q, t, f, dim)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dim,dl", [(32, 48), (400, 768)])
+def test_betae_psi_fusion_ranks(small_graph, dim, dl):
+    # BetaE + FuseSemantic: KL against the Beta parameters Psi_theta makes from
+    # the fused rows (Eq. 3)
+    info = small_graph.info()
+    store = m.semantic_store(info["n_entities"], dl, seed=5)
+    eng = m.Engine("betae", info["n_entities"], info["n_relations"], dim=dim, n_neg=16,
+                   max_queries=64, semantic=store)
+    _train(eng, small_graph)
+    T, Cst = eng.eval_entity_table()
+    E = O.fused_table(eng.download("entity"), store, eng.download("fus_f"),
+                      eng.download("fus_wp"), eng.download("fus_bp"))
+    Y = E @ eng.download("fus_psi").astype(np.float64).T + eng.download("fus_psi_b").astype(
+        np.float64).reshape(1, -1)
+    T64, C64 = O.beta_eval_table(Y, dim)
+    ok, nbad, worst = rel_close(T, T64)
+    assert ok, f"T: {nbad} beyond 1e-4 (worst {worst:.3e})"
+    ok, nbad, worst = rel_close(Cst, C64)
+    assert ok, f"C: {nbad} beyond 1e-4 (worst {worst:.3e})"
+    rng = np.random.default_rng(7)
+    q, t, f = _queries(rng, 48, info["n_entities"], 2 * dim, True)
+    assert np.array_equal(eng.eval_ranks(q, t, f), O.eval_ranks("betae", T, q, t, f, dim,
+                                                                 consts=Cst))

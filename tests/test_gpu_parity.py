@@ -86,6 +86,22 @@ def test_fuse_semantic_parity(small_graph, small_oracle_graph, backbone, mix, di
     _check(res)
 
 
+# BetaE + FuseSemantic: Psi_theta maps the fused vector to the Beta parameters
+# (Eq. 3)
+@pytest.mark.parametrize("mix", [C3_MIX, ALL])
+@pytest.mark.parametrize("dim,dl", [(16, 24), (400, 768)])
+def test_beta_psi_fusion_parity(small_graph, small_oracle_graph, mix, dim, dl):
+    res = run_pair(small_graph, small_oracle_graph, "betae", mix, b=96, k=16, dim=dim,
+                   semantic_dim=dl)
+    _check(res)
+
+
+def test_beta_psi_fusion_three_steps(small_graph, small_oracle_graph):
+    res = run_pair(small_graph, small_oracle_graph, "betae", C3_MIX, b=64, k=16, dim=32, steps=3,
+                   semantic_dim=48)
+    _check(res, steps=3)
+
+
 def test_fuse_semantic_three_steps(small_graph, small_oracle_graph):
     res = run_pair(small_graph, small_oracle_graph, "gqe", C1_MIX, b=64, k=16, dim=32, steps=3,
                    semantic_dim=48)

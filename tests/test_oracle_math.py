@@ -27,7 +27,7 @@ def _loss(om, a):
 
 
 @pytest.mark.parametrize("backbone,dl", [("gqe", 0), ("q2b", 0), ("betae", 0), ("gqe", 8),
-                                         ("q2b", 8)])
+                                         ("q2b", 8), ("betae", 8)])
 def test_finite_difference_gradients(tiny, backbone, dl):
     g, info = tiny
     d, k = 4, 3
