@@ -493,15 +493,16 @@ def bench_sharded(args):
     # e2e: the pipelined sharded trainer loop — sampling + planning on host
     # threads, metadata all-gather, owner lists, every stage and collective,
     # losses read back per step
-    producers = max(2, host_workers() // world - 1)  # this rank's share of the host cores
+    # this rank's share of the host cores (minus the launching and exchange threads)
+    producers = max(2, host_workers() // world - 2)
     eng.step_count = step_no
-    eng.train(graph, w, 3, batch, n_neg, lambda s: (1 + n_steps + s) * world + rank, producers)
+    eng.train_native(graph, w, 3, batch, n_neg, first_tag=1 + n_steps, producers=producers)
     b0, d0 = C.c_int64(), C.c_int64()
     check(lib.ngdb_transfer_bytes(ctx, C.byref(b0), C.byref(d0)))
     dist.barrier()
     t0 = time.perf_counter()
-    eng.train(graph, w, args.steps, batch, n_neg,
-              lambda s: (1 + n_steps + 3 + s) * world + rank, producers)
+    eng.train_native(graph, w, args.steps, batch, n_neg, first_tag=1 + n_steps + 3,
+                     producers=producers)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     b1, d1 = C.c_int64(), C.c_int64()
@@ -519,9 +520,11 @@ def bench_sharded(args):
             "cpu_baseline": None,
             "e2e": {"value": e2e, "unit": "queries/s",
                     "h2d_bytes_per_step": int((b1.value - b0.value) / args.steps),
-                    "api": "ShardedEngine.train (host planning threads, packed metadata "
-                           "all-gather, stages + libngdb NCCL collectives, loss read-back "
-                           "per step)",
+                    "api": "ngdb_shard_train_run (producer threads sample + plan + pack, "
+                           "exchange thread all-gathers the packed metadata over the "
+                           "metadata communicator and builds owner lists, stages + NCCL "
+                           "collectives + Adam, loss read-back per step)",
+                    "consumer": getattr(eng, "last_timings", None),
                     "d2h_bytes_per_step": 4 * batch + 16},
             "families": fams,
             "gpu_launches": int(launches),

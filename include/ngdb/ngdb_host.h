@@ -170,6 +170,17 @@ typedef struct ngdb_train_feedback {
 int ngdb_train_run_ex(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
                       const ngdb_train_feedback* fb, int64_t first_step, int32_t n_steps,
                       double* loss_per_step, float* per_query_loss, double* timings);
+/* The row-sharded trainer loop (needs ngdb_comm_init): batch i of
+ * rank r from Rng(seed).fork((first_tag + i) * world + r); producer threads
+ * sample, plan and pack, an exchange thread all-gathers the packed metadata in
+ * step order (ngdb_comm_allgather_i32) and builds the owner lists, the calling
+ * thread launches ngdb_shard_step_exec per step and reads losses back one step
+ * behind. timings (may be NULL): 6 doubles — consumer seconds waiting for
+ * plans, submitting, waiting for results; exchange-thread seconds in the
+ * all-gather and the owner-list build; producer count. */
+int ngdb_shard_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
+                         int64_t first_step, int32_t n_steps, double* loss_per_step,
+                         double* timings);
 /* The sampler's adaptive rule, exposed for tests and callers:
  * record_difficulty on one (pattern, loss); update_distribution over the
  * support of `base` (NULL: all 14 patterns). */

@@ -65,6 +65,9 @@ ShardPlanHost build_shard_plan(const ShardSpec& spec, const int32_t* anchor_ids_
 //                       unit_slots   [3*B_cap]
 //                       candidates   [B_cap * nc]
 int64_t shard_meta_stride(int32_t batch_cap, int32_t n_candidates);
+// This rank's record of a planned (sharded) step.
+struct StepPlanHost;
+void pack_shard_meta(const StepPlanHost& plan, int32_t batch_cap, int32_t* out, int64_t stride);
 // All-gathered records (rank-major, `stride` apart) -> this rank's plan.
 ShardPlanHost build_shard_plan_packed(int32_t world, int32_t rank, const int32_t* gathered,
                                       int64_t stride, int32_t batch_cap);

@@ -193,6 +193,8 @@ SIGNATURES = {
     "ngdb_train_step": (C.c_int, [C.c_void_p, C.c_void_p, i32, i64, P(f32), P(f64)]),
     "ngdb_train_run_ex": (C.c_int, [C.c_void_p, C.c_void_p, P(TrainOpts), P(TrainFeedback), i64,
                                     i32, P(f64), P(f32), P(f64)]),
+    "ngdb_shard_train_run": (C.c_int, [C.c_void_p, C.c_void_p, P(TrainOpts), i64, i32, P(f64),
+                                       P(f64)]),
     "ngdb_record_difficulty": (C.c_int, [P(f64), P(i64), f64, i32, f64]),
     "ngdb_update_distribution": (C.c_int, [P(f64), P(i64), f64, f64, P(f64), P(f64)]),
     "ngdb_train_run": (C.c_int, [C.c_void_p, C.c_void_p, P(TrainOpts), i64, i32, P(f64), P(f32),

@@ -11,6 +11,7 @@
 #include "ngdb/sampler.hpp"
 #include "ngdb/scheduler.hpp"
 #include "ngdb/shard.hpp"
+#include "ngdb/shard_loop.hpp"
 #include "ngdb/synth.hpp"
 #include "ngdb/trainer.hpp"
 #include "ngdb/train_loop.hpp"
@@ -432,27 +433,7 @@ int64_t ngdb_shard_meta_stride(int32_t batch_cap, int32_t n_candidates) {
 }
 
 int ngdb_step_shard_pack(const ngdb_step* s, int32_t batch_cap, int32_t* out, int64_t stride) {
-  return guarded([&] {
-    const auto& p = s->plan;
-    const int32_t nc = p.n_candidates, B = p.n_queries;
-    if (stride != ngdb::shard_meta_stride(batch_cap, nc))
-      throw ngdb::ShapeMismatch("shard metadata stride");
-    if (B > batch_cap || p.n_anchor_slots > 3 * batch_cap)
-      throw ngdb::ShapeMismatch("step exceeds the metadata record's batch capacity");
-    std::fill(out, out + stride, -1);
-    out[0] = p.n_anchor_slots;
-    out[1] = p.n_score_slots;
-    out[2] = B;
-    out[3] = nc;
-    int32_t* a = out + 4;
-    int32_t* k = a + 3 * int64_t(batch_cap);
-    int32_t* us = k + batch_cap;
-    int32_t* c = us + 3 * int64_t(batch_cap);
-    std::copy(p.anchor_ids.begin(), p.anchor_ids.end(), a);
-    std::copy(p.unit_k.begin(), p.unit_k.end(), k);
-    std::copy(p.unit_slots.begin(), p.unit_slots.end(), us);
-    std::copy(p.candidates.begin(), p.candidates.end(), c);
-  });
+  return guarded([&] { ngdb::pack_shard_meta(s->plan, batch_cap, out, stride); });
 }
 
 int ngdb_shard_build_packed(int32_t world, int32_t rank, const int32_t* gathered, int64_t stride,
@@ -586,6 +567,33 @@ int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
                    float* per_query_loss, double* timings) {
   return ngdb_train_run_ex(ctx, g, o, nullptr, first_step, n_steps, loss_per_step,
                            per_query_loss, timings);
+}
+
+int ngdb_shard_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* o,
+                         int64_t first_step, int32_t n_steps, double* loss_per_step,
+                         double* timings) {
+  return guarded([&] {
+    if (!ctx || !g || !o || !o->pattern_weights) throw ngdb::ConfigError("null argument");
+    ngdb::ShardLoopConfig cfg;
+    for (int i = 0; i < ngdb::kPatternCount; ++i) cfg.pi.weights[i] = o->pattern_weights[i];
+    cfg.batch = o->batch;
+    cfg.n_neg = o->n_neg;
+    cfg.b_max = o->b_max;
+    cfg.n_producers = o->n_producers;
+    cfg.queue_depth = o->queue_depth;
+    cfg.seed = o->seed;
+    cfg.first_tag = o->first_tag;
+    if (o->in_flight > 0) cfg.in_flight = o->in_flight;
+    const auto st = ngdb::run_shard_train_loop(ctx, g->split, cfg, first_step, n_steps, loss_per_step);
+    if (timings) {
+      timings[0] = st.plan_wait_s;
+      timings[1] = st.submit_s;
+      timings[2] = st.collect_wait_s;
+      timings[3] = st.exchange_s;
+      timings[4] = st.build_s;
+      timings[5] = st.producers;
+    }
+  });
 }
 
 int ngdb_record_difficulty(double* ema_loss, int64_t* observations, double decay, int32_t pattern,

@@ -5,6 +5,7 @@
 
 #include "ngdb/common.hpp"
 #include "ngdb/radix.hpp"
+#include "ngdb/trainer.hpp"
 
 namespace ngdb {
 
@@ -90,6 +91,26 @@ ShardPlanHost build_shard_plan(const ShardSpec& spec, const int32_t* anchor_ids_
 int64_t shard_meta_stride(int32_t batch_cap, int32_t n_candidates) {
   return 4 + 3 * int64_t(batch_cap) + batch_cap + 3 * int64_t(batch_cap) +
          int64_t(batch_cap) * n_candidates;
+}
+
+void pack_shard_meta(const StepPlanHost& p, int32_t batch_cap, int32_t* out, int64_t stride) {
+  const int32_t nc = p.n_candidates, B = p.n_queries;
+  if (stride != shard_meta_stride(batch_cap, nc)) throw ShapeMismatch("shard metadata stride");
+  if (B > batch_cap || p.n_anchor_slots > 3 * batch_cap)
+    throw ShapeMismatch("step exceeds the metadata record's batch capacity");
+  std::fill(out, out + stride, -1);
+  out[0] = p.n_anchor_slots;
+  out[1] = p.n_score_slots;
+  out[2] = B;
+  out[3] = nc;
+  int32_t* a = out + 4;
+  int32_t* k = a + 3 * int64_t(batch_cap);
+  int32_t* us = k + batch_cap;
+  int32_t* c = us + 3 * int64_t(batch_cap);
+  std::copy(p.anchor_ids.begin(), p.anchor_ids.end(), a);
+  std::copy(p.unit_k.begin(), p.unit_k.end(), k);
+  std::copy(p.unit_slots.begin(), p.unit_slots.end(), us);
+  std::copy(p.candidates.begin(), p.candidates.end(), c);
 }
 
 ShardPlanHost build_shard_plan_packed(int32_t world, int32_t rank, const int32_t* gathered,

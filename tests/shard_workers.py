@@ -176,6 +176,15 @@ def train_loop_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, 
                                                                  info["n_relations"], dim)}
     out["seq_sums"] = seq
     out["loop_sums"] = sums.tolist()
+    # the native loop (libngdb threads + the metadata communicator), same batches:
+    # tag((s+1)*world + rank) == (first_tag + s) * world + rank with first_tag = 1
+    eng3 = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
+                         n_neg=k, max_queries=b)
+    nsums = eng3.train_native(g, w, steps, b, k, first_tag=1, producers=3)
+    torch.cuda.synchronize()
+    out["native"] = {n: eng3.download(n) for n, *_ in m.param_specs(backbone, info["n_entities"],
+                                                                   info["n_relations"], dim)}
+    out["native_sums"] = nsums.tolist()
     with open(os.path.join(out_dir, f"loop{rank}.pkl"), "wb") as f:
         pickle.dump(out, f)
     dist.destroy_process_group()

@@ -105,7 +105,9 @@ def test_sharded_train_loop_matches_steps(tmp_path):
     out = pickle.load(open(tmp_path / "loop0.pkl", "rb"))
     for name, v in out["seq"].items():
         assert np.array_equal(v, out["loop"][name]), name
+        assert np.array_equal(v, out["native"][name]), name  # ngdb_shard_train_run
     np.testing.assert_allclose(out["loop_sums"], out["seq_sums"], rtol=1e-12)
+    np.testing.assert_allclose(out["native_sums"], out["seq_sums"], rtol=1e-12)
 
 
 @pytest.mark.parametrize("backbone,dim", [("q2b", 400), ("gqe", 32)])
