@@ -520,7 +520,28 @@ double pool_bytes(const ngdb_ctx* c, const ngdb_pool_desc& d, int ncand) {
     case NGDB_OP_EMBED_ANCHOR: return n * (d.dir == 0 ? ew + wq : 2 * ew) + n * 32;
     case NGDB_OP_PROJECT: return n * (d.dir == 0 ? (wq + rw + wq) : (2 * wq + 2 * rw)) + n * 32;
     case NGDB_OP_NEGATE: return n * 2 * wq + n * 32;
-    case NGDB_OP_INTERSECT: return n * (k + 1) * wq * (d.dir == 0 ? 1 : 2) + n * 32;
+    case NGDB_OP_INTERSECT: {
+      // node rows in and out (+ the G slots backward), plus the MLP contractions'
+      // operand traffic: every GEMM row reads its hi/lo split A row (8 B per
+      // element), writes its fp32 output and a chained hi/lo split (12 B), and
+      // every GEMM reads its hi/lo weight (8 B per weight element) — the
+      // intermediates of the class, not only its inputs
+      const double D = c->desc.dim, R = n * k;
+      double rows, gemms, w = D;  // GEMM rows of width w, and GEMMs per launch set
+      if (c->desc.backbone == NGDB_GQE) {
+        rows = d.dir == 0 ? 2 * n : 4 * n;
+        gemms = d.dir == 0 ? 2 : 4;
+      } else if (c->beta()) {
+        rows = d.dir == 0 ? 3 * R : 6 * R;
+        gemms = d.dir == 0 ? 2 : 5;
+        w = 2 * D;
+      } else {
+        rows = d.dir == 0 ? 3 * R + n : 6 * R + 2 * n;
+        gemms = d.dir == 0 ? 4 : 8;
+      }
+      return n * (k + 1) * wq * (d.dir == 0 ? 1 : 2) + n * 32 + rows * w * 20.0 +
+             gemms * w * w * 8.0;
+    }
     case NGDB_OP_UNION_SCORE: return n * (k + 1) * ncand * 4.0 * (d.dir == 0 ? 1 : 2) + n * 32;
     case NGDB_OP_SCORE:
       return n * (ncand * (ew + 4) + wq * (d.dir == 0 ? 2 : 2) + ncand * 4.0) + n * 32;
@@ -2500,7 +2521,8 @@ int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
       case NGDB_SHARD_QUERY_PACK:
         for (const auto& d : p->meta.pools)
           if (d.dir == 0 && (d.kind == NGDB_OP_SCORE || d.kind == NGDB_OP_LOSS))
-            timed(c, F_SCORE, 0.0, [&] { return launch_shard_query_pack(a, d.first, d.count, b.query_mine, lc); });
+            timed(c, F_SCORE, 2.0 * d.count * c->query_width() * 4 + 32.0 * d.count,
+                  [&] { return launch_shard_query_pack(a, d.first, d.count, b.query_mine, lc); });
         break;
       case NGDB_SHARD_SCORE: {
         const double nc = p->meta.n_candidates, ew = c->params[c->ent_idx].cols * 4.0;
@@ -2524,7 +2546,7 @@ int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
           const auto& d = pools[i];
           if (d.dir != 1 || d.kind == NGDB_OP_UNION_SCORE) continue;  // routing done by the owners
           if (d.kind == NGDB_OP_SCORE) {  // dL/dq of a union branch arrived in dqbuf
-            timed(c, F_SCORE, 0.0, [&] { return launch_loss_bwd(a, d.first, d.count, lc); });
+            timed(c, F_SCORE, pool_bytes(c, d, p->meta.n_candidates), [&] { return launch_loss_bwd(a, d.first, d.count, lc); });
           } else if (i + 1 < pools.size() && mergeable(c, d, pools[i + 1])) {
             exec_pool(c, p, d, &pools[i + 1]);
             ++i;

@@ -240,3 +240,27 @@ def python_sums_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps,
     with open(os.path.join(out_dir, f"pysums{rank}.pkl"), "wb") as f:
         pickle.dump(sums, f)
     dist.destroy_process_group()
+
+
+def wikikg2_worker(rank, world, port, out_dir, b, k, dim, steps):
+    """One NCCL rank on GPU 0: the C5 row-sharded step on the wikikg2-shaped
+    graph; per-query losses of `steps` steps (batch s: tag (s+1)*world + rank)."""
+    import numpy as np
+    dist = _init(rank, world, port)
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200.sharded import Comm, ShardedEngine
+
+    g = m.Graph.synthetic("wikikg2", 1)
+    info = g.info()
+    w = m.pattern_weights(m.PATTERNS)
+    eng = ShardedEngine(Comm(transport="nccl"), "q2b", info["n_entities"], info["n_relations"],
+                        dim=dim, n_neg=k, max_queries=b)
+    out = {"loss": [], "arrays": []}
+    for s in range(steps):
+        bt = m.Batch.sample(g, w, b, k, seed=3, tag=(s + 1) * world + rank)
+        out["arrays"].append(bt.arrays())
+        out["loss"].append(eng.train_step(bt))
+    out["relation"] = eng.download("relation")
+    with open(os.path.join(out_dir, f"wiki{rank}.pkl"), "wb") as f:
+        pickle.dump(out, f)
+    dist.destroy_process_group()
