@@ -197,6 +197,8 @@ struct ngdb_ctx {
   int64_t cap_score = 0, cap_anchor = 0, cap_project = 0, cap_queries = 0, cap_cand = 0;
   float* scratch = nullptr;
   int64_t scratch_cap = 0;
+  float* scratch2 = nullptr;  // BetaE Project GEMM scratch (independent of the intersect's)
+  int64_t scratch2_cap = 0;
   float* arena = nullptr;
   int64_t arena_cap = 0;
   // BetaE per-step entity table (beta.cu) and candidate -> CSR-row map
@@ -597,11 +599,17 @@ void exec_pool(ngdb_ctx* c, const ngdb_plan* p, const ngdb_pool_desc& d,
       if (!c->fused()) throw Fail{NGDB_ERR_MISSING_KERNEL, "FuseSemantic pool without a semantic store"};
       timed(c, fam, bytes, [&] { return launch_embed(a, d.dir, d.first, d.count, lc); });
       break;
-    case NGDB_OP_PROJECT:
+    case NGDB_OP_PROJECT: {
       if (c->profiling && c->beta())  // [q|r] 3d -> 2d -> 2d MLP, in units of 2 d^2 flops
         c->fam_flops[fam] += (d.dir == 0 ? 10.0 : 20.0) * d.count * 2.0 * c->desc.dim * c->desc.dim;
-      timed(c, fam, bytes, [&] { return launch_project(a, d.dir, d.first, d.count, lc); });
+      DevArgs ap = a;
+      if (c->scratch2) {
+        ap.scratch = c->scratch2;
+        ap.scratch_cap = c->scratch2_cap;
+      }
+      timed(c, fam, bytes, [&] { return launch_project(ap, d.dir, d.first, d.count, lc); });
       break;
+    }
     case NGDB_OP_NEGATE:
       timed(c, fam, bytes, [&] { return launch_negate(a, d.dir, d.first, d.count, lc); });
       break;
@@ -766,8 +774,9 @@ void exec_pools_concurrent(ngdb_ctx* c, const ngdb_plan* p) {
   constexpr int S = 1 + ngdb_ctx::kSide;
   std::vector<int> stream_of(n, 0);
   auto chain_stream = [&](const ngdb_pool_desc& d) {
-    if (d.kind == NGDB_OP_INTERSECT || (d.kind == NGDB_OP_PROJECT && c->beta())) return 1;
+    if (d.kind == NGDB_OP_INTERSECT) return 1;
     if (d.kind == NGDB_OP_SCORE || d.kind == NGDB_OP_UNION_SCORE || d.kind == NGDB_OP_LOSS) return 2;
+    if (d.kind == NGDB_OP_PROJECT && c->beta()) return 3;
     return -1;
   };
   for (int i = 0; i < n; ++i) {
@@ -1132,6 +1141,10 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     c->lcount = reinterpret_cast<int32_t*>(dmalloc<float>(c->desc.max_batch));
     CK(cudaMemset(c->lcount, 0, sizeof(int32_t) * c->desc.max_batch));
     c->scratch = dmalloc<float>(c->scratch_cap);
+    if (d.backbone == NGDB_BETAE) {  // BetaE Project MLPs: their own scratch, so a Project
+      c->scratch2_cap = c->scratch_cap;  // pool can run beside an Intersect pool (§3.2)
+      c->scratch2 = dmalloc<float>(c->scratch2_cap);
+    }
     c->d_bc = dmalloc<float>(4);
     tc_gemm_init();
     CK(cudaEventCreate(&c->t0));
@@ -1185,7 +1198,7 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   if (c->lcount) cudaFree(c->lcount);
   for (float* p : {c->etab, c->etab_c, c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit, c->sem, c->qbuf, c->dqbuf,
                    c->coefbuf, c->ddbuf, c->agbuf, c->rgbuf, c->loss_out, c->scratch, c->arena,
-                   c->l2_flush, c->d_bc})
+                   c->l2_flush, c->d_bc, c->scratch2})
     if (p) cudaFree(p);
   if (c->flags) cudaFree(c->flags);
   for (int i = 0; i < 2; ++i) {

@@ -208,17 +208,19 @@ ExecutionTrace Planner::run(const FusedDag& f, const InvokeFn& invoke) {
   // waits for the writers of the tensors it reads (RAW), and — when its
   // output reuses a slab — for the writer and every reader of the slab's
   // previous tenant (WAW / WAR); invocations sharing a side buffer (the MLP
-  // scratch and dense-gradient accumulators; the scoring partials) form chains.
+  // scratch and dense-gradient accumulators of the intersect MLPs, of the BetaE
+  // projection MLPs; the scoring partials) form chains.
   std::vector<int32_t> writer, rhead, dep_scratch;  // per tensor: writer, first reader entry
   std::vector<std::pair<int32_t, int32_t>> rlist;   // reader entries (invocation, next)
   rlist.reserve(4 * static_cast<size_t>(n));
-  int32_t chain_last[2] = {-1, -1};
+  int32_t chain_last[3] = {-1, -1, -1};
   inv_dep_off_.assign(1, 0);
   inv_deps_.clear();
   auto chain_of = [&](OpKind k) {
-    if (k == OpKind::Intersect || (k == OpKind::Project && cfg_.backbone == Backbone::BETAE))
-      return 0;
+    if (k == OpKind::Intersect) return 0;
     if (k == OpKind::Score || k == OpKind::UnionScore || k == OpKind::Loss) return 1;
+    // BetaE projections: their own GEMM scratch and dense gradients (prj_*)
+    if (k == OpKind::Project && cfg_.backbone == Backbone::BETAE) return 2;
     return -1;
   };
   auto track = [&](const int32_t* nodes, int32_t count, OpKind kind) {
