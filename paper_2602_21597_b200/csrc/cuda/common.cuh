@@ -75,6 +75,12 @@ struct DevArgs {
   int32_t fused;
   int32_t sem_dim;
   const float* sem;      // frozen store [n_entities][sem_dim]
+  // its 3xTF32 split, made once at upload: [n][sem_dim] hi / lo, and transposed
+  // [sem_dim][pad4(n)] hi / lo (used when a step touches every entity)
+  const float* sem_hi;
+  const float* sem_lo;
+  const float* semT_hi;
+  const float* semT_lo;
   int32_t* anchor_local;
   int32_t fus_idx;       // dense index of fus_f (fus_wp = +1, fus_bp = +2)
   // row-sharded step (shard.cu): anchor rows fetched from their owners, in
@@ -311,6 +317,9 @@ int launch_beta_prep(const DevArgs& a, const SparseTable& t, const LaunchCtx& lc
 // fuse.cu: step prologue (etab = e_fused of the touched rows) and the fused
 // backward + entity Adam
 int64_t fuse_scratch_floats(int d, int dl, int64_t rows);
+// whole-table CSR segments (row e = entity e) from a step's compact entity CSR
+int launch_expand_rows(const int32_t* rows, const int32_t* seg, int u, int32_t* seg_full, int n,
+                       cudaStream_t s);
 // BetaE with FuseSemantic: the Psi_theta output rows Y [u][2d] inside the scratch
 float* fuse_y_table(float* fs, int64_t cap, int u, int d, int dl);
 

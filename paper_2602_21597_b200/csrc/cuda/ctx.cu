@@ -198,6 +198,11 @@ struct ngdb_ctx {
   float* scratch = nullptr;
   int64_t scratch_cap = 0;
   float* scratch2 = nullptr;  // BetaE Project GEMM scratch (independent of the intersect's)
+  float* sem_split = nullptr;  // frozen store splits: hi, lo [N][dl], then hiT, loT [dl][pad4(N)]
+  // whole-table fusion form (a step touching >= 90 % of the entities fuses every
+  // entity: no per-step gather / split of the store, rows = identity)
+  int32_t* iota_rows = nullptr;  // [N] 0..N-1
+  int32_t* seg_full = nullptr;   // [N+1]
   int64_t scratch2_cap = 0;
   float* arena = nullptr;
   int64_t arena_cap = 0;
@@ -390,6 +395,13 @@ void ensure_f(float*& p, int64_t& cap, int64_t need) {
   p = dmalloc<float>(cap);
 }
 
+// Rows the fusion prologue / backward work on: every entity (whole-table form)
+// when the step touches >= 90 % of them and the store's split exists, else the
+// step's touched rows.
+bool fusion_whole(const ngdb_ctx* c, const PlanMeta& m) {
+  return c->fused() && c->iota_rows && int64_t(m.n_erows) * 10 >= int64_t(c->desc.n_entities) * 9;
+}
+
 void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
   const int64_t wq = c->query_width();
   const int64_t ew = c->op_ent_w(), rw = c->params[c->rel_idx].cols;
@@ -432,9 +444,10 @@ void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
     }
     ++c->buffer_gen;
   }
-  if (c->step_table() && m.n_erows > c->cap_erows) {
+  const int64_t erows = fusion_whole(c, m) ? int64_t(c->desc.n_entities) : m.n_erows;
+  if (c->step_table() && erows > c->cap_erows) {
     CK(cudaStreamSynchronize(c->stream));
-    c->cap_erows = std::max<int64_t>(m.n_erows, c->cap_erows + c->cap_erows / 4);
+    c->cap_erows = std::max<int64_t>(erows, c->cap_erows + c->cap_erows / 4);
     if (c->etab) CK(cudaFree(c->etab));
     if (c->etab_c) CK(cudaFree(c->etab_c));
     c->etab = dmalloc<float>(c->cap_erows * ew);
@@ -494,13 +507,21 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.fused = c->fused() ? 1 : 0;
   a.sem_dim = c->desc.semantic_dim;
   a.sem = c->sem;
+  if (c->sem_split) {
+    const int64_t N = c->desc.n_entities, L = c->desc.semantic_dim, NP = (N + 3) / 4 * 4;
+    a.sem_hi = c->sem_split;
+    a.sem_lo = a.sem_hi + N * L;
+    a.semT_hi = a.sem_lo + N * L;
+    a.semT_lo = a.semT_hi + L * NP;
+  }
   a.anchor_local = c->anchor_local;
   a.fus_idx = c->fus_idx;
   a.anc_rows = c->anc_rows;
   a.anc_pos = c->anc_pos;
   a.ytab = (c->beta() && c->fused() && p && c->fscratch)
-               ? fuse_y_table(c->fscratch, c->fscratch_cap, p->meta.n_erows, c->desc.dim,
-                              c->desc.semantic_dim)
+               ? fuse_y_table(c->fscratch, c->fscratch_cap,
+                              fusion_whole(c, p->meta) ? c->desc.n_entities : p->meta.n_erows,
+                              c->desc.dim, c->desc.semantic_dim)
                : nullptr;
   a.istash = c->istash;
   a.istash_slots = c->istash_slots;
@@ -884,6 +905,22 @@ void set_step_scalars(ngdb_ctx* c, int64_t step) {
   CK(cudaGetLastError());
 }
 
+SparseTable entity_table(ngdb_ctx* c, const ngdb_plan* p);
+
+// The fusion's entity table: the whole-table form (rows 0..N-1, the step's
+// segments expanded by `expand` on the stream) or the step's CSR.
+SparseTable fusion_table(ngdb_ctx* c, const ngdb_plan* p, bool expand) {
+  SparseTable t = entity_table(c, p);
+  if (!fusion_whole(c, p->meta)) return t;
+  if (expand)
+    c->launches += launch_expand_rows(t.rows, t.seg, t.n_rows, c->seg_full,
+                                      static_cast<int>(c->desc.n_entities), c->stream);
+  t.n_rows = static_cast<int32_t>(c->desc.n_entities);
+  t.rows = c->iota_rows;
+  t.seg = c->seg_full;
+  return t;
+}
+
 SparseTable entity_table(ngdb_ctx* c, const ngdb_plan* p) {
   Param& ent = c->params[c->ent_idx];
   return SparseTable{ent.w, ent.m, ent.v, c->debug ? ent.g : nullptr, static_cast<int32_t>(ent.cols),
@@ -901,10 +938,11 @@ void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
   Param& rel = c->params[c->rel_idx];
   const SparseTable te = entity_table(c, p);
   if (c->fused()) {
-    const double u = p->meta.n_erows, D = c->desc.dim, L = c->desc.semantic_dim;
+    const SparseTable tf = fusion_table(c, p, false);  // expanded by prep_step
+    const double u = tf.n_rows, D = c->desc.dim, L = c->desc.semantic_dim;
     if (c->profiling) c->fam_flops[F_OPT_ENTITY] += 2.0 * u * D * (2 * D + 2 * D + L);
     timed(c, F_OPT_ENTITY, 6.0 * u * D * 4 + 8.0 * p->meta.n_econ + u * L * 4, [&] {
-      return fuse_backward(a, te, c->fscratch, c->fscratch_cap, hp, bc, lc);
+      return fuse_backward(a, tf, c->fscratch, c->fscratch_cap, hp, bc, lc);
     });
   }
   SparseTable tr{rel.w, rel.m, rel.v, c->debug ? rel.g : nullptr, static_cast<int32_t>(rel.cols),
@@ -933,10 +971,11 @@ void prep_step(ngdb_ctx* c, const ngdb_plan* p) {
   const SparseTable te = entity_table(c, p);
   if (c->fused()) {
     if (!c->sem) throw Fail{NGDB_ERR_CONFIG, "semantic store not uploaded (ngdb_semantic_upload)"};
-    const double u = p->meta.n_erows, D = c->desc.dim, L = c->desc.semantic_dim;
+    const SparseTable tf = fusion_table(c, p, true);
+    const double u = tf.n_rows, D = c->desc.dim, L = c->desc.semantic_dim;
     if (c->profiling) c->fam_flops[F_ENTITY_PREP] += 2.0 * u * D * (L + 2 * D);
     timed(c, F_ENTITY_PREP, u * (L * 4 + D * 4 * 2) + 4.0 * p->meta.n_econ,
-          [&] { return fuse_prologue(a, te, c->fscratch, c->fscratch_cap, lc); });
+          [&] { return fuse_prologue(a, tf, c->fscratch, c->fscratch_cap, lc); });
     CK(cudaGetLastError());
     return;
   }
@@ -1198,7 +1237,9 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   if (c->lcount) cudaFree(c->lcount);
   for (float* p : {c->etab, c->etab_c, c->dense_w, c->dense_m, c->dense_v, c->dense_g, c->wsplit, c->sem, c->qbuf, c->dqbuf,
                    c->coefbuf, c->ddbuf, c->agbuf, c->rgbuf, c->loss_out, c->scratch, c->arena,
-                   c->l2_flush, c->d_bc, c->scratch2})
+                   c->l2_flush, c->d_bc, c->scratch2, c->sem_split})
+    if (p) cudaFree(p);
+  for (int32_t* p : {c->iota_rows, c->seg_full})
     if (p) cudaFree(p);
   if (c->flags) cudaFree(c->flags);
   for (int i = 0; i < 2; ++i) {
@@ -1302,6 +1343,26 @@ int ngdb_semantic_upload(ngdb_ctx* c, const float* host, int64_t n) {
       throw Fail{NGDB_ERR_SHAPE_MISMATCH, "semantic store size"};
     if (!c->sem) c->sem = dmalloc<float>(n);
     CK(cudaMemcpy(c->sem, host, n * 4, cudaMemcpyHostToDevice));
+    // the frozen store's operand splits, once (the fusion GEMMs read them
+    // directly when a step touches every entity: no per-step gather / split)
+    const int64_t N = c->desc.n_entities, L = c->desc.semantic_dim, NP = (N + 3) / 4 * 4;
+    if (!c->sem_split) c->sem_split = dmalloc<float>(2 * N * L + 2 * L * NP);
+    float* hi = c->sem_split;
+    float* lo = hi + N * L;
+    float* hiT = lo + N * L;
+    float* loT = hiT + L * NP;
+    split_matrix(c->sem, static_cast<int>(N), static_cast<int>(L), static_cast<int>(L), 0, 0, hi, lo,
+                 c->stream);
+    split_matrix(c->sem, static_cast<int>(N), static_cast<int>(L), static_cast<int>(L), 1, 0, hiT,
+                 loT, c->stream);
+    if (!c->iota_rows) {
+      std::vector<int32_t> iota(N);
+      for (int64_t e = 0; e < N; ++e) iota[e] = static_cast<int32_t>(e);
+      c->iota_rows = dmalloc<int32_t>(N);
+      c->seg_full = dmalloc<int32_t>(N + 1);
+      CK(cudaMemcpy(c->iota_rows, iota.data(), N * 4, cudaMemcpyHostToDevice));
+    }
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -88,7 +88,8 @@ FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
 
 // Per touched row r: candidate / anchor -> row maps, the gathered store row
 // (plain + split) and X[r][0:d] = h (plain + split).
-__global__ void __launch_bounds__(kWarps * 32) fuse_gather_kernel(DevArgs a, SparseTable t, FuseBufs f) {
+__global__ void __launch_bounds__(kWarps * 32) fuse_gather_kernel(DevArgs a, SparseTable t, FuseBufs f,
+                                                                  int gather_s) {
   pdl_start();
   const int r = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kWarps * 32) fuse_gather_kernel(DevArgs a, Spa
   }
   const int64_t e = t.rows[r];
   const float* s = a.sem + e * f.dl;
-  for (int c = lane; c < f.dl / 4; c += 32) {
+  for (int c = lane; gather_s && c < f.dl / 4; c += 32) {
     const float4 v = ldg4(s + 4 * c);
     const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -177,13 +178,14 @@ __global__ void __launch_bounds__(kWarps * 32) fuse_grad_kernel(DevArgs a, Spars
   }
 }
 
-// lazy Adam on the touched entity rows with gradient rows G[r][0:width] (stride ldg)
+// lazy Adam on the touched entity rows with gradient rows G[r][0:width] (stride ldg);
+// rows without contributions (the whole-table form) are untouched: skipped
 __global__ void __launch_bounds__(kWarps * 32) rows_adam_kernel(SparseTable t, const float* G, int ldg,
                                                                 AdamHyper hp, const float* bc) {
   pdl_start();
   const int r = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (r >= t.n_rows) return;
+  if (r >= t.n_rows || t.seg[r] == t.seg[r + 1]) return;
   const float ibc1 = 1.f / bc[0], ibc2 = 1.f / bc[1];  // bias corrections as reciprocals
   const int64_t row = t.rows[r];
   for (int c = lane; c < t.width / 4; c += 32) {
@@ -209,12 +211,40 @@ __global__ void __launch_bounds__(kWarps * 32) rows_adam_kernel(SparseTable t, c
 
 inline int row_blocks(int n) { return (n + kWarps - 1) / kWarps; }
 
+// A step that touches every entity (CSR rows ascending and unique, so rows ==
+// 0..N-1) reads the frozen store's split made at upload instead of gathering
+// and splitting it again (FB15k-237: ~66k candidates cover all 14.5k entities)
+inline bool all_rows(const DevArgs& a, const SparseTable& t) {
+  return a.sem_hi && t.n_rows == a.n_entities;
+}
+
 }  // namespace
+
+// Whole-table form of a step's entity CSR: rows 0..N-1 (row e = entity e) with
+// the compact CSR's contribution segments (empty for untouched entities)
+__global__ void expand_seg_kernel(const int32_t* rows, const int32_t* seg, int u, int32_t* seg_full,
+                                  int n) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e > n) return;
+  int lo = 0, hi = u;  // first compact row with entity >= e
+  while (lo < hi) {
+    const int mid = (lo + hi) / 2;
+    if (rows[mid] < e) lo = mid + 1;
+    else hi = mid;
+  }
+  seg_full[e] = seg[lo];
+}
 
 int64_t fuse_scratch_floats(int d, int dl, int64_t rows) {
   const int64_t U = rows + 4;
   return U * (3 * dl + 6 * d + d + 3 * d + 2 * d) + U * (2 * d + 4 * d + 2 * d + 2 * dl) +
          U * (3 * d + 2 * d + 6 * d + d + 4 * d + 2 * d) + 4096;  // + the BetaE (Psi) buffers
+}
+
+int launch_expand_rows(const int32_t* rows, const int32_t* seg, int u, int32_t* seg_full, int n,
+                       cudaStream_t s) {
+  expand_seg_kernel<<<(n + 256) / 256, 256, 0, s>>>(rows, seg, u, seg_full, n);
+  return 1;
 }
 
 float* fuse_y_table(float* fs, int64_t cap, int u, int d, int dl) {
@@ -228,10 +258,13 @@ int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
   FuseBufs f = carve(fs, cap, u, d, dl, beta);
   const float* p = a.dense;
   int launches = 0;
-  launch_pdl(fuse_gather_kernel, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
+  const bool whole = all_rows(a, t);
+  launch_pdl(fuse_gather_kernel, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f,
+             whole ? 0 : 1);
   ++launches;
   // F s -> X[:, d:2d] (plain + chained split)
-  TcGemmArgs g1 = gemm_args(u, d, dl, op(f.Ss, dl), wop(a, a.fus_idx, d, dl, false), f.X + d, 2 * d);
+  const Split Ss = whole ? Split{const_cast<float*>(a.sem_hi), const_cast<float*>(a.sem_lo)} : f.Ss;
+  TcGemmArgs g1 = gemm_args(u, d, dl, op(Ss, dl), wop(a, a.fus_idx, d, dl, false), f.X + d, 2 * d);
   g1.s_hi = f.Xs.hi + d;
   g1.s_lo = f.Xs.lo + d;
   launches += tc_gemm(g1, lc.stream);
@@ -301,17 +334,19 @@ int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
   // dX = dZ W_p  ([u][2d]; first half -> entity rows, second half -> F s)
   TcGemmArgs g3 = gemm_args(u, 2 * d, d, op(f.dZs, d), wop(a, a.fus_idx + 1, d, 2 * d, true), f.dX, 2 * d);
   launches += tc_gemm(g3, lc.stream);
+  const bool whole = all_rows(a, t);
   SplitJobs jobs{};
   jobs.job[0] = {f.dZ, u, d, d, 0, f.dZT.hi, f.dZT.lo};
   jobs.job[1] = {f.X, u, 2 * d, 2 * d, 0, f.XT.hi, f.XT.lo};
   jobs.job[2] = {f.dX + d, u, d, 2 * d, 0, f.dFsT.hi, f.dFsT.lo};
   jobs.job[3] = {f.S, u, dl, dl, 0, f.ST.hi, f.ST.lo};
-  jobs.n = 4;
+  jobs.n = whole ? 3 : 4;  // the store's transposed split exists already
   launches += split_transposed(jobs, lc.stream);
+  const Split ST = whole ? Split{const_cast<float*>(a.semT_hi), const_cast<float*>(a.semT_lo)} : f.ST;
   TcGemmArgs lvl[2];
   lvl[0] = gemm_args(d, 2 * d, u, op(f.dZT, f.uP), op(f.XT, f.uP), g + off[a.fus_idx + 1], 2 * d);
   lvl[0].accumulate = 1;  // dW_p += dZ^T X
-  lvl[1] = gemm_args(d, dl, u, op(f.dFsT, f.uP), op(f.ST, f.uP), g + off[a.fus_idx], dl);
+  lvl[1] = gemm_args(d, dl, u, op(f.dFsT, f.uP), op(ST, f.uP), g + off[a.fus_idx], dl);
   lvl[1].accumulate = 1;  // dF += (dX[:, d:])^T S
   launches += tc_gemm_batch(lvl, 2, lc.stream);
   ColsumJobs cj{};
