@@ -260,6 +260,10 @@ struct ngdb_ctx {
     ngdb_shard_buffers bufs{};
     std::vector<int32_t> send_cnt, recv_cnt;  // host copies: NCCL send/recv counts (rows)
     float* coef_all = nullptr;
+    // BetaE: the step entity table of the rows this rank owns (beta_prep over
+    // the shard CSR) and global score code -> table row
+    float *etab = nullptr, *etab_c = nullptr;
+    int32_t* cand_local = nullptr;
     int32_t n_rows = 0;
     const int32_t *rows = nullptr, *seg = nullptr, *contrib = nullptr;
     bool active = false;
@@ -504,6 +508,11 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.etab = c->etab;
   a.etab_c = c->etab_c;
   a.cand_local = c->cand_local;
+  if (c->world > 1) {
+    a.etab = c->sh.etab;
+    a.etab_c = c->sh.etab_c;
+    a.cand_local = c->sh.cand_local;
+  }
   a.fused = c->fused() ? 1 : 0;
   a.sem_dim = c->desc.semantic_dim;
   a.sem = c->sem;
@@ -1055,8 +1064,8 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       throw Fail{NGDB_ERR_CONFIG, "semantic_dim must be a multiple of 4, <= 4096"};
     const int world = d.world > 1 ? d.world : 1;
     if (world > 1 && (d.rank < 0 || d.rank >= world)) throw Fail{NGDB_ERR_CONFIG, "rank out of range"};
-    if (world > 1 && (d.backbone == NGDB_BETAE || d.semantic_dim > 0))
-      throw Fail{NGDB_ERR_MISSING_KERNEL, "row-sharded step is built for GQE / Q2B without fusion"};
+    if (world > 1 && d.semantic_dim > 0)
+      throw Fail{NGDB_ERR_MISSING_KERNEL, "row-sharded step is built without FuseSemantic"};
     c = new ngdb_ctx();
     c->desc = d;
     c->world = world;
@@ -1082,7 +1091,7 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       add_param(c, "int_w2", D, D, false);
     } else if (d.backbone == NGDB_BETAE) {  // DESIGN.md §3.5; order = trainer.hpp param_specs
       // with FuseSemantic the structural row h is d wide; Psi_theta makes the 2d
-      add_param(c, "entity", d.n_entities, d.semantic_dim > 0 ? D : 2 * D, true);
+      add_param(c, "entity", n_ent_local, d.semantic_dim > 0 ? D : 2 * D, true);
       add_param(c, "relation", d.n_relations, D, true);
       add_param(c, "prj_w1", 2 * D, 3 * D, false);
       add_param(c, "prj_b1", 1, 2 * D, false);
@@ -2347,7 +2356,8 @@ struct ShardShape {
 void validate_shard(ngdb_ctx* c, const ngdb_step_plan& plan, const ngdb_shard_plan& sp) {
   if (sp.world != c->world || sp.rank != c->rank)
     throw Fail{NGDB_ERR_CONFIG, "shard plan world/rank do not match the context"};
-  if (c->beta() || c->fused()) throw Fail{NGDB_ERR_MISSING_KERNEL, "sharded BetaE / fusion"};
+  if (c->fused()) throw Fail{NGDB_ERR_MISSING_KERNEL, "sharded FuseSemantic"};
+  if (c->beta() && c->desc.dim > 512) throw Fail{NGDB_ERR_MISSING_KERNEL, "sharded BetaE: dim > 512"};
   validate_plan(plan);
   if (plan.n_score_slots > sp.max_slots || plan.n_anchor_slots > sp.max_anchors ||
       plan.n_queries > sp.batch || plan.n_candidates != sp.n_candidates)
@@ -2363,8 +2373,9 @@ void validate_shard(ngdb_ctx* c, const ngdb_step_plan& plan, const ngdb_shard_pl
     throw Fail{NGDB_ERR_SHAPE_MISMATCH, "shard plan exchange counts do not add up"};
 }
 
-// Exchange buffer sizes of a shard shape (ngdb_shard_buffers order + coef_all).
-constexpr int kShardBufs = 10;
+// Exchange buffer sizes of a shard shape (ngdb_shard_buffers order + coef_all,
+// then BetaE's etab, etab_c, cand_local).
+constexpr int kShardBufs = 13;
 void shard_buffer_sizes(const ngdb_ctx* c, const ShardShape& sp, int64_t sizes[kShardBufs]) {
   const int64_t G = sp.world, B = sp.batch, S = sp.max_slots, nc = sp.n_candidates;
   const int64_t ew = c->params[c->ent_idx].cols, wq = c->query_width();
@@ -2372,7 +2383,9 @@ void shard_buffer_sizes(const ngdb_ctx* c, const ShardShape& sp, int64_t sizes[k
   const int64_t n_red = c->dense_n + rel.n() + rel.rows;
   const int64_t blk = S * wq + B;
   const int64_t z[kShardBufs] = {sp.n_send * ew, sp.n_recv * ew, S * wq,     G * S * wq, G * blk,
-                                 blk,            sp.n_recv * ew, sp.n_send * ew, n_red, G * S * nc};
+                                 blk,            sp.n_recv * ew, sp.n_send * ew, n_red, G * S * nc,
+                                 c->beta() ? sp.n_rows * ew : 0, c->beta() ? sp.n_rows : 0,
+                                 c->beta() ? G * S * nc : 0};
   for (int k = 0; k < kShardBufs; ++k) sizes[k] = z[k];
 }
 bool shard_buffers_fit(const ngdb_ctx* c, const ShardShape& sp) {
@@ -2411,6 +2424,9 @@ void shard_exchange_buffers(ngdb_ctx* c, const ShardShape& sp) {
   b.grad_all = ptr[7]; b.n_grad_all = sizes[7];
   b.reduce = ptr[8]; b.n_reduce = sizes[8];
   sh.coef_all = ptr[9];
+  sh.etab = ptr[10];
+  sh.etab_c = ptr[11];
+  sh.cand_local = reinterpret_cast<int32_t*>(ptr[12]);
 }
 // Make (plan, owner lists in `blob`) the active sharded step: the step
 // prologue on the stream (capturable) and the device views.
@@ -2449,6 +2465,14 @@ void shard_activate(ngdb_ctx* c, ngdb_plan* plan, const ShardShape& sp, const in
   sh.active = true;
   c->anc_pos = blob + L.o_pos;
   c->anc_rows = b.anchor_rows;
+  if (c->beta()) {  // the entity side of every owned KL, once per owned row (beta.cu)
+    const Param& ent = c->params[c->ent_idx];
+    const SparseTable te{ent.w, ent.m, ent.v, nullptr, static_cast<int32_t>(ent.cols),
+                         sh.n_rows, sh.rows, sh.seg, sh.contrib};
+    const DevArgs a = make_args(c, plan);
+    timed(c, F_ENTITY_PREP, sp.n_rows * (2.0 * ent.cols * 4 + 4),
+          [&] { return launch_beta_prep(a, te, LaunchCtx{c->stream, c->num_sms}); });
+  }
 }
 
 }  // namespace

@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "dist.cuh"
+#include "special.cuh"
 
 namespace ngdb_dev {
 namespace {
@@ -46,16 +47,54 @@ __global__ void shard_query_pack_kernel(DevArgs a, int first, float* dst) {
 // distances to the unit's 1..3 score-slot queries, union min/argmin (ties ->
 // lowest branch), loss terms, coef (routed to the argmin branch), and the
 // partial dL/dq of each branch slot. Shared: queries [3][wq], per-warp partial
-// dq [4][3][wq] summed in warp order (deterministic).
+// dq [kScoreWarps][3][wq] summed in warp order (deterministic).
+//
+// BetaE (linearised KL, beta.cu): the owned candidate's row is its step-table
+// row etab[cand_local[code]] (computed once per owned row by beta_prep over the
+// shard CSR), d = lnB(q) + etab_c + <q, etab>, and the query-side term
+// (sum of this rank's coefs) [psi(A)-psi(A+B) | psi(B)-psi(A+B)] joins the
+// partial dL/dq — linear in the coefficients, so the reduce-scatter's sum over
+// owners is the full gradient.
+template <int BB>
+__device__ __forceinline__ float chunk_dist(const float4& v, const float* qc, int c, int D,
+                                            float alpha) {
+  const float4 cc = ld4(qc + 4 * c);
+  if constexpr (BB == NGDB_BETAE) {
+    return v.x * cc.x + v.y * cc.y + v.z * cc.z + v.w * cc.w;
+  } else {
+    const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return Dist<BB>::term(v.x, cc.x, oo.x, alpha) + Dist<BB>::term(v.y, cc.y, oo.y, alpha) +
+           Dist<BB>::term(v.z, cc.z, oo.z, alpha) + Dist<BB>::term(v.w, cc.w, oo.w, alpha);
+  }
+}
+template <int BB>
+__device__ __forceinline__ void chunk_grad(const float4& v, const float* qc, int c, int D,
+                                           float coef, float alpha, float4& gc, float4& go) {
+  if constexpr (BB == NGDB_BETAE) {
+    gc.x += coef * v.x; gc.y += coef * v.y; gc.z += coef * v.z; gc.w += coef * v.w;
+  } else {
+    const float4 cc = ld4(qc + 4 * c);
+    const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    Dist<BB>::grad(v.x, cc.x, oo.x, coef, alpha, gc.x, go.x);
+    Dist<BB>::grad(v.y, cc.y, oo.y, coef, alpha, gc.y, go.y);
+    Dist<BB>::grad(v.z, cc.z, oo.z, coef, alpha, gc.z, go.z);
+    Dist<BB>::grad(v.w, cc.w, oo.w, coef, alpha, gc.w, go.w);
+  }
+}
+
 template <int BB, int NCH>
 __global__ void __launch_bounds__(kScoreThreads) shard_score_kernel(DevArgs a, ShardDev sd) {
   pdl_start();
+  constexpr bool kBeta = BB == NGDB_BETAE;
   extern __shared__ __align__(16) float sm[];
   __shared__ float lred[kScoreWarps];
+  __shared__ float csred[kScoreWarps][3];  // BetaE: per-warp coefficient sums per branch
+  __shared__ float qbias[3];               // BetaE: lnB(q_b) summed over the dims
   const int u = blockIdx.x;
   const int q = u / sd.batch, i = u % sd.batch;
   const int k = sd.unit_k[u];
-  const int wq = a.wq, D = a.dim, d4 = D / 4;
+  const int wq = a.wq, D = a.dim;
+  const int nch = kBeta ? wq / 4 : D / 4;  // float4 chunks of a candidate row
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   float* qs = sm;              // [3][wq]
   float* part = sm + 3 * wq;   // [kScoreWarps][3][wq]
@@ -68,64 +107,83 @@ __global__ void __launch_bounds__(kScoreThreads) shard_score_kernel(DevArgs a, S
       qs[b * wq + e] = sd.query_all[static_cast<int64_t>(gslot[b]) * wq + e];
   for (int e = threadIdx.x; e < kScoreWarps * 3 * wq; e += kScoreThreads) part[e] = 0.f;
   __syncthreads();
-  float loss = 0.f;  // identical in all lanes of a warp
+  if constexpr (kBeta) {
+    for (int b = 0; b < k; ++b) {
+      float t = 0.f;
+      for (int e = threadIdx.x; e < D; e += kScoreThreads) t += dg_lbeta(qs[b * wq + e], qs[b * wq + D + e]);
+      t = warp_sum(t);
+      if (lane == 0) lred[warp] = t;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float tt = 0.f;
+        for (int w = 0; w < kScoreWarps; ++w) tt += lred[w];
+        qbias[b] = tt;
+      }
+      __syncthreads();
+    }
+  }
+  float loss = 0.f;                  // identical in all lanes of a warp
+  float csum[3] = {0.f, 0.f, 0.f};   // BetaE: coefficient sums per branch
   const int32_t* cand = sd.cand + static_cast<int64_t>(u) * a.ncand;
   const int t_end = sd.unit_off[u + 1];
   // candidate rows into registers one step ahead: two rows of loads in
   // flight per warp while the current one is reduced
-  auto load_row = [&](int t, float4* v) {
-    const float* row = a.ent + static_cast<int64_t>(cand[sd.owned[t]] / sd.world) * a.ent_w;
+  auto load_row = [&](int t, float4* v, float& cst) {
+    const int j = sd.owned[t];
+    const float* row;
+    if constexpr (kBeta) {
+      const int r = __ldg(a.cand_local + static_cast<int64_t>(gslot[0]) * a.ncand + j);
+      row = a.etab + static_cast<int64_t>(r) * a.ent_w;
+      cst = __ldg(a.etab_c + r);
+    } else {
+      row = a.ent + static_cast<int64_t>(cand[j] / sd.world) * a.ent_w;
+      cst = 0.f;
+    }
 #pragma unroll
     for (int c4 = 0; c4 < NCH; ++c4) {
       const int c = lane + 32 * c4;
-      v[c4] = c < d4 ? ld4(row + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[c4] = c < nch ? ld4(row + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   };
   float4 v[NCH], vn[NCH];
+  float cst = 0.f, cstn = 0.f;
   int t = sd.unit_off[u] + warp;
-  if (t < t_end) load_row(t, v);
+  if (t < t_end) load_row(t, v, cst);
   if (k == 1) {
     // one score slot (every pattern but the unions): dL/dq accumulates in
     // registers across the warp's rows, one shared-memory write at the end
     float4 gcs[NCH], gos[NCH];
 #pragma unroll
     for (int c4 = 0; c4 < NCH; ++c4) gcs[c4] = gos[c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float qb = kBeta ? qbias[0] : 0.f;
     for (; t < t_end; t += kScoreWarps) {
       const int j = sd.owned[t];
-      if (t + kScoreWarps < t_end) load_row(t + kScoreWarps, vn);
+      if (t + kScoreWarps < t_end) load_row(t + kScoreWarps, vn, cstn);
       float s = 0.f;
 #pragma unroll
       for (int c4 = 0; c4 < NCH; ++c4) {
         const int c = lane + 32 * c4;
-        if (c < d4) {
-          const float4 cc = ld4(qs + 4 * c);
-          const float4 oo = BB == NGDB_Q2B ? ld4(qs + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          s += Dist<BB>::term(v[c4].x, cc.x, oo.x, a.alpha_box) + Dist<BB>::term(v[c4].y, cc.y, oo.y, a.alpha_box) +
-               Dist<BB>::term(v[c4].z, cc.z, oo.z, a.alpha_box) + Dist<BB>::term(v[c4].w, cc.w, oo.w, a.alpha_box);
-        }
+        if (c < nch) s += chunk_dist<BB>(v[c4], qs, c, D, a.alpha_box);
       }
-      const float coef = loss_coef(a, j, warp_sum(s), loss);
+      float dj = warp_sum(s);
+      if constexpr (kBeta) dj += qb + cst;
+      const float coef = loss_coef(a, j, dj, loss);
+      csum[0] += coef;
       if (lane == 0) sd.coef_all[static_cast<int64_t>(gslot[0]) * a.ncand + j] = coef;
 #pragma unroll
       for (int c4 = 0; c4 < NCH; ++c4) {
         const int c = lane + 32 * c4;
-        if (c < d4) {
-          const float4 cc = ld4(qs + 4 * c);
-          const float4 oo = BB == NGDB_Q2B ? ld4(qs + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          Dist<BB>::grad(v[c4].x, cc.x, oo.x, coef, a.alpha_box, gcs[c4].x, gos[c4].x);
-          Dist<BB>::grad(v[c4].y, cc.y, oo.y, coef, a.alpha_box, gcs[c4].y, gos[c4].y);
-          Dist<BB>::grad(v[c4].z, cc.z, oo.z, coef, a.alpha_box, gcs[c4].z, gos[c4].z);
-          Dist<BB>::grad(v[c4].w, cc.w, oo.w, coef, a.alpha_box, gcs[c4].w, gos[c4].w);
-        }
+        if (c < nch) chunk_grad<BB>(v[c4], qs, c, D, coef, a.alpha_box, gcs[c4], gos[c4]);
       }
 #pragma unroll
       for (int c4 = 0; c4 < NCH; ++c4) v[c4] = vn[c4];
+      cst = cstn;
     }
     float* pw = part + (warp * 3) * wq;
 #pragma unroll
     for (int c4 = 0; c4 < NCH; ++c4) {
       const int c = lane + 32 * c4;
-      if (c < d4) {
+      if (c < nch) {
         st4(pw + 4 * c, gcs[c4]);
         if (BB == NGDB_Q2B) st4(pw + D + 4 * c, gos[c4]);
       }
@@ -133,7 +191,7 @@ __global__ void __launch_bounds__(kScoreThreads) shard_score_kernel(DevArgs a, S
   }
   for (; k > 1 && t < t_end; t += kScoreWarps) {  // union branches: smem partials per branch
     const int j = sd.owned[t];
-    if (t + kScoreWarps < t_end) load_row(t + kScoreWarps, vn);
+    if (t + kScoreWarps < t_end) load_row(t + kScoreWarps, vn, cstn);
     float dist[3];
     for (int b = 0; b < k; ++b) {
       const float* qc = qs + b * wq;
@@ -141,19 +199,16 @@ __global__ void __launch_bounds__(kScoreThreads) shard_score_kernel(DevArgs a, S
 #pragma unroll
       for (int c4 = 0; c4 < NCH; ++c4) {
         const int c = lane + 32 * c4;
-        if (c < d4) {
-          const float4 cc = ld4(qc + 4 * c);
-          const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          s += Dist<BB>::term(v[c4].x, cc.x, oo.x, a.alpha_box) + Dist<BB>::term(v[c4].y, cc.y, oo.y, a.alpha_box) +
-               Dist<BB>::term(v[c4].z, cc.z, oo.z, a.alpha_box) + Dist<BB>::term(v[c4].w, cc.w, oo.w, a.alpha_box);
-        }
+        if (c < nch) s += chunk_dist<BB>(v[c4], qc, c, D, a.alpha_box);
       }
       dist[b] = warp_sum(s);
+      if constexpr (kBeta) dist[b] += qbias[b] + cst;
     }
     int bm = 0;
     for (int b = 1; b < k; ++b)
       if (dist[b] < dist[bm]) bm = b;  // min distance == max score; ties -> lowest branch
     const float coef = loss_coef(a, j, dist[bm], loss);
+    for (int b = 0; b < k; ++b) csum[b] += b == bm ? coef : 0.f;
     if (lane == 0)
       for (int b = 0; b < k; ++b)
         sd.coef_all[static_cast<int64_t>(gslot[b]) * a.ncand + j] = b == bm ? coef : 0.f;
@@ -162,14 +217,9 @@ __global__ void __launch_bounds__(kScoreThreads) shard_score_kernel(DevArgs a, S
 #pragma unroll
     for (int c4 = 0; c4 < NCH; ++c4) {
       const int c = lane + 32 * c4;
-      if (c < d4) {
-        const float4 cc = ld4(qc + 4 * c);
-        const float4 oo = BB == NGDB_Q2B ? ld4(qc + D + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < nch) {
         float4 gc = make_float4(0.f, 0.f, 0.f, 0.f), go = gc;
-        Dist<BB>::grad(v[c4].x, cc.x, oo.x, coef, a.alpha_box, gc.x, go.x);
-        Dist<BB>::grad(v[c4].y, cc.y, oo.y, coef, a.alpha_box, gc.y, go.y);
-        Dist<BB>::grad(v[c4].z, cc.z, oo.z, coef, a.alpha_box, gc.z, go.z);
-        Dist<BB>::grad(v[c4].w, cc.w, oo.w, coef, a.alpha_box, gc.w, go.w);
+        chunk_grad<BB>(v[c4], qc, c, D, coef, a.alpha_box, gc, go);
         float4 p = ld4(pw + 4 * c);
         st4(pw + 4 * c, make_float4(p.x + gc.x, p.y + gc.y, p.z + gc.z, p.w + gc.w));
         if (BB == NGDB_Q2B) {
@@ -180,15 +230,29 @@ __global__ void __launch_bounds__(kScoreThreads) shard_score_kernel(DevArgs a, S
     }
 #pragma unroll
     for (int c4 = 0; c4 < NCH; ++c4) v[c4] = vn[c4];
+    cst = cstn;
   }
-  if (lane == 0) lred[warp] = loss;
+  if (lane == 0) {
+    lred[warp] = loss;
+    for (int b = 0; b < 3; ++b) csred[warp][b] = csum[b];
+  }
   __syncthreads();
-  for (int b = 0; b < k; ++b)
+  for (int b = 0; b < k; ++b) {
+    float cb = 0.f;
+    if constexpr (kBeta)
+      for (int w = 0; w < kScoreWarps; ++w) cb += csred[w][b];
+    const float* qb = qs + b * wq;
     for (int e = threadIdx.x; e < wq; e += kScoreThreads) {
       float acc = 0.f;
       for (int w = 0; w < kScoreWarps; ++w) acc += part[(w * 3 + b) * wq + e];
+      if constexpr (kBeta) {  // query-side term of dKL/dq
+        const int ii = e < D ? e : e - D;
+        const float A = qb[ii], B = qb[D + ii];
+        acc += cb * (dg_digamma(e < D ? A : B) - dg_digamma(A + B));
+      }
       dq_blk[static_cast<int64_t>(gslot[b] - q * sd.max_slots) * wq + e] = acc;
     }
+  }
   if (threadIdx.x == 0) {
     float tl = 0.f;
     for (int w = 0; w < kScoreWarps; ++w) tl += lred[w];
@@ -283,7 +347,10 @@ int launch_shard_score(const DevArgs& a, const ShardDev& sd, const LaunchCtx& lc
     }
     launch_pdl(kernel, dim3(units), dim3(kScoreThreads), smem, lc.stream, 1, a, sd);
   };
-  if (a.dim <= 512) {
+  if (a.backbone == NGDB_BETAE) {  // rows are 2d wide (validate_shard: d <= 512)
+    if (a.dim <= 256) go(shard_score_kernel<NGDB_BETAE, 4>);
+    else go(shard_score_kernel<NGDB_BETAE, 8>);
+  } else if (a.dim <= 512) {
     if (a.backbone == NGDB_GQE) go(shard_score_kernel<NGDB_GQE, 4>);
     else go(shard_score_kernel<NGDB_Q2B, 4>);
   } else {

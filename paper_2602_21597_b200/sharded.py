@@ -211,8 +211,8 @@ class ShardedEngine:
                  gamma: float = 12.0, lr: float = 1e-4, alpha_box: float = 0.02,
                  device: int = 0, seed: int = 2, debug: bool = False):
         import torch
-        if backbone not in ("gqe", "q2b"):
-            raise NotImplementedError("row-sharded step: GQE / Q2B")
+        if backbone not in ("gqe", "q2b", "betae"):
+            raise NotImplementedError(f"row-sharded step: {backbone}")
         self.torch, self.comm = torch, comm
         self.backbone, self.dim, self.b_max = backbone, dim, b_max
         self.max_queries = max_queries
@@ -446,7 +446,7 @@ def _host_stages(eng: ShardedEngine, b: ShardBuffers, send_cnt, recv_cnt) -> Non
     t = {n: _device_view(eng.torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
     run = lambda stage: check(lib.ngdb_shard_run(eng._h, FORWARD_STAGES[stage]))  # noqa: E731
     comm = eng.comm
-    ew = eng.dim  # GQE / Q2B entity rows are d wide
+    ew = 2 * eng.dim if eng.backbone == "betae" else eng.dim  # entity row width
     run("anchor_pack")
     comm.all_to_all_v(t["anchor_rows"], t["anchor_send"], send_cnt * ew, recv_cnt * ew)
     run("forward")

@@ -25,7 +25,9 @@ def _port():
 
 
 @pytest.mark.parametrize("backbone,dim,b,k,steps", [("q2b", 32, 64, 16, 1), ("gqe", 16, 48, 8, 2),
-                                                      ("q2b", 400, 128, 32, 2)])
+                                                      ("q2b", 400, 128, 32, 2),
+                                                      ("betae", 16, 64, 16, 2),
+                                                      ("betae", 400, 64, 32, 1)])
 def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone, dim, b, k, steps):
     import torch.multiprocessing as mp
 
@@ -77,7 +79,7 @@ def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone
     check_all(res, allow_frac=0.0, steps=steps)
 
 
-@pytest.mark.parametrize("backbone,dim", [("q2b", 32), ("gqe", 16)])
+@pytest.mark.parametrize("backbone,dim", [("q2b", 32), ("gqe", 16), ("betae", 32)])
 def test_sharded_graph_replay_matches_eager(tmp_path, backbone, dim):
     # the resident sharded step (stages + NCCL collectives captured in one CUDA
     # graph, bench.py --config c5) updates the parameters bit-identically to the
@@ -110,7 +112,7 @@ def test_sharded_train_loop_matches_steps(tmp_path):
     np.testing.assert_allclose(out["native_sums"], out["seq_sums"], rtol=1e-12)
 
 
-@pytest.mark.parametrize("backbone,dim", [("q2b", 400), ("gqe", 32)])
+@pytest.mark.parametrize("backbone,dim", [("q2b", 400), ("gqe", 32), ("betae", 32)])
 def test_nccl_transport_matches_host_transport(tmp_path, backbone, dim):
     # the libngdb NCCL path (ngdb_shard_step_exec) and the host-staged path run
     # the same stages over the same exchange layouts: bit-identical results
