@@ -949,7 +949,9 @@ void optimizer(ngdb_ctx* c, const ngdb_plan* p) {
   if (c->fused()) {
     const SparseTable tf = fusion_table(c, p, false);  // expanded by prep_step
     const double u = tf.n_rows, D = c->desc.dim, L = c->desc.semantic_dim;
-    if (c->profiling) c->fam_flops[F_OPT_ENTITY] += 2.0 * u * D * (2 * D + 2 * D + L);
+    // dh, dW_h, dM (+ Psi_theta's dE, dW_psi) and the d x d_l products dW_s, dF
+    if (c->profiling)
+      c->fam_flops[F_OPT_ENTITY] += 2.0 * u * D * (2 * D + L + (c->beta() ? 4 * D : 0)) + 4.0 * D * D * L;
     timed(c, F_OPT_ENTITY, 6.0 * u * D * 4 + 8.0 * p->meta.n_econ + u * L * 4, [&] {
       return fuse_backward(a, tf, c->fscratch, c->fscratch_cap, hp, bc, lc);
     });
@@ -982,7 +984,9 @@ void prep_step(ngdb_ctx* c, const ngdb_plan* p) {
     if (!c->sem) throw Fail{NGDB_ERR_CONFIG, "semantic store not uploaded (ngdb_semantic_upload)"};
     const SparseTable tf = fusion_table(c, p, true);
     const double u = tf.n_rows, D = c->desc.dim, L = c->desc.semantic_dim;
-    if (c->profiling) c->fam_flops[F_ENTITY_PREP] += 2.0 * u * D * (L + 2 * D);
+    // M = W_s F, Z = S M^T + h W_h^T (+ Psi_theta's Y = E W_psi^T)
+    if (c->profiling)
+      c->fam_flops[F_ENTITY_PREP] += 2.0 * D * D * L + 2.0 * u * D * (L + D + (c->beta() ? 2 * D : 0));
     timed(c, F_ENTITY_PREP, u * (L * 4 + D * 4 * 2) + 4.0 * p->meta.n_econ,
           [&] { return fuse_prologue(a, tf, c->fscratch, c->fscratch_cap, lc); });
     CK(cudaGetLastError());
