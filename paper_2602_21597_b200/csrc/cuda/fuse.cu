@@ -47,7 +47,6 @@ struct FuseBufs {
   bool beta;
   float* S;  Split Ss;    // [u][dl]   gathered store rows
   float* X;  Split Xs;    // [u][2d]   [h | F s]
-  float* Zf;              // [u][d]    pre-activation
   float* dZ; Split dZs;   // [u][d]
   float* dX;              // [u][2d]   dZ W_p
   Split dZT, XT, dFsT, ST;  // transposed splits, rows padded to uP
@@ -76,7 +75,6 @@ FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
   f.Ss = take_split(sc, U * dl);
   f.X = sc.take(U * 2 * d);
   f.Xs = take_split(sc, U * 2 * d);
-  f.Zf = sc.take(U * d);
   f.dZ = sc.take(U * d);
   f.dZs = take_split(sc, U * d);
   f.dX = sc.take(U * 2 * d);
@@ -130,15 +128,6 @@ __global__ void __launch_bounds__(kWarps * 32) fuse_gather_kernel(DevArgs a, Spa
     const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) put(f.X, f.Xs, (int64_t)r * 2 * f.d + 4 * c + q, vv[q]);
-  }
-}
-
-__global__ void fuse_sigmoid_kernel(const float* Z, float* E, Split Es, int64_t n) {
-  pdl_start();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (Es.hi) put(E, Es, i, sigmoidf(Z[i]));
-    else E[i] = sigmoidf(Z[i]);
   }
 }
 
@@ -241,6 +230,7 @@ inline bool all_rows(const DevArgs& a, const SparseTable& t) {
 // the compact CSR's contribution segments (empty for untouched entities)
 __global__ void expand_seg_kernel(const int32_t* rows, const int32_t* seg, int u, int32_t* seg_full,
                                   int n) {
+  pdl_start();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e > n) return;
   int lo = 0, hi = u;  // first compact row with entity >= e
@@ -261,7 +251,7 @@ int64_t fuse_scratch_floats(int d, int dl, int64_t rows) {
 
 int launch_expand_rows(const int32_t* rows, const int32_t* seg, int u, int32_t* seg_full, int n,
                        cudaStream_t s) {
-  expand_seg_kernel<<<(n + 256) / 256, 256, 0, s>>>(rows, seg, u, seg_full, n);
+  launch_pdl(expand_seg_kernel, dim3((n + 256) / 256), dim3(256), 0, s, 1, rows, seg, u, seg_full, n);
   return 1;
 }
 
@@ -289,21 +279,21 @@ int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
   launches += tc_gemm(gm, lc.stream);
   // Z = S M^T + b_p, then Z += h W_h^T
   const Split Ss = whole ? Split{const_cast<float*>(a.sem_hi), const_cast<float*>(a.sem_lo)} : f.Ss;
-  TcGemmArgs g1 = gemm_args(u, d, dl, op(Ss, dl), op(f.Ms, dl), f.Zf, d);
+  float* zE = beta ? f.E : a.etab;  // Z, then sigmoid(Z) in place
+  TcGemmArgs g1 = gemm_args(u, d, dl, op(Ss, dl), op(f.Ms, dl), zE, d);
   g1.bias = p + a.dense_off[a.fus_idx + 2];
   launches += tc_gemm(g1, lc.stream);
-  TcGemmArgs g2 = gemm_args(u, d, d, op(f.Xs, 2 * d), wp, f.Zf, d);
+  // ... + h W_h^T, then E = sigmoid(Z) in the epilogue: the fused rows go
+  // straight to the step table (BetaE: to E, plain + split, for Psi_theta)
+  TcGemmArgs g2 = gemm_args(u, d, d, op(f.Xs, 2 * d), wp, zE, d);
   g2.accumulate = 1;
-  launches += tc_gemm(g2, lc.stream);
-  const int64_t n = (int64_t)u * d;
-  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)lc.num_sms * 8);
-  if (!beta) {
-    launch_pdl(fuse_sigmoid_kernel, dim3(blocks), dim3(256), 0, lc.stream, 1, (const float*)f.Zf,
-               a.etab, Split{nullptr, nullptr}, n);
-    return launches + 1;
+  g2.sigmoid = 1;
+  if (beta) {
+    g2.s_hi = f.Es.hi;
+    g2.s_lo = f.Es.lo;
   }
-  launch_pdl(fuse_sigmoid_kernel, dim3(blocks), dim3(256), 0, lc.stream, 1, (const float*)f.Zf, f.E,
-             f.Es, n);
+  launches += tc_gemm(g2, lc.stream);
+  if (!beta) return launches;
   // Psi_theta: Y = E W_psi^T + b_psi, then the BetaE entity table from Y
   TcGemmArgs gy = gemm_args(u, 2 * d, d, op(f.Es, d), wop(a, a.fus_idx + 3, 2 * d, d, false), f.Y, 2 * d);
   gy.bias = p + a.dense_off[a.fus_idx + 4];

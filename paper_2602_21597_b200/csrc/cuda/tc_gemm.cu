@@ -190,14 +190,16 @@ __device__ __forceinline__ void drain(uint32_t tmem, int buf, float* acc) {
 // CTA `rank` owns rows [r_beg, r_end) of the tile, sums them over the S
 // partial tiles in rank order (deterministic) and writes them out (bias, ReLU
 // mask, accumulate, row scatter, chained split).
+template <int TBN = BN>
 __device__ __forceinline__ void store_tile(const TcGemmArgs& g, float* tile_s, int m0, int n0,
                                            int r_beg, int r_end, int rank, int S, int nthreads) {
+  constexpr int kTileStride = TBN + 4;
   const int warp = threadIdx.x / 32;
   const uint32_t local = smem_u32(tile_s);
   if (((g.N | g.ldc) & 3) == 0) {
     // float4 epilogue: thread t takes 16-byte column groups of the CTA's rows;
     // the S partial loads are all issued before they are summed
-    constexpr int kQ = BN / 4;
+    constexpr int kQ = TBN / 4;
     const int n_items = (r_end - r_beg) * kQ;
     for (int it = threadIdx.x; it < n_items; it += nthreads) {
       const int r = r_beg + it / kQ, cq = (it % kQ) * 4;
@@ -241,6 +243,9 @@ __device__ __forceinline__ void store_tile(const TcGemmArgs& g, float* tile_s, i
         const float4 c0 = *reinterpret_cast<const float4*>(crow + n);
         v.x += c0.x; v.y += c0.y; v.z += c0.z; v.w += c0.w;
       }
+      if (g.sigmoid) {
+        v.x = sigmoidf(v.x); v.y = sigmoidf(v.y); v.z = sigmoidf(v.z); v.w = sigmoidf(v.w);
+      }
       *reinterpret_cast<float4*>(crow + n) = v;
       if (g.s_hi) {
         float4 h, l;
@@ -262,7 +267,7 @@ __device__ __forceinline__ void store_tile(const TcGemmArgs& g, float* tile_s, i
       if (row >= g.M) break;
       float* crow =
           g.c_rowoff ? g.C + g.c_rowoff[(int64_t)row * g.c_stride] : g.C + (int64_t)row * g.ldc;
-      for (int cc = lane; cc < BN; cc += 32) {
+      for (int cc = lane; cc < TBN; cc += 32) {
         const int n = n0 + cc;
         if (n >= g.N) break;
         float v = 0.f;
@@ -281,6 +286,7 @@ __device__ __forceinline__ void store_tile(const TcGemmArgs& g, float* tile_s, i
         if (g.bias) v += g.bias[n];
         if (g.mask && !(g.mask[(int64_t)row * g.ldc + n] > 0.f)) v = 0.f;
         if (g.accumulate) v += crow[n];
+        if (g.sigmoid) v = sigmoidf(v);
         crow[n] = v;
         if (g.s_hi) {
           float h, l;
@@ -408,10 +414,31 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
 
 
 // ---------------------------------------------------------------------------
-// TMA + warp-specialised mainloop (see the file comment).
-constexpr int kTmaStages = 4;
-constexpr int kTmaThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 drain/epilogue
-constexpr int TMA_SMEM_BYTES = kTmaStages * STAGE + 1024 + 256;
+// TMA + warp-specialised mainloop (see the file comment). Two tile widths:
+// BN = 80 (4 stages, 4 drain warps; small problems, where split-K fills the
+// GPU) and BN = 208 (2 stages, 8 drain warps — two per TMEM lane quarter, each
+// folding half the columns; problems with enough tiles to fill the GPU without
+// split-K). The wide tile reads A once per 208 output columns instead of per
+// 80: the large GEMMs (FuseSemantic, BetaE projections) are bound by the L2 ->
+// SMEM operand stream (hi + lo operands re-read per N tile), not by the MMA.
+template <int TBN>
+struct TmaCfg {
+  static constexpr int kBN = TBN;
+  static constexpr int kBTile = TBN * BK * 4;
+  static constexpr int kStage = 2 * A_TILE + 2 * kBTile;
+  static constexpr int kStages = TBN <= 80 ? 4 : (227 * 1024 - 1024 - 256) / kStage;
+  static constexpr int kGroups = TBN <= 80 ? 1 : 2;  // drain warps per TMEM lane quarter
+  static constexpr int kCols = TBN / kGroups;        // accumulator columns per drain thread
+  static constexpr int kThreads = 64 + 128 * kGroups;
+  static constexpr int kTmem = 2 * TBN <= 256 ? 256 : 512;
+  static constexpr int kSmem = kStages * kStage + 1024 + 256;
+  static constexpr uint32_t kInstr = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
+                                     ((uint32_t)(BM >> 4) << 24);
+  static_assert(kStages >= 2, "operand ring");
+  static_assert(kCols % 8 == 0 && TBN % 16 == 0 && TBN <= 256, "UMMA N");
+  static_assert(BM * (TBN + 4) * 4 <= kStages * kStage, "epilogue tile fits the ring");
+};
+constexpr int kWideBN = 208;
 
 struct TmaProblem {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;  // 2-D {K, rows} fp32 maps, box {32, BM | BN}
@@ -438,17 +465,30 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void umma_tf32_n(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
 
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <int TBN>
+__global__ void __launch_bounds__(TmaCfg<TBN>::kThreads, 1)
     tc_gemm_tma_kernel(const __grid_constant__ TcGemmTmaBatch batch) {
+  using Cfg = TmaCfg<TBN>;
+  constexpr int kSt = Cfg::kStages, kStageB = Cfg::kStage, kBT = Cfg::kBTile, kNC = Cfg::kCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 128B-swizzled tiles need 1024-byte aligned stage bases
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const uint32_t s_base = smem_u32(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTmaStages * STAGE);
-  uint64_t* empty = full + kTmaStages;
-  uint64_t* tfull = empty + kTmaStages;   // [2] TMEM buffer holds a finished chunk
-  uint64_t* tempty = tfull + 2;           // [2] TMEM buffer drained
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageB);
+  uint64_t* empty = full + kSt;
+  uint64_t* tfull = empty + kSt;   // [2] TMEM buffer holds a finished chunk
+  uint64_t* tempty = tfull + 2;    // [2] TMEM buffer drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int S = batch.S;
@@ -458,21 +498,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   const TcGemmArgs& g = batch.p[pi];
   const TmaProblem& mp = batch.maps[pi];
   const int lt = tile - batch.tile_begin[pi];
-  const int n_tiles_n = (g.N + BN - 1) / BN;
-  const int m0 = (lt / n_tiles_n) * BM, n0 = (lt % n_tiles_n) * BN;
+  const int n_tiles_n = (g.N + TBN - 1) / TBN;
+  const int m0 = (lt / n_tiles_n) * BM, n0 = (lt % n_tiles_n) * TBN;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int total_chunks = (g.K + BK - 1) / BK;
   const int c_beg = rank * total_chunks / S;
   const int n_chunks = (rank + 1) * total_chunks / S - c_beg;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kTmaStages; ++i) {
+    for (int i = 0; i < kSt; ++i) {
       mbar_init(smem_u32(&full[i]), 1);
       mbar_init(smem_u32(&empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&tfull[i]), 1);
-      mbar_init(smem_u32(&tempty[i]), 4);  // one arrive per drain warp
+      mbar_init(smem_u32(&tempty[i]), 4 * Cfg::kGroups);  // one arrive per drain warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mp.a_hi)));
@@ -483,7 +523,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "n"(kTmemCols));
+                 "n"(Cfg::kTmem));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -492,39 +532,40 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_start();  // everything above overlapped the previous kernel's tail
 
-  float acc[BN];
+  float acc[kNC];
+  const int quarter = warp & 3, group = warp >= 2 ? (warp - 2) / 4 : 0;
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
       for (int c = 0; c < n_chunks; ++c) {
-        const int st = c % kTmaStages, ph = (c / kTmaStages) & 1;
+        const int st = c % kSt, ph = (c / kSt) & 1;
         mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-        const uint32_t bar = smem_u32(&full[st]), dst = s_base + st * STAGE;
-        mbar_expect_tx(bar, STAGE);
+        const uint32_t bar = smem_u32(&full[st]), dst = s_base + st * kStageB;
+        mbar_expect_tx(bar, kStageB);
         const int k0 = (c_beg + c) * BK;
         tma_load_2d(dst, &mp.a_hi, bar, k0, m0);
         tma_load_2d(dst + A_TILE, &mp.a_lo, bar, k0, m0);
         tma_load_2d(dst + 2 * A_TILE, &mp.b_hi, bar, k0, n0);
-        tma_load_2d(dst + 2 * A_TILE + B_TILE, &mp.b_lo, bar, k0, n0);
+        tma_load_2d(dst + 2 * A_TILE + kBT, &mp.b_lo, bar, k0, n0);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
       for (int c = 0; c < n_chunks; ++c) {
-        const int st = c % kTmaStages, ph = (c / kTmaStages) & 1;
+        const int st = c % kSt, ph = (c / kSt) & 1;
         const int buf = c & 1, bph = (c >> 1) & 1;
         mbar_wait(smem_u32(&tempty[buf]), bph ^ 1);
         mbar_wait(smem_u32(&full[st]), ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t a_hi = s_base + st * STAGE, a_lo = a_hi + A_TILE;
-        const uint32_t b_hi = a_hi + 2 * A_TILE, b_lo = b_hi + B_TILE;
-        const uint32_t d = tmem + buf * BN;
+        const uint32_t a_hi = s_base + st * kStageB, a_lo = a_hi + A_TILE;
+        const uint32_t b_hi = a_hi + 2 * A_TILE, b_lo = b_hi + kBT;
+        const uint32_t d = tmem + buf * TBN;
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first, fresh accumulator per chunk
           const uint32_t off = ks * 32;
-          umma_tf32(d, umma_desc(a_lo + off), umma_desc(b_hi + off), ks == 0 ? 0u : 1u);
-          umma_tf32(d, umma_desc(a_hi + off), umma_desc(b_lo + off), 1u);
-          umma_tf32(d, umma_desc(a_hi + off), umma_desc(b_hi + off), 1u);
+          umma_tf32_n(d, umma_desc(a_lo + off), umma_desc(b_hi + off), Cfg::kInstr, ks == 0 ? 0u : 1u);
+          umma_tf32_n(d, umma_desc(a_hi + off), umma_desc(b_lo + off), Cfg::kInstr, 1u);
+          umma_tf32_n(d, umma_desc(a_hi + off), umma_desc(b_hi + off), Cfg::kInstr, 1u);
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&empty[st])));
@@ -533,49 +574,56 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       }
     }
     __syncwarp();
-  } else {  // ---- drain warps 2..5: TMEM lane quarter (warp % 4), one row per thread
+  } else {  // ---- drain warps: TMEM lane quarter (warp % 4), column group, one row per thread
 #pragma unroll
-    for (int j = 0; j < BN; ++j) acc[j] = 0.f;
-    const uint32_t lanes = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    for (int j = 0; j < kNC; ++j) acc[j] = 0.f;
+    const uint32_t lanes = (static_cast<uint32_t>(quarter * 32) << 16) + group * kNC;
+    constexpr int kPiece = kNC <= 80 ? kNC : 32;  // columns in flight per tcgen05.wait
     for (int c = 0; c < n_chunks; ++c) {
       const int buf = c & 1, bph = (c >> 1) & 1;
       mbar_wait(smem_u32(&tfull[buf]), bph);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      uint32_t r[BN];
 #pragma unroll
-      for (int j = 0; j < BN; j += 8)
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(r[j]), "=r"(r[j + 1]), "=r"(r[j + 2]), "=r"(r[j + 3]), "=r"(r[j + 4]),
-                       "=r"(r[j + 5]), "=r"(r[j + 6]), "=r"(r[j + 7])
-                     : "r"(tmem + lanes + buf * BN + j));
-      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      for (int p0 = 0; p0 < kNC; p0 += kPiece) {
+        uint32_t r[kPiece];
+#pragma unroll
+        for (int j = 0; j < kPiece; j += 8)
+          if (p0 + j < kNC)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(r[j]), "=r"(r[j + 1]), "=r"(r[j + 2]), "=r"(r[j + 3]), "=r"(r[j + 4]),
+                           "=r"(r[j + 5]), "=r"(r[j + 6]), "=r"(r[j + 7])
+                         : "r"(tmem + lanes + buf * TBN + p0 + j));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < kPiece; ++j)
+          if (p0 + j < kNC) acc[p0 + j] += __uint_as_float(r[j]);
+      }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
-#pragma unroll
-      for (int j = 0; j < BN; ++j) acc[j] += __uint_as_float(r[j]);
     }
   }
   // every chunk has been consumed by the tensor core and drained: the ring is free
   __syncthreads();
+  constexpr int kStride = TBN + 4;
   float* tile_s = reinterpret_cast<float*>(smem);
   if (warp >= 2) {
-    const int r = (warp & 3) * 32 + lane;
+    const int r = quarter * 32 + lane;
 #pragma unroll
-    for (int j = 0; j < BN; j += 4)
-      *reinterpret_cast<float4*>(&tile_s[r * kTileStride + j]) =
+    for (int j = 0; j < kNC; j += 4)
+      *reinterpret_cast<float4*>(&tile_s[r * kStride + group * kNC + j]) =
           make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
   }
   const int r_beg = rank * BM / S, r_end = (rank + 1) * BM / S;
   if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   else __syncthreads();
-  store_tile(g, tile_s, m0, n0, r_beg, r_end, rank, S, kTmaThreads);
+  store_tile<TBN>(g, tile_s, m0, n0, r_beg, r_end, rank, S, Cfg::kThreads);
   if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(kTmemCols));
+                 "n"(Cfg::kTmem));
 }
 
 // --- operand split / transpose ------------------------------------------------
@@ -643,8 +691,10 @@ void tc_gemm_init() {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(tc_gemm_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TMA_SMEM_BYTES);
+    cudaFuncSetAttribute(tc_gemm_tma_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TmaCfg<BN>::kSmem);
+    cudaFuncSetAttribute(tc_gemm_tma_kernel<kWideBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TmaCfg<kWideBN>::kSmem);
     configured = true;
   }
 }
@@ -703,24 +753,49 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
   if (tma) {
+    // tile width: the wide tile for problems with many row tiles (measured,
+    // profiles/r02/gemm_wide.jsonl: 14.5k x 400 x 768 82 -> 65 us, 4096 x 800 x
+    // 1200 84 -> 45 us); narrow where split-K must fill the GPU (C2's 731-row
+    // MLPs, 1434-row projections, the K = rows weight gradients).
+    // NGDB_GEMM_BN=80|208 forces one.
+    static const int forced_bn = [] {
+      const char* e = std::getenv("NGDB_GEMM_BN");
+      return e ? std::atoi(e) : 0;
+    }();
+    int wide_tiles = 0, min_n = 1 << 30;
+    for (int i = 0; i < b.n; ++i) {
+      wide_tiles += ((b.p[i].M + BM - 1) / BM) * ((b.p[i].N + kWideBN - 1) / kWideBN);
+      min_n = std::min(min_n, b.p[i].N);
+    }
+    bool wide = min_n >= 192 && wide_tiles >= 64;
+    if (forced_bn == 80 || g_split_override.load(std::memory_order_relaxed)) wide = false;
+    if (forced_bn == kWideBN) wide = true;
+    const int tbn = wide ? kWideBN : BN;
     TcGemmTmaBatch t{};  // ~2.6 KB of kernel parameters (4 tensor maps per problem)
+    int tiles_t = 0;
     for (int i = 0; i < b.n && tma; ++i) {
       const TcGemmArgs& g = b.p[i];
       t.p[i] = g;
       tma = encode(&t.maps[i].a_hi, g.A.hi, g.M, g.K, g.A.ld, BM) &&
             encode(&t.maps[i].a_lo, g.A.lo, g.M, g.K, g.A.ld, BM) &&
-            encode(&t.maps[i].b_hi, g.B.hi, g.N, g.K, g.B.ld, BN) &&
-            encode(&t.maps[i].b_lo, g.B.lo, g.N, g.K, g.B.ld, BN);
-      t.tile_begin[i] = b.tile_begin[i];
+            encode(&t.maps[i].b_hi, g.B.hi, g.N, g.K, g.B.ld, tbn) &&
+            encode(&t.maps[i].b_lo, g.B.lo, g.N, g.K, g.B.ld, tbn);
+      t.tile_begin[i] = tiles_t;
+      tiles_t += ((g.M + BM - 1) / BM) * ((g.N + tbn - 1) / tbn);
     }
     if (tma) {
-      t.tile_begin[b.n] = tiles;
+      t.tile_begin[b.n] = tiles_t;
       t.n = b.n;
-      // one CTA per SM (208 KB ring): split-K so the launch fills about one wave,
-      // at most 8 CTAs per cluster and at least 2 chunks per CTA
-      t.S = std::max(1, std::min({8, num_sms / std::max(tiles, 1), max_chunks / 2}));
+      // one CTA per SM (~210 KB ring): split-K so the launch fills about one
+      // wave, at most 8 CTAs per cluster and at least 2 chunks per CTA
+      t.S = std::max(1, std::min({8, num_sms / std::max(tiles_t, 1), max_chunks / 2}));
       if (const int o = g_split_override.load(std::memory_order_relaxed)) t.S = std::min(o, std::max(1, max_chunks));
-      launch_pdl(tc_gemm_tma_kernel, dim3(tiles * t.S), dim3(kTmaThreads), TMA_SMEM_BYTES, s, t.S, t);
+      if (wide)
+        launch_pdl(tc_gemm_tma_kernel<kWideBN>, dim3(tiles_t * t.S), dim3(TmaCfg<kWideBN>::kThreads),
+                   TmaCfg<kWideBN>::kSmem, s, t.S, t);
+      else
+        launch_pdl(tc_gemm_tma_kernel<BN>, dim3(tiles_t * t.S), dim3(TmaCfg<BN>::kThreads),
+                   TmaCfg<BN>::kSmem, s, t.S, t);
       return 1;
     }
   }

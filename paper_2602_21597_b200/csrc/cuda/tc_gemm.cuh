@@ -42,6 +42,8 @@ struct TcGemmArgs {
   const float* mask;
   // optional chained output: split(relu?(C)) -> s_hi/s_lo [M][ldc] (no scatter)
   float* s_hi; float* s_lo; int s_relu;
+  // optional activation after bias / accumulate: C = sigmoid(C) (FuseSemantic's E)
+  int sigmoid;
 };
 
 int tc_gemm(const TcGemmArgs& g, cudaStream_t s);

@@ -17,12 +17,15 @@ SHAPES = [  # (label, M, N, K, batch)
     ("c3 project L1 (1434 x 1200 -> 800)", 1434, 800, 1200, 1),
     ("c3 project L2 (1434 x 800 -> 800)", 1434, 800, 800, 1),
     ("c3 project dW1 (800 x 1200, K = 1434)", 800, 1200, 1434, 1),
-    ("c4 fusion F s (14.5k x 768 -> 400)", 14505, 400, 768, 1),
-    ("c4 fusion W_p (14.5k x 800 -> 400)", 14505, 400, 800, 1),
+    ("c4 fusion S M^T (14.5k x 768 -> 400)", 14505, 400, 768, 1),
+    ("c4 fusion h W_h^T / dh (14.5k x 400 -> 400)", 14505, 400, 400, 1),
+    ("c4 fusion dM = dZ^T S (400 x 768, K = 14.5k)", 400, 768, 14505, 1),
+    ("c4 fusion dW_h = dZ^T h (400 x 400, K = 14.5k)", 400, 400, 14505, 1),
+    ("c3 psi-free project L1 at 4k rows (4096 x 1200 -> 800)", 4096, 800, 1200, 1),
 ]
 f = lib.ngdb_debug_tc_gemm_time
 f.argtypes = [C.c_int] * 5 + [C.POINTER(C.c_float)]
-kind = "cpasync" if os.environ.get("NGDB_GEMM_CPASYNC") else "tma"
+kind = "cpasync" if os.environ.get("NGDB_GEMM_CPASYNC") else "tma" + os.environ.get("NGDB_GEMM_BN", "")
 for label, M, N, K, b in SHAPES:
     ms = C.c_float()
     rc = f(M, N, K, b, 50, C.byref(ms))
