@@ -571,9 +571,9 @@ def main():
     if args.impl == "reference":
         return reference_arm(args)
     if args.config == "c5" or world > 1:
-        if args.config in ("c3", "c4"):
-            raise SystemExit(f"bench.py: --config {args.config} has no row-sharded step "
-                             "(BetaE / fusion); N > 1 runs c1, c2 or c5 row-sharded")
+        if args.config == "c4":
+            raise SystemExit("bench.py: --config c4 has no row-sharded step (FuseSemantic); "
+                             "N > 1 runs c1, c2, c3 or c5 row-sharded")
         return bench_sharded(args)
     dist = None
 
