@@ -495,20 +495,24 @@ def bench_sharded(args):
     # losses read back per step
     # this rank's share of the host cores (minus the launching and exchange threads)
     producers = max(2, host_workers() // world - 2)
+    # one trainer-loop call: W warm-up steps, then the K timed ones (window
+    # measured inside the loop, as in the single-GPU e2e)
     eng.step_count = step_no
-    eng.train_native(graph, w, 3, batch, n_neg, first_tag=1 + n_steps, producers=producers)
     b0, d0 = C.c_int64(), C.c_int64()
     check(lib.ngdb_transfer_bytes(ctx, C.byref(b0), C.byref(d0)))
     dist.barrier()
+    n_call = args.warmup + args.steps
     t0 = time.perf_counter()
-    eng.train_native(graph, w, args.steps, batch, n_neg, first_tag=1 + n_steps + 3,
-                     producers=producers)
+    eng.train_native(graph, w, n_call, batch, n_neg, first_tag=1 + n_steps, producers=producers,
+                     steady_from=args.warmup)
     torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    call_s = time.perf_counter() - t0
+    e2e_s = eng.last_timings["steady_s"]
     b1, d1 = C.c_int64(), C.c_int64()
     check(lib.ngdb_transfer_bytes(ctx, C.byref(b1), C.byref(d1)))
     step_no = eng.step_count
     e2e = batch * world * args.steps / max_over_ranks(e2e_s)
+    e2e_call = batch * world * n_call / max_over_ranks(call_s)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
@@ -519,7 +523,11 @@ def bench_sharded(args):
             "roofline": roofline(fams) if fams else None,
             "cpu_baseline": None,
             "e2e": {"value": e2e, "unit": "queries/s",
-                    "h2d_bytes_per_step": int((b1.value - b0.value) / args.steps),
+                    "h2d_bytes_per_step": int((b1.value - b0.value) / n_call),
+                    "window": f"steps {args.warmup}..{n_call - 1} of one {n_call}-step "
+                              "ngdb_shard_train_run call (timed inside the loop)",
+                    "whole_call": {"value": e2e_call, "steps": n_call,
+                                   "note": "thread start-up and pipeline fill included"},
                     "api": "ngdb_shard_train_run (producer threads sample + plan + pack, "
                            "exchange thread all-gathers the packed metadata over the "
                            "metadata communicator and builds owner lists, stages + NCCL "
@@ -690,19 +698,24 @@ def main():
     w = m.pattern_weights(MIXES[mix])
     tag0 = 1_000_000 + rank * 100_000
 
-    def loop(n, tag):
-        eng.step_count = step_no
-        return eng.train(graph, w, n, batch=batch, n_neg=n_neg, seed=3, first_tag=tag,
-                         n_producers=args.producers, in_flight=args.in_flight)
-    loop(args.warmup, tag0)
-    step_no += args.warmup
+    # ONE trainer-loop call runs the W warm-up steps and then the K timed
+    # steps (a training run is one call): the timed window starts when the
+    # consumer reaches step W (that step's plan wait included) and ends when
+    # step W+K-1's losses are back on the host (steady_s, measured inside the
+    # loop). The whole call, thread start-up and pipeline fill included, is
+    # reported beside it.
     b0, d0 = C.c_int64(), C.c_int64()
     check(lib.ngdb_transfer_bytes(ctx, C.byref(b0), C.byref(d0)))
     barrier()
+    eng.step_count = step_no
     t0 = time.perf_counter()
-    loop(args.steps, tag0 + args.warmup)
-    e2e_s = time.perf_counter() - t0
-    step_no += args.steps
+    eng.train(graph, w, args.warmup + args.steps, batch=batch, n_neg=n_neg, seed=3,
+              first_tag=tag0, n_producers=args.producers, in_flight=args.in_flight,
+              steady_from=args.warmup)
+    call_s = time.perf_counter() - t0
+    e2e_s = eng.last_timings["steady_s"]
+    n_call = args.warmup + args.steps
+    step_no += n_call
     b1, d1 = C.c_int64(), C.c_int64()
     check(lib.ngdb_transfer_bytes(ctx, C.byref(b1), C.byref(d1)))
     gu, gi = C.c_int64(), C.c_int64()
@@ -713,7 +726,11 @@ def main():
         t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+        t = torch.tensor([call_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        call_s = float(t.item())
     e2e = batch * world * args.steps / e2e_s
+    e2e_call = batch * world * n_call / call_s
     producers = args.producers if args.producers > 0 else max(1, (os.cpu_count() or 2) - 1)
     # the same public API one step at a time, no overlap (ngdb_train_step on
     # pre-sampled batches): what a synchronous caller gets
@@ -772,12 +789,17 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "queries/s",
-                    "h2d_bytes_per_step": int((b1.value - b0.value) / args.steps),
-                    "d2h_bytes_per_step": int((d1.value - d0.value) / args.steps),
+                    "h2d_bytes_per_step": int((b1.value - b0.value) / n_call),
+                    "d2h_bytes_per_step": int((d1.value - d0.value) / n_call),
                     "api": "ngdb_train_run (sampling + planning on host producer threads, "
                            "plan H2D, kernels, loss D2H per step)",
+                    "window": f"steps {args.warmup}..{n_call - 1} of one {n_call}-step "
+                              "ngdb_train_run call (timed inside the loop)",
+                    "whole_call": {"value": e2e_call, "steps": n_call,
+                                   "note": "thread start-up and pipeline fill included"},
                     "producers": producers,
-                    "consumer_ms_per_step": {k[:-2]: 1000 * v / args.steps for k, v in tim.items()},
+                    "consumer_ms_per_step": {k[:-2]: 1000 * v / n_call for k, v in tim.items()
+                                             if k != "steady_s"},
                     "sequential_train_step": seq_qps,
                     "step_graphs": {"updated": gu.value, "instantiated": gi.value}},
             "gpu_launches": int(launches),

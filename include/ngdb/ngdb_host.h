@@ -143,6 +143,10 @@ typedef struct ngdb_train_opts {
   uint64_t first_tag;
   int32_t in_flight;             /* steps submitted ahead of the oldest uncollected one; 0: 2 */
   int32_t flags;                 /* NGDB_TRAIN_NO_GRAPHS: stream launches instead of step graphs */
+  int32_t steady_from;           /* > 0: timings[6] = host seconds from the consumer reaching step
+                                    steady_from (its plan wait included) to the last step's losses
+                                    read back — the steady-state window after warm-up steps
+                                    of the same call (timings then needs 7 entries) */
 } ngdb_train_opts;
 #define NGDB_TRAIN_NO_GRAPHS 1
 int ngdb_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,

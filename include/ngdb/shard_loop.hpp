@@ -25,12 +25,14 @@ struct ShardLoopConfig {
   int32_t n_producers = 0;  // 0: hardware threads - 2
   int32_t queue_depth = 0;  // 0: 2 * producers
   int32_t in_flight = 2;
+  int32_t steady_from = 0;  // > 0: ShardLoopStats::steady_s times steps [steady_from, n_steps)
 };
 
 struct ShardLoopStats {
   double plan_wait_s = 0.0, submit_s = 0.0, collect_wait_s = 0.0;
   double exchange_s = 0.0;  // on the exchange thread (all-gathers)
   double build_s = 0.0;     // unused: owner lists are built by the producers
+  double steady_s = 0.0;    // consumer at step steady_from -> last losses read back
   int32_t producers = 0;
 };
 

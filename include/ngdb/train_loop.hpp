@@ -33,6 +33,7 @@ struct TrainLoopConfig {
   int32_t queue_depth = 0;  // planned batches buffered ahead of the consumer; 0: 2 * producers
   bool graphs = true;       // launch each step as one CUDA graph (ngdb_step_launch)
   int32_t in_flight = 2;    // steps on the device before the oldest one's losses are read back
+  int32_t steady_from = 0;  // > 0: TrainLoopStats::steady_s times steps [steady_from, n_steps)
 
   // -- adaptive sampling feedback (SURVEY A-10) ---------
   // After every step the consumer records, per pattern present in the batch,
@@ -60,6 +61,7 @@ struct TrainLoopStats {
   double pools_s = 0.0;         //   ngdb_exec_pool calls
   double optim_s = 0.0;         //   ngdb_optimizer_step
   double collect_wait_s = 0.0;  // consumer waiting for a step's losses
+  double steady_s = 0.0;        // consumer at step steady_from -> last losses read back
   int32_t producers = 0;
 };
 

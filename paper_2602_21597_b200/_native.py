@@ -63,7 +63,7 @@ class ShardPlan(C.Structure):
 class TrainOpts(C.Structure):
     _fields_ = [("pattern_weights", P(f64)), ("batch", i32), ("n_neg", i32), ("b_max", i32),
                 ("n_producers", i32), ("queue_depth", i32), ("seed", u64), ("first_tag", u64),
-                ("in_flight", i32), ("flags", i32)]
+                ("in_flight", i32), ("flags", i32), ("steady_from", i32)]
 
 
 class TrainFeedback(C.Structure):

@@ -525,6 +525,7 @@ int ngdb_train_run_ex(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts*
     cfg.first_tag = o->first_tag;
     if (o->in_flight > 0) cfg.in_flight = o->in_flight;
     cfg.graphs = (o->flags & NGDB_TRAIN_NO_GRAPHS) == 0;
+    cfg.steady_from = o->steady_from;
     ngdb::DifficultyTracker tracker;
     if (fb) {
       cfg.adaptive = fb->adaptive != 0;
@@ -558,6 +559,7 @@ int ngdb_train_run_ex(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts*
       timings[3] = st.begin_s;
       timings[4] = st.pools_s;
       timings[5] = st.optim_s;
+      if (o->steady_from > 0) timings[6] = st.steady_s;
     }
   });
 }
@@ -584,6 +586,7 @@ int ngdb_shard_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_op
     cfg.seed = o->seed;
     cfg.first_tag = o->first_tag;
     if (o->in_flight > 0) cfg.in_flight = o->in_flight;
+    cfg.steady_from = o->steady_from;
     const auto st = ngdb::run_shard_train_loop(ctx, g->split, cfg, first_step, n_steps, loss_per_step);
     if (timings) {
       timings[0] = st.plan_wait_s;
@@ -592,6 +595,7 @@ int ngdb_shard_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_op
       timings[3] = st.exchange_s;
       timings[4] = st.build_s;
       timings[5] = st.producers;
+      if (o->steady_from > 0) timings[6] = st.steady_s;
     }
   });
 }

@@ -217,8 +217,10 @@ ShardLoopStats run_shard_train_loop(ngdb_ctx* ctx, const GraphSplit& graph,
     if (nonfinite) throw NonFinite("non-finite loss at step " + std::to_string(first_step + i + 1));
     if (loss_per_step) loss_per_step[i] = loss;
   };
+  std::chrono::steady_clock::time_point t_steady{};
   try {
     for (int32_t i = 0; i < n_steps; ++i) {
+      if (cfg.steady_from > 0 && i == cfg.steady_from) t_steady = std::chrono::steady_clock::now();
       StepPlanHost plan;
       ShardPlanHost shard;
       {
@@ -270,6 +272,7 @@ ShardLoopStats run_shard_train_loop(ngdb_ctx* ctx, const GraphSplit& graph,
       while (static_cast<int32_t>(pending.size()) >= in_flight) collect();
     }
     while (!pending.empty()) collect();
+    if (cfg.steady_from > 0 && cfg.steady_from < n_steps) stats.steady_s = seconds_since(t_steady);
   } catch (...) {
     shutdown();
     for (const auto& [i, ticket] : pending) ngdb_step_wait(ctx, ticket, nullptr, 0, nullptr, nullptr);

@@ -203,8 +203,10 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
   auto drain = [&] {
     while (!pending.empty()) collect();
   };
+  std::chrono::steady_clock::time_point t_steady{};
   try {
     for (int32_t i = 0; i < n_steps; ++i) {
+      if (cfg.steady_from > 0 && i == cfg.steady_from) t_steady = std::chrono::steady_clock::now();
       if (cfg.adaptive && i > 0 && i % R == 0) {
         // refresh boundary: every earlier step's losses are in the tracker
         drain();
@@ -262,6 +264,7 @@ TrainLoopStats run_train_loop(ngdb_ctx* ctx, const GraphSplit& graph, const Trai
       while (static_cast<int32_t>(pending.size()) >= in_flight) collect();
     }
     drain();
+    if (cfg.steady_from > 0 && cfg.steady_from < n_steps) stats.steady_s = seconds_since(t_steady);
   } catch (...) {
     shutdown();
     for (const auto& pd : pending) ngdb_step_wait(ctx, pd.ticket, nullptr, 0, nullptr, nullptr);

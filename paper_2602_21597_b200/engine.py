@@ -354,7 +354,7 @@ class Engine:
               graphs: bool = True, adaptive: bool = False, refresh_every: int = 100,
               tracker: Optional["DifficultyTracker"] = None, metrics_path: Optional[str] = None,
               checkpoint_path: Optional[str] = None, checkpoint_every: int = 0,
-              config_hash: int = 0, pi_per_step: bool = False):
+              config_hash: int = 0, pi_per_step: bool = False, steady_from: int = 0):
         """The trainer loop: n_steps steps of batches sampled
         from Rng(seed).fork(first_tag + i) by host producer threads, planned,
         uploaded and run back to back (ngdb_train_run_ex), with the trainer's
@@ -364,10 +364,12 @@ class Engine:
          and a checkpoint cadence. Returns the
         per-step loss sums (plus [n_steps][batch] per-query losses with
         per_query=True, plus the [n_steps][14] π of each batch with
-        pi_per_step=True)."""
+        pi_per_step=True). steady_from > 0: last_timings['steady_s'] = host
+        seconds from the loop reaching step steady_from to the end (the
+        steady-state window after warm-up steps of the same call)."""
         w = np.ascontiguousarray(weights, dtype=np.float64)
         opts = TrainOpts(_p(w, C.c_double), batch, n_neg, self.b_max, n_producers, queue_depth,
-                         seed, first_tag, in_flight, 0 if graphs else 1)
+                         seed, first_tag, in_flight, 0 if graphs else 1, steady_from)
         tr = tracker if tracker is not None else DifficultyTracker()
         pis = np.zeros((n_steps, 14), dtype=np.float64)
         fb = TrainFeedback(1 if adaptive else 0, refresh_every, tr.decay, tr.eta, tr.floor,
@@ -378,7 +380,7 @@ class Engine:
                            checkpoint_every, config_hash)
         sums = np.zeros(n_steps, dtype=np.float64)
         pq = np.zeros((n_steps, batch), dtype=np.float32) if per_query else None
-        timings = (C.c_double * 6)()
+        timings = (C.c_double * 7)()
         check(lib.ngdb_train_run_ex(self._h, graph._h, C.byref(opts), C.byref(fb),
                                     self.step_count, n_steps, _p(sums, C.c_double),
                                     _p(pq, C.c_float) if pq is not None else None, timings))
@@ -386,7 +388,8 @@ class Engine:
         # host seconds of the calling thread: waiting for plans, submitting, waiting for results
         self.last_timings = {"plan_wait_s": timings[0], "submit_s": timings[1],
                              "collect_wait_s": timings[2], "submit_begin_s": timings[3],
-                             "submit_pools_s": timings[4], "submit_optimizer_s": timings[5]}
+                             "submit_pools_s": timings[4], "submit_optimizer_s": timings[5],
+                             "steady_s": timings[6]}
         out = (sums,)
         if per_query:
             out += (pq,)

@@ -370,27 +370,28 @@ class ShardedEngine:
         return sums
 
     def train_native(self, graph, weights, n_steps: int, batch: int, n_neg: int, first_tag: int,
-                     producers: int = 0, in_flight: int = 0) -> np.ndarray:
+                     producers: int = 0, in_flight: int = 0, steady_from: int = 0) -> np.ndarray:
         """The sharded trainer loop in libngdb (ngdb_shard_train_run; NCCL
         transport): producer threads sample + plan + pack, an exchange thread
         all-gathers the packed records over the context's metadata
         communicator and builds the owner lists, the calling thread launches
         each step. Batch of step s: Rng(3).fork((first_tag + s) * world + rank).
-        Returns the per-step loss sums of this rank."""
+        Returns the per-step loss sums of this rank (steady_from: as Engine.train)."""
         from ._native import TrainOpts
         if not self.comm.nccl:
             raise RuntimeError("train_native needs the NCCL transport")
         w = np.ascontiguousarray(weights, dtype=np.float64)
         opts = TrainOpts(_p(w, C.c_double), batch, n_neg, self.b_max, producers, 0, 3, first_tag,
-                         in_flight, 0)
+                         in_flight, 0, steady_from)
         sums = np.zeros(n_steps, np.float64)
-        timings = (C.c_double * 6)()
+        timings = (C.c_double * 7)()
         check(lib.ngdb_shard_train_run(self._h, graph._h, C.byref(opts), self.step_count, n_steps,
                                        _p(sums, C.c_double), timings))
         self.step_count += n_steps
         self.last_timings = {"plan_wait_s": timings[0], "submit_s": timings[1],
                              "collect_wait_s": timings[2], "exchange_s": timings[3],
-                             "build_s": timings[4], "producers": int(timings[5])}
+                             "build_s": timings[4], "producers": int(timings[5]),
+                             "steady_s": timings[6]}
         return sums
 
     def capture(self, steps: List[ShardStep]) -> List["ShardGraph"]:
