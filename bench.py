@@ -436,9 +436,12 @@ def bench_sharded(args):
     # rank r's batch of step s: Rng(3).fork(s * world + r)
     batches = [m.Batch.sample(graph, w, batch, n_neg, seed=3, tag=(1 + s) * world + rank)
                for s in range(n_steps)]
+    sdim = SEMANTIC_DIM.get(args.config, 0)
+    store = m.semantic_store(info["n_entities"], sdim, seed=5) if sdim else None
     eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
-                        n_neg=n_neg, max_queries=batch, device=local)
-    plans = [plan_shard_step(comm, b, backbone, dim, batch_cap=batch) for b in batches]
+                        n_neg=n_neg, max_queries=batch, device=local, semantic=store)
+    plans = [plan_shard_step(comm, b, backbone, dim, batch_cap=batch, semantic=bool(sdim))
+             for b in batches]
     setup_s = time.perf_counter() - t_setup
     ctx = eng.handle
     step_no = 0
@@ -579,9 +582,6 @@ def main():
     if args.impl == "reference":
         return reference_arm(args)
     if args.config == "c5" or world > 1:
-        if args.config == "c4":
-            raise SystemExit("bench.py: --config c4 has no row-sharded step (FuseSemantic); "
-                             "N > 1 runs c1, c2, c3 or c5 row-sharded")
         return bench_sharded(args)
     dist = None
 

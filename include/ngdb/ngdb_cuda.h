@@ -174,7 +174,11 @@ typedef enum ngdb_shard_stage {
   NGDB_SHARD_SCORE = 3,       /* owner scoring of all ranks' units over owned candidates */
   NGDB_SHARD_SCORE_DONE = 4,  /* dq_mine / loss_mine -> this rank's Loss results */
   NGDB_SHARD_BACKWARD = 5,    /* backward pools (trace order) */
-  NGDB_SHARD_GRAD_PACK = 6    /* anchor grads -> grad_send; dense + relation grads -> reduce */
+  NGDB_SHARD_GRAD_PACK = 6,   /* anchor grads -> grad_send; dense + relation grads -> reduce */
+  NGDB_SHARD_FUSE_BWD = 7     /* FuseSemantic only, after the gradient all-to-all: the fusion
+                                 backward over the owned rows (returned anchor rows + owned
+                                 candidates) into the dense grads, which are re-copied into
+                                 reduce (the all-reduce follows) */
 } ngdb_shard_stage;
 
 typedef struct ngdb_ctx ngdb_ctx;

@@ -324,8 +324,12 @@ int launch_expand_rows(const int32_t* rows, const int32_t* seg, int u, int32_t* 
 float* fuse_y_table(float* fs, int64_t cap, int u, int d, int dl);
 
 int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const LaunchCtx& lc);
+// adam = false (row-sharded step): the dense gradients and dh only; the
+// entity rows' Adam then runs as fuse_entity_adam after the all-reduce
 int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const AdamHyper& hp,
-                  const float* bc, const LaunchCtx& lc);
+                  const float* bc, const LaunchCtx& lc, bool adam = true);
+int fuse_entity_adam(const SparseTable& t, float* fs, int64_t cap, int d, int dl, bool beta,
+                     const AdamHyper& hp, const float* bc, const LaunchCtx& lc);
 int launch_beta_entity_adam(const DevArgs& a, const SparseTable& t, const AdamHyper& hp,
                             const float* bc, const LaunchCtx& lc);
 // shard.cu (row-sharded step)

@@ -264,6 +264,10 @@ struct ngdb_ctx {
     // the shard CSR) and global score code -> table row
     float *etab = nullptr, *etab_c = nullptr;
     int32_t* cand_local = nullptr;
+    // FuseSemantic: the fusion scratch over the owned rows, lookup-send position -> CSR row
+    float* fscratch = nullptr;
+    int64_t fscratch_cap = 0;
+    int32_t* anchor_local = nullptr;
     int32_t n_rows = 0;
     const int32_t *rows = nullptr, *seg = nullptr, *contrib = nullptr;
     bool active = false;
@@ -449,7 +453,8 @@ void ensure_step_buffers(ngdb_ctx* c, const PlanMeta& m) {
     ++c->buffer_gen;
   }
   const int64_t erows = fusion_whole(c, m) ? int64_t(c->desc.n_entities) : m.n_erows;
-  if (c->step_table() && erows > c->cap_erows) {
+  // (row-sharded: the step table lives in the shard buffers, sized per step)
+  if (c->step_table() && c->world == 1 && erows > c->cap_erows) {
     CK(cudaStreamSynchronize(c->stream));
     c->cap_erows = std::max<int64_t>(erows, c->cap_erows + c->cap_erows / 4);
     if (c->etab) CK(cudaFree(c->etab));
@@ -508,10 +513,11 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.etab = c->etab;
   a.etab_c = c->etab_c;
   a.cand_local = c->cand_local;
-  if (c->world > 1) {
+  if (c->sh.active) {  // a row-sharded step (any world size): its own step table
     a.etab = c->sh.etab;
     a.etab_c = c->sh.etab_c;
     a.cand_local = c->sh.cand_local;
+    a.anchor_local = c->sh.anchor_local;
   }
   a.fused = c->fused() ? 1 : 0;
   a.sem_dim = c->desc.semantic_dim;
@@ -532,6 +538,11 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
                               fusion_whole(c, p->meta) ? c->desc.n_entities : p->meta.n_erows,
                               c->desc.dim, c->desc.semantic_dim)
                : nullptr;
+  if (c->sh.active)  // row-sharded: the fusion runs over the owned rows of the shard CSR
+    a.ytab = (c->beta() && c->fused() && c->sh.fscratch)
+                 ? fuse_y_table(c->sh.fscratch, c->sh.fscratch_cap, c->sh.n_rows, c->desc.dim,
+                                c->desc.semantic_dim)
+                 : nullptr;
   a.istash = c->istash;
   a.istash_slots = c->istash_slots;
   a.pstash = c->pstash;
@@ -1068,8 +1079,6 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
       throw Fail{NGDB_ERR_CONFIG, "semantic_dim must be a multiple of 4, <= 4096"};
     const int world = d.world > 1 ? d.world : 1;
     if (world > 1 && (d.rank < 0 || d.rank >= world)) throw Fail{NGDB_ERR_CONFIG, "rank out of range"};
-    if (world > 1 && d.semantic_dim > 0)
-      throw Fail{NGDB_ERR_MISSING_KERNEL, "row-sharded step is built without FuseSemantic"};
     c = new ngdb_ctx();
     c->desc = d;
     c->world = world;
@@ -1352,10 +1361,13 @@ int ngdb_param_download(ngdb_ctx* c, const char* name, float* host, int64_t n) {
 int ngdb_semantic_upload(ngdb_ctx* c, const float* host, int64_t n) {
   return guarded([&] {
     if (c->desc.semantic_dim <= 0) throw Fail{NGDB_ERR_CONFIG, "context has no semantic store"};
-    if (n != int64_t(c->desc.n_entities) * c->desc.semantic_dim)
+    // row-sharded: this rank's rows (entity e = rank + world * local row)
+    const int64_t rows = c->world > 1 ? c->params[c->ent_idx].rows : int64_t(c->desc.n_entities);
+    if (n != rows * c->desc.semantic_dim)
       throw Fail{NGDB_ERR_SHAPE_MISMATCH, "semantic store size"};
     if (!c->sem) c->sem = dmalloc<float>(n);
     CK(cudaMemcpy(c->sem, host, n * 4, cudaMemcpyHostToDevice));
+    if (c->world > 1) return;  // the whole-table form is single-GPU only
     // the frozen store's operand splits, once (the fusion GEMMs read them
     // directly when a step touches every entity: no per-step gather / split)
     const int64_t N = c->desc.n_entities, L = c->desc.semantic_dim, NP = (N + 3) / 4 * 4;
@@ -2360,7 +2372,6 @@ struct ShardShape {
 void validate_shard(ngdb_ctx* c, const ngdb_step_plan& plan, const ngdb_shard_plan& sp) {
   if (sp.world != c->world || sp.rank != c->rank)
     throw Fail{NGDB_ERR_CONFIG, "shard plan world/rank do not match the context"};
-  if (c->fused()) throw Fail{NGDB_ERR_MISSING_KERNEL, "sharded FuseSemantic"};
   if (c->beta() && c->desc.dim > 512) throw Fail{NGDB_ERR_MISSING_KERNEL, "sharded BetaE: dim > 512"};
   validate_plan(plan);
   if (plan.n_score_slots > sp.max_slots || plan.n_anchor_slots > sp.max_anchors ||
@@ -2378,8 +2389,9 @@ void validate_shard(ngdb_ctx* c, const ngdb_step_plan& plan, const ngdb_shard_pl
 }
 
 // Exchange buffer sizes of a shard shape (ngdb_shard_buffers order + coef_all,
-// then BetaE's etab, etab_c, cand_local).
-constexpr int kShardBufs = 13;
+// then the step table etab, etab_c, cand_local of BetaE / FuseSemantic, and
+// FuseSemantic's scratch and anchor_local).
+constexpr int kShardBufs = 15;
 void shard_buffer_sizes(const ngdb_ctx* c, const ShardShape& sp, int64_t sizes[kShardBufs]) {
   const int64_t G = sp.world, B = sp.batch, S = sp.max_slots, nc = sp.n_candidates;
   const int64_t ew = c->params[c->ent_idx].cols, wq = c->query_width();
@@ -2388,8 +2400,11 @@ void shard_buffer_sizes(const ngdb_ctx* c, const ShardShape& sp, int64_t sizes[k
   const int64_t blk = S * wq + B;
   const int64_t z[kShardBufs] = {sp.n_send * ew, sp.n_recv * ew, S * wq,     G * S * wq, G * blk,
                                  blk,            sp.n_recv * ew, sp.n_send * ew, n_red, G * S * nc,
-                                 c->beta() ? sp.n_rows * ew : 0, c->beta() ? sp.n_rows : 0,
-                                 c->beta() ? G * S * nc : 0};
+                                 c->step_table() ? sp.n_rows * c->op_ent_w() : 0,
+                                 c->step_table() ? sp.n_rows : 0,
+                                 c->step_table() ? G * S * nc : 0,
+                                 c->fused() ? fuse_scratch_floats(c->desc.dim, c->desc.semantic_dim, sp.n_rows) : 0,
+                                 c->fused() ? int64_t(sp.n_send) : 0};
   for (int k = 0; k < kShardBufs; ++k) sizes[k] = z[k];
 }
 bool shard_buffers_fit(const ngdb_ctx* c, const ShardShape& sp) {
@@ -2431,6 +2446,9 @@ void shard_exchange_buffers(ngdb_ctx* c, const ShardShape& sp) {
   sh.etab = ptr[10];
   sh.etab_c = ptr[11];
   sh.cand_local = reinterpret_cast<int32_t*>(ptr[12]);
+  sh.fscratch = ptr[13];
+  sh.fscratch_cap = sizes[13];
+  sh.anchor_local = reinterpret_cast<int32_t*>(ptr[14]);
 }
 // Make (plan, owner lists in `blob`) the active sharded step: the step
 // prologue on the stream (capturable) and the device views.
@@ -2469,10 +2487,19 @@ void shard_activate(ngdb_ctx* c, ngdb_plan* plan, const ShardShape& sp, const in
   sh.active = true;
   c->anc_pos = blob + L.o_pos;
   c->anc_rows = b.anchor_rows;
-  if (c->beta()) {  // the entity side of every owned KL, once per owned row (beta.cu)
-    const Param& ent = c->params[c->ent_idx];
-    const SparseTable te{ent.w, ent.m, ent.v, nullptr, static_cast<int32_t>(ent.cols),
-                         sh.n_rows, sh.rows, sh.seg, sh.contrib};
+  const Param& ent = c->params[c->ent_idx];
+  const SparseTable te{ent.w, ent.m, ent.v, nullptr, static_cast<int32_t>(ent.cols),
+                       sh.n_rows, sh.rows, sh.seg, sh.contrib};
+  if (c->fused()) {  // fused rows of every owned row (+ BetaE: Psi_theta, the KL table)
+    if (!c->sem) throw Fail{NGDB_ERR_CONFIG, "semantic store not uploaded (ngdb_semantic_upload)"};
+    const DevArgs a = make_args(c, plan);
+    const double u = sp.n_rows, D = c->desc.dim, L = c->desc.semantic_dim;
+    if (c->profiling)
+      c->fam_flops[F_ENTITY_PREP] += 2.0 * D * D * L + 2.0 * u * D * (L + D + (c->beta() ? 2 * D : 0));
+    timed(c, F_ENTITY_PREP, u * (L * 4 + D * 4 * 2), [&] {
+      return fuse_prologue(a, te, sh.fscratch, sh.fscratch_cap, LaunchCtx{c->stream, c->num_sms});
+    });
+  } else if (c->beta()) {  // the entity side of every owned KL, once per owned row (beta.cu)
     const DevArgs a = make_args(c, plan);
     timed(c, F_ENTITY_PREP, sp.n_rows * (2.0 * ent.cols * 4 + 4),
           [&] { return launch_beta_prep(a, te, LaunchCtx{c->stream, c->num_sms}); });
@@ -2672,6 +2699,30 @@ int ngdb_shard_run(ngdb_ctx* c, int32_t stage) {
         });
         break;
       }
+      case NGDB_SHARD_FUSE_BWD: {
+        if (!c->fused()) break;
+        // dL/d(fused row) of the owned rows: returned anchor rows (grad_all,
+        // send order) + owned candidates (every rank's queries and coefs)
+        DevArgs af = a;
+        af.agbuf = b.grad_all;
+        af.qbuf = b.query_all;
+        af.coefbuf = sh.coef_all;
+        const Param& ent = c->params[c->ent_idx];
+        const SparseTable te{ent.w, ent.m, ent.v, c->debug ? ent.g : nullptr,
+                             static_cast<int32_t>(ent.cols), sh.n_rows, sh.rows, sh.seg, sh.contrib};
+        const ngdb_model_desc& md = c->desc;
+        const AdamHyper hp{md.lr, md.beta1, md.beta2, md.eps_adam};
+        const double u = sh.n_rows, D = md.dim, L = md.semantic_dim;
+        if (c->profiling)
+          c->fam_flops[F_OPT_ENTITY] += 2.0 * u * D * (2 * D + L + (c->beta() ? 4 * D : 0)) + 4.0 * D * D * L;
+        timed(c, F_OPT_ENTITY, 4.0 * u * D * 4 + u * L * 4, [&] {
+          return fuse_backward(af, te, sh.fscratch, sh.fscratch_cap, hp, c->d_bc, lc, false);
+        });
+        // the fusion's dense gradients join the all-reduce
+        if (c->dense_n)
+          CK(cudaMemcpyAsync(b.reduce, c->dense_g, c->dense_n * 4, cudaMemcpyDeviceToDevice, c->stream));
+        break;
+      }
       default: throw Fail{NGDB_ERR_CONFIG, "unknown shard stage"};
     }
     CK(cudaGetLastError());
@@ -2699,8 +2750,14 @@ int ngdb_shard_optimizer(ngdb_ctx* c, int64_t step) {
     Param& rel = c->params[c->rel_idx];
     SparseTable te{ent.w, ent.m, ent.v, c->debug ? ent.g : nullptr, static_cast<int32_t>(ent.cols),
                    sh.n_rows, sh.rows, sh.seg, sh.contrib};
-    timed(c, F_OPT_ENTITY, 6.0 * sh.n_rows * ent.cols * 4,
-          [&] { return launch_sparse_adam_entity(a, te, hp, c->d_bc, lc); });
+    if (c->fused())  // Adam on dh (fuse_backward ran in NGDB_SHARD_FUSE_BWD)
+      timed(c, F_OPT_ENTITY, 6.0 * sh.n_rows * ent.cols * 4, [&] {
+        return fuse_entity_adam(te, sh.fscratch, sh.fscratch_cap, c->desc.dim, c->desc.semantic_dim,
+                                c->beta(), hp, c->d_bc, lc);
+      });
+    else
+      timed(c, F_OPT_ENTITY, 6.0 * sh.n_rows * ent.cols * 4,
+            [&] { return launch_sparse_adam_entity(a, te, hp, c->d_bc, lc); });
     timed(c, F_OPT_RELATION, 6.0 * rel.n() * 4, [&] {
       return launch_masked_rows_adam(rel.w, rel.m, rel.v, c->debug ? rel.g : nullptr,
                                      b.reduce + c->dense_n, b.reduce + c->dense_n + rel.n(),
@@ -2781,6 +2838,7 @@ void shard_exec(ngdb_ctx* c, int64_t step) {
   rc_throw(ngdb_shard_run(c, NGDB_SHARD_BACKWARD));
   rc_throw(ngdb_shard_run(c, NGDB_SHARD_GRAD_PACK));
   all_to_all_rows(c, b.grad_send, sh.recv_cnt, b.grad_all, sh.send_cnt, ew);
+  if (c->fused()) rc_throw(ngdb_shard_run(c, NGDB_SHARD_FUSE_BWD));
   nck(n.AllReduce(b.reduce, b.reduce, size_t(b.n_reduce), ncclFloat32, ncclSum, c->comm, c->stream),
       "ncclAllReduce");
   rc_throw(ngdb_shard_optimizer(c, step));

@@ -303,8 +303,17 @@ int fuse_prologue(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
   return launches + 1 + launch_beta_prep(ay, t, lc);
 }
 
+int fuse_entity_adam(const SparseTable& t, float* fs, int64_t cap, int d, int dl, bool beta,
+                     const AdamHyper& hp, const float* bc, const LaunchCtx& lc) {
+  if (t.n_rows <= 0) return 0;
+  const FuseBufs f = carve(fs, cap, t.n_rows, d, dl, beta);
+  launch_pdl(rows_adam_kernel, dim3(row_blocks(t.n_rows)), dim3(kWarps * 32), 0, lc.stream, 1, t,
+             (const float*)f.dX, d, hp, bc);
+  return 1;
+}
+
 int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap, const AdamHyper& hp,
-                  const float* bc, const LaunchCtx& lc) {
+                  const float* bc, const LaunchCtx& lc, bool adam) {
   if (t.n_rows <= 0) return 0;
   const bool beta = a.backbone == NGDB_BETAE;
   const int d = a.dim, dl = a.sem_dim, u = t.n_rows;
@@ -380,9 +389,8 @@ int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
   cj.job[0] = {f.dZ, u, d, g + off[a.fus_idx + 2]};
   cj.n = 1;
   launches += colsums(cj, d, lc.stream);
-  launch_pdl(rows_adam_kernel, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, t,
-             (const float*)f.dX, d, hp, bc);
-  return launches + 1;
+  if (!adam) return launches;
+  return launches + fuse_entity_adam(t, fs, cap, d, dl, beta, hp, bc, lc);
 }
 
 }  // namespace ngdb_dev

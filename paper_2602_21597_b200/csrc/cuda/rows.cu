@@ -46,10 +46,11 @@ __global__ void __launch_bounds__(kWarps * 32) embed_kernel(DevArgs a, int dir, 
     // FuseSemantic: the prologue's fused row of this anchor's entity
     // row-sharded: the row fetched from its owner into this anchor slot
     // (BetaE: Psi_theta's pre-activation row, realised below)
-    const float* src = a.fused      ? (a.ytab ? a.ytab : a.etab) +
-                                          static_cast<int64_t>(a.anchor_local[d.aux]) * a.ent_w
-                       : a.anc_rows ? a.anc_rows + static_cast<int64_t>(a.anc_pos[d.aux]) * a.ent_w
-                                    : a.ent + static_cast<int64_t>(d.id) * a.ent_w;
+    // (FuseSemantic: the owner sent the fused / Psi_theta row)
+    const float* src = a.anc_rows ? a.anc_rows + static_cast<int64_t>(a.anc_pos[d.aux]) * a.ent_w
+                       : a.fused  ? (a.ytab ? a.ytab : a.etab) +
+                                        static_cast<int64_t>(a.anchor_local[d.aux]) * a.ent_w
+                                  : a.ent + static_cast<int64_t>(d.id) * a.ent_w;
     FOR_CHUNKS(ew4) u[i] = ldg4(src + 4 * c);
     if (a.backbone == NGDB_BETAE) {  // realised (alpha | beta); the mirror's
       FOR_CHUNKS(ew4)                // chain rule runs in the optimizer

@@ -23,12 +23,15 @@ constexpr int kScoreThreads = 256;  // owner scoring: 8 warps per unit
 constexpr int kScoreWarps = kScoreThreads / 32;
 
 // lookup send: the owned rows every rank asked for, requester-major
-// (send[p] = local row send_rows[p]); one warp per row
+// (send[p] = local row send_rows[p]; FuseSemantic: the row's fused vector from
+// the step table — BetaE: its Psi_theta row — at CSR row anchor_local[p]);
+// one warp per row
 __global__ void shard_anchor_pack_kernel(DevArgs a, ShardDev sd, float* send) {
   pdl_start();
   const int64_t p = static_cast<int64_t>(blockIdx.x) * 4 + threadIdx.x / 32;
   if (p >= sd.n_send) return;
-  const float* src = a.ent + static_cast<int64_t>(sd.send_rows[p]) * a.ent_w;
+  const float* src = a.fused ? (a.ytab ? a.ytab : a.etab) + static_cast<int64_t>(a.anchor_local[p]) * a.ent_w
+                             : a.ent + static_cast<int64_t>(sd.send_rows[p]) * a.ent_w;
   float* dst = send + p * a.ent_w;
   for (int c = threadIdx.x & 31; c < a.ent_w / 4; c += 32) st4(dst + 4 * c, ld4(src + 4 * c));
 }
@@ -136,7 +139,9 @@ __global__ void __launch_bounds__(kScoreThreads) shard_score_kernel(DevArgs a, S
       row = a.etab + static_cast<int64_t>(r) * a.ent_w;
       cst = __ldg(a.etab_c + r);
     } else {
-      row = a.ent + static_cast<int64_t>(cand[j] / sd.world) * a.ent_w;
+      // FuseSemantic: the owned row's fused vector in the step table
+      row = a.fused ? a.etab + static_cast<int64_t>(__ldg(a.cand_local + static_cast<int64_t>(gslot[0]) * a.ncand + j)) * a.ent_w
+                    : a.ent + static_cast<int64_t>(cand[j] / sd.world) * a.ent_w;
       cst = 0.f;
     }
 #pragma unroll

@@ -63,6 +63,8 @@ ShardLoopStats run_shard_train_loop(ngdb_ctx* ctx, const GraphSplit& graph,
   tc.n_neg = cfg.n_neg;
   tc.b_max = cfg.b_max;
   tc.sharded = true;
+  tc.semantic = d.semantic_dim > 0;
+  tc.semantic_dim = d.semantic_dim;
   const int32_t cap = std::max(cfg.batch, d.max_queries);
   const int64_t stride = shard_meta_stride(cap, cfg.n_neg + 1);
 

@@ -39,7 +39,7 @@ from ._native import SHARD_BUFFERS, ModelDesc, ShardBuffers, ShardPlan, StepPlan
 from .engine import BACKBONES, Batch, PlannedStep, param_specs
 
 FORWARD_STAGES = {"anchor_pack": 0, "forward": 1, "query_pack": 2, "score": 3, "score_done": 4,
-                  "backward": 5, "grad_pack": 6}
+                  "backward": 5, "grad_pack": 6, "fuse_bwd": 7}
 NCCL_ID_BYTES = 128
 
 
@@ -195,10 +195,10 @@ def _build_shard_step(ps: PlannedStep, gathered) -> ShardStep:
 
 
 def plan_shard_step(comm: Comm, batch: Batch, backbone: str, dim: int, b_max: int = 512,
-                    batch_cap: Optional[int] = None) -> ShardStep:
+                    batch_cap: Optional[int] = None, semantic: bool = False) -> ShardStep:
     """Plan this rank's batch, exchange the packed metadata, build the owner lists.
     batch_cap (the record's query capacity) must be the same on every rank."""
-    ps = PlannedStep(batch, backbone, dim, b_max, sharded=True)
+    ps = PlannedStep(batch, backbone, dim, b_max, semantic=semantic, sharded=True)
     cap = batch_cap or ps.view().n_queries
     return _build_shard_step(ps, _gather_meta(comm, _local_meta(ps, cap)))
 
@@ -209,7 +209,10 @@ class ShardedEngine:
     def __init__(self, comm: Comm, backbone: str, n_entities: int, n_relations: int,
                  dim: int = 400, n_neg: int = 128, b_max: int = 512, max_queries: int = 512,
                  gamma: float = 12.0, lr: float = 1e-4, alpha_box: float = 0.02,
-                 device: int = 0, seed: int = 2, debug: bool = False):
+                 device: int = 0, seed: int = 2, debug: bool = False,
+                 semantic: Optional[np.ndarray] = None):
+        """semantic: the frozen store [n_entities][d_l] (FuseSemantic); this rank
+        uploads its own rows (entity e = rank + world * local row)."""
         import torch
         if backbone not in ("gqe", "q2b", "betae"):
             raise NotImplementedError(f"row-sharded step: {backbone}")
@@ -218,7 +221,9 @@ class ShardedEngine:
         self.max_queries = max_queries
         self.n_entities, self.n_relations = n_entities, n_relations
         G, r = comm.world, comm.rank
-        d = ModelDesc(BACKBONES[backbone], n_entities, n_relations, dim, n_neg, 0, gamma,
+        sd = 0 if semantic is None else int(semantic.shape[1])
+        self.semantic_dim = sd
+        d = ModelDesc(BACKBONES[backbone], n_entities, n_relations, dim, n_neg, sd, gamma,
                       alpha_box, lr, 0.9, 0.999, 1e-8, b_max, max_queries, G, r)
         self._h = C.c_void_p()
         check(lib.ngdb_ctx_create(C.byref(d), device, C.byref(self._h)))
@@ -235,15 +240,23 @@ class ShardedEngine:
             uid = (C.c_uint8 * NCCL_ID_BYTES).from_buffer_copy(got)
             check(lib.ngdb_comm_init(self._h, uid))
         self.n_local = (n_entities - r + G - 1) // G
-        for name, rows, cols, _ in param_specs(backbone, n_entities, n_relations, dim):
-            if name == "entity":
+        if semantic is not None:
+            st = np.ascontiguousarray(semantic[r::G], dtype=np.float32)
+            check(lib.ngdb_semantic_upload(self._h, _p(st, C.c_float), st.size))
+        for name, rows, cols, _ in param_specs(backbone, n_entities, n_relations, dim, sd):
+            if name == "entity" and sd:  # (the fused BetaE entity row is d wide)
+                full = np.zeros((rows, cols), np.float32)
+                check(lib.ngdb_param_init_ex(BACKBONES[backbone], n_entities, n_relations, dim, sd,
+                                             name.encode(), seed, _p(full, C.c_float), full.size))
+                a = np.ascontiguousarray(full[r::G])
+            elif name == "entity":
                 a = np.zeros((self.n_local, cols), np.float32)
                 check(lib.ngdb_param_init_shard(BACKBONES[backbone], n_entities, n_relations, dim,
                                                 name.encode(), seed, G, r, _p(a, C.c_float),
                                                 a.size))
             else:  # replicated tensors: identical deterministic init on every rank
                 a = np.zeros((rows, cols), np.float32)
-                check(lib.ngdb_param_init_ex(BACKBONES[backbone], n_entities, n_relations, dim, 0,
+                check(lib.ngdb_param_init_ex(BACKBONES[backbone], n_entities, n_relations, dim, sd,
                                              name.encode(), seed, _p(a, C.c_float), a.size))
             self.upload(name, a)
         if debug:
@@ -257,7 +270,7 @@ class ShardedEngine:
     def download(self, name: str) -> np.ndarray:
         base = name.split(":")[-1]
         spec = {s[0]: s for s in param_specs(self.backbone, self.n_entities, self.n_relations,
-                                             self.dim)}[base]
+                                             self.dim, self.semantic_dim)}[base]
         rows = self.n_local if base == "entity" else spec[1]
         out = np.zeros((rows, spec[2]), dtype=np.float32)
         check(lib.ngdb_param_download(self._h, name.encode(), _p(out, C.c_float), out.size))
@@ -265,7 +278,7 @@ class ShardedEngine:
 
     def plan(self, batch: Batch) -> ShardStep:
         return plan_shard_step(self.comm, batch, self.backbone, self.dim, self.b_max,
-                               self.max_queries)
+                               self.max_queries, semantic=self.semantic_dim > 0)
 
     def _enqueue(self, step: ShardStep, step_no: int) -> None:
         """begin + stages + collectives + optimizer of one step, enqueued."""
@@ -319,7 +332,8 @@ class ShardedEngine:
 
         def prep(s):
             b = Batch.sample(graph, weights, batch, n_neg, seed=3, tag=tag_of(s))
-            ps = PlannedStep(b, self.backbone, self.dim, self.b_max, sharded=True)
+            ps = PlannedStep(b, self.backbone, self.dim, self.b_max,
+                             semantic=self.semantic_dim > 0, sharded=True)
             return ps, _local_meta(ps, cap)
 
         sums = np.zeros(n_steps, np.float64)
@@ -447,7 +461,7 @@ def _host_stages(eng: ShardedEngine, b: ShardBuffers, send_cnt, recv_cnt) -> Non
     t = {n: _device_view(eng.torch, getattr(b, n), getattr(b, "n_" + n)) for n in SHARD_BUFFERS}
     run = lambda stage: check(lib.ngdb_shard_run(eng._h, FORWARD_STAGES[stage]))  # noqa: E731
     comm = eng.comm
-    ew = 2 * eng.dim if eng.backbone == "betae" else eng.dim  # entity row width
+    ew = 2 * eng.dim if eng.backbone == "betae" else eng.dim  # operator entity row width
     run("anchor_pack")
     comm.all_to_all_v(t["anchor_rows"], t["anchor_send"], send_cnt * ew, recv_cnt * ew)
     run("forward")
@@ -459,6 +473,8 @@ def _host_stages(eng: ShardedEngine, b: ShardBuffers, send_cnt, recv_cnt) -> Non
     run("backward")
     run("grad_pack")
     comm.all_to_all_v(t["grad_all"], t["grad_send"], recv_cnt * ew, send_cnt * ew)
+    if eng.semantic_dim:
+        run("fuse_bwd")
     comm.all_reduce(t["reduce"])
 
 

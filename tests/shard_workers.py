@@ -69,8 +69,9 @@ def host_plan_worker(rank, world, port, out_dir, shape, mix, b, k, dim):
     dist.destroy_process_group()
 
 
-def gpu_step_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
-    """Two ranks sharing GPU 0: the row-sharded step through ngdb_shard_*."""
+def gpu_step_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone, sdim=0):
+    """Two ranks sharing GPU 0: the row-sharded step through ngdb_shard_*
+    (sdim > 0: FuseSemantic over the synthetic store of that width)."""
     dist = _init(rank, world, port)
     import numpy as np
 
@@ -80,14 +81,15 @@ def gpu_step_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, ba
     comm = Comm()
     g = m.Graph.synthetic(shape, 1)
     info = g.info()
+    store = m.semantic_store(info["n_entities"], sdim, seed=5) if sdim else None
     eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim, n_neg=k,
-                        max_queries=b, device=0, debug=True)
+                        max_queries=b, device=0, debug=True, semantic=store)
     w = m.pattern_weights(mix)
     res = {"loss": [], "batches": []}
     for step in range(1, steps + 1):
         batch = m.Batch.from_arrays(_load_batch(out_dir, step, rank))
         res["loss"].append(eng.train_step(batch))
-    specs = m.param_specs(backbone, info["n_entities"], info["n_relations"], dim)
+    specs = m.param_specs(backbone, info["n_entities"], info["n_relations"], dim, sdim)
     res["params"] = {n: eng.download(n) for n, *_ in specs}
     res["grads"] = {n: eng.download("g:" + n) for n, *_ in specs}
     with open(os.path.join(out_dir, f"gpu{rank}.pkl"), "wb") as f:

@@ -24,11 +24,13 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("backbone,dim,b,k,steps", [("q2b", 32, 64, 16, 1), ("gqe", 16, 48, 8, 2),
-                                                      ("q2b", 400, 128, 32, 2),
-                                                      ("betae", 16, 64, 16, 2),
-                                                      ("betae", 400, 64, 32, 1)])
-def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone, dim, b, k, steps):
+@pytest.mark.parametrize("backbone,dim,b,k,steps,sdim", [
+    ("q2b", 32, 64, 16, 1, 0), ("gqe", 16, 48, 8, 2, 0), ("q2b", 400, 128, 32, 2, 0),
+    ("betae", 16, 64, 16, 2, 0), ("betae", 400, 64, 32, 1, 0),
+    # FuseSemantic: store rows sharded with the entity rows, fused rows exchanged
+    ("gqe", 16, 64, 16, 2, 24), ("q2b", 400, 64, 32, 1, 768), ("betae", 16, 48, 16, 2, 24)])
+def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone, dim, b, k, steps,
+                                                 sdim):
     import torch.multiprocessing as mp
 
     import oracle as O
@@ -37,7 +39,10 @@ def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone
     info = small_graph.info()
     ne, nr = info["n_entities"], info["n_relations"]
     w = m.pattern_weights(ALL)
+    store = m.semantic_store(ne, sdim, seed=5) if sdim else None
     om = O.OracleModel(backbone, ne, nr, dim, k, precision=64)
+    if sdim:
+        om.set_semantic(store)
     om.init(2)
     batches = []
     for step in range(1, steps + 1):
@@ -46,6 +51,8 @@ def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone
             bt = m.Batch.sample(small_graph, w, b, k, seed=3, tag=step * G + r)
             if step == 1:  # certify kink-free queries at the initial parameters
                 probe = O.OracleModel(backbone, ne, nr, dim, k, precision=64)
+                if sdim:
+                    probe.set_semantic(store)
                 probe.init(2)
                 bt, _ = tie_free(bt, probe, 512, 1)
             arr = bt.arrays()
@@ -54,7 +61,7 @@ def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone
                 pickle.dump(arr, f)
         batches.append(per_rank)
     mp.spawn(shard_workers.gpu_step_worker,
-             args=(G, _port(), str(tmp_path), "small", ALL, b, k, dim, steps, backbone),
+             args=(G, _port(), str(tmp_path), "small", ALL, b, k, dim, steps, backbone, sdim),
              nprocs=G, join=True)
     outs = [pickle.load(open(tmp_path / f"gpu{r}.pkl", "rb")) for r in range(G)]
 
@@ -63,7 +70,7 @@ def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone
         refs = om.step_multi(batches[step - 1], step=step)
         for r in range(G):
             res["loss"].append((outs[r]["loss"][step - 1], refs[r]))
-    specs = m.param_specs(backbone, ne, nr, dim)
+    specs = m.param_specs(backbone, ne, nr, dim, sdim)
     for name, rows, cols, sparse in specs:
         def full(key):
             if name != "entity":
