@@ -346,6 +346,9 @@ int oracle_model_step_multi(void* mp, int32_t n, const int32_t* sizes, const int
         const int32_t b = sizes[t];
         ODag d = o_build_training_dag(queries_of(b, patterns + off, anchors + 3 * off,
                                                  relations + 4 * off));
+        if (md.dl)  // FuseSemantic replaces EmbedAnchor
+          for (auto& nd : d.nodes)
+            if (nd.kind == K_EMB) nd.kind = K_FUSE;
         std::vector<int> cand((size_t)b * (md.k + 1));
         for (int i = 0; i < b; ++i) {
           cand[(size_t)i * (md.k + 1)] = positives[off + i];

@@ -2394,7 +2394,7 @@ void validate_shard(ngdb_ctx* c, const ngdb_step_plan& plan, const ngdb_shard_pl
 constexpr int kShardBufs = 15;
 void shard_buffer_sizes(const ngdb_ctx* c, const ShardShape& sp, int64_t sizes[kShardBufs]) {
   const int64_t G = sp.world, B = sp.batch, S = sp.max_slots, nc = sp.n_candidates;
-  const int64_t ew = c->params[c->ent_idx].cols, wq = c->query_width();
+  const int64_t ew = c->op_ent_w(), wq = c->query_width();
   const Param& rel = c->params[c->rel_idx];
   const int64_t n_red = c->dense_n + rel.n() + rel.rows;
   const int64_t blk = S * wq + B;
@@ -2823,7 +2823,7 @@ void shard_exec(ngdb_ctx* c, int64_t step) {
   if (!sh.active) throw Fail{NGDB_ERR_CONFIG, "ngdb_shard_step_exec outside a sharded step"};
   const NcclApi& n = nccl_api();
   const ngdb_shard_buffers b = sh.bufs;
-  const int64_t ew = c->params[c->ent_idx].cols;
+  const int64_t ew = c->op_ent_w();  // rows exchanged at the operators' width
   const int64_t blk = sh.dev.dq_block;
   rc_throw(ngdb_shard_run(c, NGDB_SHARD_ANCHOR_PACK));
   all_to_all_rows(c, b.anchor_send, sh.send_cnt, b.anchor_rows, sh.recv_cnt, ew);

@@ -103,7 +103,8 @@ def _load_batch(out_dir, step, rank):
         return pickle.load(f)
 
 
-def graph_replay_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
+def graph_replay_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone,
+                        sdim=0):
     """One NCCL rank on GPU 0: the same steps run eagerly on one engine and as
     captured CUDA graphs (stages + collectives) replayed on another."""
     import torch
@@ -120,11 +121,12 @@ def graph_replay_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps
     info = g.info()
     w = m.pattern_weights(mix)
     batches = [m.Batch.sample(g, w, b, k, seed=3, tag=s * world + rank) for s in range(steps + 1)]
-    plans = [plan_shard_step(comm, bt, backbone, dim) for bt in batches]
+    plans = [plan_shard_step(comm, bt, backbone, dim, semantic=sdim > 0) for bt in batches]
+    store = m.semantic_store(info["n_entities"], sdim, seed=5) if sdim else None
     out = {}
     for mode in ("eager", "graph"):
         eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
-                            n_neg=k, max_queries=b)
+                            n_neg=k, max_queries=b, semantic=store)
         eng.run(plans[0], 1)  # communicator warm-up (eager)
         if mode == "eager":
             for s in range(1, steps + 1):
@@ -135,7 +137,7 @@ def graph_replay_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps
                 graphs[s - 1].replay(s + 1)
         torch.cuda.synchronize()
         out[mode] = {n: eng.download(n) for n, *_ in m.param_specs(backbone, info["n_entities"],
-                                                                  info["n_relations"], dim)}
+                                                                  info["n_relations"], dim, sdim)}
     with open(os.path.join(out_dir, f"graph{rank}.pkl"), "wb") as f:
         pickle.dump(out, f)
     dist.destroy_process_group()
@@ -192,7 +194,7 @@ def train_loop_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, 
     dist.destroy_process_group()
 
 
-def transport_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
+def transport_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone, sdim=0):
     """One rank on GPU 0: the same steps through the context's NCCL transport
     (ngdb_shard_step_exec: uneven all-to-alls, all-gather, reduce-scatter,
     all-reduce inside libngdb) and through the host-staged transport."""
@@ -204,11 +206,12 @@ def transport_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, b
     g = m.Graph.synthetic(shape, 1)
     info = g.info()
     w = m.pattern_weights(mix)
+    store = m.semantic_store(info["n_entities"], sdim, seed=5) if sdim else None
     out = {}
     for transport in ("host", "nccl"):
         comm = Comm(transport=transport)
         eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
-                            n_neg=k, max_queries=b)
+                            n_neg=k, max_queries=b, semantic=store)
         losses = []
         for s in range(steps):
             batch = m.Batch.sample(g, w, b, k, seed=3, tag=(s + 1) * world + rank)
@@ -216,7 +219,7 @@ def transport_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, b
         torch.cuda.synchronize()
         out[transport] = {"loss": losses,
                           "params": {n: eng.download(n) for n, *_ in m.param_specs(
-                              backbone, info["n_entities"], info["n_relations"], dim)}}
+                              backbone, info["n_entities"], info["n_relations"], dim, sdim)}}
         del eng
     with open(os.path.join(out_dir, f"transport{rank}.pkl"), "wb") as f:
         pickle.dump(out, f)

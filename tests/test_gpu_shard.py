@@ -86,8 +86,9 @@ def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone
     check_all(res, allow_frac=0.0, steps=steps)
 
 
-@pytest.mark.parametrize("backbone,dim", [("q2b", 32), ("gqe", 16), ("betae", 32)])
-def test_sharded_graph_replay_matches_eager(tmp_path, backbone, dim):
+@pytest.mark.parametrize("backbone,dim,sdim", [("q2b", 32, 0), ("gqe", 16, 0), ("betae", 32, 0),
+                                              ("gqe", 32, 24), ("betae", 16, 24)])
+def test_sharded_graph_replay_matches_eager(tmp_path, backbone, dim, sdim):
     # the resident sharded step (stages + NCCL collectives captured in one CUDA
     # graph, bench.py --config c5) updates the parameters bit-identically to the
     # eager stage-by-stage run
@@ -95,7 +96,7 @@ def test_sharded_graph_replay_matches_eager(tmp_path, backbone, dim):
 
     import shard_workers
     mp.spawn(shard_workers.graph_replay_worker,
-             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, dim, 3, backbone),
+             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, dim, 3, backbone, sdim),
              nprocs=1, join=True)
     out = pickle.load(open(tmp_path / "graph0.pkl", "rb"))
     for name, v in out["eager"].items():
@@ -119,15 +120,16 @@ def test_sharded_train_loop_matches_steps(tmp_path):
     np.testing.assert_allclose(out["native_sums"], out["seq_sums"], rtol=1e-12)
 
 
-@pytest.mark.parametrize("backbone,dim", [("q2b", 400), ("gqe", 32), ("betae", 32)])
-def test_nccl_transport_matches_host_transport(tmp_path, backbone, dim):
+@pytest.mark.parametrize("backbone,dim,sdim", [("q2b", 400, 0), ("gqe", 32, 0), ("betae", 32, 0),
+                                              ("q2b", 32, 24)])
+def test_nccl_transport_matches_host_transport(tmp_path, backbone, dim, sdim):
     # the libngdb NCCL path (ngdb_shard_step_exec) and the host-staged path run
     # the same stages over the same exchange layouts: bit-identical results
     import torch.multiprocessing as mp
 
     import shard_workers
     mp.spawn(shard_workers.transport_worker,
-             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, dim, 3, backbone),
+             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, dim, 3, backbone, sdim),
              nprocs=1, join=True)
     out = pickle.load(open(tmp_path / "transport0.pkl", "rb"))
     for a, b in zip(out["host"]["loss"], out["nccl"]["loss"]):
