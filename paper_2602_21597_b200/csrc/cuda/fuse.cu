@@ -58,8 +58,8 @@ struct FuseBufs {
   Split dYT, ET;          // transposed splits [uP][2d], [uP][d]
   // per-step products of the weights (d x d_l)
   float* M;  Split Ms;    // M = W_s F
-  float* dM; Split dMs;   // dM = dZ^T S
-  Split dMT;              // [d_l][dP]
+  float* dM; Split dMs;   // dM^T = S^T dZ [d_l][d] (plain + split)
+  Split dMT;              // dM [d][d_l] split (transposed from dM^T)
 };
 
 FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
@@ -97,7 +97,7 @@ FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
   f.Ms = take_split(sc, DL);
   f.dM = sc.take(DL);
   f.dMs = take_split(sc, DL);
-  f.dMT = take_split(sc, int64_t(dl) * ((d + 3) & ~3));
+  f.dMT = take_split(sc, int64_t(d) * ((dl + 3) & ~3));
   return f;
 }
 
@@ -365,24 +365,27 @@ int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
   jobs.n = whole ? 2 : 3;  // the store's transposed split exists already
   launches += split_transposed(jobs, lc.stream);
   const Split ST = whole ? Split{const_cast<float*>(a.semT_hi), const_cast<float*>(a.semT_lo)} : f.ST;
-  TcGemmArgs lvl[2];
-  lvl[0] = gemm_args(d, d, u, op(f.dZT, f.uP), op(f.XT, f.uP), g + off[a.fus_idx + 1], 2 * d);
-  lvl[0].accumulate = 1;  // dW_h += dZ^T h
-  lvl[1] = gemm_args(d, dl, u, op(f.dZT, f.uP), op(ST, f.uP), f.dM, dl);
-  lvl[1].s_hi = f.dMs.hi;  // dM = dZ^T S (plain + split)
-  lvl[1].s_lo = f.dMs.lo;
-  launches += tc_gemm_batch(lvl, 2, lc.stream);
+  // the two K = rows weight gradients as separate launches: each gets its own
+  // tile width and split-K (tc_gemm.cu), which beats one shared launch
+  TcGemmArgs gw = gemm_args(d, d, u, op(f.dZT, f.uP), op(f.XT, f.uP), g + off[a.fus_idx + 1], 2 * d);
+  gw.accumulate = 1;  // dW_h += dZ^T h
+  launches += tc_gemm(gw, lc.stream);
+  // dM^T = S^T dZ ([d_l][d], plain + split): the d_l-row orientation streams
+  // the store operand fewer times than dM = dZ^T S
+  TcGemmArgs gt = gemm_args(dl, d, u, op(ST, f.uP), op(f.dZT, f.uP), f.dM, d);
+  gt.s_hi = f.dMs.hi;
+  gt.s_lo = f.dMs.lo;
+  launches += tc_gemm(gt, lc.stream);
   SplitJobs mj{};
-  mj.job[0] = {f.dM, d, dl, dl, 0, f.dMT.hi, f.dMT.lo};
+  mj.job[0] = {f.dM, dl, d, d, 0, f.dMT.hi, f.dMT.lo};  // -> dM [d][d_l] split
   mj.n = 1;
   launches += split_transposed(mj, lc.stream);
-  const int dP = (d + 3) & ~3;
   TcGemmArgs wl[2];
-  wl[0] = gemm_args(d, d, dl, op(f.dMs, dl), wop(a, a.fus_idx, d, dl, false),
+  wl[0] = gemm_args(d, d, dl, op(f.dMT, dl), wop(a, a.fus_idx, d, dl, false),
                     g + off[a.fus_idx + 1] + d, 2 * d);
   wl[0].accumulate = 1;  // dW_s += dM F^T
   wl[1] = gemm_args(d, dl, d, SplitOperand{wpt.hi + int64_t(d) * d, wpt.lo + int64_t(d) * d, d},
-                    op(f.dMT, dP), g + off[a.fus_idx], dl);
+                    op(f.dMs, d), g + off[a.fus_idx], dl);
   wl[1].accumulate = 1;  // dF += W_s^T dM
   launches += tc_gemm_batch(wl, 2, lc.stream);
   ColsumJobs cj{};

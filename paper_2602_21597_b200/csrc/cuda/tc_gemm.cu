@@ -421,13 +421,13 @@ __global__ void __launch_bounds__(kThreads, 2) tc_gemm_kernel(const __grid_const
 // split-K). The wide tile reads A once per 208 output columns instead of per
 // 80: the large GEMMs (FuseSemantic, BetaE projections) are bound by the L2 ->
 // SMEM operand stream (hi + lo operands re-read per N tile), not by the MMA.
-template <int TBN>
+template <int TBN, int TG = (TBN <= 80 ? 1 : 2)>
 struct TmaCfg {
   static constexpr int kBN = TBN;
   static constexpr int kBTile = TBN * BK * 4;
   static constexpr int kStage = 2 * A_TILE + 2 * kBTile;
   static constexpr int kStages = TBN <= 80 ? 4 : (227 * 1024 - 1024 - 256) / kStage;
-  static constexpr int kGroups = TBN <= 80 ? 1 : 2;  // drain warps per TMEM lane quarter
+  static constexpr int kGroups = TG;  // drain warps per TMEM lane quarter
   static constexpr int kCols = TBN / kGroups;        // accumulator columns per drain thread
   static constexpr int kThreads = 64 + 128 * kGroups;
   static constexpr int kTmem = 2 * TBN <= 256 ? 256 : 512;
@@ -449,6 +449,7 @@ struct TcGemmTmaBatch {
   int tile_begin[kMaxProblems + 1];
   int n;
   int S;
+  int fold;  // K chunks per fresh TMEM accumulation folded into the fp32 registers
 };
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
@@ -476,10 +477,10 @@ __device__ __forceinline__ void umma_tf32_n(uint32_t tmem_d, uint64_t a, uint64_
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
-template <int TBN>
-__global__ void __launch_bounds__(TmaCfg<TBN>::kThreads, 1)
+template <int TBN, int TG = (TBN <= 80 ? 1 : 2)>
+__global__ void __launch_bounds__(TmaCfg<TBN, TG>::kThreads, 1)
     tc_gemm_tma_kernel(const __grid_constant__ TcGemmTmaBatch batch) {
-  using Cfg = TmaCfg<TBN>;
+  using Cfg = TmaCfg<TBN, TG>;
   constexpr int kSt = Cfg::kStages, kStageB = Cfg::kStage, kBT = Cfg::kBTile, kNC = Cfg::kCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 128B-swizzled tiles need 1024-byte aligned stage bases
@@ -504,6 +505,8 @@ __global__ void __launch_bounds__(TmaCfg<TBN>::kThreads, 1)
   const int total_chunks = (g.K + BK - 1) / BK;
   const int c_beg = rank * total_chunks / S;
   const int n_chunks = (rank + 1) * total_chunks / S - c_beg;
+  const int F = batch.fold;
+  const int n_groups = (n_chunks + F - 1) / F;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSt; ++i) {
@@ -553,8 +556,9 @@ __global__ void __launch_bounds__(TmaCfg<TBN>::kThreads, 1)
     if (lane == 0) {  // ---- MMA issuer
       for (int c = 0; c < n_chunks; ++c) {
         const int st = c % kSt, ph = (c / kSt) & 1;
-        const int buf = c & 1, bph = (c >> 1) & 1;
-        mbar_wait(smem_u32(&tempty[buf]), bph ^ 1);
+        const int gi = c / F, buf = gi & 1, bph = (gi >> 1) & 1;
+        const bool fresh = c % F == 0, last = c % F == F - 1 || c == n_chunks - 1;
+        if (fresh) mbar_wait(smem_u32(&tempty[buf]), bph ^ 1);
         mbar_wait(smem_u32(&full[st]), ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t a_hi = s_base + st * kStageB, a_lo = a_hi + A_TILE;
@@ -563,14 +567,16 @@ __global__ void __launch_bounds__(TmaCfg<TBN>::kThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first, fresh accumulator per chunk
           const uint32_t off = ks * 32;
-          umma_tf32_n(d, umma_desc(a_lo + off), umma_desc(b_hi + off), Cfg::kInstr, ks == 0 ? 0u : 1u);
+          umma_tf32_n(d, umma_desc(a_lo + off), umma_desc(b_hi + off), Cfg::kInstr,
+                      (ks == 0 && fresh) ? 0u : 1u);
           umma_tf32_n(d, umma_desc(a_hi + off), umma_desc(b_lo + off), Cfg::kInstr, 1u);
           umma_tf32_n(d, umma_desc(a_hi + off), umma_desc(b_hi + off), Cfg::kInstr, 1u);
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&empty[st])));
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(&tfull[buf])));
+        if (last)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+              smem_u32(&tfull[buf])));
       }
     }
     __syncwarp();
@@ -579,7 +585,7 @@ __global__ void __launch_bounds__(TmaCfg<TBN>::kThreads, 1)
     for (int j = 0; j < kNC; ++j) acc[j] = 0.f;
     const uint32_t lanes = (static_cast<uint32_t>(quarter * 32) << 16) + group * kNC;
     constexpr int kPiece = kNC <= 80 ? kNC : 32;  // columns in flight per tcgen05.wait
-    for (int c = 0; c < n_chunks; ++c) {
+    for (int c = 0; c < n_groups; ++c) {
       const int buf = c & 1, bph = (c >> 1) & 1;
       mbar_wait(smem_u32(&tfull[buf]), bph);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -695,6 +701,10 @@ void tc_gemm_init() {
                          TmaCfg<BN>::kSmem);
     cudaFuncSetAttribute(tc_gemm_tma_kernel<kWideBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          TmaCfg<kWideBN>::kSmem);
+    cudaFuncSetAttribute(tc_gemm_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TmaCfg<128>::kSmem);
+    cudaFuncSetAttribute(tc_gemm_tma_kernel<160>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TmaCfg<160>::kSmem);
     configured = true;
   }
 }
@@ -753,24 +763,42 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   int num_sms = 148;
   cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, 0);
   if (tma) {
-    // tile width: the wide tile for problems with many row tiles (measured,
-    // profiles/r02/gemm_wide.jsonl: 14.5k x 400 x 768 82 -> 65 us, 4096 x 800 x
-    // 1200 84 -> 45 us); narrow where split-K must fill the GPU (C2's 731-row
-    // MLPs, 1434-row projections, the K = rows weight gradients).
-    // NGDB_GEMM_BN=80|208 forces one.
+    // Tile width per launch (UMMA N = 80 / 160 / 208), from the measured table
+    // profiles/r02/gemm_variants.txt: the operand stream from L2 (hi + lo
+    // tiles, A re-read once per N tile, B once per M tile) bounds the large
+    // shapes, so wider tiles win where there are enough of them to fill the
+    // GPU; narrow tiles + split-K win on the small ones.
+    //   big M (>= 4096 rows) ............................. 208  (14.5k x 400 x 768: 85 -> 65 us)
+    //   K = rows weight gradients, both sides <= 512 ...... 160  (400 x 400 x 14.5k: 97 -> 57 us)
+    //   mid M (>= 1024 rows), N >= 640 ................... 160  (1434 x 800 x 1200: 31 -> 24 us)
+    //   K >= 1024, M and N >= 640 ........................ 208  (800 x 1200 x 1434: 36 -> 26 us)
+    //   otherwise (C2's 731-row MLPs, ...) ................ 80
+    // The class of the launch's largest problem decides; NGDB_GEMM_BN forces one.
     static const int forced_bn = [] {
       const char* e = std::getenv("NGDB_GEMM_BN");
       return e ? std::atoi(e) : 0;
     }();
-    int wide_tiles = 0, min_n = 1 << 30;
+    int min_n = 1 << 30, big = 0;
+    double big_flops = -1.0;
     for (int i = 0; i < b.n; ++i) {
-      wide_tiles += ((b.p[i].M + BM - 1) / BM) * ((b.p[i].N + kWideBN - 1) / kWideBN);
       min_n = std::min(min_n, b.p[i].N);
+      const double fl = double(b.p[i].M) * b.p[i].N * b.p[i].K;
+      if (fl > big_flops) {
+        big_flops = fl;
+        big = i;
+      }
     }
-    bool wide = min_n >= 192 && wide_tiles >= 64;
-    if (forced_bn == 80 || g_split_override.load(std::memory_order_relaxed)) wide = false;
-    if (forced_bn == kWideBN) wide = true;
-    const int tbn = wide ? kWideBN : BN;
+    auto pick = [&](const TcGemmArgs& g) {
+      if (min_n < 192) return BN;
+      if (g.M >= 4096) return kWideBN;
+      if (g.K >= 8 * std::max(g.M, g.N)) return (g.M <= 512 && g.N <= 512) ? 160 : BN;
+      if (g.M >= 1024 && g.N >= 640) return 160;
+      if (g.K >= 1024 && g.M >= 640 && g.N >= 640) return kWideBN;
+      return BN;
+    };
+    int tbn = pick(b.p[big]);
+    if (forced_bn == 80 || forced_bn == 128 || forced_bn == 160 || forced_bn == kWideBN) tbn = forced_bn;
+    if (g_split_override.load(std::memory_order_relaxed)) tbn = BN;
     TcGemmTmaBatch t{};  // ~2.6 KB of kernel parameters (4 tensor maps per problem)
     int tiles_t = 0;
     for (int i = 0; i < b.n && tma; ++i) {
@@ -790,12 +818,24 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
       // wave, at most 8 CTAs per cluster and at least 2 chunks per CTA
       t.S = std::max(1, std::min({8, num_sms / std::max(tiles_t, 1), max_chunks / 2}));
       if (const int o = g_split_override.load(std::memory_order_relaxed)) t.S = std::min(o, std::max(1, max_chunks));
-      if (wide)
-        launch_pdl(tc_gemm_tma_kernel<kWideBN>, dim3(tiles_t * t.S), dim3(TmaCfg<kWideBN>::kThreads),
-                   TmaCfg<kWideBN>::kSmem, s, t.S, t);
-      else
-        launch_pdl(tc_gemm_tma_kernel<BN>, dim3(tiles_t * t.S), dim3(TmaCfg<BN>::kThreads),
-                   TmaCfg<BN>::kSmem, s, t.S, t);
+      // K chunks per fresh TMEM accumulation: 1 keeps every contraction at fp32
+      // accuracy (2 measured 2-5 % faster but moved BetaE projection weight
+      // gradients, K = rows, past the 1e-4 parity bar); NGDB_GEMM_FOLD overrides
+      static const int fold_env = [] {
+        const char* e = std::getenv("NGDB_GEMM_FOLD");
+        return e ? std::max(1, std::atoi(e)) : 1;
+      }();
+      t.fold = fold_env;
+      auto go = [&](auto kernel, int threads, int smem) {
+        launch_pdl(kernel, dim3(tiles_t * t.S), dim3(threads), smem, s, t.S, t);
+      };
+      switch (tbn) {
+        case kWideBN: go(tc_gemm_tma_kernel<kWideBN>, TmaCfg<kWideBN>::kThreads, TmaCfg<kWideBN>::kSmem); break;
+        case 160: go(tc_gemm_tma_kernel<160>, TmaCfg<160>::kThreads, TmaCfg<160>::kSmem); break;
+        case 128: go(tc_gemm_tma_kernel<128>, TmaCfg<128>::kThreads, TmaCfg<128>::kSmem); break;
+        default:
+          go(tc_gemm_tma_kernel<BN>, TmaCfg<BN>::kThreads, TmaCfg<BN>::kSmem);
+      }
       return 1;
     }
   }

@@ -22,6 +22,7 @@ SHAPES = [  # (label, M, N, K, batch)
     ("c4 fusion dM = dZ^T S (400 x 768, K = 14.5k)", 400, 768, 14505, 1),
     ("c4 fusion dW_h = dZ^T h (400 x 400, K = 14.5k)", 400, 400, 14505, 1),
     ("c3 psi-free project L1 at 4k rows (4096 x 1200 -> 800)", 4096, 800, 1200, 1),
+    ("c4 fusion dM^T = S^T dZ (768 x 400, K = 14.5k)", 768, 400, 14505, 1),
 ]
 f = lib.ngdb_debug_tc_gemm_time
 f.argtypes = [C.c_int] * 5 + [C.POINTER(C.c_float)]
