@@ -1583,6 +1583,7 @@ int ngdb_step_launch(ngdb_ctx* c, int64_t step, int32_t use_graph) {
       // streaming steps keep the serial chain: re-capturing and updating the
       // DAG-shaped graph every step costs the consumer thread more host time
       // (C2: 0.18 -> 0.25 ms/step) than the concurrency saves on the device
+      // (steady-state e2e measured 1.21 M serial vs 1.14-1.19 M concurrent)
       exec_pools(c, p, p->meta.pools);
       optimizer(c, p);
     };

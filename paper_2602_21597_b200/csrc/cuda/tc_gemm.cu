@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -826,6 +827,12 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
         return e ? std::max(1, std::atoi(e)) : 1;
       }();
       t.fold = fold_env;
+      static const bool log_shapes = std::getenv("NGDB_GEMM_LOG") != nullptr;
+      if (log_shapes) {  // one line per launch (diagnostics)
+        std::fprintf(stderr, "gemm bn=%d S=%d tiles=%d", tbn, t.S, tiles_t);
+        for (int i = 0; i < b.n; ++i) std::fprintf(stderr, " [%dx%dx%d]", b.p[i].M, b.p[i].N, b.p[i].K);
+        std::fprintf(stderr, "\n");
+      }
       auto go = [&](auto kernel, int threads, int smem) {
         launch_pdl(kernel, dim3(tiles_t * t.S), dim3(threads), smem, s, t.S, t);
       };

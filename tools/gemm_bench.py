@@ -24,9 +24,12 @@ SHAPES = [  # (label, M, N, K, batch)
     ("c3 psi-free project L1 at 4k rows (4096 x 1200 -> 800)", 4096, 800, 1200, 1),
     ("c4 fusion dM^T = S^T dZ (768 x 400, K = 14.5k)", 768, 400, 14505, 1),
 ]
+if os.environ.get("NGDB_GEMM_SPLIT"):  # fixed split-K (ngdb_set_gemm_split; forces the 80-wide tile)
+    lib.ngdb_set_gemm_split(int(os.environ["NGDB_GEMM_SPLIT"]))
 f = lib.ngdb_debug_tc_gemm_time
 f.argtypes = [C.c_int] * 5 + [C.POINTER(C.c_float)]
-kind = "cpasync" if os.environ.get("NGDB_GEMM_CPASYNC") else "tma" + os.environ.get("NGDB_GEMM_BN", "")
+kind = ("cpasync" if os.environ.get("NGDB_GEMM_CPASYNC") else "tma" + os.environ.get("NGDB_GEMM_BN", "")) + \
+    ("_s" + os.environ["NGDB_GEMM_SPLIT"] if os.environ.get("NGDB_GEMM_SPLIT") else "")
 for label, M, N, K, b in SHAPES:
     ms = C.c_float()
     rc = f(M, N, K, b, 50, C.byref(ms))
