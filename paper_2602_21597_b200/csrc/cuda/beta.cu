@@ -510,6 +510,10 @@ int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaSt
 
 }  // namespace
 
+int64_t beta_project_scratch_floats(int dim, int max_nodes) {
+  return 50 * (int64_t)(max_nodes + 4) * dim + 64 * (int64_t)dim + 256;
+}
+
 int64_t beta_scratch_floats(int dim, int max_nodes) {
   const int64_t nd = (int64_t)(max_nodes + 4) * dim, rd = 3 * nd;
   const int64_t project = 50 * nd;   // X, Xs, H, RHs, Z, gZ(s), gH(s), 4 transposed splits, gX

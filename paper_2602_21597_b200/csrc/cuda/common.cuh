@@ -290,6 +290,8 @@ int launch_score(const DevArgs& a, int dir, int first, int n, const LaunchCtx& l
 int launch_beta_project(const DevArgs& a, int dir, int first, int n, const LaunchCtx& lc);
 int launch_beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, const LaunchCtx& lc);
 int64_t beta_scratch_floats(int dim, int max_nodes);
+// the Project MLP's share alone (ctx scratch2, sized for merged drains)
+int64_t beta_project_scratch_floats(int dim, int max_nodes);
 // intersect.cu
 int launch_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, const LaunchCtx& lc);
 // scratch floats the intersect operators need for classes of up to max_nodes

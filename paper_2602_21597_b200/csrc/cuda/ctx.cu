@@ -244,6 +244,7 @@ struct ngdb_ctx {
   int32_t istash_slots = 0;
   float* pstash = nullptr;           // BetaE Project stash (DevArgs::pstash)
   int32_t pstash_slots = 0;
+  int32_t proj_merge_cap = 0;        // BetaE Project nodes one merged launch may cover
   float* lpart = nullptr;            // fused score+loss partials (DevArgs::lpart)
   float* lpart_scalar = nullptr;
   int32_t* lcount = nullptr;
@@ -718,8 +719,8 @@ bool drain_mergeable(const ngdb_ctx* c, const ngdb_pool_desc& a, const ngdb_pool
     case NGDB_OP_SCORE:
     case NGDB_OP_LOSS:
       return true;
-    case NGDB_OP_PROJECT:  // the BetaE projection MLP has B_max-sized scratch
-      return !c->beta();
+    case NGDB_OP_PROJECT:  // the BetaE projection MLP: up to its scratch's node capacity
+      return !c->beta() || a.count + b.count <= c->proj_merge_cap;
     default:
       return false;
   }
@@ -1203,7 +1204,11 @@ int ngdb_ctx_create(const ngdb_model_desc* desc, int device, ngdb_ctx** out) {
     CK(cudaMemset(c->lcount, 0, sizeof(int32_t) * c->desc.max_batch));
     c->scratch = dmalloc<float>(c->scratch_cap);
     if (d.backbone == NGDB_BETAE) {  // BetaE Project MLPs: their own scratch, so a Project
-      c->scratch2_cap = c->scratch_cap;  // pool can run beside an Intersect pool (§3.2)
+      // pool can run beside an Intersect pool (§3.2), sized for up to 4 drains
+      // of a pool merged into one launch (bigger, fewer GEMMs)
+      const char* pm = std::getenv("NGDB_PROJ_MERGE");  // drains per launch (A/B)
+      c->proj_merge_cap = (pm ? std::max(1, std::atoi(pm)) : 4) * std::max(c->desc.max_batch, 1);
+      c->scratch2_cap = beta_project_scratch_floats(d.dim, c->proj_merge_cap);
       c->scratch2 = dmalloc<float>(c->scratch2_cap);
     }
     c->d_bc = dmalloc<float>(4);
