@@ -12,7 +12,8 @@ def _init(rank, world, port):
     return dist
 
 
-def host_plan_worker(rank, world, port, out_dir, shape, mix, b, k, dim):
+def host_plan_worker(rank, world, port, out_dir, shape, mix, b, k, dim, backbone="q2b",
+                     semantic=False):
     """CPU only: plan this rank's batch, exchange metadata, build the owner lists;
     also exercise the host-staged collectives on CPU tensors."""
     dist = _init(rank, world, port)
@@ -25,7 +26,7 @@ def host_plan_worker(rank, world, port, out_dir, shape, mix, b, k, dim):
     comm = Comm()
     g = m.Graph.synthetic(shape, 1)
     batch = m.Batch.sample(g, m.pattern_weights(mix), b, k, seed=3, tag=rank)
-    st = plan_shard_step(comm, batch, "q2b", dim)
+    st = plan_shard_step(comm, batch, backbone, dim, semantic=semantic)
     v, s = st.views()
     U = s.world * s.batch
     n_owned = s.unit_off[U]

@@ -22,13 +22,18 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module")
-def plans(tmp_path_factory):
+@pytest.fixture(scope="module", params=[("q2b", False), ("betae", True)],
+                ids=["q2b", "betae-fused"])
+def plans(tmp_path_factory, request):
+    # (the FuseSemantic plan puts FuseSemantic nodes where EmbedAnchor was:
+    # their anchors must enter the lookup exchange the same way)
     import torch.multiprocessing as mp
 
     import shard_workers
+    backbone, semantic = request.param
     out = tmp_path_factory.mktemp("shard")
-    mp.spawn(shard_workers.host_plan_worker, args=(2, _port(), str(out), "small", ALL, 48, 8, 16),
+    mp.spawn(shard_workers.host_plan_worker,
+             args=(2, _port(), str(out), "small", ALL, 48, 8, 16, backbone, semantic),
              nprocs=2, join=True)
     return [pickle.load(open(out / f"plan{r}.pkl", "rb")) for r in range(2)]
 
