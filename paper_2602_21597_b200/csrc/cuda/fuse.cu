@@ -149,38 +149,75 @@ __device__ __forceinline__ float cand_term(float v, float qc, float qo, float co
   return delta > 0.f ? mag : (delta < 0.f ? -mag : 0.f);
 }
 
-// dZ[r] = (anchor grads + candidate grads of row r) * E (1 - E), plain + split
-template <int BB>
+// dZ[r] = (anchor grads + candidate grads of row r) * E (1 - E), plain + split.
+// One warp per row, the row's d/4 float4 chunks in registers (NCH per lane);
+// contributions outer: each code / coefficient is loaded once by one lane and
+// broadcast (32 at a time), and every contribution's query row is read once.
+template <int BB, int NCH>
 __global__ void __launch_bounds__(kWarps * 32) fuse_grad_kernel(DevArgs a, SparseTable t, FuseBufs f) {
   pdl_start();
   const int r = blockIdx.x * kWarps + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (r >= t.n_rows) return;
   const int beg = t.seg[r], end = t.seg[r + 1];
+  const int d4 = f.d / 4;
   const float* E = a.etab + (int64_t)r * a.ent_w;
-  for (int c = lane; c < f.d / 4; c += 32) {
-    const float4 ev = ld4(E + 4 * c);
-    float g[4] = {0.f, 0.f, 0.f, 0.f};
-    const float e4[4] = {ev.x, ev.y, ev.z, ev.w};
-    for (int kk = beg; kk < end; ++kk) {
-      const int32_t code = __ldg(t.contrib + kk);
+  float4 ev[NCH], g[NCH];
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int c = lane + 32 * i;
+    ev[i] = c < d4 ? ld4(E + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const float ca_scale = a.alpha_box;
+  for (int k0 = beg; k0 < end; k0 += 32) {
+    const int nk = min(32, end - k0);
+    int32_t my_code = 0;
+    float my_coef = 0.f;
+    if (lane < nk) {
+      my_code = __ldg(t.contrib + k0 + lane);
+      if (my_code >= 0) my_coef = __ldg(a.coefbuf + my_code);
+    }
+    for (int j = 0; j < nk; ++j) {
+      const int32_t code = __shfl_sync(0xffffffffu, my_code, j);
+      const float coef = __shfl_sync(0xffffffffu, my_coef, j);
       if (code < 0) {
-        const float4 u = ld4(a.agbuf + (int64_t)(-code - 1) * a.ent_w + 4 * c);
-        g[0] += u.x; g[1] += u.y; g[2] += u.z; g[3] += u.w;
+        const float* u = a.agbuf + (int64_t)(-code - 1) * a.ent_w;
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const int c = lane + 32 * i;
+          if (c < d4) {
+            const float4 x = ld4(u + 4 * c);
+            g[i].x += x.x; g[i].y += x.y; g[i].z += x.z; g[i].w += x.w;
+          }
+        }
       } else {
-        const float coef = __ldg(a.coefbuf + code);
         const float* q = a.qbuf + (int64_t)(code / a.ncand) * a.wq;
-        const float4 qc = ld4(q + 4 * c);
-        const float4 qo = BB == NGDB_Q2B ? ld4(q + a.dim + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        g[0] += cand_term<BB>(e4[0], qc.x, qo.x, coef, a.alpha_box);
-        g[1] += cand_term<BB>(e4[1], qc.y, qo.y, coef, a.alpha_box);
-        g[2] += cand_term<BB>(e4[2], qc.z, qo.z, coef, a.alpha_box);
-        g[3] += cand_term<BB>(e4[3], qc.w, qo.w, coef, a.alpha_box);
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const int c = lane + 32 * i;
+          if (c < d4) {
+            const float4 qc = ld4(q + 4 * c);
+            const float4 qo = BB == NGDB_Q2B ? ld4(q + a.dim + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            g[i].x += cand_term<BB>(ev[i].x, qc.x, qo.x, coef, ca_scale);
+            g[i].y += cand_term<BB>(ev[i].y, qc.y, qo.y, coef, ca_scale);
+            g[i].z += cand_term<BB>(ev[i].z, qc.z, qo.z, coef, ca_scale);
+            g[i].w += cand_term<BB>(ev[i].w, qc.w, qo.w, coef, ca_scale);
+          }
+        }
       }
     }
+  }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      put(f.dZ, f.dZs, (int64_t)r * f.d + 4 * c + q, g[q] * e4[q] * (1.f - e4[q]));
+  for (int i = 0; i < NCH; ++i) {
+    const int c = lane + 32 * i;
+    if (c < d4) {
+      const float e4[4] = {ev[i].x, ev[i].y, ev[i].z, ev[i].w};
+      const float gg[4] = {g[i].x, g[i].y, g[i].z, g[i].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        put(f.dZ, f.dZs, (int64_t)r * f.d + 4 * c + q, gg[q] * e4[q] * (1.f - e4[q]));
+    }
   }
 }
 
@@ -347,10 +384,12 @@ int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
                (const float*)f.E, f.dZ, f.dZs, n);
     ++launches;
   } else if (a.backbone == NGDB_GQE) {
-    launch_pdl(fuse_grad_kernel<NGDB_GQE>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
+    if (d <= 512) launch_pdl(fuse_grad_kernel<NGDB_GQE, 4>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
+    else launch_pdl(fuse_grad_kernel<NGDB_GQE, 8>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
     ++launches;
   } else {
-    launch_pdl(fuse_grad_kernel<NGDB_Q2B>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
+    if (d <= 512) launch_pdl(fuse_grad_kernel<NGDB_Q2B, 4>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
+    else launch_pdl(fuse_grad_kernel<NGDB_Q2B, 8>, dim3(row_blocks(u)), dim3(kWarps * 32), 0, lc.stream, 1, a, t, f);
     ++launches;
   }
   // dh = dZ W_h -> dX[:, 0:d] (the entity rows' gradient)
