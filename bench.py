@@ -523,7 +523,7 @@ def bench_sharded(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": config_dict(args.config, world),
-            "roofline": roofline(fams) if fams else None,
+            "roofline": roofline(fams, args.config) if fams else None,
             "cpu_baseline": None,
             "e2e": {"value": e2e, "unit": "queries/s",
                     "h2d_bytes_per_step": int((b1.value - b0.value) / n_call),
