@@ -144,7 +144,8 @@ def graph_replay_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps
     dist.destroy_process_group()
 
 
-def train_loop_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone):
+def train_loop_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, backbone,
+                      sdim=0):
     """One NCCL rank on GPU 0: ShardedEngine.train (pipelined: planning
     threads, async loss read-back) vs the same batches step by step."""
     import torch
@@ -164,31 +165,31 @@ def train_loop_worker(rank, world, port, out_dir, shape, mix, b, k, dim, steps, 
     w = m.pattern_weights(mix)
     tag = lambda s: (s + 1) * world + rank  # noqa: E731
     out = {}
+    store = m.semantic_store(info["n_entities"], sdim, seed=5) if sdim else None
+    specs = m.param_specs(backbone, info["n_entities"], info["n_relations"], dim, sdim)
     eng = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
-                        n_neg=k, max_queries=b)
+                        n_neg=k, max_queries=b, semantic=store)
     seq = []
     for s in range(steps):
         batch = m.Batch.sample(g, w, b, k, seed=3, tag=tag(s))
-        seq.append(float(np.sum(eng.run(plan_shard_step(comm, batch, backbone, dim)),
+        seq.append(float(np.sum(eng.run(plan_shard_step(comm, batch, backbone, dim,
+                                                         semantic=sdim > 0)),
                                 dtype=np.float64)))
-    out["seq"] = {n: eng.download(n) for n, *_ in m.param_specs(backbone, info["n_entities"],
-                                                               info["n_relations"], dim)}
+    out["seq"] = {n: eng.download(n) for n, *_ in specs}
     eng2 = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
-                         n_neg=k, max_queries=b)
+                         n_neg=k, max_queries=b, semantic=store)
     sums = eng2.train(g, w, steps, b, k, tag, producers=3)
     torch.cuda.synchronize()
-    out["loop"] = {n: eng2.download(n) for n, *_ in m.param_specs(backbone, info["n_entities"],
-                                                                 info["n_relations"], dim)}
+    out["loop"] = {n: eng2.download(n) for n, *_ in specs}
     out["seq_sums"] = seq
     out["loop_sums"] = sums.tolist()
     # the native loop (libngdb threads + the metadata communicator), same batches:
     # tag((s+1)*world + rank) == (first_tag + s) * world + rank with first_tag = 1
     eng3 = ShardedEngine(comm, backbone, info["n_entities"], info["n_relations"], dim=dim,
-                         n_neg=k, max_queries=b)
+                         n_neg=k, max_queries=b, semantic=store)
     nsums = eng3.train_native(g, w, steps, b, k, first_tag=1, producers=3)
     torch.cuda.synchronize()
-    out["native"] = {n: eng3.download(n) for n, *_ in m.param_specs(backbone, info["n_entities"],
-                                                                   info["n_relations"], dim)}
+    out["native"] = {n: eng3.download(n) for n, *_ in specs}
     out["native_sums"] = nsums.tolist()
     with open(os.path.join(out_dir, f"loop{rank}.pkl"), "wb") as f:
         pickle.dump(out, f)

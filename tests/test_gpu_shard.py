@@ -103,14 +103,15 @@ def test_sharded_graph_replay_matches_eager(tmp_path, backbone, dim, sdim):
         assert np.array_equal(v, out["graph"][name]), name
 
 
-def test_sharded_train_loop_matches_steps(tmp_path):
+@pytest.mark.parametrize("backbone,sdim", [("q2b", 0), ("gqe", 24)])
+def test_sharded_train_loop_matches_steps(tmp_path, backbone, sdim):
     # ShardedEngine.train (bench.py --config c5 e2e) = the same batches run
     # step by step: identical parameters and per-step losses
     import torch.multiprocessing as mp
 
     import shard_workers
     mp.spawn(shard_workers.train_loop_worker,
-             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, 32, 4, "q2b"),
+             args=(1, _port(), str(tmp_path), "small", ALL, 64, 16, 32, 4, backbone, sdim),
              nprocs=1, join=True)
     out = pickle.load(open(tmp_path / "loop0.pkl", "rb"))
     for name, v in out["seq"].items():
