@@ -141,7 +141,7 @@ typedef struct ngdb_train_opts {
   int32_t queue_depth;           /* planned batches ahead; 0: 2 * n_producers */
   uint64_t seed;                 /* sampler seed (3) */
   uint64_t first_tag;
-  int32_t in_flight;             /* steps submitted ahead of the oldest uncollected one; 0: 2 */
+  int32_t in_flight;             /* steps submitted ahead of the oldest uncollected one; 0: 3 */
   int32_t flags;                 /* NGDB_TRAIN_NO_GRAPHS: stream launches instead of step graphs */
   int32_t steady_from;           /* > 0: timings[6] = host seconds from the consumer reaching step
                                     steady_from (its plan wait included) to the last step's losses

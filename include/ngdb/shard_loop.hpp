@@ -24,7 +24,7 @@ struct ShardLoopConfig {
   uint64_t first_tag = 0;   // batch i of rank r: Rng(seed).fork((first_tag + i) * world + r)
   int32_t n_producers = 0;  // 0: hardware threads - 2
   int32_t queue_depth = 0;  // 0: 2 * producers
-  int32_t in_flight = 2;
+  int32_t in_flight = 3;  // (C5 N=1 steady state: 2 -> 0.77 M q/s, 3 -> 0.79 M)
   int32_t steady_from = 0;  // > 0: ShardLoopStats::steady_s times steps [steady_from, n_steps)
 };
 

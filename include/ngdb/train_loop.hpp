@@ -32,7 +32,8 @@ struct TrainLoopConfig {
   int32_t n_producers = 0;  // 0: hardware threads - 1 (at least 1)
   int32_t queue_depth = 0;  // planned batches buffered ahead of the consumer; 0: 2 * producers
   bool graphs = true;       // launch each step as one CUDA graph (ngdb_step_launch)
-  int32_t in_flight = 2;    // steps on the device before the oldest one's losses are read back
+  int32_t in_flight = 3;    // steps on the device before the oldest one's losses are read back
+                            // (C2 steady state: 2 -> 1.15 M q/s, 3 -> 1.25 M)
   int32_t steady_from = 0;  // > 0: TrainLoopStats::steady_s times steps [steady_from, n_steps)
 
   // -- adaptive sampling feedback (SURVEY A-10) ---------
