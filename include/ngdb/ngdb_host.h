@@ -181,7 +181,9 @@ int ngdb_train_run_ex(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts*
  * thread launches ngdb_shard_step_exec per step and reads losses back one step
  * behind. timings (may be NULL): 6 doubles — consumer seconds waiting for
  * plans, submitting, waiting for results; exchange-thread seconds in the
- * all-gather and the owner-list build; producer count. */
+ * all-gather; consumer seconds in ngdb_shard_begin; producer count (with
+ * opts->steady_from > 0: 8 doubles, + the steady-state window and the
+ * consumer seconds in ngdb_shard_step_exec). */
 int ngdb_shard_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_opts* opts,
                          int64_t first_step, int32_t n_steps, double* loss_per_step,
                          double* timings);

@@ -32,6 +32,8 @@ struct ShardLoopStats {
   double plan_wait_s = 0.0, submit_s = 0.0, collect_wait_s = 0.0;
   double exchange_s = 0.0;  // on the exchange thread (all-gathers)
   double build_s = 0.0;     // unused: owner lists are built by the producers
+  double begin_s = 0.0;     // of submit_s: ngdb_shard_begin (pack + H2D of plan and owner lists)
+  double exec_s = 0.0;      // of submit_s: ngdb_shard_step_exec (stages + collectives enqueued)
   double steady_s = 0.0;    // consumer at step steady_from -> last losses read back
   int32_t producers = 0;
 };

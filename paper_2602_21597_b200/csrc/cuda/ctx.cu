@@ -250,8 +250,8 @@ struct ngdb_ctx {
   int32_t* lcount = nullptr;
   int32_t lpart_items = 0;
   struct ShardState {
-    int32_t* blob = nullptr;
-    int64_t blob_cap = 0;
+    int32_t* blobs[2] = {nullptr, nullptr};  // owner lists of streaming steps (double-buffered)
+    int64_t blobs_cap[2] = {0, 0};
     int32_t* staging[2] = {nullptr, nullptr};  // pinned, alternating with the plan staging
     int64_t staging_cap[2] = {0, 0};
     cudaEvent_t staged[2] = {nullptr, nullptr};
@@ -1291,7 +1291,8 @@ int ngdb_ctx_destroy(ngdb_ctx* c) {
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
-  if (c->sh.blob) cudaFree(c->sh.blob);
+  for (int32_t* b : c->sh.blobs)
+    if (b) cudaFree(b);
   if (c->sh.buf) cudaFree(c->sh.buf);
   for (int k = 0; k < 2; ++k) {
     if (c->sh.staging[k]) cudaFreeHost(c->sh.staging[k]);
@@ -2538,11 +2539,19 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
                      ngdb_shard_buffers* out) {
   return guarded([&] {
     validate_shard(c, *plan, *sp);
-    // 1) the rank's own step plan, as ngdb_step_begin
+    // Both blobs of this step (its step plan and its owner work lists) go up on
+    // the copy stream into double-buffered device slots, as ngdb_step_begin
+    // does for the plan: slot i is rewritten once the step two back (its last
+    // reader) is done, and this step's kernels wait for the upload — the H2D
+    // overlaps the previous step's kernels instead of sitting between them.
     const int i = c->cur;
     c->cur ^= 1;
+    auto& sh = c->sh;
     const PlanLayout L(*plan);
+    const ShardLayout SL(*sp);
+    // host staging of slot i: its previous H2D (two steps back) must be done
     CK(cudaEventSynchronize(c->staged[i]));
+    CK(cudaEventSynchronize(sh.staged[i]));
     if (L.total > c->staging_cap[i]) {
       if (c->staging[i]) CK(cudaFreeHost(c->staging[i]));
       c->staging_cap[i] = L.total + L.total / 2;
@@ -2550,15 +2559,6 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
       CK(cudaMallocHost(&hp, c->staging_cap[i] * sizeof(int32_t)));
       c->staging[i] = static_cast<int32_t*>(hp);
     }
-    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->stream);
-    CK(cudaEventRecord(c->staged[i], c->stream));
-    ensure_step_buffers(c, c->stream_plan[i].meta);
-
-    // 2) the owner work lists
-    auto& sh = c->sh;
-    const ShardLayout SL(*sp);
-    // the pinned buffer of two steps ago may still feed its H2D copy
-    CK(cudaEventSynchronize(sh.staged[i]));
     if (SL.total > sh.staging_cap[i]) {
       if (sh.staging[i]) CK(cudaFreeHost(sh.staging[i]));
       sh.staging_cap[i] = SL.total + SL.total / 2;
@@ -2566,21 +2566,30 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
       CK(cudaMallocHost(&hp, sh.staging_cap[i] * sizeof(int32_t)));
       sh.staging[i] = static_cast<int32_t*>(hp);
     }
-    if (SL.total > sh.blob_cap) {
+    if (SL.total > sh.blobs_cap[i]) {  // growth: nothing may still read the slot
       CK(cudaStreamSynchronize(c->stream));
-      if (sh.blob) CK(cudaFree(sh.blob));
-      sh.blob_cap = SL.total + SL.total / 2;
-      sh.blob = dmalloc<int32_t>(sh.blob_cap);
+      CK(cudaStreamSynchronize(c->copy_stream));
+      if (sh.blobs[i]) CK(cudaFree(sh.blobs[i]));
+      sh.blobs_cap[i] = SL.total + SL.total / 2;
+      sh.blobs[i] = dmalloc<int32_t>(sh.blobs_cap[i]);
     }
+    CK(cudaEventRecord(c->blob_free[i ^ 1], c->stream));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->blob_free[i], 0));
+    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->copy_stream);
+    CK(cudaEventRecord(c->staged[i], c->copy_stream));
     SL.pack(*sp, sh.staging[i]);
-    CK(cudaMemcpyAsync(sh.blob, sh.staging[i], SL.total * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(sh.blobs[i], sh.staging[i], SL.total * 4, cudaMemcpyHostToDevice,
+                       c->copy_stream));
     c->h2d_bytes += SL.total * 4;
-    CK(cudaEventRecord(sh.staged[i], c->stream));
+    CK(cudaEventRecord(sh.staged[i], c->copy_stream));
+    CK(cudaEventRecord(c->blob_ready[i], c->copy_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->blob_ready[i], 0));
+    ensure_step_buffers(c, c->stream_plan[i].meta);
 
-    // 3) exchange buffers, then the step prologue and device views
+    // exchange buffers, then the step prologue and device views
     const ShardShape shape(*sp);
     shard_exchange_buffers(c, shape);
-    shard_activate(c, &c->stream_plan[i], shape, sh.blob, SL);
+    shard_activate(c, &c->stream_plan[i], shape, sh.blobs[i], SL);
     if (out) *out = sh.bufs;
   });
 }

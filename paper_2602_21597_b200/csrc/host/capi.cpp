@@ -593,9 +593,12 @@ int ngdb_shard_train_run(ngdb_ctx* ctx, const ngdb_graph* g, const ngdb_train_op
       timings[1] = st.submit_s;
       timings[2] = st.collect_wait_s;
       timings[3] = st.exchange_s;
-      timings[4] = st.build_s;
+      timings[4] = st.begin_s;  // (owner lists are built on the producers: no build time)
       timings[5] = st.producers;
-      if (o->steady_from > 0) timings[6] = st.steady_s;
+      if (o->steady_from > 0) {  // timings then needs 8 entries
+        timings[6] = st.steady_s;
+        timings[7] = st.exec_s;
+      }
     }
   });
 }

@@ -266,7 +266,10 @@ ShardLoopStats run_shard_train_loop(ngdb_ctx* ctx, const GraphSplit& graph,
       sv.n_anchor_pos = static_cast<int32_t>(shard.anchor_pos.size());
       sv.anchor_pos = shard.anchor_pos.data();
       check_status(ngdb_shard_begin(ctx, &view, &sv, nullptr));
+      const auto t_exec = std::chrono::steady_clock::now();
+      stats.begin_s += std::chrono::duration<double>(t_exec - t_submit).count();
       check_status(ngdb_shard_step_exec(ctx, first_step + i + 1));
+      stats.exec_s += seconds_since(t_exec);
       int64_t ticket = -1;
       check_status(ngdb_step_end_async(ctx, &ticket));
       pending.emplace_back(i, ticket);

@@ -398,14 +398,14 @@ class ShardedEngine:
         opts = TrainOpts(_p(w, C.c_double), batch, n_neg, self.b_max, producers, 0, 3, first_tag,
                          in_flight, 0, steady_from)
         sums = np.zeros(n_steps, np.float64)
-        timings = (C.c_double * 7)()
+        timings = (C.c_double * 8)()
         check(lib.ngdb_shard_train_run(self._h, graph._h, C.byref(opts), self.step_count, n_steps,
                                        _p(sums, C.c_double), timings))
         self.step_count += n_steps
         self.last_timings = {"plan_wait_s": timings[0], "submit_s": timings[1],
                              "collect_wait_s": timings[2], "exchange_s": timings[3],
-                             "build_s": timings[4], "producers": int(timings[5]),
-                             "steady_s": timings[6]}
+                             "begin_s": timings[4], "producers": int(timings[5]),
+                             "steady_s": timings[6], "exec_s": timings[7]}
         return sums
 
     def capture(self, steps: List[ShardStep]) -> List["ShardGraph"]:
