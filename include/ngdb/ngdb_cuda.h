@@ -262,6 +262,15 @@ int ngdb_plan_prepare(ngdb_ctx* ctx, ngdb_plan* plan);
  * ngdb_shard_buffers between them, then ngdb_shard_optimizer and ngdb_step_end. */
 int ngdb_shard_begin(ngdb_ctx* ctx, const ngdb_step_plan* plan, const ngdb_shard_plan* shard,
                      ngdb_shard_buffers* bufs);
+/* The same with the plan and the owner lists pre-packed by the caller (e.g. on
+ * producer threads) into pinned memory that stays unchanged until the step's
+ * results are collected: only the H2D copies are issued here. */
+int64_t ngdb_shard_packed_size(const ngdb_shard_plan* shard);
+int ngdb_shard_pack(const ngdb_shard_plan* shard, int32_t* out, int64_t cap);
+int ngdb_shard_begin_packed(ngdb_ctx* ctx, const ngdb_step_plan* plan, const int32_t* plan_packed,
+                            int64_t plan_n, const ngdb_shard_plan* shard,
+                            const int32_t* shard_packed, int64_t shard_n,
+                            ngdb_shard_buffers* bufs);
 int ngdb_shard_run(ngdb_ctx* ctx, int32_t stage);
 /* step <= 0: keep the Adam step scalars of the last ngdb_set_step (graph capture) */
 int ngdb_shard_optimizer(ngdb_ctx* ctx, int64_t step);

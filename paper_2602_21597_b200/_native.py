@@ -107,6 +107,10 @@ SIGNATURES = {
     "ngdb_plan_run": (C.c_int, [C.c_void_p, C.c_void_p, i64]),
     "ngdb_plan_prepare": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ngdb_shard_begin": (C.c_int, [C.c_void_p, P(StepPlan), P(ShardPlan), P(ShardBuffers)]),
+    "ngdb_shard_packed_size": (i64, [P(ShardPlan)]),
+    "ngdb_shard_pack": (C.c_int, [P(ShardPlan), P(i32), i64]),
+    "ngdb_shard_begin_packed": (C.c_int, [C.c_void_p, P(StepPlan), P(i32), i64, P(ShardPlan),
+                                          P(i32), i64, P(ShardBuffers)]),
     "ngdb_shard_run": (C.c_int, [C.c_void_p, i32]),
     "ngdb_shard_step_create": (C.c_int, [C.c_void_p, P(StepPlan), P(ShardPlan), P(C.c_void_p)]),
     "ngdb_shard_step_begin": (C.c_int, [C.c_void_p, C.c_void_p, P(ShardBuffers)]),

@@ -2533,11 +2533,12 @@ struct ngdb_shard_step {
   cudaGraphExec_t exec = nullptr;  // ngdb_shard_step_capture
 };
 
-extern "C" {
-
-int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_plan* sp,
-                     ngdb_shard_buffers* out) {
-  return guarded([&] {
+namespace {
+// ngdb_shard_begin[_packed]: plan_pk / shard_pk are the caller's pre-packed
+// pinned blobs (or null: packed here into the context's staging)
+void shard_begin_impl(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_plan* sp,
+                      const int32_t* plan_pk, int64_t plan_n, const int32_t* shard_pk,
+                      int64_t shard_n, ngdb_shard_buffers* out) {
     validate_shard(c, *plan, *sp);
     // Both blobs of this step (its step plan and its owner work lists) go up on
     // the copy stream into double-buffered device slots, as ngdb_step_begin
@@ -2549,17 +2550,19 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
     auto& sh = c->sh;
     const PlanLayout L(*plan);
     const ShardLayout SL(*sp);
+    if ((plan_pk && plan_n != L.total) || (shard_pk && shard_n != SL.total))
+      throw Fail{NGDB_ERR_SHAPE_MISMATCH, "shard_begin_packed: packed sizes"};
     // host staging of slot i: its previous H2D (two steps back) must be done
     CK(cudaEventSynchronize(c->staged[i]));
     CK(cudaEventSynchronize(sh.staged[i]));
-    if (L.total > c->staging_cap[i]) {
+    if (!plan_pk && L.total > c->staging_cap[i]) {
       if (c->staging[i]) CK(cudaFreeHost(c->staging[i]));
       c->staging_cap[i] = L.total + L.total / 2;
       void* hp = nullptr;
       CK(cudaMallocHost(&hp, c->staging_cap[i] * sizeof(int32_t)));
       c->staging[i] = static_cast<int32_t*>(hp);
     }
-    if (SL.total > sh.staging_cap[i]) {
+    if (!shard_pk && SL.total > sh.staging_cap[i]) {
       if (sh.staging[i]) CK(cudaFreeHost(sh.staging[i]));
       sh.staging_cap[i] = SL.total + SL.total / 2;
       void* hp = nullptr;
@@ -2575,11 +2578,12 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
     }
     CK(cudaEventRecord(c->blob_free[i ^ 1], c->stream));
     CK(cudaStreamWaitEvent(c->copy_stream, c->blob_free[i], 0));
-    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->copy_stream);
+    upload_plan(c, *plan, &c->stream_plan[i], c->stream_cap[i], c->staging[i], c->copy_stream,
+                plan_pk);
     CK(cudaEventRecord(c->staged[i], c->copy_stream));
-    SL.pack(*sp, sh.staging[i]);
-    CK(cudaMemcpyAsync(sh.blobs[i], sh.staging[i], SL.total * 4, cudaMemcpyHostToDevice,
-                       c->copy_stream));
+    if (!shard_pk) SL.pack(*sp, sh.staging[i]);
+    CK(cudaMemcpyAsync(sh.blobs[i], shard_pk ? shard_pk : sh.staging[i], SL.total * 4,
+                       cudaMemcpyHostToDevice, c->copy_stream));
     c->h2d_bytes += SL.total * 4;
     CK(cudaEventRecord(sh.staged[i], c->copy_stream));
     CK(cudaEventRecord(c->blob_ready[i], c->copy_stream));
@@ -2591,6 +2595,31 @@ int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_p
     shard_exchange_buffers(c, shape);
     shard_activate(c, &c->stream_plan[i], shape, sh.blobs[i], SL);
     if (out) *out = sh.bufs;
+}
+}  // namespace
+
+extern "C" {
+
+int ngdb_shard_begin(ngdb_ctx* c, const ngdb_step_plan* plan, const ngdb_shard_plan* sp,
+                     ngdb_shard_buffers* out) {
+  return guarded([&] { shard_begin_impl(c, plan, sp, nullptr, 0, nullptr, 0, out); });
+}
+
+int64_t ngdb_shard_packed_size(const ngdb_shard_plan* sp) { return ShardLayout(*sp).total; }
+
+int ngdb_shard_pack(const ngdb_shard_plan* sp, int32_t* out, int64_t cap) {
+  return guarded([&] {
+    const ShardLayout SL(*sp);
+    if (cap < SL.total) throw Fail{NGDB_ERR_SHAPE_MISMATCH, "shard_pack: buffer too small"};
+    SL.pack(*sp, out);
+  });
+}
+
+int ngdb_shard_begin_packed(ngdb_ctx* c, const ngdb_step_plan* plan, const int32_t* plan_packed,
+                            int64_t plan_n, const ngdb_shard_plan* sp, const int32_t* shard_packed,
+                            int64_t shard_n, ngdb_shard_buffers* out) {
+  return guarded([&] {
+    shard_begin_impl(c, plan, sp, plan_packed, plan_n, shard_packed, shard_n, out);
   });
 }
 

@@ -6,7 +6,8 @@
 //                          slabs, the phase-ordered step) and pack its metadata
 //                          record; and — first, when one is waiting — build the
 //                          owner work lists of an exchanged step (several steps'
-//                          lists are built in parallel)
+//                          lists are built in parallel) and pack the step's
+//                          device plan and owner lists into its pinned slot
 //   exchange (1 thread)    in step order: all-gather the records over the
 //                          context's metadata communicator (ngdb_comm_allgather_i32:
 //                          its own NCCL communicator and stream, so it runs ahead
@@ -31,9 +32,43 @@ namespace ngdb {
 
 namespace {
 
+// the C view of a rank's owner work lists (points into `s`)
+ngdb_shard_plan shard_view(const ShardPlanHost& s) {
+  ngdb_shard_plan sv{};
+  sv.world = s.spec.world;
+  sv.rank = s.spec.rank;
+  sv.batch = s.spec.batch;
+  sv.max_anchors = s.spec.max_anchors;
+  sv.max_slots = s.spec.max_slots;
+  sv.n_candidates = s.spec.n_candidates;
+  sv.anchor_ids = s.anchor_ids.data();
+  sv.unit_k = s.unit_k.data();
+  sv.unit_slots = s.unit_slots.data();
+  sv.cand = s.cand.data();
+  sv.unit_off = s.unit_off.data();
+  sv.owned = s.owned.data();
+  sv.n_rows = static_cast<int32_t>(s.rows.size());
+  sv.rows = s.rows.data();
+  sv.seg = s.seg.data();
+  sv.contrib = s.contrib.data();
+  sv.send_cnt = s.send_cnt.data();
+  sv.recv_cnt = s.recv_cnt.data();
+  sv.n_send = static_cast<int32_t>(s.send_rows.size());
+  sv.n_recv = static_cast<int32_t>(s.recv_slot.size());
+  sv.send_rows = s.send_rows.data();
+  sv.recv_slot = s.recv_slot.data();
+  sv.n_anchor_pos = static_cast<int32_t>(s.anchor_pos.size());
+  sv.anchor_pos = s.anchor_pos.data();
+  return sv;
+}
+
 double seconds_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
+
+struct Pinned {  // a producer-packed pinned slot: [device plan | owner lists]
+  int64_t plan_n = 0, shard_n = 0;  // 0: too large for the slot, packed by the consumer
+};
 
 struct Slot {
   std::optional<StepPlanHost> plan;
@@ -76,6 +111,20 @@ ShardLoopStats run_shard_train_loop(ngdb_ctx* ctx, const GraphSplit& graph,
   const int32_t in_flight = std::clamp(cfg.in_flight, 1, 3);
 
   std::vector<Slot> ring(depth);
+  // pinned slot of step i: i % RP. A producer packs step j only while
+  // j < consumed + depth, so the slot's previous step (j - RP) was submitted at
+  // least 4 steps earlier and — with at most 3 steps in flight — collected:
+  // its H2D copies are long done.
+  // (one context-owned pinned allocation, reused by later calls: allocating
+  // pinned memory while the other threads issue CUDA calls stalls them)
+  const int32_t RP = depth + 4;
+  std::vector<Pinned> pinned(RP);
+  const int64_t nc = cfg.n_neg + 1, U = int64_t(world) * cap;
+  const int64_t slot_ints = int64_t(cap) * nc * 3 + int64_t(cap) * 512 + 65536  // device plan
+                            + U * nc + 4 * int64_t(cap) * nc + 8 * U + 65536;     // owner lists
+  int32_t* ring_base = nullptr;
+  check_status(ngdb_ctx_pinned_ring(ctx, slot_ints * RP, &ring_base));
+  auto slot_ptr = [&](int64_t i) { return ring_base + (i % RP) * slot_ints; };
   std::mutex mu;
   std::condition_variable cv;
   int64_t next_claim = 0, consumed = 0, next_build = 0, gathered_upto = 0;
@@ -91,6 +140,19 @@ ShardLoopStats run_shard_train_loop(ngdb_ctx* ctx, const GraphSplit& graph,
     std::exception_ptr err;
     try {
       sp.emplace(build_shard_plan_packed(world, rank, all.data(), stride, cap));
+      // the device plan and the owner lists, packed here (off the consumer)
+      const ngdb_step_plan view = ring[i % depth].plan->view();
+      const ngdb_shard_plan sv = shard_view(*sp);
+      Pinned& pk = pinned[i % RP];
+      pk.plan_n = ngdb_plan_packed_size(&view);
+      pk.shard_n = ngdb_shard_packed_size(&sv);
+      if (pk.plan_n + pk.shard_n <= slot_ints) {
+        int32_t* p = slot_ptr(i);
+        check_status(ngdb_plan_pack(&view, p, pk.plan_n));
+        check_status(ngdb_shard_pack(&sv, p + pk.plan_n, pk.shard_n));
+      } else {
+        pk.plan_n = pk.shard_n = 0;
+      }
     } catch (...) {
       err = std::current_exception();
     }
@@ -240,32 +302,13 @@ ShardLoopStats run_shard_train_loop(ngdb_ctx* ctx, const GraphSplit& graph,
       cv.notify_all();
       const auto t_submit = std::chrono::steady_clock::now();
       const ngdb_step_plan view = plan.view();
-      ngdb_shard_plan sv{};
-      sv.world = shard.spec.world;
-      sv.rank = shard.spec.rank;
-      sv.batch = shard.spec.batch;
-      sv.max_anchors = shard.spec.max_anchors;
-      sv.max_slots = shard.spec.max_slots;
-      sv.n_candidates = shard.spec.n_candidates;
-      sv.anchor_ids = shard.anchor_ids.data();
-      sv.unit_k = shard.unit_k.data();
-      sv.unit_slots = shard.unit_slots.data();
-      sv.cand = shard.cand.data();
-      sv.unit_off = shard.unit_off.data();
-      sv.owned = shard.owned.data();
-      sv.n_rows = static_cast<int32_t>(shard.rows.size());
-      sv.rows = shard.rows.data();
-      sv.seg = shard.seg.data();
-      sv.contrib = shard.contrib.data();
-      sv.send_cnt = shard.send_cnt.data();
-      sv.recv_cnt = shard.recv_cnt.data();
-      sv.n_send = static_cast<int32_t>(shard.send_rows.size());
-      sv.n_recv = static_cast<int32_t>(shard.recv_slot.size());
-      sv.send_rows = shard.send_rows.data();
-      sv.recv_slot = shard.recv_slot.data();
-      sv.n_anchor_pos = static_cast<int32_t>(shard.anchor_pos.size());
-      sv.anchor_pos = shard.anchor_pos.data();
-      check_status(ngdb_shard_begin(ctx, &view, &sv, nullptr));
+      const ngdb_shard_plan sv = shard_view(shard);
+      const Pinned& pk = pinned[i % RP];
+      if (pk.plan_n > 0)
+        check_status(ngdb_shard_begin_packed(ctx, &view, slot_ptr(i), pk.plan_n, &sv,
+                                             slot_ptr(i) + pk.plan_n, pk.shard_n, nullptr));
+      else
+        check_status(ngdb_shard_begin(ctx, &view, &sv, nullptr));
       const auto t_exec = std::chrono::steady_clock::now();
       stats.begin_s += std::chrono::duration<double>(t_exec - t_submit).count();
       check_status(ngdb_shard_step_exec(ctx, first_step + i + 1));
@@ -281,9 +324,11 @@ ShardLoopStats run_shard_train_loop(ngdb_ctx* ctx, const GraphSplit& graph,
   } catch (...) {
     shutdown();
     for (const auto& [i, ticket] : pending) ngdb_step_wait(ctx, ticket, nullptr, 0, nullptr, nullptr);
+    ngdb_sync(ctx);
     throw;
   }
   shutdown();
+  ngdb_sync(ctx);  // no H2D may still read a pinned slot
   return stats;
 }
 
