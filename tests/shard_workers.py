@@ -50,7 +50,14 @@ def host_plan_worker(rank, world, port, out_dir, shape, mix, b, k, dim, backbone
     plan["recv_slot"] = _arr(s.recv_slot, s.n_recv)
     plan["anchor_pos"] = _arr(s.anchor_pos, s.n_anchor_pos)
     plan["n_score_slots"] = v.n_score_slots
-    # collectives (host-staged path) on CPU tensors
+    # collectives (host-staged path) on CPU tensors (their expectations are
+    # written for two ranks)
+    if world != 2:
+        with open(os.path.join(out_dir, f"plan{rank}.pkl"), "wb") as f:
+            pickle.dump(plan, f)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     x = torch.arange(6, dtype=torch.float32) + 10 * rank
     ag = torch.zeros(6 * world)
     comm.all_gather(ag, x)

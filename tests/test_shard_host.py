@@ -22,23 +22,25 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=[("q2b", False), ("betae", True)],
-                ids=["q2b", "betae-fused"])
+@pytest.fixture(scope="module", params=[("q2b", False, 2), ("betae", True, 2), ("q2b", False, 3)],
+                ids=["q2b", "betae-fused", "q2b-world3"])
 def plans(tmp_path_factory, request):
     # (the FuseSemantic plan puts FuseSemantic nodes where EmbedAnchor was:
     # their anchors must enter the lookup exchange the same way)
     import torch.multiprocessing as mp
 
     import shard_workers
-    backbone, semantic = request.param
+    backbone, semantic, world = request.param
     out = tmp_path_factory.mktemp("shard")
     mp.spawn(shard_workers.host_plan_worker,
-             args=(2, _port(), str(out), "small", ALL, 48, 8, 16, backbone, semantic),
-             nprocs=2, join=True)
-    return [pickle.load(open(out / f"plan{r}.pkl", "rb")) for r in range(2)]
+             args=(world, _port(), str(out), "small", ALL, 48, 8, 16, backbone, semantic),
+             nprocs=world, join=True)
+    return [pickle.load(open(out / f"plan{r}.pkl", "rb")) for r in range(world)]
 
 
 def test_collectives_host_staged(plans):
+    if len(plans) != 2:
+        pytest.skip("collective expectations are written for two ranks")
     x = [np.arange(6, dtype=np.float32) + 10 * r for r in range(2)]
     for r, p in enumerate(plans):
         c = p["coll"]
@@ -52,11 +54,12 @@ def test_collectives_host_staged(plans):
 
 def test_metadata_identical_on_all_ranks(plans):
     for key in ("anchor_ids", "unit_k", "unit_slots", "cand"):
-        assert np.array_equal(plans[0][key], plans[1][key])
+        for p in plans[1:]:
+            assert np.array_equal(plans[0][key], p[key])
 
 
 def test_owned_candidates_partition(plans):
-    G = 2
+    G = len(plans)
     p0 = plans[0]
     U, nc = G * p0["batch"], p0["nc"]
     cand = p0["cand"].reshape(U, nc)
@@ -71,7 +74,7 @@ def test_owned_candidates_partition(plans):
 
 
 def test_owner_csr_partitions_contributions(plans):
-    G = 2
+    G = len(plans)
     p0 = plans[0]
     A, S, B, nc = p0["A"], p0["S"], p0["batch"], p0["nc"]
     codes = []
@@ -100,7 +103,7 @@ def test_lookup_exchange_lists(plans):
     # the uneven all-to-all carries exactly the owned rows: owner q's block for
     # rank r lists r's anchors owned by q in slot order; r places them by
     # recv_slot / anchor_pos; counts agree on both sides
-    G = 2
+    G = len(plans)
     p0 = plans[0]
     A = p0["A"]
     anc = p0["anchor_ids"].reshape(G, A)
