@@ -24,18 +24,19 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("backbone,dim,b,k,steps,sdim", [
-    ("q2b", 32, 64, 16, 1, 0), ("gqe", 16, 48, 8, 2, 0), ("q2b", 400, 128, 32, 2, 0),
-    ("betae", 16, 64, 16, 2, 0), ("betae", 400, 64, 32, 1, 0),
+@pytest.mark.parametrize("backbone,dim,b,k,steps,sdim,G", [
+    ("q2b", 32, 64, 16, 1, 0, 2), ("gqe", 16, 48, 8, 2, 0, 2), ("q2b", 400, 128, 32, 2, 0, 2),
+    ("betae", 16, 64, 16, 2, 0, 2), ("betae", 400, 64, 32, 1, 0, 2),
     # FuseSemantic: store rows sharded with the entity rows, fused rows exchanged
-    ("gqe", 16, 64, 16, 2, 24), ("q2b", 400, 64, 32, 1, 768), ("betae", 16, 48, 16, 2, 24)])
+    ("gqe", 16, 64, 16, 2, 24, 2), ("q2b", 400, 64, 32, 1, 768, 2), ("betae", 16, 48, 16, 2, 24, 2),
+    # three ranks: every exchange has two remote peers
+    ("q2b", 32, 48, 16, 2, 0, 3), ("gqe", 16, 48, 16, 1, 24, 3)])
 def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone, dim, b, k, steps,
-                                                 sdim):
+                                                 sdim, G):
     import torch.multiprocessing as mp
 
     import oracle as O
     import shard_workers
-    G = 2
     info = small_graph.info()
     ne, nr = info["n_entities"], info["n_relations"]
     w = m.pattern_weights(ALL)
@@ -82,7 +83,8 @@ def test_sharded_step_matches_oracle_sub_batches(small_graph, tmp_path, backbone
         res["grads"][name] = (full("grads"), om.get("g:" + name, (rows, cols)))
         res["params"][name] = (full("params"), om.get(name, (rows, cols)))
         if name != "entity":  # replicated tensors are identical on every rank
-            assert np.array_equal(outs[0]["params"][name], outs[1]["params"][name]), name
+            for o in outs[1:]:
+                assert np.array_equal(outs[0]["params"][name], o["params"][name]), name
     check_all(res, allow_frac=0.0, steps=steps)
 
 
