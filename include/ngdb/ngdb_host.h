@@ -34,6 +34,12 @@ int ngdb_graph_triples(const ngdb_graph* g, int32_t split, int32_t* out, int64_t
  * writes up to cap ids (kg.hpp:83-85) */
 int ngdb_graph_answer(const ngdb_graph* g, int32_t full, int32_t pattern, const int32_t* anchors,
                       const int32_t* relations, int32_t* out, int64_t cap, int64_t* n);
+/* predictive_answers (kg.hpp:87-89): obs = answers on the train
+ * graph, miss = full-graph answers not in obs (obs ⊎ miss = full answers);
+ * counts via *n_obs / *n_miss, up to the caps written */
+int ngdb_graph_predictive_answers(const ngdb_graph* g, int32_t pattern, const int32_t* anchors,
+                                  const int32_t* relations, int32_t* obs, int64_t obs_cap,
+                                  int64_t* n_obs, int32_t* miss, int64_t miss_cap, int64_t* n_miss);
 int ngdb_graph_destroy(ngdb_graph* g);
 
 /* --- sampler ----------------------------------- */

@@ -162,6 +162,8 @@ SIGNATURES = {
     "ngdb_graph_info": (C.c_int, [C.c_void_p, P(i32), P(i32), P(i64), P(i64), P(i64)]),
     "ngdb_graph_triples": (C.c_int, [C.c_void_p, i32, P(i32), i64]),
     "ngdb_graph_answer": (C.c_int, [C.c_void_p, i32, i32, P(i32), P(i32), P(i32), i64, P(i64)]),
+    "ngdb_graph_predictive_answers": (C.c_int, [C.c_void_p, i32, P(i32), P(i32), P(i32), i64,
+                                                P(i64), P(i32), i64, P(i64)]),
     "ngdb_graph_destroy": (C.c_int, [C.c_void_p]),
     "ngdb_batch_sample": (C.c_int, [C.c_void_p, P(f64), i32, i32, u64, u64, P(C.c_void_p)]),
     "ngdb_batch_from_arrays": (C.c_int, [i32, P(i32), P(i32), P(i32), P(i32), i32, P(i32),

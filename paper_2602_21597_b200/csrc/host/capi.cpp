@@ -155,6 +155,19 @@ int ngdb_graph_answer(const ngdb_graph* g, int32_t full, int32_t pattern, const 
   });
 }
 
+int ngdb_graph_predictive_answers(const ngdb_graph* g, int32_t pattern, const int32_t* anchors,
+                                  const int32_t* relations, int32_t* obs, int64_t obs_cap,
+                                  int64_t* n_obs, int32_t* miss, int64_t miss_cap, int64_t* n_miss) {
+  return guarded([&] {
+    const auto [o, m] = ngdb::predictive_answers(g->split, query_of(pattern, anchors, relations));
+    *n_obs = static_cast<int64_t>(o.size());
+    *n_miss = static_cast<int64_t>(m.size());
+    const int64_t ko = std::min<int64_t>(obs_cap, *n_obs), km = std::min<int64_t>(miss_cap, *n_miss);
+    if (ko > 0) std::memcpy(obs, o.data(), ko * sizeof(int32_t));
+    if (km > 0) std::memcpy(miss, m.data(), km * sizeof(int32_t));
+  });
+}
+
 int ngdb_graph_destroy(ngdb_graph* g) {
   delete g;
   return NGDB_OK;

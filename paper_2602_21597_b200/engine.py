@@ -122,6 +122,20 @@ class Graph:
                                     _p(r, C.c_int32), _p(out, C.c_int32), cap, C.byref(n)))
         return out[: n.value].copy()
 
+    def predictive_answers(self, pattern: str, anchors, relations):
+        """(obs, miss): answers on the train graph, and the full-graph answers
+        missing from it (kg.hpp:87-89; SPEC.md:63, 76)."""
+        a = np.array(list(anchors) + [-1] * 3, dtype=np.int32)[:3]
+        r = np.array(list(relations) + [-1] * 4, dtype=np.int32)[:4]
+        cap = self.info()["n_entities"]
+        obs, miss = np.zeros(cap, dtype=np.int32), np.zeros(cap, dtype=np.int32)
+        no, nm = C.c_int64(), C.c_int64()
+        check(lib.ngdb_graph_predictive_answers(self._h, PATTERNS.index(pattern), _p(a, C.c_int32),
+                                                _p(r, C.c_int32), _p(obs, C.c_int32), cap,
+                                                C.byref(no), _p(miss, C.c_int32), cap,
+                                                C.byref(nm)))
+        return obs[: no.value].copy(), miss[: nm.value].copy()
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib.ngdb_graph_destroy(self._h)

@@ -141,3 +141,26 @@ def test_sampled_queries_have_answers(small_graph):
         na, nrel = m.PATTERN_ARITY[pat]
         ans = small_graph.answer(pat, bt.anchors[i, :na], bt.relations[i, :nrel])
         assert bt.positives[i] in set(ans.tolist())
+
+
+def test_predictive_answers_partition(small_graph):
+    # obs = train-graph answers, miss = full-graph answers not in
+    # obs, obs ⊎ miss = full-graph answers — for every sampled query, with the
+    # full-graph answers checked against the oracle's independent graph
+    info = small_graph.info()
+    full = np.concatenate([small_graph.triples(s) for s in (0, 1, 2)])
+    og = O.OracleGraph(info["n_entities"], info["n_relations"], full)
+    bt = m.Batch.sample(small_graph, m.pattern_weights(P), 300, 1, seed=3, tag=78).arrays()
+    n_miss = 0
+    for i in range(300):
+        pat = P[bt.patterns[i]]
+        na, nrel = m.PATTERN_ARITY[pat]
+        a, r = bt.anchors[i, :na], bt.relations[i, :nrel]
+        obs, miss = small_graph.predictive_answers(pat, a, r)
+        assert obs.tolist() == small_graph.answer(pat, a, r).tolist()
+        assert not set(obs.tolist()) & set(miss.tolist())
+        both = sorted(obs.tolist() + miss.tolist())
+        assert both == small_graph.answer(pat, a, r, full=True).tolist()
+        assert both == og.answer(int(bt.patterns[i]), a.tolist(), r.tolist()).tolist()
+        n_miss += len(miss)
+    assert n_miss > 0  # the held-out edges do produce missing answers
