@@ -1,7 +1,10 @@
 """Learning sanity (acceptance SPEC.md:754): 2,000 steps of GQE on
 a 200-entity synthetic compositional KG — relation r_k maps h to h + s_k, so
 r2∘r1 is deterministic — must rank held-out 1p answers with a filtered MRR
-above 10x the random-ranking baseline (E[1/rank] under uniform ranking)."""
+above 10x the random-ranking baseline (E[1/rank] under uniform ranking); and
+with an informative synthetic semantic store (cluster-id vectors: one-hot of
+the entity's position bucket, predictive of the tails h + s_k), fusion-enabled
+training must beat structural-only MRR by >= 5 absolute points at equal steps."""
 import numpy as np
 import pytest
 
@@ -13,13 +16,47 @@ N = 200
 SHIFTS = [1, 2, 3, 5, 8]
 
 
-def test_gqe_learns_compositional_kg():
+def _kg():
     triples = np.array([(h, r, h + s) for r, s in enumerate(SHIFTS) for h in range(N)
                         if h + s < N], np.int32)
     rng = np.random.default_rng(0)
     idx = rng.permutation(len(triples))
     test, train = triples[idx[:60]], triples[idx[60:]]
-    g = m.Graph.from_triples(N, len(SHIFTS), train, None, test)
+    return m.Graph.from_triples(N, len(SHIFTS), train, None, test), test
+
+
+def _train_and_rank(g, test, store=None):
+    eng = m.Engine("gqe", N, len(SHIFTS), dim=400, n_neg=128, max_queries=512, semantic=store)
+    sums = eng.train(g, m.pattern_weights(["1p", "2p", "3p"]), 2000, batch=512,
+                     n_neg=128, seed=3, first_tag=0)
+    n = len(test)
+    arrs = m.BatchArrays(np.zeros(n, np.int32),
+                         np.stack([test[:, 0], -np.ones(n), -np.ones(n)], 1).astype(np.int32),
+                         np.concatenate([test[:, 1:2], -np.ones((n, 3))], 1).astype(np.int32),
+                         test[:, 2].astype(np.int32), np.zeros((n, 128), np.int32))
+    emb, _ = eng.query_embeddings(m.PlannedStep(m.Batch.from_arrays(arrs), "gqe", 400,
+                                                semantic=store is not None))
+    q = np.stack([emb[i][0] for i in range(n)]).astype(np.float32)
+    ranks = eng.eval_ranks(q, test[:, 2], [[] for _ in range(n)])
+    return m.rank_metrics(ranks)["mrr"], sums
+
+
+def test_fusion_with_informative_store_beats_structural():
+    # measured (tools/fusion_learn_sweep.py): structural 0.319, cluster-id store
+    # 0.516, thermometer store 0.732, random store 0.344 (the uninformative control)
+    g, test = _kg()
+    dl = 32
+    store = np.zeros((N, dl), np.float32)
+    store[np.arange(N), np.arange(N) * dl // N] = 1.0
+    mrr_s, _ = _train_and_rank(g, test)
+    mrr_f, sums = _train_and_rank(g, test, store)
+    print(f"fusion acceptance: MRR structural {mrr_s:.4f}, fused (cluster-id store) {mrr_f:.4f}")
+    assert np.all(np.isfinite(sums))
+    assert mrr_f >= mrr_s + 0.05, (mrr_f, mrr_s)
+
+
+def test_gqe_learns_compositional_kg():
+    g, test = _kg()
     eng = m.Engine("gqe", N, len(SHIFTS), dim=400, n_neg=128, max_queries=512)
     # path queries (the compositional structure), the config defaults otherwise
     # (d 400, lr 1e-4, gamma 12, batch 512, K 128); measured on B200 with
