@@ -184,3 +184,26 @@ def test_concurrent_pools_match_serial(small_graph, monkeypatch, backbone, mix):
             check(lib.ngdb_plan_destroy(h))
     for name in out["1"]:
         np.testing.assert_array_equal(out["0"][name], out["1"][name])
+
+
+def test_seeded_runs_are_bitwise_reproducible(small_graph, tmp_path):
+    # SPEC acceptance 11: identical seed + single-threaded mode
+    # (one producer) -> bitwise-identical checkpoints and metrics logs across
+    # two runs (the log's wall-clock throughput field excluded: it is a timing)
+    import json
+    b, k, dim, steps = 96, 16, 32, 12
+    w = m.pattern_weights(ALL)
+    logs, blobs = [], []
+    for run in range(2):
+        eng = _engine(small_graph, "q2b", dim, k, b)
+        ck, ml = tmp_path / f"run{run}.ngck", tmp_path / f"m{run}.jsonl"
+        eng.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=500, n_producers=1,
+                  adaptive=True, refresh_every=5, metrics_path=str(ml), checkpoint_path=str(ck),
+                  checkpoint_every=steps)
+        blobs.append(ck.read_bytes())
+        recs = [json.loads(x) for x in ml.read_text().splitlines()]
+        for r in recs:
+            r.pop("queries_per_s")
+        logs.append(json.dumps(recs, sort_keys=True))
+    assert blobs[0] == blobs[1]
+    assert logs[0] == logs[1]

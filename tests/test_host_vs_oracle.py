@@ -164,3 +164,28 @@ def test_predictive_answers_partition(small_graph):
         assert both == og.answer(int(bt.patterns[i]), a.tolist(), r.tolist()).tolist()
         n_miss += len(miss)
     assert n_miss > 0  # the held-out edges do produce missing answers
+
+
+def test_sampler_validity_10k_and_scaling(small_graph):
+    # SPEC acceptance 8: 10,000 online-sampled queries across all
+    # patterns all have non-empty train-graph answer sets (the sampled positive
+    # is an answer per the traversal oracle), and batch sampling time scales
+    # sub-linearly-bounded: time(2048) / time(512) <= 8
+    import time
+    bt = m.Batch.sample(small_graph, m.pattern_weights(P), 10000, 1, seed=3, tag=91).arrays()
+    assert len(set(bt.patterns.tolist())) == len(P)
+    for i in range(10000):
+        pat = P[bt.patterns[i]]
+        na, nrel = m.PATTERN_ARITY[pat]
+        ans = small_graph.answer(pat, bt.anchors[i, :na], bt.relations[i, :nrel])
+        assert ans.size > 0 and bt.positives[i] in set(ans.tolist()), i
+
+    def best_of(b, reps=5):
+        ts = []
+        for r in range(reps):
+            t0 = time.perf_counter()
+            m.Batch.sample(small_graph, m.pattern_weights(P), b, 128, seed=3, tag=1000 + r)
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+    ratio = best_of(2048) / best_of(512)
+    assert ratio <= 8.0, ratio
