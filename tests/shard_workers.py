@@ -278,3 +278,61 @@ def wikikg2_worker(rank, world, port, out_dir, b, k, dim, steps):
     with open(os.path.join(out_dir, f"wiki{rank}.pkl"), "wb") as f:
         pickle.dump(out, f)
     dist.destroy_process_group()
+
+
+def packed_begin_worker(rank, world, port, out_dir):
+    """One rank: ngdb_shard_begin_packed with a wrong size, then a packed step
+    and the same step through ngdb_shard_begin on a fresh engine."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    dist = _init(rank, world, port)
+    import paper_2602_21597_b200 as m
+    from paper_2602_21597_b200._native import NgdbError, ShardBuffers, check, lib
+    from paper_2602_21597_b200.sharded import Comm, ShardedEngine, plan_shard_step
+
+    g = m.Graph.synthetic("small", 1)
+    info = g.info()
+    comm = Comm()
+    batch = m.Batch.sample(g, m.pattern_weights(["1p", "2i", "2u"]), 48, 8, seed=3, tag=5)
+    st = plan_shard_step(comm, batch, "q2b", 16)
+    v, s = st.views()
+    n_plan = int(lib.ngdb_plan_packed_size(C.byref(v)))
+    n_shard = int(lib.ngdb_shard_packed_size(C.byref(s)))
+    pk = np.zeros(n_plan + n_shard, np.int32)
+    P32 = C.POINTER(C.c_int32)
+    check(lib.ngdb_plan_pack(C.byref(v), pk.ctypes.data_as(P32), n_plan))
+    check(lib.ngdb_shard_pack(C.byref(s), pk[n_plan:].ctypes.data_as(P32), n_shard))
+    out = {}
+    eng = ShardedEngine(comm, "q2b", info["n_entities"], info["n_relations"], dim=16, n_neg=8,
+                        max_queries=48)
+    b = ShardBuffers()
+    try:
+        check(lib.ngdb_shard_begin_packed(eng.handle, C.byref(v), pk.ctypes.data_as(P32), n_plan + 1,
+                                          C.byref(s), pk[n_plan:].ctypes.data_as(P32), n_shard,
+                                          C.byref(b)))
+        out["bad_kind"] = "accepted"
+    except NgdbError as e:
+        out["bad_kind"] = e.kind
+    # a correct packed begin, then the host-staged stages (world 1)
+    from paper_2602_21597_b200.sharded import _host_stages
+    with torch.cuda.stream(eng.stream):
+        check(lib.ngdb_shard_begin_packed(eng.handle, C.byref(v), pk.ctypes.data_as(P32), n_plan,
+                                          C.byref(s), pk[n_plan:].ctypes.data_as(P32), n_shard,
+                                          C.byref(b)))
+        _host_stages(eng, b, np.array(st.counts()[0]), np.array(st.counts()[1]))
+        check(lib.ngdb_shard_optimizer(eng.handle, 1))
+    losses = np.zeros(st.n_queries, np.float32)
+    tot, bad = C.c_double(), C.c_int32()
+    check(lib.ngdb_step_end(eng.handle, losses.ctypes.data_as(C.POINTER(C.c_float)), st.n_queries,
+                            C.byref(tot), C.byref(bad)))
+    out["loss_packed"] = losses
+    eng2 = ShardedEngine(comm, "q2b", info["n_entities"], info["n_relations"], dim=16, n_neg=8,
+                         max_queries=48)
+    out["loss_plain"] = eng2.run(st, 1)
+    with open(os.path.join(out_dir, f"packed{rank}.pkl"), "wb") as f:
+        pickle.dump(out, f)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -191,3 +191,19 @@ def test_c5_wikikg2_sharded_step_vs_oracle(tmp_path):
     rel = om.get("relation", out["relation"].shape)
     ok, nbad, worst = rel_close(out["relation"], rel)
     assert ok, f"relation: {nbad} beyond 1e-4 (worst {worst:.3e})"
+
+
+def test_packed_shard_begin_rejects_wrong_sizes(small_graph, tmp_path):
+    # ngdb_shard_begin_packed validates the caller's packed blob sizes against
+    # the plans (ShapeMismatch), and a correctly packed step runs like
+    # ngdb_shard_begin (same losses)
+    import ctypes as C
+
+    import torch.multiprocessing as mp
+
+    import shard_workers
+    mp.spawn(shard_workers.packed_begin_worker, args=(1, _port(), str(tmp_path)), nprocs=1,
+             join=True)
+    out = pickle.load(open(tmp_path / "packed0.pkl", "rb"))
+    assert out["bad_kind"] == "ShapeMismatch"
+    assert np.array_equal(out["loss_packed"], out["loss_plain"])
