@@ -207,3 +207,23 @@ def test_seeded_runs_are_bitwise_reproducible(small_graph, tmp_path):
         logs.append(json.dumps(recs, sort_keys=True))
     assert blobs[0] == blobs[1]
     assert logs[0] == logs[1]
+
+
+def test_steady_state_window(small_graph):
+    # steady_from = W: the loop times steps W..n-1 itself (the bench's e2e);
+    # the window is positive and shorter than the whole call, and the run's
+    # results do not depend on it
+    import time
+    b, k, dim, steps = 64, 16, 32, 20
+    w = m.pattern_weights(ALL)
+    eng = _engine(small_graph, "q2b", dim, k, b)
+    t0 = time.perf_counter()
+    sums = eng.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=900,
+                     steady_from=5)
+    whole = time.perf_counter() - t0
+    win = eng.last_timings["steady_s"]
+    assert 0.0 < win < whole
+    other = _engine(small_graph, "q2b", dim, k, b)
+    s2 = other.train(small_graph, w, steps, batch=b, n_neg=k, seed=3, first_tag=900)
+    np.testing.assert_array_equal(sums, s2)
+    assert other.last_timings["steady_s"] == 0.0  # not requested
