@@ -562,13 +562,18 @@ def main():
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the query-level executor and evaluator side measurements")
     ap.add_argument("--in-flight", type=int, default=0,
-                    help="e2e steps on the device before the oldest one's losses are read (0: 2)")
+                    help="e2e steps on the device before the oldest one's losses are read (0: 3)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     rank, world, local = dist_env()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `--gpus N` without a launcher: one process per GPU via torchrun
+        if args.impl == "ours":
+            import torch
+            if torch.cuda.device_count() < args.gpus:
+                raise SystemExit(f"bench.py: --gpus {args.gpus} but {torch.cuda.device_count()} "
+                                 "visible GPU(s)")
         port = 29400 + os.getpid() % 500
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
