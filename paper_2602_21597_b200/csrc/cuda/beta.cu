@@ -231,8 +231,10 @@ __global__ void beta_proj_out_kernel(DevArgs a, int first, const float* Z, const
 }
 // Backward gather: X = [q | r] (plain; the weight-gradient operand), the
 // stashed H (the ReLU mask) and gZ = dL/dout * realize'(Z) (plain + split)
-__global__ void beta_proj_bwd_pack_kernel(DevArgs a, int first, float* X, float* H, float* gZ,
-                                          Split gZs) {
+// (X and relu(H) are written split row-major only: the weight gradients read
+// them MN-major; H stays plain as the ReLU mask)
+__global__ void beta_proj_bwd_pack_kernel(DevArgs a, int first, Split Xs, float* H, Split RHs,
+                                          float* gZ, Split gZs) {
   pdl_start();
   const int i = blockIdx.x;
   const ngdb_node_desc d = a.nodes[first + i];
@@ -243,10 +245,11 @@ __global__ void beta_proj_bwd_pack_kernel(DevArgs a, int first, float* X, float*
   const float* r = a.rel + static_cast<int64_t>(ok ? d.id : 0) * a.rel_w;
   const float* st = proj_stash(a, d.aux);
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < 3 * D; e += blockDim.x * gridDim.y) {
-    X[static_cast<int64_t>(i) * 3 * D + e] = e < W ? q[e] : r[e - W];
+    put(nullptr, Xs, static_cast<int64_t>(i) * 3 * D + e, e < W ? q[e] : r[e - W]);
     if (e < W) {
       const int64_t o = static_cast<int64_t>(i) * W + e;
       H[o] = st[e];
+      put(nullptr, RHs, o, fmaxf(st[e], 0.f));
       put(gZ, gZs, o, a.arena[d.grad + e] * beta_drealize(st[W + e]));
     }
   }
@@ -275,7 +278,6 @@ __global__ void beta_proj_scatter_kernel(DevArgs a, int first, const float* gX) 
 
 int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
   const int D = a.dim, D2 = 2 * D, D3 = 3 * D;
-  const int nP = (n + 3) & ~3;
   Scratch sc{a.scratch, a.scratch_cap};
   float* X = sc.take((int64_t)n * D3);
   float* H = sc.take((int64_t)n * D2);
@@ -303,30 +305,23 @@ int beta_project(const DevArgs& a, int dir, int first, int n, cudaStream_t s) {
   Split gZs = take_split(sc, (int64_t)n * D2);
   float* gH = sc.take((int64_t)n * D2);
   Split gHs = take_split(sc, (int64_t)n * D2);
-  Split gZT = take_split(sc, (int64_t)nP * D2), RHT = take_split(sc, (int64_t)nP * D2),
-        gHT = take_split(sc, (int64_t)nP * D2), XT = take_split(sc, (int64_t)nP * D3);
+  Split Xs = take_split(sc, (int64_t)n * D3), RHs = take_split(sc, (int64_t)n * D2);
   float* gX = sc.take((int64_t)n * D3);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
-  launch_pdl(beta_proj_bwd_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, X, H,
-             gZ, gZs);
+  launch_pdl(beta_proj_bwd_pack_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, first, Xs, H,
+             RHs, gZ, gZs);
   ++launches;
   // gH = (gZ W2) * (H > 0)
   TcGemmArgs gh = gemm_args(n, D2, D2, op(gZs, D2), wop(a, BETA_P2, D2, D2, true), gH, D2);
   gh.mask = H;
   gh.s_hi = gHs.hi; gh.s_lo = gHs.lo;
   launches += tc_gemm(gh, s);
-  SplitJobs jobs{};
-  jobs.job[0] = {gZ, n, D2, D2, 0, gZT.hi, gZT.lo};
-  jobs.job[1] = {H, n, D2, D2, 1, RHT.hi, RHT.lo};
-  jobs.job[2] = {gH, n, D2, D2, 0, gHT.hi, gHT.lo};
-  jobs.job[3] = {X, n, D3, D3, 0, XT.hi, XT.lo};
-  jobs.n = 4;
-  launches += split_transposed(jobs, s);
+  // weight gradients: row-major splits read MN-major (no transposed copies)
   TcGemmArgs lvl[3];
-  lvl[0] = gemm_args(D2, D2, n, op(gZT, nP), op(RHT, nP), g + off[BETA_P2], D2);  // gW2 += gZ^T relu(H)
+  lvl[0] = gemm_args(D2, D2, n, mop(gZs, D2), mop(RHs, D2), g + off[BETA_P2], D2);  // gW2 += gZ^T relu(H)
   lvl[0].accumulate = 1;
-  lvl[1] = gemm_args(D2, D3, n, op(gHT, nP), op(XT, nP), g + off[BETA_P1], D3);   // gW1 += gH^T X
+  lvl[1] = gemm_args(D2, D3, n, mop(gHs, D2), mop(Xs, D3), g + off[BETA_P1], D3);   // gW1 += gH^T X
   lvl[1].accumulate = 1;
   lvl[2] = gemm_args(n, D3, D2, op(gHs, D2), wop(a, BETA_P1, D2, D3, true), gX, D3);  // gX = gH W1
   launches += tc_gemm_batch(lvl, 3, s);
@@ -398,8 +393,8 @@ __global__ void beta_inter_combine_kernel(DevArgs a, KSpan ks, int first, const 
 }
 // Backward combine from the node's stash; also gathers the inputs Q and the
 // stashed Z rows into class order (weight-gradient operands, ReLU mask).
-__global__ void beta_inter_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Q, float* Z,
-                                              float* gS, Split gSs, float* dQ) {
+__global__ void beta_inter_combine_bwd_kernel(DevArgs a, KSpan ks, int first, Split Qs, float* Z,
+                                              Split RZs, float* gS, Split gSs, float* dQ) {
   pdl_start();
   const int i = blockIdx.x;
   const int D = a.dim, W = 2 * D;
@@ -409,8 +404,9 @@ __global__ void beta_inter_combine_bwd_kernel(DevArgs a, KSpan ks, int first, fl
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < W; e += blockDim.x * gridDim.y)
     for (int l = 0; l < k; ++l) {
       const int64_t r = (static_cast<int64_t>(r0) + l) * W + e;
-      Q[r] = a.arena[d.in[l] + e];
-      Z[r] = st[l * W + e];
+      put(nullptr, Qs, r, a.arena[d.in[l] + e]);  // split only: read MN-major
+      Z[r] = st[l * W + e];                      // ReLU mask
+      put(nullptr, RZs, r, fmaxf(st[l * W + e], 0.f));
     }
   const float* S = st + 3 * W;  // the node's k score rows [k][D]
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < D; e += blockDim.x * gridDim.y) {
@@ -443,7 +439,7 @@ __global__ void beta_inter_scatter_kernel(DevArgs a, KSpan ks, int first, const 
 
 int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStream_t s) {
   const int D = a.dim, W = 2 * D;
-  const int R = ks.row0(n), RP = (R + 3) & ~3;
+  const int R = ks.row0(n);
   Scratch sc{a.scratch, a.scratch_cap};
   float* Q = sc.take((int64_t)R * W);
   float* Z = sc.take((int64_t)R * W);
@@ -472,29 +468,22 @@ int beta_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaSt
   float* dQ = sc.take((int64_t)R * W);
   float* gZ = sc.take((int64_t)R * W);
   Split gZs = take_split(sc, (int64_t)R * W);
-  Split gST = take_split(sc, (int64_t)RP * D), RZT = take_split(sc, (int64_t)RP * W),
-        gZT = take_split(sc, (int64_t)RP * W), QT = take_split(sc, (int64_t)RP * W);
+  Split Qs = take_split(sc, (int64_t)R * W), RZs = take_split(sc, (int64_t)R * W);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
   launch_pdl(beta_inter_combine_bwd_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first,
-             Q, Z, gS, gSs, dQ);
+             Qs, Z, RZs, gS, gSs, dQ);
   ++launches;
   // gZ = (gS A2) * (Z > 0)
   TcGemmArgs gz = gemm_args(R, W, D, op(gSs, D), wop(a, BETA_A2, D, W, true), gZ, W);
   gz.mask = Z;
   gz.s_hi = gZs.hi; gz.s_lo = gZs.lo;
   launches += tc_gemm(gz, s);
-  SplitJobs jobs{};
-  jobs.job[0] = {gS, R, D, D, 0, gST.hi, gST.lo};
-  jobs.job[1] = {Z, R, W, W, 1, RZT.hi, RZT.lo};
-  jobs.job[2] = {gZ, R, W, W, 0, gZT.hi, gZT.lo};
-  jobs.job[3] = {Q, R, W, W, 0, QT.hi, QT.lo};
-  jobs.n = 4;
-  launches += split_transposed(jobs, s);
+  // weight gradients: row-major splits read MN-major (no transposed copies)
   TcGemmArgs lvl[3];
-  lvl[0] = gemm_args(D, W, R, op(gST, RP), op(RZT, RP), g + off[BETA_A2], W);  // gA2 += gS^T relu(Z)
+  lvl[0] = gemm_args(D, W, R, mop(gSs, D), mop(RZs, W), g + off[BETA_A2], W);  // gA2 += gS^T relu(Z)
   lvl[0].accumulate = 1;
-  lvl[1] = gemm_args(W, W, R, op(gZT, RP), op(QT, RP), g + off[BETA_A1], W);   // gA1 += gZ^T Q
+  lvl[1] = gemm_args(W, W, R, mop(gZs, W), mop(Qs, W), g + off[BETA_A1], W);   // gA1 += gZ^T Q
   lvl[1].accumulate = 1;
   lvl[2] = gemm_args(R, W, W, op(gZs, W), wop(a, BETA_A1, W, W, true), dQ, W);  // dQ += gZ A1
   lvl[2].accumulate = 1;
@@ -516,8 +505,8 @@ int64_t beta_project_scratch_floats(int dim, int max_nodes) {
 
 int64_t beta_scratch_floats(int dim, int max_nodes) {
   const int64_t nd = (int64_t)(max_nodes + 4) * dim, rd = 3 * nd;
-  const int64_t project = 50 * nd;   // X, Xs, H, RHs, Z, gZ(s), gH(s), 4 transposed splits, gX
-  const int64_t intersect = 38 * rd; // Q(s), Z, RZs, S, gS(s), dQ, gZ(s), 4 transposed splits
+  const int64_t project = 50 * nd;   // X, Xs, H, RHs, Z, gZ(s), gH(s), gX (bound: 30 nd used)
+  const int64_t intersect = 38 * rd; // Q(s), Z, RZs, S, gS(s), dQ, gZ(s) (bound)
   return std::max(project, intersect) + 64 * (int64_t)dim + 256;
 }
 

@@ -75,12 +75,10 @@ struct DevArgs {
   int32_t fused;
   int32_t sem_dim;
   const float* sem;      // frozen store [n_entities][sem_dim]
-  // its 3xTF32 split, made once at upload: [n][sem_dim] hi / lo, and transposed
-  // [sem_dim][pad4(n)] hi / lo (used when a step touches every entity)
+  // its 3xTF32 split, made once at upload: [n][sem_dim] hi / lo (used when a
+  // step touches every entity; read MN-major by the weight gradients)
   const float* sem_hi;
   const float* sem_lo;
-  const float* semT_hi;
-  const float* semT_lo;
   int32_t* anchor_local;
   int32_t fus_idx;       // dense index of fus_f (fus_wp = +1, fus_bp = +2)
   // row-sharded step (shard.cu): anchor rows fetched from their owners, in

@@ -198,7 +198,7 @@ struct ngdb_ctx {
   float* scratch = nullptr;
   int64_t scratch_cap = 0;
   float* scratch2 = nullptr;  // BetaE Project GEMM scratch (independent of the intersect's)
-  float* sem_split = nullptr;  // frozen store splits: hi, lo [N][dl], then hiT, loT [dl][pad4(N)]
+  float* sem_split = nullptr;  // frozen store splits: hi, lo [N][dl]
   // whole-table fusion form (a step touching >= 90 % of the entities fuses every
   // entity: no per-step gather / split of the store, rows = identity)
   int32_t* iota_rows = nullptr;  // [N] 0..N-1
@@ -524,11 +524,9 @@ DevArgs make_args(ngdb_ctx* c, const ngdb_plan* p) {
   a.sem_dim = c->desc.semantic_dim;
   a.sem = c->sem;
   if (c->sem_split) {
-    const int64_t N = c->desc.n_entities, L = c->desc.semantic_dim, NP = (N + 3) / 4 * 4;
+    const int64_t N = c->desc.n_entities, L = c->desc.semantic_dim;
     a.sem_hi = c->sem_split;
     a.sem_lo = a.sem_hi + N * L;
-    a.semT_hi = a.sem_lo + N * L;
-    a.semT_lo = a.semT_hi + L * NP;
   }
   a.anchor_local = c->anchor_local;
   a.fus_idx = c->fus_idx;
@@ -1375,17 +1373,14 @@ int ngdb_semantic_upload(ngdb_ctx* c, const float* host, int64_t n) {
     CK(cudaMemcpy(c->sem, host, n * 4, cudaMemcpyHostToDevice));
     if (c->world > 1) return;  // the whole-table form is single-GPU only
     // the frozen store's operand splits, once (the fusion GEMMs read them
-    // directly when a step touches every entity: no per-step gather / split)
-    const int64_t N = c->desc.n_entities, L = c->desc.semantic_dim, NP = (N + 3) / 4 * 4;
-    if (!c->sem_split) c->sem_split = dmalloc<float>(2 * N * L + 2 * L * NP);
+    // directly when a step touches every entity: no per-step gather / split;
+    // the weight gradients read them MN-major, so no transposed copy)
+    const int64_t N = c->desc.n_entities, L = c->desc.semantic_dim;
+    if (!c->sem_split) c->sem_split = dmalloc<float>(2 * N * L);
     float* hi = c->sem_split;
     float* lo = hi + N * L;
-    float* hiT = lo + N * L;
-    float* loT = hiT + L * NP;
     split_matrix(c->sem, static_cast<int>(N), static_cast<int>(L), static_cast<int>(L), 0, 0, hi, lo,
                  c->stream);
-    split_matrix(c->sem, static_cast<int>(N), static_cast<int>(L), static_cast<int>(L), 1, 0, hiT,
-                 loT, c->stream);
     if (!c->iota_rows) {
       std::vector<int32_t> iota(N);
       for (int64_t e = 0; e < N; ++e) iota[e] = static_cast<int32_t>(e);

@@ -49,17 +49,14 @@ struct FuseBufs {
   float* X;  Split Xs;    // [u][2d]   [h | F s]
   float* dZ; Split dZs;   // [u][d]
   float* dX;              // [u][2d]   dZ W_p
-  Split dZT, XT, dFsT, ST;  // transposed splits, rows padded to uP
   // BetaE (Psi_theta)
   float* E;  Split Es;    // [u][d]    sigma(Z)
   float* Y;               // [u][2d]   Beta pre-activations (read by the step's kernels)
   float* dY; Split dYs;   // [u][2d]
   float* dE;              // [u][d]
-  Split dYT, ET;          // transposed splits [uP][2d], [uP][d]
   // per-step products of the weights (d x d_l)
   float* M;  Split Ms;    // M = W_s F
   float* dM; Split dMs;   // dM^T = S^T dZ [d_l][d] (plain + split)
-  Split dMT;              // dM [d][d_l] split (transposed from dM^T)
 };
 
 FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
@@ -70,7 +67,7 @@ FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
   f.d = d;
   f.dl = dl;
   f.beta = beta;
-  const int64_t U = u, UP = f.uP;
+  const int64_t U = u;
   f.S = sc.take(U * dl);
   f.Ss = take_split(sc, U * dl);
   f.X = sc.take(U * 2 * d);
@@ -78,10 +75,6 @@ FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
   f.dZ = sc.take(U * d);
   f.dZs = take_split(sc, U * d);
   f.dX = sc.take(U * 2 * d);
-  f.dZT = take_split(sc, UP * d);
-  f.XT = take_split(sc, UP * 2 * d);
-  f.dFsT = take_split(sc, UP * d);
-  f.ST = take_split(sc, UP * dl);
   if (beta) {
     f.E = sc.take(U * d);
     f.Es = take_split(sc, U * d);
@@ -89,15 +82,12 @@ FuseBufs carve(float* base, int64_t cap, int u, int d, int dl, bool beta) {
     f.dY = sc.take(U * 2 * d);
     f.dYs = take_split(sc, U * 2 * d);
     f.dE = sc.take(U * d);
-    f.dYT = take_split(sc, UP * 2 * d);
-    f.ET = take_split(sc, UP * d);
   }
   const int64_t DL = int64_t(d) * dl;
   f.M = sc.take(DL);
   f.Ms = take_split(sc, DL);
   f.dM = sc.take(DL);
   f.dMs = take_split(sc, DL);
-  f.dMT = take_split(sc, int64_t(d) * ((dl + 3) & ~3));
   return f;
 }
 
@@ -281,9 +271,9 @@ __global__ void expand_seg_kernel(const int32_t* rows, const int32_t* seg, int u
 
 int64_t fuse_scratch_floats(int d, int dl, int64_t rows) {
   const int64_t U = rows + 4;
-  return U * (3 * dl + 6 * d + d + 3 * d + 2 * d) + U * (2 * d + 4 * d + 2 * d + 2 * dl) +
-         U * (3 * d + 2 * d + 6 * d + d + 4 * d + 2 * d) +  // + the BetaE (Psi) buffers
-         int64_t(d + 4) * dl * 8 + 4096;                     // + M, dM (plain, split, transposed)
+  // S, X, dZ (plain + split), dX; the BetaE (Psi) buffers; M, dM (plain + split)
+  return U * (3 * dl + 6 * d + d + 3 * d + 2 * d) + U * (3 * d + 2 * d + 6 * d + d) +
+         int64_t(d + 4) * dl * 6 + 4096;
 }
 
 int launch_expand_rows(const int32_t* rows, const int32_t* seg, int u, int32_t* seg_full, int n,
@@ -366,12 +356,8 @@ int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
     TcGemmArgs ge = gemm_args(u, d, 2 * d, op(f.dYs, 2 * d), wop(a, a.fus_idx + 3, 2 * d, d, true),
                               f.dE, d);  // dE = dY W_psi
     launches += tc_gemm(ge, lc.stream);
-    SplitJobs pj{};
-    pj.job[0] = {f.dY, u, 2 * d, 2 * d, 0, f.dYT.hi, f.dYT.lo};
-    pj.job[1] = {f.E, u, d, d, 0, f.ET.hi, f.ET.lo};
-    pj.n = 2;
-    launches += split_transposed(pj, lc.stream);
-    TcGemmArgs gw = gemm_args(2 * d, d, u, op(f.dYT, f.uP), op(f.ET, f.uP), g + off[a.fus_idx + 3], d);
+    // dY and E (prologue epilogue) split row-major, read MN-major
+    TcGemmArgs gw = gemm_args(2 * d, d, u, mop(f.dYs, 2 * d), mop(f.Es, d), g + off[a.fus_idx + 3], d);
     gw.accumulate = 1;  // dW_psi += dY^T E
     launches += tc_gemm(gw, lc.stream);
     ColsumJobs pc{};
@@ -397,30 +383,22 @@ int fuse_backward(const DevArgs& a, const SparseTable& t, float* fs, int64_t cap
   TcGemmArgs g3 = gemm_args(u, d, d, op(f.dZs, d), wpt, f.dX, d);
   launches += tc_gemm(g3, lc.stream);
   const bool whole = all_rows(a, t);
-  SplitJobs jobs{};
-  jobs.job[0] = {f.dZ, u, d, d, 0, f.dZT.hi, f.dZT.lo};
-  jobs.job[1] = {f.X, u, d, 2 * d, 0, f.XT.hi, f.XT.lo};
-  jobs.job[2] = {f.S, u, dl, dl, 0, f.ST.hi, f.ST.lo};
-  jobs.n = whole ? 2 : 3;  // the store's transposed split exists already
-  launches += split_transposed(jobs, lc.stream);
-  const Split ST = whole ? Split{const_cast<float*>(a.semT_hi), const_cast<float*>(a.semT_lo)} : f.ST;
-  // the two K = rows weight gradients as separate launches: each gets its own
-  // tile width and split-K (tc_gemm.cu), which beats one shared launch
-  TcGemmArgs gw = gemm_args(d, d, u, op(f.dZT, f.uP), op(f.XT, f.uP), g + off[a.fus_idx + 1], 2 * d);
+  // the K = rows weight gradients read the row-major splits of dZ, h (= X[:,
+  // 0:d], the prologue's split) and the store rows S MN-major: no transposed
+  // copies. The two as separate launches: each gets its own tile width and
+  // split-K (tc_gemm.cu), which beats one shared launch
+  const Split Ss = whole ? Split{const_cast<float*>(a.sem_hi), const_cast<float*>(a.sem_lo)} : f.Ss;
+  TcGemmArgs gw = gemm_args(d, d, u, mop(f.dZs, d), mop(f.Xs, 2 * d), g + off[a.fus_idx + 1], 2 * d);
   gw.accumulate = 1;  // dW_h += dZ^T h
   launches += tc_gemm(gw, lc.stream);
   // dM^T = S^T dZ ([d_l][d], plain + split): the d_l-row orientation streams
   // the store operand fewer times than dM = dZ^T S
-  TcGemmArgs gt = gemm_args(dl, d, u, op(ST, f.uP), op(f.dZT, f.uP), f.dM, d);
+  TcGemmArgs gt = gemm_args(dl, d, u, mop(Ss, dl), mop(f.dZs, d), f.dM, d);
   gt.s_hi = f.dMs.hi;
   gt.s_lo = f.dMs.lo;
   launches += tc_gemm(gt, lc.stream);
-  SplitJobs mj{};
-  mj.job[0] = {f.dM, dl, d, d, 0, f.dMT.hi, f.dMT.lo};  // -> dM [d][d_l] split
-  mj.n = 1;
-  launches += split_transposed(mj, lc.stream);
   TcGemmArgs wl[2];
-  wl[0] = gemm_args(d, d, dl, op(f.dMT, dl), wop(a, a.fus_idx, d, dl, false),
+  wl[0] = gemm_args(d, d, dl, mop(f.dMs, d), wop(a, a.fus_idx, d, dl, false),
                     g + off[a.fus_idx + 1] + d, 2 * d);
   wl[0].accumulate = 1;  // dW_s += dM F^T
   wl[1] = gemm_args(d, dl, d, SplitOperand{wpt.hi + int64_t(d) * d, wpt.lo + int64_t(d) * d, d},

@@ -124,8 +124,6 @@ __global__ void gqe_scatter_kernel(DevArgs a, KSpan ks, int first, const float* 
 int gqe_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStream_t s) {
   const int D = a.dim;
   const int64_t nd = (int64_t)n * D;
-  const int nP = (n + 3) & ~3;  // transposed operands: rows padded for 16-B cp.async
-  const int64_t ndp = (int64_t)nP * D;
   Scratch sc{a.scratch, a.scratch_cap};
   float* M = sc.take(nd);
   Split Ms = take_split(sc, nd);
@@ -149,8 +147,6 @@ int gqe_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   }
   float* dH = sc.take(nd);
   Split dHs = take_split(sc, nd);
-  Split GT = take_split(sc, ndp), RHT = take_split(sc, ndp), dHT = take_split(sc, ndp),
-        MT = take_split(sc, ndp);
   float* dM = sc.take(nd);
   float* gW1 = a.dense_g + a.dense_off[GQE_W1];
   float* gW2 = a.dense_g + a.dense_off[GQE_W2];
@@ -159,17 +155,12 @@ int gqe_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   da.mask = H;
   da.s_hi = dHs.hi; da.s_lo = dHs.lo;
   launches += tc_gemm(da, s);
-  SplitJobs jobs{};
-  jobs.job[0] = {G, n, D, D, 0, GT.hi, GT.lo};
-  jobs.job[1] = {H, n, D, D, 1, RHT.hi, RHT.lo};
-  jobs.job[2] = {dH, n, D, D, 0, dHT.hi, dHT.lo};
-  jobs.job[3] = {M, n, D, D, 0, MT.hi, MT.lo};
-  jobs.n = 4;
-  launches += split_transposed(jobs, s);
+  // weight gradients read the row-major splits of G, relu(H), dH and M (pack
+  // kernel / GEMM epilogues) MN-major: no transposed copies
   TcGemmArgs lvl[3];
-  lvl[0] = gemm_args(D, D, n, op(GT, nP), op(RHT, nP), gW2, D);  // gW2 += G^T relu(H)
+  lvl[0] = gemm_args(D, D, n, mop(Gs, D), mop(RHs, D), gW2, D);  // gW2 += G^T relu(H)
   lvl[0].accumulate = 1;
-  lvl[1] = gemm_args(D, D, n, op(dHT, nP), op(MT, nP), gW1, D);  // gW1 += dH^T M
+  lvl[1] = gemm_args(D, D, n, mop(dHs, D), mop(Ms, D), gW1, D);  // gW1 += dH^T M
   lvl[1].accumulate = 1;
   lvl[2] = gemm_args(n, D, D, op(dHs, D), wop(a, GQE_W1, D, D, true), dM, D);  // dM = dH W1
   launches += tc_gemm_batch(lvl, 3, s);
@@ -259,10 +250,11 @@ __global__ void q2b_combine_kernel(DevArgs a, KSpan ks, int first, const float* 
   }
 }
 // Backward combine. Also gathers the node's inputs (arena) and its stashed Z,
-// P rows and Lm into class order: the operands of the weight-gradient GEMMs
-// and the ReLU masks.
-__global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Cin, float* Oin,
-                                       float* Z, float* P, float* Lm, float* gS, Split gSs,
+// P rows and Lm into class order: the ReLU masks (Z, P plain) and, split
+// row-major, the weight-gradient GEMMs' operands (Cin, Oin, relu(Z), Lm —
+// read MN-major by the GEMMs, so no transposed copies).
+__global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, Split Cs, Split Os,
+                                       float* Z, Split RZs, float* P, Split Lms, float* gS, Split gSs,
                                        float* dCin, float* dOin, float* gU, Split gUs) {
   pdl_launch();
   const int i = blockIdx.x;
@@ -283,14 +275,16 @@ __global__ void q2b_combine_bwd_kernel(DevArgs a, KSpan ks, int first, float* Ci
       const int64_t r = base + (int64_t)l * D + e;
       cin[l] = a.arena[d.in[l] + e];
       oin[l] = a.arena[d.in[l] + D + e];
-      Cin[r] = cin[l];
-      Oin[r] = oin[l];
-      Z[r] = st[l * D + e];
+      put(nullptr, Cs, r, cin[l]);
+      put(nullptr, Os, r, oin[l]);
+      const float z = st[l * D + e];
+      Z[r] = z;
+      put(nullptr, RZs, r, fmaxf(z, 0.f));
       P[r] = st[6 * D + l * D + e];
       ga[l] = gC * cin[l];
       dot += w[l] * ga[l];
     }
-    Lm[(int64_t)i * D + e] = st[10 * D + e];
+    put(nullptr, Lms, (int64_t)i * D + e, st[10 * D + e]);
     int arg = 0;
     float mn = oin[0];
     for (int l = 1; l < k; ++l)
@@ -356,9 +350,6 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   const int D = a.dim;
   const int R = ks.row0(n);
   const int64_t rd = (int64_t)R * D, nd = (int64_t)n * D;
-  // transposed (weight-gradient) operands: rows padded for 16-byte cp.async
-  const int nP = (n + 3) & ~3, RP = (R + 3) & ~3;
-  const int64_t ndp = (int64_t)nP * D, rdp = (int64_t)RP * D;
   Scratch sc{a.scratch, a.scratch_cap};
   float* Cin = sc.take(rd);
   float* Oin = sc.take(rd);
@@ -404,7 +395,9 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
                (const float*)P, (const float*)Lm);
     return launches + 1;
   }
-  // Backward: the forward's Z, S, P, U, Lm come from the node's stash slot
+  // Backward: the forward's Z, S, P, U, Lm come from the node's stash slot.
+  // The weight gradients dW += dY^T X read dY and X as row-major splits
+  // through MN-major UMMA operands (K = rows): no transposed copies.
   float* gS = sc.take(rd);
   Split gSs = take_split(sc, rd);
   float* dCin = sc.take(rd);
@@ -416,28 +409,20 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
   Split gPs = take_split(sc, rd);
   float* gZ = sc.take(rd);
   Split gZs = take_split(sc, rd);
-  Split gUT = take_split(sc, ndp), LmT = take_split(sc, ndp), gST = take_split(sc, rdp),
-        RZT = take_split(sc, rdp), gPT = take_split(sc, rdp), OT = take_split(sc, rdp),
-        gZT = take_split(sc, rdp), CT = take_split(sc, rdp);
+  Split Cs = take_split(sc, rd), Os = take_split(sc, rd), RZs = take_split(sc, rd),
+        Lms = take_split(sc, nd);
   float* g = a.dense_g;
   const int64_t* off = a.dense_off;
 
   float* Pc = sc.take(rd);  // stashed P rows in class order (ReLU mask of gP)
-  launch_pdl(q2b_combine_bwd_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Cin, Oin, Z, Pc,
-             Lm, gS, gSs, dCin, dOin, gU, gUs);
+  launch_pdl(q2b_combine_bwd_kernel, node_grid(n, a.dim), dim3(128), 0, s, 1, a, ks, first, Cs, Os, Z,
+             RZs, Pc, Lms, gS, gSs, dCin, dOin, gU, gUs);
   ++launches;
-  SplitJobs j1{};
-  j1.job[0] = {gU, n, D, D, 0, gUT.hi, gUT.lo};
-  j1.job[1] = {Lm, n, D, D, 0, LmT.hi, LmT.lo};
-  j1.job[2] = {gS, R, D, D, 0, gST.hi, gST.lo};
-  j1.job[3] = {Z, R, D, D, 1, RZT.hi, RZT.lo};
-  j1.n = 4;
-  launches += split_transposed(j1, s);
   {  // level 3: weight grads of V2, A2; gLm = gU V2; gZ = (gS A2) * (Z > 0)
     TcGemmArgs lvl[4];
-    lvl[0] = gemm_args(D, D, n, op(gUT, nP), op(LmT, nP), g + off[Q2B_V2], D);
+    lvl[0] = gemm_args(D, D, n, mop(gUs, D), mop(Lms, D), g + off[Q2B_V2], D);
     lvl[0].accumulate = 1;
-    lvl[1] = gemm_args(D, D, R, op(gST, RP), op(RZT, RP), g + off[Q2B_A2], D);
+    lvl[1] = gemm_args(D, D, R, mop(gSs, D), mop(RZs, D), g + off[Q2B_A2], D);
     lvl[1].accumulate = 1;
     lvl[2] = gemm_args(n, D, D, op(gUs, D), wop(a, Q2B_V2, D, D, true), gLm, D);
     lvl[3] = gemm_args(R, D, D, op(gSs, D), wop(a, Q2B_A2, D, D, true), gZ, D);
@@ -446,19 +431,15 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
     launches += tc_gemm_batch(lvl, 4, s);
   }
   SplitJobs j2{};
-  // gP = gLm / k * (P > 0), computed inside the transposing split (plain,
-  // row-major split and transposed split in one pass)
-  j2.job[0] = {gP, R, D, D, 0, gPT.hi, gPT.lo, gLm, Pc, ks.n1, ks.k1, ks.k2, gP, gPs.hi, gPs.lo};
-  j2.job[1] = {Oin, R, D, D, 0, OT.hi, OT.lo};
-  j2.job[2] = {gZ, R, D, D, 0, gZT.hi, gZT.lo};
-  j2.job[3] = {Cin, R, D, D, 0, CT.hi, CT.lo};
-  j2.n = 4;
+  // gP = gLm / k * (P > 0), computed and written plain + split row-major
+  j2.job[0] = {gP, R, D, D, 0, nullptr, nullptr, gLm, Pc, ks.n1, ks.k1, ks.k2, gP, gPs.hi, gPs.lo};
+  j2.n = 1;
   launches += split_transposed(j2, s);
   {  // level 4: weight grads of V1, A1; input grads dOin += gP V1, dCin += gZ A1
     TcGemmArgs lvl[4];
-    lvl[0] = gemm_args(D, D, R, op(gPT, RP), op(OT, RP), g + off[Q2B_V1], D);
+    lvl[0] = gemm_args(D, D, R, mop(gPs, D), mop(Os, D), g + off[Q2B_V1], D);
     lvl[0].accumulate = 1;
-    lvl[1] = gemm_args(D, D, R, op(gZT, RP), op(CT, RP), g + off[Q2B_A1], D);
+    lvl[1] = gemm_args(D, D, R, mop(gZs, D), mop(Cs, D), g + off[Q2B_A1], D);
     lvl[1].accumulate = 1;
     lvl[2] = gemm_args(R, D, D, op(gPs, D), wop(a, Q2B_V1, D, D, true), dOin, D);
     lvl[2].accumulate = 1;
@@ -482,7 +463,7 @@ int q2b_intersect(const DevArgs& a, int dir, KSpan ks, int first, int n, cudaStr
 
 int64_t intersect_scratch_floats(int backbone, int dim, int max_nodes) {
   const int64_t nd = (int64_t)max_nodes * dim, rd = 3 * nd;
-  // + padding of the transposed operands (<= 3 rows each)
+  // (upper bounds; the weight gradients read row-major splits MN-major)
   if (backbone == NGDB_GQE) return 24 * nd + 32 * (int64_t)dim + 64;
   if (backbone == NGDB_BETAE) return beta_scratch_floats(dim, max_nodes);
   return 36 * rd + 14 * nd + 64 * (int64_t)dim + 256;

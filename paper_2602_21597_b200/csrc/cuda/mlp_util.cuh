@@ -30,7 +30,10 @@ inline Split take_split(Scratch& s, int64_t n) { return {s.take(n), s.take(n)}; 
 int launch_beta_fuse_grad(const DevArgs& a, const SparseTable& t, float* gY, Split gYs,
                           const LaunchCtx& lc);
 
-inline SplitOperand op(Split x, int ld) { return {x.hi, x.lo, ld}; }
+inline SplitOperand op(Split x, int ld) { return {x.hi, x.lo, ld, 0}; }
+// a row-major [rows][ld] split read MN-major: the transposed operand of a
+// weight gradient (dW += dY^T X, K = rows) without a transposed copy
+inline SplitOperand mop(Split x, int ld) { return {x.hi, x.lo, ld, 1}; }
 
 // Grid of the per-node elementwise kernels: blockIdx.x = node, blockIdx.y
 // strides the row elements (128 threads each), so every thread handles ~one
@@ -40,7 +43,8 @@ inline dim3 node_grid(int n, int dim) { return dim3(n, (2 * dim + 127) / 128); }
 inline SplitOperand wop(const DevArgs& a, int i, int rows, int cols, bool transposed) {
   const int64_t n = (int64_t)rows * cols;
   const float* base = a.wsplit + a.wsplit_off[i];
-  return transposed ? SplitOperand{base + 2 * n, base + 3 * n, rows} : SplitOperand{base, base + n, cols};
+  return transposed ? SplitOperand{base + 2 * n, base + 3 * n, rows, 0}
+                    : SplitOperand{base, base + n, cols, 0};
 }
 
 inline TcGemmArgs gemm_args(int M, int N, int K, SplitOperand A, SplitOperand B, float* C, int ldc) {

@@ -84,6 +84,19 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
          (static_cast<uint64_t>(2) << 61);
 }
 
+// MN-major operand tile (tf32 admits only the 128B swizzle with 32-byte
+// atoms, UMMA layout type SWIZZLE_128B_BASE32B = 1, Swizzle<2,5,2>): per
+// 32-row block (4096 B, one TMA box {32 rows, 32 K} with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) a 128-byte line holds 32 consecutive
+// rows at one k, 4-line (4-k) atoms of 512 B. LBO = 4096 B (next 32-row
+// block), SBO = 512 B (next 4-k atom); one tf32 UMMA (k = 8) spans two atoms.
+__device__ __forceinline__ uint64_t umma_desc_mn(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3fff) | (static_cast<uint64_t>(4096 >> 4) << 16) |
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(1) << 61);
+}
+constexpr int kMnBlock = 32 * BK * 4;  // bytes of one 32-row MN-major block (4096)
+
 // byte offset of the 16-byte chunk (row r, k4 = k/4) in a swizzled K-major tile
 __device__ __forceinline__ uint32_t swz16(int r, int k4) {
   return static_cast<uint32_t>(r * 128 + ((k4 ^ (r & 7)) << 4));
@@ -546,8 +559,26 @@ __global__ void __launch_bounds__(TmaCfg<TBN, TG>::kThreads, 1)
         const uint32_t bar = smem_u32(&full[st]), dst = s_base + st * kStageB;
         mbar_expect_tx(bar, kStageB);
         const int k0 = (c_beg + c) * BK;
-        tma_load_2d(dst, &mp.a_hi, bar, k0, m0);
-        tma_load_2d(dst + A_TILE, &mp.a_lo, bar, k0, m0);
+        if (g.A.mn) {  // MN-major: {rows, K} map, one box per 32-row block
+#pragma unroll
+          for (int blk = 0; blk < BM / 32; ++blk) {
+            tma_load_2d(dst + blk * kMnBlock, &mp.a_hi, bar, m0 + 32 * blk, k0);
+            tma_load_2d(dst + A_TILE + blk * kMnBlock, &mp.a_lo, bar, m0 + 32 * blk, k0);
+          }
+        } else {
+          tma_load_2d(dst, &mp.a_hi, bar, k0, m0);
+          tma_load_2d(dst + A_TILE, &mp.a_lo, bar, k0, m0);
+        }
+        if constexpr (TBN % 32 == 0) {
+          if (g.B.mn) {
+#pragma unroll
+            for (int blk = 0; blk < TBN / 32; ++blk) {
+              tma_load_2d(dst + 2 * A_TILE + blk * kMnBlock, &mp.b_hi, bar, n0 + 32 * blk, k0);
+              tma_load_2d(dst + 2 * A_TILE + kBT + blk * kMnBlock, &mp.b_lo, bar, n0 + 32 * blk, k0);
+            }
+            continue;
+          }
+        }
         tma_load_2d(dst + 2 * A_TILE, &mp.b_hi, bar, k0, n0);
         tma_load_2d(dst + 2 * A_TILE + kBT, &mp.b_lo, bar, k0, n0);
       }
@@ -555,6 +586,12 @@ __global__ void __launch_bounds__(TmaCfg<TBN, TG>::kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
+      // operand majors (instruction descriptor bits 15 / 16) and the k-step
+      // advance: 32 B along a K-major 128-byte line, or one 1024-byte 8-k atom
+      const uint32_t idesc = Cfg::kInstr | (g.A.mn ? 1u << 15 : 0u) | (g.B.mn ? 1u << 16 : 0u);
+      const uint32_t a_step = g.A.mn ? 1024u : 32u, b_step = g.B.mn ? 1024u : 32u;
+      auto desc_a = [&](uint32_t addr) { return g.A.mn ? umma_desc_mn(addr) : umma_desc(addr); };
+      auto desc_b = [&](uint32_t addr) { return g.B.mn ? umma_desc_mn(addr) : umma_desc(addr); };
       for (int c = 0; c < n_chunks; ++c) {
         const int st = c % kSt, ph = (c / kSt) & 1;
         const int gi = c / F, buf = gi & 1, bph = (gi >> 1) & 1;
@@ -567,11 +604,10 @@ __global__ void __launch_bounds__(TmaCfg<TBN, TG>::kThreads, 1)
         const uint32_t d = tmem + buf * TBN;
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {  // small terms first, fresh accumulator per chunk
-          const uint32_t off = ks * 32;
-          umma_tf32_n(d, umma_desc(a_lo + off), umma_desc(b_hi + off), Cfg::kInstr,
-                      (ks == 0 && fresh) ? 0u : 1u);
-          umma_tf32_n(d, umma_desc(a_hi + off), umma_desc(b_lo + off), Cfg::kInstr, 1u);
-          umma_tf32_n(d, umma_desc(a_hi + off), umma_desc(b_hi + off), Cfg::kInstr, 1u);
+          const uint32_t ao = ks * a_step, bo = ks * b_step;
+          umma_tf32_n(d, desc_a(a_lo + ao), desc_b(b_hi + bo), idesc, (ks == 0 && fresh) ? 0u : 1u);
+          umma_tf32_n(d, desc_a(a_hi + ao), desc_b(b_lo + bo), idesc, 1u);
+          umma_tf32_n(d, desc_a(a_hi + ao), desc_b(b_hi + bo), idesc, 1u);
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&empty[st])));
@@ -678,6 +714,7 @@ __global__ void split_t_multi_kernel(SplitJobs jobs) {
     tile[y][threadIdx.x] = j.relu ? fmaxf(v, 0.f) : v;
   }
   __syncthreads();
+  if (!j.hi) return;  // computed source written row-major only (MN-major consumer)
   const int ldp = (j.rows + 3) & ~3;  // 16-byte aligned rows for cp.async; zero padded
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int c = c0 + y, r = r0 + threadIdx.x;
@@ -741,13 +778,35 @@ bool encode(CUtensorMap* m, const float* base, int rows, int K, int ld, int box_
                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// MN-major operand [K][rows] (row stride ld): {rows, K} map, box {32, 32}
+// (one 4096-byte block per box, 32-byte-atom 128B swizzle; rows / K beyond
+// the matrix zero)
+bool encode_mn(CUtensorMap* m, const float* base, int rows, int K, int ld) {
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(K)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(BK)};
+  const cuuint32_t estr[2] = {1, 1};
+  return tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool encode_op(CUtensorMap* m, const float* base, const SplitOperand& o, int rows, int K, int box_rows) {
+  return o.mn ? encode_mn(m, base, rows, K, o.ld) : encode(m, base, rows, K, o.ld, box_rows);
+}
 }  // namespace
 
 int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
   tc_gemm_init();
   TcGemmBatch b{};
   int max_chunks = 0, tiles = 0;
-  bool tma = tensor_map_encoder() != nullptr && !std::getenv("NGDB_GEMM_CPASYNC");
+  bool any_mn = false, b_mn = false;
+  for (int i = 0; i < n && i < kMaxProblems; ++i) {
+    any_mn = any_mn || probs[i].A.mn || probs[i].B.mn;
+    b_mn = b_mn || probs[i].B.mn;
+  }
+  // MN-major operands exist only in the TMA mainloop (the cp.async knob is ignored)
+  bool tma = tensor_map_encoder() != nullptr && (any_mn || !std::getenv("NGDB_GEMM_CPASYNC"));
   b.n = 0;
   for (int i = 0; i < n && b.n < kMaxProblems; ++i) {
     const TcGemmArgs& g = probs[i];
@@ -800,15 +859,17 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
     int tbn = pick(b.p[big]);
     if (forced_bn == 80 || forced_bn == 128 || forced_bn == 160 || forced_bn == kWideBN) tbn = forced_bn;
     if (g_split_override.load(std::memory_order_relaxed)) tbn = BN;
+    // an MN-major B is loaded in 32-row blocks: the tile width is a multiple of 32
+    if (b_mn && tbn % 32 != 0) tbn = 160;
     TcGemmTmaBatch t{};  // ~2.6 KB of kernel parameters (4 tensor maps per problem)
     int tiles_t = 0;
     for (int i = 0; i < b.n && tma; ++i) {
       const TcGemmArgs& g = b.p[i];
       t.p[i] = g;
-      tma = encode(&t.maps[i].a_hi, g.A.hi, g.M, g.K, g.A.ld, BM) &&
-            encode(&t.maps[i].a_lo, g.A.lo, g.M, g.K, g.A.ld, BM) &&
-            encode(&t.maps[i].b_hi, g.B.hi, g.N, g.K, g.B.ld, tbn) &&
-            encode(&t.maps[i].b_lo, g.B.lo, g.N, g.K, g.B.ld, tbn);
+      tma = encode_op(&t.maps[i].a_hi, g.A.hi, g.A, g.M, g.K, BM) &&
+            encode_op(&t.maps[i].a_lo, g.A.lo, g.A, g.M, g.K, BM) &&
+            encode_op(&t.maps[i].b_hi, g.B.hi, g.B, g.N, g.K, tbn) &&
+            encode_op(&t.maps[i].b_lo, g.B.lo, g.B, g.N, g.K, tbn);
       t.tile_begin[i] = tiles_t;
       tiles_t += ((g.M + BM - 1) / BM) * ((g.N + tbn - 1) / tbn);
     }
@@ -830,7 +891,9 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
       static const bool log_shapes = std::getenv("NGDB_GEMM_LOG") != nullptr;
       if (log_shapes) {  // one line per launch (diagnostics)
         std::fprintf(stderr, "gemm bn=%d S=%d tiles=%d", tbn, t.S, tiles_t);
-        for (int i = 0; i < b.n; ++i) std::fprintf(stderr, " [%dx%dx%d]", b.p[i].M, b.p[i].N, b.p[i].K);
+        for (int i = 0; i < b.n; ++i)
+          std::fprintf(stderr, " [%dx%dx%d%s%s]", b.p[i].M, b.p[i].N, b.p[i].K, b.p[i].A.mn ? " A:mn" : "",
+                       b.p[i].B.mn ? " B:mn" : "");
         std::fprintf(stderr, "\n");
       }
       auto go = [&](auto kernel, int threads, int smem) {
@@ -845,6 +908,11 @@ int tc_gemm_batch(const TcGemmArgs* probs, int n, cudaStream_t s) {
       }
       return 1;
     }
+  }
+  if (any_mn) {  // no cp.async form of an MN-major operand: fail loudly
+    std::fprintf(stderr, "ngdb: tc_gemm_batch: MN-major operand needs the TMA mainloop "
+                         "(16-byte aligned hi/lo, ld %% 4 == 0)\n");
+    std::abort();
   }
   // split-K so the launch fills about one wave (2 CTAs per SM), at most 8 CTAs
   // per cluster (portable size) and at least 2 chunks per CTA
@@ -897,14 +965,21 @@ int split_weight(const float* w, int rows, int cols, float* dst, cudaStream_t s)
 
 // Debug entry point for the GEMM unit test (host pointers, synchronous):
 // C = op_a(A) op_b(B)^T with A [M][K] (a_major 0) or [K][M] (1), B [N][K] (0)
-// or [K][N] (1); ops bit0 = relu(A), bit1 = relu(B).
+// or [K][N] (1); ops bit0 = relu(A), bit1 = relu(B), bit2 = route [K][rows]
+// operands through the transposing split (K-major) instead of reading them
+// MN-major in place (the two must agree bit for bit).
 extern "C" int ngdb_debug_tc_gemm(int M, int N, int K, int a_major, int b_major, int ops,
                                   const float* A, int lda, const float* B, int ldb, float* C,
                                   int ldc, const float* bias, int accumulate) {
   using namespace ngdb_dev;
   const int64_t nc = (int64_t)M * ldc;
-  // Route every operand through the transposed split (which pads rows to a
-  // multiple of 4 floats): K-major inputs are transposed on the host first.
+  // [K][rows] operands with 16-byte rows go MN-major (non-transposing split,
+  // dense [K][rows]); everything else goes K-major through the transposing
+  // split (which pads rows to a multiple of 4 floats): K-major inputs are
+  // transposed on the host first.
+  const bool legacy = (ops & 4) != 0;
+  const bool a_mn = a_major == 1 && (M & 3) == 0 && !legacy;
+  const bool b_mn = b_major == 1 && (N & 3) == 0 && !legacy;
   std::vector<float> At, Bt;
   if (a_major == 0) {
     At.resize((size_t)K * M);
@@ -922,9 +997,11 @@ extern "C" int ngdb_debug_tc_gemm(int M, int N, int K, int a_major, int b_major,
   }
   const int64_t na2 = (int64_t)K * lda, nb2 = (int64_t)K * ldb;
   const int KP = (K + 3) & ~3;
+  const int64_t sa = std::max<int64_t>((int64_t)M * KP, (int64_t)K * M);
+  const int64_t sb = std::max<int64_t>((int64_t)N * KP, (int64_t)K * N);
   float *dA, *dB, *dC, *dbias = nullptr, *sp;
   if (cudaMalloc(&dA, na2 * 4) || cudaMalloc(&dB, nb2 * 4) || cudaMalloc(&dC, nc * 4)) return 8;
-  if (cudaMalloc(&sp, ((int64_t)M * KP + (int64_t)N * KP) * 2 * 4)) return 8;
+  if (cudaMalloc(&sp, (sa + sb) * 2 * 4)) return 8;
   cudaMemcpy(dA, A, na2 * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B, nb2 * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dC, C, nc * 4, cudaMemcpyHostToDevice);
@@ -932,18 +1009,29 @@ extern "C" int ngdb_debug_tc_gemm(int M, int N, int K, int a_major, int b_major,
     cudaMalloc(&dbias, N * 4);
     cudaMemcpy(dbias, bias, N * 4, cudaMemcpyHostToDevice);
   }
-  float *ahi = sp, *alo = ahi + (int64_t)M * KP, *bhi = alo + (int64_t)M * KP,
-        *blo = bhi + (int64_t)N * KP;
-  split_matrix(dA, K, M, lda, 1, ops & 1, ahi, alo, 0);
-  split_matrix(dB, K, N, ldb, 1, (ops >> 1) & 1, bhi, blo, 0);
+  float *ahi = sp, *alo = ahi + sa, *bhi = alo + sa, *blo = bhi + sb;
   TcGemmArgs g{};
   g.M = M; g.N = N; g.K = K;
-  g.A = {ahi, alo, KP};
-  g.B = {bhi, blo, KP};
+  if (a_mn) {
+    split_matrix(dA, K, M, lda, 0, ops & 1, ahi, alo, 0);
+    g.A = {ahi, alo, M, 1};
+  } else {
+    split_matrix(dA, K, M, lda, 1, ops & 1, ahi, alo, 0);
+    g.A = {ahi, alo, KP, 0};
+  }
+  if (b_mn) {
+    split_matrix(dB, K, N, ldb, 0, (ops >> 1) & 1, bhi, blo, 0);
+    g.B = {bhi, blo, N, 1};
+  } else {
+    split_matrix(dB, K, N, ldb, 1, (ops >> 1) & 1, bhi, blo, 0);
+    g.B = {bhi, blo, KP, 0};
+  }
   g.C = dC; g.ldc = ldc;
   g.bias = dbias; g.accumulate = accumulate;
   tc_gemm(g, 0);
-  cudaError_t e = cudaDeviceSynchronize();
+  cudaError_t e = cudaGetLastError();  // launch-configuration errors
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) std::fprintf(stderr, "ngdb_debug_tc_gemm: %s\n", cudaGetErrorString(e));
   cudaMemcpy(C, dC, nc * 4, cudaMemcpyDeviceToHost);
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(sp);
   if (dbias) cudaFree(dbias);

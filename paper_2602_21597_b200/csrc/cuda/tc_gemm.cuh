@@ -28,6 +28,12 @@ struct SplitOperand {
   const float* hi;
   const float* lo;
   int ld;  // row stride (elements); rows are K-contiguous
+  // 1: MN-major — stored [K][rows] (element (row, k) at k*ld + row), e.g. dY
+  // of a weight gradient dW = dY^T X read in place as [rows][features]; the
+  // TMA mainloop loads it in 32-row blocks and the UMMA reads it through an
+  // MN-major descriptor (no transposed copy). Needs the TMA path (ld % 4 == 0,
+  // 16-byte aligned hi/lo).
+  int mn;
 };
 
 struct TcGemmArgs {
@@ -75,6 +81,8 @@ struct SplitJob {
   float* plain;
   float* rhi;
   float* rlo;
+  // (hi == nullptr: no transposed output — the computed source is written
+  // plain and split row-major only, for MN-major weight-gradient operands)
 };
 struct SplitJobs {
   SplitJob job[4];

@@ -69,3 +69,37 @@ def test_weight_grad_layout(K):
 
 def test_weight_grad_relu_b():
     assert run(400, 400, 300, MAJ_MN, MAJ_MN, relu=False, acc=True, brelu=True) < TOL
+
+
+def _raw(M, N, K, a_major, b_major, ops, seed=3, acc=True):
+    from paper_2602_21597_b200._native import lib
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    As = np.ascontiguousarray(A if a_major == MAJ_K else A.T)
+    Bs = np.ascontiguousarray(B if b_major == MAJ_K else B.T)
+    Cd = rng.standard_normal((M, N)).astype(np.float32) if acc else np.zeros((M, N), np.float32)
+    rc = lib.ngdb_debug_tc_gemm(M, N, K, a_major, b_major, ops, _p(As), As.shape[1], _p(Bs),
+                                Bs.shape[1], _p(Cd), N, None, int(acc))
+    assert rc == 0
+    return Cd
+
+
+@pytest.mark.parametrize("M,N,K,am,bm", [(400, 400, 731, MAJ_MN, MAJ_MN), (400, 400, 5, MAJ_MN, MAJ_MN),
+                                         (400, 400, 2193, MAJ_MN, MAJ_MN), (256, 96, 300, MAJ_MN, MAJ_K),
+                                         (512, 400, 400, MAJ_K, MAJ_MN), (36, 800, 1434, MAJ_MN, MAJ_MN)])
+@pytest.mark.parametrize("relu", [0, 2])
+def test_mn_major_operands_equal_transposed_split(M, N, K, am, bm, relu):
+    """[K][rows] operands read in place through MN-major UMMA descriptors (TMA
+    32-row blocks) give the same bits as the transposed K-major copies (the
+    products and their order are the same); both within TOL of fp64."""
+    from paper_2602_21597_b200._native import lib
+    try:
+        for split in (1, 3):  # same K partition on both paths (the tile widths differ)
+            assert lib.ngdb_set_gemm_split(split) == 0
+            mn = _raw(M, N, K, am, bm, relu)
+            legacy = _raw(M, N, K, am, bm, relu | 4)
+            assert np.array_equal(mn, legacy), (split, np.max(np.abs(mn - legacy)))
+    finally:
+        lib.ngdb_set_gemm_split(0)
+    assert run(M, N, K, am, bm, acc=True, brelu=bool(relu)) < TOL
